@@ -1,0 +1,38 @@
+# Builds the product library (sm_100a) and the CPU oracle (test infrastructure).
+#   paper_2312_10615_b200/libsmg.so  — C-ABI of include/smg.h (CUDA kernels + host driver)
+#   oracle/liboracle.so              — CPU restatement used only by tests / baselines
+NVCC ?= /usr/local/cuda/bin/nvcc
+CXX ?= g++
+ARCH := -gencode arch=compute_100a,code=sm_100a
+PKG := paper_2312_10615_b200
+CSRC := $(PKG)/csrc
+# -fmad=false / -ffp-contract=off: no FMA contraction, so per-point arithmetic
+# matches the oracle bit for bit.
+NVFLAGS := $(ARCH) -O3 -lineinfo -fmad=false -std=c++17 -Xcompiler -fPIC -Xptxas -warn-spills
+HOSTFLAGS := -O2 -std=c++17 -fPIC -ffp-contract=off -pthread -Wall -Wextra -I/usr/local/cuda/include
+
+LIB := $(PKG)/libsmg.so
+OBJS := build/kernels.o build/host.o
+
+all: $(LIB) oracle
+
+build:
+	mkdir -p build
+
+build/kernels.o: $(CSRC)/kernels.cu $(CSRC)/smg_internal.h | build
+	$(NVCC) $(NVFLAGS) -c $< -o $@
+
+build/host.o: $(CSRC)/host.cpp $(CSRC)/smg_internal.h include/smg.h | build
+	$(CXX) $(HOSTFLAGS) -c $< -o $@
+
+$(LIB): $(OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcudart_static -lpthread -ldl -lrt
+
+oracle:
+	$(MAKE) -s -C oracle
+
+clean:
+	rm -rf build $(LIB)
+	$(MAKE) -s -C oracle clean
+
+.PHONY: all oracle clean

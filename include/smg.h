@@ -1,0 +1,141 @@
+/*
+ * smg.h — C-ABI of the B200-native MG-preconditioned SQMR Stokes solver.
+ *
+ * Drop-in boundary for the hot path of arXiv 2312.10615.  The
+ * reference ships only proj/include/stokesmg/util.hpp (kept verbatim in
+ * signature as include/stokesmg/util.hpp); its solver exists only as the
+ * behavioural spec SPEC.md, so every entry point below cites the SPEC
+ * operation it replaces.  The host C++ API (include/stokesmg/solver.hpp) and
+ * the Python tests call exactly these symbols; plain pointers and sizes only.
+ *
+ * Vectors crossing the boundary are the SPEC's compact FieldVector: the active
+ * DOFs of one level numbered u-lex, v-lex, w-lex, p-lex, x fastest
+ * (SPEC:34-42, 48, 84, 111-114).  The context owns all device memory.
+ * Return values: 0 on success, negative smg_err on failure (details in
+ * smg_last_error).  Solver status is reported separately.
+ * A context is not thread-safe; distinct contexts are independent.
+ */
+#ifndef SMG_H
+#define SMG_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct smg_ctx smg_ctx;
+
+enum smg_err {
+    SMG_OK = 0,
+    SMG_EINVAL = -1,   /* bad argument / length mismatch   */
+    SMG_ECUDA = -2,    /* CUDA runtime error                                  */
+    SMG_ENCCL = -3,    /* NCCL error                                          */
+    SMG_ECAP = -4,     /* coarsest system above the dense cap      */
+    SMG_ENOMEM = -5,   /* device allocation failed                            */
+    SMG_ESINGULAR = -6 /* singular local/coarse matrix             */
+};
+
+enum smg_status {
+    SMG_CONVERGED = 0,
+    SMG_MAX_ITERATIONS = 1,
+    SMG_BREAKDOWN = 2
+};
+
+/* Walled box: nx*ny*nz interior cells of spacing h inside an implicit no-slip
+ * Dirichlet ring (cube and channel configs of BASELINE.json). */
+typedef struct smg_grid_desc {
+    int dim; /* must be 3 */
+    int nx, ny, nz;
+    double h;
+} smg_grid_desc;
+
+/* SmootherConfig + CycleConfig + LevelOperator parameters. */
+typedef struct smg_params {
+    double eta;      /* viscosity eta                                  */
+    double gamma;    /* penalty gamma of L~ (preconditioner only)      */
+    int levels;      /* V-cycle levels n >= 1                          */
+    int nu;          /* symmetric multiplicative Vanka sweeps per side */
+    int band_width;  /* V1 band width (Chebyshev)                      */
+    int flags;       /* SMG_FLAG_*                                     */
+} smg_params;
+
+#define SMG_FLAG_SKIP_REVERSE_DGS 1 /* fault injection: symmetry negative control */
+
+/* ResidualHistory: caller-owned arrays of `capacity` entries. */
+typedef struct smg_history {
+    int capacity;
+    int count;
+    double* rel_residual; /* ||b - L x_j|| / ||b||                 */
+    double* seconds;      /* wall seconds since solve start       */
+} smg_history;
+
+/* Timing of the last solve, measured with CUDA events on the solver stream. */
+typedef struct smg_timing {
+    double solve_ms;        /* SQMR loop on device-resident data           */
+    double h2d_ms, d2h_ms;  /* host<->device transfers of the last e2e call */
+    int iterations;
+    int64_t kernel_launches; /* own kernels launched during the solve      */
+} smg_timing;
+
+/* build_hierarchy: grids, operators, transfers, Vanka tables,
+ * coarse dense inverse; uploads everything.  ngpu must be 1 in this build. */
+int smg_create(const smg_grid_desc* grid, const smg_params* params, int ngpu, const int* dev_ids,
+               smg_ctx** out);
+void smg_destroy(smg_ctx* ctx);
+const char* smg_last_error(const smg_ctx* ctx);
+const char* smg_version(void);
+
+int smg_num_levels(const smg_ctx* ctx);
+/* Active DOF counts of a level: out5 = {n_u, n_v, n_w, n_p, |V1|}; returns N. */
+int64_t smg_level_ndof(const smg_ctx* ctx, int level, int64_t* out5);
+
+/* discretization.apply: y = L x (penalized = 0) or L~ x. */
+int smg_apply(smg_ctx* ctx, int level, int penalized, const double* x, double* y);
+/* r = b - L~ x on a level (Alg. 1 line 9). */
+int smg_residual(smg_ctx* ctx, int level, const double* x, const double* b, double* r);
+
+/* Smoother entry points.  op: 0 one DGS phase (arg = phase
+ * 0..19: forward 0,1 velocity red/black, 2..9 pressure parity colours 0..7;
+ * reverse 10..17 pressure colours 7..0, 18,19 velocity black/red), 1
+ * symmetric_dgs, 2 one Vanka colour (arg = colour 0..7), 3 symmetric
+ * multiplicative Vanka, 4 smooth (Alg. 3).  x is updated in place. */
+int smg_smoother(smg_ctx* ctx, int level, int op, int arg, double* x, const double* b);
+
+/* transfer between level and level+1: rc = R rf, xf = P xc. */
+int smg_restrict(smg_ctx* ctx, int level, const double* rf, double* rc);
+int smg_prolong(smg_ctx* ctx, int level, const double* xc, double* xf);
+/* exact coarsest solve: x = L~_c^{-1} b on the last level. */
+int smg_coarse_solve(smg_ctx* ctx, const double* b, double* x);
+/* cycle: x = V-cycle(L~, b, 0). */
+int smg_vcycle(smg_ctx* ctx, const double* b, double* x);
+
+/* sqmr_solve with the V-cycle preconditioner: host buffers in,
+ * host solution out (end-to-end path).  *status gets an smg_status. */
+int smg_sqmr_solve(smg_ctx* ctx, const double* b, double* x, double tol, int maxit, smg_history* hist,
+                   int* status);
+
+/* Device-resident path used for kernel-level timing: upload b once, solve with
+ * everything in HBM, read x back separately. */
+int smg_set_rhs(smg_ctx* ctx, const double* b);
+int smg_solve_resident(smg_ctx* ctx, double tol, int maxit, smg_history* hist, int* status);
+int smg_get_solution(smg_ctx* ctx, double* x);
+int smg_last_timing(const smg_ctx* ctx, smg_timing* out);
+/* Times `reps` back-to-back launches of one fine-level kernel (CUDA events,
+ * average ms per launch).  which: 0 apply L, 1 residual, 2 symmetric DGS sweep
+ * (8 phases), 3 one V-cycle. */
+int smg_time_kernel(smg_ctx* ctx, int which, int reps, double* avg_ms);
+
+/* Pinned host buffers for the end-to-end path. */
+void* smg_host_alloc(int64_t bytes);
+void smg_host_free(void* p);
+
+/* Synthetic forcing of the BASELINE configs (OD-9), host side, compact order.
+ * kind 0: iid U[-1,1]; 1: 8 Fourier modes; 2: channel 1 + U[-0.1,0.1] on u.
+ * b must hold smg_level_ndof(ctx, 0) doubles.  threads <= 1: sequential. */
+int smg_forcing(const smg_grid_desc* grid, int kind, uint64_t seed, double* b, int threads);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SMG_H */

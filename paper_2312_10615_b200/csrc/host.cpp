@@ -1,0 +1,848 @@
+// host.cpp — host driver and C-ABI of the B200 MG-SQMR Stokes solver.
+//
+// Builds the hierarchy for a walled box, precomputes the Vanka
+// local inverses and the coarsest dense inverse (
+// OD-4), owns all device memory, and drives the V-cycle (PAPER Alg. 1, 3) and
+// SQMR (PAPER Alg. 4) on one CUDA stream.  There is no CPU fallback: every
+// numeric step of a solve runs in kernels.cu.  Compiled with
+// -ffp-contract=off so the host-side tables (local/coarse inverses, forcing)
+// follow the arithmetic contract of DESIGN.md §4.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/smg.h"
+#include "smg_internal.h"
+
+using namespace smg;
+
+namespace {
+
+struct SmgError : std::runtime_error {
+    int code;
+    SmgError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define CK(call)                                                                                  \
+    do {                                                                                          \
+        cudaError_t e_ = (call);                                                                  \
+        if (e_ != cudaSuccess)                                                                    \
+            throw SmgError(SMG_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_));        \
+    } while (0)
+
+void host_parallel(int64_t n, int threads, const std::function<void(int64_t, int64_t)>& body) {
+    threads = std::max<int>(1, std::min<int64_t>(threads, n));
+    if (threads == 1) { body(0, n); return; }
+    std::vector<std::thread> ts;
+    for (int t = 0; t < threads; ++t) {
+        const int64_t lo = n * t / threads, hi = n * (t + 1) / threads;
+        ts.emplace_back([lo, hi, &body] { body(lo, hi); });
+    }
+    for (auto& t : ts) t.join();
+}
+
+int host_threads() {
+    const unsigned hc = std::thread::hardware_concurrency();
+    return hc == 0 ? 1 : static_cast<int>(std::min(hc, 32u));
+}
+
+// ------------------------------------------------------- dense algebra ------
+// LU with partial pivoting (full-row swaps), inverse by per-column forward /
+// back substitution, then exact symmetrisation K = (A^-1 + A^-T)/2 (OD-4).
+std::vector<double> dense_inverse_sym(std::vector<double> a, int n) {
+    std::vector<int> piv(n);
+    const int T = host_threads();
+    for (int k = 0; k < n; ++k) {
+        int p = k;
+        double best = std::fabs(a[static_cast<size_t>(k) * n + k]);
+        for (int i = k + 1; i < n; ++i) {
+            const double v = std::fabs(a[static_cast<size_t>(i) * n + k]);
+            if (v > best) { best = v; p = i; }
+        }
+        if (best == 0.0) throw SmgError(SMG_ESINGULAR, "coarse LU: singular matrix");
+        piv[k] = p;
+        if (p != k)
+            for (int j = 0; j < n; ++j) std::swap(a[static_cast<size_t>(k) * n + j], a[static_cast<size_t>(p) * n + j]);
+        const double d = a[static_cast<size_t>(k) * n + k];
+        const int rows = n - k - 1;
+        auto elim = [&](int64_t lo, int64_t hi) {
+            const double* rk = &a[static_cast<size_t>(k) * n];
+            for (int64_t t = lo; t < hi; ++t) {
+                double* ri = &a[static_cast<size_t>(k + 1 + t) * n];
+                const double m = ri[k] / d;
+                ri[k] = m;
+                if (m != 0.0)
+                    for (int j = k + 1; j < n; ++j) ri[j] = ri[j] - m * rk[j];
+            }
+        };
+        if (static_cast<int64_t>(rows) * (n - k) > 200000) host_parallel(rows, T, elim);
+        else elim(0, rows);
+    }
+    std::vector<double> inv(static_cast<size_t>(n) * n, 0.0);  // inv[col*n + i] = (A^-1)_{i,col}
+    host_parallel(n, T, [&](int64_t lo, int64_t hi) {
+        std::vector<double> y(n);
+        for (int64_t col = lo; col < hi; ++col) {
+            std::fill(y.begin(), y.end(), 0.0);
+            y[col] = 1.0;
+            for (int k = 0; k < n; ++k)
+                if (piv[k] != k) std::swap(y[k], y[piv[k]]);
+            for (int i = 0; i < n; ++i) {
+                double s = y[i];
+                const double* ri = &a[static_cast<size_t>(i) * n];
+                for (int j = 0; j < i; ++j) s = s - ri[j] * y[j];
+                y[i] = s;
+            }
+            for (int i = n - 1; i >= 0; --i) {
+                double s = y[i];
+                const double* ri = &a[static_cast<size_t>(i) * n];
+                for (int j = i + 1; j < n; ++j) s = s - ri[j] * y[j];
+                y[i] = s / ri[i];
+            }
+            for (int i = 0; i < n; ++i) inv[static_cast<size_t>(col) * n + i] = y[i];
+        }
+    });
+    std::vector<double> k(static_cast<size_t>(n) * n);
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j)
+            k[static_cast<size_t>(i) * n + j] =
+                0.5 * (inv[static_cast<size_t>(j) * n + i] + inv[static_cast<size_t>(i) * n + j]);
+    return k;
+}
+
+// Gauss-Jordan with partial pivoting for the <= 7x7 Vanka blocks.
+void small_inverse(const double* m, int n, double* out /* n x n */) {
+    double a[49], e[49];
+    for (int i = 0; i < n * n; ++i) { a[i] = m[i]; e[i] = 0.0; }
+    for (int i = 0; i < n; ++i) e[i * n + i] = 1.0;
+    for (int k = 0; k < n; ++k) {
+        int p = k;
+        double best = std::fabs(a[k * n + k]);
+        for (int i = k + 1; i < n; ++i)
+            if (std::fabs(a[i * n + k]) > best) { best = std::fabs(a[i * n + k]); p = i; }
+        if (best == 0.0) throw SmgError(SMG_ESINGULAR, "vanka: singular local matrix (SPEC:288)");
+        if (p != k)
+            for (int j = 0; j < n; ++j) { std::swap(a[k * n + j], a[p * n + j]); std::swap(e[k * n + j], e[p * n + j]); }
+        const double d = a[k * n + k];
+        for (int j = 0; j < n; ++j) { a[k * n + j] = a[k * n + j] / d; e[k * n + j] = e[k * n + j] / d; }
+        for (int i = 0; i < n; ++i) {
+            if (i == k) continue;
+            const double f = a[i * n + k];
+            if (f == 0.0) continue;
+            for (int j = 0; j < n; ++j) { a[i * n + j] = a[i * n + j] - f * a[k * n + j]; e[i * n + j] = e[i * n + j] - f * e[k * n + j]; }
+        }
+    }
+    for (int i = 0; i < n * n; ++i) out[i] = e[i];
+}
+
+// ----------------------------------------------------------- forcing --------
+inline uint64_t mix64(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+inline uint64_t key5(uint64_t seed, uint64_t c, uint64_t i, uint64_t j, uint64_t k) {
+    return mix64(mix64(mix64(mix64(mix64(seed) ^ c) ^ k) ^ j) ^ i);
+}
+inline double unit01(uint64_t h) { return static_cast<double>(h >> 11) * 0x1.0p-53; }
+
+// ------------------------------------------------------------ context -------
+struct DevLevel {
+    LevelK k{};
+    int64_t counts[5] = {0, 0, 0, 0, 0};  // nu, nv, nw, np, |V1|
+    int64_t N = 0;
+    double *x = nullptr, *b = nullptr, *r = nullptr, *pd = nullptr;  // pd: DGS delta (one field)
+    int32_t* vk_cells[8] = {};
+    uint8_t* vk_mask[8] = {};
+    int vk_n[8] = {};
+    double* ktab = nullptr;  // [64][49]
+};
+
+}  // namespace
+
+struct smg_ctx {
+    int device = 0;
+    cudaStream_t st = nullptr;
+    smg_params prm{};
+    smg_grid_desc grid{};
+    std::vector<DevLevel> lv;
+    double* coarse_k = nullptr;
+    int32_t* coarse_slots = nullptr;
+    int nc = 0;
+    double* vk_delta = nullptr;
+    // SQMR vectors on the fine level (s = lv[0].b, t = lv[0].x, scratch = lv[0].r)
+    double *q = nullptr, *d = nullptr, *xs = nullptr, *rhs = nullptr;
+    double* compact = nullptr;
+    double* partials = nullptr;
+    double* dscal = nullptr;
+    double* hscal = nullptr;  // pinned
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    std::string err;
+    smg_timing timing{};
+    std::vector<void*> allocs;
+    bool rhs_set = false;
+
+    template <class T>
+    T* dalloc(int64_t count) {
+        void* p = nullptr;
+        const size_t bytes = static_cast<size_t>(count) * sizeof(T);
+        cudaError_t e = cudaMalloc(&p, bytes ? bytes : 8);
+        if (e != cudaSuccess) throw SmgError(SMG_ENOMEM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+        CK(cudaMemsetAsync(p, 0, bytes ? bytes : 8, st));
+        allocs.push_back(p);
+        return static_cast<T*>(p);
+    }
+    ~smg_ctx() {
+        if (st) cudaStreamSynchronize(st);
+        for (void* p : allocs) cudaFree(p);
+        if (hscal) cudaFreeHost(hscal);
+        if (ev0) cudaEventDestroy(ev0);
+        if (ev1) cudaEventDestroy(ev1);
+        if (st) cudaStreamDestroy(st);
+    }
+};
+
+namespace {
+
+int64_t vlen(const DevLevel& L) { return L.k.g.vec_len(); }
+
+// ---- setup ----
+void build(smg_ctx* c) {
+    const smg_grid_desc& g = c->grid;
+    const smg_params& p = c->prm;
+    if (g.dim != 3) throw SmgError(SMG_EINVAL, "dim must be 3");
+    if (p.levels < 1) throw SmgError(SMG_EINVAL, "levels < 1");
+    if (p.nu < 1 || p.band_width < 1) throw SmgError(SMG_EINVAL, "nu and band_width must be >= 1");
+    if (!(g.h > 0)) throw SmgError(SMG_EINVAL, "h must be > 0");
+    const int div = 1 << (p.levels - 1);
+    if (g.nx % div || g.ny % div || g.nz % div)
+        throw SmgError(SMG_EINVAL, "extents must be divisible by 2^(levels-1)");
+    if (g.nx / div < 2 || g.ny / div < 2 || g.nz / div < 2)
+        throw SmgError(SMG_EINVAL, "coarsened extent below 2 (SPEC:82)");
+    CK(cudaSetDevice(c->device));
+    CK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+    CK(cudaEventCreate(&c->ev0));
+    CK(cudaEventCreate(&c->ev1));
+    c->lv.resize(p.levels);
+    int max_vk = 1;
+    for (int l = 0; l < p.levels; ++l) {
+        DevLevel& L = c->lv[l];
+        const int nx = g.nx >> l, ny = g.ny >> l, nz = g.nz >> l;
+        const double h = g.h * static_cast<double>(1 << l);
+        L.k.g = make_geom(nx, ny, nz);
+        L.k.eta_h2 = p.eta / (h * h);
+        L.k.inv_h = 1.0 / h;
+        L.k.gamma = p.gamma;
+        L.k.dv = 6.0 * L.k.eta_h2;
+        L.k.dp = -6.0 * (1.0 + p.gamma * p.eta) / (h * h);
+        L.k.bw = p.band_width;
+        L.counts[0] = static_cast<int64_t>(nx - 1) * ny * nz;
+        L.counts[1] = static_cast<int64_t>(nx) * (ny - 1) * nz;
+        L.counts[2] = static_cast<int64_t>(nx) * ny * (nz - 1);
+        L.counts[3] = static_cast<int64_t>(nx) * ny * nz;
+        L.N = L.counts[0] + L.counts[1] + L.counts[2] + L.counts[3];
+        const int64_t vl = vlen(L);
+        L.x = c->dalloc<double>(vl);
+        L.b = c->dalloc<double>(vl);
+        L.r = c->dalloc<double>(vl);
+        L.pd = c->dalloc<double>(L.k.g.fs);
+        // Vanka blocks: band cells, slot + active-face mask, by colour
+        const int bw = p.band_width;
+        auto band = [&](int x, int y, int z) {
+            return x < bw || y < bw || z < bw || x >= nx - bw || y >= ny - bw || z >= nz - bw;
+        };
+        std::vector<int32_t> cells[8];
+        std::vector<uint8_t> masks[8];
+        bool used[64] = {};
+        int64_t v1 = 0;
+        for (int z = 0; z < nz; ++z)
+            for (int y = 0; y < ny; ++y)
+                for (int x = 0; x < nx; ++x) {
+                    const bool bc = band(x, y, z);
+                    // V1 census: faces on the low side of this cell + its pressure
+                    if (x >= 1 && (bc || band(x - 1, y, z))) ++v1;
+                    if (y >= 1 && (bc || band(x, y - 1, z))) ++v1;
+                    if (z >= 1 && (bc || band(x, y, z - 1))) ++v1;
+                    if (!bc) continue;
+                    ++v1;
+                    int m = 0;
+                    if (x >= 1) m |= 1;
+                    if (x + 1 <= nx - 1) m |= 2;
+                    if (y >= 1) m |= 4;
+                    if (y + 1 <= ny - 1) m |= 8;
+                    if (z >= 1) m |= 16;
+                    if (z + 1 <= nz - 1) m |= 32;
+                    const int col = (x & 1) + 2 * (y & 1) + 4 * (z & 1);
+                    cells[col].push_back(static_cast<int32_t>(L.k.g.slot(x, y, z)));
+                    masks[col].push_back(static_cast<uint8_t>(m));
+                    used[m] = true;
+                }
+        L.counts[4] = v1;
+        for (int col = 0; col < 8; ++col) {
+            L.vk_n[col] = static_cast<int>(cells[col].size());
+            max_vk = std::max(max_vk, L.vk_n[col]);
+            L.vk_cells[col] = c->dalloc<int32_t>(L.vk_n[col]);
+            L.vk_mask[col] = c->dalloc<uint8_t>(L.vk_n[col]);
+            CK(cudaMemcpyAsync(L.vk_cells[col], cells[col].data(), cells[col].size() * sizeof(int32_t),
+                               cudaMemcpyHostToDevice, c->st));
+            CK(cudaMemcpyAsync(L.vk_mask[col], masks[col].data(), masks[col].size(), cudaMemcpyHostToDevice, c->st));
+            CK(cudaStreamSynchronize(c->st));
+        }
+        // local inverses C_i L~ C_i^T per face mask, scattered to the 7-slot layout
+        std::vector<double> ktab(64 * 49, 0.0);
+        for (int m = 0; m < 64; ++m) {
+            if (!used[m]) continue;
+            int slot[7], nb = 0;
+            for (int s = 0; s < 6; ++s)
+                if (m & (1 << s)) slot[nb++] = s;
+            slot[nb++] = 6;
+            double lm[49] = {}, inv[49];
+            for (int a = 0; a < nb; ++a)
+                for (int b2 = 0; b2 < nb; ++b2) {
+                    const int sa = slot[a], sb = slot[b2];
+                    double v = 0.0;
+                    if (sa < 6 && sb < 6) {
+                        if (sa == sb) v = 6.0 * L.k.eta_h2;
+                        else if ((sa >> 1) == (sb >> 1)) v = -L.k.eta_h2;  // uL-uR of one cell
+                    } else if (sa < 6 && sb == 6) {
+                        v = (sa & 1) ? -L.k.inv_h : L.k.inv_h;  // left face: cell is p_right
+                    } else if (sa == 6 && sb < 6) {
+                        v = (sb & 1) ? -L.k.inv_h : L.k.inv_h;
+                    } else {
+                        v = -p.gamma;
+                    }
+                    lm[a * nb + b2] = v;
+                }
+            small_inverse(lm, nb, inv);
+            for (int a = 0; a < nb; ++a)
+                for (int b2 = 0; b2 < nb; ++b2) ktab[m * 49 + slot[a] * 7 + slot[b2]] = inv[a * nb + b2];
+        }
+        L.ktab = c->dalloc<double>(64 * 49);
+        CK(cudaMemcpyAsync(L.ktab, ktab.data(), ktab.size() * sizeof(double), cudaMemcpyHostToDevice, c->st));
+        CK(cudaStreamSynchronize(c->st));
+    }
+    c->vk_delta = c->dalloc<double>(static_cast<int64_t>(max_vk) * 8);
+
+    // coarsest level: dense L~ in compact order, symmetric inverse (OD-4)
+    DevLevel& C = c->lv.back();
+    if (C.N > 20000) throw SmgError(SMG_ECAP, "coarsest system above dense cap 20000 (SPEC:365): add levels");
+    const int n = static_cast<int>(C.N);
+    c->nc = n;
+    const int nx = C.k.g.nx, ny = C.k.g.ny, nz = C.k.g.nz;
+    const int64_t nu = C.counts[0], nv = C.counts[1], nw = C.counts[2];
+    auto uid = [&](int x, int y, int z) -> int {
+        if (x < 1 || x > nx - 1 || y < 0 || y >= ny || z < 0 || z >= nz) return -1;
+        return static_cast<int>((static_cast<int64_t>(z) * ny + y) * (nx - 1) + (x - 1));
+    };
+    auto vid = [&](int x, int y, int z) -> int {
+        if (x < 0 || x >= nx || y < 1 || y > ny - 1 || z < 0 || z >= nz) return -1;
+        return static_cast<int>(nu + (static_cast<int64_t>(z) * (ny - 1) + (y - 1)) * nx + x);
+    };
+    auto wid = [&](int x, int y, int z) -> int {
+        if (x < 0 || x >= nx || y < 0 || y >= ny || z < 1 || z > nz - 1) return -1;
+        return static_cast<int>(nu + nv + (static_cast<int64_t>(z - 1) * ny + y) * nx + x);
+    };
+    auto pid = [&](int x, int y, int z) -> int {
+        if (x < 0 || x >= nx || y < 0 || y >= ny || z < 0 || z >= nz) return -1;
+        return static_cast<int>(nu + nv + nw + (static_cast<int64_t>(z) * ny + y) * nx + x);
+    };
+    std::vector<double> A(static_cast<size_t>(n) * n, 0.0);
+    std::vector<int32_t> slots(n);
+    const double e2 = C.k.eta_h2, ih = C.k.inv_h;
+    auto put = [&](int r, int col, double v) {
+        if (col >= 0) A[static_cast<size_t>(r) * n + col] += v;
+    };
+    for (int z = 0; z < nz; ++z)
+        for (int y = 0; y < ny; ++y)
+            for (int x = 0; x < nx; ++x) {
+                const int64_t sl = C.k.g.slot(x, y, z);
+                for (int comp = 0; comp < 3; ++comp) {
+                    auto fid = [&](int a, int b2, int c3) {
+                        return comp == 0 ? uid(a, b2, c3) : comp == 1 ? vid(a, b2, c3) : wid(a, b2, c3);
+                    };
+                    const int id = fid(x, y, z);
+                    if (id < 0) continue;
+                    slots[id] = static_cast<int32_t>(comp * C.k.g.fs + sl);
+                    // row order as ltilde_row of the oracle: diag, 6 nbrs, p_left, p_right
+                    put(id, id, 6.0 * e2);
+                    const int d[6][3] = {{-1, 0, 0}, {1, 0, 0}, {0, -1, 0}, {0, 1, 0}, {0, 0, -1}, {0, 0, 1}};
+                    for (int k = 0; k < 6; ++k) put(id, fid(x + d[k][0], y + d[k][1], z + d[k][2]), -e2);
+                    const int lx = x - (comp == 0), ly = y - (comp == 1), lz = z - (comp == 2);
+                    put(id, pid(lx, ly, lz), -ih);
+                    put(id, pid(x, y, z), ih);
+                }
+                const int id = pid(x, y, z);
+                slots[id] = static_cast<int32_t>(3 * C.k.g.fs + sl);
+                put(id, uid(x, y, z), ih);
+                put(id, uid(x + 1, y, z), -ih);
+                put(id, vid(x, y, z), ih);
+                put(id, vid(x, y + 1, z), -ih);
+                put(id, wid(x, y, z), ih);
+                put(id, wid(x, y, z + 1), -ih);
+                put(id, id, -p.gamma);
+            }
+    std::vector<double> K = dense_inverse_sym(std::move(A), n);
+    c->coarse_k = c->dalloc<double>(static_cast<int64_t>(n) * n);
+    c->coarse_slots = c->dalloc<int32_t>(n);
+    CK(cudaMemcpyAsync(c->coarse_k, K.data(), K.size() * sizeof(double), cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemcpyAsync(c->coarse_slots, slots.data(), slots.size() * sizeof(int32_t), cudaMemcpyHostToDevice, c->st));
+
+    // SQMR vectors and reduction scratch
+    const int64_t vl0 = vlen(c->lv[0]);
+    c->q = c->dalloc<double>(vl0);
+    c->d = c->dalloc<double>(vl0);
+    c->xs = c->dalloc<double>(vl0);
+    c->rhs = c->dalloc<double>(vl0);
+    int64_t maxN = 0;
+    for (auto& L : c->lv) maxN = std::max(maxN, L.N);
+    c->compact = c->dalloc<double>(maxN);
+    c->partials = c->dalloc<double>(2 * kRedBlocks);
+    c->dscal = c->dalloc<double>(8);
+    CK(cudaMallocHost(&c->hscal, 8 * sizeof(double)));
+    CK(cudaStreamSynchronize(c->st));
+}
+
+// ---- V-cycle orchestration (Alg. 1 + Alg. 3) ----
+void vanka_sym(smg_ctx* c, int l, double* x, const double* b) {
+    DevLevel& L = c->lv[l];
+    for (int pass = 0; pass < 2; ++pass)
+        for (int k = 0; k < 8; ++k) {
+            const int col = pass == 0 ? k : 7 - k;
+            launch_vanka_delta(L.k, x, b, L.vk_cells[col], L.vk_mask[col], L.vk_n[col], L.ktab, c->vk_delta, c->st);
+            launch_vanka_apply(L.k, x, L.vk_cells[col], L.vk_mask[col], L.vk_n[col], c->vk_delta, c->st);
+        }
+}
+
+// DGS phases (OD-1): forward 0,1 velocity red/black; 2..9 pressure parity
+// colours 0..7; reverse 10..17 pressure colours 7..0; 18,19 velocity black/red.
+constexpr int kDgsPhases = 20;
+void dgs_phase(smg_ctx* c, int l, double* x, const double* b, int ph) {
+    DevLevel& L = c->lv[l];
+    if (ph == 0 || ph == 1) {
+        launch_dgs_vel(L.k, x, b, ph, c->st);
+    } else if (ph >= 2 && ph <= 9) {
+        launch_dgs_pdelta(L.k, x, b, L.pd, ph - 2, c->st);
+        launch_dgs_papply(L.k, x, L.pd, c->st);
+    } else if (ph >= 10 && ph <= 17) {
+        launch_dgs_prev(L.k, x, b, 17 - ph, c->st);
+    } else if (ph == 18 || ph == 19) {
+        launch_dgs_vel(L.k, x, b, 19 - ph, c->st);
+    } else {
+        throw SmgError(SMG_EINVAL, "bad DGS phase");
+    }
+}
+
+void symmetric_dgs(smg_ctx* c, int l, double* x, const double* b) {
+    const int nph = (c->prm.flags & SMG_FLAG_SKIP_REVERSE_DGS) ? kDgsPhases / 2 : kDgsPhases;
+    for (int ph = 0; ph < nph; ++ph) dgs_phase(c, l, x, b, ph);
+}
+
+void smooth(smg_ctx* c, int l, double* x, const double* b) {
+    for (int k = 0; k < c->prm.nu; ++k) vanka_sym(c, l, x, b);
+    symmetric_dgs(c, l, x, b);
+    for (int k = 0; k < c->prm.nu; ++k) vanka_sym(c, l, x, b);
+}
+
+void coarse_solve(smg_ctx* c, const double* b, double* x) {
+    launch_coarse_gemv(c->coarse_k, c->coarse_slots, c->nc, b, x, c->st);
+}
+
+void vcycle(smg_ctx* c, int l, const double* b, double* x) {
+    DevLevel& L = c->lv[l];
+    if (l == static_cast<int>(c->lv.size()) - 1) { coarse_solve(c, b, x); return; }
+    CK(cudaMemsetAsync(x, 0, vlen(L) * sizeof(double), c->st));
+    smooth(c, l, x, b);
+    launch_apply(L.k, x, b, L.r, L.k.gamma, c->st);
+    DevLevel& C = c->lv[l + 1];
+    launch_restrict(L.k, C.k, L.r, C.b, c->st);
+    vcycle(c, l + 1, C.b, C.x);
+    launch_prolong_add(L.k, C.k, C.x, x, c->st);
+    smooth(c, l, x, b);
+}
+
+// ---- BLAS-1 helpers with host readback ----
+void dot2(smg_ctx* c, const double* a, const double* b, const double* e, const double* f, double* out2) {
+    launch_dot2(a, b, e, f, vlen(c->lv[0]), c->partials, c->dscal, c->st);
+    CK(cudaMemcpyAsync(c->hscal, c->dscal, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    out2[0] = c->hscal[0];
+    out2[1] = c->hscal[1];
+}
+
+// ---- SQMR, Alg. 4; b in c->rhs, x into c->xs ----
+int sqmr(smg_ctx* c, double tol, int maxit, smg_history* hist, int* status) {
+    DevLevel& F = c->lv[0];
+    const int64_t n = vlen(F);
+    double* s = F.b;
+    double* t = F.x;
+    double* r = F.r;
+    double sc[2];
+    const int64_t l0 = launch_count();
+    auto t0 = std::chrono::steady_clock::now();
+    CK(cudaEventRecord(c->ev0, c->st));
+    if (hist) hist->count = 0;
+    CK(cudaMemsetAsync(c->xs, 0, n * sizeof(double), c->st));
+    CK(cudaMemsetAsync(c->d, 0, n * sizeof(double), c->st));
+    dot2(c, c->rhs, c->rhs, nullptr, nullptr, sc);
+    const double bnorm = std::sqrt(sc[0]);
+    int iters = 0;
+    int st = SMG_MAX_ITERATIONS;
+    if (bnorm == 0.0) {
+        st = SMG_CONVERGED;
+    } else {
+        CK(cudaMemcpyAsync(s, c->rhs, n * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
+        vcycle(c, 0, s, t);
+        CK(cudaMemcpyAsync(c->q, t, n * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
+        dot2(c, t, t, s, c->q, sc);
+        double tau = std::sqrt(sc[0]), nu_old = 0.0, rho = sc[1];
+        if (std::fabs(rho) < 1e-300) st = SMG_BREAKDOWN;
+        for (int j = 1; j <= maxit && st == SMG_MAX_ITERATIONS; ++j) {
+            launch_apply(F.k, c->q, nullptr, t, 0.0, c->st);  // t = L q
+            dot2(c, c->q, t, nullptr, nullptr, sc);
+            const double sigma = sc[0];
+            if (std::fabs(sigma) < 1e-300) { st = SMG_BREAKDOWN; break; }
+            const double alpha = rho / sigma;
+            launch_axpy(s, t, -alpha, n, c->st);  // s = s - alpha t
+            vcycle(c, 0, s, t);                  // t = V(s)
+            dot2(c, t, t, s, t, sc);             // ||t||^2, rho_j = s.t
+            const double nu = std::sqrt(sc[0]) / tau;
+            const double cc = 1.0 / std::sqrt(1.0 + nu * nu);
+            tau = tau * nu * cc;
+            const double c2 = cc * cc;
+            launch_dx_update(c->d, c->xs, c->q, c2 * (nu_old * nu_old), c2 * alpha, n, c->st);
+            launch_apply(F.k, c->xs, c->rhs, r, 0.0, c->st);  // r = b - L x (true residual)
+            double rr[2];
+            dot2(c, r, r, nullptr, nullptr, rr);
+            const double rel = std::sqrt(rr[0]) / bnorm;
+            iters = j;
+            if (hist && hist->count < hist->capacity) {
+                hist->rel_residual[hist->count] = rel;
+                hist->seconds[hist->count] =
+                    std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+                hist->count++;
+            }
+            if (rel < tol) { st = SMG_CONVERGED; break; }
+            const double rho_new = sc[1];
+            if (std::fabs(rho_new) < 1e-300) { st = SMG_BREAKDOWN; break; }
+            const double beta = rho_new / rho;
+            launch_xpby(c->q, t, beta, n, c->st);  // q = t + beta q
+            rho = rho_new;
+            nu_old = nu;
+        }
+    }
+    CK(cudaEventRecord(c->ev1, c->st));
+    CK(cudaEventSynchronize(c->ev1));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+    c->timing.solve_ms = ms;
+    c->timing.iterations = iters;
+    c->timing.kernel_launches = launch_count() - l0;
+    *status = st;
+    return 0;
+}
+
+// ---- host <-> device compact vectors ----
+void upload(smg_ctx* c, int l, const double* host, double* dev_padded) {
+    DevLevel& L = c->lv[l];
+    CK(cudaMemcpyAsync(c->compact, host, L.N * sizeof(double), cudaMemcpyHostToDevice, c->st));
+    launch_unpack(L.k, c->compact, dev_padded, c->st);
+}
+void download(smg_ctx* c, int l, const double* dev_padded, double* host) {
+    DevLevel& L = c->lv[l];
+    launch_pack(L.k, dev_padded, c->compact, c->st);
+    CK(cudaMemcpyAsync(host, c->compact, L.N * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+}
+
+template <class F>
+int guard(smg_ctx* c, F&& f) {
+    try {
+        f();
+        return 0;
+    } catch (const SmgError& e) {
+        if (c) c->err = e.what();
+        return e.code;
+    } catch (const std::exception& e) {
+        if (c) c->err = e.what();
+        return SMG_EINVAL;
+    }
+}
+
+void check_level(smg_ctx* c, int l) {
+    if (l < 0 || l >= static_cast<int>(c->lv.size())) throw SmgError(SMG_EINVAL, "level out of range");
+}
+
+}  // namespace
+
+// ================================================================ C ABI =====
+extern "C" {
+
+const char* smg_version(void) { return "smg-b200 0.1 (sm_100a, fp64)"; }
+
+int smg_create(const smg_grid_desc* grid, const smg_params* params, int ngpu, const int* dev_ids, smg_ctx** out) {
+    if (!grid || !params || !out) return SMG_EINVAL;
+    *out = nullptr;
+    if (ngpu != 1) return SMG_EINVAL;  // multi-GPU z-slab decomposition: see DESIGN.md §7
+    auto c = std::make_unique<smg_ctx>();
+    c->grid = *grid;
+    c->prm = *params;
+    c->device = dev_ids ? dev_ids[0] : 0;
+    static thread_local std::string create_err;
+    const int rc = guard(c.get(), [&] { build(c.get()); });
+    if (rc != 0) {
+        create_err = c->err;
+        std::fprintf(stderr, "smg_create: %s\n", c->err.c_str());
+        return rc;
+    }
+    *out = c.release();
+    return 0;
+}
+
+void smg_destroy(smg_ctx* ctx) { delete ctx; }
+
+const char* smg_last_error(const smg_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int smg_num_levels(const smg_ctx* ctx) { return ctx ? static_cast<int>(ctx->lv.size()) : 0; }
+
+int64_t smg_level_ndof(const smg_ctx* ctx, int level, int64_t* out5) {
+    if (!ctx || level < 0 || level >= static_cast<int>(ctx->lv.size())) return SMG_EINVAL;
+    const DevLevel& L = ctx->lv[level];
+    if (out5)
+        for (int k = 0; k < 5; ++k) out5[k] = L.counts[k];
+    return L.N;
+}
+
+int smg_apply(smg_ctx* c, int level, int penalized, const double* x, double* y) {
+    return guard(c, [&] {
+        check_level(c, level);
+        DevLevel& L = c->lv[level];
+        upload(c, level, x, L.x);
+        launch_apply(L.k, L.x, nullptr, L.r, penalized ? L.k.gamma : 0.0, c->st);
+        download(c, level, L.r, y);
+    });
+}
+
+int smg_residual(smg_ctx* c, int level, const double* x, const double* b, double* r) {
+    return guard(c, [&] {
+        check_level(c, level);
+        DevLevel& L = c->lv[level];
+        upload(c, level, x, L.x);
+        upload(c, level, b, L.b);
+        launch_apply(L.k, L.x, L.b, L.r, L.k.gamma, c->st);
+        download(c, level, L.r, r);
+    });
+}
+
+int smg_smoother(smg_ctx* c, int level, int op, int arg, double* x, const double* b) {
+    return guard(c, [&] {
+        check_level(c, level);
+        DevLevel& L = c->lv[level];
+        upload(c, level, x, L.x);
+        upload(c, level, b, L.b);
+        if (op == 0) dgs_phase(c, level, L.x, L.b, arg);
+        else if (op == 1) symmetric_dgs(c, level, L.x, L.b);
+        else if (op == 2) {
+            if (arg < 0 || arg > 7) throw SmgError(SMG_EINVAL, "colour out of range");
+            launch_vanka_delta(L.k, L.x, L.b, L.vk_cells[arg], L.vk_mask[arg], L.vk_n[arg], L.ktab, c->vk_delta, c->st);
+            launch_vanka_apply(L.k, L.x, L.vk_cells[arg], L.vk_mask[arg], L.vk_n[arg], c->vk_delta, c->st);
+        } else if (op == 3) vanka_sym(c, level, L.x, L.b);
+        else if (op == 4) smooth(c, level, L.x, L.b);
+        else throw SmgError(SMG_EINVAL, "bad smoother op");
+        download(c, level, L.x, x);
+    });
+}
+
+int smg_restrict(smg_ctx* c, int level, const double* rf, double* rc) {
+    return guard(c, [&] {
+        check_level(c, level);
+        check_level(c, level + 1);
+        DevLevel &F = c->lv[level], &C = c->lv[level + 1];
+        upload(c, level, rf, F.r);
+        launch_restrict(F.k, C.k, F.r, C.b, c->st);
+        download(c, level + 1, C.b, rc);
+    });
+}
+
+int smg_prolong(smg_ctx* c, int level, const double* xc, double* xf) {
+    return guard(c, [&] {
+        check_level(c, level);
+        check_level(c, level + 1);
+        DevLevel &F = c->lv[level], &C = c->lv[level + 1];
+        upload(c, level + 1, xc, C.x);
+        CK(cudaMemsetAsync(F.x, 0, vlen(F) * sizeof(double), c->st));
+        launch_prolong_add(F.k, C.k, C.x, F.x, c->st);
+        download(c, level, F.x, xf);
+    });
+}
+
+int smg_coarse_solve(smg_ctx* c, const double* b, double* x) {
+    return guard(c, [&] {
+        const int l = static_cast<int>(c->lv.size()) - 1;
+        DevLevel& C = c->lv[l];
+        upload(c, l, b, C.b);
+        coarse_solve(c, C.b, C.x);
+        download(c, l, C.x, x);
+    });
+}
+
+int smg_vcycle(smg_ctx* c, const double* b, double* x) {
+    return guard(c, [&] {
+        DevLevel& F = c->lv[0];
+        upload(c, 0, b, F.b);
+        vcycle(c, 0, F.b, F.x);
+        download(c, 0, F.x, x);
+    });
+}
+
+int smg_set_rhs(smg_ctx* c, const double* b) {
+    return guard(c, [&] {
+        upload(c, 0, b, c->rhs);
+        CK(cudaStreamSynchronize(c->st));
+        c->rhs_set = true;
+    });
+}
+
+int smg_solve_resident(smg_ctx* c, double tol, int maxit, smg_history* hist, int* status) {
+    return guard(c, [&] {
+        if (!c->rhs_set) throw SmgError(SMG_EINVAL, "smg_set_rhs not called");
+        if (!status) throw SmgError(SMG_EINVAL, "status is null");
+        sqmr(c, tol, maxit, hist, status);
+    });
+}
+
+int smg_get_solution(smg_ctx* c, double* x) {
+    return guard(c, [&] { download(c, 0, c->xs, x); });
+}
+
+int smg_sqmr_solve(smg_ctx* c, const double* b, double* x, double tol, int maxit, smg_history* hist, int* status) {
+    return guard(c, [&] {
+        if (!b || !x || !status) throw SmgError(SMG_EINVAL, "null argument");
+        CK(cudaEventRecord(c->ev0, c->st));
+        upload(c, 0, b, c->rhs);
+        CK(cudaEventRecord(c->ev1, c->st));
+        CK(cudaEventSynchronize(c->ev1));
+        float h2d = 0.f;
+        CK(cudaEventElapsedTime(&h2d, c->ev0, c->ev1));
+        c->rhs_set = true;
+        sqmr(c, tol, maxit, hist, status);
+        CK(cudaEventRecord(c->ev0, c->st));
+        download(c, 0, c->xs, x);
+        CK(cudaEventRecord(c->ev1, c->st));
+        CK(cudaEventSynchronize(c->ev1));
+        float d2h = 0.f;
+        CK(cudaEventElapsedTime(&d2h, c->ev0, c->ev1));
+        c->timing.h2d_ms = h2d;
+        c->timing.d2h_ms = d2h;
+    });
+}
+
+int smg_last_timing(const smg_ctx* c, smg_timing* out) {
+    if (!c || !out) return SMG_EINVAL;
+    *out = c->timing;
+    return 0;
+}
+
+int smg_time_kernel(smg_ctx* c, int which, int reps, double* avg_ms) {
+    return guard(c, [&] {
+        if (reps < 1 || !avg_ms) throw SmgError(SMG_EINVAL, "bad reps");
+        DevLevel& F = c->lv[0];
+        auto one = [&] {
+            switch (which) {
+                case 0: launch_apply(F.k, c->q, nullptr, F.r, 0.0, c->st); break;
+                case 1: launch_apply(F.k, c->xs, c->rhs, F.r, F.k.gamma, c->st); break;
+                case 2: symmetric_dgs(c, 0, F.x, F.b); break;
+                case 3: vcycle(c, 0, F.b, F.x); break;
+                default: throw SmgError(SMG_EINVAL, "bad kernel id");
+            }
+        };
+        one();
+        CK(cudaEventRecord(c->ev0, c->st));
+        for (int k = 0; k < reps; ++k) one();
+        CK(cudaEventRecord(c->ev1, c->st));
+        CK(cudaEventSynchronize(c->ev1));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+        *avg_ms = ms / reps;
+    });
+}
+
+void* smg_host_alloc(int64_t bytes) {
+    void* p = nullptr;
+    if (cudaMallocHost(&p, static_cast<size_t>(bytes)) != cudaSuccess) return nullptr;
+    return p;
+}
+void smg_host_free(void* p) {
+    if (p) cudaFreeHost(p);
+}
+
+int smg_forcing(const smg_grid_desc* grid, int kind, uint64_t seed, double* b, int threads) {
+    if (!grid || !b || kind < 0 || kind > 2 || grid->dim != 3) return SMG_EINVAL;
+    const int nx = grid->nx, ny = grid->ny, nz = grid->nz;
+    const double h = grid->h;
+    double amp[3][8];
+    int kw[3][8][3];
+    if (kind == 1)
+        for (int c = 0; c < 3; ++c)
+            for (int md = 0; md < 8; ++md) {
+                for (int a = 0; a < 3; ++a) kw[c][md][a] = 1 + static_cast<int>(key5(seed, 16 + c, md, a, 0) % 8);
+                const double u1 = 1.0 - unit01(key5(seed, 32 + c, md, 0, 1));
+                const double u2 = unit01(key5(seed, 32 + c, md, 0, 2));
+                amp[c][md] = std::sqrt(-2.0 * std::log(u1)) * std::cos(6.283185307179586 * u2);
+            }
+    const int64_t nu = static_cast<int64_t>(nx - 1) * ny * nz, nv = static_cast<int64_t>(nx) * (ny - 1) * nz;
+    const int64_t nw = static_cast<int64_t>(nx) * ny * (nz - 1), np = static_cast<int64_t>(nx) * ny * nz;
+    // one task per (component, z-plane)
+    const int64_t tasks = 3 * static_cast<int64_t>(nz);
+    host_parallel(tasks, threads < 1 ? 1 : threads, [&](int64_t lo, int64_t hi) {
+        for (int64_t t = lo; t < hi; ++t) {
+            const int c = static_cast<int>(t / nz), z = static_cast<int>(t % nz);
+            const int ex = nx + (c == 0 ? 1 : 0), ey = ny + (c == 1 ? 1 : 0), ez = nz + (c == 2 ? 1 : 0);
+            if (z >= ez) continue;
+            for (int y = 0; y < ey; ++y)
+                for (int x = 0; x < ex; ++x) {
+                    int64_t id;
+                    if (c == 0) {
+                        if (x < 1 || x > nx - 1) continue;
+                        id = (static_cast<int64_t>(z) * ny + y) * (nx - 1) + (x - 1);
+                    } else if (c == 1) {
+                        if (y < 1 || y > ny - 1) continue;
+                        id = nu + (static_cast<int64_t>(z) * (ny - 1) + (y - 1)) * nx + x;
+                    } else {
+                        if (z < 1 || z > nz - 1) continue;
+                        id = nu + nv + (static_cast<int64_t>(z - 1) * ny + y) * nx + x;
+                    }
+                    const double u = 2.0 * unit01(key5(seed, c, x, y, z)) - 1.0;
+                    double v;
+                    if (kind == 0) v = u;
+                    else if (kind == 2) v = (c == 0 ? 1.0 : 0.0) + 0.1 * u;
+                    else {
+                        const int p[3] = {x, y, z};
+                        double xyz[3];
+                        for (int a = 0; a < 3; ++a) xyz[a] = (a == c) ? p[a] * h : (p[a] + 0.5) * h;
+                        double s = 0.0;
+                        for (int md = 0; md < 8; ++md)
+                            s = s + amp[c][md] * std::sin(3.141592653589793 * kw[c][md][0] * xyz[0]) *
+                                        std::sin(3.141592653589793 * kw[c][md][1] * xyz[1]) *
+                                        std::sin(3.141592653589793 * kw[c][md][2] * xyz[2]);
+                        v = s;
+                    }
+                    b[id] = v;
+                }
+        }
+    });
+    // pressure rows: b_p = 0 (zero divergence RHS)
+    for (int64_t k = 0; k < np; ++k) b[nu + nv + nw + k] = 0.0;
+    return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,555 @@
+// kernels.cu — sm_100a CUDA kernels of the MG-SQMR Stokes hot path.
+//
+// Every per-point formula follows the arithmetic contract of DESIGN.md §4
+// (same operand order as oracle/stokes_oracle.cpp; compiled with -fmad=false so
+// no contraction), which makes each kernel bit-identical to the CPU oracle.
+// Only the BLAS-1 reductions use a different (fixed, deterministic) order.
+//
+// Reference: SPEC.md modules discretization (apply),
+// smoothers (DGS SPEC:258-283, Vanka SPEC:284-301), transfer,
+// multigrid coarse solve, krylov.
+#include <atomic>
+#include <cstdint>
+
+#include "smg_internal.h"
+
+namespace smg {
+
+static std::atomic<int64_t> g_launches{0};
+int64_t launch_count() { return g_launches.load(); }
+static inline void count() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+namespace {
+
+constexpr int BX = 32, BY = 8;
+
+inline dim3 cell_grid(const Geom& g) { return dim3((g.nx + BX - 1) / BX, (g.ny + BY - 1) / BY, g.nz); }
+
+struct Cell {
+    int x, y, z;
+    int64_t i;
+};
+
+__device__ __forceinline__ bool thread_cell(const Geom& g, Cell& c) {
+    c.x = blockIdx.x * BX + threadIdx.x;
+    c.y = blockIdx.y * BY + threadIdx.y;
+    c.z = blockIdx.z;
+    if (c.x >= g.nx || c.y >= g.ny) return false;
+    c.i = g.slot(c.x, c.y, c.z);
+    return true;
+}
+
+__device__ __forceinline__ bool band_cell(const LevelK& L, int x, int y, int z) {
+    const Geom& g = L.g;
+    return x < L.bw || y < L.bw || z < L.bw || x >= g.nx - L.bw || y >= g.ny - L.bw || z >= g.nz - L.bw;
+}
+
+// Momentum row of L~ at the face stored at slot i of field F (stride of the
+// normal axis sn): eta/h^2 (6 u - sum of 6 neighbours, order x-,x+,y-,y+,z-,z+)
+// + (p_right - p_left)/h.
+__device__ __forceinline__ double mom(const LevelK& L, const double* __restrict__ F,
+                                      const double* __restrict__ P, int64_t i, int64_t sn) {
+    const int64_t sy = L.g.sy, sz = L.g.sz;
+    double s = F[i - 1] + F[i + 1];
+    s = s + F[i - sy];
+    s = s + F[i + sy];
+    s = s + F[i - sz];
+    s = s + F[i + sz];
+    const double lap = 6.0 * F[i] - s;
+    return L.eta_h2 * lap + (P[i] - P[i - sn]) * L.inv_h;
+}
+
+// Continuity row of L~ at cell slot i: -(div u)/h - gamma p.
+__device__ __forceinline__ double cont(const LevelK& L, const double* __restrict__ U,
+                                       const double* __restrict__ V, const double* __restrict__ W,
+                                       const double* __restrict__ P, int64_t i, double gamma) {
+    const double div = (U[i + 1] - U[i]) + (V[i + L.g.sy] - V[i]) + (W[i + L.g.sz] - W[i]);
+    return -div * L.inv_h - gamma * P[i];
+}
+
+// ------------------------------------------------------------- apply ------
+__global__ void k_apply(LevelK L, const double* __restrict__ X, const double* __restrict__ B,
+                        double* __restrict__ Y, double gamma) {
+    Cell c;
+    if (!thread_cell(L.g, c)) return;
+    const Geom& g = L.g;
+    const int64_t fs = g.fs;
+    const double *U = X, *V = X + fs, *W = X + 2 * fs, *P = X + 3 * fs;
+    const int64_t i = c.i;
+    if (c.x >= 1) {
+        const double y = mom(L, U, P, i, 1);
+        Y[i] = B ? B[i] - y : y;
+    }
+    if (c.y >= 1) {
+        const double y = mom(L, V, P, i, g.sy);
+        Y[fs + i] = B ? B[fs + i] - y : y;
+    }
+    if (c.z >= 1) {
+        const double y = mom(L, W, P, i, g.sz);
+        Y[2 * fs + i] = B ? B[2 * fs + i] - y : y;
+    }
+    const double y = cont(L, U, V, W, P, i, gamma);
+    Y[3 * fs + i] = B ? B[3 * fs + i] - y : y;
+}
+
+// ---------------------------------------------------------------- DGS ------
+// Velocity phase (Alg. 2 with M_.j = e_j): GS on V2 faces of one red-black
+// colour, x_f += (b_f - (L~x)_f) / d_v.  Same-colour faces do not couple.
+__global__ void k_dgs_vel(LevelK L, double* __restrict__ X, const double* __restrict__ B, int colour) {
+    Cell c;
+    if (!thread_cell(L.g, c)) return;
+    if (((c.x + c.y + c.z) & 1) != colour) return;
+    const Geom& g = L.g;
+    const int64_t fs = g.fs, i = c.i;
+    double *U = X, *V = X + fs, *W = X + 2 * fs;
+    const double* P = X + 3 * fs;
+    const bool here = band_cell(L, c.x, c.y, c.z);
+    if (c.x >= 1 && !here && !band_cell(L, c.x - 1, c.y, c.z)) {
+        const double r = B[i] - mom(L, U, P, i, 1);
+        U[i] = U[i] + r / L.dv;
+    }
+    if (c.y >= 1 && !here && !band_cell(L, c.x, c.y - 1, c.z)) {
+        const double r = B[fs + i] - mom(L, V, P, i, g.sy);
+        V[i] = V[i] + r / L.dv;
+    }
+    if (c.z >= 1 && !here && !band_cell(L, c.x, c.y, c.z - 1)) {
+        const double r = B[2 * fs + i] - mom(L, W, P, i, g.sz);
+        W[i] = W[i] + r / L.dv;
+    }
+}
+
+__device__ __forceinline__ int pcolour(const Cell& c) { return (c.x & 1) + 2 * (c.y & 1) + 4 * (c.z & 1); }
+
+// Forward pressure phase, part 1: delta_C = (b_C - (L~x)_C) / d_p on V2 cells of
+// the parity colour (8 colours, OD-1), 0 elsewhere (written for every cell).
+__global__ void k_dgs_pdelta(LevelK L, const double* __restrict__ X, const double* __restrict__ B,
+                             double* __restrict__ D, int colour) {
+    Cell c;
+    if (!thread_cell(L.g, c)) return;
+    const int64_t fs = L.g.fs, i = c.i;
+    double d = 0.0;
+    if (pcolour(c) == colour && !band_cell(L, c.x, c.y, c.z)) {
+        const double r = B[3 * fs + i] - cont(L, X, X + fs, X + 2 * fs, X + 3 * fs, i, L.gamma);
+        d = r / L.dp;
+    }
+    D[i] = d;
+}
+
+// Forward pressure phase, part 2: x += sum_C delta_C M_.C in gather form
+// (faces: (delta_left - delta_right)/h; pressures: eta/h^2 (6 delta - sum nbr)).
+__global__ void k_dgs_papply(LevelK L, double* __restrict__ X, const double* __restrict__ D) {
+    Cell c;
+    if (!thread_cell(L.g, c)) return;
+    const Geom& g = L.g;
+    const int64_t fs = g.fs, i = c.i, sy = g.sy, sz = g.sz;
+    const double dc = D[i];
+    if (c.x >= 1) X[i] = X[i] + (D[i - 1] - dc) * L.inv_h;
+    if (c.y >= 1) X[fs + i] = X[fs + i] + (D[i - sy] - dc) * L.inv_h;
+    if (c.z >= 1) X[2 * fs + i] = X[2 * fs + i] + (D[i - sz] - dc) * L.inv_h;
+    double s = D[i - 1] + D[i + 1];
+    s = s + D[i - sy];
+    s = s + D[i + sy];
+    s = s + D[i - sz];
+    s = s + D[i + sz];
+    X[3 * fs + i] = X[3 * fs + i] + L.eta_h2 * (6.0 * dc - s);
+}
+
+// Reverse (left-preconditioned) pressure phase: x_C += m_C^T (b - L~x) / d_p on
+// V2 cells of the parity colour (radius-2 gather; same-colour cells are never
+// face neighbours and never read each other's pressure: one pass is race-free).
+__global__ void k_dgs_prev(LevelK L, double* __restrict__ X, const double* __restrict__ B, int colour) {
+    Cell c;
+    if (!thread_cell(L.g, c)) return;
+    if (pcolour(c) != colour || band_cell(L, c.x, c.y, c.z)) return;
+    const Geom& g = L.g;
+    const int64_t fs = g.fs, i = c.i, sy = g.sy, sz = g.sz;
+    const double *U = X, *V = X + fs, *W = X + 2 * fs;
+    double* P = X + 3 * fs;
+    const double *BU = B, *BV = B + fs, *BW = B + 2 * fs, *BP = B + 3 * fs;
+    const double ruL = BU[i] - mom(L, U, P, i, 1);
+    const double ruR = BU[i + 1] - mom(L, U, P, i + 1, 1);
+    const double rvL = BV[i] - mom(L, V, P, i, sy);
+    const double rvR = BV[i + sy] - mom(L, V, P, i + sy, sy);
+    const double rwL = BW[i] - mom(L, W, P, i, sz);
+    const double rwR = BW[i + sz] - mom(L, W, P, i + sz, sz);
+    const double fl = ((ruR - ruL) + (rvR - rvL)) + (rwR - rwL);
+    const double rc = BP[i] - cont(L, U, V, W, P, i, L.gamma);
+    double s = BP[i - 1] - cont(L, U, V, W, P, i - 1, L.gamma);
+    s = s + (BP[i + 1] - cont(L, U, V, W, P, i + 1, L.gamma));
+    s = s + (BP[i - sy] - cont(L, U, V, W, P, i - sy, L.gamma));
+    s = s + (BP[i + sy] - cont(L, U, V, W, P, i + sy, L.gamma));
+    s = s + (BP[i - sz] - cont(L, U, V, W, P, i - sz, L.gamma));
+    s = s + (BP[i + sz] - cont(L, U, V, W, P, i + sz, L.gamma));
+    const double cj = fl * L.inv_h + L.eta_h2 * (6.0 * rc - s);
+    P[i] = P[i] + cj / L.dp;
+}
+
+// --------------------------------------------------------------- Vanka ------
+// One colour phase, Jacobi within the colour: part 1 computes every block's
+// correction from the pre-phase state (slots [uL,uR,vL,vR,wL,wR,p]).
+__global__ void k_vanka_delta(LevelK L, const double* __restrict__ X, const double* __restrict__ B,
+                              const int32_t* __restrict__ cells, const uint8_t* __restrict__ masks, int n,
+                              const double* __restrict__ ktab, double* __restrict__ delta) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const Geom& g = L.g;
+    const int64_t fs = g.fs, sy = g.sy, sz = g.sz, i = cells[t];
+    const int m = masks[t];
+    const double *U = X, *V = X + fs, *W = X + 2 * fs, *P = X + 3 * fs;
+    double r[7];
+    r[0] = (m & 1) ? B[i] - mom(L, U, P, i, 1) : 0.0;
+    r[1] = (m & 2) ? B[i + 1] - mom(L, U, P, i + 1, 1) : 0.0;
+    r[2] = (m & 4) ? B[fs + i] - mom(L, V, P, i, sy) : 0.0;
+    r[3] = (m & 8) ? B[fs + i + sy] - mom(L, V, P, i + sy, sy) : 0.0;
+    r[4] = (m & 16) ? B[2 * fs + i] - mom(L, W, P, i, sz) : 0.0;
+    r[5] = (m & 32) ? B[2 * fs + i + sz] - mom(L, W, P, i + sz, sz) : 0.0;
+    r[6] = B[3 * fs + i] - cont(L, U, V, W, P, i, L.gamma);
+    const double* K = ktab + m * 49;
+#pragma unroll
+    for (int s = 0; s < 7; ++s) {
+        double acc = 0.0;
+#pragma unroll
+        for (int q = 0; q < 7; ++q) acc = acc + K[s * 7 + q] * r[q];
+        delta[static_cast<int64_t>(t) * 8 + s] = acc;
+    }
+}
+
+__global__ void k_vanka_apply(LevelK L, double* __restrict__ X, const int32_t* __restrict__ cells,
+                              const uint8_t* __restrict__ masks, int n, const double* __restrict__ delta) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const Geom& g = L.g;
+    const int64_t fs = g.fs, i = cells[t];
+    const int m = masks[t];
+    const double* d = delta + static_cast<int64_t>(t) * 8;
+    if (m & 1) X[i] = X[i] + d[0];
+    if (m & 2) X[i + 1] = X[i + 1] + d[1];
+    if (m & 4) X[fs + i] = X[fs + i] + d[2];
+    if (m & 8) X[fs + i + g.sy] = X[fs + i + g.sy] + d[3];
+    if (m & 16) X[2 * fs + i] = X[2 * fs + i] + d[4];
+    if (m & 32) X[2 * fs + i + g.sz] = X[2 * fs + i + g.sz] + d[5];
+    X[3 * fs + i] = X[3 * fs + i] + d[6];
+}
+
+// ------------------------------------------------------------ transfer ------
+// Restriction R = (1/8) P^T, gathered per coarse DOF.  Weight
+// tables: normal {1/2, 1, 1/2} over fine faces 2I-1..2I+1, tangential
+// {1/4, 3/4, 3/4, 1/4} over fine cells 2J-1..2J+2; summation order: normal
+// innermost, then the tangential axes in x,y,z order.
+__device__ __forceinline__ double restrict_face(const double* __restrict__ R, int64_t base, int64_t sn,
+                                                int64_t sa, int64_t sb) {
+    // base = fine slot of (normal 2I, tangential 2J, 2K); legs offset from it
+    const double wI[3] = {0.5, 1.0, 0.5};
+    const double wT[4] = {0.25, 0.75, 0.75, 0.25};
+    double acc_b = 0.0;
+#pragma unroll
+    for (int ib = 0; ib < 4; ++ib) {
+        double acc_a = 0.0;
+#pragma unroll
+        for (int ia = 0; ia < 4; ++ia) {
+            const int64_t o = base + (ib - 1) * sb + (ia - 1) * sa;
+            double sn_ = 0.0;
+#pragma unroll
+            for (int in = 0; in < 3; ++in) sn_ = sn_ + wI[in] * R[o + (in - 1) * sn];
+            acc_a = acc_a + wT[ia] * sn_;
+        }
+        acc_b = acc_b + wT[ib] * acc_a;
+    }
+    return 0.125 * acc_b;
+}
+
+__global__ void k_restrict(LevelK F, LevelK C, const double* __restrict__ R, double* __restrict__ BC) {
+    Cell c;
+    if (!thread_cell(C.g, c)) return;
+    const Geom &fg = F.g, &cg = C.g;
+    const int64_t ffs = fg.fs, cfs = cg.fs;
+    const int64_t fb = fg.slot(2 * c.x, 2 * c.y, 2 * c.z);
+    const int64_t sx = 1, sy = fg.sy, sz = fg.sz;
+    if (c.x >= 1) BC[c.i] = restrict_face(R, fb, sx, sy, sz);                   // u: a = y, b = z
+    if (c.y >= 1) BC[cfs + c.i] = restrict_face(R + ffs, fb, sy, sx, sz);       // v: a = x, b = z
+    if (c.z >= 1) BC[2 * cfs + c.i] = restrict_face(R + 2 * ffs, fb, sz, sx, sy);  // w: a = x, b = y
+    const double* RP = R + 3 * ffs;
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int ii = 0; ii < 2; ++ii) s = s + RP[fb + k * sz + j * sy + ii];
+    BC[3 * cfs + c.i] = 0.125 * s;
+}
+
+// Prolongation x_f += P e_c.  Tangential legs of fine index J:
+// (J>>1, 3/4) then (J odd ? (J>>1)+1 : (J>>1)-1, 1/4); normal: I even ->
+// (I/2, 1), I odd -> ((I-1)/2, 1/2), ((I+1)/2, 1/2).  Legs to wall/ghost slots
+// read 0 (dropped, no renormalisation).
+__device__ __forceinline__ double prolong_face(const double* __restrict__ E, const Geom& cg, int comp, int fx,
+                                               int fy, int fz) {
+    int f[3] = {fx, fy, fz};
+    const int ta = comp == 0 ? 1 : 0, tb = comp == 2 ? 1 : 2;
+    int ni[2];
+    double nw[2];
+    int nn;
+    const int I = f[comp];
+    if ((I & 1) == 0) {
+        ni[0] = I >> 1;
+        nw[0] = 1.0;
+        nn = 1;
+    } else {
+        ni[0] = (I - 1) >> 1;
+        ni[1] = (I + 1) >> 1;
+        nw[0] = 0.5;
+        nw[1] = 0.5;
+        nn = 2;
+    }
+    const int pa = f[ta] >> 1, pb = f[tb] >> 1;
+    const int ia_[2] = {pa, (f[ta] & 1) ? pa + 1 : pa - 1};
+    const int ib_[2] = {pb, (f[tb] & 1) ? pb + 1 : pb - 1};
+    const double wt[2] = {0.75, 0.25};
+    double acc_b = 0.0;
+    for (int ib = 0; ib < 2; ++ib) {
+        double acc_a = 0.0;
+        for (int ia = 0; ia < 2; ++ia) {
+            double acc_n = 0.0;
+            for (int in = 0; in < nn; ++in) {
+                int cc[3];
+                cc[comp] = ni[in];
+                cc[ta] = ia_[ia];
+                cc[tb] = ib_[ib];
+                acc_n = acc_n + nw[in] * E[cg.slot(cc[0], cc[1], cc[2])];
+            }
+            acc_a = acc_a + wt[ia] * acc_n;
+        }
+        acc_b = acc_b + wt[ib] * acc_a;
+    }
+    return acc_b;
+}
+
+__global__ void k_prolong_add(LevelK F, LevelK C, const double* __restrict__ E, double* __restrict__ X) {
+    Cell c;
+    if (!thread_cell(F.g, c)) return;
+    const Geom &fg = F.g, &cg = C.g;
+    const int64_t ffs = fg.fs, cfs = cg.fs;
+    if (c.x >= 1) X[c.i] = X[c.i] + prolong_face(E, cg, 0, c.x, c.y, c.z);
+    if (c.y >= 1) X[ffs + c.i] = X[ffs + c.i] + prolong_face(E + cfs, cg, 1, c.x, c.y, c.z);
+    if (c.z >= 1) X[2 * ffs + c.i] = X[2 * ffs + c.i] + prolong_face(E + 2 * cfs, cg, 2, c.x, c.y, c.z);
+    X[3 * ffs + c.i] = X[3 * ffs + c.i] + E[3 * cfs + cg.slot(c.x >> 1, c.y >> 1, c.z >> 1)];
+}
+
+// ------------------------------------------------------------- coarse ------
+// x = K b with the symmetric dense inverse K (OD-4).  Fixed order: partial sums
+// over 64-column chunks, chunks accumulated in ascending order (same as the
+// oracle).  K symmetric => column j of K is row j, read coalesced across rows.
+constexpr int CG_ROWS = 32, CG_LANES = 32;
+__global__ void k_coarse_gemv(const double* __restrict__ K, const int32_t* __restrict__ slots, int n,
+                              const double* __restrict__ B, double* __restrict__ X) {
+    extern __shared__ double part[];  // [nchunks][CG_ROWS]
+    const int row = blockIdx.x * CG_ROWS + threadIdx.x;
+    const int nchunks = (n + 63) / 64;
+    for (int ch = threadIdx.y; ch < nchunks; ch += CG_LANES) {
+        double p = 0.0;
+        if (row < n) {
+            const int j1 = min(n, ch * 64 + 64);
+            for (int j = ch * 64; j < j1; ++j) p = p + K[static_cast<int64_t>(j) * n + row] * __ldg(&B[slots[j]]);
+        }
+        part[ch * CG_ROWS + threadIdx.x] = p;
+    }
+    __syncthreads();
+    if (threadIdx.y == 0 && row < n) {
+        double s = 0.0;
+        for (int ch = 0; ch < nchunks; ++ch) s = s + part[ch * CG_ROWS + threadIdx.x];
+        X[slots[row]] = s;
+    }
+}
+
+// --------------------------------------------------------- pack/unpack ------
+// Compact FieldVector order: u (x in 1..nx-1), v, w, p, each lexicographic with
+// x fastest.
+__global__ void k_pack(LevelK L, const double* __restrict__ X, double* __restrict__ out, int unpack) {
+    Cell c;
+    if (!thread_cell(L.g, c)) return;
+    const Geom& g = L.g;
+    const int64_t nx = g.nx, ny = g.ny, nz = g.nz, fs = g.fs;
+    const int64_t nu = (nx - 1) * ny * nz, nv = nx * (ny - 1) * nz, nw = nx * ny * (nz - 1);
+    const int64_t x = c.x, y = c.y, z = c.z;
+    if (x >= 1) {
+        const int64_t k = (z * ny + y) * (nx - 1) + (x - 1);
+        if (unpack) const_cast<double*>(X)[c.i] = out[k]; else out[k] = X[c.i];
+    }
+    if (y >= 1) {
+        const int64_t k = nu + (z * (ny - 1) + (y - 1)) * nx + x;
+        if (unpack) const_cast<double*>(X)[fs + c.i] = out[k]; else out[k] = X[fs + c.i];
+    }
+    if (z >= 1) {
+        const int64_t k = nu + nv + ((z - 1) * ny + y) * nx + x;
+        if (unpack) const_cast<double*>(X)[2 * fs + c.i] = out[k]; else out[k] = X[2 * fs + c.i];
+    }
+    const int64_t k = nu + nv + nw + (z * ny + y) * nx + x;
+    if (unpack) const_cast<double*>(X)[3 * fs + c.i] = out[k]; else out[k] = X[3 * fs + c.i];
+}
+
+// ------------------------------------------------------------- BLAS-1 ------
+constexpr int RED_T = 256;
+
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = v + __shfl_down_sync(0xffffffffu, v, o);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) sh[w] = v;
+    __syncthreads();
+    double r = 0.0;
+    if (w == 0) {
+        r = (l < RED_T / 32) ? sh[l] : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) r = r + __shfl_down_sync(0xffffffffu, r, o);
+    }
+    __syncthreads();
+    return r;
+}
+
+__global__ void __launch_bounds__(RED_T) k_dot2(const double* __restrict__ a, const double* __restrict__ b,
+                                                const double* __restrict__ c, const double* __restrict__ d,
+                                                int64_t n, double* __restrict__ partials) {
+    __shared__ double sh[RED_T / 32];
+    double s0 = 0.0, s1 = 0.0;
+    const int64_t n2 = n / 2;
+    const double2* a2 = reinterpret_cast<const double2*>(a);
+    const double2* b2 = reinterpret_cast<const double2*>(b);
+    const double2* c2 = reinterpret_cast<const double2*>(c);
+    const double2* d2 = reinterpret_cast<const double2*>(d);
+    for (int64_t k = blockIdx.x * (int64_t)RED_T + threadIdx.x; k < n2; k += (int64_t)gridDim.x * RED_T) {
+        const double2 x = a2[k], y = b2[k];
+        s0 = s0 + x.x * y.x;
+        s0 = s0 + x.y * y.y;
+        if (c) {
+            const double2 u = c2[k], v = d2[k];
+            s1 = s1 + u.x * v.x;
+            s1 = s1 + u.y * v.y;
+        }
+    }
+    const double t0 = block_sum(s0, sh);
+    const double t1 = c ? block_sum(s1, sh) : 0.0;
+    if (threadIdx.x == 0) {
+        partials[blockIdx.x] = t0;
+        partials[gridDim.x + blockIdx.x] = t1;
+    }
+}
+
+__global__ void k_dot_final(const double* __restrict__ partials, int nb, double* __restrict__ out) {
+    // one warp per output; lanes sum strided subsets in order, then a fixed tree
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    const double* p = partials + w * nb;
+    double s = 0.0;
+    for (int k = l; k < nb; k += 32) s = s + p[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s = s + __shfl_down_sync(0xffffffffu, s, o);
+    if (l == 0) out[w] = s;
+}
+
+__global__ void k_axpy(double* __restrict__ y, const double* __restrict__ x, double alpha, int64_t n) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
+        y[k] = y[k] + alpha * x[k];
+}
+__global__ void k_xpby(double* __restrict__ y, const double* __restrict__ x, double beta, int64_t n) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
+        y[k] = x[k] + beta * y[k];
+}
+__global__ void k_dx_update(double* __restrict__ d, double* __restrict__ x, const double* __restrict__ q,
+                            double cd, double cq, int64_t n) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+        const double dn = cd * d[k] + cq * q[k];
+        d[k] = dn;
+        x[k] = x[k] + dn;
+    }
+}
+
+inline int stream_blocks(int64_t n) {
+    const int64_t b = (n + 255) / 256;
+    return static_cast<int>(b < 148 * 16 ? b : 148 * 16);
+}
+
+}  // namespace
+
+// ----------------------------------------------------------- launchers ------
+void launch_apply(const LevelK& L, const double* x, const double* b, double* y, double gamma, cudaStream_t s) {
+    k_apply<<<cell_grid(L.g), dim3(BX, BY), 0, s>>>(L, x, b, y, gamma);
+    count();
+}
+void launch_dgs_vel(const LevelK& L, double* x, const double* b, int colour, cudaStream_t s) {
+    k_dgs_vel<<<cell_grid(L.g), dim3(BX, BY), 0, s>>>(L, x, b, colour);
+    count();
+}
+void launch_dgs_pdelta(const LevelK& L, const double* x, const double* b, double* delta, int colour,
+                       cudaStream_t s) {
+    k_dgs_pdelta<<<cell_grid(L.g), dim3(BX, BY), 0, s>>>(L, x, b, delta, colour);
+    count();
+}
+void launch_dgs_papply(const LevelK& L, double* x, const double* delta, cudaStream_t s) {
+    k_dgs_papply<<<cell_grid(L.g), dim3(BX, BY), 0, s>>>(L, x, delta);
+    count();
+}
+void launch_dgs_prev(const LevelK& L, double* x, const double* b, int colour, cudaStream_t s) {
+    k_dgs_prev<<<cell_grid(L.g), dim3(BX, BY), 0, s>>>(L, x, b, colour);
+    count();
+}
+void launch_vanka_delta(const LevelK& L, const double* x, const double* b, const int32_t* cells,
+                        const uint8_t* masks, int ncells, const double* ktab, double* delta, cudaStream_t s) {
+    if (ncells <= 0) return;
+    k_vanka_delta<<<(ncells + 127) / 128, 128, 0, s>>>(L, x, b, cells, masks, ncells, ktab, delta);
+    count();
+}
+void launch_vanka_apply(const LevelK& L, double* x, const int32_t* cells, const uint8_t* masks, int ncells,
+                        const double* delta, cudaStream_t s) {
+    if (ncells <= 0) return;
+    k_vanka_apply<<<(ncells + 127) / 128, 128, 0, s>>>(L, x, cells, masks, ncells, delta);
+    count();
+}
+void launch_restrict(const LevelK& F, const LevelK& C, const double* rf, double* bc, cudaStream_t s) {
+    k_restrict<<<cell_grid(C.g), dim3(BX, BY), 0, s>>>(F, C, rf, bc);
+    count();
+}
+void launch_prolong_add(const LevelK& F, const LevelK& C, const double* xc, double* xf, cudaStream_t s) {
+    k_prolong_add<<<cell_grid(F.g), dim3(BX, BY), 0, s>>>(F, C, xc, xf);
+    count();
+}
+void launch_coarse_gemv(const double* ksym, const int32_t* slots, int n, const double* b, double* x,
+                        cudaStream_t s) {
+    const int nchunks = (n + 63) / 64;
+    const size_t smem = static_cast<size_t>(nchunks) * CG_ROWS * sizeof(double);
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(k_coarse_gemv, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr_set = true;
+    }
+    k_coarse_gemv<<<(n + CG_ROWS - 1) / CG_ROWS, dim3(CG_ROWS, CG_LANES), smem, s>>>(ksym, slots, n, b, x);
+    count();
+}
+void launch_pack(const LevelK& L, const double* padded, double* compact, cudaStream_t s) {
+    k_pack<<<cell_grid(L.g), dim3(BX, BY), 0, s>>>(L, padded, compact, 0);
+    count();
+}
+void launch_unpack(const LevelK& L, const double* compact, double* padded, cudaStream_t s) {
+    k_pack<<<cell_grid(L.g), dim3(BX, BY), 0, s>>>(L, padded, const_cast<double*>(compact), 1);
+    count();
+}
+void launch_dot2(const double* a, const double* b, const double* c, const double* d, int64_t n, double* partials,
+                 double* out, cudaStream_t s) {
+    k_dot2<<<kRedBlocks, RED_T, 0, s>>>(a, b, c, d, n, partials);
+    k_dot_final<<<1, 64, 0, s>>>(partials, kRedBlocks, out);
+    count();
+    count();
+}
+void launch_axpy(double* y, const double* x, double alpha, int64_t n, cudaStream_t s) {
+    k_axpy<<<stream_blocks(n), 256, 0, s>>>(y, x, alpha, n);
+    count();
+}
+void launch_xpby(double* y, const double* x, double beta, int64_t n, cudaStream_t s) {
+    k_xpby<<<stream_blocks(n), 256, 0, s>>>(y, x, beta, n);
+    count();
+}
+void launch_dx_update(double* d, double* x, const double* q, double cd, double cq, int64_t n, cudaStream_t s) {
+    k_dx_update<<<stream_blocks(n), 256, 0, s>>>(d, x, q, cd, cq, n);
+    count();
+}
+
+}  // namespace smg

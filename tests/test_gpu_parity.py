@@ -1,0 +1,220 @@
+"""GPU parity: every hot-path op of libsmg.so (through the C-ABI) against the CPU
+oracle on identical seeded inputs.
+
+Per-point ops follow the shared arithmetic contract (no FMA on
+either side), so they are required to be BIT-IDENTICAL.  Only SQMR's inner
+products use a different (deterministic) summation order; solve-level parity is
+held to the north_star bar: per-iteration residuals within 1e-10 relative,
+iteration count within +-1, solution within 1e-6 relative L2.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2312_10615_b200 as smg
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def pair16():
+    oracle.set_threads(4)
+    o = oracle.Oracle(16, levels=3)
+    s = smg.Solver(16, levels=3)
+    yield o, s
+    s.close()
+
+
+def rnd(n, seed):
+    return np.random.default_rng(seed).uniform(-1, 1, n)
+
+
+def same(a, b):
+    assert a.shape == b.shape
+    if not np.array_equal(a, b):
+        d = np.abs(a - b).max() / max(np.abs(b).max(), 1e-300)
+        pytest.fail(f"not bit-identical: max rel diff {d:.3e}")
+
+
+@pytest.mark.parametrize("level", [0, 1, 2])
+@pytest.mark.parametrize("pen", [False, True])
+def test_apply(pair16, level, pen):
+    o, s = pair16
+    x = rnd(o.ndof(level), 10 + level)
+    same(s.apply(x, level, pen), o.apply(x, level, pen))
+
+
+@pytest.mark.parametrize("level", [0, 1])
+def test_residual(pair16, level):
+    o, s = pair16
+    n = o.ndof(level)
+    x, b = rnd(n, 1), rnd(n, 2)
+    same(s.residual(x, b, level), o.residual(x, b, level))
+
+
+def test_counts(pair16):
+    o, s = pair16
+    for l in range(3):
+        assert s.counts(l) == o.counts(l)
+        assert s.ndof(l) == o.ndof(l)
+
+
+@pytest.mark.parametrize("phase", list(range(20)))
+def test_dgs_phase(pair16, phase):
+    o, s = pair16
+    n = o.ndof(0)
+    x, b = rnd(n, 3 + phase), rnd(n, 4)
+    same(s.smoother(smg.OP_DGS_PHASE, x, b, arg=phase), o.smoother(0, x, b, arg=phase))
+
+
+@pytest.mark.parametrize("colour", list(range(8)))
+def test_vanka_colour(pair16, colour):
+    o, s = pair16
+    n = o.ndof(0)
+    x, b = rnd(n, 30 + colour), rnd(n, 5)
+    same(s.smoother(smg.OP_VANKA_COLOUR, x, b, arg=colour), o.smoother(2, x, b, arg=colour))
+
+
+@pytest.mark.parametrize("op,oop", [(smg.OP_DGS_SYM, 1), (smg.OP_VANKA_SYM, 3), (smg.OP_SMOOTH, 4)])
+@pytest.mark.parametrize("level", [0, 1])
+def test_symmetric_smoothers(pair16, op, oop, level):
+    o, s = pair16
+    n = o.ndof(level)
+    x, b = rnd(n, 6), rnd(n, 7)
+    same(s.smoother(op, x, b, level), o.smoother(oop, x, b, level))
+    z = np.zeros(n)
+    same(s.smoother(op, z, b, level), o.smoother(oop, z, b, level))
+
+
+@pytest.mark.parametrize("level", [0, 1])
+def test_transfers(pair16, level):
+    o, s = pair16
+    rf = rnd(o.ndof(level), 8)
+    xc = rnd(o.ndof(level + 1), 9)
+    same(s.restrict(rf, level), o.restrict(rf, level))
+    same(s.prolong(xc, level), o.prolong(xc, level))
+
+
+def test_coarse_solve(pair16):
+    o, s = pair16
+    b = rnd(o.ndof(2), 11)
+    same(s.coarse_solve(b), o.coarse_solve(b))
+
+
+def test_vcycle(pair16):
+    o, s = pair16
+    b = rnd(o.ndof(0), 12)
+    same(s.vcycle(b), o.vcycle(b))
+
+
+def test_vcycle_symmetry_gpu_materialized():
+    # SURVEY §7 f1 / SPEC AC 4 on the GPU map itself
+    s = smg.Solver(8, levels=2)
+    n = s.ndof()
+    W = np.zeros((n, n))
+    for j in range(n):
+        e = np.zeros(n)
+        e[j] = 1.0
+        W[:, j] = s.vcycle(e)
+    assert np.linalg.norm(W - W.T) / np.linalg.norm(W) < 1e-10
+    s.close()
+
+
+def test_fault_injection_detected_on_gpu():
+    s = smg.Solver(6, levels=1, flags=smg.FLAG_SKIP_REVERSE_DGS)
+    n = s.ndof()
+    C = np.zeros((n, n))
+    for j in range(n):
+        e = np.zeros(n)
+        e[j] = 1.0
+        C[:, j] = s.smoother(smg.OP_DGS_SYM, np.zeros(n), e)
+    assert np.linalg.norm(C - C.T) / np.linalg.norm(C) > 1e-3
+    s.close()
+
+
+def check_solve(o, s, b, tol, maxit=100):
+    xo, ho, _, sto = o.sqmr(b, tol=tol, maxit=maxit)
+    xg, hg, _, stg = s.sqmr(b, tol=tol, maxit=maxit)
+    assert sto == stg == smg.SMG_CONVERGED
+    assert abs(len(ho) - len(hg)) <= 1
+    k = min(len(ho), len(hg))
+    rel = np.abs(hg[:k] - ho[:k]) / ho[:k]
+    assert rel.max() < 1e-10, rel
+    npres = o.counts(0)["np"]
+    assert np.linalg.norm(xg[:-npres] - xo[:-npres]) / np.linalg.norm(xo[:-npres]) < 1e-6
+    pg = xg[-npres:] - xg[-npres:].mean()
+    po = xo[-npres:] - xo[-npres:].mean()
+    assert np.linalg.norm(pg - po) / np.linalg.norm(po) < 1e-6
+    return hg
+
+
+@pytest.mark.parametrize("n,levels,kind,seed", [(16, 2, 0, 0), (32, 3, 0, 0), (32, 3, 1, 2), (64, 4, 0, 3)])
+def test_sqmr_history_parity(n, levels, kind, seed):
+    oracle.set_threads(os.cpu_count() or 1)
+    o = oracle.Oracle(n, levels=levels)
+    s = smg.Solver(n, levels=levels)
+    b = o.forcing(kind, seed)
+    check_solve(o, s, b, 1e-6)
+    s.close()
+
+
+def test_channel_anisotropic_parity():
+    # cfg-4 shape (4:1:1 box, h = 1/ny), reduced
+    oracle.set_threads(os.cpu_count() or 1)
+    o = oracle.Oracle(64, 16, 16, h=1 / 16, levels=3)
+    s = smg.Solver(64, 16, 16, h=1 / 16, levels=3)
+    b = o.forcing(oracle.FORCE_CHANNEL, 4)
+    check_solve(o, s, b, 1e-8)
+    s.close()
+
+
+@pytest.mark.parametrize("name", ["cfg0", "cfg1"])
+def test_golden_history(name):
+    """BASELINE configs 0 and 1 against the committed oracle histories."""
+    g = json.load(open(os.path.join(ROOT, "tests", "golden", f"{name}_history.json")))
+    n = g["grid"][0]
+    s = smg.Solver(n, levels=g["levels"])
+    b = smg.forcing(n, kind=g["forcing"], seed=g["seed"])
+    assert float(np.linalg.norm(b)) == g["b_norm"]
+    x, h, _, st = s.sqmr(b, tol=g["tol"], maxit=200)
+    assert st == g["status"]
+    assert abs(len(h) - g["iterations"]) <= 1
+    k = min(len(h), g["iterations"])
+    rel = np.abs(h[:k] - np.array(g["history"][:k])) / np.array(g["history"][:k])
+    assert rel.max() < 1e-10, rel
+    npres = n ** 3
+    assert abs(np.linalg.norm(x[:-npres]) - g["u_norm"]) / g["u_norm"] < 1e-6
+    s.close()
+
+
+def test_edge_cases():
+    s = smg.Solver(8, levels=2)
+    n = s.ndof()
+    x, h, _, st = s.sqmr(np.zeros(n), 1e-6, 10)
+    assert st == smg.SMG_CONVERGED and len(h) == 0 and not x.any()
+    x, h, _, st = s.sqmr(smg.forcing(8, seed=1), 1e-14, 2)
+    assert st == smg.SMG_MAX_ITERATIONS and len(h) == 2
+    with pytest.raises(ValueError):
+        s.apply(np.zeros(n + 1))  # length mismatch
+    with pytest.raises(smg.SmgError):
+        s.smoother(smg.OP_DGS_PHASE, np.zeros(n), np.zeros(n), arg=20)
+    with pytest.raises(smg.SmgError):
+        s.smoother(99, np.zeros(n), np.zeros(n))
+    s.close()
+
+
+def test_resident_path_matches_e2e():
+    s = smg.Solver(32, levels=3)
+    b = smg.forcing(32, seed=0)
+    x1, h1, _, st1 = s.sqmr(b, 1e-6, 100)
+    s.set_rhs(b)
+    h2, st2 = s.solve_resident(1e-6, 100)
+    x2 = s.solution()
+    assert st1 == st2 == 0 and np.array_equal(h1, h2) and np.array_equal(x1, x2)  # deterministic
+    t = s.timing()
+    assert t["iterations"] == len(h2) and t["solve_ms"] > 0 and t["kernel_launches"] > 100
+    s.close()

@@ -1,0 +1,218 @@
+"""Structural known-answer tests that pin the oracle (SPEC AC 3, 4, 5; SPEC:128,
+168-170, 198, 219-224, 264-283, 300, 321-325, 390-391, 597).  These are the
+reference's own invariants; no reference artefact pins the per-iteration values
+(SPEC:624), so these plus the direct-solve checks are what validate the oracle.
+"""
+import numpy as np
+import pytest
+
+import oracle
+
+OP_PHASE, OP_DGS, OP_VCOL, OP_VANKA, OP_SMOOTH = 0, 1, 2, 3, 4
+
+
+def materialize(f, n):
+    cols = []
+    for j in range(n):
+        e = np.zeros(n)
+        e[j] = 1.0
+        cols.append(f(e))
+    return np.stack(cols, axis=1)
+
+
+def defect(A):
+    return np.linalg.norm(A - A.T) / max(np.linalg.norm(A), 1e-300)
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _serial():
+    oracle.set_threads(1)  # tiny grids: thread start-up would dominate
+    yield
+
+
+@pytest.fixture(scope="module")
+def o8():
+    return oracle.Oracle(8, levels=2)
+
+
+def test_operator_symmetric_and_matches_apply(o8):
+    for pen in (False, True):
+        A = o8.dense(0, pen)
+        assert defect(A) == 0.0
+        x = np.random.default_rng(1).standard_normal(A.shape[0])
+        assert np.allclose(o8.apply(x, penalized=pen), A @ x, rtol=0, atol=1e-10 * np.abs(A @ x).max())
+
+
+def test_penalty_diagonal(o8):
+    # gamma = 1e-3: pressure diagonal entries equal -1e-3
+    A = o8.dense(0, True)
+    c = o8.counts(0)
+    npres = c["np"]
+    assert np.all(np.diag(A)[-npres:] == -1e-3)
+    assert np.all(np.diag(o8.dense(0, False))[-npres:] == 0.0)
+
+
+def test_apply_linear_zero(o8):
+    n = o8.ndof()
+    assert not o8.apply(np.zeros(n)).any()
+    rng = np.random.default_rng(2)
+    a, b = rng.standard_normal(n), rng.standard_normal(n)
+    lhs = o8.apply(2.5 * a - 0.75 * b)
+    rhs = 2.5 * o8.apply(a) - 0.75 * o8.apply(b)
+    assert np.allclose(lhs, rhs, atol=1e-10 * np.abs(rhs).max())
+
+
+def test_prolong_is_8_restrict_transpose(o8):
+    # P = c R^T exactly (c = 8 in 3-D)
+    nf, nc = o8.ndof(0), o8.ndof(1)
+    P = materialize(lambda e: o8.prolong(e, 0), nc)
+    R = materialize(lambda e: o8.restrict(e, 0), nf)
+    assert P.shape == (nf, nc) and R.shape == (nc, nf)
+    assert np.array_equal(P, 8.0 * R.T)
+
+
+def test_transfer_adjoint_and_partition_of_unity():
+    o = oracle.Oracle(16, levels=2)
+    nf, nc = o.ndof(0), o.ndof(1)
+    rng = np.random.default_rng(3)
+    xc, rf = rng.standard_normal(nc), rng.standard_normal(nf)
+    assert np.isclose(o.prolong(xc) @ rf, 8.0 * (xc @ o.restrict(rf)), rtol=1e-13)
+    pf = o.prolong(np.ones(nc))
+    # partition of unity on fully-interior regions: pressures all 1, deep faces 1
+    cnt = o.counts(0)
+    assert np.all(pf[-cnt["np"]:] == 1.0)
+    u = pf[: cnt["nu"]].reshape(16, 16, 15)
+    assert np.all(u[2:-2, 2:-2, 1:-1] == 1.0)
+
+
+def test_transfer_zero():
+    o = oracle.Oracle(8, levels=2)
+    assert not o.prolong(np.zeros(o.ndof(1))).any()
+    assert not o.restrict(np.zeros(o.ndof(0))).any()
+
+
+@pytest.mark.parametrize("op", [OP_DGS, OP_VANKA, OP_SMOOTH])
+def test_smoother_symmetry_8(o8, op):
+    # Theorems 1, 3, 4 (SPEC AC 3): relative symmetry defect < 1e-10
+    n = o8.ndof()
+    C = materialize(lambda e: o8.smoother(op, np.zeros(n), e), n)
+    assert defect(C) < 1e-10
+    assert np.abs(C).max() > 0
+
+
+@pytest.mark.parametrize("nu", [1, 2, 3])
+def test_smoother_symmetry_6cubed(nu):
+    # SPEC AC 3 at 6^3 for nu in {1,2,3} (one level, smoother only)
+    o = oracle.Oracle(6, levels=1, nu=nu)
+    n = o.ndof()
+    for op in (OP_VANKA, OP_SMOOTH):
+        C = materialize(lambda e: o.smoother(op, np.zeros(n), e), n)
+        assert defect(C) < 1e-10
+
+
+def test_dgs_fixed_point(o8):
+    # b = L~x  =>  x unchanged by every phase
+    n = o8.ndof()
+    x = np.random.default_rng(4).standard_normal(n)
+    b = o8.apply(x, penalized=True)
+    for ph in range(20):
+        y = o8.smoother(OP_PHASE, x, b, arg=ph)
+        assert np.allclose(y, x, atol=1e-11 * np.abs(x).max())
+
+
+def test_vanka_block_residual_zero_after_solve(o8):
+    # after a colour phase the block-local residuals of that colour vanish
+    n = o8.ndof()
+    rng = np.random.default_rng(5)
+    x, b = rng.standard_normal(n), rng.standard_normal(n)
+    y = o8.smoother(OP_VCOL, x, b, arg=0)
+    r = o8.residual(y, b)
+    # colour-0 band cells: pressure rows of cells with even (i,j,k) on the shell
+    nx = 8
+    cnt = o8.counts(0)
+    rp = r[-cnt["np"]:].reshape(nx, nx, nx)
+    shell = np.zeros((nx, nx, nx), bool)
+    shell[[0, -1], :, :] = shell[:, [0, -1], :] = shell[:, :, [0, -1]] = True
+    par = np.zeros_like(shell)
+    par[::2, ::2, ::2] = True
+    assert np.abs(rp[shell & par]).max() < 1e-9 * np.abs(b).max()
+
+
+def test_skip_reverse_breaks_symmetry():
+    # fault injection must be detected by the symmetry check
+    o = oracle.Oracle(6, levels=1)
+    o.set_skip_reverse(True)
+    n = o.ndof()
+    C = materialize(lambda e: o.smoother(OP_DGS, np.zeros(n), e), n)
+    assert defect(C) > 1e-3
+
+
+@pytest.mark.parametrize("levels", [2, 3])
+def test_vcycle_symmetric_linear(levels):
+    # SPEC AC 4 / SPEC:377,390-391: materialized cycle symmetric < 1e-10, linear
+    o = oracle.Oracle(8, levels=levels)
+    n = o.ndof()
+    W = materialize(o.vcycle, n)
+    assert defect(W) < 1e-10
+    rng = np.random.default_rng(6)
+    a, b = rng.standard_normal(n), rng.standard_normal(n)
+    lhs = o.vcycle(3 * a - 2 * b)
+    assert np.allclose(lhs, 3 * o.vcycle(a) - 2 * o.vcycle(b), atol=1e-12 * np.abs(lhs).max())
+    assert not o.vcycle(np.zeros(n)).any()
+    # symmetric indefinite
+    ev = np.linalg.eigvalsh(0.5 * (W + W.T))
+    assert ev.min() < 0 < ev.max()
+
+
+def test_single_level_cycle_is_direct_solve():
+    # one level: cycle = exact solve of L~ x = b
+    o = oracle.Oracle(4, levels=1)
+    n = o.ndof()
+    b = np.random.default_rng(7).standard_normal(n)
+    x = o.vcycle(b)
+    assert np.allclose(o.dense(0, True) @ x, b, atol=1e-10 * np.abs(b).max())
+
+
+def test_commutativity_deep_interior():
+    # SPEC AC 5: L*M velocity rows vanish for deep-interior pressure columns
+    nx = 12
+    o = oracle.Oracle(nx, levels=2)
+    L = o.dense(0, False)
+    cnt = o.counts(0)
+    nu_, nv_, nw_ = cnt["nu"], cnt["nv"], cnt["nw"]
+    npv = nu_ + nv_ + nw_
+    h = 1.0 / nx
+
+    def uidx(I, j, k):
+        return (k * nx + j) * (nx - 1) + (I - 1)
+
+    def vidx(i, J, k):
+        return nu_ + (k * (nx - 1) + (J - 1)) * nx + i
+
+    def widx(i, j, K):
+        return nu_ + nv_ + ((K - 1) * nx + j) * nx + i
+
+    def pidx(i, j, k):
+        return npv + (k * nx + j) * nx + i
+
+    bad_deep, nonzero_edge = 0, 0
+    for (i, j, k) in [(5, 5, 5), (6, 4, 7), (1, 1, 1), (0, 5, 5)]:
+        m = np.zeros(L.shape[0])
+        for a, (lo, hi) in enumerate([(uidx(i, j, k) if i >= 1 else None, uidx(i + 1, j, k) if i + 1 <= nx - 1 else None),
+                                      (vidx(i, j, k) if j >= 1 else None, vidx(i, j + 1, k) if j + 1 <= nx - 1 else None),
+                                      (widx(i, j, k) if k >= 1 else None, widx(i, j, k + 1) if k + 1 <= nx - 1 else None)]):
+            if lo is not None:
+                m[lo] -= 1.0 / h
+            if hi is not None:
+                m[hi] += 1.0 / h
+        m[pidx(i, j, k)] += 6.0 / h ** 2
+        for d in [(-1, 0, 0), (1, 0, 0), (0, -1, 0), (0, 1, 0), (0, 0, -1), (0, 0, 1)]:
+            ii, jj, kk = i + d[0], j + d[1], k + d[2]
+            if 0 <= ii < nx and 0 <= jj < nx and 0 <= kk < nx:
+                m[pidx(ii, jj, kk)] -= 1.0 / h ** 2
+        top = (L @ m)[:npv]
+        if min(i, j, k) >= 2 and max(i, j, k) <= nx - 3:
+            bad_deep += np.abs(top).max() > 1e-12 * np.abs(L).max()
+        else:
+            nonzero_edge += np.abs(top).max() > 1e-9
+    assert bad_deep == 0 and nonzero_edge >= 1
