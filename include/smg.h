@@ -126,6 +126,9 @@ int smg_last_timing(const smg_ctx* ctx, smg_timing* out);
  * (8 phases), 3 one V-cycle. */
 int smg_time_kernel(smg_ctx* ctx, int which, int reps, double* avg_ms);
 
+/* Brackets a region for ncu --profile-from-start off (cudaProfilerStart/Stop). */
+int smg_profiler_range(int on);
+
 /* Pinned host buffers for the end-to-end path. */
 void* smg_host_alloc(int64_t bytes);
 void smg_host_free(void* p);

@@ -37,8 +37,6 @@
 
 namespace orc {
 
-using stokesmg::dot;
-using stokesmg::norm2;
 using stokesmg::parallel_for;
 using vec = std::vector<double>;
 
@@ -783,6 +781,49 @@ static void vcycle(const Hierarchy& H, int l, const vec& b, vec& x) {
     smooth(L, x, b, H.nu, H.skip_reverse);
 }
 
+// ----------------------------------------------------- canonical dot -------
+// Fixed reduction order of every SQMR inner product (OD-12), the
+// one the GPU computes natively: for each field (u, v, w, p), plane z, row y of
+// the field's storage box, 32 lane accumulators take x = lane, lane+32, ... in
+// ascending order and are combined by the tree acc[l] += acc[l+o], o = 16..1;
+// row sums are added in ascending y to a plane sum; plane sums (fields in
+// order, z ascending) go through the same 32-lane scheme.  Zero slots (walls,
+// inactive) contribute exactly +0 and are skipped here.
+static double lane_tree(double* acc) {
+    for (int o = 16; o > 0; o >>= 1)
+        for (int l = 0; l < o; ++l) acc[l] = acc[l] + acc[l + o];
+    return acc[0];
+}
+
+static double cdot(const Level& L, const vec& a, const vec& b) {
+    const DofMap& m = L.map;
+    std::vector<double> planes;
+    for (int c = 0; c < 4; ++c) {
+        const int ex = c < 3 ? m.fext[c][0] : m.n[0], ey = c < 3 ? m.fext[c][1] : m.n[1];
+        const int ez = c < 3 ? m.fext[c][2] : m.n[2];
+        const size_t base = planes.size();
+        planes.resize(base + ez);
+        parallel_for(ez, g_threads, [&](int64_t z) {
+            double p = 0.0;
+            for (int y = 0; y < ey; ++y) {
+                double acc[32];
+                for (int l = 0; l < 32; ++l) acc[l] = 0.0;
+                for (int x = 0; x < ex; ++x) {
+                    const int32_t id = c < 3 ? m.face(c, x, y, static_cast<int>(z)) : m.cell(x, y, static_cast<int>(z));
+                    if (id < 0) continue;
+                    acc[x & 31] = acc[x & 31] + a[id] * b[id];
+                }
+                p = p + lane_tree(acc);
+            }
+            planes[base + z] = p;
+        });
+    }
+    double acc[32];
+    for (int l = 0; l < 32; ++l) acc[l] = 0.0;
+    for (size_t q = 0; q < planes.size(); ++q) acc[q & 31] = acc[q & 31] + planes[q];
+    return lane_tree(acc);
+}
+
 // -------------------------------------------------------------- krylov ------
 enum { ST_CONVERGED = 0, ST_MAXIT = 1, ST_BREAKDOWN = 2 };
 
@@ -796,7 +837,7 @@ static int sqmr(const Hierarchy& H, const vec& b, vec& x, double tol, int maxit,
     hist.clear();
     secs.clear();
     x.assign(n, 0.0);
-    const double bnorm = norm2(b);
+    const double bnorm = std::sqrt(cdot(L0, b, b));
     if (bnorm == 0.0) return ST_CONVERGED;
     auto M = [&](const vec& in, vec& out) {
         if (precond) vcycle(H, 0, in, out);
@@ -805,16 +846,16 @@ static int sqmr(const Hierarchy& H, const vec& b, vec& x, double tol, int maxit,
     vec s = b, t, q, d(n, 0.0), r;
     M(s, t);
     q = t;
-    double tau = norm2(t), nu_old = 0.0, rho = dot(s, q);
+    double tau = std::sqrt(cdot(L0, t, t)), nu_old = 0.0, rho = cdot(L0, s, q);
     if (std::fabs(rho) < 1e-300) return ST_BREAKDOWN;
     for (int j = 1; j <= maxit; ++j) {
         apply(L0, q, t, false);
-        const double sigma = dot(q, t);
+        const double sigma = cdot(L0, q, t);
         if (std::fabs(sigma) < 1e-300) return ST_BREAKDOWN;
         const double alpha = rho / sigma;
         for (int64_t i = 0; i < n; ++i) s[i] = s[i] - alpha * t[i];
         M(s, t);
-        const double nu = norm2(t) / tau;
+        const double nu = std::sqrt(cdot(L0, t, t)) / tau;
         const double c = 1.0 / std::sqrt(1.0 + nu * nu);
         tau = tau * nu * c;
         const double c2 = c * c;
@@ -826,11 +867,11 @@ static int sqmr(const Hierarchy& H, const vec& b, vec& x, double tol, int maxit,
         vec lx;
         apply(L0, x, lx, false);
         for (int64_t i = 0; i < n; ++i) lx[i] = b[i] - lx[i];
-        const double rel = norm2(lx) / bnorm;
+        const double rel = std::sqrt(cdot(L0, lx, lx)) / bnorm;
         hist.push_back(rel);
         secs.push_back(std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
         if (rel < tol) return ST_CONVERGED;
-        const double rho_new = dot(s, t);
+        const double rho_new = cdot(L0, s, t);
         if (std::fabs(rho_new) < 1e-300) return ST_BREAKDOWN;
         const double beta = rho_new / rho;
         for (int64_t i = 0; i < n; ++i) q[i] = t[i] + beta * q[i];
@@ -1040,6 +1081,10 @@ int orc_sqmr(void* h, const double* b, double* x, double tol, int maxit, int pre
     for (size_t k = 0; k < hh.size(); ++k) { hist[k] = hh[k]; secs[k] = ss[k]; }
     *iters = static_cast<int>(hh.size());
     return st;
+}
+double orc_cdot(void* h, const double* a, const double* b) {
+    const Level& L = *HH(h).lv[0];
+    return cdot(L, V(a, L.map.N), V(b, L.map.N));
 }
 void orc_forcing(void* h, int kind, uint64_t seed, double* b) {
     const Level& L = *HH(h).lv[0];

@@ -19,6 +19,7 @@
 #include <thread>
 #include <vector>
 
+#include <cuda_profiler_api.h>
 #include <cuda_runtime.h>
 
 #include "../../include/smg.h"
@@ -227,6 +228,7 @@ void build(smg_ctx* c) {
     const int div = 1 << (p.levels - 1);
     if (g.nx % div || g.ny % div || g.nz % div)
         throw SmgError(SMG_EINVAL, "extents must be divisible by 2^(levels-1)");
+    if (g.nx > 1024 || g.ny > 1024 || g.nz > 1024) throw SmgError(SMG_EINVAL, "extents above 1024 per GPU");
     if (g.nx / div < 2 || g.ny / div < 2 || g.nz / div < 2)
         throw SmgError(SMG_EINVAL, "coarsened extent below 2 (SPEC:82)");
     CK(cudaSetDevice(c->device));
@@ -406,7 +408,7 @@ void build(smg_ctx* c) {
     int64_t maxN = 0;
     for (auto& L : c->lv) maxN = std::max(maxN, L.N);
     c->compact = c->dalloc<double>(maxN);
-    c->partials = c->dalloc<double>(2 * kRedBlocks);
+    c->partials = c->dalloc<double>(kPartials);
     c->dscal = c->dalloc<double>(8);
     CK(cudaMallocHost(&c->hscal, 8 * sizeof(double)));
     CK(cudaStreamSynchronize(c->st));
@@ -472,7 +474,7 @@ void vcycle(smg_ctx* c, int l, const double* b, double* x) {
 
 // ---- BLAS-1 helpers with host readback ----
 void dot2(smg_ctx* c, const double* a, const double* b, const double* e, const double* f, double* out2) {
-    launch_dot2(a, b, e, f, vlen(c->lv[0]), c->partials, c->dscal, c->st);
+    launch_cdot2(c->lv[0].k.g, a, b, e, f, c->partials, c->dscal, c->st);
     CK(cudaMemcpyAsync(c->hscal, c->dscal, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->st));
     CK(cudaStreamSynchronize(c->st));
     out2[0] = c->hscal[0];
@@ -774,6 +776,11 @@ int smg_time_kernel(smg_ctx* c, int which, int reps, double* avg_ms) {
         CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
         *avg_ms = ms / reps;
     });
+}
+
+int smg_profiler_range(int on) {
+    const cudaError_t e = on ? cudaProfilerStart() : cudaProfilerStop();
+    return e == cudaSuccess ? 0 : SMG_ECUDA;
 }
 
 void* smg_host_alloc(int64_t bytes) {

@@ -391,56 +391,56 @@ __global__ void k_pack(LevelK L, const double* __restrict__ X, double* __restric
 // ------------------------------------------------------------- BLAS-1 ------
 constexpr int RED_T = 256;
 
-__device__ __forceinline__ double block_sum(double v, double* sh) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v = v + __shfl_down_sync(0xffffffffu, v, o);
-    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-    if (l == 0) sh[w] = v;
-    __syncthreads();
-    double r = 0.0;
-    if (w == 0) {
-        r = (l < RED_T / 32) ? sh[l] : 0.0;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) r = r + __shfl_down_sync(0xffffffffu, r, o);
-    }
-    __syncthreads();
-    return r;
-}
-
-__global__ void __launch_bounds__(RED_T) k_dot2(const double* __restrict__ a, const double* __restrict__ b,
+// Canonical inner product (OD-12) — bit-identical to the oracle:
+// block (z, field): each warp owns rows y (stride 8); lane l accumulates
+// x = l, l+32, ... ascending; lanes combine through the shuffle-down tree
+// (o = 16..1); row sums are added in ascending y by one thread; plane sums
+// are reduced by k_cdot_final with the same 32-lane scheme.
+constexpr int kMaxPlanes = 4 * 1025 + 4;
+__global__ void __launch_bounds__(RED_T) k_cdot(Geom g, const double* __restrict__ a, const double* __restrict__ b,
                                                 const double* __restrict__ c, const double* __restrict__ d,
-                                                int64_t n, double* __restrict__ partials) {
-    __shared__ double sh[RED_T / 32];
-    double s0 = 0.0, s1 = 0.0;
-    const int64_t n2 = n / 2;
-    const double2* a2 = reinterpret_cast<const double2*>(a);
-    const double2* b2 = reinterpret_cast<const double2*>(b);
-    const double2* c2 = reinterpret_cast<const double2*>(c);
-    const double2* d2 = reinterpret_cast<const double2*>(d);
-    for (int64_t k = blockIdx.x * (int64_t)RED_T + threadIdx.x; k < n2; k += (int64_t)gridDim.x * RED_T) {
-        const double2 x = a2[k], y = b2[k];
-        s0 = s0 + x.x * y.x;
-        s0 = s0 + x.y * y.y;
-        if (c) {
-            const double2 u = c2[k], v = d2[k];
-            s1 = s1 + u.x * v.x;
-            s1 = s1 + u.y * v.y;
+                                                double* __restrict__ partials) {
+    __shared__ double rows0[1040], rows1[1040];
+    const int z = blockIdx.x, f = blockIdx.y;
+    const int ex = g.nx + (f == 0), ey = g.ny + (f == 1), ez = g.nz + (f == 2);
+    if (z >= ez) return;
+    const int q = f * g.nz + (f == 3 ? 1 : 0) + z;  // plane index: u nz, v nz, w nz+1, p nz
+    const int64_t off = f * g.fs;
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    for (int y = w; y < ey; y += RED_T / 32) {
+        const int64_t row = off + g.slot(0, y, z);
+        double s0 = 0.0, s1 = 0.0;
+        for (int x = l; x < ex; x += 32) {
+            s0 = s0 + a[row + x] * b[row + x];
+            if (c) s1 = s1 + c[row + x] * d[row + x];
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            s0 = s0 + __shfl_down_sync(0xffffffffu, s0, o);
+            s1 = s1 + __shfl_down_sync(0xffffffffu, s1, o);
+        }
+        if (l == 0) {
+            rows0[y] = s0;
+            rows1[y] = s1;
         }
     }
-    const double t0 = block_sum(s0, sh);
-    const double t1 = c ? block_sum(s1, sh) : 0.0;
+    __syncthreads();
     if (threadIdx.x == 0) {
-        partials[blockIdx.x] = t0;
-        partials[gridDim.x + blockIdx.x] = t1;
+        double p0 = 0.0, p1 = 0.0;
+        for (int y = 0; y < ey; ++y) {
+            p0 = p0 + rows0[y];
+            p1 = p1 + rows1[y];
+        }
+        partials[q] = p0;
+        partials[kMaxPlanes + q] = p1;
     }
 }
 
-__global__ void k_dot_final(const double* __restrict__ partials, int nb, double* __restrict__ out) {
-    // one warp per output; lanes sum strided subsets in order, then a fixed tree
+__global__ void k_cdot_final(const double* __restrict__ partials, int nq, double* __restrict__ out) {
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-    const double* p = partials + w * nb;
+    const double* p = partials + w * kMaxPlanes;
     double s = 0.0;
-    for (int k = l; k < nb; k += 32) s = s + p[k];
+    for (int k = l; k < nq; k += 32) s = s + p[k];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s = s + __shfl_down_sync(0xffffffffu, s, o);
     if (l == 0) out[w] = s;
@@ -532,10 +532,10 @@ void launch_unpack(const LevelK& L, const double* compact, double* padded, cudaS
     k_pack<<<cell_grid(L.g), dim3(BX, BY), 0, s>>>(L, padded, const_cast<double*>(compact), 1);
     count();
 }
-void launch_dot2(const double* a, const double* b, const double* c, const double* d, int64_t n, double* partials,
-                 double* out, cudaStream_t s) {
-    k_dot2<<<kRedBlocks, RED_T, 0, s>>>(a, b, c, d, n, partials);
-    k_dot_final<<<1, 64, 0, s>>>(partials, kRedBlocks, out);
+void launch_cdot2(const Geom& g, const double* a, const double* b, const double* c, const double* d,
+                  double* partials, double* out, cudaStream_t s) {
+    k_cdot<<<dim3(g.nz + 1, 4), RED_T, 0, s>>>(g, a, b, c, d, partials);
+    k_cdot_final<<<1, 64, 0, s>>>(partials, 4 * g.nz + 1, out);
     count();
     count();
 }

@@ -73,10 +73,11 @@ void launch_pack(const LevelK& L, const double* padded, double* compact, cudaStr
 void launch_unpack(const LevelK& L, const double* compact, double* padded, cudaStream_t s);
 
 // ---- BLAS-1 (kernels.cu); n = padded vector length (multiple of 32) ----
-constexpr int kRedBlocks = 592;  // 4 x 148 SMs; fixed => deterministic reductions
-// partial sums of a.b (and c.d if c != nullptr) -> out[0], out[1] (device), deterministic.
-void launch_dot2(const double* a, const double* b, const double* c, const double* d, int64_t n,
-                 double* partials, double* out, cudaStream_t s);
+constexpr int kPartials = 2 * (4 * 1025 + 4);  // scratch doubles for launch_cdot2
+// Canonical (bit-reproducible, oracle-identical) a.b and, if c != nullptr,
+// c.d over the level geometry g -> out[0], out[1] on the device.  nz <= 1024.
+void launch_cdot2(const Geom& g, const double* a, const double* b, const double* c, const double* d,
+                  double* partials, double* out, cudaStream_t s);
 void launch_axpy(double* y, const double* x, double alpha, int64_t n, cudaStream_t s);          // y += alpha x
 void launch_xpby(double* y, const double* x, double beta, int64_t n, cudaStream_t s);           // y = x + beta y
 void launch_dx_update(double* d, double* x, const double* q, double cd, double cq, int64_t n,

@@ -8,6 +8,7 @@ oracle against accidental change.
 
     python tests/golden/make_golden.py
 """
+import hashlib
 import json
 import os
 import sys
@@ -38,7 +39,7 @@ def main():
             "grid": [n, n, n], "levels": lv, "forcing": kind, "seed": seed, "tol": tol,
             "eta": 1.0, "gamma": 1e-3, "nu": 1, "band_width": 1,
             "status": st, "iterations": len(hist), "history": [float(v) for v in hist],
-            "b_norm": float(np.linalg.norm(b)), "b_sum": float(b.sum()),
+            "b_sha256": hashlib.sha256(np.ascontiguousarray(b).tobytes()).hexdigest(),
             "u_norm": float(np.linalg.norm(x[:-npres])), "p_norm_meanfree": float(np.linalg.norm(p)),
             "u_sum": float(x[:-npres].sum()),
         }

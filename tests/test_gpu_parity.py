@@ -7,6 +7,7 @@ products use a different (deterministic) summation order; solve-level parity is
 held to the north_star bar: per-iteration residuals within 1e-10 relative,
 iteration count within +-1, solution within 1e-6 relative L2.
 """
+import hashlib
 import json
 import os
 
@@ -143,7 +144,9 @@ def check_solve(o, s, b, tol, maxit=100):
     assert abs(len(ho) - len(hg)) <= 1
     k = min(len(ho), len(hg))
     rel = np.abs(hg[:k] - ho[:k]) / ho[:k]
-    assert rel.max() < 1e-10, rel
+    assert rel.max() < 1e-10, rel  # north_star bar
+    # canonical reductions (OD-12): the whole solve is bit-identical
+    assert np.array_equal(hg, ho) and np.array_equal(xg, xo), rel.max()
     npres = o.counts(0)["np"]
     assert np.linalg.norm(xg[:-npres] - xo[:-npres]) / np.linalg.norm(xo[:-npres]) < 1e-6
     pg = xg[-npres:] - xg[-npres:].mean()
@@ -179,13 +182,14 @@ def test_golden_history(name):
     n = g["grid"][0]
     s = smg.Solver(n, levels=g["levels"])
     b = smg.forcing(n, kind=g["forcing"], seed=g["seed"])
-    assert float(np.linalg.norm(b)) == g["b_norm"]
+    assert hashlib.sha256(b.tobytes()).hexdigest() == g["b_sha256"]
     x, h, _, st = s.sqmr(b, tol=g["tol"], maxit=200)
     assert st == g["status"]
     assert abs(len(h) - g["iterations"]) <= 1
     k = min(len(h), g["iterations"])
     rel = np.abs(h[:k] - np.array(g["history"][:k])) / np.array(g["history"][:k])
     assert rel.max() < 1e-10, rel
+    assert h.tolist() == g["history"]  # bit-identical (canonical reductions, OD-12)
     npres = n ** 3
     assert abs(np.linalg.norm(x[:-npres]) - g["u_norm"]) / g["u_norm"] < 1e-6
     s.close()
