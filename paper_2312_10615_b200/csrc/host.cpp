@@ -163,6 +163,7 @@ struct DevLevel {
     int64_t counts[5] = {0, 0, 0, 0, 0};  // nu, nv, nw, np, |V1|
     int64_t N = 0;
     double *x = nullptr, *b = nullptr, *r = nullptr, *pd = nullptr;  // pd: DGS delta (one field)
+    double *pd0 = nullptr, *pd1 = nullptr;  // alternating delta buffers of the cooperative DGS sweep
     int32_t* vk_cells[8] = {};
     uint8_t* vk_mask[8] = {};
     int vk_n[8] = {};
@@ -188,6 +189,9 @@ struct smg_ctx {
     double* dscal = nullptr;
     double* hscal = nullptr;  // pinned
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    cudaGraphExec_t graph = nullptr;  // one SQMR iteration
+    int64_t graph_kernels = 0;
+    bool graph_captured_now = false;
     std::string err;
     smg_timing timing{};
     std::vector<void*> allocs;
@@ -207,6 +211,7 @@ struct smg_ctx {
         if (st) cudaStreamSynchronize(st);
         for (void* p : allocs) cudaFree(p);
         if (hscal) cudaFreeHost(hscal);
+        if (graph) cudaGraphExecDestroy(graph);
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);
         if (st) cudaStreamDestroy(st);
@@ -258,6 +263,8 @@ void build(smg_ctx* c) {
         L.b = c->dalloc<double>(vl);
         L.r = c->dalloc<double>(vl);
         L.pd = c->dalloc<double>(L.k.g.fs);
+        L.pd0 = c->dalloc<double>(L.k.g.fs);
+        L.pd1 = c->dalloc<double>(L.k.g.fs);
         // Vanka blocks: band cells, slot + active-face mask, by colour
         const int bw = p.band_width;
         auto band = [&](int x, int y, int z) {
@@ -446,13 +453,19 @@ void dgs_phase(smg_ctx* c, int l, double* x, const double* b, int ph) {
 
 void symmetric_dgs(smg_ctx* c, int l, double* x, const double* b) {
     const int nph = (c->prm.flags & SMG_FLAG_SKIP_REVERSE_DGS) ? kDgsPhases / 2 : kDgsPhases;
-    for (int ph = 0; ph < nph; ++ph) dgs_phase(c, l, x, b, ph);
+    DevLevel& L = c->lv[l];
+    launch_dgs_sym_coop(L.k, x, b, L.pd0, L.pd1, nph, c->st);
+}
+
+void vanka_sym_coop(smg_ctx* c, int l, double* x, const double* b) {
+    DevLevel& L = c->lv[l];
+    launch_vanka_sym_coop(L.k, x, b, L.vk_cells, L.vk_mask, L.vk_n, L.ktab, c->vk_delta, c->prm.nu, c->st);
 }
 
 void smooth(smg_ctx* c, int l, double* x, const double* b) {
-    for (int k = 0; k < c->prm.nu; ++k) vanka_sym(c, l, x, b);
+    vanka_sym_coop(c, l, x, b);
     symmetric_dgs(c, l, x, b);
-    for (int k = 0; k < c->prm.nu; ++k) vanka_sym(c, l, x, b);
+    vanka_sym_coop(c, l, x, b);
 }
 
 void coarse_solve(smg_ctx* c, const double* b, double* x) {
@@ -472,60 +485,83 @@ void vcycle(smg_ctx* c, int l, const double* b, double* x) {
     smooth(c, l, x, b);
 }
 
-// ---- BLAS-1 helpers with host readback ----
-void dot2(smg_ctx* c, const double* a, const double* b, const double* e, const double* f, double* out2) {
-    launch_cdot2(c->lv[0].k.g, a, b, e, f, c->partials, c->dscal, c->st);
-    CK(cudaMemcpyAsync(c->hscal, c->dscal, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->st));
-    CK(cudaStreamSynchronize(c->st));
-    out2[0] = c->hscal[0];
-    out2[1] = c->hscal[1];
+// ---- SQMR, Alg. 4 (SPEC:422-430); b in c->rhs, x into c->xs ----
+// One iteration (lines 5-10) is a fixed kernel sequence with its scalars on
+// the device; it is captured once as a CUDA graph and replayed.  The host
+// reads back only (rel, status) per iteration for the convergence test.
+void sqmr_iteration(smg_ctx* c) {
+    DevLevel& F = c->lv[0];
+    const int64_t n = vlen(F);
+    double *s = F.b, *t = F.x, *r = F.r, *sc = c->dscal;
+    const Geom& g = F.k.g;
+    launch_apply(F.k, c->q, nullptr, t, 0.0, c->st);                     // t = L q
+    launch_cdot2(g, c->q, t, nullptr, nullptr, c->partials, sc + S_D0, c->st);  // sigma
+    launch_sqmr_scalar(1, sc, c->st);                                    // alpha
+    launch_axpy_s(s, t, sc, n, c->st);                                   // s -= alpha t
+    vcycle(c, 0, s, t);                                                  // t = V(s)
+    launch_cdot2(g, t, t, s, t, c->partials, sc + S_D0, c->st);          // ||t||^2, rho_j
+    launch_sqmr_scalar(2, sc, c->st);                                    // nu, c, tau, cd, cq
+    launch_dx_dev(c->d, c->xs, c->q, sc, n, c->st);                      // d, x
+    launch_apply(F.k, c->xs, c->rhs, r, 0.0, c->st);                     // r = b - L x
+    launch_cdot2(g, r, r, nullptr, nullptr, c->partials, sc + S_D0, c->st);
+    launch_sqmr_scalar(3, sc, c->st);                                    // rel, beta
+    launch_xpby_dev(c->q, t, sc, n, c->st);                              // q = t + beta q
 }
 
-// ---- SQMR, Alg. 4 (SPEC:422-430); b in c->rhs, x into c->xs ----
 int sqmr(smg_ctx* c, double tol, int maxit, smg_history* hist, int* status) {
     DevLevel& F = c->lv[0];
     const int64_t n = vlen(F);
     double* s = F.b;
     double* t = F.x;
-    double* r = F.r;
-    double sc[2];
+    double* sc = c->dscal;
     const int64_t l0 = launch_count();
+    int64_t graph_launches = 0;
     auto t0 = std::chrono::steady_clock::now();
     CK(cudaEventRecord(c->ev0, c->st));
     if (hist) hist->count = 0;
     CK(cudaMemsetAsync(c->xs, 0, n * sizeof(double), c->st));
     CK(cudaMemsetAsync(c->d, 0, n * sizeof(double), c->st));
-    dot2(c, c->rhs, c->rhs, nullptr, nullptr, sc);
-    const double bnorm = std::sqrt(sc[0]);
+    CK(cudaMemsetAsync(sc, 0, S_COUNT * sizeof(double), c->st));
+    launch_cdot2(F.k.g, c->rhs, c->rhs, nullptr, nullptr, c->partials, sc + S_D0, c->st);
+    CK(cudaMemcpyAsync(c->hscal, sc, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    const double bnorm = std::sqrt(c->hscal[0]);
     int iters = 0;
     int st = SMG_MAX_ITERATIONS;
     if (bnorm == 0.0) {
         st = SMG_CONVERGED;
     } else {
+        c->hscal[2] = bnorm;
+        c->hscal[3] = tol;
+        CK(cudaMemcpyAsync(sc + S_BNORM, &c->hscal[2], sizeof(double), cudaMemcpyHostToDevice, c->st));
+        CK(cudaMemcpyAsync(sc + S_TOL, &c->hscal[3], sizeof(double), cudaMemcpyHostToDevice, c->st));
         CK(cudaMemcpyAsync(s, c->rhs, n * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
         vcycle(c, 0, s, t);
         CK(cudaMemcpyAsync(c->q, t, n * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
-        dot2(c, t, t, s, c->q, sc);
-        double tau = std::sqrt(sc[0]), nu_old = 0.0, rho = sc[1];
-        if (std::fabs(rho) < 1e-300) st = SMG_BREAKDOWN;
+        launch_cdot2(F.k.g, t, t, s, c->q, c->partials, sc + S_D0, c->st);
+        launch_sqmr_scalar(0, sc, c->st);
+        CK(cudaMemcpyAsync(c->hscal, sc + S_STATUS, sizeof(double), cudaMemcpyDeviceToHost, c->st));
+        CK(cudaStreamSynchronize(c->st));
+        if (c->hscal[0] != 0.0) st = SMG_BREAKDOWN;
+        if (st == SMG_MAX_ITERATIONS && maxit > 0 && !c->graph) {
+            const int64_t before = launch_count();
+            CK(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeRelaxed));
+            sqmr_iteration(c);
+            cudaGraph_t gr = nullptr;
+            CK(cudaStreamEndCapture(c->st, &gr));
+            CK(cudaGraphInstantiate(&c->graph, gr, 0));
+            CK(cudaGraphDestroy(gr));
+            c->graph_kernels = launch_count() - before;
+            c->graph_captured_now = true;
+        }
         for (int j = 1; j <= maxit && st == SMG_MAX_ITERATIONS; ++j) {
-            launch_apply(F.k, c->q, nullptr, t, 0.0, c->st);  // t = L q
-            dot2(c, c->q, t, nullptr, nullptr, sc);
-            const double sigma = sc[0];
-            if (std::fabs(sigma) < 1e-300) { st = SMG_BREAKDOWN; break; }
-            const double alpha = rho / sigma;
-            launch_axpy(s, t, -alpha, n, c->st);  // s = s - alpha t
-            vcycle(c, 0, s, t);                  // t = V(s)
-            dot2(c, t, t, s, t, sc);             // ||t||^2, rho_j = s.t
-            const double nu = std::sqrt(sc[0]) / tau;
-            const double cc = 1.0 / std::sqrt(1.0 + nu * nu);
-            tau = tau * nu * cc;
-            const double c2 = cc * cc;
-            launch_dx_update(c->d, c->xs, c->q, c2 * (nu_old * nu_old), c2 * alpha, n, c->st);
-            launch_apply(F.k, c->xs, c->rhs, r, 0.0, c->st);  // r = b - L x (true residual)
-            double rr[2];
-            dot2(c, r, r, nullptr, nullptr, rr);
-            const double rel = std::sqrt(rr[0]) / bnorm;
+            CK(cudaGraphLaunch(c->graph, c->st));
+            graph_launches += c->graph_kernels;
+            CK(cudaMemcpyAsync(c->hscal, sc + S_REL, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+            CK(cudaStreamSynchronize(c->st));
+            const double rel = c->hscal[0];
+            const int code = static_cast<int>(c->hscal[1]);
+            if (code == 2) { st = SMG_BREAKDOWN; break; }  // sigma breakdown: no residual this iteration
             iters = j;
             if (hist && hist->count < hist->capacity) {
                 hist->rel_residual[hist->count] = rel;
@@ -533,13 +569,8 @@ int sqmr(smg_ctx* c, double tol, int maxit, smg_history* hist, int* status) {
                     std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
                 hist->count++;
             }
-            if (rel < tol) { st = SMG_CONVERGED; break; }
-            const double rho_new = sc[1];
-            if (std::fabs(rho_new) < 1e-300) { st = SMG_BREAKDOWN; break; }
-            const double beta = rho_new / rho;
-            launch_xpby(c->q, t, beta, n, c->st);  // q = t + beta q
-            rho = rho_new;
-            nu_old = nu;
+            if (code == 1) st = SMG_CONVERGED;
+            else if (code == 3) st = SMG_BREAKDOWN;
         }
     }
     CK(cudaEventRecord(c->ev1, c->st));
@@ -548,7 +579,10 @@ int sqmr(smg_ctx* c, double tol, int maxit, smg_history* hist, int* status) {
     CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
     c->timing.solve_ms = ms;
     c->timing.iterations = iters;
-    c->timing.kernel_launches = launch_count() - l0;
+    // eager launches of this solve (capture-time launches are not executions) + graph replays
+    const int64_t eager = (launch_count() - l0) - (c->graph_captured_now ? c->graph_kernels : 0);
+    c->timing.kernel_launches = eager + graph_launches;
+    c->graph_captured_now = false;
     *status = st;
     return 0;
 }
@@ -657,7 +691,12 @@ int smg_smoother(smg_ctx* c, int level, int op, int arg, double* x, const double
             if (arg < 0 || arg > 7) throw SmgError(SMG_EINVAL, "colour out of range");
             launch_vanka_delta(L.k, L.x, L.b, L.vk_cells[arg], L.vk_mask[arg], L.vk_n[arg], L.ktab, c->vk_delta, c->st);
             launch_vanka_apply(L.k, L.x, L.vk_cells[arg], L.vk_mask[arg], L.vk_n[arg], c->vk_delta, c->st);
-        } else if (op == 3) vanka_sym(c, level, L.x, L.b);
+        } else if (op == 3) {
+            launch_vanka_sym_coop(L.k, L.x, L.b, L.vk_cells, L.vk_mask, L.vk_n, L.ktab, c->vk_delta, 1, c->st);
+        } else if (op == 5) {  // per-phase reference path of the symmetric sweeps (test only)
+            for (int ph = 0; ph < kDgsPhases; ++ph) dgs_phase(c, level, L.x, L.b, ph);
+            vanka_sym(c, level, L.x, L.b);
+        }
         else if (op == 4) smooth(c, level, L.x, L.b);
         else throw SmgError(SMG_EINVAL, "bad smoother op");
         download(c, level, L.x, x);

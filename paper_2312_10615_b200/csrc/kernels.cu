@@ -11,6 +11,8 @@
 #include <atomic>
 #include <cstdint>
 
+#include <cooperative_groups.h>
+
 #include "smg_internal.h"
 
 namespace smg {
@@ -463,6 +465,277 @@ __global__ void k_dx_update(double* __restrict__ d, double* __restrict__ x, cons
     }
 }
 
+// ------------------------------------------- cooperative smoother sweeps ------
+// One launch per symmetric sweep: the phases of the sweep run back to back in a
+// persistent grid separated by grid-wide barriers (all blocks co-resident).
+// Per-point arithmetic is the same as the single-phase kernels above.
+namespace cg = cooperative_groups;
+
+struct VankaLists {
+    const int32_t* cells[8];
+    const uint8_t* masks[8];
+    int n[8];
+};
+
+__device__ __forceinline__ void vanka_cell_delta(const LevelK& L, const double* __restrict__ X,
+                                                 const double* __restrict__ B, int64_t i, int m,
+                                                 const double* __restrict__ ktab, double* __restrict__ out) {
+    const Geom& g = L.g;
+    const int64_t fs = g.fs, sy = g.sy, sz = g.sz;
+    const double *U = X, *V = X + fs, *W = X + 2 * fs, *P = X + 3 * fs;
+    double r[7];
+    r[0] = (m & 1) ? B[i] - mom(L, U, P, i, 1) : 0.0;
+    r[1] = (m & 2) ? B[i + 1] - mom(L, U, P, i + 1, 1) : 0.0;
+    r[2] = (m & 4) ? B[fs + i] - mom(L, V, P, i, sy) : 0.0;
+    r[3] = (m & 8) ? B[fs + i + sy] - mom(L, V, P, i + sy, sy) : 0.0;
+    r[4] = (m & 16) ? B[2 * fs + i] - mom(L, W, P, i, sz) : 0.0;
+    r[5] = (m & 32) ? B[2 * fs + i + sz] - mom(L, W, P, i + sz, sz) : 0.0;
+    r[6] = B[3 * fs + i] - cont(L, U, V, W, P, i, L.gamma);
+    const double* K = ktab + m * 49;
+#pragma unroll
+    for (int s = 0; s < 7; ++s) {
+        double acc = 0.0;
+#pragma unroll
+        for (int q = 0; q < 7; ++q) acc = acc + K[s * 7 + q] * r[q];
+        out[s] = acc;
+    }
+}
+
+__device__ __forceinline__ void vanka_cell_apply(const LevelK& L, double* __restrict__ X, int64_t i, int m,
+                                                 const double* __restrict__ d) {
+    const Geom& g = L.g;
+    const int64_t fs = g.fs;
+    if (m & 1) X[i] = X[i] + d[0];
+    if (m & 2) X[i + 1] = X[i + 1] + d[1];
+    if (m & 4) X[fs + i] = X[fs + i] + d[2];
+    if (m & 8) X[fs + i + g.sy] = X[fs + i + g.sy] + d[3];
+    if (m & 16) X[2 * fs + i] = X[2 * fs + i] + d[4];
+    if (m & 32) X[2 * fs + i + g.sz] = X[2 * fs + i + g.sz] + d[5];
+    X[3 * fs + i] = X[3 * fs + i] + d[6];
+}
+
+// nu symmetric multiplicative Vanka sweeps (colours 0..7 then 7..0), Jacobi
+// within a colour: compute all deltas, barrier, apply, barrier.
+__global__ void __launch_bounds__(256) k_vanka_sym_coop(LevelK L, double* __restrict__ X,
+                                                        const double* __restrict__ B, VankaLists vl,
+                                                        const double* __restrict__ ktab,
+                                                        double* __restrict__ delta, int nu) {
+    cg::grid_group grid = cg::this_grid();
+    const int nth = gridDim.x * blockDim.x;
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+    for (int sweep = 0; sweep < nu; ++sweep)
+        for (int k = 0; k < 16; ++k) {
+            const int col = k < 8 ? k : 15 - k;
+            const int n = vl.n[col];
+            const int32_t* cells = vl.cells[col];
+            const uint8_t* masks = vl.masks[col];
+            for (int t = tid; t < n; t += nth) {
+                double d[7];
+                vanka_cell_delta(L, X, B, cells[t], masks[t], ktab, d);
+#pragma unroll
+                for (int s = 0; s < 7; ++s) delta[static_cast<int64_t>(t) * 8 + s] = d[s];
+            }
+            grid.sync();
+            for (int t = tid; t < n; t += nth) vanka_cell_apply(L, X, cells[t], masks[t], delta + static_cast<int64_t>(t) * 8);
+            grid.sync();
+        }
+}
+
+__device__ __forceinline__ void dgs_vel_cell(const LevelK& L, double* __restrict__ X, const double* __restrict__ B,
+                                             int x, int y, int z) {
+    const Geom& g = L.g;
+    const int64_t fs = g.fs, i = g.slot(x, y, z);
+    double *U = X, *V = X + fs, *W = X + 2 * fs;
+    const double* P = X + 3 * fs;
+    const bool here = band_cell(L, x, y, z);
+    if (x >= 1 && !here && !band_cell(L, x - 1, y, z)) {
+        const double r = B[i] - mom(L, U, P, i, 1);
+        U[i] = U[i] + r / L.dv;
+    }
+    if (y >= 1 && !here && !band_cell(L, x, y - 1, z)) {
+        const double r = B[fs + i] - mom(L, V, P, i, g.sy);
+        V[i] = V[i] + r / L.dv;
+    }
+    if (z >= 1 && !here && !band_cell(L, x, y, z - 1)) {
+        const double r = B[2 * fs + i] - mom(L, W, P, i, g.sz);
+        W[i] = W[i] + r / L.dv;
+    }
+}
+
+__device__ __forceinline__ void dgs_prev_cell(const LevelK& L, double* __restrict__ X, const double* __restrict__ B,
+                                              int64_t i) {
+    const Geom& g = L.g;
+    const int64_t fs = g.fs, sy = g.sy, sz = g.sz;
+    const double *U = X, *V = X + fs, *W = X + 2 * fs;
+    double* P = X + 3 * fs;
+    const double *BU = B, *BV = B + fs, *BW = B + 2 * fs, *BP = B + 3 * fs;
+    const double ruL = BU[i] - mom(L, U, P, i, 1);
+    const double ruR = BU[i + 1] - mom(L, U, P, i + 1, 1);
+    const double rvL = BV[i] - mom(L, V, P, i, sy);
+    const double rvR = BV[i + sy] - mom(L, V, P, i + sy, sy);
+    const double rwL = BW[i] - mom(L, W, P, i, sz);
+    const double rwR = BW[i + sz] - mom(L, W, P, i + sz, sz);
+    const double fl = ((ruR - ruL) + (rvR - rvL)) + (rwR - rwL);
+    const double rc = BP[i] - cont(L, U, V, W, P, i, L.gamma);
+    double s = BP[i - 1] - cont(L, U, V, W, P, i - 1, L.gamma);
+    s = s + (BP[i + 1] - cont(L, U, V, W, P, i + 1, L.gamma));
+    s = s + (BP[i - sy] - cont(L, U, V, W, P, i - sy, L.gamma));
+    s = s + (BP[i + sy] - cont(L, U, V, W, P, i + sy, L.gamma));
+    s = s + (BP[i - sz] - cont(L, U, V, W, P, i - sz, L.gamma));
+    s = s + (BP[i + sz] - cont(L, U, V, W, P, i + sz, L.gamma));
+    const double cj = fl * L.inv_h + L.eta_h2 * (6.0 * rc - s);
+    P[i] = P[i] + cj / L.dp;
+}
+
+// cells of parity colour c: t -> (x,y,z) on the half-grid of that parity
+__device__ __forceinline__ bool colour_cell(const Geom& g, int c, int64_t t, int& x, int& y, int& z) {
+    const int px = c & 1, py = (c >> 1) & 1, pz = (c >> 2) & 1;
+    const int hx = (g.nx - px + 1) >> 1, hy = (g.ny - py + 1) >> 1, hz = (g.nz - pz + 1) >> 1;
+    if (t >= static_cast<int64_t>(hx) * hy * hz) return false;
+    const int64_t r = t / hx;
+    x = 2 * static_cast<int>(t - r * hx) + px;
+    y = 2 * static_cast<int>(r % hy) + py;
+    z = 2 * static_cast<int>(r / hy) + pz;
+    return true;
+}
+
+// Symmetric DGS sweep (20 phases, OD-1) in one persistent launch.  Forward
+// pressure colour c uses delta buffer D[c&1]; its delta step also clears the
+// entries of colour c-2 left in that buffer, so only colour-c entries are
+// non-zero when the apply step gathers.
+__global__ void __launch_bounds__(256) k_dgs_sym_coop(LevelK L, double* __restrict__ X, const double* __restrict__ B,
+                                                      double* __restrict__ D0, double* __restrict__ D1, int nph) {
+    cg::grid_group grid = cg::this_grid();
+    const Geom& g = L.g;
+    const int64_t nth = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t ncell = static_cast<int64_t>(g.nx) * g.ny * g.nz;
+    const int64_t nxy = static_cast<int64_t>(g.nx) * g.ny;
+    const int64_t fs = g.fs, sy = g.sy, sz = g.sz;
+    for (int ph = 0; ph < nph; ++ph) {
+        if (ph == 0 || ph == 1 || ph == 18 || ph == 19) {
+            const int colour = ph < 2 ? ph : 19 - ph;
+            for (int64_t t = tid; t < ncell; t += nth) {
+                const int z = static_cast<int>(t / nxy);
+                const int64_t r = t - z * nxy;
+                const int y = static_cast<int>(r / g.nx), x = static_cast<int>(r - static_cast<int64_t>(y) * g.nx);
+                if (((x + y + z) & 1) == colour) dgs_vel_cell(L, X, B, x, y, z);
+            }
+        } else if (ph <= 9) {
+            const int c = ph - 2;
+            double* D = (c & 1) ? D1 : D0;
+            const int cold = (c + 6) & 7;  // colour c-2 (mod 8), same buffer
+            int x, y, z;
+            for (int64_t t = tid; colour_cell(g, cold, t, x, y, z); t += nth) D[g.slot(x, y, z)] = 0.0;
+            for (int64_t t = tid; colour_cell(g, c, t, x, y, z); t += nth) {
+                if (band_cell(L, x, y, z)) continue;
+                const int64_t i = g.slot(x, y, z);
+                const double rr = B[3 * fs + i] - cont(L, X, X + fs, X + 2 * fs, X + 3 * fs, i, L.gamma);
+                D[i] = rr / L.dp;
+            }
+            grid.sync();
+            // faces and pressure of colour-c cells
+            for (int64_t t = tid; colour_cell(g, c, t, x, y, z); t += nth) {
+                if (band_cell(L, x, y, z)) continue;
+                const int64_t i = g.slot(x, y, z);
+                const double dc = D[i];
+                X[i] = X[i] + (0.0 - dc) * L.inv_h;  // left u face of C: (d_left - d_right)/h with d_left = 0
+                X[i + 1] = X[i + 1] + (dc - 0.0) * L.inv_h;
+                X[fs + i] = X[fs + i] + (0.0 - dc) * L.inv_h;
+                X[fs + i + sy] = X[fs + i + sy] + (dc - 0.0) * L.inv_h;
+                X[2 * fs + i] = X[2 * fs + i] + (0.0 - dc) * L.inv_h;
+                X[2 * fs + i + sz] = X[2 * fs + i + sz] + (dc - 0.0) * L.inv_h;
+                double sn = D[i - 1] + D[i + 1];
+                sn = sn + D[i - sy];
+                sn = sn + D[i + sy];
+                sn = sn + D[i - sz];
+                sn = sn + D[i + sz];
+                X[3 * fs + i] = X[3 * fs + i] + L.eta_h2 * (6.0 * dc - sn);
+            }
+            // pressures of the three colours one parity bit away (the only cells with colour-c neighbours)
+            for (int bit = 1; bit < 8; bit <<= 1)
+                for (int64_t t = tid; colour_cell(g, c ^ bit, t, x, y, z); t += nth) {
+                    const int64_t i = g.slot(x, y, z);
+                    double sn = D[i - 1] + D[i + 1];
+                    sn = sn + D[i - sy];
+                    sn = sn + D[i + sy];
+                    sn = sn + D[i - sz];
+                    sn = sn + D[i + sz];
+                    X[3 * fs + i] = X[3 * fs + i] + L.eta_h2 * (6.0 * D[i] - sn);
+                }
+        } else {
+            const int c = 17 - ph;
+            int x, y, z;
+            for (int64_t t = tid; colour_cell(g, c, t, x, y, z); t += nth)
+                if (!band_cell(L, x, y, z)) dgs_prev_cell(L, X, B, g.slot(x, y, z));
+        }
+        if (ph + 1 < nph) grid.sync();
+    }
+}
+
+// ------------------------------------------------ SQMR device scalars ------
+// Alg. 4 scalar recurrences evaluated on the device (same expressions and
+// order as the oracle), so one SQMR iteration is a fixed kernel sequence that
+// can be replayed as a CUDA graph.  sc[] layout: see SqmrSlot in smg_internal.h.
+__global__ void k_sqmr_first(double* sc) {  // after dot2(t,t, s,q) of the initial V-cycle
+    sc[S_TAU] = sqrt(sc[S_D0]);
+    sc[S_NUOLD] = 0.0;
+    sc[S_RHO] = sc[S_D1];
+    sc[S_STATUS] = fabs(sc[S_RHO]) < 1e-300 ? 2.0 : 0.0;
+}
+__global__ void k_sqmr_alpha(double* sc) {  // after sigma = q.t
+    if (sc[S_STATUS] != 0.0) return;
+    const double sigma = sc[S_D0];
+    if (fabs(sigma) < 1e-300) { sc[S_STATUS] = 2.0; return; }
+    sc[S_ALPHA] = sc[S_RHO] / sigma;
+}
+__global__ void k_sqmr_nu(double* sc) {  // after ||t||^2 and rho_j = s.t
+    if (sc[S_STATUS] != 0.0) return;
+    const double nu = sqrt(sc[S_D0]) / sc[S_TAU];
+    const double c = 1.0 / sqrt(1.0 + nu * nu);
+    sc[S_TAU] = sc[S_TAU] * nu * c;
+    const double c2 = c * c;
+    sc[S_CD] = c2 * (sc[S_NUOLD] * sc[S_NUOLD]);
+    sc[S_CQ] = c2 * sc[S_ALPHA];
+    sc[S_NU] = nu;
+    sc[S_RHONEW] = sc[S_D1];
+}
+__global__ void k_sqmr_beta(double* sc) {  // after ||b - L x||^2
+    if (sc[S_STATUS] != 0.0) return;
+    const double rel = sqrt(sc[S_D0]) / sc[S_BNORM];
+    sc[S_REL] = rel;
+    if (rel < sc[S_TOL]) { sc[S_STATUS] = 1.0; return; }  // converged
+    const double rho_new = sc[S_RHONEW];
+    if (fabs(rho_new) < 1e-300) { sc[S_STATUS] = 3.0; return; }
+    sc[S_BETA] = rho_new / sc[S_RHO];
+    sc[S_RHO] = rho_new;
+    sc[S_NUOLD] = sc[S_NU];
+}
+__global__ void k_axpy_s(double* __restrict__ s, const double* __restrict__ t, const double* __restrict__ sc,
+                         int64_t n) {  // s = s - alpha t
+    if (sc[S_STATUS] != 0.0) return;
+    const double a = sc[S_ALPHA];
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
+        s[k] = s[k] - a * t[k];
+}
+__global__ void k_dx_dev(double* __restrict__ d, double* __restrict__ x, const double* __restrict__ q,
+                         const double* __restrict__ sc, int64_t n) {  // d = cd d + cq q; x += d
+    if (sc[S_STATUS] != 0.0) return;
+    const double cd = sc[S_CD], cq = sc[S_CQ];
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+        const double dn = cd * d[k] + cq * q[k];
+        d[k] = dn;
+        x[k] = x[k] + dn;
+    }
+}
+__global__ void k_xpby_dev(double* __restrict__ q, const double* __restrict__ t, const double* __restrict__ sc,
+                           int64_t n) {  // q = t + beta q
+    if (sc[S_STATUS] != 0.0) return;
+    const double b = sc[S_BETA];
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
+        q[k] = t[k] + b * q[k];
+}
+
 inline int stream_blocks(int64_t n) {
     const int64_t b = (n + 255) / 256;
     return static_cast<int>(b < 148 * 16 ? b : 148 * 16);
@@ -537,6 +810,77 @@ void launch_cdot2(const Geom& g, const double* a, const double* b, const double*
     k_cdot<<<dim3(g.nz + 1, 4), RED_T, 0, s>>>(g, a, b, c, d, partials);
     k_cdot_final<<<1, 64, 0, s>>>(partials, 4 * g.nz + 1, out);
     count();
+    count();
+}
+static int coop_blocks(const void* fn, int64_t work) {
+    static int sms = 0;
+    if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, 0);
+    const int64_t maxb = static_cast<int64_t>(sms) * (per_sm > 0 ? per_sm : 1);
+    const int64_t want = (work + 255) / 256;
+    return static_cast<int>(want < 1 ? 1 : (want < maxb ? want : maxb));
+}
+
+static void launch_coop(const void* fn, int blocks, void** args, cudaStream_t s) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(blocks);
+    cfg.blockDim = dim3(256);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelExC(&cfg, fn, args);
+    count();
+}
+
+void launch_vanka_sym_coop(const LevelK& L, double* x, const double* b, const int32_t* const* cells,
+                           const uint8_t* const* masks, const int* n, const double* ktab, double* delta, int nu,
+                           cudaStream_t s) {
+    VankaLists vl;
+    int maxn = 1;
+    for (int c = 0; c < 8; ++c) {
+        vl.cells[c] = cells[c];
+        vl.masks[c] = masks[c];
+        vl.n[c] = n[c];
+        maxn = n[c] > maxn ? n[c] : maxn;
+    }
+    LevelK Lc = L;
+    void* args[] = {&Lc, &x, const_cast<double**>(&b), &vl, const_cast<double**>(&ktab), &delta, &nu};
+    launch_coop(reinterpret_cast<const void*>(k_vanka_sym_coop), coop_blocks(reinterpret_cast<const void*>(k_vanka_sym_coop), maxn),
+                args, s);
+}
+
+void launch_dgs_sym_coop(const LevelK& L, double* x, const double* b, double* d0, double* d1, int nph,
+                         cudaStream_t s) {
+    const int64_t ncell = static_cast<int64_t>(L.g.nx) * L.g.ny * L.g.nz;
+    LevelK Lc = L;
+    void* args[] = {&Lc, &x, const_cast<double**>(&b), &d0, &d1, &nph};
+    launch_coop(reinterpret_cast<const void*>(k_dgs_sym_coop), coop_blocks(reinterpret_cast<const void*>(k_dgs_sym_coop), ncell),
+                args, s);
+}
+
+void launch_sqmr_scalar(int which, double* sc, cudaStream_t s) {
+    switch (which) {
+        case 0: k_sqmr_first<<<1, 1, 0, s>>>(sc); break;
+        case 1: k_sqmr_alpha<<<1, 1, 0, s>>>(sc); break;
+        case 2: k_sqmr_nu<<<1, 1, 0, s>>>(sc); break;
+        default: k_sqmr_beta<<<1, 1, 0, s>>>(sc); break;
+    }
+    count();
+}
+void launch_axpy_s(double* s_, const double* t, const double* sc, int64_t n, cudaStream_t s) {
+    k_axpy_s<<<stream_blocks(n), 256, 0, s>>>(s_, t, sc, n);
+    count();
+}
+void launch_dx_dev(double* d, double* x, const double* q, const double* sc, int64_t n, cudaStream_t s) {
+    k_dx_dev<<<stream_blocks(n), 256, 0, s>>>(d, x, q, sc, n);
+    count();
+}
+void launch_xpby_dev(double* q, const double* t, const double* sc, int64_t n, cudaStream_t s) {
+    k_xpby_dev<<<stream_blocks(n), 256, 0, s>>>(q, t, sc, n);
     count();
 }
 void launch_axpy(double* y, const double* x, double alpha, int64_t n, cudaStream_t s) {

@@ -65,6 +65,13 @@ void launch_vanka_delta(const LevelK& L, const double* x, const double* b, const
                         const uint8_t* masks, int ncells, const double* ktab, double* delta, cudaStream_t s);
 void launch_vanka_apply(const LevelK& L, double* x, const int32_t* cells, const uint8_t* masks, int ncells,
                         const double* delta, cudaStream_t s);
+// Cooperative (persistent, grid-synchronised) symmetric sweeps: nu Vanka sweeps
+// over the 8 colour lists; nph DGS phases (20 = full symmetric sweep).
+void launch_vanka_sym_coop(const LevelK& L, double* x, const double* b, const int32_t* const* cells,
+                           const uint8_t* const* masks, const int* n, const double* ktab, double* delta, int nu,
+                           cudaStream_t s);
+void launch_dgs_sym_coop(const LevelK& L, double* x, const double* b, double* d0, double* d1, int nph,
+                         cudaStream_t s);
 void launch_restrict(const LevelK& F, const LevelK& C, const double* rf, double* bc, cudaStream_t s);
 void launch_prolong_add(const LevelK& F, const LevelK& C, const double* xc, double* xf, cudaStream_t s);
 void launch_coarse_gemv(const double* ksym, const int32_t* slots, int n, const double* b, double* x,
@@ -82,6 +89,18 @@ void launch_axpy(double* y, const double* x, double alpha, int64_t n, cudaStream
 void launch_xpby(double* y, const double* x, double beta, int64_t n, cudaStream_t s);           // y = x + beta y
 void launch_dx_update(double* d, double* x, const double* q, double cd, double cq, int64_t n,
                       cudaStream_t s);  // d = cd d + cq q; x = x + d
+
+// SQMR scalar slots in device memory (Alg. 4 state + dot results).
+enum SqmrSlot {
+    S_D0 = 0, S_D1 = 1, S_BNORM = 2, S_TAU = 3, S_NUOLD = 4, S_RHO = 5, S_ALPHA = 6, S_NU = 7, S_CD = 8,
+    S_CQ = 9, S_RHONEW = 10, S_BETA = 11, S_REL = 12, S_STATUS = 13, S_TOL = 14, S_COUNT = 16
+};
+// which: 0 first (tau, rho from the initial dots), 1 alpha, 2 nu/c/tau/cd/cq, 3 rel/convergence/beta.
+// status slot: 0 running, 1 converged, 2 breakdown before the residual (sigma), 3 breakdown after it (rho).
+void launch_sqmr_scalar(int which, double* sc, cudaStream_t s);
+void launch_axpy_s(double* s_, const double* t, const double* sc, int64_t n, cudaStream_t s);
+void launch_dx_dev(double* d, double* x, const double* q, const double* sc, int64_t n, cudaStream_t s);
+void launch_xpby_dev(double* q, const double* t, const double* sc, int64_t n, cudaStream_t s);
 
 // Number of our kernels launched so far (per process), for the bench's gpu_launches.
 int64_t launch_count();
