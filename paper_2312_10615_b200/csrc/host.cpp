@@ -416,7 +416,7 @@ void build(smg_ctx* c) {
     for (auto& L : c->lv) maxN = std::max(maxN, L.N);
     c->compact = c->dalloc<double>(maxN);
     c->partials = c->dalloc<double>(kPartials);
-    c->dscal = c->dalloc<double>(8);
+    c->dscal = c->dalloc<double>(S_COUNT);
     CK(cudaMallocHost(&c->hscal, 8 * sizeof(double)));
     CK(cudaStreamSynchronize(c->st));
 }
