@@ -247,7 +247,7 @@ def run_ours(args, ws, rank, local):
 def roofline(s, n, nx, ny, nz, peak, peak_kind):
     """Fine-level symmetric DGS sweep (the largest V-cycle cost)."""
     reps = 5
-    ms = s.time_kernel(2, reps)
+    ms = s.time_kernel(2, reps, 0)
     # algorithmic bytes of one symmetric DGS sweep (DESIGN.md §5): every one of
     # the 20 phases reads the 7 fields it needs once and writes the updated one:
     # velocity phase: read u,v,w,p,bu,bv,bw (7 fields) + write u,v,w (3);
@@ -257,7 +257,7 @@ def roofline(s, n, nx, ny, nz, peak, peak_kind):
     fields = 4 * (7 + 3) + 8 * (5 + 4) + 8 * (8 + 1)
     alg_bytes = fields * 8 * cells
     achieved = alg_bytes / (ms / 1e3) / 1e9
-    apply_ms = s.time_kernel(0, 20)
+    apply_ms = s.time_kernel(0, 20, 0)
     return {"bound": "hbm", "kernel": "symmetric DGS sweep (20 phases), fine level", "achieved": achieved,
             "peak": peak, "peak_source": peak_kind, "unit": "GB/s", "frac": achieved / peak,
             "traffic": None, "algorithmic_bytes_per_launch": alg_bytes, "avg_ms": ms,

@@ -121,10 +121,12 @@ int smg_set_rhs(smg_ctx* ctx, const double* b);
 int smg_solve_resident(smg_ctx* ctx, double tol, int maxit, smg_history* hist, int* status);
 int smg_get_solution(smg_ctx* ctx, double* x);
 int smg_last_timing(const smg_ctx* ctx, smg_timing* out);
-/* Times `reps` back-to-back launches of one fine-level kernel (CUDA events,
- * average ms per launch).  which: 0 apply L, 1 residual, 2 symmetric DGS sweep
- * (8 phases), 3 one V-cycle. */
-int smg_time_kernel(smg_ctx* ctx, int which, int reps, double* avg_ms);
+/* Times `reps` back-to-back launches of one component on `level` (CUDA events
+ * on the solver stream, average ms per launch).  which: 0 apply L, 1 residual,
+ * 2 symmetric DGS sweep (20 phases), 3 V-cycle from this level, 4 symmetric
+ * Vanka sweep(s), 5 smooth (Alg. 3), 6 restrict, 7 prolong-add, 8 coarse
+ * solve, 9 fused pair of inner products, 10 axpy, 11 one SQMR iteration graph. */
+int smg_time_kernel(smg_ctx* ctx, int which, int level, int reps, double* avg_ms);
 
 /* Brackets a region for ncu --profile-from-start off (cudaProfilerStart/Stop). */
 int smg_profiler_range(int on);

@@ -793,16 +793,33 @@ int smg_last_timing(const smg_ctx* c, smg_timing* out) {
     return 0;
 }
 
-int smg_time_kernel(smg_ctx* c, int which, int reps, double* avg_ms) {
+int smg_time_kernel(smg_ctx* c, int which, int level, int reps, double* avg_ms) {
     return guard(c, [&] {
         if (reps < 1 || !avg_ms) throw SmgError(SMG_EINVAL, "bad reps");
-        DevLevel& F = c->lv[0];
+        check_level(c, level);
+        DevLevel& L = c->lv[level];
+        const bool coarse = level == static_cast<int>(c->lv.size()) - 1;
         auto one = [&] {
             switch (which) {
-                case 0: launch_apply(F.k, c->q, nullptr, F.r, 0.0, c->st); break;
-                case 1: launch_apply(F.k, c->xs, c->rhs, F.r, F.k.gamma, c->st); break;
-                case 2: symmetric_dgs(c, 0, F.x, F.b); break;
-                case 3: vcycle(c, 0, F.b, F.x); break;
+                case 0: launch_apply(L.k, L.x, nullptr, L.r, 0.0, c->st); break;
+                case 1: launch_apply(L.k, L.x, L.b, L.r, L.k.gamma, c->st); break;
+                case 2: symmetric_dgs(c, level, L.x, L.b); break;
+                case 3: vcycle(c, level, L.b, L.x); break;
+                case 4: vanka_sym_coop(c, level, L.x, L.b); break;
+                case 5: smooth(c, level, L.x, L.b); break;
+                case 6:
+                    if (!coarse) launch_restrict(L.k, c->lv[level + 1].k, L.r, c->lv[level + 1].b, c->st);
+                    break;
+                case 7:
+                    if (!coarse) launch_prolong_add(L.k, c->lv[level + 1].k, c->lv[level + 1].x, L.x, c->st);
+                    break;
+                case 8: coarse_solve(c, c->lv.back().b, c->lv.back().x); break;
+                case 9: launch_cdot2(L.k.g, L.x, L.x, L.b, L.b, c->partials, c->dscal, c->st); break;
+                case 10: launch_axpy_s(L.b, L.x, c->dscal, vlen(L), c->st); break;
+                case 11:
+                    if (!c->graph) throw SmgError(SMG_EINVAL, "no SQMR graph captured yet");
+                    CK(cudaGraphLaunch(c->graph, c->st));
+                    break;
                 default: throw SmgError(SMG_EINVAL, "bad kernel id");
             }
         };

@@ -10,6 +10,7 @@
 // multigrid coarse solve, krylov.
 #include <atomic>
 #include <cstdint>
+#include <cstdlib>
 
 #include <cooperative_groups.h>
 
@@ -813,10 +814,15 @@ void launch_cdot2(const Geom& g, const double* a, const double* b, const double*
     count();
 }
 static int coop_blocks(const void* fn, int64_t work) {
-    static int sms = 0;
+    static int sms = 0, cap = -1;
     if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    if (cap < 0) {
+        const char* e = std::getenv("SMG_COOP_BLOCKS_PER_SM");  // tuning knob
+        cap = e ? std::atoi(e) : 0;
+    }
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, 0);
+    if (cap > 0 && cap < per_sm) per_sm = cap;
     const int64_t maxb = static_cast<int64_t>(sms) * (per_sm > 0 ? per_sm : 1);
     const int64_t want = (work + 255) / 256;
     return static_cast<int>(want < 1 ? 1 : (want < maxb ? want : maxb));
