@@ -472,6 +472,14 @@ __global__ void k_dx_update(double* __restrict__ d, double* __restrict__ x, cons
 // Per-point arithmetic is the same as the single-phase kernels above.
 namespace cg = cooperative_groups;
 
+// Barrier between phases: MODE 0 = whole cooperative grid, MODE 1 = one thread
+// block cluster (<= 16 CTAs; barrier.cluster with release/acquire semantics).
+template <int MODE>
+__device__ __forceinline__ void phase_sync() {
+    if constexpr (MODE == 0) cg::this_grid().sync();
+    else cg::this_cluster().sync();
+}
+
 struct VankaLists {
     const int32_t* cells[8];
     const uint8_t* masks[8];
@@ -517,11 +525,11 @@ __device__ __forceinline__ void vanka_cell_apply(const LevelK& L, double* __rest
 
 // nu symmetric multiplicative Vanka sweeps (colours 0..7 then 7..0), Jacobi
 // within a colour: compute all deltas, barrier, apply, barrier.
-__global__ void __launch_bounds__(256) k_vanka_sym_coop(LevelK L, double* __restrict__ X,
+template <int MODE>
+__global__ void __launch_bounds__(512) k_vanka_sym_coop(LevelK L, double* __restrict__ X,
                                                         const double* __restrict__ B, VankaLists vl,
                                                         const double* __restrict__ ktab,
                                                         double* __restrict__ delta, int nu) {
-    cg::grid_group grid = cg::this_grid();
     const int nth = gridDim.x * blockDim.x;
     const int tid = blockIdx.x * blockDim.x + threadIdx.x;
     for (int sweep = 0; sweep < nu; ++sweep)
@@ -536,9 +544,9 @@ __global__ void __launch_bounds__(256) k_vanka_sym_coop(LevelK L, double* __rest
 #pragma unroll
                 for (int s = 0; s < 7; ++s) delta[static_cast<int64_t>(t) * 8 + s] = d[s];
             }
-            grid.sync();
+            phase_sync<MODE>();
             for (int t = tid; t < n; t += nth) vanka_cell_apply(L, X, cells[t], masks[t], delta + static_cast<int64_t>(t) * 8);
-            grid.sync();
+            phase_sync<MODE>();
         }
 }
 
@@ -604,9 +612,9 @@ __device__ __forceinline__ bool colour_cell(const Geom& g, int c, int64_t t, int
 // pressure colour c uses delta buffer D[c&1]; its delta step also clears the
 // entries of colour c-2 left in that buffer, so only colour-c entries are
 // non-zero when the apply step gathers.
-__global__ void __launch_bounds__(256) k_dgs_sym_coop(LevelK L, double* __restrict__ X, const double* __restrict__ B,
+template <int MODE>
+__global__ void __launch_bounds__(512) k_dgs_sym_coop(LevelK L, double* __restrict__ X, const double* __restrict__ B,
                                                       double* __restrict__ D0, double* __restrict__ D1, int nph) {
-    cg::grid_group grid = cg::this_grid();
     const Geom& g = L.g;
     const int64_t nth = static_cast<int64_t>(gridDim.x) * blockDim.x;
     const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -634,7 +642,7 @@ __global__ void __launch_bounds__(256) k_dgs_sym_coop(LevelK L, double* __restri
                 const double rr = B[3 * fs + i] - cont(L, X, X + fs, X + 2 * fs, X + 3 * fs, i, L.gamma);
                 D[i] = rr / L.dp;
             }
-            grid.sync();
+            phase_sync<MODE>();
             // faces and pressure of colour-c cells
             for (int64_t t = tid; colour_cell(g, c, t, x, y, z); t += nth) {
                 if (band_cell(L, x, y, z)) continue;
@@ -670,7 +678,7 @@ __global__ void __launch_bounds__(256) k_dgs_sym_coop(LevelK L, double* __restri
             for (int64_t t = tid; colour_cell(g, c, t, x, y, z); t += nth)
                 if (!band_cell(L, x, y, z)) dgs_prev_cell(L, X, B, g.slot(x, y, z));
         }
-        if (ph + 1 < nph) grid.sync();
+        if (ph + 1 < nph) phase_sync<MODE>();
     }
 }
 
@@ -813,33 +821,61 @@ void launch_cdot2(const Geom& g, const double* a, const double* b, const double*
     count();
     count();
 }
+static int env_int(const char* name, int dflt) {
+    const char* e = std::getenv(name);
+    return e ? std::atoi(e) : dflt;
+}
+
+// Grid size of a cooperative (grid-synchronised) launch: enough 256-thread
+// blocks for `work` items, capped at full co-residency.
 static int coop_blocks(const void* fn, int64_t work) {
-    static int sms = 0, cap = -1;
+    static int sms = 0;
     if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    if (cap < 0) {
-        const char* e = std::getenv("SMG_COOP_BLOCKS_PER_SM");  // tuning knob
-        cap = e ? std::atoi(e) : 0;
-    }
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, 0);
+    const int cap = env_int("SMG_COOP_BLOCKS_PER_SM", 0);  // tuning knob
     if (cap > 0 && cap < per_sm) per_sm = cap;
     const int64_t maxb = static_cast<int64_t>(sms) * (per_sm > 0 ? per_sm : 1);
     const int64_t want = (work + 255) / 256;
     return static_cast<int>(want < 1 ? 1 : (want < maxb ? want : maxb));
 }
 
-static void launch_coop(const void* fn, int blocks, void** args, cudaStream_t s) {
+constexpr int kClusterCTAs = 16, kClusterThreads = 512;
+
+// Launch either as one cooperative grid (MODE 0) or as a single cluster of
+// kClusterCTAs CTAs (MODE 1) whose phases are separated by cluster barriers.
+static void launch_sweep(const void* fn_grid, const void* fn_cluster, bool cluster, int64_t work, void** args,
+                         cudaStream_t s) {
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(blocks);
-    cfg.blockDim = dim3(256);
-    cfg.stream = s;
     cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeCooperative;
-    attr[0].val.cooperative = 1;
+    cfg.stream = s;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaLaunchKernelExC(&cfg, fn, args);
+    if (cluster) {
+        cudaFuncSetAttribute(fn_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        cfg.gridDim = dim3(kClusterCTAs);
+        cfg.blockDim = dim3(kClusterThreads);
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = kClusterCTAs;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cudaLaunchKernelExC(&cfg, fn_cluster, args);
+    } else {
+        cfg.gridDim = dim3(coop_blocks(fn_grid, work));
+        cfg.blockDim = dim3(256);
+        attr[0].id = cudaLaunchAttributeCooperative;
+        attr[0].val.cooperative = 1;
+        cudaLaunchKernelExC(&cfg, fn_grid, args);
+    }
     count();
+}
+
+// SMG_SYNC_MODE: 0 auto (cluster when the sweep is small enough), 1 grid, 2 cluster.
+static bool use_cluster(int64_t work, int64_t max_items_per_thread) {
+    const int mode = env_int("SMG_SYNC_MODE", 0);
+    if (mode == 1) return false;
+    if (mode == 2) return true;
+    return work <= static_cast<int64_t>(kClusterCTAs) * kClusterThreads * max_items_per_thread;
 }
 
 void launch_vanka_sym_coop(const LevelK& L, double* x, const double* b, const int32_t* const* cells,
@@ -855,8 +891,8 @@ void launch_vanka_sym_coop(const LevelK& L, double* x, const double* b, const in
     }
     LevelK Lc = L;
     void* args[] = {&Lc, &x, const_cast<double**>(&b), &vl, const_cast<double**>(&ktab), &delta, &nu};
-    launch_coop(reinterpret_cast<const void*>(k_vanka_sym_coop), coop_blocks(reinterpret_cast<const void*>(k_vanka_sym_coop), maxn),
-                args, s);
+    launch_sweep(reinterpret_cast<const void*>(k_vanka_sym_coop<0>), reinterpret_cast<const void*>(k_vanka_sym_coop<1>),
+                 use_cluster(maxn, 4), maxn, args, s);
 }
 
 void launch_dgs_sym_coop(const LevelK& L, double* x, const double* b, double* d0, double* d1, int nph,
@@ -864,8 +900,8 @@ void launch_dgs_sym_coop(const LevelK& L, double* x, const double* b, double* d0
     const int64_t ncell = static_cast<int64_t>(L.g.nx) * L.g.ny * L.g.nz;
     LevelK Lc = L;
     void* args[] = {&Lc, &x, const_cast<double**>(&b), &d0, &d1, &nph};
-    launch_coop(reinterpret_cast<const void*>(k_dgs_sym_coop), coop_blocks(reinterpret_cast<const void*>(k_dgs_sym_coop), ncell),
-                args, s);
+    launch_sweep(reinterpret_cast<const void*>(k_dgs_sym_coop<0>), reinterpret_cast<const void*>(k_dgs_sym_coop<1>),
+                 use_cluster(ncell, 4), ncell, args, s);
 }
 
 void launch_sqmr_scalar(int which, double* sc, cudaStream_t s) {

@@ -112,6 +112,19 @@ def test_vcycle(pair16):
     same(s.vcycle(b), o.vcycle(b))
 
 
+@pytest.mark.parametrize("mode", ["1", "2"])
+def test_sweep_sync_modes_bitwise(pair16, mode, monkeypatch):
+    """Grid-wide (1) and single-cluster (2) barrier variants of the sweeps agree bit for bit."""
+    o, s = pair16
+    monkeypatch.setenv("SMG_SYNC_MODE", mode)
+    for level in (0, 1):
+        n = o.ndof(level)
+        x, b = rnd(n, 40 + level), rnd(n, 41)
+        same(s.smoother(smg.OP_SMOOTH, x, b, level), o.smoother(4, x, b, level))
+    b = rnd(o.ndof(0), 42)
+    same(s.vcycle(b), o.vcycle(b))
+
+
 def test_vcycle_symmetry_gpu_materialized():
     # SURVEY §7 f1 / SPEC AC 4 on the GPU map itself
     s = smg.Solver(8, levels=2)
