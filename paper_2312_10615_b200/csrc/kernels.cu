@@ -486,66 +486,72 @@ struct VankaLists {
     int n[8];
 };
 
-__device__ __forceinline__ void vanka_cell_delta(const LevelK& L, const double* __restrict__ X,
-                                                 const double* __restrict__ B, int64_t i, int m,
-                                                 const double* __restrict__ ktab, double* __restrict__ out) {
-    const Geom& g = L.g;
-    const int64_t fs = g.fs, sy = g.sy, sz = g.sz;
-    const double *U = X, *V = X + fs, *W = X + 2 * fs, *P = X + 3 * fs;
-    double r[7];
-    r[0] = (m & 1) ? B[i] - mom(L, U, P, i, 1) : 0.0;
-    r[1] = (m & 2) ? B[i + 1] - mom(L, U, P, i + 1, 1) : 0.0;
-    r[2] = (m & 4) ? B[fs + i] - mom(L, V, P, i, sy) : 0.0;
-    r[3] = (m & 8) ? B[fs + i + sy] - mom(L, V, P, i + sy, sy) : 0.0;
-    r[4] = (m & 16) ? B[2 * fs + i] - mom(L, W, P, i, sz) : 0.0;
-    r[5] = (m & 32) ? B[2 * fs + i + sz] - mom(L, W, P, i + sz, sz) : 0.0;
-    r[6] = B[3 * fs + i] - cont(L, U, V, W, P, i, L.gamma);
-    const double* K = ktab + m * 49;
-#pragma unroll
-    for (int s = 0; s < 7; ++s) {
-        double acc = 0.0;
-#pragma unroll
-        for (int q = 0; q < 7; ++q) acc = acc + K[s * 7 + q] * r[q];
-        out[s] = acc;
-    }
-}
-
-__device__ __forceinline__ void vanka_cell_apply(const LevelK& L, double* __restrict__ X, int64_t i, int m,
-                                                 const double* __restrict__ d) {
-    const Geom& g = L.g;
-    const int64_t fs = g.fs;
-    if (m & 1) X[i] = X[i] + d[0];
-    if (m & 2) X[i + 1] = X[i + 1] + d[1];
-    if (m & 4) X[fs + i] = X[fs + i] + d[2];
-    if (m & 8) X[fs + i + g.sy] = X[fs + i + g.sy] + d[3];
-    if (m & 16) X[2 * fs + i] = X[2 * fs + i] + d[4];
-    if (m & 32) X[2 * fs + i + g.sz] = X[2 * fs + i + g.sz] + d[5];
-    X[3 * fs + i] = X[3 * fs + i] + d[6];
-}
-
 // nu symmetric multiplicative Vanka sweeps (colours 0..7 then 7..0), Jacobi
-// within a colour: compute all deltas, barrier, apply, barrier.
-template <int MODE>
+// within a colour.  Each thread owns up to CPT blocks of the colour: it loads
+// their residual stencils, keeps the block's own 7 values and its correction
+// in registers, waits at the barrier (all reads of the phase done), then
+// stores own + delta (bit-identical to re-loading, since only this thread
+// writes those DOFs in the phase) and waits again.  The 64 local inverses sit
+// in shared memory.
+template <int MODE, int CPT>
 __global__ void __launch_bounds__(512) k_vanka_sym_coop(LevelK L, double* __restrict__ X,
                                                         const double* __restrict__ B, VankaLists vl,
-                                                        const double* __restrict__ ktab,
-                                                        double* __restrict__ delta, int nu) {
+                                                        const double* __restrict__ ktab, int nu) {
+    __shared__ double Ks[64 * 49];
+    for (int k = threadIdx.x; k < 64 * 49; k += blockDim.x) Ks[k] = ktab[k];
+    __syncthreads();
+    const Geom& g = L.g;
+    const int64_t fs = g.fs, sy = g.sy, sz = g.sz;
     const int nth = gridDim.x * blockDim.x;
     const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t off[7] = {0, 1, fs, fs + sy, 2 * fs, 2 * fs + sz, 3 * fs};
     for (int sweep = 0; sweep < nu; ++sweep)
         for (int k = 0; k < 16; ++k) {
             const int col = k < 8 ? k : 15 - k;
             const int n = vl.n[col];
-            const int32_t* cells = vl.cells[col];
-            const uint8_t* masks = vl.masks[col];
-            for (int t = tid; t < n; t += nth) {
-                double d[7];
-                vanka_cell_delta(L, X, B, cells[t], masks[t], ktab, d);
+            int64_t slot[CPT];
+            int msk[CPT];
+            double own[CPT][7], dl[CPT][7];
 #pragma unroll
-                for (int s = 0; s < 7; ++s) delta[static_cast<int64_t>(t) * 8 + s] = d[s];
+            for (int j = 0; j < CPT; ++j) {
+                const int t = tid + j * nth;
+                msk[j] = -1;
+                if (t >= n) continue;
+                const int64_t i = vl.cells[col][t];
+                const int m = vl.masks[col][t];
+                slot[j] = i;
+                msk[j] = m;
+                const double *U = X, *V = X + fs, *W = X + 2 * fs, *P = X + 3 * fs;
+                double r[7];
+                r[0] = (m & 1) ? B[i] - mom(L, U, P, i, 1) : 0.0;
+                r[1] = (m & 2) ? B[i + 1] - mom(L, U, P, i + 1, 1) : 0.0;
+                r[2] = (m & 4) ? B[fs + i] - mom(L, V, P, i, sy) : 0.0;
+                r[3] = (m & 8) ? B[fs + i + sy] - mom(L, V, P, i + sy, sy) : 0.0;
+                r[4] = (m & 16) ? B[2 * fs + i] - mom(L, W, P, i, sz) : 0.0;
+                r[5] = (m & 32) ? B[2 * fs + i + sz] - mom(L, W, P, i + sz, sz) : 0.0;
+                r[6] = B[3 * fs + i] - cont(L, U, V, W, P, i, L.gamma);
+#pragma unroll
+                for (int q = 0; q < 7; ++q) own[j][q] = X[i + off[q]];
+                const double* K = Ks + m * 49;
+#pragma unroll
+                for (int s2 = 0; s2 < 7; ++s2) {
+                    double acc = 0.0;
+#pragma unroll
+                    for (int q = 0; q < 7; ++q) acc = acc + K[s2 * 7 + q] * r[q];
+                    dl[j][s2] = acc;
+                }
             }
             phase_sync<MODE>();
-            for (int t = tid; t < n; t += nth) vanka_cell_apply(L, X, cells[t], masks[t], delta + static_cast<int64_t>(t) * 8);
+#pragma unroll
+            for (int j = 0; j < CPT; ++j) {
+                const int m = msk[j];
+                if (m < 0) continue;
+                const int64_t i = slot[j];
+#pragma unroll
+                for (int q = 0; q < 6; ++q)
+                    if (m & (1 << q)) X[i + off[q]] = own[j][q] + dl[j][q];
+                X[i + off[6]] = own[j][6] + dl[j][6];
+            }
             phase_sync<MODE>();
         }
 }
@@ -881,6 +887,7 @@ static bool use_cluster(int64_t work, int64_t max_items_per_thread) {
 void launch_vanka_sym_coop(const LevelK& L, double* x, const double* b, const int32_t* const* cells,
                            const uint8_t* const* masks, const int* n, const double* ktab, double* delta, int nu,
                            cudaStream_t s) {
+    (void)delta;
     VankaLists vl;
     int maxn = 1;
     for (int c = 0; c < 8; ++c) {
@@ -890,9 +897,28 @@ void launch_vanka_sym_coop(const LevelK& L, double* x, const double* b, const in
         maxn = n[c] > maxn ? n[c] : maxn;
     }
     LevelK Lc = L;
-    void* args[] = {&Lc, &x, const_cast<double**>(&b), &vl, const_cast<double**>(&ktab), &delta, &nu};
-    launch_sweep(reinterpret_cast<const void*>(k_vanka_sym_coop<0>), reinterpret_cast<const void*>(k_vanka_sym_coop<1>),
-                 use_cluster(maxn, 4), maxn, args, s);
+    void* args[] = {&Lc, &x, const_cast<double**>(&b), &vl, const_cast<double**>(&ktab), &nu};
+    constexpr int CPT = 2;
+    // every block of a colour must fit in registers: grid mode is sized for ceil(maxn / CPT) threads
+    const bool cl = use_cluster(maxn, CPT);
+    if (!cl) {
+        static int sms = 0;
+        if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_vanka_sym_coop<0, CPT>, 256, 0);
+        if (static_cast<int64_t>(sms) * per_sm * 256 * CPT < maxn) {  // too large: per-phase kernels
+            for (int sweep = 0; sweep < nu; ++sweep)
+                for (int k = 0; k < 16; ++k) {
+                    const int col = k < 8 ? k : 15 - k;
+                    launch_vanka_delta(L, x, b, cells[col], masks[col], n[col], ktab, delta, s);
+                    launch_vanka_apply(L, x, cells[col], masks[col], n[col], delta, s);
+                }
+            return;
+        }
+    }
+    launch_sweep(reinterpret_cast<const void*>(k_vanka_sym_coop<0, CPT>),
+                 reinterpret_cast<const void*>(k_vanka_sym_coop<1, CPT>), cl, (maxn + CPT - 1) / CPT,
+                 args, s);
 }
 
 void launch_dgs_sym_coop(const LevelK& L, double* x, const double* b, double* d0, double* d1, int nph,
