@@ -688,6 +688,83 @@ __global__ void __launch_bounds__(512) k_dgs_sym_coop(LevelK L, double* __restri
     }
 }
 
+// -------------------------------------- colour-compact per-phase DGS kernels ------
+// For large levels: one kernel per phase (graph-captured; a kernel boundary is
+// cheaper than a grid barrier), threads mapped onto the cells of the phase's
+// colour only, so every thread works and only the needed rows are touched.
+// Per-cell arithmetic is shared with the kernels above (bit-identical).
+__global__ void __launch_bounds__(256) k_dgs_vel_c(LevelK L, double* __restrict__ X, const double* __restrict__ B,
+                                                   int colour) {
+    const Geom& g = L.g;
+    const int i = blockIdx.x * 32 + threadIdx.x, y = blockIdx.y * 8 + threadIdx.y, z = blockIdx.z;
+    const int x = 2 * i + ((y + z + colour) & 1);
+    if (x >= g.nx || y >= g.ny) return;
+    dgs_vel_cell(L, X, B, x, y, z);
+}
+
+__device__ __forceinline__ bool half_cell(const Geom& g, int c, int i, int j, int k, int& x, int& y, int& z) {
+    x = 2 * i + (c & 1);
+    y = 2 * j + ((c >> 1) & 1);
+    z = 2 * k + ((c >> 2) & 1);
+    return x < g.nx && y < g.ny && z < g.nz;
+}
+
+__global__ void __launch_bounds__(256) k_dgs_pf_delta_c(LevelK L, const double* __restrict__ X,
+                                                        const double* __restrict__ B, double* __restrict__ D,
+                                                        int c) {
+    const Geom& g = L.g;
+    const int i = blockIdx.x * 32 + threadIdx.x, j = blockIdx.y * 8 + threadIdx.y, k = blockIdx.z;
+    int x, y, z;
+    if (half_cell(g, (c + 6) & 7, i, j, k, x, y, z)) D[g.slot(x, y, z)] = 0.0;  // stale colour c-2
+    if (!half_cell(g, c, i, j, k, x, y, z) || band_cell(L, x, y, z)) return;
+    const int64_t fs = g.fs, ii = g.slot(x, y, z);
+    const double rr = B[3 * fs + ii] - cont(L, X, X + fs, X + 2 * fs, X + 3 * fs, ii, L.gamma);
+    D[ii] = rr / L.dp;
+}
+
+__device__ __forceinline__ void p_gather_update(const LevelK& L, double* __restrict__ X, const double* __restrict__ D,
+                                                int64_t i) {
+    const Geom& g = L.g;
+    const int64_t fs = g.fs, sy = g.sy, sz = g.sz;
+    double sn = D[i - 1] + D[i + 1];
+    sn = sn + D[i - sy];
+    sn = sn + D[i + sy];
+    sn = sn + D[i - sz];
+    sn = sn + D[i + sz];
+    X[3 * fs + i] = X[3 * fs + i] + L.eta_h2 * (6.0 * D[i] - sn);
+}
+
+__global__ void __launch_bounds__(256) k_dgs_pf_apply_c(LevelK L, double* __restrict__ X, const double* __restrict__ D,
+                                                        int c) {
+    const Geom& g = L.g;
+    const int i = blockIdx.x * 32 + threadIdx.x, j = blockIdx.y * 8 + threadIdx.y, k = blockIdx.z;
+    const int64_t fs = g.fs, sy = g.sy, sz = g.sz;
+    int x, y, z;
+    if (half_cell(g, c, i, j, k, x, y, z) && !band_cell(L, x, y, z)) {
+        const int64_t ii = g.slot(x, y, z);
+        const double dc = D[ii];
+        X[ii] = X[ii] + (0.0 - dc) * L.inv_h;
+        X[ii + 1] = X[ii + 1] + (dc - 0.0) * L.inv_h;
+        X[fs + ii] = X[fs + ii] + (0.0 - dc) * L.inv_h;
+        X[fs + ii + sy] = X[fs + ii + sy] + (dc - 0.0) * L.inv_h;
+        X[2 * fs + ii] = X[2 * fs + ii] + (0.0 - dc) * L.inv_h;
+        X[2 * fs + ii + sz] = X[2 * fs + ii + sz] + (dc - 0.0) * L.inv_h;
+        p_gather_update(L, X, D, ii);
+    }
+#pragma unroll
+    for (int bit = 1; bit < 8; bit <<= 1)
+        if (half_cell(g, c ^ bit, i, j, k, x, y, z)) p_gather_update(L, X, D, g.slot(x, y, z));
+}
+
+__global__ void __launch_bounds__(256) k_dgs_prev_c(LevelK L, double* __restrict__ X, const double* __restrict__ B,
+                                                    int c) {
+    const Geom& g = L.g;
+    const int i = blockIdx.x * 32 + threadIdx.x, j = blockIdx.y * 8 + threadIdx.y, k = blockIdx.z;
+    int x, y, z;
+    if (!half_cell(g, c, i, j, k, x, y, z) || band_cell(L, x, y, z)) return;
+    dgs_prev_cell(L, X, B, g.slot(x, y, z));
+}
+
 // ------------------------------------------------ SQMR device scalars ------
 // Alg. 4 scalar recurrences evaluated on the device (same expressions and
 // order as the oracle), so one SQMR iteration is a fixed kernel sequence that
@@ -921,8 +998,36 @@ void launch_vanka_sym_coop(const LevelK& L, double* x, const double* b, const in
                  args, s);
 }
 
+// Per-phase launches of a symmetric DGS sweep (same phase numbering and
+// delta-buffer protocol as k_dgs_sym_coop).
+static void launch_dgs_sym_phases(const LevelK& L, double* x, const double* b, double* d0, double* d1, int nph,
+                                  cudaStream_t s) {
+    const Geom& g = L.g;
+    const dim3 blk(32, 8);
+    const dim3 gv((((g.nx + 1) / 2) + 31) / 32, (g.ny + 7) / 8, g.nz);
+    const dim3 gh((((g.nx + 1) / 2) + 31) / 32, (((g.ny + 1) / 2) + 7) / 8, (g.nz + 1) / 2);
+    for (int ph = 0; ph < nph; ++ph) {
+        if (ph == 0 || ph == 1 || ph == 18 || ph == 19) {
+            k_dgs_vel_c<<<gv, blk, 0, s>>>(L, x, b, ph < 2 ? ph : 19 - ph);
+        } else if (ph <= 9) {
+            const int c = ph - 2;
+            double* D = (c & 1) ? d1 : d0;
+            k_dgs_pf_delta_c<<<gh, blk, 0, s>>>(L, x, b, D, c);
+            k_dgs_pf_apply_c<<<gh, blk, 0, s>>>(L, x, D, c);
+            count();
+        } else {
+            k_dgs_prev_c<<<gh, blk, 0, s>>>(L, x, b, 17 - ph);
+        }
+        count();
+    }
+}
+
 void launch_dgs_sym_coop(const LevelK& L, double* x, const double* b, double* d0, double* d1, int nph,
                          cudaStream_t s) {
+    if (static_cast<int64_t>(L.g.nx) * L.g.ny * L.g.nz > 32768 && env_int("SMG_DGS_COOP", 0) == 0) {
+        launch_dgs_sym_phases(L, x, b, d0, d1, nph, s);
+        return;
+    }
     const int64_t ncell = static_cast<int64_t>(L.g.nx) * L.g.ny * L.g.nz;
     LevelK Lc = L;
     void* args[] = {&Lc, &x, const_cast<double**>(&b), &d0, &d1, &nph};
