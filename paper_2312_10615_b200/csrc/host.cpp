@@ -463,6 +463,12 @@ void vanka_sym_coop(smg_ctx* c, int l, double* x, const double* b) {
 }
 
 void smooth(smg_ctx* c, int l, double* x, const double* b) {
+    DevLevel& L = c->lv[l];
+    if (smooth_smem_fits(L.k)) {
+        const int nph = (c->prm.flags & SMG_FLAG_SKIP_REVERSE_DGS) ? kDgsPhases / 2 : kDgsPhases;
+        launch_smooth_smem(L.k, x, b, L.vk_cells, L.vk_mask, L.vk_n, L.ktab, L.pd0, L.pd1, c->prm.nu, nph, c->st);
+        return;
+    }
     vanka_sym_coop(c, l, x, b);
     symmetric_dgs(c, l, x, b);
     vanka_sym_coop(c, l, x, b);

@@ -477,7 +477,8 @@ namespace cg = cooperative_groups;
 template <int MODE>
 __device__ __forceinline__ void phase_sync() {
     if constexpr (MODE == 0) cg::this_grid().sync();
-    else cg::this_cluster().sync();
+    else if constexpr (MODE == 1) cg::this_cluster().sync();
+    else __syncthreads();  // MODE 2: single CTA (shared-memory-resident level)
 }
 
 struct VankaLists {
@@ -494,16 +495,11 @@ struct VankaLists {
 // writes those DOFs in the phase) and waits again.  The 64 local inverses sit
 // in shared memory.
 template <int MODE, int CPT>
-__global__ void __launch_bounds__(512) k_vanka_sym_coop(LevelK L, double* __restrict__ X,
-                                                        const double* __restrict__ B, VankaLists vl,
-                                                        const double* __restrict__ ktab, int nu) {
-    __shared__ double Ks[64 * 49];
-    for (int k = threadIdx.x; k < 64 * 49; k += blockDim.x) Ks[k] = ktab[k];
-    __syncthreads();
+__device__ __forceinline__ void vanka_sweeps(const LevelK& L, double* __restrict__ X, const double* __restrict__ B,
+                                             const VankaLists& vl, const double* __restrict__ Ks, int nu, int tid,
+                                             int nth) {
     const Geom& g = L.g;
     const int64_t fs = g.fs, sy = g.sy, sz = g.sz;
-    const int nth = gridDim.x * blockDim.x;
-    const int tid = blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t off[7] = {0, 1, fs, fs + sy, 2 * fs, 2 * fs + sz, 3 * fs};
     for (int sweep = 0; sweep < nu; ++sweep)
         for (int k = 0; k < 16; ++k) {
@@ -554,6 +550,16 @@ __global__ void __launch_bounds__(512) k_vanka_sym_coop(LevelK L, double* __rest
             }
             phase_sync<MODE>();
         }
+}
+
+template <int MODE, int CPT>
+__global__ void __launch_bounds__(512) k_vanka_sym_coop(LevelK L, double* __restrict__ X,
+                                                        const double* __restrict__ B, VankaLists vl,
+                                                        const double* __restrict__ ktab, int nu) {
+    __shared__ double Ks[64 * 49];
+    for (int k = threadIdx.x; k < 64 * 49; k += blockDim.x) Ks[k] = ktab[k];
+    __syncthreads();
+    vanka_sweeps<MODE, CPT>(L, X, B, vl, Ks, nu, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
 }
 
 __device__ __forceinline__ void dgs_vel_cell(const LevelK& L, double* __restrict__ X, const double* __restrict__ B,
@@ -619,11 +625,10 @@ __device__ __forceinline__ bool colour_cell(const Geom& g, int c, int64_t t, int
 // entries of colour c-2 left in that buffer, so only colour-c entries are
 // non-zero when the apply step gathers.
 template <int MODE>
-__global__ void __launch_bounds__(512) k_dgs_sym_coop(LevelK L, double* __restrict__ X, const double* __restrict__ B,
-                                                      double* __restrict__ D0, double* __restrict__ D1, int nph) {
+__device__ __forceinline__ void dgs_sweep(const LevelK& L, double* __restrict__ X, const double* __restrict__ B,
+                                          double* __restrict__ D0, double* __restrict__ D1, int nph, int64_t tid,
+                                          int64_t nth) {
     const Geom& g = L.g;
-    const int64_t nth = static_cast<int64_t>(gridDim.x) * blockDim.x;
-    const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const int64_t ncell = static_cast<int64_t>(g.nx) * g.ny * g.nz;
     const int64_t nxy = static_cast<int64_t>(g.nx) * g.ny;
     const int64_t fs = g.fs, sy = g.sy, sz = g.sz;
@@ -686,6 +691,35 @@ __global__ void __launch_bounds__(512) k_dgs_sym_coop(LevelK L, double* __restri
         }
         if (ph + 1 < nph) phase_sync<MODE>();
     }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(512) k_dgs_sym_coop(LevelK L, double* __restrict__ X, const double* __restrict__ B,
+                                                      double* __restrict__ D0, double* __restrict__ D1, int nph) {
+    dgs_sweep<MODE>(L, X, B, D0, D1, nph, static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x,
+                    static_cast<int64_t>(gridDim.x) * blockDim.x);
+}
+
+// Whole Alg. 3 smooth of a small level in ONE CTA with the level vector held
+// in shared memory (layout identical to the global one, compact geometry):
+// every phase barrier is a __syncthreads, no global fences.  b and the DGS
+// delta buffers stay in global memory (visible within the CTA at barriers).
+__global__ void __launch_bounds__(512) k_smooth_smem(LevelK L, double* __restrict__ Xg, const double* __restrict__ B,
+                                                      VankaLists vl, const double* __restrict__ ktab,
+                                                      double* __restrict__ D0, double* __restrict__ D1, int nu,
+                                                      int nph) {
+    extern __shared__ double smem[];
+    double* Ks = smem;
+    double* X = smem + 64 * 49;
+    const int64_t nv = 4 * L.g.fs;
+    for (int k = threadIdx.x; k < 64 * 49; k += blockDim.x) Ks[k] = ktab[k];
+    for (int64_t k = threadIdx.x; k < nv; k += blockDim.x) X[k] = Xg[k];
+    __syncthreads();
+    vanka_sweeps<2, 1>(L, X, B, vl, Ks, nu, threadIdx.x, blockDim.x);
+    dgs_sweep<2>(L, X, B, D0, D1, nph, threadIdx.x, blockDim.x);
+    __syncthreads();
+    vanka_sweeps<2, 1>(L, X, B, vl, Ks, nu, threadIdx.x, blockDim.x);
+    for (int64_t k = threadIdx.x; k < nv; k += blockDim.x) Xg[k] = X[k];
 }
 
 // -------------------------------------- colour-compact per-phase DGS kernels ------
@@ -996,6 +1030,26 @@ void launch_vanka_sym_coop(const LevelK& L, double* x, const double* b, const in
     launch_sweep(reinterpret_cast<const void*>(k_vanka_sym_coop<0, CPT>),
                  reinterpret_cast<const void*>(k_vanka_sym_coop<1, CPT>), cl, (maxn + CPT - 1) / CPT,
                  args, s);
+}
+
+bool smooth_smem_fits(const LevelK& L) {
+    return (64 * 49 + 4 * L.g.fs) * static_cast<int64_t>(sizeof(double)) <= 227 * 1024 &&
+           env_int("SMG_NO_SMEM_SMOOTH", 0) == 0;
+}
+
+void launch_smooth_smem(const LevelK& L, double* x, const double* b, const int32_t* const* cells,
+                        const uint8_t* const* masks, const int* n, const double* ktab, double* d0, double* d1, int nu,
+                        int nph, cudaStream_t s) {
+    VankaLists vl;
+    for (int c = 0; c < 8; ++c) {
+        vl.cells[c] = cells[c];
+        vl.masks[c] = masks[c];
+        vl.n[c] = n[c];
+    }
+    const size_t smem = (64 * 49 + 4 * L.g.fs) * sizeof(double);
+    cudaFuncSetAttribute(k_smooth_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    k_smooth_smem<<<1, 512, smem, s>>>(L, x, b, vl, ktab, d0, d1, nu, nph);
+    count();
 }
 
 // Per-phase launches of a symmetric DGS sweep (same phase numbering and

@@ -21,18 +21,25 @@ struct Geom {
     int px, py, pz;      // padded extents (doubles)
     int64_t sy, sz;      // strides of y and z
     int64_t fs;          // stride between fields of one vector (multiple of 32)
+    int xo;              // row offset of slot x = 0 (4: 32-byte aligned rows; 1: compact small levels)
     __host__ __device__ __forceinline__ int64_t slot(int x, int y, int z) const {
-        return static_cast<int64_t>(z + 1) * sz + static_cast<int64_t>(y + 1) * sy + (x + 4);
+        return static_cast<int64_t>(z + 1) * sz + static_cast<int64_t>(y + 1) * sy + (x + xo);
     }
     int64_t vec_len() const { return 4 * fs; }
 };
+
+// Levels whose whole vector fits in one SM's shared memory use a compact
+// layout (x-offset 1, unaligned pitch) so a CTA can smooth them in smem.
+constexpr int64_t kSmemLevelCells = 6144;
 
 inline Geom make_geom(int nx, int ny, int nz) {
     Geom g;
     g.nx = nx;
     g.ny = ny;
     g.nz = nz;
-    g.px = ((nx + 5) + 7) / 8 * 8;
+    const bool compact = static_cast<int64_t>(nx + 2) * (ny + 2) * (nz + 2) <= kSmemLevelCells;
+    g.xo = compact ? 1 : 4;
+    g.px = compact ? nx + 2 : ((nx + 5) + 7) / 8 * 8;
     g.py = ny + 2;
     g.pz = nz + 2;
     g.sy = g.px;
@@ -72,6 +79,11 @@ void launch_vanka_sym_coop(const LevelK& L, double* x, const double* b, const in
                            cudaStream_t s);
 void launch_dgs_sym_coop(const LevelK& L, double* x, const double* b, double* d0, double* d1, int nph,
                          cudaStream_t s);
+// Whole smooth (Alg. 3) of a level small enough for one CTA's shared memory.
+bool smooth_smem_fits(const LevelK& L);
+void launch_smooth_smem(const LevelK& L, double* x, const double* b, const int32_t* const* cells,
+                        const uint8_t* const* masks, const int* n, const double* ktab, double* d0, double* d1, int nu,
+                        int nph, cudaStream_t s);
 void launch_restrict(const LevelK& F, const LevelK& C, const double* rf, double* bc, cudaStream_t s);
 void launch_prolong_add(const LevelK& F, const LevelK& C, const double* xc, double* xf, cudaStream_t s);
 void launch_coarse_gemv(const double* ksym, const int32_t* slots, int n, const double* b, double* x,
