@@ -562,6 +562,79 @@ __global__ void __launch_bounds__(512) k_vanka_sym_coop(LevelK L, double* __rest
     vanka_sweeps<MODE, CPT>(L, X, B, vl, Ks, nu, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
 }
 
+// Lane-parallel Vanka: 8 lanes per block; lane s < 7 computes residual slot s
+// and owns DOF s; delta_s = sum_q K[s][q] r_q gathers r_q by warp shuffles in
+// ascending q (same order as the oracle).  Each thread holds at most CPT
+// (own, delta) pairs across the barrier.
+template <int MODE, int CPT>
+__device__ __forceinline__ void vanka_sweeps8(const LevelK& L, double* __restrict__ X, const double* __restrict__ B,
+                                              const VankaLists& vl, const double* __restrict__ Ks, int nu, int tid,
+                                              int nth) {
+    const Geom& g = L.g;
+    const int64_t fs = g.fs, sy = g.sy, sz = g.sz;
+    const int lane = threadIdx.x & 31, s8 = lane & 7;
+    const int groups = nth >> 3, grp = tid >> 3;
+    const int64_t offs = s8 == 0 ? 0 : s8 == 1 ? 1 : s8 == 2 ? fs : s8 == 3 ? fs + sy : s8 == 4 ? 2 * fs
+                         : s8 == 5 ? 2 * fs + sz : 3 * fs;
+    for (int sweep = 0; sweep < nu; ++sweep)
+        for (int k = 0; k < 16; ++k) {
+            const int col = k < 8 ? k : 15 - k;
+            const int n = vl.n[col];
+            double own[CPT], dl[CPT];
+            int64_t dst[CPT];
+#pragma unroll
+            for (int j = 0; j < CPT; ++j) {
+                const int t = grp + j * groups;
+                dst[j] = -1;
+                // whole warps iterate together (shuffles); inactive groups use t = -1
+                const bool act = t < n;
+                int64_t i = 0;
+                int m = 0;
+                if (act) {
+                    i = vl.cells[col][t];
+                    m = vl.masks[col][t];
+                }
+                double r = 0.0;
+                if (act && s8 < 7) {
+                    const double *U = X, *V = X + fs, *W = X + 2 * fs, *P = X + 3 * fs;
+                    switch (s8) {
+                        case 0: r = (m & 1) ? B[i] - mom(L, U, P, i, 1) : 0.0; break;
+                        case 1: r = (m & 2) ? B[i + 1] - mom(L, U, P, i + 1, 1) : 0.0; break;
+                        case 2: r = (m & 4) ? B[fs + i] - mom(L, V, P, i, sy) : 0.0; break;
+                        case 3: r = (m & 8) ? B[fs + i + sy] - mom(L, V, P, i + sy, sy) : 0.0; break;
+                        case 4: r = (m & 16) ? B[2 * fs + i] - mom(L, W, P, i, sz) : 0.0; break;
+                        case 5: r = (m & 32) ? B[2 * fs + i + sz] - mom(L, W, P, i + sz, sz) : 0.0; break;
+                        default: r = B[3 * fs + i] - cont(L, U, V, W, P, i, L.gamma); break;
+                    }
+                    own[j] = X[i + offs];
+                }
+                const double* K = Ks + m * 49 + (s8 < 7 ? s8 : 0) * 7;
+                double acc = 0.0;
+#pragma unroll
+                for (int q = 0; q < 7; ++q) {
+                    const double rq = __shfl_sync(0xffffffffu, r, (lane & ~7) + q);
+                    acc = acc + K[q] * rq;
+                }
+                dl[j] = acc;
+                if (act && s8 < 7 && (s8 == 6 || (m & (1 << s8)))) dst[j] = i + offs;
+            }
+            phase_sync<MODE>();
+#pragma unroll
+            for (int j = 0; j < CPT; ++j)
+                if (dst[j] >= 0) X[dst[j]] = own[j] + dl[j];
+            phase_sync<MODE>();
+        }
+}
+
+template <int MODE, int CPT>
+__global__ void __launch_bounds__(512) k_vanka8(LevelK L, double* __restrict__ X, const double* __restrict__ B,
+                                                VankaLists vl, const double* __restrict__ ktab, int nu) {
+    __shared__ double Ks[64 * 49];
+    for (int k = threadIdx.x; k < 64 * 49; k += blockDim.x) Ks[k] = ktab[k];
+    __syncthreads();
+    vanka_sweeps8<MODE, CPT>(L, X, B, vl, Ks, nu, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
+}
+
 __device__ __forceinline__ void dgs_vel_cell(const LevelK& L, double* __restrict__ X, const double* __restrict__ B,
                                              int x, int y, int z) {
     const Geom& g = L.g;
@@ -995,10 +1068,15 @@ static bool use_cluster(int64_t work, int64_t max_items_per_thread) {
     return work <= static_cast<int64_t>(kClusterCTAs) * kClusterThreads * max_items_per_thread;
 }
 
+template <int CPT>
+static void launch_vanka8(bool cl, int64_t threads, void** args, cudaStream_t s) {
+    launch_sweep(reinterpret_cast<const void*>(k_vanka8<0, CPT>), reinterpret_cast<const void*>(k_vanka8<1, CPT>), cl,
+                 threads, args, s);
+}
+
 void launch_vanka_sym_coop(const LevelK& L, double* x, const double* b, const int32_t* const* cells,
                            const uint8_t* const* masks, const int* n, const double* ktab, double* delta, int nu,
                            cudaStream_t s) {
-    (void)delta;
     VankaLists vl;
     int maxn = 1;
     for (int c = 0; c < 8; ++c) {
@@ -1009,27 +1087,28 @@ void launch_vanka_sym_coop(const LevelK& L, double* x, const double* b, const in
     }
     LevelK Lc = L;
     void* args[] = {&Lc, &x, const_cast<double**>(&b), &vl, const_cast<double**>(&ktab), &nu};
-    constexpr int CPT = 2;
-    // every block of a colour must fit in registers: grid mode is sized for ceil(maxn / CPT) threads
-    const bool cl = use_cluster(maxn, CPT);
-    if (!cl) {
-        static int sms = 0;
-        if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-        int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_vanka_sym_coop<0, CPT>, 256, 0);
-        if (static_cast<int64_t>(sms) * per_sm * 256 * CPT < maxn) {  // too large: per-phase kernels
-            for (int sweep = 0; sweep < nu; ++sweep)
-                for (int k = 0; k < 16; ++k) {
-                    const int col = k < 8 ? k : 15 - k;
-                    launch_vanka_delta(L, x, b, cells[col], masks[col], n[col], ktab, delta, s);
-                    launch_vanka_apply(L, x, cells[col], masks[col], n[col], delta, s);
-                }
-            return;
-        }
+    const int64_t lanes = 8 * static_cast<int64_t>(maxn);
+    static int sms = 0;
+    if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_vanka8<0, 1>, 256, 0);
+    const int64_t grid_threads = static_cast<int64_t>(sms) * (per_sm > 0 ? per_sm : 1) * 256;
+    const int64_t cl_threads = static_cast<int64_t>(kClusterCTAs) * kClusterThreads;
+    const bool cl = env_int("SMG_SYNC_MODE", 0) == 2 || (env_int("SMG_SYNC_MODE", 0) == 0 && lanes <= cl_threads);
+    const int64_t cap = cl ? cl_threads : grid_threads;
+    const int64_t need = (lanes + cap - 1) / cap;  // cells per thread-group
+    if (need <= 1) launch_vanka8<1>(cl, lanes, args, s);
+    else if (need <= 2) launch_vanka8<2>(cl, (lanes + 1) / 2, args, s);
+    else if (need <= 4) launch_vanka8<4>(cl, (lanes + 3) / 4, args, s);
+    else if (need <= 8) launch_vanka8<8>(cl, (lanes + 7) / 8, args, s);
+    else {  // beyond co-resident capacity: per-phase kernels
+        for (int sweep = 0; sweep < nu; ++sweep)
+            for (int k = 0; k < 16; ++k) {
+                const int col = k < 8 ? k : 15 - k;
+                launch_vanka_delta(L, x, b, cells[col], masks[col], n[col], ktab, delta, s);
+                launch_vanka_apply(L, x, cells[col], masks[col], n[col], delta, s);
+            }
     }
-    launch_sweep(reinterpret_cast<const void*>(k_vanka_sym_coop<0, CPT>),
-                 reinterpret_cast<const void*>(k_vanka_sym_coop<1, CPT>), cl, (maxn + CPT - 1) / CPT,
-                 args, s);
 }
 
 bool smooth_smem_fits(const LevelK& L) {
