@@ -212,9 +212,9 @@ def run_ours(args, ws, rank, local):
         e2e_it += len(hh)
     e2e_s = allmax(time.perf_counter() - t0, ws)
     e2e_val = ws * n * e2e_it / e2e_s
-    # ---- roofline of the dominant kernel (symmetric DGS sweep on the fine level) ----
+    # ---- roofline of the dominant component (fine-level smooth) + whole iteration ----
     peak, peak_kind = measured_peak_gbs()
-    roof = roofline(s, n, nx, ny, nz, peak, peak_kind)
+    roof = roofline(s, lv, peak, peak_kind, dev_ms / max(iters, 1))
     out = None
     if rank == 0:
         cpu = None
@@ -244,24 +244,58 @@ def run_ours(args, ws, rank, local):
     return out
 
 
-def roofline(s, n, nx, ny, nz, peak, peak_kind):
-    """Fine-level symmetric DGS sweep (the largest V-cycle cost)."""
+def level_counts(s, levels):
+    out = []
+    for l in range(levels):
+        c = s.counts(l)
+        n = c["nu"] + c["nv"] + c["nw"] + c["np"]
+        out.append((n, c["V1"], n - c["V1"]))
+    return out
+
+
+def b_iter_model(cnt, nu=1):
+    """Algorithmic bytes of one SQMR iteration, SURVEY §8(d):
+    136 N0 + sum_{l<L-1} [2 (48 N_l^V2 + 96 nu N_l^V1) + 24 N_l + (8 N_l + 8 N_l+1) + (16 N_l + 8 N_l+1)]
+    + 8 Nc^2 + 16 Nc."""
+    b = 136 * cnt[0][0]
+    for l in range(len(cnt) - 1):
+        n, v1, v2 = cnt[l]
+        nc = cnt[l + 1][0]
+        b += 2 * (48 * v2 + 96 * nu * v1) + 24 * n + (8 * n + 8 * nc) + (16 * n + 8 * nc)
+    nc = cnt[-1][0]
+    return b + 8 * nc * nc + 16 * nc
+
+
+def roofline(s, levels, peak, peak_kind, iter_ms):
+    """Dominant component: the fine-level smooth (Alg. 3 = nu Vanka + symmetric DGS + nu Vanka), which is
+    ~45% of an iteration at cfg 1.  Algorithmic bytes per SURVEY §8(d): 48 B per V2 DOF (symmetric DGS) +
+    96 nu B per V1 DOF (two symmetric Vanka sweeps)."""
+    cnt = level_counts(s, levels)
+    n0, v1, v2 = cnt[0]
     reps = 5
-    ms = s.time_kernel(2, reps, 0)
-    # algorithmic bytes of one symmetric DGS sweep (DESIGN.md §5): every one of
-    # the 20 phases reads the 7 fields it needs once and writes the updated one:
-    # velocity phase: read u,v,w,p,bu,bv,bw (7 fields) + write u,v,w (3);
-    # pressure fwd phase: read u,v,w,p,bp (5) + write u,v,w,p (4);
-    # pressure rev phase: read u,v,w,p,bu,bv,bw,bp (8) + write p (1).
-    cells = nx * ny * nz
-    fields = 4 * (7 + 3) + 8 * (5 + 4) + 8 * (8 + 1)
-    alg_bytes = fields * 8 * cells
-    achieved = alg_bytes / (ms / 1e3) / 1e9
+    smooth_ms = s.time_kernel(5, reps, 0)
+    dgs_ms = s.time_kernel(2, reps, 0)
+    vanka_ms = s.time_kernel(4, reps, 0)
     apply_ms = s.time_kernel(0, 20, 0)
-    return {"bound": "hbm", "kernel": "symmetric DGS sweep (20 phases), fine level", "achieved": achieved,
-            "peak": peak, "peak_source": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": None, "algorithmic_bytes_per_launch": alg_bytes, "avg_ms": ms,
-            "apply_L": {"avg_ms": apply_ms, "achieved_gbs": 16 * n / (apply_ms / 1e3) / 1e9}}
+    alg = 48 * v2 + 96 * v1
+    achieved = alg / (smooth_ms / 1e3) / 1e9
+    biter = b_iter_model(cnt)
+    return {
+        "bound": "hbm", "kernel": "fine-level smooth (Alg. 3: Vanka sweep, 20-phase symmetric DGS, Vanka sweep)",
+        "achieved": achieved, "peak": peak, "peak_source": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+        "traffic": None, "algorithmic_bytes_per_launch": alg, "avg_ms": smooth_ms,
+        "units": {"N_V2": v2, "N_V1": v1, "bytes_per_V2_dof": 48, "bytes_per_V1_dof": 96},
+        "components": {
+            "dgs_sym_sweep": {"avg_ms": dgs_ms, "alg_bytes": 48 * v2,
+                              "achieved_gbs": 48 * v2 / (dgs_ms / 1e3) / 1e9},
+            "vanka_sym_sweep": {"avg_ms": vanka_ms, "alg_bytes": 48 * v1,
+                                "achieved_gbs": 48 * v1 / (vanka_ms / 1e3) / 1e9,
+                                "note": "latency-bound: 32 dependent barrier steps per sweep"},
+            "apply_L": {"avg_ms": apply_ms, "alg_bytes": 16 * n0, "achieved_gbs": 16 * n0 / (apply_ms / 1e3) / 1e9},
+        },
+        "iteration": {"alg_bytes": biter, "ms": iter_ms, "achieved_gbs": biter / (iter_ms / 1e3) / 1e9,
+                      "frac": biter / (iter_ms / 1e3) / 1e9 / peak, "model": "SURVEY §8(d) B_iter"},
+    }
 
 
 def main():
