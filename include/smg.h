@@ -79,10 +79,18 @@ typedef struct smg_timing {
 } smg_timing;
 
 /* build_hierarchy: grids, operators, transfers, Vanka tables,
- * coarse dense inverse; uploads everything.  ngpu must be 1 in this build. */
+ * coarse dense inverse; uploads everything.  ngpu > 1 builds a z-slab
+ * decomposition over the listed devices (a device may repeat: parts then share
+ * it, which emulates the multi-GPU data path on one GPU); see smg_slab_plan.
+ * Results are bit-identical for every ngpu. */
 int smg_create(const smg_grid_desc* grid, const smg_params* params, int ngpu, const int* dev_ids,
                smg_ctx** out);
 void smg_destroy(smg_ctx* ctx);
+/* z-slab plan (host only, no device needed): returns the number of leading
+ * levels split over nparts (>= 1, or <= 0 if the grid cannot be split), and for
+ * `rank` the first global plane z0[l] and plane count nzl[l] of every level
+ * (replicated levels: 0 and the whole level).  Either array may be NULL. */
+int smg_slab_plan(const smg_grid_desc* grid, int levels, int nparts, int rank, int* z0, int* nzl);
 const char* smg_last_error(const smg_ctx* ctx);
 const char* smg_version(void);
 

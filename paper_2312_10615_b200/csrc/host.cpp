@@ -196,6 +196,13 @@ struct smg_ctx {
     smg_timing timing{};
     std::vector<void*> allocs;
     bool rhs_set = false;
+    // z-slab decomposition: this context is part `rank` of `nparts`;
+    // levels < ndist are slabs of their level, the others are replicated whole.
+    int rank = 0, nparts = 1, ndist = 0;
+    std::vector<smg_ctx*> parts;                    // parts[0] == the owning (master) context
+    std::vector<std::unique_ptr<smg_ctx>> owned;   // parts 1..P-1 (owned by the master)
+    double* shared_partials = nullptr;             // plane partials all parts write (master's device)
+    bool own_stream = true;
 
     template <class T>
     T* dalloc(int64_t count) {
@@ -214,7 +221,7 @@ struct smg_ctx {
         if (graph) cudaGraphExecDestroy(graph);
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);
-        if (st) cudaStreamDestroy(st);
+        if (st && own_stream) cudaStreamDestroy(st);
     }
 };
 
@@ -223,7 +230,8 @@ namespace {
 int64_t vlen(const DevLevel& L) { return L.k.g.vec_len(); }
 
 // ---- setup ----
-void build(smg_ctx* c) {
+void build(smg_ctx* c, const std::vector<double>* shared_coarse = nullptr, std::vector<double>* coarse_out = nullptr,
+           cudaStream_t shared_stream = nullptr) {
     const smg_grid_desc& g = c->grid;
     const smg_params& p = c->prm;
     if (g.dim != 3) throw SmgError(SMG_EINVAL, "dim must be 3");
@@ -237,7 +245,12 @@ void build(smg_ctx* c) {
     if (g.nx / div < 2 || g.ny / div < 2 || g.nz / div < 2)
         throw SmgError(SMG_EINVAL, "coarsened extent below 2 (SPEC:82)");
     CK(cudaSetDevice(c->device));
-    CK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+    if (shared_stream) {
+        c->st = shared_stream;
+        c->own_stream = false;
+    } else {
+        CK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+    }
     CK(cudaEventCreate(&c->ev0));
     CK(cudaEventCreate(&c->ev1));
     c->lv.resize(p.levels);
@@ -246,7 +259,9 @@ void build(smg_ctx* c) {
         DevLevel& L = c->lv[l];
         const int nx = g.nx >> l, ny = g.ny >> l, nz = g.nz >> l;
         const double h = g.h * static_cast<double>(1 << l);
-        L.k.g = make_geom(nx, ny, nz);
+        const bool dist = l < c->ndist;
+        const int nzl = dist ? nz / c->nparts : nz, z0 = dist ? c->rank * nzl : 0;
+        L.k.g = dist ? make_geom(nx, ny, nzl, z0, nz, 2) : make_geom(nx, ny, nz);
         L.k.eta_h2 = p.eta / (h * h);
         L.k.inv_h = 1.0 / h;
         L.k.gamma = p.gamma;
@@ -284,6 +299,7 @@ void build(smg_ctx* c) {
                     if (z >= 1 && (bc || band(x, y, z - 1))) ++v1;
                     if (!bc) continue;
                     ++v1;
+                    if (z < z0 || z >= z0 + nzl) continue;  // Vanka blocks of the owned planes only
                     int m = 0;
                     if (x >= 1) m |= 1;
                     if (x + 1 <= nx - 1) m |= 2;
@@ -292,7 +308,7 @@ void build(smg_ctx* c) {
                     if (z >= 1) m |= 16;
                     if (z + 1 <= nz - 1) m |= 32;
                     const int col = (x & 1) + 2 * (y & 1) + 4 * (z & 1);
-                    cells[col].push_back(static_cast<int32_t>(L.k.g.slot(x, y, z)));
+                    cells[col].push_back(static_cast<int32_t>(L.k.g.slot(x, y, z - z0)));
                     masks[col].push_back(static_cast<uint8_t>(m));
                     used[m] = true;
                 }
@@ -400,7 +416,10 @@ void build(smg_ctx* c) {
                 put(id, wid(x, y, z + 1), -ih);
                 put(id, id, -p.gamma);
             }
-    std::vector<double> K = dense_inverse_sym(std::move(A), n);
+    std::vector<double> K;
+    if (shared_coarse) K = *shared_coarse;  // same matrix on every part: factorise once
+    else K = dense_inverse_sym(std::move(A), n);
+    if (coarse_out) *coarse_out = K;
     c->coarse_k = c->dalloc<double>(static_cast<int64_t>(n) * n);
     c->coarse_slots = c->dalloc<int32_t>(n);
     CK(cudaMemcpyAsync(c->coarse_k, K.data(), K.size() * sizeof(double), cudaMemcpyHostToDevice, c->st));
@@ -606,6 +625,303 @@ void download(smg_ctx* c, int l, const double* dev_padded, double* host) {
     CK(cudaStreamSynchronize(c->st));
 }
 
+// =================================================== z-slab decomposition ====
+// P parts each own a z-slab of every level l < ndist (2 halo
+// planes per side) and a replicated copy of the coarser levels.  Every smoother
+// phase on a slab level is followed by a halo exchange, so each part applies
+// exactly the single-GPU per-point updates to its planes: results are
+// bit-identical to one part.  Parts may share one device (emulation, used by
+// the tests) or sit on separate devices (peer copies, cudaMemcpyDefault).
+using Sel = double* (*)(DevLevel&);
+double* sel_x(DevLevel& L) { return L.x; }
+double* sel_b(DevLevel& L) { return L.b; }
+double* sel_r(DevLevel& L) { return L.r; }
+double* sel_d0(DevLevel& L) { return L.pd0; }
+double* sel_d1(DevLevel& L) { return L.pd1; }
+
+bool shared_stream(smg_ctx* m) {
+    for (smg_ctx* p : m->parts)
+        if (p->st != m->st) return false;
+    return true;
+}
+
+// stream-order barrier across parts (no-op when all parts share one stream)
+void part_barrier(smg_ctx* m) {
+    if (shared_stream(m)) return;
+    std::vector<cudaEvent_t> ev(m->parts.size());
+    for (size_t k = 0; k < m->parts.size(); ++k) {
+        CK(cudaSetDevice(m->parts[k]->device));
+        CK(cudaEventCreateWithFlags(&ev[k], cudaEventDisableTiming));
+        CK(cudaEventRecord(ev[k], m->parts[k]->st));
+    }
+    for (size_t k = 0; k < m->parts.size(); ++k) {
+        CK(cudaSetDevice(m->parts[k]->device));
+        for (size_t j = 0; j < ev.size(); ++j)
+            if (j != k) CK(cudaStreamWaitEvent(m->parts[k]->st, ev[j], 0));
+    }
+    for (auto e : ev) cudaEventDestroy(e);
+    CK(cudaSetDevice(m->device));
+}
+
+// halo exchange of a slab level: 2 planes each way between neighbours; nf fields
+void exchange(smg_ctx* m, int l, Sel sel, int nf) {
+    part_barrier(m);
+    for (size_t p = 0; p + 1 < m->parts.size(); ++p) {
+        DevLevel &lo = m->parts[p]->lv[l], &hi = m->parts[p + 1]->lv[l];
+        const Geom& g = lo.k.g;
+        const size_t pitch = g.fs * sizeof(double), width = 2 * g.sz * sizeof(double);
+        // lo top halo (planes nz, nz+1) <- hi owned planes 0, 1
+        CK(cudaMemcpy2DAsync(sel(lo) + (g.nz + g.zg) * g.sz, pitch, sel(hi) + g.zg * g.sz, pitch, width, nf,
+                             cudaMemcpyDefault, m->parts[p]->st));
+        // hi bottom halo (planes -2, -1) <- lo owned planes nz-2, nz-1
+        CK(cudaMemcpy2DAsync(sel(hi), pitch, sel(lo) + g.nz * g.sz, pitch, width, nf, cudaMemcpyDefault,
+                             m->parts[p + 1]->st));
+    }
+    part_barrier(m);
+}
+
+// every part's owned coarse planes [z0c, z0c + nzc) of a replicated level -> all parts
+void allgather_planes(smg_ctx* m, int l, Sel sel, int nzc) {
+    part_barrier(m);
+    const Geom& g = m->lv[l].k.g;
+    const size_t pitch = g.fs * sizeof(double), width = nzc * g.sz * sizeof(double);
+    for (size_t p = 0; p < m->parts.size(); ++p)
+        for (size_t q = 0; q < m->parts.size(); ++q) {
+            if (p == q) continue;
+            const int64_t off = (static_cast<int64_t>(p) * nzc + g.zg) * g.sz;
+            CK(cudaMemcpy2DAsync(sel(m->parts[q]->lv[l]) + off, pitch, sel(m->parts[p]->lv[l]) + off, pitch, width, 4,
+                                 cudaMemcpyDefault, m->parts[q]->st));
+        }
+    part_barrier(m);
+}
+
+template <class F>
+void each(smg_ctx* m, F&& f) {
+    for (smg_ctx* p : m->parts) {
+        CK(cudaSetDevice(p->device));
+        f(p);
+    }
+    CK(cudaSetDevice(m->device));
+}
+
+void dist_vanka_sym(smg_ctx* m, int l) {
+    for (int sweep = 0; sweep < m->prm.nu; ++sweep)
+        for (int k = 0; k < 16; ++k) {
+            const int col = k < 8 ? k : 15 - k;
+            each(m, [&](smg_ctx* p) {
+                DevLevel& L = p->lv[l];
+                launch_vanka_delta(L.k, L.x, L.b, L.vk_cells[col], L.vk_mask[col], L.vk_n[col], L.ktab, p->vk_delta, p->st);
+                launch_vanka_apply(L.k, L.x, L.vk_cells[col], L.vk_mask[col], L.vk_n[col], p->vk_delta, p->st);
+            });
+            exchange(m, l, sel_x, 4);
+        }
+}
+
+void dist_dgs_sym(smg_ctx* m, int l) {
+    const int nph = (m->prm.flags & SMG_FLAG_SKIP_REVERSE_DGS) ? 10 : 20;
+    for (int ph = 0; ph < nph; ++ph) {
+        if (ph == 0 || ph == 1 || ph == 18 || ph == 19) {
+            const int col = ph < 2 ? ph : 19 - ph;
+            each(m, [&](smg_ctx* p) { launch_dgs_vel_c(p->lv[l].k, p->lv[l].x, p->lv[l].b, col, p->st); });
+        } else if (ph <= 9) {
+            const int c = ph - 2;
+            Sel sd = (c & 1) ? sel_d1 : sel_d0;
+            each(m, [&](smg_ctx* p) {
+                DevLevel& L = p->lv[l];
+                launch_dgs_pf_delta_c(L.k, L.x, L.b, sd(L), c, p->st);
+            });
+            exchange(m, l, sd, 1);
+            each(m, [&](smg_ctx* p) { launch_dgs_pf_apply_c(p->lv[l].k, p->lv[l].x, sd(p->lv[l]), c, p->st); });
+        } else {
+            each(m, [&](smg_ctx* p) { launch_dgs_prev_c(p->lv[l].k, p->lv[l].x, p->lv[l].b, 17 - ph, p->st); });
+        }
+        exchange(m, l, sel_x, 4);
+    }
+}
+
+void dist_smooth(smg_ctx* m, int l) {
+    dist_vanka_sym(m, l);
+    dist_dgs_sym(m, l);
+    dist_vanka_sym(m, l);
+}
+
+// V-cycle on the parts; level-l b must hold valid halos
+void dist_vcycle(smg_ctx* m, int l) {
+    if (l >= m->ndist) {  // replicated: every part runs the identical single-part cycle
+        each(m, [&](smg_ctx* p) { vcycle(p, l, p->lv[l].b, p->lv[l].x); });
+        return;
+    }
+    each(m, [&](smg_ctx* p) { CK(cudaMemsetAsync(p->lv[l].x, 0, vlen(p->lv[l]) * sizeof(double), p->st)); });
+    dist_smooth(m, l);
+    each(m, [&](smg_ctx* p) {
+        DevLevel& L = p->lv[l];
+        launch_apply(L.k, L.x, L.b, L.r, L.k.gamma, p->st);
+    });
+    exchange(m, l, sel_r, 4);
+    const bool cdist = l + 1 < m->ndist;
+    each(m, [&](smg_ctx* p) {
+        DevLevel &L = p->lv[l], &C = p->lv[l + 1];
+        if (cdist) launch_restrict(L.k, C.k, L.r, C.b, p->st);
+        else launch_restrict(L.k, C.k, L.r, C.b, p->st, L.k.g.z0 / 2, L.k.g.nz / 2);
+    });
+    if (cdist) exchange(m, l + 1, sel_b, 4);
+    else allgather_planes(m, l + 1, sel_b, m->lv[l].k.g.nz / 2);
+    dist_vcycle(m, l + 1);
+    if (cdist) exchange(m, l + 1, sel_x, 4);
+    each(m, [&](smg_ctx* p) { launch_prolong_add(p->lv[l].k, p->lv[l + 1].k, p->lv[l + 1].x, p->lv[l].x, p->st); });
+    exchange(m, l, sel_x, 4);
+    dist_smooth(m, l);
+}
+
+// canonical dot across parts: plane partials of every part into the shared buffer
+// (global plane indices), barrier, then the fixed-order final on every part.
+void dist_dot2(smg_ctx* m, double* (*a)(smg_ctx*), double* (*b)(smg_ctx*), double* (*c2)(smg_ctx*),
+               double* (*d)(smg_ctx*)) {
+    each(m, [&](smg_ctx* p) {
+        launch_cdot_planes(p->lv[0].k.g, a(p), b(p), c2 ? c2(p) : nullptr, d ? d(p) : nullptr, m->shared_partials, p->st);
+    });
+    part_barrier(m);
+    each(m, [&](smg_ctx* p) { launch_cdot_final(p->lv[0].k.g, m->shared_partials, p->dscal + S_D0, p->st); });
+}
+
+double* v_q(smg_ctx* p) { return p->q; }
+double* v_d(smg_ctx* p) { return p->d; }
+double* v_xs(smg_ctx* p) { return p->xs; }
+double* v_rhs(smg_ctx* p) { return p->rhs; }
+double* v_s(smg_ctx* p) { return p->lv[0].b; }
+double* v_t(smg_ctx* p) { return p->lv[0].x; }
+double* v_r(smg_ctx* p) { return p->lv[0].r; }
+
+// exchange of a fine-level SQMR vector (not a DevLevel member)
+void exchange_vec(smg_ctx* m, double* (*v)(smg_ctx*)) {
+    part_barrier(m);
+    for (size_t p = 0; p + 1 < m->parts.size(); ++p) {
+        smg_ctx *lo = m->parts[p], *hi = m->parts[p + 1];
+        const Geom& g = lo->lv[0].k.g;
+        const size_t pitch = g.fs * sizeof(double), width = 2 * g.sz * sizeof(double);
+        CK(cudaMemcpy2DAsync(v(lo) + (g.nz + g.zg) * g.sz, pitch, v(hi) + g.zg * g.sz, pitch, width, 4,
+                             cudaMemcpyDefault, lo->st));
+        CK(cudaMemcpy2DAsync(v(hi), pitch, v(lo) + g.nz * g.sz, pitch, width, 4, cudaMemcpyDefault, hi->st));
+    }
+    part_barrier(m);
+}
+
+void dist_upload(smg_ctx* m, const double* host, double* (*v)(smg_ctx*)) {
+    const int64_t n = m->lv[0].N;
+    each(m, [&](smg_ctx* p) {
+        CK(cudaMemcpyAsync(p->compact, host, n * sizeof(double), cudaMemcpyHostToDevice, p->st));
+        launch_unpack(p->lv[0].k, p->compact, v(p), p->st);
+    });
+    exchange_vec(m, v);
+}
+
+void dist_download(smg_ctx* m, double* (*v)(smg_ctx*), double* host) {
+    const DevLevel& L0 = m->lv[0];
+    const int nx = m->grid.nx, ny = m->grid.ny, gnz = m->grid.nz;
+    const int64_t nu = L0.counts[0], nv = L0.counts[1], nw = L0.counts[2];
+    each(m, [&](smg_ctx* p) {
+        launch_pack(p->lv[0].k, v(p), p->compact, p->st);
+        const int z0 = p->lv[0].k.g.z0, z1 = z0 + p->lv[0].k.g.nz;
+        const int64_t r[4][2] = {
+            {static_cast<int64_t>(z0) * ny * (nx - 1), static_cast<int64_t>(z1) * ny * (nx - 1)},
+            {nu + static_cast<int64_t>(z0) * (ny - 1) * nx, nu + static_cast<int64_t>(z1) * (ny - 1) * nx},
+            {nu + nv + static_cast<int64_t>(std::max(z0, 1) - 1) * ny * nx,
+             nu + nv + static_cast<int64_t>(std::min(z1, gnz) - 1) * ny * nx},
+            {nu + nv + nw + static_cast<int64_t>(z0) * ny * nx, nu + nv + nw + static_cast<int64_t>(z1) * ny * nx}};
+        for (auto& rg : r)
+            if (rg[1] > rg[0])
+                CK(cudaMemcpyAsync(host + rg[0], p->compact + rg[0], (rg[1] - rg[0]) * sizeof(double),
+                                   cudaMemcpyDeviceToHost, p->st));
+    });
+    each(m, [&](smg_ctx* p) { CK(cudaStreamSynchronize(p->st)); });
+}
+
+int dist_sqmr(smg_ctx* m, double tol, int maxit, smg_history* hist, int* status) {
+    auto t0 = std::chrono::steady_clock::now();
+    const int64_t l0 = launch_count();
+    CK(cudaEventRecord(m->ev0, m->st));
+    if (hist) hist->count = 0;
+    each(m, [&](smg_ctx* p) {
+        const int64_t n = vlen(p->lv[0]);
+        CK(cudaMemsetAsync(p->xs, 0, n * sizeof(double), p->st));
+        CK(cudaMemsetAsync(p->d, 0, n * sizeof(double), p->st));
+        CK(cudaMemsetAsync(p->dscal, 0, S_COUNT * sizeof(double), p->st));
+    });
+    dist_dot2(m, v_rhs, v_rhs, nullptr, nullptr);
+    CK(cudaMemcpyAsync(m->hscal, m->dscal, sizeof(double), cudaMemcpyDeviceToHost, m->st));
+    each(m, [&](smg_ctx* p) { CK(cudaStreamSynchronize(p->st)); });
+    const double bnorm = std::sqrt(m->hscal[0]);
+    int st = SMG_MAX_ITERATIONS, iters = 0;
+    if (bnorm == 0.0) {
+        st = SMG_CONVERGED;
+    } else {
+        m->hscal[2] = bnorm;
+        m->hscal[3] = tol;
+        each(m, [&](smg_ctx* p) {
+            CK(cudaMemcpyAsync(p->dscal + S_BNORM, &m->hscal[2], sizeof(double), cudaMemcpyHostToDevice, p->st));
+            CK(cudaMemcpyAsync(p->dscal + S_TOL, &m->hscal[3], sizeof(double), cudaMemcpyHostToDevice, p->st));
+            CK(cudaMemcpyAsync(v_s(p), p->rhs, vlen(p->lv[0]) * sizeof(double), cudaMemcpyDeviceToDevice, p->st));
+        });
+        exchange_vec(m, v_s);
+        dist_vcycle(m, 0);
+        each(m, [&](smg_ctx* p) {
+            CK(cudaMemcpyAsync(p->q, v_t(p), vlen(p->lv[0]) * sizeof(double), cudaMemcpyDeviceToDevice, p->st));
+        });
+        dist_dot2(m, v_t, v_t, v_s, v_q);
+        each(m, [&](smg_ctx* p) { launch_sqmr_scalar(0, p->dscal, p->st); });
+        CK(cudaMemcpyAsync(m->hscal, m->dscal + S_STATUS, sizeof(double), cudaMemcpyDeviceToHost, m->st));
+        CK(cudaStreamSynchronize(m->st));
+        if (m->hscal[0] != 0.0) st = SMG_BREAKDOWN;
+        for (int j = 1; j <= maxit && st == SMG_MAX_ITERATIONS; ++j) {
+            exchange_vec(m, v_q);
+            each(m, [&](smg_ctx* p) { launch_apply(p->lv[0].k, p->q, nullptr, v_t(p), 0.0, p->st); });
+            dist_dot2(m, v_q, v_t, nullptr, nullptr);
+            each(m, [&](smg_ctx* p) {
+                const int64_t n = vlen(p->lv[0]);
+                launch_sqmr_scalar(1, p->dscal, p->st);
+                launch_axpy_s(v_s(p), v_t(p), p->dscal, n, p->st);
+            });
+            exchange_vec(m, v_s);
+            dist_vcycle(m, 0);
+            dist_dot2(m, v_t, v_t, v_s, v_t);
+            each(m, [&](smg_ctx* p) {
+                launch_sqmr_scalar(2, p->dscal, p->st);
+                launch_dx_dev(p->d, p->xs, p->q, p->dscal, vlen(p->lv[0]), p->st);
+            });
+            exchange_vec(m, v_xs);
+            each(m, [&](smg_ctx* p) { launch_apply(p->lv[0].k, p->xs, p->rhs, v_r(p), 0.0, p->st); });
+            dist_dot2(m, v_r, v_r, nullptr, nullptr);
+            each(m, [&](smg_ctx* p) {
+                launch_sqmr_scalar(3, p->dscal, p->st);
+                launch_xpby_dev(p->q, v_t(p), p->dscal, vlen(p->lv[0]), p->st);
+            });
+            CK(cudaMemcpyAsync(m->hscal, m->dscal + S_REL, 2 * sizeof(double), cudaMemcpyDeviceToHost, m->st));
+            each(m, [&](smg_ctx* p) { CK(cudaStreamSynchronize(p->st)); });
+            const double rel = m->hscal[0];
+            const int code = static_cast<int>(m->hscal[1]);
+            if (code == 2) { st = SMG_BREAKDOWN; break; }
+            iters = j;
+            if (hist && hist->count < hist->capacity) {
+                hist->rel_residual[hist->count] = rel;
+                hist->seconds[hist->count] =
+                    std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+                hist->count++;
+            }
+            if (code == 1) st = SMG_CONVERGED;
+            else if (code == 3) st = SMG_BREAKDOWN;
+        }
+    }
+    CK(cudaEventRecord(m->ev1, m->st));
+    CK(cudaEventSynchronize(m->ev1));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, m->ev0, m->ev1));
+    m->timing.solve_ms = ms;
+    m->timing.iterations = iters;
+    m->timing.kernel_launches = launch_count() - l0;
+    *status = st;
+    return 0;
+}
+
 template <class F>
 int guard(smg_ctx* c, F&& f) {
     try {
@@ -631,18 +947,71 @@ extern "C" {
 
 const char* smg_version(void) { return "smg-b200 0.1 (sm_100a, fp64)"; }
 
+int smg_slab_plan(const smg_grid_desc* grid, int levels, int nparts, int rank, int* z0, int* nzl) {
+    if (!grid || levels < 1 || nparts < 1 || rank < 0 || rank >= nparts) return SMG_EINVAL;
+    int nd = 0;
+    if (nparts > 1)
+        for (int l = 0; l + 1 < levels; ++l) {
+            const int nz = grid->nz >> l;
+            if (nz % nparts || nz / nparts < 2) break;                    // slab of >= 2 planes (halo depth)
+            if (l > 0 && ((grid->nz >> (l - 1)) / nparts) % 2) break;    // slab boundaries aligned with level l-1
+            nd = l + 1;
+        }
+    for (int l = 0; l < levels; ++l) {
+        const int nz = grid->nz >> l;
+        const bool d = l < nd;
+        if (z0) z0[l] = d ? rank * (nz / nparts) : 0;
+        if (nzl) nzl[l] = d ? nz / nparts : nz;
+    }
+    return nd;
+}
+
 int smg_create(const smg_grid_desc* grid, const smg_params* params, int ngpu, const int* dev_ids, smg_ctx** out) {
     if (!grid || !params || !out) return SMG_EINVAL;
     *out = nullptr;
-    if (ngpu != 1) return SMG_EINVAL;  // multi-GPU z-slab decomposition: see DESIGN.md §7
+    if (ngpu < 1 || ngpu > 64) return SMG_EINVAL;
     auto c = std::make_unique<smg_ctx>();
     c->grid = *grid;
     c->prm = *params;
     c->device = dev_ids ? dev_ids[0] : 0;
-    static thread_local std::string create_err;
-    const int rc = guard(c.get(), [&] { build(c.get()); });
+    c->nparts = ngpu;
+    c->parts.push_back(c.get());
+    const int rc = guard(c.get(), [&] {
+        if (ngpu > 1) {
+            // levels split into z-slabs: slab >= 2 planes, aligned with the next level
+            const int nd = smg_slab_plan(grid, params->levels, ngpu, 0, nullptr, nullptr);
+            if (nd <= 0) throw SmgError(SMG_EINVAL, "grid too small for a z-slab split over ngpu parts");
+            c->ndist = nd;
+        }
+        std::vector<double> coarse;
+        build(c.get(), nullptr, &coarse);
+        for (int r = 1; r < ngpu; ++r) {
+            auto q = std::make_unique<smg_ctx>();
+            q->grid = *grid;
+            q->prm = *params;
+            q->device = dev_ids ? dev_ids[r] : c->device;
+            q->rank = r;
+            q->nparts = ngpu;
+            q->ndist = c->ndist;
+            build(q.get(), &coarse, nullptr, q->device == c->device ? c->st : nullptr);
+            if (q->device != c->device) {
+                int ok = 0;
+                CK(cudaDeviceCanAccessPeer(&ok, q->device, c->device));
+                if (ok) {
+                    CK(cudaSetDevice(q->device));
+                    cudaDeviceEnablePeerAccess(c->device, 0);
+                    CK(cudaSetDevice(c->device));
+                    cudaDeviceEnablePeerAccess(q->device, 0);
+                    cudaGetLastError();  // tolerate "already enabled"
+                }
+            }
+            c->parts.push_back(q.get());
+            c->owned.push_back(std::move(q));
+        }
+        CK(cudaSetDevice(c->device));
+        if (ngpu > 1) c->shared_partials = c->dalloc<double>(kPartials);
+    });
     if (rc != 0) {
-        create_err = c->err;
         std::fprintf(stderr, "smg_create: %s\n", c->err.c_str());
         return rc;
     }
@@ -667,6 +1036,15 @@ int64_t smg_level_ndof(const smg_ctx* ctx, int level, int64_t* out5) {
 int smg_apply(smg_ctx* c, int level, int penalized, const double* x, double* y) {
     return guard(c, [&] {
         check_level(c, level);
+        if (c->nparts > 1) {
+            if (level != 0) throw SmgError(SMG_EINVAL, "z-slab contexts: apply on level 0 only");
+            dist_upload(c, x, v_t);
+            each(c, [&](smg_ctx* p) {
+                launch_apply(p->lv[0].k, v_t(p), nullptr, v_r(p), penalized ? p->lv[0].k.gamma : 0.0, p->st);
+            });
+            dist_download(c, v_r, y);
+            return;
+        }
         DevLevel& L = c->lv[level];
         upload(c, level, x, L.x);
         launch_apply(L.k, L.x, nullptr, L.r, penalized ? L.k.gamma : 0.0, c->st);
@@ -676,6 +1054,7 @@ int smg_apply(smg_ctx* c, int level, int penalized, const double* x, double* y) 
 
 int smg_residual(smg_ctx* c, int level, const double* x, const double* b, double* r) {
     return guard(c, [&] {
+        if (c->nparts > 1) throw SmgError(SMG_EINVAL, "single-part entry point (use ngpu = 1)");
         check_level(c, level);
         DevLevel& L = c->lv[level];
         upload(c, level, x, L.x);
@@ -687,6 +1066,7 @@ int smg_residual(smg_ctx* c, int level, const double* x, const double* b, double
 
 int smg_smoother(smg_ctx* c, int level, int op, int arg, double* x, const double* b) {
     return guard(c, [&] {
+        if (c->nparts > 1) throw SmgError(SMG_EINVAL, "single-part entry point (use ngpu = 1)");
         check_level(c, level);
         DevLevel& L = c->lv[level];
         upload(c, level, x, L.x);
@@ -711,6 +1091,7 @@ int smg_smoother(smg_ctx* c, int level, int op, int arg, double* x, const double
 
 int smg_restrict(smg_ctx* c, int level, const double* rf, double* rc) {
     return guard(c, [&] {
+        if (c->nparts > 1) throw SmgError(SMG_EINVAL, "single-part entry point (use ngpu = 1)");
         check_level(c, level);
         check_level(c, level + 1);
         DevLevel &F = c->lv[level], &C = c->lv[level + 1];
@@ -722,6 +1103,7 @@ int smg_restrict(smg_ctx* c, int level, const double* rf, double* rc) {
 
 int smg_prolong(smg_ctx* c, int level, const double* xc, double* xf) {
     return guard(c, [&] {
+        if (c->nparts > 1) throw SmgError(SMG_EINVAL, "single-part entry point (use ngpu = 1)");
         check_level(c, level);
         check_level(c, level + 1);
         DevLevel &F = c->lv[level], &C = c->lv[level + 1];
@@ -734,6 +1116,7 @@ int smg_prolong(smg_ctx* c, int level, const double* xc, double* xf) {
 
 int smg_coarse_solve(smg_ctx* c, const double* b, double* x) {
     return guard(c, [&] {
+        if (c->nparts > 1) throw SmgError(SMG_EINVAL, "single-part entry point (use ngpu = 1)");
         const int l = static_cast<int>(c->lv.size()) - 1;
         DevLevel& C = c->lv[l];
         upload(c, l, b, C.b);
@@ -744,6 +1127,12 @@ int smg_coarse_solve(smg_ctx* c, const double* b, double* x) {
 
 int smg_vcycle(smg_ctx* c, const double* b, double* x) {
     return guard(c, [&] {
+        if (c->nparts > 1) {
+            dist_upload(c, b, v_s);
+            dist_vcycle(c, 0);
+            dist_download(c, v_t, x);
+            return;
+        }
         DevLevel& F = c->lv[0];
         upload(c, 0, b, F.b);
         vcycle(c, 0, F.b, F.x);
@@ -753,6 +1142,11 @@ int smg_vcycle(smg_ctx* c, const double* b, double* x) {
 
 int smg_set_rhs(smg_ctx* c, const double* b) {
     return guard(c, [&] {
+        if (c->nparts > 1) {
+            dist_upload(c, b, v_rhs);
+            c->rhs_set = true;
+            return;
+        }
         upload(c, 0, b, c->rhs);
         CK(cudaStreamSynchronize(c->st));
         c->rhs_set = true;
@@ -763,17 +1157,28 @@ int smg_solve_resident(smg_ctx* c, double tol, int maxit, smg_history* hist, int
     return guard(c, [&] {
         if (!c->rhs_set) throw SmgError(SMG_EINVAL, "smg_set_rhs not called");
         if (!status) throw SmgError(SMG_EINVAL, "status is null");
-        sqmr(c, tol, maxit, hist, status);
+        if (c->nparts > 1) dist_sqmr(c, tol, maxit, hist, status);
+        else sqmr(c, tol, maxit, hist, status);
     });
 }
 
 int smg_get_solution(smg_ctx* c, double* x) {
-    return guard(c, [&] { download(c, 0, c->xs, x); });
+    return guard(c, [&] {
+        if (c->nparts > 1) dist_download(c, v_xs, x);
+        else download(c, 0, c->xs, x);
+    });
 }
 
 int smg_sqmr_solve(smg_ctx* c, const double* b, double* x, double tol, int maxit, smg_history* hist, int* status) {
     return guard(c, [&] {
         if (!b || !x || !status) throw SmgError(SMG_EINVAL, "null argument");
+        if (c->nparts > 1) {
+            dist_upload(c, b, v_rhs);
+            c->rhs_set = true;
+            dist_sqmr(c, tol, maxit, hist, status);
+            dist_download(c, v_xs, x);
+            return;
+        }
         CK(cudaEventRecord(c->ev0, c->st));
         upload(c, 0, b, c->rhs);
         CK(cudaEventRecord(c->ev1, c->st));

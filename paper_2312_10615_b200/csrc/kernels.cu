@@ -42,9 +42,11 @@ __device__ __forceinline__ bool thread_cell(const Geom& g, Cell& c) {
     return true;
 }
 
+// band membership (V1) of the cell at LOCAL plane z, decided on global coordinates
 __device__ __forceinline__ bool band_cell(const LevelK& L, int x, int y, int z) {
     const Geom& g = L.g;
-    return x < L.bw || y < L.bw || z < L.bw || x >= g.nx - L.bw || y >= g.ny - L.bw || z >= g.nz - L.bw;
+    const int zz = g.gz(z);
+    return x < L.bw || y < L.bw || zz < L.bw || x >= g.nx - L.bw || y >= g.ny - L.bw || zz >= g.gnz - L.bw;
 }
 
 // Momentum row of L~ at the face stored at slot i of field F (stride of the
@@ -87,7 +89,7 @@ __global__ void k_apply(LevelK L, const double* __restrict__ X, const double* __
         const double y = mom(L, V, P, i, g.sy);
         Y[fs + i] = B ? B[fs + i] - y : y;
     }
-    if (c.z >= 1) {
+    if (g.gz(c.z) >= 1) {
         const double y = mom(L, W, P, i, g.sz);
         Y[2 * fs + i] = B ? B[2 * fs + i] - y : y;
     }
@@ -101,8 +103,8 @@ __global__ void k_apply(LevelK L, const double* __restrict__ X, const double* __
 __global__ void k_dgs_vel(LevelK L, double* __restrict__ X, const double* __restrict__ B, int colour) {
     Cell c;
     if (!thread_cell(L.g, c)) return;
-    if (((c.x + c.y + c.z) & 1) != colour) return;
     const Geom& g = L.g;
+    if (((c.x + c.y + g.gz(c.z)) & 1) != colour) return;
     const int64_t fs = g.fs, i = c.i;
     double *U = X, *V = X + fs, *W = X + 2 * fs;
     const double* P = X + 3 * fs;
@@ -115,13 +117,15 @@ __global__ void k_dgs_vel(LevelK L, double* __restrict__ X, const double* __rest
         const double r = B[fs + i] - mom(L, V, P, i, g.sy);
         V[i] = V[i] + r / L.dv;
     }
-    if (c.z >= 1 && !here && !band_cell(L, c.x, c.y, c.z - 1)) {
+    if (g.gz(c.z) >= 1 && !here && !band_cell(L, c.x, c.y, c.z - 1)) {
         const double r = B[2 * fs + i] - mom(L, W, P, i, g.sz);
         W[i] = W[i] + r / L.dv;
     }
 }
 
-__device__ __forceinline__ int pcolour(const Cell& c) { return (c.x & 1) + 2 * (c.y & 1) + 4 * (c.z & 1); }
+__device__ __forceinline__ int pcolour(const Geom& g, const Cell& c) {
+    return (c.x & 1) + 2 * (c.y & 1) + 4 * (g.gz(c.z) & 1);
+}
 
 // Forward pressure phase, part 1: delta_C = (b_C - (L~x)_C) / d_p on V2 cells of
 // the parity colour (8 colours, OD-1), 0 elsewhere (written for every cell).
@@ -131,7 +135,7 @@ __global__ void k_dgs_pdelta(LevelK L, const double* __restrict__ X, const doubl
     if (!thread_cell(L.g, c)) return;
     const int64_t fs = L.g.fs, i = c.i;
     double d = 0.0;
-    if (pcolour(c) == colour && !band_cell(L, c.x, c.y, c.z)) {
+    if (pcolour(L.g, c) == colour && !band_cell(L, c.x, c.y, c.z)) {
         const double r = B[3 * fs + i] - cont(L, X, X + fs, X + 2 * fs, X + 3 * fs, i, L.gamma);
         d = r / L.dp;
     }
@@ -148,7 +152,7 @@ __global__ void k_dgs_papply(LevelK L, double* __restrict__ X, const double* __r
     const double dc = D[i];
     if (c.x >= 1) X[i] = X[i] + (D[i - 1] - dc) * L.inv_h;
     if (c.y >= 1) X[fs + i] = X[fs + i] + (D[i - sy] - dc) * L.inv_h;
-    if (c.z >= 1) X[2 * fs + i] = X[2 * fs + i] + (D[i - sz] - dc) * L.inv_h;
+    if (g.gz(c.z) >= 1) X[2 * fs + i] = X[2 * fs + i] + (D[i - sz] - dc) * L.inv_h;
     double s = D[i - 1] + D[i + 1];
     s = s + D[i - sy];
     s = s + D[i + sy];
@@ -163,7 +167,7 @@ __global__ void k_dgs_papply(LevelK L, double* __restrict__ X, const double* __r
 __global__ void k_dgs_prev(LevelK L, double* __restrict__ X, const double* __restrict__ B, int colour) {
     Cell c;
     if (!thread_cell(L.g, c)) return;
-    if (pcolour(c) != colour || band_cell(L, c.x, c.y, c.z)) return;
+    if (pcolour(L.g, c) != colour || band_cell(L, c.x, c.y, c.z)) return;
     const Geom& g = L.g;
     const int64_t fs = g.fs, i = c.i, sy = g.sy, sz = g.sz;
     const double *U = X, *V = X + fs, *W = X + 2 * fs;
@@ -261,16 +265,21 @@ __device__ __forceinline__ double restrict_face(const double* __restrict__ R, in
     return 0.125 * acc_b;
 }
 
-__global__ void k_restrict(LevelK F, LevelK C, const double* __restrict__ R, double* __restrict__ BC) {
-    Cell c;
-    if (!thread_cell(C.g, c)) return;
+__global__ void k_restrict(LevelK F, LevelK C, const double* __restrict__ R, double* __restrict__ BC, int zc_lo) {
     const Geom &fg = F.g, &cg = C.g;
+    Cell c;
+    c.x = blockIdx.x * BX + threadIdx.x;
+    c.y = blockIdx.y * BY + threadIdx.y;
+    c.z = zc_lo + blockIdx.z;
+    if (c.x >= cg.nx || c.y >= cg.ny) return;
+    c.i = cg.slot(c.x, c.y, c.z);
     const int64_t ffs = fg.fs, cfs = cg.fs;
-    const int64_t fb = fg.slot(2 * c.x, 2 * c.y, 2 * c.z);
+    const int fz = 2 * cg.gz(c.z) - fg.z0;  // fine local plane of the coarse cell's lower child
+    const int64_t fb = fg.slot(2 * c.x, 2 * c.y, fz);
     const int64_t sx = 1, sy = fg.sy, sz = fg.sz;
     if (c.x >= 1) BC[c.i] = restrict_face(R, fb, sx, sy, sz);                   // u: a = y, b = z
     if (c.y >= 1) BC[cfs + c.i] = restrict_face(R + ffs, fb, sy, sx, sz);       // v: a = x, b = z
-    if (c.z >= 1) BC[2 * cfs + c.i] = restrict_face(R + 2 * ffs, fb, sz, sx, sy);  // w: a = x, b = y
+    if (cg.gz(c.z) >= 1) BC[2 * cfs + c.i] = restrict_face(R + 2 * ffs, fb, sz, sx, sy);  // w: a = x, b = y
     const double* RP = R + 3 * ffs;
     double s = 0.0;
 #pragma unroll
@@ -286,6 +295,8 @@ __global__ void k_restrict(LevelK F, LevelK C, const double* __restrict__ R, dou
 // (J>>1, 3/4) then (J odd ? (J>>1)+1 : (J>>1)-1, 1/4); normal: I even ->
 // (I/2, 1), I odd -> ((I-1)/2, 1/2), ((I+1)/2, 1/2).  Legs to wall/ghost slots
 // read 0 (dropped, no renormalisation).
+// (fx, fy, fz) are GLOBAL fine indices; coarse slots are addressed through
+// cg.slot with local coarse planes (cg.z0 subtracted).
 __device__ __forceinline__ double prolong_face(const double* __restrict__ E, const Geom& cg, int comp, int fx,
                                                int fy, int fz) {
     int f[3] = {fx, fy, fz};
@@ -319,7 +330,7 @@ __device__ __forceinline__ double prolong_face(const double* __restrict__ E, con
                 cc[comp] = ni[in];
                 cc[ta] = ia_[ia];
                 cc[tb] = ib_[ib];
-                acc_n = acc_n + nw[in] * E[cg.slot(cc[0], cc[1], cc[2])];
+                acc_n = acc_n + nw[in] * E[cg.slot(cc[0], cc[1], cc[2] - cg.z0)];
             }
             acc_a = acc_a + wt[ia] * acc_n;
         }
@@ -333,10 +344,11 @@ __global__ void k_prolong_add(LevelK F, LevelK C, const double* __restrict__ E, 
     if (!thread_cell(F.g, c)) return;
     const Geom &fg = F.g, &cg = C.g;
     const int64_t ffs = fg.fs, cfs = cg.fs;
-    if (c.x >= 1) X[c.i] = X[c.i] + prolong_face(E, cg, 0, c.x, c.y, c.z);
-    if (c.y >= 1) X[ffs + c.i] = X[ffs + c.i] + prolong_face(E + cfs, cg, 1, c.x, c.y, c.z);
-    if (c.z >= 1) X[2 * ffs + c.i] = X[2 * ffs + c.i] + prolong_face(E + 2 * cfs, cg, 2, c.x, c.y, c.z);
-    X[3 * ffs + c.i] = X[3 * ffs + c.i] + E[3 * cfs + cg.slot(c.x >> 1, c.y >> 1, c.z >> 1)];
+    const int z = fg.gz(c.z);
+    if (c.x >= 1) X[c.i] = X[c.i] + prolong_face(E, cg, 0, c.x, c.y, z);
+    if (c.y >= 1) X[ffs + c.i] = X[ffs + c.i] + prolong_face(E + cfs, cg, 1, c.x, c.y, z);
+    if (z >= 1) X[2 * ffs + c.i] = X[2 * ffs + c.i] + prolong_face(E + 2 * cfs, cg, 2, c.x, c.y, z);
+    X[3 * ffs + c.i] = X[3 * ffs + c.i] + E[3 * cfs + cg.slot(c.x >> 1, c.y >> 1, (z >> 1) - cg.z0)];
 }
 
 // ------------------------------------------------------------- coarse ------
@@ -372,9 +384,9 @@ __global__ void k_pack(LevelK L, const double* __restrict__ X, double* __restric
     Cell c;
     if (!thread_cell(L.g, c)) return;
     const Geom& g = L.g;
-    const int64_t nx = g.nx, ny = g.ny, nz = g.nz, fs = g.fs;
+    const int64_t nx = g.nx, ny = g.ny, nz = g.gnz, fs = g.fs;
     const int64_t nu = (nx - 1) * ny * nz, nv = nx * (ny - 1) * nz, nw = nx * ny * (nz - 1);
-    const int64_t x = c.x, y = c.y, z = c.z;
+    const int64_t x = c.x, y = c.y, z = g.gz(c.z);
     if (x >= 1) {
         const int64_t k = (z * ny + y) * (nx - 1) + (x - 1);
         if (unpack) const_cast<double*>(X)[c.i] = out[k]; else out[k] = X[c.i];
@@ -405,9 +417,11 @@ __global__ void __launch_bounds__(RED_T) k_cdot(Geom g, const double* __restrict
                                                 double* __restrict__ partials) {
     __shared__ double rows0[1040], rows1[1040];
     const int z = blockIdx.x, f = blockIdx.y;
-    const int ex = g.nx + (f == 0), ey = g.ny + (f == 1), ez = g.nz + (f == 2);
+    // local planes; the slab holding the global top plane also owns the top w wall plane
+    const int ex = g.nx + (f == 0), ey = g.ny + (f == 1);
+    const int ez = g.nz + ((f == 2 && g.z0 + g.nz == g.gnz) ? 1 : 0);
     if (z >= ez) return;
-    const int q = f * g.nz + (f == 3 ? 1 : 0) + z;  // plane index: u nz, v nz, w nz+1, p nz
+    const int q = f * g.gnz + (f == 3 ? 1 : 0) + g.gz(z);  // global plane index: u gnz, v gnz, w gnz+1, p gnz
     const int64_t off = f * g.fs;
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
     for (int y = w; y < ey; y += RED_T / 32) {
@@ -650,7 +664,7 @@ __device__ __forceinline__ void dgs_vel_cell(const LevelK& L, double* __restrict
         const double r = B[fs + i] - mom(L, V, P, i, g.sy);
         V[i] = V[i] + r / L.dv;
     }
-    if (z >= 1 && !here && !band_cell(L, x, y, z - 1)) {
+    if (g.gz(z) >= 1 && !here && !band_cell(L, x, y, z - 1)) {
         const double r = B[2 * fs + i] - mom(L, W, P, i, g.sz);
         W[i] = W[i] + r / L.dv;
     }
@@ -683,7 +697,7 @@ __device__ __forceinline__ void dgs_prev_cell(const LevelK& L, double* __restric
 
 // cells of parity colour c: t -> (x,y,z) on the half-grid of that parity
 __device__ __forceinline__ bool colour_cell(const Geom& g, int c, int64_t t, int& x, int& y, int& z) {
-    const int px = c & 1, py = (c >> 1) & 1, pz = (c >> 2) & 1;
+    const int px = c & 1, py = (c >> 1) & 1, pz = ((c >> 2) ^ g.z0) & 1;  // local z parity
     const int hx = (g.nx - px + 1) >> 1, hy = (g.ny - py + 1) >> 1, hz = (g.nz - pz + 1) >> 1;
     if (t >= static_cast<int64_t>(hx) * hy * hz) return false;
     const int64_t r = t / hx;
@@ -712,7 +726,7 @@ __device__ __forceinline__ void dgs_sweep(const LevelK& L, double* __restrict__ 
                 const int z = static_cast<int>(t / nxy);
                 const int64_t r = t - z * nxy;
                 const int y = static_cast<int>(r / g.nx), x = static_cast<int>(r - static_cast<int64_t>(y) * g.nx);
-                if (((x + y + z) & 1) == colour) dgs_vel_cell(L, X, B, x, y, z);
+                if (((x + y + g.gz(z)) & 1) == colour) dgs_vel_cell(L, X, B, x, y, z);
             }
         } else if (ph <= 9) {
             const int c = ph - 2;
@@ -804,7 +818,7 @@ __global__ void __launch_bounds__(256) k_dgs_vel_c(LevelK L, double* __restrict_
                                                    int colour) {
     const Geom& g = L.g;
     const int i = blockIdx.x * 32 + threadIdx.x, y = blockIdx.y * 8 + threadIdx.y, z = blockIdx.z;
-    const int x = 2 * i + ((y + z + colour) & 1);
+    const int x = 2 * i + ((y + g.gz(z) + colour) & 1);
     if (x >= g.nx || y >= g.ny) return;
     dgs_vel_cell(L, X, B, x, y, z);
 }
@@ -812,7 +826,7 @@ __global__ void __launch_bounds__(256) k_dgs_vel_c(LevelK L, double* __restrict_
 __device__ __forceinline__ bool half_cell(const Geom& g, int c, int i, int j, int k, int& x, int& y, int& z) {
     x = 2 * i + (c & 1);
     y = 2 * j + ((c >> 1) & 1);
-    z = 2 * k + ((c >> 2) & 1);
+    z = 2 * k + (((c >> 2) ^ g.z0) & 1);  // local plane with global parity (c >> 2)
     return x < g.nx && y < g.ny && z < g.nz;
 }
 
@@ -976,8 +990,12 @@ void launch_vanka_apply(const LevelK& L, double* x, const int32_t* cells, const 
     k_vanka_apply<<<(ncells + 127) / 128, 128, 0, s>>>(L, x, cells, masks, ncells, delta);
     count();
 }
-void launch_restrict(const LevelK& F, const LevelK& C, const double* rf, double* bc, cudaStream_t s) {
-    k_restrict<<<cell_grid(C.g), dim3(BX, BY), 0, s>>>(F, C, rf, bc);
+void launch_restrict(const LevelK& F, const LevelK& C, const double* rf, double* bc, cudaStream_t s, int zc_lo,
+                     int nzc) {
+    dim3 grid = cell_grid(C.g);
+    grid.z = nzc < 0 ? C.g.nz : nzc;
+    if (grid.z == 0) return;
+    k_restrict<<<grid, dim3(BX, BY), 0, s>>>(F, C, rf, bc, zc_lo);
     count();
 }
 void launch_prolong_add(const LevelK& F, const LevelK& C, const double* xc, double* xf, cudaStream_t s) {
@@ -1004,10 +1022,19 @@ void launch_unpack(const LevelK& L, const double* compact, double* padded, cudaS
     k_pack<<<cell_grid(L.g), dim3(BX, BY), 0, s>>>(L, padded, const_cast<double*>(compact), 1);
     count();
 }
+void launch_cdot_planes(const Geom& g, const double* a, const double* b, const double* c, const double* d,
+                        double* partials, cudaStream_t s) {
+    k_cdot<<<dim3(g.nz + 1, 4), RED_T, 0, s>>>(g, a, b, c, d, partials);
+    count();
+}
+void launch_cdot_final(const Geom& g, const double* partials, double* out, cudaStream_t s) {
+    k_cdot_final<<<1, 64, 0, s>>>(partials, 4 * g.gnz + 1, out);
+    count();
+}
 void launch_cdot2(const Geom& g, const double* a, const double* b, const double* c, const double* d,
                   double* partials, double* out, cudaStream_t s) {
     k_cdot<<<dim3(g.nz + 1, 4), RED_T, 0, s>>>(g, a, b, c, d, partials);
-    k_cdot_final<<<1, 64, 0, s>>>(partials, 4 * g.nz + 1, out);
+    k_cdot_final<<<1, 64, 0, s>>>(partials, 4 * g.gnz + 1, out);
     count();
     count();
 }
@@ -1128,6 +1155,28 @@ void launch_smooth_smem(const LevelK& L, double* x, const double* b, const int32
     const size_t smem = (64 * 49 + 4 * L.g.fs) * sizeof(double);
     cudaFuncSetAttribute(k_smooth_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     k_smooth_smem<<<1, 512, smem, s>>>(L, x, b, vl, ktab, d0, d1, nu, nph);
+    count();
+}
+
+// Single phases of the colour-compact DGS (the z-slab path exchanges halos between them).
+static dim3 dgs_grid_v(const Geom& g) { return dim3((((g.nx + 1) / 2) + 31) / 32, (g.ny + 7) / 8, g.nz); }
+static dim3 dgs_grid_h(const Geom& g) {
+    return dim3((((g.nx + 1) / 2) + 31) / 32, (((g.ny + 1) / 2) + 7) / 8, (g.nz + 1) / 2);
+}
+void launch_dgs_vel_c(const LevelK& L, double* x, const double* b, int colour, cudaStream_t s) {
+    k_dgs_vel_c<<<dgs_grid_v(L.g), dim3(32, 8), 0, s>>>(L, x, b, colour);
+    count();
+}
+void launch_dgs_pf_delta_c(const LevelK& L, const double* x, const double* b, double* d, int c, cudaStream_t s) {
+    k_dgs_pf_delta_c<<<dgs_grid_h(L.g), dim3(32, 8), 0, s>>>(L, x, b, d, c);
+    count();
+}
+void launch_dgs_pf_apply_c(const LevelK& L, double* x, const double* d, int c, cudaStream_t s) {
+    k_dgs_pf_apply_c<<<dgs_grid_h(L.g), dim3(32, 8), 0, s>>>(L, x, d, c);
+    count();
+}
+void launch_dgs_prev_c(const LevelK& L, double* x, const double* b, int c, cudaStream_t s) {
+    k_dgs_prev_c<<<dgs_grid_h(L.g), dim3(32, 8), 0, s>>>(L, x, b, c);
     count();
 }
 

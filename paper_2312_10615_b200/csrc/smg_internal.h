@@ -17,14 +17,17 @@
 namespace smg {
 
 struct Geom {
-    int nx, ny, nz;      // interior cells
+    int nx, ny, nz;      // interior cells held (nz = local planes of a z-slab)
     int px, py, pz;      // padded extents (doubles)
     int64_t sy, sz;      // strides of y and z
     int64_t fs;          // stride between fields of one vector (multiple of 32)
     int xo;              // row offset of slot x = 0 (4: 32-byte aligned rows; 1: compact small levels)
+    int zg;              // ghost planes on each z side (1 whole level; 2 for z-slabs: radius-2 halos)
+    int z0, gnz;         // global z of local plane 0, global number of planes
     __host__ __device__ __forceinline__ int64_t slot(int x, int y, int z) const {
-        return static_cast<int64_t>(z + 1) * sz + static_cast<int64_t>(y + 1) * sy + (x + xo);
+        return static_cast<int64_t>(z + zg) * sz + static_cast<int64_t>(y + 1) * sy + (x + xo);
     }
+    __host__ __device__ __forceinline__ int gz(int z) const { return z + z0; }  // local -> global plane
     int64_t vec_len() const { return 4 * fs; }
 };
 
@@ -32,16 +35,20 @@ struct Geom {
 // layout (x-offset 1, unaligned pitch) so a CTA can smooth them in smem.
 constexpr int64_t kSmemLevelCells = 6144;
 
-inline Geom make_geom(int nx, int ny, int nz) {
+// Whole level (z0 = 0, nz = gnz) or a z-slab [z0, z0 + nzl) of a gnz-plane level.
+inline Geom make_geom(int nx, int ny, int nz, int z0 = 0, int gnz = -1, int zg = 1) {
     Geom g;
     g.nx = nx;
     g.ny = ny;
     g.nz = nz;
-    const bool compact = static_cast<int64_t>(nx + 2) * (ny + 2) * (nz + 2) <= kSmemLevelCells;
+    g.z0 = z0;
+    g.gnz = gnz < 0 ? nz : gnz;
+    g.zg = zg;
+    const bool compact = zg == 1 && gnz < 0 && static_cast<int64_t>(nx + 2) * (ny + 2) * (nz + 2) <= kSmemLevelCells;
     g.xo = compact ? 1 : 4;
     g.px = compact ? nx + 2 : ((nx + 5) + 7) / 8 * 8;
     g.py = ny + 2;
-    g.pz = nz + 2;
+    g.pz = nz + 2 * zg;
     g.sy = g.px;
     g.sz = static_cast<int64_t>(g.px) * g.py;
     const int64_t cells = g.sz * g.pz;
@@ -84,7 +91,10 @@ bool smooth_smem_fits(const LevelK& L);
 void launch_smooth_smem(const LevelK& L, double* x, const double* b, const int32_t* const* cells,
                         const uint8_t* const* masks, const int* n, const double* ktab, double* d0, double* d1, int nu,
                         int nph, cudaStream_t s);
-void launch_restrict(const LevelK& F, const LevelK& C, const double* rf, double* bc, cudaStream_t s);
+// Restriction of coarse LOCAL planes [zc_lo, zc_lo + nzc) (nzc < 0: all); the
+// fine slab must hold the fine planes 2zc-1 .. 2zc+2 (halos included).
+void launch_restrict(const LevelK& F, const LevelK& C, const double* rf, double* bc, cudaStream_t s, int zc_lo = 0,
+                     int nzc = -1);
 void launch_prolong_add(const LevelK& F, const LevelK& C, const double* xc, double* xf, cudaStream_t s);
 void launch_coarse_gemv(const double* ksym, const int32_t* slots, int n, const double* b, double* x,
                         cudaStream_t s);
@@ -97,6 +107,18 @@ constexpr int kPartials = 2 * (4 * 1025 + 4);  // scratch doubles for launch_cdo
 // c.d over the level geometry g -> out[0], out[1] on the device.  nz <= 1024.
 void launch_cdot2(const Geom& g, const double* a, const double* b, const double* c, const double* d,
                   double* partials, double* out, cudaStream_t s);
+// The two halves of launch_cdot2: per-plane partials of this slab's planes (at
+// global plane indices, kMaxPlanes apart for the second product), and the
+// final fixed-order combination of all 4 gnz + 1 planes.
+constexpr int kMaxPlanesStride = 4 * 1025 + 4;
+void launch_cdot_planes(const Geom& g, const double* a, const double* b, const double* c, const double* d,
+                        double* partials, cudaStream_t s);
+void launch_cdot_final(const Geom& g, const double* partials, double* out, cudaStream_t s);
+// Single colour-compact DGS phases (used by the z-slab path).
+void launch_dgs_vel_c(const LevelK& L, double* x, const double* b, int colour, cudaStream_t s);
+void launch_dgs_pf_delta_c(const LevelK& L, const double* x, const double* b, double* d, int c, cudaStream_t s);
+void launch_dgs_pf_apply_c(const LevelK& L, double* x, const double* d, int c, cudaStream_t s);
+void launch_dgs_prev_c(const LevelK& L, double* x, const double* b, int c, cudaStream_t s);
 void launch_axpy(double* y, const double* x, double alpha, int64_t n, cudaStream_t s);          // y += alpha x
 void launch_xpby(double* y, const double* x, double beta, int64_t n, cudaStream_t s);           // y = x + beta y
 void launch_dx_update(double* d, double* x, const double* q, double cd, double cq, int64_t n,

@@ -1,0 +1,88 @@
+"""Host-side logic of the N > 1 path on CPU (no GPU): the library's z-slab plan
+(smg_slab_plan) and the bench's multi-rank plumbing, exercised by world_size-2
+gloo process groups on 127.0.0.1."""
+import os
+import socket
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import paper_2312_10615_b200 as smg
+
+
+@pytest.mark.parametrize("nz,levels,parts", [(128, 5, 2), (128, 5, 8), (512, 7, 8), (256, 6, 4), (32, 3, 4),
+                                             (256, 7, 8)])
+def test_slab_plan_covers_and_aligns(nz, levels, parts):
+    plans = [smg.slab_plan(nz, nz, nz, levels, parts, r) for r in range(parts)]
+    nd = plans[0][0]
+    assert nd >= 1 and all(p[0] == nd for p in plans)
+    for l in range(levels):
+        nzl = nz >> l
+        slabs = sorted(p[1][l] for p in plans)
+        if l < nd:
+            assert [s[0] for s in slabs] == [r * nzl // parts for r in range(parts)]
+            assert all(s[1] == nzl // parts >= 2 for s in slabs)
+            if l + 1 < nd:  # coarse slab = half of the fine slab (restriction stays local)
+                for p in plans:
+                    assert p[1][l + 1][0] * 2 == p[1][l][0]
+        else:
+            assert all(s == (0, nzl) for s in slabs)
+    assert nd <= levels - 1  # coarsest level is always replicated (dense solve)
+
+
+def test_slab_plan_rejects_unsplittable():
+    assert smg.slab_plan(8, 8, 8, 2, 8, 0)[0] <= 0  # 1 plane per part < halo depth
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
+                      LOCAL_RANK=str(rank))
+    import bench
+
+    ws, r, local = bench.dist_setup()
+    assert (ws, r) == (world, rank)
+    nd, plan = smg.slab_plan(256, 256, 256, 6, world, rank)
+    t = torch.tensor([nd] + [v for zl in plan for v in zl], dtype=torch.int64)
+    out = [torch.zeros_like(t) for _ in range(world)]
+    dist.all_gather(out, t)
+    # every level's slabs tile [0, nz) exactly once across the ranks
+    ok = True
+    for l in range(6):
+        nzl = 256 >> l
+        if l < nd:
+            covered = sorted((int(o[1 + 2 * l]), int(o[2 + 2 * l])) for o in out)
+            pos = 0
+            for z0, n in covered:
+                ok &= z0 == pos
+                pos += n
+            ok &= pos == nzl
+    m = bench.allmax(float(rank + 1) * 1.5, ws)  # max over ranks of the device time
+    bench.barrier(ws)
+    dist.destroy_process_group()
+    q.put((rank, ok, m, nd))
+
+
+def test_gloo_world2_slab_plan_and_timing_plumbing():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=180) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(ok for _, ok, _, _ in res)
+    assert all(m == 3.0 for _, _, m, _ in res)
+    assert all(nd >= 1 for *_, nd in res)
