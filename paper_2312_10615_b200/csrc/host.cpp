@@ -216,6 +216,7 @@ struct smg_ctx {
     }
     ~smg_ctx() {
         if (st) cudaStreamSynchronize(st);
+        owned.clear();  // parts may share this context's stream: destroy them first
         for (void* p : allocs) cudaFree(p);
         if (hscal) cudaFreeHost(hscal);
         if (graph) cudaGraphExecDestroy(graph);
