@@ -166,6 +166,7 @@ struct DevLevel {
     double *pd0 = nullptr, *pd1 = nullptr;  // alternating delta buffers of the cooperative DGS sweep
     int32_t* vk_cells[8] = {};
     uint8_t* vk_mask[8] = {};
+    uint8_t* vk_amask[8] = {};  // z-slab levels: owned slots per block (nullptr: all)
     int vk_n[8] = {};
     double* ktab = nullptr;  // [64][49]
 };
@@ -287,7 +288,7 @@ void build(smg_ctx* c, const std::vector<double>* shared_coarse = nullptr, std::
             return x < bw || y < bw || z < bw || x >= nx - bw || y >= ny - bw || z >= nz - bw;
         };
         std::vector<int32_t> cells[8];
-        std::vector<uint8_t> masks[8];
+        std::vector<uint8_t> masks[8], amasks[8];
         bool used[64] = {};
         int64_t v1 = 0;
         for (int z = 0; z < nz; ++z)
@@ -300,7 +301,14 @@ void build(smg_ctx* c, const std::vector<double>* shared_coarse = nullptr, std::
                     if (z >= 1 && (bc || band(x, y, z - 1))) ++v1;
                     if (!bc) continue;
                     ++v1;
-                    if (z < z0 || z >= z0 + nzl) continue;  // Vanka blocks of the owned planes only
+                    // Vanka blocks of the owned planes, plus (z-slabs) the band blocks of the halo plane
+                    // below, recomputed here only to apply their top w face, which lives in plane z0
+                    const bool owned = z >= z0 && z < z0 + nzl;
+                    const bool halo_below = dist && c->rank > 0 && z == z0 - 1;
+                    if (!owned && !halo_below) continue;
+                    int am = 127;
+                    if (halo_below) am = 32;
+                    else if (dist && z == z0 + nzl - 1 && z + 1 < nz) am = 127 & ~32;
                     int m = 0;
                     if (x >= 1) m |= 1;
                     if (x + 1 <= nx - 1) m |= 2;
@@ -311,6 +319,7 @@ void build(smg_ctx* c, const std::vector<double>* shared_coarse = nullptr, std::
                     const int col = (x & 1) + 2 * (y & 1) + 4 * (z & 1);
                     cells[col].push_back(static_cast<int32_t>(L.k.g.slot(x, y, z - z0)));
                     masks[col].push_back(static_cast<uint8_t>(m));
+                    amasks[col].push_back(static_cast<uint8_t>(am));
                     used[m] = true;
                 }
         L.counts[4] = v1;
@@ -322,6 +331,11 @@ void build(smg_ctx* c, const std::vector<double>* shared_coarse = nullptr, std::
             CK(cudaMemcpyAsync(L.vk_cells[col], cells[col].data(), cells[col].size() * sizeof(int32_t),
                                cudaMemcpyHostToDevice, c->st));
             CK(cudaMemcpyAsync(L.vk_mask[col], masks[col].data(), masks[col].size(), cudaMemcpyHostToDevice, c->st));
+            if (dist) {
+                L.vk_amask[col] = c->dalloc<uint8_t>(L.vk_n[col]);
+                CK(cudaMemcpyAsync(L.vk_amask[col], amasks[col].data(), amasks[col].size(), cudaMemcpyHostToDevice,
+                                   c->st));
+            }
             CK(cudaStreamSynchronize(c->st));
         }
         // local inverses C_i L~ C_i^T per face mask, scattered to the 7-slot layout
@@ -712,7 +726,8 @@ void dist_vanka_sym(smg_ctx* m, int l) {
             each(m, [&](smg_ctx* p) {
                 DevLevel& L = p->lv[l];
                 launch_vanka_delta(L.k, L.x, L.b, L.vk_cells[col], L.vk_mask[col], L.vk_n[col], L.ktab, p->vk_delta, p->st);
-                launch_vanka_apply(L.k, L.x, L.vk_cells[col], L.vk_mask[col], L.vk_n[col], p->vk_delta, p->st);
+                launch_vanka_apply(L.k, L.x, L.vk_cells[col], L.vk_mask[col], L.vk_n[col], p->vk_delta, p->st,
+                                   L.vk_amask[col]);
             });
             exchange(m, l, sel_x, 4);
         }

@@ -222,12 +222,15 @@ __global__ void k_vanka_delta(LevelK L, const double* __restrict__ X, const doub
 }
 
 __global__ void k_vanka_apply(LevelK L, double* __restrict__ X, const int32_t* __restrict__ cells,
-                              const uint8_t* __restrict__ masks, int n, const double* __restrict__ delta) {
+                              const uint8_t* __restrict__ masks, int n, const double* __restrict__ delta,
+                              const uint8_t* __restrict__ amask) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= n) return;
     const Geom& g = L.g;
     const int64_t fs = g.fs, i = cells[t];
-    const int m = masks[t];
+    // amask (z-slabs): which of the 7 slots this part owns (bit 6 = pressure)
+    const int am = amask ? amask[t] : 127;
+    const int m = masks[t] & am;
     const double* d = delta + static_cast<int64_t>(t) * 8;
     if (m & 1) X[i] = X[i] + d[0];
     if (m & 2) X[i + 1] = X[i + 1] + d[1];
@@ -235,7 +238,7 @@ __global__ void k_vanka_apply(LevelK L, double* __restrict__ X, const int32_t* _
     if (m & 8) X[fs + i + g.sy] = X[fs + i + g.sy] + d[3];
     if (m & 16) X[2 * fs + i] = X[2 * fs + i] + d[4];
     if (m & 32) X[2 * fs + i + g.sz] = X[2 * fs + i + g.sz] + d[5];
-    X[3 * fs + i] = X[3 * fs + i] + d[6];
+    if (am & 64) X[3 * fs + i] = X[3 * fs + i] + d[6];
 }
 
 // ------------------------------------------------------------ transfer ------
@@ -869,12 +872,22 @@ __global__ void __launch_bounds__(256) k_dgs_pf_apply_c(LevelK L, double* __rest
         X[fs + ii] = X[fs + ii] + (0.0 - dc) * L.inv_h;
         X[fs + ii + sy] = X[fs + ii + sy] + (dc - 0.0) * L.inv_h;
         X[2 * fs + ii] = X[2 * fs + ii] + (0.0 - dc) * L.inv_h;
-        X[2 * fs + ii + sz] = X[2 * fs + ii + sz] + (dc - 0.0) * L.inv_h;
+        // the top w face of a slab's top plane belongs to the next part (applied there, below)
+        if (z + 1 < g.nz) X[2 * fs + ii + sz] = X[2 * fs + ii + sz] + (dc - 0.0) * L.inv_h;
         p_gather_update(L, X, D, ii);
     }
 #pragma unroll
     for (int bit = 1; bit < 8; bit <<= 1)
         if (half_cell(g, c ^ bit, i, j, k, x, y, z)) p_gather_update(L, X, D, g.slot(x, y, z));
+    // z-slab: colour-c cell in the halo plane below -> its top w face is this part's plane 0
+    if (k == 0 && g.z0 > 0 && ((g.z0 - 1) & 1) == ((c >> 2) & 1)) {
+        x = 2 * i + (c & 1);
+        y = 2 * j + ((c >> 1) & 1);
+        if (x < g.nx && y < g.ny && !band_cell(L, x, y, -1)) {
+            const int64_t ih = g.slot(x, y, -1);
+            X[2 * fs + ih + sz] = X[2 * fs + ih + sz] + (D[ih] - 0.0) * L.inv_h;
+        }
+    }
 }
 
 __global__ void __launch_bounds__(256) k_dgs_prev_c(LevelK L, double* __restrict__ X, const double* __restrict__ B,
@@ -985,9 +998,9 @@ void launch_vanka_delta(const LevelK& L, const double* x, const double* b, const
     count();
 }
 void launch_vanka_apply(const LevelK& L, double* x, const int32_t* cells, const uint8_t* masks, int ncells,
-                        const double* delta, cudaStream_t s) {
+                        const double* delta, cudaStream_t s, const uint8_t* amask) {
     if (ncells <= 0) return;
-    k_vanka_apply<<<(ncells + 127) / 128, 128, 0, s>>>(L, x, cells, masks, ncells, delta);
+    k_vanka_apply<<<(ncells + 127) / 128, 128, 0, s>>>(L, x, cells, masks, ncells, delta, amask);
     count();
 }
 void launch_restrict(const LevelK& F, const LevelK& C, const double* rf, double* bc, cudaStream_t s, int zc_lo,

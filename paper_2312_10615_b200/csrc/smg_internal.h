@@ -77,8 +77,9 @@ void launch_dgs_papply(const LevelK& L, double* x, const double* delta, cudaStre
 void launch_dgs_prev(const LevelK& L, double* x, const double* b, int colour, cudaStream_t s);
 void launch_vanka_delta(const LevelK& L, const double* x, const double* b, const int32_t* cells,
                         const uint8_t* masks, int ncells, const double* ktab, double* delta, cudaStream_t s);
+// amask (z-slabs, optional): per block, the slots this part owns (bit s = slot s, bit 6 = p).
 void launch_vanka_apply(const LevelK& L, double* x, const int32_t* cells, const uint8_t* masks, int ncells,
-                        const double* delta, cudaStream_t s);
+                        const double* delta, cudaStream_t s, const uint8_t* amask = nullptr);
 // Cooperative (persistent, grid-synchronised) symmetric sweeps: nu Vanka sweeps
 // over the 8 colour lists; nph DGS phases (20 = full symmetric sweep).
 void launch_vanka_sym_coop(const LevelK& L, double* x, const double* b, const int32_t* const* cells,
