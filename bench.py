@@ -190,7 +190,10 @@ def run_ours(args, ws, rank, local):
         barrier(ws)
         allmax(0.0, ws)
         return None
-    s = smg.Solver(nx, ny, nz, h=h, levels=lv, device=local, devices=list(range(ws)) if slabs else None)
+    devs = list(range(ws))
+    if slabs and os.environ.get("SMG_EMULATE_SLABS"):  # plumbing check on a 1-GPU box: all slabs on device 0
+        devs = [0] * ws
+    s = smg.Solver(nx, ny, nz, h=h, levels=lv, device=local, devices=devs if slabs else None)
     wsum = 1 if slabs else ws  # problem copies solved (replicas) -> aggregate DOF/s
     # host input in pinned memory (e2e path) and the same b resident in HBM
     bpin = smg.PinnedArray(n)
