@@ -1091,8 +1091,10 @@ static void launch_sweep(const void* fn_grid, const void* fn_cluster, bool clust
         attr[0].val.clusterDim.z = 1;
         cudaLaunchKernelExC(&cfg, fn_cluster, args);
     } else {
-        cfg.gridDim = dim3(coop_blocks(fn_grid, work));
-        cfg.blockDim = dim3(256);
+        const int bt = env_int("SMG_COOP_THREADS", 256) == 512 ? 512 : 256;  // tuning knob
+        const int blocks = coop_blocks(fn_grid, work);
+        cfg.gridDim = dim3(bt == 512 ? (blocks + 1) / 2 : blocks);
+        cfg.blockDim = dim3(bt);
         attr[0].id = cudaLaunchAttributeCooperative;
         attr[0].val.cooperative = 1;
         cudaLaunchKernelExC(&cfg, fn_grid, args);
