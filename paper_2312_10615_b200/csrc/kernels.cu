@@ -652,81 +652,6 @@ __global__ void __launch_bounds__(512) k_vanka8(LevelK L, double* __restrict__ X
     vanka_sweeps8<MODE, CPT>(L, X, B, vl, Ks, nu, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
 }
 
-// Vanka sweeps of a small level in ONE CTA (<= kVankaBlockCells blocks per
-// colour): 8 lanes per block as in vanka_sweeps8, deltas staged in shared
-// memory, __syncthreads between the compute and apply steps (global data is
-// coherent within the SM), so no global fences.
-constexpr int kVankaBlockCells = 1024;
-template <bool XSMEM>
-__device__ __forceinline__ void vanka_sweeps_block(const LevelK& L, double* __restrict__ X,
-                                                   const double* __restrict__ B, const VankaLists& vl,
-                                                   const double* __restrict__ Ks, double* __restrict__ dsm, int nu) {
-    const Geom& g = L.g;
-    const int64_t fs = g.fs, sy = g.sy, sz = g.sz;
-    const int lane = threadIdx.x & 31, s8 = lane & 7;
-    const int groups = blockDim.x >> 3, grp = threadIdx.x >> 3;
-    const int64_t offs = s8 == 0 ? 0 : s8 == 1 ? 1 : s8 == 2 ? fs : s8 == 3 ? fs + sy : s8 == 4 ? 2 * fs
-                         : s8 == 5 ? 2 * fs + sz : 3 * fs;
-    for (int sweep = 0; sweep < nu; ++sweep)
-        for (int k = 0; k < 16; ++k) {
-            const int col = k < 8 ? k : 15 - k;
-            const int n = vl.n[col];
-            const int rounds = (n + groups - 1) / groups;
-            for (int rd = 0; rd < rounds; ++rd) {
-                const int t = grp + rd * groups;
-                const bool act = t < n;
-                int64_t i = 0;
-                int m = 0;
-                if (act) {
-                    i = vl.cells[col][t];
-                    m = vl.masks[col][t];
-                }
-                double r = 0.0;
-                if (act && s8 < 7) {
-                    const double *U = X, *V = X + fs, *W = X + 2 * fs, *P = X + 3 * fs;
-                    switch (s8) {
-                        case 0: r = (m & 1) ? B[i] - mom(L, U, P, i, 1) : 0.0; break;
-                        case 1: r = (m & 2) ? B[i + 1] - mom(L, U, P, i + 1, 1) : 0.0; break;
-                        case 2: r = (m & 4) ? B[fs + i] - mom(L, V, P, i, sy) : 0.0; break;
-                        case 3: r = (m & 8) ? B[fs + i + sy] - mom(L, V, P, i + sy, sy) : 0.0; break;
-                        case 4: r = (m & 16) ? B[2 * fs + i] - mom(L, W, P, i, sz) : 0.0; break;
-                        case 5: r = (m & 32) ? B[2 * fs + i + sz] - mom(L, W, P, i + sz, sz) : 0.0; break;
-                        default: r = B[3 * fs + i] - cont(L, U, V, W, P, i, L.gamma); break;
-                    }
-                }
-                const double* K = Ks + m * 49 + (s8 < 7 ? s8 : 0) * 7;
-                double acc = 0.0;
-#pragma unroll
-                for (int q = 0; q < 7; ++q) {
-                    const double rq = __shfl_sync(0xffffffffu, r, (lane & ~7) + q);
-                    acc = acc + K[q] * rq;
-                }
-                if (act) dsm[t * 8 + s8] = acc;
-            }
-            __syncthreads();
-            for (int rd = 0; rd < rounds; ++rd) {
-                const int t = grp + rd * groups;
-                if (t >= n || s8 >= 7) continue;
-                const int m = vl.masks[col][t];
-                if (s8 == 6 || (m & (1 << s8))) {
-                    const int64_t a = vl.cells[col][t] + offs;
-                    X[a] = X[a] + dsm[t * 8 + s8];
-                }
-            }
-            __syncthreads();
-        }
-}
-
-__global__ void __launch_bounds__(1024) k_vanka_block(LevelK L, double* __restrict__ X, const double* __restrict__ B,
-                                                      VankaLists vl, const double* __restrict__ ktab, int nu) {
-    extern __shared__ double vsm[];
-    double* Ks = vsm;
-    double* dsm = vsm + 64 * 49;
-    for (int k = threadIdx.x; k < 64 * 49; k += blockDim.x) Ks[k] = ktab[k];
-    __syncthreads();
-    vanka_sweeps_block<false>(L, X, B, vl, Ks, dsm, nu);
-}
-
 __device__ __forceinline__ void dgs_vel_cell(const LevelK& L, double* __restrict__ X, const double* __restrict__ B,
                                              int x, int y, int z) {
     const Geom& g = L.g;
@@ -1205,13 +1130,6 @@ void launch_vanka_sym_coop(const LevelK& L, double* x, const double* b, const in
     LevelK Lc = L;
     void* args[] = {&Lc, &x, const_cast<double**>(&b), &vl, const_cast<double**>(&ktab), &nu};
     const int64_t lanes = 8 * static_cast<int64_t>(maxn);
-    if (maxn <= kVankaBlockCells && env_int("SMG_SYNC_MODE", 0) == 0) {  // small level: one CTA
-        const size_t smem = (64 * 49 + kVankaBlockCells * 8) * sizeof(double);
-        cudaFuncSetAttribute(k_vanka_block, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        k_vanka_block<<<1, 1024, smem, s>>>(L, x, b, vl, ktab, nu);
-        count();
-        return;
-    }
     static int sms = 0;
     if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     int per_sm = 0;
