@@ -597,6 +597,9 @@ int sqmr(smg_ctx* c, double tol, int maxit, smg_history* hist, int* status) {
         for (int j = 1; j <= maxit && st == SMG_MAX_ITERATIONS; ++j) {
             CK(cudaGraphLaunch(c->graph, c->st));
             graph_launches += c->graph_kernels;
+            if (const int e = take_launch_error())
+                throw SmgError(SMG_ECUDA, std::string("kernel launch rejected: ") +
+                                              cudaGetErrorString(static_cast<cudaError_t>(e)));
             CK(cudaMemcpyAsync(c->hscal, sc + S_REL, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->st));
             CK(cudaStreamSynchronize(c->st));
             const double rel = c->hscal[0];
@@ -942,6 +945,9 @@ template <class F>
 int guard(smg_ctx* c, F&& f) {
     try {
         f();
+        if (const int e = take_launch_error())
+            throw SmgError(SMG_ECUDA, std::string("kernel launch rejected: ") +
+                                          cudaGetErrorString(static_cast<cudaError_t>(e)));
         return 0;
     } catch (const SmgError& e) {
         if (c) c->err = e.what();

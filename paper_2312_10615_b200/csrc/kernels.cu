@@ -19,7 +19,17 @@
 namespace smg {
 
 static std::atomic<int64_t> g_launches{0};
+static std::atomic<int> g_launch_err{0};
 int64_t launch_count() { return g_launches.load(); }
+// First launch-configuration error since the last call (0 if none); the host
+// turns it into SMG_ECUDA so a rejected launch can never pass silently.
+int take_launch_error() { return g_launch_err.exchange(0); }
+static inline void note(cudaError_t e) {
+    if (e != cudaSuccess) {
+        int z = 0;
+        g_launch_err.compare_exchange_strong(z, static_cast<int>(e));
+    }
+}
 static inline void count() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 namespace {
@@ -1056,21 +1066,30 @@ static int env_int(const char* name, int dflt) {
     return e ? std::atoi(e) : dflt;
 }
 
-// Grid size of a cooperative (grid-synchronised) launch: enough 256-thread
-// blocks for `work` items, capped at full co-residency.
-static int coop_blocks(const void* fn, int64_t work) {
+static int num_sms() {
     static int sms = 0;
     if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    return sms;
+}
+
+// Co-resident block capacity of a cooperative kernel at `threads` per block.
+static int64_t coop_capacity_blocks(const void* fn, int threads) {
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, 0);
     const int cap = env_int("SMG_COOP_BLOCKS_PER_SM", 0);  // tuning knob
     if (cap > 0 && cap < per_sm) per_sm = cap;
-    const int64_t maxb = static_cast<int64_t>(sms) * (per_sm > 0 ? per_sm : 1);
-    const int64_t want = (work + 255) / 256;
+    return static_cast<int64_t>(num_sms()) * (per_sm > 0 ? per_sm : 0);
+}
+
+// Grid size of a cooperative launch: enough blocks for `work` threads, capped at co-residency.
+static int coop_blocks(const void* fn, int64_t work, int threads) {
+    const int64_t maxb = coop_capacity_blocks(fn, threads);
+    const int64_t want = (work + threads - 1) / threads;
     return static_cast<int>(want < 1 ? 1 : (want < maxb ? want : maxb));
 }
 
 constexpr int kClusterCTAs = 16, kClusterThreads = 512;
+static int coop_threads() { return env_int("SMG_COOP_THREADS", 512) == 256 ? 256 : 512; }  // tuning knob
 
 // Launch either as one cooperative grid (MODE 0) or as a single cluster of
 // kClusterCTAs CTAs (MODE 1) whose phases are separated by cluster barriers.
@@ -1082,22 +1101,21 @@ static void launch_sweep(const void* fn_grid, const void* fn_cluster, bool clust
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     if (cluster) {
-        cudaFuncSetAttribute(fn_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        note(cudaFuncSetAttribute(fn_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
         cfg.gridDim = dim3(kClusterCTAs);
         cfg.blockDim = dim3(kClusterThreads);
         attr[0].id = cudaLaunchAttributeClusterDimension;
         attr[0].val.clusterDim.x = kClusterCTAs;
         attr[0].val.clusterDim.y = 1;
         attr[0].val.clusterDim.z = 1;
-        cudaLaunchKernelExC(&cfg, fn_cluster, args);
+        note(cudaLaunchKernelExC(&cfg, fn_cluster, args));
     } else {
-        const int bt = env_int("SMG_COOP_THREADS", 512) == 256 ? 256 : 512;  // tuning knob
-        const int blocks = coop_blocks(fn_grid, work);
-        cfg.gridDim = dim3(bt == 512 ? (blocks + 1) / 2 : blocks);
+        const int bt = coop_threads();
+        cfg.gridDim = dim3(coop_blocks(fn_grid, work, bt));
         cfg.blockDim = dim3(bt);
         attr[0].id = cudaLaunchAttributeCooperative;
         attr[0].val.cooperative = 1;
-        cudaLaunchKernelExC(&cfg, fn_grid, args);
+        note(cudaLaunchKernelExC(&cfg, fn_grid, args));
     }
     count();
 }
@@ -1130,20 +1148,22 @@ void launch_vanka_sym_coop(const LevelK& L, double* x, const double* b, const in
     LevelK Lc = L;
     void* args[] = {&Lc, &x, const_cast<double**>(&b), &vl, const_cast<double**>(&ktab), &nu};
     const int64_t lanes = 8 * static_cast<int64_t>(maxn);
-    static int sms = 0;
-    if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_vanka8<0, 1>, 256, 0);
-    const int64_t grid_threads = static_cast<int64_t>(sms) * (per_sm > 0 ? per_sm : 1) * 256;
     const int64_t cl_threads = static_cast<int64_t>(kClusterCTAs) * kClusterThreads;
-    const bool cl = env_int("SMG_SYNC_MODE", 0) == 2 || (env_int("SMG_SYNC_MODE", 0) == 0 && lanes <= cl_threads);
-    const int64_t cap = cl ? cl_threads : grid_threads;
-    const int64_t need = (lanes + cap - 1) / cap;  // cells per thread-group
-    if (need <= 1) launch_vanka8<1>(cl, lanes, args, s);
-    else if (need <= 2) launch_vanka8<2>(cl, (lanes + 1) / 2, args, s);
-    else if (need <= 4) launch_vanka8<4>(cl, (lanes + 3) / 4, args, s);
-    else if (need <= 8) launch_vanka8<8>(cl, (lanes + 7) / 8, args, s);
-    else {  // beyond co-resident capacity: per-phase kernels
+    const int mode = env_int("SMG_SYNC_MODE", 0);
+    const bool cl = mode == 2 || (mode == 0 && lanes <= cl_threads);
+    // every block of a colour must be held in registers by some lane group:
+    // threads * CPT >= lanes with threads = co-resident capacity of THAT instance
+    auto fits = [&](const void* fn, int cpt) {
+        const int64_t threads = cl ? cl_threads : coop_capacity_blocks(fn, coop_threads()) * coop_threads();
+        return threads * cpt >= lanes;
+    };
+    bool done = true;
+    if (fits(reinterpret_cast<const void*>(k_vanka8<0, 1>), 1)) launch_vanka8<1>(cl, lanes, args, s);
+    else if (fits(reinterpret_cast<const void*>(k_vanka8<0, 2>), 2)) launch_vanka8<2>(cl, (lanes + 1) / 2, args, s);
+    else if (fits(reinterpret_cast<const void*>(k_vanka8<0, 4>), 4)) launch_vanka8<4>(cl, (lanes + 3) / 4, args, s);
+    else if (fits(reinterpret_cast<const void*>(k_vanka8<0, 8>), 8)) launch_vanka8<8>(cl, (lanes + 7) / 8, args, s);
+    else done = false;
+    if (!done) {
         for (int sweep = 0; sweep < nu; ++sweep)
             for (int k = 0; k < 16; ++k) {
                 const int col = k < 8 ? k : 15 - k;

@@ -139,5 +139,7 @@ void launch_xpby_dev(double* q, const double* t, const double* sc, int64_t n, cu
 
 // Number of our kernels launched so far (per process), for the bench's gpu_launches.
 int64_t launch_count();
+// First rejected launch (cudaError_t) since the last call, 0 if none.
+int take_launch_error();
 
 }  // namespace smg
