@@ -205,10 +205,12 @@ def run_ours(args, ws, rank, local):
     # ---- device-resident timed region ----
     barrier(ws)
     dev_ms, iters, launches = 0.0, 0, 0
+    statuses = []
     with ClockSampler(local) as clk:
         t0 = time.perf_counter()
         for _ in range(args.steps):
             hist, st = s.solve_resident(tol, 500)
+            statuses.append(st)
             t = s.timing()
             dev_ms += t["solve_ms"]
             iters += t["iterations"]
@@ -245,6 +247,8 @@ def run_ours(args, ws, rank, local):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": name, "N_dof": n, "iterations_per_solve": iters / args.steps,
                        "time_to_tol_ms": dev_ms / args.steps,
+                       "converged": all(v == smg.SMG_CONVERGED for v in statuses),
+                       "final_rel_residual": float(hist[-1]) if len(hist) else None, "tol": tol,
                        "parallelism": (f"z-slab x{ws}" if slabs else f"replicas x{ws}") if ws > 1 else "1 GPU",
                        "l2": "inputs larger than L2 (fine-level vectors 73 MB each, 7 live)"},
             "e2e": {"value": e2e_val, "unit": "DOF/s", "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n,
