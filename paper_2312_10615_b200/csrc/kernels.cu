@@ -720,6 +720,73 @@ __device__ __forceinline__ bool colour_cell(const Geom& g, int c, int64_t t, int
     return true;
 }
 
+// ---- lazy-gather forward pressure phases (single-part levels) ----
+// Eager form: after phase c every cell K gets p_K += eta/h^2 (6 D_c[K] - sum_nbr D_c),
+// which is a no-op unless colour(K) == c (self term) or colour(K) == c ^ bit
+// (gather from the colour-c neighbours along one axis).  p_K is only read by
+// K's own phase (its continuity residual) before the pressure sweep ends, so
+// the gathers are applied when K is next read: those from phases c' < colour(K)
+// at the start of K's phase, the others in a flush after phase 7 — the same
+// additions in the same order, hence bit-identical.  One combined delta buffer
+// holds delta_c at the V2 cells of colour c (band cells stay 0); a gather from
+// phase c' masks the neighbour sum to colour-c' cells.
+__device__ __forceinline__ double masked_nbr_sum(const Geom& g, const double* __restrict__ D, int64_t i, int x, int y,
+                                                 int zg, int cc) {
+    // neighbour colours: x +-1 flips bit 1, y +-1 bit 2, z +-1 bit 4 of colour (x,y,zg)
+    const int ck = (x & 1) + 2 * (y & 1) + 4 * (zg & 1);
+    const bool mx = (ck ^ 1) == cc, my = (ck ^ 2) == cc, mz = (ck ^ 4) == cc;
+    double s = (mx ? D[i - 1] : 0.0) + (mx ? D[i + 1] : 0.0);
+    s = s + (my ? D[i - g.sy] : 0.0);
+    s = s + (my ? D[i + g.sy] : 0.0);
+    s = s + (mz ? D[i - g.sz] : 0.0);
+    s = s + (mz ? D[i + g.sz] : 0.0);
+    return s;
+}
+
+__device__ __forceinline__ void pending_gathers(const LevelK& L, double* __restrict__ X, const double* __restrict__ D,
+                                                int x, int y, int z, bool later) {
+    const Geom& g = L.g;
+    const int zg = g.gz(z);
+    const int k = (x & 1) + 2 * (y & 1) + 4 * (zg & 1);
+    const int64_t i = g.slot(x, y, z), ip = 3 * g.fs + i;
+    const int c1 = k ^ 1, c2 = k ^ 2, c4 = k ^ 4;  // ascending order among the three
+    int cs[3] = {c1, c2, c4};
+    if (cs[0] > cs[1]) { const int t = cs[0]; cs[0] = cs[1]; cs[1] = t; }
+    if (cs[1] > cs[2]) { const int t = cs[1]; cs[1] = cs[2]; cs[2] = t; }
+    if (cs[0] > cs[1]) { const int t = cs[0]; cs[0] = cs[1]; cs[1] = t; }
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        const int cc = cs[q];
+        if ((cc < k) == later) continue;
+        const double sn = masked_nbr_sum(g, D, i, x, y, zg, cc);
+        X[ip] = X[ip] + L.eta_h2 * (6.0 * 0.0 - sn);
+    }
+}
+
+__device__ __forceinline__ void pf_lazy_cell(const LevelK& L, double* __restrict__ X, const double* __restrict__ B,
+                                             double* __restrict__ D, int x, int y, int z) {
+    const Geom& g = L.g;
+    pending_gathers(L, X, D, x, y, z, false);
+    if (band_cell(L, x, y, z)) return;
+    const int64_t fs = g.fs, sy = g.sy, sz = g.sz, ii = g.slot(x, y, z);
+    const double rr = B[3 * fs + ii] - cont(L, X, X + fs, X + 2 * fs, X + 3 * fs, ii, L.gamma);
+    const double dc = rr / L.dp;
+    D[ii] = dc;
+    X[ii] = X[ii] + (0.0 - dc) * L.inv_h;
+    X[ii + 1] = X[ii + 1] + (dc - 0.0) * L.inv_h;
+    X[fs + ii] = X[fs + ii] + (0.0 - dc) * L.inv_h;
+    X[fs + ii + sy] = X[fs + ii + sy] + (dc - 0.0) * L.inv_h;
+    X[2 * fs + ii] = X[2 * fs + ii] + (0.0 - dc) * L.inv_h;
+    X[2 * fs + ii + sz] = X[2 * fs + ii + sz] + (dc - 0.0) * L.inv_h;
+    // self term: the colour-c neighbour sum is a sum of six zeros
+    double sn = 0.0 + 0.0;
+    sn = sn + 0.0;
+    sn = sn + 0.0;
+    sn = sn + 0.0;
+    sn = sn + 0.0;
+    X[3 * fs + ii] = X[3 * fs + ii] + L.eta_h2 * (6.0 * dc - sn);
+}
+
 // Symmetric DGS sweep (20 phases, OD-1) in one persistent launch.  Forward
 // pressure colour c uses delta buffer D[c&1]; its delta step also clears the
 // entries of colour c-2 left in that buffer, so only colour-c entries are
@@ -741,48 +808,19 @@ __device__ __forceinline__ void dgs_sweep(const LevelK& L, double* __restrict__ 
                 const int y = static_cast<int>(r / g.nx), x = static_cast<int>(r - static_cast<int64_t>(y) * g.nx);
                 if (((x + y + g.gz(z)) & 1) == colour) dgs_vel_cell(L, X, B, x, y, z);
             }
-        } else if (ph <= 9) {
+        } else if (ph <= 9) {  // lazy-gather forward pressure phase (see pf_lazy_cell); D0 combined
             const int c = ph - 2;
-            double* D = (c & 1) ? D1 : D0;
-            const int cold = (c + 6) & 7;  // colour c-2 (mod 8), same buffer
             int x, y, z;
-            for (int64_t t = tid; colour_cell(g, cold, t, x, y, z); t += nth) D[g.slot(x, y, z)] = 0.0;
-            for (int64_t t = tid; colour_cell(g, c, t, x, y, z); t += nth) {
-                if (band_cell(L, x, y, z)) continue;
-                const int64_t i = g.slot(x, y, z);
-                const double rr = B[3 * fs + i] - cont(L, X, X + fs, X + 2 * fs, X + 3 * fs, i, L.gamma);
-                D[i] = rr / L.dp;
-            }
-            phase_sync<MODE>();
-            // faces and pressure of colour-c cells
-            for (int64_t t = tid; colour_cell(g, c, t, x, y, z); t += nth) {
-                if (band_cell(L, x, y, z)) continue;
-                const int64_t i = g.slot(x, y, z);
-                const double dc = D[i];
-                X[i] = X[i] + (0.0 - dc) * L.inv_h;  // left u face of C: (d_left - d_right)/h with d_left = 0
-                X[i + 1] = X[i + 1] + (dc - 0.0) * L.inv_h;
-                X[fs + i] = X[fs + i] + (0.0 - dc) * L.inv_h;
-                X[fs + i + sy] = X[fs + i + sy] + (dc - 0.0) * L.inv_h;
-                X[2 * fs + i] = X[2 * fs + i] + (0.0 - dc) * L.inv_h;
-                X[2 * fs + i + sz] = X[2 * fs + i + sz] + (dc - 0.0) * L.inv_h;
-                double sn = D[i - 1] + D[i + 1];
-                sn = sn + D[i - sy];
-                sn = sn + D[i + sy];
-                sn = sn + D[i - sz];
-                sn = sn + D[i + sz];
-                X[3 * fs + i] = X[3 * fs + i] + L.eta_h2 * (6.0 * dc - sn);
-            }
-            // pressures of the three colours one parity bit away (the only cells with colour-c neighbours)
-            for (int bit = 1; bit < 8; bit <<= 1)
-                for (int64_t t = tid; colour_cell(g, c ^ bit, t, x, y, z); t += nth) {
-                    const int64_t i = g.slot(x, y, z);
-                    double sn = D[i - 1] + D[i + 1];
-                    sn = sn + D[i - sy];
-                    sn = sn + D[i + sy];
-                    sn = sn + D[i - sz];
-                    sn = sn + D[i + sz];
-                    X[3 * fs + i] = X[3 * fs + i] + L.eta_h2 * (6.0 * D[i] - sn);
+            for (int64_t t = tid; colour_cell(g, c, t, x, y, z); t += nth) pf_lazy_cell(L, X, B, D0, x, y, z);
+            if (ph == 9) {
+                phase_sync<MODE>();
+                for (int64_t t = tid; t < ncell; t += nth) {
+                    const int zz = static_cast<int>(t / nxy);
+                    const int64_t r = t - zz * nxy;
+                    const int yy = static_cast<int>(r / g.nx), xx = static_cast<int>(r - static_cast<int64_t>(yy) * g.nx);
+                    pending_gathers(L, X, D0, xx, yy, zz, true);
                 }
+            }
         } else {
             const int c = 17 - ph;
             int x, y, z;
@@ -898,6 +936,21 @@ __global__ void __launch_bounds__(256) k_dgs_pf_apply_c(LevelK L, double* __rest
             X[2 * fs + ih + sz] = X[2 * fs + ih + sz] + (D[ih] - 0.0) * L.inv_h;
         }
     }
+}
+
+__global__ void __launch_bounds__(256) k_dgs_pf_lazy_c(LevelK L, double* __restrict__ X, const double* __restrict__ B,
+                                                       double* __restrict__ D, int c) {
+    const Geom& g = L.g;
+    const int i = blockIdx.x * 32 + threadIdx.x, j = blockIdx.y * 8 + threadIdx.y, k = blockIdx.z;
+    int x, y, z;
+    if (!half_cell(g, c, i, j, k, x, y, z)) return;
+    pf_lazy_cell(L, X, B, D, x, y, z);
+}
+
+__global__ void __launch_bounds__(256) k_dgs_pf_flush(LevelK L, double* __restrict__ X, const double* __restrict__ D) {
+    Cell c;
+    if (!thread_cell(L.g, c)) return;
+    pending_gathers(L, X, D, c.x, c.y, c.z, true);
 }
 
 __global__ void __launch_bounds__(256) k_dgs_prev_c(LevelK L, double* __restrict__ X, const double* __restrict__ B,
@@ -1219,19 +1272,19 @@ void launch_dgs_prev_c(const LevelK& L, double* x, const double* b, int c, cudaS
 // delta-buffer protocol as k_dgs_sym_coop).
 static void launch_dgs_sym_phases(const LevelK& L, double* x, const double* b, double* d0, double* d1, int nph,
                                   cudaStream_t s) {
+    (void)d1;
     const Geom& g = L.g;
     const dim3 blk(32, 8);
-    const dim3 gv((((g.nx + 1) / 2) + 31) / 32, (g.ny + 7) / 8, g.nz);
-    const dim3 gh((((g.nx + 1) / 2) + 31) / 32, (((g.ny + 1) / 2) + 7) / 8, (g.nz + 1) / 2);
+    const dim3 gv = dgs_grid_v(g), gh = dgs_grid_h(g);
     for (int ph = 0; ph < nph; ++ph) {
         if (ph == 0 || ph == 1 || ph == 18 || ph == 19) {
             k_dgs_vel_c<<<gv, blk, 0, s>>>(L, x, b, ph < 2 ? ph : 19 - ph);
         } else if (ph <= 9) {
-            const int c = ph - 2;
-            double* D = (c & 1) ? d1 : d0;
-            k_dgs_pf_delta_c<<<gh, blk, 0, s>>>(L, x, b, D, c);
-            k_dgs_pf_apply_c<<<gh, blk, 0, s>>>(L, x, D, c);
-            count();
+            k_dgs_pf_lazy_c<<<gh, blk, 0, s>>>(L, x, b, d0, ph - 2);
+            if (ph == 9) {
+                k_dgs_pf_flush<<<cell_grid(g), blk, 0, s>>>(L, x, d0);
+                count();
+            }
         } else {
             k_dgs_prev_c<<<gh, blk, 0, s>>>(L, x, b, 17 - ph);
         }
