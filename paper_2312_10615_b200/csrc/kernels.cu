@@ -603,6 +603,14 @@ __device__ __forceinline__ void vanka_sweeps8(const LevelK& L, double* __restric
     const int groups = nth >> 3, grp = tid >> 3;
     const int64_t offs = s8 == 0 ? 0 : s8 == 1 ? 1 : s8 == 2 ? fs : s8 == 3 ? fs + sy : s8 == 4 ? 2 * fs
                          : s8 == 5 ? 2 * fs + sz : 3 * fs;
+    // this group's block of every colour, loaded once (slot << 7 | mask; -1 = none): removes a
+    // dependent global load from every phase step
+    constexpr bool kPre = CPT == 1;
+    int64_t pre[8];
+    if (kPre)
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+            pre[c] = grp < vl.n[c] ? ((static_cast<int64_t>(vl.cells[c][grp]) << 7) | vl.masks[c][grp]) : -1;
     for (int sweep = 0; sweep < nu; ++sweep)
         for (int k = 0; k < 16; ++k) {
             const int col = k < 8 ? k : 15 - k;
@@ -618,8 +626,17 @@ __device__ __forceinline__ void vanka_sweeps8(const LevelK& L, double* __restric
                 int64_t i = 0;
                 int m = 0;
                 if (act) {
-                    i = vl.cells[col][t];
-                    m = vl.masks[col][t];
+                    if (kPre) {
+                        int64_t e = 0;
+#pragma unroll
+                        for (int c = 0; c < 8; ++c)
+                            if (c == col) e = pre[c];
+                        i = e >> 7;
+                        m = static_cast<int>(e & 127);
+                    } else {
+                        i = vl.cells[col][t];
+                        m = vl.masks[col][t];
+                    }
                 }
                 double r = 0.0;
                 if (act && s8 < 7) {
