@@ -167,6 +167,9 @@ struct DevLevel {
     int32_t* vk_cells[8] = {};
     uint8_t* vk_mask[8] = {};
     uint8_t* vk_amask[8] = {};  // z-slab levels: owned slots per block (nullptr: all)
+    double* xb = nullptr;         // ping-pong partner of x for the Vanka sweep
+    int32_t* vk_refresh = nullptr;  // slots every Vanka residual reads (refreshed x -> xb per sweep)
+    int64_t vk_nrefresh = 0;
     int vk_n[8] = {};
     double* ktab = nullptr;  // [64][49]
 };
@@ -323,6 +326,39 @@ void build(smg_ctx* c, const std::vector<double>* shared_coarse = nullptr, std::
                     used[m] = true;
                 }
         L.counts[4] = v1;
+        if (!dist) {  // read set of the band blocks: their 7 DOFs and every stencil input of their residuals
+            const Geom& G = L.k.g;
+            std::vector<uint8_t> need(static_cast<size_t>(G.vec_len()), 0);
+            auto mark_mom = [&](int64_t f, int64_t sn, int64_t pfield) {
+                const int64_t o[7] = {0, -1, 1, -G.sy, G.sy, -G.sz, G.sz};
+                for (int64_t d : o) need[f + d] = 1;
+                need[pfield] = 1;
+                need[pfield - sn] = 1;
+            };
+            for (int col = 0; col < 8; ++col)
+                for (size_t t = 0; t < cells[col].size(); ++t) {
+                    const int64_t i = cells[col][t];
+                    const int m = masks[col][t];
+                    const int64_t fs = G.fs;
+                    const int64_t P = 3 * fs + i;
+                    if (m & 1) mark_mom(i, 1, P);
+                    if (m & 2) mark_mom(i + 1, 1, P + 1);
+                    if (m & 4) mark_mom(fs + i, G.sy, P);
+                    if (m & 8) mark_mom(fs + i + G.sy, G.sy, P + G.sy);
+                    if (m & 16) mark_mom(2 * fs + i, G.sz, P);
+                    if (m & 32) mark_mom(2 * fs + i + G.sz, G.sz, P + G.sz);
+                    need[i] = need[i + 1] = need[fs + i] = need[fs + i + G.sy] = need[2 * fs + i] =
+                        need[2 * fs + i + G.sz] = need[P] = 1;
+                }
+            std::vector<int32_t> lst;
+            for (int64_t k = 0; k < static_cast<int64_t>(need.size()); ++k)
+                if (need[k]) lst.push_back(static_cast<int32_t>(k));
+            L.vk_nrefresh = static_cast<int64_t>(lst.size());
+            L.vk_refresh = c->dalloc<int32_t>(L.vk_nrefresh);
+            CK(cudaMemcpyAsync(L.vk_refresh, lst.data(), lst.size() * sizeof(int32_t), cudaMemcpyHostToDevice, c->st));
+            L.xb = c->dalloc<double>(G.vec_len());
+            CK(cudaStreamSynchronize(c->st));
+        }
         for (int col = 0; col < 8; ++col) {
             L.vk_n[col] = static_cast<int>(cells[col].size());
             max_vk = std::max(max_vk, L.vk_n[col]);
@@ -493,7 +529,8 @@ void symmetric_dgs(smg_ctx* c, int l, double* x, const double* b) {
 
 void vanka_sym_coop(smg_ctx* c, int l, double* x, const double* b) {
     DevLevel& L = c->lv[l];
-    launch_vanka_sym_coop(L.k, x, b, L.vk_cells, L.vk_mask, L.vk_n, L.ktab, c->vk_delta, c->prm.nu, c->st);
+    launch_vanka_sym_coop(L.k, x, b, L.vk_cells, L.vk_mask, L.vk_n, L.ktab, c->vk_delta, c->prm.nu, c->st, L.xb,
+                          L.vk_refresh, L.vk_nrefresh);
 }
 
 void smooth(smg_ctx* c, int l, double* x, const double* b) {

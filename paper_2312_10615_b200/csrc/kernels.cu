@@ -670,6 +670,124 @@ __device__ __forceinline__ void vanka_sweeps8(const LevelK& L, double* __restric
         }
 }
 
+// Ping-pong variant: one barrier per colour phase.  Phase k (k = 0..16 nu - 1)
+// reads buffer X_k (XA for even k) and writes X_{k+1}: the new values of its
+// colour's blocks and a copy of the blocks updated by phase k-1, so X_{k+1}
+// holds the full state after phase k (it held the state after phase k-2, and
+// only those two colours changed).  Reads and writes never share a buffer
+// within a phase.  Before the sweep XB must equal XA on every DOF a Vanka
+// residual reads (refresh list).  16 nu phases: the result ends in XA.
+template <int MODE, int CPT>
+__device__ __forceinline__ void vanka_sweeps_pp(const LevelK& L, double* __restrict__ XA, double* __restrict__ XB,
+                                                const double* __restrict__ B, const VankaLists& vl,
+                                                const double* __restrict__ Ks, int nu, int tid, int nth) {
+    const Geom& g = L.g;
+    const int64_t fs = g.fs, sy = g.sy, sz = g.sz;
+    const int lane = threadIdx.x & 31, s8 = lane & 7;
+    const int groups = nth >> 3, grp = tid >> 3;
+    const int64_t offs = s8 == 0 ? 0 : s8 == 1 ? 1 : s8 == 2 ? fs : s8 == 3 ? fs + sy : s8 == 4 ? 2 * fs
+                         : s8 == 5 ? 2 * fs + sz : 3 * fs;
+    constexpr bool kPre = CPT == 1;
+    int64_t pre[8];
+    if (kPre)
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+            pre[c] = grp < vl.n[c] ? ((static_cast<int64_t>(vl.cells[c][grp]) << 7) | vl.masks[c][grp]) : -1;
+    auto block_of = [&](int c, int t, int64_t& i, int& m) {
+        if (kPre) {
+            int64_t e = 0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                if (q == c) e = pre[q];
+            i = e >> 7;
+            m = static_cast<int>(e & 127);
+        } else {
+            i = vl.cells[c][t];
+            m = vl.masks[c][t];
+        }
+    };
+    const int nph = 16 * nu;
+    for (int ph = 0; ph < nph; ++ph) {
+        const int k = ph & 15;
+        const int col = k < 8 ? k : 15 - k;
+        const int kp = (ph - 1) & 15;
+        const int pcol = ph == 0 ? -1 : (kp < 8 ? kp : 15 - kp);
+        const double* __restrict__ Xc = (ph & 1) ? XB : XA;
+        double* __restrict__ Xn = (ph & 1) ? XA : XB;
+        const int n = vl.n[col];
+#pragma unroll
+        for (int j = 0; j < CPT; ++j) {
+            const int t = grp + j * groups;
+            const bool act = t < n;
+            int64_t i = 0;
+            int m = 0;
+            if (act) block_of(col, t, i, m);
+            double r = 0.0, own = 0.0;
+            if (act && s8 < 7) {
+                const double *U = Xc, *V = Xc + fs, *W = Xc + 2 * fs, *P = Xc + 3 * fs;
+                switch (s8) {
+                    case 0: r = (m & 1) ? B[i] - mom(L, U, P, i, 1) : 0.0; break;
+                    case 1: r = (m & 2) ? B[i + 1] - mom(L, U, P, i + 1, 1) : 0.0; break;
+                    case 2: r = (m & 4) ? B[fs + i] - mom(L, V, P, i, sy) : 0.0; break;
+                    case 3: r = (m & 8) ? B[fs + i + sy] - mom(L, V, P, i + sy, sy) : 0.0; break;
+                    case 4: r = (m & 16) ? B[2 * fs + i] - mom(L, W, P, i, sz) : 0.0; break;
+                    case 5: r = (m & 32) ? B[2 * fs + i + sz] - mom(L, W, P, i + sz, sz) : 0.0; break;
+                    default: r = B[3 * fs + i] - cont(L, U, V, W, P, i, L.gamma); break;
+                }
+                own = Xc[i + offs];
+            }
+            const double* K = Ks + m * 49 + (s8 < 7 ? s8 : 0) * 7;
+            double acc = 0.0;
+#pragma unroll
+            for (int q = 0; q < 7; ++q) {
+                const double rq = __shfl_sync(0xffffffffu, r, (lane & ~7) + q);
+                acc = acc + K[q] * rq;
+            }
+            if (act && s8 < 7 && (s8 == 6 || (m & (1 << s8)))) Xn[i + offs] = own + acc;
+            // carry the previous phase's blocks into the buffer being written, except DOFs
+            // this phase rewrites: the same colour twice in a row (turning points), or a face
+            // shared with a band cell of the current colour (colours one parity bit apart)
+            if (pcol >= 0 && pcol != col && t < vl.n[pcol] && s8 < 7) {
+                int64_t ip;
+                int mp;
+                block_of(pcol, t, ip, mp);
+                bool carry = s8 == 6 || (mp & (1 << s8));
+                if (carry && s8 < 6 && (pcol ^ (1 << (s8 >> 1))) == col) {
+                    const int zl = static_cast<int>(ip / sz) - g.zg;
+                    const int64_t rem = ip - static_cast<int64_t>(zl + g.zg) * sz;
+                    const int y = static_cast<int>(rem / sy) - 1;
+                    const int x = static_cast<int>(rem - static_cast<int64_t>(y + 1) * sy) - g.xo;
+                    const int d = (s8 & 1) ? 1 : -1;
+                    const int ax = s8 >> 1;
+                    if (band_cell(L, x + (ax == 0 ? d : 0), y + (ax == 1 ? d : 0), zl + (ax == 2 ? d : 0)))
+                        carry = false;
+                }
+                if (carry) Xn[ip + offs] = Xc[ip + offs];
+            }
+        }
+        phase_sync<MODE>();
+    }
+}
+
+template <int MODE, int CPT>
+__global__ void __launch_bounds__(512) k_vanka_pp(LevelK L, double* __restrict__ XA, double* __restrict__ XB,
+                                                  const double* __restrict__ B, VankaLists vl,
+                                                  const double* __restrict__ ktab, int nu) {
+    __shared__ double Ks[64 * 49];
+    for (int k = threadIdx.x; k < 64 * 49; k += blockDim.x) Ks[k] = ktab[k];
+    __syncthreads();
+    vanka_sweeps_pp<MODE, CPT>(L, XA, XB, B, vl, Ks, nu, blockIdx.x * blockDim.x + threadIdx.x,
+                               gridDim.x * blockDim.x);
+}
+
+__global__ void k_refresh(const int32_t* __restrict__ lst, int64_t n, const double* __restrict__ src,
+                          double* __restrict__ dst) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t k = lst[t];
+        dst[k] = src[k];
+    }
+}
+
 template <int MODE, int CPT>
 __global__ void __launch_bounds__(512) k_vanka8(LevelK L, double* __restrict__ X, const double* __restrict__ B,
                                                 VankaLists vl, const double* __restrict__ ktab, int nu) {
@@ -1204,9 +1322,15 @@ static void launch_vanka8(bool cl, int64_t threads, void** args, cudaStream_t s)
                  threads, args, s);
 }
 
+template <int CPT>
+static void launch_vanka_pp(bool cl, int64_t threads, void** args, cudaStream_t s) {
+    launch_sweep(reinterpret_cast<const void*>(k_vanka_pp<0, CPT>), reinterpret_cast<const void*>(k_vanka_pp<1, CPT>),
+                 cl, threads, args, s);
+}
+
 void launch_vanka_sym_coop(const LevelK& L, double* x, const double* b, const int32_t* const* cells,
                            const uint8_t* const* masks, const int* n, const double* ktab, double* delta, int nu,
-                           cudaStream_t s) {
+                           cudaStream_t s, double* xb, const int32_t* refresh, int64_t nrefresh) {
     VankaLists vl;
     int maxn = 1;
     for (int c = 0; c < 8; ++c) {
@@ -1228,6 +1352,17 @@ void launch_vanka_sym_coop(const LevelK& L, double* x, const double* b, const in
         return threads * cpt >= lanes;
     };
     bool done = true;
+    if (xb && env_int("SMG_VANKA_PP", 1)) {  // ping-pong: one barrier per phase
+        if (nrefresh > 0) {
+            const int64_t blocks = (nrefresh + 255) / 256;
+            k_refresh<<<static_cast<int>(blocks < 4096 ? blocks : 4096), 256, 0, s>>>(refresh, nrefresh, x, xb);
+            count();
+        }
+        void* pargs[] = {args[0], &x, &xb, args[2], args[3], args[4], args[5]};
+        if (fits(reinterpret_cast<const void*>(k_vanka_pp<0, 1>), 1)) { launch_vanka_pp<1>(cl, lanes, pargs, s); return; }
+        if (fits(reinterpret_cast<const void*>(k_vanka_pp<0, 2>), 2)) { launch_vanka_pp<2>(cl, (lanes + 1) / 2, pargs, s); return; }
+        if (fits(reinterpret_cast<const void*>(k_vanka_pp<0, 4>), 4)) { launch_vanka_pp<4>(cl, (lanes + 3) / 4, pargs, s); return; }
+    }
     if (fits(reinterpret_cast<const void*>(k_vanka8<0, 1>), 1)) launch_vanka8<1>(cl, lanes, args, s);
     else if (fits(reinterpret_cast<const void*>(k_vanka8<0, 2>), 2)) launch_vanka8<2>(cl, (lanes + 1) / 2, args, s);
     else if (fits(reinterpret_cast<const void*>(k_vanka8<0, 4>), 4)) launch_vanka8<4>(cl, (lanes + 3) / 4, args, s);

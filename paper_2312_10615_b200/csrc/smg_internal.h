@@ -82,9 +82,12 @@ void launch_vanka_apply(const LevelK& L, double* x, const int32_t* cells, const 
                         const double* delta, cudaStream_t s, const uint8_t* amask = nullptr);
 // Cooperative (persistent, grid-synchronised) symmetric sweeps: nu Vanka sweeps
 // over the 8 colour lists; nph DGS phases (20 = full symmetric sweep).
+// xb (optional): second level vector for the ping-pong sweep (one barrier per
+// phase); refresh[0..nrefresh) lists the slots Vanka reads, copied x -> xb first.
 void launch_vanka_sym_coop(const LevelK& L, double* x, const double* b, const int32_t* const* cells,
                            const uint8_t* const* masks, const int* n, const double* ktab, double* delta, int nu,
-                           cudaStream_t s);
+                           cudaStream_t s, double* xb = nullptr, const int32_t* refresh = nullptr,
+                           int64_t nrefresh = 0);
 void launch_dgs_sym_coop(const LevelK& L, double* x, const double* b, double* d0, double* d1, int nph,
                          cudaStream_t s);
 // Whole smooth (Alg. 3) of a level small enough for one CTA's shared memory.
