@@ -1352,7 +1352,7 @@ void launch_vanka_sym_coop(const LevelK& L, double* x, const double* b, const in
         return threads * cpt >= lanes;
     };
     bool done = true;
-    if (xb && env_int("SMG_VANKA_PP", 1)) {  // ping-pong: one barrier per phase
+    if (xb && !cl && env_int("SMG_VANKA_PP", 1)) {  // ping-pong (grid mode): one barrier per phase
         if (nrefresh > 0) {
             const int64_t blocks = (nrefresh + 255) / 256;
             k_refresh<<<static_cast<int>(blocks < 4096 ? blocks : 4096), 256, 0, s>>>(refresh, nrefresh, x, xb);
