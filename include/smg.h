@@ -58,6 +58,7 @@ typedef struct smg_params {
     int nu;          /* symmetric multiplicative Vanka sweeps per side */
     int band_width;  /* V1 band width (Chebyshev)                      */
     int flags;       /* SMG_FLAG_*                                     */
+    int cycle;       /* 0 V-cycle, 1 W-cycle       */
 } smg_params;
 
 #define SMG_FLAG_SKIP_REVERSE_DGS 1 /* fault injection: symmetry negative control */
@@ -122,6 +123,10 @@ int smg_vcycle(smg_ctx* ctx, const double* b, double* x);
  * host solution out (end-to-end path).  *status gets an smg_status. */
 int smg_sqmr_solve(smg_ctx* ctx, const double* b, double* x, double tol, int maxit, smg_history* hist,
                    int* status);
+
+/* mg_solve: pure multigrid on L~, x_j = x_{j-1} + cycle(b - L~ x_{j-1}),
+ * history of ||b - L~ x_j|| / ||b||; single-part contexts. */
+int smg_mg_solve(smg_ctx* ctx, const double* b, double* x, double tol, int maxit, smg_history* hist, int* status);
 
 /* Device-resident path used for kernel-level timing: upload b once, solve with
  * everything in HBM, read x back separately. */

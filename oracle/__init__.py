@@ -60,6 +60,8 @@ def lib():
         L.orc_sqmr.argtypes = [C.c_void_p, _D, _D, C.c_double, C.c_int, C.c_int, _D, _D,
                                C.POINTER(C.c_int)]
         L.orc_forcing.argtypes = [C.c_void_p, C.c_int, C.c_uint64, _D]
+        L.orc_set_cycle.argtypes = [C.c_void_p, C.c_int]
+        L.orc_mg_solve.argtypes = [C.c_void_p, _D, _D, C.c_double, C.c_int, _D, _D, C.POINTER(C.c_int)]
         L.orc_census_box.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _I64]
         L.orc_coarsen_labels.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, _U8, _U8]
         L.orc_census_labels.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, _U8, C.c_int, _I64]
@@ -112,7 +114,7 @@ class Oracle:
     """Walled box of nx*ny*nz interior cells (implicit Dirichlet ring), spacing h."""
 
     def __init__(self, nx, ny=None, nz=None, h=None, eta=1.0, gamma=1e-3, levels=2, nu=1,
-                 band_width=1):
+                 band_width=1, cycle=0):
         ny = nx if ny is None else ny
         nz = nx if nz is None else nz
         h = 1.0 / nx if h is None else h
@@ -123,6 +125,7 @@ class Oracle:
         self.dims = (nx, ny, nz)
         self.levels = L.orc_nlevels(self._h)
         self.nu = nu
+        L.orc_set_cycle(self._h, int(cycle))
 
     def __del__(self):
         if getattr(self, "_h", None):
@@ -203,6 +206,16 @@ class Oracle:
         secs = np.zeros(maxit)
         it = C.c_int(0)
         st = lib().orc_sqmr(self._h, b, x, tol, maxit, int(precond), hist, secs, C.byref(it))
+        return x, hist[: it.value].copy(), secs[: it.value].copy(), int(st)
+
+    def mg_solve(self, b, tol=1e-6, maxit=100):
+        """Pure multigrid on L~: returns (x, history, seconds, status)."""
+        b = np.ascontiguousarray(b, np.float64)
+        x = np.empty(self.ndof(0))
+        hist = np.zeros(maxit)
+        secs = np.zeros(maxit)
+        it = C.c_int(0)
+        st = lib().orc_mg_solve(self._h, b, x, tol, maxit, hist, secs, C.byref(it))
         return x, hist[: it.value].copy(), secs[: it.value].copy(), int(st)
 
     def forcing(self, kind=FORCE_UNIFORM, seed=0):

@@ -709,6 +709,7 @@ struct Hierarchy {
     std::vector<std::unique_ptr<Level>> lv;
     std::vector<double> coarse_inv;  // symmetric dense inverse of the coarsest L̃, row-major
     int nu = 1;
+    int cycle = 0;              // 0 V-cycle, 1 W-cycle
     bool skip_reverse = false;  // fault injection for the symmetry negative control
 };
 
@@ -776,6 +777,14 @@ static void vcycle(const Hierarchy& H, int l, const vec& b, vec& x) {
     residual(L, x, b, r);
     restrict_(L, *H.lv[l + 1], r, rc);
     vcycle(H, l + 1, rc, ec);
+    // W-cycle: a second recursive call at every level below the finest, on the
+    // residual of the first; skipped when the child is the exact coarsest solve.
+    if (H.cycle == 1 && l >= 1 && l + 2 < static_cast<int>(H.lv.size())) {
+        vec r2, e2;
+        residual(*H.lv[l + 1], ec, rc, r2);
+        vcycle(H, l + 1, r2, e2);
+        for (size_t q = 0; q < ec.size(); ++q) ec[q] = ec[q] + e2[q];
+    }
     prolong(L, *H.lv[l + 1], ec, ef);
     for (int64_t q = 0; q < L.map.N; ++q) x[q] = x[q] + ef[q];
     smooth(L, x, b, H.nu, H.skip_reverse);
@@ -877,6 +886,31 @@ static int sqmr(const Hierarchy& H, const vec& b, vec& x, double tol, int maxit,
         for (int64_t i = 0; i < n; ++i) q[i] = t[i] + beta * q[i];
         rho = rho_new;
         nu_old = nu;
+    }
+    return ST_MAXIT;
+}
+
+// mg_solve: x_j = x_{j-1} + cycle(b - L~ x_{j-1}), x_0 = 0, history of
+// the true relative residual ||b - L~ x_j|| / ||b|| (canonical inner product).
+static int mg_solve(const Hierarchy& H, const vec& b, vec& x, double tol, int maxit, std::vector<double>& hist,
+                    std::vector<double>& secs) {
+    const Level& L0 = *H.lv[0];
+    const int64_t n = L0.map.N;
+    auto t0 = std::chrono::steady_clock::now();
+    hist.clear();
+    secs.clear();
+    x.assign(n, 0.0);
+    const double bnorm = std::sqrt(cdot(L0, b, b));
+    if (bnorm == 0.0) return ST_CONVERGED;
+    vec r = b, e;
+    for (int j = 1; j <= maxit; ++j) {
+        vcycle(H, 0, r, e);
+        for (int64_t i = 0; i < n; ++i) x[i] = x[i] + e[i];
+        residual(L0, x, b, r);
+        const double rel = std::sqrt(cdot(L0, r, r)) / bnorm;
+        hist.push_back(rel);
+        secs.push_back(std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+        if (rel < tol) return ST_CONVERGED;
     }
     return ST_MAXIT;
 }
@@ -1003,6 +1037,17 @@ void orc_v1_mask(void* h, int l, uint8_t* mask) {
     std::memcpy(mask, m.v1.data(), m.v1.size());
 }
 void orc_set_skip_reverse(void* h, int s) { HH(h).skip_reverse = s != 0; }
+void orc_set_cycle(void* h, int kind) { HH(h).cycle = kind; }
+int orc_mg_solve(void* h, const double* b, double* x, double tol, int maxit, double* hist, double* secs, int* iters) {
+    Hierarchy& H = HH(h);
+    const int64_t n = H.lv[0]->map.N;
+    vec xx, hh, ss;
+    const int st = mg_solve(H, V(b, n), xx, tol, maxit, hh, ss);
+    out(xx, x);
+    for (size_t k = 0; k < hh.size(); ++k) { hist[k] = hh[k]; secs[k] = ss[k]; }
+    *iters = static_cast<int>(hh.size());
+    return st;
+}
 
 void orc_apply(void* h, int l, int penalized, const double* x, double* y) {
     const Level& L = *HH(h).lv[l];

@@ -168,6 +168,7 @@ struct DevLevel {
     uint8_t* vk_mask[8] = {};
     uint8_t* vk_amask[8] = {};  // z-slab levels: owned slots per block (nullptr: all)
     double* xb = nullptr;         // ping-pong partner of x for the Vanka sweep
+    double *wb = nullptr, *wx = nullptr;  // W-cycle: rhs / correction of the second recursive call
     int32_t* vk_refresh = nullptr;  // slots every Vanka residual reads (refreshed x -> xb per sweep)
     int64_t vk_nrefresh = 0;
     int vk_n[8] = {};
@@ -242,6 +243,7 @@ void build(smg_ctx* c, const std::vector<double>* shared_coarse = nullptr, std::
     if (g.dim != 3) throw SmgError(SMG_EINVAL, "dim must be 3");
     if (p.levels < 1) throw SmgError(SMG_EINVAL, "levels < 1");
     if (p.nu < 1 || p.band_width < 1) throw SmgError(SMG_EINVAL, "nu and band_width must be >= 1");
+    if (p.cycle != 0 && p.cycle != 1) throw SmgError(SMG_EINVAL, "cycle must be 0 (V) or 1 (W)");
     if (!(g.h > 0)) throw SmgError(SMG_EINVAL, "h must be > 0");
     const int div = 1 << (p.levels - 1);
     if (g.nx % div || g.ny % div || g.nz % div)
@@ -283,6 +285,10 @@ void build(smg_ctx* c, const std::vector<double>* shared_coarse = nullptr, std::
         L.b = c->dalloc<double>(vl);
         L.r = c->dalloc<double>(vl);
         L.pd = c->dalloc<double>(L.k.g.fs);
+        if (p.cycle == 1 && l >= 2 && l + 1 < p.levels) {
+            L.wb = c->dalloc<double>(vl);
+            L.wx = c->dalloc<double>(vl);
+        }
         L.pd0 = c->dalloc<double>(L.k.g.fs);
         L.pd1 = c->dalloc<double>(L.k.g.fs);
         // Vanka blocks: band cells, slot + active-face mask, by colour
@@ -558,6 +564,13 @@ void vcycle(smg_ctx* c, int l, const double* b, double* x) {
     DevLevel& C = c->lv[l + 1];
     launch_restrict(L.k, C.k, L.r, C.b, c->st);
     vcycle(c, l + 1, C.b, C.x);
+    // W-cycle: second recursive call below the finest level, on the residual of
+    // the first (skipped when the child is the exact coarsest solve)
+    if (c->prm.cycle == 1 && l >= 1 && l + 2 < static_cast<int>(c->lv.size())) {
+        launch_apply(C.k, C.x, C.b, C.wb, C.k.gamma, c->st);
+        vcycle(c, l + 1, C.wb, C.wx);
+        launch_axpy(C.x, C.wx, 1.0, vlen(C), c->st);
+    }
     launch_prolong_add(L.k, C.k, C.x, x, c->st);
     smooth(c, l, x, b);
 }
@@ -1196,6 +1209,58 @@ int smg_vcycle(smg_ctx* c, const double* b, double* x) {
         upload(c, 0, b, F.b);
         vcycle(c, 0, F.b, F.x);
         download(c, 0, F.x, x);
+    });
+}
+
+int smg_mg_solve(smg_ctx* c, const double* b, double* x, double tol, int maxit, smg_history* hist, int* status) {
+    return guard(c, [&] {
+        if (!b || !x || !status) throw SmgError(SMG_EINVAL, "null argument");
+        if (c->nparts > 1) throw SmgError(SMG_EINVAL, "single-part entry point (use ngpu = 1)");
+        DevLevel& F = c->lv[0];
+        const int64_t n = vlen(F);
+        double* sc = c->dscal;
+        auto t0 = std::chrono::steady_clock::now();
+        const int64_t l0 = launch_count();
+        upload(c, 0, b, c->rhs);
+        CK(cudaEventRecord(c->ev0, c->st));
+        if (hist) hist->count = 0;
+        CK(cudaMemsetAsync(c->xs, 0, n * sizeof(double), c->st));
+        launch_cdot2(F.k.g, c->rhs, c->rhs, nullptr, nullptr, c->partials, sc + S_D0, c->st);
+        CK(cudaMemcpyAsync(c->hscal, sc, sizeof(double), cudaMemcpyDeviceToHost, c->st));
+        CK(cudaStreamSynchronize(c->st));
+        const double bnorm = std::sqrt(c->hscal[0]);
+        int st = SMG_MAX_ITERATIONS, iters = 0;
+        if (bnorm == 0.0) {
+            st = SMG_CONVERGED;
+        } else {
+            CK(cudaMemcpyAsync(F.b, c->rhs, n * sizeof(double), cudaMemcpyDeviceToDevice, c->st));  // r_0 = b
+            for (int j = 1; j <= maxit; ++j) {
+                vcycle(c, 0, F.b, F.x);                                 // e = cycle(r)
+                launch_axpy(c->xs, F.x, 1.0, n, c->st);                 // x += e
+                launch_apply(F.k, c->xs, c->rhs, F.b, F.k.gamma, c->st);  // r = b - L~ x
+                launch_cdot2(F.k.g, F.b, F.b, nullptr, nullptr, c->partials, sc + S_D0, c->st);
+                CK(cudaMemcpyAsync(c->hscal, sc, sizeof(double), cudaMemcpyDeviceToHost, c->st));
+                CK(cudaStreamSynchronize(c->st));
+                const double rel = std::sqrt(c->hscal[0]) / bnorm;
+                iters = j;
+                if (hist && hist->count < hist->capacity) {
+                    hist->rel_residual[hist->count] = rel;
+                    hist->seconds[hist->count] =
+                        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+                    hist->count++;
+                }
+                if (rel < tol) { st = SMG_CONVERGED; break; }
+            }
+        }
+        CK(cudaEventRecord(c->ev1, c->st));
+        CK(cudaEventSynchronize(c->ev1));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+        c->timing.solve_ms = ms;
+        c->timing.iterations = iters;
+        c->timing.kernel_launches = launch_count() - l0;
+        download(c, 0, c->xs, x);
+        *status = st;
     });
 }
 

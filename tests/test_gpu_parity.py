@@ -235,3 +235,34 @@ def test_resident_path_matches_e2e():
     t = s.timing()
     assert t["iterations"] == len(h2) and t["solve_ms"] > 0 and t["kernel_launches"] > 100
     s.close()
+
+
+@pytest.mark.parametrize("n,levels", [(32, 3), (64, 4)])
+def test_mg_solve_and_wcycle_bitwise(n, levels):
+    """SPEC:379-388 (mg_solve) and SPEC:395 (W-cycle) against the oracle, bit for bit."""
+    oracle.set_threads(os.cpu_count() or 1)
+    b = smg.forcing(n, seed=5)
+    for cyc in (0, 1):
+        o = oracle.Oracle(n, levels=levels, cycle=cyc)
+        s = smg.Solver(n, levels=levels, cycle=cyc)
+        xo, ho, _, sto = o.mg_solve(b, 1e-6, 60)
+        xg, hg, _, stg = s.mg_solve(b, 1e-6, 60)
+        assert sto == stg == smg.SMG_CONVERGED
+        assert np.array_equal(ho, hg) and np.array_equal(xo, xg)
+        xo, ho, _, _ = o.sqmr(b, 1e-6, 60)
+        xg, hg, _, _ = s.sqmr(b, 1e-6, 60)
+        assert np.array_equal(ho, hg) and np.array_equal(xo, xg)
+        s.close()
+
+
+def test_wcycle_symmetric_gpu():
+    s = smg.Solver(16, levels=4, cycle=1)  # 16 -> 8 -> 4 -> 2: W active at level 1
+    o = oracle.Oracle(16, levels=4, cycle=1)
+    n = s.ndof()
+    rng = np.random.default_rng(12)
+    for _ in range(3):
+        a, c = rng.standard_normal(n), rng.standard_normal(n)
+        wa, wc = s.vcycle(a), s.vcycle(c)
+        assert abs(c @ wa - a @ wc) <= 1e-11 * np.abs(c * wa).sum()
+        assert np.array_equal(wa, o.vcycle(a))
+    s.close()

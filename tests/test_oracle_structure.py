@@ -216,3 +216,20 @@ def test_commutativity_deep_interior():
         else:
             nonzero_edge += np.abs(top).max() > 1e-9
     assert bad_deep == 0 and nonzero_edge >= 1
+
+
+def test_wcycle_symmetric_and_mg_solve_converges():
+    # SPEC:392 (W-cycle) and SPEC:379-388 (mg_solve); the W-cycle's coarse correction
+    # 2C - C L~ C is symmetric whenever C is
+    oracle.set_threads(4)
+    o = oracle.Oracle(16, levels=4, cycle=1)  # W active at level 1 (child 4^3 is not the coarsest)
+    n = o.ndof()
+    rng = np.random.default_rng(11)
+    for _ in range(3):  # symmetry by random probes: a^T W c = c^T W a
+        a, c = rng.standard_normal(n), rng.standard_normal(n)
+        wa, wc = o.vcycle(a), o.vcycle(c)
+        assert abs(c @ wa - a @ wc) <= 1e-11 * np.abs(c * wa).sum()
+    b = o.forcing(oracle.FORCE_UNIFORM, 1)
+    x, h, _, st = o.mg_solve(b, 1e-6, 60)
+    assert st == oracle.ST_CONVERGED and np.all(np.diff(h) < 0)
+    assert np.isclose(np.linalg.norm(b - o.apply(x, penalized=True)) / np.linalg.norm(b), h[-1], rtol=1e-12)
