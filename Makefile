@@ -14,7 +14,12 @@ HOSTFLAGS := -O2 -std=c++17 -fPIC -ffp-contract=off -pthread -Wall -Wextra -I/us
 LIB := $(PKG)/libsmg.so
 OBJS := build/kernels.o build/host.o
 
-all: $(LIB) oracle
+CLI := $(PKG)/solver
+
+all: $(LIB) $(CLI) oracle
+
+$(CLI): $(CSRC)/cli.cpp include/smg.h $(LIB)
+	$(CXX) -O2 -std=c++17 -Wall -Wextra -o $@ $(CSRC)/cli.cpp -L$(PKG) -lsmg -Wl,-rpath,'$$ORIGIN'
 
 build:
 	mkdir -p build
@@ -32,7 +37,7 @@ oracle:
 	$(MAKE) -s -C oracle
 
 clean:
-	rm -rf build $(LIB)
+	rm -rf build $(LIB) $(CLI)
 	$(MAKE) -s -C oracle clean
 
 .PHONY: all oracle clean

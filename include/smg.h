@@ -87,6 +87,9 @@ typedef struct smg_timing {
 int smg_create(const smg_grid_desc* grid, const smg_params* params, int ngpu, const int* dev_ids,
                smg_ctx** out);
 void smg_destroy(smg_ctx* ctx);
+/* DOF census of the walled box (host only): out2 = {N, |V1|}; returns N
+ * (classify_dofs + partition_band counts; PAPER Table 1). */
+int64_t smg_census(const smg_grid_desc* grid, int band_width, int64_t* out2);
 /* z-slab plan (host only, no device needed): returns the number of leading
  * levels split over nparts (>= 1, or <= 0 if the grid cannot be split), and for
  * `rank` the first global plane z0[l] and plane count nzl[l] of every level

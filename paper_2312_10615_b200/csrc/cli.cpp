@@ -1,0 +1,184 @@
+// cli.cpp — `solver` command line above the C-ABI (the
+// reference's cli module restricted to the walled-box scenario of the hot path).
+//
+//   solver run <config.json>      solve; writes history_<method>.csv and summary.txt
+//   solver census <config.json>   prints "N V1 pct%" (PAPER Table 1 layout)
+//
+// RunConfig (JSON, flat): nx, ny, nz (cells), h (default 1/nx), eta (1e-3),
+// gamma (1e-3), levels, nu (1), band_width (1), cycle ("V"|"W"), method
+// ("mg-sqmr"|"mg"), tol (1e-8), maxit (200), forcing ("uniform"|"fourier"|
+// "channel"), seed (0), output_dir (env SMG_OUTPUT_DIR, else "."), devices ([0]).
+// Defaults follow SPEC:567-569.  Exit codes: 0 converged,
+// 2 not converged, 1 usage/config error.
+#include <cerrno>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <fstream>
+#include <map>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "../../include/smg.h"
+
+namespace {
+
+// Minimal JSON reader for one flat object of numbers, strings and number arrays.
+struct Config {
+    std::map<std::string, std::string> str;
+    std::map<std::string, double> num;
+    std::map<std::string, std::vector<double>> arr;
+};
+
+bool parse_json(const std::string& t, Config& c, std::string& err) {
+    size_t i = 0;
+    auto ws = [&] { while (i < t.size() && std::isspace(static_cast<unsigned char>(t[i]))) ++i; };
+    auto str = [&](std::string& out) {
+        if (t[i] != '"') return false;
+        ++i;
+        out.clear();
+        while (i < t.size() && t[i] != '"') out += t[i++];
+        if (i >= t.size()) return false;
+        ++i;
+        return true;
+    };
+    auto number = [&](double& v) {
+        const char* b = t.c_str() + i;
+        char* e = nullptr;
+        errno = 0;
+        v = std::strtod(b, &e);
+        if (e == b || errno) return false;
+        i += static_cast<size_t>(e - b);
+        return true;
+    };
+    ws();
+    if (i >= t.size() || t[i] != '{') { err = "expected '{'"; return false; }
+    ++i;
+    ws();
+    if (t[i] == '}') return true;
+    while (true) {
+        ws();
+        std::string key;
+        if (!str(key)) { err = "expected a quoted key"; return false; }
+        ws();
+        if (t[i] != ':') { err = "expected ':' after " + key; return false; }
+        ++i;
+        ws();
+        if (t[i] == '"') {
+            std::string v;
+            if (!str(v)) { err = "bad string for " + key; return false; }
+            c.str[key] = v;
+        } else if (t[i] == '[') {
+            ++i;
+            std::vector<double> a;
+            ws();
+            while (t[i] != ']') {
+                double v;
+                if (!number(v)) { err = "bad array for " + key; return false; }
+                a.push_back(v);
+                ws();
+                if (t[i] == ',') { ++i; ws(); }
+            }
+            ++i;
+            c.arr[key] = a;
+        } else {
+            double v;
+            if (!number(v)) { err = "bad value for " + key; return false; }
+            c.num[key] = v;
+        }
+        ws();
+        if (t[i] == ',') { ++i; continue; }
+        if (t[i] == '}') return true;
+        err = "expected ',' or '}'";
+        return false;
+    }
+}
+
+int usage() {
+    std::fprintf(stderr, "usage: solver run <config.json> | solver census <config.json>\n");
+    return 1;
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+    if (argc != 3) return usage();
+    const std::string cmd = argv[1];
+    std::ifstream f(argv[2]);
+    if (!f) { std::fprintf(stderr, "cannot read %s\n", argv[2]); return 1; }
+    std::stringstream ss;
+    ss << f.rdbuf();
+    Config c;
+    std::string err;
+    if (!parse_json(ss.str(), c, err)) { std::fprintf(stderr, "config error: %s\n", err.c_str()); return 1; }
+    auto num = [&](const char* k, double d) { return c.num.count(k) ? c.num[k] : d; };
+    auto str = [&](const char* k, const char* d) { return c.str.count(k) ? c.str[k] : std::string(d); };
+    if (!c.num.count("nx")) { std::fprintf(stderr, "config error: nx is required\n"); return 1; }
+    smg_grid_desc g{3, static_cast<int>(num("nx", 0)), 0, 0, 0.0};
+    g.ny = static_cast<int>(num("ny", g.nx));
+    g.nz = static_cast<int>(num("nz", g.nx));
+    g.h = num("h", 1.0 / g.nx);
+    const int bw = static_cast<int>(num("band_width", 1));
+    if (cmd == "census") {
+        int64_t out[2];
+        if (smg_census(&g, bw, out) < 0) { std::fprintf(stderr, "config error: bad grid\n"); return 1; }
+        std::printf("%lld %lld %.2f%%\n", static_cast<long long>(out[0]), static_cast<long long>(out[1]),
+                    100.0 * static_cast<double>(out[1]) / static_cast<double>(out[0]));
+        return 0;
+    }
+    if (cmd != "run") return usage();
+    smg_params p{num("eta", 1e-3), num("gamma", 1e-3), static_cast<int>(num("levels", 2)),
+                 static_cast<int>(num("nu", 1)), bw, 0, str("cycle", "V") == "W" ? 1 : 0};
+    const std::string method = str("method", "mg-sqmr");
+    if (method != "mg-sqmr" && method != "mg") { std::fprintf(stderr, "config error: method\n"); return 1; }
+    const std::string fk = str("forcing", "uniform");
+    const int kind = fk == "fourier" ? 1 : fk == "channel" ? 2 : 0;
+    const double tol = num("tol", 1e-8);
+    const int maxit = static_cast<int>(num("maxit", 200));
+    const char* envdir = std::getenv("SMG_OUTPUT_DIR");
+    const std::string dir = str("output_dir", envdir ? envdir : ".");
+    std::vector<int> devs;
+    for (double d : c.arr.count("devices") ? c.arr["devices"] : std::vector<double>{0}) devs.push_back(static_cast<int>(d));
+    smg_ctx* ctx = nullptr;
+    if (smg_create(&g, &p, static_cast<int>(devs.size()), devs.data(), &ctx) != SMG_OK) {
+        std::fprintf(stderr, "config error: smg_create failed\n");
+        return 1;
+    }
+    int64_t cnt[5];
+    const int64_t n = smg_level_ndof(ctx, 0, cnt);
+    std::vector<double> b(n), x(n), hist(maxit), secs(maxit), lx(n);
+    smg_forcing(&g, kind, static_cast<uint64_t>(num("seed", 0)), b.data(), 8);
+    smg_history h{maxit, 0, hist.data(), secs.data()};
+    int status = -1;
+    const auto t0 = std::chrono::steady_clock::now();
+    const int rc = method == "mg" ? smg_mg_solve(ctx, b.data(), x.data(), tol, maxit, &h, &status)
+                                  : smg_sqmr_solve(ctx, b.data(), x.data(), tol, maxit, &h, &status);
+    const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (rc != SMG_OK) {
+        std::fprintf(stderr, "solve failed: %s\n", smg_last_error(ctx));
+        smg_destroy(ctx);
+        return 1;
+    }
+    // ||B u||_inf from the continuity rows of L x
+    double bu = 0.0;
+    if (smg_apply(ctx, 0, 0, x.data(), lx.data()) == SMG_OK)
+        for (int64_t k = n - cnt[3]; k < n; ++k) bu = std::fmax(bu, std::fabs(lx[k]));
+    const std::string csv = dir + "/history_" + method + ".csv", sum = dir + "/summary.txt";
+    if (FILE* fo = std::fopen(csv.c_str(), "w")) {
+        std::fprintf(fo, "iteration,rel_residual,seconds\n");
+        for (int k = 0; k < h.count; ++k) std::fprintf(fo, "%d,%.17g,%.9g\n", k + 1, hist[k], secs[k]);
+        std::fclose(fo);
+    }
+    if (FILE* fo = std::fopen(sum.c_str(), "w")) {
+        std::fprintf(fo, "method: %s\nstatus: %s\niterations: %d\nfinal_rel_residual: %.17g\n"
+                         "div_u_inf: %.17g\nwall_seconds: %.6f\ndof: %lld\n",
+                     method.c_str(), status == SMG_CONVERGED ? "converged" : status == SMG_BREAKDOWN ? "breakdown" : "max-iterations",
+                     h.count, h.count ? hist[h.count - 1] : 0.0, bu, wall, static_cast<long long>(n));
+        std::fclose(fo);
+    }
+    smg_destroy(ctx);
+    return status == SMG_CONVERGED ? 0 : 2;
+}

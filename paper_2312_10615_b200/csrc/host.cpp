@@ -854,7 +854,6 @@ void dist_dot2(smg_ctx* m, double* (*a)(smg_ctx*), double* (*b)(smg_ctx*), doubl
 }
 
 double* v_q(smg_ctx* p) { return p->q; }
-double* v_d(smg_ctx* p) { return p->d; }
 double* v_xs(smg_ctx* p) { return p->xs; }
 double* v_rhs(smg_ctx* p) { return p->rhs; }
 double* v_s(smg_ctx* p) { return p->lv[0].b; }
@@ -1018,6 +1017,31 @@ void check_level(smg_ctx* c, int l) {
 extern "C" {
 
 const char* smg_version(void) { return "smg-b200 0.1 (sm_100a, fp64)"; }
+
+int64_t smg_census(const smg_grid_desc* grid, int band_width, int64_t* out2) {
+    if (!grid || grid->dim != 3 || band_width < 1 || grid->nx < 1 || grid->ny < 1 || grid->nz < 1) return SMG_EINVAL;
+    const int nx = grid->nx, ny = grid->ny, nz = grid->nz, bw = band_width;
+    auto band = [&](int x, int y, int z) {
+        return x < bw || y < bw || z < bw || x >= nx - bw || y >= ny - bw || z >= nz - bw;
+    };
+    int64_t n = 0, v1 = 0;
+    for (int z = 0; z < nz; ++z)
+        for (int y = 0; y < ny; ++y)
+            for (int x = 0; x < nx; ++x) {
+                const bool bc = band(x, y, z);
+                const int nf = (x >= 1) + (y >= 1) + (z >= 1);
+                n += nf + 1;
+                if (x >= 1 && (bc || band(x - 1, y, z))) ++v1;
+                if (y >= 1 && (bc || band(x, y - 1, z))) ++v1;
+                if (z >= 1 && (bc || band(x, y, z - 1))) ++v1;
+                if (bc) ++v1;
+            }
+    if (out2) {
+        out2[0] = n;
+        out2[1] = v1;
+    }
+    return n;
+}
 
 int smg_slab_plan(const smg_grid_desc* grid, int levels, int nparts, int rank, int* z0, int* nzl) {
     if (!grid || levels < 1 || nparts < 1 || rank < 0 || rank >= nparts) return SMG_EINVAL;

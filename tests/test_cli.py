@@ -1,0 +1,58 @@
+"""`solver` CLI above the C-ABI: census layout of PAPER Table 1,
+RunConfig errors -> exit 1, run -> history CSV + summary, exit 0/2."""
+import json
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+import paper_2312_10615_b200 as smg
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+CLI = os.path.join(ROOT, "paper_2312_10615_b200", "solver")
+
+
+def run(args, cfg=None, tmp=None):
+    path = None
+    if cfg is not None:
+        path = os.path.join(tmp, "cfg.json")
+        with open(path, "w") as f:
+            f.write(cfg if isinstance(cfg, str) else json.dumps(cfg))
+    return subprocess.run([CLI] + args + ([path] if path else []), capture_output=True, text=True, timeout=600)
+
+
+def test_census_table1(tmp_path):
+    r = run(["census"], {"nx": 128, "band_width": 1}, str(tmp_path))
+    assert r.returncode == 0 and r.stdout.strip() == "8339456 385580 4.62%"
+    n = smg.lib().smg_census(smg.GridDesc(3, 32, 32, 32, 1 / 32), 1, None)
+    assert n == 32 ** 3 + 3 * 32 * 32 * 31
+
+
+@pytest.mark.parametrize("cfg", ['{"nx": ', '{"ny": 8}', "not json"])
+def test_malformed_config_exit_1(tmp_path, cfg):
+    assert run(["census"], cfg, str(tmp_path)).returncode == 1
+
+
+def test_usage_exit_1():
+    assert subprocess.run([CLI], capture_output=True).returncode == 1
+
+
+@pytest.mark.gpu
+def test_run_writes_csv_and_summary(tmp_path):
+    cfg = {"nx": 32, "levels": 3, "eta": 1.0, "tol": 1e-6, "seed": 0, "output_dir": str(tmp_path)}
+    r = run(["run"], cfg, str(tmp_path))
+    assert r.returncode == 0, r.stderr
+    rows = open(tmp_path / "history_mg-sqmr.csv").read().splitlines()
+    assert rows[0] == "iteration,rel_residual,seconds"
+    h = np.array([float(x.split(",")[1]) for x in rows[1:]])
+    s = smg.Solver(32, levels=3, eta=1.0)
+    _, hp, _, _ = s.sqmr(smg.forcing(32, seed=0), 1e-6, 200)
+    assert np.array_equal(h, hp)  # same path, %.17g round-trips
+    summ = dict(l.split(": ") for l in open(tmp_path / "summary.txt").read().splitlines())
+    assert summ["status"] == "converged" and int(summ["iterations"]) == len(h)
+    assert float(summ["div_u_inf"]) < 1e-6
+    cfg.update(method="mg", maxit=2, tol=1e-12)
+    r = run(["run"], cfg, str(tmp_path))
+    assert r.returncode == 2  # not converged
+    assert len(open(tmp_path / "history_mg.csv").read().splitlines()) == 3
