@@ -1000,13 +1000,18 @@ __global__ void __launch_bounds__(512) k_smooth_smem(LevelK L, double* __restric
 // cheaper than a grid barrier), threads mapped onto the cells of the phase's
 // colour only, so every thread works and only the needed rows are touched.
 // Per-cell arithmetic is shared with the kernels above (bit-identical).
+// ZC independent cells per thread (planes z, z + gridDim.z, ...): more loads in flight
+template <int ZC>
 __global__ void __launch_bounds__(256) k_dgs_vel_c(LevelK L, double* __restrict__ X, const double* __restrict__ B,
                                                    int colour) {
     const Geom& g = L.g;
-    const int i = blockIdx.x * 32 + threadIdx.x, y = blockIdx.y * 8 + threadIdx.y, z = blockIdx.z;
-    const int x = 2 * i + ((y + g.gz(z) + colour) & 1);
-    if (x >= g.nx || y >= g.ny) return;
-    dgs_vel_cell(L, X, B, x, y, z);
+    const int i = blockIdx.x * 32 + threadIdx.x, y = blockIdx.y * 8 + threadIdx.y;
+#pragma unroll
+    for (int q = 0; q < ZC; ++q) {
+        const int z = blockIdx.z + q * gridDim.z;
+        const int x = 2 * i + ((y + g.gz(z) + colour) & 1);
+        if (x < g.nx && y < g.ny && z < g.nz) dgs_vel_cell(L, X, B, x, y, z);
+    }
 }
 
 __device__ __forceinline__ bool half_cell(const Geom& g, int c, int i, int j, int k, int& x, int& y, int& z) {
@@ -1073,13 +1078,16 @@ __global__ void __launch_bounds__(256) k_dgs_pf_apply_c(LevelK L, double* __rest
     }
 }
 
+template <int ZC>
 __global__ void __launch_bounds__(256) k_dgs_pf_lazy_c(LevelK L, double* __restrict__ X, const double* __restrict__ B,
                                                        double* __restrict__ D, int c) {
     const Geom& g = L.g;
-    const int i = blockIdx.x * 32 + threadIdx.x, j = blockIdx.y * 8 + threadIdx.y, k = blockIdx.z;
-    int x, y, z;
-    if (!half_cell(g, c, i, j, k, x, y, z)) return;
-    pf_lazy_cell(L, X, B, D, x, y, z);
+    const int i = blockIdx.x * 32 + threadIdx.x, j = blockIdx.y * 8 + threadIdx.y;
+#pragma unroll
+    for (int q = 0; q < ZC; ++q) {
+        int x, y, z;
+        if (half_cell(g, c, i, j, blockIdx.z + q * gridDim.z, x, y, z)) pf_lazy_cell(L, X, B, D, x, y, z);
+    }
 }
 
 __global__ void __launch_bounds__(256) k_dgs_pf_flush(LevelK L, double* __restrict__ X, const double* __restrict__ D) {
@@ -1088,13 +1096,17 @@ __global__ void __launch_bounds__(256) k_dgs_pf_flush(LevelK L, double* __restri
     pending_gathers(L, X, D, c.x, c.y, c.z, true);
 }
 
+template <int ZC>
 __global__ void __launch_bounds__(256) k_dgs_prev_c(LevelK L, double* __restrict__ X, const double* __restrict__ B,
                                                     int c) {
     const Geom& g = L.g;
-    const int i = blockIdx.x * 32 + threadIdx.x, j = blockIdx.y * 8 + threadIdx.y, k = blockIdx.z;
-    int x, y, z;
-    if (!half_cell(g, c, i, j, k, x, y, z) || band_cell(L, x, y, z)) return;
-    dgs_prev_cell(L, X, B, g.slot(x, y, z));
+    const int i = blockIdx.x * 32 + threadIdx.x, j = blockIdx.y * 8 + threadIdx.y;
+#pragma unroll
+    for (int q = 0; q < ZC; ++q) {
+        int x, y, z;
+        if (half_cell(g, c, i, j, blockIdx.z + q * gridDim.z, x, y, z) && !band_cell(L, x, y, z))
+            dgs_prev_cell(L, X, B, g.slot(x, y, z));
+    }
 }
 
 // ------------------------------------------------ SQMR device scalars ------
@@ -1404,7 +1416,7 @@ static dim3 dgs_grid_h(const Geom& g) {
     return dim3((((g.nx + 1) / 2) + 31) / 32, (((g.ny + 1) / 2) + 7) / 8, (g.nz + 1) / 2);
 }
 void launch_dgs_vel_c(const LevelK& L, double* x, const double* b, int colour, cudaStream_t s) {
-    k_dgs_vel_c<<<dgs_grid_v(L.g), dim3(32, 8), 0, s>>>(L, x, b, colour);
+    k_dgs_vel_c<1><<<dgs_grid_v(L.g), dim3(32, 8), 0, s>>>(L, x, b, colour);
     count();
 }
 void launch_dgs_pf_delta_c(const LevelK& L, const double* x, const double* b, double* d, int c, cudaStream_t s) {
@@ -1416,32 +1428,42 @@ void launch_dgs_pf_apply_c(const LevelK& L, double* x, const double* d, int c, c
     count();
 }
 void launch_dgs_prev_c(const LevelK& L, double* x, const double* b, int c, cudaStream_t s) {
-    k_dgs_prev_c<<<dgs_grid_h(L.g), dim3(32, 8), 0, s>>>(L, x, b, c);
+    k_dgs_prev_c<1><<<dgs_grid_h(L.g), dim3(32, 8), 0, s>>>(L, x, b, c);
     count();
 }
 
 // Per-phase launches of a symmetric DGS sweep (same phase numbering and
 // delta-buffer protocol as k_dgs_sym_coop).
-static void launch_dgs_sym_phases(const LevelK& L, double* x, const double* b, double* d0, double* d1, int nph,
-                                  cudaStream_t s) {
-    (void)d1;
+template <int ZC>
+static void dgs_sym_phases_zc(const LevelK& L, double* x, const double* b, double* d0, int nph, cudaStream_t s) {
     const Geom& g = L.g;
     const dim3 blk(32, 8);
-    const dim3 gv = dgs_grid_v(g), gh = dgs_grid_h(g);
+    dim3 gv = dgs_grid_v(g), gh = dgs_grid_h(g);
+    gv.z = (gv.z + ZC - 1) / ZC;
+    gh.z = (gh.z + ZC - 1) / ZC;
     for (int ph = 0; ph < nph; ++ph) {
         if (ph == 0 || ph == 1 || ph == 18 || ph == 19) {
-            k_dgs_vel_c<<<gv, blk, 0, s>>>(L, x, b, ph < 2 ? ph : 19 - ph);
+            k_dgs_vel_c<ZC><<<gv, blk, 0, s>>>(L, x, b, ph < 2 ? ph : 19 - ph);
         } else if (ph <= 9) {
-            k_dgs_pf_lazy_c<<<gh, blk, 0, s>>>(L, x, b, d0, ph - 2);
+            k_dgs_pf_lazy_c<ZC><<<gh, blk, 0, s>>>(L, x, b, d0, ph - 2);
             if (ph == 9) {
                 k_dgs_pf_flush<<<cell_grid(g), blk, 0, s>>>(L, x, d0);
                 count();
             }
         } else {
-            k_dgs_prev_c<<<gh, blk, 0, s>>>(L, x, b, 17 - ph);
+            k_dgs_prev_c<ZC><<<gh, blk, 0, s>>>(L, x, b, 17 - ph);
         }
         count();
     }
+}
+
+static void launch_dgs_sym_phases(const LevelK& L, double* x, const double* b, double* d0, double* d1, int nph,
+                                  cudaStream_t s) {
+    (void)d1;
+    const int zc = env_int("SMG_DGS_ZC", 2);
+    if (zc >= 4) dgs_sym_phases_zc<4>(L, x, b, d0, nph, s);
+    else if (zc == 2) dgs_sym_phases_zc<2>(L, x, b, d0, nph, s);
+    else dgs_sym_phases_zc<1>(L, x, b, d0, nph, s);
 }
 
 void launch_dgs_sym_coop(const LevelK& L, double* x, const double* b, double* d0, double* d1, int nph,
