@@ -1460,7 +1460,9 @@ static void dgs_sym_phases_zc(const LevelK& L, double* x, const double* b, doubl
 static void launch_dgs_sym_phases(const LevelK& L, double* x, const double* b, double* d0, double* d1, int nph,
                                   cudaStream_t s) {
     (void)d1;
-    const int zc = env_int("SMG_DGS_ZC", 2);
+    // two cells per thread only pays on the largest levels (>= 128^3 cells); smaller levels need blocks
+    const int64_t ncell = static_cast<int64_t>(L.g.nx) * L.g.ny * L.g.nz;
+    const int zc = env_int("SMG_DGS_ZC", ncell >= (int64_t(1) << 21) ? 2 : 1);
     if (zc >= 4) dgs_sym_phases_zc<4>(L, x, b, d0, nph, s);
     else if (zc == 2) dgs_sym_phases_zc<2>(L, x, b, d0, nph, s);
     else dgs_sym_phases_zc<1>(L, x, b, d0, nph, s);
