@@ -266,3 +266,18 @@ def test_wcycle_symmetric_gpu():
         assert abs(c @ wa - a @ wc) <= 1e-11 * np.abs(c * wa).sum()
         assert np.array_equal(wa, o.vcycle(a))
     s.close()
+
+
+@pytest.mark.parametrize("nu,bw,eta,gamma", [(2, 1, 1.0, 1e-3), (3, 1, 1.0, 1e-3), (1, 2, 1.0, 1e-3),
+                                             (1, 1, 1e-3, 1e-3), (2, 2, 0.5, 1e-2)])
+def test_parameter_sweep_bitwise(nu, bw, eta, gamma):
+    """SPEC AC 3 parameter range (nu in {1,2,3}), band width, eta/gamma: whole solve bit-identical."""
+    oracle.set_threads(os.cpu_count() or 1)
+    o = oracle.Oracle(32, levels=3, nu=nu, band_width=bw, eta=eta, gamma=gamma)
+    s = smg.Solver(32, levels=3, nu=nu, band_width=bw, eta=eta, gamma=gamma)
+    b = o.forcing(oracle.FORCE_UNIFORM, 9)
+    assert np.array_equal(s.vcycle(b), o.vcycle(b))
+    xo, ho, _, sto = o.sqmr(b, 1e-6, 100)
+    xg, hg, _, stg = s.sqmr(b, 1e-6, 100)
+    assert sto == stg and np.array_equal(ho, hg) and np.array_equal(xo, xg)
+    s.close()
