@@ -541,6 +541,11 @@ void vanka_sym_coop(smg_ctx* c, int l, double* x, const double* b) {
 
 void smooth(smg_ctx* c, int l, double* x, const double* b) {
     DevLevel& L = c->lv[l];
+    if (smooth_dsm_fits(L.k, L.vk_n)) {
+        const int nph = (c->prm.flags & SMG_FLAG_SKIP_REVERSE_DGS) ? kDgsPhases / 2 : kDgsPhases;
+        launch_smooth_dsm(L.k, x, b, L.vk_cells, L.vk_mask, L.vk_n, L.ktab, c->prm.nu, nph, c->st);
+        return;
+    }
     if (smooth_smem_fits(L.k)) {
         const int nph = (c->prm.flags & SMG_FLAG_SKIP_REVERSE_DGS) ? kDgsPhases / 2 : kDgsPhases;
         launch_smooth_smem(L.k, x, b, L.vk_cells, L.vk_mask, L.vk_n, L.ktab, L.pd0, L.pd1, c->prm.nu, nph, c->st);

@@ -62,8 +62,8 @@ __device__ __forceinline__ bool band_cell(const LevelK& L, int x, int y, int z) 
 // Momentum row of L~ at the face stored at slot i of field F (stride of the
 // normal axis sn): eta/h^2 (6 u - sum of 6 neighbours, order x-,x+,y-,y+,z-,z+)
 // + (p_right - p_left)/h.
-__device__ __forceinline__ double mom(const LevelK& L, const double* __restrict__ F,
-                                      const double* __restrict__ P, int64_t i, int64_t sn) {
+template <class AF, class AP>
+__device__ __forceinline__ double mom(const LevelK& L, AF F, AP P, int64_t i, int64_t sn) {
     const int64_t sy = L.g.sy, sz = L.g.sz;
     double s = F[i - 1] + F[i + 1];
     s = s + F[i - sy];
@@ -75,9 +75,8 @@ __device__ __forceinline__ double mom(const LevelK& L, const double* __restrict_
 }
 
 // Continuity row of L~ at cell slot i: -(div u)/h - gamma p.
-__device__ __forceinline__ double cont(const LevelK& L, const double* __restrict__ U,
-                                       const double* __restrict__ V, const double* __restrict__ W,
-                                       const double* __restrict__ P, int64_t i, double gamma) {
+template <class AU, class AV, class AW, class AP>
+__device__ __forceinline__ double cont(const LevelK& L, AU U, AV V, AW W, AP P, int64_t i, double gamma) {
     const double div = (U[i + 1] - U[i]) + (V[i + L.g.sy] - V[i]) + (W[i + L.g.sz] - W[i]);
     return -div * L.inv_h - gamma * P[i];
 }
@@ -593,8 +592,8 @@ __global__ void __launch_bounds__(512) k_vanka_sym_coop(LevelK L, double* __rest
 // and owns DOF s; delta_s = sum_q K[s][q] r_q gathers r_q by warp shuffles in
 // ascending q (same order as the oracle).  Each thread holds at most CPT
 // (own, delta) pairs across the barrier.
-template <int MODE, int CPT>
-__device__ __forceinline__ void vanka_sweeps8(const LevelK& L, double* __restrict__ X, const double* __restrict__ B,
+template <int MODE, int CPT, class AX = double*>
+__device__ __forceinline__ void vanka_sweeps8(const LevelK& L, AX X, const double* __restrict__ B,
                                               const VankaLists& vl, const double* __restrict__ Ks, int nu, int tid,
                                               int nth) {
     const Geom& g = L.g;
@@ -640,7 +639,7 @@ __device__ __forceinline__ void vanka_sweeps8(const LevelK& L, double* __restric
                 }
                 double r = 0.0;
                 if (act && s8 < 7) {
-                    const double *U = X, *V = X + fs, *W = X + 2 * fs, *P = X + 3 * fs;
+                    const auto U = X, V = X + fs, W = X + 2 * fs, P = X + 3 * fs;
                     switch (s8) {
                         case 0: r = (m & 1) ? B[i] - mom(L, U, P, i, 1) : 0.0; break;
                         case 1: r = (m & 2) ? B[i + 1] - mom(L, U, P, i + 1, 1) : 0.0; break;
@@ -797,12 +796,11 @@ __global__ void __launch_bounds__(512) k_vanka8(LevelK L, double* __restrict__ X
     vanka_sweeps8<MODE, CPT>(L, X, B, vl, Ks, nu, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
 }
 
-__device__ __forceinline__ void dgs_vel_cell(const LevelK& L, double* __restrict__ X, const double* __restrict__ B,
-                                             int x, int y, int z) {
+template <class AX>
+__device__ __forceinline__ void dgs_vel_cell(const LevelK& L, AX X, const double* __restrict__ B, int x, int y, int z) {
     const Geom& g = L.g;
     const int64_t fs = g.fs, i = g.slot(x, y, z);
-    double *U = X, *V = X + fs, *W = X + 2 * fs;
-    const double* P = X + 3 * fs;
+    const auto U = X, V = X + fs, W = X + 2 * fs, P = X + 3 * fs;
     const bool here = band_cell(L, x, y, z);
     if (x >= 1 && !here && !band_cell(L, x - 1, y, z)) {
         const double r = B[i] - mom(L, U, P, i, 1);
@@ -818,12 +816,11 @@ __device__ __forceinline__ void dgs_vel_cell(const LevelK& L, double* __restrict
     }
 }
 
-__device__ __forceinline__ void dgs_prev_cell(const LevelK& L, double* __restrict__ X, const double* __restrict__ B,
-                                              int64_t i) {
+template <class AX>
+__device__ __forceinline__ void dgs_prev_cell(const LevelK& L, AX X, const double* __restrict__ B, int64_t i) {
     const Geom& g = L.g;
     const int64_t fs = g.fs, sy = g.sy, sz = g.sz;
-    const double *U = X, *V = X + fs, *W = X + 2 * fs;
-    double* P = X + 3 * fs;
+    const auto U = X, V = X + fs, W = X + 2 * fs, P = X + 3 * fs;
     const double *BU = B, *BV = B + fs, *BW = B + 2 * fs, *BP = B + 3 * fs;
     const double ruL = BU[i] - mom(L, U, P, i, 1);
     const double ruR = BU[i + 1] - mom(L, U, P, i + 1, 1);
@@ -865,8 +862,8 @@ __device__ __forceinline__ bool colour_cell(const Geom& g, int c, int64_t t, int
 // additions in the same order, hence bit-identical.  One combined delta buffer
 // holds delta_c at the V2 cells of colour c (band cells stay 0); a gather from
 // phase c' masks the neighbour sum to colour-c' cells.
-__device__ __forceinline__ double masked_nbr_sum(const Geom& g, const double* __restrict__ D, int64_t i, int x, int y,
-                                                 int zg, int cc) {
+template <class AD>
+__device__ __forceinline__ double masked_nbr_sum(const Geom& g, AD D, int64_t i, int x, int y, int zg, int cc) {
     // neighbour colours: x +-1 flips bit 1, y +-1 bit 2, z +-1 bit 4 of colour (x,y,zg)
     const int ck = (x & 1) + 2 * (y & 1) + 4 * (zg & 1);
     const bool mx = (ck ^ 1) == cc, my = (ck ^ 2) == cc, mz = (ck ^ 4) == cc;
@@ -878,8 +875,8 @@ __device__ __forceinline__ double masked_nbr_sum(const Geom& g, const double* __
     return s;
 }
 
-__device__ __forceinline__ void pending_gathers(const LevelK& L, double* __restrict__ X, const double* __restrict__ D,
-                                                int x, int y, int z, bool later) {
+template <class AX, class AD>
+__device__ __forceinline__ void pending_gathers(const LevelK& L, AX X, AD D, int x, int y, int z, bool later) {
     const Geom& g = L.g;
     const int zg = g.gz(z);
     const int k = (x & 1) + 2 * (y & 1) + 4 * (zg & 1);
@@ -898,8 +895,9 @@ __device__ __forceinline__ void pending_gathers(const LevelK& L, double* __restr
     }
 }
 
-__device__ __forceinline__ void pf_lazy_cell(const LevelK& L, double* __restrict__ X, const double* __restrict__ B,
-                                             double* __restrict__ D, int x, int y, int z) {
+template <class AX, class AD>
+__device__ __forceinline__ void pf_lazy_cell(const LevelK& L, AX X, const double* __restrict__ B, AD D, int x, int y,
+                                             int z) {
     const Geom& g = L.g;
     pending_gathers(L, X, D, x, y, z, false);
     if (band_cell(L, x, y, z)) return;
@@ -926,10 +924,9 @@ __device__ __forceinline__ void pf_lazy_cell(const LevelK& L, double* __restrict
 // pressure colour c uses delta buffer D[c&1]; its delta step also clears the
 // entries of colour c-2 left in that buffer, so only colour-c entries are
 // non-zero when the apply step gathers.
-template <int MODE>
-__device__ __forceinline__ void dgs_sweep(const LevelK& L, double* __restrict__ X, const double* __restrict__ B,
-                                          double* __restrict__ D0, double* __restrict__ D1, int nph, int64_t tid,
-                                          int64_t nth) {
+template <int MODE, class AX = double*, class AD = double*>
+__device__ __forceinline__ void dgs_sweep(const LevelK& L, AX X, const double* __restrict__ B, AD D0, AD D1, int nph,
+                                          int64_t tid, int64_t nth) {
     const Geom& g = L.g;
     const int64_t ncell = static_cast<int64_t>(g.nx) * g.ny * g.nz;
     const int64_t nxy = static_cast<int64_t>(g.nx) * g.ny;
@@ -993,6 +990,55 @@ __global__ void __launch_bounds__(512) k_smooth_smem(LevelK L, double* __restric
     __syncthreads();
     vanka_sweeps<2, 1>(L, X, B, vl, Ks, nu, threadIdx.x, blockDim.x);
     for (int64_t k = threadIdx.x; k < nv; k += blockDim.x) Xg[k] = X[k];
+}
+
+// ------------------------------- cluster-resident (DSMEM) smoother -------------
+// Levels whose vector plus DGS delta field fit in the distributed shared memory
+// of one 16-CTA cluster: the linear vector index k lives in CTA k >> 14 at
+// offset k & 16383 (128 KB per CTA).  The whole Alg. 3 smooth then runs with
+// cluster barriers only and every x/delta access is an SM-to-SM DSMEM access
+// (no L2 round trips, no global fences).  b stays in global memory (read-only).
+constexpr int kDsmLog = 14;
+constexpr int kDsmChunk = 1 << kDsmLog;
+constexpr int kDsmCTAs = 16;
+
+struct DAcc {
+    double* const* bases;  // generic addresses of the 16 CTAs' chunks (in shared memory)
+    int64_t off;
+    __device__ __forceinline__ double& operator[](int64_t i) const {
+        const int64_t k = i + off;
+        return bases[k >> kDsmLog][k & (kDsmChunk - 1)];
+    }
+    __device__ __forceinline__ DAcc operator+(int64_t d) const { return DAcc{bases, off + d}; }
+};
+
+__global__ void __launch_bounds__(512) k_smooth_dsm(LevelK L, double* __restrict__ Xg, const double* __restrict__ B,
+                                                    VankaLists vl, const double* __restrict__ ktab, int nu, int nph) {
+    extern __shared__ double dsm[];
+    double* Ks = dsm;
+    double* chunk = dsm + 64 * 49;
+    double** bases = reinterpret_cast<double**>(chunk + kDsmChunk);
+    cg::cluster_group cl = cg::this_cluster();
+    const int rank = static_cast<int>(cl.block_rank()), nct = static_cast<int>(cl.num_blocks());
+    if (threadIdx.x < static_cast<unsigned>(nct)) bases[threadIdx.x] = cl.map_shared_rank(chunk, threadIdx.x);
+    for (int k = threadIdx.x; k < 64 * 49; k += blockDim.x) Ks[k] = ktab[k];
+    const int64_t nv = 4 * L.g.fs;  // x, then the delta field (one field) at [nv, nv + fs)
+    for (int k = threadIdx.x; k < kDsmChunk; k += blockDim.x) {
+        const int64_t idx = static_cast<int64_t>(rank) * kDsmChunk + k;
+        chunk[k] = idx < nv ? Xg[idx] : 0.0;
+    }
+    cl.sync();
+    const DAcc X{bases, 0}, D{bases, nv};
+    const int tid = rank * blockDim.x + threadIdx.x, nth = nct * blockDim.x;
+    vanka_sweeps8<1, 1, DAcc>(L, X, B, vl, Ks, nu, tid, nth);
+    dgs_sweep<1, DAcc, DAcc>(L, X, B, D, D, nph, tid, nth);
+    cl.sync();
+    vanka_sweeps8<1, 1, DAcc>(L, X, B, vl, Ks, nu, tid, nth);
+    cl.sync();
+    for (int k = threadIdx.x; k < kDsmChunk; k += blockDim.x) {
+        const int64_t idx = static_cast<int64_t>(rank) * kDsmChunk + k;
+        if (idx < nv) Xg[idx] = chunk[k];
+    }
 }
 
 // -------------------------------------- colour-compact per-phase DGS kernels ------
@@ -1388,6 +1434,43 @@ void launch_vanka_sym_coop(const LevelK& L, double* x, const double* b, const in
                 launch_vanka_apply(L, x, cells[col], masks[col], n[col], delta, s);
             }
     }
+}
+
+bool smooth_dsm_fits(const LevelK& L, const int* n) {
+    int maxn = 0;
+    for (int c = 0; c < 8; ++c) maxn = n[c] > maxn ? n[c] : maxn;
+    return env_int("SMG_NO_DSM_SMOOTH", 0) == 0 && 5 * L.g.fs <= static_cast<int64_t>(kDsmCTAs) * kDsmChunk &&
+           8 * static_cast<int64_t>(maxn) <= static_cast<int64_t>(kDsmCTAs) * 512;
+}
+
+void launch_smooth_dsm(const LevelK& L, double* x, const double* b, const int32_t* const* cells,
+                       const uint8_t* const* masks, const int* n, const double* ktab, int nu, int nph,
+                       cudaStream_t s) {
+    VankaLists vl;
+    for (int c = 0; c < 8; ++c) {
+        vl.cells[c] = cells[c];
+        vl.masks[c] = masks[c];
+        vl.n[c] = n[c];
+    }
+    const size_t smem = (64 * 49 + kDsmChunk) * sizeof(double) + kDsmCTAs * sizeof(double*);
+    note(cudaFuncSetAttribute(k_smooth_dsm, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    note(cudaFuncSetAttribute(k_smooth_dsm, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    cfg.gridDim = dim3(kDsmCTAs);
+    cfg.blockDim = dim3(512);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = kDsmCTAs;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    LevelK Lc = L;
+    void* args[] = {&Lc, &x, const_cast<double**>(&b), &vl, const_cast<double**>(&ktab), &nu, &nph};
+    note(cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(k_smooth_dsm), args));
+    count();
 }
 
 bool smooth_smem_fits(const LevelK& L) {

@@ -90,6 +90,12 @@ void launch_vanka_sym_coop(const LevelK& L, double* x, const double* b, const in
                            int64_t nrefresh = 0);
 void launch_dgs_sym_coop(const LevelK& L, double* x, const double* b, double* d0, double* d1, int nph,
                          cudaStream_t s);
+// Whole smooth (Alg. 3) of a level held in the distributed shared memory of one
+// 16-CTA cluster (vector + DGS delta <= 2 MB).
+bool smooth_dsm_fits(const LevelK& L, const int* n);
+void launch_smooth_dsm(const LevelK& L, double* x, const double* b, const int32_t* const* cells,
+                       const uint8_t* const* masks, const int* n, const double* ktab, int nu, int nph,
+                       cudaStream_t s);
 // Whole smooth (Alg. 3) of a level small enough for one CTA's shared memory.
 bool smooth_smem_fits(const LevelK& L);
 void launch_smooth_smem(const LevelK& L, double* x, const double* b, const int32_t* const* cells,
