@@ -1439,7 +1439,9 @@ void launch_vanka_sym_coop(const LevelK& L, double* x, const double* b, const in
 bool smooth_dsm_fits(const LevelK& L, const int* n) {
     int maxn = 0;
     for (int c = 0; c < 8; ++c) maxn = n[c] > maxn ? n[c] : maxn;
-    return env_int("SMG_NO_DSM_SMOOTH", 0) == 0 && 5 * L.g.fs <= static_cast<int64_t>(kDsmCTAs) * kDsmChunk &&
+    // opt-in: measured slower than the L2-resident kernels on B200 (remote DSMEM loads through the
+    // accessor, 126 registers -> 16 warps per SM): 32^3 smooth 0.67 ms vs 0.30 ms
+    return env_int("SMG_DSM_SMOOTH", 0) == 1 && 5 * L.g.fs <= static_cast<int64_t>(kDsmCTAs) * kDsmChunk &&
            8 * static_cast<int64_t>(maxn) <= static_cast<int64_t>(kDsmCTAs) * 512;
 }
 

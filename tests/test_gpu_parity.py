@@ -281,3 +281,17 @@ def test_parameter_sweep_bitwise(nu, bw, eta, gamma):
     xg, hg, _, stg = s.sqmr(b, 1e-6, 100)
     assert sto == stg and np.array_equal(ho, hg) and np.array_equal(xo, xg)
     s.close()
+
+
+def test_dsm_smoother_bitwise(monkeypatch):
+    """Opt-in cluster-resident (DSMEM) smoother: same arithmetic, bit-identical."""
+    monkeypatch.setenv("SMG_DSM_SMOOTH", "1")
+    oracle.set_threads(4)
+    for n, lv in ((16, 2), (32, 3)):
+        o = oracle.Oracle(n, levels=lv)
+        s = smg.Solver(n, levels=lv)
+        b = o.forcing(oracle.FORCE_UNIFORM, 3)
+        x = np.random.default_rng(n).uniform(-1, 1, o.ndof())
+        same(s.smoother(smg.OP_SMOOTH, x, b), o.smoother(4, x, b))
+        assert np.array_equal(s.vcycle(b), o.vcycle(b))
+        s.close()
