@@ -688,27 +688,22 @@ __device__ __forceinline__ void vanka_sweeps_pp(const LevelK& L, double* __restr
     const int64_t offs = s8 == 0 ? 0 : s8 == 1 ? 1 : s8 == 2 ? fs : s8 == 3 ? fs + sy : s8 == 4 ? 2 * fs
                          : s8 == 5 ? 2 * fs + sz : 3 * fs;
     constexpr bool kPre = CPT == 1;
-    // per colour: slot << 14 | neighbour-band mask << 7 | face mask, loaded once
     int64_t pre[8];
     if (kPre)
 #pragma unroll
         for (int c = 0; c < 8; ++c)
-            pre[c] = grp < vl.n[c] ? ((static_cast<int64_t>(vl.cells[c][grp]) << 14) |
-                                      (static_cast<int64_t>(vl.nbm[c][grp]) << 7) | vl.masks[c][grp])
-                                   : -1;
-    auto block_of = [&](int c, int t, int64_t& i, int& m, int& nb) {
+            pre[c] = grp < vl.n[c] ? ((static_cast<int64_t>(vl.cells[c][grp]) << 7) | vl.masks[c][grp]) : -1;
+    auto block_of = [&](int c, int t, int64_t& i, int& m) {
         if (kPre) {
             int64_t e = 0;
 #pragma unroll
             for (int q = 0; q < 8; ++q)
                 if (q == c) e = pre[q];
-            i = e >> 14;
-            nb = static_cast<int>((e >> 7) & 127);
+            i = e >> 7;
             m = static_cast<int>(e & 127);
         } else {
             i = vl.cells[c][t];
             m = vl.masks[c][t];
-            nb = vl.nbm[c][t];
         }
     };
     const int nph = 16 * nu;
@@ -725,8 +720,8 @@ __device__ __forceinline__ void vanka_sweeps_pp(const LevelK& L, double* __restr
             const int t = grp + j * groups;
             const bool act = t < n;
             int64_t i = 0;
-            int m = 0, nbu = 0;
-            if (act) block_of(col, t, i, m, nbu);
+            int m = 0;
+            if (act) block_of(col, t, i, m);
             double r = 0.0, own = 0.0;
             if (act && s8 < 7) {
                 const double *U = Xc, *V = Xc + fs, *W = Xc + 2 * fs, *P = Xc + 3 * fs;
@@ -754,10 +749,11 @@ __device__ __forceinline__ void vanka_sweeps_pp(const LevelK& L, double* __restr
             // shared with a band cell of the current colour (colours one parity bit apart)
             if (pcol >= 0 && pcol != col && t < vl.n[pcol] && s8 < 7) {
                 int64_t ip;
-                int mp, nbp;
-                block_of(pcol, t, ip, mp, nbp);
+                int mp;
+                block_of(pcol, t, ip, mp);
                 bool carry = s8 == 6 || (mp & (1 << s8));
-                if (carry && s8 < 6 && (pcol ^ (1 << (s8 >> 1))) == col && (nbp & (1 << s8))) carry = false;
+                if (carry && s8 < 6 && (pcol ^ (1 << (s8 >> 1))) == col && (vl.nbm[pcol][t] & (1 << s8)))
+                    carry = false;
                 if (carry) Xn[ip + offs] = Xc[ip + offs];
             }
         }
