@@ -1377,7 +1377,7 @@ template <int CPT>
 static void launch_vanka_pp(bool cl, int64_t threads, void** args, cudaStream_t s) {
     // small blocks: the per-phase work is instruction-bound, spread it over every SM
     launch_sweep(reinterpret_cast<const void*>(k_vanka_pp<0, CPT>), reinterpret_cast<const void*>(k_vanka_pp<1, CPT>),
-                 cl, threads, args, s, env_int("SMG_VANKA_THREADS", 512));
+                 cl, threads, args, s, env_int("SMG_VANKA_THREADS", 128));
 }
 
 void launch_vanka_sym_coop(const LevelK& L, double* x, const double* b, const int32_t* const* cells,
@@ -1406,7 +1406,7 @@ void launch_vanka_sym_coop(const LevelK& L, double* x, const double* b, const in
         return threads * cpt >= lanes;
     };
     auto fits = [&](const void* fn, int cpt) { return fits_bt(fn, cpt, coop_threads()); };
-    const int ppt = env_int("SMG_VANKA_THREADS", 512);
+    const int ppt = env_int("SMG_VANKA_THREADS", 128);
     auto fits_pp = [&](const void* fn, int cpt) { return fits_bt(fn, cpt, ppt); };
     bool done = true;
     if (xb && nbm && !cl && env_int("SMG_VANKA_PP", 1)) {  // ping-pong (grid mode): one barrier per phase
