@@ -167,7 +167,6 @@ struct DevLevel {
     int32_t* vk_cells[8] = {};
     uint8_t* vk_mask[8] = {};
     uint8_t* vk_amask[8] = {};  // z-slab levels: owned slots per block (nullptr: all)
-    uint8_t* vk_nbm[8] = {};    // bit s: the cell across face slot s is a band cell
     double* xb = nullptr;         // ping-pong partner of x for the Vanka sweep
     double *wb = nullptr, *wx = nullptr;  // W-cycle: rhs / correction of the second recursive call
     int32_t* vk_refresh = nullptr;  // slots every Vanka residual reads (refreshed x -> xb per sweep)
@@ -298,7 +297,7 @@ void build(smg_ctx* c, const std::vector<double>* shared_coarse = nullptr, std::
             return x < bw || y < bw || z < bw || x >= nx - bw || y >= ny - bw || z >= nz - bw;
         };
         std::vector<int32_t> cells[8];
-        std::vector<uint8_t> masks[8], amasks[8], nbms[8];
+        std::vector<uint8_t> masks[8], amasks[8];
         bool used[64] = {};
         int64_t v1 = 0;
         for (int z = 0; z < nz; ++z)
@@ -330,14 +329,6 @@ void build(smg_ctx* c, const std::vector<double>* shared_coarse = nullptr, std::
                     cells[col].push_back(static_cast<int32_t>(L.k.g.slot(x, y, z - z0)));
                     masks[col].push_back(static_cast<uint8_t>(m));
                     amasks[col].push_back(static_cast<uint8_t>(am));
-                    int nb = 0;
-                    if (band(x - 1, y, z)) nb |= 1;
-                    if (band(x + 1, y, z)) nb |= 2;
-                    if (band(x, y - 1, z)) nb |= 4;
-                    if (band(x, y + 1, z)) nb |= 8;
-                    if (band(x, y, z - 1)) nb |= 16;
-                    if (band(x, y, z + 1)) nb |= 32;
-                    nbms[col].push_back(static_cast<uint8_t>(nb));
                     used[m] = true;
                 }
         L.counts[4] = v1;
@@ -382,8 +373,6 @@ void build(smg_ctx* c, const std::vector<double>* shared_coarse = nullptr, std::
             CK(cudaMemcpyAsync(L.vk_cells[col], cells[col].data(), cells[col].size() * sizeof(int32_t),
                                cudaMemcpyHostToDevice, c->st));
             CK(cudaMemcpyAsync(L.vk_mask[col], masks[col].data(), masks[col].size(), cudaMemcpyHostToDevice, c->st));
-            L.vk_nbm[col] = c->dalloc<uint8_t>(L.vk_n[col]);
-            CK(cudaMemcpyAsync(L.vk_nbm[col], nbms[col].data(), nbms[col].size(), cudaMemcpyHostToDevice, c->st));
             if (dist) {
                 L.vk_amask[col] = c->dalloc<uint8_t>(L.vk_n[col]);
                 CK(cudaMemcpyAsync(L.vk_amask[col], amasks[col].data(), amasks[col].size(), cudaMemcpyHostToDevice,
@@ -547,7 +536,7 @@ void symmetric_dgs(smg_ctx* c, int l, double* x, const double* b) {
 void vanka_sym_coop(smg_ctx* c, int l, double* x, const double* b) {
     DevLevel& L = c->lv[l];
     launch_vanka_sym_coop(L.k, x, b, L.vk_cells, L.vk_mask, L.vk_n, L.ktab, c->vk_delta, c->prm.nu, c->st, L.xb,
-                          L.vk_refresh, L.vk_nrefresh, L.vk_nbm);
+                          L.vk_refresh, L.vk_nrefresh);
 }
 
 void smooth(smg_ctx* c, int l, double* x, const double* b) {

@@ -510,7 +510,6 @@ __device__ __forceinline__ void phase_sync() {
 struct VankaLists {
     const int32_t* cells[8];
     const uint8_t* masks[8];
-    const uint8_t* nbm[8];  // bit s: the cell across face slot s is a band cell (ping-pong carry rule)
     int n[8];
 };
 
@@ -752,8 +751,16 @@ __device__ __forceinline__ void vanka_sweeps_pp(const LevelK& L, double* __restr
                 int mp;
                 block_of(pcol, t, ip, mp);
                 bool carry = s8 == 6 || (mp & (1 << s8));
-                if (carry && s8 < 6 && (pcol ^ (1 << (s8 >> 1))) == col && (vl.nbm[pcol][t] & (1 << s8)))
-                    carry = false;
+                if (carry && s8 < 6 && (pcol ^ (1 << (s8 >> 1))) == col) {
+                    const int zl = static_cast<int>(ip / sz) - g.zg;
+                    const int64_t rem = ip - static_cast<int64_t>(zl + g.zg) * sz;
+                    const int y = static_cast<int>(rem / sy) - 1;
+                    const int x = static_cast<int>(rem - static_cast<int64_t>(y + 1) * sy) - g.xo;
+                    const int d = (s8 & 1) ? 1 : -1;
+                    const int ax = s8 >> 1;
+                    if (band_cell(L, x + (ax == 0 ? d : 0), y + (ax == 1 ? d : 0), zl + (ax == 2 ? d : 0)))
+                        carry = false;
+                }
                 if (carry) Xn[ip + offs] = Xc[ip + offs];
             }
         }
@@ -1333,7 +1340,7 @@ static int coop_threads() { return env_int("SMG_COOP_THREADS", 512) == 256 ? 256
 // Launch either as one cooperative grid (MODE 0) or as a single cluster of
 // kClusterCTAs CTAs (MODE 1) whose phases are separated by cluster barriers.
 static void launch_sweep(const void* fn_grid, const void* fn_cluster, bool cluster, int64_t work, void** args,
-                         cudaStream_t s, int grid_threads = 0) {
+                         cudaStream_t s) {
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[1];
     cfg.stream = s;
@@ -1349,7 +1356,7 @@ static void launch_sweep(const void* fn_grid, const void* fn_cluster, bool clust
         attr[0].val.clusterDim.z = 1;
         note(cudaLaunchKernelExC(&cfg, fn_cluster, args));
     } else {
-        const int bt = grid_threads > 0 ? grid_threads : coop_threads();
+        const int bt = coop_threads();
         cfg.gridDim = dim3(coop_blocks(fn_grid, work, bt));
         cfg.blockDim = dim3(bt);
         attr[0].id = cudaLaunchAttributeCooperative;
@@ -1375,21 +1382,18 @@ static void launch_vanka8(bool cl, int64_t threads, void** args, cudaStream_t s)
 
 template <int CPT>
 static void launch_vanka_pp(bool cl, int64_t threads, void** args, cudaStream_t s) {
-    // small blocks: the per-phase work is instruction-bound, spread it over every SM
     launch_sweep(reinterpret_cast<const void*>(k_vanka_pp<0, CPT>), reinterpret_cast<const void*>(k_vanka_pp<1, CPT>),
-                 cl, threads, args, s, env_int("SMG_VANKA_THREADS", 128));
+                 cl, threads, args, s);
 }
 
 void launch_vanka_sym_coop(const LevelK& L, double* x, const double* b, const int32_t* const* cells,
                            const uint8_t* const* masks, const int* n, const double* ktab, double* delta, int nu,
-                           cudaStream_t s, double* xb, const int32_t* refresh, int64_t nrefresh,
-                           const uint8_t* const* nbm) {
+                           cudaStream_t s, double* xb, const int32_t* refresh, int64_t nrefresh) {
     VankaLists vl;
     int maxn = 1;
     for (int c = 0; c < 8; ++c) {
         vl.cells[c] = cells[c];
         vl.masks[c] = masks[c];
-        vl.nbm[c] = nbm ? nbm[c] : nullptr;
         vl.n[c] = n[c];
         maxn = n[c] > maxn ? n[c] : maxn;
     }
@@ -1401,24 +1405,21 @@ void launch_vanka_sym_coop(const LevelK& L, double* x, const double* b, const in
     const bool cl = mode == 2 || (mode == 0 && lanes <= cl_threads);
     // every block of a colour must be held in registers by some lane group:
     // threads * CPT >= lanes with threads = co-resident capacity of THAT instance
-    auto fits_bt = [&](const void* fn, int cpt, int bt) {
-        const int64_t threads = cl ? cl_threads : coop_capacity_blocks(fn, bt) * bt;
+    auto fits = [&](const void* fn, int cpt) {
+        const int64_t threads = cl ? cl_threads : coop_capacity_blocks(fn, coop_threads()) * coop_threads();
         return threads * cpt >= lanes;
     };
-    auto fits = [&](const void* fn, int cpt) { return fits_bt(fn, cpt, coop_threads()); };
-    const int ppt = env_int("SMG_VANKA_THREADS", 128);
-    auto fits_pp = [&](const void* fn, int cpt) { return fits_bt(fn, cpt, ppt); };
     bool done = true;
-    if (xb && nbm && !cl && env_int("SMG_VANKA_PP", 1)) {  // ping-pong (grid mode): one barrier per phase
+    if (xb && !cl && env_int("SMG_VANKA_PP", 1)) {  // ping-pong (grid mode): one barrier per phase
         if (nrefresh > 0) {
             const int64_t blocks = (nrefresh + 255) / 256;
             k_refresh<<<static_cast<int>(blocks < 4096 ? blocks : 4096), 256, 0, s>>>(refresh, nrefresh, x, xb);
             count();
         }
         void* pargs[] = {args[0], &x, &xb, args[2], args[3], args[4], args[5]};
-        if (fits_pp(reinterpret_cast<const void*>(k_vanka_pp<0, 1>), 1)) { launch_vanka_pp<1>(cl, lanes, pargs, s); return; }
-        if (fits_pp(reinterpret_cast<const void*>(k_vanka_pp<0, 2>), 2)) { launch_vanka_pp<2>(cl, (lanes + 1) / 2, pargs, s); return; }
-        if (fits_pp(reinterpret_cast<const void*>(k_vanka_pp<0, 4>), 4)) { launch_vanka_pp<4>(cl, (lanes + 3) / 4, pargs, s); return; }
+        if (fits(reinterpret_cast<const void*>(k_vanka_pp<0, 1>), 1)) { launch_vanka_pp<1>(cl, lanes, pargs, s); return; }
+        if (fits(reinterpret_cast<const void*>(k_vanka_pp<0, 2>), 2)) { launch_vanka_pp<2>(cl, (lanes + 1) / 2, pargs, s); return; }
+        if (fits(reinterpret_cast<const void*>(k_vanka_pp<0, 4>), 4)) { launch_vanka_pp<4>(cl, (lanes + 3) / 4, pargs, s); return; }
     }
     if (fits(reinterpret_cast<const void*>(k_vanka8<0, 1>), 1)) launch_vanka8<1>(cl, lanes, args, s);
     else if (fits(reinterpret_cast<const void*>(k_vanka8<0, 2>), 2)) launch_vanka8<2>(cl, (lanes + 1) / 2, args, s);

@@ -87,7 +87,7 @@ void launch_vanka_apply(const LevelK& L, double* x, const int32_t* cells, const 
 void launch_vanka_sym_coop(const LevelK& L, double* x, const double* b, const int32_t* const* cells,
                            const uint8_t* const* masks, const int* n, const double* ktab, double* delta, int nu,
                            cudaStream_t s, double* xb = nullptr, const int32_t* refresh = nullptr,
-                           int64_t nrefresh = 0, const uint8_t* const* nbm = nullptr);
+                           int64_t nrefresh = 0);
 void launch_dgs_sym_coop(const LevelK& L, double* x, const double* b, double* d0, double* d1, int nph,
                          cudaStream_t s);
 // Whole smooth (Alg. 3) of a level held in the distributed shared memory of one
