@@ -87,6 +87,10 @@ typedef struct smg_timing {
 int smg_create(const smg_grid_desc* grid, const smg_params* params, int ngpu, const int* dev_ids,
                smg_ctx** out);
 void smg_destroy(smg_ctx* ctx);
+/* assemble_rhs, host only: adds the Dirichlet-data contributions
+ * of a scenario to b (compact order).  scenario 0: lid-driven cavity (PAPER:368,
+ * 434), tangential u = value on the top (y = ny) lid, no-slip elsewhere. */
+int smg_assemble_rhs(const smg_grid_desc* grid, double eta, int scenario, double value, double* b);
 /* DOF census of the walled box (host only): out2 = {N, |V1|}; returns N
  * (classify_dofs + partition_band counts; PAPER Table 1). */
 int64_t smg_census(const smg_grid_desc* grid, int band_width, int64_t* out2);

@@ -73,8 +73,13 @@ def set_threads(n: int) -> None:
     lib().orc_set_threads(int(n))
 
 
-def forcing_box(nx, ny, nz, h, kind=FORCE_UNIFORM, seed=0):
+FORCE_CAVITY = 3  # lid-driven cavity: Dirichlet data only (u = 1 on the top y face)
+
+
+def forcing_box(nx, ny, nz, h, kind=FORCE_UNIFORM, seed=0, eta=1.0):
     L = lib()
+    L.orc_set_forcing_eta.argtypes = [C.c_double]
+    L.orc_set_forcing_eta(eta)
     L.orc_forcing_box.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_int, C.c_uint64, _D]
     n = (nx - 1) * ny * nz + nx * (ny - 1) * nz + nx * ny * (nz - 1) + nx * ny * nz
     b = np.empty(n)

@@ -929,10 +929,55 @@ static inline uint64_t key5(uint64_t seed, uint64_t c, uint64_t i, uint64_t j, u
 }
 static inline double unit01(uint64_t h) { return static_cast<double>(h >> 11) * 0x1.0p-53; }
 
-// kind: 0 = iid U[-1,1] (cfg 0,1,3); 1 = 8 Fourier modes (cfg 2); 2 = channel (cfg 4).
+// Dirichlet value of a (non-active) face of component c at storage coordinates
+// (x,y,z) for the lid-driven cavity: u = 1 on the
+// faces of the ring cells above the top (y = ny), 0 elsewhere.
+static double lid_value(const Level& L, int c, int x, int y, int z) {
+    (void)x;
+    (void)z;
+    return (c == 0 && y == L.map.n[1]) ? 1.0 : 0.0;
+}
+
+// assemble_rhs: b = f - L_{active,Dirichlet} g, i.e. every
+// stencil leg of an active row into a Dirichlet face moves to the right-hand
+// side with the opposite sign of its matrix entry (momentum: -eta/h^2 legs;
+// continuity: +-1/h legs to Dirichlet faces).
+static void dirichlet_rhs(const Level& L, vec& b) {
+    const DofMap& m = L.map;
+    const int d[6][3] = {{-1, 0, 0}, {1, 0, 0}, {0, -1, 0}, {0, 1, 0}, {0, 0, -1}, {0, 0, 1}};
+    for (int64_t q = 0; q < m.off[3]; ++q) {
+        const int c = m.comp[q];
+        const auto& p = m.pos[q];
+        for (int k = 0; k < 6; ++k) {
+            const int x = p[0] + d[k][0], y = p[1] + d[k][1], z = p[2] + d[k][2];
+            if (m.face(c, x, y, z) != ST_DIRICHLET) continue;
+            const double gv = lid_value(L, c, x, y, z);
+            if (gv != 0.0) b[q] = b[q] + L.eta_h2 * gv;  // row entry -eta/h^2 -> rhs +eta/h^2 g
+        }
+    }
+    for (int64_t q = m.off[3]; q < m.N; ++q) {  // continuity legs to Dirichlet faces
+        const auto& p = m.pos[q];
+        for (int c = 0; c < 3; ++c)
+            for (int side = 0; side < 2; ++side) {
+                int f3[3] = {p[0], p[1], p[2]};
+                f3[c] += side;
+                if (m.face(c, f3[0], f3[1], f3[2]) != ST_DIRICHLET) continue;
+                const double gv = lid_value(L, c, f3[0], f3[1], f3[2]);
+                // (L~x)_C = -(x_R - x_L)/h: entry -1/h on the right face, +1/h on the left face
+                if (gv != 0.0) b[q] = b[q] - (side ? -L.inv_h : L.inv_h) * gv;
+            }
+    }
+}
+
+// kind: 0 = iid U[-1,1] (cfg 0,1,3); 1 = 8 Fourier modes (cfg 2); 2 = channel (cfg 4);
+// 3 = lid-driven cavity (zero body force, lid u = 1 at the top y face).
 static void forcing(const Level& L, int kind, uint64_t seed, vec& b) {
     const DofMap& m = L.map;
     b.assign(m.N, 0.0);
+    if (kind == 3) {
+        dirichlet_rhs(L, b);
+        return;
+    }
     double amp[3][8];
     int kw[3][8][3];
     if (kind == 1)
@@ -1137,6 +1182,8 @@ void orc_forcing(void* h, int kind, uint64_t seed, double* b) {
     forcing(L, kind, seed, bb);
     out(bb, b);
 }
+static double g_forcing_eta = 1.0;  // eta used by the lid (Dirichlet) contributions of forcing_box
+void orc_set_forcing_eta(double eta) { g_forcing_eta = eta; }
 // Forcing on a walled box without building a hierarchy (no coarse factorisation).
 void orc_forcing_box(int nx, int ny, int nz, double h, int kind, uint64_t seed, double* b) {
     CellGrid g;
@@ -1149,6 +1196,8 @@ void orc_forcing_box(int nx, int ny, int nz, double h, int kind, uint64_t seed, 
     Level L;
     L.map = classify(g, 1);
     L.h = h;
+    L.eta_h2 = g_forcing_eta / (h * h);
+    L.inv_h = 1.0 / h;
     vec bb;
     forcing(L, kind, seed, bb);
     out(bb, b);

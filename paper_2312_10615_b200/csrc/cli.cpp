@@ -7,7 +7,7 @@
 // RunConfig (JSON, flat): nx, ny, nz (cells), h (default 1/nx), eta (1e-3),
 // gamma (1e-3), levels, nu (1), band_width (1), cycle ("V"|"W"), method
 // ("mg-sqmr"|"mg"), tol (1e-8), maxit (200), forcing ("uniform"|"fourier"|
-// "channel"), seed (0), output_dir (env SMG_OUTPUT_DIR, else "."), devices ([0]).
+// "channel"|"cavity": lid-driven, u = lid (1) on the top y face), seed (0), output_dir (env SMG_OUTPUT_DIR, else "."), devices ([0]).
 // Defaults follow SPEC:567-569.  Exit codes: 0 converged,
 // 2 not converged, 1 usage/config error.
 #include <cerrno>
@@ -150,7 +150,8 @@ int main(int argc, char** argv) {
     int64_t cnt[5];
     const int64_t n = smg_level_ndof(ctx, 0, cnt);
     std::vector<double> b(n), x(n), hist(maxit), secs(maxit), lx(n);
-    smg_forcing(&g, kind, static_cast<uint64_t>(num("seed", 0)), b.data(), 8);
+    if (fk == "cavity") smg_assemble_rhs(&g, p.eta, 0, num("lid", 1.0), b.data());  // zero force, lid u
+    else smg_forcing(&g, kind, static_cast<uint64_t>(num("seed", 0)), b.data(), 8);
     smg_history h{maxit, 0, hist.data(), secs.data()};
     int status = -1;
     const auto t0 = std::chrono::steady_clock::now();

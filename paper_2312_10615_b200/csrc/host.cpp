@@ -1023,6 +1023,23 @@ extern "C" {
 
 const char* smg_version(void) { return "smg-b200 0.1 (sm_100a, fp64)"; }
 
+int smg_assemble_rhs(const smg_grid_desc* grid, double eta, int scenario, double value, double* b) {
+    // Dirichlet data folded into the right-hand side: scenario 0 = lid-driven
+    // cavity, u = value on the ring faces above the top (y = ny): each u-face of the top
+    // interior row gets +eta/h^2 * value (its stencil leg to the lid).  Continuity rows see
+    // only the no-penetration (zero) normal velocity.
+    if (!grid || !b || grid->dim != 3 || scenario != 0 || !(grid->h > 0)) return SMG_EINVAL;
+    const int nx = grid->nx, ny = grid->ny, nz = grid->nz;
+    const double eta_h2 = eta / (grid->h * grid->h);
+    if (value == 0.0) return 0;
+    for (int z = 0; z < nz; ++z)
+        for (int x = 1; x <= nx - 1; ++x) {
+            const int64_t id = (static_cast<int64_t>(z) * ny + (ny - 1)) * (nx - 1) + (x - 1);
+            b[id] = b[id] + eta_h2 * value;
+        }
+    return 0;
+}
+
 int64_t smg_census(const smg_grid_desc* grid, int band_width, int64_t* out2) {
     if (!grid || grid->dim != 3 || band_width < 1 || grid->nx < 1 || grid->ny < 1 || grid->nz < 1) return SMG_EINVAL;
     const int nx = grid->nx, ny = grid->ny, nz = grid->nz, bw = band_width;

@@ -118,3 +118,15 @@ def test_create_fails_cleanly_without_gpu_or_bad_args():
     # invalid extents must be rejected before touching a device
     with pytest.raises(smg.SmgError):
         smg.Solver(12, levels=4)  # 12 not divisible by 8
+
+
+@pytest.mark.parametrize("dims,eta", [((8, 8, 8), 1.0), ((12, 6, 10), 1e-3)])
+def test_cavity_rhs_bitwise_matches_oracle(dims, eta):
+    # assemble_rhs: Dirichlet lid data folded into b, oracle's generic legs vs host formula
+    nx, ny, nz = dims
+    ref = oracle.forcing_box(nx, ny, nz, 1.0 / nx, oracle.FORCE_CAVITY, 0, eta=eta)
+    got = smg.cavity_rhs(nx, ny, nz, h=1.0 / nx, eta=eta)
+    assert np.array_equal(ref, got)
+    nu = (nx - 1) * ny * nz
+    assert np.count_nonzero(got) == (nx - 1) * nz and np.all(got[:nu].reshape(nz, ny, nx - 1)[:, -1, :] > 0)
+    assert not got[nu:].any()  # RHS compatibility: continuity entries sum to 0 (tangential lid)

@@ -295,3 +295,17 @@ def test_dsm_smoother_bitwise(monkeypatch):
         same(s.smoother(smg.OP_SMOOTH, x, b), o.smoother(4, x, b))
         assert np.array_equal(s.vcycle(b), o.vcycle(b))
         s.close()
+
+
+def test_lid_driven_cavity_bitwise():
+    """The paper's 3-D cavity: zero force, lid u = 1; GPU solve == oracle, flow follows the lid."""
+    oracle.set_threads(os.cpu_count() or 1)
+    n = 32
+    b = smg.cavity_rhs(n, eta=1e-3)
+    o = oracle.Oracle(n, levels=3, eta=1e-3)
+    s = smg.Solver(n, levels=3, eta=1e-3)
+    xo, ho, _, sto = o.sqmr(b, 1e-8, 100)
+    xg, hg, _, stg = s.sqmr(b, 1e-8, 100)
+    assert sto == stg == smg.SMG_CONVERGED and np.array_equal(ho, hg) and np.array_equal(xo, xg)
+    u = xg[: (n - 1) * n * n].reshape(n, n, n - 1)
+    assert u[:, -1, :].mean() > 0.1 and u[:, 0, :].mean() < u[:, -1, :].mean()
