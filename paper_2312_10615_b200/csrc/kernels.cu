@@ -588,6 +588,47 @@ __global__ void __launch_bounds__(512) k_vanka_sym_coop(LevelK L, double* __rest
     vanka_sweeps<MODE, CPT>(L, X, B, vl, Ks, nu, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
 }
 
+// Row residual of one Vanka block slot, gathered without divergence: lane s8 of
+// the block's 8-lane group (0..5 the faces uL,uR,vL,vR,wL,wR; 6 the pressure)
+// issues the same nine loads at lane-dependent offsets, then evaluates mom()
+// (faces) or cont() (pressure) on them in exactly their operation order.  A
+// per-lane switch would serialise seven dependent L2 round trips per phase.
+// own = the slot's current value (the centre load).  Call only for s8 < 7 on
+// a real block (every offset then stays inside the padded vector).
+template <class AX>
+__device__ __forceinline__ double vanka_slot_residual(const LevelK& L, AX X, const double* __restrict__ B,
+                                                      int64_t i, int m, int s8, double& own) {
+    const Geom& g = L.g;
+    const int64_t fs = g.fs, sy = g.sy, sz = g.sz;
+    const bool mom_row = s8 < 6;
+    const int d = s8 >> 1;
+    const int64_t st = d == 0 ? 1 : (d == 1 ? sy : sz);
+    const int64_t jj = i + ((s8 & 1) ? st : 0);  // face slot (cell slot for the pressure row)
+    const int64_t j = d * fs + jj;
+    const int64_t p3 = 3 * fs;
+    const int64_t o0 = mom_row ? j - 1 : i + 1, o1 = mom_row ? j + 1 : i;
+    const int64_t o2 = mom_row ? j - sy : fs + i + sy, o3 = mom_row ? j + sy : fs + i;
+    const int64_t o4 = mom_row ? j - sz : 2 * fs + i + sz, o5 = mom_row ? j + sz : 2 * fs + i;
+    const int64_t o6 = mom_row ? j : p3 + i;
+    const int64_t o7 = p3 + (mom_row ? jj : i), o8 = p3 + (mom_row ? jj - st : i);
+    const double a0 = X[o0], a1 = X[o1], a2 = X[o2], a3 = X[o3], a4 = X[o4], a5 = X[o5], a6 = X[o6];
+    const double a7 = X[o7], a8 = X[o8], bb = B[o6];
+    own = a6;
+    // mom(): eta/h^2 (6 F[j] - sum of the 6 neighbours x-,x+,y-,y+,z-,z+) + (P[j] - P[j - st]) / h
+    double sm = a0 + a1;
+    sm = sm + a2;
+    sm = sm + a3;
+    sm = sm + a4;
+    sm = sm + a5;
+    const double lap = 6.0 * a6 - sm;
+    const double vm = L.eta_h2 * lap + (a7 - a8) * L.inv_h;
+    // cont(): -((U[i+1]-U[i]) + (V[i+sy]-V[i]) + (W[i+sz]-W[i])) / h - gamma p
+    const double div = (a0 - a1) + (a2 - a3) + (a4 - a5);
+    const double vc = -div * L.inv_h - L.gamma * a6;
+    const bool on = mom_row ? ((m >> s8) & 1) != 0 : true;
+    return on ? bb - (mom_row ? vm : vc) : 0.0;
+}
+
 // Lane-parallel Vanka: 8 lanes per block; lane s < 7 computes residual slot s
 // and owns DOF s; delta_s = sum_q K[s][q] r_q gathers r_q by warp shuffles in
 // ascending q (same order as the oracle).  Each thread holds at most CPT
@@ -638,19 +679,7 @@ __device__ __forceinline__ void vanka_sweeps8(const LevelK& L, AX X, const doubl
                     }
                 }
                 double r = 0.0;
-                if (act && s8 < 7) {
-                    const auto U = X, V = X + fs, W = X + 2 * fs, P = X + 3 * fs;
-                    switch (s8) {
-                        case 0: r = (m & 1) ? B[i] - mom(L, U, P, i, 1) : 0.0; break;
-                        case 1: r = (m & 2) ? B[i + 1] - mom(L, U, P, i + 1, 1) : 0.0; break;
-                        case 2: r = (m & 4) ? B[fs + i] - mom(L, V, P, i, sy) : 0.0; break;
-                        case 3: r = (m & 8) ? B[fs + i + sy] - mom(L, V, P, i + sy, sy) : 0.0; break;
-                        case 4: r = (m & 16) ? B[2 * fs + i] - mom(L, W, P, i, sz) : 0.0; break;
-                        case 5: r = (m & 32) ? B[2 * fs + i + sz] - mom(L, W, P, i + sz, sz) : 0.0; break;
-                        default: r = B[3 * fs + i] - cont(L, U, V, W, P, i, L.gamma); break;
-                    }
-                    own[j] = X[i + offs];
-                }
+                if (act && s8 < 7) r = vanka_slot_residual(L, X, B, i, m, s8, own[j]);
                 const double* K = Ks + m * 49 + (s8 < 7 ? s8 : 0) * 7;
                 double acc = 0.0;
 #pragma unroll
@@ -722,19 +751,7 @@ __device__ __forceinline__ void vanka_sweeps_pp(const LevelK& L, double* __restr
             int m = 0;
             if (act) block_of(col, t, i, m);
             double r = 0.0, own = 0.0;
-            if (act && s8 < 7) {
-                const double *U = Xc, *V = Xc + fs, *W = Xc + 2 * fs, *P = Xc + 3 * fs;
-                switch (s8) {
-                    case 0: r = (m & 1) ? B[i] - mom(L, U, P, i, 1) : 0.0; break;
-                    case 1: r = (m & 2) ? B[i + 1] - mom(L, U, P, i + 1, 1) : 0.0; break;
-                    case 2: r = (m & 4) ? B[fs + i] - mom(L, V, P, i, sy) : 0.0; break;
-                    case 3: r = (m & 8) ? B[fs + i + sy] - mom(L, V, P, i + sy, sy) : 0.0; break;
-                    case 4: r = (m & 16) ? B[2 * fs + i] - mom(L, W, P, i, sz) : 0.0; break;
-                    case 5: r = (m & 32) ? B[2 * fs + i + sz] - mom(L, W, P, i + sz, sz) : 0.0; break;
-                    default: r = B[3 * fs + i] - cont(L, U, V, W, P, i, L.gamma); break;
-                }
-                own = Xc[i + offs];
-            }
+            if (act && s8 < 7) r = vanka_slot_residual(L, Xc, B, i, m, s8, own);
             const double* K = Ks + m * 49 + (s8 < 7 ? s8 : 0) * 7;
             double acc = 0.0;
 #pragma unroll
@@ -930,7 +947,6 @@ __device__ __forceinline__ void dgs_sweep(const LevelK& L, AX X, const double* _
     const Geom& g = L.g;
     const int64_t ncell = static_cast<int64_t>(g.nx) * g.ny * g.nz;
     const int64_t nxy = static_cast<int64_t>(g.nx) * g.ny;
-    const int64_t fs = g.fs, sy = g.sy, sz = g.sz;
     for (int ph = 0; ph < nph; ++ph) {
         if (ph == 0 || ph == 1 || ph == 18 || ph == 19) {
             const int colour = ph < 2 ? ph : 19 - ph;
