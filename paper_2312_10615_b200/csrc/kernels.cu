@@ -813,24 +813,26 @@ __global__ void __launch_bounds__(512) k_vanka8(LevelK L, double* __restrict__ X
     vanka_sweeps8<MODE, CPT>(L, X, B, vl, Ks, nu, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
 }
 
+// Cell updates below load everything a cell needs before their first store:
+// X, D and the faces of one cell are reached through one pointer, so a store
+// would otherwise order every later load behind it (one L2 round trip each).
+// Same additions in the same order as the plain forms, hence bit-identical.
 template <class AX>
 __device__ __forceinline__ void dgs_vel_cell(const LevelK& L, AX X, const double* __restrict__ B, int x, int y, int z) {
     const Geom& g = L.g;
     const int64_t fs = g.fs, i = g.slot(x, y, z);
     const auto U = X, V = X + fs, W = X + 2 * fs, P = X + 3 * fs;
     const bool here = band_cell(L, x, y, z);
-    if (x >= 1 && !here && !band_cell(L, x - 1, y, z)) {
-        const double r = B[i] - mom(L, U, P, i, 1);
-        U[i] = U[i] + r / L.dv;
-    }
-    if (y >= 1 && !here && !band_cell(L, x, y - 1, z)) {
-        const double r = B[fs + i] - mom(L, V, P, i, g.sy);
-        V[i] = V[i] + r / L.dv;
-    }
-    if (g.gz(z) >= 1 && !here && !band_cell(L, x, y, z - 1)) {
-        const double r = B[2 * fs + i] - mom(L, W, P, i, g.sz);
-        W[i] = W[i] + r / L.dv;
-    }
+    const bool du = x >= 1 && !here && !band_cell(L, x - 1, y, z);
+    const bool dv = y >= 1 && !here && !band_cell(L, x, y - 1, z);
+    const bool dw = g.gz(z) >= 1 && !here && !band_cell(L, x, y, z - 1);
+    double ru = 0.0, rv = 0.0, rw = 0.0, u0 = 0.0, v0 = 0.0, w0 = 0.0;
+    if (du) { u0 = U[i]; ru = B[i] - mom(L, U, P, i, 1); }
+    if (dv) { v0 = V[i]; rv = B[fs + i] - mom(L, V, P, i, g.sy); }
+    if (dw) { w0 = W[i]; rw = B[2 * fs + i] - mom(L, W, P, i, g.sz); }
+    if (du) U[i] = u0 + ru / L.dv;
+    if (dv) V[i] = v0 + rv / L.dv;
+    if (dw) W[i] = w0 + rw / L.dv;
 }
 
 template <class AX>
@@ -879,25 +881,30 @@ __device__ __forceinline__ bool colour_cell(const Geom& g, int c, int64_t t, int
 // additions in the same order, hence bit-identical.  One combined delta buffer
 // holds delta_c at the V2 cells of colour c (band cells stay 0); a gather from
 // phase c' masks the neighbour sum to colour-c' cells.
+// The six delta neighbours of a cell (x-, x+, y-, y+, z-, z+), loaded once.
+struct Nbr6 {
+    double v[6];
+};
 template <class AD>
-__device__ __forceinline__ double masked_nbr_sum(const Geom& g, AD D, int64_t i, int x, int y, int zg, int cc) {
+__device__ __forceinline__ Nbr6 load_nbr6(const Geom& g, AD D, int64_t i) {
+    return Nbr6{{D[i - 1], D[i + 1], D[i - g.sy], D[i + g.sy], D[i - g.sz], D[i + g.sz]}};
+}
+__device__ __forceinline__ double masked_nbr_sum(const Nbr6& d, int x, int y, int zg, int cc) {
     // neighbour colours: x +-1 flips bit 1, y +-1 bit 2, z +-1 bit 4 of colour (x,y,zg)
     const int ck = (x & 1) + 2 * (y & 1) + 4 * (zg & 1);
     const bool mx = (ck ^ 1) == cc, my = (ck ^ 2) == cc, mz = (ck ^ 4) == cc;
-    double s = (mx ? D[i - 1] : 0.0) + (mx ? D[i + 1] : 0.0);
-    s = s + (my ? D[i - g.sy] : 0.0);
-    s = s + (my ? D[i + g.sy] : 0.0);
-    s = s + (mz ? D[i - g.sz] : 0.0);
-    s = s + (mz ? D[i + g.sz] : 0.0);
+    double s = (mx ? d.v[0] : 0.0) + (mx ? d.v[1] : 0.0);
+    s = s + (my ? d.v[2] : 0.0);
+    s = s + (my ? d.v[3] : 0.0);
+    s = s + (mz ? d.v[4] : 0.0);
+    s = s + (mz ? d.v[5] : 0.0);
     return s;
 }
 
-template <class AX, class AD>
-__device__ __forceinline__ void pending_gathers(const LevelK& L, AX X, AD D, int x, int y, int z, bool later) {
-    const Geom& g = L.g;
-    const int zg = g.gz(z);
+// p_K after the pending gathers (earlier colours if !later, the others if later).
+__device__ __forceinline__ double apply_gathers(const LevelK& L, double p, const Nbr6& d, int x, int y, int zg,
+                                                bool later) {
     const int k = (x & 1) + 2 * (y & 1) + 4 * (zg & 1);
-    const int64_t i = g.slot(x, y, z), ip = 3 * g.fs + i;
     const int c1 = k ^ 1, c2 = k ^ 2, c4 = k ^ 4;  // ascending order among the three
     int cs[3] = {c1, c2, c4};
     if (cs[0] > cs[1]) { const int t = cs[0]; cs[0] = cs[1]; cs[1] = t; }
@@ -907,34 +914,62 @@ __device__ __forceinline__ void pending_gathers(const LevelK& L, AX X, AD D, int
     for (int q = 0; q < 3; ++q) {
         const int cc = cs[q];
         if ((cc < k) == later) continue;
-        const double sn = masked_nbr_sum(g, D, i, x, y, zg, cc);
-        X[ip] = X[ip] + L.eta_h2 * (6.0 * 0.0 - sn);
+        const double sn = masked_nbr_sum(d, x, y, zg, cc);
+        p = p + L.eta_h2 * (6.0 * 0.0 - sn);
     }
+    return p;
+}
+
+template <class AX, class AD>
+__device__ __forceinline__ void pending_gathers(const LevelK& L, AX X, AD D, int x, int y, int z, bool later) {
+    const Geom& g = L.g;
+    const int64_t i = g.slot(x, y, z), ip = 3 * g.fs + i;
+    const Nbr6 d = load_nbr6(g, D, i);
+    const double p0 = X[ip];
+    X[ip] = apply_gathers(L, p0, d, x, y, g.gz(z), later);
 }
 
 template <class AX, class AD>
 __device__ __forceinline__ void pf_lazy_cell(const LevelK& L, AX X, const double* __restrict__ B, AD D, int x, int y,
                                              int z) {
     const Geom& g = L.g;
-    pending_gathers(L, X, D, x, y, z, false);
-    if (band_cell(L, x, y, z)) return;
     const int64_t fs = g.fs, sy = g.sy, sz = g.sz, ii = g.slot(x, y, z);
-    const double rr = B[3 * fs + ii] - cont(L, X, X + fs, X + 2 * fs, X + 3 * fs, ii, L.gamma);
+    const Nbr6 d = load_nbr6(g, D, ii);
+    const double p0 = X[3 * fs + ii];
+    const bool band = band_cell(L, x, y, z);
+    double uL = 0.0, uR = 0.0, vL = 0.0, vR = 0.0, wL = 0.0, wR = 0.0, bp = 0.0;
+    if (!band) {
+        uL = X[ii];
+        uR = X[ii + 1];
+        vL = X[fs + ii];
+        vR = X[fs + ii + sy];
+        wL = X[2 * fs + ii];
+        wR = X[2 * fs + ii + sz];
+        bp = B[3 * fs + ii];
+    }
+    const double p = apply_gathers(L, p0, d, x, y, g.gz(z), false);
+    if (band) {
+        X[3 * fs + ii] = p;
+        return;
+    }
+    // cont(): -((uR-uL) + (vR-vL) + (wR-wL)) / h - gamma p
+    const double div = (uR - uL) + (vR - vL) + (wR - wL);
+    const double rr = bp - (-div * L.inv_h - L.gamma * p);
     const double dc = rr / L.dp;
     D[ii] = dc;
-    X[ii] = X[ii] + (0.0 - dc) * L.inv_h;
-    X[ii + 1] = X[ii + 1] + (dc - 0.0) * L.inv_h;
-    X[fs + ii] = X[fs + ii] + (0.0 - dc) * L.inv_h;
-    X[fs + ii + sy] = X[fs + ii + sy] + (dc - 0.0) * L.inv_h;
-    X[2 * fs + ii] = X[2 * fs + ii] + (0.0 - dc) * L.inv_h;
-    X[2 * fs + ii + sz] = X[2 * fs + ii + sz] + (dc - 0.0) * L.inv_h;
+    X[ii] = uL + (0.0 - dc) * L.inv_h;
+    X[ii + 1] = uR + (dc - 0.0) * L.inv_h;
+    X[fs + ii] = vL + (0.0 - dc) * L.inv_h;
+    X[fs + ii + sy] = vR + (dc - 0.0) * L.inv_h;
+    X[2 * fs + ii] = wL + (0.0 - dc) * L.inv_h;
+    X[2 * fs + ii + sz] = wR + (dc - 0.0) * L.inv_h;
     // self term: the colour-c neighbour sum is a sum of six zeros
     double sn = 0.0 + 0.0;
     sn = sn + 0.0;
     sn = sn + 0.0;
     sn = sn + 0.0;
     sn = sn + 0.0;
-    X[3 * fs + ii] = X[3 * fs + ii] + L.eta_h2 * (6.0 * dc - sn);
+    X[3 * fs + ii] = p + L.eta_h2 * (6.0 * dc - sn);
 }
 
 // Symmetric DGS sweep (20 phases, OD-1) in one persistent launch.  Forward
