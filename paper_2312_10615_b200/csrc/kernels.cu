@@ -817,26 +817,48 @@ __global__ void __launch_bounds__(512) k_vanka8(LevelK L, double* __restrict__ X
 // X, D and the faces of one cell are reached through one pointer, so a store
 // would otherwise order every later load behind it (one L2 round trip each).
 // Same additions in the same order as the plain forms, hence bit-identical.
+// A velocity-phase cell update split into its loads and its stores, so a thread
+// holding several cells issues all their loads first (cells of one phase never
+// read each other's writes).
+struct VelUpd {
+    int64_t i;
+    double u0, v0, w0, ru, rv, rw;
+    bool du, dv, dw;
+};
+template <class AX>
+__device__ __forceinline__ VelUpd vel_load(const LevelK& L, AX X, const double* __restrict__ B, int x, int y, int z,
+                                           bool valid) {
+    const Geom& g = L.g;
+    const int64_t fs = g.fs;
+    VelUpd u;
+    u.i = valid ? g.slot(x, y, z) : 0;
+    const int64_t i = u.i;
+    const auto U = X, V = X + fs, W = X + 2 * fs, P = X + 3 * fs;
+    const bool here = !valid || band_cell(L, x, y, z);
+    u.du = x >= 1 && !here && !band_cell(L, x - 1, y, z);
+    u.dv = y >= 1 && !here && !band_cell(L, x, y - 1, z);
+    u.dw = g.gz(z) >= 1 && !here && !band_cell(L, x, y, z - 1);
+    u.ru = u.rv = u.rw = u.u0 = u.v0 = u.w0 = 0.0;
+    if (u.du) { u.u0 = U[i]; u.ru = B[i] - mom(L, U, P, i, 1); }
+    if (u.dv) { u.v0 = V[i]; u.rv = B[fs + i] - mom(L, V, P, i, g.sy); }
+    if (u.dw) { u.w0 = W[i]; u.rw = B[2 * fs + i] - mom(L, W, P, i, g.sz); }
+    return u;
+}
+template <class AX>
+__device__ __forceinline__ void vel_store(const LevelK& L, AX X, const VelUpd& u) {
+    const int64_t fs = L.g.fs;
+    if (u.du) X[u.i] = u.u0 + u.ru / L.dv;
+    if (u.dv) X[fs + u.i] = u.v0 + u.rv / L.dv;
+    if (u.dw) X[2 * fs + u.i] = u.w0 + u.rw / L.dv;
+}
 template <class AX>
 __device__ __forceinline__ void dgs_vel_cell(const LevelK& L, AX X, const double* __restrict__ B, int x, int y, int z) {
-    const Geom& g = L.g;
-    const int64_t fs = g.fs, i = g.slot(x, y, z);
-    const auto U = X, V = X + fs, W = X + 2 * fs, P = X + 3 * fs;
-    const bool here = band_cell(L, x, y, z);
-    const bool du = x >= 1 && !here && !band_cell(L, x - 1, y, z);
-    const bool dv = y >= 1 && !here && !band_cell(L, x, y - 1, z);
-    const bool dw = g.gz(z) >= 1 && !here && !band_cell(L, x, y, z - 1);
-    double ru = 0.0, rv = 0.0, rw = 0.0, u0 = 0.0, v0 = 0.0, w0 = 0.0;
-    if (du) { u0 = U[i]; ru = B[i] - mom(L, U, P, i, 1); }
-    if (dv) { v0 = V[i]; rv = B[fs + i] - mom(L, V, P, i, g.sy); }
-    if (dw) { w0 = W[i]; rw = B[2 * fs + i] - mom(L, W, P, i, g.sz); }
-    if (du) U[i] = u0 + ru / L.dv;
-    if (dv) V[i] = v0 + rv / L.dv;
-    if (dw) W[i] = w0 + rw / L.dv;
+    vel_store(L, X, vel_load(L, X, B, x, y, z, true));
 }
 
+// Reverse (left-preconditioned) pressure update of the cell at slot i: the new p_i.
 template <class AX>
-__device__ __forceinline__ void dgs_prev_cell(const LevelK& L, AX X, const double* __restrict__ B, int64_t i) {
+__device__ __forceinline__ double prev_value(const LevelK& L, AX X, const double* __restrict__ B, int64_t i) {
     const Geom& g = L.g;
     const int64_t fs = g.fs, sy = g.sy, sz = g.sz;
     const auto U = X, V = X + fs, W = X + 2 * fs, P = X + 3 * fs;
@@ -856,7 +878,11 @@ __device__ __forceinline__ void dgs_prev_cell(const LevelK& L, AX X, const doubl
     s = s + (BP[i - sz] - cont(L, U, V, W, P, i - sz, L.gamma));
     s = s + (BP[i + sz] - cont(L, U, V, W, P, i + sz, L.gamma));
     const double cj = fl * L.inv_h + L.eta_h2 * (6.0 * rc - s);
-    P[i] = P[i] + cj / L.dp;
+    return P[i] + cj / L.dp;
+}
+template <class AX>
+__device__ __forceinline__ void dgs_prev_cell(const LevelK& L, AX X, const double* __restrict__ B, int64_t i) {
+    X[3 * L.g.fs + i] = prev_value(L, X, B, i);
 }
 
 // cells of parity colour c: t -> (x,y,z) on the half-grid of that parity
@@ -920,49 +946,67 @@ __device__ __forceinline__ double apply_gathers(const LevelK& L, double p, const
     return p;
 }
 
+// Split load / store forms of the lazy forward-pressure cell update and of
+// the flush (same reasoning as VelUpd).
+struct PfUpd {
+    Nbr6 d;
+    int64_t ii;
+    double p0, uL, uR, vL, vR, wL, wR, bp;
+    int x, y, zg;
+    bool valid, band;
+};
 template <class AX, class AD>
-__device__ __forceinline__ void pending_gathers(const LevelK& L, AX X, AD D, int x, int y, int z, bool later) {
+__device__ __forceinline__ PfUpd pf_load(const LevelK& L, AX X, const double* __restrict__ B, AD D, int x, int y,
+                                         int z, bool valid, bool flush) {
     const Geom& g = L.g;
-    const int64_t i = g.slot(x, y, z), ip = 3 * g.fs + i;
-    const Nbr6 d = load_nbr6(g, D, i);
-    const double p0 = X[ip];
-    X[ip] = apply_gathers(L, p0, d, x, y, g.gz(z), later);
-}
-
-template <class AX, class AD>
-__device__ __forceinline__ void pf_lazy_cell(const LevelK& L, AX X, const double* __restrict__ B, AD D, int x, int y,
-                                             int z) {
-    const Geom& g = L.g;
-    const int64_t fs = g.fs, sy = g.sy, sz = g.sz, ii = g.slot(x, y, z);
-    const Nbr6 d = load_nbr6(g, D, ii);
-    const double p0 = X[3 * fs + ii];
-    const bool band = band_cell(L, x, y, z);
-    double uL = 0.0, uR = 0.0, vL = 0.0, vR = 0.0, wL = 0.0, wR = 0.0, bp = 0.0;
-    if (!band) {
-        uL = X[ii];
-        uR = X[ii + 1];
-        vL = X[fs + ii];
-        vR = X[fs + ii + sy];
-        wL = X[2 * fs + ii];
-        wR = X[2 * fs + ii + sz];
-        bp = B[3 * fs + ii];
+    const int64_t fs = g.fs, sy = g.sy, sz = g.sz;
+    PfUpd u;
+    u.valid = valid;
+    u.x = x;
+    u.y = y;
+    u.zg = g.gz(z);
+    u.ii = valid ? g.slot(x, y, z) : 0;
+    const int64_t ii = u.ii;
+    u.band = flush || !valid || band_cell(L, x, y, z);
+    u.uL = u.uR = u.vL = u.vR = u.wL = u.wR = u.bp = 0.0;
+    u.p0 = 0.0;
+    u.d = Nbr6{{0.0, 0.0, 0.0, 0.0, 0.0, 0.0}};
+    if (valid) {
+        u.d = load_nbr6(g, D, ii);
+        u.p0 = X[3 * fs + ii];
     }
-    const double p = apply_gathers(L, p0, d, x, y, g.gz(z), false);
-    if (band) {
+    if (!u.band) {
+        u.uL = X[ii];
+        u.uR = X[ii + 1];
+        u.vL = X[fs + ii];
+        u.vR = X[fs + ii + sy];
+        u.wL = X[2 * fs + ii];
+        u.wR = X[2 * fs + ii + sz];
+        u.bp = B[3 * fs + ii];
+    }
+    return u;
+}
+template <bool FLUSH, class AX, class AD>
+__device__ __forceinline__ void pf_store(const LevelK& L, AX X, AD D, const PfUpd& u) {
+    if (!u.valid) return;
+    const int64_t fs = L.g.fs, sy = L.g.sy, sz = L.g.sz, ii = u.ii;
+    const double p = apply_gathers(L, u.p0, u.d, u.x, u.y, u.zg, FLUSH);
+    if (FLUSH || u.band) {
         X[3 * fs + ii] = p;
         return;
     }
+    if constexpr (!FLUSH) {
     // cont(): -((uR-uL) + (vR-vL) + (wR-wL)) / h - gamma p
-    const double div = (uR - uL) + (vR - vL) + (wR - wL);
-    const double rr = bp - (-div * L.inv_h - L.gamma * p);
+    const double div = (u.uR - u.uL) + (u.vR - u.vL) + (u.wR - u.wL);
+    const double rr = u.bp - (-div * L.inv_h - L.gamma * p);
     const double dc = rr / L.dp;
     D[ii] = dc;
-    X[ii] = uL + (0.0 - dc) * L.inv_h;
-    X[ii + 1] = uR + (dc - 0.0) * L.inv_h;
-    X[fs + ii] = vL + (0.0 - dc) * L.inv_h;
-    X[fs + ii + sy] = vR + (dc - 0.0) * L.inv_h;
-    X[2 * fs + ii] = wL + (0.0 - dc) * L.inv_h;
-    X[2 * fs + ii + sz] = wR + (dc - 0.0) * L.inv_h;
+    X[ii] = u.uL + (0.0 - dc) * L.inv_h;
+    X[ii + 1] = u.uR + (dc - 0.0) * L.inv_h;
+    X[fs + ii] = u.vL + (0.0 - dc) * L.inv_h;
+    X[fs + ii + sy] = u.vR + (dc - 0.0) * L.inv_h;
+    X[2 * fs + ii] = u.wL + (0.0 - dc) * L.inv_h;
+    X[2 * fs + ii + sz] = u.wR + (dc - 0.0) * L.inv_h;
     // self term: the colour-c neighbour sum is a sum of six zeros
     double sn = 0.0 + 0.0;
     sn = sn + 0.0;
@@ -970,6 +1014,19 @@ __device__ __forceinline__ void pf_lazy_cell(const LevelK& L, AX X, const double
     sn = sn + 0.0;
     sn = sn + 0.0;
     X[3 * fs + ii] = p + L.eta_h2 * (6.0 * dc - sn);
+    }
+}
+
+// flush after phase 7: the gathers from the later colours (cell p only)
+template <class AX, class AD>
+__device__ __forceinline__ void flush_gathers(const LevelK& L, AX X, AD D, int x, int y, int z) {
+    pf_store<true>(L, X, D, pf_load(L, X, nullptr, D, x, y, z, true, true));
+}
+
+template <class AX, class AD>
+__device__ __forceinline__ void pf_lazy_cell(const LevelK& L, AX X, const double* __restrict__ B, AD D, int x, int y,
+                                             int z) {
+    pf_store<false>(L, X, D, pf_load(L, X, B, D, x, y, z, true, false));
 }
 
 // Symmetric DGS sweep (20 phases, OD-1) in one persistent launch.  Forward
@@ -985,11 +1042,32 @@ __device__ __forceinline__ void dgs_sweep(const LevelK& L, AX X, const double* _
     for (int ph = 0; ph < nph; ++ph) {
         if (ph == 0 || ph == 1 || ph == 18 || ph == 19) {
             const int colour = ph < 2 ? ph : 19 - ph;
-            for (int64_t t = tid; t < ncell; t += nth) {
-                const int z = static_cast<int>(t / nxy);
-                const int64_t r = t - z * nxy;
-                const int y = static_cast<int>(r / g.nx), x = static_cast<int>(r - static_cast<int64_t>(y) * g.nx);
-                if (((x + y + g.gz(z)) & 1) == colour) dgs_vel_cell(L, X, B, x, y, z);
+            if ((g.nx & 1) == 0) {  // this colour's cells only, two per step (loads of both first)
+                const int hx = g.nx >> 1;
+                const int64_t nc = static_cast<int64_t>(hx) * g.ny * g.nz;
+                auto cell = [&](int64_t t, int& x, int& y, int& z) {
+                    const int64_t r = t / hx;
+                    y = static_cast<int>(r % g.ny);
+                    z = static_cast<int>(r / g.ny);
+                    x = 2 * static_cast<int>(t - r * hx) + ((y + g.gz(z) + colour) & 1);
+                };
+                for (int64_t t = tid; t < nc; t += 2 * nth) {
+                    int x0, y0, z0, x1 = 0, y1 = 0, z1 = 0;
+                    cell(t, x0, y0, z0);
+                    const bool v1 = t + nth < nc;
+                    if (v1) cell(t + nth, x1, y1, z1);
+                    const VelUpd a = vel_load(L, X, B, x0, y0, z0, true);
+                    const VelUpd b = vel_load(L, X, B, x1, y1, z1, v1);
+                    vel_store(L, X, a);
+                    vel_store(L, X, b);
+                }
+            } else {
+                for (int64_t t = tid; t < ncell; t += nth) {
+                    const int z = static_cast<int>(t / nxy);
+                    const int64_t r = t - z * nxy;
+                    const int y = static_cast<int>(r / g.nx), x = static_cast<int>(r - static_cast<int64_t>(y) * g.nx);
+                    if (((x + y + g.gz(z)) & 1) == colour) dgs_vel_cell(L, X, B, x, y, z);
+                }
             }
         } else if (ph <= 9) {  // lazy-gather forward pressure phase (see pf_lazy_cell); D0 combined
             const int c = ph - 2;
@@ -997,11 +1075,21 @@ __device__ __forceinline__ void dgs_sweep(const LevelK& L, AX X, const double* _
             for (int64_t t = tid; colour_cell(g, c, t, x, y, z); t += nth) pf_lazy_cell(L, X, B, D0, x, y, z);
             if (ph == 9) {
                 phase_sync<MODE>();
-                for (int64_t t = tid; t < ncell; t += nth) {
-                    const int zz = static_cast<int>(t / nxy);
-                    const int64_t r = t - zz * nxy;
-                    const int yy = static_cast<int>(r / g.nx), xx = static_cast<int>(r - static_cast<int64_t>(yy) * g.nx);
-                    pending_gathers(L, X, D0, xx, yy, zz, true);
+                auto cell = [&](int64_t t, int& x, int& y, int& z) {
+                    z = static_cast<int>(t / nxy);
+                    const int64_t r = t - z * nxy;
+                    y = static_cast<int>(r / g.nx);
+                    x = static_cast<int>(r - static_cast<int64_t>(y) * g.nx);
+                };
+                for (int64_t t = tid; t < ncell; t += 2 * nth) {
+                    int x0, y0, z0, x1 = 0, y1 = 0, z1 = 0;
+                    cell(t, x0, y0, z0);
+                    const bool v1 = t + nth < ncell;
+                    if (v1) cell(t + nth, x1, y1, z1);
+                    const PfUpd a = pf_load(L, X, B, D0, x0, y0, z0, true, true);
+                    const PfUpd b = pf_load(L, X, B, D0, x1, y1, z1, v1, true);
+                    pf_store<true>(L, X, D0, a);
+                    pf_store<true>(L, X, D0, b);
                 }
             }
         } else {
@@ -1190,7 +1278,7 @@ __global__ void __launch_bounds__(256) k_dgs_pf_lazy_c(LevelK L, double* __restr
 __global__ void __launch_bounds__(256) k_dgs_pf_flush(LevelK L, double* __restrict__ X, const double* __restrict__ D) {
     Cell c;
     if (!thread_cell(L.g, c)) return;
-    pending_gathers(L, X, D, c.x, c.y, c.z, true);
+    flush_gathers(L, X, D, c.x, c.y, c.z);
 }
 
 template <int ZC>
