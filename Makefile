@@ -36,8 +36,13 @@ $(LIB): $(OBJS)
 oracle:
 	$(MAKE) -s -C oracle
 
+# tools-only instrumented library (per-warp phase timestamps; tools/trace_vanka.py)
+trace: build/host.o | build
+	$(NVCC) $(NVFLAGS) -DSMG_TRACE -c $(CSRC)/kernels.cu -o build/kernels_trace.o
+	$(NVCC) $(ARCH) -shared -o tools/libsmg_trace.so build/kernels_trace.o build/host.o -lcudart_static -lpthread -ldl -lrt
+
 clean:
 	rm -rf build $(LIB) $(CLI)
 	$(MAKE) -s -C oracle clean
 
-.PHONY: all oracle clean
+.PHONY: all oracle clean trace

@@ -14,7 +14,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsmg.so")
+LIB_PATH = os.environ.get("SMG_LIB") or os.path.join(_HERE, "libsmg.so")  # SMG_LIB: tools-only builds
 
 SMG_CONVERGED, SMG_MAX_ITERATIONS, SMG_BREAKDOWN = 0, 1, 2
 FLAG_SKIP_REVERSE_DGS = 1

@@ -498,6 +498,21 @@ __global__ void k_dx_update(double* __restrict__ d, double* __restrict__ x, cons
 // Per-point arithmetic is the same as the single-phase kernels above.
 namespace cg = cooperative_groups;
 
+#ifdef SMG_TRACE  // tools-only build (make trace): per-warp phase timestamps of the Vanka sweep
+__device__ unsigned long long* g_trace = nullptr;
+__device__ __forceinline__ void trace_stamp(int ph, int stamp) {
+    if (g_trace && (threadIdx.x & 31) == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        const int64_t w = (static_cast<int64_t>(ph) * gridDim.x + blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+        g_trace[w * 4 + stamp] = t;
+    }
+}
+#define SMG_TRACE_STAMP(ph, k) trace_stamp(ph, k)
+#else
+#define SMG_TRACE_STAMP(ph, k)
+#endif
+
 // Barrier between phases: MODE 0 = whole cooperative grid, MODE 1 = one thread
 // block cluster (<= 16 CTAs; barrier.cluster with release/acquire semantics).
 template <int MODE>
@@ -743,6 +758,7 @@ __device__ __forceinline__ void vanka_sweeps_pp(const LevelK& L, double* __restr
         const double* __restrict__ Xc = (ph & 1) ? XB : XA;
         double* __restrict__ Xn = (ph & 1) ? XA : XB;
         const int n = vl.n[col];
+        SMG_TRACE_STAMP(ph, 0);
 #pragma unroll
         for (int j = 0; j < CPT; ++j) {
             const int t = grp + j * groups;
@@ -752,6 +768,10 @@ __device__ __forceinline__ void vanka_sweeps_pp(const LevelK& L, double* __restr
             if (act) block_of(col, t, i, m);
             double r = 0.0, own = 0.0;
             if (act && s8 < 7) r = vanka_slot_residual(L, Xc, B, i, m, s8, own);
+#ifdef SMG_TRACE
+            if (__any_sync(0xffffffffu, r == 1.2345e300)) g_trace[0] = 0;  // wait for the gather
+            if (j == 0) SMG_TRACE_STAMP(ph, 1);
+#endif
             const double* K = Ks + m * 49 + (s8 < 7 ? s8 : 0) * 7;
             double acc = 0.0;
 #pragma unroll
@@ -781,7 +801,9 @@ __device__ __forceinline__ void vanka_sweeps_pp(const LevelK& L, double* __restr
                 if (carry) Xn[ip + offs] = Xc[ip + offs];
             }
         }
+        SMG_TRACE_STAMP(ph, 2);
         phase_sync<MODE>();
+        SMG_TRACE_STAMP(ph, 3);
     }
 }
 
@@ -1495,9 +1517,27 @@ static void launch_sweep(const void* fn_grid, const void* fn_cluster, bool clust
         attr[0].val.clusterDim.z = 1;
         note(cudaLaunchKernelExC(&cfg, fn_cluster, args));
     } else {
+        // spread the work evenly: k blocks on every SM (k as small as fits), block size
+        // trimmed to the per-SM share, so no SM carries twice the lanes of another
         const int bt = coop_threads();
-        cfg.gridDim = dim3(coop_blocks(fn_grid, work, bt));
-        cfg.blockDim = dim3(bt);
+        const int sms = num_sms();
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn_grid, bt, 0);
+        const int cap = env_int("SMG_COOP_BLOCKS_PER_SM", 0);
+        if (cap > 0 && cap < per_sm) per_sm = cap;
+        const int64_t need = (work + sms - 1) / sms;  // threads per SM
+        int k = static_cast<int>((need + bt - 1) / bt);
+        int threads = bt;
+        if (per_sm > 0 && k <= per_sm && env_int("SMG_EVEN_GRID", 1)) {
+            k = k < 1 ? 1 : k;
+            const int64_t per_block = (work + static_cast<int64_t>(sms) * k - 1) / (static_cast<int64_t>(sms) * k);
+            threads = static_cast<int>((per_block + 31) / 32 * 32);
+            threads = threads < 32 ? 32 : (threads > bt ? bt : threads);
+            cfg.gridDim = dim3(sms * k);
+        } else {
+            cfg.gridDim = dim3(coop_blocks(fn_grid, work, bt));
+        }
+        cfg.blockDim = dim3(threads);
         attr[0].id = cudaLaunchAttributeCooperative;
         attr[0].val.cooperative = 1;
         note(cudaLaunchKernelExC(&cfg, fn_grid, args));
@@ -1740,3 +1780,17 @@ void launch_dx_update(double* d, double* x, const double* q, double cd, double c
 }
 
 }  // namespace smg
+
+#ifdef SMG_TRACE
+extern "C" int smg_trace_enable(long long n) {
+    unsigned long long* p = nullptr;
+    if (cudaMalloc(&p, n * sizeof(unsigned long long)) != cudaSuccess) return -1;
+    cudaMemset(p, 0, n * sizeof(unsigned long long));
+    return cudaMemcpyToSymbol(smg::g_trace, &p, sizeof(p)) == cudaSuccess ? 0 : -1;
+}
+extern "C" int smg_trace_read(unsigned long long* host, long long n) {
+    unsigned long long* p = nullptr;
+    cudaMemcpyFromSymbol(&p, smg::g_trace, sizeof(p));
+    return cudaMemcpy(host, p, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost) == cudaSuccess ? 0 : -1;
+}
+#endif
