@@ -1734,7 +1734,10 @@ static void launch_dgs_sym_phases(const LevelK& L, double* x, const double* b, d
 
 void launch_dgs_sym_coop(const LevelK& L, double* x, const double* b, double* d0, double* d1, int nph,
                          cudaStream_t s) {
-    if (static_cast<int64_t>(L.g.nx) * L.g.ny * L.g.nz > 32768 && env_int("SMG_DGS_COOP", 0) == 0) {
+    // one persistent sweep up to 64^3 cells (measured: a grid barrier beats a kernel
+    // boundary + tail there); larger levels run one kernel per phase
+    const int64_t coop_max = env_int("SMG_DGS_COOP", 0) ? (int64_t{1} << 40) : env_int("SMG_DGS_COOP_MAX", 262144);
+    if (static_cast<int64_t>(L.g.nx) * L.g.ny * L.g.nz > coop_max) {
         launch_dgs_sym_phases(L, x, b, d0, d1, nph, s);
         return;
     }
@@ -1742,7 +1745,7 @@ void launch_dgs_sym_coop(const LevelK& L, double* x, const double* b, double* d0
     LevelK Lc = L;
     void* args[] = {&Lc, &x, const_cast<double**>(&b), &d0, &d1, &nph};
     launch_sweep(reinterpret_cast<const void*>(k_dgs_sym_coop<0>), reinterpret_cast<const void*>(k_dgs_sym_coop<1>),
-                 use_cluster(ncell, 4), ncell, args, s);
+                 use_cluster(ncell, env_int("SMG_DGS_CL_ITEMS", 1)), ncell, args, s);
 }
 
 void launch_sqmr_scalar(int which, double* sc, cudaStream_t s) {
