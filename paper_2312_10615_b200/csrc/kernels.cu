@@ -1051,77 +1051,114 @@ __device__ __forceinline__ void pf_lazy_cell(const LevelK& L, AX X, const double
     pf_store<false>(L, X, D, pf_load(L, X, B, D, x, y, z, true, false));
 }
 
-// Symmetric DGS sweep (20 phases, OD-1) in one persistent launch.  Forward
-// pressure colour c uses delta buffer D[c&1]; its delta step also clears the
-// entries of colour c-2 left in that buffer, so only colour-c entries are
-// non-zero when the apply step gathers.
+// Colour groups of the 8-colour pressure phases.  A pressure phase of colour c
+// reads what phase c' wrote only if c ^ c' is a single bit (axis neighbours
+// share faces / pressures; diagonal neighbours share nothing), so colours of
+// equal popcount commute and each popcount class runs as ONE step: forward
+// 0 | 1,2,4 | 3,5,6 | 7, reverse 7 | 6,5,3 | 4,2,1 | 0.  Every dependent pair
+// keeps its order, so results are bit-identical to the 8-step sequence.
+// Packed as 3 bits per colour, count in bits 9..10.
+__host__ __device__ constexpr int colour_group(int c0, int c1, int c2, int n) {
+    return c0 | (c1 << 3) | (c2 << 6) | (n << 9);
+}
+__host__ __device__ constexpr int group_size(int grp) { return grp >> 9; }
+__host__ __device__ constexpr int group_colour(int grp, int k) { return (grp >> (3 * k)) & 7; }
+__host__ __device__ constexpr int fwd_group(int q) {
+    return q == 0 ? colour_group(0, 0, 0, 1)
+                  : q == 1 ? colour_group(1, 2, 4, 3) : q == 2 ? colour_group(3, 5, 6, 3) : colour_group(7, 0, 0, 1);
+}
+__host__ __device__ constexpr int rev_group(int q) {
+    return q == 0 ? colour_group(7, 0, 0, 1)
+                  : q == 1 ? colour_group(6, 5, 3, 3) : q == 2 ? colour_group(4, 2, 1, 3) : colour_group(0, 0, 0, 1);
+}
+
+// Symmetric DGS sweep (OD-1) in one persistent launch: velocity red, black,
+// the 4 forward pressure groups (lazy gathers, one combined delta buffer D0),
+// the flush, then (nph = 20) the 4 reverse pressure groups and velocity
+// black, red: 13 barrier-separated steps for the 20 phases.
 template <int MODE, class AX = double*, class AD = double*>
 __device__ __forceinline__ void dgs_sweep(const LevelK& L, AX X, const double* __restrict__ B, AD D0, AD D1, int nph,
                                           int64_t tid, int64_t nth) {
+    (void)D1;
     const Geom& g = L.g;
     const int64_t ncell = static_cast<int64_t>(g.nx) * g.ny * g.nz;
     const int64_t nxy = static_cast<int64_t>(g.nx) * g.ny;
-    for (int ph = 0; ph < nph; ++ph) {
-        if (ph == 0 || ph == 1 || ph == 18 || ph == 19) {
-            const int colour = ph < 2 ? ph : 19 - ph;
-            if ((g.nx & 1) == 0) {  // this colour's cells only, two per step (loads of both first)
-                const int hx = g.nx >> 1;
-                const int64_t nc = static_cast<int64_t>(hx) * g.ny * g.nz;
-                auto cell = [&](int64_t t, int& x, int& y, int& z) {
-                    const int64_t r = t / hx;
-                    y = static_cast<int>(r % g.ny);
-                    z = static_cast<int>(r / g.ny);
-                    x = 2 * static_cast<int>(t - r * hx) + ((y + g.gz(z) + colour) & 1);
-                };
-                for (int64_t t = tid; t < nc; t += 2 * nth) {
-                    int x0, y0, z0, x1 = 0, y1 = 0, z1 = 0;
-                    cell(t, x0, y0, z0);
-                    const bool v1 = t + nth < nc;
-                    if (v1) cell(t + nth, x1, y1, z1);
-                    const VelUpd a = vel_load(L, X, B, x0, y0, z0, true);
-                    const VelUpd b = vel_load(L, X, B, x1, y1, z1, v1);
-                    vel_store(L, X, a);
-                    vel_store(L, X, b);
-                }
-            } else {
-                for (int64_t t = tid; t < ncell; t += nth) {
-                    const int z = static_cast<int>(t / nxy);
-                    const int64_t r = t - z * nxy;
-                    const int y = static_cast<int>(r / g.nx), x = static_cast<int>(r - static_cast<int64_t>(y) * g.nx);
-                    if (((x + y + g.gz(z)) & 1) == colour) dgs_vel_cell(L, X, B, x, y, z);
-                }
-            }
-        } else if (ph <= 9) {  // lazy-gather forward pressure phase (see pf_lazy_cell); D0 combined
-            const int c = ph - 2;
-            int x, y, z;
-            for (int64_t t = tid; colour_cell(g, c, t, x, y, z); t += nth) pf_lazy_cell(L, X, B, D0, x, y, z);
-            if (ph == 9) {
-                phase_sync<MODE>();
-                auto cell = [&](int64_t t, int& x, int& y, int& z) {
-                    z = static_cast<int>(t / nxy);
-                    const int64_t r = t - z * nxy;
-                    y = static_cast<int>(r / g.nx);
-                    x = static_cast<int>(r - static_cast<int64_t>(y) * g.nx);
-                };
-                for (int64_t t = tid; t < ncell; t += 2 * nth) {
-                    int x0, y0, z0, x1 = 0, y1 = 0, z1 = 0;
-                    cell(t, x0, y0, z0);
-                    const bool v1 = t + nth < ncell;
-                    if (v1) cell(t + nth, x1, y1, z1);
-                    const PfUpd a = pf_load(L, X, B, D0, x0, y0, z0, true, true);
-                    const PfUpd b = pf_load(L, X, B, D0, x1, y1, z1, v1, true);
-                    pf_store<true>(L, X, D0, a);
-                    pf_store<true>(L, X, D0, b);
-                }
+    auto vel = [&](int colour) {
+        if ((g.nx & 1) == 0) {  // this colour's cells only, two per step (loads of both first)
+            const int hx = g.nx >> 1;
+            const int64_t nc = static_cast<int64_t>(hx) * g.ny * g.nz;
+            auto cell = [&](int64_t t, int& x, int& y, int& z) {
+                const int64_t r = t / hx;
+                y = static_cast<int>(r % g.ny);
+                z = static_cast<int>(r / g.ny);
+                x = 2 * static_cast<int>(t - r * hx) + ((y + g.gz(z) + colour) & 1);
+            };
+            for (int64_t t = tid; t < nc; t += 2 * nth) {
+                int x0, y0, z0, x1 = 0, y1 = 0, z1 = 0;
+                cell(t, x0, y0, z0);
+                const bool v1 = t + nth < nc;
+                if (v1) cell(t + nth, x1, y1, z1);
+                const VelUpd a = vel_load(L, X, B, x0, y0, z0, true);
+                const VelUpd b = vel_load(L, X, B, x1, y1, z1, v1);
+                vel_store(L, X, a);
+                vel_store(L, X, b);
             }
         } else {
-            const int c = 17 - ph;
+            for (int64_t t = tid; t < ncell; t += nth) {
+                const int z = static_cast<int>(t / nxy);
+                const int64_t r = t - z * nxy;
+                const int y = static_cast<int>(r / g.nx), x = static_cast<int>(r - static_cast<int64_t>(y) * g.nx);
+                if (((x + y + g.gz(z)) & 1) == colour) dgs_vel_cell(L, X, B, x, y, z);
+            }
+        }
+    };
+    auto flush = [&]() {
+        auto cell = [&](int64_t t, int& x, int& y, int& z) {
+            z = static_cast<int>(t / nxy);
+            const int64_t r = t - z * nxy;
+            y = static_cast<int>(r / g.nx);
+            x = static_cast<int>(r - static_cast<int64_t>(y) * g.nx);
+        };
+        for (int64_t t = tid; t < ncell; t += 2 * nth) {
+            int x0, y0, z0, x1 = 0, y1 = 0, z1 = 0;
+            cell(t, x0, y0, z0);
+            const bool v1 = t + nth < ncell;
+            if (v1) cell(t + nth, x1, y1, z1);
+            const PfUpd a = pf_load(L, X, B, D0, x0, y0, z0, true, true);
+            const PfUpd b = pf_load(L, X, B, D0, x1, y1, z1, v1, true);
+            pf_store<true>(L, X, D0, a);
+            pf_store<true>(L, X, D0, b);
+        }
+    };
+    vel(0);
+    phase_sync<MODE>();
+    vel(1);
+    phase_sync<MODE>();
+    for (int q = 0; q < 4; ++q) {  // lazy-gather forward pressure groups (see pf_lazy_cell)
+        const int grp = fwd_group(q);
+        for (int k = 0; k < group_size(grp); ++k) {
+            const int c = group_colour(grp, k);
+            int x, y, z;
+            for (int64_t t = tid; colour_cell(g, c, t, x, y, z); t += nth) pf_lazy_cell(L, X, B, D0, x, y, z);
+        }
+        phase_sync<MODE>();
+    }
+    flush();
+    if (nph <= 10) return;
+    phase_sync<MODE>();
+    for (int q = 0; q < 4; ++q) {
+        const int grp = rev_group(q);
+        for (int k = 0; k < group_size(grp); ++k) {
+            const int c = group_colour(grp, k);
             int x, y, z;
             for (int64_t t = tid; colour_cell(g, c, t, x, y, z); t += nth)
                 if (!band_cell(L, x, y, z)) dgs_prev_cell(L, X, B, g.slot(x, y, z));
         }
-        if (ph + 1 < nph) phase_sync<MODE>();
+        phase_sync<MODE>();
     }
+    vel(1);
+    phase_sync<MODE>();
+    vel(0);
 }
 
 template <int MODE>
@@ -1286,14 +1323,18 @@ __global__ void __launch_bounds__(256) k_dgs_pf_apply_c(LevelK L, double* __rest
 }
 
 template <int ZC>
+// grid.z = (z blocks) x (colours of the group), colour fastest so the group's
+// colours of one plane pair run side by side
 __global__ void __launch_bounds__(256) k_dgs_pf_lazy_c(LevelK L, double* __restrict__ X, const double* __restrict__ B,
-                                                       double* __restrict__ D, int c) {
+                                                       double* __restrict__ D, int grp) {
     const Geom& g = L.g;
     const int i = blockIdx.x * 32 + threadIdx.x, j = blockIdx.y * 8 + threadIdx.y;
+    const int nc = group_size(grp), c = group_colour(grp, blockIdx.z % nc);
+    const int kz = blockIdx.z / nc, nkz = gridDim.z / nc;
 #pragma unroll
     for (int q = 0; q < ZC; ++q) {
         int x, y, z;
-        if (half_cell(g, c, i, j, blockIdx.z + q * gridDim.z, x, y, z)) pf_lazy_cell(L, X, B, D, x, y, z);
+        if (half_cell(g, c, i, j, kz + q * nkz, x, y, z)) pf_lazy_cell(L, X, B, D, x, y, z);
     }
 }
 
@@ -1305,13 +1346,15 @@ __global__ void __launch_bounds__(256) k_dgs_pf_flush(LevelK L, double* __restri
 
 template <int ZC>
 __global__ void __launch_bounds__(256) k_dgs_prev_c(LevelK L, double* __restrict__ X, const double* __restrict__ B,
-                                                    int c) {
+                                                    int grp) {
     const Geom& g = L.g;
     const int i = blockIdx.x * 32 + threadIdx.x, j = blockIdx.y * 8 + threadIdx.y;
+    const int nc = group_size(grp), c = group_colour(grp, blockIdx.z % nc);
+    const int kz = blockIdx.z / nc, nkz = gridDim.z / nc;
 #pragma unroll
     for (int q = 0; q < ZC; ++q) {
         int x, y, z;
-        if (half_cell(g, c, i, j, blockIdx.z + q * gridDim.z, x, y, z) && !band_cell(L, x, y, z))
+        if (half_cell(g, c, i, j, kz + q * nkz, x, y, z) && !band_cell(L, x, y, z))
             dgs_prev_cell(L, X, B, g.slot(x, y, z));
     }
 }
@@ -1692,7 +1735,7 @@ void launch_dgs_pf_apply_c(const LevelK& L, double* x, const double* d, int c, c
     count();
 }
 void launch_dgs_prev_c(const LevelK& L, double* x, const double* b, int c, cudaStream_t s) {
-    k_dgs_prev_c<1><<<dgs_grid_h(L.g), dim3(32, 8), 0, s>>>(L, x, b, c);
+    k_dgs_prev_c<1><<<dgs_grid_h(L.g), dim3(32, 8), 0, s>>>(L, x, b, colour_group(c, 0, 0, 1));
     count();
 }
 
@@ -1705,20 +1748,17 @@ static void dgs_sym_phases_zc(const LevelK& L, double* x, const double* b, doubl
     dim3 gv = dgs_grid_v(g), gh = dgs_grid_h(g);
     gv.z = (gv.z + ZC - 1) / ZC;
     gh.z = (gh.z + ZC - 1) / ZC;
-    for (int ph = 0; ph < nph; ++ph) {
-        if (ph == 0 || ph == 1 || ph == 18 || ph == 19) {
-            k_dgs_vel_c<ZC><<<gv, blk, 0, s>>>(L, x, b, ph < 2 ? ph : 19 - ph);
-        } else if (ph <= 9) {
-            k_dgs_pf_lazy_c<ZC><<<gh, blk, 0, s>>>(L, x, b, d0, ph - 2);
-            if (ph == 9) {
-                k_dgs_pf_flush<<<cell_grid(g), blk, 0, s>>>(L, x, d0);
-                count();
-            }
-        } else {
-            k_dgs_prev_c<ZC><<<gh, blk, 0, s>>>(L, x, b, 17 - ph);
-        }
-        count();
-    }
+    auto groups_grid = [&](int grp) { return dim3(gh.x, gh.y, gh.z * group_size(grp)); };
+    k_dgs_vel_c<ZC><<<gv, blk, 0, s>>>(L, x, b, 0);
+    k_dgs_vel_c<ZC><<<gv, blk, 0, s>>>(L, x, b, 1);
+    for (int q = 0; q < 4; ++q) k_dgs_pf_lazy_c<ZC><<<groups_grid(fwd_group(q)), blk, 0, s>>>(L, x, b, d0, fwd_group(q));
+    k_dgs_pf_flush<<<cell_grid(g), blk, 0, s>>>(L, x, d0);
+    for (int k = 0; k < 7; ++k) count();
+    if (nph <= 10) return;
+    for (int q = 0; q < 4; ++q) k_dgs_prev_c<ZC><<<groups_grid(rev_group(q)), blk, 0, s>>>(L, x, b, rev_group(q));
+    k_dgs_vel_c<ZC><<<gv, blk, 0, s>>>(L, x, b, 1);
+    k_dgs_vel_c<ZC><<<gv, blk, 0, s>>>(L, x, b, 0);
+    for (int k = 0; k < 6; ++k) count();
 }
 
 static void launch_dgs_sym_phases(const LevelK& L, double* x, const double* b, double* d0, double* d1, int nph,
