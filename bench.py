@@ -237,7 +237,7 @@ def run_ours(args, ws, rank, local):
     e2e_val = wsum * n * e2e_it / e2e_s
     # ---- roofline of the dominant component (fine-level smooth) + whole iteration ----
     peak, peak_kind = measured_peak_gbs()
-    roof = roofline(s, lv, peak, peak_kind, dev_ms / max(iters, 1))
+    roof = roofline(s, lv, peak, peak_kind, dev_ms / max(iters, 1), f"cfg{args.config}")
     out = None
     if rank == 0:
         cpu = None
@@ -293,7 +293,7 @@ def b_iter_model(cnt, nu=1):
     return b + 8 * nc * nc + 16 * nc
 
 
-def roofline(s, levels, peak, peak_kind, iter_ms):
+def roofline(s, levels, peak, peak_kind, iter_ms, config_key=None):
     """Dominant component: the fine-level smooth (Alg. 3 = nu Vanka + symmetric DGS + nu Vanka), which is
     ~45% of an iteration at cfg 1.  Algorithmic bytes per SURVEY §8(d): 48 B per V2 DOF (symmetric DGS) +
     96 nu B per V1 DOF (two symmetric Vanka sweeps)."""
@@ -307,17 +307,27 @@ def roofline(s, levels, peak, peak_kind, iter_ms):
     alg = 48 * v2 + 96 * v1
     achieved = alg / (smooth_ms / 1e3) / 1e9
     biter = b_iter_model(cnt)
+    # measured DRAM bytes of one fine-level smooth (all its kernels), from the committed ncu
+    # launch list of `tools/profile_kernel.py --which 5 --level 0` (profiles/smooth_traffic.json)
+    traffic = None
+    tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "smooth_traffic.json")
+    if os.path.exists(tpath):
+        rec = json.load(open(tpath)).get(config_key)
+        if rec:
+            traffic = rec["dram_bytes"]
     return {
-        "bound": "hbm", "kernel": "fine-level smooth (Alg. 3: Vanka sweep, 20-phase symmetric DGS, Vanka sweep)",
+        "bound": "hbm",
+        "kernel": "fine-level smooth (Alg. 3: Vanka sweep, symmetric DGS = 20 phases in 13 steps, Vanka sweep)",
         "achieved": achieved, "peak": peak, "peak_source": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-        "traffic": None, "algorithmic_bytes_per_launch": alg, "avg_ms": smooth_ms,
+        "traffic": traffic, "traffic_source": "ncu dram__bytes_read+write, all kernels of one smooth (cold caches)",
+        "algorithmic_bytes_per_launch": alg, "avg_ms": smooth_ms,
         "units": {"N_V2": v2, "N_V1": v1, "bytes_per_V2_dof": 48, "bytes_per_V1_dof": 96},
         "components": {
             "dgs_sym_sweep": {"avg_ms": dgs_ms, "alg_bytes": 48 * v2,
                               "achieved_gbs": 48 * v2 / (dgs_ms / 1e3) / 1e9},
             "vanka_sym_sweep": {"avg_ms": vanka_ms, "alg_bytes": 48 * v1,
                                 "achieved_gbs": 48 * v1 / (vanka_ms / 1e3) / 1e9,
-                                "note": "latency-bound: 32 dependent barrier steps per sweep"},
+                                "note": "latency-bound: 16 dependent barrier steps per sweep"},
             "apply_L": {"avg_ms": apply_ms, "alg_bytes": 16 * n0, "achieved_gbs": 16 * n0 / (apply_ms / 1e3) / 1e9},
         },
         "iteration": {"alg_bytes": biter, "ms": iter_ms, "achieved_gbs": biter / (iter_ms / 1e3) / 1e9,
