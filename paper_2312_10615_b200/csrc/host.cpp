@@ -173,6 +173,7 @@ struct DevLevel {
     int64_t vk_nrefresh = 0;
     int vk_n[8] = {};
     double* ktab = nullptr;  // [64][49]
+    std::vector<WavePass> wave;  // fused wavefront DGS sweep (large single-part levels), empty: per-phase/coop
 };
 
 }  // namespace
@@ -235,6 +236,39 @@ namespace {
 
 int64_t vlen(const DevLevel& L) { return L.k.g.vec_len(); }
 
+int env_int(const char* name, int dflt) {
+    const char* e = std::getenv(name);
+    return e ? std::atoi(e) : dflt;
+}
+
+// Fused wavefront DGS plan (opt-in: SMG_WAVE=1) for levels above SMG_WAVE_MIN_CELLS
+// cells (default: larger than 64^3); SMG_WAVE_MB sets the L2 budget of the live
+// planes.  Measured slower than the per-step kernels on B200 (the
+// per-unit dependency round trips cost more than the L2 reuse saves), so it is
+// kept only as a bit-identical alternative.
+void build_wave(smg_ctx* c, DevLevel& L) {
+    const Geom& g = L.k.g;
+    const int64_t ncell = static_cast<int64_t>(g.nx) * g.ny * g.nz;
+    const bool forced = std::getenv("SMG_WAVE_MIN_CELLS") != nullptr;  // tests: any level, any pass split
+    if (!env_int("SMG_WAVE", 0) || ncell < env_int("SMG_WAVE_MIN_CELLS", 262145)) return;
+    const int nph = (c->prm.flags & SMG_FLAG_SKIP_REVERSE_DGS) ? 10 : 20;
+    std::vector<WaveHostPass> plan = wave_build(L.k, nph, static_cast<int64_t>(env_int("SMG_WAVE_MB", 48)) << 20);
+    if (plan.empty()) return;
+    // fusion only pays when passes hold several steps (else: per-step kernels)
+    int nsteps = 0;
+    for (const WaveHostPass& hp : plan) nsteps += hp.p.nsteps;
+    if (!forced && nsteps < env_int("SMG_WAVE_MIN_STEPS_PER_PASS", 3) * static_cast<int>(plan.size())) return;
+    int* cnt = c->dalloc<int>(1 + static_cast<int64_t>(kWaveMaxSteps) * g.nz);
+    for (WaveHostPass& hp : plan) {
+        uint32_t* d = c->dalloc<uint32_t>(static_cast<int64_t>(hp.units.size()));
+        CK(cudaMemcpyAsync(d, hp.units.data(), hp.units.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, c->st));
+        hp.p.units = d;
+        hp.p.cnt = cnt;
+        L.wave.push_back(hp.p);
+    }
+    CK(cudaStreamSynchronize(c->st));
+}
+
 // ---- setup ----
 void build(smg_ctx* c, const std::vector<double>* shared_coarse = nullptr, std::vector<double>* coarse_out = nullptr,
            cudaStream_t shared_stream = nullptr) {
@@ -291,6 +325,7 @@ void build(smg_ctx* c, const std::vector<double>* shared_coarse = nullptr, std::
         }
         L.pd0 = c->dalloc<double>(L.k.g.fs);
         L.pd1 = c->dalloc<double>(L.k.g.fs);
+        build_wave(c, L);
         // Vanka blocks: band cells, slot + active-face mask, by colour
         const int bw = p.band_width;
         auto band = [&](int x, int y, int z) {
@@ -530,6 +565,10 @@ void dgs_phase(smg_ctx* c, int l, double* x, const double* b, int ph) {
 void symmetric_dgs(smg_ctx* c, int l, double* x, const double* b) {
     const int nph = (c->prm.flags & SMG_FLAG_SKIP_REVERSE_DGS) ? kDgsPhases / 2 : kDgsPhases;
     DevLevel& L = c->lv[l];
+    if (!L.wave.empty()) {
+        launch_dgs_wave(L.k, L.wave.data(), static_cast<int>(L.wave.size()), x, b, L.pd0, c->st);
+        return;
+    }
     launch_dgs_sym_coop(L.k, x, b, L.pd0, L.pd1, nph, c->st);
 }
 

@@ -8,6 +8,7 @@
 // Reference: SPEC.md modules discretization (apply),
 // smoothers (DGS SPEC:258-283, Vanka SPEC:284-301), transfer,
 // multigrid coarse solve, krylov.
+#include <algorithm>
 #include <atomic>
 #include <cstdint>
 #include <cstdlib>
@@ -1359,6 +1360,142 @@ __global__ void __launch_bounds__(256) k_dgs_prev_c(LevelK L, double* __restrict
     }
 }
 
+// ------------------------------------- fused wavefront DGS sweep (large levels) ------
+// See WavePass in smg_internal.h.  A unit is up to kWaveCellsPerUnit cells of
+// one step on one plane, colour-compact (every thread works).
+__host__ __device__ __forceinline__ int wave_group(int kind, int arg) {
+    return kind == WK_PF ? fwd_group(arg) : rev_group(arg);
+}
+// cells of step (kind, arg) on the plane of global parity zpar (nx, ny even)
+__host__ __device__ __forceinline__ int64_t wave_cells(int kind, int arg, int zpar, int nx, int ny) {
+    const int64_t hx = nx / 2, hy = ny / 2;
+    if (kind == WK_VEL) return hx * ny;
+    if (kind == WK_FLUSH) return static_cast<int64_t>(nx) * ny;
+    const int grp = wave_group(kind, arg);
+    int m = 0;
+    for (int k = 0; k < group_size(grp); ++k) m += ((group_colour(grp, k) >> 2) & 1) == zpar;
+    return m * hx * hy;
+}
+__host__ __device__ __forceinline__ int wave_units(int kind, int arg, int zpar, int nx, int ny) {
+    return static_cast<int>((wave_cells(kind, arg, zpar, nx, ny) + kWaveCellsPerUnit - 1) / kWaveCellsPerUnit);
+}
+// work item t of step (kind, arg) on plane z -> cell (x, y)
+__device__ __forceinline__ void wave_cell(const Geom& g, int kind, int arg, int gz, int64_t t, int& x, int& y) {
+    const int hx = g.nx >> 1;
+    if (kind == WK_VEL) {
+        y = static_cast<int>(t / hx);
+        x = 2 * static_cast<int>(t - static_cast<int64_t>(y) * hx) + ((y + gz + arg) & 1);
+    } else if (kind == WK_FLUSH) {
+        y = static_cast<int>(t / g.nx);
+        x = static_cast<int>(t - static_cast<int64_t>(y) * g.nx);
+    } else {
+        const int64_t q = static_cast<int64_t>(hx) * (g.ny >> 1);
+        const int grp = wave_group(kind, arg);
+        int k = static_cast<int>(t / q), c = 0;
+        const int64_t r = t - k * q;
+        for (int j = 0; j < group_size(grp); ++j) {
+            const int cj = group_colour(grp, j);
+            if (((cj >> 2) & 1) != (gz & 1)) continue;
+            if (k-- == 0) { c = cj; break; }
+        }
+        const int j = static_cast<int>(r / hx);
+        x = 2 * static_cast<int>(r - static_cast<int64_t>(j) * hx) + (c & 1);
+        y = 2 * j + ((c >> 1) & 1);
+    }
+}
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+constexpr int kWaveThreads = kWaveCellsPerUnit / 2;
+
+// Persistent loop over tickets.  Warp 0 decodes the unit, its lanes wait on the
+// step-(s-1) plane counters in parallel, and lane 0 prefetches the next ticket
+// before the CTA works on this one (a held-but-unstarted ticket only depends on
+// smaller tickets, so progress is still guaranteed).
+__global__ void __launch_bounds__(kWaveThreads, 3) k_dgs_wave(LevelK L, double* __restrict__ X,
+                                                              const double* __restrict__ B,
+                                                              double* __restrict__ D, WavePass P) {
+    __shared__ uint32_t s_unit;
+    __shared__ int8_t s_kind[kWaveMaxSteps], s_arg[kWaveMaxSteps], s_lo[kWaveMaxSteps], s_hi[kWaveMaxSteps];
+    const Geom& g = L.g;
+    const int tid = threadIdx.x, lane = tid & 31;
+    if (tid == 0) {  // step table in shared memory (static indices: the parameter block stays in constant bank)
+#pragma unroll
+        for (int k = 0; k < kWaveMaxSteps; ++k) {
+            s_kind[k] = P.kind[k];
+            s_arg[k] = P.arg[k];
+            s_lo[k] = P.lo[k];
+            s_hi[k] = P.hi[k];
+        }
+    }
+    __syncthreads();
+    int next = tid == 0 ? atomicAdd(P.cnt, 1) : 0;
+    for (;;) {
+        if (tid < 32) {
+            uint32_t u = 0xffffffffu;
+            if (lane == 0 && next < P.nunits) u = __ldg(P.units + next);
+            u = __shfl_sync(0xffffffffu, u, 0);
+            if (u != 0xffffffffu) {
+                const int s = static_cast<int>(u >> 28), z = static_cast<int>((u >> 16) & 0xfff);
+                if (s > 0) {  // step s-1 done on the planes this unit reads or overwrites
+                    const int zz = z - s_lo[s] + lane;
+                    if (zz >= 0 && zz < g.nz && zz <= z + s_hi[s]) {
+                        const int need = wave_units(s_kind[s - 1], s_arg[s - 1], g.gz(zz) & 1, g.nx, g.ny);
+                        const int* c = P.cnt + 1 + (s - 1) * g.nz + zz;
+                        while (ld_acquire(c) < need) __nanosleep(20);
+                    }
+                    __syncwarp();
+                }
+                if (lane == 0) {
+                    __threadfence();  // acquire side: also drops this SM's L1 lines
+                    next = atomicAdd(P.cnt, 1);
+                }
+            }
+            if (lane == 0) s_unit = u;
+        }
+        __syncthreads();
+        const uint32_t u = s_unit;
+        if (u == 0xffffffffu) return;
+        const int s = static_cast<int>(u >> 28), z = static_cast<int>((u >> 16) & 0xfff);
+        const int kind = s_kind[s], arg = s_arg[s], gz = g.gz(z);
+        const int64_t ncell = wave_cells(kind, arg, gz & 1, g.nx, g.ny);
+        const int64_t t0 = static_cast<int64_t>(u & 0xffff) * kWaveCellsPerUnit + tid;
+        const int64_t t1 = t0 + kWaveThreads;
+        const bool v0 = t0 < ncell, v1 = t1 < ncell;
+        int x0 = 0, y0 = 0, x1 = 0, y1 = 0;
+        if (v0) wave_cell(g, kind, arg, gz, t0, x0, y0);
+        if (v1) wave_cell(g, kind, arg, gz, t1, x1, y1);
+        if (kind == WK_VEL) {
+            const VelUpd a = vel_load(L, X, B, x0, y0, z, v0);
+            const VelUpd b = vel_load(L, X, B, x1, y1, z, v1);
+            vel_store(L, X, a);
+            vel_store(L, X, b);
+        } else if (kind == WK_PF || kind == WK_FLUSH) {
+            const bool fl = kind == WK_FLUSH;
+            const PfUpd a = pf_load(L, X, B, D, x0, y0, z, v0, fl);
+            const PfUpd b = pf_load(L, X, B, D, x1, y1, z, v1, fl);
+            if (fl) {
+                pf_store<true>(L, X, D, a);
+                pf_store<true>(L, X, D, b);
+            } else {
+                pf_store<false>(L, X, D, a);
+                pf_store<false>(L, X, D, b);
+            }
+        } else {
+            // one cell after the other (the radius-2 gather of two cells would spill)
+            if (v0 && !band_cell(L, x0, y0, z)) dgs_prev_cell(L, X, B, g.slot(x0, y0, z));
+            if (v1 && !band_cell(L, x1, y1, z)) dgs_prev_cell(L, X, B, g.slot(x1, y1, z));
+        }
+        __syncthreads();
+        if (tid == 0)  // release: the CTA's stores before the completion count
+            asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(P.cnt + 1 + s * g.nz + z) : "memory");
+    }
+}
+
 // ------------------------------------------------ SQMR device scalars ------
 // Alg. 4 scalar recurrences evaluated on the device (same expressions and
 // order as the oracle), so one SQMR iteration is a fixed kernel sequence that
@@ -1786,6 +1923,87 @@ void launch_dgs_sym_coop(const LevelK& L, double* x, const double* b, double* d0
     void* args[] = {&Lc, &x, const_cast<double**>(&b), &d0, &d1, &nph};
     launch_sweep(reinterpret_cast<const void*>(k_dgs_sym_coop<0>), reinterpret_cast<const void*>(k_dgs_sym_coop<1>),
                  use_cluster(ncell, env_int("SMG_DGS_CL_ITEMS", 1)), ncell, args, s);
+}
+
+// ---- fused wavefront sweep: host plan + launch ----
+std::vector<WaveHostPass> wave_build(const LevelK& L, int nph, int64_t budget) {
+    const Geom& g = L.g;
+    // extra planes between consecutive steps: a unit's dependencies then lie more than
+    // one ticket slice back, so several slices can be in flight at once
+    const int lag = env_int("SMG_WAVE_LAG", 1);
+    std::vector<WaveHostPass> out;
+    if (g.z0 != 0 || g.nz != g.gnz || (g.nx & 1) || (g.ny & 1) || g.nz > 4095) return out;
+    // the 13 steps (kind, arg) of a symmetric sweep; the forward half is the first 7
+    const int8_t kinds[kWaveMaxSteps] = {WK_VEL, WK_VEL, WK_PF, WK_PF, WK_PF, WK_PF, WK_FLUSH,
+                                         WK_PREV, WK_PREV, WK_PREV, WK_PREV, WK_VEL, WK_VEL};
+    const int8_t args[kWaveMaxSteps] = {0, 1, 0, 1, 2, 3, 0, 0, 1, 2, 3, 1, 0};
+    const int nstep = nph <= 10 ? 7 : 13;
+    // z footprint of a step at plane z: reads [z - rd, z + ru], writes [z, z + wu]
+    auto rd = [](int) { return 1; };
+    auto ru = [](int k) { return k == WK_PREV ? 2 : 1; };
+    auto wu = [](int k) { return k == WK_PF ? 1 : 0; };
+    const int64_t plane_bytes = g.sz * 8 * 9;  // x (4 fields), delta, b (4 fields)
+    int s0 = 0;
+    while (s0 < nstep) {
+        WaveHostPass hp;
+        WavePass& p = hp.p;
+        std::vector<int> off;
+        int s1 = s0;
+        while (s1 < nstep) {
+            const int k = kinds[s1], j = s1 - s0;
+            int lo = 0, hi = 0, o = 0;
+            if (j > 0) {
+                const int q = kinds[s1 - 1];
+                // RAW [z-rd-wu', z+ru], WAR [z-ru', z+wu+rd'], WAW [z-wu', z+wu]
+                lo = std::max(std::max(rd(k) + wu(q), ru(q)), wu(q));
+                hi = std::max(std::max(ru(k), wu(k) + rd(q)), wu(k));
+                o = off.back() + hi + 1 + lag;
+            }
+            const int window = o + 1 + 2;
+            if (j > 0 && window * plane_bytes > budget) break;
+            p.kind[j] = kinds[s1];
+            p.arg[j] = args[s1];
+            p.lo[j] = static_cast<int8_t>(lo);
+            p.hi[j] = static_cast<int8_t>(hi);
+            p.window = window;
+            off.push_back(o);
+            ++s1;
+        }
+        p.nsteps = s1 - s0;
+        // ticket order: tau = z + off_s ascending; units of step s at plane z depend only on
+        // step s-1 units with a smaller tau, so any CTA holding a ticket can make progress
+        for (int tau = 0; tau < g.nz + off.back(); ++tau)
+            for (int s = p.nsteps - 1; s >= 0; --s) {
+                const int z = tau - off[s];
+                if (z < 0 || z >= g.nz) continue;
+                const int nu = wave_units(p.kind[s], p.arg[s], g.gz(z) & 1, g.nx, g.ny);
+                for (int u = 0; u < nu; ++u)
+                    hp.units.push_back((static_cast<uint32_t>(s) << 28) | (static_cast<uint32_t>(z) << 16) |
+                                       static_cast<uint32_t>(u));
+            }
+        p.nunits = static_cast<int>(hp.units.size());
+        out.push_back(std::move(hp));
+        s0 = s1;
+    }
+    return out;
+}
+
+void launch_dgs_wave(const LevelK& L, const WavePass* passes, int npass, double* x, const double* b, double* d0,
+                     cudaStream_t s) {
+    static int per_sm = 0;
+    if (!per_sm) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dgs_wave, kWaveThreads, 0);
+        const int cap = env_int("SMG_WAVE_BLOCKS_PER_SM", 0);
+        if (cap > 0 && cap < per_sm) per_sm = cap;
+        if (per_sm < 1) per_sm = 1;
+    }
+    for (int k = 0; k < npass; ++k) {
+        const WavePass& p = passes[k];
+        note(cudaMemsetAsync(p.cnt, 0, (1 + static_cast<size_t>(p.nsteps) * L.g.nz) * sizeof(int), s));
+        const int grid = std::min<int64_t>(p.nunits, static_cast<int64_t>(num_sms()) * per_sm);
+        k_dgs_wave<<<grid, kWaveThreads, 0, s>>>(L, x, b, d0, p);
+        count();
+    }
 }
 
 void launch_sqmr_scalar(int which, double* sc, cudaStream_t s) {

@@ -12,6 +12,8 @@
 #pragma once
 
 #include <cstdint>
+#include <vector>
+
 #include <cuda_runtime.h>
 
 namespace smg {
@@ -145,6 +147,39 @@ void launch_sqmr_scalar(int which, double* sc, cudaStream_t s);
 void launch_axpy_s(double* s_, const double* t, const double* sc, int64_t n, cudaStream_t s);
 void launch_dx_dev(double* d, double* x, const double* q, const double* sc, int64_t n, cudaStream_t s);
 void launch_xpby_dev(double* q, const double* t, const double* sc, int64_t n, cudaStream_t s);
+
+// ---- fused (dataflow wavefront) symmetric DGS sweep, large single-part levels ----
+// The 13 steps of a sweep (vel 0, vel 1, 4 forward pressure groups, flush, 4
+// reverse pressure groups, vel 1, vel 0) run inside ONE persistent launch per
+// pass: work units (step s, plane z, tile u) are taken in ticket order
+// (tau = z + off_s), and a unit starts once step s-1 has completed the planes
+// it reads or overwrites (per-(s,z) completion counters).  A plane is then
+// touched by all steps of the pass while it is still L2-resident, so the sweep
+// reads x and b from HBM once per pass instead of once per step.  Passes are
+// split so that the live plane window fits the L2 budget.  Same per-cell
+// functions and the same order of updates per cell: bit-identical.
+constexpr int kWaveMaxSteps = 13;
+enum WaveKind : int8_t { WK_VEL = 0, WK_PF = 1, WK_FLUSH = 2, WK_PREV = 3 };
+struct WavePass {
+    int nsteps = 0;
+    int8_t kind[kWaveMaxSteps] = {}, arg[kWaveMaxSteps] = {};
+    int8_t lo[kWaveMaxSteps] = {}, hi[kWaveMaxSteps] = {};  // planes of step s-1 a unit of step s waits for
+    const uint32_t* units = nullptr;  // device: packed (s << 28 | z << 16 | u) in ticket order
+    int nunits = 0;
+    int* cnt = nullptr;  // device: [0] ticket counter, [1 + s * nz + z] completed units of (s, z)
+    int window = 0;      // live planes (for the report)
+};
+constexpr int kWaveCellsPerUnit = 512;  // 256 threads x 2 cells
+struct WaveHostPass {
+    WavePass p;
+    std::vector<uint32_t> units;
+};
+// Plan of a sweep (nph = 20 symmetric, 10 forward half) on level L, passes
+// sized to `budget` bytes of live planes.  Empty if the level does not qualify.
+std::vector<WaveHostPass> wave_build(const LevelK& L, int nph, int64_t budget);
+// One pass per entry; cnt must hold 1 + nsteps * nz ints (reset here).
+void launch_dgs_wave(const LevelK& L, const WavePass* passes, int npass, double* x, const double* b, double* d0,
+                     cudaStream_t s);
 
 // Number of our kernels launched so far (per process), for the bench's gpu_launches.
 int64_t launch_count();

@@ -309,3 +309,44 @@ def test_lid_driven_cavity_bitwise():
     assert sto == stg == smg.SMG_CONVERGED and np.array_equal(ho, hg) and np.array_equal(xo, xg)
     u = xg[: (n - 1) * n * n].reshape(n, n, n - 1)
     assert u[:, -1, :].mean() > 0.1 and u[:, 0, :].mean() < u[:, -1, :].mean()
+
+
+@pytest.mark.parametrize("mb", ["1", "48"])
+@pytest.mark.parametrize("shape", [(32, 32, 32, 3), (64, 64, 64, 4), (64, 16, 16, 3), (48, 40, 24, 3)])
+def test_wave_dgs_bitwise(shape, mb, monkeypatch):
+    """Opt-in fused wavefront DGS sweep (forced onto small levels; 1 MB budget = one step
+    per pass, 48 MB = all 13 steps in one pass): bit-identical to the oracle's phase order."""
+    monkeypatch.setenv("SMG_WAVE", "1")
+    monkeypatch.setenv("SMG_WAVE_MIN_CELLS", "1")
+    monkeypatch.setenv("SMG_WAVE_MB", mb)
+    monkeypatch.setenv("SMG_NO_SMEM_SMOOTH", "1")
+    oracle.set_threads(os.cpu_count() or 1)
+    nx, ny, nz, lv = shape
+    o = oracle.Oracle(nx, ny, nz, h=1 / ny, levels=lv)
+    s = smg.Solver(nx, ny, nz, h=1 / ny, levels=lv)
+    for level in range(lv - 1):
+        n = o.ndof(level)
+        x, b = rnd(n, 60 + level), rnd(n, 61 + level)
+        same(s.smoother(smg.OP_SMOOTH, x, b, level), o.smoother(4, x, b, level))
+    b = o.forcing(oracle.FORCE_UNIFORM, 5)
+    same(s.vcycle(b), o.vcycle(b))
+    xo, ho, _, sto = o.sqmr(b, 1e-6, 6)
+    xg, hg, _, stg = s.sqmr(b, 1e-6, 6)
+    assert sto == stg and np.array_equal(ho, hg) and np.array_equal(xo, xg)
+    s.close()
+
+
+def test_wave_dgs_forward_half_bitwise(monkeypatch):
+    """Forward half only (FLAG_SKIP_REVERSE_DGS: 7 steps): wavefront == cooperative sweep."""
+    monkeypatch.setenv("SMG_NO_SMEM_SMOOTH", "1")
+    x, b = None, None
+    out = []
+    for wave in ("0", "1"):
+        monkeypatch.setenv("SMG_WAVE", wave)
+        monkeypatch.setenv("SMG_WAVE_MIN_CELLS", "1")
+        s = smg.Solver(32, levels=3, flags=smg.FLAG_SKIP_REVERSE_DGS)
+        if x is None:
+            x, b = rnd(s.ndof(), 7), rnd(s.ndof(), 8)
+        out.append(s.smoother(smg.OP_SMOOTH, x, b))
+        s.close()
+    same(out[1], out[0])
