@@ -9,11 +9,12 @@ time-to-1e-6 (ms_per_step) and the HBM roofline of the dominant kernel.
 
 --impl reference times the CPU implementation of the path (the oracle port —
 the reference ships no solver) on the host cores.
-Under torchrun (N > 1) rank 0 builds one z-slab decomposed solver over devices
-0..N-1 (one slab per GPU, halo planes exchanged by peer copies
-after every smoother phase, coarse levels replicated) and solves the same
-config (strong scaling); the other ranks join the barriers with zero time and
-the max over ranks is reported.  --replicas runs N independent copies instead.
+Under torchrun (N > 1) every rank builds its own z-slab of the same config on
+its GPU (smg_create_rank: one process per GPU, halo planes by
+NCCL send/recv after every smoother phase, inner-product plane partials by one
+NCCL all-reduce, coarse levels replicated) and the max over ranks of the device
+time is reported (strong scaling).  --replicas runs N independent copies
+instead; SMG_EMULATE_SLABS=1 puts all slabs in rank 0's process on device 0.
 """
 from __future__ import annotations
 
@@ -135,6 +136,19 @@ def barrier(ws):
         dist.barrier()
 
 
+def share_nccl_id(ws, rank):
+    """Rank 0's NCCL unique id (smg_nccl_unique_id), broadcast over the launcher's gloo group."""
+    import paper_2312_10615_b200 as smg
+
+    if ws == 1:
+        return smg.nccl_unique_id()
+    import torch.distributed as dist
+
+    obj = [smg.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    return obj[0]
+
+
 def cpu_sample(cfg, threads, iters=2):
     """Oracle port on host cores: `iters` MG-SQMR iterations of the config (bounded sample)."""
     import oracle
@@ -190,17 +204,20 @@ def run_ours(args, ws, rank, local):
     nx, ny, nz, h, lv, kind, seed, tol, name = CONFIGS[cfg]
     n = ndof(nx, ny, nz)
     slabs = ws > 1 and not args.replicas
-    if slabs and rank != 0:  # rank 0 drives all GPUs of the z-slab decomposition;
-        barrier(ws)          # mirror rank 0's collective sequence: B, B, max, B, max
+    emulate = slabs and os.environ.get("SMG_EMULATE_SLABS")  # 1-GPU box: rank 0 holds all slabs on device 0
+    if emulate and rank != 0:
+        barrier(ws)  # mirror rank 0's collective sequence: B, B, max, B, max
         barrier(ws)
         allmax(0.0, ws)
         barrier(ws)
         allmax(0.0, ws)
         return None
-    devs = list(range(ws))
-    if slabs and os.environ.get("SMG_EMULATE_SLABS"):  # plumbing check on a 1-GPU box: all slabs on device 0
-        devs = [0] * ws
-    s = smg.Solver(nx, ny, nz, h=h, levels=lv, device=local, devices=devs if slabs else None)
+    if emulate:
+        s = smg.Solver(nx, ny, nz, h=h, levels=lv, devices=[0] * ws)
+    elif slabs:  # one process per GPU: this rank's z-slab, NCCL halos / reductions (smg_create_rank)
+        s = smg.Solver.for_rank(rank, ws, share_nccl_id(ws, rank), nx, ny, nz, h=h, levels=lv, device=local)
+    else:
+        s = smg.Solver(nx, ny, nz, h=h, levels=lv, device=local)
     wsum = 1 if slabs else ws  # problem copies solved (replicas) -> aggregate DOF/s
     # host input in pinned memory (e2e path) and the same b resident in HBM
     bpin = smg.PinnedArray(n)
@@ -237,7 +254,8 @@ def run_ours(args, ws, rank, local):
     e2e_val = wsum * n * e2e_it / e2e_s
     # ---- roofline of the dominant component (fine-level smooth) + whole iteration ----
     peak, peak_kind = measured_peak_gbs()
-    roof = roofline(s, lv, peak, peak_kind, dev_ms / max(iters, 1), f"cfg{args.config}")
+    roof = roofline(s, lv, peak, peak_kind, dev_ms / max(iters, 1), f"cfg{args.config}",
+                    share=1.0 / ws if slabs and not emulate else 1.0)
     out = None
     if rank == 0:
         cpu = None
@@ -293,12 +311,14 @@ def b_iter_model(cnt, nu=1):
     return b + 8 * nc * nc + 16 * nc
 
 
-def roofline(s, levels, peak, peak_kind, iter_ms, config_key=None):
+def roofline(s, levels, peak, peak_kind, iter_ms, config_key=None, share=1.0):
     """Dominant component: the fine-level smooth (Alg. 3 = nu Vanka + symmetric DGS + nu Vanka), which is
     ~45% of an iteration at cfg 1.  Algorithmic bytes per SURVEY §8(d): 48 B per V2 DOF (symmetric DGS) +
     96 nu B per V1 DOF (two symmetric Vanka sweeps)."""
     cnt = level_counts(s, levels)
     n0, v1, v2 = cnt[0]
+    if share != 1.0:  # one rank of a z-slab run: its kernels cover its share of the fine level
+        v1, v2, n0 = v1 * share, v2 * share, n0 * share
     reps = 5
     smooth_ms = s.time_kernel(5, reps, 0)
     dgs_ms = s.time_kernel(2, reps, 0)
@@ -331,7 +351,8 @@ def roofline(s, levels, peak, peak_kind, iter_ms, config_key=None):
             "apply_L": {"avg_ms": apply_ms, "alg_bytes": 16 * n0, "achieved_gbs": 16 * n0 / (apply_ms / 1e3) / 1e9},
         },
         "iteration": {"alg_bytes": biter, "ms": iter_ms, "achieved_gbs": biter / (iter_ms / 1e3) / 1e9,
-                      "frac": biter / (iter_ms / 1e3) / 1e9 / peak, "model": "SURVEY §8(d) B_iter"},
+                      "frac": biter / (iter_ms / 1e3) / 1e9 / (peak / share), "model": "SURVEY §8(d) B_iter",
+                      "peak_gbs_all_gpus": peak / share},
     }
 
 

@@ -86,6 +86,21 @@ typedef struct smg_timing {
  * Results are bit-identical for every ngpu. */
 int smg_create(const smg_grid_desc* grid, const smg_params* params, int ngpu, const int* dev_ids,
                smg_ctx** out);
+/* Multi-process z-slab decomposition: one process per GPU, NCCL over NVLink.
+ * Rank 0 calls smg_nccl_unique_id and the caller's launcher (torch.distributed,
+ * MPI, ...) broadcasts the 128-byte id; every rank then calls smg_create_rank
+ * with its own device.  The context holds the rank's slab of the distributed
+ * levels (smg_slab_plan) and a replicated copy of the coarser ones; halo planes
+ * travel by ncclSend/ncclRecv with the z neighbours, the canonical plane
+ * partials of every inner product by one ncclAllReduce, the restricted residual
+ * of the first replicated level by ncclAllGather.  Every later call on the
+ * context is collective (same calls, same order on all ranks); host vectors
+ * are the full compact FieldVector on every rank.  Results are bit-identical
+ * to one GPU.  libnccl.so.2 is loaded at run time (SMG_NCCL_LIB overrides the
+ * name), so single-process contexts never need NCCL. */
+int smg_nccl_unique_id(unsigned char id[128]);
+int smg_create_rank(const smg_grid_desc* grid, const smg_params* params, int rank, int nranks, int device,
+                    const unsigned char id[128], smg_ctx** out);
 void smg_destroy(smg_ctx* ctx);
 /* assemble_rhs, host only: adds the Dirichlet-data contributions
  * of a scenario to b (compact order).  scenario 0: lid-driven cavity (PAPER:368,

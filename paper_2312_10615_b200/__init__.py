@@ -54,6 +54,7 @@ EXPORTED = [
     "smg_vcycle", "smg_sqmr_solve", "smg_set_rhs", "smg_solve_resident", "smg_get_solution",
     "smg_last_timing", "smg_time_kernel", "smg_host_alloc", "smg_host_free", "smg_forcing",
     "smg_profiler_range", "smg_slab_plan", "smg_mg_solve", "smg_census", "smg_assemble_rhs",
+    "smg_nccl_unique_id", "smg_create_rank",
 ]
 
 _lib = None
@@ -72,6 +73,9 @@ def lib():
     L.smg_create.argtypes = [C.POINTER(GridDesc), C.POINTER(Params), C.c_int, C.POINTER(C.c_int),
                              C.POINTER(P)]
     L.smg_destroy.argtypes = [P]
+    L.smg_nccl_unique_id.argtypes = [C.c_char_p]
+    L.smg_create_rank.argtypes = [C.POINTER(GridDesc), C.POINTER(Params), C.c_int, C.c_int, C.c_int, C.c_char_p,
+                                  C.POINTER(P)]
     L.smg_last_error.restype = C.c_char_p
     L.smg_last_error.argtypes = [P]
     L.smg_version.restype = C.c_char_p
@@ -163,6 +167,15 @@ class PinnedArray:
             self.ptr = None
 
 
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id (smg_nccl_unique_id) for Solver.for_rank; call on rank 0 only."""
+    buf = C.create_string_buffer(128)
+    rc = lib().smg_nccl_unique_id(buf)
+    if rc != 0:
+        raise SmgError(f"smg_nccl_unique_id failed ({rc}); see stderr")
+    return buf.raw
+
+
 class Solver:
     """One device context (hierarchy + buffers) for a walled box of nx*ny*nz cells."""
 
@@ -185,6 +198,30 @@ class Solver:
         self._ctx = ctx
         self.levels = L.smg_num_levels(ctx)
         self.dims = (nx, ny, nz)
+
+    @classmethod
+    def for_rank(cls, rank, nranks, nccl_id, nx, ny=None, nz=None, h=None, eta=1.0, gamma=1e-3, levels=2, nu=1,
+                 band_width=1, flags=0, device=0, cycle=0):
+        """Rank `rank` of a one-process-per-GPU z-slab solver (smg_create_rank): every rank
+        calls this with the same 128-byte NCCL id (nccl_unique_id() on rank 0, broadcast by
+        the launcher) and its own device; later calls are collective."""
+        ny = nx if ny is None else ny
+        nz = nx if nz is None else nz
+        h = 1.0 / nx if h is None else h
+        self = cls.__new__(cls)
+        self.grid = GridDesc(3, nx, ny, nz, h)
+        self.params = Params(eta, gamma, levels, nu, band_width, flags, cycle)
+        if len(nccl_id) != 128:
+            raise ValueError("NCCL unique id must be 128 bytes")
+        ctx = C.c_void_p()
+        rc = lib().smg_create_rank(C.byref(self.grid), C.byref(self.params), rank, nranks, device,
+                                   bytes(nccl_id), C.byref(ctx))
+        if rc != 0:
+            raise SmgError(f"smg_create_rank failed ({rc}); see stderr")
+        self._ctx = ctx
+        self.levels = lib().smg_num_levels(ctx)
+        self.dims = (nx, ny, nz)
+        return self
 
     def close(self):
         if getattr(self, "_ctx", None):

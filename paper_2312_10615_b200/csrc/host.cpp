@@ -17,10 +17,13 @@
 #include <stdexcept>
 #include <string>
 #include <thread>
+#include <type_traits>
 #include <vector>
 
 #include <cuda_profiler_api.h>
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>  // types only: libnccl.so.2 is loaded at run time (single-process contexts never need it)
 
 #include "../../include/smg.h"
 #include "smg_internal.h"
@@ -39,6 +42,59 @@ struct SmgError : std::runtime_error {
         cudaError_t e_ = (call);                                                                  \
         if (e_ != cudaSuccess)                                                                    \
             throw SmgError(SMG_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_));        \
+    } while (0)
+
+// ---- NCCL, resolved with dlopen on first use (multi-process z-slab contexts only) ----
+struct NcclApi {
+    decltype(&ncclGetUniqueId) getUniqueId = nullptr;
+    decltype(&ncclCommInitRank) commInitRank = nullptr;
+    decltype(&ncclCommDestroy) commDestroy = nullptr;
+    decltype(&ncclGroupStart) groupStart = nullptr;
+    decltype(&ncclGroupEnd) groupEnd = nullptr;
+    decltype(&ncclSend) send = nullptr;
+    decltype(&ncclRecv) recv = nullptr;
+    decltype(&ncclAllReduce) allReduce = nullptr;
+    decltype(&ncclAllGather) allGather = nullptr;
+    decltype(&ncclBroadcast) broadcast = nullptr;
+    decltype(&ncclGetErrorString) errorString = nullptr;
+    std::string err;
+};
+
+const NcclApi& nccl() {
+    static NcclApi api = [] {
+        NcclApi a;
+        const char* name = std::getenv("SMG_NCCL_LIB");
+        void* h = dlopen(name ? name : "libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) {
+            a.err = std::string("dlopen libnccl.so.2: ") + dlerror();
+            return a;
+        }
+        auto sym = [&](auto& f, const char* n) { f = reinterpret_cast<std::remove_reference_t<decltype(f)>>(dlsym(h, n)); };
+        sym(a.getUniqueId, "ncclGetUniqueId");
+        sym(a.commInitRank, "ncclCommInitRank");
+        sym(a.commDestroy, "ncclCommDestroy");
+        sym(a.groupStart, "ncclGroupStart");
+        sym(a.groupEnd, "ncclGroupEnd");
+        sym(a.send, "ncclSend");
+        sym(a.recv, "ncclRecv");
+        sym(a.allReduce, "ncclAllReduce");
+        sym(a.allGather, "ncclAllGather");
+        sym(a.broadcast, "ncclBroadcast");
+        sym(a.errorString, "ncclGetErrorString");
+        if (!a.getUniqueId || !a.commInitRank || !a.commDestroy || !a.groupStart || !a.groupEnd || !a.send ||
+            !a.recv || !a.allReduce || !a.allGather || !a.broadcast || !a.errorString)
+            a.err = "libnccl.so.2: missing symbols";
+        return a;
+    }();
+    if (!api.err.empty()) throw SmgError(SMG_ENCCL, api.err);
+    return api;
+}
+
+#define NK(call)                                                                                  \
+    do {                                                                                          \
+        ncclResult_t r_ = (call);                                                                 \
+        if (r_ != ncclSuccess)                                                                    \
+            throw SmgError(SMG_ENCCL, std::string(#call) + ": " + nccl().errorString(r_));        \
     } while (0)
 
 void host_parallel(int64_t n, int threads, const std::function<void(int64_t, int64_t)>& body) {
@@ -209,6 +265,10 @@ struct smg_ctx {
     std::vector<std::unique_ptr<smg_ctx>> owned;   // parts 1..P-1 (owned by the master)
     double* shared_partials = nullptr;             // plane partials all parts write (master's device)
     bool own_stream = true;
+    // multi-process mode (smg_create_rank): this process holds part `rank` only; halos,
+    // plane partials and gathers travel through NCCL on the part's stream
+    bool mp = false;
+    ncclComm_t comm = nullptr;
 
     template <class T>
     T* dalloc(int64_t count) {
@@ -228,6 +288,7 @@ struct smg_ctx {
         if (graph) cudaGraphExecDestroy(graph);
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);
+        if (comm) nccl().commDestroy(comm);
         if (st && own_stream) cudaStreamDestroy(st);
     }
 };
@@ -775,8 +836,33 @@ void part_barrier(smg_ctx* m) {
     CK(cudaSetDevice(m->device));
 }
 
+// multi-process halo exchange of this rank's slab vector `v` (geometry g, nf fields):
+// the same 2-plane transfers as the in-process copies below, as NCCL send/recv
+// pairs with the z neighbours (rank -+ 1), grouped into one launch on the part stream
+void halo_nccl(smg_ctx* m, double* v, const Geom& g, int nf) {
+    const NcclApi& N = nccl();
+    const size_t n2 = static_cast<size_t>(2 * g.sz);
+    NK(N.groupStart());
+    for (int f = 0; f < nf; ++f) {
+        double* a = v + f * g.fs;
+        if (m->rank + 1 < m->nparts) {  // top halo (planes nz, nz+1) <-> upper part's planes 0, 1
+            NK(N.send(a + (g.zg + g.nz - 2) * g.sz, n2, ncclDouble, m->rank + 1, m->comm, m->st));
+            NK(N.recv(a + (g.zg + g.nz) * g.sz, n2, ncclDouble, m->rank + 1, m->comm, m->st));
+        }
+        if (m->rank > 0) {  // bottom halo (planes -2, -1) <-> lower part's planes nz-2, nz-1
+            NK(N.send(a + g.zg * g.sz, n2, ncclDouble, m->rank - 1, m->comm, m->st));
+            NK(N.recv(a, n2, ncclDouble, m->rank - 1, m->comm, m->st));
+        }
+    }
+    NK(N.groupEnd());
+}
+
 // halo exchange of a slab level: 2 planes each way between neighbours; nf fields
 void exchange(smg_ctx* m, int l, Sel sel, int nf) {
+    if (m->mp) {
+        halo_nccl(m, sel(m->lv[l]), m->lv[l].k.g, nf);
+        return;
+    }
     part_barrier(m);
     for (size_t p = 0; p + 1 < m->parts.size(); ++p) {
         DevLevel &lo = m->parts[p]->lv[l], &hi = m->parts[p + 1]->lv[l];
@@ -794,8 +880,19 @@ void exchange(smg_ctx* m, int l, Sel sel, int nf) {
 
 // every part's owned coarse planes [z0c, z0c + nzc) of a replicated level -> all parts
 void allgather_planes(smg_ctx* m, int l, Sel sel, int nzc) {
-    part_barrier(m);
     const Geom& g = m->lv[l].k.g;
+    if (m->mp) {  // per field, the parts' plane ranges are contiguous and rank-ordered: in-place all-gather
+        const NcclApi& N = nccl();
+        const size_t cnt = static_cast<size_t>(nzc) * g.sz;
+        NK(N.groupStart());
+        for (int f = 0; f < 4; ++f) {
+            double* base = sel(m->lv[l]) + f * g.fs + g.zg * g.sz;
+            NK(N.allGather(base + m->rank * cnt, base, cnt, ncclDouble, m->comm, m->st));
+        }
+        NK(N.groupEnd());
+        return;
+    }
+    part_barrier(m);
     const size_t pitch = g.fs * sizeof(double), width = nzc * g.sz * sizeof(double);
     for (size_t p = 0; p < m->parts.size(); ++p)
         for (size_t q = 0; q < m->parts.size(); ++q) {
@@ -890,6 +987,14 @@ void dist_vcycle(smg_ctx* m, int l) {
 // (global plane indices), barrier, then the fixed-order final on every part.
 void dist_dot2(smg_ctx* m, double* (*a)(smg_ctx*), double* (*b)(smg_ctx*), double* (*c2)(smg_ctx*),
                double* (*d)(smg_ctx*)) {
+    if (m->mp) {  // own planes' partials (zeros elsewhere), summed over ranks: x + 0 = x exactly
+        const Geom& g = m->lv[0].k.g;
+        CK(cudaMemsetAsync(m->shared_partials, 0, kPartials * sizeof(double), m->st));
+        launch_cdot_planes(g, a(m), b(m), c2 ? c2(m) : nullptr, d ? d(m) : nullptr, m->shared_partials, m->st);
+        NK(nccl().allReduce(m->shared_partials, m->shared_partials, kPartials, ncclDouble, ncclSum, m->comm, m->st));
+        launch_cdot_final(g, m->shared_partials, m->dscal + S_D0, m->st);
+        return;
+    }
     each(m, [&](smg_ctx* p) {
         launch_cdot_planes(p->lv[0].k.g, a(p), b(p), c2 ? c2(p) : nullptr, d ? d(p) : nullptr, m->shared_partials, p->st);
     });
@@ -906,6 +1011,10 @@ double* v_r(smg_ctx* p) { return p->lv[0].r; }
 
 // exchange of a fine-level SQMR vector (not a DevLevel member)
 void exchange_vec(smg_ctx* m, double* (*v)(smg_ctx*)) {
+    if (m->mp) {
+        halo_nccl(m, v(m), m->lv[0].k.g, 4);
+        return;
+    }
     part_barrier(m);
     for (size_t p = 0; p + 1 < m->parts.size(); ++p) {
         smg_ctx *lo = m->parts[p], *hi = m->parts[p + 1];
@@ -931,15 +1040,39 @@ void dist_download(smg_ctx* m, double* (*v)(smg_ctx*), double* host) {
     const DevLevel& L0 = m->lv[0];
     const int nx = m->grid.nx, ny = m->grid.ny, gnz = m->grid.nz;
     const int64_t nu = L0.counts[0], nv = L0.counts[1], nw = L0.counts[2];
-    each(m, [&](smg_ctx* p) {
-        launch_pack(p->lv[0].k, v(p), p->compact, p->st);
-        const int z0 = p->lv[0].k.g.z0, z1 = z0 + p->lv[0].k.g.nz;
-        const int64_t r[4][2] = {
+    // compact ranges of the planes [z0, z1): u, v, w (faces z >= 1), p
+    auto ranges = [&](int z0, int z1, int64_t r[4][2]) {
+        const int64_t q[4][2] = {
             {static_cast<int64_t>(z0) * ny * (nx - 1), static_cast<int64_t>(z1) * ny * (nx - 1)},
             {nu + static_cast<int64_t>(z0) * (ny - 1) * nx, nu + static_cast<int64_t>(z1) * (ny - 1) * nx},
             {nu + nv + static_cast<int64_t>(std::max(z0, 1) - 1) * ny * nx,
              nu + nv + static_cast<int64_t>(std::min(z1, gnz) - 1) * ny * nx},
             {nu + nv + nw + static_cast<int64_t>(z0) * ny * nx, nu + nv + nw + static_cast<int64_t>(z1) * ny * nx}};
+        std::memcpy(r, q, sizeof(q));
+    };
+    if (m->mp) {  // every rank's ranges broadcast from their owner, then the whole vector to the host
+        launch_pack(m->lv[0].k, v(m), m->compact, m->st);
+        const NcclApi& N = nccl();
+        const int nzl = m->lv[0].k.g.nz;
+        NK(N.groupStart());
+        for (int r = 0; r < m->nparts; ++r) {
+            int64_t rg[4][2];
+            ranges(r * nzl, (r + 1) * nzl, rg);
+            for (auto& q : rg)
+                if (q[1] > q[0])
+                    NK(N.broadcast(m->compact + q[0], m->compact + q[0], static_cast<size_t>(q[1] - q[0]), ncclDouble,
+                                   r, m->comm, m->st));
+        }
+        NK(N.groupEnd());
+        CK(cudaMemcpyAsync(host, m->compact, L0.N * sizeof(double), cudaMemcpyDeviceToHost, m->st));
+        CK(cudaStreamSynchronize(m->st));
+        return;
+    }
+    each(m, [&](smg_ctx* p) {
+        launch_pack(p->lv[0].k, v(p), p->compact, p->st);
+        const int z0 = p->lv[0].k.g.z0, z1 = z0 + p->lv[0].k.g.nz;
+        int64_t r[4][2];
+        ranges(z0, z1, r);
         for (auto& rg : r)
             if (rg[1] > rg[0])
                 CK(cudaMemcpyAsync(host + rg[0], p->compact + rg[0], (rg[1] - rg[0]) * sizeof(double),
@@ -1104,16 +1237,21 @@ int64_t smg_census(const smg_grid_desc* grid, int band_width, int64_t* out2) {
     return n;
 }
 
+// leading levels that split into nparts z-slabs (slab >= 2 planes, aligned with the finer level)
+static int slab_levels(const smg_grid_desc* grid, int levels, int nparts) {
+    int nd = 0;
+    for (int l = 0; l + 1 < levels; ++l) {
+        const int nz = grid->nz >> l;
+        if (nz % nparts || nz / nparts < 2) break;                    // slab of >= 2 planes (halo depth)
+        if (l > 0 && ((grid->nz >> (l - 1)) / nparts) % 2) break;    // slab boundaries aligned with level l-1
+        nd = l + 1;
+    }
+    return nd;
+}
+
 int smg_slab_plan(const smg_grid_desc* grid, int levels, int nparts, int rank, int* z0, int* nzl) {
     if (!grid || levels < 1 || nparts < 1 || rank < 0 || rank >= nparts) return SMG_EINVAL;
-    int nd = 0;
-    if (nparts > 1)
-        for (int l = 0; l + 1 < levels; ++l) {
-            const int nz = grid->nz >> l;
-            if (nz % nparts || nz / nparts < 2) break;                    // slab of >= 2 planes (halo depth)
-            if (l > 0 && ((grid->nz >> (l - 1)) / nparts) % 2) break;    // slab boundaries aligned with level l-1
-            nd = l + 1;
-        }
+    const int nd = nparts > 1 ? slab_levels(grid, levels, nparts) : 0;
     for (int l = 0; l < levels; ++l) {
         const int nz = grid->nz >> l;
         const bool d = l < nd;
@@ -1176,6 +1314,61 @@ int smg_create(const smg_grid_desc* grid, const smg_params* params, int ngpu, co
     return 0;
 }
 
+int smg_nccl_unique_id(unsigned char id[128]) {
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+    if (!id) return SMG_EINVAL;
+    try {
+        ncclUniqueId u;
+        NK(nccl().getUniqueId(&u));
+        std::memcpy(id, &u, sizeof(u));
+        return 0;
+    } catch (const SmgError& e) {
+        std::fprintf(stderr, "smg_nccl_unique_id: %s\n", e.what());
+        return e.code;
+    }
+}
+
+int smg_create_rank(const smg_grid_desc* grid, const smg_params* params, int rank, int nranks, int device,
+                    const unsigned char id[128], smg_ctx** out) {
+    if (!grid || !params || !out || !id || nranks < 1 || nranks > 1024 || rank < 0 || rank >= nranks)
+        return SMG_EINVAL;
+    *out = nullptr;
+    auto c = std::make_unique<smg_ctx>();
+    c->grid = *grid;
+    c->prm = *params;
+    c->device = device;
+    c->rank = rank;
+    c->nparts = nranks;
+    c->mp = true;
+    c->parts.push_back(c.get());
+    const int rc = guard(c.get(), [&] {
+        // SMG_FORCE_SLABS=1 with one rank: the slab path on one part (exercises the NCCL transport on one GPU)
+        const bool force = nranks == 1 && std::getenv("SMG_FORCE_SLABS") && std::atoi(std::getenv("SMG_FORCE_SLABS"));
+        if (nranks > 1 || force) {
+            const int nd = slab_levels(grid, params->levels, nranks);
+            if (nd <= 0) throw SmgError(SMG_EINVAL, "grid too small for a z-slab split over nranks parts");
+            c->ndist = nd;
+        } else {
+            c->nparts = 1;
+            c->mp = false;  // one rank, no slabs: the single-part path
+        }
+        CK(cudaSetDevice(device));
+        build(c.get());
+        if (c->mp) {
+            ncclUniqueId u;
+            std::memcpy(&u, id, sizeof(u));
+            NK(nccl().commInitRank(&c->comm, nranks, u, rank));
+            c->shared_partials = c->dalloc<double>(kPartials);
+        }
+    });
+    if (rc != 0) {
+        std::fprintf(stderr, "smg_create_rank: %s\n", c->err.c_str());
+        return rc;
+    }
+    *out = c.release();
+    return 0;
+}
+
 void smg_destroy(smg_ctx* ctx) { delete ctx; }
 
 const char* smg_last_error(const smg_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
@@ -1193,7 +1386,7 @@ int64_t smg_level_ndof(const smg_ctx* ctx, int level, int64_t* out5) {
 int smg_apply(smg_ctx* c, int level, int penalized, const double* x, double* y) {
     return guard(c, [&] {
         check_level(c, level);
-        if (c->nparts > 1) {
+        if (c->ndist > 0) {
             if (level != 0) throw SmgError(SMG_EINVAL, "z-slab contexts: apply on level 0 only");
             dist_upload(c, x, v_t);
             each(c, [&](smg_ctx* p) {
@@ -1211,7 +1404,7 @@ int smg_apply(smg_ctx* c, int level, int penalized, const double* x, double* y) 
 
 int smg_residual(smg_ctx* c, int level, const double* x, const double* b, double* r) {
     return guard(c, [&] {
-        if (c->nparts > 1) throw SmgError(SMG_EINVAL, "single-part entry point (use ngpu = 1)");
+        if (c->ndist > 0) throw SmgError(SMG_EINVAL, "single-part entry point (use ngpu = 1)");
         check_level(c, level);
         DevLevel& L = c->lv[level];
         upload(c, level, x, L.x);
@@ -1223,7 +1416,7 @@ int smg_residual(smg_ctx* c, int level, const double* x, const double* b, double
 
 int smg_smoother(smg_ctx* c, int level, int op, int arg, double* x, const double* b) {
     return guard(c, [&] {
-        if (c->nparts > 1) throw SmgError(SMG_EINVAL, "single-part entry point (use ngpu = 1)");
+        if (c->ndist > 0) throw SmgError(SMG_EINVAL, "single-part entry point (use ngpu = 1)");
         check_level(c, level);
         DevLevel& L = c->lv[level];
         upload(c, level, x, L.x);
@@ -1248,7 +1441,7 @@ int smg_smoother(smg_ctx* c, int level, int op, int arg, double* x, const double
 
 int smg_restrict(smg_ctx* c, int level, const double* rf, double* rc) {
     return guard(c, [&] {
-        if (c->nparts > 1) throw SmgError(SMG_EINVAL, "single-part entry point (use ngpu = 1)");
+        if (c->ndist > 0) throw SmgError(SMG_EINVAL, "single-part entry point (use ngpu = 1)");
         check_level(c, level);
         check_level(c, level + 1);
         DevLevel &F = c->lv[level], &C = c->lv[level + 1];
@@ -1260,7 +1453,7 @@ int smg_restrict(smg_ctx* c, int level, const double* rf, double* rc) {
 
 int smg_prolong(smg_ctx* c, int level, const double* xc, double* xf) {
     return guard(c, [&] {
-        if (c->nparts > 1) throw SmgError(SMG_EINVAL, "single-part entry point (use ngpu = 1)");
+        if (c->ndist > 0) throw SmgError(SMG_EINVAL, "single-part entry point (use ngpu = 1)");
         check_level(c, level);
         check_level(c, level + 1);
         DevLevel &F = c->lv[level], &C = c->lv[level + 1];
@@ -1273,7 +1466,7 @@ int smg_prolong(smg_ctx* c, int level, const double* xc, double* xf) {
 
 int smg_coarse_solve(smg_ctx* c, const double* b, double* x) {
     return guard(c, [&] {
-        if (c->nparts > 1) throw SmgError(SMG_EINVAL, "single-part entry point (use ngpu = 1)");
+        if (c->ndist > 0) throw SmgError(SMG_EINVAL, "single-part entry point (use ngpu = 1)");
         const int l = static_cast<int>(c->lv.size()) - 1;
         DevLevel& C = c->lv[l];
         upload(c, l, b, C.b);
@@ -1284,7 +1477,7 @@ int smg_coarse_solve(smg_ctx* c, const double* b, double* x) {
 
 int smg_vcycle(smg_ctx* c, const double* b, double* x) {
     return guard(c, [&] {
-        if (c->nparts > 1) {
+        if (c->ndist > 0) {
             dist_upload(c, b, v_s);
             dist_vcycle(c, 0);
             dist_download(c, v_t, x);
@@ -1300,7 +1493,7 @@ int smg_vcycle(smg_ctx* c, const double* b, double* x) {
 int smg_mg_solve(smg_ctx* c, const double* b, double* x, double tol, int maxit, smg_history* hist, int* status) {
     return guard(c, [&] {
         if (!b || !x || !status) throw SmgError(SMG_EINVAL, "null argument");
-        if (c->nparts > 1) throw SmgError(SMG_EINVAL, "single-part entry point (use ngpu = 1)");
+        if (c->ndist > 0) throw SmgError(SMG_EINVAL, "single-part entry point (use ngpu = 1)");
         DevLevel& F = c->lv[0];
         const int64_t n = vlen(F);
         double* sc = c->dscal;
@@ -1351,7 +1544,7 @@ int smg_mg_solve(smg_ctx* c, const double* b, double* x, double tol, int maxit, 
 
 int smg_set_rhs(smg_ctx* c, const double* b) {
     return guard(c, [&] {
-        if (c->nparts > 1) {
+        if (c->ndist > 0) {
             dist_upload(c, b, v_rhs);
             c->rhs_set = true;
             return;
@@ -1366,14 +1559,14 @@ int smg_solve_resident(smg_ctx* c, double tol, int maxit, smg_history* hist, int
     return guard(c, [&] {
         if (!c->rhs_set) throw SmgError(SMG_EINVAL, "smg_set_rhs not called");
         if (!status) throw SmgError(SMG_EINVAL, "status is null");
-        if (c->nparts > 1) dist_sqmr(c, tol, maxit, hist, status);
+        if (c->ndist > 0) dist_sqmr(c, tol, maxit, hist, status);
         else sqmr(c, tol, maxit, hist, status);
     });
 }
 
 int smg_get_solution(smg_ctx* c, double* x) {
     return guard(c, [&] {
-        if (c->nparts > 1) dist_download(c, v_xs, x);
+        if (c->ndist > 0) dist_download(c, v_xs, x);
         else download(c, 0, c->xs, x);
     });
 }
@@ -1381,7 +1574,7 @@ int smg_get_solution(smg_ctx* c, double* x) {
 int smg_sqmr_solve(smg_ctx* c, const double* b, double* x, double tol, int maxit, smg_history* hist, int* status) {
     return guard(c, [&] {
         if (!b || !x || !status) throw SmgError(SMG_EINVAL, "null argument");
-        if (c->nparts > 1) {
+        if (c->ndist > 0) {
             dist_upload(c, b, v_rhs);
             c->rhs_set = true;
             dist_sqmr(c, tol, maxit, hist, status);

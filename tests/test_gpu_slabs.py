@@ -51,3 +51,21 @@ def test_resident_path_slabs():
     many.set_rhs(b)
     h2, st = many.solve_resident(1e-6, 100)
     assert st == 0 and np.array_equal(h1, h2) and np.array_equal(many.solution(), x1)
+
+
+def test_nccl_rank_path_bitwise(monkeypatch):
+    """smg_create_rank (one process per GPU, NCCL transport) with one rank and the slab path
+    forced: NCCL all-reduce of the plane partials, in-place all-gather of the first replicated
+    level, per-rank broadcast of the solution and (empty) halo groups; bit-identical to 1 part."""
+    monkeypatch.setenv("SMG_FORCE_SLABS", "1")
+    one = smg.Solver(32, levels=3)
+    r0 = smg.Solver.for_rank(0, 1, smg.nccl_unique_id(), 32, levels=3, device=0)
+    b = smg.forcing(32, kind=smg.FORCE_UNIFORM, seed=9)
+    assert np.array_equal(r0.apply(b), one.apply(b))
+    assert np.array_equal(r0.vcycle(b), one.vcycle(b))
+    x1, h1, _, s1 = one.sqmr(b, 1e-6, 100)
+    x2, h2, _, s2 = r0.sqmr(b, 1e-6, 100)
+    assert s1 == s2 == smg.SMG_CONVERGED
+    assert np.array_equal(h1, h2) and np.array_equal(x1, x2)
+    r0.close()
+    one.close()

@@ -86,3 +86,42 @@ def test_gloo_world2_slab_plan_and_timing_plumbing():
     assert all(ok for _, ok, _, _ in res)
     assert all(m == 3.0 for _, _, m, _ in res)
     assert all(nd >= 1 for *_, nd in res)
+
+
+def _id_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
+                      LOCAL_RANK=str(rank))
+    import bench
+
+    ws, r, _ = bench.dist_setup()
+    uid = bench.share_nccl_id(ws, r)  # rank 0: smg_nccl_unique_id (dlopen'ed NCCL); broadcast over gloo
+    dist.destroy_process_group()
+    q.put((rank, uid))
+
+
+def test_gloo_world2_nccl_id_broadcast():
+    """The one-process-per-GPU path's bootstrap: rank 0's 128-byte NCCL id reaches every rank."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_id_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=180) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert len(res[0]) == 128 and res[0] == res[1] and any(res[0])
+
+
+def test_create_rank_rejects_bad_arguments():
+    import ctypes as C
+
+    L = smg.lib()
+    g = smg.GridDesc(3, 32, 32, 32, 1 / 32)
+    prm = smg.Params(1.0, 1e-3, 3, 1, 1, 0, 0)
+    ctx = C.c_void_p()
+    uid = bytes(128)
+    assert L.smg_create_rank(C.byref(g), C.byref(prm), 2, 2, 0, uid, C.byref(ctx)) == -1  # rank >= nranks
+    assert L.smg_create_rank(C.byref(g), C.byref(prm), 0, 0, 0, uid, C.byref(ctx)) == -1  # no ranks
+    assert L.smg_create_rank(C.byref(g), C.byref(prm), 0, 1, 0, None, C.byref(ctx)) == -1  # no id
