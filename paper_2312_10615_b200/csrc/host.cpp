@@ -228,6 +228,11 @@ struct DevLevel {
     int32_t* vk_refresh = nullptr;  // slots every Vanka residual reads (refreshed x -> xb per sweep)
     int64_t vk_nrefresh = 0;
     int vk_n[8] = {};
+    // lists of the symmetric sweeps: as vk_* with colour 4 appended to list 3 (sw_merged = colour-3 count)
+    int32_t* sw_cells[8] = {};
+    uint8_t* sw_mask[8] = {};
+    int sw_n[8] = {};
+    int sw_merged = -1;
     double* ktab = nullptr;  // [64][49]
     std::vector<WavePass> wave;  // fused wavefront DGS sweep (large single-part levels), empty: per-phase/coop
 };
@@ -476,6 +481,28 @@ void build(smg_ctx* c, const std::vector<double>* shared_coarse = nullptr, std::
             }
             CK(cudaStreamSynchronize(c->st));
         }
+        // sweep lists: colour 4 folded into list 3 (one phase; see VankaLists in kernels.cu)
+        for (int col = 0; col < 8; ++col) {
+            L.sw_cells[col] = L.vk_cells[col];
+            L.sw_mask[col] = L.vk_mask[col];
+            L.sw_n[col] = L.vk_n[col];
+        }
+        L.sw_merged = -1;
+        if (env_int("SMG_VANKA_MERGE34", 1) == 2 || (env_int("SMG_VANKA_MERGE34", 1) == 1 && vanka_merge_pays(L.vk_n))) {
+            std::vector<int32_t> mc(cells[3]);
+            mc.insert(mc.end(), cells[4].begin(), cells[4].end());
+            std::vector<uint8_t> mm(masks[3]);
+            mm.insert(mm.end(), masks[4].begin(), masks[4].end());
+            L.sw_n[3] = static_cast<int>(mc.size());
+            L.sw_n[4] = 0;
+            max_vk = std::max(max_vk, L.sw_n[3]);
+            L.sw_cells[3] = c->dalloc<int32_t>(L.sw_n[3]);
+            L.sw_mask[3] = c->dalloc<uint8_t>(L.sw_n[3]);
+            CK(cudaMemcpyAsync(L.sw_cells[3], mc.data(), mc.size() * sizeof(int32_t), cudaMemcpyHostToDevice, c->st));
+            CK(cudaMemcpyAsync(L.sw_mask[3], mm.data(), mm.size(), cudaMemcpyHostToDevice, c->st));
+            CK(cudaStreamSynchronize(c->st));
+            L.sw_merged = static_cast<int>(cells[3].size());
+        }
         // local inverses C_i L~ C_i^T per face mask, scattered to the 7-slot layout
         std::vector<double> ktab(64 * 49, 0.0);
         for (int m = 0; m < 64; ++m) {
@@ -635,20 +662,21 @@ void symmetric_dgs(smg_ctx* c, int l, double* x, const double* b) {
 
 void vanka_sym_coop(smg_ctx* c, int l, double* x, const double* b) {
     DevLevel& L = c->lv[l];
-    launch_vanka_sym_coop(L.k, x, b, L.vk_cells, L.vk_mask, L.vk_n, L.ktab, c->vk_delta, c->prm.nu, c->st, L.xb,
-                          L.vk_refresh, L.vk_nrefresh);
+    launch_vanka_sym_coop(L.k, x, b, L.sw_cells, L.sw_mask, L.sw_n, L.ktab, c->vk_delta, c->prm.nu, c->st, L.xb,
+                          L.vk_refresh, L.vk_nrefresh, L.sw_merged);
 }
 
 void smooth(smg_ctx* c, int l, double* x, const double* b) {
     DevLevel& L = c->lv[l];
-    if (smooth_dsm_fits(L.k, L.vk_n)) {
+    if (smooth_dsm_fits(L.k, L.sw_n)) {
         const int nph = (c->prm.flags & SMG_FLAG_SKIP_REVERSE_DGS) ? kDgsPhases / 2 : kDgsPhases;
-        launch_smooth_dsm(L.k, x, b, L.vk_cells, L.vk_mask, L.vk_n, L.ktab, c->prm.nu, nph, c->st);
+        launch_smooth_dsm(L.k, x, b, L.sw_cells, L.sw_mask, L.sw_n, L.ktab, c->prm.nu, nph, c->st, L.sw_merged);
         return;
     }
-    if (smooth_smem_fits(L.k)) {
+    if (smooth_smem_fits(L.k, L.sw_n)) {
         const int nph = (c->prm.flags & SMG_FLAG_SKIP_REVERSE_DGS) ? kDgsPhases / 2 : kDgsPhases;
-        launch_smooth_smem(L.k, x, b, L.vk_cells, L.vk_mask, L.vk_n, L.ktab, L.pd0, L.pd1, c->prm.nu, nph, c->st);
+        launch_smooth_smem(L.k, x, b, L.sw_cells, L.sw_mask, L.sw_n, L.ktab, L.pd0, L.pd1, c->prm.nu, nph, c->st,
+                           L.sw_merged);
         return;
     }
     vanka_sym_coop(c, l, x, b);
@@ -1428,7 +1456,8 @@ int smg_smoother(smg_ctx* c, int level, int op, int arg, double* x, const double
             launch_vanka_delta(L.k, L.x, L.b, L.vk_cells[arg], L.vk_mask[arg], L.vk_n[arg], L.ktab, c->vk_delta, c->st);
             launch_vanka_apply(L.k, L.x, L.vk_cells[arg], L.vk_mask[arg], L.vk_n[arg], c->vk_delta, c->st);
         } else if (op == 3) {
-            launch_vanka_sym_coop(L.k, L.x, L.b, L.vk_cells, L.vk_mask, L.vk_n, L.ktab, c->vk_delta, 1, c->st);
+            launch_vanka_sym_coop(L.k, L.x, L.b, L.sw_cells, L.sw_mask, L.sw_n, L.ktab, c->vk_delta, 1, c->st,
+                                  nullptr, nullptr, 0, L.sw_merged);
         } else if (op == 5) {  // per-phase reference path of the symmetric sweeps (test only)
             for (int ph = 0; ph < kDgsPhases; ++ph) dgs_phase(c, level, L.x, L.b, ph);
             vanka_sym(c, level, L.x, L.b);

@@ -527,7 +527,22 @@ struct VankaLists {
     const int32_t* cells[8];
     const uint8_t* masks[8];
     int n[8];
+    // merged >= 0: list 3 holds the colour-3 blocks (first `merged` entries) followed by the
+    // colour-4 blocks, and colour 4 has no phase of its own.  Colours 3 and 4 = 3 ^ 7 differ in
+    // all three parities: every residual stencil reaches along one axis only, so no block of one
+    // reads or writes a DOF of the other, and the adjacent phases 3, 4 (and 4, 3) run as ONE
+    // Jacobi phase with bit-identical results: 14 phases per symmetric sweep instead of 16.
+    int merged;
 };
+// phase k (0..15) of a symmetric sweep -> colour list, -1 if the phase is folded away
+__device__ __forceinline__ int vanka_phase_list(const VankaLists& vl, int k) {
+    const int col = k < 8 ? k : 15 - k;
+    return (vl.merged >= 0 && col == 4) ? -1 : col;
+}
+// parity colour of entry t of list c
+__device__ __forceinline__ int vanka_entry_colour(const VankaLists& vl, int c, int t) {
+    return (vl.merged >= 0 && c == 3 && t >= vl.merged) ? 4 : c;
+}
 
 // nu symmetric multiplicative Vanka sweeps (colours 0..7 then 7..0), Jacobi
 // within a colour.  Each thread owns up to CPT blocks of the colour: it loads
@@ -545,7 +560,8 @@ __device__ __forceinline__ void vanka_sweeps(const LevelK& L, double* __restrict
     const int64_t off[7] = {0, 1, fs, fs + sy, 2 * fs, 2 * fs + sz, 3 * fs};
     for (int sweep = 0; sweep < nu; ++sweep)
         for (int k = 0; k < 16; ++k) {
-            const int col = k < 8 ? k : 15 - k;
+            const int col = vanka_phase_list(vl, k);
+            if (col < 0) continue;
             const int n = vl.n[col];
             int64_t slot[CPT];
             int msk[CPT];
@@ -669,7 +685,8 @@ __device__ __forceinline__ void vanka_sweeps8(const LevelK& L, AX X, const doubl
             pre[c] = grp < vl.n[c] ? ((static_cast<int64_t>(vl.cells[c][grp]) << 7) | vl.masks[c][grp]) : -1;
     for (int sweep = 0; sweep < nu; ++sweep)
         for (int k = 0; k < 16; ++k) {
-            const int col = k < 8 ? k : 15 - k;
+            const int col = vanka_phase_list(vl, k);
+            if (col < 0) continue;
             const int n = vl.n[col];
             double own[CPT], dl[CPT];
             int64_t dst[CPT];
@@ -750,12 +767,12 @@ __device__ __forceinline__ void vanka_sweeps_pp(const LevelK& L, double* __restr
             m = vl.masks[c][t];
         }
     };
-    const int nph = 16 * nu;
-    for (int ph = 0; ph < nph; ++ph) {
-        const int k = ph & 15;
-        const int col = k < 8 ? k : 15 - k;
-        const int kp = (ph - 1) & 15;
-        const int pcol = ph == 0 ? -1 : (kp < 8 ? kp : 15 - kp);
+    // executed phases alternate the buffers; 16 or 14 (merged) per sweep, so the result ends in XA
+    int ph = 0, pcol = -1;
+    for (int kk = 0; kk < 16 * nu; ++kk) {
+        const int col = vanka_phase_list(vl, kk & 15);
+        if (col < 0) continue;
+        const int cmask = (vl.merged >= 0 && col == 3) ? 0x18 : (1 << col);  // parity colours of this phase
         const double* __restrict__ Xc = (ph & 1) ? XB : XA;
         double* __restrict__ Xn = (ph & 1) ? XA : XB;
         const int n = vl.n[col];
@@ -789,7 +806,7 @@ __device__ __forceinline__ void vanka_sweeps_pp(const LevelK& L, double* __restr
                 int mp;
                 block_of(pcol, t, ip, mp);
                 bool carry = s8 == 6 || (mp & (1 << s8));
-                if (carry && s8 < 6 && (pcol ^ (1 << (s8 >> 1))) == col) {
+                if (carry && s8 < 6 && ((cmask >> (vanka_entry_colour(vl, pcol, t) ^ (1 << (s8 >> 1)))) & 1)) {
                     const int zl = static_cast<int>(ip / sz) - g.zg;
                     const int64_t rem = ip - static_cast<int64_t>(zl + g.zg) * sz;
                     const int y = static_cast<int>(rem / sy) - 1;
@@ -805,6 +822,8 @@ __device__ __forceinline__ void vanka_sweeps_pp(const LevelK& L, double* __restr
         SMG_TRACE_STAMP(ph, 2);
         phase_sync<MODE>();
         SMG_TRACE_STAMP(ph, 3);
+        pcol = col;
+        ++ph;
     }
 }
 
@@ -1173,6 +1192,7 @@ __global__ void __launch_bounds__(512) k_dgs_sym_coop(LevelK L, double* __restri
 // in shared memory (layout identical to the global one, compact geometry):
 // every phase barrier is a __syncthreads, no global fences.  b and the DGS
 // delta buffers stay in global memory (visible within the CTA at barriers).
+template <int CPT>
 __global__ void __launch_bounds__(512) k_smooth_smem(LevelK L, double* __restrict__ Xg, const double* __restrict__ B,
                                                       VankaLists vl, const double* __restrict__ ktab,
                                                       double* __restrict__ D0, double* __restrict__ D1, int nu,
@@ -1184,10 +1204,10 @@ __global__ void __launch_bounds__(512) k_smooth_smem(LevelK L, double* __restric
     for (int k = threadIdx.x; k < 64 * 49; k += blockDim.x) Ks[k] = ktab[k];
     for (int64_t k = threadIdx.x; k < nv; k += blockDim.x) X[k] = Xg[k];
     __syncthreads();
-    vanka_sweeps<2, 1>(L, X, B, vl, Ks, nu, threadIdx.x, blockDim.x);
+    vanka_sweeps<2, CPT>(L, X, B, vl, Ks, nu, threadIdx.x, blockDim.x);
     dgs_sweep<2>(L, X, B, D0, D1, nph, threadIdx.x, blockDim.x);
     __syncthreads();
-    vanka_sweeps<2, 1>(L, X, B, vl, Ks, nu, threadIdx.x, blockDim.x);
+    vanka_sweeps<2, CPT>(L, X, B, vl, Ks, nu, threadIdx.x, blockDim.x);
     for (int64_t k = threadIdx.x; k < nv; k += blockDim.x) Xg[k] = X[k];
 }
 
@@ -1747,8 +1767,9 @@ static void launch_vanka_pp(bool cl, int64_t threads, void** args, cudaStream_t 
 
 void launch_vanka_sym_coop(const LevelK& L, double* x, const double* b, const int32_t* const* cells,
                            const uint8_t* const* masks, const int* n, const double* ktab, double* delta, int nu,
-                           cudaStream_t s, double* xb, const int32_t* refresh, int64_t nrefresh) {
+                           cudaStream_t s, double* xb, const int32_t* refresh, int64_t nrefresh, int merged) {
     VankaLists vl;
+    vl.merged = merged;
     int maxn = 1;
     for (int c = 0; c < 8; ++c) {
         vl.cells[c] = cells[c];
@@ -1768,8 +1789,8 @@ void launch_vanka_sym_coop(const LevelK& L, double* x, const double* b, const in
         const int64_t threads = cl ? cl_threads : coop_capacity_blocks(fn, coop_threads()) * coop_threads();
         return threads * cpt >= lanes;
     };
-    bool done = true;
-    if (xb && !cl && env_int("SMG_VANKA_PP", 1)) {  // ping-pong (grid mode): one barrier per phase
+    bool done = !env_int("SMG_VANKA_PHASES", 0);  // 1: per-phase delta/apply launches (tests)
+    if (done && xb && !cl && env_int("SMG_VANKA_PP", 1)) {  // ping-pong (grid mode): one barrier per phase
         if (nrefresh > 0) {
             const int64_t blocks = (nrefresh + 255) / 256;
             k_refresh<<<static_cast<int>(blocks < 4096 ? blocks : 4096), 256, 0, s>>>(refresh, nrefresh, x, xb);
@@ -1780,7 +1801,8 @@ void launch_vanka_sym_coop(const LevelK& L, double* x, const double* b, const in
         if (fits(reinterpret_cast<const void*>(k_vanka_pp<0, 2>), 2)) { launch_vanka_pp<2>(cl, (lanes + 1) / 2, pargs, s); return; }
         if (fits(reinterpret_cast<const void*>(k_vanka_pp<0, 4>), 4)) { launch_vanka_pp<4>(cl, (lanes + 3) / 4, pargs, s); return; }
     }
-    if (fits(reinterpret_cast<const void*>(k_vanka8<0, 1>), 1)) launch_vanka8<1>(cl, lanes, args, s);
+    if (!done) {
+    } else if (fits(reinterpret_cast<const void*>(k_vanka8<0, 1>), 1)) launch_vanka8<1>(cl, lanes, args, s);
     else if (fits(reinterpret_cast<const void*>(k_vanka8<0, 2>), 2)) launch_vanka8<2>(cl, (lanes + 1) / 2, args, s);
     else if (fits(reinterpret_cast<const void*>(k_vanka8<0, 4>), 4)) launch_vanka8<4>(cl, (lanes + 3) / 4, args, s);
     else if (fits(reinterpret_cast<const void*>(k_vanka8<0, 8>), 8)) launch_vanka8<8>(cl, (lanes + 7) / 8, args, s);
@@ -1789,10 +1811,28 @@ void launch_vanka_sym_coop(const LevelK& L, double* x, const double* b, const in
         for (int sweep = 0; sweep < nu; ++sweep)
             for (int k = 0; k < 16; ++k) {
                 const int col = k < 8 ? k : 15 - k;
+                if (merged >= 0 && col == 4) continue;  // folded into the colour-3 list
                 launch_vanka_delta(L, x, b, cells[col], masks[col], n[col], ktab, delta, s);
                 launch_vanka_apply(L, x, cells[col], masks[col], n[col], delta, s);
             }
     }
+}
+
+// Folding colour 4 into colour 3 doubles that phase's lanes; in grid mode that only pays
+// while the merged phase still fits the one-block-per-lane-group (CPT = 1) capacity.
+bool vanka_merge_pays(const int* n) {
+    int maxn = 0;
+    for (int c = 0; c < 8; ++c) maxn = n[c] > maxn ? n[c] : maxn;
+    const int64_t merged = std::max<int64_t>(maxn, static_cast<int64_t>(n[3]) + n[4]);
+    const int64_t cap = coop_capacity_blocks(reinterpret_cast<const void*>(k_vanka_pp<0, 1>), coop_threads()) *
+                        coop_threads();
+    const int64_t cl = static_cast<int64_t>(kClusterCTAs) * kClusterThreads;
+    // sweep class of a phase of `lanes` lanes: cluster, or grid with ceil(lanes / cap) blocks per group
+    // (measured: cluster -> grid at CPT = 1 still pays at 32^3, CPT 1 -> 2 does not at 128^3)
+    auto cls = [&](int64_t lanes) {
+        return lanes <= std::max(cl, cap) ? int64_t{1} : (lanes + cap - 1) / std::max<int64_t>(cap, 1);
+    };
+    return cls(8 * merged) == cls(8 * static_cast<int64_t>(maxn));
 }
 
 bool smooth_dsm_fits(const LevelK& L, const int* n) {
@@ -1806,8 +1846,9 @@ bool smooth_dsm_fits(const LevelK& L, const int* n) {
 
 void launch_smooth_dsm(const LevelK& L, double* x, const double* b, const int32_t* const* cells,
                        const uint8_t* const* masks, const int* n, const double* ktab, int nu, int nph,
-                       cudaStream_t s) {
+                       cudaStream_t s, int merged) {
     VankaLists vl;
+    vl.merged = merged;
     for (int c = 0; c < 8; ++c) {
         vl.cells[c] = cells[c];
         vl.masks[c] = masks[c];
@@ -1834,23 +1875,34 @@ void launch_smooth_dsm(const LevelK& L, double* x, const double* b, const int32_
     count();
 }
 
-bool smooth_smem_fits(const LevelK& L) {
-    return (64 * 49 + 4 * L.g.fs) * static_cast<int64_t>(sizeof(double)) <= 227 * 1024 &&
+bool smooth_smem_fits(const LevelK& L, const int* n) {
+    int maxn = 0;
+    for (int c = 0; c < 8; ++c) maxn = n[c] > maxn ? n[c] : maxn;
+    return (64 * 49 + 4 * L.g.fs) * static_cast<int64_t>(sizeof(double)) <= 227 * 1024 && maxn <= 4 * 512 &&
            env_int("SMG_NO_SMEM_SMOOTH", 0) == 0;
 }
 
 void launch_smooth_smem(const LevelK& L, double* x, const double* b, const int32_t* const* cells,
                         const uint8_t* const* masks, const int* n, const double* ktab, double* d0, double* d1, int nu,
-                        int nph, cudaStream_t s) {
+                        int nph, cudaStream_t s, int merged) {
     VankaLists vl;
+    vl.merged = merged;
     for (int c = 0; c < 8; ++c) {
         vl.cells[c] = cells[c];
         vl.masks[c] = masks[c];
         vl.n[c] = n[c];
     }
     const size_t smem = (64 * 49 + 4 * L.g.fs) * sizeof(double);
-    cudaFuncSetAttribute(k_smooth_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    k_smooth_smem<<<1, 512, smem, s>>>(L, x, b, vl, ktab, d0, d1, nu, nph);
+    // every block of a colour list needs a thread: 512 threads x CPT blocks
+    int maxn = 0;
+    for (int c = 0; c < 8; ++c) maxn = n[c] > maxn ? n[c] : maxn;
+    auto go = [&](auto kern) {
+        note(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        kern<<<1, 512, smem, s>>>(L, x, b, vl, ktab, d0, d1, nu, nph);
+    };
+    if (maxn <= 512) go(k_smooth_smem<1>);
+    else if (maxn <= 1024) go(k_smooth_smem<2>);
+    else go(k_smooth_smem<4>);  // smooth_smem_fits caps the list size
     count();
 }
 

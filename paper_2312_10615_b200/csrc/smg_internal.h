@@ -84,12 +84,15 @@ void launch_vanka_apply(const LevelK& L, double* x, const int32_t* cells, const 
                         const double* delta, cudaStream_t s, const uint8_t* amask = nullptr);
 // Cooperative (persistent, grid-synchronised) symmetric sweeps: nu Vanka sweeps
 // over the 8 colour lists; nph DGS phases (20 = full symmetric sweep).
+// merged >= 0: list 3 = colour-3 blocks (first `merged`) + colour-4 blocks, run as
+// one phase (14 phases per sweep; see VankaLists in kernels.cu).
 // xb (optional): second level vector for the ping-pong sweep (one barrier per
 // phase); refresh[0..nrefresh) lists the slots Vanka reads, copied x -> xb first.
 void launch_vanka_sym_coop(const LevelK& L, double* x, const double* b, const int32_t* const* cells,
                            const uint8_t* const* masks, const int* n, const double* ktab, double* delta, int nu,
                            cudaStream_t s, double* xb = nullptr, const int32_t* refresh = nullptr,
-                           int64_t nrefresh = 0);
+                           int64_t nrefresh = 0, int merged = -1);
+bool vanka_merge_pays(const int* n);  // merged lists keep the grid sweep at one block per lane group
 void launch_dgs_sym_coop(const LevelK& L, double* x, const double* b, double* d0, double* d1, int nph,
                          cudaStream_t s);
 // Whole smooth (Alg. 3) of a level held in the distributed shared memory of one
@@ -97,12 +100,12 @@ void launch_dgs_sym_coop(const LevelK& L, double* x, const double* b, double* d0
 bool smooth_dsm_fits(const LevelK& L, const int* n);
 void launch_smooth_dsm(const LevelK& L, double* x, const double* b, const int32_t* const* cells,
                        const uint8_t* const* masks, const int* n, const double* ktab, int nu, int nph,
-                       cudaStream_t s);
+                       cudaStream_t s, int merged = -1);
 // Whole smooth (Alg. 3) of a level small enough for one CTA's shared memory.
-bool smooth_smem_fits(const LevelK& L);
+bool smooth_smem_fits(const LevelK& L, const int* n);
 void launch_smooth_smem(const LevelK& L, double* x, const double* b, const int32_t* const* cells,
                         const uint8_t* const* masks, const int* n, const double* ktab, double* d0, double* d1, int nu,
-                        int nph, cudaStream_t s);
+                        int nph, cudaStream_t s, int merged = -1);
 // Restriction of coarse LOCAL planes [zc_lo, zc_lo + nzc) (nzc < 0: all); the
 // fine slab must hold the fine planes 2zc-1 .. 2zc+2 (halos included).
 void launch_restrict(const LevelK& F, const LevelK& C, const double* rf, double* bc, cudaStream_t s, int zc_lo = 0,

@@ -350,3 +350,36 @@ def test_wave_dgs_forward_half_bitwise(monkeypatch):
         out.append(s.smoother(smg.OP_SMOOTH, x, b))
         s.close()
     same(out[1], out[0])
+
+
+@pytest.mark.parametrize("mode", [{}, {"SMG_SYNC_MODE": "1"}, {"SMG_SYNC_MODE": "2"}, {"SMG_VANKA_PP": "0"},
+                                  {"SMG_VANKA_PHASES": "1"}, {"SMG_NO_SMEM_SMOOTH": "1"}])
+def test_vanka_merged_phase_bitwise(mode, monkeypatch):
+    """Colours 3 and 4 (= 3 ^ 7) share one Jacobi phase (14 phases per sweep): every sweep
+    variant stays bit-identical to the oracle's 16-phase order."""
+    for k, v in mode.items():
+        monkeypatch.setenv(k, v)
+    oracle.set_threads(4)
+    o = oracle.Oracle(32, levels=3)
+    s = smg.Solver(32, levels=3)
+    for level in (0, 1):
+        n = o.ndof(level)
+        x, b = rnd(n, 70 + level), rnd(n, 71 + level)
+        same(s.smoother(smg.OP_VANKA_SYM, x, b, level), o.smoother(3, x, b, level))
+        same(s.smoother(smg.OP_SMOOTH, x, b, level), o.smoother(4, x, b, level))
+    s.close()
+
+
+@pytest.mark.parametrize("n,levels", [(64, 4), (128, 5)])
+def test_vanka_merged_matches_unmerged(n, levels, monkeypatch):
+    """Large levels (grid ping-pong sweeps): merged (14-phase) == unmerged (16-phase) sweep."""
+    out = []
+    for merge in ("0", "2"):  # 2: merge even where the default would not
+        monkeypatch.setenv("SMG_VANKA_MERGE34", merge)
+        s = smg.Solver(n, levels=levels)
+        x = np.random.default_rng(n).uniform(-1, 1, s.ndof())
+        b = np.random.default_rng(n + 1).uniform(-1, 1, s.ndof())
+        out.append((s.smoother(smg.OP_VANKA_SYM, x, b), s.smoother(smg.OP_SMOOTH, x, b), s.vcycle(b)))
+        s.close()
+    for a, c in zip(*out):
+        same(a, c)
