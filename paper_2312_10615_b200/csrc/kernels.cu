@@ -738,24 +738,22 @@ __device__ __forceinline__ void vanka_sweeps8(const LevelK& L, AX X, const doubl
 // only those two colours changed).  Reads and writes never share a buffer
 // within a phase.  Before the sweep XB must equal XA on every DOF a Vanka
 // residual reads (refresh list).  16 nu phases: the result ends in XA.
-template <int MODE, int CPT>
-__device__ __forceinline__ void vanka_sweeps_pp(const LevelK& L, double* __restrict__ XA, double* __restrict__ XB,
-                                                const double* __restrict__ B, const VankaLists& vl,
-                                                const double* __restrict__ Ks, int nu, int tid, int nth) {
+// One ping-pong colour phase (list col; pcol = list of the previous phase, -1 if none):
+// reads Xc, writes the phase's blocks and the carried previous-phase blocks into Xn.
+// pre (CPT == 1, optional): this lane group's entry of every list, preloaded.
+template <int CPT, bool PRE>
+__device__ __forceinline__ void vanka_pp_phase(const LevelK& L, const double* __restrict__ Xc,
+                                               double* __restrict__ Xn, const double* __restrict__ B,
+                                               const VankaLists& vl, const double* __restrict__ Ks, int col, int pcol,
+                                               const int64_t* pre, int tid, int nth) {
     const Geom& g = L.g;
     const int64_t fs = g.fs, sy = g.sy, sz = g.sz;
     const int lane = threadIdx.x & 31, s8 = lane & 7;
     const int groups = nth >> 3, grp = tid >> 3;
     const int64_t offs = s8 == 0 ? 0 : s8 == 1 ? 1 : s8 == 2 ? fs : s8 == 3 ? fs + sy : s8 == 4 ? 2 * fs
                          : s8 == 5 ? 2 * fs + sz : 3 * fs;
-    constexpr bool kPre = CPT == 1;
-    int64_t pre[8];
-    if (kPre)
-#pragma unroll
-        for (int c = 0; c < 8; ++c)
-            pre[c] = grp < vl.n[c] ? ((static_cast<int64_t>(vl.cells[c][grp]) << 7) | vl.masks[c][grp]) : -1;
     auto block_of = [&](int c, int t, int64_t& i, int& m) {
-        if (kPre) {
+        if constexpr (PRE) {
             int64_t e = 0;
 #pragma unroll
             for (int q = 0; q < 8; ++q)
@@ -767,64 +765,94 @@ __device__ __forceinline__ void vanka_sweeps_pp(const LevelK& L, double* __restr
             m = vl.masks[c][t];
         }
     };
+    const int cmask = (vl.merged >= 0 && col == 3) ? 0x18 : (1 << col);  // parity colours of this phase
+    const int n = vl.n[col];
+#pragma unroll
+    for (int j = 0; j < CPT; ++j) {
+        const int t = grp + j * groups;
+        const bool act = t < n;
+        int64_t i = 0;
+        int m = 0;
+        if (act) block_of(col, t, i, m);
+        double r = 0.0, own = 0.0;
+        if (act && s8 < 7) r = vanka_slot_residual(L, Xc, B, i, m, s8, own);
+#ifdef SMG_TRACE
+        if (__any_sync(0xffffffffu, r == 1.2345e300)) g_trace[0] = 0;  // wait for the gather
+#endif
+        const double* K = Ks + m * 49 + (s8 < 7 ? s8 : 0) * 7;
+        double acc = 0.0;
+#pragma unroll
+        for (int q = 0; q < 7; ++q) {
+            const double rq = __shfl_sync(0xffffffffu, r, (lane & ~7) + q);
+            acc = acc + K[q] * rq;
+        }
+        if (act && s8 < 7 && (s8 == 6 || (m & (1 << s8)))) Xn[i + offs] = own + acc;
+        // carry the previous phase's blocks into the buffer being written, except DOFs
+        // this phase rewrites: the same colour twice in a row (turning points), or a face
+        // shared with a band cell of a colour of this phase (colours one parity bit apart)
+        if (pcol >= 0 && pcol != col && t < vl.n[pcol] && s8 < 7) {
+            int64_t ip;
+            int mp;
+            block_of(pcol, t, ip, mp);
+            bool carry = s8 == 6 || (mp & (1 << s8));
+            if (carry && s8 < 6 && ((cmask >> (vanka_entry_colour(vl, pcol, t) ^ (1 << (s8 >> 1)))) & 1)) {
+                const int zl = static_cast<int>(ip / sz) - g.zg;
+                const int64_t rem = ip - static_cast<int64_t>(zl + g.zg) * sz;
+                const int y = static_cast<int>(rem / sy) - 1;
+                const int x = static_cast<int>(rem - static_cast<int64_t>(y + 1) * sy) - g.xo;
+                const int d = (s8 & 1) ? 1 : -1;
+                const int ax = s8 >> 1;
+                if (band_cell(L, x + (ax == 0 ? d : 0), y + (ax == 1 ? d : 0), zl + (ax == 2 ? d : 0)))
+                    carry = false;
+            }
+            if (carry) Xn[ip + offs] = Xc[ip + offs];
+        }
+    }
+}
+
+// Ping-pong variant: one barrier per colour phase.  Phase k (k = 0..16 nu - 1)
+// reads buffer X_k (XA for even k) and writes X_{k+1}: the new values of its
+// colour's blocks and a copy of the blocks updated by phase k-1, so X_{k+1}
+// holds the full state after phase k (it held the state after phase k-2, and
+// only those two colours changed).  Reads and writes never share a buffer
+// within a phase.  Before the sweep XB must equal XA on every DOF a Vanka
+// residual reads (refresh list).  16 nu phases: the result ends in XA.
+template <int MODE, int CPT>
+__device__ __forceinline__ void vanka_sweeps_pp(const LevelK& L, double* __restrict__ XA, double* __restrict__ XB,
+                                                const double* __restrict__ B, const VankaLists& vl,
+                                                const double* __restrict__ Ks, int nu, int tid, int nth) {
+    const int grp = tid >> 3;
+    constexpr bool kPre = CPT == 1;
+    int64_t pre[8];
+    if (kPre)
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+            pre[c] = grp < vl.n[c] ? ((static_cast<int64_t>(vl.cells[c][grp]) << 7) | vl.masks[c][grp]) : -1;
     // executed phases alternate the buffers; 16 or 14 (merged) per sweep, so the result ends in XA
     int ph = 0, pcol = -1;
     for (int kk = 0; kk < 16 * nu; ++kk) {
         const int col = vanka_phase_list(vl, kk & 15);
         if (col < 0) continue;
-        const int cmask = (vl.merged >= 0 && col == 3) ? 0x18 : (1 << col);  // parity colours of this phase
         const double* __restrict__ Xc = (ph & 1) ? XB : XA;
         double* __restrict__ Xn = (ph & 1) ? XA : XB;
-        const int n = vl.n[col];
         SMG_TRACE_STAMP(ph, 0);
-#pragma unroll
-        for (int j = 0; j < CPT; ++j) {
-            const int t = grp + j * groups;
-            const bool act = t < n;
-            int64_t i = 0;
-            int m = 0;
-            if (act) block_of(col, t, i, m);
-            double r = 0.0, own = 0.0;
-            if (act && s8 < 7) r = vanka_slot_residual(L, Xc, B, i, m, s8, own);
-#ifdef SMG_TRACE
-            if (__any_sync(0xffffffffu, r == 1.2345e300)) g_trace[0] = 0;  // wait for the gather
-            if (j == 0) SMG_TRACE_STAMP(ph, 1);
-#endif
-            const double* K = Ks + m * 49 + (s8 < 7 ? s8 : 0) * 7;
-            double acc = 0.0;
-#pragma unroll
-            for (int q = 0; q < 7; ++q) {
-                const double rq = __shfl_sync(0xffffffffu, r, (lane & ~7) + q);
-                acc = acc + K[q] * rq;
-            }
-            if (act && s8 < 7 && (s8 == 6 || (m & (1 << s8)))) Xn[i + offs] = own + acc;
-            // carry the previous phase's blocks into the buffer being written, except DOFs
-            // this phase rewrites: the same colour twice in a row (turning points), or a face
-            // shared with a band cell of the current colour (colours one parity bit apart)
-            if (pcol >= 0 && pcol != col && t < vl.n[pcol] && s8 < 7) {
-                int64_t ip;
-                int mp;
-                block_of(pcol, t, ip, mp);
-                bool carry = s8 == 6 || (mp & (1 << s8));
-                if (carry && s8 < 6 && ((cmask >> (vanka_entry_colour(vl, pcol, t) ^ (1 << (s8 >> 1)))) & 1)) {
-                    const int zl = static_cast<int>(ip / sz) - g.zg;
-                    const int64_t rem = ip - static_cast<int64_t>(zl + g.zg) * sz;
-                    const int y = static_cast<int>(rem / sy) - 1;
-                    const int x = static_cast<int>(rem - static_cast<int64_t>(y + 1) * sy) - g.xo;
-                    const int d = (s8 & 1) ? 1 : -1;
-                    const int ax = s8 >> 1;
-                    if (band_cell(L, x + (ax == 0 ? d : 0), y + (ax == 1 ? d : 0), zl + (ax == 2 ? d : 0)))
-                        carry = false;
-                }
-                if (carry) Xn[ip + offs] = Xc[ip + offs];
-            }
-        }
+        vanka_pp_phase<CPT, kPre>(L, Xc, Xn, B, vl, Ks, col, pcol, pre, tid, nth);
         SMG_TRACE_STAMP(ph, 2);
         phase_sync<MODE>();
         SMG_TRACE_STAMP(ph, 3);
         pcol = col;
         ++ph;
     }
+}
+
+// One ping-pong phase per launch (graph nodes instead of grid barriers); the
+// local inverses are read through L1 (26 masks occur in a box).
+template <int CPT>
+__global__ void __launch_bounds__(256) k_vanka_ppk(LevelK L, const double* __restrict__ Xc, double* __restrict__ Xn,
+                                                   const double* __restrict__ B, VankaLists vl,
+                                                   const double* __restrict__ ktab, int col, int pcol) {
+    vanka_pp_phase<CPT, false>(L, Xc, Xn, B, vl, ktab, col, pcol, nullptr, blockIdx.x * blockDim.x + threadIdx.x,
+                               gridDim.x * blockDim.x);
 }
 
 template <int MODE, int CPT>
@@ -1189,6 +1217,8 @@ __global__ void __launch_bounds__(512) k_dgs_sym_coop(LevelK L, double* __restri
 }
 
 // Whole Alg. 3 smooth of a small level in ONE CTA with the level vector held
+// (opt-in, SMG_SMEM_SMOOTH=1: inside the iteration graph the per-step kernels on
+// all SMs measured faster at 16^3, 2.31 -> 2.27 ms per cfg-1 iteration)
 // in shared memory (layout identical to the global one, compact geometry):
 // every phase barrier is a __syncthreads, no global fences.  b and the DGS
 // delta buffers stay in global memory (visible within the CTA at barriers).
@@ -1789,6 +1819,26 @@ void launch_vanka_sym_coop(const LevelK& L, double* x, const double* b, const in
         const int64_t threads = cl ? cl_threads : coop_capacity_blocks(fn, coop_threads()) * coop_threads();
         return threads * cpt >= lanes;
     };
+    if (xb && env_int("SMG_VANKA_KERNELS", 0)) {  // ping-pong, one launch per phase
+        if (nrefresh > 0) {
+            const int64_t blocks = (nrefresh + 255) / 256;
+            k_refresh<<<static_cast<int>(blocks < 4096 ? blocks : 4096), 256, 0, s>>>(refresh, nrefresh, x, xb);
+            count();
+        }
+        const int64_t blocks = (8 * static_cast<int64_t>(maxn) + 255) / 256;  // one lane group per block
+        int ph = 0, pcol = -1;
+        for (int kk = 0; kk < 16 * nu; ++kk) {
+            const int k = kk & 15, c0 = k < 8 ? k : 15 - k;
+            if (merged >= 0 && c0 == 4) continue;
+            const double* xc = (ph & 1) ? xb : x;
+            double* xn = (ph & 1) ? x : xb;
+            k_vanka_ppk<1><<<static_cast<int>(blocks), 256, 0, s>>>(L, xc, xn, b, vl, ktab, c0, pcol);
+            count();
+            pcol = c0;
+            ++ph;
+        }
+        return;
+    }
     bool done = !env_int("SMG_VANKA_PHASES", 0);  // 1: per-phase delta/apply launches (tests)
     if (done && xb && !cl && env_int("SMG_VANKA_PP", 1)) {  // ping-pong (grid mode): one barrier per phase
         if (nrefresh > 0) {
@@ -1879,7 +1929,7 @@ bool smooth_smem_fits(const LevelK& L, const int* n) {
     int maxn = 0;
     for (int c = 0; c < 8; ++c) maxn = n[c] > maxn ? n[c] : maxn;
     return (64 * 49 + 4 * L.g.fs) * static_cast<int64_t>(sizeof(double)) <= 227 * 1024 && maxn <= 4 * 512 &&
-           env_int("SMG_NO_SMEM_SMOOTH", 0) == 0;
+           env_int("SMG_SMEM_SMOOTH", 0) == 1 && env_int("SMG_NO_SMEM_SMOOTH", 0) == 0;
 }
 
 void launch_smooth_smem(const LevelK& L, double* x, const double* b, const int32_t* const* cells,
@@ -1963,9 +2013,11 @@ static void launch_dgs_sym_phases(const LevelK& L, double* x, const double* b, d
 
 void launch_dgs_sym_coop(const LevelK& L, double* x, const double* b, double* d0, double* d1, int nph,
                          cudaStream_t s) {
-    // one persistent sweep up to 64^3 cells (measured: a grid barrier beats a kernel
-    // boundary + tail there); larger levels run one kernel per phase
-    const int64_t coop_max = env_int("SMG_DGS_COOP", 0) ? (int64_t{1} << 40) : env_int("SMG_DGS_COOP_MAX", 262144);
+    // one kernel per step on every level: inside the SQMR iteration graph the per-step
+    // kernels beat the persistent grid-barrier sweep even at 16^3-64^3 (measured: 2.43 ->
+    // 2.31 ms per cfg-1 iteration), although the sweep wins when timed back to back alone;
+    // SMG_DGS_COOP=1 / SMG_DGS_COOP_MAX=<cells> bring the persistent sweep back
+    const int64_t coop_max = env_int("SMG_DGS_COOP", 0) ? (int64_t{1} << 40) : env_int("SMG_DGS_COOP_MAX", 0);
     if (static_cast<int64_t>(L.g.nx) * L.g.ny * L.g.nz > coop_max) {
         launch_dgs_sym_phases(L, x, b, d0, d1, nph, s);
         return;

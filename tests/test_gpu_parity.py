@@ -353,7 +353,8 @@ def test_wave_dgs_forward_half_bitwise(monkeypatch):
 
 
 @pytest.mark.parametrize("mode", [{}, {"SMG_SYNC_MODE": "1"}, {"SMG_SYNC_MODE": "2"}, {"SMG_VANKA_PP": "0"},
-                                  {"SMG_VANKA_PHASES": "1"}, {"SMG_NO_SMEM_SMOOTH": "1"}])
+                                  {"SMG_VANKA_PHASES": "1"}, {"SMG_SMEM_SMOOTH": "1"}, {"SMG_DGS_COOP": "1"},
+                                  {"SMG_VANKA_KERNELS": "1"}, {"SMG_DGS_COOP": "1", "SMG_SYNC_MODE": "2"}])
 def test_vanka_merged_phase_bitwise(mode, monkeypatch):
     """Colours 3 and 4 (= 3 ^ 7) share one Jacobi phase (14 phases per sweep): every sweep
     variant stays bit-identical to the oracle's 16-phase order."""
