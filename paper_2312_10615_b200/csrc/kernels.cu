@@ -37,6 +37,16 @@ namespace {
 
 constexpr int BX = 32, BY = 8;
 
+// Programmatic dependent launch: kernels launched by launch_k may start while the
+// previous kernel drains; they wait here (before touching memory) until it has
+// completed and its writes are visible.  A no-op for ordinary launches.
+// The trigger right after lets the next kernel's blocks be scheduled as soon as every
+// block of this one has started (they then wait for this grid's completion).
+__device__ __forceinline__ void pdl_wait() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 inline dim3 cell_grid(const Geom& g) { return dim3((g.nx + BX - 1) / BX, (g.ny + BY - 1) / BY, g.nz); }
 
 struct Cell {
@@ -85,6 +95,7 @@ __device__ __forceinline__ double cont(const LevelK& L, AU U, AV V, AW W, AP P, 
 // ------------------------------------------------------------- apply ------
 __global__ void k_apply(LevelK L, const double* __restrict__ X, const double* __restrict__ B,
                         double* __restrict__ Y, double gamma) {
+    pdl_wait();
     Cell c;
     if (!thread_cell(L.g, c)) return;
     const Geom& g = L.g;
@@ -279,6 +290,7 @@ __device__ __forceinline__ double restrict_face(const double* __restrict__ R, in
 }
 
 __global__ void k_restrict(LevelK F, LevelK C, const double* __restrict__ R, double* __restrict__ BC, int zc_lo) {
+    pdl_wait();
     const Geom &fg = F.g, &cg = C.g;
     Cell c;
     c.x = blockIdx.x * BX + threadIdx.x;
@@ -353,6 +365,7 @@ __device__ __forceinline__ double prolong_face(const double* __restrict__ E, con
 }
 
 __global__ void k_prolong_add(LevelK F, LevelK C, const double* __restrict__ E, double* __restrict__ X) {
+    pdl_wait();
     Cell c;
     if (!thread_cell(F.g, c)) return;
     const Geom &fg = F.g, &cg = C.g;
@@ -371,6 +384,7 @@ __global__ void k_prolong_add(LevelK F, LevelK C, const double* __restrict__ E, 
 constexpr int CG_ROWS = 32, CG_LANES = 32;
 __global__ void k_coarse_gemv(const double* __restrict__ K, const int32_t* __restrict__ slots, int n,
                               const double* __restrict__ B, double* __restrict__ X) {
+    pdl_wait();
     extern __shared__ double part[];  // [nchunks][CG_ROWS]
     const int row = blockIdx.x * CG_ROWS + threadIdx.x;
     const int nchunks = (n + 63) / 64;
@@ -394,6 +408,7 @@ __global__ void k_coarse_gemv(const double* __restrict__ K, const int32_t* __res
 // Compact FieldVector order: u (x in 1..nx-1), v, w, p, each lexicographic with
 // x fastest.
 __global__ void k_pack(LevelK L, const double* __restrict__ X, double* __restrict__ out, int unpack) {
+    pdl_wait();
     Cell c;
     if (!thread_cell(L.g, c)) return;
     const Geom& g = L.g;
@@ -428,6 +443,7 @@ constexpr int kMaxPlanes = 4 * 1025 + 4;
 __global__ void __launch_bounds__(RED_T) k_cdot(Geom g, const double* __restrict__ a, const double* __restrict__ b,
                                                 const double* __restrict__ c, const double* __restrict__ d,
                                                 double* __restrict__ partials) {
+    pdl_wait();
     __shared__ double rows0[1040], rows1[1040];
     const int z = blockIdx.x, f = blockIdx.y;
     // local planes; the slab holding the global top plane also owns the top w wall plane
@@ -467,6 +483,7 @@ __global__ void __launch_bounds__(RED_T) k_cdot(Geom g, const double* __restrict
 }
 
 __global__ void k_cdot_final(const double* __restrict__ partials, int nq, double* __restrict__ out) {
+    pdl_wait();
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
     const double* p = partials + w * kMaxPlanes;
     double s = 0.0;
@@ -851,6 +868,7 @@ template <int CPT>
 __global__ void __launch_bounds__(256) k_vanka_ppk(LevelK L, const double* __restrict__ Xc, double* __restrict__ Xn,
                                                    const double* __restrict__ B, VankaLists vl,
                                                    const double* __restrict__ ktab, int col, int pcol) {
+    pdl_wait();
     vanka_pp_phase<CPT, false>(L, Xc, Xn, B, vl, ktab, col, pcol, nullptr, blockIdx.x * blockDim.x + threadIdx.x,
                                gridDim.x * blockDim.x);
 }
@@ -868,6 +886,7 @@ __global__ void __launch_bounds__(512) k_vanka_pp(LevelK L, double* __restrict__
 
 __global__ void k_refresh(const int32_t* __restrict__ lst, int64_t n, const double* __restrict__ src,
                           double* __restrict__ dst) {
+    pdl_wait();
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
         const int64_t k = lst[t];
         dst[k] = src[k];
@@ -1299,6 +1318,7 @@ __global__ void __launch_bounds__(512) k_smooth_dsm(LevelK L, double* __restrict
 template <int ZC>
 __global__ void __launch_bounds__(256) k_dgs_vel_c(LevelK L, double* __restrict__ X, const double* __restrict__ B,
                                                    int colour) {
+    pdl_wait();
     const Geom& g = L.g;
     const int i = blockIdx.x * 32 + threadIdx.x, y = blockIdx.y * 8 + threadIdx.y;
 #pragma unroll
@@ -1378,6 +1398,7 @@ template <int ZC>
 // colours of one plane pair run side by side
 __global__ void __launch_bounds__(256) k_dgs_pf_lazy_c(LevelK L, double* __restrict__ X, const double* __restrict__ B,
                                                        double* __restrict__ D, int grp) {
+    pdl_wait();
     const Geom& g = L.g;
     const int i = blockIdx.x * 32 + threadIdx.x, j = blockIdx.y * 8 + threadIdx.y;
     const int nc = group_size(grp), c = group_colour(grp, blockIdx.z % nc);
@@ -1390,6 +1411,7 @@ __global__ void __launch_bounds__(256) k_dgs_pf_lazy_c(LevelK L, double* __restr
 }
 
 __global__ void __launch_bounds__(256) k_dgs_pf_flush(LevelK L, double* __restrict__ X, const double* __restrict__ D) {
+    pdl_wait();
     Cell c;
     if (!thread_cell(L.g, c)) return;
     flush_gathers(L, X, D, c.x, c.y, c.z);
@@ -1398,6 +1420,7 @@ __global__ void __launch_bounds__(256) k_dgs_pf_flush(LevelK L, double* __restri
 template <int ZC>
 __global__ void __launch_bounds__(256) k_dgs_prev_c(LevelK L, double* __restrict__ X, const double* __restrict__ B,
                                                     int grp) {
+    pdl_wait();
     const Geom& g = L.g;
     const int i = blockIdx.x * 32 + threadIdx.x, j = blockIdx.y * 8 + threadIdx.y;
     const int nc = group_size(grp), c = group_colour(grp, blockIdx.z % nc);
@@ -1551,18 +1574,21 @@ __global__ void __launch_bounds__(kWaveThreads, 3) k_dgs_wave(LevelK L, double* 
 // order as the oracle), so one SQMR iteration is a fixed kernel sequence that
 // can be replayed as a CUDA graph.  sc[] layout: see SqmrSlot in smg_internal.h.
 __global__ void k_sqmr_first(double* sc) {  // after dot2(t,t, s,q) of the initial V-cycle
+    pdl_wait();
     sc[S_TAU] = sqrt(sc[S_D0]);
     sc[S_NUOLD] = 0.0;
     sc[S_RHO] = sc[S_D1];
     sc[S_STATUS] = fabs(sc[S_RHO]) < 1e-300 ? 2.0 : 0.0;
 }
 __global__ void k_sqmr_alpha(double* sc) {  // after sigma = q.t
+    pdl_wait();
     if (sc[S_STATUS] != 0.0) return;
     const double sigma = sc[S_D0];
     if (fabs(sigma) < 1e-300) { sc[S_STATUS] = 2.0; return; }
     sc[S_ALPHA] = sc[S_RHO] / sigma;
 }
 __global__ void k_sqmr_nu(double* sc) {  // after ||t||^2 and rho_j = s.t
+    pdl_wait();
     if (sc[S_STATUS] != 0.0) return;
     const double nu = sqrt(sc[S_D0]) / sc[S_TAU];
     const double c = 1.0 / sqrt(1.0 + nu * nu);
@@ -1574,6 +1600,7 @@ __global__ void k_sqmr_nu(double* sc) {  // after ||t||^2 and rho_j = s.t
     sc[S_RHONEW] = sc[S_D1];
 }
 __global__ void k_sqmr_beta(double* sc) {  // after ||b - L x||^2
+    pdl_wait();
     if (sc[S_STATUS] != 0.0) return;
     const double rel = sqrt(sc[S_D0]) / sc[S_BNORM];
     sc[S_REL] = rel;
@@ -1586,6 +1613,7 @@ __global__ void k_sqmr_beta(double* sc) {  // after ||b - L x||^2
 }
 __global__ void k_axpy_s(double* __restrict__ s, const double* __restrict__ t, const double* __restrict__ sc,
                          int64_t n) {  // s = s - alpha t
+    pdl_wait();
     if (sc[S_STATUS] != 0.0) return;
     const double a = sc[S_ALPHA];
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
@@ -1593,6 +1621,7 @@ __global__ void k_axpy_s(double* __restrict__ s, const double* __restrict__ t, c
 }
 __global__ void k_dx_dev(double* __restrict__ d, double* __restrict__ x, const double* __restrict__ q,
                          const double* __restrict__ sc, int64_t n) {  // d = cd d + cq q; x += d
+    pdl_wait();
     if (sc[S_STATUS] != 0.0) return;
     const double cd = sc[S_CD], cq = sc[S_CQ];
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
@@ -1603,6 +1632,7 @@ __global__ void k_dx_dev(double* __restrict__ d, double* __restrict__ x, const d
 }
 __global__ void k_xpby_dev(double* __restrict__ q, const double* __restrict__ t, const double* __restrict__ sc,
                            int64_t n) {  // q = t + beta q
+    pdl_wait();
     if (sc[S_STATUS] != 0.0) return;
     const double b = sc[S_BETA];
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
@@ -1617,8 +1647,26 @@ inline int stream_blocks(int64_t n) {
 }  // namespace
 
 // ----------------------------------------------------------- launchers ------
+static int env_int(const char* name, int dflt);
+// Launch with the programmatic-stream-serialization attribute (SMG_PDL=0 disables):
+// the kernel's launch and block scheduling overlap the previous kernel's tail.
+template <typename... KArgs, typename... Args>
+static void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+    static const int pdl = env_int("SMG_PDL", 1);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    note(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...));
+}
 void launch_apply(const LevelK& L, const double* x, const double* b, double* y, double gamma, cudaStream_t s) {
-    k_apply<<<cell_grid(L.g), dim3(BX, BY), 0, s>>>(L, x, b, y, gamma);
+    launch_k(k_apply, cell_grid(L.g), dim3(BX, BY), 0, s, L, x, b, y, gamma);
     count();
 }
 void launch_dgs_vel(const LevelK& L, double* x, const double* b, int colour, cudaStream_t s) {
@@ -1655,11 +1703,11 @@ void launch_restrict(const LevelK& F, const LevelK& C, const double* rf, double*
     dim3 grid = cell_grid(C.g);
     grid.z = nzc < 0 ? C.g.nz : nzc;
     if (grid.z == 0) return;
-    k_restrict<<<grid, dim3(BX, BY), 0, s>>>(F, C, rf, bc, zc_lo);
+    launch_k(k_restrict, grid, dim3(BX, BY), 0, s, F, C, rf, bc, zc_lo);
     count();
 }
 void launch_prolong_add(const LevelK& F, const LevelK& C, const double* xc, double* xf, cudaStream_t s) {
-    k_prolong_add<<<cell_grid(F.g), dim3(BX, BY), 0, s>>>(F, C, xc, xf);
+    launch_k(k_prolong_add, cell_grid(F.g), dim3(BX, BY), 0, s, F, C, xc, xf);
     count();
 }
 void launch_coarse_gemv(const double* ksym, const int32_t* slots, int n, const double* b, double* x,
@@ -1671,30 +1719,30 @@ void launch_coarse_gemv(const double* ksym, const int32_t* slots, int n, const d
         cudaFuncSetAttribute(k_coarse_gemv, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         attr_set = true;
     }
-    k_coarse_gemv<<<(n + CG_ROWS - 1) / CG_ROWS, dim3(CG_ROWS, CG_LANES), smem, s>>>(ksym, slots, n, b, x);
+    launch_k(k_coarse_gemv, (n + CG_ROWS - 1) / CG_ROWS, dim3(CG_ROWS, CG_LANES), smem, s, ksym, slots, n, b, x);
     count();
 }
 void launch_pack(const LevelK& L, const double* padded, double* compact, cudaStream_t s) {
-    k_pack<<<cell_grid(L.g), dim3(BX, BY), 0, s>>>(L, padded, compact, 0);
+    launch_k(k_pack, cell_grid(L.g), dim3(BX, BY), 0, s, L, padded, compact, 0);
     count();
 }
 void launch_unpack(const LevelK& L, const double* compact, double* padded, cudaStream_t s) {
-    k_pack<<<cell_grid(L.g), dim3(BX, BY), 0, s>>>(L, padded, const_cast<double*>(compact), 1);
+    launch_k(k_pack, cell_grid(L.g), dim3(BX, BY), 0, s, L, padded, const_cast<double*>(compact), 1);
     count();
 }
 void launch_cdot_planes(const Geom& g, const double* a, const double* b, const double* c, const double* d,
                         double* partials, cudaStream_t s) {
-    k_cdot<<<dim3(g.nz + 1, 4), RED_T, 0, s>>>(g, a, b, c, d, partials);
+    launch_k(k_cdot, dim3(g.nz + 1, 4), RED_T, 0, s, g, a, b, c, d, partials);
     count();
 }
 void launch_cdot_final(const Geom& g, const double* partials, double* out, cudaStream_t s) {
-    k_cdot_final<<<1, 64, 0, s>>>(partials, 4 * g.gnz + 1, out);
+    launch_k(k_cdot_final, 1, 64, 0, s, partials, 4 * g.gnz + 1, out);
     count();
 }
 void launch_cdot2(const Geom& g, const double* a, const double* b, const double* c, const double* d,
                   double* partials, double* out, cudaStream_t s) {
-    k_cdot<<<dim3(g.nz + 1, 4), RED_T, 0, s>>>(g, a, b, c, d, partials);
-    k_cdot_final<<<1, 64, 0, s>>>(partials, 4 * g.gnz + 1, out);
+    launch_k(k_cdot, dim3(g.nz + 1, 4), RED_T, 0, s, g, a, b, c, d, partials);
+    launch_k(k_cdot_final, 1, 64, 0, s, partials, 4 * g.gnz + 1, out);
     count();
     count();
 }
@@ -1822,7 +1870,7 @@ void launch_vanka_sym_coop(const LevelK& L, double* x, const double* b, const in
     if (xb && env_int("SMG_VANKA_KERNELS", 0)) {  // ping-pong, one launch per phase
         if (nrefresh > 0) {
             const int64_t blocks = (nrefresh + 255) / 256;
-            k_refresh<<<static_cast<int>(blocks < 4096 ? blocks : 4096), 256, 0, s>>>(refresh, nrefresh, x, xb);
+            launch_k(k_refresh, static_cast<int>(blocks < 4096 ? blocks : 4096), 256, 0, s, refresh, nrefresh, x, xb);
             count();
         }
         const int64_t blocks = (8 * static_cast<int64_t>(maxn) + 255) / 256;  // one lane group per block
@@ -1832,7 +1880,7 @@ void launch_vanka_sym_coop(const LevelK& L, double* x, const double* b, const in
             if (merged >= 0 && c0 == 4) continue;
             const double* xc = (ph & 1) ? xb : x;
             double* xn = (ph & 1) ? x : xb;
-            k_vanka_ppk<1><<<static_cast<int>(blocks), 256, 0, s>>>(L, xc, xn, b, vl, ktab, c0, pcol);
+            launch_k(k_vanka_ppk<1>, static_cast<int>(blocks), 256, 0, s, L, xc, xn, b, vl, ktab, c0, pcol);
             count();
             pcol = c0;
             ++ph;
@@ -1843,7 +1891,7 @@ void launch_vanka_sym_coop(const LevelK& L, double* x, const double* b, const in
     if (done && xb && !cl && env_int("SMG_VANKA_PP", 1)) {  // ping-pong (grid mode): one barrier per phase
         if (nrefresh > 0) {
             const int64_t blocks = (nrefresh + 255) / 256;
-            k_refresh<<<static_cast<int>(blocks < 4096 ? blocks : 4096), 256, 0, s>>>(refresh, nrefresh, x, xb);
+            launch_k(k_refresh, static_cast<int>(blocks < 4096 ? blocks : 4096), 256, 0, s, refresh, nrefresh, x, xb);
             count();
         }
         void* pargs[] = {args[0], &x, &xb, args[2], args[3], args[4], args[5]};
@@ -1962,7 +2010,7 @@ static dim3 dgs_grid_h(const Geom& g) {
     return dim3((((g.nx + 1) / 2) + 31) / 32, (((g.ny + 1) / 2) + 7) / 8, (g.nz + 1) / 2);
 }
 void launch_dgs_vel_c(const LevelK& L, double* x, const double* b, int colour, cudaStream_t s) {
-    k_dgs_vel_c<1><<<dgs_grid_v(L.g), dim3(32, 8), 0, s>>>(L, x, b, colour);
+    launch_k(k_dgs_vel_c<1>, dgs_grid_v(L.g), dim3(32, 8), 0, s, L, x, b, colour);
     count();
 }
 void launch_dgs_pf_delta_c(const LevelK& L, const double* x, const double* b, double* d, int c, cudaStream_t s) {
@@ -1974,7 +2022,7 @@ void launch_dgs_pf_apply_c(const LevelK& L, double* x, const double* d, int c, c
     count();
 }
 void launch_dgs_prev_c(const LevelK& L, double* x, const double* b, int c, cudaStream_t s) {
-    k_dgs_prev_c<1><<<dgs_grid_h(L.g), dim3(32, 8), 0, s>>>(L, x, b, colour_group(c, 0, 0, 1));
+    launch_k(k_dgs_prev_c<1>, dgs_grid_h(L.g), dim3(32, 8), 0, s, L, x, b, colour_group(c, 0, 0, 1));
     count();
 }
 
@@ -1988,15 +2036,15 @@ static void dgs_sym_phases_zc(const LevelK& L, double* x, const double* b, doubl
     gv.z = (gv.z + ZC - 1) / ZC;
     gh.z = (gh.z + ZC - 1) / ZC;
     auto groups_grid = [&](int grp) { return dim3(gh.x, gh.y, gh.z * group_size(grp)); };
-    k_dgs_vel_c<ZC><<<gv, blk, 0, s>>>(L, x, b, 0);
-    k_dgs_vel_c<ZC><<<gv, blk, 0, s>>>(L, x, b, 1);
-    for (int q = 0; q < 4; ++q) k_dgs_pf_lazy_c<ZC><<<groups_grid(fwd_group(q)), blk, 0, s>>>(L, x, b, d0, fwd_group(q));
-    k_dgs_pf_flush<<<cell_grid(g), blk, 0, s>>>(L, x, d0);
+    launch_k(k_dgs_vel_c<ZC>, gv, blk, 0, s, L, x, b, 0);
+    launch_k(k_dgs_vel_c<ZC>, gv, blk, 0, s, L, x, b, 1);
+    for (int q = 0; q < 4; ++q) launch_k(k_dgs_pf_lazy_c<ZC>, groups_grid(fwd_group(q)), blk, 0, s, L, x, b, d0, fwd_group(q));
+    launch_k(k_dgs_pf_flush, cell_grid(g), blk, 0, s, L, x, d0);
     for (int k = 0; k < 7; ++k) count();
     if (nph <= 10) return;
-    for (int q = 0; q < 4; ++q) k_dgs_prev_c<ZC><<<groups_grid(rev_group(q)), blk, 0, s>>>(L, x, b, rev_group(q));
-    k_dgs_vel_c<ZC><<<gv, blk, 0, s>>>(L, x, b, 1);
-    k_dgs_vel_c<ZC><<<gv, blk, 0, s>>>(L, x, b, 0);
+    for (int q = 0; q < 4; ++q) launch_k(k_dgs_prev_c<ZC>, groups_grid(rev_group(q)), blk, 0, s, L, x, b, rev_group(q));
+    launch_k(k_dgs_vel_c<ZC>, gv, blk, 0, s, L, x, b, 1);
+    launch_k(k_dgs_vel_c<ZC>, gv, blk, 0, s, L, x, b, 0);
     for (int k = 0; k < 6; ++k) count();
 }
 
@@ -2112,23 +2160,23 @@ void launch_dgs_wave(const LevelK& L, const WavePass* passes, int npass, double*
 
 void launch_sqmr_scalar(int which, double* sc, cudaStream_t s) {
     switch (which) {
-        case 0: k_sqmr_first<<<1, 1, 0, s>>>(sc); break;
-        case 1: k_sqmr_alpha<<<1, 1, 0, s>>>(sc); break;
-        case 2: k_sqmr_nu<<<1, 1, 0, s>>>(sc); break;
-        default: k_sqmr_beta<<<1, 1, 0, s>>>(sc); break;
+        case 0: launch_k(k_sqmr_first, 1, 1, 0, s, sc); break;
+        case 1: launch_k(k_sqmr_alpha, 1, 1, 0, s, sc); break;
+        case 2: launch_k(k_sqmr_nu, 1, 1, 0, s, sc); break;
+        default: launch_k(k_sqmr_beta, 1, 1, 0, s, sc); break;
     }
     count();
 }
 void launch_axpy_s(double* s_, const double* t, const double* sc, int64_t n, cudaStream_t s) {
-    k_axpy_s<<<stream_blocks(n), 256, 0, s>>>(s_, t, sc, n);
+    launch_k(k_axpy_s, stream_blocks(n), 256, 0, s, s_, t, sc, n);
     count();
 }
 void launch_dx_dev(double* d, double* x, const double* q, const double* sc, int64_t n, cudaStream_t s) {
-    k_dx_dev<<<stream_blocks(n), 256, 0, s>>>(d, x, q, sc, n);
+    launch_k(k_dx_dev, stream_blocks(n), 256, 0, s, d, x, q, sc, n);
     count();
 }
 void launch_xpby_dev(double* q, const double* t, const double* sc, int64_t n, cudaStream_t s) {
-    k_xpby_dev<<<stream_blocks(n), 256, 0, s>>>(q, t, sc, n);
+    launch_k(k_xpby_dev, stream_blocks(n), 256, 0, s, q, t, sc, n);
     count();
 }
 void launch_axpy(double* y, const double* x, double alpha, int64_t n, cudaStream_t s) {
