@@ -1314,20 +1314,36 @@ __global__ void __launch_bounds__(512) k_smooth_dsm(LevelK L, double* __restrict
 // cheaper than a grid barrier), threads mapped onto the cells of the phase's
 // colour only, so every thread works and only the needed rows are touched.
 // Per-cell arithmetic is shared with the kernels above (bit-identical).
+// Block coordinates, traversed in reverse order when rev (bit 16 of the step argument):
+// consecutive steps alternate direction, so a step starts on the planes the previous
+// one touched last, while they are still in L2.
+struct BlkIdx {
+    int x, y, z;
+};
+__device__ __forceinline__ BlkIdx blk_idx(bool rev) {
+    if (!rev) return BlkIdx{static_cast<int>(blockIdx.x), static_cast<int>(blockIdx.y), static_cast<int>(blockIdx.z)};
+    return BlkIdx{static_cast<int>(gridDim.x - 1 - blockIdx.x), static_cast<int>(gridDim.y - 1 - blockIdx.y),
+                  static_cast<int>(gridDim.z - 1 - blockIdx.z)};
+}
+constexpr int kRevBit = 1 << 16;
+
 // ZC independent cells per thread (planes z, z + gridDim.z, ...): more loads in flight
 template <int ZC>
 __global__ void __launch_bounds__(256) k_dgs_vel_c(LevelK L, double* __restrict__ X, const double* __restrict__ B,
                                                    int colour) {
     pdl_wait();
     const Geom& g = L.g;
-    const int i = blockIdx.x * 32 + threadIdx.x, y = blockIdx.y * 8 + threadIdx.y;
+    const BlkIdx bk = blk_idx(colour & kRevBit);
+    colour &= 1;
+    const int i = bk.x * 32 + threadIdx.x, y = bk.y * 8 + threadIdx.y;
 #pragma unroll
     for (int q = 0; q < ZC; ++q) {
-        const int z = blockIdx.z + q * gridDim.z;
+        const int z = bk.z + q * gridDim.z;
         const int x = 2 * i + ((y + g.gz(z) + colour) & 1);
         if (x < g.nx && y < g.ny && z < g.nz) dgs_vel_cell(L, X, B, x, y, z);
     }
 }
+
 
 __device__ __forceinline__ bool half_cell(const Geom& g, int c, int i, int j, int k, int& x, int& y, int& z) {
     x = 2 * i + (c & 1);
@@ -1400,9 +1416,11 @@ __global__ void __launch_bounds__(256) k_dgs_pf_lazy_c(LevelK L, double* __restr
                                                        double* __restrict__ D, int grp) {
     pdl_wait();
     const Geom& g = L.g;
-    const int i = blockIdx.x * 32 + threadIdx.x, j = blockIdx.y * 8 + threadIdx.y;
-    const int nc = group_size(grp), c = group_colour(grp, blockIdx.z % nc);
-    const int kz = blockIdx.z / nc, nkz = gridDim.z / nc;
+    const BlkIdx bk = blk_idx(grp & kRevBit);
+    grp &= kRevBit - 1;
+    const int i = bk.x * 32 + threadIdx.x, j = bk.y * 8 + threadIdx.y;
+    const int nc = group_size(grp), c = group_colour(grp, bk.z % nc);
+    const int kz = bk.z / nc, nkz = gridDim.z / nc;
 #pragma unroll
     for (int q = 0; q < ZC; ++q) {
         int x, y, z;
@@ -1410,11 +1428,13 @@ __global__ void __launch_bounds__(256) k_dgs_pf_lazy_c(LevelK L, double* __restr
     }
 }
 
-__global__ void __launch_bounds__(256) k_dgs_pf_flush(LevelK L, double* __restrict__ X, const double* __restrict__ D) {
+__global__ void __launch_bounds__(256) k_dgs_pf_flush(LevelK L, double* __restrict__ X, const double* __restrict__ D,
+                                                      int rev) {
     pdl_wait();
-    Cell c;
-    if (!thread_cell(L.g, c)) return;
-    flush_gathers(L, X, D, c.x, c.y, c.z);
+    const BlkIdx bk = blk_idx(rev);
+    const int x = bk.x * BX + threadIdx.x, y = bk.y * BY + threadIdx.y;
+    if (x >= L.g.nx || y >= L.g.ny) return;
+    flush_gathers(L, X, D, x, y, bk.z);
 }
 
 template <int ZC>
@@ -1422,9 +1442,11 @@ __global__ void __launch_bounds__(256) k_dgs_prev_c(LevelK L, double* __restrict
                                                     int grp) {
     pdl_wait();
     const Geom& g = L.g;
-    const int i = blockIdx.x * 32 + threadIdx.x, j = blockIdx.y * 8 + threadIdx.y;
-    const int nc = group_size(grp), c = group_colour(grp, blockIdx.z % nc);
-    const int kz = blockIdx.z / nc, nkz = gridDim.z / nc;
+    const BlkIdx bk = blk_idx(grp & kRevBit);
+    grp &= kRevBit - 1;
+    const int i = bk.x * 32 + threadIdx.x, j = bk.y * 8 + threadIdx.y;
+    const int nc = group_size(grp), c = group_colour(grp, bk.z % nc);
+    const int kz = bk.z / nc, nkz = gridDim.z / nc;
 #pragma unroll
     for (int q = 0; q < ZC; ++q) {
         int x, y, z;
@@ -2036,14 +2058,18 @@ static void dgs_sym_phases_zc(const LevelK& L, double* x, const double* b, doubl
     gv.z = (gv.z + ZC - 1) / ZC;
     gh.z = (gh.z + ZC - 1) / ZC;
     auto groups_grid = [&](int grp) { return dim3(gh.x, gh.y, gh.z * group_size(grp)); };
+    // consecutive steps alternate the traversal direction (kRevBit): L2 reuse between steps
+    const int alt = env_int("SMG_DGS_ALT", 1) ? kRevBit : 0;
     launch_k(k_dgs_vel_c<ZC>, gv, blk, 0, s, L, x, b, 0);
-    launch_k(k_dgs_vel_c<ZC>, gv, blk, 0, s, L, x, b, 1);
-    for (int q = 0; q < 4; ++q) launch_k(k_dgs_pf_lazy_c<ZC>, groups_grid(fwd_group(q)), blk, 0, s, L, x, b, d0, fwd_group(q));
-    launch_k(k_dgs_pf_flush, cell_grid(g), blk, 0, s, L, x, d0);
+    launch_k(k_dgs_vel_c<ZC>, gv, blk, 0, s, L, x, b, 1 | alt);
+    for (int q = 0; q < 4; ++q)
+        launch_k(k_dgs_pf_lazy_c<ZC>, groups_grid(fwd_group(q)), blk, 0, s, L, x, b, d0, fwd_group(q) | (q & 1 ? alt : 0));
+    launch_k(k_dgs_pf_flush, cell_grid(g), blk, 0, s, L, x, d0, 0);
     for (int k = 0; k < 7; ++k) count();
     if (nph <= 10) return;
-    for (int q = 0; q < 4; ++q) launch_k(k_dgs_prev_c<ZC>, groups_grid(rev_group(q)), blk, 0, s, L, x, b, rev_group(q));
-    launch_k(k_dgs_vel_c<ZC>, gv, blk, 0, s, L, x, b, 1);
+    for (int q = 0; q < 4; ++q)
+        launch_k(k_dgs_prev_c<ZC>, groups_grid(rev_group(q)), blk, 0, s, L, x, b, rev_group(q) | (q & 1 ? 0 : alt));
+    launch_k(k_dgs_vel_c<ZC>, gv, blk, 0, s, L, x, b, 1 | alt);
     launch_k(k_dgs_vel_c<ZC>, gv, blk, 0, s, L, x, b, 0);
     for (int k = 0; k < 6; ++k) count();
 }
