@@ -274,6 +274,10 @@ struct smg_ctx {
     // plane partials and gathers travel through NCCL on the part's stream
     bool mp = false;
     ncclComm_t comm = nullptr;
+    // single-part SQMR: apply + inner product + scalar update fused (opt-in, SMG_FUSED_DOT=1)
+    bool fused_dot = true;
+    unsigned* dot_done = nullptr;
+    double* dot_rows = nullptr;
 
     template <class T>
     T* dalloc(int64_t count) {
@@ -615,6 +619,9 @@ void build(smg_ctx* c, const std::vector<double>* shared_coarse = nullptr, std::
     for (auto& L : c->lv) maxN = std::max(maxN, L.N);
     c->compact = c->dalloc<double>(maxN);
     c->partials = c->dalloc<double>(kPartials);
+    c->dot_done = c->dalloc<unsigned>(c->lv[0].k.g.nz + 2);
+    c->dot_rows = c->dalloc<double>(4 * static_cast<int64_t>(c->lv[0].k.g.ny + 1) * (c->lv[0].k.g.nz + 1));
+    c->fused_dot = env_int("SMG_FUSED_DOT", 0) != 0;  // opt-in: measured slower
     c->dscal = c->dalloc<double>(S_COUNT);
     CK(cudaMallocHost(&c->hscal, 8 * sizeof(double)));
     CK(cudaStreamSynchronize(c->st));
@@ -717,17 +724,25 @@ void sqmr_iteration(smg_ctx* c) {
     const int64_t n = vlen(F);
     double *s = F.b, *t = F.x, *r = F.r, *sc = c->dscal;
     const Geom& g = F.k.g;
-    launch_apply(F.k, c->q, nullptr, t, 0.0, c->st);                     // t = L q
-    launch_cdot2(g, c->q, t, nullptr, nullptr, c->partials, sc + S_D0, c->st);  // sigma
-    launch_sqmr_scalar(1, sc, c->st);                                    // alpha
+    if (c->fused_dot) {  // t = L q, sigma = q.t, alpha: one kernel
+        launch_apply_dot(F.k, c->q, nullptr, t, 0.0, 0, c->dot_rows, c->partials, sc, c->dot_done, 1, c->st);
+    } else {
+        launch_apply(F.k, c->q, nullptr, t, 0.0, c->st);                     // t = L q
+        launch_cdot2(g, c->q, t, nullptr, nullptr, c->partials, sc + S_D0, c->st);  // sigma
+        launch_sqmr_scalar(1, sc, c->st);                                    // alpha
+    }
     launch_axpy_s(s, t, sc, n, c->st);                                   // s -= alpha t
     vcycle(c, 0, s, t);                                                  // t = V(s)
     launch_cdot2(g, t, t, s, t, c->partials, sc + S_D0, c->st);          // ||t||^2, rho_j
     launch_sqmr_scalar(2, sc, c->st);                                    // nu, c, tau, cd, cq
     launch_dx_dev(c->d, c->xs, c->q, sc, n, c->st);                      // d, x
-    launch_apply(F.k, c->xs, c->rhs, r, 0.0, c->st);                     // r = b - L x
-    launch_cdot2(g, r, r, nullptr, nullptr, c->partials, sc + S_D0, c->st);
-    launch_sqmr_scalar(3, sc, c->st);                                    // rel, beta
+    if (c->fused_dot) {  // r = b - L x, ||r||^2, rel and beta: one kernel
+        launch_apply_dot(F.k, c->xs, c->rhs, r, 0.0, 1, c->dot_rows, c->partials, sc, c->dot_done, 3, c->st);
+    } else {
+        launch_apply(F.k, c->xs, c->rhs, r, 0.0, c->st);                     // r = b - L x
+        launch_cdot2(g, r, r, nullptr, nullptr, c->partials, sc + S_D0, c->st);
+        launch_sqmr_scalar(3, sc, c->st);                                    // rel, beta
+    }
     launch_xpby_dev(c->q, t, sc, n, c->st);                              // q = t + beta q
 }
 

@@ -1602,12 +1602,15 @@ __global__ void k_sqmr_first(double* sc) {  // after dot2(t,t, s,q) of the initi
     sc[S_RHO] = sc[S_D1];
     sc[S_STATUS] = fabs(sc[S_RHO]) < 1e-300 ? 2.0 : 0.0;
 }
-__global__ void k_sqmr_alpha(double* sc) {  // after sigma = q.t
-    pdl_wait();
+__device__ __forceinline__ void sqmr_alpha(double* sc) {  // after sigma = q.t
     if (sc[S_STATUS] != 0.0) return;
     const double sigma = sc[S_D0];
     if (fabs(sigma) < 1e-300) { sc[S_STATUS] = 2.0; return; }
     sc[S_ALPHA] = sc[S_RHO] / sigma;
+}
+__global__ void k_sqmr_alpha(double* sc) {
+    pdl_wait();
+    sqmr_alpha(sc);
 }
 __global__ void k_sqmr_nu(double* sc) {  // after ||t||^2 and rho_j = s.t
     pdl_wait();
@@ -1621,8 +1624,12 @@ __global__ void k_sqmr_nu(double* sc) {  // after ||t||^2 and rho_j = s.t
     sc[S_NU] = nu;
     sc[S_RHONEW] = sc[S_D1];
 }
-__global__ void k_sqmr_beta(double* sc) {  // after ||b - L x||^2
+__device__ __forceinline__ void sqmr_beta(double* sc);
+__global__ void k_sqmr_beta(double* sc) {
     pdl_wait();
+    sqmr_beta(sc);
+}
+__device__ __forceinline__ void sqmr_beta(double* sc) {  // after ||b - L x||^2
     if (sc[S_STATUS] != 0.0) return;
     const double rel = sqrt(sc[S_D0]) / sc[S_BNORM];
     sc[S_REL] = rel;
@@ -1633,6 +1640,144 @@ __global__ void k_sqmr_beta(double* sc) {  // after ||b - L x||^2
     sc[S_RHO] = rho_new;
     sc[S_NUOLD] = sc[S_NU];
 }
+// Fused y = L x (B == nullptr) or y = B - L x, and the canonical inner product
+// sc[S_D0] = a.y with a = x (sigma = q.(L q)) or a = y (||b - L x||^2), followed by
+// the SQMR scalar update `which` (1 alpha, 3 beta) -- one launch instead of four.
+// Block = R whole rows of one plane, one thread per cell (all four fields, as
+// k_apply); the products go to shared memory and warp (row, field) adds them in
+// k_cdot's order (lane l: x = l, l+32, ... ascending, then the shuffle tree).
+// Row sums go to rowbuf; the last block of a plane adds them in ascending y
+// (k_cdot's plane partial) and the last plane combines all partials in
+// k_cdot_final's order: bit-identical to apply + launch_cdot2 + scalar kernel.
+constexpr int kAdThreads = 512;
+__global__ void __launch_bounds__(1024) k_apply_dot(LevelK L, const double* __restrict__ X,
+                                                          const double* __restrict__ B, double* __restrict__ Y,
+                                                          double gamma, int dot_y, int R,
+                                                          double* __restrict__ rowbuf, double* __restrict__ partials,
+                                                          double* __restrict__ sc, unsigned* __restrict__ cnt,
+                                                          int which) {
+    pdl_wait();
+    extern __shared__ double prod[];  // [R][4][nx + 1]
+    __shared__ int flag;
+    const Geom& g = L.g;
+    const int nx = g.nx, px = nx + 1;
+    const int r = threadIdx.x / nx, x = threadIdx.x - r * nx;
+    const int y = blockIdx.x * R + r, z = blockIdx.y;
+    const int64_t fs = g.fs;
+    const double *U = X, *V = X + fs, *W = X + 2 * fs, *P = X + 3 * fs;
+    const int gzz = g.gz(z);
+    const bool top = g.z0 + g.nz == g.gnz;
+    if (r < R) {
+        double* pr = prod + r * 4 * px;
+        double pu = 0.0, pv = 0.0, pw = 0.0, pp = 0.0;
+        if (y < g.ny && z < g.nz) {
+            const int64_t i = g.slot(x, y, z);
+            if (x >= 1) {
+                const double yv = mom(L, U, P, i, 1);
+                const double v = B ? B[i] - yv : yv;
+                Y[i] = v;
+                pu = (dot_y ? v : U[i]) * v;
+            } else {
+                pu = (dot_y ? 0.0 : U[i]) * 0.0;
+            }
+            if (y >= 1) {
+                const double yv = mom(L, V, P, i, g.sy);
+                const double v = B ? B[fs + i] - yv : yv;
+                Y[fs + i] = v;
+                pv = (dot_y ? v : V[i]) * v;
+            } else {
+                pv = (dot_y ? 0.0 : V[i]) * 0.0;
+            }
+            if (gzz >= 1) {
+                const double yv = mom(L, W, P, i, g.sz);
+                const double v = B ? B[2 * fs + i] - yv : yv;
+                Y[2 * fs + i] = v;
+                pw = (dot_y ? v : W[i]) * v;
+            } else {
+                pw = (dot_y ? 0.0 : W[i]) * 0.0;
+            }
+            const double yv = cont(L, U, V, W, P, i, gamma);
+            const double v = B ? B[3 * fs + i] - yv : yv;
+            Y[3 * fs + i] = v;
+            pp = (dot_y ? v : P[i]) * v;
+        } else if (y <= g.ny) {  // wall row of v (y = ny) / top wall plane of w (z = nz): zero products
+            const int64_t i = g.slot(x, y, z);
+            if (y == g.ny && z < g.nz) pv = (dot_y ? 0.0 : V[i]) * 0.0;
+            if (z == g.nz && y < g.ny) pw = (dot_y ? 0.0 : W[i]) * 0.0;
+        }
+        pr[x] = pu;
+        pr[px + x] = pv;
+        pr[2 * px + x] = pw;
+        pr[3 * px + x] = pp;
+        if (x == 0) pr[nx] = y <= g.ny ? (dot_y ? 0.0 : U[g.slot(nx, y, z)]) * 0.0 : 0.0;  // u wall face x = nx
+    }
+    __syncthreads();
+    // warp (row rr, field f) forms the row sum in the canonical lane order
+    const int wid = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (wid < 4 * R) {
+        const int rr = wid >> 2, f = wid & 3, yy = blockIdx.x * R + rr;
+        const bool has = f == 1 ? (yy <= g.ny && z < g.nz)
+                                : (yy < g.ny && (z < g.nz || (f == 2 && z == g.nz && top)));
+        if (has) {
+            const double* pr = prod + (rr * 4 + f) * px;
+            const int ex = nx + (f == 0);
+            double s0 = 0.0;
+            for (int xx = l; xx < ex; xx += 32) s0 = s0 + pr[xx];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) s0 = s0 + __shfl_down_sync(0xffffffffu, s0, o);
+            if (l == 0) rowbuf[(f * (g.nz + 1) + z) * (g.ny + 1) + yy] = s0;
+        }
+    }
+    // last block of this plane: plane partials (rows ascending); last plane: the final
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        flag = atomicAdd(cnt + 1 + z, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!flag) return;
+    __threadfence();
+    // stage the plane's row sums in shared memory (parallel loads), then add them in order
+    double* rs = prod;  // [4][ny + 1]
+    for (int k = threadIdx.x; k < 4 * (g.ny + 1); k += blockDim.x) {
+        const int f = k / (g.ny + 1), yy = k - f * (g.ny + 1);
+        rs[k] = __ldcg(rowbuf + (f * (g.nz + 1) + z) * (g.ny + 1) + yy);
+    }
+    __syncthreads();
+    if (threadIdx.x < 4) {
+        const int f = threadIdx.x;
+        const int ey = g.ny + (f == 1);
+        const bool has = f == 2 ? (z < g.nz || top) : z < g.nz;
+        if (has) {
+            double p0 = 0.0;
+            for (int yy = 0; yy < ey; ++yy) p0 = p0 + rs[f * (g.ny + 1) + yy];
+            partials[f * g.gnz + (f == 3 ? 1 : 0) + gzz] = p0;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        cnt[1 + z] = 0u;
+        __threadfence();
+        flag = atomicAdd(cnt, 1u) == gridDim.y - 1;
+    }
+    __syncthreads();
+    if (!flag) return;
+    __threadfence();
+    if (wid == 0) {
+        const int nq = 4 * g.gnz + 1;
+        double s1 = 0.0;
+        for (int k = l; k < nq; k += 32) s1 = s1 + __ldcg(partials + k);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s1 = s1 + __shfl_down_sync(0xffffffffu, s1, o);
+        if (l == 0) {
+            sc[S_D0] = s1;
+            if (which == 1) sqmr_alpha(sc);
+            else if (which == 3) sqmr_beta(sc);
+            cnt[0] = 0u;  // ready for the next launch (graph replay)
+        }
+    }
+}
+
 __global__ void k_axpy_s(double* __restrict__ s, const double* __restrict__ t, const double* __restrict__ sc,
                          int64_t n) {  // s = s - alpha t
     pdl_wait();
@@ -2182,6 +2327,22 @@ void launch_dgs_wave(const LevelK& L, const WavePass* passes, int npass, double*
         k_dgs_wave<<<grid, kWaveThreads, 0, s>>>(L, x, b, d0, p);
         count();
     }
+}
+
+void launch_apply_dot(const LevelK& L, const double* x, const double* b, double* y, double gamma, int dot_y,
+                      double* rowbuf, double* partials, double* sc, unsigned* cnt, int which, cudaStream_t s) {
+    const Geom& g = L.g;
+    const int R = std::max(1, std::min(kAdThreads / g.nx, 8));  // whole rows per block (nx <= 1024)
+    const size_t smem = std::max<size_t>(static_cast<size_t>(R) * 4 * (g.nx + 1), 4 * static_cast<size_t>(g.ny + 1)) *
+                        sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+        note(cudaFuncSetAttribute(k_apply_dot, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+        attr = true;
+    }
+    launch_k(k_apply_dot, dim3((g.ny + 1 + R - 1) / R, g.nz + 1), dim3(std::max(R * g.nx, 4 * R * 32)), smem, s, L,
+             x, b, y, gamma, dot_y, R, rowbuf, partials, sc, cnt, which);
+    count();
 }
 
 void launch_sqmr_scalar(int which, double* sc, cudaStream_t s) {

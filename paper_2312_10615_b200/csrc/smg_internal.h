@@ -147,6 +147,12 @@ enum SqmrSlot {
 // which: 0 first (tau, rho from the initial dots), 1 alpha, 2 nu/c/tau/cd/cq, 3 rel/convergence/beta.
 // status slot: 0 running, 1 converged, 2 breakdown before the residual (sigma), 3 breakdown after it (rho).
 void launch_sqmr_scalar(int which, double* sc, cudaStream_t s);
+// Fused y = L x (b null) or y = b - L x, sc[S_D0] = x.y (dot_y = 0) or y.y (dot_y = 1) in
+// the canonical order, then the scalar update `which` (1 alpha, 3 beta) -- bit-identical to
+// launch_apply + launch_cdot2 + launch_sqmr_scalar.  rowbuf: 4 (ny+1)(nz+1) doubles;
+// cnt: nz + 2 zeroed device counters (reset by the kernel).
+void launch_apply_dot(const LevelK& L, const double* x, const double* b, double* y, double gamma, int dot_y,
+                      double* rowbuf, double* partials, double* sc, unsigned* cnt, int which, cudaStream_t s);
 void launch_axpy_s(double* s_, const double* t, const double* sc, int64_t n, cudaStream_t s);
 void launch_dx_dev(double* d, double* x, const double* q, const double* sc, int64_t n, cudaStream_t s);
 void launch_xpby_dev(double* q, const double* t, const double* sc, int64_t n, cudaStream_t s);

@@ -384,3 +384,18 @@ def test_vanka_merged_matches_unmerged(n, levels, monkeypatch):
         s.close()
     for a, c in zip(*out):
         same(a, c)
+
+
+@pytest.mark.parametrize("dims,levels", [((32, 32, 32), 3), ((64, 16, 16), 3), ((48, 40, 24), 3)])
+def test_fused_apply_dot_matches_separate(dims, levels, monkeypatch):
+    """Opt-in fused apply + canonical dot + scalar kernel (SMG_FUSED_DOT=1) == separate kernels, bit for bit."""
+    out = []
+    nx, ny, nz = dims
+    for fused in ("0", "1"):
+        monkeypatch.setenv("SMG_FUSED_DOT", fused)
+        s = smg.Solver(nx, ny, nz, h=1 / ny, levels=levels)
+        b = smg.forcing(nx, ny, nz, h=1 / ny, kind=smg.FORCE_UNIFORM, seed=11)
+        out.append(s.sqmr(b, 1e-8, 40))
+        s.close()
+    (x0, h0, _, s0), (x1, h1, _, s1) = out
+    assert s0 == s1 and np.array_equal(h0, h1) and np.array_equal(x0, x1)
