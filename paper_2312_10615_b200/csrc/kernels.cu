@@ -792,6 +792,33 @@ __device__ __forceinline__ void vanka_pp_phase(const LevelK& L, const double* __
         int m = 0;
         if (act) block_of(col, t, i, m);
         double r = 0.0, own = 0.0;
+        // the previous phase's block this lane carries into Xn (decided and loaded before the
+        // gather, so its L2 round trip overlaps the residual loads): all its DOFs except those
+        // this phase rewrites -- the same colour twice in a row (turning points), or a face
+        // shared with a band cell of a colour of this phase (colours one parity bit apart)
+        bool carry = false;
+        int64_t cdst = 0;
+        double cval = 0.0;
+        if (pcol >= 0 && pcol != col && t < vl.n[pcol] && s8 < 7) {
+            int64_t ip;
+            int mp;
+            block_of(pcol, t, ip, mp);
+            carry = s8 == 6 || (mp & (1 << s8));
+            if (carry && s8 < 6 && ((cmask >> (vanka_entry_colour(vl, pcol, t) ^ (1 << (s8 >> 1)))) & 1)) {
+                const int zl = static_cast<int>(ip / sz) - g.zg;
+                const int64_t rem = ip - static_cast<int64_t>(zl + g.zg) * sz;
+                const int y = static_cast<int>(rem / sy) - 1;
+                const int x = static_cast<int>(rem - static_cast<int64_t>(y + 1) * sy) - g.xo;
+                const int d = (s8 & 1) ? 1 : -1;
+                const int ax = s8 >> 1;
+                if (band_cell(L, x + (ax == 0 ? d : 0), y + (ax == 1 ? d : 0), zl + (ax == 2 ? d : 0)))
+                    carry = false;
+            }
+            if (carry) {
+                cdst = ip + offs;
+                cval = Xc[cdst];
+            }
+        }
         if (act && s8 < 7) r = vanka_slot_residual(L, Xc, B, i, m, s8, own);
 #ifdef SMG_TRACE
         if (__any_sync(0xffffffffu, r == 1.2345e300)) g_trace[0] = 0;  // wait for the gather
@@ -804,26 +831,7 @@ __device__ __forceinline__ void vanka_pp_phase(const LevelK& L, const double* __
             acc = acc + K[q] * rq;
         }
         if (act && s8 < 7 && (s8 == 6 || (m & (1 << s8)))) Xn[i + offs] = own + acc;
-        // carry the previous phase's blocks into the buffer being written, except DOFs
-        // this phase rewrites: the same colour twice in a row (turning points), or a face
-        // shared with a band cell of a colour of this phase (colours one parity bit apart)
-        if (pcol >= 0 && pcol != col && t < vl.n[pcol] && s8 < 7) {
-            int64_t ip;
-            int mp;
-            block_of(pcol, t, ip, mp);
-            bool carry = s8 == 6 || (mp & (1 << s8));
-            if (carry && s8 < 6 && ((cmask >> (vanka_entry_colour(vl, pcol, t) ^ (1 << (s8 >> 1)))) & 1)) {
-                const int zl = static_cast<int>(ip / sz) - g.zg;
-                const int64_t rem = ip - static_cast<int64_t>(zl + g.zg) * sz;
-                const int y = static_cast<int>(rem / sy) - 1;
-                const int x = static_cast<int>(rem - static_cast<int64_t>(y + 1) * sy) - g.xo;
-                const int d = (s8 & 1) ? 1 : -1;
-                const int ax = s8 >> 1;
-                if (band_cell(L, x + (ax == 0 ? d : 0), y + (ax == 1 ? d : 0), zl + (ax == 2 ? d : 0)))
-                    carry = false;
-            }
-            if (carry) Xn[ip + offs] = Xc[ip + offs];
-        }
+        if (carry) Xn[cdst] = cval;
     }
 }
 
