@@ -59,6 +59,8 @@ typedef struct smg_params {
     int band_width;  /* V1 band width (Chebyshev)                      */
     int flags;       /* SMG_FLAG_*                                     */
     int cycle;       /* 0 V-cycle, 1 W-cycle       */
+    int vanka;       /* 0 symmetric multiplicative, 1 additive */
+    double omega;    /* additive damping in (0, 1]; <= 0 means 1.0 (SPEC default) */
 } smg_params;
 
 #define SMG_FLAG_SKIP_REVERSE_DGS 1 /* fault injection: symmetry negative control */
@@ -130,7 +132,8 @@ int smg_residual(smg_ctx* ctx, int level, const double* x, const double* b, doub
  * 0..19: forward 0,1 velocity red/black, 2..9 pressure parity colours 0..7;
  * reverse 10..17 pressure colours 7..0, 18,19 velocity black/red), 1
  * symmetric_dgs, 2 one Vanka colour (arg = colour 0..7), 3 symmetric
- * multiplicative Vanka, 4 smooth (Alg. 3).  x is updated in place. */
+ * multiplicative Vanka, 4 smooth (Alg. 3, with the params' Vanka flavour), 5 one
+ * additive Vanka application.  x is updated in place. */
 int smg_smoother(smg_ctx* ctx, int level, int op, int arg, double* x, const double* b);
 
 /* transfer between level and level+1: rc = R rf, xf = P xc. */

@@ -61,6 +61,7 @@ def lib():
                                C.POINTER(C.c_int)]
         L.orc_forcing.argtypes = [C.c_void_p, C.c_int, C.c_uint64, _D]
         L.orc_set_cycle.argtypes = [C.c_void_p, C.c_int]
+        L.orc_set_vanka.argtypes = [C.c_void_p, C.c_int, C.c_double]
         L.orc_mg_solve.argtypes = [C.c_void_p, _D, _D, C.c_double, C.c_int, _D, _D, C.POINTER(C.c_int)]
         L.orc_census_box.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _I64]
         L.orc_coarsen_labels.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, _U8, _U8]
@@ -119,7 +120,7 @@ class Oracle:
     """Walled box of nx*ny*nz interior cells (implicit Dirichlet ring), spacing h."""
 
     def __init__(self, nx, ny=None, nz=None, h=None, eta=1.0, gamma=1e-3, levels=2, nu=1,
-                 band_width=1, cycle=0):
+                 band_width=1, cycle=0, vanka=0, omega=1.0):
         ny = nx if ny is None else ny
         nz = nx if nz is None else nz
         h = 1.0 / nx if h is None else h
@@ -131,6 +132,7 @@ class Oracle:
         self.levels = L.orc_nlevels(self._h)
         self.nu = nu
         L.orc_set_cycle(self._h, int(cycle))
+        L.orc_set_vanka(self._h, int(vanka), float(omega))  # 0 multiplicative, 1 additive
 
     def __del__(self):
         if getattr(self, "_h", None):

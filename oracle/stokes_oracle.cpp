@@ -221,6 +221,7 @@ struct Level {
     // Vanka blocks (band cells with an active pressure), by colour (OD-2)
     struct Block { std::array<int32_t, 7> dof; int mask; };
     std::vector<Block> vk[8];
+    std::vector<Block> vk_all;  // every block, ascending cell index (additive Vanka's summation order)
     std::map<int, std::array<double, 49>> vk_inv;  // factorisation cache keyed by face mask
     // face -> (left cell, right cell) pressure ids, for the distributive update
     std::vector<std::array<int32_t, 2>> fcells;
@@ -444,6 +445,7 @@ static void build_level(Level& L, const CellGrid& g, double eta, double gamma, i
     // Vanka blocks: one per band cell with an active
     // pressure; slots [uL,uR,vL,vR,wL,wR,p]; colour (i&1)+2(j&1)+4(k&1).
     for (int k = 0; k < 8; ++k) L.vk[k].clear();
+    L.vk_all.clear();
     L.vk_inv.clear();
     std::vector<std::pair<int32_t, double>> row;
     for (int z = 0; z < g.n[2]; ++z)
@@ -462,6 +464,7 @@ static void build_level(Level& L, const CellGrid& g, double eta, double gamma, i
                 blk.mask = mask;
                 const int col = (x & 1) + 2 * (y & 1) + 4 * (z & 1);
                 L.vk[col].push_back(blk);
+                L.vk_all.push_back(blk);
                 if (!L.vk_inv.count(mask)) {
                     // local matrix C_i L̃ C_i^T over the active slots, in slot order
                     std::vector<int32_t> act;
@@ -596,11 +599,60 @@ static void vanka_symmetric(const Level& L, vec& x, const vec& b) {
     for (int c = 7; c >= 0; --c) vanka_colour(L, x, b, c);
 }
 
+// vanka_additive (Eq. S_AV): r = b - L~x once; every block solves
+// against that same residual; each V1 DOF gets omega times the sum of the
+// corrections of the blocks containing it, added in ascending block (cell lex)
+// order starting from 0.0 -- a fixed order, so the result is deterministic and
+// independent of how the block solves are scheduled.
+static void vanka_additive(const Level& L, vec& x, const vec& b, double omega) {
+    const auto& blocks = L.vk_all;
+    std::vector<std::array<double, 7>> dl(blocks.size());
+    parallel_for(static_cast<int64_t>(blocks.size()), g_threads, [&](int64_t t) {
+        const auto& blk = blocks[t];
+        double r[7];
+        for (int s = 0; s < 7; ++s) {
+            const int32_t id = blk.dof[s];
+            if (id < 0) { r[s] = 0.0; continue; }
+            r[s] = b[id] - (s < 6 ? mom_row(L, x, id) : cont_row(L, x, id, L.gamma));
+        }
+        const auto& K = L.vk_inv.at(blk.mask);
+        for (int s = 0; s < 7; ++s) {
+            double acc = 0.0;
+            for (int q = 0; q < 7; ++q) acc = acc + K[s * 7 + q] * r[q];
+            dl[t][s] = acc;
+        }
+    });
+    vec acc(x.size(), 0.0);
+    std::vector<uint8_t> hit(x.size(), 0);
+    for (size_t t = 0; t < blocks.size(); ++t)
+        for (int s = 0; s < 7; ++s) {
+            const int32_t id = blocks[t].dof[s];
+            if (id < 0) continue;
+            acc[id] = acc[id] + dl[t][s];
+            hit[id] = 1;
+        }
+    for (size_t q = 0; q < x.size(); ++q)
+        if (hit[q]) x[q] = x[q] + omega * acc[q];
+}
+
+// Vanka flavour of the smoother (SmootherConfig).
+struct VankaCfg {
+    int kind = 0;        // 0 symmetric multiplicative, 1 additive
+    double omega = 1.0;  // additive damping
+};
+static VankaCfg g_vanka_default;
+
+static void vanka_apply(const Level& L, vec& x, const vec& b, const VankaCfg& vc) {
+    if (vc.kind == 1) vanka_additive(L, x, b, vc.omega);
+    else vanka_symmetric(L, x, b);
+}
+
 // smooth, Alg. 3: nu x Vanka(V1), symmetric DGS(V2), nu x Vanka(V1).
-static void smooth(const Level& L, vec& x, const vec& b, int nu, bool skip_reverse = false) {
-    for (int k = 0; k < nu; ++k) vanka_symmetric(L, x, b);
+static void smooth(const Level& L, vec& x, const vec& b, int nu, bool skip_reverse = false,
+                   const VankaCfg& vc = g_vanka_default) {
+    for (int k = 0; k < nu; ++k) vanka_apply(L, x, b, vc);
     symmetric_dgs(L, x, b, skip_reverse);
-    for (int k = 0; k < nu; ++k) vanka_symmetric(L, x, b);
+    for (int k = 0; k < nu; ++k) vanka_apply(L, x, b, vc);
 }
 
 // ------------------------------------------------------------ transfer ------
@@ -711,6 +763,7 @@ struct Hierarchy {
     int nu = 1;
     int cycle = 0;              // 0 V-cycle, 1 W-cycle
     bool skip_reverse = false;  // fault injection for the symmetry negative control
+    VankaCfg vanka;             // multiplicative (default) or additive Vanka on V1
 };
 
 static std::vector<double> assemble_dense(const Level& L, bool penalized) {
@@ -772,7 +825,7 @@ static void vcycle(const Hierarchy& H, int l, const vec& b, vec& x) {
     const Level& L = *H.lv[l];
     if (l == static_cast<int>(H.lv.size()) - 1) { coarse_solve(H, b, x); return; }
     x.assign(L.map.N, 0.0);
-    smooth(L, x, b, H.nu, H.skip_reverse);
+    smooth(L, x, b, H.nu, H.skip_reverse, H.vanka);
     vec r, rc, ec, ef;
     residual(L, x, b, r);
     restrict_(L, *H.lv[l + 1], r, rc);
@@ -787,7 +840,7 @@ static void vcycle(const Hierarchy& H, int l, const vec& b, vec& x) {
     }
     prolong(L, *H.lv[l + 1], ec, ef);
     for (int64_t q = 0; q < L.map.N; ++q) x[q] = x[q] + ef[q];
-    smooth(L, x, b, H.nu, H.skip_reverse);
+    smooth(L, x, b, H.nu, H.skip_reverse, H.vanka);
 }
 
 // ----------------------------------------------------- canonical dot -------
@@ -1083,6 +1136,11 @@ void orc_v1_mask(void* h, int l, uint8_t* mask) {
 }
 void orc_set_skip_reverse(void* h, int s) { HH(h).skip_reverse = s != 0; }
 void orc_set_cycle(void* h, int kind) { HH(h).cycle = kind; }
+// Vanka flavour: kind 0 symmetric multiplicative, 1 additive with damping omega.
+void orc_set_vanka(void* h, int kind, double omega) {
+    HH(h).vanka.kind = kind;
+    HH(h).vanka.omega = omega;
+}
 int orc_mg_solve(void* h, const double* b, double* x, double tol, int maxit, double* hist, double* secs, int* iters) {
     Hierarchy& H = HH(h);
     const int64_t n = H.lv[0]->map.N;
@@ -1107,7 +1165,7 @@ void orc_residual(void* h, int l, const double* x, const double* b, double* r) {
     out(rr, r);
 }
 // op: 0 one DGS phase (arg = phase 0..19), 1 symmetric DGS, 2 one Vanka colour
-// (arg = colour), 3 symmetric Vanka, 4 smooth (Alg. 3).
+// (arg = colour), 3 symmetric Vanka, 4 smooth (Alg. 3), 5 one additive Vanka.
 int orc_smoother(void* h, int l, int op, int arg, double* x, const double* b) {
     try {
         Hierarchy& H = HH(h);
@@ -1117,7 +1175,8 @@ int orc_smoother(void* h, int l, int op, int arg, double* x, const double* b) {
         else if (op == 1) symmetric_dgs(L, xx, bb, H.skip_reverse);
         else if (op == 2) vanka_colour(L, xx, bb, arg);
         else if (op == 3) vanka_symmetric(L, xx, bb);
-        else if (op == 4) smooth(L, xx, bb, H.nu, H.skip_reverse);
+        else if (op == 4) smooth(L, xx, bb, H.nu, H.skip_reverse, H.vanka);
+        else if (op == 5) vanka_additive(L, xx, bb, H.vanka.omega);
         else throw std::runtime_error("bad smoother op");
         out(xx, x);
         return 0;

@@ -21,7 +21,8 @@ FLAG_SKIP_REVERSE_DGS = 1
 FORCE_UNIFORM, FORCE_FOURIER, FORCE_CHANNEL = 0, 1, 2
 
 # smoother op codes of smg_smoother (include/smg.h)
-OP_DGS_PHASE, OP_DGS_SYM, OP_VANKA_COLOUR, OP_VANKA_SYM, OP_SMOOTH = 0, 1, 2, 3, 4
+OP_DGS_PHASE, OP_DGS_SYM, OP_VANKA_COLOUR, OP_VANKA_SYM, OP_SMOOTH, OP_VANKA_ADD = 0, 1, 2, 3, 4, 5
+VANKA_MULTIPLICATIVE, VANKA_ADDITIVE = 0, 1
 DGS_PHASES = 20
 
 
@@ -35,7 +36,8 @@ class GridDesc(C.Structure):
 
 class Params(C.Structure):
     _fields_ = [("eta", C.c_double), ("gamma", C.c_double), ("levels", C.c_int), ("nu", C.c_int),
-                ("band_width", C.c_int), ("flags", C.c_int), ("cycle", C.c_int)]
+                ("band_width", C.c_int), ("flags", C.c_int), ("cycle", C.c_int), ("vanka", C.c_int),
+                ("omega", C.c_double)]
 
 
 class History(C.Structure):
@@ -180,7 +182,7 @@ class Solver:
     """One device context (hierarchy + buffers) for a walled box of nx*ny*nz cells."""
 
     def __init__(self, nx, ny=None, nz=None, h=None, eta=1.0, gamma=1e-3, levels=2, nu=1, band_width=1,
-                 flags=0, device=0, devices=None, cycle=0):
+                 flags=0, device=0, devices=None, cycle=0, vanka=0, omega=1.0):
         """devices: list of CUDA device ids, one z-slab part each (repeat an id to emulate several
         parts on one GPU).  Default: a single part on `device`."""
         ny = nx if ny is None else ny
@@ -188,7 +190,7 @@ class Solver:
         h = 1.0 / nx if h is None else h
         L = lib()
         self.grid = GridDesc(3, nx, ny, nz, h)
-        self.params = Params(eta, gamma, levels, nu, band_width, flags, cycle)
+        self.params = Params(eta, gamma, levels, nu, band_width, flags, cycle, vanka, omega)
         ctx = C.c_void_p()
         devs = list(devices) if devices else [device]
         arr = (C.c_int * len(devs))(*devs)
@@ -201,7 +203,7 @@ class Solver:
 
     @classmethod
     def for_rank(cls, rank, nranks, nccl_id, nx, ny=None, nz=None, h=None, eta=1.0, gamma=1e-3, levels=2, nu=1,
-                 band_width=1, flags=0, device=0, cycle=0):
+                 band_width=1, flags=0, device=0, cycle=0, vanka=0, omega=1.0):
         """Rank `rank` of a one-process-per-GPU z-slab solver (smg_create_rank): every rank
         calls this with the same 128-byte NCCL id (nccl_unique_id() on rank 0, broadcast by
         the launcher) and its own device; later calls are collective."""
@@ -210,7 +212,7 @@ class Solver:
         h = 1.0 / nx if h is None else h
         self = cls.__new__(cls)
         self.grid = GridDesc(3, nx, ny, nz, h)
-        self.params = Params(eta, gamma, levels, nu, band_width, flags, cycle)
+        self.params = Params(eta, gamma, levels, nu, band_width, flags, cycle, vanka, omega)
         if len(nccl_id) != 128:
             raise ValueError("NCCL unique id must be 128 bytes")
         ctx = C.c_void_p()

@@ -130,8 +130,11 @@ int main(int argc, char** argv) {
         return 0;
     }
     if (cmd != "run") return usage();
+    const std::string vk = str("vanka", "multiplicative");  // SmootherConfig.kind
+    if (vk != "multiplicative" && vk != "additive") { std::fprintf(stderr, "config error: vanka\n"); return 1; }
     smg_params p{num("eta", 1e-3), num("gamma", 1e-3), static_cast<int>(num("levels", 2)),
-                 static_cast<int>(num("nu", 1)), bw, 0, str("cycle", "V") == "W" ? 1 : 0};
+                 static_cast<int>(num("nu", 1)), bw, 0, str("cycle", "V") == "W" ? 1 : 0,
+                 vk == "additive" ? 1 : 0, num("omega", 1.0)};
     const std::string method = str("method", "mg-sqmr");
     if (method != "mg-sqmr" && method != "mg") { std::fprintf(stderr, "config error: method\n"); return 1; }
     const std::string fk = str("forcing", "uniform");

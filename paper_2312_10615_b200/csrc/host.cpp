@@ -233,6 +233,11 @@ struct DevLevel {
     uint8_t* sw_mask[8] = {};
     int sw_n[8] = {};
     int sw_merged = -1;
+    // additive Vanka (params.vanka == 1): every block in one list + the 7-field correction scratch
+    int32_t* va_cells = nullptr;
+    uint8_t* va_mask = nullptr;
+    int va_n = 0;
+    double* va_d7 = nullptr;
     double* ktab = nullptr;  // [64][49]
     std::vector<WavePass> wave;  // fused wavefront DGS sweep (large single-part levels), empty: per-phase/coop
 };
@@ -343,11 +348,15 @@ void build_wave(smg_ctx* c, DevLevel& L) {
 void build(smg_ctx* c, const std::vector<double>* shared_coarse = nullptr, std::vector<double>* coarse_out = nullptr,
            cudaStream_t shared_stream = nullptr) {
     const smg_grid_desc& g = c->grid;
+    if (!(c->prm.omega > 0.0)) c->prm.omega = 1.0;  // SPEC default inside the preconditioner
     const smg_params& p = c->prm;
     if (g.dim != 3) throw SmgError(SMG_EINVAL, "dim must be 3");
     if (p.levels < 1) throw SmgError(SMG_EINVAL, "levels < 1");
     if (p.nu < 1 || p.band_width < 1) throw SmgError(SMG_EINVAL, "nu and band_width must be >= 1");
     if (p.cycle != 0 && p.cycle != 1) throw SmgError(SMG_EINVAL, "cycle must be 0 (V) or 1 (W)");
+    if (p.vanka != 0 && p.vanka != 1) throw SmgError(SMG_EINVAL, "vanka must be 0 (multiplicative) or 1 (additive)");
+    if (p.omega > 1.0) throw SmgError(SMG_EINVAL, "omega must lie in (0, 1] (<= 0: default 1)");
+    if (p.vanka == 1 && c->ndist > 0) throw SmgError(SMG_EINVAL, "additive Vanka: single-part contexts only");
     if (!(g.h > 0)) throw SmgError(SMG_EINVAL, "h must be > 0");
     const int div = 1 << (p.levels - 1);
     if (g.nx % div || g.ny % div || g.nz % div)
@@ -506,6 +515,21 @@ void build(smg_ctx* c, const std::vector<double>* shared_coarse = nullptr, std::
             CK(cudaMemcpyAsync(L.sw_mask[3], mm.data(), mm.size(), cudaMemcpyHostToDevice, c->st));
             CK(cudaStreamSynchronize(c->st));
             L.sw_merged = static_cast<int>(cells[3].size());
+        }
+        if (p.vanka == 1 && !dist) {
+            std::vector<int32_t> ac;
+            std::vector<uint8_t> am;
+            for (int col = 0; col < 8; ++col) {
+                ac.insert(ac.end(), cells[col].begin(), cells[col].end());
+                am.insert(am.end(), masks[col].begin(), masks[col].end());
+            }
+            L.va_n = static_cast<int>(ac.size());
+            L.va_cells = c->dalloc<int32_t>(L.va_n);
+            L.va_mask = c->dalloc<uint8_t>(L.va_n);
+            L.va_d7 = c->dalloc<double>(7 * L.k.g.fs);
+            CK(cudaMemcpyAsync(L.va_cells, ac.data(), ac.size() * sizeof(int32_t), cudaMemcpyHostToDevice, c->st));
+            CK(cudaMemcpyAsync(L.va_mask, am.data(), am.size(), cudaMemcpyHostToDevice, c->st));
+            CK(cudaStreamSynchronize(c->st));
         }
         // local inverses C_i L~ C_i^T per face mask, scattered to the 7-slot layout
         std::vector<double> ktab(64 * 49, 0.0);
@@ -673,8 +697,20 @@ void vanka_sym_coop(smg_ctx* c, int l, double* x, const double* b) {
                           L.vk_refresh, L.vk_nrefresh, L.sw_merged);
 }
 
+void vanka_additive(smg_ctx* c, int l, double* x, const double* b) {
+    DevLevel& L = c->lv[l];
+    if (!L.va_d7) throw SmgError(SMG_EINVAL, "additive Vanka needs params.vanka = 1 (single-part contexts)");
+    launch_vanka_additive(L.k, x, b, L.va_cells, L.va_mask, L.va_n, L.ktab, L.va_d7, c->prm.omega, c->st);
+}
+
 void smooth(smg_ctx* c, int l, double* x, const double* b) {
     DevLevel& L = c->lv[l];
+    if (c->prm.vanka == 1) {  // Alg. 3 with additive Vanka on V1
+        for (int k = 0; k < c->prm.nu; ++k) vanka_additive(c, l, x, b);
+        symmetric_dgs(c, l, x, b);
+        for (int k = 0; k < c->prm.nu; ++k) vanka_additive(c, l, x, b);
+        return;
+    }
     if (smooth_dsm_fits(L.k, L.sw_n)) {
         const int nph = (c->prm.flags & SMG_FLAG_SKIP_REVERSE_DGS) ? kDgsPhases / 2 : kDgsPhases;
         launch_smooth_dsm(L.k, x, b, L.sw_cells, L.sw_mask, L.sw_n, L.ktab, c->prm.nu, nph, c->st, L.sw_merged);
@@ -1473,7 +1509,9 @@ int smg_smoother(smg_ctx* c, int level, int op, int arg, double* x, const double
         } else if (op == 3) {
             launch_vanka_sym_coop(L.k, L.x, L.b, L.sw_cells, L.sw_mask, L.sw_n, L.ktab, c->vk_delta, 1, c->st,
                                   nullptr, nullptr, 0, L.sw_merged);
-        } else if (op == 5) {  // per-phase reference path of the symmetric sweeps (test only)
+        } else if (op == 5) {  // one additive Vanka application
+            vanka_additive(c, level, L.x, L.b);
+        } else if (op == 6) {  // per-phase reference path of the symmetric sweeps (test only)
             for (int ph = 0; ph < kDgsPhases; ++ph) dgs_phase(c, level, L.x, L.b, ph);
             vanka_sym(c, level, L.x, L.b);
         }

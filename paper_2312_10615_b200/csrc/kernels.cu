@@ -870,6 +870,80 @@ __device__ __forceinline__ void vanka_sweeps_pp(const LevelK& L, double* __restr
     }
 }
 
+// ---- additive Vanka (Eq. S_AV) ----
+// k_vadd_delta: every band block solves against the same x (8 lanes per block, the
+// multiplicative sweep's slot residuals and shuffle-gathered local solve) and
+// stores its correction by destination: D7 = [lo faces u, v, w at the block's own
+// slot | hi faces u, v, w at the neighbour slot | p].  k_vadd_apply: each V1 DOF
+// is written by one thread, x += omega * ((0.0 + corr of the lower block) + corr
+// of the upper block), i.e. the oracle's ascending-cell summation order.
+__global__ void __launch_bounds__(256) k_vadd_delta(LevelK L, const double* __restrict__ X,
+                                                    const double* __restrict__ B, const int32_t* __restrict__ cells,
+                                                    const uint8_t* __restrict__ masks, int n,
+                                                    const double* __restrict__ ktab, double* __restrict__ D7) {
+    pdl_wait();
+    const Geom& g = L.g;
+    const int64_t fs = g.fs;
+    const int lane = threadIdx.x & 31, s8 = lane & 7;
+    const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 3;
+    const bool act = t < n;
+    int64_t i = 0;
+    int m = 0;
+    if (act) {
+        i = cells[t];
+        m = masks[t];
+    }
+    double r = 0.0, own = 0.0;
+    if (act && s8 < 7) r = vanka_slot_residual(L, X, B, i, m, s8, own);
+    const double* K = ktab + m * 49 + (s8 < 7 ? s8 : 0) * 7;
+    double acc = 0.0;
+#pragma unroll
+    for (int q = 0; q < 7; ++q) {
+        const double rq = __shfl_sync(0xffffffffu, r, (lane & ~7) + q);
+        acc = acc + __ldg(K + q) * rq;
+    }
+    if (!act || s8 >= 7 || !(s8 == 6 || (m & (1 << s8)))) return;
+    if (s8 == 6) {
+        D7[6 * fs + i] = acc;
+    } else {
+        const int ax = s8 >> 1;
+        const int64_t st = ax == 0 ? 1 : (ax == 1 ? g.sy : g.sz);
+        if (s8 & 1) D7[(3 + ax) * fs + i + st] = acc;
+        else D7[ax * fs + i] = acc;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_vadd_apply(LevelK L, double* __restrict__ X,
+                                                    const int32_t* __restrict__ cells,
+                                                    const uint8_t* __restrict__ masks, int n,
+                                                    const double* __restrict__ D7, double omega) {
+    pdl_wait();
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const Geom& g = L.g;
+    const int64_t fs = g.fs, i = cells[t];
+    const int m = masks[t];
+    const int zl = static_cast<int>(i / g.sz) - g.zg;
+    const int64_t rem = i - static_cast<int64_t>(zl + g.zg) * g.sz;
+    const int y = static_cast<int>(rem / g.sy) - 1;
+    const int x = static_cast<int>(rem - static_cast<int64_t>(y + 1) * g.sy) - g.xo;
+    X[3 * fs + i] = X[3 * fs + i] + omega * (0.0 + D7[6 * fs + i]);
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+        const int64_t st = ax == 0 ? 1 : (ax == 1 ? g.sy : g.sz);
+        const int dx = ax == 0, dy = ax == 1, dz = ax == 2;
+        if (m & (1 << (2 * ax))) {  // low face: the lower cell's block (if band) first, then this one
+            double acc = 0.0;
+            if (band_cell(L, x - dx, y - dy, zl - dz)) acc = acc + D7[(3 + ax) * fs + i];
+            acc = acc + D7[ax * fs + i];
+            X[ax * fs + i] = X[ax * fs + i] + omega * acc;
+        }
+        if ((m & (1 << (2 * ax + 1))) && !band_cell(L, x + dx, y + dy, zl + dz)) {  // high face, this block only
+            X[ax * fs + i + st] = X[ax * fs + i + st] + omega * (0.0 + D7[(3 + ax) * fs + i + st]);
+        }
+    }
+}
+
 // One ping-pong phase per launch (graph nodes instead of grid barriers); the
 // local inverses are read through L1 (26 masks occur in a box).
 template <int CPT>
@@ -2350,6 +2424,17 @@ void launch_apply_dot(const LevelK& L, const double* x, const double* b, double*
     }
     launch_k(k_apply_dot, dim3((g.ny + 1 + R - 1) / R, g.nz + 1), dim3(std::max(R * g.nx, 4 * R * 32)), smem, s, L,
              x, b, y, gamma, dot_y, R, rowbuf, partials, sc, cnt, which);
+    count();
+}
+
+void launch_vanka_additive(const LevelK& L, double* x, const double* b, const int32_t* cells, const uint8_t* masks,
+                           int n, const double* ktab, double* d7, double omega, cudaStream_t s) {
+    if (n <= 0) return;
+    launch_k(k_vadd_delta, dim3(static_cast<unsigned>((8 * static_cast<int64_t>(n) + 255) / 256)), dim3(256), 0, s, L,
+             x, b, cells, masks, n, ktab, d7);
+    launch_k(k_vadd_apply, dim3(static_cast<unsigned>((n + 255) / 256)), dim3(256), 0, s, L, x, cells, masks, n, d7,
+             omega);
+    count();
     count();
 }
 

@@ -147,6 +147,10 @@ enum SqmrSlot {
 // which: 0 first (tau, rho from the initial dots), 1 alpha, 2 nu/c/tau/cd/cq, 3 rel/convergence/beta.
 // status slot: 0 running, 1 converged, 2 breakdown before the residual (sigma), 3 breakdown after it (rho).
 void launch_sqmr_scalar(int which, double* sc, cudaStream_t s);
+// One additive Vanka application over all n band blocks (any order);
+// d7: scratch of 7 fields (g.fs each).  Bit-identical to the oracle's fixed order.
+void launch_vanka_additive(const LevelK& L, double* x, const double* b, const int32_t* cells, const uint8_t* masks,
+                           int n, const double* ktab, double* d7, double omega, cudaStream_t s);
 // Fused y = L x (b null) or y = b - L x, sc[S_D0] = x.y (dot_y = 0) or y.y (dot_y = 1) in
 // the canonical order, then the scalar update `which` (1 alpha, 3 beta) -- bit-identical to
 // launch_apply + launch_cdot2 + launch_sqmr_scalar.  rowbuf: 4 (ny+1)(nz+1) doubles;

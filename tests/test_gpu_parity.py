@@ -399,3 +399,24 @@ def test_fused_apply_dot_matches_separate(dims, levels, monkeypatch):
         s.close()
     (x0, h0, _, s0), (x1, h1, _, s1) = out
     assert s0 == s1 and np.array_equal(h0, h1) and np.array_equal(x0, x1)
+
+
+@pytest.mark.parametrize("dims,levels,omega", [((16, 16, 16), 3, 0.5), ((32, 32, 32), 3, 0.5), ((64, 16, 16), 3, 1.0),
+                                               ((48, 40, 24), 3, 0.7)])
+def test_additive_vanka_bitwise(dims, levels, omega):
+    """Additive Vanka: one application, Alg. 3 with it, V-cycle and MG-SQMR bit-identical."""
+    oracle.set_threads(os.cpu_count() or 1)
+    nx, ny, nz = dims
+    o = oracle.Oracle(nx, ny, nz, h=1 / ny, levels=levels, vanka=1, omega=omega)
+    s = smg.Solver(nx, ny, nz, h=1 / ny, levels=levels, vanka=smg.VANKA_ADDITIVE, omega=omega)
+    for level in range(levels - 1):
+        n = o.ndof(level)
+        x, b = rnd(n, 80 + level), rnd(n, 81 + level)
+        same(s.smoother(smg.OP_VANKA_ADD, x, b, level), o.smoother(5, x, b, level))
+        same(s.smoother(smg.OP_SMOOTH, x, b, level), o.smoother(4, x, b, level))
+    b = o.forcing(oracle.FORCE_UNIFORM, 12)
+    same(s.vcycle(b), o.vcycle(b))
+    xo, ho, _, sto = o.sqmr(b, 1e-8, 30)
+    xg, hg, _, stg = s.sqmr(b, 1e-8, 30)
+    assert sto == stg and np.array_equal(ho, hg) and np.array_equal(xo, xg)
+    s.close()

@@ -233,3 +233,58 @@ def test_wcycle_symmetric_and_mg_solve_converges():
     x, h, _, st = o.mg_solve(b, 1e-6, 60)
     assert st == oracle.ST_CONVERGED and np.all(np.diff(h) < 0)
     assert np.isclose(np.linalg.norm(b - o.apply(x, penalized=True)) / np.linalg.norm(b), h[-1], rtol=1e-12)
+
+
+# ---- additive Vanka (Eq. S_AV) ----
+OP_VADD = 5
+
+
+def test_additive_vanka_symmetric_single_application():
+    """S_AV materialized with x0 = 0 is symmetric for ONE application (Theorem 2)."""
+    o = oracle.Oracle(8, levels=2, vanka=1)
+    n = o.ndof()
+    C = materialize(lambda e: o.smoother(OP_VADD, np.zeros(n), e), n)
+    assert np.abs(C).max() > 0
+    assert defect(C) < 1e-10
+
+
+def test_additive_vanka_linear_and_touches_only_v1():
+    o = oracle.Oracle(8, levels=2, vanka=1, omega=0.7)
+    n = o.ndof()
+    rng = np.random.default_rng(5)
+    x, b1, b2 = rng.standard_normal(n), rng.standard_normal(n), rng.standard_normal(n)
+    y1, y2 = o.smoother(OP_VADD, x, b1), o.smoother(OP_VADD, x, b2)
+    y12 = o.smoother(OP_VADD, x, 0.5 * b1 + 0.5 * b2)
+    assert np.allclose(y12, 0.5 * y1 + 0.5 * y2, rtol=0, atol=1e-12 * np.abs(y12).max())
+    v1 = o.v1_mask(0).astype(bool)
+    assert np.array_equal(y1[~v1], x[~v1])  # V2 DOFs untouched
+    assert not np.array_equal(y1[v1], x[v1])
+
+
+def test_additive_vanka_damping_scales_correction():
+    n8 = oracle.Oracle(8, levels=2).ndof()
+    rng = np.random.default_rng(6)
+    x, b = rng.standard_normal(n8), rng.standard_normal(n8)
+    d1 = oracle.Oracle(8, levels=2, vanka=1, omega=1.0).smoother(OP_VADD, x, b) - x
+    dh = oracle.Oracle(8, levels=2, vanka=1, omega=0.5).smoother(OP_VADD, x, b) - x
+    assert np.allclose(dh, 0.5 * d1, rtol=1e-12, atol=1e-14)
+
+
+def test_smooth_and_vcycle_with_additive_vanka_symmetric():
+    """Alg. 3 with additive Vanka and the V-cycle built on it stay symmetric (Theorem 4)."""
+    o = oracle.Oracle(8, levels=2, vanka=1)
+    n = o.ndof()
+    S = materialize(lambda e: o.smoother(OP_SMOOTH, np.zeros(n), e), n)
+    assert defect(S) < 1e-10
+    V = materialize(o.vcycle, n)
+    assert defect(V) < 1e-10
+
+
+def test_mg_sqmr_with_additive_vanka_converges():
+    """Damped (omega = 1/2: every band face sits in two overlapping blocks) additive Vanka inside
+    the preconditioner converges; undamped it stagnates, as SPEC:318's design note warns."""
+    oracle.set_threads(4)
+    o = oracle.Oracle(16, levels=3, vanka=1, omega=0.5)
+    b = o.forcing(oracle.FORCE_UNIFORM, 0)
+    _, hist, _, st = o.sqmr(b, 1e-8, 100)
+    assert st == 0 and hist[-1] < 1e-8 and len(hist) <= 15
