@@ -322,46 +322,45 @@ __global__ void k_restrict(LevelK F, LevelK C, const double* __restrict__ R, dou
 // read 0 (dropped, no renormalisation).
 // (fx, fy, fz) are GLOBAL fine indices; coarse slots are addressed through
 // cg.slot with local coarse planes (cg.z0 subtracted).
-__device__ __forceinline__ double prolong_face(const double* __restrict__ E, const Geom& cg, int comp, int fx,
-                                               int fy, int fz) {
-    int f[3] = {fx, fy, fz};
-    const int ta = comp == 0 ? 1 : 0, tb = comp == 2 ? 1 : 2;
-    int ni[2];
-    double nw[2];
-    int nn;
-    const int I = f[comp];
-    if ((I & 1) == 0) {
-        ni[0] = I >> 1;
-        nw[0] = 1.0;
-        nn = 1;
-    } else {
-        ni[0] = (I - 1) >> 1;
-        ni[1] = (I + 1) >> 1;
-        nw[0] = 0.5;
-        nw[1] = 0.5;
-        nn = 2;
-    }
-    const int pa = f[ta] >> 1, pb = f[tb] >> 1;
-    const int ia_[2] = {pa, (f[ta] & 1) ? pa + 1 : pa - 1};
-    const int ib_[2] = {pb, (f[tb] & 1) ? pb + 1 : pb - 1};
-    const double wt[2] = {0.75, 0.25};
-    double acc_b = 0.0;
-    for (int ib = 0; ib < 2; ++ib) {
-        double acc_a = 0.0;
-        for (int ia = 0; ia < 2; ++ia) {
-            double acc_n = 0.0;
-            for (int in = 0; in < nn; ++in) {
-                int cc[3];
-                cc[comp] = ni[in];
-                cc[ta] = ia_[ia];
-                cc[tb] = ib_[ib];
-                acc_n = acc_n + nw[in] * E[cg.slot(cc[0], cc[1], cc[2] - cg.z0)];
-            }
-            acc_a = acc_a + wt[ia] * acc_n;
+// Unrolled per component: the coarse legs are base, base + da (second tangential
+// a leg), base + db, base + db + da, and + dn for the second normal leg; the same
+// operations in the same order as the loop form (normal innermost, then a, then b).
+template <int COMP>
+__device__ __forceinline__ double prolong_face(const double* __restrict__ E, const Geom& cg, int fx, int fy, int fz) {
+    constexpr int TA = COMP == 0 ? 1 : 0, TB = COMP == 2 ? 1 : 2;
+    const int f[3] = {fx, fy, fz};
+    const int I = f[COMP];
+    int c[3];
+    c[COMP] = I >> 1;  // even I: I/2 (weight 1); odd I: (I-1)/2 and (I+1)/2 (1/2 each)
+    c[TA] = f[TA] >> 1;
+    c[TB] = f[TB] >> 1;
+    const int64_t st[3] = {1, cg.sy, cg.sz};
+    const int64_t base = cg.slot(c[0], c[1], c[2] - cg.z0);
+    const int64_t da = (f[TA] & 1) ? st[TA] : -st[TA];
+    const int64_t db = (f[TB] & 1) ? st[TB] : -st[TB];
+    const int64_t dn = st[COMP];
+    const bool odd = I & 1;
+    auto sn = [&](int64_t o) {
+        double s = 0.0;
+        if (!odd) {
+            s = s + 1.0 * E[o];
+        } else {
+            s = s + 0.5 * E[o];
+            s = s + 0.5 * E[o + dn];
         }
-        acc_b = acc_b + wt[ib] * acc_a;
-    }
-    return acc_b;
+        return s;
+    };
+    const double s00 = sn(base), s01 = sn(base + da), s10 = sn(base + db), s11 = sn(base + db + da);
+    double sb = 0.0;
+    double sa = 0.0;
+    sa = sa + 0.75 * s00;
+    sa = sa + 0.25 * s01;
+    sb = sb + 0.75 * sa;
+    sa = 0.0;
+    sa = sa + 0.75 * s10;
+    sa = sa + 0.25 * s11;
+    sb = sb + 0.25 * sa;
+    return sb;
 }
 
 __global__ void k_prolong_add(LevelK F, LevelK C, const double* __restrict__ E, double* __restrict__ X) {
@@ -371,9 +370,9 @@ __global__ void k_prolong_add(LevelK F, LevelK C, const double* __restrict__ E, 
     const Geom &fg = F.g, &cg = C.g;
     const int64_t ffs = fg.fs, cfs = cg.fs;
     const int z = fg.gz(c.z);
-    if (c.x >= 1) X[c.i] = X[c.i] + prolong_face(E, cg, 0, c.x, c.y, z);
-    if (c.y >= 1) X[ffs + c.i] = X[ffs + c.i] + prolong_face(E + cfs, cg, 1, c.x, c.y, z);
-    if (z >= 1) X[2 * ffs + c.i] = X[2 * ffs + c.i] + prolong_face(E + 2 * cfs, cg, 2, c.x, c.y, z);
+    if (c.x >= 1) X[c.i] = X[c.i] + prolong_face<0>(E, cg, c.x, c.y, z);
+    if (c.y >= 1) X[ffs + c.i] = X[ffs + c.i] + prolong_face<1>(E + cfs, cg, c.x, c.y, z);
+    if (z >= 1) X[2 * ffs + c.i] = X[2 * ffs + c.i] + prolong_face<2>(E + 2 * cfs, cg, c.x, c.y, z);
     X[3 * ffs + c.i] = X[3 * ffs + c.i] + E[3 * cfs + cg.slot(c.x >> 1, c.y >> 1, (z >> 1) - cg.z0)];
 }
 
