@@ -455,6 +455,8 @@ __global__ void __launch_bounds__(RED_T) k_cdot(Geom g, const double* __restrict
     for (int y = w; y < ey; y += RED_T / 32) {
         const int64_t row = off + g.slot(0, y, z);
         double s0 = 0.0, s1 = 0.0;
+        // unrolled: loads of several chunks in flight, additions still in ascending x
+#pragma unroll 4
         for (int x = l; x < ex; x += 32) {
             s0 = s0 + a[row + x] * b[row + x];
             if (c) s1 = s1 + c[row + x] * d[row + x];
