@@ -7,7 +7,8 @@
 // RunConfig (JSON, flat): nx, ny, nz (cells), h (default 1/nx), eta (1e-3),
 // gamma (1e-3), levels, nu (1), band_width (1), cycle ("V"|"W"), method
 // ("mg-sqmr"|"mg"), tol (1e-8), maxit (200), forcing ("uniform"|"fourier"|
-// "channel"|"cavity": lid-driven, u = lid (1) on the top y face), seed (0), output_dir (env SMG_OUTPUT_DIR, else "."), devices ([0]).
+// "channel"|"cavity": lid-driven, u = lid (1) on the top y face), seed (0), output_dir (env SMG_OUTPUT_DIR, else "."), devices ([0]),
+// vanka ("multiplicative"|"additive"), omega (1), vtk (0; 1 writes fields.vtk).
 // Defaults follow SPEC:567-569.  Exit codes: 0 converged,
 // 2 not converged, 1 usage/config error.
 #include <cerrno>
@@ -97,6 +98,39 @@ bool parse_json(const std::string& t, Config& c, std::string& err) {
     }
 }
 
+// fields.vtk: legacy ASCII STRUCTURED_POINTS, pressure as CELL_DATA
+// scalar, velocity averaged to cell centres (wall faces are 0, Dirichlet) as CELL_DATA
+// vector.  x is the compact FieldVector: u (faces 1..nx-1), v, w, p, x fastest.
+bool write_vtk(const std::string& path, int nx, int ny, int nz, double h, const std::vector<double>& x) {
+    FILE* fo = std::fopen(path.c_str(), "w");
+    if (!fo) return false;
+    const int64_t nu = static_cast<int64_t>(nx - 1) * ny * nz, nv = static_cast<int64_t>(nx) * (ny - 1) * nz;
+    const int64_t nw = static_cast<int64_t>(nx) * ny * (nz - 1);
+    auto U = [&](int i, int y, int z) {  // u-face i (0..nx), 0 on the walls
+        return (i <= 0 || i >= nx) ? 0.0 : x[(static_cast<int64_t>(z) * ny + y) * (nx - 1) + (i - 1)];
+    };
+    auto V = [&](int xx, int j, int z) {
+        return (j <= 0 || j >= ny) ? 0.0 : x[nu + (static_cast<int64_t>(z) * (ny - 1) + (j - 1)) * nx + xx];
+    };
+    auto W = [&](int xx, int y, int k) {
+        return (k <= 0 || k >= nz) ? 0.0 : x[nu + nv + (static_cast<int64_t>(k - 1) * ny + y) * nx + xx];
+    };
+    std::fprintf(fo, "# vtk DataFile Version 3.0\nstokes MG-SQMR solution\nASCII\nDATASET STRUCTURED_POINTS\n");
+    std::fprintf(fo, "DIMENSIONS %d %d %d\nORIGIN 0 0 0\nSPACING %.17g %.17g %.17g\n", nx + 1, ny + 1, nz + 1, h, h, h);
+    std::fprintf(fo, "CELL_DATA %lld\nSCALARS pressure double 1\nLOOKUP_TABLE default\n",
+                 static_cast<long long>(nx) * ny * nz);
+    for (int64_t k = 0; k < static_cast<int64_t>(nx) * ny * nz; ++k) std::fprintf(fo, "%.17g\n", x[nu + nv + nw + k]);
+    std::fprintf(fo, "VECTORS velocity double\n");
+    for (int z = 0; z < nz; ++z)
+        for (int y = 0; y < ny; ++y)
+            for (int xx = 0; xx < nx; ++xx)
+                std::fprintf(fo, "%.17g %.17g %.17g\n", 0.5 * (U(xx, y, z) + U(xx + 1, y, z)),
+                             0.5 * (V(xx, y, z) + V(xx, y + 1, z)), 0.5 * (W(xx, y, z) + W(xx, y, z + 1)));
+    const bool ok = std::ferror(fo) == 0;
+    std::fclose(fo);
+    return ok;
+}
+
 int usage() {
     std::fprintf(stderr, "usage: solver run <config.json> | solver census <config.json>\n");
     return 1;
@@ -184,5 +218,10 @@ int main(int argc, char** argv) {
         std::fclose(fo);
     }
     smg_destroy(ctx);
+    // emit flags: "vtk": 1 writes output_dir/fields.vtk
+    if (num("vtk", 0) != 0 && !write_vtk(dir + "/fields.vtk", g.nx, g.ny, g.nz, g.h, x)) {
+        std::fprintf(stderr, "cannot write %s/fields.vtk\n", dir.c_str());
+        return 1;
+    }
     return status == SMG_CONVERGED ? 0 : 2;
 }

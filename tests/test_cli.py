@@ -56,3 +56,27 @@ def test_run_writes_csv_and_summary(tmp_path):
     r = run(["run"], cfg, str(tmp_path))
     assert r.returncode == 2  # not converged
     assert len(open(tmp_path / "history_mg.csv").read().splitlines()) == 3
+
+
+@pytest.mark.gpu
+def test_run_writes_vtk_fields(tmp_path):
+    """emit flag vtk: legacy ASCII structured points, pressure + cell-centred velocity."""
+    cfg = {"nx": 16, "ny": 8, "nz": 12, "h": 1 / 8, "levels": 2, "eta": 1.0, "tol": 1e-8, "seed": 3,
+           "vtk": 1, "output_dir": str(tmp_path)}
+    r = run(["run"], cfg, str(tmp_path))
+    assert r.returncode == 0, r.stderr
+    lines = open(tmp_path / "fields.vtk").read().splitlines()
+    assert lines[0].startswith("# vtk DataFile") and lines[2] == "ASCII"
+    assert "DIMENSIONS 17 9 13" in lines and "CELL_DATA 1536" in lines
+    i = lines.index("LOOKUP_TABLE default")
+    p = np.array([float(v) for v in lines[i + 1:i + 1 + 1536]])
+    j = lines.index("VECTORS velocity double")
+    vel = np.array([[float(t) for t in l.split()] for l in lines[j + 1:j + 1 + 1536]])
+    s = smg.Solver(16, 8, 12, h=1 / 8, levels=2, eta=1.0)
+    x, _, _, _ = s.sqmr(smg.forcing(16, 8, 12, h=1 / 8, seed=3), 1e-8, 200)
+    nu, nv, nw = 15 * 8 * 12, 16 * 7 * 12, 16 * 8 * 11
+    assert np.array_equal(p, x[nu + nv + nw:])  # %.17g round-trips doubles exactly
+    u = np.zeros((12, 8, 17))
+    u[:, :, 1:16] = x[:nu].reshape(12, 8, 15)
+    assert np.allclose(vel[:, 0], (0.5 * (u[:, :, :-1] + u[:, :, 1:])).ravel(), rtol=0, atol=1e-15)
+    s.close()
