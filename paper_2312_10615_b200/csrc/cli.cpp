@@ -3,6 +3,7 @@
 //
 //   solver run <config.json>      solve; writes history_<method>.csv and summary.txt
 //   solver census <config.json>   prints "N V1 pct%" (PAPER Table 1 layout)
+//   solver verify [--max-n N]     symmetry of the materialised GPU smoother / V-cycle maps
 //
 // RunConfig (JSON, flat): nx, ny, nz (cells), h (default 1/nx), eta (1e-3),
 // gamma (1e-3), levels, nu (1), band_width (1), cycle ("V"|"W"), method
@@ -11,6 +12,7 @@
 // vanka ("multiplicative"|"additive"), omega (1), vtk (0; 1 writes fields.vtk).
 // Defaults follow SPEC:567-569.  Exit codes: 0 converged,
 // 2 not converged, 1 usage/config error.
+#include <algorithm>
 #include <cerrno>
 #include <chrono>
 #include <cmath>
@@ -132,13 +134,68 @@ bool write_vtk(const std::string& path, int nx, int ny, int nz, double h, const 
 }
 
 int usage() {
-    std::fprintf(stderr, "usage: solver run <config.json> | solver census <config.json>\n");
+    std::fprintf(stderr, "usage: solver run <config.json> | solver census <config.json> | solver verify [--max-n N]\n");
     return 1;
+}
+
+// verify (AC 3/4): materialise b -> x of the GPU smoothers and the
+// V-cycle on n^3 cubes (n = 4, 8, ... <= max_n, x0 = 0) and report ||C - C^T||_F / ||C||_F.
+int verify(int max_n) {
+    bool ok = true;
+    for (int n = 4; n <= max_n; n *= 2) {
+        smg_grid_desc g{3, n, n, n, 1.0 / n};
+        for (int vk = 0; vk < 2; ++vk) {
+            smg_params p{1.0, 1e-3, 2, 1, 1, 0, 0, vk, 0.5};
+            int dev = 0;
+            smg_ctx* ctx = nullptr;
+            if (smg_create(&g, &p, 1, &dev, &ctx) != SMG_OK) return 1;
+            const int64_t N = smg_level_ndof(ctx, 0, nullptr);
+            struct Map { const char* name; int op; };
+            const Map maps[] = {{"smooth", 4}, {vk ? "vanka_additive" : "vanka_symmetric", vk ? 5 : 3}, {"vcycle", -1}};
+            for (const Map& m : maps) {
+                std::vector<double> C(static_cast<size_t>(N * N)), e(N, 0.0), col(N);
+                for (int64_t j = 0; j < N; ++j) {
+                    e[j] = 1.0;
+                    int rc;
+                    if (m.op < 0) {
+                        rc = smg_vcycle(ctx, e.data(), col.data());
+                    } else {
+                        std::fill(col.begin(), col.end(), 0.0);
+                        rc = smg_smoother(ctx, 0, m.op, 0, col.data(), e.data());
+                    }
+                    if (rc != SMG_OK) { smg_destroy(ctx); return 1; }
+                    for (int64_t i = 0; i < N; ++i) C[static_cast<size_t>(i * N + j)] = col[i];
+                    e[j] = 0.0;
+                }
+                double d = 0.0, a = 0.0;
+                for (int64_t i = 0; i < N; ++i)
+                    for (int64_t j = 0; j < N; ++j) {
+                        const double c = C[static_cast<size_t>(i * N + j)], t = C[static_cast<size_t>(j * N + i)];
+                        d += (c - t) * (c - t);
+                        a += c * c;
+                    }
+                const double defect = std::sqrt(d) / std::fmax(std::sqrt(a), 1e-300);
+                const bool pass = defect < 1e-10 && a > 0.0;
+                ok = ok && pass;
+                std::printf("n=%d vanka=%s %s symmetry_defect=%.3e %s\n", n, vk ? "additive" : "multiplicative",
+                            m.name, defect, pass ? "PASS" : "FAIL");
+            }
+            smg_destroy(ctx);
+        }
+    }
+    return ok ? 0 : 2;
 }
 
 }  // namespace
 
 int main(int argc, char** argv) {
+    if (argc >= 2 && std::string(argv[1]) == "verify") {
+        int max_n = 8;
+        if (argc == 4 && std::string(argv[2]) == "--max-n") max_n = std::atoi(argv[3]);
+        else if (argc != 2) return usage();
+        if (max_n < 4) return usage();
+        return verify(max_n);
+    }
     if (argc != 3) return usage();
     const std::string cmd = argv[1];
     std::ifstream f(argv[2]);

@@ -80,3 +80,16 @@ def test_run_writes_vtk_fields(tmp_path):
     u[:, :, 1:16] = x[:nu].reshape(12, 8, 15)
     assert np.allclose(vel[:, 0], (0.5 * (u[:, :, :-1] + u[:, :, 1:])).ravel(), rtol=0, atol=1e-15)
     s.close()
+
+
+@pytest.mark.gpu
+def test_verify_symmetry():
+    """`solver verify`: materialised GPU smoother and V-cycle maps symmetric < 1e-10."""
+    r = subprocess.run([CLI, "verify", "--max-n", "8"], capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout + r.stderr
+    lines = r.stdout.splitlines()
+    assert len(lines) == 12 and all(l.endswith("PASS") for l in lines)
+
+
+def test_verify_usage():
+    assert subprocess.run([CLI, "verify", "--max-n"], capture_output=True).returncode == 1
