@@ -736,9 +736,13 @@ void vcycle(smg_ctx* c, int l, const double* b, double* x) {
     if (l == static_cast<int>(c->lv.size()) - 1) { coarse_solve(c, b, x); return; }
     CK(cudaMemsetAsync(x, 0, vlen(L) * sizeof(double), c->st));
     smooth(c, l, x, b);
-    launch_apply(L.k, x, b, L.r, L.k.gamma, c->st);
     DevLevel& C = c->lv[l + 1];
-    launch_restrict(L.k, C.k, L.r, C.b, c->st);
+    if (resrestrict_ok(L.k, C.k)) {
+        launch_residual_restrict(L.k, C.k, x, b, C.b, c->st);  // b_c = R (b - L~ x), one pass
+    } else {
+        launch_apply(L.k, x, b, L.r, L.k.gamma, c->st);
+        launch_restrict(L.k, C.k, L.r, C.b, c->st);
+    }
     vcycle(c, l + 1, C.b, C.x);
     // W-cycle: second recursive call below the finest level, on the residual of
     // the first (skipped when the child is the exact coarsest solve)

@@ -111,6 +111,11 @@ void launch_smooth_smem(const LevelK& L, double* x, const double* b, const int32
 void launch_restrict(const LevelK& F, const LevelK& C, const double* rf, double* bc, cudaStream_t s, int zc_lo = 0,
                      int nzc = -1);
 void launch_prolong_add(const LevelK& F, const LevelK& C, const double* xc, double* xf, cudaStream_t s);
+// Fused b_c = R (b - L~ x) (no fine residual vector), single-part levels; bit-identical
+// to launch_apply(b) + launch_restrict.  resrestrict_ok: the fused path applies (opt-in, SMG_FUSED_RR=1).
+bool resrestrict_ok(const LevelK& F, const LevelK& C);
+void launch_residual_restrict(const LevelK& F, const LevelK& C, const double* x, const double* b, double* bc,
+                              cudaStream_t s);
 void launch_coarse_gemv(const double* ksym, const int32_t* slots, int n, const double* b, double* x,
                         cudaStream_t s);
 void launch_pack(const LevelK& L, const double* padded, double* compact, cudaStream_t s);

@@ -420,3 +420,19 @@ def test_additive_vanka_bitwise(dims, levels, omega):
     xg, hg, _, stg = s.sqmr(b, 1e-8, 30)
     assert sto == stg and np.array_equal(ho, hg) and np.array_equal(xo, xg)
     s.close()
+
+
+@pytest.mark.parametrize("dims,levels", [((32, 32, 32), 3), ((64, 16, 16), 3), ((48, 40, 24), 3)])
+def test_fused_residual_restrict_bitwise(dims, levels, monkeypatch):
+    """Opt-in fused b_c = R (b - L~ x) (SMG_FUSED_RR=1): V-cycle and MG-SQMR bit-identical to the oracle."""
+    monkeypatch.setenv("SMG_FUSED_RR", "1")
+    oracle.set_threads(os.cpu_count() or 1)
+    nx, ny, nz = dims
+    o = oracle.Oracle(nx, ny, nz, h=1 / ny, levels=levels)
+    s = smg.Solver(nx, ny, nz, h=1 / ny, levels=levels)
+    b = o.forcing(oracle.FORCE_UNIFORM, 13)
+    same(s.vcycle(b), o.vcycle(b))
+    xo, ho, _, sto = o.sqmr(b, 1e-8, 20)
+    xg, hg, _, stg = s.sqmr(b, 1e-8, 20)
+    assert sto == stg and np.array_equal(ho, hg) and np.array_equal(xo, xg)
+    s.close()
