@@ -529,22 +529,27 @@ static void dgs_p_fwd(const Level& L, vec& x, const vec& b, int col, vec& delta)
 }
 
 // DGS reverse (left-preconditioned) pressure phase:
-// x_C += m_C^T (b - L̃ x) / d_p for V2 cells C of colour col.
-static void dgs_p_rev(const Level& L, vec& x, const vec& b, int col, vec& r) {
-    residual(L, x, b, r);
+// x_C += m_C^T (b - L̃ x) / d_p for V2 cells C of colour col, evaluated as
+// (m_C^T b - m_C^T (L̃ x)) / d_p: the b part is fixed while b is (the GPU computes it
+// once per sweep), each part with the same operation order.
+static double m_col_dot(const Level& L, const vec& v, int32_t c) {
+    const auto& f = L.pface[c];
+    const auto& nc = L.pcell[c];
+    const double fl = ((v[f[1]] - v[f[0]]) + (v[f[3]] - v[f[2]])) + (v[f[5]] - v[f[4]]);
+    double s = v[nc[0]] + v[nc[1]];
+    s = s + v[nc[2]];
+    s = s + v[nc[3]];
+    s = s + v[nc[4]];
+    s = s + v[nc[5]];
+    return fl * L.inv_h + L.eta_h2 * (6.0 * v[c] - s);
+}
+static void dgs_p_rev(const Level& L, vec& x, const vec& b, int col, vec& lx) {
+    apply(L, x, lx, true);  // L̃ x
     const auto& lst = L.dgs_p[col];
     parallel_for(static_cast<int64_t>(lst.size()), g_threads, [&](int64_t t) {
         const int32_t c = lst[t];
-        const auto& f = L.pface[c];
-        const auto& nc = L.pcell[c];
-        const double fl = ((r[f[1]] - r[f[0]]) + (r[f[3]] - r[f[2]])) + (r[f[5]] - r[f[4]]);
-        double s = r[nc[0]] + r[nc[1]];
-        s = s + r[nc[2]];
-        s = s + r[nc[3]];
-        s = s + r[nc[4]];
-        s = s + r[nc[5]];
-        const double cj = fl * L.inv_h + L.eta_h2 * (6.0 * r[c] - s);
-        x[c] = x[c] + cj / L.dp;
+        const double cb = m_col_dot(L, b, c), cl = m_col_dot(L, lx, c);
+        x[c] = x[c] + (cb - cl) / L.dp;
     });
 }
 

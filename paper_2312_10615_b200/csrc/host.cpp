@@ -404,6 +404,7 @@ void build(smg_ctx* c, const std::vector<double>* shared_coarse = nullptr, std::
         }
         L.pd0 = c->dalloc<double>(L.k.g.fs);
         L.pd1 = c->dalloc<double>(L.k.g.fs);
+        L.k.cb = c->dalloc<double>(L.k.g.fs);
         build_wave(c, L);
         // Vanka blocks: band cells, slot + active-face mask, by colour
         const int bw = p.band_width;
@@ -673,6 +674,7 @@ void dgs_phase(smg_ctx* c, int l, double* x, const double* b, int ph) {
         launch_dgs_pdelta(L.k, x, b, L.pd, ph - 2, c->st);
         launch_dgs_papply(L.k, x, L.pd, c->st);
     } else if (ph >= 10 && ph <= 17) {
+        launch_dgs_cb(L.k, b, c->st);
         launch_dgs_prev(L.k, x, b, 17 - ph, c->st);
     } else if (ph == 18 || ph == 19) {
         launch_dgs_vel(L.k, x, b, 19 - ph, c->st);
@@ -681,9 +683,12 @@ void dgs_phase(smg_ctx* c, int l, double* x, const double* b, int ph) {
     }
 }
 
-void symmetric_dgs(smg_ctx* c, int l, double* x, const double* b) {
+// cb_ready: L.k.cb already holds m_C^T b for this b (the V-cycle fills it once for
+// the pre- and post-smooth of a level visit)
+void symmetric_dgs(smg_ctx* c, int l, double* x, const double* b, bool cb_ready = false) {
     const int nph = (c->prm.flags & SMG_FLAG_SKIP_REVERSE_DGS) ? kDgsPhases / 2 : kDgsPhases;
     DevLevel& L = c->lv[l];
+    if (nph > kDgsPhases / 2 && !cb_ready) launch_dgs_cb(L.k, b, c->st);  // m_C^T b for the reverse steps
     if (!L.wave.empty()) {
         launch_dgs_wave(L.k, L.wave.data(), static_cast<int>(L.wave.size()), x, b, L.pd0, c->st);
         return;
@@ -703,14 +708,15 @@ void vanka_additive(smg_ctx* c, int l, double* x, const double* b) {
     launch_vanka_additive(L.k, x, b, L.va_cells, L.va_mask, L.va_n, L.ktab, L.va_d7, c->prm.omega, c->st);
 }
 
-void smooth(smg_ctx* c, int l, double* x, const double* b) {
+void smooth(smg_ctx* c, int l, double* x, const double* b, bool cb_ready = false) {
     DevLevel& L = c->lv[l];
     if (c->prm.vanka == 1) {  // Alg. 3 with additive Vanka on V1
         for (int k = 0; k < c->prm.nu; ++k) vanka_additive(c, l, x, b);
-        symmetric_dgs(c, l, x, b);
+        symmetric_dgs(c, l, x, b, cb_ready);
         for (int k = 0; k < c->prm.nu; ++k) vanka_additive(c, l, x, b);
         return;
     }
+    if (!cb_ready && (smooth_dsm_fits(L.k, L.sw_n) || smooth_smem_fits(L.k, L.sw_n))) launch_dgs_cb(L.k, b, c->st);
     if (smooth_dsm_fits(L.k, L.sw_n)) {
         const int nph = (c->prm.flags & SMG_FLAG_SKIP_REVERSE_DGS) ? kDgsPhases / 2 : kDgsPhases;
         launch_smooth_dsm(L.k, x, b, L.sw_cells, L.sw_mask, L.sw_n, L.ktab, c->prm.nu, nph, c->st, L.sw_merged);
@@ -723,7 +729,7 @@ void smooth(smg_ctx* c, int l, double* x, const double* b) {
         return;
     }
     vanka_sym_coop(c, l, x, b);
-    symmetric_dgs(c, l, x, b);
+    symmetric_dgs(c, l, x, b, cb_ready);
     vanka_sym_coop(c, l, x, b);
 }
 
@@ -735,7 +741,9 @@ void vcycle(smg_ctx* c, int l, const double* b, double* x) {
     DevLevel& L = c->lv[l];
     if (l == static_cast<int>(c->lv.size()) - 1) { coarse_solve(c, b, x); return; }
     CK(cudaMemsetAsync(x, 0, vlen(L) * sizeof(double), c->st));
-    smooth(c, l, x, b);
+    const bool cb = !(c->prm.flags & SMG_FLAG_SKIP_REVERSE_DGS);
+    if (cb) launch_dgs_cb(L.k, b, c->st);  // m_C^T b once for both smooths of this visit
+    smooth(c, l, x, b, cb);
     DevLevel& C = c->lv[l + 1];
     if (resrestrict_ok(L.k, C.k)) {
         launch_residual_restrict(L.k, C.k, x, b, C.b, c->st);  // b_c = R (b - L~ x), one pass
@@ -752,7 +760,7 @@ void vcycle(smg_ctx* c, int l, const double* b, double* x) {
         launch_axpy(C.x, C.wx, 1.0, vlen(C), c->st);
     }
     launch_prolong_add(L.k, C.k, C.x, x, c->st);
-    smooth(c, l, x, b);
+    smooth(c, l, x, b, cb);
 }
 
 // ---- SQMR, Alg. 4; b in c->rhs, x into c->xs ----
@@ -1012,6 +1020,7 @@ void dist_vanka_sym(smg_ctx* m, int l) {
 
 void dist_dgs_sym(smg_ctx* m, int l) {
     const int nph = (m->prm.flags & SMG_FLAG_SKIP_REVERSE_DGS) ? 10 : 20;
+    each(m, [&](smg_ctx* p) { launch_dgs_cb(p->lv[l].k, p->lv[l].b, p->st); });  // b halos are valid here
     for (int ph = 0; ph < nph; ++ph) {
         if (ph == 0 || ph == 1 || ph == 18 || ph == 19) {
             const int col = ph < 2 ? ph : 19 - ph;

@@ -185,36 +185,34 @@ __global__ void k_dgs_papply(LevelK L, double* __restrict__ X, const double* __r
 // Reverse (left-preconditioned) pressure phase: x_C += m_C^T (b - L~x) / d_p on
 // V2 cells of the parity colour (radius-2 gather; same-colour cells are never
 // face neighbours and never read each other's pressure: one pass is race-free).
+template <class AX>
+__device__ __forceinline__ double prev_value(const LevelK& L, AX X, int64_t i);
 __global__ void k_dgs_prev(LevelK L, double* __restrict__ X, const double* __restrict__ B, int colour) {
+    (void)B;
     Cell c;
     if (!thread_cell(L.g, c)) return;
     if (pcolour(L.g, c) != colour || band_cell(L, c.x, c.y, c.z)) return;
-    const Geom& g = L.g;
-    const int64_t fs = g.fs, i = c.i, sy = g.sy, sz = g.sz;
-    const double *U = X, *V = X + fs, *W = X + 2 * fs;
-    double* P = X + 3 * fs;
-    const double *BU = B, *BV = B + fs, *BW = B + 2 * fs, *BP = B + 3 * fs;
-    const double ruL = BU[i] - mom(L, U, P, i, 1);
-    const double ruR = BU[i + 1] - mom(L, U, P, i + 1, 1);
-    const double rvL = BV[i] - mom(L, V, P, i, sy);
-    const double rvR = BV[i + sy] - mom(L, V, P, i + sy, sy);
-    const double rwL = BW[i] - mom(L, W, P, i, sz);
-    const double rwR = BW[i + sz] - mom(L, W, P, i + sz, sz);
-    const double fl = ((ruR - ruL) + (rvR - rvL)) + (rwR - rwL);
-    const double rc = BP[i] - cont(L, U, V, W, P, i, L.gamma);
-    double s = BP[i - 1] - cont(L, U, V, W, P, i - 1, L.gamma);
-    s = s + (BP[i + 1] - cont(L, U, V, W, P, i + 1, L.gamma));
-    s = s + (BP[i - sy] - cont(L, U, V, W, P, i - sy, L.gamma));
-    s = s + (BP[i + sy] - cont(L, U, V, W, P, i + sy, L.gamma));
-    s = s + (BP[i - sz] - cont(L, U, V, W, P, i - sz, L.gamma));
-    s = s + (BP[i + sz] - cont(L, U, V, W, P, i + sz, L.gamma));
-    const double cj = fl * L.inv_h + L.eta_h2 * (6.0 * rc - s);
-    P[i] = P[i] + cj / L.dp;
+    X[3 * L.g.fs + c.i] = prev_value(L, X, c.i);
 }
 
-// --------------------------------------------------------------- Vanka ------
-// One colour phase, Jacobi within the colour: part 1 computes every block's
-// correction from the pre-phase state (slots [uL,uR,vL,vR,wL,wR,p]).
+// c_b = m_C^T b: the b part of the reverse pressure update, same operation order as
+// the L~x part in prev_value (faces right - left in x, y, z; 6 r_C - neighbours x-, x+, ...).
+__global__ void k_dgs_cb(LevelK L, const double* __restrict__ B, double* __restrict__ CB) {
+    pdl_wait();
+    Cell c;
+    if (!thread_cell(L.g, c)) return;
+    const Geom& g = L.g;
+    const int64_t fs = g.fs, sy = g.sy, sz = g.sz, i = c.i;
+    const double *BU = B, *BV = B + fs, *BW = B + 2 * fs, *BP = B + 3 * fs;
+    const double fl = ((BU[i + 1] - BU[i]) + (BV[i + sy] - BV[i])) + (BW[i + sz] - BW[i]);
+    double s = BP[i - 1] + BP[i + 1];
+    s = s + BP[i - sy];
+    s = s + BP[i + sy];
+    s = s + BP[i - sz];
+    s = s + BP[i + sz];
+    CB[i] = fl * L.inv_h + L.eta_h2 * (6.0 * BP[i] - s);
+}
+
 __global__ void k_vanka_delta(LevelK L, const double* __restrict__ X, const double* __restrict__ B,
                               const int32_t* __restrict__ cells, const uint8_t* __restrict__ masks, int n,
                               const double* __restrict__ ktab, double* __restrict__ delta) {
@@ -1130,33 +1128,34 @@ __device__ __forceinline__ void dgs_vel_cell(const LevelK& L, AX X, const double
     vel_store(L, X, vel_load(L, X, B, x, y, z, true));
 }
 
-// Reverse (left-preconditioned) pressure update of the cell at slot i: the new p_i.
+// Reverse (left-preconditioned) pressure update of the cell at slot i: the new p_i =
+// p_i + (c_b - m_i^T L~x) / d_p, with c_b = m_i^T b from L.cb (k_dgs_cb) and the
+// L~x part in the same operation order.  Reads only x around the cell (radius 2).
 template <class AX>
-__device__ __forceinline__ double prev_value(const LevelK& L, AX X, const double* __restrict__ B, int64_t i) {
+__device__ __forceinline__ double prev_value(const LevelK& L, AX X, int64_t i) {
     const Geom& g = L.g;
     const int64_t fs = g.fs, sy = g.sy, sz = g.sz;
     const auto U = X, V = X + fs, W = X + 2 * fs, P = X + 3 * fs;
-    const double *BU = B, *BV = B + fs, *BW = B + 2 * fs, *BP = B + 3 * fs;
-    const double ruL = BU[i] - mom(L, U, P, i, 1);
-    const double ruR = BU[i + 1] - mom(L, U, P, i + 1, 1);
-    const double rvL = BV[i] - mom(L, V, P, i, sy);
-    const double rvR = BV[i + sy] - mom(L, V, P, i + sy, sy);
-    const double rwL = BW[i] - mom(L, W, P, i, sz);
-    const double rwR = BW[i + sz] - mom(L, W, P, i + sz, sz);
-    const double fl = ((ruR - ruL) + (rvR - rvL)) + (rwR - rwL);
-    const double rc = BP[i] - cont(L, U, V, W, P, i, L.gamma);
-    double s = BP[i - 1] - cont(L, U, V, W, P, i - 1, L.gamma);
-    s = s + (BP[i + 1] - cont(L, U, V, W, P, i + 1, L.gamma));
-    s = s + (BP[i - sy] - cont(L, U, V, W, P, i - sy, L.gamma));
-    s = s + (BP[i + sy] - cont(L, U, V, W, P, i + sy, L.gamma));
-    s = s + (BP[i - sz] - cont(L, U, V, W, P, i - sz, L.gamma));
-    s = s + (BP[i + sz] - cont(L, U, V, W, P, i + sz, L.gamma));
-    const double cj = fl * L.inv_h + L.eta_h2 * (6.0 * rc - s);
-    return P[i] + cj / L.dp;
+    const double luL = mom(L, U, P, i, 1);
+    const double luR = mom(L, U, P, i + 1, 1);
+    const double lvL = mom(L, V, P, i, sy);
+    const double lvR = mom(L, V, P, i + sy, sy);
+    const double lwL = mom(L, W, P, i, sz);
+    const double lwR = mom(L, W, P, i + sz, sz);
+    const double fl = ((luR - luL) + (lvR - lvL)) + (lwR - lwL);
+    const double lc = cont(L, U, V, W, P, i, L.gamma);
+    double s = cont(L, U, V, W, P, i - 1, L.gamma) + cont(L, U, V, W, P, i + 1, L.gamma);
+    s = s + cont(L, U, V, W, P, i - sy, L.gamma);
+    s = s + cont(L, U, V, W, P, i + sy, L.gamma);
+    s = s + cont(L, U, V, W, P, i - sz, L.gamma);
+    s = s + cont(L, U, V, W, P, i + sz, L.gamma);
+    const double cl = fl * L.inv_h + L.eta_h2 * (6.0 * lc - s);
+    return P[i] + (L.cb[i] - cl) / L.dp;
 }
 template <class AX>
 __device__ __forceinline__ void dgs_prev_cell(const LevelK& L, AX X, const double* __restrict__ B, int64_t i) {
-    X[3 * L.g.fs + i] = prev_value(L, X, B, i);
+    (void)B;
+    X[3 * L.g.fs + i] = prev_value(L, X, i);
 }
 
 // cells of parity colour c: t -> (x,y,z) on the half-grid of that parity
@@ -2033,6 +2032,10 @@ void launch_dgs_pdelta(const LevelK& L, const double* x, const double* b, double
 }
 void launch_dgs_papply(const LevelK& L, double* x, const double* delta, cudaStream_t s) {
     k_dgs_papply<<<cell_grid(L.g), dim3(BX, BY), 0, s>>>(L, x, delta);
+    count();
+}
+void launch_dgs_cb(const LevelK& L, const double* b, cudaStream_t s) {
+    launch_k(k_dgs_cb, cell_grid(L.g), dim3(BX, BY), 0, s, L, b, L.cb);
     count();
 }
 void launch_dgs_prev(const LevelK& L, double* x, const double* b, int colour, cudaStream_t s) {

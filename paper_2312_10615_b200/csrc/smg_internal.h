@@ -67,6 +67,9 @@ struct LevelK {
     double dv;      // DGS diagonal, velocity: 6 eta / h^2
     double dp;      // DGS diagonal, pressure: -6 (1 + gamma eta) / h^2
     int bw;         // band width
+    // c_b = m_C^T b per cell (the b part of the reverse DGS pressure update, fixed while b
+    // is): launch_dgs_cb fills it before a sweep; prev steps then read L~x only
+    double* cb = nullptr;
 };
 
 // ---- stencil launchers (kernels.cu) ----
@@ -77,6 +80,8 @@ void launch_dgs_pdelta(const LevelK& L, const double* x, const double* b, double
                        cudaStream_t s);
 void launch_dgs_papply(const LevelK& L, double* x, const double* delta, cudaStream_t s);
 void launch_dgs_prev(const LevelK& L, double* x, const double* b, int colour, cudaStream_t s);
+// L.cb[C] = m_C^T b for every cell (reverse pressure phases need it; call when b changes).
+void launch_dgs_cb(const LevelK& L, const double* b, cudaStream_t s);
 void launch_vanka_delta(const LevelK& L, const double* x, const double* b, const int32_t* cells,
                         const uint8_t* masks, int ncells, const double* ktab, double* delta, cudaStream_t s);
 // amask (z-slabs, optional): per block, the slots this part owns (bit s = slot s, bit 6 = p).
