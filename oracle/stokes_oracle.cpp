@@ -598,10 +598,20 @@ static void vanka_colour(const Level& L, vec& x, const vec& b, int col) {
     });
 }
 
-// vanka_multiplicative_symmetric: colours 0..7 then 7..0.
+// vanka_multiplicative_symmetric: the 8 parity colours in
+// the order kVankaOrder, then exactly reversed (SPEC: "reverse multiplicative
+// sweep reverses both block order and color order").  The SPEC fixes only the
+// 2^d parity colouring, not the order of the colours (OD-2); this order puts
+// complementary parities (p, 7 - p) next to each other.  Two such colours never
+// touch each other's DOFs (every residual stencil reaches along one axis, so a
+// block reads DOFs of cells differing in at most two parities), hence each
+// adjacent pair commutes and a GPU may run it as ONE Jacobi phase with
+// bit-identical results: 8 dependent phases per symmetric sweep instead of 16.
+// Measured MG/SQMR convergence equals the 0..7 order.
+static const int kVankaOrder[8] = {0, 7, 1, 6, 2, 5, 3, 4};
 static void vanka_symmetric(const Level& L, vec& x, const vec& b) {
-    for (int c = 0; c < 8; ++c) vanka_colour(L, x, b, c);
-    for (int c = 7; c >= 0; --c) vanka_colour(L, x, b, c);
+    for (int c = 0; c < 8; ++c) vanka_colour(L, x, b, kVankaOrder[c]);
+    for (int c = 7; c >= 0; --c) vanka_colour(L, x, b, kVankaOrder[c]);
 }
 
 // vanka_additive (Eq. S_AV): r = b - L~x once; every block solves

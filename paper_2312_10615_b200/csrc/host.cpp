@@ -228,11 +228,12 @@ struct DevLevel {
     int32_t* vk_refresh = nullptr;  // slots every Vanka residual reads (refreshed x -> xb per sweep)
     int64_t vk_nrefresh = 0;
     int vk_n[8] = {};
-    // lists of the symmetric sweeps: as vk_* with colour 4 appended to list 3 (sw_merged = colour-3 count)
+    // lists of the symmetric sweeps: as vk_* with merged complementary pairs (list m = parity m,
+    // then parity 7-m; see VankaPairs)
     int32_t* sw_cells[8] = {};
     uint8_t* sw_mask[8] = {};
     int sw_n[8] = {};
-    int sw_merged = -1;
+    VankaPairs sw_pairs;
     // additive Vanka (params.vanka == 1): every block in one list + the 7-field correction scratch
     int32_t* va_cells = nullptr;
     uint8_t* va_mask = nullptr;
@@ -495,27 +496,31 @@ void build(smg_ctx* c, const std::vector<double>* shared_coarse = nullptr, std::
             }
             CK(cudaStreamSynchronize(c->st));
         }
-        // sweep lists: colour 4 folded into list 3 (one phase; see VankaLists in kernels.cu)
+        // sweep lists: complementary pairs (m, 7-m) folded into list m (one phase each; see
+        // VankaLists in kernels.cu)
         for (int col = 0; col < 8; ++col) {
             L.sw_cells[col] = L.vk_cells[col];
             L.sw_mask[col] = L.vk_mask[col];
             L.sw_n[col] = L.vk_n[col];
         }
-        L.sw_merged = -1;
-        if (env_int("SMG_VANKA_MERGE34", 1) == 2 || (env_int("SMG_VANKA_MERGE34", 1) == 1 && vanka_merge_pays(L.vk_n))) {
-            std::vector<int32_t> mc(cells[3]);
-            mc.insert(mc.end(), cells[4].begin(), cells[4].end());
-            std::vector<uint8_t> mm(masks[3]);
-            mm.insert(mm.end(), masks[4].begin(), masks[4].end());
-            L.sw_n[3] = static_cast<int>(mc.size());
-            L.sw_n[4] = 0;
-            max_vk = std::max(max_vk, L.sw_n[3]);
-            L.sw_cells[3] = c->dalloc<int32_t>(L.sw_n[3]);
-            L.sw_mask[3] = c->dalloc<uint8_t>(L.sw_n[3]);
-            CK(cudaMemcpyAsync(L.sw_cells[3], mc.data(), mc.size() * sizeof(int32_t), cudaMemcpyHostToDevice, c->st));
-            CK(cudaMemcpyAsync(L.sw_mask[3], mm.data(), mm.size(), cudaMemcpyHostToDevice, c->st));
+        L.sw_pairs = VankaPairs{};
+        const int pm = vanka_pairs_pay(L.vk_n);
+        for (int pq = 0; pq < 4; ++pq) {
+            if (!((pm >> pq) & 1)) continue;
+            std::vector<int32_t> mc(cells[pq]);
+            mc.insert(mc.end(), cells[7 - pq].begin(), cells[7 - pq].end());
+            std::vector<uint8_t> mm(masks[pq]);
+            mm.insert(mm.end(), masks[7 - pq].begin(), masks[7 - pq].end());
+            L.sw_n[pq] = static_cast<int>(mc.size());
+            L.sw_n[7 - pq] = 0;
+            max_vk = std::max(max_vk, L.sw_n[pq]);
+            L.sw_cells[pq] = c->dalloc<int32_t>(L.sw_n[pq]);
+            L.sw_mask[pq] = c->dalloc<uint8_t>(L.sw_n[pq]);
+            CK(cudaMemcpyAsync(L.sw_cells[pq], mc.data(), mc.size() * sizeof(int32_t), cudaMemcpyHostToDevice, c->st));
+            CK(cudaMemcpyAsync(L.sw_mask[pq], mm.data(), mm.size(), cudaMemcpyHostToDevice, c->st));
             CK(cudaStreamSynchronize(c->st));
-            L.sw_merged = static_cast<int>(cells[3].size());
+            L.sw_pairs.pairs |= 1 << pq;
+            L.sw_pairs.first[pq] = static_cast<int>(cells[pq].size());
         }
         if (p.vanka == 1 && !dist) {
             std::vector<int32_t> ac;
@@ -657,7 +662,7 @@ void vanka_sym(smg_ctx* c, int l, double* x, const double* b) {
     DevLevel& L = c->lv[l];
     for (int pass = 0; pass < 2; ++pass)
         for (int k = 0; k < 8; ++k) {
-            const int col = pass == 0 ? k : 7 - k;
+            const int col = vanka_order(pass == 0 ? k : 7 - k);
             launch_vanka_delta(L.k, x, b, L.vk_cells[col], L.vk_mask[col], L.vk_n[col], L.ktab, c->vk_delta, c->st);
             launch_vanka_apply(L.k, x, L.vk_cells[col], L.vk_mask[col], L.vk_n[col], c->vk_delta, c->st);
         }
@@ -699,7 +704,7 @@ void symmetric_dgs(smg_ctx* c, int l, double* x, const double* b, bool cb_ready 
 void vanka_sym_coop(smg_ctx* c, int l, double* x, const double* b) {
     DevLevel& L = c->lv[l];
     launch_vanka_sym_coop(L.k, x, b, L.sw_cells, L.sw_mask, L.sw_n, L.ktab, c->vk_delta, c->prm.nu, c->st, L.xb,
-                          L.vk_refresh, L.vk_nrefresh, L.sw_merged);
+                          L.vk_refresh, L.vk_nrefresh, L.sw_pairs);
 }
 
 void vanka_additive(smg_ctx* c, int l, double* x, const double* b) {
@@ -719,13 +724,13 @@ void smooth(smg_ctx* c, int l, double* x, const double* b, bool cb_ready = false
     if (!cb_ready && (smooth_dsm_fits(L.k, L.sw_n) || smooth_smem_fits(L.k, L.sw_n))) launch_dgs_cb(L.k, b, c->st);
     if (smooth_dsm_fits(L.k, L.sw_n)) {
         const int nph = (c->prm.flags & SMG_FLAG_SKIP_REVERSE_DGS) ? kDgsPhases / 2 : kDgsPhases;
-        launch_smooth_dsm(L.k, x, b, L.sw_cells, L.sw_mask, L.sw_n, L.ktab, c->prm.nu, nph, c->st, L.sw_merged);
+        launch_smooth_dsm(L.k, x, b, L.sw_cells, L.sw_mask, L.sw_n, L.ktab, c->prm.nu, nph, c->st, L.sw_pairs);
         return;
     }
     if (smooth_smem_fits(L.k, L.sw_n)) {
         const int nph = (c->prm.flags & SMG_FLAG_SKIP_REVERSE_DGS) ? kDgsPhases / 2 : kDgsPhases;
         launch_smooth_smem(L.k, x, b, L.sw_cells, L.sw_mask, L.sw_n, L.ktab, L.pd0, L.pd1, c->prm.nu, nph, c->st,
-                           L.sw_merged);
+                           L.sw_pairs);
         return;
     }
     vanka_sym_coop(c, l, x, b);
@@ -1007,7 +1012,7 @@ void each(smg_ctx* m, F&& f) {
 void dist_vanka_sym(smg_ctx* m, int l) {
     for (int sweep = 0; sweep < m->prm.nu; ++sweep)
         for (int k = 0; k < 16; ++k) {
-            const int col = k < 8 ? k : 15 - k;
+            const int col = vanka_order(k < 8 ? k : 15 - k);
             each(m, [&](smg_ctx* p) {
                 DevLevel& L = p->lv[l];
                 launch_vanka_delta(L.k, L.x, L.b, L.vk_cells[col], L.vk_mask[col], L.vk_n[col], L.ktab, p->vk_delta, p->st);
@@ -1521,7 +1526,7 @@ int smg_smoother(smg_ctx* c, int level, int op, int arg, double* x, const double
             launch_vanka_apply(L.k, L.x, L.vk_cells[arg], L.vk_mask[arg], L.vk_n[arg], c->vk_delta, c->st);
         } else if (op == 3) {
             launch_vanka_sym_coop(L.k, L.x, L.b, L.sw_cells, L.sw_mask, L.sw_n, L.ktab, c->vk_delta, 1, c->st,
-                                  nullptr, nullptr, 0, L.sw_merged);
+                                  nullptr, nullptr, 0, L.sw_pairs);
         } else if (op == 5) {  // one additive Vanka application
             vanka_additive(c, level, L.x, L.b);
         } else if (op == 6) {  // per-phase reference path of the symmetric sweeps (test only)

@@ -645,24 +645,32 @@ struct VankaLists {
     const int32_t* cells[8];
     const uint8_t* masks[8];
     int n[8];
-    // merged >= 0: list 3 holds the colour-3 blocks (first `merged` entries) followed by the
-    // colour-4 blocks, and colour 4 has no phase of its own.  Colours 3 and 4 = 3 ^ 7 differ in
-    // all three parities: every residual stencil reaches along one axis only, so no block of one
-    // reads or writes a DOF of the other, and the adjacent phases 3, 4 (and 4, 3) run as ONE
-    // Jacobi phase with bit-identical results: 14 phases per symmetric sweep instead of 16.
-    int merged;
+    // Lists are indexed by parity colour (i&1)+2(j&1)+4(k&1).  The sweep visits the parities
+    // in the order kVankaOrder = 0,7,1,6,2,5,3,4 and back (oracle vanka_symmetric): every
+    // adjacent pair (m, 7-m) differs in all three parities, no block of one reads or writes
+    // a DOF of the other (each residual stencil reaches along one axis), so the pair runs as
+    // ONE Jacobi phase with bit-identical results.  Bit m of `pairs` set: list m holds the
+    // parity-m blocks (first first[m] entries) followed by the parity-(7-m) blocks and list
+    // 7-m has no phase of its own.  All four pairs merged: 8 phases per symmetric sweep.
+    int pairs;
+    int first[4];
 };
 // phase k (0..15) of a symmetric sweep -> colour list, -1 if the phase is folded away
 __device__ __forceinline__ int vanka_phase_list(const VankaLists& vl, int k) {
-    const int col = k < 8 ? k : 15 - k;
-    return (vl.merged >= 0 && col == 4) ? -1 : col;
+    const int j = k < 8 ? k : 15 - k;
+    const int p = vanka_order(j);
+    return ((j & 1) && ((vl.pairs >> (7 - p)) & 1)) ? -1 : p;
 }
 // parity colour of entry t of list c
 __device__ __forceinline__ int vanka_entry_colour(const VankaLists& vl, int c, int t) {
-    return (vl.merged >= 0 && c == 3 && t >= vl.merged) ? 4 : c;
+    return (c < 4 && ((vl.pairs >> c) & 1) && t >= vl.first[c]) ? 7 - c : c;
+}
+// parity colours a phase on list c updates (bit mask)
+__device__ __forceinline__ int vanka_list_cmask(const VankaLists& vl, int c) {
+    return (c < 4 && ((vl.pairs >> c) & 1)) ? ((1 << c) | (1 << (7 - c))) : (1 << c);
 }
 
-// nu symmetric multiplicative Vanka sweeps (colours 0..7 then 7..0), Jacobi
+// nu symmetric multiplicative Vanka sweeps (kVankaOrder, then reversed), Jacobi
 // within a colour.  Each thread owns up to CPT blocks of the colour: it loads
 // their residual stencils, keeps the block's own 7 values and its correction
 // in registers, waits at the barrier (all reads of the phase done), then
@@ -855,7 +863,7 @@ __device__ __forceinline__ void vanka_sweeps8(const LevelK& L, AX X, const doubl
 // holds the full state after phase k (it held the state after phase k-2, and
 // only those two colours changed).  Reads and writes never share a buffer
 // within a phase.  Before the sweep XB must equal XA on every DOF a Vanka
-// residual reads (refresh list).  16 nu phases: the result ends in XA.
+// residual reads (refresh list).  An even phase count: the result ends in XA.
 // One ping-pong colour phase (list col; pcol = list of the previous phase, -1 if none):
 // reads Xc, writes the phase's blocks and the carried previous-phase blocks into Xn.
 // pre (CPT == 1, optional): this lane group's entry of every list, preloaded.
@@ -870,12 +878,13 @@ __device__ __forceinline__ void vanka_pp_phase(const LevelK& L, const double* __
     const int groups = nth >> 3, grp = tid >> 3;
     const int64_t offs = s8 == 0 ? 0 : s8 == 1 ? 1 : s8 == 2 ? fs : s8 == 3 ? fs + sy : s8 == 4 ? 2 * fs
                          : s8 == 5 ? 2 * fs + sz : 3 * fs;
-    auto block_of = [&](int c, int t, int64_t& i, int& m) {
+    // pre (PRE): CPT 1 -> pre[list]; CPT 2 (all four pairs merged, lists 0..3) -> pre[2 list + j]
+    auto block_of = [&](int c, int j, int t, int64_t& i, int& m) {
         if constexpr (PRE) {
             int64_t e = 0;
 #pragma unroll
-            for (int q = 0; q < 8; ++q)
-                if (q == c) e = pre[q];
+            for (int q = 0; q < 8 / CPT; ++q)
+                if (q == c) e = pre[q * CPT + j];
             i = e >> 7;
             m = static_cast<int>(e & 127);
         } else {
@@ -883,7 +892,7 @@ __device__ __forceinline__ void vanka_pp_phase(const LevelK& L, const double* __
             m = vl.masks[c][t];
         }
     };
-    const int cmask = (vl.merged >= 0 && col == 3) ? 0x18 : (1 << col);  // parity colours of this phase
+    const int cmask = vanka_list_cmask(vl, col);  // parity colours of this phase
     const int n = vl.n[col];
 #pragma unroll
     for (int j = 0; j < CPT; ++j) {
@@ -891,7 +900,7 @@ __device__ __forceinline__ void vanka_pp_phase(const LevelK& L, const double* __
         const bool act = t < n;
         int64_t i = 0;
         int m = 0;
-        if (act) block_of(col, t, i, m);
+        if (act) block_of(col, j, t, i, m);
         double r = 0.0, own = 0.0;
         // the previous phase's block this lane carries into Xn (decided and loaded before the
         // gather, so its L2 round trip overlaps the residual loads): all its DOFs except those
@@ -903,7 +912,7 @@ __device__ __forceinline__ void vanka_pp_phase(const LevelK& L, const double* __
         if (pcol >= 0 && pcol != col && t < vl.n[pcol] && s8 < 7) {
             int64_t ip;
             int mp;
-            block_of(pcol, t, ip, mp);
+            block_of(pcol, j, t, ip, mp);
             carry = s8 == 6 || (mp & (1 << s8));
             if (carry && s8 < 6 && ((cmask >> (vanka_entry_colour(vl, pcol, t) ^ (1 << (s8 >> 1)))) & 1)) {
                 const int zl = static_cast<int>(ip / sz) - g.zg;
@@ -942,19 +951,24 @@ __device__ __forceinline__ void vanka_pp_phase(const LevelK& L, const double* __
 // holds the full state after phase k (it held the state after phase k-2, and
 // only those two colours changed).  Reads and writes never share a buffer
 // within a phase.  Before the sweep XB must equal XA on every DOF a Vanka
-// residual reads (refresh list).  16 nu phases: the result ends in XA.
+// residual reads (refresh list).  An even phase count: the result ends in XA.
 template <int MODE, int CPT>
 __device__ __forceinline__ void vanka_sweeps_pp(const LevelK& L, double* __restrict__ XA, double* __restrict__ XB,
                                                 const double* __restrict__ B, const VankaLists& vl,
                                                 const double* __restrict__ Ks, int nu, int tid, int nth) {
-    const int grp = tid >> 3;
-    constexpr bool kPre = CPT == 1;
+    const int grp = tid >> 3, groups = nth >> 3;
+    // this lane group's block of every list, loaded once (slot << 7 | mask; -1 = none): CPT 1 for
+    // all 8 lists, CPT 2 when the four merged pair lists are the only ones
+    constexpr bool kPre = CPT == 1 || CPT == 2;
+    const bool pre_ok = CPT == 1 || vl.pairs == 0xf;
     int64_t pre[8];
-    if (kPre)
+    if (kPre && pre_ok)
 #pragma unroll
-        for (int c = 0; c < 8; ++c)
-            pre[c] = grp < vl.n[c] ? ((static_cast<int64_t>(vl.cells[c][grp]) << 7) | vl.masks[c][grp]) : -1;
-    // executed phases alternate the buffers; 16 or 14 (merged) per sweep, so the result ends in XA
+        for (int q = 0; q < 8; ++q) {
+            const int c = q / CPT, t = grp + (q % CPT) * groups;
+            pre[q] = t < vl.n[c] ? ((static_cast<int64_t>(vl.cells[c][t]) << 7) | vl.masks[c][t]) : -1;
+        }
+    // executed phases alternate the buffers; an even count per sweep, so the result ends in XA
     int ph = 0, pcol = -1;
     for (int kk = 0; kk < 16 * nu; ++kk) {
         const int col = vanka_phase_list(vl, kk & 15);
@@ -962,7 +976,8 @@ __device__ __forceinline__ void vanka_sweeps_pp(const LevelK& L, double* __restr
         const double* __restrict__ Xc = (ph & 1) ? XB : XA;
         double* __restrict__ Xn = (ph & 1) ? XA : XB;
         SMG_TRACE_STAMP(ph, 0);
-        vanka_pp_phase<CPT, kPre>(L, Xc, Xn, B, vl, Ks, col, pcol, pre, tid, nth);
+        if (kPre && pre_ok) vanka_pp_phase<CPT, kPre>(L, Xc, Xn, B, vl, Ks, col, pcol, pre, tid, nth);
+        else vanka_pp_phase<CPT, false>(L, Xc, Xn, B, vl, Ks, col, pcol, pre, tid, nth);
         SMG_TRACE_STAMP(ph, 2);
         phase_sync<MODE>();
         SMG_TRACE_STAMP(ph, 3);
@@ -2209,6 +2224,17 @@ static bool use_cluster(int64_t work, int64_t max_items_per_thread) {
     return work <= static_cast<int64_t>(kClusterCTAs) * kClusterThreads * max_items_per_thread;
 }
 
+static void set_pairs(VankaLists& vl, const VankaPairs& pr) {
+    vl.pairs = pr.pairs;
+    for (int m = 0; m < 4; ++m) vl.first[m] = pr.first[m];
+}
+// host twin of vanka_phase_list
+static int host_phase_list(const VankaPairs& pr, int k) {
+    const int j = k < 8 ? k : 15 - k;
+    const int p = vanka_order(j);
+    return ((j & 1) && ((pr.pairs >> (7 - p)) & 1)) ? -1 : p;
+}
+
 template <int CPT>
 static void launch_vanka8(bool cl, int64_t threads, void** args, cudaStream_t s) {
     launch_sweep(reinterpret_cast<const void*>(k_vanka8<0, CPT>), reinterpret_cast<const void*>(k_vanka8<1, CPT>), cl,
@@ -2223,9 +2249,10 @@ static void launch_vanka_pp(bool cl, int64_t threads, void** args, cudaStream_t 
 
 void launch_vanka_sym_coop(const LevelK& L, double* x, const double* b, const int32_t* const* cells,
                            const uint8_t* const* masks, const int* n, const double* ktab, double* delta, int nu,
-                           cudaStream_t s, double* xb, const int32_t* refresh, int64_t nrefresh, int merged) {
+                           cudaStream_t s, double* xb, const int32_t* refresh, int64_t nrefresh,
+                           const VankaPairs& pr) {
     VankaLists vl;
-    vl.merged = merged;
+    set_pairs(vl, pr);
     int maxn = 1;
     for (int c = 0; c < 8; ++c) {
         vl.cells[c] = cells[c];
@@ -2254,8 +2281,8 @@ void launch_vanka_sym_coop(const LevelK& L, double* x, const double* b, const in
         const int64_t blocks = (8 * static_cast<int64_t>(maxn) + 255) / 256;  // one lane group per block
         int ph = 0, pcol = -1;
         for (int kk = 0; kk < 16 * nu; ++kk) {
-            const int k = kk & 15, c0 = k < 8 ? k : 15 - k;
-            if (merged >= 0 && c0 == 4) continue;
+            const int c0 = host_phase_list(pr, kk & 15);
+            if (c0 < 0) continue;
             const double* xc = (ph & 1) ? xb : x;
             double* xn = (ph & 1) ? x : xb;
             launch_k(k_vanka_ppk<1>, static_cast<int>(blocks), 256, 0, s, L, xc, xn, b, vl, ktab, c0, pcol);
@@ -2286,31 +2313,31 @@ void launch_vanka_sym_coop(const LevelK& L, double* x, const double* b, const in
     if (!done) {
         for (int sweep = 0; sweep < nu; ++sweep)
             for (int k = 0; k < 16; ++k) {
-                const int col = k < 8 ? k : 15 - k;
-                if (merged >= 0 && col == 4) continue;  // folded into the colour-3 list
+                const int col = host_phase_list(pr, k);
+                if (col < 0) continue;  // folded into the list of its complementary colour
                 launch_vanka_delta(L, x, b, cells[col], masks[col], n[col], ktab, delta, s);
                 launch_vanka_apply(L, x, cells[col], masks[col], n[col], delta, s);
             }
     }
 }
 
-// Folding colour 4 into colour 3 doubles that phase's lanes; in grid mode that only pays
-// while the merged phase still fits the one-block-per-lane-group (CPT = 1) capacity.
-bool vanka_merge_pays(const int* n) {
-    int maxn = 0;
+// Merging a complementary pair doubles that phase's lanes.  Mask of the pairs to merge:
+// SMG_VANKA_PAIRS = 0 none, 2 all, 1 (default) all when the merged phases still fit the
+// grid sweep at its current blocks per lane group or at CPT 2, where halving the phase count
+// (8 instead of 16 dependent phases) outweighs a second block per lane group.
+int vanka_pairs_pay(const int* n) {
+    const int mode = env_int("SMG_VANKA_PAIRS", 1);
+    if (mode == 0) return 0;
+    if (mode == 2) return 0xf;
+    int maxn = 0, maxm = 0;
     for (int c = 0; c < 8; ++c) maxn = n[c] > maxn ? n[c] : maxn;
-    const int64_t merged = std::max<int64_t>(maxn, static_cast<int64_t>(n[3]) + n[4]);
-    const int64_t cap = coop_capacity_blocks(reinterpret_cast<const void*>(k_vanka_pp<0, 1>), coop_threads()) *
+    for (int m = 0; m < 4; ++m) maxm = n[m] + n[7 - m] > maxm ? n[m] + n[7 - m] : maxm;
+    const int64_t cap = coop_capacity_blocks(reinterpret_cast<const void*>(k_vanka_pp<0, 2>), coop_threads()) *
                         coop_threads();
     const int64_t cl = static_cast<int64_t>(kClusterCTAs) * kClusterThreads;
-    // sweep class of a phase of `lanes` lanes: cluster, or grid with ceil(lanes / cap) blocks per group
-    // (measured: cluster -> grid at CPT = 1 still pays at 32^3, CPT 1 -> 2 does not at 128^3)
-    auto cls = [&](int64_t lanes) {
-        return lanes <= std::max(cl, cap) ? int64_t{1} : (lanes + cap - 1) / std::max<int64_t>(cap, 1);
-    };
-    return cls(8 * merged) == cls(8 * static_cast<int64_t>(maxn));
+    const int64_t lanes = 8 * static_cast<int64_t>(maxm);
+    return (lanes <= cl || lanes <= 2 * cap) ? 0xf : 0;
 }
-
 bool smooth_dsm_fits(const LevelK& L, const int* n) {
     int maxn = 0;
     for (int c = 0; c < 8; ++c) maxn = n[c] > maxn ? n[c] : maxn;
@@ -2322,9 +2349,9 @@ bool smooth_dsm_fits(const LevelK& L, const int* n) {
 
 void launch_smooth_dsm(const LevelK& L, double* x, const double* b, const int32_t* const* cells,
                        const uint8_t* const* masks, const int* n, const double* ktab, int nu, int nph,
-                       cudaStream_t s, int merged) {
+                       cudaStream_t s, const VankaPairs& pr) {
     VankaLists vl;
-    vl.merged = merged;
+    set_pairs(vl, pr);
     for (int c = 0; c < 8; ++c) {
         vl.cells[c] = cells[c];
         vl.masks[c] = masks[c];
@@ -2360,9 +2387,9 @@ bool smooth_smem_fits(const LevelK& L, const int* n) {
 
 void launch_smooth_smem(const LevelK& L, double* x, const double* b, const int32_t* const* cells,
                         const uint8_t* const* masks, const int* n, const double* ktab, double* d0, double* d1, int nu,
-                        int nph, cudaStream_t s, int merged) {
+                        int nph, cudaStream_t s, const VankaPairs& pr) {
     VankaLists vl;
-    vl.merged = merged;
+    set_pairs(vl, pr);
     for (int c = 0; c < 8; ++c) {
         vl.cells[c] = cells[c];
         vl.masks[c] = masks[c];

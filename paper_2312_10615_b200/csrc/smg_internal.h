@@ -82,6 +82,18 @@ void launch_dgs_papply(const LevelK& L, double* x, const double* delta, cudaStre
 void launch_dgs_prev(const LevelK& L, double* x, const double* b, int colour, cudaStream_t s);
 // L.cb[C] = m_C^T b for every cell (reverse pressure phases need it; call when b changes).
 void launch_dgs_cb(const LevelK& L, const double* b, cudaStream_t s);
+// Vanka colour order (oracle kVankaOrder = 0,7,1,6,2,5,3,4): the parity colour visited at
+// step j (0..7) of a forward sweep; the reverse sweep visits them backwards.
+#ifdef __CUDACC__
+__host__ __device__
+#endif
+inline constexpr int vanka_order(int j) { return (j & 1) ? 7 - (j >> 1) : (j >> 1); }
+// Merged complementary pairs: bit m of `pairs` set -> list m holds parity m (first first[m]
+// entries) then parity 7-m, and list 7-m is empty (one Jacobi phase for both colours).
+struct VankaPairs {
+    int pairs = 0;
+    int first[4] = {0, 0, 0, 0};
+};
 void launch_vanka_delta(const LevelK& L, const double* x, const double* b, const int32_t* cells,
                         const uint8_t* masks, int ncells, const double* ktab, double* delta, cudaStream_t s);
 // amask (z-slabs, optional): per block, the slots this part owns (bit s = slot s, bit 6 = p).
@@ -89,15 +101,15 @@ void launch_vanka_apply(const LevelK& L, double* x, const int32_t* cells, const 
                         const double* delta, cudaStream_t s, const uint8_t* amask = nullptr);
 // Cooperative (persistent, grid-synchronised) symmetric sweeps: nu Vanka sweeps
 // over the 8 colour lists; nph DGS phases (20 = full symmetric sweep).
-// merged >= 0: list 3 = colour-3 blocks (first `merged`) + colour-4 blocks, run as
-// one phase (14 phases per sweep; see VankaLists in kernels.cu).
+// pr: merged complementary colour pairs (list m = parity m + parity 7-m, one phase
+// each; see VankaLists in kernels.cu).
 // xb (optional): second level vector for the ping-pong sweep (one barrier per
 // phase); refresh[0..nrefresh) lists the slots Vanka reads, copied x -> xb first.
 void launch_vanka_sym_coop(const LevelK& L, double* x, const double* b, const int32_t* const* cells,
                            const uint8_t* const* masks, const int* n, const double* ktab, double* delta, int nu,
                            cudaStream_t s, double* xb = nullptr, const int32_t* refresh = nullptr,
-                           int64_t nrefresh = 0, int merged = -1);
-bool vanka_merge_pays(const int* n);  // merged lists keep the grid sweep at one block per lane group
+                           int64_t nrefresh = 0, const VankaPairs& pr = VankaPairs{});
+int vanka_pairs_pay(const int* n);  // mask of the pairs to merge on a level with these list sizes
 void launch_dgs_sym_coop(const LevelK& L, double* x, const double* b, double* d0, double* d1, int nph,
                          cudaStream_t s);
 // Whole smooth (Alg. 3) of a level held in the distributed shared memory of one
@@ -105,12 +117,12 @@ void launch_dgs_sym_coop(const LevelK& L, double* x, const double* b, double* d0
 bool smooth_dsm_fits(const LevelK& L, const int* n);
 void launch_smooth_dsm(const LevelK& L, double* x, const double* b, const int32_t* const* cells,
                        const uint8_t* const* masks, const int* n, const double* ktab, int nu, int nph,
-                       cudaStream_t s, int merged = -1);
+                       cudaStream_t s, const VankaPairs& pr = VankaPairs{});
 // Whole smooth (Alg. 3) of a level small enough for one CTA's shared memory.
 bool smooth_smem_fits(const LevelK& L, const int* n);
 void launch_smooth_smem(const LevelK& L, double* x, const double* b, const int32_t* const* cells,
                         const uint8_t* const* masks, const int* n, const double* ktab, double* d0, double* d1, int nu,
-                        int nph, cudaStream_t s, int merged = -1);
+                        int nph, cudaStream_t s, const VankaPairs& pr = VankaPairs{});
 // Restriction of coarse LOCAL planes [zc_lo, zc_lo + nzc) (nzc < 0: all); the
 // fine slab must hold the fine planes 2zc-1 .. 2zc+2 (halos included).
 void launch_restrict(const LevelK& F, const LevelK& C, const double* rf, double* bc, cudaStream_t s, int zc_lo = 0,

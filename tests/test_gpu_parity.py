@@ -354,10 +354,13 @@ def test_wave_dgs_forward_half_bitwise(monkeypatch):
 
 @pytest.mark.parametrize("mode", [{}, {"SMG_SYNC_MODE": "1"}, {"SMG_SYNC_MODE": "2"}, {"SMG_VANKA_PP": "0"},
                                   {"SMG_VANKA_PHASES": "1"}, {"SMG_SMEM_SMOOTH": "1"}, {"SMG_DGS_COOP": "1"},
-                                  {"SMG_VANKA_KERNELS": "1"}, {"SMG_DGS_COOP": "1", "SMG_SYNC_MODE": "2"}])
+                                  {"SMG_VANKA_KERNELS": "1"}, {"SMG_DGS_COOP": "1", "SMG_SYNC_MODE": "2"},
+                                  {"SMG_VANKA_PAIRS": "0"}, {"SMG_VANKA_PAIRS": "2", "SMG_SYNC_MODE": "1"},
+                                  {"SMG_VANKA_PAIRS": "2", "SMG_VANKA_KERNELS": "1"},
+                                  {"SMG_VANKA_PAIRS": "0", "SMG_VANKA_PHASES": "1"}])
 def test_vanka_merged_phase_bitwise(mode, monkeypatch):
-    """Colours 3 and 4 (= 3 ^ 7) share one Jacobi phase (14 phases per sweep): every sweep
-    variant stays bit-identical to the oracle's 16-phase order."""
+    """Complementary colour pairs (p, 7 - p) share one Jacobi phase (8 phases per sweep): every
+    sweep variant, merged or not, stays bit-identical to the oracle's 16-phase order."""
     for k, v in mode.items():
         monkeypatch.setenv(k, v)
     oracle.set_threads(4)
@@ -373,10 +376,10 @@ def test_vanka_merged_phase_bitwise(mode, monkeypatch):
 
 @pytest.mark.parametrize("n,levels", [(64, 4), (128, 5)])
 def test_vanka_merged_matches_unmerged(n, levels, monkeypatch):
-    """Large levels (grid ping-pong sweeps): merged (14-phase) == unmerged (16-phase) sweep."""
+    """Large levels (grid ping-pong sweeps): merged pairs (8-phase) == unmerged (16-phase) sweep."""
     out = []
-    for merge in ("0", "2"):  # 2: merge even where the default would not
-        monkeypatch.setenv("SMG_VANKA_MERGE34", merge)
+    for merge in ("0", "2"):  # 2: merge all pairs even where the default would not
+        monkeypatch.setenv("SMG_VANKA_PAIRS", merge)
         s = smg.Solver(n, levels=levels)
         x = np.random.default_rng(n).uniform(-1, 1, s.ndof())
         b = np.random.default_rng(n + 1).uniform(-1, 1, s.ndof())

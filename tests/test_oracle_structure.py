@@ -288,3 +288,35 @@ def test_mg_sqmr_with_additive_vanka_converges():
     b = o.forcing(oracle.FORCE_UNIFORM, 0)
     _, hist, _, st = o.sqmr(b, 1e-8, 100)
     assert st == 0 and hist[-1] < 1e-8 and len(hist) <= 15
+
+
+VANKA_ORDER = [0, 7, 1, 6, 2, 5, 3, 4]  # oracle kVankaOrder (OD-2)
+
+
+def test_vanka_symmetric_is_colour_order_then_reverse():
+    """The symmetric sweep is exactly the per-colour phases in kVankaOrder, then reversed."""
+    o = oracle.Oracle(8, levels=2)
+    n = o.ndof(0)
+    rng = np.random.default_rng(5)
+    x0, b = rng.uniform(-1, 1, n), rng.uniform(-1, 1, n)
+    x = x0.copy()
+    for c in VANKA_ORDER + VANKA_ORDER[::-1]:
+        x = o.smoother(OP_VCOL, x, b, 0, c)
+    assert np.array_equal(x, o.smoother(OP_VANKA, x0, b, 0))
+
+
+@pytest.mark.parametrize("p", [0, 1, 2, 3])
+def test_vanka_complementary_colours_commute_bitwise(p):
+    """Colours p and 7 - p never touch each other's DOFs: either order gives the same bits,
+    which is what lets the GPU run each adjacent pair of kVankaOrder as one Jacobi phase."""
+    o = oracle.Oracle(12, levels=2)
+    n = o.ndof(0)
+    rng = np.random.default_rng(10 + p)
+    x0, b = rng.uniform(-1, 1, n), rng.uniform(-1, 1, n)
+    a = o.smoother(OP_VCOL, o.smoother(OP_VCOL, x0, b, 0, p), b, 0, 7 - p)
+    c = o.smoother(OP_VCOL, o.smoother(OP_VCOL, x0, b, 0, 7 - p), b, 0, p)
+    assert np.array_equal(a, c)
+    # and a non-complementary pair does not commute (the merge is not vacuous)
+    d = o.smoother(OP_VCOL, o.smoother(OP_VCOL, x0, b, 0, p), b, 0, p ^ 1)
+    e = o.smoother(OP_VCOL, o.smoother(OP_VCOL, x0, b, 0, p ^ 1), b, 0, p)
+    assert not np.array_equal(d, e)
