@@ -1526,7 +1526,7 @@ int smg_smoother(smg_ctx* c, int level, int op, int arg, double* x, const double
             launch_vanka_apply(L.k, L.x, L.vk_cells[arg], L.vk_mask[arg], L.vk_n[arg], c->vk_delta, c->st);
         } else if (op == 3) {
             launch_vanka_sym_coop(L.k, L.x, L.b, L.sw_cells, L.sw_mask, L.sw_n, L.ktab, c->vk_delta, 1, c->st,
-                                  nullptr, nullptr, 0, L.sw_pairs);
+                                  L.xb, L.vk_refresh, L.vk_nrefresh, L.sw_pairs);
         } else if (op == 5) {  // one additive Vanka application
             vanka_additive(c, level, L.x, L.b);
         } else if (op == 6) {  // per-phase reference path of the symmetric sweeps (test only)

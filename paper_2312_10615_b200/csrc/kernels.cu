@@ -2272,12 +2272,18 @@ void launch_vanka_sym_coop(const LevelK& L, double* x, const double* b, const in
         const int64_t threads = cl ? cl_threads : coop_capacity_blocks(fn, coop_threads()) * coop_threads();
         return threads * cpt >= lanes;
     };
-    if (xb && env_int("SMG_VANKA_KERNELS", 0)) {  // ping-pong, one launch per phase
-        if (nrefresh > 0) {
-            const int64_t blocks = (nrefresh + 255) / 256;
-            launch_k(k_refresh, static_cast<int>(blocks < 4096 ? blocks : 4096), 256, 0, s, refresh, nrefresh, x, xb);
-            count();
-        }
+    auto refresh_xb = [&] {
+        if (nrefresh <= 0) return;
+        const int64_t blocks = (nrefresh + 255) / 256;
+        launch_k(k_refresh, static_cast<int>(blocks < 4096 ? blocks : 4096), 256, 0, s, refresh, nrefresh, x, xb);
+        count();
+    };
+    // ping-pong, one launch per phase: forced (SMG_VANKA_KERNELS=1), or on levels whose phases
+    // fit none of the persistent sweeps below (there a kernel boundary per phase is cheap next
+    // to the phase's work; SMG_VANKA_KERNELS=0 falls back to per-phase delta/apply launches)
+    const int vk_kernels = env_int("SMG_VANKA_KERNELS", -1);
+    auto ppk = [&] {
+        refresh_xb();
         const int64_t blocks = (8 * static_cast<int64_t>(maxn) + 255) / 256;  // one lane group per block
         int ph = 0, pcol = -1;
         for (int kk = 0; kk < 16 * nu; ++kk) {
@@ -2290,25 +2296,34 @@ void launch_vanka_sym_coop(const LevelK& L, double* x, const double* b, const in
             pcol = c0;
             ++ph;
         }
-        return;
-    }
-    bool done = !env_int("SMG_VANKA_PHASES", 0);  // 1: per-phase delta/apply launches (tests)
-    if (done && xb && !cl && env_int("SMG_VANKA_PP", 1)) {  // ping-pong (grid mode): one barrier per phase
-        if (nrefresh > 0) {
-            const int64_t blocks = (nrefresh + 255) / 256;
-            launch_k(k_refresh, static_cast<int>(blocks < 4096 ? blocks : 4096), 256, 0, s, refresh, nrefresh, x, xb);
-            count();
-        }
+    };
+    if (xb && vk_kernels == 1) { ppk(); return; }
+    const bool phases = env_int("SMG_VANKA_PHASES", 0) != 0;  // 1: per-phase delta/apply launches (tests)
+    if (!phases && xb && !cl && env_int("SMG_VANKA_PP", 1)) {  // ping-pong (grid mode): one barrier per phase
         void* pargs[] = {args[0], &x, &xb, args[2], args[3], args[4], args[5]};
-        if (fits(reinterpret_cast<const void*>(k_vanka_pp<0, 1>), 1)) { launch_vanka_pp<1>(cl, lanes, pargs, s); return; }
-        if (fits(reinterpret_cast<const void*>(k_vanka_pp<0, 2>), 2)) { launch_vanka_pp<2>(cl, (lanes + 1) / 2, pargs, s); return; }
-        if (fits(reinterpret_cast<const void*>(k_vanka_pp<0, 4>), 4)) { launch_vanka_pp<4>(cl, (lanes + 3) / 4, pargs, s); return; }
+        if (fits(reinterpret_cast<const void*>(k_vanka_pp<0, 1>), 1)) {
+            refresh_xb();
+            launch_vanka_pp<1>(cl, lanes, pargs, s);
+            return;
+        }
+        if (fits(reinterpret_cast<const void*>(k_vanka_pp<0, 2>), 2)) {
+            refresh_xb();
+            launch_vanka_pp<2>(cl, (lanes + 1) / 2, pargs, s);
+            return;
+        }
+        if (fits(reinterpret_cast<const void*>(k_vanka_pp<0, 4>), 4)) {
+            refresh_xb();
+            launch_vanka_pp<4>(cl, (lanes + 3) / 4, pargs, s);
+            return;
+        }
     }
+    bool done = !phases;
     if (!done) {
     } else if (fits(reinterpret_cast<const void*>(k_vanka8<0, 1>), 1)) launch_vanka8<1>(cl, lanes, args, s);
     else if (fits(reinterpret_cast<const void*>(k_vanka8<0, 2>), 2)) launch_vanka8<2>(cl, (lanes + 1) / 2, args, s);
     else if (fits(reinterpret_cast<const void*>(k_vanka8<0, 4>), 4)) launch_vanka8<4>(cl, (lanes + 3) / 4, args, s);
     else if (fits(reinterpret_cast<const void*>(k_vanka8<0, 8>), 8)) launch_vanka8<8>(cl, (lanes + 7) / 8, args, s);
+    else if (xb && vk_kernels != 0) { ppk(); return; }
     else done = false;
     if (!done) {
         for (int sweep = 0; sweep < nu; ++sweep)
@@ -2321,10 +2336,11 @@ void launch_vanka_sym_coop(const LevelK& L, double* x, const double* b, const in
     }
 }
 
-// Merging a complementary pair doubles that phase's lanes.  Mask of the pairs to merge:
-// SMG_VANKA_PAIRS = 0 none, 2 all, 1 (default) all when the merged phases still fit the
-// grid sweep at its current blocks per lane group or at CPT 2, where halving the phase count
-// (8 instead of 16 dependent phases) outweighs a second block per lane group.
+// Merging a complementary pair halves the dependent phases and doubles each phase's lanes.
+// Mask of the pairs to merge: SMG_VANKA_PAIRS = 0 none, 2 all, 1 (default) all unless the
+// merged phases would leave the persistent ping-pong sweep (> 2 blocks per lane group) while
+// the unmerged ones still fit it at 1 block per lane group.  Levels beyond the persistent
+// sweep run one kernel per phase, where merging always pays (half the launches, same work).
 int vanka_pairs_pay(const int* n) {
     const int mode = env_int("SMG_VANKA_PAIRS", 1);
     if (mode == 0) return 0;
@@ -2335,8 +2351,10 @@ int vanka_pairs_pay(const int* n) {
     const int64_t cap = coop_capacity_blocks(reinterpret_cast<const void*>(k_vanka_pp<0, 2>), coop_threads()) *
                         coop_threads();
     const int64_t cl = static_cast<int64_t>(kClusterCTAs) * kClusterThreads;
-    const int64_t lanes = 8 * static_cast<int64_t>(maxm);
-    return (lanes <= cl || lanes <= 2 * cap) ? 0xf : 0;
+    const int64_t lm = 8 * static_cast<int64_t>(maxm), lu = 8 * static_cast<int64_t>(maxn);
+    const bool merged_fits = lm <= cl || lm <= 2 * cap;
+    const bool unmerged_cpt1 = lu <= cl || lu <= cap;
+    return (merged_fits || !unmerged_cpt1) ? 0xf : 0;
 }
 bool smooth_dsm_fits(const LevelK& L, const int* n) {
     int maxn = 0;

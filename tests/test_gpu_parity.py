@@ -389,6 +389,26 @@ def test_vanka_merged_matches_unmerged(n, levels, monkeypatch):
         same(a, c)
 
 
+def test_vanka_per_launch_large_level_matches_persistent(monkeypatch):
+    """256^3 (lists beyond the persistent ping-pong sweep): default merged persistent sweep ==
+    one ping-pong launch per merged phase (the 512^3 default) == unmerged per-launch phases ==
+    unmerged persistent sweep."""
+    out = []
+    for env in ({}, {"SMG_VANKA_KERNELS": "1"}, {"SMG_VANKA_KERNELS": "1", "SMG_VANKA_PAIRS": "0"},
+                {"SMG_VANKA_KERNELS": "0", "SMG_VANKA_PAIRS": "0"}):
+        for k in ("SMG_VANKA_PAIRS", "SMG_VANKA_KERNELS"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        s = smg.Solver(256, levels=6)
+        x = np.random.default_rng(3).uniform(-1, 1, s.ndof())
+        b = np.random.default_rng(4).uniform(-1, 1, s.ndof())
+        out.append(s.smoother(smg.OP_VANKA_SYM, x, b))
+        s.close()
+    for o in out[1:]:
+        same(o, out[0])
+
+
 @pytest.mark.parametrize("dims,levels", [((32, 32, 32), 3), ((64, 16, 16), 3), ((48, 40, 24), 3)])
 def test_fused_apply_dot_matches_separate(dims, levels, monkeypatch):
     """Opt-in fused apply + canonical dot + scalar kernel (SMG_FUSED_DOT=1) == separate kernels, bit for bit."""
