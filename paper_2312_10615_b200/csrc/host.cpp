@@ -698,7 +698,7 @@ void symmetric_dgs(smg_ctx* c, int l, double* x, const double* b, bool cb_ready 
         launch_dgs_wave(L.k, L.wave.data(), static_cast<int>(L.wave.size()), x, b, L.pd0, c->st);
         return;
     }
-    launch_dgs_sym_coop(L.k, x, b, L.pd0, L.pd1, nph, c->st);
+    launch_dgs_sym_coop(L.k, x, b, L.pd0, L.pd1, nph, c->st, L.xb);
 }
 
 void vanka_sym_coop(smg_ctx* c, int l, double* x, const double* b) {

@@ -1544,6 +1544,110 @@ __global__ void __launch_bounds__(256) k_dgs_vel_c(LevelK L, double* __restrict_
 }
 
 
+// ---- fused velocity pair: colour c0, then colour 1 - c0, in ONE pass Xi -> Xo ----
+// At march step tau a CTA updates the c0 cells of plane tau on its kV2X x kV2Y tile plus a
+// one-cell halo ring (redundantly with the neighbouring tiles: identical inputs, identical
+// arithmetic) into a 3-plane shared-memory ring of post-c0 values, then the 1 - c0 cells of
+// plane tau - 1, whose six same-component neighbours are all c0 positions (held in the ring).
+// Every read of the old state goes to Xi, which nothing writes during the launch; the tile's
+// cells of all four fields (p copied) go to Xo.  CTAs are independent (no inter-CTA sync);
+// a CTA marches zch planes (+1 halo plane on each side).  The per-point operations and their
+// order are those of vel_load / vel_store, hence bit-identical to two k_dgs_vel_c phases.
+constexpr int kV2X = 32, kV2Y = 8, kV2HX = kV2X + 2, kV2H = kV2HX * (kV2Y + 2);
+
+// mom() on explicit operands (same operation order)
+__device__ __forceinline__ double mom_v(const LevelK& L, double c, double xm, double xp, double ym, double yp,
+                                        double zm, double zp, double pr, double pl) {
+    double s = xm + xp;
+    s = s + ym;
+    s = s + yp;
+    s = s + zm;
+    s = s + zp;
+    const double lap = 6.0 * c - s;
+    return L.eta_h2 * lap + (pr - pl) * L.inv_h;
+}
+
+__global__ void __launch_bounds__(256) k_dgs_vel2(LevelK L, const double* __restrict__ Xi, double* __restrict__ Xo,
+                                                  const double* __restrict__ B, int c0, int zch) {
+    pdl_wait();
+    __shared__ double ring[3][3 * kV2H];  // [plane % 3][component * kV2H + halo-tile position]
+    const Geom& g = L.g;
+    const int64_t fs = g.fs, sy = g.sy, sz = g.sz;
+    const int tx0 = blockIdx.x * kV2X, ty0 = blockIdx.y * kV2Y;
+    const int z0 = blockIdx.z * zch, z1 = min(z0 + zch, g.nz);
+    const int tid = threadIdx.x + threadIdx.y * kV2X;
+    const int bx = tx0 + threadIdx.x, by = ty0 + threadIdx.y;
+    const bool bcell = bx < g.nx && by < g.ny;
+    const int kc = (threadIdx.y + 1) * kV2HX + threadIdx.x + 1;
+    for (int tau = z0 - 1; tau <= z1; ++tau) {
+        double* R = ring[(tau + 3) % 3];
+        // phase A: post-c0 state of plane tau on the tile + halo ring
+        for (int k = tid; k < kV2H; k += kV2X * kV2Y) {
+            const int x = tx0 - 1 + k % kV2HX, y = ty0 - 1 + k / kV2HX;
+            if (x > g.nx || y > g.ny) continue;  // never read (black cells have x < nx, y < ny)
+            const int64_t i = g.slot(x, y, tau);
+            double u = Xi[i], v = Xi[fs + i], w = Xi[2 * fs + i];
+            if (x >= 0 && y >= 0 && x < g.nx && y < g.ny && tau >= 0 && tau < g.nz &&
+                ((x + y + g.gz(tau) + c0) & 1) == 0) {
+                const VelUpd q = vel_load(L, Xi, B, x, y, tau, true);
+                if (q.du) u = q.u0 + q.ru / L.dv;
+                if (q.dv) v = q.v0 + q.rv / L.dv;
+                if (q.dw) w = q.w0 + q.rw / L.dv;
+            }
+            R[k] = u;
+            R[kV2H + k] = v;
+            R[2 * kV2H + k] = w;
+        }
+        __syncthreads();
+        // phase B: plane zb = tau - 1 of the tile -> Xo (c1 cells updated from the ring)
+        const int zb = tau - 1;
+        if (zb >= z0 && zb < z1 && bcell) {
+            const double* Rm = ring[(zb + 2) % 3];
+            const double* Rc = ring[zb % 3];
+            const double* Rp = R;
+            const int64_t i = g.slot(bx, by, zb);
+            double u, v, w;
+            if (((bx + by + g.gz(zb) + c0) & 1) == 0) {
+                u = Rc[kc];
+                v = Rc[kV2H + kc];
+                w = Rc[2 * kV2H + kc];
+            } else {
+                const double* P = Xi + 3 * fs;
+                u = Xi[i];
+                v = Xi[fs + i];
+                w = Xi[2 * fs + i];
+                const bool here = band_cell(L, bx, by, zb);
+                const bool du = bx >= 1 && !here && !band_cell(L, bx - 1, by, zb);
+                const bool dv = by >= 1 && !here && !band_cell(L, bx, by - 1, zb);
+                const bool dw = g.gz(zb) >= 1 && !here && !band_cell(L, bx, by, zb - 1);
+                const double pc = P[i];
+                if (du) {
+                    const double r = B[i] - mom_v(L, u, Rc[kc - 1], Rc[kc + 1], Rc[kc - kV2HX], Rc[kc + kV2HX], Rm[kc],
+                                                  Rp[kc], pc, P[i - 1]);
+                    u = u + r / L.dv;
+                }
+                if (dv) {
+                    const double* C = Rc + kV2H;
+                    const double r = B[fs + i] - mom_v(L, v, C[kc - 1], C[kc + 1], C[kc - kV2HX], C[kc + kV2HX],
+                                                       Rm[kV2H + kc], Rp[kV2H + kc], pc, P[i - sy]);
+                    v = v + r / L.dv;
+                }
+                if (dw) {
+                    const double* C = Rc + 2 * kV2H;
+                    const double r = B[2 * fs + i] - mom_v(L, w, C[kc - 1], C[kc + 1], C[kc - kV2HX], C[kc + kV2HX],
+                                                           Rm[2 * kV2H + kc], Rp[2 * kV2H + kc], pc, P[i - sz]);
+                    w = w + r / L.dv;
+                }
+            }
+            Xo[i] = u;
+            Xo[fs + i] = v;
+            Xo[2 * fs + i] = w;
+            Xo[3 * fs + i] = Xi[3 * fs + i];
+        }
+        __syncthreads();
+    }
+}
+
 __device__ __forceinline__ bool half_cell(const Geom& g, int c, int i, int j, int k, int& x, int& y, int& z) {
     x = 2 * i + (c & 1);
     y = 2 * j + ((c >> 1) & 1);
@@ -2451,8 +2555,34 @@ void launch_dgs_prev_c(const LevelK& L, double* x, const double* b, int c, cudaS
 
 // Per-phase launches of a symmetric DGS sweep (same phase numbering and
 // delta-buffer protocol as k_dgs_sym_coop).
+// Fused velocity pair (k_dgs_vel2) launch: x -> xo, colour c0 then 1 - c0.
+static void launch_vel2(const LevelK& L, const double* xi, double* xo, const double* b, int c0, cudaStream_t s) {
+    const Geom& g = L.g;
+    const int64_t tiles = static_cast<int64_t>((g.nx + kV2X - 1) / kV2X) * ((g.ny + kV2Y - 1) / kV2Y);
+    // z-chunks per tile: about SMG_VEL2_CTAS CTAs in all, each marching >= SMG_VEL2_MINZ planes
+    const int64_t want = env_int("SMG_VEL2_CTAS", 148 * 8);
+    const int minz = std::max(1, env_int("SMG_VEL2_MINZ", 8));
+    const int64_t chunks = std::max<int64_t>(1, (want + tiles - 1) / tiles);
+    const int zch = std::max<int>(minz, static_cast<int>((g.nz + chunks - 1) / chunks));
+    const dim3 grid((g.nx + kV2X - 1) / kV2X, (g.ny + kV2Y - 1) / kV2Y, (g.nz + zch - 1) / zch);
+    launch_k(k_dgs_vel2, grid, dim3(kV2X, kV2Y), 0, s, L, xi, xo, b, c0, zch);
+    count();
+}
+
+// Opt-in (SMG_VEL2=1): the velocity pairs at both ends of a symmetric sweep run fused
+// (k_dgs_vel2) when the level has a second vector xb: the forward pair writes xb, the pressure
+// steps run in xb, the reverse pair writes back into x (bit-identical).  Measured slower than
+// the separate colour phases (cfg 1 fine sweep 0.296 -> 0.503 ms, cfg 3 20.0 -> 28.5 ms): the
+// z-march per tile serialises two dependent load round trips and two barriers per plane.
+static bool vel2_on(const LevelK& L, const double* xb, int nph) {
+    const int64_t ncell = static_cast<int64_t>(L.g.nx) * L.g.ny * L.g.nz;
+    return xb && nph > 10 && env_int("SMG_VEL2", 0) != 0 && L.g.z0 == 0 && L.g.nz == L.g.gnz &&
+           ncell >= env_int("SMG_VEL2_MIN_CELLS", 0);
+}
+
 template <int ZC>
-static void dgs_sym_phases_zc(const LevelK& L, double* x, const double* b, double* d0, int nph, cudaStream_t s) {
+static void dgs_sym_phases_zc(const LevelK& L, double* x, const double* b, double* d0, int nph, cudaStream_t s,
+                              double* xb) {
     const Geom& g = L.g;
     const dim3 blk(32, 8);
     dim3 gv = dgs_grid_v(g), gh = dgs_grid_h(g);
@@ -2461,40 +2591,55 @@ static void dgs_sym_phases_zc(const LevelK& L, double* x, const double* b, doubl
     auto groups_grid = [&](int grp) { return dim3(gh.x, gh.y, gh.z * group_size(grp)); };
     // consecutive steps alternate the traversal direction (kRevBit): L2 reuse between steps
     const int alt = env_int("SMG_DGS_ALT", 1) ? kRevBit : 0;
-    launch_k(k_dgs_vel_c<ZC>, gv, blk, 0, s, L, x, b, 0);
-    launch_k(k_dgs_vel_c<ZC>, gv, blk, 0, s, L, x, b, 1 | alt);
+    const bool fuse = vel2_on(L, xb, nph);
+    double* xp = x;  // where the pressure steps run
+    if (fuse) {
+        launch_vel2(L, x, xb, b, 0, s);
+        xp = xb;
+    } else {
+        launch_k(k_dgs_vel_c<ZC>, gv, blk, 0, s, L, x, b, 0);
+        launch_k(k_dgs_vel_c<ZC>, gv, blk, 0, s, L, x, b, 1 | alt);
+        count();
+        count();
+    }
     for (int q = 0; q < 4; ++q)
-        launch_k(k_dgs_pf_lazy_c<ZC>, groups_grid(fwd_group(q)), blk, 0, s, L, x, b, d0, fwd_group(q) | (q & 1 ? alt : 0));
-    launch_k(k_dgs_pf_flush, cell_grid(g), blk, 0, s, L, x, d0, 0);
-    for (int k = 0; k < 7; ++k) count();
+        launch_k(k_dgs_pf_lazy_c<ZC>, groups_grid(fwd_group(q)), blk, 0, s, L, xp, b, d0, fwd_group(q) | (q & 1 ? alt : 0));
+    launch_k(k_dgs_pf_flush, cell_grid(g), blk, 0, s, L, xp, d0, 0);
+    for (int k = 0; k < 5; ++k) count();
     if (nph <= 10) return;
     for (int q = 0; q < 4; ++q)
-        launch_k(k_dgs_prev_c<ZC>, groups_grid(rev_group(q)), blk, 0, s, L, x, b, rev_group(q) | (q & 1 ? 0 : alt));
-    launch_k(k_dgs_vel_c<ZC>, gv, blk, 0, s, L, x, b, 1 | alt);
-    launch_k(k_dgs_vel_c<ZC>, gv, blk, 0, s, L, x, b, 0);
-    for (int k = 0; k < 6; ++k) count();
+        launch_k(k_dgs_prev_c<ZC>, groups_grid(rev_group(q)), blk, 0, s, L, xp, b, rev_group(q) | (q & 1 ? 0 : alt));
+    for (int k = 0; k < 4; ++k) count();
+    if (fuse) {
+        launch_vel2(L, xb, x, b, 1, s);
+    } else {
+        launch_k(k_dgs_vel_c<ZC>, gv, blk, 0, s, L, x, b, 1 | alt);
+        launch_k(k_dgs_vel_c<ZC>, gv, blk, 0, s, L, x, b, 0);
+        count();
+        count();
+    }
 }
 
 static void launch_dgs_sym_phases(const LevelK& L, double* x, const double* b, double* d0, double* d1, int nph,
-                                  cudaStream_t s) {
+                                  cudaStream_t s, double* xb) {
     (void)d1;
     // two cells per thread only pays on the largest levels (>= 128^3 cells); smaller levels need blocks
     const int64_t ncell = static_cast<int64_t>(L.g.nx) * L.g.ny * L.g.nz;
     const int zc = env_int("SMG_DGS_ZC", ncell >= (int64_t(1) << 21) ? 2 : 1);
-    if (zc >= 4) dgs_sym_phases_zc<4>(L, x, b, d0, nph, s);
-    else if (zc == 2) dgs_sym_phases_zc<2>(L, x, b, d0, nph, s);
-    else dgs_sym_phases_zc<1>(L, x, b, d0, nph, s);
+    if (zc >= 4) dgs_sym_phases_zc<4>(L, x, b, d0, nph, s, xb);
+    else if (zc == 2) dgs_sym_phases_zc<2>(L, x, b, d0, nph, s, xb);
+    else dgs_sym_phases_zc<1>(L, x, b, d0, nph, s, xb);
 }
 
 void launch_dgs_sym_coop(const LevelK& L, double* x, const double* b, double* d0, double* d1, int nph,
-                         cudaStream_t s) {
+                         cudaStream_t s, double* xb) {
     // one kernel per step on every level: inside the SQMR iteration graph the per-step
     // kernels beat the persistent grid-barrier sweep even at 16^3-64^3 (measured: 2.43 ->
     // 2.31 ms per cfg-1 iteration), although the sweep wins when timed back to back alone;
     // SMG_DGS_COOP=1 / SMG_DGS_COOP_MAX=<cells> bring the persistent sweep back
     const int64_t coop_max = env_int("SMG_DGS_COOP", 0) ? (int64_t{1} << 40) : env_int("SMG_DGS_COOP_MAX", 0);
     if (static_cast<int64_t>(L.g.nx) * L.g.ny * L.g.nz > coop_max) {
-        launch_dgs_sym_phases(L, x, b, d0, d1, nph, s);
+        launch_dgs_sym_phases(L, x, b, d0, d1, nph, s, xb);
         return;
     }
     const int64_t ncell = static_cast<int64_t>(L.g.nx) * L.g.ny * L.g.nz;

@@ -110,8 +110,10 @@ void launch_vanka_sym_coop(const LevelK& L, double* x, const double* b, const in
                            cudaStream_t s, double* xb = nullptr, const int32_t* refresh = nullptr,
                            int64_t nrefresh = 0, const VankaPairs& pr = VankaPairs{});
 int vanka_pairs_pay(const int* n);  // mask of the pairs to merge on a level with these list sizes
+// xb (optional, a second vector of the level, used as scratch): the velocity pairs at both
+// ends of the sweep run fused (k_dgs_vel2, x -> xb ... xb -> x).
 void launch_dgs_sym_coop(const LevelK& L, double* x, const double* b, double* d0, double* d1, int nph,
-                         cudaStream_t s);
+                         cudaStream_t s, double* xb = nullptr);
 // Whole smooth (Alg. 3) of a level held in the distributed shared memory of one
 // 16-CTA cluster (vector + DGS delta <= 2 MB).
 bool smooth_dsm_fits(const LevelK& L, const int* n);

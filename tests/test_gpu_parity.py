@@ -389,6 +389,24 @@ def test_vanka_merged_matches_unmerged(n, levels, monkeypatch):
         same(a, c)
 
 
+@pytest.mark.parametrize("dims,levels", [((32, 32, 32), 3), ((48, 40, 24), 3), ((64, 16, 16), 3), ((128, 128, 128), 5)])
+def test_fused_velocity_pair_matches_separate(dims, levels, monkeypatch):
+    """Fused red+black velocity DGS pass (k_dgs_vel2, ping-pong through the level's second
+    vector) == the two separate colour phases, bit for bit: symmetric DGS, smooth, V-cycle."""
+    nx, ny, nz = dims
+    out = []
+    for fused in ("0", "1"):
+        monkeypatch.setenv("SMG_VEL2", fused)
+        monkeypatch.setenv("SMG_VEL2_CTAS", "64")  # long marches too (several planes per CTA)
+        s = smg.Solver(nx, ny, nz, h=1 / ny, levels=levels)
+        x = np.random.default_rng(nx + ny).uniform(-1, 1, s.ndof())
+        b = np.random.default_rng(nz).uniform(-1, 1, s.ndof())
+        out.append((s.smoother(smg.OP_DGS_SYM, x, b), s.smoother(smg.OP_SMOOTH, x, b), s.vcycle(b)))
+        s.close()
+    for a, c in zip(*out):
+        same(a, c)
+
+
 def test_vanka_per_launch_large_level_matches_persistent(monkeypatch):
     """256^3 (lists beyond the persistent ping-pong sweep): default merged persistent sweep ==
     one ping-pong launch per merged phase (the 512^3 default) == unmerged per-launch phases ==
