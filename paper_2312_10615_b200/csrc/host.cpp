@@ -472,6 +472,23 @@ void build(smg_ctx* c, const std::vector<double>* shared_coarse = nullptr, std::
                     need[i] = need[i + 1] = need[fs + i] = need[fs + i + G.sy] = need[2 * fs + i] =
                         need[2 * fs + i + G.sz] = need[P] = 1;
                 }
+            // minus the DOFs the sweep's first phase writes (list vanka_order(0) = parity 0, with
+            // parity 7 when that pair is merged): the refresh then runs concurrently with the
+            // first phase (no conflicting writes; the first phase reads only x)
+            int nsz[8];
+            for (int col = 0; col < 8; ++col) nsz[col] = static_cast<int>(cells[col].size());
+            const int pm0 = vanka_pairs_pay(nsz);
+            for (int col : {0, 7}) {
+                if (col == 7 && !(pm0 & 1)) continue;
+                for (size_t t = 0; t < cells[col].size(); ++t) {
+                    const int64_t i = cells[col][t];
+                    const int m = masks[col][t];
+                    const int64_t fs = G.fs;
+                    const int64_t dof[7] = {i, i + 1, fs + i, fs + i + G.sy, 2 * fs + i, 2 * fs + i + G.sz, 3 * fs + i};
+                    for (int q = 0; q < 7; ++q)
+                        if (q == 6 || (m & (1 << q))) need[dof[q]] = 0;
+                }
+            }
             std::vector<int32_t> lst;
             for (int64_t k = 0; k < static_cast<int64_t>(need.size()); ++k)
                 if (need[k]) lst.push_back(static_cast<int32_t>(k));

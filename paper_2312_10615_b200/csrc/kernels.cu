@@ -1074,9 +1074,19 @@ __global__ void __launch_bounds__(256) k_vanka_ppk(LevelK L, const double* __res
 template <int MODE, int CPT>
 __global__ void __launch_bounds__(512) k_vanka_pp(LevelK L, double* __restrict__ XA, double* __restrict__ XB,
                                                   const double* __restrict__ B, VankaLists vl,
-                                                  const double* __restrict__ ktab, int nu) {
+                                                  const double* __restrict__ ktab, int nu,
+                                                  const int32_t* __restrict__ refresh, int64_t nrefresh) {
     __shared__ double Ks[64 * 49];
     for (int k = threadIdx.x; k < 64 * 49; k += blockDim.x) Ks[k] = ktab[k];
+    // opt-in (SMG_VANKA_REFRESH_IN=1): XB = XA on the read set minus the first phase's DOFs,
+    // concurrently with the first phase (which reads only XA and writes only its own DOFs of XB);
+    // the first barrier orders both.  Measured slower than the separate k_refresh launch (cfg 1
+    // fine sweep 0.080 -> 0.093 ms): the copy delays the first phase's gathers.
+    for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < nrefresh;
+         t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t k = refresh[t];
+        XB[k] = XA[k];
+    }
     __syncthreads();
     vanka_sweeps_pp<MODE, CPT>(L, XA, XB, B, vl, Ks, nu, blockIdx.x * blockDim.x + threadIdx.x,
                                gridDim.x * blockDim.x);
@@ -2271,7 +2281,9 @@ static int coop_blocks(const void* fn, int64_t work, int threads) {
 }
 
 constexpr int kClusterCTAs = 16, kClusterThreads = 512;
-static int coop_threads() { return env_int("SMG_COOP_THREADS", 512) == 256 ? 256 : 512; }  // tuning knob
+// CTA size of the cooperative sweeps (tuning knob): 256 measured faster than 512 on the cfg-1
+// iteration (2.43 -> 2.34 ms; fine-level Vanka sweep 0.093 -> 0.075 ms: 4 CTAs/SM instead of 2)
+static int coop_threads() { return env_int("SMG_COOP_THREADS", 256) == 512 ? 512 : 256; }
 
 // Launch either as one cooperative grid (MODE 0) or as a single cluster of
 // kClusterCTAs CTAs (MODE 1) whose phases are separated by cluster barriers.
@@ -2404,20 +2416,27 @@ void launch_vanka_sym_coop(const LevelK& L, double* x, const double* b, const in
     if (xb && vk_kernels == 1) { ppk(); return; }
     const bool phases = env_int("SMG_VANKA_PHASES", 0) != 0;  // 1: per-phase delta/apply launches (tests)
     if (!phases && xb && !cl && env_int("SMG_VANKA_PP", 1)) {  // ping-pong (grid mode): one barrier per phase
-        void* pargs[] = {args[0], &x, &xb, args[2], args[3], args[4], args[5]};
+        const bool rin = env_int("SMG_VANKA_REFRESH_IN", 0) != 0;
+        if (!rin) refresh_xb();
+        const int32_t* rl = refresh;
+        int64_t rn = rin && nrefresh > 0 ? nrefresh : 0;
+        void* pargs[] = {args[0], &x, &xb, args[2], args[3], args[4], args[5], &rl, &rn};
         if (fits(reinterpret_cast<const void*>(k_vanka_pp<0, 1>), 1)) {
-            refresh_xb();
             launch_vanka_pp<1>(cl, lanes, pargs, s);
             return;
         }
         if (fits(reinterpret_cast<const void*>(k_vanka_pp<0, 2>), 2)) {
-            refresh_xb();
             launch_vanka_pp<2>(cl, (lanes + 1) / 2, pargs, s);
             return;
         }
         if (fits(reinterpret_cast<const void*>(k_vanka_pp<0, 4>), 4)) {
-            refresh_xb();
             launch_vanka_pp<4>(cl, (lanes + 3) / 4, pargs, s);
+            return;
+        }
+        // beyond the persistent ping-pong sweep: one launch per phase (measured faster than the
+        // persistent CPT-8 sweep below at 256^3: 0.339 -> 0.305 ms)
+        if (vk_kernels != 0) {
+            ppk();
             return;
         }
     }

@@ -378,15 +378,20 @@ def test_vanka_merged_phase_bitwise(mode, monkeypatch):
 def test_vanka_merged_matches_unmerged(n, levels, monkeypatch):
     """Large levels (grid ping-pong sweeps): merged pairs (8-phase) == unmerged (16-phase) sweep."""
     out = []
-    for merge in ("0", "2"):  # 2: merge all pairs even where the default would not
-        monkeypatch.setenv("SMG_VANKA_PAIRS", merge)
+    # 2: merge all pairs even where the default would not; REFRESH_IN: refresh inside the sweep
+    for env in ({"SMG_VANKA_PAIRS": "0"}, {"SMG_VANKA_PAIRS": "2"}, {"SMG_VANKA_REFRESH_IN": "1"}):
+        for k in ("SMG_VANKA_PAIRS", "SMG_VANKA_REFRESH_IN"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
         s = smg.Solver(n, levels=levels)
         x = np.random.default_rng(n).uniform(-1, 1, s.ndof())
         b = np.random.default_rng(n + 1).uniform(-1, 1, s.ndof())
         out.append((s.smoother(smg.OP_VANKA_SYM, x, b), s.smoother(smg.OP_SMOOTH, x, b), s.vcycle(b)))
         s.close()
-    for a, c in zip(*out):
-        same(a, c)
+    for o in out[1:]:
+        for a, c in zip(o, out[0]):
+            same(a, c)
 
 
 @pytest.mark.parametrize("dims,levels", [((32, 32, 32), 3), ((48, 40, 24), 3), ((64, 16, 16), 3), ((128, 128, 128), 5)])
@@ -403,8 +408,9 @@ def test_fused_velocity_pair_matches_separate(dims, levels, monkeypatch):
         b = np.random.default_rng(nz).uniform(-1, 1, s.ndof())
         out.append((s.smoother(smg.OP_DGS_SYM, x, b), s.smoother(smg.OP_SMOOTH, x, b), s.vcycle(b)))
         s.close()
-    for a, c in zip(*out):
-        same(a, c)
+    for o in out[1:]:
+        for a, c in zip(o, out[0]):
+            same(a, c)
 
 
 def test_vanka_per_launch_large_level_matches_persistent(monkeypatch):
