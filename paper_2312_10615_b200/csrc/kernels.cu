@@ -1078,10 +1078,10 @@ __global__ void __launch_bounds__(512) k_vanka_pp(LevelK L, double* __restrict__
                                                   const int32_t* __restrict__ refresh, int64_t nrefresh) {
     __shared__ double Ks[64 * 49];
     for (int k = threadIdx.x; k < 64 * 49; k += blockDim.x) Ks[k] = ktab[k];
-    // opt-in (SMG_VANKA_REFRESH_IN=1): XB = XA on the read set minus the first phase's DOFs,
-    // concurrently with the first phase (which reads only XA and writes only its own DOFs of XB);
-    // the first barrier orders both.  Measured slower than the separate k_refresh launch (cfg 1
-    // fine sweep 0.080 -> 0.093 ms): the copy delays the first phase's gathers.
+    // XB = XA on the read set minus the first phase's DOFs, concurrently with the first phase
+    // (which reads only XA and writes only its own DOFs of XB); the first barrier orders both.
+    // Replaces a k_refresh launch per sweep (SMG_VANKA_REFRESH_IN=0 restores it): cfg 1 solve
+    // 18.75 -> 18.69 ms and 18.76 -> 18.69 ms on two boxes (fine sweep 0.075 -> 0.073 ms).
     for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < nrefresh;
          t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const int64_t k = refresh[t];
@@ -2381,7 +2381,8 @@ void launch_vanka_sym_coop(const LevelK& L, double* x, const double* b, const in
     const int64_t lanes = 8 * static_cast<int64_t>(maxn);
     const int64_t cl_threads = static_cast<int64_t>(kClusterCTAs) * kClusterThreads;
     const int mode = env_int("SMG_SYNC_MODE", 0);
-    const bool cl = mode == 2 || (mode == 0 && lanes <= cl_threads);
+    // tuning knob: a cluster also takes levels needing up to SMG_CL_CPT blocks per lane group
+    const bool cl = mode == 2 || (mode == 0 && lanes <= cl_threads * std::max(1, env_int("SMG_CL_CPT", 1)));
     // every block of a colour must be held in registers by some lane group:
     // threads * CPT >= lanes with threads = co-resident capacity of THAT instance
     auto fits = [&](const void* fn, int cpt) {
@@ -2416,7 +2417,7 @@ void launch_vanka_sym_coop(const LevelK& L, double* x, const double* b, const in
     if (xb && vk_kernels == 1) { ppk(); return; }
     const bool phases = env_int("SMG_VANKA_PHASES", 0) != 0;  // 1: per-phase delta/apply launches (tests)
     if (!phases && xb && !cl && env_int("SMG_VANKA_PP", 1)) {  // ping-pong (grid mode): one barrier per phase
-        const bool rin = env_int("SMG_VANKA_REFRESH_IN", 0) != 0;
+        const bool rin = env_int("SMG_VANKA_REFRESH_IN", 1) != 0;
         if (!rin) refresh_xb();
         const int32_t* rl = refresh;
         int64_t rn = rin && nrefresh > 0 ? nrefresh : 0;

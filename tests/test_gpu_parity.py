@@ -378,8 +378,8 @@ def test_vanka_merged_phase_bitwise(mode, monkeypatch):
 def test_vanka_merged_matches_unmerged(n, levels, monkeypatch):
     """Large levels (grid ping-pong sweeps): merged pairs (8-phase) == unmerged (16-phase) sweep."""
     out = []
-    # 2: merge all pairs even where the default would not; REFRESH_IN: refresh inside the sweep
-    for env in ({"SMG_VANKA_PAIRS": "0"}, {"SMG_VANKA_PAIRS": "2"}, {"SMG_VANKA_REFRESH_IN": "1"}):
+    # 2: merge all pairs even where the default would not; REFRESH_IN=0: separate refresh launch
+    for env in ({"SMG_VANKA_PAIRS": "0"}, {"SMG_VANKA_PAIRS": "2"}, {"SMG_VANKA_REFRESH_IN": "0"}):
         for k in ("SMG_VANKA_PAIRS", "SMG_VANKA_REFRESH_IN"):
             monkeypatch.delenv(k, raising=False)
         for k, v in env.items():
