@@ -1658,6 +1658,179 @@ __global__ void __launch_bounds__(256) k_dgs_vel2(LevelK L, const double* __rest
     }
 }
 
+// Staged variant (SMG_VEL2=2): the old state of each plane (u, v, w, p on the tile + 2 halo,
+// b on the tile + 1 halo) is copied into shared-memory rings with cp.async two planes (x) /
+// one plane (b) ahead of use, so the loads of the next planes are in flight while the CTA
+// computes the current one from shared memory.  Same per-point operations as k_dgs_vel2.
+// Measured slower than both (cfg 1 solve 18.69 -> 24.6 ms).
+constexpr int kS2X = 32, kS2Y = 16, kS2SX = kS2X + 4, kS2SY = kS2Y + 4, kS2SP = kS2SX * kS2SY;
+constexpr int kS2BX = kS2X + 2, kS2BP = kS2BX * (kS2Y + 2);
+constexpr int kS2XR = 5, kS2BR = 3;
+constexpr size_t kS2Smem = sizeof(double) * (static_cast<size_t>(kS2XR) * 4 * kS2SP + kS2BR * 3 * kS2BP + 3 * 3 * kS2BP);
+
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+__global__ void __launch_bounds__(kS2X * kS2Y, 1) k_dgs_vel2s(LevelK L, const double* __restrict__ Xi,
+                                                              double* __restrict__ Xo, const double* __restrict__ B,
+                                                              int c0, int zch) {
+    pdl_wait();
+    extern __shared__ double sm2[];
+    double* XR = sm2;                               // [kS2XR][4][kS2SP]  u, v, w, p (tile + 2)
+    double* BR = XR + kS2XR * 4 * kS2SP;            // [kS2BR][3][kS2BP]  b_u, b_v, b_w (tile + 1)
+    double* RR = BR + kS2BR * 3 * kS2BP;            // [3][3][kS2BP]      post-c0 u, v, w (tile + 1)
+    const Geom& g = L.g;
+    const int64_t fs = g.fs;
+    const int tx0 = blockIdx.x * kS2X, ty0 = blockIdx.y * kS2Y;
+    const int z0 = blockIdx.z * zch, z1 = min(z0 + zch, g.nz);
+    const int tid = threadIdx.x + threadIdx.y * kS2X, nth = kS2X * kS2Y;
+    // stage plane z of x (tile + 2) / of b (tile + 1); slots outside the padded box read as 0
+    auto stage_x = [&](int z) {
+        double* D = XR + ((z + 2 * kS2XR) % kS2XR) * 4 * kS2SP;
+        const bool zin = z >= -g.zg && z < g.nz + g.zg;
+        for (int k = tid; k < kS2SP; k += nth) {
+            const int x = tx0 - 2 + k % kS2SX, y = ty0 - 2 + k / kS2SX;
+            if (zin && x >= -g.xo && x < g.px - g.xo && y >= -1 && y <= g.ny) {
+                const int64_t i = g.slot(x, y, z);
+#pragma unroll
+                for (int f = 0; f < 4; ++f) cp_async8(D + f * kS2SP + k, Xi + f * fs + i);
+            } else {
+#pragma unroll
+                for (int f = 0; f < 4; ++f) D[f * kS2SP + k] = 0.0;
+            }
+        }
+    };
+    auto stage_b = [&](int z) {
+        double* D = BR + ((z + 2 * kS2BR) % kS2BR) * 3 * kS2BP;
+        const bool zin = z >= 0 && z < g.nz;
+        for (int k = tid; k < kS2BP; k += nth) {
+            const int x = tx0 - 1 + k % kS2BX, y = ty0 - 1 + k / kS2BX;
+            if (zin && x >= 0 && x < g.nx && y >= 0 && y < g.ny) {
+                const int64_t i = g.slot(x, y, z);
+#pragma unroll
+                for (int f = 0; f < 3; ++f) cp_async8(D + f * kS2BP + k, B + f * fs + i);
+            }
+        }
+    };
+    auto xs = [&](int z) { return XR + ((z + 2 * kS2XR) % kS2XR) * 4 * kS2SP; };
+    stage_x(z0 - 2);
+    stage_x(z0 - 1);
+    stage_x(z0);
+    stage_b(z0 - 1);
+    cp_async_commit();
+    const double idv = L.dv;
+    for (int tau = z0 - 1; tau <= z1; ++tau) {
+        // prefetch: x plane tau + 2, b plane tau + 1 (one group per step)
+        if (tau + 2 <= z1 + 1) stage_x(tau + 2);
+        if (tau + 1 <= z1) stage_b(tau + 1);
+        cp_async_commit();
+        cp_async_wait<1>();  // everything but this step's prefetch has landed
+        __syncthreads();
+        const double* Xm = xs(tau - 1);
+        const double* Xc = xs(tau);
+        const double* Xp = xs(tau + 1);
+        const double* Bc = BR + ((tau + 2 * kS2BR) % kS2BR) * 3 * kS2BP;
+        double* R = RR + ((tau + 3) % 3) * 3 * kS2BP;
+        // phase A: post-c0 state of plane tau on the tile + 1 halo
+        for (int k = tid; k < kS2BP; k += nth) {
+            const int hx = k % kS2BX, hy = k / kS2BX;
+            const int x = tx0 - 1 + hx, y = ty0 - 1 + hy;
+            const int s = (hy + 1) * kS2SX + hx + 1;  // staged position
+            double u = Xc[s], v = Xc[kS2SP + s], w = Xc[2 * kS2SP + s];
+            if (x >= 0 && y >= 0 && x < g.nx && y < g.ny && tau >= 0 && tau < g.nz &&
+                ((x + y + g.gz(tau) + c0) & 1) == 0) {
+                const bool here = band_cell(L, x, y, tau);
+                const bool du = x >= 1 && !here && !band_cell(L, x - 1, y, tau);
+                const bool dv = y >= 1 && !here && !band_cell(L, x, y - 1, tau);
+                const bool dw = g.gz(tau) >= 1 && !here && !band_cell(L, x, y, tau - 1);
+                const double* P = Xc + 3 * kS2SP;
+                if (du) {
+                    const double r = Bc[k] - mom_v(L, u, Xc[s - 1], Xc[s + 1], Xc[s - kS2SX], Xc[s + kS2SX], Xm[s],
+                                                   Xp[s], P[s], P[s - 1]);
+                    u = u + r / idv;
+                }
+                if (dv) {
+                    const double* C = Xc + kS2SP;
+                    const double r = Bc[kS2BP + k] - mom_v(L, v, C[s - 1], C[s + 1], C[s - kS2SX], C[s + kS2SX],
+                                                           Xm[kS2SP + s], Xp[kS2SP + s], P[s], P[s - kS2SX]);
+                    v = v + r / idv;
+                }
+                if (dw) {
+                    const double* C = Xc + 2 * kS2SP;
+                    const double r = Bc[2 * kS2BP + k] - mom_v(L, w, C[s - 1], C[s + 1], C[s - kS2SX], C[s + kS2SX],
+                                                               Xm[2 * kS2SP + s], Xp[2 * kS2SP + s], P[s],
+                                                               Xm[3 * kS2SP + s]);
+                    w = w + r / idv;
+                }
+            }
+            R[k] = u;
+            R[kS2BP + k] = v;
+            R[2 * kS2BP + k] = w;
+        }
+        __syncthreads();
+        // phase B: plane zb = tau - 1 of the tile -> Xo
+        const int zb = tau - 1;
+        const int bx = tx0 + threadIdx.x, by = ty0 + threadIdx.y;
+        if (zb >= z0 && zb < z1 && bx < g.nx && by < g.ny) {
+            const double* Rm = RR + ((zb + 2) % 3) * 3 * kS2BP;
+            const double* Rc = RR + (zb % 3) * 3 * kS2BP;
+            const double* Rp = R;
+            const double* Xb = Xm;            // staged plane zb
+            const double* Xbm = xs(zb - 1);   // staged plane zb - 1 (p for the w row)
+            const double* Bb = BR + ((zb + 2 * kS2BR) % kS2BR) * 3 * kS2BP;
+            const int kc = (threadIdx.y + 1) * kS2BX + threadIdx.x + 1;
+            const int s = (threadIdx.y + 2) * kS2SX + threadIdx.x + 2;
+            const int64_t i = g.slot(bx, by, zb);
+            double u, v, w;
+            if (((bx + by + g.gz(zb) + c0) & 1) == 0) {
+                u = Rc[kc];
+                v = Rc[kS2BP + kc];
+                w = Rc[2 * kS2BP + kc];
+            } else {
+                const double* P = Xb + 3 * kS2SP;
+                u = Xb[s];
+                v = Xb[kS2SP + s];
+                w = Xb[2 * kS2SP + s];
+                const bool here = band_cell(L, bx, by, zb);
+                const bool du = bx >= 1 && !here && !band_cell(L, bx - 1, by, zb);
+                const bool dv = by >= 1 && !here && !band_cell(L, bx, by - 1, zb);
+                const bool dw = g.gz(zb) >= 1 && !here && !band_cell(L, bx, by, zb - 1);
+                const double pc = P[s];
+                if (du) {
+                    const double r = Bb[kc] - mom_v(L, u, Rc[kc - 1], Rc[kc + 1], Rc[kc - kS2BX], Rc[kc + kS2BX],
+                                                    Rm[kc], Rp[kc], pc, P[s - 1]);
+                    u = u + r / idv;
+                }
+                if (dv) {
+                    const double* C = Rc + kS2BP;
+                    const double r = Bb[kS2BP + kc] - mom_v(L, v, C[kc - 1], C[kc + 1], C[kc - kS2BX], C[kc + kS2BX],
+                                                            Rm[kS2BP + kc], Rp[kS2BP + kc], pc, P[s - kS2SX]);
+                    v = v + r / idv;
+                }
+                if (dw) {
+                    const double* C = Rc + 2 * kS2BP;
+                    const double r = Bb[2 * kS2BP + kc] - mom_v(L, w, C[kc - 1], C[kc + 1], C[kc - kS2BX],
+                                                                C[kc + kS2BX], Rm[2 * kS2BP + kc], Rp[2 * kS2BP + kc],
+                                                                pc, Xbm[3 * kS2SP + s]);
+                    w = w + r / idv;
+                }
+            }
+            Xo[i] = u;
+            Xo[fs + i] = v;
+            Xo[2 * fs + i] = w;
+            Xo[3 * fs + i] = Xb[3 * kS2SP + s];
+        }
+        // the next step's prefetch overwrites the ring slots of planes tau - 2 (x) and tau - 1 (b)
+        __syncthreads();
+    }
+    cp_async_wait<0>();
+}
+
 __device__ __forceinline__ bool half_cell(const Geom& g, int c, int i, int j, int k, int& x, int& y, int& z) {
     x = 2 * i + (c & 1);
     y = 2 * j + ((c >> 1) & 1);
@@ -2584,6 +2757,21 @@ static void launch_vel2(const LevelK& L, const double* xi, double* xo, const dou
     const int minz = std::max(1, env_int("SMG_VEL2_MINZ", 8));
     const int64_t chunks = std::max<int64_t>(1, (want + tiles - 1) / tiles);
     const int zch = std::max<int>(minz, static_cast<int>((g.nz + chunks - 1) / chunks));
+    if (env_int("SMG_VEL2", 0) == 2) {  // cp.async-staged variant: one 512-thread CTA per SM
+        static bool attr = false;
+        if (!attr) {
+            note(cudaFuncSetAttribute(k_dgs_vel2s, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(kS2Smem)));
+            attr = true;
+        }
+        const int64_t t2 = static_cast<int64_t>((g.nx + kS2X - 1) / kS2X) * ((g.ny + kS2Y - 1) / kS2Y);
+        const int64_t ch2 = std::max<int64_t>(1, (env_int("SMG_VEL2_CTAS", 148 * 4) + t2 - 1) / t2);
+        const int z2 = std::max<int>(minz, static_cast<int>((g.nz + ch2 - 1) / ch2));
+        const dim3 grid2((g.nx + kS2X - 1) / kS2X, (g.ny + kS2Y - 1) / kS2Y, (g.nz + z2 - 1) / z2);
+        launch_k(k_dgs_vel2s, grid2, dim3(kS2X, kS2Y), kS2Smem, s, L, xi, xo, b, c0, z2);
+        count();
+        return;
+    }
     const dim3 grid((g.nx + kV2X - 1) / kV2X, (g.ny + kV2Y - 1) / kV2Y, (g.nz + zch - 1) / zch);
     launch_k(k_dgs_vel2, grid, dim3(kV2X, kV2Y), 0, s, L, xi, xo, b, c0, zch);
     count();

@@ -400,7 +400,7 @@ def test_fused_velocity_pair_matches_separate(dims, levels, monkeypatch):
     vector) == the two separate colour phases, bit for bit: symmetric DGS, smooth, V-cycle."""
     nx, ny, nz = dims
     out = []
-    for fused in ("0", "1"):
+    for fused in ("0", "1", "2"):  # 2: cp.async-staged variant
         monkeypatch.setenv("SMG_VEL2", fused)
         monkeypatch.setenv("SMG_VEL2_CTAS", "64")  # long marches too (several planes per CTA)
         s = smg.Solver(nx, ny, nz, h=1 / ny, levels=levels)
