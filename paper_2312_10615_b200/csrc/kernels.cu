@@ -918,20 +918,12 @@ __device__ __forceinline__ void vanka_pp_phase(const LevelK& L, const double* __
             if (carry && s8 < 6 && ((cmask >> (vanka_entry_colour(vl, pcol, t) ^ (1 << (s8 >> 1)))) & 1)) {
                 // cell slots are int32 list entries: 32-bit unsigned division (a 64-bit one is a
                 // long software sequence on the carry decision's critical path)
-                int zl, y, x;
-                if (vl.div64) {
-                    zl = static_cast<int>(ip / sz) - g.zg;
-                    const int64_t r64 = ip - static_cast<int64_t>(zl + g.zg) * sz;
-                    y = static_cast<int>(r64 / sy) - 1;
-                    x = static_cast<int>(r64 - static_cast<int64_t>(y + 1) * sy) - g.xo;
-                } else {
-                    const uint32_t ipu = static_cast<uint32_t>(ip), szu = static_cast<uint32_t>(sz);
-                    const uint32_t syu = static_cast<uint32_t>(sy);
-                    const uint32_t zq = ipu / szu, rem = ipu - zq * szu, yq = rem / syu;
-                    zl = static_cast<int>(zq) - g.zg;
-                    y = static_cast<int>(yq) - 1;
-                    x = static_cast<int>(rem - yq * syu) - g.xo;
-                }
+                const uint32_t ipu = static_cast<uint32_t>(ip), szu = static_cast<uint32_t>(sz);
+                const uint32_t syu = static_cast<uint32_t>(sy);
+                const uint32_t zq = ipu / szu, rem = ipu - zq * szu, yq = rem / syu;
+                const int zl = static_cast<int>(zq) - g.zg;
+                const int y = static_cast<int>(yq) - 1;
+                const int x = static_cast<int>(rem - yq * syu) - g.xo;
                 const int d = (s8 & 1) ? 1 : -1;
                 const int ax = s8 >> 1;
                 if (band_cell(L, x + (ax == 0 ? d : 0), y + (ax == 1 ? d : 0), zl + (ax == 2 ? d : 0)))
