@@ -654,7 +654,6 @@ struct VankaLists {
     // 7-m has no phase of its own.  All four pairs merged: 8 phases per symmetric sweep.
     int pairs;
     int first[4];
-    int div64 = 0;  // A/B knob (SMG_VANKA_DIV64=1): the carry decision's former 64-bit divisions
 };
 // phase k (0..15) of a symmetric sweep -> colour list, -1 if the phase is folded away
 __device__ __forceinline__ int vanka_phase_list(const VankaLists& vl, int k) {
@@ -916,14 +915,10 @@ __device__ __forceinline__ void vanka_pp_phase(const LevelK& L, const double* __
             block_of(pcol, j, t, ip, mp);
             carry = s8 == 6 || (mp & (1 << s8));
             if (carry && s8 < 6 && ((cmask >> (vanka_entry_colour(vl, pcol, t) ^ (1 << (s8 >> 1)))) & 1)) {
-                // cell slots are int32 list entries: 32-bit unsigned division (a 64-bit one is a
-                // long software sequence on the carry decision's critical path)
-                const uint32_t ipu = static_cast<uint32_t>(ip), szu = static_cast<uint32_t>(sz);
-                const uint32_t syu = static_cast<uint32_t>(sy);
-                const uint32_t zq = ipu / szu, rem = ipu - zq * szu, yq = rem / syu;
-                const int zl = static_cast<int>(zq) - g.zg;
-                const int y = static_cast<int>(yq) - 1;
-                const int x = static_cast<int>(rem - yq * syu) - g.xo;
+                const int zl = static_cast<int>(ip / sz) - g.zg;
+                const int64_t rem = ip - static_cast<int64_t>(zl + g.zg) * sz;
+                const int y = static_cast<int>(rem / sy) - 1;
+                const int x = static_cast<int>(rem - static_cast<int64_t>(y + 1) * sy) - g.xo;
                 const int d = (s8 & 1) ? 1 : -1;
                 const int ax = s8 >> 1;
                 if (band_cell(L, x + (ax == 0 ? d : 0), y + (ax == 1 ? d : 0), zl + (ax == 2 ? d : 0)))
@@ -2519,7 +2514,6 @@ static bool use_cluster(int64_t work, int64_t max_items_per_thread) {
 }
 
 static void set_pairs(VankaLists& vl, const VankaPairs& pr) {
-    vl.div64 = env_int("SMG_VANKA_DIV64", 0);
     vl.pairs = pr.pairs;
     for (int m = 0; m < 4; ++m) vl.first[m] = pr.first[m];
 }
