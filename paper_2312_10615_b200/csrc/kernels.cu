@@ -1071,8 +1071,19 @@ __global__ void __launch_bounds__(256) k_vanka_ppk(LevelK L, const double* __res
                                gridDim.x * blockDim.x);
 }
 
+// SMG_VKPP_THREADS / SMG_VKPP_MINB (build-time A/B): launch bounds of the persistent ping-pong
+// sweep.  Its occupancy matters (build A/Bs on one box, cfg 1 solve): 74 -> 94 registers
+// (3 -> 2 CTAs/SM) cost 19.43 vs 18.63 ms; (256, 4) = 64 registers, 4 CTAs/SM: 19.12 -> 18.87 ms.
+// (A 512-thread cooperative CTA, SMG_COOP_THREADS=512, then finds no occupancy and takes the
+// next sweep variant.)
+#ifndef SMG_VKPP_THREADS
+#define SMG_VKPP_THREADS 256
+#endif
+#ifndef SMG_VKPP_MINB
+#define SMG_VKPP_MINB 4
+#endif
 template <int MODE, int CPT>
-__global__ void __launch_bounds__(512) k_vanka_pp(LevelK L, double* __restrict__ XA, double* __restrict__ XB,
+__global__ void __launch_bounds__(SMG_VKPP_THREADS, SMG_VKPP_MINB) k_vanka_pp(LevelK L, double* __restrict__ XA, double* __restrict__ XB,
                                                   const double* __restrict__ B, VankaLists vl,
                                                   const double* __restrict__ ktab, int nu,
                                                   const int32_t* __restrict__ refresh, int64_t nrefresh) {
