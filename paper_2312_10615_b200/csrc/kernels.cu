@@ -314,6 +314,109 @@ __global__ void k_restrict(LevelK F, LevelK C, const double* __restrict__ R, dou
     BC[3 * cfs + c.i] = 0.125 * s;
 }
 
+// z-marching restriction: a thread owns one coarse column (x, y) and walks a segment of
+// coarse planes.  For the u and v faces the tangential-b axis is z, so restrict_face's inner
+// partial acc_a depends on the fine plane only: computed once per fine plane (same
+// operations), it serves coarse planes K and K+1 (fine planes 2K+1, 2K+2 are 2K'-1, 2K' of
+// K' = K+1).  For w the normal axis is z: the 16 values of fine plane 2K+1 are kept in
+// registers for the next coarse plane.  Loads per coarse cell 152 -> 88; every sum is
+// restrict_face's in the same order, so the result is bit-identical to k_restrict.
+// u: normal x, a = y, b = z.  v: normal y, a = x, b = z.
+__device__ __forceinline__ double restrict_partial_a(const double* __restrict__ R, int64_t o, int64_t sn,
+                                                     int64_t sa) {
+    // o = fine slot (normal 2I, a 2J, plane zf); acc_a of restrict_face for that plane
+    const double wI[3] = {0.5, 1.0, 0.5};
+    const double wT[4] = {0.25, 0.75, 0.75, 0.25};
+    double acc_a = 0.0;
+#pragma unroll
+    for (int ia = 0; ia < 4; ++ia) {
+        double sn_ = 0.0;
+#pragma unroll
+        for (int in = 0; in < 3; ++in) sn_ = sn_ + wI[in] * R[o + (ia - 1) * sa + (in - 1) * sn];
+        acc_a = acc_a + wT[ia] * sn_;
+    }
+    return acc_a;
+}
+
+__global__ void __launch_bounds__(256) k_restrict_zm(LevelK F, LevelK C, const double* __restrict__ R,
+                                                     double* __restrict__ BC, int zc_lo, int zc_hi, int zseg) {
+    pdl_wait();
+    const Geom &fg = F.g, &cg = C.g;
+    const int cx = blockIdx.x * BX + threadIdx.x, cy = blockIdx.y * BY + threadIdx.y;
+    if (cx >= cg.nx || cy >= cg.ny) return;
+    const int K0 = zc_lo + blockIdx.z * zseg, K1 = min(K0 + zseg, zc_hi);
+    if (K0 >= K1) return;
+    const int64_t ffs = fg.fs, cfs = cg.fs;
+    const int64_t sx = 1, sy = fg.sy, sz = fg.sz;
+    const double *RU = R, *RV = R + ffs, *RW = R + 2 * ffs, *RP = R + 3 * ffs;
+    const double wI[3] = {0.5, 1.0, 0.5};
+    const double wT[4] = {0.25, 0.75, 0.75, 0.25};
+    // fine slot of (2cx, 2cy, local fine plane 2K) for coarse local plane K
+    auto fbase = [&](int K) { return fg.slot(2 * cx, 2 * cy, 2 * cg.gz(K) - fg.z0); };
+    int64_t fb = fbase(K0);
+    // fine planes 2K-1 and 2K of the first coarse plane
+    double au0 = restrict_partial_a(RU, fb - sz, sx, sy), au1 = restrict_partial_a(RU, fb, sx, sy);
+    double av0 = restrict_partial_a(RV, fb - sz, sy, sx), av1 = restrict_partial_a(RV, fb, sy, sx);
+    double wm[4][4];  // w at fine plane 2K-1: [ib (y)][ia (x)]
+#pragma unroll
+    for (int ib = 0; ib < 4; ++ib)
+#pragma unroll
+        for (int ia = 0; ia < 4; ++ia) wm[ib][ia] = RW[fb - sz + (ib - 1) * sy + (ia - 1) * sx];
+    for (int K = K0; K < K1; ++K) {
+        if (K > K0) fb = fbase(K);
+        const int64_t ci = cg.slot(cx, cy, K);
+        const double au2 = restrict_partial_a(RU, fb + sz, sx, sy), au3 = restrict_partial_a(RU, fb + 2 * sz, sx, sy);
+        const double av2 = restrict_partial_a(RV, fb + sz, sy, sx), av3 = restrict_partial_a(RV, fb + 2 * sz, sy, sx);
+        if (cx >= 1) {
+            double acc_b = 0.0;
+            acc_b = acc_b + wT[0] * au0;
+            acc_b = acc_b + wT[1] * au1;
+            acc_b = acc_b + wT[2] * au2;
+            acc_b = acc_b + wT[3] * au3;
+            BC[ci] = 0.125 * acc_b;
+        }
+        if (cy >= 1) {
+            double acc_b = 0.0;
+            acc_b = acc_b + wT[0] * av0;
+            acc_b = acc_b + wT[1] * av1;
+            acc_b = acc_b + wT[2] * av2;
+            acc_b = acc_b + wT[3] * av3;
+            BC[cfs + ci] = 0.125 * acc_b;
+        }
+        au0 = au2;
+        au1 = au3;
+        av0 = av2;
+        av1 = av3;
+        // w: normal z innermost over fine planes 2K-1 (carried), 2K, 2K+1 (carried on)
+        double acc_b = 0.0;
+#pragma unroll
+        for (int ib = 0; ib < 4; ++ib) {
+            double acc_a = 0.0;
+#pragma unroll
+            for (int ia = 0; ia < 4; ++ia) {
+                const int64_t o = fb + (ib - 1) * sy + (ia - 1) * sx;
+                const double w1 = RW[o], w2 = RW[o + sz];
+                double sn_ = 0.0;
+                sn_ = sn_ + wI[0] * wm[ib][ia];
+                sn_ = sn_ + wI[1] * w1;
+                sn_ = sn_ + wI[2] * w2;
+                acc_a = acc_a + wT[ia] * sn_;
+                wm[ib][ia] = w2;
+            }
+            acc_b = acc_b + wT[ib] * acc_a;
+        }
+        if (cg.gz(K) >= 1) BC[2 * cfs + ci] = 0.125 * acc_b;
+        double s = 0.0;
+#pragma unroll
+        for (int k = 0; k < 2; ++k)
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+#pragma unroll
+                for (int ii = 0; ii < 2; ++ii) s = s + RP[fb + k * sz + j * sy + ii];
+        BC[3 * cfs + ci] = 0.125 * s;
+    }
+}
+
 // Fused residual + restriction: b_c = R (b - L~ x) without materialising the fine
 // residual.  A CTA owns a 16 x 8 tile of coarse cells and marches over a range of
 // coarse planes; the fine residual of the tile's footprint (fine x 2X0-1 .. 2X0+32,
@@ -474,6 +577,115 @@ __global__ void k_prolong_add(LevelK F, LevelK C, const double* __restrict__ E, 
     if (c.y >= 1) X[ffs + c.i] = X[ffs + c.i] + prolong_face<1>(E + cfs, cg, c.x, c.y, z);
     if (z >= 1) X[2 * ffs + c.i] = X[2 * ffs + c.i] + prolong_face<2>(E + 2 * cfs, cg, c.x, c.y, z);
     X[3 * ffs + c.i] = X[3 * ffs + c.i] + E[3 * cfs + cg.slot(c.x >> 1, c.y >> 1, (z >> 1) - cg.z0)];
+}
+
+// z-marching prolongation: a thread owns one fine column (x, y) and walks a segment of fine
+// plane pairs (2K, 2K+1).  For u and v the tangential-b axis is z: prolong_face's
+// sa = 0.75 sn(base) + 0.25 sn(base + da) depends on the coarse plane only (the column fixes
+// da and the normal parity), so it is computed once per coarse plane and reused by the four
+// fine planes 2K-1 .. 2K+2 that reference it.  For w the normal axis is z: the four coarse
+// values of plane K+1 are carried to the next pair; the pressure parent is loaded once per
+// pair.  Same operations in the same order as k_prolong_add: bit-identical.
+template <int COMP>
+__device__ __forceinline__ double prolong_sa(const double* __restrict__ E, int64_t base, int64_t da, int64_t dn,
+                                             bool odd) {
+    auto sn = [&](int64_t o) {
+        double s = 0.0;
+        if (!odd) {
+            s = s + 1.0 * E[o];
+        } else {
+            s = s + 0.5 * E[o];
+            s = s + 0.5 * E[o + dn];
+        }
+        return s;
+    };
+    const double s00 = sn(base), s01 = sn(base + da);
+    double sa = 0.0;
+    sa = sa + 0.75 * s00;
+    sa = sa + 0.25 * s01;
+    return sa;
+}
+
+__global__ void __launch_bounds__(256) k_prolong_zm(LevelK F, LevelK C, const double* __restrict__ E,
+                                                    double* __restrict__ X, int zpairs) {
+    pdl_wait();
+    const Geom &fg = F.g, &cg = C.g;
+    const int x = blockIdx.x * BX + threadIdx.x, y = blockIdx.y * BY + threadIdx.y;
+    if (x >= fg.nx || y >= fg.ny) return;
+    const int zl0 = 2 * blockIdx.z * zpairs, zl1 = min(zl0 + 2 * zpairs, fg.nz);  // local fine planes
+    if (zl0 >= zl1) return;
+    const int64_t ffs = fg.fs, cfs = cg.fs;
+    const double *EU = E, *EV = E + cfs, *EW = E + 2 * cfs, *EP = E + 3 * cfs;
+    const int cx = x >> 1, cy = y >> 1;
+    const int64_t dxs = (x & 1) ? 1 : -1, dys = (y & 1) ? cg.sy : -cg.sy;
+    // coarse local plane of the pair (global fine plane gz(zl0) is even)
+    const int K0 = (fg.gz(zl0) >> 1) - cg.z0;
+    auto cslot = [&](int K) { return cg.slot(cx, cy, K); };
+    // u: normal x (parity x&1), a = y (da = dys).  v: normal y, a = x (da = dxs).
+    const bool ox = x & 1, oy = y & 1;
+    double su_m = prolong_sa<0>(EU, cslot(K0 - 1), dys, 1, ox), su_0 = prolong_sa<0>(EU, cslot(K0), dys, 1, ox);
+    double sv_m = prolong_sa<1>(EV, cslot(K0 - 1), dxs, cg.sy, oy), sv_0 = prolong_sa<1>(EV, cslot(K0), dxs, cg.sy, oy);
+    // w at coarse plane K: legs base, base + da (x), base + db (y), base + db + da
+    double w00 = EW[cslot(K0)], w01 = EW[cslot(K0) + dxs], w10 = EW[cslot(K0) + dys], w11 = EW[cslot(K0) + dys + dxs];
+    for (int zl = zl0, K = K0; zl < zl1; zl += 2, ++K) {
+        const int64_t cb1 = cslot(K + 1);
+        const double su_p = prolong_sa<0>(EU, cb1, dys, 1, ox);
+        const double sv_p = prolong_sa<1>(EV, cb1, dxs, cg.sy, oy);
+        const double n00 = EW[cb1], n01 = EW[cb1 + dxs], n10 = EW[cb1 + dys], n11 = EW[cb1 + dys + dxs];
+        const double ep = EP[cslot(K)];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int z = zl + h;
+            if (z >= zl1) break;
+            const int64_t i = fg.slot(x, y, z);
+            // b = z legs: even fine z -> (K, 3/4), (K-1, 1/4); odd -> (K, 3/4), (K+1, 1/4)
+            if (x >= 1) {
+                double sb = 0.0;
+                sb = sb + 0.75 * su_0;
+                sb = sb + 0.25 * (h ? su_p : su_m);
+                X[i] = X[i] + sb;
+            }
+            if (y >= 1) {
+                double sb = 0.0;
+                sb = sb + 0.75 * sv_0;
+                sb = sb + 0.25 * (h ? sv_p : sv_m);
+                X[ffs + i] = X[ffs + i] + sb;
+            }
+            if (fg.gz(z) >= 1) {
+                // normal z: even -> plane K (weight 1); odd -> K and K+1 (1/2 each)
+                auto sn = [&](double a, double b) {
+                    double s = 0.0;
+                    if (!h) {
+                        s = s + 1.0 * a;
+                    } else {
+                        s = s + 0.5 * a;
+                        s = s + 0.5 * b;
+                    }
+                    return s;
+                };
+                const double s00 = sn(w00, n00), s01 = sn(w01, n01), s10 = sn(w10, n10), s11 = sn(w11, n11);
+                double sb = 0.0;
+                double sa = 0.0;
+                sa = sa + 0.75 * s00;
+                sa = sa + 0.25 * s01;
+                sb = sb + 0.75 * sa;
+                sa = 0.0;
+                sa = sa + 0.75 * s10;
+                sa = sa + 0.25 * s11;
+                sb = sb + 0.25 * sa;
+                X[2 * ffs + i] = X[2 * ffs + i] + sb;
+            }
+            X[3 * ffs + i] = X[3 * ffs + i] + ep;
+        }
+        su_m = su_0;
+        su_0 = su_p;
+        sv_m = sv_0;
+        sv_0 = sv_p;
+        w00 = n00;
+        w01 = n01;
+        w10 = n10;
+        w11 = n11;
+    }
 }
 
 // ------------------------------------------------------------- coarse ------
@@ -2372,7 +2584,21 @@ void launch_restrict(const LevelK& F, const LevelK& C, const double* rf, double*
     dim3 grid = cell_grid(C.g);
     grid.z = nzc < 0 ? C.g.nz : nzc;
     if (grid.z == 0) return;
-    launch_k(k_restrict, grid, dim3(BX, BY), 0, s, F, C, rf, bc, zc_lo);
+    // z-marching variant (SMG_RESTRICT_ZM, default on) when the columns alone leave segments of
+    // >= 2 coarse planes at ~one full-occupancy wave; otherwise one thread per coarse cell
+    const int zm = env_int("SMG_RESTRICT_ZM", 1);
+    const int64_t cols = static_cast<int64_t>(grid.x) * grid.y * BX * BY;
+    const int64_t target = static_cast<int64_t>(num_sms()) * 2048;
+    int nseg = static_cast<int>(std::min<int64_t>(grid.z, (target + cols - 1) / cols));
+    const int force_zseg = env_int("SMG_RESTRICT_ZSEG", 0);  // tests: segment length on every level
+    const int zseg = force_zseg > 0 ? force_zseg : (static_cast<int>(grid.z) + nseg - 1) / nseg;
+    if (zm && zseg >= 2) {
+        nseg = (static_cast<int>(grid.z) + zseg - 1) / zseg;
+        launch_k(k_restrict_zm, dim3(grid.x, grid.y, nseg), dim3(BX, BY), 0, s, F, C, rf, bc, zc_lo,
+                 zc_lo + static_cast<int>(grid.z), zseg);
+    } else {
+        launch_k(k_restrict, grid, dim3(BX, BY), 0, s, F, C, rf, bc, zc_lo);
+    }
     count();
 }
 bool resrestrict_ok(const LevelK& F, const LevelK& C) {
@@ -2398,7 +2624,24 @@ void launch_residual_restrict(const LevelK& F, const LevelK& C, const double* x,
 }
 
 void launch_prolong_add(const LevelK& F, const LevelK& C, const double* xc, double* xf, cudaStream_t s) {
-    launch_k(k_prolong_add, cell_grid(F.g), dim3(BX, BY), 0, s, F, C, xc, xf);
+    // z-marching variant: opt-in (SMG_PROLONG_ZM=1), measured slower than the per-cell kernel
+    // (cfg 3 fine level 2.16 -> 3.9 ms: one marching thread per column keeps too few
+    // read-modify-writes in flight); segments of >= 2 plane pairs, slab starting on an even plane
+    const Geom& fg = F.g;
+    const dim3 g2 = cell_grid(fg);
+    const int pairs = (fg.nz + 1) / 2;
+    const int64_t cols = static_cast<int64_t>(g2.x) * g2.y * BX * BY;
+    const int64_t target = static_cast<int64_t>(num_sms()) * 2048;
+    const int nseg = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(pairs, (target + cols - 1) / cols)));
+    const int force = env_int("SMG_PROLONG_ZPAIRS", 0);  // tests: segment length on every level
+    const int zpairs = force > 0 ? force : (pairs + nseg - 1) / nseg;
+    if (env_int("SMG_PROLONG_ZM", 0) && (force > 0 || zpairs >= 2) && (fg.gz(0) & 1) == 0 && 2 * C.g.nx == fg.nx &&
+        2 * C.g.ny == fg.ny) {
+        launch_k(k_prolong_zm, dim3(g2.x, g2.y, (pairs + zpairs - 1) / zpairs), dim3(BX, BY), 0, s, F, C, xc, xf,
+                 zpairs);
+    } else {
+        launch_k(k_prolong_add, g2, dim3(BX, BY), 0, s, F, C, xc, xf);
+    }
     count();
 }
 void launch_coarse_gemv(const double* ksym, const int32_t* slots, int n, const double* b, double* x,

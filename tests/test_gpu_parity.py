@@ -483,3 +483,49 @@ def test_fused_residual_restrict_bitwise(dims, levels, monkeypatch):
     xg, hg, _, stg = s.sqmr(b, 1e-8, 20)
     assert sto == stg and np.array_equal(ho, hg) and np.array_equal(xo, xg)
     s.close()
+
+
+@pytest.mark.parametrize("zseg", ["1", "2", "3", "5"])
+@pytest.mark.parametrize("dims", [(16, 16, 16), (24, 16, 40)])
+def test_restrict_zmarch_bitwise(dims, zseg, monkeypatch):
+    """z-marching restriction and prolongation (k_restrict_zm / k_prolong_zm: per-plane
+    partials reused across planes, ragged segments) == the oracle's R = P^T/8 and P, bit for
+    bit, on every level."""
+    monkeypatch.setenv("SMG_RESTRICT_ZSEG", zseg)
+    monkeypatch.setenv("SMG_PROLONG_ZPAIRS", zseg)
+    monkeypatch.setenv("SMG_PROLONG_ZM", "1")
+    nx, ny, nz = dims
+    o = oracle.Oracle(nx, ny, nz, h=1 / ny, levels=3)
+    s = smg.Solver(nx, ny, nz, h=1 / ny, levels=3)
+    try:
+        for level in (0, 1):
+            rf = rnd(o.ndof(level), 21 + level)
+            same(s.restrict(rf, level), o.restrict(rf, level))
+            xc = rnd(o.ndof(level + 1), 31 + level)
+            same(s.prolong(xc, level), o.prolong(xc, level))
+        b = rnd(o.ndof(0), 23)
+        same(s.vcycle(b), o.vcycle(b))
+    finally:
+        s.close()
+
+
+def test_restrict_zmarch_matches_per_cell_at_256():
+    """At 256^3 the default transfers march (segments of several planes): same results as
+    the per-cell kernels (SMG_RESTRICT_ZM=0, SMG_PROLONG_ZM=0)."""
+    out = []
+    for zm in ("1", "0"):
+        os.environ["SMG_RESTRICT_ZM"] = zm
+        os.environ["SMG_PROLONG_ZM"] = zm
+        os.environ["SMG_PROLONG_ZPAIRS"] = "0"
+        try:
+            s = smg.Solver(256, levels=6)
+            rf = rnd(s.ndof(0), 29)
+            xc = rnd(s.ndof(1), 30)
+            out.append((s.restrict(rf, 0), s.prolong(xc, 0)))
+            s.close()
+        finally:
+            os.environ.pop("SMG_RESTRICT_ZM", None)
+            os.environ.pop("SMG_PROLONG_ZM", None)
+            os.environ.pop("SMG_PROLONG_ZPAIRS", None)
+    same(out[0][0], out[1][0])
+    same(out[0][1], out[1][1])

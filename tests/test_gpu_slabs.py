@@ -69,3 +69,17 @@ def test_nccl_rank_path_bitwise(monkeypatch):
     assert np.array_equal(h1, h2) and np.array_equal(x1, x2)
     r0.close()
     one.close()
+
+
+@pytest.mark.parametrize("zseg", ["2", "3"])
+def test_restrict_zmarch_slabs_bitwise(zseg, monkeypatch):
+    """z-marching restriction and prolongation on slab parts (local plane ranges, ghost planes) == one part."""
+    monkeypatch.setenv("SMG_RESTRICT_ZSEG", zseg)
+    monkeypatch.setenv("SMG_PROLONG_ZPAIRS", zseg)
+    monkeypatch.setenv("SMG_PROLONG_ZM", "1")
+    one = smg.Solver(32, levels=3)
+    many = smg.Solver(32, levels=3, devices=[0, 0])
+    b = np.random.default_rng(7).uniform(-1, 1, one.ndof())
+    assert np.array_equal(many.vcycle(b), one.vcycle(b))
+    one.close()
+    many.close()
