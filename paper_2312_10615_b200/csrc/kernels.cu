@@ -1759,6 +1759,26 @@ __device__ __forceinline__ BlkIdx blk_idx(bool rev) {
 }
 constexpr int kRevBit = 1 << 16;
 
+// Chunked velocity pair: one launch updates colour c0 on planes [za0, za1) and colour c0^1 on
+// planes [zb0, zb1) (disjoint ranges one chunk apart, so neither reads what the other writes).
+// The host walks the level in chunks of C planes: launch j = first colour on chunk j + second
+// colour on chunk j-2.  Second-colour cells of chunk k read first-colour values of chunks k-1..k+1
+// (done in launches <= k+1) and first-colour cells of chunk j read second-colour values of chunk
+// j-1 still untouched (updated in launch j+1): exactly the values the two whole-level phases see,
+// so the result is bit-identical, while the second colour finds its planes in L2.
+__global__ void __launch_bounds__(256) k_dgs_vel_chunk(LevelK L, double* __restrict__ X, const double* __restrict__ B,
+                                                       int c0, int za0, int za1, int zb0) {
+    pdl_wait();
+    const Geom& g = L.g;
+    const int na = za1 - za0;
+    const bool first = static_cast<int>(blockIdx.z) < na;
+    const int z = first ? za0 + static_cast<int>(blockIdx.z) : zb0 + static_cast<int>(blockIdx.z) - na;
+    const int colour = first ? c0 : (c0 ^ 1);
+    const int i = blockIdx.x * 32 + threadIdx.x, y = blockIdx.y * 8 + threadIdx.y;
+    const int x = 2 * i + ((y + g.gz(z) + colour) & 1);
+    if (x < g.nx && y < g.ny) dgs_vel_cell(L, X, B, x, y, z);
+}
+
 // ZC independent cells per thread (planes z, z + gridDim.z, ...): more loads in flight
 template <int ZC>
 __global__ void __launch_bounds__(256) k_dgs_vel_c(LevelK L, double* __restrict__ X, const double* __restrict__ B,
@@ -3031,6 +3051,28 @@ static void launch_vel2(const LevelK& L, const double* xi, double* xo, const dou
     count();
 }
 
+// Velocity pair in chunks of C planes (SMG_VEL_CHUNK=C): nz/C + 2 launches, see k_dgs_vel_chunk.
+static int vel_chunk(const LevelK& L) {
+    const int64_t ncell = static_cast<int64_t>(L.g.nx) * L.g.ny * L.g.nz;
+    const int c = env_int("SMG_VEL_CHUNK", 0);
+    if (c <= 0 || L.g.z0 != 0 || L.g.nz != L.g.gnz) return 0;
+    return ncell >= env_int("SMG_VEL_CHUNK_MIN_CELLS", 1 << 24) ? c : 0;
+}
+static void launch_vel_pair_chunked(const LevelK& L, double* x, const double* b, int c0, int C, cudaStream_t s) {
+    const Geom& g = L.g;
+    const dim3 gv = dgs_grid_v(g);
+    const int nch = (g.nz + C - 1) / C;
+    for (int j = 0; j < nch + 2; ++j) {
+        const int za0 = j < nch ? j * C : 0, za1 = j < nch ? std::min(g.nz, (j + 1) * C) : 0;
+        const int k = j - 2;
+        const int zb0 = k >= 0 ? k * C : 0, zb1 = k >= 0 ? std::min(g.nz, (k + 1) * C) : 0;
+        const int nz = (za1 - za0) + (zb1 - zb0);
+        if (nz == 0) continue;
+        launch_k(k_dgs_vel_chunk, dim3(gv.x, gv.y, nz), dim3(32, 8), 0, s, L, x, b, c0, za0, za1, zb0);
+        count();
+    }
+}
+
 // Opt-in (SMG_VEL2=1): the velocity pairs at both ends of a symmetric sweep run fused
 // (k_dgs_vel2) when the level has a second vector xb: the forward pair writes xb, the pressure
 // steps run in xb, the reverse pair writes back into x (bit-identical).  Measured slower than
@@ -3055,9 +3097,12 @@ static void dgs_sym_phases_zc(const LevelK& L, double* x, const double* b, doubl
     const int alt = env_int("SMG_DGS_ALT", 1) ? kRevBit : 0;
     const bool fuse = vel2_on(L, xb, nph);
     double* xp = x;  // where the pressure steps run
+    const int vch = fuse ? 0 : vel_chunk(L);
     if (fuse) {
         launch_vel2(L, x, xb, b, 0, s);
         xp = xb;
+    } else if (vch) {
+        launch_vel_pair_chunked(L, x, b, 0, vch, s);
     } else {
         launch_k(k_dgs_vel_c<ZC>, gv, blk, 0, s, L, x, b, 0);
         launch_k(k_dgs_vel_c<ZC>, gv, blk, 0, s, L, x, b, 1 | alt);
@@ -3074,6 +3119,8 @@ static void dgs_sym_phases_zc(const LevelK& L, double* x, const double* b, doubl
     for (int k = 0; k < 4; ++k) count();
     if (fuse) {
         launch_vel2(L, xb, x, b, 1, s);
+    } else if (vch) {
+        launch_vel_pair_chunked(L, x, b, 1, vch, s);
     } else {
         launch_k(k_dgs_vel_c<ZC>, gv, blk, 0, s, L, x, b, 1 | alt);
         launch_k(k_dgs_vel_c<ZC>, gv, blk, 0, s, L, x, b, 0);

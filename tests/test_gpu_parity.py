@@ -529,3 +529,25 @@ def test_restrict_zmarch_matches_per_cell_at_256():
             os.environ.pop("SMG_PROLONG_ZPAIRS", None)
     same(out[0][0], out[1][0])
     same(out[0][1], out[1][1])
+
+
+@pytest.mark.parametrize("chunk", ["1", "2", "3", "5"])
+@pytest.mark.parametrize("dims,levels", [((32, 32, 32), 3), ((48, 40, 24), 3)])
+def test_velocity_pair_chunked_bitwise(dims, levels, chunk, monkeypatch):
+    """Chunked velocity pair (k_dgs_vel_chunk: first colour on chunk j with the second colour on
+    chunk j-2 in one launch) == the two whole-level colour phases, bit for bit: symmetric DGS,
+    smooth and V-cycle, and the oracle's DGS sweep."""
+    nx, ny, nz = dims
+    x = np.random.default_rng(nx + ny).uniform(-1, 1, smg.ndof_box(nx, ny, nz))
+    b = np.random.default_rng(nz).uniform(-1, 1, smg.ndof_box(nx, ny, nz))
+    out = []
+    for c in ("0", chunk):
+        monkeypatch.setenv("SMG_VEL_CHUNK", c)
+        monkeypatch.setenv("SMG_VEL_CHUNK_MIN_CELLS", "0")
+        s = smg.Solver(nx, ny, nz, h=1 / ny, levels=levels)
+        out.append((s.smoother(smg.OP_DGS_SYM, x, b), s.smoother(smg.OP_SMOOTH, x, b), s.vcycle(b)))
+        s.close()
+    for a, c in zip(out[1], out[0]):
+        same(a, c)
+    o = oracle.Oracle(nx, ny, nz, h=1 / ny, levels=levels)
+    same(out[1][0], o.smoother(1, x, b, 0))  # oracle op 1: symmetric DGS
