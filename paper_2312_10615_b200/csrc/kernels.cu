@@ -322,6 +322,12 @@ __global__ void k_restrict(LevelK F, LevelK C, const double* __restrict__ R, dou
 // registers for the next coarse plane.  Loads per coarse cell 152 -> 88; every sum is
 // restrict_face's in the same order, so the result is bit-identical to k_restrict.
 // u: normal x, a = y, b = z.  v: normal y, a = x, b = z.
+// build-time A/B: CTAs per SM the register allocation of k_restrict_zm targets.  4 (64 registers, no
+// spill) measured slower than the free allocation (80 registers, 3 CTAs/SM): cfg 3 fine restrict
+// 1.27 -> 1.65 ms (profiles/r1s5_rzm4_ab.txt)
+#ifndef SMG_RZM_MINB
+#define SMG_RZM_MINB 1
+#endif
 __device__ __forceinline__ double restrict_partial_a(const double* __restrict__ R, int64_t o, int64_t sn,
                                                      int64_t sa) {
     // o = fine slot (normal 2I, a 2J, plane zf); acc_a of restrict_face for that plane
@@ -338,7 +344,7 @@ __device__ __forceinline__ double restrict_partial_a(const double* __restrict__ 
     return acc_a;
 }
 
-__global__ void __launch_bounds__(256) k_restrict_zm(LevelK F, LevelK C, const double* __restrict__ R,
+__global__ void __launch_bounds__(256, SMG_RZM_MINB) k_restrict_zm(LevelK F, LevelK C, const double* __restrict__ R,
                                                      double* __restrict__ BC, int zc_lo, int zc_hi, int zseg) {
     pdl_wait();
     const Geom &fg = F.g, &cg = C.g;
