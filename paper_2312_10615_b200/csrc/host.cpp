@@ -265,6 +265,12 @@ struct smg_ctx {
     cudaGraphExec_t graph = nullptr;  // one SQMR iteration
     int64_t graph_kernels = 0;
     bool graph_captured_now = false;
+    // device-side SQMR loop: a WHILE conditional node around the iteration + k_sqmr_loop_ctl
+    cudaGraphExec_t loop_graph = nullptr;
+    bool loop_failed = false;
+    int* dloop = nullptr;                  // {iterations, maxit, last code}
+    double* dhist = nullptr;               // rel per iteration (kLoopCap)
+    unsigned long long* dstamp = nullptr;  // globaltimer: [0] loop start, [j] iteration j
     std::string err;
     smg_timing timing{};
     std::vector<void*> allocs;
@@ -301,6 +307,7 @@ struct smg_ctx {
         for (void* p : allocs) cudaFree(p);
         if (hscal) cudaFreeHost(hscal);
         if (graph) cudaGraphExecDestroy(graph);
+        if (loop_graph) cudaGraphExecDestroy(loop_graph);
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);
         if (comm) nccl().commDestroy(comm);
@@ -816,6 +823,55 @@ void sqmr_iteration(smg_ctx* c) {
     launch_xpby_dev(c->q, t, sc, n, c->st);                              // q = t + beta q
 }
 
+// Device-side loop (opt-in, SMG_DEVICE_LOOP=1): one graph launch runs every iteration; the host
+// no longer syncs, reads (rel, status) and relaunches the iteration graph per iteration.  Built on
+// first use; any failure falls back to the host loop for the context's lifetime.  Bit-identical
+// (same kernels, same order), but measured neutral on cfg 1 (18.85 ms host loop vs 18.89 ms,
+// profiles/r1s5_devloop_cfg1.txt): the per-iteration sync and relaunch were already hidden.
+constexpr int kLoopCap = 1 << 16;
+static bool build_loop_graph(smg_ctx* c) {
+    if (c->loop_graph) return true;
+    if (c->loop_failed || env_int("SMG_DEVICE_LOOP", 0) == 0) return false;
+    cudaGraph_t g = nullptr;
+    bool ok = false;
+    do {
+        if (!c->dloop) {
+            c->dloop = c->dalloc<int>(4);
+            c->dhist = c->dalloc<double>(kLoopCap);
+            c->dstamp = c->dalloc<unsigned long long>(kLoopCap + 1);
+        }
+        if (cudaGraphCreate(&g, 0) != cudaSuccess) break;
+        cudaGraphConditionalHandle h;
+        if (cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault) != cudaSuccess) break;
+        cudaGraphNodeParams p = {};
+        p.type = cudaGraphNodeTypeConditional;
+        p.conditional.handle = h;
+        p.conditional.type = cudaGraphCondTypeWhile;
+        p.conditional.size = 1;
+        cudaGraphNode_t node;
+        if (cudaGraphAddNode(&node, g, nullptr, 0, &p) != cudaSuccess) break;
+        cudaGraph_t body = p.conditional.phGraph_out[0];
+        if (cudaStreamBeginCaptureToGraph(c->st, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed) !=
+            cudaSuccess)
+            break;
+        sqmr_iteration(c);
+        launch_sqmr_loop_ctl(h, c->dscal, c->dhist, c->dstamp, c->dloop, c->st);
+        cudaGraph_t out = nullptr;
+        const cudaError_t ec = cudaStreamEndCapture(c->st, &out);
+        if (ec != cudaSuccess || take_launch_error() != 0) break;
+        if (cudaGraphInstantiate(&c->loop_graph, g, 0) != cudaSuccess) break;
+        ok = true;
+    } while (false);
+    if (g) cudaGraphDestroy(g);
+    if (!ok) {
+        c->loop_failed = true;
+        c->loop_graph = nullptr;
+        cudaGetLastError();  // clear the sticky-free error of the failed build
+        std::fprintf(stderr, "smg: device-side SQMR loop unavailable, using the host loop\n");
+    }
+    return ok;
+}
+
 int sqmr(smg_ctx* c, double tol, int maxit, smg_history* hist, int* status) {
     DevLevel& F = c->lv[0];
     const int64_t n = vlen(F);
@@ -862,7 +918,44 @@ int sqmr(smg_ctx* c, double tol, int maxit, smg_history* hist, int* status) {
             c->graph_kernels = launch_count() - before;
             c->graph_captured_now = true;
         }
-        for (int j = 1; j <= maxit && st == SMG_MAX_ITERATIONS; ++j) {
+        const int64_t lc0 = launch_count();
+        const bool dev_loop = st == SMG_MAX_ITERATIONS && maxit > 0 && maxit <= kLoopCap && build_loop_graph(c);
+        const int64_t loop_capture = launch_count() - lc0;  // launches recorded while building (not run)
+        if (dev_loop) {
+            const double t_start = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+            int h4[4] = {0, maxit, 0, 0};
+            static_assert(sizeof(h4) <= 4 * sizeof(double), "pinned scratch");
+            std::memcpy(&c->hscal[4], h4, sizeof(h4));
+            CK(cudaMemcpyAsync(c->dloop, &c->hscal[4], sizeof(h4), cudaMemcpyHostToDevice, c->st));
+            launch_stamp(c->dstamp, c->st);
+            CK(cudaGraphLaunch(c->loop_graph, c->st));
+            if (const int e = take_launch_error())
+                throw SmgError(SMG_ECUDA, std::string("kernel launch rejected: ") +
+                                              cudaGetErrorString(static_cast<cudaError_t>(e)));
+            CK(cudaMemcpyAsync(&c->hscal[4], c->dloop, sizeof(h4), cudaMemcpyDeviceToHost, c->st));
+            CK(cudaStreamSynchronize(c->st));
+            std::memcpy(h4, &c->hscal[4], sizeof(h4));
+            iters = h4[0];
+            const int code = h4[2];
+            std::vector<double> rel(iters);
+            std::vector<unsigned long long> stamp(iters + 1);
+            if (iters > 0) {
+                CK(cudaMemcpy(rel.data(), c->dhist, iters * sizeof(double), cudaMemcpyDeviceToHost));
+                CK(cudaMemcpy(stamp.data(), c->dstamp, (iters + 1) * sizeof(unsigned long long),
+                              cudaMemcpyDeviceToHost));
+            }
+            for (int j = 0; j < iters && hist && hist->count < hist->capacity; ++j) {
+                hist->rel_residual[hist->count] = rel[j];
+                hist->seconds[hist->count] = t_start + 1e-9 * static_cast<double>(stamp[j + 1] - stamp[0]);
+                hist->count++;
+            }
+            graph_launches += static_cast<int64_t>(iters + (code == 2 ? 1 : 0)) * (c->graph_kernels + 1);
+            // eager-launch accounting below subtracts the capture-time launches of this call
+            graph_launches -= loop_capture;
+            if (code == 2 || code == 3) st = SMG_BREAKDOWN;
+            else if (code == 1) st = SMG_CONVERGED;
+        }
+        for (int j = 1; !dev_loop && j <= maxit && st == SMG_MAX_ITERATIONS; ++j) {
             CK(cudaGraphLaunch(c->graph, c->st));
             graph_launches += c->graph_kernels;
             if (const int e = take_launch_error())

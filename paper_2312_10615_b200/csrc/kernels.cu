@@ -3272,6 +3272,42 @@ void launch_vanka_additive(const LevelK& L, double* x, const double* b, const in
     count();
 }
 
+// Device-side SQMR loop (the body of a WHILE conditional graph node, after one captured
+// iteration): records rel into the device history with a globaltimer stamp and keeps the loop
+// running while the status code is 0 and fewer than loop[1] (maxit) iterations ran.  Mirrors the
+// host loop: code 2 (sigma breakdown) records nothing; codes 1 / 3 record the iteration and stop.
+// loop = {iterations, maxit, last code}.
+__global__ void k_sqmr_loop_ctl(cudaGraphConditionalHandle h, const double* __restrict__ sc, double* hist,
+                                unsigned long long* stamp, int* loop) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    const int code = static_cast<int>(sc[S_STATUS]);
+    loop[2] = code;
+    if (code == 2) {
+        cudaGraphSetConditional(h, 0u);
+        return;
+    }
+    const int j = loop[0] + 1;
+    hist[j - 1] = sc[S_REL];
+    stamp[j] = t;
+    loop[0] = j;
+    cudaGraphSetConditional(h, (code == 0 && j < loop[1]) ? 1u : 0u);
+}
+__global__ void k_stamp(unsigned long long* stamp) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    stamp[0] = t;
+}
+void launch_sqmr_loop_ctl(cudaGraphConditionalHandle h, const double* sc, double* hist, unsigned long long* stamp,
+                          int* loop, cudaStream_t s) {
+    k_sqmr_loop_ctl<<<1, 1, 0, s>>>(h, sc, hist, stamp, loop);
+    count();
+}
+void launch_stamp(unsigned long long* stamp, cudaStream_t s) {
+    k_stamp<<<1, 1, 0, s>>>(stamp);
+    count();
+}
+
 void launch_sqmr_scalar(int which, double* sc, cudaStream_t s) {
     switch (which) {
         case 0: launch_k(k_sqmr_first, 1, 1, 0, s, sc); break;

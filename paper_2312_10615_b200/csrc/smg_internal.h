@@ -171,6 +171,9 @@ enum SqmrSlot {
 // which: 0 first (tau, rho from the initial dots), 1 alpha, 2 nu/c/tau/cd/cq, 3 rel/convergence/beta.
 // status slot: 0 running, 1 converged, 2 breakdown before the residual (sigma), 3 breakdown after it (rho).
 void launch_sqmr_scalar(int which, double* sc, cudaStream_t s);
+void launch_sqmr_loop_ctl(cudaGraphConditionalHandle h, const double* sc, double* hist, unsigned long long* stamp,
+                          int* loop, cudaStream_t s);
+void launch_stamp(unsigned long long* stamp, cudaStream_t s);
 // One additive Vanka application over all n band blocks (any order);
 // d7: scratch of 7 fields (g.fs each).  Bit-identical to the oracle's fixed order.
 void launch_vanka_additive(const LevelK& L, double* x, const double* b, const int32_t* cells, const uint8_t* masks,

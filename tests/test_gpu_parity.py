@@ -551,3 +551,23 @@ def test_velocity_pair_chunked_bitwise(dims, levels, chunk, monkeypatch):
         same(a, c)
     o = oracle.Oracle(nx, ny, nz, h=1 / ny, levels=levels)
     same(out[1][0], o.smoother(1, x, b, 0))  # oracle op 1: symmetric DGS
+
+
+@pytest.mark.parametrize("maxit", [500, 2])
+def test_device_loop_matches_host_loop(maxit, monkeypatch):
+    """Device-side SQMR loop (WHILE conditional graph node, SMG_DEVICE_LOOP=1) == the host loop:
+    same residual history, status and solution, bit for bit (also when maxit stops it)."""
+    res = []
+    for dl in ("0", "1"):
+        monkeypatch.setenv("SMG_DEVICE_LOOP", dl)
+        s = smg.Solver(32, levels=3)
+        x, h, _, st = s.sqmr(smg.forcing(32, seed=5), 1e-8, maxit)
+        res.append((x, np.asarray(h), st))
+        s.close()
+    assert res[0][2] == res[1][2]
+    assert np.array_equal(res[0][1], res[1][1])
+    assert np.array_equal(res[0][0], res[1][0])
+    if maxit == 2:
+        assert res[1][2] == smg.SMG_MAX_ITERATIONS and len(res[1][1]) == 2
+    else:
+        assert res[1][2] == smg.SMG_CONVERGED
