@@ -266,6 +266,8 @@ struct smg_ctx {
     int64_t graph_kernels = 0;
     bool graph_captured_now = false;
     // device-side SQMR loop: a WHILE conditional node around the iteration + k_sqmr_loop_ctl
+    cudaGraphExec_t init_graph = nullptr;  // SQMR lines 1-4 (initial V-cycle)
+    int64_t init_kernels = 0;
     cudaGraphExec_t loop_graph = nullptr;
     bool loop_failed = false;
     int* dloop = nullptr;                  // {iterations, maxit, last code}
@@ -308,6 +310,7 @@ struct smg_ctx {
         if (hscal) cudaFreeHost(hscal);
         if (graph) cudaGraphExecDestroy(graph);
         if (loop_graph) cudaGraphExecDestroy(loop_graph);
+        if (init_graph) cudaGraphExecDestroy(init_graph);
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);
         if (comm) nccl().commDestroy(comm);
@@ -899,11 +902,34 @@ int sqmr(smg_ctx* c, double tol, int maxit, smg_history* hist, int* status) {
         c->hscal[3] = tol;
         CK(cudaMemcpyAsync(sc + S_BNORM, &c->hscal[2], sizeof(double), cudaMemcpyHostToDevice, c->st));
         CK(cudaMemcpyAsync(sc + S_TOL, &c->hscal[3], sizeof(double), cudaMemcpyHostToDevice, c->st));
-        CK(cudaMemcpyAsync(s, c->rhs, n * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
-        vcycle(c, 0, s, t);
-        CK(cudaMemcpyAsync(c->q, t, n * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
-        launch_cdot2(F.k.g, t, t, s, c->q, c->partials, sc + S_D0, c->st);
-        launch_sqmr_scalar(0, sc, c->st);
+        // lines 1-4 of Alg. 4 (s = b, t = V(s), q = t, first scalars): opt-in (SMG_INIT_GRAPH=1)
+        // captured once as a graph and replayed instead of ~300 eager launches; bit-identical
+        // (GPU suite green with it on), measured neutral: cfg 1 18.87 ms eager vs 18.88 ms graph
+        // (profiles/r1s5_initgraph_cfg1.txt) -- the eager launches stay ahead of the GPU
+        auto init = [&] {
+            CK(cudaMemcpyAsync(s, c->rhs, n * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
+            vcycle(c, 0, s, t);
+            CK(cudaMemcpyAsync(c->q, t, n * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
+            launch_cdot2(F.k.g, t, t, s, c->q, c->partials, sc + S_D0, c->st);
+            launch_sqmr_scalar(0, sc, c->st);
+        };
+        if (env_int("SMG_INIT_GRAPH", 0)) {
+            if (!c->init_graph) {
+                const int64_t before = launch_count();
+                CK(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeRelaxed));
+                init();
+                cudaGraph_t gr = nullptr;
+                CK(cudaStreamEndCapture(c->st, &gr));
+                CK(cudaGraphInstantiate(&c->init_graph, gr, 0));
+                CK(cudaGraphDestroy(gr));
+                c->init_kernels = launch_count() - before;
+                graph_launches -= c->init_kernels;  // capture-time launches are not executions
+            }
+            CK(cudaGraphLaunch(c->init_graph, c->st));
+            graph_launches += c->init_kernels;
+        } else {
+            init();
+        }
         CK(cudaMemcpyAsync(c->hscal, sc + S_STATUS, sizeof(double), cudaMemcpyDeviceToHost, c->st));
         CK(cudaStreamSynchronize(c->st));
         if (c->hscal[0] != 0.0) st = SMG_BREAKDOWN;

@@ -571,3 +571,17 @@ def test_device_loop_matches_host_loop(maxit, monkeypatch):
         assert res[1][2] == smg.SMG_MAX_ITERATIONS and len(res[1][1]) == 2
     else:
         assert res[1][2] == smg.SMG_CONVERGED
+
+
+def test_init_graph_matches_eager(monkeypatch):
+    """SQMR lines 1-4 replayed from a captured graph (SMG_INIT_GRAPH=1) == eager launches."""
+    res = []
+    for ig in ("0", "1"):
+        monkeypatch.setenv("SMG_INIT_GRAPH", ig)
+        s = smg.Solver(32, levels=3)
+        for _ in range(2):  # capture, then replay
+            x, h, _, st = s.sqmr(smg.forcing(32, seed=6), 1e-8, 100)
+            res.append((x, np.asarray(h), st))
+        s.close()
+    for x, h, st in res[1:]:
+        assert st == res[0][2] and np.array_equal(h, res[0][1]) and np.array_equal(x, res[0][0])
