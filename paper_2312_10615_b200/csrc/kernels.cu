@@ -2173,7 +2173,13 @@ __global__ void __launch_bounds__(256) k_dgs_pf_flush(LevelK L, double* __restri
 }
 
 template <int ZC>
-__global__ void __launch_bounds__(256) k_dgs_prev_c(LevelK L, double* __restrict__ X, const double* __restrict__ B,
+// build-time A/B: CTAs per SM the register allocation of k_dgs_prev_c targets.  The free allocation
+// (104 registers, 2 CTAs/SM) measured best: 3 (80 registers, no spill) cfg 3 fine DGS sweep
+// 20.74 -> 20.88 ms, 4 (64 registers, spills) 20.78 -> 21.44 ms (profiles/r1s5_prev_minb_ab.txt)
+#ifndef SMG_PREV_MINB
+#define SMG_PREV_MINB 1
+#endif
+__global__ void __launch_bounds__(256, SMG_PREV_MINB) k_dgs_prev_c(LevelK L, double* __restrict__ X, const double* __restrict__ B,
                                                     int grp) {
     pdl_wait();
     const Geom& g = L.g;
