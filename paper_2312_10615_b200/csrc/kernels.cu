@@ -3144,9 +3144,11 @@ static void dgs_sym_phases_zc(const LevelK& L, double* x, const double* b, doubl
 static void launch_dgs_sym_phases(const LevelK& L, double* x, const double* b, double* d0, double* d1, int nph,
                                   cudaStream_t s, double* xb) {
     (void)d1;
-    // two cells per thread only pays on the largest levels (>= 128^3 cells); smaller levels need blocks
-    const int64_t ncell = static_cast<int64_t>(L.g.nx) * L.g.ny * L.g.nz;
-    const int zc = env_int("SMG_DGS_ZC", ncell >= (int64_t(1) << 21) ? 2 : 1);
+    // one cell per thread on every level (SMG_DGS_ZC=2/4: two/four z-planes per thread).  Two cells
+    // per thread on levels >= 128^3 was the default until re-measured in session 5 (interleaved on
+    // one box, profiles/r1s5_zc_*.txt): ZC 1 vs 2 cfg 1 solve 18.49 vs 18.63-19.40 ms, cfg 3
+    // iteration 67.5 vs 68.3 ms, cfg 2 9.29 vs 9.39 ms, cfg 4 33.33 vs 33.69 ms
+    const int zc = env_int("SMG_DGS_ZC", 1);
     if (zc >= 4) dgs_sym_phases_zc<4>(L, x, b, d0, nph, s, xb);
     else if (zc == 2) dgs_sym_phases_zc<2>(L, x, b, d0, nph, s, xb);
     else dgs_sym_phases_zc<1>(L, x, b, d0, nph, s, xb);
