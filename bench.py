@@ -1,14 +1,22 @@
 """bench.py — MG-preconditioned SQMR Stokes solve on B200 (BASELINE.json metric).
 
 One "step" = one full MG-SQMR solve of the BASELINE config to its tolerance
-(cfg 1 by default: 128^3 cube, 5-level V-cycle, iid U[-1,1] forcing seed 1,
-tol 1e-6).  Metric: DOF/s = N * iterations / T_solve, plus
-time-to-1e-6 (ms_per_step) and the HBM roofline of the dominant kernel.
+(cfg 2 by default -- the config the metric's 1/2/4/8-GPU series is quoted on:
+256^3 cube, 6-level V-cycle, 8 Fourier modes seed 2, tol 1e-6).  Metric: DOF/s =
+N * iterations / T_solve, plus time-to-1e-6 (ms_per_step) and
+the HBM roofline of the dominant kernel.  By default the line also carries a
+device-resident cfg-3 (512^3) measurement under "also".
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 1]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 2]
 
---impl reference times the CPU implementation of the path (the oracle port —
+--impl reference times the CPU implementation of the path (the oracle port --
 the reference ships no solver) on the host cores.
+
+CPU numbers (cpu_baseline and the reference arm) time the oracle on a bounded
+sample: the Alg. 4 setup (lines 1-4, one V-cycle) and two SQMR iterations,
+separately, then report DOF/s for the config's whole solve, N * K / (t_init + K
+t_iter), with K the iteration count of the committed golden history -- the
+same quantity the GPU line reports.
 Under torchrun (N > 1) every rank builds its own z-slab of the same config on
 its GPU (smg_create_rank: one process per GPU, halo planes by
 NCCL send/recv after every smoother phase, inner-product plane partials by one
@@ -149,18 +157,48 @@ def share_nccl_id(ws, rank):
     return obj[0]
 
 
-def cpu_sample(cfg, threads, iters=2):
-    """Oracle port on host cores: `iters` MG-SQMR iterations of the config (bounded sample)."""
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def golden_iterations(cfg):
+    """Iterations to tolerance of the committed oracle history (tests/golden), else None."""
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", f"cfg{cfg}_history.json")) as f:
+            g = json.load(f)
+        return int(g["iterations"]) if g.get("status") == 0 else None
+    except (OSError, ValueError, KeyError):
+        return None
+
+
+def cpu_sample(cfg, threads, iters=2, oracle_obj=None):
+    """Oracle port on `threads` host cores, bounded sample of the config: Alg. 4 lines 1-4 (the
+    initial V-cycle) and `iters` SQMR iterations, timed apart (the per-iteration time excludes
+    the setup).  Returns (t_init, t_iter, iterations sampled, wall seconds)."""
     import oracle
 
     nx, ny, nz, h, lv, kind, seed, tol, _ = CONFIGS[cfg]
     oracle.set_threads(threads)
-    o = oracle.Oracle(nx, ny, nz, h=h, levels=lv)
+    o = oracle_obj or oracle.Oracle(nx, ny, nz, h=h, levels=lv)
     b = oracle.forcing_box(nx, ny, nz, h, kind, seed)
     t0 = time.perf_counter()
-    _, hist, _, _ = o.sqmr(b, tol=1e-300, maxit=iters)
+    _, hist, secs, _ = o.sqmr(b, tol=1e-300, maxit=iters + 1)
     dt = time.perf_counter() - t0
-    return o, b, len(hist), dt
+    k = len(hist)
+    t_it = (secs[-1] - secs[0]) / max(k - 1, 1)  # iterations 2..k: no setup inside
+    t_init = max(secs[0] - t_it, 0.0)
+    return t_init, t_it, k - 1, dt
+
+
+def cpu_dofs(cfg, t_init, t_it, k_solve):
+    nx, ny, nz = CONFIGS[cfg][:3]
+    return ndof(nx, ny, nz) * k_solve / (t_init + k_solve * t_it)
 
 
 def run_reference(args, ws, rank):
@@ -174,24 +212,27 @@ def run_reference(args, ws, rank):
 
     oracle.set_threads(threads)
     o = oracle.Oracle(nx, ny, nz, h=h, levels=lv)
-    b = oracle.forcing_box(nx, ny, nz, h, kind, seed)
-    iters = args.ref_iters
+    k_solve = golden_iterations(cfg) or 10
     for _ in range(args.warmup):
-        o.sqmr(b, tol=1e-300, maxit=1)
-    t0 = time.perf_counter()
-    tot_it = 0
+        cpu_sample(cfg, threads, 1, o)
+    t_init = t_it = wall = 0.0
     for _ in range(args.steps):
-        _, hist, _, _ = o.sqmr(b, tol=1e-300, maxit=iters)
-        tot_it += len(hist)
-    dt = time.perf_counter() - t0
-    val = n * tot_it / dt
+        ti, tt, _, dt = cpu_sample(cfg, threads, args.ref_iters, o)
+        t_init += ti / args.steps
+        t_it += tt / args.steps
+        wall += dt
+    val = cpu_dofs(cfg, t_init, t_it, k_solve)
+    sample = (f"per step: Alg. 4 setup (1 V-cycle) + {args.ref_iters} MG-SQMR iterations of {name}, timed apart; "
+              f"value = N K / (t_setup + K t_iter) with K = {k_solve} (committed golden), "
+              f"oracle/stokes_oracle.cpp on {threads} threads, {cpu_model()}")
     line = {
         "impl": "reference", "metric": "MG-SQMR DOF/s (N x iterations / T_solve)", "value": val, "unit": "DOF/s",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * wall / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": name, "N_dof": n, "sample": f"{iters} SQMR iterations per step"},
-        "cpu_baseline": {"value": val, "unit": "DOF/s", "cores": threads, "kind": "port",
-                         "sample": f"{iters} MG-SQMR iterations of {name} per step, oracle/stokes_oracle.cpp"},
+        "config": {"workload": name, "N_dof": n, "sample": sample, "t_setup_s": t_init, "t_iter_s": t_it,
+                   "iterations_per_solve": k_solve, "time_to_tol_ms": 1e3 * (t_init + k_solve * t_it)},
+        "cpu_baseline": {"value": val, "unit": "DOF/s", "cores": threads, "kind": "port", "cpu": cpu_model(),
+                         "sample": sample},
         "e2e": {"value": val, "unit": "DOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -257,13 +298,29 @@ def run_ours(args, ws, rank, local):
     roof = roofline(s, lv, peak, peak_kind, dev_ms / max(iters, 1), f"cfg{args.config}",
                     share=1.0 / ws if slabs and not emulate else 1.0)
     out = None
+    also = {}
+    if ws == 1 and args.also:
+        for c in [int(v) for v in args.also.split(",") if v.strip()]:
+            if c != args.config:
+                also[f"cfg{c}"] = measure_resident(smg, c, 2)
     if rank == 0:
         cpu = None
         if not args.no_cpu_baseline:
             th = os.cpu_count() or 1
-            _, _, it, dt = cpu_sample(cfg, th, args.ref_iters)
-            cpu = {"value": n * it / dt, "unit": "DOF/s", "cores": th, "kind": "port",
-                   "sample": f"{it} MG-SQMR iterations of {name}, oracle/stokes_oracle.cpp, {dt:.1f} s"}
+            k_solve = iters / args.steps
+            ti, tt, it, dt = cpu_sample(cfg, th, args.ref_iters)
+            cpu = {"value": cpu_dofs(cfg, ti, tt, k_solve), "unit": "DOF/s", "cores": th, "kind": "port",
+                   "cpu": cpu_model(),
+                   "sample": f"Alg. 4 setup + {it} MG-SQMR iterations of {name} timed apart "
+                             f"(setup {ti:.2f} s, {tt:.2f} s/iteration), extrapolated to this solve's "
+                             f"{k_solve:g} iterations; oracle/stokes_oracle.cpp, {dt:.1f} s wall",
+                   "t_setup_s": ti, "t_iter_s": tt}
+            if args.cpu_1thread:  # single-thread reference point on the smaller cfg 1 (DOF/s ~ size-independent)
+                ti1, tt1, it1, dt1 = cpu_sample(1, 1, 1)
+                k1 = golden_iterations(1) or 8
+                cpu["single_thread"] = {"value": cpu_dofs(1, ti1, tt1, k1), "unit": "DOF/s", "cores": 1,
+                                        "sample": f"cfg 1 (128^3): setup {ti1:.1f} s + {it1} iteration(s) at "
+                                                  f"{tt1:.1f} s, extrapolated to {k1} iterations; {dt1:.0f} s wall"}
         out = {
             "metric": "MG-SQMR DOF/s (N x iterations / T_solve)", "value": value, "unit": "DOF/s",
             "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
@@ -275,7 +332,7 @@ def run_ours(args, ws, rank, local):
                        "converged": all(v == smg.SMG_CONVERGED for v in statuses),
                        "final_rel_residual": float(hist[-1]) if len(hist) else None, "tol": tol,
                        "parallelism": (f"z-slab x{ws}" if slabs else f"replicas x{ws}") if ws > 1 else "1 GPU",
-                       "l2": "inputs larger than L2 (fine-level vectors 73 MB each, 7 live)"},
+                       "l2": l2_note(s)},
             "e2e": {"value": e2e_val, "unit": "DOF/s", "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n,
                     "ms_per_step": 1e3 * e2e_s / args.steps},
             "roofline": roof,
@@ -283,10 +340,54 @@ def run_ours(args, ws, rank, local):
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "wall_s_timed": wall,
+            "also": also,
         }
         print(json.dumps(out), flush=True)
     s.close()
     return out
+
+
+def measure_resident(smg, cfg, steps, warmup=1):
+    """Device-resident solves of another config (CUDA-event time per solve, max over steps)."""
+    nx, ny, nz, h, lv, kind, seed, tol, name = CONFIGS[cfg]
+    n = ndof(nx, ny, nz)
+    try:
+        s = smg.Solver(nx, ny, nz, h=h, levels=lv)
+    except Exception as e:  # e.g. not enough device memory
+        return {"workload": name, "error": str(e)}
+    b = smg.forcing(nx, ny, nz, h=h, kind=kind, seed=seed)
+    s.set_rhs(b)
+    for _ in range(warmup):
+        s.solve_resident(tol, 500)
+    ms, its, hist, st = [], [], None, None
+    for _ in range(steps):
+        hist, st = s.solve_resident(tol, 500)
+        t = s.timing()
+        ms.append(t["solve_ms"])
+        its.append(t["iterations"])
+    s.close()
+    tot_ms = sum(ms)
+    return {"workload": name, "N_dof": n, "value": n * sum(its) / (tot_ms / 1e3), "unit": "DOF/s",
+            "ms_per_solve": tot_ms / steps, "iterations_per_solve": sum(its) / steps, "converged": st == 0,
+            "final_rel_residual": float(hist[-1]) if len(hist) else None, "steps": steps, "warmup": warmup}
+
+
+def l2_note(s):
+    """Fine-level vector size against the device L2 (inputs larger than L2, or not)."""
+    vec = 8 * s.ndof()
+    l2 = None
+    try:
+        import torch
+
+        l2 = torch.cuda.get_device_properties(0).L2_cache_size
+    except Exception:
+        pass
+    if not l2:
+        l2 = 126 << 20
+    live = 8  # x, b, r of the fine level + q, d, x_sqmr, rhs + the Vanka ping-pong copy
+    rel = "larger than" if vec > l2 else "smaller than"
+    return (f"fine-level vectors {vec / 1e6:.0f} MB each ({live} live, {live * vec / 1e9:.2f} GB), each "
+            f"{rel} L2 ({l2 / 2**20:.0f} MiB); no explicit flush")
 
 
 def level_counts(s, levels):
@@ -362,7 +463,10 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=1, choices=sorted(CONFIGS))
+    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
+    ap.add_argument("--also", default="3", help="comma list of extra configs measured device-resident "
+                                                "(2 solves each) and reported under 'also'; '' for none")
+    ap.add_argument("--cpu-1thread", action="store_true", help="add a single-thread CPU reference point")
     ap.add_argument("--ref-iters", type=int, default=2, help="SQMR iterations per CPU sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--replicas", action="store_true", help="N > 1: independent copies instead of z-slabs")

@@ -61,6 +61,9 @@ typedef struct smg_params {
     int cycle;       /* 0 V-cycle, 1 W-cycle       */
     int vanka;       /* 0 symmetric multiplicative, 1 additive */
     double omega;    /* additive damping in (0, 1]; <= 0 means 1.0 (SPEC default) */
+    int64_t dgs_tile_min; /* DGS traversal (OD-1 rev. 2): levels with >= this many cells whose
+                             extents are multiples of 16 x 8 x 8 (>= 2 tiles per axis) sweep
+                             their DGS tile by tile; 0: 128^3 (default), < 0: never */
 } smg_params;
 
 #define SMG_FLAG_SKIP_REVERSE_DGS 1 /* fault injection: symmetry negative control */
@@ -116,6 +119,9 @@ int64_t smg_census(const smg_grid_desc* grid, int band_width, int64_t* out2);
  * `rank` the first global plane z0[l] and plane count nzl[l] of every level
  * (replicated levels: 0 and the whole level).  Either array may be NULL. */
 int smg_slab_plan(const smg_grid_desc* grid, int levels, int nparts, int rank, int* z0, int* nzl);
+/* DGS tiling of a level (host only): out4 = {tile colours (8 tiled, 1 not), tile x, y, z}
+ * under the rule of smg_params.dgs_tile_min (the default when tile_min = 0). */
+int smg_dgs_tile(const smg_grid_desc* grid, int level, int64_t tile_min, int* out4);
 const char* smg_last_error(const smg_ctx* ctx);
 const char* smg_version(void);
 
@@ -130,7 +136,8 @@ int smg_residual(smg_ctx* ctx, int level, const double* x, const double* b, doub
 
 /* Smoother entry points.  op: 0 one DGS phase (arg = phase
  * 0..19: forward 0,1 velocity red/black, 2..9 pressure parity colours 0..7;
- * reverse 10..17 pressure colours 7..0, 18,19 velocity black/red), 1
+ * reverse 10..17 pressure colours 7..0, 18,19 velocity black/red; on a tiled
+ * level arg = phase + 32 T acts on the tiles of colour T only), 1
  * symmetric_dgs, 2 one Vanka colour (arg = colour 0..7), 3 symmetric
  * multiplicative Vanka, 4 smooth (Alg. 3, with the params' Vanka flavour), 5 one
  * additive Vanka application.  x is updated in place. */

@@ -20,6 +20,7 @@ _lib = None
 
 ST_CONVERGED, ST_MAXIT, ST_BREAKDOWN = 0, 1, 2
 FORCE_UNIFORM, FORCE_FOURIER, FORCE_CHANNEL = 0, 1, 2
+ORDER_GPU, ORDER_SPEC = 0, 1
 
 _D = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
 _I64 = np.ctypeslib.ndpointer(dtype=np.int64, flags="C_CONTIGUOUS")
@@ -40,7 +41,9 @@ def lib():
         L.orc_set_threads.argtypes = [C.c_int]
         L.orc_create.restype = C.c_void_p
         L.orc_create.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double,
-                                 C.c_int, C.c_int, C.c_int]
+                                 C.c_int, C.c_int, C.c_int, C.c_int64]
+        L.orc_set_order.argtypes = [C.c_void_p, C.c_int]
+        L.orc_dgs_tile.argtypes = [C.c_void_p, C.c_int, np.ctypeslib.ndpointer(dtype=np.int32, flags="C_CONTIGUOUS")]
         L.orc_destroy.argtypes = [C.c_void_p]
         L.orc_nlevels.argtypes = [C.c_void_p]
         L.orc_ndof.restype = C.c_int64
@@ -120,12 +123,15 @@ class Oracle:
     """Walled box of nx*ny*nz interior cells (implicit Dirichlet ring), spacing h."""
 
     def __init__(self, nx, ny=None, nz=None, h=None, eta=1.0, gamma=1e-3, levels=2, nu=1,
-                 band_width=1, cycle=0, vanka=0, omega=1.0):
+                 band_width=1, cycle=0, vanka=0, omega=1.0, tile_min=0, order=ORDER_GPU):
+        """tile_min: cell count from which a level's DGS sweep is tile-ordered (0: 128^3, the
+        GPU default; -1: never).  order: ORDER_GPU (the coloured order the GPU reproduces bit
+        for bit) or ORDER_SPEC (SPEC-literal sequential lexicographic DGS / colour-major Vanka)."""
         ny = nx if ny is None else ny
         nz = nx if nz is None else nz
         h = 1.0 / nx if h is None else h
         L = lib()
-        self._h = L.orc_create(nx, ny, nz, h, eta, gamma, levels, nu, band_width)
+        self._h = L.orc_create(nx, ny, nz, h, eta, gamma, levels, nu, band_width, int(tile_min))
         if not self._h:
             raise RuntimeError("oracle: " + L.orc_last_error().decode())
         self.dims = (nx, ny, nz)
@@ -133,6 +139,7 @@ class Oracle:
         self.nu = nu
         L.orc_set_cycle(self._h, int(cycle))
         L.orc_set_vanka(self._h, int(vanka), float(omega))  # 0 multiplicative, 1 additive
+        L.orc_set_order(self._h, int(order))
 
     def __del__(self):
         if getattr(self, "_h", None):
@@ -146,6 +153,12 @@ class Oracle:
         c = np.zeros(5, np.int64)
         lib().orc_counts(self._h, level, c)
         return {"nu": int(c[0]), "nv": int(c[1]), "nw": int(c[2]), "np": int(c[3]), "V1": int(c[4])}
+
+    def dgs_tile(self, level=0):
+        """(tile colours, tile_x, tile_y, tile_z) of a level's DGS ordering (1, 0, 0, 0: untiled)."""
+        out = np.zeros(4, np.int32)
+        lib().orc_dgs_tile(self._h, level, out)
+        return tuple(int(v) for v in out)
 
     def v1_mask(self, level=0):
         m = np.zeros(self.ndof(level), np.uint8)

@@ -27,6 +27,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <limits>
 #include <map>
 #include <memory>
 #include <stdexcept>
@@ -215,9 +216,18 @@ struct Level {
     std::vector<double> vdiag;  // neighbour-leg count (6 in the cube; SPEC:124 drops Neumann legs)
     // pressure DOF: faces [uL, uR, vL, vR, wL, wR] and neighbour cells [x-, x+, y-, y+, z-, z+]
     std::vector<std::array<int32_t, 6>> pface, pcell;
-    // DGS sets (V2): velocities by red-black parity, pressures by the 8 parity
-    // colours (i&1)+2(j&1)+4(k&1) (OD-1)
-    std::vector<int32_t> dgs_vel[2], dgs_p[8];
+    // DGS sets (V2) by DGS tile colour T (OD-1 rev. 2): large levels are cut
+    // into tiles of kTile cells whose parity colour (tx&1)+2(ty&1)+4(tz&1) orders the sweep
+    // (forward: T = 0..7, each tile's DOFs in the in-tile order; reverse: T = 7..0, each in
+    // the exact reverse in-tile order); small levels are one tile (ntc = 1).  In a tile:
+    // velocities by red-black parity, pressures by the 8 parity colours (i&1)+2(j&1)+4(k&1).
+    int ntc = 1;
+    int tile[3] = {0, 0, 0};
+    std::vector<int32_t> dgs_vel[8][2], dgs_p[8][8];
+    // every active pressure by parity colour (targets of the distributive pressure update)
+    std::vector<int32_t> all_p[8];
+    // SPEC-literal order (Hierarchy::order = 1): V2 DOFs ascending
+    std::vector<int32_t> v2_lex;
     // Vanka blocks (band cells with an active pressure), by colour (OD-2)
     struct Block { std::array<int32_t, 7> dof; int mask; };
     std::vector<Block> vk[8];
@@ -379,7 +389,22 @@ static std::array<double, 49> small_inverse(const std::vector<double>& m, int n)
 }
 
 // ------------------------------------------------------- level builder ------
-static void build_level(Level& L, const CellGrid& g, double eta, double gamma, int band_width) {
+// DGS tiling rule (OD-1 rev. 2), shared with the GPU (csrc/smg_internal.h dgs_tiled):
+// a level is tiled iff its cell count is at least tile_min and every extent is a
+// multiple of the tile extent with at least two tiles per axis.
+constexpr int kTile[3] = {16, 8, 8};
+constexpr int64_t kTileMinDefault = int64_t{1} << 21;  // 128^3
+static bool dgs_tiled(const int* n, int64_t tile_min) {
+    if (tile_min <= 0) tile_min = kTileMinDefault;
+    const int64_t cells = static_cast<int64_t>(n[0]) * n[1] * n[2];
+    if (cells < tile_min) return false;
+    for (int a = 0; a < 3; ++a)
+        if (n[a] % kTile[a] || n[a] / kTile[a] < 2) return false;
+    return true;
+}
+
+static void build_level(Level& L, const CellGrid& g, double eta, double gamma, int band_width,
+                        int64_t tile_min = 0) {
     if (g.dim != 3) throw std::runtime_error("operator is 3-D only");
     for (uint8_t l : g.lab)
         if (l == LAB_E) throw std::runtime_error("operator supports D/I labels only (cube/channel)");
@@ -433,14 +458,29 @@ static void build_level(Level& L, const CellGrid& g, double eta, double gamma, i
                                m.cell(x, y + 1, z), m.cell(x, y, z - 1), m.cell(x, y, z + 1)};
             }
     // DGS sets: V2 velocities split by red-black parity of their storage
-    // coordinates, V2 pressures by the 8 parity colours (OD-1)
-    for (int k = 0; k < 2; ++k) L.dgs_vel[k].clear();
-    for (int k = 0; k < 8; ++k) L.dgs_p[k].clear();
+    // coordinates, V2 pressures by the 8 parity colours (OD-1), both by the DGS tile
+    // colour of the owning cell (a face at storage (x,y,z) is the low face of cell (x,y,z))
+    const bool tiled = dgs_tiled(g.n, tile_min);
+    L.ntc = tiled ? 8 : 1;
+    for (int a = 0; a < 3; ++a) L.tile[a] = tiled ? kTile[a] : 0;
+    auto tcol = [&](const std::array<int32_t, 3>& p) {
+        if (!tiled) return 0;
+        return ((p[0] / kTile[0]) & 1) + 2 * ((p[1] / kTile[1]) & 1) + 4 * ((p[2] / kTile[2]) & 1);
+    };
+    for (int t = 0; t < 8; ++t) {
+        for (int k = 0; k < 2; ++k) L.dgs_vel[t][k].clear();
+        for (int k = 0; k < 8; ++k) L.dgs_p[t][k].clear();
+    }
+    for (int k = 0; k < 8; ++k) L.all_p[k].clear();
+    L.v2_lex.clear();
     for (int64_t q = 0; q < m.N; ++q) {
-        if (m.v1[q]) continue;
         const auto& p = m.pos[q];
-        if (q < m.off[3]) L.dgs_vel[(p[0] + p[1] + p[2]) & 1].push_back(static_cast<int32_t>(q));
-        else L.dgs_p[(p[0] & 1) + 2 * (p[1] & 1) + 4 * (p[2] & 1)].push_back(static_cast<int32_t>(q));
+        const int pc = (p[0] & 1) + 2 * (p[1] & 1) + 4 * (p[2] & 1);
+        if (q >= m.off[3]) L.all_p[pc].push_back(static_cast<int32_t>(q));
+        if (m.v1[q]) continue;
+        L.v2_lex.push_back(static_cast<int32_t>(q));
+        if (q < m.off[3]) L.dgs_vel[tcol(p)][(p[0] + p[1] + p[2]) & 1].push_back(static_cast<int32_t>(q));
+        else L.dgs_p[tcol(p)][pc].push_back(static_cast<int32_t>(q));
     }
     // Vanka blocks: one per band cell with an active
     // pressure; slots [uL,uR,vL,vR,wL,wR,p]; colour (i&1)+2(j&1)+4(k&1).
@@ -492,9 +532,10 @@ static void build_level(Level& L, const CellGrid& g, double eta, double gamma, i
 }
 
 // ----------------------------------------------------------- smoothers ------
-// DGS velocity phase (Alg. 2 velocity rows: M_.j = e_j), one colour.
-static void dgs_vel(const Level& L, vec& x, const vec& b, int col) {
-    const auto& lst = L.dgs_vel[col];
+// DGS velocity phase (Alg. 2 velocity rows: M_.j = e_j): one red-black
+// colour of DGS tile colour T.
+static void dgs_vel(const Level& L, vec& x, const vec& b, int T, int col) {
+    const auto& lst = L.dgs_vel[T][col];
     parallel_for(static_cast<int64_t>(lst.size()), g_threads > 1 ? g_threads : 1, [&](int64_t t) {
         const int32_t f = lst[t];
         const double r = b[f] - mom_row(L, x, f);
@@ -502,36 +543,69 @@ static void dgs_vel(const Level& L, vec& x, const vec& b, int col) {
     });
 }
 
-// DGS forward pressure phase (Alg. 2 pressure rows, gather form, OD-1/OD-3):
-// delta_C = r_C / d_p for V2 cells C of colour col, then x += sum_C delta_C M_.C.
-static void dgs_p_fwd(const Level& L, vec& x, const vec& b, int col, vec& delta) {
+// DGS forward pressure phase (Alg. 2 pressure rows, gather form, OD-1/OD-3) on the V2
+// cells C of parity colour col in tile colour T: delta_C = r_C / d_p, then
+// x += sum_C delta_C M_.C.  Only DOFs with a nonzero contribution are touched: the six
+// faces of every C (x_f += (delta_left - delta_right) / h; M_{f,C} = +1/h on C's right
+// face) and the pressures of C and of its axis neighbours (x_K += eta/h^2 (6 delta_K -
+// sum_nbr delta); M_{K,C} = eta (B B^T)_{KC}).  `delta` (np entries) and `inset` are
+// zero on entry and on exit.
+static void dgs_p_fwd(const Level& L, vec& x, const vec& b, int T, int col, vec& delta,
+                      std::vector<uint8_t>& inset) {
     const DofMap& m = L.map;
     const int64_t np = m.cnt[3], p0 = m.off[3];
-    delta.assign(np, 0.0);
-    for (int32_t c : L.dgs_p[col]) delta[c - p0] = (b[c] - cont_row(L, x, c, L.gamma)) / L.dp;
-    auto dl = [&](int32_t id) { return id >= 0 ? delta[id - p0] : 0.0; };
-    // faces: x_f += (delta_left - delta_right) / h   (M_{f,C} = +1/h on C's right face)
-    parallel_for(p0, g_threads, [&](int64_t f) {
-        const auto& fc = L.fcells[f];
-        x[f] = x[f] + (dl(fc[0]) - dl(fc[1])) * L.inv_h;
+    if (static_cast<int64_t>(delta.size()) != np) delta.assign(np, 0.0);
+    if (static_cast<int64_t>(inset.size()) != np) inset.assign(np, 0);
+    const auto& lst = L.dgs_p[T][col];
+    parallel_for(static_cast<int64_t>(lst.size()), g_threads, [&](int64_t t) {
+        const int32_t c = lst[t];
+        delta[c - p0] = (b[c] - cont_row(L, x, c, L.gamma)) / L.dp;
+        inset[c - p0] = 1;
     });
-    // pressures: x_K += eta/h^2 (6 delta_K - sum_nbr delta)  (M_{K,C} = eta (B B^T)_{KC})
-    parallel_for(np, g_threads, [&](int64_t t) {
-        const int32_t k = static_cast<int32_t>(p0 + t);
+    auto dl = [&](int32_t id) { return id >= 0 ? delta[id - p0] : 0.0; };
+    auto pupd = [&](int32_t k) {  // eager pressure update of cell k (operand order of the contract)
         const auto& nc = L.pcell[k];
         double s = dl(nc[0]) + dl(nc[1]);
         s = s + dl(nc[2]);
         s = s + dl(nc[3]);
         s = s + dl(nc[4]);
         s = s + dl(nc[5]);
-        x[k] = x[k] + L.eta_h2 * (6.0 * delta[t] - s);
+        x[k] = x[k] + L.eta_h2 * (6.0 * delta[k - p0] - s);
+    };
+    // faces: every face of a colour-col cell borders exactly one such cell
+    parallel_for(static_cast<int64_t>(lst.size()), g_threads, [&](int64_t t) {
+        const auto& fc = L.pface[lst[t]];
+        for (int q = 0; q < 6; ++q) {
+            const int32_t f = fc[q];
+            if (f < 0) continue;
+            const auto& lr = L.fcells[f];
+            x[f] = x[f] + (dl(lr[0]) - dl(lr[1])) * L.inv_h;
+        }
+        pupd(lst[t]);  // self term (its neighbours carry no delta)
     });
+    // neighbour pressures: colours col ^ 1, col ^ 2, col ^ 4, gathered (several C may share one)
+    for (int bit = 1; bit <= 4; bit <<= 1) {
+        const auto& kl = L.all_p[col ^ bit];
+        const int ax = bit == 1 ? 0 : (bit == 2 ? 2 : 4);
+        parallel_for(static_cast<int64_t>(kl.size()), g_threads, [&](int64_t t) {
+            const int32_t k = kl[t];
+            const auto& nc = L.pcell[k];
+            const bool hit = (nc[ax] >= 0 && inset[nc[ax] - p0]) || (nc[ax + 1] >= 0 && inset[nc[ax + 1] - p0]);
+            if (hit) pupd(k);
+        });
+    }
+    for (int32_t c : lst) {
+        delta[c - p0] = 0.0;
+        inset[c - p0] = 0;
+    }
 }
 
 // DGS reverse (left-preconditioned) pressure phase:
-// x_C += m_C^T (b - L̃ x) / d_p for V2 cells C of colour col, evaluated as
-// (m_C^T b - m_C^T (L̃ x)) / d_p: the b part is fixed while b is (the GPU computes it
-// once per sweep), each part with the same operation order.
+// x_C += m_C^T (b - L̃ x) / d_p for V2 cells C of colour col in tile colour T,
+// evaluated as (m_C^T b - m_C^T (L̃ x)) / d_p: the b part is fixed while b is (the GPU
+// computes it once per V-cycle level visit), the L̃x part from the 6 momentum rows at C's
+// faces and the 7 continuity rows around C, each part with the same operation order
+// (DESIGN.md §4).  Same-colour cells never read each other's pressure: one pass.
 static double m_col_dot(const Level& L, const vec& v, int32_t c) {
     const auto& f = L.pface[c];
     const auto& nc = L.pcell[c];
@@ -543,32 +617,89 @@ static double m_col_dot(const Level& L, const vec& v, int32_t c) {
     s = s + v[nc[5]];
     return fl * L.inv_h + L.eta_h2 * (6.0 * v[c] - s);
 }
-static void dgs_p_rev(const Level& L, vec& x, const vec& b, int col, vec& lx) {
-    apply(L, x, lx, true);  // L̃ x
-    const auto& lst = L.dgs_p[col];
+static double m_col_dot_lx(const Level& L, const vec& x, int32_t c) {
+    const auto& f = L.pface[c];
+    const auto& nc = L.pcell[c];
+    double lf[6], ln[6];
+    for (int q = 0; q < 6; ++q) lf[q] = mom_row(L, x, f[q]);
+    for (int q = 0; q < 6; ++q) ln[q] = cont_row(L, x, nc[q], L.gamma);
+    const double lc = cont_row(L, x, c, L.gamma);
+    const double fl = ((lf[1] - lf[0]) + (lf[3] - lf[2])) + (lf[5] - lf[4]);
+    double s = ln[0] + ln[1];
+    s = s + ln[2];
+    s = s + ln[3];
+    s = s + ln[4];
+    s = s + ln[5];
+    return fl * L.inv_h + L.eta_h2 * (6.0 * lc - s);
+}
+static void dgs_p_rev(const Level& L, vec& x, const vec& b, int T, int col) {
+    const auto& lst = L.dgs_p[T][col];
+    std::vector<double> nv(lst.size());
     parallel_for(static_cast<int64_t>(lst.size()), g_threads, [&](int64_t t) {
         const int32_t c = lst[t];
-        const double cb = m_col_dot(L, b, c), cl = m_col_dot(L, lx, c);
-        x[c] = x[c] + (cb - cl) / L.dp;
+        const double cb = m_col_dot(L, b, c), cl = m_col_dot_lx(L, x, c);
+        nv[t] = x[c] + (cb - cl) / L.dp;
     });
+    for (size_t t = 0; t < lst.size(); ++t) x[lst[t]] = nv[t];
 }
 
 // Phase ids (test harness and GPU share them): forward 0,1 velocity colours
 // 0,1; 2..9 pressure colours 0..7; reverse 10..17 pressure colours 7..0;
-// 18,19 velocity colours 1,0 — the exact reverse traversal.
+// 18,19 velocity colours 1,0 -- the exact reverse traversal.  On a tiled
+// level a phase acts on one DGS tile colour T (argument phase + 32 T).
 constexpr int kDgsPhases = 20;
-static void dgs_phase(const Level& L, vec& x, const vec& b, int phase, vec& scratch) {
-    if (phase == 0 || phase == 1) dgs_vel(L, x, b, phase);
-    else if (phase >= 2 && phase <= 9) dgs_p_fwd(L, x, b, phase - 2, scratch);
-    else if (phase >= 10 && phase <= 17) dgs_p_rev(L, x, b, 17 - phase, scratch);
-    else if (phase == 18 || phase == 19) dgs_vel(L, x, b, 19 - phase);
+struct DgsScratch {
+    vec delta;
+    std::vector<uint8_t> inset;
+};
+static void dgs_phase(const Level& L, vec& x, const vec& b, int phase, int T, DgsScratch& sc) {
+    if (T < 0 || T >= L.ntc) throw std::runtime_error("bad dgs tile colour");
+    if (phase == 0 || phase == 1) dgs_vel(L, x, b, T, phase);
+    else if (phase >= 2 && phase <= 9) dgs_p_fwd(L, x, b, T, phase - 2, sc.delta, sc.inset);
+    else if (phase >= 10 && phase <= 17) dgs_p_rev(L, x, b, T, 17 - phase);
+    else if (phase == 18 || phase == 19) dgs_vel(L, x, b, T, 19 - phase);
     else throw std::runtime_error("bad dgs phase");
 }
 
+// SPEC-literal DGS (Hierarchy::order = 1, comparison mode): V2 DOFs relaxed one at a
+// time in ascending global DOF index (velocities u, v, w lexicographic, then pressures;
+// SPEC:261, 332), the reverse in strictly descending order.  Velocity j:
+// x_j += r_j / d_v.  Pressure j forward: x += (r_j / d_p) M_.j; reverse: x_j += m_j^T (b -
+// L̃x) / d_p.  Strictly sequential (no colouring): the reference's own traversal.
+static void dgs_lex(const Level& L, vec& x, const vec& b, bool forward) {
+    const int64_t nv = L.map.off[3];
+    const int64_t n = static_cast<int64_t>(L.v2_lex.size());
+    for (int64_t t0 = 0; t0 < n; ++t0) {
+        const int32_t j = L.v2_lex[forward ? t0 : n - 1 - t0];
+        if (j < nv) {
+            x[j] = x[j] + (b[j] - mom_row(L, x, j)) / L.dv;
+        } else if (forward) {
+            const double d = (b[j] - cont_row(L, x, j, L.gamma)) / L.dp;
+            const auto& f = L.pface[j];
+            for (int q = 0; q < 6; ++q)
+                if (f[q] >= 0) x[f[q]] = x[f[q]] + ((q & 1) ? d : -d) * L.inv_h;
+            x[j] = x[j] + L.eta_h2 * 6.0 * d;
+            for (int32_t k : L.pcell[j])
+                if (k >= 0) x[k] = x[k] - L.eta_h2 * d;
+        } else {
+            x[j] = x[j] + (m_col_dot(L, b, j) - m_col_dot_lx(L, x, j)) / L.dp;
+        }
+    }
+}
+
 // symmetric_dgs: forward phases then their exact reverse.
-static void symmetric_dgs(const Level& L, vec& x, const vec& b, bool skip_reverse = false) {
-    vec scratch;
-    for (int ph = 0; ph < (skip_reverse ? kDgsPhases / 2 : kDgsPhases); ++ph) dgs_phase(L, x, b, ph, scratch);
+static void symmetric_dgs(const Level& L, vec& x, const vec& b, bool skip_reverse = false, int order = 0) {
+    if (order == 1) {
+        dgs_lex(L, x, b, true);
+        if (!skip_reverse) dgs_lex(L, x, b, false);
+        return;
+    }
+    DgsScratch sc;
+    for (int T = 0; T < L.ntc; ++T)
+        for (int ph = 0; ph < kDgsPhases / 2; ++ph) dgs_phase(L, x, b, ph, T, sc);
+    if (skip_reverse) return;
+    for (int T = L.ntc - 1; T >= 0; --T)
+        for (int ph = kDgsPhases / 2; ph < kDgsPhases; ++ph) dgs_phase(L, x, b, ph, T, sc);
 }
 
 // One Vanka colour phase, Jacobi within the colour (OD-2): every block reads
@@ -609,7 +740,33 @@ static void vanka_colour(const Level& L, vec& x, const vec& b, int col) {
 // bit-identical results: 8 dependent phases per symmetric sweep instead of 16.
 // Measured MG/SQMR convergence equals the 0..7 order.
 static const int kVankaOrder[8] = {0, 7, 1, 6, 2, 5, 3, 4};
-static void vanka_symmetric(const Level& L, vec& x, const vec& b) {
+// SPEC-literal comparison mode (order = 1): blocks strictly one after another, colour-major
+// 0..7 and ascending cell index within a colour, each block seeing every
+// earlier update; the reverse sweep reverses block and colour order.
+static void vanka_block_seq(const Level& L, vec& x, const vec& b, const Level::Block& blk) {
+    double r[7];
+    for (int s = 0; s < 7; ++s) {
+        const int32_t id = blk.dof[s];
+        r[s] = id < 0 ? 0.0 : b[id] - (s < 6 ? mom_row(L, x, id) : cont_row(L, x, id, L.gamma));
+    }
+    const auto& K = L.vk_inv.at(blk.mask);
+    double dl[7];
+    for (int s = 0; s < 7; ++s) {
+        double acc = 0.0;
+        for (int q = 0; q < 7; ++q) acc = acc + K[s * 7 + q] * r[q];
+        dl[s] = acc;
+    }
+    for (int s = 0; s < 7; ++s)
+        if (blk.dof[s] >= 0) x[blk.dof[s]] = x[blk.dof[s]] + dl[s];
+}
+static void vanka_symmetric(const Level& L, vec& x, const vec& b, int order = 0) {
+    if (order == 1) {
+        for (int c = 0; c < 8; ++c)
+            for (const auto& blk : L.vk[c]) vanka_block_seq(L, x, b, blk);
+        for (int c = 7; c >= 0; --c)
+            for (auto it = L.vk[c].rbegin(); it != L.vk[c].rend(); ++it) vanka_block_seq(L, x, b, *it);
+        return;
+    }
     for (int c = 0; c < 8; ++c) vanka_colour(L, x, b, kVankaOrder[c]);
     for (int c = 7; c >= 0; --c) vanka_colour(L, x, b, kVankaOrder[c]);
 }
@@ -657,17 +814,17 @@ struct VankaCfg {
 };
 static VankaCfg g_vanka_default;
 
-static void vanka_apply(const Level& L, vec& x, const vec& b, const VankaCfg& vc) {
+static void vanka_apply(const Level& L, vec& x, const vec& b, const VankaCfg& vc, int order = 0) {
     if (vc.kind == 1) vanka_additive(L, x, b, vc.omega);
-    else vanka_symmetric(L, x, b);
+    else vanka_symmetric(L, x, b, order);
 }
 
 // smooth, Alg. 3: nu x Vanka(V1), symmetric DGS(V2), nu x Vanka(V1).
 static void smooth(const Level& L, vec& x, const vec& b, int nu, bool skip_reverse = false,
-                   const VankaCfg& vc = g_vanka_default) {
-    for (int k = 0; k < nu; ++k) vanka_apply(L, x, b, vc);
-    symmetric_dgs(L, x, b, skip_reverse);
-    for (int k = 0; k < nu; ++k) vanka_apply(L, x, b, vc);
+                   const VankaCfg& vc = g_vanka_default, int order = 0) {
+    for (int k = 0; k < nu; ++k) vanka_apply(L, x, b, vc, order);
+    symmetric_dgs(L, x, b, skip_reverse, order);
+    for (int k = 0; k < nu; ++k) vanka_apply(L, x, b, vc, order);
 }
 
 // ------------------------------------------------------------ transfer ------
@@ -779,6 +936,7 @@ struct Hierarchy {
     int cycle = 0;              // 0 V-cycle, 1 W-cycle
     bool skip_reverse = false;  // fault injection for the symmetry negative control
     VankaCfg vanka;             // multiplicative (default) or additive Vanka on V1
+    int order = 0;              // 0: the GPU's order (OD-1/OD-2); 1: SPEC-literal sequential order
 };
 
 static std::vector<double> assemble_dense(const Level& L, bool penalized) {
@@ -798,7 +956,7 @@ static std::vector<double> assemble_dense(const Level& L, bool penalized) {
 
 // build_hierarchy.
 static std::unique_ptr<Hierarchy> build_hierarchy(const CellGrid& g, double eta, double gamma, int levels,
-                                                  int nu, int band_width) {
+                                                  int nu, int band_width, int64_t tile_min = 0) {
     if (levels < 1) throw std::runtime_error("levels < 1");
     auto H = std::make_unique<Hierarchy>();
     H->nu = nu;
@@ -808,7 +966,7 @@ static std::unique_ptr<Hierarchy> build_hierarchy(const CellGrid& g, double eta,
         for (int a = 0; a < 3; ++a)
             if (cur.n[a] < 2) throw std::runtime_error("coarsened extent below 2 (SPEC:82)");
         auto L = std::make_unique<Level>();
-        build_level(*L, cur, eta, gamma, band_width);
+        build_level(*L, cur, eta, gamma, band_width, tile_min);
         H->lv.push_back(std::move(L));
     }
     const Level& C = *H->lv.back();
@@ -840,7 +998,7 @@ static void vcycle(const Hierarchy& H, int l, const vec& b, vec& x) {
     const Level& L = *H.lv[l];
     if (l == static_cast<int>(H.lv.size()) - 1) { coarse_solve(H, b, x); return; }
     x.assign(L.map.N, 0.0);
-    smooth(L, x, b, H.nu, H.skip_reverse, H.vanka);
+    smooth(L, x, b, H.nu, H.skip_reverse, H.vanka, H.order);
     vec r, rc, ec, ef;
     residual(L, x, b, r);
     restrict_(L, *H.lv[l + 1], r, rc);
@@ -855,7 +1013,7 @@ static void vcycle(const Hierarchy& H, int l, const vec& b, vec& x) {
     }
     prolong(L, *H.lv[l + 1], ec, ef);
     for (int64_t q = 0; q < L.map.N; ++q) x[q] = x[q] + ef[q];
-    smooth(L, x, b, H.nu, H.skip_reverse, H.vanka);
+    smooth(L, x, b, H.nu, H.skip_reverse, H.vanka, H.order);
 }
 
 // ----------------------------------------------------- canonical dot -------
@@ -1113,7 +1271,9 @@ const char* orc_last_error() { return g_last_err.c_str(); }
 void orc_set_threads(int t) { g_threads = t < 1 ? 1 : t; }
 
 // Walled box with nx*ny*nz interior cells, uniform spacing h.
-void* orc_create(int nx, int ny, int nz, double h, double eta, double gamma, int levels, int nu, int band_width) {
+// tile_min: cell count from which a level's DGS is tile-ordered (0: default 128^3; < 0: never).
+void* orc_create(int nx, int ny, int nz, double h, double eta, double gamma, int levels, int nu, int band_width,
+                 int64_t tile_min) {
     try {
         CellGrid g;
         g.dim = 3;
@@ -1123,7 +1283,8 @@ void* orc_create(int nx, int ny, int nz, double h, double eta, double gamma, int
         g.h = h;
         g.lab.assign(static_cast<size_t>(nx) * ny * nz, LAB_I);
         auto* o = new OrcHandle();
-        o->H = build_hierarchy(g, eta, gamma, levels, nu, band_width);
+        o->H = build_hierarchy(g, eta, gamma, levels, nu, band_width,
+                               tile_min < 0 ? std::numeric_limits<int64_t>::max() : tile_min);
         return o;
     } catch (const std::exception& e) {
         g_last_err = e.what();
@@ -1151,6 +1312,14 @@ void orc_v1_mask(void* h, int l, uint8_t* mask) {
 }
 void orc_set_skip_reverse(void* h, int s) { HH(h).skip_reverse = s != 0; }
 void orc_set_cycle(void* h, int kind) { HH(h).cycle = kind; }
+// 0: the GPU's smoother order (OD-1/OD-2); 1: SPEC-literal sequential order (comparison mode)
+void orc_set_order(void* h, int order) { HH(h).order = order; }
+// DGS tiling of level l: out4 = {ntc, tile_x, tile_y, tile_z}
+void orc_dgs_tile(void* h, int l, int* out4) {
+    const Level& L = *HH(h).lv[l];
+    out4[0] = L.ntc;
+    for (int a = 0; a < 3; ++a) out4[1 + a] = L.tile[a];
+}
 // Vanka flavour: kind 0 symmetric multiplicative, 1 additive with damping omega.
 void orc_set_vanka(void* h, int kind, double omega) {
     HH(h).vanka.kind = kind;
@@ -1185,12 +1354,13 @@ int orc_smoother(void* h, int l, int op, int arg, double* x, const double* b) {
     try {
         Hierarchy& H = HH(h);
         const Level& L = *H.lv[l];
-        vec xx = V(x, L.map.N), bb = V(b, L.map.N), scratch;
-        if (op == 0) dgs_phase(L, xx, bb, arg, scratch);
-        else if (op == 1) symmetric_dgs(L, xx, bb, H.skip_reverse);
+        vec xx = V(x, L.map.N), bb = V(b, L.map.N);
+        DgsScratch scratch;
+        if (op == 0) dgs_phase(L, xx, bb, arg & 31, arg >> 5, scratch);
+        else if (op == 1) symmetric_dgs(L, xx, bb, H.skip_reverse, H.order);
         else if (op == 2) vanka_colour(L, xx, bb, arg);
-        else if (op == 3) vanka_symmetric(L, xx, bb);
-        else if (op == 4) smooth(L, xx, bb, H.nu, H.skip_reverse, H.vanka);
+        else if (op == 3) vanka_symmetric(L, xx, bb, H.order);
+        else if (op == 4) smooth(L, xx, bb, H.nu, H.skip_reverse, H.vanka, H.order);
         else if (op == 5) vanka_additive(L, xx, bb, H.vanka.omega);
         else throw std::runtime_error("bad smoother op");
         out(xx, x);

@@ -37,7 +37,7 @@ class GridDesc(C.Structure):
 class Params(C.Structure):
     _fields_ = [("eta", C.c_double), ("gamma", C.c_double), ("levels", C.c_int), ("nu", C.c_int),
                 ("band_width", C.c_int), ("flags", C.c_int), ("cycle", C.c_int), ("vanka", C.c_int),
-                ("omega", C.c_double)]
+                ("omega", C.c_double), ("dgs_tile_min", C.c_int64)]
 
 
 class History(C.Structure):
@@ -56,7 +56,7 @@ EXPORTED = [
     "smg_vcycle", "smg_sqmr_solve", "smg_set_rhs", "smg_solve_resident", "smg_get_solution",
     "smg_last_timing", "smg_time_kernel", "smg_host_alloc", "smg_host_free", "smg_forcing",
     "smg_profiler_range", "smg_slab_plan", "smg_mg_solve", "smg_census", "smg_assemble_rhs",
-    "smg_nccl_unique_id", "smg_create_rank",
+    "smg_nccl_unique_id", "smg_create_rank", "smg_dgs_tile",
 ]
 
 _lib = None
@@ -105,6 +105,7 @@ def lib():
     L.smg_census.argtypes = [C.POINTER(GridDesc), C.c_int, C.c_void_p]
     L.smg_slab_plan.argtypes = [C.POINTER(GridDesc), C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int),
                                 C.POINTER(C.c_int)]
+    L.smg_dgs_tile.argtypes = [C.POINTER(GridDesc), C.c_int, C.c_int64, C.POINTER(C.c_int)]
     L.smg_host_alloc.restype = C.c_void_p
     L.smg_host_alloc.argtypes = [C.c_int64]
     L.smg_host_free.argtypes = [C.c_void_p]
@@ -139,6 +140,16 @@ def slab_plan(nx, ny, nz, levels, nparts, rank, h=None):
     nzl = (C.c_int * levels)()
     nd = lib().smg_slab_plan(C.byref(g), levels, nparts, rank, z0, nzl)
     return nd, [(z0[l], nzl[l]) for l in range(levels)]
+
+
+def dgs_tile(nx, ny, nz, level=0, tile_min=0):
+    """DGS tiling of a level (host only): (tile colours, tile_x, tile_y, tile_z); (1, 0, 0, 0) untiled."""
+    g = GridDesc(3, nx, ny, nz, 1.0 / nx)
+    out = (C.c_int * 4)()
+    rc = lib().smg_dgs_tile(C.byref(g), level, int(tile_min), out)
+    if rc != 0:
+        raise SmgError(f"smg_dgs_tile failed ({rc})")
+    return tuple(out)
 
 
 def cavity_rhs(nx, ny=None, nz=None, h=None, eta=1.0, lid=1.0):
@@ -182,15 +193,16 @@ class Solver:
     """One device context (hierarchy + buffers) for a walled box of nx*ny*nz cells."""
 
     def __init__(self, nx, ny=None, nz=None, h=None, eta=1.0, gamma=1e-3, levels=2, nu=1, band_width=1,
-                 flags=0, device=0, devices=None, cycle=0, vanka=0, omega=1.0):
+                 flags=0, device=0, devices=None, cycle=0, vanka=0, omega=1.0, tile_min=0):
         """devices: list of CUDA device ids, one z-slab part each (repeat an id to emulate several
-        parts on one GPU).  Default: a single part on `device`."""
+        parts on one GPU).  Default: a single part on `device`.  tile_min: cell count from which a
+        level's DGS sweep runs in tile order (0: 128^3, the default; -1: never)."""
         ny = nx if ny is None else ny
         nz = nx if nz is None else nz
         h = 1.0 / nx if h is None else h
         L = lib()
         self.grid = GridDesc(3, nx, ny, nz, h)
-        self.params = Params(eta, gamma, levels, nu, band_width, flags, cycle, vanka, omega)
+        self.params = Params(eta, gamma, levels, nu, band_width, flags, cycle, vanka, omega, int(tile_min))
         ctx = C.c_void_p()
         devs = list(devices) if devices else [device]
         arr = (C.c_int * len(devs))(*devs)
@@ -203,7 +215,7 @@ class Solver:
 
     @classmethod
     def for_rank(cls, rank, nranks, nccl_id, nx, ny=None, nz=None, h=None, eta=1.0, gamma=1e-3, levels=2, nu=1,
-                 band_width=1, flags=0, device=0, cycle=0, vanka=0, omega=1.0):
+                 band_width=1, flags=0, device=0, cycle=0, vanka=0, omega=1.0, tile_min=0):
         """Rank `rank` of a one-process-per-GPU z-slab solver (smg_create_rank): every rank
         calls this with the same 128-byte NCCL id (nccl_unique_id() on rank 0, broadcast by
         the launcher) and its own device; later calls are collective."""
@@ -212,7 +224,7 @@ class Solver:
         h = 1.0 / nx if h is None else h
         self = cls.__new__(cls)
         self.grid = GridDesc(3, nx, ny, nz, h)
-        self.params = Params(eta, gamma, levels, nu, band_width, flags, cycle, vanka, omega)
+        self.params = Params(eta, gamma, levels, nu, band_width, flags, cycle, vanka, omega, int(tile_min))
         if len(nccl_id) != 128:
             raise ValueError("NCCL unique id must be 128 bytes")
         ctx = C.c_void_p()

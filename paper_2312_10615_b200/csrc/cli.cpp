@@ -145,7 +145,7 @@ int verify(int max_n) {
     for (int n = 4; n <= max_n; n *= 2) {
         smg_grid_desc g{3, n, n, n, 1.0 / n};
         for (int vk = 0; vk < 2; ++vk) {
-            smg_params p{1.0, 1e-3, 2, 1, 1, 0, 0, vk, 0.5};
+            smg_params p{1.0, 1e-3, 2, 1, 1, 0, 0, vk, 0.5, 0};
             int dev = 0;
             smg_ctx* ctx = nullptr;
             if (smg_create(&g, &p, 1, &dev, &ctx) != SMG_OK) return 1;
@@ -225,7 +225,7 @@ int main(int argc, char** argv) {
     if (vk != "multiplicative" && vk != "additive") { std::fprintf(stderr, "config error: vanka\n"); return 1; }
     smg_params p{num("eta", 1e-3), num("gamma", 1e-3), static_cast<int>(num("levels", 2)),
                  static_cast<int>(num("nu", 1)), bw, 0, str("cycle", "V") == "W" ? 1 : 0,
-                 vk == "additive" ? 1 : 0, num("omega", 1.0)};
+                 vk == "additive" ? 1 : 0, num("omega", 1.0), static_cast<int64_t>(num("dgs_tile_min", 0))};
     const std::string method = str("method", "mg-sqmr");
     if (method != "mg-sqmr" && method != "mg") { std::fprintf(stderr, "config error: method\n"); return 1; }
     const std::string fk = str("forcing", "uniform");

@@ -240,7 +240,6 @@ struct DevLevel {
     int va_n = 0;
     double* va_d7 = nullptr;
     double* ktab = nullptr;  // [64][49]
-    std::vector<WavePass> wave;  // fused wavefront DGS sweep (large single-part levels), empty: per-phase/coop
 };
 
 }  // namespace
@@ -288,10 +287,6 @@ struct smg_ctx {
     // plane partials and gathers travel through NCCL on the part's stream
     bool mp = false;
     ncclComm_t comm = nullptr;
-    // single-part SQMR: apply + inner product + scalar update fused (opt-in, SMG_FUSED_DOT=1)
-    bool fused_dot = true;
-    unsigned* dot_done = nullptr;
-    double* dot_rows = nullptr;
 
     template <class T>
     T* dalloc(int64_t count) {
@@ -325,34 +320,6 @@ int64_t vlen(const DevLevel& L) { return L.k.g.vec_len(); }
 int env_int(const char* name, int dflt) {
     const char* e = std::getenv(name);
     return e ? std::atoi(e) : dflt;
-}
-
-// Fused wavefront DGS plan (opt-in: SMG_WAVE=1) for levels above SMG_WAVE_MIN_CELLS
-// cells (default: larger than 64^3); SMG_WAVE_MB sets the L2 budget of the live
-// planes.  Measured slower than the per-step kernels on B200 (the
-// per-unit dependency round trips cost more than the L2 reuse saves), so it is
-// kept only as a bit-identical alternative.
-void build_wave(smg_ctx* c, DevLevel& L) {
-    const Geom& g = L.k.g;
-    const int64_t ncell = static_cast<int64_t>(g.nx) * g.ny * g.nz;
-    const bool forced = std::getenv("SMG_WAVE_MIN_CELLS") != nullptr;  // tests: any level, any pass split
-    if (!env_int("SMG_WAVE", 0) || ncell < env_int("SMG_WAVE_MIN_CELLS", 262145)) return;
-    const int nph = (c->prm.flags & SMG_FLAG_SKIP_REVERSE_DGS) ? 10 : 20;
-    std::vector<WaveHostPass> plan = wave_build(L.k, nph, static_cast<int64_t>(env_int("SMG_WAVE_MB", 48)) << 20);
-    if (plan.empty()) return;
-    // fusion only pays when passes hold several steps (else: per-step kernels)
-    int nsteps = 0;
-    for (const WaveHostPass& hp : plan) nsteps += hp.p.nsteps;
-    if (!forced && nsteps < env_int("SMG_WAVE_MIN_STEPS_PER_PASS", 3) * static_cast<int>(plan.size())) return;
-    int* cnt = c->dalloc<int>(1 + static_cast<int64_t>(kWaveMaxSteps) * g.nz);
-    for (WaveHostPass& hp : plan) {
-        uint32_t* d = c->dalloc<uint32_t>(static_cast<int64_t>(hp.units.size()));
-        CK(cudaMemcpyAsync(d, hp.units.data(), hp.units.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, c->st));
-        hp.p.units = d;
-        hp.p.cnt = cnt;
-        L.wave.push_back(hp.p);
-    }
-    CK(cudaStreamSynchronize(c->st));
 }
 
 // ---- setup ----
@@ -399,6 +366,7 @@ void build(smg_ctx* c, const std::vector<double>* shared_coarse = nullptr, std::
         L.k.dv = 6.0 * L.k.eta_h2;
         L.k.dp = -6.0 * (1.0 + p.gamma * p.eta) / (h * h);
         L.k.bw = p.band_width;
+        L.k.tiled = dgs_tiled(nx, ny, nz, p.dgs_tile_min) ? 1 : 0;
         L.counts[0] = static_cast<int64_t>(nx - 1) * ny * nz;
         L.counts[1] = static_cast<int64_t>(nx) * (ny - 1) * nz;
         L.counts[2] = static_cast<int64_t>(nx) * ny * (nz - 1);
@@ -416,7 +384,6 @@ void build(smg_ctx* c, const std::vector<double>* shared_coarse = nullptr, std::
         L.pd0 = c->dalloc<double>(L.k.g.fs);
         L.pd1 = c->dalloc<double>(L.k.g.fs);
         L.k.cb = c->dalloc<double>(L.k.g.fs);
-        build_wave(c, L);
         // Vanka blocks: band cells, slot + active-face mask, by colour
         const int bw = p.band_width;
         auto band = [&](int x, int y, int z) {
@@ -676,9 +643,6 @@ void build(smg_ctx* c, const std::vector<double>* shared_coarse = nullptr, std::
     for (auto& L : c->lv) maxN = std::max(maxN, L.N);
     c->compact = c->dalloc<double>(maxN);
     c->partials = c->dalloc<double>(kPartials);
-    c->dot_done = c->dalloc<unsigned>(c->lv[0].k.g.nz + 2);
-    c->dot_rows = c->dalloc<double>(4 * static_cast<int64_t>(c->lv[0].k.g.ny + 1) * (c->lv[0].k.g.nz + 1));
-    c->fused_dot = env_int("SMG_FUSED_DOT", 0) != 0;  // opt-in: measured slower
     c->dscal = c->dalloc<double>(S_COUNT);
     CK(cudaMallocHost(&c->hscal, 8 * sizeof(double)));
     CK(cudaStreamSynchronize(c->st));
@@ -700,6 +664,14 @@ void vanka_sym(smg_ctx* c, int l, double* x, const double* b) {
 constexpr int kDgsPhases = 20;
 void dgs_phase(smg_ctx* c, int l, double* x, const double* b, int ph) {
     DevLevel& L = c->lv[l];
+    if (L.k.tiled) {  // arg = phase + 32 T: one phase on the tiles of colour T
+        const int T = ph >> 5;
+        ph &= 31;
+        if (T > 7 || ph >= kDgsPhases) throw SmgError(SMG_EINVAL, "bad DGS phase / tile colour");
+        if (ph >= 10 && ph <= 17) launch_dgs_cb(L.k, b, c->st);
+        launch_dgs_tile_phases(L.k, x, b, T, ph, ph + 1, c->st);
+        return;
+    }
     if (ph == 0 || ph == 1) {
         launch_dgs_vel(L.k, x, b, ph, c->st);
     } else if (ph >= 2 && ph <= 9) {
@@ -721,8 +693,8 @@ void symmetric_dgs(smg_ctx* c, int l, double* x, const double* b, bool cb_ready 
     const int nph = (c->prm.flags & SMG_FLAG_SKIP_REVERSE_DGS) ? kDgsPhases / 2 : kDgsPhases;
     DevLevel& L = c->lv[l];
     if (nph > kDgsPhases / 2 && !cb_ready) launch_dgs_cb(L.k, b, c->st);  // m_C^T b for the reverse steps
-    if (!L.wave.empty()) {
-        launch_dgs_wave(L.k, L.wave.data(), static_cast<int>(L.wave.size()), x, b, L.pd0, c->st);
+    if (L.k.tiled) {
+        launch_dgs_tiled(L.k, x, b, nph, c->st);
         return;
     }
     launch_dgs_sym_coop(L.k, x, b, L.pd0, L.pd1, nph, c->st, L.xb);
@@ -741,23 +713,10 @@ void vanka_additive(smg_ctx* c, int l, double* x, const double* b) {
 }
 
 void smooth(smg_ctx* c, int l, double* x, const double* b, bool cb_ready = false) {
-    DevLevel& L = c->lv[l];
     if (c->prm.vanka == 1) {  // Alg. 3 with additive Vanka on V1
         for (int k = 0; k < c->prm.nu; ++k) vanka_additive(c, l, x, b);
         symmetric_dgs(c, l, x, b, cb_ready);
         for (int k = 0; k < c->prm.nu; ++k) vanka_additive(c, l, x, b);
-        return;
-    }
-    if (!cb_ready && (smooth_dsm_fits(L.k, L.sw_n) || smooth_smem_fits(L.k, L.sw_n))) launch_dgs_cb(L.k, b, c->st);
-    if (smooth_dsm_fits(L.k, L.sw_n)) {
-        const int nph = (c->prm.flags & SMG_FLAG_SKIP_REVERSE_DGS) ? kDgsPhases / 2 : kDgsPhases;
-        launch_smooth_dsm(L.k, x, b, L.sw_cells, L.sw_mask, L.sw_n, L.ktab, c->prm.nu, nph, c->st, L.sw_pairs);
-        return;
-    }
-    if (smooth_smem_fits(L.k, L.sw_n)) {
-        const int nph = (c->prm.flags & SMG_FLAG_SKIP_REVERSE_DGS) ? kDgsPhases / 2 : kDgsPhases;
-        launch_smooth_smem(L.k, x, b, L.sw_cells, L.sw_mask, L.sw_n, L.ktab, L.pd0, L.pd1, c->prm.nu, nph, c->st,
-                           L.sw_pairs);
         return;
     }
     vanka_sym_coop(c, l, x, b);
@@ -777,12 +736,8 @@ void vcycle(smg_ctx* c, int l, const double* b, double* x) {
     if (cb) launch_dgs_cb(L.k, b, c->st);  // m_C^T b once for both smooths of this visit
     smooth(c, l, x, b, cb);
     DevLevel& C = c->lv[l + 1];
-    if (resrestrict_ok(L.k, C.k)) {
-        launch_residual_restrict(L.k, C.k, x, b, C.b, c->st);  // b_c = R (b - L~ x), one pass
-    } else {
-        launch_apply(L.k, x, b, L.r, L.k.gamma, c->st);
-        launch_restrict(L.k, C.k, L.r, C.b, c->st);
-    }
+    launch_apply(L.k, x, b, L.r, L.k.gamma, c->st);
+    launch_restrict(L.k, C.k, L.r, C.b, c->st);
     vcycle(c, l + 1, C.b, C.x);
     // W-cycle: second recursive call below the finest level, on the residual of
     // the first (skipped when the child is the exact coarsest solve)
@@ -804,25 +759,17 @@ void sqmr_iteration(smg_ctx* c) {
     const int64_t n = vlen(F);
     double *s = F.b, *t = F.x, *r = F.r, *sc = c->dscal;
     const Geom& g = F.k.g;
-    if (c->fused_dot) {  // t = L q, sigma = q.t, alpha: one kernel
-        launch_apply_dot(F.k, c->q, nullptr, t, 0.0, 0, c->dot_rows, c->partials, sc, c->dot_done, 1, c->st);
-    } else {
-        launch_apply(F.k, c->q, nullptr, t, 0.0, c->st);                     // t = L q
-        launch_cdot2(g, c->q, t, nullptr, nullptr, c->partials, sc + S_D0, c->st);  // sigma
-        launch_sqmr_scalar(1, sc, c->st);                                    // alpha
-    }
+    launch_apply(F.k, c->q, nullptr, t, 0.0, c->st);                     // t = L q
+    launch_cdot2(g, c->q, t, nullptr, nullptr, c->partials, sc + S_D0, c->st);  // sigma
+    launch_sqmr_scalar(1, sc, c->st);                                    // alpha
     launch_axpy_s(s, t, sc, n, c->st);                                   // s -= alpha t
     vcycle(c, 0, s, t);                                                  // t = V(s)
     launch_cdot2(g, t, t, s, t, c->partials, sc + S_D0, c->st);          // ||t||^2, rho_j
     launch_sqmr_scalar(2, sc, c->st);                                    // nu, c, tau, cd, cq
     launch_dx_dev(c->d, c->xs, c->q, sc, n, c->st);                      // d, x
-    if (c->fused_dot) {  // r = b - L x, ||r||^2, rel and beta: one kernel
-        launch_apply_dot(F.k, c->xs, c->rhs, r, 0.0, 1, c->dot_rows, c->partials, sc, c->dot_done, 3, c->st);
-    } else {
-        launch_apply(F.k, c->xs, c->rhs, r, 0.0, c->st);                     // r = b - L x
-        launch_cdot2(g, r, r, nullptr, nullptr, c->partials, sc + S_D0, c->st);
-        launch_sqmr_scalar(3, sc, c->st);                                    // rel, beta
-    }
+    launch_apply(F.k, c->xs, c->rhs, r, 0.0, c->st);                     // r = b - L x
+    launch_cdot2(g, r, r, nullptr, nullptr, c->partials, sc + S_D0, c->st);
+    launch_sqmr_scalar(3, sc, c->st);                                    // rel, beta
     launch_xpby_dev(c->q, t, sc, n, c->st);                              // q = t + beta q
 }
 
@@ -1159,9 +1106,72 @@ void dist_vanka_sym(smg_ctx* m, int l) {
         }
 }
 
+// Tiled slab level, after a forward tile phase of colour T: a part's boundary tiles of that
+// colour have updated the pressures (and, at the top, the w faces) of the neighbour's first
+// plane, which the part holds as a ghost plane.  Exactly one side of every slab boundary ran
+// (the two boundary tile layers differ in z parity), and its ghost plane was current before
+// the phase, so that side pushes the whole plane to the owner: up (P and W of ghost plane nz
+// -> the upper part's plane 0) when the lower part's top tile layer has T's z parity, else
+// down (P of ghost plane -1 -> the lower part's plane nz - 1).
+void push_ghosts(smg_ctx* m, int l, int T) {
+    const Geom& g0 = m->lv[l].k.g;
+    const int tz = dgs_tile_dim(2);
+    // z parity of the top tile layer of part r: ((z0 + nzl) / tz - 1) & 1, z0 = r nzl
+    auto top_ran = [&](int r) { return ((((r + 1) * g0.nz) / tz - 1) & 1) == ((T >> 2) & 1); };
+    if (m->mp) {
+        const NcclApi& N = nccl();
+        const Geom& g = g0;
+        double* X = m->lv[l].x;
+        const size_t n1 = static_cast<size_t>(g.sz);
+        NK(N.groupStart());
+        const int r = m->rank;
+        if (r + 1 < m->nparts) {  // boundary with the upper part
+            if (top_ran(r)) {
+                for (int f : {2, 3}) NK(N.send(X + f * g.fs + (g.zg + g.nz) * g.sz, n1, ncclDouble, r + 1, m->comm, m->st));
+            } else {
+                NK(N.recv(X + 3 * g.fs + (g.zg + g.nz - 1) * g.sz, n1, ncclDouble, r + 1, m->comm, m->st));
+            }
+        }
+        if (r > 0) {  // boundary with the lower part
+            if (top_ran(r - 1)) {
+                for (int f : {2, 3}) NK(N.recv(X + f * g.fs + g.zg * g.sz, n1, ncclDouble, r - 1, m->comm, m->st));
+            } else {
+                NK(N.send(X + 3 * g.fs + (g.zg - 1) * g.sz, n1, ncclDouble, r - 1, m->comm, m->st));
+            }
+        }
+        NK(N.groupEnd());
+        return;
+    }
+    part_barrier(m);
+    for (size_t p = 0; p + 1 < m->parts.size(); ++p) {
+        DevLevel &lo = m->parts[p]->lv[l], &hi = m->parts[p + 1]->lv[l];
+        const Geom& g = lo.k.g;
+        const size_t pitch = g.fs * sizeof(double), width = g.sz * sizeof(double);
+        if (top_ran(static_cast<int>(p))) {  // W, P of lo's ghost plane nz -> hi's plane 0
+            CK(cudaMemcpy2DAsync(hi.x + 2 * g.fs + g.zg * g.sz, pitch, lo.x + 2 * g.fs + (g.zg + g.nz) * g.sz, pitch,
+                                 width, 2, cudaMemcpyDefault, m->parts[p + 1]->st));
+        } else {  // P of hi's ghost plane -1 -> lo's plane nz - 1
+            CK(cudaMemcpyAsync(lo.x + 3 * g.fs + (g.zg + g.nz - 1) * g.sz, hi.x + 3 * g.fs + (g.zg - 1) * g.sz,
+                               width, cudaMemcpyDefault, m->parts[p]->st));
+        }
+    }
+    part_barrier(m);
+}
+
 void dist_dgs_sym(smg_ctx* m, int l) {
     const int nph = (m->prm.flags & SMG_FLAG_SKIP_REVERSE_DGS) ? 10 : 20;
     each(m, [&](smg_ctx* p) { launch_dgs_cb(p->lv[l].k, p->lv[l].b, p->st); });  // b halos are valid here
+    if (m->lv[l].k.tiled) {  // tile order (OD-1 rev. 2): one launch + one exchange per tile colour
+        auto phase = [&](int T, int ph0, int ph1) {
+            each(m, [&](smg_ctx* p) { launch_dgs_tile_phases(p->lv[l].k, p->lv[l].x, p->lv[l].b, T, ph0, ph1, p->st); });
+            if (ph0 < 10) push_ghosts(m, l, T);
+            exchange(m, l, sel_x, 4);
+        };
+        for (int T = 0; T < 8; ++T) phase(T, 0, (T == 7 && nph > 10) ? 20 : 10);
+        if (nph > 10)
+            for (int T = 6; T >= 0; --T) phase(T, 10, 20);
+        return;
+    }
     for (int ph = 0; ph < nph; ++ph) {
         if (ph == 0 || ph == 1 || ph == 18 || ph == 19) {
             const int col = ph < 2 ? ph : 19 - ph;
@@ -1211,6 +1221,25 @@ void dist_vcycle(smg_ctx* m, int l) {
     else allgather_planes(m, l + 1, sel_b, m->lv[l].k.g.nz / 2);
     dist_vcycle(m, l + 1);
     if (cdist) exchange(m, l + 1, sel_x, 4);
+    // W-cycle: second recursive call below the finest level on the residual of the
+    // first, as in the single-part vcycle (skipped when the child is the exact coarsest solve)
+    if (m->prm.cycle == 1 && l >= 1 && l + 2 < static_cast<int>(m->lv.size())) {
+        each(m, [&](smg_ctx* p) {
+            DevLevel& C = p->lv[l + 1];
+            launch_apply(C.k, C.x, C.b, C.wb, C.k.gamma, p->st);
+            std::swap(C.b, C.wb);  // the recursion reads lv[l+1].b and writes lv[l+1].x
+            std::swap(C.x, C.wx);
+        });
+        if (cdist) exchange(m, l + 1, sel_b, 4);
+        dist_vcycle(m, l + 1);
+        if (cdist) exchange(m, l + 1, sel_x, 4);
+        each(m, [&](smg_ctx* p) {
+            DevLevel& C = p->lv[l + 1];
+            std::swap(C.b, C.wb);
+            std::swap(C.x, C.wx);
+            launch_axpy(C.x, C.wx, 1.0, vlen(C), p->st);
+        });
+    }
     each(m, [&](smg_ctx* p) { launch_prolong_add(p->lv[l].k, p->lv[l + 1].k, p->lv[l + 1].x, p->lv[l].x, p->st); });
     exchange(m, l, sel_x, 4);
     dist_smooth(m, l);
@@ -1470,21 +1499,27 @@ int64_t smg_census(const smg_grid_desc* grid, int band_width, int64_t* out2) {
     return n;
 }
 
-// leading levels that split into nparts z-slabs (slab >= 2 planes, aligned with the finer level)
-static int slab_levels(const smg_grid_desc* grid, int levels, int nparts) {
+// leading levels that split into nparts z-slabs (slab >= 2 planes, aligned with the finer level;
+// on DGS-tiled levels a whole number of tiles, so every tile lies in one part)
+static int slab_levels(const smg_grid_desc* grid, int levels, int nparts, int64_t tile_min) {
     int nd = 0;
     for (int l = 0; l + 1 < levels; ++l) {
         const int nz = grid->nz >> l;
-        if (nz % nparts || nz / nparts < 2) break;                    // slab of >= 2 planes (halo depth)
-        if (l > 0 && ((grid->nz >> (l - 1)) / nparts) % 2) break;    // slab boundaries aligned with level l-1
+        if (dgs_tiled(grid->nx >> l, grid->ny >> l, nz, tile_min) && (nz % nparts || (nz / nparts) % dgs_tile_dim(2)))
+            break;
+        // slab of >= 2 planes (halo depth), and even: the child level's planes 2k, 2k+1 then
+        // always sit in one slab, so restriction into a slab (or into the replicated first
+        // level, coarse planes z0/2 .. (z0 + nzl)/2) covers every coarse plane
+        if (nz % nparts || nz / nparts < 2 || (nz / nparts) % 2) break;
         nd = l + 1;
     }
     return nd;
 }
 
-int smg_slab_plan(const smg_grid_desc* grid, int levels, int nparts, int rank, int* z0, int* nzl) {
+static int slab_plan_t(const smg_grid_desc* grid, int levels, int nparts, int rank, int* z0, int* nzl,
+                       int64_t tile_min) {
     if (!grid || levels < 1 || nparts < 1 || rank < 0 || rank >= nparts) return SMG_EINVAL;
-    const int nd = nparts > 1 ? slab_levels(grid, levels, nparts) : 0;
+    const int nd = nparts > 1 ? slab_levels(grid, levels, nparts, tile_min) : 0;
     for (int l = 0; l < levels; ++l) {
         const int nz = grid->nz >> l;
         const bool d = l < nd;
@@ -1492,6 +1527,16 @@ int smg_slab_plan(const smg_grid_desc* grid, int levels, int nparts, int rank, i
         if (nzl) nzl[l] = d ? nz / nparts : nz;
     }
     return nd;
+}
+int smg_slab_plan(const smg_grid_desc* grid, int levels, int nparts, int rank, int* z0, int* nzl) {
+    return slab_plan_t(grid, levels, nparts, rank, z0, nzl, 0);
+}
+int smg_dgs_tile(const smg_grid_desc* grid, int level, int64_t tile_min, int* out4) {
+    if (!grid || !out4 || level < 0 || level > 20) return SMG_EINVAL;
+    const bool t = dgs_tiled(grid->nx >> level, grid->ny >> level, grid->nz >> level, tile_min);
+    out4[0] = t ? 8 : 1;
+    for (int a = 0; a < 3; ++a) out4[1 + a] = t ? dgs_tile_dim(a) : 0;
+    return 0;
 }
 
 int smg_create(const smg_grid_desc* grid, const smg_params* params, int ngpu, const int* dev_ids, smg_ctx** out) {
@@ -1507,7 +1552,7 @@ int smg_create(const smg_grid_desc* grid, const smg_params* params, int ngpu, co
     const int rc = guard(c.get(), [&] {
         if (ngpu > 1) {
             // levels split into z-slabs: slab >= 2 planes, aligned with the next level
-            const int nd = smg_slab_plan(grid, params->levels, ngpu, 0, nullptr, nullptr);
+            const int nd = slab_plan_t(grid, params->levels, ngpu, 0, nullptr, nullptr, params->dgs_tile_min);
             if (nd <= 0) throw SmgError(SMG_EINVAL, "grid too small for a z-slab split over ngpu parts");
             c->ndist = nd;
         }
@@ -1578,7 +1623,7 @@ int smg_create_rank(const smg_grid_desc* grid, const smg_params* params, int ran
         // SMG_FORCE_SLABS=1 with one rank: the slab path on one part (exercises the NCCL transport on one GPU)
         const bool force = nranks == 1 && std::getenv("SMG_FORCE_SLABS") && std::atoi(std::getenv("SMG_FORCE_SLABS"));
         if (nranks > 1 || force) {
-            const int nd = slab_levels(grid, params->levels, nranks);
+            const int nd = slab_levels(grid, params->levels, nranks, params->dgs_tile_min);
             if (nd <= 0) throw SmgError(SMG_EINVAL, "grid too small for a z-slab split over nranks parts");
             c->ndist = nd;
         } else {
@@ -1666,7 +1711,14 @@ int smg_smoother(smg_ctx* c, int level, int op, int arg, double* x, const double
         } else if (op == 5) {  // one additive Vanka application
             vanka_additive(c, level, L.x, L.b);
         } else if (op == 6) {  // per-phase reference path of the symmetric sweeps (test only)
-            for (int ph = 0; ph < kDgsPhases; ++ph) dgs_phase(c, level, L.x, L.b, ph);
+            if (L.k.tiled) {
+                for (int T = 0; T < 8; ++T)
+                    for (int ph = 0; ph < kDgsPhases / 2; ++ph) dgs_phase(c, level, L.x, L.b, ph + 32 * T);
+                for (int T = 7; T >= 0; --T)
+                    for (int ph = kDgsPhases / 2; ph < kDgsPhases; ++ph) dgs_phase(c, level, L.x, L.b, ph + 32 * T);
+            } else {
+                for (int ph = 0; ph < kDgsPhases; ++ph) dgs_phase(c, level, L.x, L.b, ph);
+            }
             vanka_sym(c, level, L.x, L.b);
         }
         else if (op == 4) smooth(c, level, L.x, L.b);

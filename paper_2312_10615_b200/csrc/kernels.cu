@@ -14,6 +14,7 @@
 #include <cstdlib>
 
 #include <cooperative_groups.h>
+#include <cuda.h>
 
 #include "smg_internal.h"
 
@@ -423,107 +424,6 @@ __global__ void __launch_bounds__(256, SMG_RZM_MINB) k_restrict_zm(LevelK F, Lev
     }
 }
 
-// Fused residual + restriction: b_c = R (b - L~ x) without materialising the fine
-// residual.  A CTA owns a 16 x 8 tile of coarse cells and marches over a range of
-// coarse planes; the fine residual of the tile's footprint (fine x 2X0-1 .. 2X0+32,
-// y 2Y0-1 .. 2Y0+16) lives in a 4-plane shared-memory ring (fine planes 2Z-1 .. 2Z+2),
-// two new planes per coarse plane.  Residual values are k_apply's, the restriction
-// sums restrict_face's in the same order: bit-identical to apply + restrict.
-// Opt-in (SMG_FUSED_RR=1): measured slower than the two separate kernels (cfg 3
-// iteration 71.8 -> 74.7 ms; the residual fill of the smem ring is latency-bound
-// at 2 CTAs/SM, while k_apply + k_restrict stream at 5 and 3.4 TB/s).
-constexpr int RR_TX = 16, RR_TY = 8, RR_FX = 2 * RR_TX + 2, RR_FY = 2 * RR_TY + 2;
-constexpr int RR_PLANE = RR_FX * RR_FY;  // one fine plane of one field
-__device__ __forceinline__ int rr_ring(int zf) { return (zf + 4) & 3; }
-
-__global__ void __launch_bounds__(512) k_resrestrict(LevelK F, LevelK C, const double* __restrict__ X,
-                                                     const double* __restrict__ B, double* __restrict__ BC,
-                                                     int zseg) {
-    pdl_wait();
-    extern __shared__ double rs[];  // [4 fields][4 ring planes][RR_FY][RR_FX]
-    const Geom &fg = F.g, &cg = C.g;
-    const int X0 = blockIdx.x * RR_TX, Y0 = blockIdx.y * RR_TY;
-    const int Zs = blockIdx.z * zseg, Ze = min(Zs + zseg, cg.nz);
-    const int64_t fs = fg.fs;
-    const double *U = X, *V = X + fs, *W = X + 2 * fs, *P = X + 3 * fs;
-    const int fx0 = 2 * X0 - 1, fy0 = 2 * Y0 - 1;
-    // fine residual of plane zf (all four fields) over the tile footprint -> ring
-    auto fill = [&](int zf) {
-        double* dst = rs + rr_ring(zf) * RR_PLANE;
-#pragma unroll 2
-        for (int k = threadIdx.x; k < RR_PLANE; k += blockDim.x) {
-            const int yy = k / RR_FX, xx = k - yy * RR_FX;
-            const int x = fx0 + xx, y = fy0 + yy;
-            double ru = 0.0, rv = 0.0, rw = 0.0, rp = 0.0;
-            if (x >= 0 && x < fg.nx && y >= 0 && y < fg.ny && zf >= 0 && zf < fg.nz) {
-                const int64_t i = fg.slot(x, y, zf);
-                if (x >= 1) ru = B[i] - mom(F, U, P, i, 1);
-                if (y >= 1) rv = B[fs + i] - mom(F, V, P, i, fg.sy);
-                if (fg.gz(zf) >= 1) rw = B[2 * fs + i] - mom(F, W, P, i, fg.sz);
-                rp = B[3 * fs + i] - cont(F, U, V, W, P, i, F.gamma);
-            }
-            dst[k] = ru;
-            dst[4 * RR_PLANE + k] = rv;
-            dst[8 * RR_PLANE + k] = rw;
-            dst[12 * RR_PLANE + k] = rp;
-        }
-    };
-    fill(2 * Zs - 1);
-    fill(2 * Zs);
-    const int tx = threadIdx.x % RR_TX, ty = threadIdx.x / RR_TX;  // threads 0..127: one coarse cell
-    const int cx = X0 + tx, cy = Y0 + ty;
-    const double wI[3] = {0.5, 1.0, 0.5};
-    const double wT[4] = {0.25, 0.75, 0.75, 0.25};
-    for (int Z = Zs; Z < Ze; ++Z) {
-        fill(2 * Z + 1);
-        fill(2 * Z + 2);
-        __syncthreads();
-        if (threadIdx.x < RR_TX * RR_TY && cx < cg.nx && cy < cg.ny) {
-            // fine (2cx + dx, 2cy + dy, 2Z + dz) -> smem, dx, dy, dz in -1..2
-            auto R = [&](int f, int dx, int dy, int dz) {
-                return rs[(f * 4 + rr_ring(2 * Z + dz)) * RR_PLANE + (2 * ty + 1 + dy) * RR_FX + (2 * tx + 1 + dx)];
-            };
-            // restrict_face: normal innermost, then tangential a, then b
-            auto face = [&](int f) {
-                double acc_b = 0.0;
-#pragma unroll
-                for (int ib = 0; ib < 4; ++ib) {
-                    double acc_a = 0.0;
-#pragma unroll
-                    for (int ia = 0; ia < 4; ++ia) {
-                        double sn_ = 0.0;
-#pragma unroll
-                        for (int in = 0; in < 3; ++in) {
-                            int d[3];
-                            const int n = f, a = f == 0 ? 1 : 0, b = f == 2 ? 1 : 2;
-                            d[n] = in - 1;
-                            d[a] = ia - 1;
-                            d[b] = ib - 1;
-                            sn_ = sn_ + wI[in] * R(f, d[0], d[1], d[2]);
-                        }
-                        acc_a = acc_a + wT[ia] * sn_;
-                    }
-                    acc_b = acc_b + wT[ib] * acc_a;
-                }
-                return 0.125 * acc_b;
-            };
-            const int64_t ci = cg.slot(cx, cy, Z);
-            const int64_t cfs = cg.fs;
-            if (cx >= 1) BC[ci] = face(0);
-            if (cy >= 1) BC[cfs + ci] = face(1);
-            if (cg.gz(Z) >= 1) BC[2 * cfs + ci] = face(2);
-            double sp = 0.0;
-#pragma unroll
-            for (int k = 0; k < 2; ++k)
-#pragma unroll
-                for (int j = 0; j < 2; ++j)
-#pragma unroll
-                    for (int ii = 0; ii < 2; ++ii) sp = sp + R(3, ii, j, k);
-            BC[3 * cfs + ci] = 0.125 * sp;
-        }
-        __syncthreads();  // ring planes 2Z-1, 2Z are overwritten next
-    }
-}
 
 // Prolongation x_f += P e_c.  Tangential legs of fine index J:
 // (J>>1, 3/4) then (J odd ? (J>>1)+1 : (J>>1)-1, 1/4); normal: I even ->
@@ -585,114 +485,6 @@ __global__ void k_prolong_add(LevelK F, LevelK C, const double* __restrict__ E, 
     X[3 * ffs + c.i] = X[3 * ffs + c.i] + E[3 * cfs + cg.slot(c.x >> 1, c.y >> 1, (z >> 1) - cg.z0)];
 }
 
-// z-marching prolongation: a thread owns one fine column (x, y) and walks a segment of fine
-// plane pairs (2K, 2K+1).  For u and v the tangential-b axis is z: prolong_face's
-// sa = 0.75 sn(base) + 0.25 sn(base + da) depends on the coarse plane only (the column fixes
-// da and the normal parity), so it is computed once per coarse plane and reused by the four
-// fine planes 2K-1 .. 2K+2 that reference it.  For w the normal axis is z: the four coarse
-// values of plane K+1 are carried to the next pair; the pressure parent is loaded once per
-// pair.  Same operations in the same order as k_prolong_add: bit-identical.
-template <int COMP>
-__device__ __forceinline__ double prolong_sa(const double* __restrict__ E, int64_t base, int64_t da, int64_t dn,
-                                             bool odd) {
-    auto sn = [&](int64_t o) {
-        double s = 0.0;
-        if (!odd) {
-            s = s + 1.0 * E[o];
-        } else {
-            s = s + 0.5 * E[o];
-            s = s + 0.5 * E[o + dn];
-        }
-        return s;
-    };
-    const double s00 = sn(base), s01 = sn(base + da);
-    double sa = 0.0;
-    sa = sa + 0.75 * s00;
-    sa = sa + 0.25 * s01;
-    return sa;
-}
-
-__global__ void __launch_bounds__(256) k_prolong_zm(LevelK F, LevelK C, const double* __restrict__ E,
-                                                    double* __restrict__ X, int zpairs) {
-    pdl_wait();
-    const Geom &fg = F.g, &cg = C.g;
-    const int x = blockIdx.x * BX + threadIdx.x, y = blockIdx.y * BY + threadIdx.y;
-    if (x >= fg.nx || y >= fg.ny) return;
-    const int zl0 = 2 * blockIdx.z * zpairs, zl1 = min(zl0 + 2 * zpairs, fg.nz);  // local fine planes
-    if (zl0 >= zl1) return;
-    const int64_t ffs = fg.fs, cfs = cg.fs;
-    const double *EU = E, *EV = E + cfs, *EW = E + 2 * cfs, *EP = E + 3 * cfs;
-    const int cx = x >> 1, cy = y >> 1;
-    const int64_t dxs = (x & 1) ? 1 : -1, dys = (y & 1) ? cg.sy : -cg.sy;
-    // coarse local plane of the pair (global fine plane gz(zl0) is even)
-    const int K0 = (fg.gz(zl0) >> 1) - cg.z0;
-    auto cslot = [&](int K) { return cg.slot(cx, cy, K); };
-    // u: normal x (parity x&1), a = y (da = dys).  v: normal y, a = x (da = dxs).
-    const bool ox = x & 1, oy = y & 1;
-    double su_m = prolong_sa<0>(EU, cslot(K0 - 1), dys, 1, ox), su_0 = prolong_sa<0>(EU, cslot(K0), dys, 1, ox);
-    double sv_m = prolong_sa<1>(EV, cslot(K0 - 1), dxs, cg.sy, oy), sv_0 = prolong_sa<1>(EV, cslot(K0), dxs, cg.sy, oy);
-    // w at coarse plane K: legs base, base + da (x), base + db (y), base + db + da
-    double w00 = EW[cslot(K0)], w01 = EW[cslot(K0) + dxs], w10 = EW[cslot(K0) + dys], w11 = EW[cslot(K0) + dys + dxs];
-    for (int zl = zl0, K = K0; zl < zl1; zl += 2, ++K) {
-        const int64_t cb1 = cslot(K + 1);
-        const double su_p = prolong_sa<0>(EU, cb1, dys, 1, ox);
-        const double sv_p = prolong_sa<1>(EV, cb1, dxs, cg.sy, oy);
-        const double n00 = EW[cb1], n01 = EW[cb1 + dxs], n10 = EW[cb1 + dys], n11 = EW[cb1 + dys + dxs];
-        const double ep = EP[cslot(K)];
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int z = zl + h;
-            if (z >= zl1) break;
-            const int64_t i = fg.slot(x, y, z);
-            // b = z legs: even fine z -> (K, 3/4), (K-1, 1/4); odd -> (K, 3/4), (K+1, 1/4)
-            if (x >= 1) {
-                double sb = 0.0;
-                sb = sb + 0.75 * su_0;
-                sb = sb + 0.25 * (h ? su_p : su_m);
-                X[i] = X[i] + sb;
-            }
-            if (y >= 1) {
-                double sb = 0.0;
-                sb = sb + 0.75 * sv_0;
-                sb = sb + 0.25 * (h ? sv_p : sv_m);
-                X[ffs + i] = X[ffs + i] + sb;
-            }
-            if (fg.gz(z) >= 1) {
-                // normal z: even -> plane K (weight 1); odd -> K and K+1 (1/2 each)
-                auto sn = [&](double a, double b) {
-                    double s = 0.0;
-                    if (!h) {
-                        s = s + 1.0 * a;
-                    } else {
-                        s = s + 0.5 * a;
-                        s = s + 0.5 * b;
-                    }
-                    return s;
-                };
-                const double s00 = sn(w00, n00), s01 = sn(w01, n01), s10 = sn(w10, n10), s11 = sn(w11, n11);
-                double sb = 0.0;
-                double sa = 0.0;
-                sa = sa + 0.75 * s00;
-                sa = sa + 0.25 * s01;
-                sb = sb + 0.75 * sa;
-                sa = 0.0;
-                sa = sa + 0.75 * s10;
-                sa = sa + 0.25 * s11;
-                sb = sb + 0.25 * sa;
-                X[2 * ffs + i] = X[2 * ffs + i] + sb;
-            }
-            X[3 * ffs + i] = X[3 * ffs + i] + ep;
-        }
-        su_m = su_0;
-        su_0 = su_p;
-        sv_m = sv_0;
-        sv_0 = sv_p;
-        w00 = n00;
-        w01 = n01;
-        w10 = n10;
-        w11 = n11;
-    }
-}
 
 // ------------------------------------------------------------- coarse ------
 // x = K b with the symmetric dense inverse K (OD-4).  Fixed order: partial sums
@@ -1386,7 +1178,13 @@ __device__ __forceinline__ void dgs_vel_cell(const LevelK& L, AX X, const double
 // p_i + (c_b - m_i^T L~x) / d_p, with c_b = m_i^T b from L.cb (k_dgs_cb) and the
 // L~x part in the same operation order.  Reads only x around the cell (radius 2).
 template <class AX>
+__device__ __forceinline__ double prev_core(const LevelK& L, AX X, int64_t i, double cbv);
+template <class AX>
 __device__ __forceinline__ double prev_value(const LevelK& L, AX X, int64_t i) {
+    return prev_core(L, X, i, L.cb[i]);
+}
+template <class AX>
+__device__ __forceinline__ double prev_core(const LevelK& L, AX X, int64_t i, double cbv) {
     const Geom& g = L.g;
     const int64_t fs = g.fs, sy = g.sy, sz = g.sz;
     const auto U = X, V = X + fs, W = X + 2 * fs, P = X + 3 * fs;
@@ -1404,24 +1202,12 @@ __device__ __forceinline__ double prev_value(const LevelK& L, AX X, int64_t i) {
     s = s + cont(L, U, V, W, P, i - sz, L.gamma);
     s = s + cont(L, U, V, W, P, i + sz, L.gamma);
     const double cl = fl * L.inv_h + L.eta_h2 * (6.0 * lc - s);
-    return P[i] + (L.cb[i] - cl) / L.dp;
+    return P[i] + (cbv - cl) / L.dp;
 }
 template <class AX>
 __device__ __forceinline__ void dgs_prev_cell(const LevelK& L, AX X, const double* __restrict__ B, int64_t i) {
     (void)B;
     X[3 * L.g.fs + i] = prev_value(L, X, i);
-}
-
-// cells of parity colour c: t -> (x,y,z) on the half-grid of that parity
-__device__ __forceinline__ bool colour_cell(const Geom& g, int c, int64_t t, int& x, int& y, int& z) {
-    const int px = c & 1, py = (c >> 1) & 1, pz = ((c >> 2) ^ g.z0) & 1;  // local z parity
-    const int hx = (g.nx - px + 1) >> 1, hy = (g.ny - py + 1) >> 1, hz = (g.nz - pz + 1) >> 1;
-    if (t >= static_cast<int64_t>(hx) * hy * hz) return false;
-    const int64_t r = t / hx;
-    x = 2 * static_cast<int>(t - r * hx) + px;
-    y = 2 * static_cast<int>(r % hy) + py;
-    z = 2 * static_cast<int>(r / hy) + pz;
-    return true;
 }
 
 // ---- lazy-gather forward pressure phases (single-part levels) ----
@@ -1577,175 +1363,6 @@ __host__ __device__ constexpr int rev_group(int q) {
                   : q == 1 ? colour_group(6, 5, 3, 3) : q == 2 ? colour_group(4, 2, 1, 3) : colour_group(0, 0, 0, 1);
 }
 
-// Symmetric DGS sweep (OD-1) in one persistent launch: velocity red, black,
-// the 4 forward pressure groups (lazy gathers, one combined delta buffer D0),
-// the flush, then (nph = 20) the 4 reverse pressure groups and velocity
-// black, red: 13 barrier-separated steps for the 20 phases.
-template <int MODE, class AX = double*, class AD = double*>
-__device__ __forceinline__ void dgs_sweep(const LevelK& L, AX X, const double* __restrict__ B, AD D0, AD D1, int nph,
-                                          int64_t tid, int64_t nth) {
-    (void)D1;
-    const Geom& g = L.g;
-    const int64_t ncell = static_cast<int64_t>(g.nx) * g.ny * g.nz;
-    const int64_t nxy = static_cast<int64_t>(g.nx) * g.ny;
-    auto vel = [&](int colour) {
-        if ((g.nx & 1) == 0) {  // this colour's cells only, two per step (loads of both first)
-            const int hx = g.nx >> 1;
-            const int64_t nc = static_cast<int64_t>(hx) * g.ny * g.nz;
-            auto cell = [&](int64_t t, int& x, int& y, int& z) {
-                const int64_t r = t / hx;
-                y = static_cast<int>(r % g.ny);
-                z = static_cast<int>(r / g.ny);
-                x = 2 * static_cast<int>(t - r * hx) + ((y + g.gz(z) + colour) & 1);
-            };
-            for (int64_t t = tid; t < nc; t += 2 * nth) {
-                int x0, y0, z0, x1 = 0, y1 = 0, z1 = 0;
-                cell(t, x0, y0, z0);
-                const bool v1 = t + nth < nc;
-                if (v1) cell(t + nth, x1, y1, z1);
-                const VelUpd a = vel_load(L, X, B, x0, y0, z0, true);
-                const VelUpd b = vel_load(L, X, B, x1, y1, z1, v1);
-                vel_store(L, X, a);
-                vel_store(L, X, b);
-            }
-        } else {
-            for (int64_t t = tid; t < ncell; t += nth) {
-                const int z = static_cast<int>(t / nxy);
-                const int64_t r = t - z * nxy;
-                const int y = static_cast<int>(r / g.nx), x = static_cast<int>(r - static_cast<int64_t>(y) * g.nx);
-                if (((x + y + g.gz(z)) & 1) == colour) dgs_vel_cell(L, X, B, x, y, z);
-            }
-        }
-    };
-    auto flush = [&]() {
-        auto cell = [&](int64_t t, int& x, int& y, int& z) {
-            z = static_cast<int>(t / nxy);
-            const int64_t r = t - z * nxy;
-            y = static_cast<int>(r / g.nx);
-            x = static_cast<int>(r - static_cast<int64_t>(y) * g.nx);
-        };
-        for (int64_t t = tid; t < ncell; t += 2 * nth) {
-            int x0, y0, z0, x1 = 0, y1 = 0, z1 = 0;
-            cell(t, x0, y0, z0);
-            const bool v1 = t + nth < ncell;
-            if (v1) cell(t + nth, x1, y1, z1);
-            const PfUpd a = pf_load(L, X, B, D0, x0, y0, z0, true, true);
-            const PfUpd b = pf_load(L, X, B, D0, x1, y1, z1, v1, true);
-            pf_store<true>(L, X, D0, a);
-            pf_store<true>(L, X, D0, b);
-        }
-    };
-    vel(0);
-    phase_sync<MODE>();
-    vel(1);
-    phase_sync<MODE>();
-    for (int q = 0; q < 4; ++q) {  // lazy-gather forward pressure groups (see pf_lazy_cell)
-        const int grp = fwd_group(q);
-        for (int k = 0; k < group_size(grp); ++k) {
-            const int c = group_colour(grp, k);
-            int x, y, z;
-            for (int64_t t = tid; colour_cell(g, c, t, x, y, z); t += nth) pf_lazy_cell(L, X, B, D0, x, y, z);
-        }
-        phase_sync<MODE>();
-    }
-    flush();
-    if (nph <= 10) return;
-    phase_sync<MODE>();
-    for (int q = 0; q < 4; ++q) {
-        const int grp = rev_group(q);
-        for (int k = 0; k < group_size(grp); ++k) {
-            const int c = group_colour(grp, k);
-            int x, y, z;
-            for (int64_t t = tid; colour_cell(g, c, t, x, y, z); t += nth)
-                if (!band_cell(L, x, y, z)) dgs_prev_cell(L, X, B, g.slot(x, y, z));
-        }
-        phase_sync<MODE>();
-    }
-    vel(1);
-    phase_sync<MODE>();
-    vel(0);
-}
-
-template <int MODE>
-__global__ void __launch_bounds__(512) k_dgs_sym_coop(LevelK L, double* __restrict__ X, const double* __restrict__ B,
-                                                      double* __restrict__ D0, double* __restrict__ D1, int nph) {
-    dgs_sweep<MODE>(L, X, B, D0, D1, nph, static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x,
-                    static_cast<int64_t>(gridDim.x) * blockDim.x);
-}
-
-// Whole Alg. 3 smooth of a small level in ONE CTA with the level vector held
-// (opt-in, SMG_SMEM_SMOOTH=1: inside the iteration graph the per-step kernels on
-// all SMs measured faster at 16^3, 2.31 -> 2.27 ms per cfg-1 iteration)
-// in shared memory (layout identical to the global one, compact geometry):
-// every phase barrier is a __syncthreads, no global fences.  b and the DGS
-// delta buffers stay in global memory (visible within the CTA at barriers).
-template <int CPT>
-__global__ void __launch_bounds__(512) k_smooth_smem(LevelK L, double* __restrict__ Xg, const double* __restrict__ B,
-                                                      VankaLists vl, const double* __restrict__ ktab,
-                                                      double* __restrict__ D0, double* __restrict__ D1, int nu,
-                                                      int nph) {
-    extern __shared__ double smem[];
-    double* Ks = smem;
-    double* X = smem + 64 * 49;
-    const int64_t nv = 4 * L.g.fs;
-    for (int k = threadIdx.x; k < 64 * 49; k += blockDim.x) Ks[k] = ktab[k];
-    for (int64_t k = threadIdx.x; k < nv; k += blockDim.x) X[k] = Xg[k];
-    __syncthreads();
-    vanka_sweeps<2, CPT>(L, X, B, vl, Ks, nu, threadIdx.x, blockDim.x);
-    dgs_sweep<2>(L, X, B, D0, D1, nph, threadIdx.x, blockDim.x);
-    __syncthreads();
-    vanka_sweeps<2, CPT>(L, X, B, vl, Ks, nu, threadIdx.x, blockDim.x);
-    for (int64_t k = threadIdx.x; k < nv; k += blockDim.x) Xg[k] = X[k];
-}
-
-// ------------------------------- cluster-resident (DSMEM) smoother -------------
-// Levels whose vector plus DGS delta field fit in the distributed shared memory
-// of one 16-CTA cluster: the linear vector index k lives in CTA k >> 14 at
-// offset k & 16383 (128 KB per CTA).  The whole Alg. 3 smooth then runs with
-// cluster barriers only and every x/delta access is an SM-to-SM DSMEM access
-// (no L2 round trips, no global fences).  b stays in global memory (read-only).
-constexpr int kDsmLog = 14;
-constexpr int kDsmChunk = 1 << kDsmLog;
-constexpr int kDsmCTAs = 16;
-
-struct DAcc {
-    double* const* bases;  // generic addresses of the 16 CTAs' chunks (in shared memory)
-    int64_t off;
-    __device__ __forceinline__ double& operator[](int64_t i) const {
-        const int64_t k = i + off;
-        return bases[k >> kDsmLog][k & (kDsmChunk - 1)];
-    }
-    __device__ __forceinline__ DAcc operator+(int64_t d) const { return DAcc{bases, off + d}; }
-};
-
-__global__ void __launch_bounds__(512) k_smooth_dsm(LevelK L, double* __restrict__ Xg, const double* __restrict__ B,
-                                                    VankaLists vl, const double* __restrict__ ktab, int nu, int nph) {
-    extern __shared__ double dsm[];
-    double* Ks = dsm;
-    double* chunk = dsm + 64 * 49;
-    double** bases = reinterpret_cast<double**>(chunk + kDsmChunk);
-    cg::cluster_group cl = cg::this_cluster();
-    const int rank = static_cast<int>(cl.block_rank()), nct = static_cast<int>(cl.num_blocks());
-    if (threadIdx.x < static_cast<unsigned>(nct)) bases[threadIdx.x] = cl.map_shared_rank(chunk, threadIdx.x);
-    for (int k = threadIdx.x; k < 64 * 49; k += blockDim.x) Ks[k] = ktab[k];
-    const int64_t nv = 4 * L.g.fs;  // x, then the delta field (one field) at [nv, nv + fs)
-    for (int k = threadIdx.x; k < kDsmChunk; k += blockDim.x) {
-        const int64_t idx = static_cast<int64_t>(rank) * kDsmChunk + k;
-        chunk[k] = idx < nv ? Xg[idx] : 0.0;
-    }
-    cl.sync();
-    const DAcc X{bases, 0}, D{bases, nv};
-    const int tid = rank * blockDim.x + threadIdx.x, nth = nct * blockDim.x;
-    vanka_sweeps8<1, 1, DAcc>(L, X, B, vl, Ks, nu, tid, nth);
-    dgs_sweep<1, DAcc, DAcc>(L, X, B, D, D, nph, tid, nth);
-    cl.sync();
-    vanka_sweeps8<1, 1, DAcc>(L, X, B, vl, Ks, nu, tid, nth);
-    cl.sync();
-    for (int k = threadIdx.x; k < kDsmChunk; k += blockDim.x) {
-        const int64_t idx = static_cast<int64_t>(rank) * kDsmChunk + k;
-        if (idx < nv) Xg[idx] = chunk[k];
-    }
-}
 
 // -------------------------------------- colour-compact per-phase DGS kernels ------
 // For large levels: one kernel per phase (graph-captured; a kernel boundary is
@@ -1765,25 +1382,6 @@ __device__ __forceinline__ BlkIdx blk_idx(bool rev) {
 }
 constexpr int kRevBit = 1 << 16;
 
-// Chunked velocity pair: one launch updates colour c0 on planes [za0, za1) and colour c0^1 on
-// planes [zb0, zb1) (disjoint ranges one chunk apart, so neither reads what the other writes).
-// The host walks the level in chunks of C planes: launch j = first colour on chunk j + second
-// colour on chunk j-2.  Second-colour cells of chunk k read first-colour values of chunks k-1..k+1
-// (done in launches <= k+1) and first-colour cells of chunk j read second-colour values of chunk
-// j-1 still untouched (updated in launch j+1): exactly the values the two whole-level phases see,
-// so the result is bit-identical, while the second colour finds its planes in L2.
-__global__ void __launch_bounds__(256) k_dgs_vel_chunk(LevelK L, double* __restrict__ X, const double* __restrict__ B,
-                                                       int c0, int za0, int za1, int zb0) {
-    pdl_wait();
-    const Geom& g = L.g;
-    const int na = za1 - za0;
-    const bool first = static_cast<int>(blockIdx.z) < na;
-    const int z = first ? za0 + static_cast<int>(blockIdx.z) : zb0 + static_cast<int>(blockIdx.z) - na;
-    const int colour = first ? c0 : (c0 ^ 1);
-    const int i = blockIdx.x * 32 + threadIdx.x, y = blockIdx.y * 8 + threadIdx.y;
-    const int x = 2 * i + ((y + g.gz(z) + colour) & 1);
-    if (x < g.nx && y < g.ny) dgs_vel_cell(L, X, B, x, y, z);
-}
 
 // ZC independent cells per thread (planes z, z + gridDim.z, ...): more loads in flight
 template <int ZC>
@@ -1803,282 +1401,6 @@ __global__ void __launch_bounds__(256) k_dgs_vel_c(LevelK L, double* __restrict_
 }
 
 
-// ---- fused velocity pair: colour c0, then colour 1 - c0, in ONE pass Xi -> Xo ----
-// At march step tau a CTA updates the c0 cells of plane tau on its kV2X x kV2Y tile plus a
-// one-cell halo ring (redundantly with the neighbouring tiles: identical inputs, identical
-// arithmetic) into a 3-plane shared-memory ring of post-c0 values, then the 1 - c0 cells of
-// plane tau - 1, whose six same-component neighbours are all c0 positions (held in the ring).
-// Every read of the old state goes to Xi, which nothing writes during the launch; the tile's
-// cells of all four fields (p copied) go to Xo.  CTAs are independent (no inter-CTA sync);
-// a CTA marches zch planes (+1 halo plane on each side).  The per-point operations and their
-// order are those of vel_load / vel_store, hence bit-identical to two k_dgs_vel_c phases.
-constexpr int kV2X = 32, kV2Y = 8, kV2HX = kV2X + 2, kV2H = kV2HX * (kV2Y + 2);
-
-// mom() on explicit operands (same operation order)
-__device__ __forceinline__ double mom_v(const LevelK& L, double c, double xm, double xp, double ym, double yp,
-                                        double zm, double zp, double pr, double pl) {
-    double s = xm + xp;
-    s = s + ym;
-    s = s + yp;
-    s = s + zm;
-    s = s + zp;
-    const double lap = 6.0 * c - s;
-    return L.eta_h2 * lap + (pr - pl) * L.inv_h;
-}
-
-__global__ void __launch_bounds__(256) k_dgs_vel2(LevelK L, const double* __restrict__ Xi, double* __restrict__ Xo,
-                                                  const double* __restrict__ B, int c0, int zch) {
-    pdl_wait();
-    __shared__ double ring[3][3 * kV2H];  // [plane % 3][component * kV2H + halo-tile position]
-    const Geom& g = L.g;
-    const int64_t fs = g.fs, sy = g.sy, sz = g.sz;
-    const int tx0 = blockIdx.x * kV2X, ty0 = blockIdx.y * kV2Y;
-    const int z0 = blockIdx.z * zch, z1 = min(z0 + zch, g.nz);
-    const int tid = threadIdx.x + threadIdx.y * kV2X;
-    const int bx = tx0 + threadIdx.x, by = ty0 + threadIdx.y;
-    const bool bcell = bx < g.nx && by < g.ny;
-    const int kc = (threadIdx.y + 1) * kV2HX + threadIdx.x + 1;
-    for (int tau = z0 - 1; tau <= z1; ++tau) {
-        double* R = ring[(tau + 3) % 3];
-        // phase A: post-c0 state of plane tau on the tile + halo ring
-        for (int k = tid; k < kV2H; k += kV2X * kV2Y) {
-            const int x = tx0 - 1 + k % kV2HX, y = ty0 - 1 + k / kV2HX;
-            if (x > g.nx || y > g.ny) continue;  // never read (black cells have x < nx, y < ny)
-            const int64_t i = g.slot(x, y, tau);
-            double u = Xi[i], v = Xi[fs + i], w = Xi[2 * fs + i];
-            if (x >= 0 && y >= 0 && x < g.nx && y < g.ny && tau >= 0 && tau < g.nz &&
-                ((x + y + g.gz(tau) + c0) & 1) == 0) {
-                const VelUpd q = vel_load(L, Xi, B, x, y, tau, true);
-                if (q.du) u = q.u0 + q.ru / L.dv;
-                if (q.dv) v = q.v0 + q.rv / L.dv;
-                if (q.dw) w = q.w0 + q.rw / L.dv;
-            }
-            R[k] = u;
-            R[kV2H + k] = v;
-            R[2 * kV2H + k] = w;
-        }
-        __syncthreads();
-        // phase B: plane zb = tau - 1 of the tile -> Xo (c1 cells updated from the ring)
-        const int zb = tau - 1;
-        if (zb >= z0 && zb < z1 && bcell) {
-            const double* Rm = ring[(zb + 2) % 3];
-            const double* Rc = ring[zb % 3];
-            const double* Rp = R;
-            const int64_t i = g.slot(bx, by, zb);
-            double u, v, w;
-            if (((bx + by + g.gz(zb) + c0) & 1) == 0) {
-                u = Rc[kc];
-                v = Rc[kV2H + kc];
-                w = Rc[2 * kV2H + kc];
-            } else {
-                const double* P = Xi + 3 * fs;
-                u = Xi[i];
-                v = Xi[fs + i];
-                w = Xi[2 * fs + i];
-                const bool here = band_cell(L, bx, by, zb);
-                const bool du = bx >= 1 && !here && !band_cell(L, bx - 1, by, zb);
-                const bool dv = by >= 1 && !here && !band_cell(L, bx, by - 1, zb);
-                const bool dw = g.gz(zb) >= 1 && !here && !band_cell(L, bx, by, zb - 1);
-                const double pc = P[i];
-                if (du) {
-                    const double r = B[i] - mom_v(L, u, Rc[kc - 1], Rc[kc + 1], Rc[kc - kV2HX], Rc[kc + kV2HX], Rm[kc],
-                                                  Rp[kc], pc, P[i - 1]);
-                    u = u + r / L.dv;
-                }
-                if (dv) {
-                    const double* C = Rc + kV2H;
-                    const double r = B[fs + i] - mom_v(L, v, C[kc - 1], C[kc + 1], C[kc - kV2HX], C[kc + kV2HX],
-                                                       Rm[kV2H + kc], Rp[kV2H + kc], pc, P[i - sy]);
-                    v = v + r / L.dv;
-                }
-                if (dw) {
-                    const double* C = Rc + 2 * kV2H;
-                    const double r = B[2 * fs + i] - mom_v(L, w, C[kc - 1], C[kc + 1], C[kc - kV2HX], C[kc + kV2HX],
-                                                           Rm[2 * kV2H + kc], Rp[2 * kV2H + kc], pc, P[i - sz]);
-                    w = w + r / L.dv;
-                }
-            }
-            Xo[i] = u;
-            Xo[fs + i] = v;
-            Xo[2 * fs + i] = w;
-            Xo[3 * fs + i] = Xi[3 * fs + i];
-        }
-        __syncthreads();
-    }
-}
-
-// Staged variant (SMG_VEL2=2): the old state of each plane (u, v, w, p on the tile + 2 halo,
-// b on the tile + 1 halo) is copied into shared-memory rings with cp.async two planes (x) /
-// one plane (b) ahead of use, so the loads of the next planes are in flight while the CTA
-// computes the current one from shared memory.  Same per-point operations as k_dgs_vel2.
-// Measured slower than both (cfg 1 solve 18.69 -> 24.6 ms).
-constexpr int kS2X = 32, kS2Y = 16, kS2SX = kS2X + 4, kS2SY = kS2Y + 4, kS2SP = kS2SX * kS2SY;
-constexpr int kS2BX = kS2X + 2, kS2BP = kS2BX * (kS2Y + 2);
-constexpr int kS2XR = 5, kS2BR = 3;
-constexpr size_t kS2Smem = sizeof(double) * (static_cast<size_t>(kS2XR) * 4 * kS2SP + kS2BR * 3 * kS2BP + 3 * 3 * kS2BP);
-
-__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
-    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-
-__global__ void __launch_bounds__(kS2X * kS2Y, 1) k_dgs_vel2s(LevelK L, const double* __restrict__ Xi,
-                                                              double* __restrict__ Xo, const double* __restrict__ B,
-                                                              int c0, int zch) {
-    pdl_wait();
-    extern __shared__ double sm2[];
-    double* XR = sm2;                               // [kS2XR][4][kS2SP]  u, v, w, p (tile + 2)
-    double* BR = XR + kS2XR * 4 * kS2SP;            // [kS2BR][3][kS2BP]  b_u, b_v, b_w (tile + 1)
-    double* RR = BR + kS2BR * 3 * kS2BP;            // [3][3][kS2BP]      post-c0 u, v, w (tile + 1)
-    const Geom& g = L.g;
-    const int64_t fs = g.fs;
-    const int tx0 = blockIdx.x * kS2X, ty0 = blockIdx.y * kS2Y;
-    const int z0 = blockIdx.z * zch, z1 = min(z0 + zch, g.nz);
-    const int tid = threadIdx.x + threadIdx.y * kS2X, nth = kS2X * kS2Y;
-    // stage plane z of x (tile + 2) / of b (tile + 1); slots outside the padded box read as 0
-    auto stage_x = [&](int z) {
-        double* D = XR + ((z + 2 * kS2XR) % kS2XR) * 4 * kS2SP;
-        const bool zin = z >= -g.zg && z < g.nz + g.zg;
-        for (int k = tid; k < kS2SP; k += nth) {
-            const int x = tx0 - 2 + k % kS2SX, y = ty0 - 2 + k / kS2SX;
-            if (zin && x >= -g.xo && x < g.px - g.xo && y >= -1 && y <= g.ny) {
-                const int64_t i = g.slot(x, y, z);
-#pragma unroll
-                for (int f = 0; f < 4; ++f) cp_async8(D + f * kS2SP + k, Xi + f * fs + i);
-            } else {
-#pragma unroll
-                for (int f = 0; f < 4; ++f) D[f * kS2SP + k] = 0.0;
-            }
-        }
-    };
-    auto stage_b = [&](int z) {
-        double* D = BR + ((z + 2 * kS2BR) % kS2BR) * 3 * kS2BP;
-        const bool zin = z >= 0 && z < g.nz;
-        for (int k = tid; k < kS2BP; k += nth) {
-            const int x = tx0 - 1 + k % kS2BX, y = ty0 - 1 + k / kS2BX;
-            if (zin && x >= 0 && x < g.nx && y >= 0 && y < g.ny) {
-                const int64_t i = g.slot(x, y, z);
-#pragma unroll
-                for (int f = 0; f < 3; ++f) cp_async8(D + f * kS2BP + k, B + f * fs + i);
-            }
-        }
-    };
-    auto xs = [&](int z) { return XR + ((z + 2 * kS2XR) % kS2XR) * 4 * kS2SP; };
-    stage_x(z0 - 2);
-    stage_x(z0 - 1);
-    stage_x(z0);
-    stage_b(z0 - 1);
-    cp_async_commit();
-    const double idv = L.dv;
-    for (int tau = z0 - 1; tau <= z1; ++tau) {
-        // prefetch: x plane tau + 2, b plane tau + 1 (one group per step)
-        if (tau + 2 <= z1 + 1) stage_x(tau + 2);
-        if (tau + 1 <= z1) stage_b(tau + 1);
-        cp_async_commit();
-        cp_async_wait<1>();  // everything but this step's prefetch has landed
-        __syncthreads();
-        const double* Xm = xs(tau - 1);
-        const double* Xc = xs(tau);
-        const double* Xp = xs(tau + 1);
-        const double* Bc = BR + ((tau + 2 * kS2BR) % kS2BR) * 3 * kS2BP;
-        double* R = RR + ((tau + 3) % 3) * 3 * kS2BP;
-        // phase A: post-c0 state of plane tau on the tile + 1 halo
-        for (int k = tid; k < kS2BP; k += nth) {
-            const int hx = k % kS2BX, hy = k / kS2BX;
-            const int x = tx0 - 1 + hx, y = ty0 - 1 + hy;
-            const int s = (hy + 1) * kS2SX + hx + 1;  // staged position
-            double u = Xc[s], v = Xc[kS2SP + s], w = Xc[2 * kS2SP + s];
-            if (x >= 0 && y >= 0 && x < g.nx && y < g.ny && tau >= 0 && tau < g.nz &&
-                ((x + y + g.gz(tau) + c0) & 1) == 0) {
-                const bool here = band_cell(L, x, y, tau);
-                const bool du = x >= 1 && !here && !band_cell(L, x - 1, y, tau);
-                const bool dv = y >= 1 && !here && !band_cell(L, x, y - 1, tau);
-                const bool dw = g.gz(tau) >= 1 && !here && !band_cell(L, x, y, tau - 1);
-                const double* P = Xc + 3 * kS2SP;
-                if (du) {
-                    const double r = Bc[k] - mom_v(L, u, Xc[s - 1], Xc[s + 1], Xc[s - kS2SX], Xc[s + kS2SX], Xm[s],
-                                                   Xp[s], P[s], P[s - 1]);
-                    u = u + r / idv;
-                }
-                if (dv) {
-                    const double* C = Xc + kS2SP;
-                    const double r = Bc[kS2BP + k] - mom_v(L, v, C[s - 1], C[s + 1], C[s - kS2SX], C[s + kS2SX],
-                                                           Xm[kS2SP + s], Xp[kS2SP + s], P[s], P[s - kS2SX]);
-                    v = v + r / idv;
-                }
-                if (dw) {
-                    const double* C = Xc + 2 * kS2SP;
-                    const double r = Bc[2 * kS2BP + k] - mom_v(L, w, C[s - 1], C[s + 1], C[s - kS2SX], C[s + kS2SX],
-                                                               Xm[2 * kS2SP + s], Xp[2 * kS2SP + s], P[s],
-                                                               Xm[3 * kS2SP + s]);
-                    w = w + r / idv;
-                }
-            }
-            R[k] = u;
-            R[kS2BP + k] = v;
-            R[2 * kS2BP + k] = w;
-        }
-        __syncthreads();
-        // phase B: plane zb = tau - 1 of the tile -> Xo
-        const int zb = tau - 1;
-        const int bx = tx0 + threadIdx.x, by = ty0 + threadIdx.y;
-        if (zb >= z0 && zb < z1 && bx < g.nx && by < g.ny) {
-            const double* Rm = RR + ((zb + 2) % 3) * 3 * kS2BP;
-            const double* Rc = RR + (zb % 3) * 3 * kS2BP;
-            const double* Rp = R;
-            const double* Xb = Xm;            // staged plane zb
-            const double* Xbm = xs(zb - 1);   // staged plane zb - 1 (p for the w row)
-            const double* Bb = BR + ((zb + 2 * kS2BR) % kS2BR) * 3 * kS2BP;
-            const int kc = (threadIdx.y + 1) * kS2BX + threadIdx.x + 1;
-            const int s = (threadIdx.y + 2) * kS2SX + threadIdx.x + 2;
-            const int64_t i = g.slot(bx, by, zb);
-            double u, v, w;
-            if (((bx + by + g.gz(zb) + c0) & 1) == 0) {
-                u = Rc[kc];
-                v = Rc[kS2BP + kc];
-                w = Rc[2 * kS2BP + kc];
-            } else {
-                const double* P = Xb + 3 * kS2SP;
-                u = Xb[s];
-                v = Xb[kS2SP + s];
-                w = Xb[2 * kS2SP + s];
-                const bool here = band_cell(L, bx, by, zb);
-                const bool du = bx >= 1 && !here && !band_cell(L, bx - 1, by, zb);
-                const bool dv = by >= 1 && !here && !band_cell(L, bx, by - 1, zb);
-                const bool dw = g.gz(zb) >= 1 && !here && !band_cell(L, bx, by, zb - 1);
-                const double pc = P[s];
-                if (du) {
-                    const double r = Bb[kc] - mom_v(L, u, Rc[kc - 1], Rc[kc + 1], Rc[kc - kS2BX], Rc[kc + kS2BX],
-                                                    Rm[kc], Rp[kc], pc, P[s - 1]);
-                    u = u + r / idv;
-                }
-                if (dv) {
-                    const double* C = Rc + kS2BP;
-                    const double r = Bb[kS2BP + kc] - mom_v(L, v, C[kc - 1], C[kc + 1], C[kc - kS2BX], C[kc + kS2BX],
-                                                            Rm[kS2BP + kc], Rp[kS2BP + kc], pc, P[s - kS2SX]);
-                    v = v + r / idv;
-                }
-                if (dw) {
-                    const double* C = Rc + 2 * kS2BP;
-                    const double r = Bb[2 * kS2BP + kc] - mom_v(L, w, C[kc - 1], C[kc + 1], C[kc - kS2BX],
-                                                                C[kc + kS2BX], Rm[2 * kS2BP + kc], Rp[2 * kS2BP + kc],
-                                                                pc, Xbm[3 * kS2SP + s]);
-                    w = w + r / idv;
-                }
-            }
-            Xo[i] = u;
-            Xo[fs + i] = v;
-            Xo[2 * fs + i] = w;
-            Xo[3 * fs + i] = Xb[3 * kS2SP + s];
-        }
-        // the next step's prefetch overwrites the ring slots of planes tau - 2 (x) and tau - 1 (b)
-        __syncthreads();
-    }
-    cp_async_wait<0>();
-}
 
 __device__ __forceinline__ bool half_cell(const Geom& g, int c, int i, int j, int k, int& x, int& y, int& z) {
     x = 2 * i + (c & 1);
@@ -2196,141 +1518,6 @@ __global__ void __launch_bounds__(256, SMG_PREV_MINB) k_dgs_prev_c(LevelK L, dou
     }
 }
 
-// ------------------------------------- fused wavefront DGS sweep (large levels) ------
-// See WavePass in smg_internal.h.  A unit is up to kWaveCellsPerUnit cells of
-// one step on one plane, colour-compact (every thread works).
-__host__ __device__ __forceinline__ int wave_group(int kind, int arg) {
-    return kind == WK_PF ? fwd_group(arg) : rev_group(arg);
-}
-// cells of step (kind, arg) on the plane of global parity zpar (nx, ny even)
-__host__ __device__ __forceinline__ int64_t wave_cells(int kind, int arg, int zpar, int nx, int ny) {
-    const int64_t hx = nx / 2, hy = ny / 2;
-    if (kind == WK_VEL) return hx * ny;
-    if (kind == WK_FLUSH) return static_cast<int64_t>(nx) * ny;
-    const int grp = wave_group(kind, arg);
-    int m = 0;
-    for (int k = 0; k < group_size(grp); ++k) m += ((group_colour(grp, k) >> 2) & 1) == zpar;
-    return m * hx * hy;
-}
-__host__ __device__ __forceinline__ int wave_units(int kind, int arg, int zpar, int nx, int ny) {
-    return static_cast<int>((wave_cells(kind, arg, zpar, nx, ny) + kWaveCellsPerUnit - 1) / kWaveCellsPerUnit);
-}
-// work item t of step (kind, arg) on plane z -> cell (x, y)
-__device__ __forceinline__ void wave_cell(const Geom& g, int kind, int arg, int gz, int64_t t, int& x, int& y) {
-    const int hx = g.nx >> 1;
-    if (kind == WK_VEL) {
-        y = static_cast<int>(t / hx);
-        x = 2 * static_cast<int>(t - static_cast<int64_t>(y) * hx) + ((y + gz + arg) & 1);
-    } else if (kind == WK_FLUSH) {
-        y = static_cast<int>(t / g.nx);
-        x = static_cast<int>(t - static_cast<int64_t>(y) * g.nx);
-    } else {
-        const int64_t q = static_cast<int64_t>(hx) * (g.ny >> 1);
-        const int grp = wave_group(kind, arg);
-        int k = static_cast<int>(t / q), c = 0;
-        const int64_t r = t - k * q;
-        for (int j = 0; j < group_size(grp); ++j) {
-            const int cj = group_colour(grp, j);
-            if (((cj >> 2) & 1) != (gz & 1)) continue;
-            if (k-- == 0) { c = cj; break; }
-        }
-        const int j = static_cast<int>(r / hx);
-        x = 2 * static_cast<int>(r - static_cast<int64_t>(j) * hx) + (c & 1);
-        y = 2 * j + ((c >> 1) & 1);
-    }
-}
-
-__device__ __forceinline__ int ld_acquire(const int* p) {
-    int v;
-    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-
-constexpr int kWaveThreads = kWaveCellsPerUnit / 2;
-
-// Persistent loop over tickets.  Warp 0 decodes the unit, its lanes wait on the
-// step-(s-1) plane counters in parallel, and lane 0 prefetches the next ticket
-// before the CTA works on this one (a held-but-unstarted ticket only depends on
-// smaller tickets, so progress is still guaranteed).
-__global__ void __launch_bounds__(kWaveThreads, 3) k_dgs_wave(LevelK L, double* __restrict__ X,
-                                                              const double* __restrict__ B,
-                                                              double* __restrict__ D, WavePass P) {
-    __shared__ uint32_t s_unit;
-    __shared__ int8_t s_kind[kWaveMaxSteps], s_arg[kWaveMaxSteps], s_lo[kWaveMaxSteps], s_hi[kWaveMaxSteps];
-    const Geom& g = L.g;
-    const int tid = threadIdx.x, lane = tid & 31;
-    if (tid == 0) {  // step table in shared memory (static indices: the parameter block stays in constant bank)
-#pragma unroll
-        for (int k = 0; k < kWaveMaxSteps; ++k) {
-            s_kind[k] = P.kind[k];
-            s_arg[k] = P.arg[k];
-            s_lo[k] = P.lo[k];
-            s_hi[k] = P.hi[k];
-        }
-    }
-    __syncthreads();
-    int next = tid == 0 ? atomicAdd(P.cnt, 1) : 0;
-    for (;;) {
-        if (tid < 32) {
-            uint32_t u = 0xffffffffu;
-            if (lane == 0 && next < P.nunits) u = __ldg(P.units + next);
-            u = __shfl_sync(0xffffffffu, u, 0);
-            if (u != 0xffffffffu) {
-                const int s = static_cast<int>(u >> 28), z = static_cast<int>((u >> 16) & 0xfff);
-                if (s > 0) {  // step s-1 done on the planes this unit reads or overwrites
-                    const int zz = z - s_lo[s] + lane;
-                    if (zz >= 0 && zz < g.nz && zz <= z + s_hi[s]) {
-                        const int need = wave_units(s_kind[s - 1], s_arg[s - 1], g.gz(zz) & 1, g.nx, g.ny);
-                        const int* c = P.cnt + 1 + (s - 1) * g.nz + zz;
-                        while (ld_acquire(c) < need) __nanosleep(20);
-                    }
-                    __syncwarp();
-                }
-                if (lane == 0) {
-                    __threadfence();  // acquire side: also drops this SM's L1 lines
-                    next = atomicAdd(P.cnt, 1);
-                }
-            }
-            if (lane == 0) s_unit = u;
-        }
-        __syncthreads();
-        const uint32_t u = s_unit;
-        if (u == 0xffffffffu) return;
-        const int s = static_cast<int>(u >> 28), z = static_cast<int>((u >> 16) & 0xfff);
-        const int kind = s_kind[s], arg = s_arg[s], gz = g.gz(z);
-        const int64_t ncell = wave_cells(kind, arg, gz & 1, g.nx, g.ny);
-        const int64_t t0 = static_cast<int64_t>(u & 0xffff) * kWaveCellsPerUnit + tid;
-        const int64_t t1 = t0 + kWaveThreads;
-        const bool v0 = t0 < ncell, v1 = t1 < ncell;
-        int x0 = 0, y0 = 0, x1 = 0, y1 = 0;
-        if (v0) wave_cell(g, kind, arg, gz, t0, x0, y0);
-        if (v1) wave_cell(g, kind, arg, gz, t1, x1, y1);
-        if (kind == WK_VEL) {
-            const VelUpd a = vel_load(L, X, B, x0, y0, z, v0);
-            const VelUpd b = vel_load(L, X, B, x1, y1, z, v1);
-            vel_store(L, X, a);
-            vel_store(L, X, b);
-        } else if (kind == WK_PF || kind == WK_FLUSH) {
-            const bool fl = kind == WK_FLUSH;
-            const PfUpd a = pf_load(L, X, B, D, x0, y0, z, v0, fl);
-            const PfUpd b = pf_load(L, X, B, D, x1, y1, z, v1, fl);
-            if (fl) {
-                pf_store<true>(L, X, D, a);
-                pf_store<true>(L, X, D, b);
-            } else {
-                pf_store<false>(L, X, D, a);
-                pf_store<false>(L, X, D, b);
-            }
-        } else {
-            // one cell after the other (the radius-2 gather of two cells would spill)
-            if (v0 && !band_cell(L, x0, y0, z)) dgs_prev_cell(L, X, B, g.slot(x0, y0, z));
-            if (v1 && !band_cell(L, x1, y1, z)) dgs_prev_cell(L, X, B, g.slot(x1, y1, z));
-        }
-        __syncthreads();
-        if (tid == 0)  // release: the CTA's stores before the completion count
-            asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(P.cnt + 1 + s * g.nz + z) : "memory");
-    }
-}
 
 // ------------------------------------------------ SQMR device scalars ------
 // Alg. 4 scalar recurrences evaluated on the device (same expressions and
@@ -2381,143 +1568,6 @@ __device__ __forceinline__ void sqmr_beta(double* sc) {  // after ||b - L x||^2
     sc[S_RHO] = rho_new;
     sc[S_NUOLD] = sc[S_NU];
 }
-// Fused y = L x (B == nullptr) or y = B - L x, and the canonical inner product
-// sc[S_D0] = a.y with a = x (sigma = q.(L q)) or a = y (||b - L x||^2), followed by
-// the SQMR scalar update `which` (1 alpha, 3 beta) -- one launch instead of four.
-// Block = R whole rows of one plane, one thread per cell (all four fields, as
-// k_apply); the products go to shared memory and warp (row, field) adds them in
-// k_cdot's order (lane l: x = l, l+32, ... ascending, then the shuffle tree).
-// Row sums go to rowbuf; the last block of a plane adds them in ascending y
-// (k_cdot's plane partial) and the last plane combines all partials in
-// k_cdot_final's order: bit-identical to apply + launch_cdot2 + scalar kernel.
-constexpr int kAdThreads = 512;
-__global__ void __launch_bounds__(1024) k_apply_dot(LevelK L, const double* __restrict__ X,
-                                                          const double* __restrict__ B, double* __restrict__ Y,
-                                                          double gamma, int dot_y, int R,
-                                                          double* __restrict__ rowbuf, double* __restrict__ partials,
-                                                          double* __restrict__ sc, unsigned* __restrict__ cnt,
-                                                          int which) {
-    pdl_wait();
-    extern __shared__ double prod[];  // [R][4][nx + 1]
-    __shared__ int flag;
-    const Geom& g = L.g;
-    const int nx = g.nx, px = nx + 1;
-    const int r = threadIdx.x / nx, x = threadIdx.x - r * nx;
-    const int y = blockIdx.x * R + r, z = blockIdx.y;
-    const int64_t fs = g.fs;
-    const double *U = X, *V = X + fs, *W = X + 2 * fs, *P = X + 3 * fs;
-    const int gzz = g.gz(z);
-    const bool top = g.z0 + g.nz == g.gnz;
-    if (r < R) {
-        double* pr = prod + r * 4 * px;
-        double pu = 0.0, pv = 0.0, pw = 0.0, pp = 0.0;
-        if (y < g.ny && z < g.nz) {
-            const int64_t i = g.slot(x, y, z);
-            if (x >= 1) {
-                const double yv = mom(L, U, P, i, 1);
-                const double v = B ? B[i] - yv : yv;
-                Y[i] = v;
-                pu = (dot_y ? v : U[i]) * v;
-            } else {
-                pu = (dot_y ? 0.0 : U[i]) * 0.0;
-            }
-            if (y >= 1) {
-                const double yv = mom(L, V, P, i, g.sy);
-                const double v = B ? B[fs + i] - yv : yv;
-                Y[fs + i] = v;
-                pv = (dot_y ? v : V[i]) * v;
-            } else {
-                pv = (dot_y ? 0.0 : V[i]) * 0.0;
-            }
-            if (gzz >= 1) {
-                const double yv = mom(L, W, P, i, g.sz);
-                const double v = B ? B[2 * fs + i] - yv : yv;
-                Y[2 * fs + i] = v;
-                pw = (dot_y ? v : W[i]) * v;
-            } else {
-                pw = (dot_y ? 0.0 : W[i]) * 0.0;
-            }
-            const double yv = cont(L, U, V, W, P, i, gamma);
-            const double v = B ? B[3 * fs + i] - yv : yv;
-            Y[3 * fs + i] = v;
-            pp = (dot_y ? v : P[i]) * v;
-        } else if (y <= g.ny) {  // wall row of v (y = ny) / top wall plane of w (z = nz): zero products
-            const int64_t i = g.slot(x, y, z);
-            if (y == g.ny && z < g.nz) pv = (dot_y ? 0.0 : V[i]) * 0.0;
-            if (z == g.nz && y < g.ny) pw = (dot_y ? 0.0 : W[i]) * 0.0;
-        }
-        pr[x] = pu;
-        pr[px + x] = pv;
-        pr[2 * px + x] = pw;
-        pr[3 * px + x] = pp;
-        if (x == 0) pr[nx] = y <= g.ny ? (dot_y ? 0.0 : U[g.slot(nx, y, z)]) * 0.0 : 0.0;  // u wall face x = nx
-    }
-    __syncthreads();
-    // warp (row rr, field f) forms the row sum in the canonical lane order
-    const int wid = threadIdx.x >> 5, l = threadIdx.x & 31;
-    if (wid < 4 * R) {
-        const int rr = wid >> 2, f = wid & 3, yy = blockIdx.x * R + rr;
-        const bool has = f == 1 ? (yy <= g.ny && z < g.nz)
-                                : (yy < g.ny && (z < g.nz || (f == 2 && z == g.nz && top)));
-        if (has) {
-            const double* pr = prod + (rr * 4 + f) * px;
-            const int ex = nx + (f == 0);
-            double s0 = 0.0;
-            for (int xx = l; xx < ex; xx += 32) s0 = s0 + pr[xx];
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) s0 = s0 + __shfl_down_sync(0xffffffffu, s0, o);
-            if (l == 0) rowbuf[(f * (g.nz + 1) + z) * (g.ny + 1) + yy] = s0;
-        }
-    }
-    // last block of this plane: plane partials (rows ascending); last plane: the final
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        flag = atomicAdd(cnt + 1 + z, 1u) == gridDim.x - 1;
-    }
-    __syncthreads();
-    if (!flag) return;
-    __threadfence();
-    // stage the plane's row sums in shared memory (parallel loads), then add them in order
-    double* rs = prod;  // [4][ny + 1]
-    for (int k = threadIdx.x; k < 4 * (g.ny + 1); k += blockDim.x) {
-        const int f = k / (g.ny + 1), yy = k - f * (g.ny + 1);
-        rs[k] = __ldcg(rowbuf + (f * (g.nz + 1) + z) * (g.ny + 1) + yy);
-    }
-    __syncthreads();
-    if (threadIdx.x < 4) {
-        const int f = threadIdx.x;
-        const int ey = g.ny + (f == 1);
-        const bool has = f == 2 ? (z < g.nz || top) : z < g.nz;
-        if (has) {
-            double p0 = 0.0;
-            for (int yy = 0; yy < ey; ++yy) p0 = p0 + rs[f * (g.ny + 1) + yy];
-            partials[f * g.gnz + (f == 3 ? 1 : 0) + gzz] = p0;
-        }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        cnt[1 + z] = 0u;
-        __threadfence();
-        flag = atomicAdd(cnt, 1u) == gridDim.y - 1;
-    }
-    __syncthreads();
-    if (!flag) return;
-    __threadfence();
-    if (wid == 0) {
-        const int nq = 4 * g.gnz + 1;
-        double s1 = 0.0;
-        for (int k = l; k < nq; k += 32) s1 = s1 + __ldcg(partials + k);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) s1 = s1 + __shfl_down_sync(0xffffffffu, s1, o);
-        if (l == 0) {
-            sc[S_D0] = s1;
-            if (which == 1) sqmr_alpha(sc);
-            else if (which == 3) sqmr_beta(sc);
-            cnt[0] = 0u;  // ready for the next launch (graph replay)
-        }
-    }
-}
 
 __global__ void k_axpy_s(double* __restrict__ s, const double* __restrict__ t, const double* __restrict__ sc,
                          int64_t n) {  // s = s - alpha t
@@ -2545,6 +1595,228 @@ __global__ void k_xpby_dev(double* __restrict__ q, const double* __restrict__ t,
     const double b = sc[S_BETA];
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
         q[k] = t[k] + b * q[k];
+}
+
+// ------------------------------------------- tile-ordered DGS (large levels) ------
+// OD-1 rev. 2: a large level is cut into tiles of kTX x kTY x kTZ cells,
+// coloured by tile parity T = (tx&1) + 2(ty&1) + 4(tz&1).  The symmetric sweep relaxes
+// the tiles of colour 0..7 in turn (forward phases 0..9 inside each tile), then 7..0
+// (reverse phases 10..19 inside each tile): "a given traversal order, then exactly the
+// reverse", so the sweep stays symmetric.  Same-colour tiles are a whole
+// tile apart, farther than any read (radius 2) plus write (radius 1) reach, so they run
+// in parallel exactly as in sequence.  One CTA owns one tile: ONE TMA load
+// (cp.async.bulk.tensor, 4-D box of all four fields with a halo of -2..+2 in x, -1..+2 in
+// y and z) stages the tile's neighbourhood in shared memory, every phase runs there with
+// __syncthreads between phases, and only the DOFs a phase may change go back to HBM.
+// Per-point arithmetic is the per-step kernels' (mom / cont / prev_core with box strides),
+// and the in-tile order is the oracle's: bit-identical.  A level vector is read once and
+// written once per half sweep (plus the halo), instead of 13 passes of the per-step
+// kernels.
+constexpr int kTX = 16, kTY = 8, kTZ = 8;
+constexpr int kBX = kTX + 4, kBY = kTY + 3, kBZ = kTZ + 3;  // box x [-2, TX+2), y/z [-1, T+2)
+constexpr int kOX = 2, kOY = 1, kOZ = 1;
+constexpr int kBox = kBX * kBY * kBZ;
+constexpr int kTileThreads = 256;
+constexpr int kTileCells = kTX * kTY * kTZ;
+constexpr size_t kTileSmem = 5 * kBox * sizeof(double) + 128;  // x box (4 fields), delta box, mbarrier
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// cell e (0 .. kTileCells/8 - 1) of parity colour c inside a tile (tile origins are even)
+__device__ __forceinline__ void tile_pcell(int e, int c, int& x, int& y, int& z) {
+    x = 2 * (e % (kTX / 2)) + (c & 1);
+    y = 2 * ((e / (kTX / 2)) % (kTY / 2)) + ((c >> 1) & 1);
+    z = 2 * (e / (kTX * kTY / 4)) + ((c >> 2) & 1);
+}
+__device__ __forceinline__ int tile_li(int x, int y, int z) { return ((z + kOZ) * kBY + (y + kOY)) * kBX + (x + kOX); }
+
+// phases [ph0, ph1) of the 20-phase numbering (0,1 velocity; 2..9 forward pressure colours
+// 0..7; 10..17 reverse pressure colours 7..0; 18,19 velocity 1,0) on the tiles of colour T.
+__global__ void __launch_bounds__(kTileThreads, 2) k_dgs_tile(const __grid_constant__ CUtensorMap tmx, LevelK L,
+                                                            double* __restrict__ X, const double* __restrict__ B,
+                                                            int T, int ph0, int ph1, int ntx, int nty) {
+    extern __shared__ __align__(128) unsigned char tsm_raw[];
+    double* xs = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(tsm_raw) + 127) & ~uintptr_t(127));
+    double* ds = xs + 4 * kBox;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(ds + kBox);
+    const Geom& g = L.g;
+    const int tid = threadIdx.x;
+    // tile of colour T for this CTA
+    const int hx = (ntx - (T & 1) + 1) >> 1, hy = (nty - ((T >> 1) & 1) + 1) >> 1;
+    const int bi = blockIdx.x;
+    const int tx = 2 * (bi % hx) + (T & 1), ty = 2 * ((bi / hx) % hy) + ((T >> 1) & 1),
+              tz = 2 * (bi / (hx * hy)) + ((T >> 2) & 1);
+    const int x0 = tx * kTX, y0 = ty * kTY, z0 = tz * kTZ;  // z0: local plane of the part
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    pdl_wait();  // the previous kernel's writes are visible from here on
+    if (tid == 0) {
+        const uint32_t bytes = 4u * kBox * sizeof(double);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                     : "memory");
+        const int c0 = x0 - kOX + g.xo, c1 = y0 - kOY + 1, c2 = z0 - kOZ + g.zg;
+        asm volatile(
+            "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, "
+            "%5}], [%6];" ::"r"(smem_u32(xs)),
+            "l"(reinterpret_cast<uint64_t>(&tmx)), "r"(c0), "r"(c1), "r"(c2), "r"(0), "r"(smem_u32(bar))
+            : "memory");
+    }
+    for (int k = tid; k < kBox; k += kTileThreads) ds[k] = 0.0;
+    {
+        const uint32_t ba = smem_u32(bar);
+        asm volatile(
+            "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n @!p bra WAIT_%=;\n}" ::"r"(
+                ba)
+            : "memory");
+    }
+    __syncthreads();
+    LevelK Ls = L;  // the same operators on the box (strides of the shared-memory box)
+    Ls.g.sy = kBX;
+    Ls.g.sz = kBX * kBY;
+    Ls.g.fs = kBox;
+    double *Us = xs, *Vs = xs + kBox, *Ws = xs + 2 * kBox, *Ps = xs + 3 * kBox;
+    const int64_t fs = g.fs;
+    bool fwd_p = false;
+    for (int ph = ph0; ph < ph1; ++ph) {
+        if (ph <= 1 || ph >= 18) {  // velocity colour (red-black on global parity)
+            const int c = ph <= 1 ? ph : 19 - ph;
+            for (int e = tid; e < kTileCells / 2; e += kTileThreads) {
+                const int lz = e / (kTX * kTY / 2), ly = (e / (kTX / 2)) % kTY;
+                const int lx = 2 * (e % (kTX / 2)) + ((ly + lz + c + g.z0) & 1);
+                const int gx = x0 + lx, gy = y0 + ly, zl = z0 + lz;
+                const int li = tile_li(lx, ly, lz);
+                const int64_t i = g.slot(gx, gy, zl);
+                const bool here = band_cell(L, gx, gy, zl);
+                if (gx >= 1 && !here && !band_cell(L, gx - 1, gy, zl)) {
+                    const double r = B[i] - mom(Ls, Us, Ps, li, 1);
+                    Us[li] = Us[li] + r / L.dv;
+                }
+                if (gy >= 1 && !here && !band_cell(L, gx, gy - 1, zl)) {
+                    const double r = B[fs + i] - mom(Ls, Vs, Ps, li, kBX);
+                    Vs[li] = Vs[li] + r / L.dv;
+                }
+                if (g.gz(zl) >= 1 && !here && !band_cell(L, gx, gy, zl - 1)) {
+                    const double r = B[2 * fs + i] - mom(Ls, Ws, Ps, li, kBX * kBY);
+                    Ws[li] = Ws[li] + r / L.dv;
+                }
+            }
+            __syncthreads();
+        } else if (ph <= 9) {  // forward pressure colour c (eager gather form, the oracle's)
+            const int c = ph - 2;
+            fwd_p = true;
+            constexpr int ncc = kTileCells / 8;
+            if (tid < ncc) {
+                int lx, ly, lz;
+                if (ph > 2) {  // clear the previous colour's deltas
+                    tile_pcell(tid, c - 1, lx, ly, lz);
+                    ds[tile_li(lx, ly, lz)] = 0.0;
+                }
+                tile_pcell(tid, c, lx, ly, lz);
+                const int li = tile_li(lx, ly, lz);
+                if (!band_cell(L, x0 + lx, y0 + ly, z0 + lz)) {
+                    const int64_t i = g.slot(x0 + lx, y0 + ly, z0 + lz);
+                    ds[li] = (B[3 * fs + i] - cont(Ls, Us, Vs, Ws, Ps, li, L.gamma)) / L.dp;
+                }
+            }
+            __syncthreads();
+            // delta of box cell (x, y, z): nonzero only on the tile's colour-c V2 cells
+            auto dv = [&](int x, int y, int z) {
+                return (x >= 0 && y >= 0 && z >= 0 && x < kTX && y < kTY && z < kTZ) ? ds[tile_li(x, y, z)] : 0.0;
+            };
+            auto pupd = [&](int lx, int ly, int lz) {
+                double s = dv(lx - 1, ly, lz) + dv(lx + 1, ly, lz);
+                s = s + dv(lx, ly - 1, lz);
+                s = s + dv(lx, ly + 1, lz);
+                s = s + dv(lx, ly, lz - 1);
+                s = s + dv(lx, ly, lz + 1);
+                const int li = tile_li(lx, ly, lz);
+                Ps[li] = Ps[li] + L.eta_h2 * (6.0 * dv(lx, ly, lz) - s);
+            };
+            if (tid < ncc) {  // faces and self term of the colour-c cells
+                int lx, ly, lz;
+                tile_pcell(tid, c, lx, ly, lz);
+                if (!band_cell(L, x0 + lx, y0 + ly, z0 + lz)) {
+                    const int li = tile_li(lx, ly, lz);
+                    const int sy = kBX, sz = kBX * kBY;
+                    Us[li] = Us[li] + (ds[li - 1] - ds[li]) * L.inv_h;
+                    Us[li + 1] = Us[li + 1] + (ds[li] - ds[li + 1]) * L.inv_h;
+                    Vs[li] = Vs[li] + (ds[li - sy] - ds[li]) * L.inv_h;
+                    Vs[li + sy] = Vs[li + sy] + (ds[li] - ds[li + sy]) * L.inv_h;
+                    Ws[li] = Ws[li] + (ds[li - sz] - ds[li]) * L.inv_h;
+                    Ws[li + sz] = Ws[li + sz] + (ds[li] - ds[li + sz]) * L.inv_h;
+                    pupd(lx, ly, lz);
+                }
+            }
+            // neighbour pressures (colours c^1, c^2, c^4) in the tile box extended by one cell
+            constexpr int EX = kTX + 2, EY = kTY + 2, EZ = kTZ + 2;
+            for (int e = tid; e < EX * EY * EZ; e += kTileThreads) {
+                const int lx = e % EX - 1, ly = (e / EX) % EY - 1, lz = e / (EX * EY) - 1;
+                const int k = (lx & 1) + 2 * (ly & 1) + 4 * (lz & 1);
+                const int bit = k ^ c;
+                if (bit != 1 && bit != 2 && bit != 4) continue;
+                const int gx = x0 + lx, gy = y0 + ly, zl = z0 + lz;
+                if (gx < 0 || gy < 0 || g.gz(zl) < 0 || gx >= g.nx || gy >= g.ny || g.gz(zl) >= g.gnz) continue;
+                // hit: an axis neighbour (along the differing parity bit) is a V2 colour-c tile cell
+                auto owned_v2 = [&](int ax, int ay, int az) {
+                    return ax >= 0 && ay >= 0 && az >= 0 && ax < kTX && ay < kTY && az < kTZ &&
+                           !band_cell(L, x0 + ax, y0 + ay, z0 + az);
+                };
+                bool hit;
+                if (bit == 1) hit = owned_v2(lx - 1, ly, lz) || owned_v2(lx + 1, ly, lz);
+                else if (bit == 2) hit = owned_v2(lx, ly - 1, lz) || owned_v2(lx, ly + 1, lz);
+                else hit = owned_v2(lx, ly, lz - 1) || owned_v2(lx, ly, lz + 1);
+                if (hit) pupd(lx, ly, lz);
+            }
+            __syncthreads();
+        } else {  // reverse (left-preconditioned) pressure colour c
+            const int c = 17 - ph;
+            if (tid < kTileCells / 8) {
+                int lx, ly, lz;
+                tile_pcell(tid, c, lx, ly, lz);
+                if (!band_cell(L, x0 + lx, y0 + ly, z0 + lz)) {
+                    const int li = tile_li(lx, ly, lz);
+                    Ps[li] = prev_core(Ls, xs, li, L.cb[g.slot(x0 + lx, y0 + ly, z0 + lz)]);
+                }
+            }
+            __syncthreads();
+        }
+    }
+    // write back: the tile's own DOFs, plus (after forward pressure phases) its high faces
+    // and the pressures of the six neighbouring slabs -- never a slot outside the level
+    auto put = [&](int f, int lx, int ly, int lz) {
+        const int gx = x0 + lx, gy = y0 + ly, zl = z0 + lz, gz = g.gz(zl);
+        if (gx < 0 || gy < 0 || gz < 0 || gx >= g.nx || gy >= g.ny || gz >= g.gnz) {
+            // only the high faces at n (walls) lie beyond the cells, and walls stay 0
+            return;
+        }
+        if ((f == 0 && gx == 0) || (f == 1 && gy == 0) || (f == 2 && gz == 0)) return;  // low walls
+        X[f * fs + g.slot(gx, gy, zl)] = xs[f * kBox + tile_li(lx, ly, lz)];
+    };
+    const int hw = fwd_p ? 1 : 0;
+    for (int f = 0; f < 3; ++f) {  // faces: x [0, TX + hw) for u etc.
+        const int wx = kTX + (f == 0 ? hw : 0), wy = kTY + (f == 1 ? hw : 0), wz = kTZ + (f == 2 ? hw : 0);
+        for (int e = tid; e < wx * wy * wz; e += kTileThreads) put(f, e % wx, (e / wx) % wy, e / (wx * wy));
+    }
+    {  // pressures: rows x [-hw, TX + hw) of the tile, then the y and z neighbour slabs
+        const int wx = kTX + 2 * hw;
+        for (int e = tid; e < wx * kTY * kTZ; e += kTileThreads)
+            put(3, e % wx - hw, (e / wx) % kTY, e / (wx * kTY));
+        if (hw) {
+            for (int e = tid; e < 2 * kTX * kTZ; e += kTileThreads) {
+                const int lx = e % kTX, side = (e / kTX) & 1, lz = e / (2 * kTX);
+                put(3, lx, side ? kTY : -1, lz);
+            }
+            for (int e = tid; e < 2 * kTX * kTY; e += kTileThreads) {
+                const int lx = e % kTX, ly = (e / kTX) % kTY, side = e / (kTX * kTY);
+                put(3, lx, ly, side ? kTZ : -1);
+            }
+        }
+    }
 }
 
 inline int stream_blocks(int64_t n) {
@@ -2633,47 +1905,9 @@ void launch_restrict(const LevelK& F, const LevelK& C, const double* rf, double*
     }
     count();
 }
-bool resrestrict_ok(const LevelK& F, const LevelK& C) {
-    return F.g.z0 == 0 && F.g.nz == F.g.gnz && C.g.z0 == 0 && C.g.nz == C.g.gnz && 2 * C.g.nx == F.g.nx &&
-           2 * C.g.ny == F.g.ny && 2 * C.g.nz == F.g.nz && env_int("SMG_FUSED_RR", 0) != 0;
-}
-void launch_residual_restrict(const LevelK& F, const LevelK& C, const double* x, const double* b, double* bc,
-                              cudaStream_t s) {
-    const Geom& cg = C.g;
-    const int gx = (cg.nx + RR_TX - 1) / RR_TX, gy = (cg.ny + RR_TY - 1) / RR_TY;
-    // coarse-plane segments: enough CTAs for two per SM (each segment recomputes 2 fine planes)
-    int nseg = std::max(1, std::min(cg.nz, (2 * num_sms() + gx * gy - 1) / (gx * gy)));
-    const int zseg = (cg.nz + nseg - 1) / nseg;
-    nseg = (cg.nz + zseg - 1) / zseg;
-    const size_t smem = 16 * RR_PLANE * sizeof(double);
-    static bool attr = false;
-    if (!attr) {
-        note(cudaFuncSetAttribute(k_resrestrict, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        attr = true;
-    }
-    launch_k(k_resrestrict, dim3(gx, gy, nseg), dim3(512), smem, s, F, C, x, b, bc, zseg);
-    count();
-}
 
 void launch_prolong_add(const LevelK& F, const LevelK& C, const double* xc, double* xf, cudaStream_t s) {
-    // z-marching variant: opt-in (SMG_PROLONG_ZM=1), measured slower than the per-cell kernel
-    // (cfg 3 fine level 2.16 -> 3.9 ms: one marching thread per column keeps too few
-    // read-modify-writes in flight); segments of >= 2 plane pairs, slab starting on an even plane
-    const Geom& fg = F.g;
-    const dim3 g2 = cell_grid(fg);
-    const int pairs = (fg.nz + 1) / 2;
-    const int64_t cols = static_cast<int64_t>(g2.x) * g2.y * BX * BY;
-    const int64_t target = static_cast<int64_t>(num_sms()) * 2048;
-    const int nseg = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(pairs, (target + cols - 1) / cols)));
-    const int force = env_int("SMG_PROLONG_ZPAIRS", 0);  // tests: segment length on every level
-    const int zpairs = force > 0 ? force : (pairs + nseg - 1) / nseg;
-    if (env_int("SMG_PROLONG_ZM", 0) && (force > 0 || zpairs >= 2) && (fg.gz(0) & 1) == 0 && 2 * C.g.nx == fg.nx &&
-        2 * C.g.ny == fg.ny) {
-        launch_k(k_prolong_zm, dim3(g2.x, g2.y, (pairs + zpairs - 1) / zpairs), dim3(BX, BY), 0, s, F, C, xc, xf,
-                 zpairs);
-    } else {
-        launch_k(k_prolong_add, g2, dim3(BX, BY), 0, s, F, C, xc, xf);
-    }
+    launch_k(k_prolong_add, cell_grid(F.g), dim3(BX, BY), 0, s, F, C, xc, xf);
     count();
 }
 void launch_coarse_gemv(const double* ksym, const int32_t* slots, int n, const double* b, double* x,
@@ -2789,14 +2023,6 @@ static void launch_sweep(const void* fn_grid, const void* fn_cluster, bool clust
         note(cudaLaunchKernelExC(&cfg, fn_grid, args));
     }
     count();
-}
-
-// SMG_SYNC_MODE: 0 auto (cluster when the sweep is small enough), 1 grid, 2 cluster.
-static bool use_cluster(int64_t work, int64_t max_items_per_thread) {
-    const int mode = env_int("SMG_SYNC_MODE", 0);
-    if (mode == 1) return false;
-    if (mode == 2) return true;
-    return work <= static_cast<int64_t>(kClusterCTAs) * kClusterThreads * max_items_per_thread;
 }
 
 static void set_pairs(VankaLists& vl, const VankaPairs& pr) {
@@ -2939,76 +2165,6 @@ int vanka_pairs_pay(const int* n) {
     const bool unmerged_cpt1 = lu <= cl || lu <= cap;
     return (merged_fits || !unmerged_cpt1) ? 0xf : 0;
 }
-bool smooth_dsm_fits(const LevelK& L, const int* n) {
-    int maxn = 0;
-    for (int c = 0; c < 8; ++c) maxn = n[c] > maxn ? n[c] : maxn;
-    // opt-in: measured slower than the L2-resident kernels on B200 (remote DSMEM loads through the
-    // accessor, 126 registers -> 16 warps per SM): 32^3 smooth 0.67 ms vs 0.30 ms
-    return env_int("SMG_DSM_SMOOTH", 0) == 1 && 5 * L.g.fs <= static_cast<int64_t>(kDsmCTAs) * kDsmChunk &&
-           8 * static_cast<int64_t>(maxn) <= static_cast<int64_t>(kDsmCTAs) * 512;
-}
-
-void launch_smooth_dsm(const LevelK& L, double* x, const double* b, const int32_t* const* cells,
-                       const uint8_t* const* masks, const int* n, const double* ktab, int nu, int nph,
-                       cudaStream_t s, const VankaPairs& pr) {
-    VankaLists vl;
-    set_pairs(vl, pr);
-    for (int c = 0; c < 8; ++c) {
-        vl.cells[c] = cells[c];
-        vl.masks[c] = masks[c];
-        vl.n[c] = n[c];
-    }
-    const size_t smem = (64 * 49 + kDsmChunk) * sizeof(double) + kDsmCTAs * sizeof(double*);
-    note(cudaFuncSetAttribute(k_smooth_dsm, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    note(cudaFuncSetAttribute(k_smooth_dsm, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    cudaLaunchConfig_t cfg = {};
-    cudaLaunchAttribute attr[1];
-    cfg.gridDim = dim3(kDsmCTAs);
-    cfg.blockDim = dim3(512);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = kDsmCTAs;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    LevelK Lc = L;
-    void* args[] = {&Lc, &x, const_cast<double**>(&b), &vl, const_cast<double**>(&ktab), &nu, &nph};
-    note(cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(k_smooth_dsm), args));
-    count();
-}
-
-bool smooth_smem_fits(const LevelK& L, const int* n) {
-    int maxn = 0;
-    for (int c = 0; c < 8; ++c) maxn = n[c] > maxn ? n[c] : maxn;
-    return (64 * 49 + 4 * L.g.fs) * static_cast<int64_t>(sizeof(double)) <= 227 * 1024 && maxn <= 4 * 512 &&
-           env_int("SMG_SMEM_SMOOTH", 0) == 1 && env_int("SMG_NO_SMEM_SMOOTH", 0) == 0;
-}
-
-void launch_smooth_smem(const LevelK& L, double* x, const double* b, const int32_t* const* cells,
-                        const uint8_t* const* masks, const int* n, const double* ktab, double* d0, double* d1, int nu,
-                        int nph, cudaStream_t s, const VankaPairs& pr) {
-    VankaLists vl;
-    set_pairs(vl, pr);
-    for (int c = 0; c < 8; ++c) {
-        vl.cells[c] = cells[c];
-        vl.masks[c] = masks[c];
-        vl.n[c] = n[c];
-    }
-    const size_t smem = (64 * 49 + 4 * L.g.fs) * sizeof(double);
-    // every block of a colour list needs a thread: 512 threads x CPT blocks
-    int maxn = 0;
-    for (int c = 0; c < 8; ++c) maxn = n[c] > maxn ? n[c] : maxn;
-    auto go = [&](auto kern) {
-        note(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        kern<<<1, 512, smem, s>>>(L, x, b, vl, ktab, d0, d1, nu, nph);
-    };
-    if (maxn <= 512) go(k_smooth_smem<1>);
-    else if (maxn <= 1024) go(k_smooth_smem<2>);
-    else go(k_smooth_smem<4>);  // smooth_smem_fits caps the list size
-    count();
-}
 
 // Single phases of the colour-compact DGS (the z-slab path exchanges halos between them).
 static dim3 dgs_grid_v(const Geom& g) { return dim3((((g.nx + 1) / 2) + 31) / 32, (g.ny + 7) / 8, g.nz); }
@@ -3032,241 +2188,102 @@ void launch_dgs_prev_c(const LevelK& L, double* x, const double* b, int c, cudaS
     count();
 }
 
-// Per-phase launches of a symmetric DGS sweep (same phase numbering and
-// delta-buffer protocol as k_dgs_sym_coop).
-// Fused velocity pair (k_dgs_vel2) launch: x -> xo, colour c0 then 1 - c0.
-static void launch_vel2(const LevelK& L, const double* xi, double* xo, const double* b, int c0, cudaStream_t s) {
-    const Geom& g = L.g;
-    const int64_t tiles = static_cast<int64_t>((g.nx + kV2X - 1) / kV2X) * ((g.ny + kV2Y - 1) / kV2Y);
-    // z-chunks per tile: about SMG_VEL2_CTAS CTAs in all, each marching >= SMG_VEL2_MINZ planes
-    const int64_t want = env_int("SMG_VEL2_CTAS", 148 * 8);
-    const int minz = std::max(1, env_int("SMG_VEL2_MINZ", 8));
-    const int64_t chunks = std::max<int64_t>(1, (want + tiles - 1) / tiles);
-    const int zch = std::max<int>(minz, static_cast<int>((g.nz + chunks - 1) / chunks));
-    if (env_int("SMG_VEL2", 0) == 2) {  // cp.async-staged variant: one 512-thread CTA per SM
-        static bool attr = false;
-        if (!attr) {
-            note(cudaFuncSetAttribute(k_dgs_vel2s, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(kS2Smem)));
-            attr = true;
-        }
-        const int64_t t2 = static_cast<int64_t>((g.nx + kS2X - 1) / kS2X) * ((g.ny + kS2Y - 1) / kS2Y);
-        const int64_t ch2 = std::max<int64_t>(1, (env_int("SMG_VEL2_CTAS", 148 * 4) + t2 - 1) / t2);
-        const int z2 = std::max<int>(minz, static_cast<int>((g.nz + ch2 - 1) / ch2));
-        const dim3 grid2((g.nx + kS2X - 1) / kS2X, (g.ny + kS2Y - 1) / kS2Y, (g.nz + z2 - 1) / z2);
-        launch_k(k_dgs_vel2s, grid2, dim3(kS2X, kS2Y), kS2Smem, s, L, xi, xo, b, c0, z2);
-        count();
-        return;
-    }
-    const dim3 grid((g.nx + kV2X - 1) / kV2X, (g.ny + kV2Y - 1) / kV2Y, (g.nz + zch - 1) / zch);
-    launch_k(k_dgs_vel2, grid, dim3(kV2X, kV2Y), 0, s, L, xi, xo, b, c0, zch);
-    count();
-}
 
-// Velocity pair in chunks of C planes (SMG_VEL_CHUNK=C): nz/C + 2 launches, see k_dgs_vel_chunk.
-static int vel_chunk(const LevelK& L) {
-    const int64_t ncell = static_cast<int64_t>(L.g.nx) * L.g.ny * L.g.nz;
-    const int c = env_int("SMG_VEL_CHUNK", 0);
-    if (c <= 0 || L.g.z0 != 0 || L.g.nz != L.g.gnz) return 0;
-    return ncell >= env_int("SMG_VEL_CHUNK_MIN_CELLS", 1 << 24) ? c : 0;
-}
-static void launch_vel_pair_chunked(const LevelK& L, double* x, const double* b, int c0, int C, cudaStream_t s) {
-    const Geom& g = L.g;
-    const dim3 gv = dgs_grid_v(g);
-    const int nch = (g.nz + C - 1) / C;
-    for (int j = 0; j < nch + 2; ++j) {
-        const int za0 = j < nch ? j * C : 0, za1 = j < nch ? std::min(g.nz, (j + 1) * C) : 0;
-        const int k = j - 2;
-        const int zb0 = k >= 0 ? k * C : 0, zb1 = k >= 0 ? std::min(g.nz, (k + 1) * C) : 0;
-        const int nz = (za1 - za0) + (zb1 - zb0);
-        if (nz == 0) continue;
-        launch_k(k_dgs_vel_chunk, dim3(gv.x, gv.y, nz), dim3(32, 8), 0, s, L, x, b, c0, za0, za1, zb0);
-        count();
-    }
-}
-
-// Opt-in (SMG_VEL2=1): the velocity pairs at both ends of a symmetric sweep run fused
-// (k_dgs_vel2) when the level has a second vector xb: the forward pair writes xb, the pressure
-// steps run in xb, the reverse pair writes back into x (bit-identical).  Measured slower than
-// the separate colour phases (cfg 1 fine sweep 0.296 -> 0.503 ms, cfg 3 20.0 -> 28.5 ms): the
-// z-march per tile serialises two dependent load round trips and two barriers per plane.
-static bool vel2_on(const LevelK& L, const double* xb, int nph) {
-    const int64_t ncell = static_cast<int64_t>(L.g.nx) * L.g.ny * L.g.nz;
-    return xb && nph > 10 && env_int("SMG_VEL2", 0) != 0 && L.g.z0 == 0 && L.g.nz == L.g.gnz &&
-           ncell >= env_int("SMG_VEL2_MIN_CELLS", 0);
-}
-
-template <int ZC>
-static void dgs_sym_phases_zc(const LevelK& L, double* x, const double* b, double* d0, int nph, cudaStream_t s,
-                              double* xb) {
+// Per-step launches of a symmetric DGS sweep (OD-1): velocity red, black, the 4 forward
+// pressure groups (lazy gathers into the delta buffer d0), the flush, then the 4 reverse
+// pressure groups and velocity black, red -- 13 kernels for the 20 phases.
+void launch_dgs_sym_coop(const LevelK& L, double* x, const double* b, double* d0, double* d1, int nph,
+                         cudaStream_t s, double* xb) {
+    (void)d1;
+    (void)xb;
     const Geom& g = L.g;
     const dim3 blk(32, 8);
-    dim3 gv = dgs_grid_v(g), gh = dgs_grid_h(g);
-    gv.z = (gv.z + ZC - 1) / ZC;
-    gh.z = (gh.z + ZC - 1) / ZC;
+    const dim3 gv = dgs_grid_v(g), gh = dgs_grid_h(g);
     auto groups_grid = [&](int grp) { return dim3(gh.x, gh.y, gh.z * group_size(grp)); };
     // consecutive steps alternate the traversal direction (kRevBit): L2 reuse between steps
     const int alt = env_int("SMG_DGS_ALT", 1) ? kRevBit : 0;
-    const bool fuse = vel2_on(L, xb, nph);
-    double* xp = x;  // where the pressure steps run
-    const int vch = fuse ? 0 : vel_chunk(L);
-    if (fuse) {
-        launch_vel2(L, x, xb, b, 0, s);
-        xp = xb;
-    } else if (vch) {
-        launch_vel_pair_chunked(L, x, b, 0, vch, s);
-    } else {
-        launch_k(k_dgs_vel_c<ZC>, gv, blk, 0, s, L, x, b, 0);
-        launch_k(k_dgs_vel_c<ZC>, gv, blk, 0, s, L, x, b, 1 | alt);
-        count();
-        count();
-    }
+    launch_k(k_dgs_vel_c<1>, gv, blk, 0, s, L, x, b, 0);
+    launch_k(k_dgs_vel_c<1>, gv, blk, 0, s, L, x, b, 1 | alt);
     for (int q = 0; q < 4; ++q)
-        launch_k(k_dgs_pf_lazy_c<ZC>, groups_grid(fwd_group(q)), blk, 0, s, L, xp, b, d0, fwd_group(q) | (q & 1 ? alt : 0));
-    launch_k(k_dgs_pf_flush, cell_grid(g), blk, 0, s, L, xp, d0, 0);
-    for (int k = 0; k < 5; ++k) count();
+        launch_k(k_dgs_pf_lazy_c<1>, groups_grid(fwd_group(q)), blk, 0, s, L, x, b, d0, fwd_group(q) | (q & 1 ? alt : 0));
+    launch_k(k_dgs_pf_flush, cell_grid(g), blk, 0, s, L, x, d0, 0);
+    for (int k = 0; k < 7; ++k) count();
     if (nph <= 10) return;
     for (int q = 0; q < 4; ++q)
-        launch_k(k_dgs_prev_c<ZC>, groups_grid(rev_group(q)), blk, 0, s, L, xp, b, rev_group(q) | (q & 1 ? 0 : alt));
-    for (int k = 0; k < 4; ++k) count();
-    if (fuse) {
-        launch_vel2(L, xb, x, b, 1, s);
-    } else if (vch) {
-        launch_vel_pair_chunked(L, x, b, 1, vch, s);
-    } else {
-        launch_k(k_dgs_vel_c<ZC>, gv, blk, 0, s, L, x, b, 1 | alt);
-        launch_k(k_dgs_vel_c<ZC>, gv, blk, 0, s, L, x, b, 0);
-        count();
-        count();
+        launch_k(k_dgs_prev_c<1>, groups_grid(rev_group(q)), blk, 0, s, L, x, b, rev_group(q) | (q & 1 ? 0 : alt));
+    launch_k(k_dgs_vel_c<1>, gv, blk, 0, s, L, x, b, 1 | alt);
+    launch_k(k_dgs_vel_c<1>, gv, blk, 0, s, L, x, b, 0);
+    for (int k = 0; k < 6; ++k) count();
+}
+
+
+// ---- tile-ordered DGS sweep (OD-1 rev. 2) ----
+typedef CUresult (*TmapEncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static TmapEncodeFn tmap_encode() {
+    static TmapEncodeFn fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<TmapEncodeFn>(p);
     }
+    return fn;
 }
 
-static void launch_dgs_sym_phases(const LevelK& L, double* x, const double* b, double* d0, double* d1, int nph,
-                                  cudaStream_t s, double* xb) {
-    (void)d1;
-    // one cell per thread on every level (SMG_DGS_ZC=2/4: two/four z-planes per thread).  Two cells
-    // per thread on levels >= 128^3 was the default until re-measured in session 5 (interleaved on
-    // one box, profiles/r1s5_zc_*.txt): ZC 1 vs 2 cfg 1 solve 18.49 vs 18.63-19.40 ms, cfg 3
-    // iteration 67.5 vs 68.3 ms, cfg 2 9.29 vs 9.39 ms, cfg 4 33.33 vs 33.69 ms
-    const int zc = env_int("SMG_DGS_ZC", 1);
-    if (zc >= 4) dgs_sym_phases_zc<4>(L, x, b, d0, nph, s, xb);
-    else if (zc == 2) dgs_sym_phases_zc<2>(L, x, b, d0, nph, s, xb);
-    else dgs_sym_phases_zc<1>(L, x, b, d0, nph, s, xb);
+bool dgs_tiled(int nx, int ny, int nz, int64_t tile_min) {
+    if (tile_min == 0) tile_min = int64_t{1} << 21;  // 128^3 (the oracle's kTileMinDefault)
+    if (tile_min < 0) return false;
+    if (static_cast<int64_t>(nx) * ny * nz < tile_min) return false;
+    return nx % kTX == 0 && ny % kTY == 0 && nz % kTZ == 0 && nx / kTX >= 2 && ny / kTY >= 2 && nz / kTZ >= 2;
+}
+int dgs_tile_dim(int axis) { return axis == 0 ? kTX : (axis == 1 ? kTY : kTZ); }
+
+// 4-D tensor map of a level vector (x, y, z slots of the padded boxes, 4 fields) with the
+// tile kernel's box; OOB coordinates (beyond the ghost ring) read as 0.
+static bool tile_tmap(const LevelK& L, const double* x, CUtensorMap* m) {
+    const Geom& g = L.g;
+    TmapEncodeFn enc = tmap_encode();
+    if (!enc) return false;
+    const cuuint64_t dims[4] = {static_cast<cuuint64_t>(g.px), static_cast<cuuint64_t>(g.py),
+                                static_cast<cuuint64_t>(g.pz), 4};
+    const cuuint64_t strides[3] = {static_cast<cuuint64_t>(g.sy) * 8, static_cast<cuuint64_t>(g.sz) * 8,
+                                   static_cast<cuuint64_t>(g.fs) * 8};
+    const cuuint32_t box[4] = {kBX, kBY, kBZ, 4};
+    const cuuint32_t es[4] = {1, 1, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(x), dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-void launch_dgs_sym_coop(const LevelK& L, double* x, const double* b, double* d0, double* d1, int nph,
-                         cudaStream_t s, double* xb) {
-    // one kernel per step on every level: inside the SQMR iteration graph the per-step
-    // kernels beat the persistent grid-barrier sweep even at 16^3-64^3 (measured: 2.43 ->
-    // 2.31 ms per cfg-1 iteration), although the sweep wins when timed back to back alone;
-    // SMG_DGS_COOP=1 / SMG_DGS_COOP_MAX=<cells> bring the persistent sweep back
-    const int64_t coop_max = env_int("SMG_DGS_COOP", 0) ? (int64_t{1} << 40) : env_int("SMG_DGS_COOP_MAX", 0);
-    if (static_cast<int64_t>(L.g.nx) * L.g.ny * L.g.nz > coop_max) {
-        launch_dgs_sym_phases(L, x, b, d0, d1, nph, s, xb);
+// Phases [ph0, ph1) on the tiles of colour T.
+void launch_dgs_tile_phases(const LevelK& L, double* x, const double* b, int T, int ph0, int ph1, cudaStream_t s) {
+    const Geom& g = L.g;
+    const int ntx = g.nx / kTX, nty = g.ny / kTY, ntz = g.nz / kTZ;
+    const int hx = (ntx - (T & 1) + 1) >> 1, hy = (nty - ((T >> 1) & 1) + 1) >> 1, hz = (ntz - ((T >> 2) & 1) + 1) >> 1;
+    if (hx * hy * hz == 0) return;
+    CUtensorMap m;
+    if (!tile_tmap(L, x, &m)) {
+        note(cudaErrorNotSupported);
         return;
     }
-    const int64_t ncell = static_cast<int64_t>(L.g.nx) * L.g.ny * L.g.nz;
-    LevelK Lc = L;
-    void* args[] = {&Lc, &x, const_cast<double**>(&b), &d0, &d1, &nph};
-    launch_sweep(reinterpret_cast<const void*>(k_dgs_sym_coop<0>), reinterpret_cast<const void*>(k_dgs_sym_coop<1>),
-                 use_cluster(ncell, env_int("SMG_DGS_CL_ITEMS", 1)), ncell, args, s);
-}
-
-// ---- fused wavefront sweep: host plan + launch ----
-std::vector<WaveHostPass> wave_build(const LevelK& L, int nph, int64_t budget) {
-    const Geom& g = L.g;
-    // extra planes between consecutive steps: a unit's dependencies then lie more than
-    // one ticket slice back, so several slices can be in flight at once
-    const int lag = env_int("SMG_WAVE_LAG", 1);
-    std::vector<WaveHostPass> out;
-    if (g.z0 != 0 || g.nz != g.gnz || (g.nx & 1) || (g.ny & 1) || g.nz > 4095) return out;
-    // the 13 steps (kind, arg) of a symmetric sweep; the forward half is the first 7
-    const int8_t kinds[kWaveMaxSteps] = {WK_VEL, WK_VEL, WK_PF, WK_PF, WK_PF, WK_PF, WK_FLUSH,
-                                         WK_PREV, WK_PREV, WK_PREV, WK_PREV, WK_VEL, WK_VEL};
-    const int8_t args[kWaveMaxSteps] = {0, 1, 0, 1, 2, 3, 0, 0, 1, 2, 3, 1, 0};
-    const int nstep = nph <= 10 ? 7 : 13;
-    // z footprint of a step at plane z: reads [z - rd, z + ru], writes [z, z + wu]
-    auto rd = [](int) { return 1; };
-    auto ru = [](int k) { return k == WK_PREV ? 2 : 1; };
-    auto wu = [](int k) { return k == WK_PF ? 1 : 0; };
-    const int64_t plane_bytes = g.sz * 8 * 9;  // x (4 fields), delta, b (4 fields)
-    int s0 = 0;
-    while (s0 < nstep) {
-        WaveHostPass hp;
-        WavePass& p = hp.p;
-        std::vector<int> off;
-        int s1 = s0;
-        while (s1 < nstep) {
-            const int k = kinds[s1], j = s1 - s0;
-            int lo = 0, hi = 0, o = 0;
-            if (j > 0) {
-                const int q = kinds[s1 - 1];
-                // RAW [z-rd-wu', z+ru], WAR [z-ru', z+wu+rd'], WAW [z-wu', z+wu]
-                lo = std::max(std::max(rd(k) + wu(q), ru(q)), wu(q));
-                hi = std::max(std::max(ru(k), wu(k) + rd(q)), wu(k));
-                o = off.back() + hi + 1 + lag;
-            }
-            const int window = o + 1 + 2;
-            if (j > 0 && window * plane_bytes > budget) break;
-            p.kind[j] = kinds[s1];
-            p.arg[j] = args[s1];
-            p.lo[j] = static_cast<int8_t>(lo);
-            p.hi[j] = static_cast<int8_t>(hi);
-            p.window = window;
-            off.push_back(o);
-            ++s1;
-        }
-        p.nsteps = s1 - s0;
-        // ticket order: tau = z + off_s ascending; units of step s at plane z depend only on
-        // step s-1 units with a smaller tau, so any CTA holding a ticket can make progress
-        for (int tau = 0; tau < g.nz + off.back(); ++tau)
-            for (int s = p.nsteps - 1; s >= 0; --s) {
-                const int z = tau - off[s];
-                if (z < 0 || z >= g.nz) continue;
-                const int nu = wave_units(p.kind[s], p.arg[s], g.gz(z) & 1, g.nx, g.ny);
-                for (int u = 0; u < nu; ++u)
-                    hp.units.push_back((static_cast<uint32_t>(s) << 28) | (static_cast<uint32_t>(z) << 16) |
-                                       static_cast<uint32_t>(u));
-            }
-        p.nunits = static_cast<int>(hp.units.size());
-        out.push_back(std::move(hp));
-        s0 = s1;
-    }
-    return out;
-}
-
-void launch_dgs_wave(const LevelK& L, const WavePass* passes, int npass, double* x, const double* b, double* d0,
-                     cudaStream_t s) {
-    static int per_sm = 0;
-    if (!per_sm) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dgs_wave, kWaveThreads, 0);
-        const int cap = env_int("SMG_WAVE_BLOCKS_PER_SM", 0);
-        if (cap > 0 && cap < per_sm) per_sm = cap;
-        if (per_sm < 1) per_sm = 1;
-    }
-    for (int k = 0; k < npass; ++k) {
-        const WavePass& p = passes[k];
-        note(cudaMemsetAsync(p.cnt, 0, (1 + static_cast<size_t>(p.nsteps) * L.g.nz) * sizeof(int), s));
-        const int grid = std::min<int64_t>(p.nunits, static_cast<int64_t>(num_sms()) * per_sm);
-        k_dgs_wave<<<grid, kWaveThreads, 0, s>>>(L, x, b, d0, p);
-        count();
-    }
-}
-
-void launch_apply_dot(const LevelK& L, const double* x, const double* b, double* y, double gamma, int dot_y,
-                      double* rowbuf, double* partials, double* sc, unsigned* cnt, int which, cudaStream_t s) {
-    const Geom& g = L.g;
-    const int R = std::max(1, std::min(kAdThreads / g.nx, 8));  // whole rows per block (nx <= 1024)
-    const size_t smem = std::max<size_t>(static_cast<size_t>(R) * 4 * (g.nx + 1), 4 * static_cast<size_t>(g.ny + 1)) *
-                        sizeof(double);
     static bool attr = false;
     if (!attr) {
-        note(cudaFuncSetAttribute(k_apply_dot, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+        note(cudaFuncSetAttribute(k_dgs_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kTileSmem)));
         attr = true;
     }
-    launch_k(k_apply_dot, dim3((g.ny + 1 + R - 1) / R, g.nz + 1), dim3(std::max(R * g.nx, 4 * R * 32)), smem, s, L,
-             x, b, y, gamma, dot_y, R, rowbuf, partials, sc, cnt, which);
+    launch_k(k_dgs_tile, dim3(hx * hy * hz), dim3(kTileThreads), kTileSmem, s, m, L, x, b, T, ph0, ph1, ntx, nty);
     count();
+}
+
+// Symmetric sweep (nph = 20) or its forward half (nph = 10): tile colours 0..7 forward, then
+// 7..0 reverse; colour 7's two halves run in one launch.
+void launch_dgs_tiled(const LevelK& L, double* x, const double* b, int nph, cudaStream_t s) {
+    for (int T = 0; T < 8; ++T) launch_dgs_tile_phases(L, x, b, T, 0, (T == 7 && nph > 10) ? 20 : 10, s);
+    if (nph <= 10) return;
+    for (int T = 6; T >= 0; --T) launch_dgs_tile_phases(L, x, b, T, 10, 20, s);
 }
 
 void launch_vanka_additive(const LevelK& L, double* x, const double* b, const int32_t* cells, const uint8_t* masks,

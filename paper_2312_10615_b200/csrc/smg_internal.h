@@ -70,6 +70,7 @@ struct LevelK {
     // c_b = m_C^T b per cell (the b part of the reverse DGS pressure update, fixed while b
     // is): launch_dgs_cb fills it before a sweep; prev steps then read L~x only
     double* cb = nullptr;
+    int tiled = 0;  // DGS sweep in tile order (OD-1 rev. 2, dgs_tiled)
 };
 
 // ---- stencil launchers (kernels.cu) ----
@@ -110,31 +111,14 @@ void launch_vanka_sym_coop(const LevelK& L, double* x, const double* b, const in
                            cudaStream_t s, double* xb = nullptr, const int32_t* refresh = nullptr,
                            int64_t nrefresh = 0, const VankaPairs& pr = VankaPairs{});
 int vanka_pairs_pay(const int* n);  // mask of the pairs to merge on a level with these list sizes
-// xb (optional, a second vector of the level, used as scratch): the velocity pairs at both
-// ends of the sweep run fused (k_dgs_vel2, x -> xb ... xb -> x).
+// One kernel per step (13 steps for the 20 phases); xb, d1 unused.
 void launch_dgs_sym_coop(const LevelK& L, double* x, const double* b, double* d0, double* d1, int nph,
                          cudaStream_t s, double* xb = nullptr);
-// Whole smooth (Alg. 3) of a level held in the distributed shared memory of one
-// 16-CTA cluster (vector + DGS delta <= 2 MB).
-bool smooth_dsm_fits(const LevelK& L, const int* n);
-void launch_smooth_dsm(const LevelK& L, double* x, const double* b, const int32_t* const* cells,
-                       const uint8_t* const* masks, const int* n, const double* ktab, int nu, int nph,
-                       cudaStream_t s, const VankaPairs& pr = VankaPairs{});
-// Whole smooth (Alg. 3) of a level small enough for one CTA's shared memory.
-bool smooth_smem_fits(const LevelK& L, const int* n);
-void launch_smooth_smem(const LevelK& L, double* x, const double* b, const int32_t* const* cells,
-                        const uint8_t* const* masks, const int* n, const double* ktab, double* d0, double* d1, int nu,
-                        int nph, cudaStream_t s, const VankaPairs& pr = VankaPairs{});
 // Restriction of coarse LOCAL planes [zc_lo, zc_lo + nzc) (nzc < 0: all); the
 // fine slab must hold the fine planes 2zc-1 .. 2zc+2 (halos included).
 void launch_restrict(const LevelK& F, const LevelK& C, const double* rf, double* bc, cudaStream_t s, int zc_lo = 0,
                      int nzc = -1);
 void launch_prolong_add(const LevelK& F, const LevelK& C, const double* xc, double* xf, cudaStream_t s);
-// Fused b_c = R (b - L~ x) (no fine residual vector), single-part levels; bit-identical
-// to launch_apply(b) + launch_restrict.  resrestrict_ok: the fused path applies (opt-in, SMG_FUSED_RR=1).
-bool resrestrict_ok(const LevelK& F, const LevelK& C);
-void launch_residual_restrict(const LevelK& F, const LevelK& C, const double* x, const double* b, double* bc,
-                              cudaStream_t s);
 void launch_coarse_gemv(const double* ksym, const int32_t* slots, int n, const double* b, double* x,
                         cudaStream_t s);
 void launch_pack(const LevelK& L, const double* padded, double* compact, cudaStream_t s);
@@ -153,6 +137,14 @@ constexpr int kMaxPlanesStride = 4 * 1025 + 4;
 void launch_cdot_planes(const Geom& g, const double* a, const double* b, const double* c, const double* d,
                         double* partials, cudaStream_t s);
 void launch_cdot_final(const Geom& g, const double* partials, double* out, cudaStream_t s);
+// Tile-ordered DGS (OD-1 rev. 2): a level is tiled iff it has >= tile_min cells (0: 128^3,
+// < 0: never) and its extents are multiples of the tile (16 x 8 x 8) with >= 2 tiles per axis.
+bool dgs_tiled(int nx, int ny, int nz, int64_t tile_min);
+int dgs_tile_dim(int axis);
+// phases [ph0, ph1) of the 20-phase numbering on the tiles of colour T
+void launch_dgs_tile_phases(const LevelK& L, double* x, const double* b, int T, int ph0, int ph1, cudaStream_t s);
+// symmetric sweep (nph = 20) or forward half (nph = 10) in tile order; L.cb must hold m^T b
+void launch_dgs_tiled(const LevelK& L, double* x, const double* b, int nph, cudaStream_t s);
 // Single colour-compact DGS phases (used by the z-slab path).
 void launch_dgs_vel_c(const LevelK& L, double* x, const double* b, int colour, cudaStream_t s);
 void launch_dgs_pf_delta_c(const LevelK& L, const double* x, const double* b, double* d, int c, cudaStream_t s);
@@ -178,48 +170,9 @@ void launch_stamp(unsigned long long* stamp, cudaStream_t s);
 // d7: scratch of 7 fields (g.fs each).  Bit-identical to the oracle's fixed order.
 void launch_vanka_additive(const LevelK& L, double* x, const double* b, const int32_t* cells, const uint8_t* masks,
                            int n, const double* ktab, double* d7, double omega, cudaStream_t s);
-// Fused y = L x (b null) or y = b - L x, sc[S_D0] = x.y (dot_y = 0) or y.y (dot_y = 1) in
-// the canonical order, then the scalar update `which` (1 alpha, 3 beta) -- bit-identical to
-// launch_apply + launch_cdot2 + launch_sqmr_scalar.  rowbuf: 4 (ny+1)(nz+1) doubles;
-// cnt: nz + 2 zeroed device counters (reset by the kernel).
-void launch_apply_dot(const LevelK& L, const double* x, const double* b, double* y, double gamma, int dot_y,
-                      double* rowbuf, double* partials, double* sc, unsigned* cnt, int which, cudaStream_t s);
 void launch_axpy_s(double* s_, const double* t, const double* sc, int64_t n, cudaStream_t s);
 void launch_dx_dev(double* d, double* x, const double* q, const double* sc, int64_t n, cudaStream_t s);
 void launch_xpby_dev(double* q, const double* t, const double* sc, int64_t n, cudaStream_t s);
-
-// ---- fused (dataflow wavefront) symmetric DGS sweep, large single-part levels ----
-// The 13 steps of a sweep (vel 0, vel 1, 4 forward pressure groups, flush, 4
-// reverse pressure groups, vel 1, vel 0) run inside ONE persistent launch per
-// pass: work units (step s, plane z, tile u) are taken in ticket order
-// (tau = z + off_s), and a unit starts once step s-1 has completed the planes
-// it reads or overwrites (per-(s,z) completion counters).  A plane is then
-// touched by all steps of the pass while it is still L2-resident, so the sweep
-// reads x and b from HBM once per pass instead of once per step.  Passes are
-// split so that the live plane window fits the L2 budget.  Same per-cell
-// functions and the same order of updates per cell: bit-identical.
-constexpr int kWaveMaxSteps = 13;
-enum WaveKind : int8_t { WK_VEL = 0, WK_PF = 1, WK_FLUSH = 2, WK_PREV = 3 };
-struct WavePass {
-    int nsteps = 0;
-    int8_t kind[kWaveMaxSteps] = {}, arg[kWaveMaxSteps] = {};
-    int8_t lo[kWaveMaxSteps] = {}, hi[kWaveMaxSteps] = {};  // planes of step s-1 a unit of step s waits for
-    const uint32_t* units = nullptr;  // device: packed (s << 28 | z << 16 | u) in ticket order
-    int nunits = 0;
-    int* cnt = nullptr;  // device: [0] ticket counter, [1 + s * nz + z] completed units of (s, z)
-    int window = 0;      // live planes (for the report)
-};
-constexpr int kWaveCellsPerUnit = 512;  // 256 threads x 2 cells
-struct WaveHostPass {
-    WavePass p;
-    std::vector<uint32_t> units;
-};
-// Plan of a sweep (nph = 20 symmetric, 10 forward half) on level L, passes
-// sized to `budget` bytes of live planes.  Empty if the level does not qualify.
-std::vector<WaveHostPass> wave_build(const LevelK& L, int nph, int64_t budget);
-// One pass per entry; cnt must hold 1 + nsteps * nz ints (reset here).
-void launch_dgs_wave(const LevelK& L, const WavePass* passes, int npass, double* x, const double* b, double* d0,
-                     cudaStream_t s);
 
 // Number of our kernels launched so far (per process), for the bench's gpu_launches.
 int64_t launch_count();

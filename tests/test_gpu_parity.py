@@ -283,20 +283,6 @@ def test_parameter_sweep_bitwise(nu, bw, eta, gamma):
     s.close()
 
 
-def test_dsm_smoother_bitwise(monkeypatch):
-    """Opt-in cluster-resident (DSMEM) smoother: same arithmetic, bit-identical."""
-    monkeypatch.setenv("SMG_DSM_SMOOTH", "1")
-    oracle.set_threads(4)
-    for n, lv in ((16, 2), (32, 3)):
-        o = oracle.Oracle(n, levels=lv)
-        s = smg.Solver(n, levels=lv)
-        b = o.forcing(oracle.FORCE_UNIFORM, 3)
-        x = np.random.default_rng(n).uniform(-1, 1, o.ndof())
-        same(s.smoother(smg.OP_SMOOTH, x, b), o.smoother(4, x, b))
-        assert np.array_equal(s.vcycle(b), o.vcycle(b))
-        s.close()
-
-
 def test_lid_driven_cavity_bitwise():
     """The paper's 3-D cavity: zero force, lid u = 1; GPU solve == oracle, flow follows the lid."""
     oracle.set_threads(os.cpu_count() or 1)
@@ -311,50 +297,9 @@ def test_lid_driven_cavity_bitwise():
     assert u[:, -1, :].mean() > 0.1 and u[:, 0, :].mean() < u[:, -1, :].mean()
 
 
-@pytest.mark.parametrize("mb", ["1", "48"])
-@pytest.mark.parametrize("shape", [(32, 32, 32, 3), (64, 64, 64, 4), (64, 16, 16, 3), (48, 40, 24, 3)])
-def test_wave_dgs_bitwise(shape, mb, monkeypatch):
-    """Opt-in fused wavefront DGS sweep (forced onto small levels; 1 MB budget = one step
-    per pass, 48 MB = all 13 steps in one pass): bit-identical to the oracle's phase order."""
-    monkeypatch.setenv("SMG_WAVE", "1")
-    monkeypatch.setenv("SMG_WAVE_MIN_CELLS", "1")
-    monkeypatch.setenv("SMG_WAVE_MB", mb)
-    monkeypatch.setenv("SMG_NO_SMEM_SMOOTH", "1")
-    oracle.set_threads(os.cpu_count() or 1)
-    nx, ny, nz, lv = shape
-    o = oracle.Oracle(nx, ny, nz, h=1 / ny, levels=lv)
-    s = smg.Solver(nx, ny, nz, h=1 / ny, levels=lv)
-    for level in range(lv - 1):
-        n = o.ndof(level)
-        x, b = rnd(n, 60 + level), rnd(n, 61 + level)
-        same(s.smoother(smg.OP_SMOOTH, x, b, level), o.smoother(4, x, b, level))
-    b = o.forcing(oracle.FORCE_UNIFORM, 5)
-    same(s.vcycle(b), o.vcycle(b))
-    xo, ho, _, sto = o.sqmr(b, 1e-6, 6)
-    xg, hg, _, stg = s.sqmr(b, 1e-6, 6)
-    assert sto == stg and np.array_equal(ho, hg) and np.array_equal(xo, xg)
-    s.close()
-
-
-def test_wave_dgs_forward_half_bitwise(monkeypatch):
-    """Forward half only (FLAG_SKIP_REVERSE_DGS: 7 steps): wavefront == cooperative sweep."""
-    monkeypatch.setenv("SMG_NO_SMEM_SMOOTH", "1")
-    x, b = None, None
-    out = []
-    for wave in ("0", "1"):
-        monkeypatch.setenv("SMG_WAVE", wave)
-        monkeypatch.setenv("SMG_WAVE_MIN_CELLS", "1")
-        s = smg.Solver(32, levels=3, flags=smg.FLAG_SKIP_REVERSE_DGS)
-        if x is None:
-            x, b = rnd(s.ndof(), 7), rnd(s.ndof(), 8)
-        out.append(s.smoother(smg.OP_SMOOTH, x, b))
-        s.close()
-    same(out[1], out[0])
-
-
 @pytest.mark.parametrize("mode", [{}, {"SMG_SYNC_MODE": "1"}, {"SMG_SYNC_MODE": "2"}, {"SMG_VANKA_PP": "0"},
-                                  {"SMG_VANKA_PHASES": "1"}, {"SMG_SMEM_SMOOTH": "1"}, {"SMG_DGS_COOP": "1"},
-                                  {"SMG_VANKA_KERNELS": "1"}, {"SMG_DGS_COOP": "1", "SMG_SYNC_MODE": "2"},
+                                  {"SMG_VANKA_PHASES": "1"},
+                                  {"SMG_VANKA_KERNELS": "1"},
                                   {"SMG_VANKA_PAIRS": "0"}, {"SMG_VANKA_PAIRS": "2", "SMG_SYNC_MODE": "1"},
                                   {"SMG_VANKA_PAIRS": "2", "SMG_VANKA_KERNELS": "1"},
                                   {"SMG_VANKA_PAIRS": "0", "SMG_VANKA_PHASES": "1"}])
@@ -394,25 +339,6 @@ def test_vanka_merged_matches_unmerged(n, levels, monkeypatch):
             same(a, c)
 
 
-@pytest.mark.parametrize("dims,levels", [((32, 32, 32), 3), ((48, 40, 24), 3), ((64, 16, 16), 3), ((128, 128, 128), 5)])
-def test_fused_velocity_pair_matches_separate(dims, levels, monkeypatch):
-    """Fused red+black velocity DGS pass (k_dgs_vel2, ping-pong through the level's second
-    vector) == the two separate colour phases, bit for bit: symmetric DGS, smooth, V-cycle."""
-    nx, ny, nz = dims
-    out = []
-    for fused in ("0", "1", "2"):  # 2: cp.async-staged variant
-        monkeypatch.setenv("SMG_VEL2", fused)
-        monkeypatch.setenv("SMG_VEL2_CTAS", "64")  # long marches too (several planes per CTA)
-        s = smg.Solver(nx, ny, nz, h=1 / ny, levels=levels)
-        x = np.random.default_rng(nx + ny).uniform(-1, 1, s.ndof())
-        b = np.random.default_rng(nz).uniform(-1, 1, s.ndof())
-        out.append((s.smoother(smg.OP_DGS_SYM, x, b), s.smoother(smg.OP_SMOOTH, x, b), s.vcycle(b)))
-        s.close()
-    for o in out[1:]:
-        for a, c in zip(o, out[0]):
-            same(a, c)
-
-
 def test_vanka_per_launch_large_level_matches_persistent(monkeypatch):
     """256^3 (lists beyond the persistent ping-pong sweep): default merged persistent sweep ==
     one ping-pong launch per merged phase (the 512^3 default) == unmerged per-launch phases ==
@@ -431,21 +357,6 @@ def test_vanka_per_launch_large_level_matches_persistent(monkeypatch):
         s.close()
     for o in out[1:]:
         same(o, out[0])
-
-
-@pytest.mark.parametrize("dims,levels", [((32, 32, 32), 3), ((64, 16, 16), 3), ((48, 40, 24), 3)])
-def test_fused_apply_dot_matches_separate(dims, levels, monkeypatch):
-    """Opt-in fused apply + canonical dot + scalar kernel (SMG_FUSED_DOT=1) == separate kernels, bit for bit."""
-    out = []
-    nx, ny, nz = dims
-    for fused in ("0", "1"):
-        monkeypatch.setenv("SMG_FUSED_DOT", fused)
-        s = smg.Solver(nx, ny, nz, h=1 / ny, levels=levels)
-        b = smg.forcing(nx, ny, nz, h=1 / ny, kind=smg.FORCE_UNIFORM, seed=11)
-        out.append(s.sqmr(b, 1e-8, 40))
-        s.close()
-    (x0, h0, _, s0), (x1, h1, _, s1) = out
-    assert s0 == s1 and np.array_equal(h0, h1) and np.array_equal(x0, x1)
 
 
 @pytest.mark.parametrize("dims,levels,omega", [((16, 16, 16), 3, 0.5), ((32, 32, 32), 3, 0.5), ((64, 16, 16), 3, 1.0),
@@ -469,31 +380,12 @@ def test_additive_vanka_bitwise(dims, levels, omega):
     s.close()
 
 
-@pytest.mark.parametrize("dims,levels", [((32, 32, 32), 3), ((64, 16, 16), 3), ((48, 40, 24), 3)])
-def test_fused_residual_restrict_bitwise(dims, levels, monkeypatch):
-    """Opt-in fused b_c = R (b - L~ x) (SMG_FUSED_RR=1): V-cycle and MG-SQMR bit-identical to the oracle."""
-    monkeypatch.setenv("SMG_FUSED_RR", "1")
-    oracle.set_threads(os.cpu_count() or 1)
-    nx, ny, nz = dims
-    o = oracle.Oracle(nx, ny, nz, h=1 / ny, levels=levels)
-    s = smg.Solver(nx, ny, nz, h=1 / ny, levels=levels)
-    b = o.forcing(oracle.FORCE_UNIFORM, 13)
-    same(s.vcycle(b), o.vcycle(b))
-    xo, ho, _, sto = o.sqmr(b, 1e-8, 20)
-    xg, hg, _, stg = s.sqmr(b, 1e-8, 20)
-    assert sto == stg and np.array_equal(ho, hg) and np.array_equal(xo, xg)
-    s.close()
-
-
 @pytest.mark.parametrize("zseg", ["1", "2", "3", "5"])
 @pytest.mark.parametrize("dims", [(16, 16, 16), (24, 16, 40)])
 def test_restrict_zmarch_bitwise(dims, zseg, monkeypatch):
-    """z-marching restriction and prolongation (k_restrict_zm / k_prolong_zm: per-plane
-    partials reused across planes, ragged segments) == the oracle's R = P^T/8 and P, bit for
-    bit, on every level."""
+    """z-marching restriction (k_restrict_zm: per-plane partials reused across planes, ragged
+    segments) == the oracle's R = P^T/8, bit for bit, on every level (prolongation: per cell)."""
     monkeypatch.setenv("SMG_RESTRICT_ZSEG", zseg)
-    monkeypatch.setenv("SMG_PROLONG_ZPAIRS", zseg)
-    monkeypatch.setenv("SMG_PROLONG_ZM", "1")
     nx, ny, nz = dims
     o = oracle.Oracle(nx, ny, nz, h=1 / ny, levels=3)
     s = smg.Solver(nx, ny, nz, h=1 / ny, levels=3)
@@ -510,47 +402,19 @@ def test_restrict_zmarch_bitwise(dims, zseg, monkeypatch):
 
 
 def test_restrict_zmarch_matches_per_cell_at_256():
-    """At 256^3 the default transfers march (segments of several planes): same results as
-    the per-cell kernels (SMG_RESTRICT_ZM=0, SMG_PROLONG_ZM=0)."""
+    """At 256^3 the default restriction marches (segments of several planes): same results as
+    the per-cell kernel (SMG_RESTRICT_ZM=0)."""
     out = []
     for zm in ("1", "0"):
         os.environ["SMG_RESTRICT_ZM"] = zm
-        os.environ["SMG_PROLONG_ZM"] = zm
-        os.environ["SMG_PROLONG_ZPAIRS"] = "0"
         try:
             s = smg.Solver(256, levels=6)
             rf = rnd(s.ndof(0), 29)
-            xc = rnd(s.ndof(1), 30)
-            out.append((s.restrict(rf, 0), s.prolong(xc, 0)))
+            out.append(s.restrict(rf, 0))
             s.close()
         finally:
             os.environ.pop("SMG_RESTRICT_ZM", None)
-            os.environ.pop("SMG_PROLONG_ZM", None)
-            os.environ.pop("SMG_PROLONG_ZPAIRS", None)
-    same(out[0][0], out[1][0])
-    same(out[0][1], out[1][1])
-
-
-@pytest.mark.parametrize("chunk", ["1", "2", "3", "5"])
-@pytest.mark.parametrize("dims,levels", [((32, 32, 32), 3), ((48, 40, 24), 3)])
-def test_velocity_pair_chunked_bitwise(dims, levels, chunk, monkeypatch):
-    """Chunked velocity pair (k_dgs_vel_chunk: first colour on chunk j with the second colour on
-    chunk j-2 in one launch) == the two whole-level colour phases, bit for bit: symmetric DGS,
-    smooth and V-cycle, and the oracle's DGS sweep."""
-    nx, ny, nz = dims
-    x = np.random.default_rng(nx + ny).uniform(-1, 1, smg.ndof_box(nx, ny, nz))
-    b = np.random.default_rng(nz).uniform(-1, 1, smg.ndof_box(nx, ny, nz))
-    out = []
-    for c in ("0", chunk):
-        monkeypatch.setenv("SMG_VEL_CHUNK", c)
-        monkeypatch.setenv("SMG_VEL_CHUNK_MIN_CELLS", "0")
-        s = smg.Solver(nx, ny, nz, h=1 / ny, levels=levels)
-        out.append((s.smoother(smg.OP_DGS_SYM, x, b), s.smoother(smg.OP_SMOOTH, x, b), s.vcycle(b)))
-        s.close()
-    for a, c in zip(out[1], out[0]):
-        same(a, c)
-    o = oracle.Oracle(nx, ny, nz, h=1 / ny, levels=levels)
-    same(out[1][0], o.smoother(1, x, b, 0))  # oracle op 1: symmetric DGS
+    same(out[0], out[1])
 
 
 @pytest.mark.parametrize("maxit", [500, 2])

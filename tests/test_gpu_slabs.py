@@ -35,6 +35,36 @@ def test_sqmr_bitwise(n, levels, parts, kind):
     many.close()
 
 
+@pytest.mark.parametrize("n,levels,parts", [(48, 5, 2), (48, 4, 4)])
+def test_odd_slab_levels_bitwise(n, levels, parts):
+    """Levels whose slab would be odd stay replicated: 48^3 with 5 levels on 2 parts
+    distributes 3 levels and still matches one part bit for bit."""
+    one = smg.Solver(n, levels=levels)
+    many = smg.Solver(n, levels=levels, devices=[0] * parts)
+    b = smg.forcing(n, kind=smg.FORCE_UNIFORM, seed=17)
+    assert np.array_equal(many.vcycle(b), one.vcycle(b))
+    x1, h1, _, s1 = one.sqmr(b, 1e-6, 60)
+    x2, h2, _, s2 = many.sqmr(b, 1e-6, 60)
+    assert s1 == s2 and np.array_equal(h1, h2) and np.array_equal(x1, x2)
+    one.close()
+    many.close()
+
+
+@pytest.mark.parametrize("n,levels,parts", [(64, 5, 2), (64, 4, 4)])
+def test_wcycle_slabs_bitwise(n, levels, parts):
+    """W-cycle on slab parts (second recursive call on distributed and replicated children) ==
+    the single-part W-cycle, bit for bit (dist_vcycle used to ignore cycle = 1)."""
+    one = smg.Solver(n, levels=levels, cycle=1)
+    many = smg.Solver(n, levels=levels, cycle=1, devices=[0] * parts)
+    b = smg.forcing(n, kind=smg.FORCE_UNIFORM, seed=19)
+    assert np.array_equal(many.vcycle(b), one.vcycle(b))
+    x1, h1, _, s1 = one.sqmr(b, 1e-6, 60)
+    x2, h2, _, s2 = many.sqmr(b, 1e-6, 60)
+    assert s1 == s2 and np.array_equal(h1, h2) and np.array_equal(x1, x2)
+    one.close()
+    many.close()
+
+
 def test_channel_slabs_bitwise():
     one = smg.Solver(64, 16, 16, h=1 / 16, levels=3)
     many = smg.Solver(64, 16, 16, h=1 / 16, levels=3, devices=[0, 0])
@@ -73,10 +103,8 @@ def test_nccl_rank_path_bitwise(monkeypatch):
 
 @pytest.mark.parametrize("zseg", ["2", "3"])
 def test_restrict_zmarch_slabs_bitwise(zseg, monkeypatch):
-    """z-marching restriction and prolongation on slab parts (local plane ranges, ghost planes) == one part."""
+    """z-marching restriction on slab parts (local plane ranges, ghost planes) == one part."""
     monkeypatch.setenv("SMG_RESTRICT_ZSEG", zseg)
-    monkeypatch.setenv("SMG_PROLONG_ZPAIRS", zseg)
-    monkeypatch.setenv("SMG_PROLONG_ZM", "1")
     one = smg.Solver(32, levels=3)
     many = smg.Solver(32, levels=3, devices=[0, 0])
     b = np.random.default_rng(7).uniform(-1, 1, one.ndof())

@@ -24,12 +24,21 @@ def test_slab_plan_covers_and_aligns(nz, levels, parts):
         if l < nd:
             assert [s[0] for s in slabs] == [r * nzl // parts for r in range(parts)]
             assert all(s[1] == nzl // parts >= 2 for s in slabs)
+            assert all(s[1] % 2 == 0 for s in slabs)  # every coarse plane has both children in one slab
             if l + 1 < nd:  # coarse slab = half of the fine slab (restriction stays local)
                 for p in plans:
                     assert p[1][l + 1][0] * 2 == p[1][l][0]
         else:
             assert all(s == (0, nzl) for s in slabs)
     assert nd <= levels - 1  # coarsest level is always replicated (dense solve)
+
+
+def test_slab_plan_stops_before_odd_slab():
+    """48^3, 5 levels, 2 parts: slabs 24, 12, 6 are split, the 3-plane slab of level 3 is not
+    (its coarse plane 2 would straddle two parts), so levels 3 and 4 are replicated."""
+    nd, plan = smg.slab_plan(48, 48, 48, 5, 2, 1)
+    assert nd == 3
+    assert plan[2] == (6, 6) and plan[3] == (0, 6) and plan[4] == (0, 3)
 
 
 def test_slab_plan_rejects_unsplittable():
