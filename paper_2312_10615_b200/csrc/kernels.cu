@@ -1604,21 +1604,31 @@ __global__ void k_xpby_dev(double* __restrict__ q, const double* __restrict__ t,
 // (reverse phases 10..19 inside each tile): "a given traversal order, then exactly the
 // reverse", so the sweep stays symmetric.  Same-colour tiles are a whole
 // tile apart, farther than any read (radius 2) plus write (radius 1) reach, so they run
-// in parallel exactly as in sequence.  One CTA owns one tile: ONE TMA load
-// (cp.async.bulk.tensor, 4-D box of all four fields with a halo of -2..+2 in x, -1..+2 in
-// y and z) stages the tile's neighbourhood in shared memory, every phase runs there with
-// __syncthreads between phases, and only the DOFs a phase may change go back to HBM.
-// Per-point arithmetic is the per-step kernels' (mom / cont / prev_core with box strides),
-// and the in-tile order is the oracle's: bit-identical.  A level vector is read once and
-// written once per half sweep (plus the halo), instead of 13 passes of the per-step
-// kernels.
+// in parallel exactly as in sequence.  One CTA owns one tile.  TMA (cp.async.bulk.tensor)
+// stages the tile's neighbourhood of x (4-D box: all four fields), the tile's b and (for
+// the reverse half) its m^T b in shared memory; every phase runs there with __syncthreads
+// between phases, and only the DOFs a phase may change go back to HBM.  Per-point
+// arithmetic is the per-step kernels' (mom / cont / prev_core with box strides) and the
+// in-tile order is the oracle's: bit-identical.  A level vector is read once and written
+// once per half sweep (plus the halo), instead of 13 passes of the per-step kernels.
+//
+// Two variants keep two CTAs per SM: FWD (phases 0..9; x box [-1, T+1) per axis, the
+// pressure deltas of the tile) and REV (phases 10..19; x box x [-2, TX+2), y, z [-1, T+2)
+// for the radius-2 reads of the reverse pressure update; m^T b of the tile).
 constexpr int kTX = 16, kTY = 8, kTZ = 8;
-constexpr int kBX = kTX + 4, kBY = kTY + 3, kBZ = kTZ + 3;  // box x [-2, TX+2), y/z [-1, T+2)
-constexpr int kOX = 2, kOY = 1, kOZ = 1;
-constexpr int kBox = kBX * kBY * kBZ;
 constexpr int kTileThreads = 256;
 constexpr int kTileCells = kTX * kTY * kTZ;
-constexpr size_t kTileSmem = 5 * kBox * sizeof(double) + 128;  // x box (4 fields), delta box, mbarrier
+template <bool FWD>
+struct TileBox {
+    static constexpr int OX = FWD ? 1 : 2, OY = 1, OZ = 1;
+    static constexpr int BX = FWD ? kTX + 2 : kTX + 4, BY = FWD ? kTY + 2 : kTY + 3, BZ = FWD ? kTZ + 2 : kTZ + 3;
+    static constexpr int BOX = BX * BY * BZ;
+    static constexpr int NB = FWD ? 4 : 3;  // fields of b staged
+    // x box (4 fields), b (NB fields of the tile), delta (FWD) or m^T b (REV) of the tile, mbarrier
+    static constexpr size_t SMEM = (4 * BOX + (NB + 1) * kTileCells) * sizeof(double) + 128 + 16;
+    static __device__ __forceinline__ int li(int x, int y, int z) { return ((z + OZ) * BY + (y + OY)) * BX + (x + OX); }
+};
+__device__ __forceinline__ int tile_ti(int x, int y, int z) { return (z * kTY + y) * kTX + x; }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -1630,24 +1640,190 @@ __device__ __forceinline__ void tile_pcell(int e, int c, int& x, int& y, int& z)
     y = 2 * ((e / (kTX / 2)) % (kTY / 2)) + ((c >> 1) & 1);
     z = 2 * (e / (kTX * kTY / 4)) + ((c >> 2) & 1);
 }
-__device__ __forceinline__ int tile_li(int x, int y, int z) { return ((z + kOZ) * kBY + (y + kOY)) * kBX + (x + kOX); }
 
-// phases [ph0, ph1) of the 20-phase numbering (0,1 velocity; 2..9 forward pressure colours
-// 0..7; 10..17 reverse pressure colours 7..0; 18,19 velocity 1,0) on the tiles of colour T.
-__global__ void __launch_bounds__(kTileThreads, 2) k_dgs_tile(const __grid_constant__ CUtensorMap tmx, LevelK L,
-                                                            double* __restrict__ X, const double* __restrict__ B,
-                                                            int T, int ph0, int ph1, int ntx, int nty) {
-    extern __shared__ __align__(128) unsigned char tsm_raw[];
-    double* xs = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(tsm_raw) + 127) & ~uintptr_t(127));
-    double* ds = xs + 4 * kBox;
-    uint64_t* bar = reinterpret_cast<uint64_t*>(ds + kBox);
+// The phases of one tile.  IN: an interior tile (no band cell in the tile or one cell around
+// it, every cell of the extended box active): no band or bounds tests at all.
+template <bool IN>
+__device__ __forceinline__ bool tile_v2(const LevelK& L, int x0, int y0, int z0, int lx, int ly, int lz) {
+    if (IN) return lx >= 0 && ly >= 0 && lz >= 0 && lx < kTX && ly < kTY && lz < kTZ;
+    return lx >= 0 && ly >= 0 && lz >= 0 && lx < kTX && ly < kTY && lz < kTZ &&
+           !band_cell(L, x0 + lx, y0 + ly, z0 + lz);
+}
+
+template <bool FWD, bool IN>
+__device__ __forceinline__ void tile_phases(const LevelK& L, const LevelK& Ls, double* __restrict__ xs,
+                                            const double* __restrict__ bs, double* __restrict__ ts, int x0, int y0,
+                                            int z0, int ph0, int ph1) {
+    using TB = TileBox<FWD>;
     const Geom& g = L.g;
     const int tid = threadIdx.x;
-    // tile of colour T for this CTA
+    constexpr int SY = TB::BX, SZ = TB::BX * TB::BY;
+    double *Us = xs, *Vs = xs + TB::BOX, *Ws = xs + 2 * TB::BOX, *Ps = xs + 3 * TB::BOX;
+    for (int ph = ph0; ph < ph1; ++ph) {
+        if (ph <= 1 || ph >= 18) {  // velocity colour (red-black on global parity)
+            const int c = ph <= 1 ? ph : 19 - ph;
+#pragma unroll
+            for (int k = 0; k < kTileCells / 2 / kTileThreads; ++k) {
+                const int e = tid + k * kTileThreads;
+                const int lz = e / (kTX * kTY / 2), ly = (e / (kTX / 2)) % kTY;
+                const int lx = 2 * (e % (kTX / 2)) + ((ly + lz + c + g.z0) & 1);
+                const int li = TB::li(lx, ly, lz), ti = tile_ti(lx, ly, lz);
+                const int gx = x0 + lx, gy = y0 + ly, zl = z0 + lz;
+                const bool here = !IN && band_cell(L, gx, gy, zl);
+                if (IN || (gx >= 1 && !here && !band_cell(L, gx - 1, gy, zl))) {
+                    const double r = bs[ti] - mom(Ls, Us, Ps, li, 1);
+                    Us[li] = Us[li] + r / L.dv;
+                }
+                if (IN || (gy >= 1 && !here && !band_cell(L, gx, gy - 1, zl))) {
+                    const double r = bs[kTileCells + ti] - mom(Ls, Vs, Ps, li, SY);
+                    Vs[li] = Vs[li] + r / L.dv;
+                }
+                if (IN || (g.gz(zl) >= 1 && !here && !band_cell(L, gx, gy, zl - 1))) {
+                    const double r = bs[2 * kTileCells + ti] - mom(Ls, Ws, Ps, li, SZ);
+                    Ws[li] = Ws[li] + r / L.dv;
+                }
+            }
+            __syncthreads();
+        } else if (FWD) {  // forward pressure colour c (eager gather form, the oracle's); ts = deltas
+            const int c = ph - 2;
+            constexpr int ncc = kTileCells / 8;
+            if (tid < ncc) {
+                int lx, ly, lz;
+                if (ph > 2) {  // clear the previous colour's deltas
+                    tile_pcell(tid, c - 1, lx, ly, lz);
+                    ts[tile_ti(lx, ly, lz)] = 0.0;
+                }
+                tile_pcell(tid, c, lx, ly, lz);
+                if (tile_v2<IN>(L, x0, y0, z0, lx, ly, lz)) {
+                    const int li = TB::li(lx, ly, lz), ti = tile_ti(lx, ly, lz);
+                    ts[ti] = (bs[3 * kTileCells + ti] - cont(Ls, Us, Vs, Ws, Ps, li, L.gamma)) / L.dp;
+                }
+            }
+            __syncthreads();
+            if (tid < ncc) {  // faces and self term of the colour-c cells (their neighbours carry no delta)
+                int lx, ly, lz;
+                tile_pcell(tid, c, lx, ly, lz);
+                if (tile_v2<IN>(L, x0, y0, z0, lx, ly, lz)) {
+                    const int li = TB::li(lx, ly, lz);
+                    const double dc = ts[tile_ti(lx, ly, lz)];
+                    Us[li] = Us[li] + (0.0 - dc) * L.inv_h;
+                    Us[li + 1] = Us[li + 1] + (dc - 0.0) * L.inv_h;
+                    Vs[li] = Vs[li] + (0.0 - dc) * L.inv_h;
+                    Vs[li + SY] = Vs[li + SY] + (dc - 0.0) * L.inv_h;
+                    Ws[li] = Ws[li] + (0.0 - dc) * L.inv_h;
+                    Ws[li + SZ] = Ws[li + SZ] + (dc - 0.0) * L.inv_h;
+                    double sn = 0.0 + 0.0;
+                    sn = sn + 0.0;
+                    sn = sn + 0.0;
+                    sn = sn + 0.0;
+                    sn = sn + 0.0;
+                    Ps[li] = Ps[li] + L.eta_h2 * (6.0 * dc - sn);
+                }
+            }
+            // neighbour pressures K = C -+ e_a of the colour-c cells: 9x4x4 (a = x), 8x5x4 (y),
+            // 8x4x5 (z); each K borders colour c along one axis only, so it gets one update
+            constexpr int NKX = (kTX / 2 + 1) * (kTY / 2) * (kTZ / 2);
+            constexpr int NKY = (kTX / 2) * (kTY / 2 + 1) * (kTZ / 2);
+            constexpr int NKZ = (kTX / 2) * (kTY / 2) * (kTZ / 2 + 1);
+            const int cx = c & 1, cy = (c >> 1) & 1, cz = (c >> 2) & 1;
+            for (int e = tid; e < NKX + NKY + NKZ; e += kTileThreads) {
+                int ax, lx, ly, lz;
+                if (e < NKX) {
+                    ax = 0;
+                    lx = cx - 1 + 2 * (e % (kTX / 2 + 1));
+                    ly = cy + 2 * ((e / (kTX / 2 + 1)) % (kTY / 2));
+                    lz = cz + 2 * (e / ((kTX / 2 + 1) * (kTY / 2)));
+                } else if (e < NKX + NKY) {
+                    const int f = e - NKX;
+                    ax = 1;
+                    lx = cx + 2 * (f % (kTX / 2));
+                    ly = cy - 1 + 2 * ((f / (kTX / 2)) % (kTY / 2 + 1));
+                    lz = cz + 2 * (f / ((kTX / 2) * (kTY / 2 + 1)));
+                } else {
+                    const int f = e - NKX - NKY;
+                    ax = 2;
+                    lx = cx + 2 * (f % (kTX / 2));
+                    ly = cy + 2 * ((f / (kTX / 2)) % (kTY / 2));
+                    lz = cz - 1 + 2 * (f / ((kTX / 2) * (kTY / 2)));
+                }
+                const int dx = ax == 0, dy = ax == 1, dz = ax == 2;
+                const bool lo = tile_v2<IN>(L, x0, y0, z0, lx - dx, ly - dy, lz - dz);
+                const bool hi = tile_v2<IN>(L, x0, y0, z0, lx + dx, ly + dy, lz + dz);
+                if (!IN) {  // K must be an active cell of the level
+                    const int gx = x0 + lx, gy = y0 + ly, gz = g.gz(z0 + lz);
+                    if (gx < 0 || gy < 0 || gz < 0 || gx >= g.nx || gy >= g.ny || gz >= g.gnz) continue;
+                    if (!lo && !hi) continue;
+                }
+                const int tst = dx + dy * kTX + dz * kTX * kTY;
+                const int ti = tile_ti(lx, ly, lz);  // may lie outside the tile: only ti -+ tst is read
+                const double a = lo ? ts[ti - tst] : 0.0, bb = hi ? ts[ti + tst] : 0.0;
+                double sn;
+                if (ax == 0) {
+                    sn = a + bb;
+                    sn = sn + 0.0;
+                    sn = sn + 0.0;
+                    sn = sn + 0.0;
+                    sn = sn + 0.0;
+                } else if (ax == 1) {
+                    sn = 0.0 + 0.0;
+                    sn = sn + a;
+                    sn = sn + bb;
+                    sn = sn + 0.0;
+                    sn = sn + 0.0;
+                } else {
+                    sn = 0.0 + 0.0;
+                    sn = sn + 0.0;
+                    sn = sn + 0.0;
+                    sn = sn + a;
+                    sn = sn + bb;
+                }
+                const int li = TB::li(lx, ly, lz);
+                Ps[li] = Ps[li] + L.eta_h2 * (6.0 * 0.0 - sn);
+            }
+            __syncthreads();
+        } else {  // reverse (left-preconditioned) pressure colour c; ts = m^T b of the tile
+            const int c = 17 - ph;
+            if (tid < kTileCells / 8) {
+                int lx, ly, lz;
+                tile_pcell(tid, c, lx, ly, lz);
+                if (tile_v2<IN>(L, x0, y0, z0, lx, ly, lz)) {
+                    const int li = TB::li(lx, ly, lz);
+                    Ps[li] = prev_core(Ls, xs, li, ts[tile_ti(lx, ly, lz)]);
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+__device__ __forceinline__ void tma_load(void* dst, const CUtensorMap* m, int c0, int c1, int c2, int c3, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, "
+        "%5}], [%6];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// FWD: phases [ph0, ph1) within 0..9; REV: within 10..19 -- on the tiles of colour T.
+// tmx: x box map; tmb: b (tile box, NB fields); tmc: m^T b (tile box, one field; REV only).
+template <bool FWD>
+__global__ void __launch_bounds__(kTileThreads, 2)
+    k_dgs_tile(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmb,
+               const __grid_constant__ CUtensorMap tmc, LevelK L, double* __restrict__ X, int T, int ph0, int ph1,
+               int ntx, int nty) {
+    using TB = TileBox<FWD>;
+    extern __shared__ __align__(128) unsigned char tsm_raw[];
+    double* xs = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(tsm_raw) + 127) & ~uintptr_t(127));
+    double* bs = xs + 4 * TB::BOX;          // b of the tile, NB fields
+    double* ts = bs + TB::NB * kTileCells;  // deltas (FWD) / m^T b (REV)
+    uint64_t* bar = reinterpret_cast<uint64_t*>(ts + kTileCells);
+    const Geom& g = L.g;
+    const int tid = threadIdx.x;
+    // tile of colour T for this CTA (z parity on global tile indices: slab parts start on a tile)
+    const int pz = ((T >> 2) ^ (g.z0 / kTZ)) & 1;
     const int hx = (ntx - (T & 1) + 1) >> 1, hy = (nty - ((T >> 1) & 1) + 1) >> 1;
     const int bi = blockIdx.x;
-    const int tx = 2 * (bi % hx) + (T & 1), ty = 2 * ((bi / hx) % hy) + ((T >> 1) & 1),
-              tz = 2 * (bi / (hx * hy)) + ((T >> 2) & 1);
+    const int tx = 2 * (bi % hx) + (T & 1), ty = 2 * ((bi / hx) % hy) + ((T >> 1) & 1), tz = 2 * (bi / (hx * hy)) + pz;
     const int x0 = tx * kTX, y0 = ty * kTY, z0 = tz * kTZ;  // z0: local plane of the part
     if (tid == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)));
@@ -1656,18 +1832,16 @@ __global__ void __launch_bounds__(kTileThreads, 2) k_dgs_tile(const __grid_const
     __syncthreads();
     pdl_wait();  // the previous kernel's writes are visible from here on
     if (tid == 0) {
-        const uint32_t bytes = 4u * kBox * sizeof(double);
+        const uint32_t bytes = (4u * TB::BOX + (TB::NB + (FWD ? 0 : 1)) * kTileCells) * sizeof(double);
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                      : "memory");
-        const int c0 = x0 - kOX + g.xo, c1 = y0 - kOY + 1, c2 = z0 - kOZ + g.zg;
-        asm volatile(
-            "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, "
-            "%5}], [%6];" ::"r"(smem_u32(xs)),
-            "l"(reinterpret_cast<uint64_t>(&tmx)), "r"(c0), "r"(c1), "r"(c2), "r"(0), "r"(smem_u32(bar))
-            : "memory");
+        tma_load(xs, &tmx, x0 - TB::OX + g.xo, y0 - TB::OY + 1, z0 - TB::OZ + g.zg, 0, bar);
+        tma_load(bs, &tmb, x0 + g.xo, y0 + 1, z0 + g.zg, 0, bar);
+        if (!FWD) tma_load(ts, &tmc, x0 + g.xo, y0 + 1, z0 + g.zg, 0, bar);
     }
-    for (int k = tid; k < kBox; k += kTileThreads) ds[k] = 0.0;
-    {
+    if (FWD)
+        for (int k = tid; k < kTileCells; k += kTileThreads) ts[k] = 0.0;
+    if (tid == 0) {
         const uint32_t ba = smem_u32(bar);
         asm volatile(
             "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n @!p bra WAIT_%=;\n}" ::"r"(
@@ -1676,128 +1850,28 @@ __global__ void __launch_bounds__(kTileThreads, 2) k_dgs_tile(const __grid_const
     }
     __syncthreads();
     LevelK Ls = L;  // the same operators on the box (strides of the shared-memory box)
-    Ls.g.sy = kBX;
-    Ls.g.sz = kBX * kBY;
-    Ls.g.fs = kBox;
-    double *Us = xs, *Vs = xs + kBox, *Ws = xs + 2 * kBox, *Ps = xs + 3 * kBox;
-    const int64_t fs = g.fs;
-    bool fwd_p = false;
-    for (int ph = ph0; ph < ph1; ++ph) {
-        if (ph <= 1 || ph >= 18) {  // velocity colour (red-black on global parity)
-            const int c = ph <= 1 ? ph : 19 - ph;
-            for (int e = tid; e < kTileCells / 2; e += kTileThreads) {
-                const int lz = e / (kTX * kTY / 2), ly = (e / (kTX / 2)) % kTY;
-                const int lx = 2 * (e % (kTX / 2)) + ((ly + lz + c + g.z0) & 1);
-                const int gx = x0 + lx, gy = y0 + ly, zl = z0 + lz;
-                const int li = tile_li(lx, ly, lz);
-                const int64_t i = g.slot(gx, gy, zl);
-                const bool here = band_cell(L, gx, gy, zl);
-                if (gx >= 1 && !here && !band_cell(L, gx - 1, gy, zl)) {
-                    const double r = B[i] - mom(Ls, Us, Ps, li, 1);
-                    Us[li] = Us[li] + r / L.dv;
-                }
-                if (gy >= 1 && !here && !band_cell(L, gx, gy - 1, zl)) {
-                    const double r = B[fs + i] - mom(Ls, Vs, Ps, li, kBX);
-                    Vs[li] = Vs[li] + r / L.dv;
-                }
-                if (g.gz(zl) >= 1 && !here && !band_cell(L, gx, gy, zl - 1)) {
-                    const double r = B[2 * fs + i] - mom(Ls, Ws, Ps, li, kBX * kBY);
-                    Ws[li] = Ws[li] + r / L.dv;
-                }
-            }
-            __syncthreads();
-        } else if (ph <= 9) {  // forward pressure colour c (eager gather form, the oracle's)
-            const int c = ph - 2;
-            fwd_p = true;
-            constexpr int ncc = kTileCells / 8;
-            if (tid < ncc) {
-                int lx, ly, lz;
-                if (ph > 2) {  // clear the previous colour's deltas
-                    tile_pcell(tid, c - 1, lx, ly, lz);
-                    ds[tile_li(lx, ly, lz)] = 0.0;
-                }
-                tile_pcell(tid, c, lx, ly, lz);
-                const int li = tile_li(lx, ly, lz);
-                if (!band_cell(L, x0 + lx, y0 + ly, z0 + lz)) {
-                    const int64_t i = g.slot(x0 + lx, y0 + ly, z0 + lz);
-                    ds[li] = (B[3 * fs + i] - cont(Ls, Us, Vs, Ws, Ps, li, L.gamma)) / L.dp;
-                }
-            }
-            __syncthreads();
-            // delta of box cell (x, y, z): nonzero only on the tile's colour-c V2 cells
-            auto dv = [&](int x, int y, int z) {
-                return (x >= 0 && y >= 0 && z >= 0 && x < kTX && y < kTY && z < kTZ) ? ds[tile_li(x, y, z)] : 0.0;
-            };
-            auto pupd = [&](int lx, int ly, int lz) {
-                double s = dv(lx - 1, ly, lz) + dv(lx + 1, ly, lz);
-                s = s + dv(lx, ly - 1, lz);
-                s = s + dv(lx, ly + 1, lz);
-                s = s + dv(lx, ly, lz - 1);
-                s = s + dv(lx, ly, lz + 1);
-                const int li = tile_li(lx, ly, lz);
-                Ps[li] = Ps[li] + L.eta_h2 * (6.0 * dv(lx, ly, lz) - s);
-            };
-            if (tid < ncc) {  // faces and self term of the colour-c cells
-                int lx, ly, lz;
-                tile_pcell(tid, c, lx, ly, lz);
-                if (!band_cell(L, x0 + lx, y0 + ly, z0 + lz)) {
-                    const int li = tile_li(lx, ly, lz);
-                    const int sy = kBX, sz = kBX * kBY;
-                    Us[li] = Us[li] + (ds[li - 1] - ds[li]) * L.inv_h;
-                    Us[li + 1] = Us[li + 1] + (ds[li] - ds[li + 1]) * L.inv_h;
-                    Vs[li] = Vs[li] + (ds[li - sy] - ds[li]) * L.inv_h;
-                    Vs[li + sy] = Vs[li + sy] + (ds[li] - ds[li + sy]) * L.inv_h;
-                    Ws[li] = Ws[li] + (ds[li - sz] - ds[li]) * L.inv_h;
-                    Ws[li + sz] = Ws[li + sz] + (ds[li] - ds[li + sz]) * L.inv_h;
-                    pupd(lx, ly, lz);
-                }
-            }
-            // neighbour pressures (colours c^1, c^2, c^4) in the tile box extended by one cell
-            constexpr int EX = kTX + 2, EY = kTY + 2, EZ = kTZ + 2;
-            for (int e = tid; e < EX * EY * EZ; e += kTileThreads) {
-                const int lx = e % EX - 1, ly = (e / EX) % EY - 1, lz = e / (EX * EY) - 1;
-                const int k = (lx & 1) + 2 * (ly & 1) + 4 * (lz & 1);
-                const int bit = k ^ c;
-                if (bit != 1 && bit != 2 && bit != 4) continue;
-                const int gx = x0 + lx, gy = y0 + ly, zl = z0 + lz;
-                if (gx < 0 || gy < 0 || g.gz(zl) < 0 || gx >= g.nx || gy >= g.ny || g.gz(zl) >= g.gnz) continue;
-                // hit: an axis neighbour (along the differing parity bit) is a V2 colour-c tile cell
-                auto owned_v2 = [&](int ax, int ay, int az) {
-                    return ax >= 0 && ay >= 0 && az >= 0 && ax < kTX && ay < kTY && az < kTZ &&
-                           !band_cell(L, x0 + ax, y0 + ay, z0 + az);
-                };
-                bool hit;
-                if (bit == 1) hit = owned_v2(lx - 1, ly, lz) || owned_v2(lx + 1, ly, lz);
-                else if (bit == 2) hit = owned_v2(lx, ly - 1, lz) || owned_v2(lx, ly + 1, lz);
-                else hit = owned_v2(lx, ly, lz - 1) || owned_v2(lx, ly, lz + 1);
-                if (hit) pupd(lx, ly, lz);
-            }
-            __syncthreads();
-        } else {  // reverse (left-preconditioned) pressure colour c
-            const int c = 17 - ph;
-            if (tid < kTileCells / 8) {
-                int lx, ly, lz;
-                tile_pcell(tid, c, lx, ly, lz);
-                if (!band_cell(L, x0 + lx, y0 + ly, z0 + lz)) {
-                    const int li = tile_li(lx, ly, lz);
-                    Ps[li] = prev_core(Ls, xs, li, L.cb[g.slot(x0 + lx, y0 + ly, z0 + lz)]);
-                }
-            }
-            __syncthreads();
-        }
-    }
+    Ls.g.sy = TB::BX;
+    Ls.g.sz = TB::BX * TB::BY;
+    Ls.g.fs = TB::BOX;
+    // interior: every cell of the tile and of the cell layer around it is a V2 cell of the level
+    const int gz0 = g.gz(z0), bw = L.bw;
+    const bool interior = x0 - 1 >= bw && y0 - 1 >= bw && gz0 - 1 >= bw && x0 + kTX + 1 <= g.nx - bw &&
+                          y0 + kTY + 1 <= g.ny - bw && gz0 + kTZ + 1 <= g.gnz - bw;
+    if (interior) tile_phases<FWD, true>(L, Ls, xs, bs, ts, x0, y0, z0, ph0, ph1);
+    else tile_phases<FWD, false>(L, Ls, xs, bs, ts, x0, y0, z0, ph0, ph1);
     // write back: the tile's own DOFs, plus (after forward pressure phases) its high faces
-    // and the pressures of the six neighbouring slabs -- never a slot outside the level
+    // and the pressures of the six neighbouring slabs -- never a wall or ghost slot
+    const int64_t fs = g.fs;
     auto put = [&](int f, int lx, int ly, int lz) {
-        const int gx = x0 + lx, gy = y0 + ly, zl = z0 + lz, gz = g.gz(zl);
-        if (gx < 0 || gy < 0 || gz < 0 || gx >= g.nx || gy >= g.ny || gz >= g.gnz) {
-            // only the high faces at n (walls) lie beyond the cells, and walls stay 0
-            return;
+        const int gx = x0 + lx, gy = y0 + ly, zl = z0 + lz;
+        if (!interior) {
+            const int gz = g.gz(zl);
+            if (gx < 0 || gy < 0 || gz < 0 || gx >= g.nx || gy >= g.ny || gz >= g.gnz) return;
+            if ((f == 0 && gx == 0) || (f == 1 && gy == 0) || (f == 2 && gz == 0)) return;  // low walls
         }
-        if ((f == 0 && gx == 0) || (f == 1 && gy == 0) || (f == 2 && gz == 0)) return;  // low walls
-        X[f * fs + g.slot(gx, gy, zl)] = xs[f * kBox + tile_li(lx, ly, lz)];
+        X[f * fs + g.slot(gx, gy, zl)] = xs[f * TB::BOX + TB::li(lx, ly, lz)];
     };
-    const int hw = fwd_p ? 1 : 0;
+    const int hw = (FWD && ph1 > 2) ? 1 : 0;  // a forward pressure phase ran
     for (int f = 0; f < 3; ++f) {  // faces: x [0, TX + hw) for u etc.
         const int wx = kTX + (f == 0 ? hw : 0), wy = kTY + (f == 1 ? hw : 0), wz = kTZ + (f == 2 ? hw : 0);
         for (int e = tid; e < wx * wy * wz; e += kTileThreads) put(f, e % wx, (e / wx) % wy, e / (wx * wy));
@@ -2241,49 +2315,74 @@ bool dgs_tiled(int nx, int ny, int nz, int64_t tile_min) {
 }
 int dgs_tile_dim(int axis) { return axis == 0 ? kTX : (axis == 1 ? kTY : kTZ); }
 
-// 4-D tensor map of a level vector (x, y, z slots of the padded boxes, 4 fields) with the
-// tile kernel's box; OOB coordinates (beyond the ghost ring) read as 0.
-static bool tile_tmap(const LevelK& L, const double* x, CUtensorMap* m) {
-    const Geom& g = L.g;
+// 4-D tensor map (x, y, z slots of the padded boxes, nf fields) of a level vector with box
+// (bx, by, bz, nf); OOB coordinates (beyond the ghost ring) read as 0.
+static bool level_tmap(const Geom& g, const double* x, int nf, int bx, int by, int bz, CUtensorMap* m) {
     TmapEncodeFn enc = tmap_encode();
     if (!enc) return false;
     const cuuint64_t dims[4] = {static_cast<cuuint64_t>(g.px), static_cast<cuuint64_t>(g.py),
-                                static_cast<cuuint64_t>(g.pz), 4};
+                                static_cast<cuuint64_t>(g.pz), static_cast<cuuint64_t>(nf)};
     const cuuint64_t strides[3] = {static_cast<cuuint64_t>(g.sy) * 8, static_cast<cuuint64_t>(g.sz) * 8,
                                    static_cast<cuuint64_t>(g.fs) * 8};
-    const cuuint32_t box[4] = {kBX, kBY, kBZ, 4};
+    const cuuint32_t box[4] = {static_cast<cuuint32_t>(bx), static_cast<cuuint32_t>(by), static_cast<cuuint32_t>(bz),
+                               static_cast<cuuint32_t>(nf)};
     const cuuint32_t es[4] = {1, 1, 1, 1};
     return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(x), dims, strides, box, es,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// Phases [ph0, ph1) on the tiles of colour T.
+// Phases [ph0, ph1) on the tiles of colour T (a range within one half: 0..9 or 10..19).
 void launch_dgs_tile_phases(const LevelK& L, double* x, const double* b, int T, int ph0, int ph1, cudaStream_t s) {
     const Geom& g = L.g;
     const int ntx = g.nx / kTX, nty = g.ny / kTY, ntz = g.nz / kTZ;
-    const int hx = (ntx - (T & 1) + 1) >> 1, hy = (nty - ((T >> 1) & 1) + 1) >> 1, hz = (ntz - ((T >> 2) & 1) + 1) >> 1;
-    if (hx * hy * hz == 0) return;
-    CUtensorMap m;
-    if (!tile_tmap(L, x, &m)) {
+    const int pz = ((T >> 2) ^ (g.z0 / kTZ)) & 1;
+    const int hx = (ntx - (T & 1) + 1) >> 1, hy = (nty - ((T >> 1) & 1) + 1) >> 1, hz = (ntz - pz + 1) >> 1;
+    if (hx * hy * hz == 0 || ph1 <= ph0) return;
+    const bool fwd = ph1 <= 10;
+    if (!fwd && ph0 < 10) {  // split at the half boundary
+        launch_dgs_tile_phases(L, x, b, T, ph0, 10, s);
+        launch_dgs_tile_phases(L, x, b, T, 10, ph1, s);
+        return;
+    }
+    CUtensorMap mx, mb, mc;
+    bool ok;
+    if (fwd) {
+        using TB = TileBox<true>;
+        ok = level_tmap(g, x, 4, TB::BX, TB::BY, TB::BZ, &mx) && level_tmap(g, b, 4, kTX, kTY, kTZ, &mb);
+        mc = mb;
+    } else {
+        using TB = TileBox<false>;
+        ok = level_tmap(g, x, 4, TB::BX, TB::BY, TB::BZ, &mx) && level_tmap(g, b, 3, kTX, kTY, kTZ, &mb) &&
+             level_tmap(g, L.cb, 1, kTX, kTY, kTZ, &mc);
+    }
+    if (!ok) {
         note(cudaErrorNotSupported);
         return;
     }
     static bool attr = false;
     if (!attr) {
-        note(cudaFuncSetAttribute(k_dgs_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kTileSmem)));
+        note(cudaFuncSetAttribute(k_dgs_tile<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(TileBox<true>::SMEM)));
+        note(cudaFuncSetAttribute(k_dgs_tile<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(TileBox<false>::SMEM)));
         attr = true;
     }
-    launch_k(k_dgs_tile, dim3(hx * hy * hz), dim3(kTileThreads), kTileSmem, s, m, L, x, b, T, ph0, ph1, ntx, nty);
+    if (fwd)
+        launch_k(k_dgs_tile<true>, dim3(hx * hy * hz), dim3(kTileThreads), TileBox<true>::SMEM, s, mx, mb, mc, L, x, T,
+                 ph0, ph1, ntx, nty);
+    else
+        launch_k(k_dgs_tile<false>, dim3(hx * hy * hz), dim3(kTileThreads), TileBox<false>::SMEM, s, mx, mb, mc, L, x,
+                 T, ph0, ph1, ntx, nty);
     count();
 }
 
 // Symmetric sweep (nph = 20) or its forward half (nph = 10): tile colours 0..7 forward, then
-// 7..0 reverse; colour 7's two halves run in one launch.
+// 7..0 reverse (16 launches; the two halves use different kernel variants).
 void launch_dgs_tiled(const LevelK& L, double* x, const double* b, int nph, cudaStream_t s) {
-    for (int T = 0; T < 8; ++T) launch_dgs_tile_phases(L, x, b, T, 0, (T == 7 && nph > 10) ? 20 : 10, s);
+    for (int T = 0; T < 8; ++T) launch_dgs_tile_phases(L, x, b, T, 0, 10, s);
     if (nph <= 10) return;
-    for (int T = 6; T >= 0; --T) launch_dgs_tile_phases(L, x, b, T, 10, 20, s);
+    for (int T = 7; T >= 0; --T) launch_dgs_tile_phases(L, x, b, T, 10, 20, s);
 }
 
 void launch_vanka_additive(const LevelK& L, double* x, const double* b, const int32_t* cells, const uint8_t* masks,

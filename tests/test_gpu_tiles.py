@@ -25,7 +25,7 @@ def same(a, b):
         pytest.fail(f"not bit-identical: max rel diff {d:.3e}")
 
 
-SHAPES = [((32, 16, 16), 2), ((64, 32, 32), 3), ((48, 40, 24), 2), ((64, 64, 64), 3)]
+SHAPES = [((32, 16, 16), 2), ((64, 32, 32), 3), ((48, 40, 24), 3), ((64, 64, 64), 4)]
 
 
 @pytest.mark.parametrize("dims,levels", SHAPES)
@@ -51,15 +51,15 @@ def test_tiled_forward_half_and_phases_bitwise():
     """Forward half alone (FLAG_SKIP_REVERSE_DGS) and every single phase of every tile colour."""
     oracle.set_threads(os.cpu_count() or 1)
     dims = (48, 40, 24)
-    o = oracle.Oracle(*dims, h=1 / 40, levels=2, tile_min=1)
+    o = oracle.Oracle(*dims, h=1 / 40, levels=3, tile_min=1)
     o.set_skip_reverse(True)
-    s = smg.Solver(*dims, h=1 / 40, levels=2, tile_min=1, flags=smg.FLAG_SKIP_REVERSE_DGS)
+    s = smg.Solver(*dims, h=1 / 40, levels=3, tile_min=1, flags=smg.FLAG_SKIP_REVERSE_DGS)
     n = o.ndof(0)
     x, b = rnd(n, 4), rnd(n, 5)
     same(s.smoother(smg.OP_DGS_SYM, x, b), o.smoother(1, x, b))
     s.close()
     o.set_skip_reverse(False)
-    s = smg.Solver(*dims, h=1 / 40, levels=2, tile_min=1)
+    s = smg.Solver(*dims, h=1 / 40, levels=3, tile_min=1)
     for T in (0, 3, 7):
         for ph in range(20):
             arg = ph + 32 * T
@@ -81,8 +81,8 @@ def test_tiled_matches_untiled_rule_and_default():
                 assert got == ((8, 16, 8, 8) if tiled else (1, 0, 0, 0)), (dims, lv, tm, got)
 
 
-@pytest.mark.parametrize("dims,levels,parts", [((64, 64, 64), 3, 2), ((64, 64, 64), 3, 4), ((32, 32, 64), 3, 4),
-                                               ((48, 40, 48), 2, 2)])
+@pytest.mark.parametrize("dims,levels,parts", [((64, 64, 64), 4, 2), ((64, 64, 64), 4, 4), ((32, 32, 64), 3, 4),
+                                               ((48, 40, 48), 4, 2)])
 def test_tiled_slabs_bitwise(dims, levels, parts):
     """z-slab parts with tiled levels: per tile colour one launch, the ghost-plane push of the
     boundary tiles' pressure / w-face updates, then the halo refresh -- bit-identical to one part."""
