@@ -1612,16 +1612,18 @@ __global__ void k_xpby_dev(double* __restrict__ q, const double* __restrict__ t,
 // in-tile order is the oracle's: bit-identical.  A level vector is read once and written
 // once per half sweep (plus the halo), instead of 13 passes of the per-step kernels.
 //
-// Two variants keep two CTAs per SM: FWD (phases 0..9; x box [-1, T+1) per axis, the
-// pressure deltas of the tile) and REV (phases 10..19; x box x [-2, TX+2), y, z [-1, T+2)
+// Two variants keep two CTAs per SM: FWD (phases 0..9; x box x [-2, TX+2), y, z [-1, T+1),
+// the pressure deltas of the tile) and REV (phases 10..19; x box x [-2, TX+2), y, z [-1, T+2)
 // for the radius-2 reads of the reverse pressure update; m^T b of the tile).
 constexpr int kTX = 16, kTY = 8, kTZ = 8;
 constexpr int kTileThreads = 256;
 constexpr int kTileCells = kTX * kTY * kTZ;
 template <bool FWD>
 struct TileBox {
-    static constexpr int OX = FWD ? 1 : 2, OY = 1, OZ = 1;
-    static constexpr int BX = FWD ? kTX + 2 : kTX + 4, BY = FWD ? kTY + 2 : kTY + 3, BZ = FWD ? kTZ + 2 : kTZ + 3;
+    // x from -2: a TMA box of 8-byte elements must start 16-byte aligned (tools/tma_probe.cu:
+    // an odd start coordinate raises "illegal instruction" on B200)
+    static constexpr int OX = 2, OY = 1, OZ = 1;
+    static constexpr int BX = kTX + 4, BY = FWD ? kTY + 2 : kTY + 3, BZ = FWD ? kTZ + 2 : kTZ + 3;
     static constexpr int BOX = BX * BY * BZ;
     static constexpr int NB = FWD ? 4 : 3;  // fields of b staged
     // x box (4 fields), b (NB fields of the tile), delta (FWD) or m^T b (REV) of the tile, mbarrier
