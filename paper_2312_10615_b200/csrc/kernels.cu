@@ -1652,6 +1652,53 @@ __device__ __forceinline__ bool tile_v2(const LevelK& L, int x0, int y0, int z0,
            !band_cell(L, x0 + lx, y0 + ly, z0 + lz);
 }
 
+// p_K plus the forward-pressure terms of colours c' in [lo, hi] among K's axis-neighbour colours
+// k ^ 1, k ^ 2, k ^ 4 (ascending, as the eager phases add them): eta/h^2 (6 * 0 - sum), the sum
+// over K's six neighbours in x-, x+, y-, y+, z-, z+ order with only the two colour-c' ones
+// nonzero; skipped when neither is a V2 cell of the tile (the oracle touches no other K).
+template <bool IN>
+__device__ __forceinline__ double tile_gathers(const LevelK& L, const double* __restrict__ ts, double p, int x0,
+                                               int y0, int z0, int lx, int ly, int lz, int k, int lo, int hi) {
+    int cs[3] = {k ^ 1, k ^ 2, k ^ 4};  // ascending
+    if (cs[0] > cs[1]) { const int t = cs[0]; cs[0] = cs[1]; cs[1] = t; }
+    if (cs[1] > cs[2]) { const int t = cs[1]; cs[1] = cs[2]; cs[2] = t; }
+    if (cs[0] > cs[1]) { const int t = cs[0]; cs[0] = cs[1]; cs[1] = t; }
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        const int cc = cs[q];
+        if (cc < lo || cc > hi) continue;
+        const int bit = cc ^ k, ax = bit == 1 ? 0 : (bit == 2 ? 1 : 2);
+        const int dx = ax == 0, dy = ax == 1, dz = ax == 2;
+        const bool m0 = tile_v2<IN>(L, x0, y0, z0, lx - dx, ly - dy, lz - dz);
+        const bool m1 = tile_v2<IN>(L, x0, y0, z0, lx + dx, ly + dy, lz + dz);
+        if (!m0 && !m1) continue;
+        const int ti = tile_ti(lx, ly, lz), tst = dx + dy * kTX + dz * kTX * kTY;
+        const double a = m0 ? ts[ti - tst] : 0.0, b = m1 ? ts[ti + tst] : 0.0;
+        double sn;
+        if (ax == 0) {
+            sn = a + b;
+            sn = sn + 0.0;
+            sn = sn + 0.0;
+            sn = sn + 0.0;
+            sn = sn + 0.0;
+        } else if (ax == 1) {
+            sn = 0.0 + 0.0;
+            sn = sn + a;
+            sn = sn + b;
+            sn = sn + 0.0;
+            sn = sn + 0.0;
+        } else {
+            sn = 0.0 + 0.0;
+            sn = sn + 0.0;
+            sn = sn + 0.0;
+            sn = sn + a;
+            sn = sn + b;
+        }
+        p = p + L.eta_h2 * (6.0 * 0.0 - sn);
+    }
+    return p;
+}
+
 template <bool FWD, bool IN>
 __device__ __forceinline__ void tile_phases(const LevelK& L, const LevelK& Ls, double* __restrict__ xs,
                                             const double* __restrict__ bs, double* __restrict__ ts, int x0, int y0,
@@ -1661,6 +1708,7 @@ __device__ __forceinline__ void tile_phases(const LevelK& L, const LevelK& Ls, d
     const int tid = threadIdx.x;
     constexpr int SY = TB::BX, SZ = TB::BX * TB::BY;
     double *Us = xs, *Vs = xs + TB::BOX, *Ws = xs + 2 * TB::BOX, *Ps = xs + 3 * TB::BOX;
+    const int cfirst = ph0 > 2 ? ph0 - 2 : 0;  // first forward pressure colour of this launch
     for (int ph = ph0; ph < ph1; ++ph) {
         if (ph <= 1 || ph >= 18) {  // velocity colour (red-black on global parity)
             const int c = ph <= 1 ? ph : 19 - ph;
@@ -1686,103 +1734,79 @@ __device__ __forceinline__ void tile_phases(const LevelK& L, const LevelK& Ls, d
                 }
             }
             __syncthreads();
-        } else if (FWD) {  // forward pressure colour c (eager gather form, the oracle's); ts = deltas
+        } else if (FWD) {  // forward pressure colour c, lazy gathers; ts = deltas of the colours so far
+            // Eager form (the oracle's): phase c adds eta/h^2 (6 delta_K - sum_nbr delta) to every
+            // pressure K, nonzero only for K of colour c (self) or c ^ bit (the axis neighbours of a
+            // colour-c cell).  p_K is read only by K's own phase before the pressure phases end, so
+            // the neighbour terms are added when K is next read -- those of earlier colours at the
+            // start of K's phase, the rest in the flush after the last colour: the same additions
+            // in the same order, hence bit-identical, with 9 barriers instead of 16.
             const int c = ph - 2;
-            constexpr int ncc = kTileCells / 8;
-            if (tid < ncc) {
+            if (tid < kTileCells / 8) {
                 int lx, ly, lz;
-                if (ph > 2) {  // clear the previous colour's deltas
-                    tile_pcell(tid, c - 1, lx, ly, lz);
-                    ts[tile_ti(lx, ly, lz)] = 0.0;
-                }
                 tile_pcell(tid, c, lx, ly, lz);
                 if (tile_v2<IN>(L, x0, y0, z0, lx, ly, lz)) {
                     const int li = TB::li(lx, ly, lz), ti = tile_ti(lx, ly, lz);
-                    ts[ti] = (bs[3 * kTileCells + ti] - cont(Ls, Us, Vs, Ws, Ps, li, L.gamma)) / L.dp;
-                }
-            }
-            __syncthreads();
-            if (tid < ncc) {  // faces and self term of the colour-c cells (their neighbours carry no delta)
-                int lx, ly, lz;
-                tile_pcell(tid, c, lx, ly, lz);
-                if (tile_v2<IN>(L, x0, y0, z0, lx, ly, lz)) {
-                    const int li = TB::li(lx, ly, lz);
-                    const double dc = ts[tile_ti(lx, ly, lz)];
+                    const double p = tile_gathers<IN>(L, ts, Ps[li], x0, y0, z0, lx, ly, lz, c, cfirst, c);
+                    const double div = (Us[li + 1] - Us[li]) + (Vs[li + SY] - Vs[li]) + (Ws[li + SZ] - Ws[li]);
+                    const double rr = bs[3 * kTileCells + ti] - (-div * L.inv_h - L.gamma * p);
+                    const double dc = rr / L.dp;
+                    ts[ti] = dc;
                     Us[li] = Us[li] + (0.0 - dc) * L.inv_h;
                     Us[li + 1] = Us[li + 1] + (dc - 0.0) * L.inv_h;
                     Vs[li] = Vs[li] + (0.0 - dc) * L.inv_h;
                     Vs[li + SY] = Vs[li + SY] + (dc - 0.0) * L.inv_h;
                     Ws[li] = Ws[li] + (0.0 - dc) * L.inv_h;
                     Ws[li + SZ] = Ws[li + SZ] + (dc - 0.0) * L.inv_h;
-                    double sn = 0.0 + 0.0;
+                    double sn = 0.0 + 0.0;  // the colour-c neighbour sum of a colour-c cell: six zeros
                     sn = sn + 0.0;
                     sn = sn + 0.0;
                     sn = sn + 0.0;
                     sn = sn + 0.0;
-                    Ps[li] = Ps[li] + L.eta_h2 * (6.0 * dc - sn);
+                    Ps[li] = p + L.eta_h2 * (6.0 * dc - sn);
                 }
-            }
-            // neighbour pressures K = C -+ e_a of the colour-c cells: 9x4x4 (a = x), 8x5x4 (y),
-            // 8x4x5 (z); each K borders colour c along one axis only, so it gets one update
-            constexpr int NKX = (kTX / 2 + 1) * (kTY / 2) * (kTZ / 2);
-            constexpr int NKY = (kTX / 2) * (kTY / 2 + 1) * (kTZ / 2);
-            constexpr int NKZ = (kTX / 2) * (kTY / 2) * (kTZ / 2 + 1);
-            const int cx = c & 1, cy = (c >> 1) & 1, cz = (c >> 2) & 1;
-            for (int e = tid; e < NKX + NKY + NKZ; e += kTileThreads) {
-                int ax, lx, ly, lz;
-                if (e < NKX) {
-                    ax = 0;
-                    lx = cx - 1 + 2 * (e % (kTX / 2 + 1));
-                    ly = cy + 2 * ((e / (kTX / 2 + 1)) % (kTY / 2));
-                    lz = cz + 2 * (e / ((kTX / 2 + 1) * (kTY / 2)));
-                } else if (e < NKX + NKY) {
-                    const int f = e - NKX;
-                    ax = 1;
-                    lx = cx + 2 * (f % (kTX / 2));
-                    ly = cy - 1 + 2 * ((f / (kTX / 2)) % (kTY / 2 + 1));
-                    lz = cz + 2 * (f / ((kTX / 2) * (kTY / 2 + 1)));
-                } else {
-                    const int f = e - NKX - NKY;
-                    ax = 2;
-                    lx = cx + 2 * (f % (kTX / 2));
-                    ly = cy + 2 * ((f / (kTX / 2)) % (kTY / 2));
-                    lz = cz - 1 + 2 * (f / ((kTX / 2) * (kTY / 2)));
-                }
-                const int dx = ax == 0, dy = ax == 1, dz = ax == 2;
-                const bool lo = tile_v2<IN>(L, x0, y0, z0, lx - dx, ly - dy, lz - dz);
-                const bool hi = tile_v2<IN>(L, x0, y0, z0, lx + dx, ly + dy, lz + dz);
-                if (!IN) {  // K must be an active cell of the level
-                    const int gx = x0 + lx, gy = y0 + ly, gz = g.gz(z0 + lz);
-                    if (gx < 0 || gy < 0 || gz < 0 || gx >= g.nx || gy >= g.ny || gz >= g.gnz) continue;
-                    if (!lo && !hi) continue;
-                }
-                const int tst = dx + dy * kTX + dz * kTX * kTY;
-                const int ti = tile_ti(lx, ly, lz);  // may lie outside the tile: only ti -+ tst is read
-                const double a = lo ? ts[ti - tst] : 0.0, bb = hi ? ts[ti + tst] : 0.0;
-                double sn;
-                if (ax == 0) {
-                    sn = a + bb;
-                    sn = sn + 0.0;
-                    sn = sn + 0.0;
-                    sn = sn + 0.0;
-                    sn = sn + 0.0;
-                } else if (ax == 1) {
-                    sn = 0.0 + 0.0;
-                    sn = sn + a;
-                    sn = sn + bb;
-                    sn = sn + 0.0;
-                    sn = sn + 0.0;
-                } else {
-                    sn = 0.0 + 0.0;
-                    sn = sn + 0.0;
-                    sn = sn + 0.0;
-                    sn = sn + a;
-                    sn = sn + bb;
-                }
-                const int li = TB::li(lx, ly, lz);
-                Ps[li] = Ps[li] + L.eta_h2 * (6.0 * 0.0 - sn);
             }
             __syncthreads();
+            if (ph == 9 || ph + 1 == ph1) {  // flush: the terms of colours [cfirst, c] still pending
+                constexpr int EX = kTX + 2, EY = kTY + 2;
+                constexpr int NTILE = kTileCells, NSX = 2 * kTY * kTZ, NSY = 2 * kTX * kTZ, NSZ = 2 * kTX * kTY;
+                for (int e = tid; e < NTILE + NSX + NSY + NSZ; e += kTileThreads) {
+                    int lx, ly, lz;
+                    if (e < NTILE) {
+                        lx = e % kTX;
+                        ly = (e / kTX) % kTY;
+                        lz = e / (kTX * kTY);
+                    } else if (e < NTILE + NSX) {
+                        const int f = e - NTILE;
+                        lx = (f & 1) ? kTX : -1;
+                        ly = (f >> 1) % kTY;
+                        lz = (f >> 1) / kTY;
+                    } else if (e < NTILE + NSX + NSY) {
+                        const int f = e - NTILE - NSX;
+                        lx = f % kTX;
+                        ly = ((f / kTX) & 1) ? kTY : -1;
+                        lz = f / (2 * kTX);
+                    } else {
+                        const int f = e - NTILE - NSX - NSY;
+                        lx = f % kTX;
+                        ly = (f / kTX) % kTY;
+                        lz = (f / (kTX * kTY)) ? kTZ : -1;
+                    }
+                    if (!IN) {  // K must be an active cell of the level
+                        const int gx = x0 + lx, gy = y0 + ly, gz = g.gz(z0 + lz);
+                        if (gx < 0 || gy < 0 || gz < 0 || gx >= g.nx || gy >= g.ny || gz >= g.gnz) continue;
+                    }
+                    const int k = (lx & 1) + 2 * (ly & 1) + 4 * (lz & 1);
+                    // colours whose terms K already took: below k, if K relaxed in this launch
+                    const bool relaxed = k >= cfirst && k <= c && tile_v2<IN>(L, x0, y0, z0, lx, ly, lz);
+                    const int lo = relaxed ? k + 1 : cfirst;
+                    const int li = TB::li(lx, ly, lz);
+                    Ps[li] = tile_gathers<IN>(L, ts, Ps[li], x0, y0, z0, lx, ly, lz, k, lo, c);
+                }
+                __syncthreads();
+                (void)EX;
+                (void)EY;
+            }
         } else {  // reverse (left-preconditioned) pressure colour c; ts = m^T b of the tile
             const int c = 17 - ph;
             if (tid < kTileCells / 8) {
@@ -1861,37 +1885,39 @@ __global__ void __launch_bounds__(kTileThreads, 2)
                           y0 + kTY + 1 <= g.ny - bw && gz0 + kTZ + 1 <= g.gnz - bw;
     if (interior) tile_phases<FWD, true>(L, Ls, xs, bs, ts, x0, y0, z0, ph0, ph1);
     else tile_phases<FWD, false>(L, Ls, xs, bs, ts, x0, y0, z0, ph0, ph1);
-    // write back: the tile's own DOFs, plus (after forward pressure phases) its high faces
-    // and the pressures of the six neighbouring slabs -- never a wall or ghost slot
+    // Write back the DOFs the phases may have changed: the tile's own, plus (after forward
+    // pressure phases) its high faces and the pressures of the six neighbouring slabs.  Rows of
+    // 16 go out as 16-byte stores.  Every slot written was loaded by this CTA and no other CTA
+    // touches it during the launch; wall and ghost slots were loaded as 0 and never changed.
     const int64_t fs = g.fs;
-    auto put = [&](int f, int lx, int ly, int lz) {
-        const int gx = x0 + lx, gy = y0 + ly, zl = z0 + lz;
-        if (!interior) {
-            const int gz = g.gz(zl);
-            if (gx < 0 || gy < 0 || gz < 0 || gx >= g.nx || gy >= g.ny || gz >= g.gnz) return;
-            if ((f == 0 && gx == 0) || (f == 1 && gy == 0) || (f == 2 && gz == 0)) return;  // low walls
-        }
-        X[f * fs + g.slot(gx, gy, zl)] = xs[f * TB::BOX + TB::li(lx, ly, lz)];
-    };
     const int hw = (FWD && ph1 > 2) ? 1 : 0;  // a forward pressure phase ran
-    for (int f = 0; f < 3; ++f) {  // faces: x [0, TX + hw) for u etc.
-        const int wx = kTX + (f == 0 ? hw : 0), wy = kTY + (f == 1 ? hw : 0), wz = kTZ + (f == 2 ? hw : 0);
-        for (int e = tid; e < wx * wy * wz; e += kTileThreads) put(f, e % wx, (e / wx) % wy, e / (wx * wy));
-    }
-    {  // pressures: rows x [-hw, TX + hw) of the tile, then the y and z neighbour slabs
-        const int wx = kTX + 2 * hw;
-        for (int e = tid; e < wx * kTY * kTZ; e += kTileThreads)
-            put(3, e % wx - hw, (e / wx) % kTY, e / (wx * kTY));
-        if (hw) {
-            for (int e = tid; e < 2 * kTX * kTZ; e += kTileThreads) {
-                const int lx = e % kTX, side = (e / kTX) & 1, lz = e / (2 * kTX);
-                put(3, lx, side ? kTY : -1, lz);
-            }
-            for (int e = tid; e < 2 * kTX * kTY; e += kTileThreads) {
-                const int lx = e % kTX, ly = (e / kTX) % kTY, side = e / (kTX * kTY);
-                put(3, lx, ly, side ? kTZ : -1);
-            }
+    auto rows = [&](int f, int ylo, int nyr, int zlo, int nzr) {
+        const int n = nyr * nzr * (kTX / 2);
+        for (int e = tid; e < n; e += kTileThreads) {
+            const int q = e % (kTX / 2), r = e / (kTX / 2);
+            const int ly = ylo + r % nyr, lz = zlo + r / nyr;
+            const double2 v = *reinterpret_cast<const double2*>(&xs[f * TB::BOX + TB::li(2 * q, ly, lz)]);
+            *reinterpret_cast<double2*>(&X[f * fs + g.slot(x0 + 2 * q, y0 + ly, z0 + lz)]) = v;
         }
+    };
+    auto col = [&](int f, int lx) {  // one x column of the tile's rows
+        for (int e = tid; e < kTY * kTZ; e += kTileThreads) {
+            const int ly = e % kTY, lz = e / kTY;
+            X[f * fs + g.slot(x0 + lx, y0 + ly, z0 + lz)] = xs[f * TB::BOX + TB::li(lx, ly, lz)];
+        }
+    };
+    rows(0, 0, kTY, 0, kTZ);
+    rows(1, 0, kTY + hw, 0, kTZ);
+    rows(2, 0, kTY, 0, kTZ + hw);
+    rows(3, 0, kTY, 0, kTZ);
+    if (hw) {
+        col(0, kTX);
+        col(3, -1);
+        col(3, kTX);
+        rows(3, -1, 1, 0, kTZ);
+        rows(3, kTY, 1, 0, kTZ);
+        rows(3, 0, kTY, -1, 1);
+        rows(3, 0, kTY, kTZ, 1);
     }
 }
 
