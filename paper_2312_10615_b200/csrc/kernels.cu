@@ -1626,11 +1626,75 @@ struct TileBox {
     static constexpr int BX = kTX + 4, BY = FWD ? kTY + 2 : kTY + 3, BZ = FWD ? kTZ + 2 : kTZ + 3;
     static constexpr int BOX = BX * BY * BZ;
     static constexpr int NB = FWD ? 4 : 3;  // fields of b staged
-    // x box (4 fields), b (NB fields of the tile), delta (FWD) or m^T b (REV) of the tile, mbarrier
-    static constexpr size_t SMEM = (4 * BOX + (NB + 1) * kTileCells) * sizeof(double) + 128 + 16;
+    // FWD: pressure deltas on the tile plus a ring of zeros (the neighbours outside the tile carry
+    // no delta, so gathers need no bounds tests); REV: m^T b of the tile
+    static constexpr int TS = FWD ? (kTX + 2) * (kTY + 2) * (kTZ + 2) : kTileCells;
+    // x box (4 fields), b (NB fields of the tile), ts, mbarrier
+    static constexpr size_t SMEM = (4 * BOX + NB * kTileCells + TS) * sizeof(double) + 128 + 16;
     static __device__ __forceinline__ int li(int x, int y, int z) { return ((z + OZ) * BY + (y + OY)) * BX + (x + OX); }
 };
 __device__ __forceinline__ int tile_ti(int x, int y, int z) { return (z * kTY + y) * kTX + x; }
+// delta box (FWD): the tile plus a one-cell ring
+constexpr int kDX = kTX + 2, kDXY = (kTX + 2) * (kTY + 2);
+__device__ __forceinline__ int tile_td(int x, int y, int z) { return ((z + 1) * (kTY + 2) + (y + 1)) * kDX + (x + 1); }
+
+// eta/h^2 (6 * 0 - s): the forward-pressure term of colour k ^ (1 << AX) on a cell K of colour k,
+// s the six-neighbour delta sum in x-, x+, y-, y+, z-, z+ order whose nonzero entries are the two
+// neighbours along AX (t: K's index in the delta box)
+template <int AX>
+__device__ __forceinline__ double gsum(const double* __restrict__ ts, int t) {
+    constexpr int ST = AX == 0 ? 1 : (AX == 1 ? kDX : kDXY);
+    const double a = ts[t - ST], b = ts[t + ST];
+    double sn;
+    if (AX == 0) {
+        sn = a + b;
+        sn = sn + 0.0;
+        sn = sn + 0.0;
+        sn = sn + 0.0;
+        sn = sn + 0.0;
+    } else if (AX == 1) {
+        sn = 0.0 + 0.0;
+        sn = sn + a;
+        sn = sn + b;
+        sn = sn + 0.0;
+        sn = sn + 0.0;
+    } else {
+        sn = 0.0 + 0.0;
+        sn = sn + 0.0;
+        sn = sn + 0.0;
+        sn = sn + a;
+        sn = sn + b;
+    }
+    return sn;
+}
+// The pending terms of a cell of colour K over a full forward half: the colours below K (LOWER,
+// added before K's own update) or above K (the flush), ascending.  Cells whose neighbours carry
+// no delta get + 0 (the oracle skips them; the value is the same).
+template <int K, bool LOWER>
+__device__ __forceinline__ double gath(double p, const double* __restrict__ ts, int t, double e2) {
+#pragma unroll
+    for (int cc = 0; cc < 8; ++cc) {
+        const int bit = cc ^ K;
+        if (bit != 1 && bit != 2 && bit != 4) continue;
+        if (LOWER ? cc > K : cc < K) continue;
+        const double sn = bit == 1 ? gsum<0>(ts, t) : (bit == 2 ? gsum<1>(ts, t) : gsum<2>(ts, t));
+        p = p + e2 * (6.0 * 0.0 - sn);
+    }
+    return p;
+}
+template <bool LOWER>
+__device__ __forceinline__ double gath_k(int k, double p, const double* __restrict__ ts, int t, double e2) {
+    switch (k) {
+        case 0: return gath<0, LOWER>(p, ts, t, e2);
+        case 1: return gath<1, LOWER>(p, ts, t, e2);
+        case 2: return gath<2, LOWER>(p, ts, t, e2);
+        case 3: return gath<3, LOWER>(p, ts, t, e2);
+        case 4: return gath<4, LOWER>(p, ts, t, e2);
+        case 5: return gath<5, LOWER>(p, ts, t, e2);
+        case 6: return gath<6, LOWER>(p, ts, t, e2);
+        default: return gath<7, LOWER>(p, ts, t, e2);
+    }
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -1672,7 +1736,7 @@ __device__ __forceinline__ double tile_gathers(const LevelK& L, const double* __
         const bool m0 = tile_v2<IN>(L, x0, y0, z0, lx - dx, ly - dy, lz - dz);
         const bool m1 = tile_v2<IN>(L, x0, y0, z0, lx + dx, ly + dy, lz + dz);
         if (!m0 && !m1) continue;
-        const int ti = tile_ti(lx, ly, lz), tst = dx + dy * kTX + dz * kTX * kTY;
+        const int ti = tile_td(lx, ly, lz), tst = dx + dy * kDX + dz * kDXY;
         const double a = m0 ? ts[ti - tst] : 0.0, b = m1 ? ts[ti + tst] : 0.0;
         double sn;
         if (ax == 0) {
@@ -1709,6 +1773,7 @@ __device__ __forceinline__ void tile_phases(const LevelK& L, const LevelK& Ls, d
     constexpr int SY = TB::BX, SZ = TB::BX * TB::BY;
     double *Us = xs, *Vs = xs + TB::BOX, *Ws = xs + 2 * TB::BOX, *Ps = xs + 3 * TB::BOX;
     const int cfirst = ph0 > 2 ? ph0 - 2 : 0;  // first forward pressure colour of this launch
+    const bool full = ph0 <= 2 && ph1 >= 10;    // all eight colours run in this launch
     for (int ph = ph0; ph < ph1; ++ph) {
         if (ph <= 1 || ph >= 18) {  // velocity colour (red-black on global parity)
             const int c = ph <= 1 ? ph : 19 - ph;
@@ -1746,12 +1811,13 @@ __device__ __forceinline__ void tile_phases(const LevelK& L, const LevelK& Ls, d
                 int lx, ly, lz;
                 tile_pcell(tid, c, lx, ly, lz);
                 if (tile_v2<IN>(L, x0, y0, z0, lx, ly, lz)) {
-                    const int li = TB::li(lx, ly, lz), ti = tile_ti(lx, ly, lz);
-                    const double p = tile_gathers<IN>(L, ts, Ps[li], x0, y0, z0, lx, ly, lz, c, cfirst, c);
+                    const int li = TB::li(lx, ly, lz), ti = tile_ti(lx, ly, lz), td = tile_td(lx, ly, lz);
+                    const double p = full ? gath_k<true>(c, Ps[li], ts, td, L.eta_h2)
+                                          : tile_gathers<IN>(L, ts, Ps[li], x0, y0, z0, lx, ly, lz, c, cfirst, c);
                     const double div = (Us[li + 1] - Us[li]) + (Vs[li + SY] - Vs[li]) + (Ws[li + SZ] - Ws[li]);
                     const double rr = bs[3 * kTileCells + ti] - (-div * L.inv_h - L.gamma * p);
                     const double dc = rr / L.dp;
-                    ts[ti] = dc;
+                    ts[td] = dc;
                     Us[li] = Us[li] + (0.0 - dc) * L.inv_h;
                     Us[li + 1] = Us[li + 1] + (dc - 0.0) * L.inv_h;
                     Vs[li] = Vs[li] + (0.0 - dc) * L.inv_h;
@@ -1768,44 +1834,54 @@ __device__ __forceinline__ void tile_phases(const LevelK& L, const LevelK& Ls, d
             }
             __syncthreads();
             if (ph == 9 || ph + 1 == ph1) {  // flush: the terms of colours [cfirst, c] still pending
-                constexpr int EX = kTX + 2, EY = kTY + 2;
-                constexpr int NTILE = kTileCells, NSX = 2 * kTY * kTZ, NSY = 2 * kTX * kTZ, NSZ = 2 * kTX * kTY;
-                for (int e = tid; e < NTILE + NSX + NSY + NSZ; e += kTileThreads) {
-                    int lx, ly, lz;
-                    if (e < NTILE) {
-                        lx = e % kTX;
-                        ly = (e / kTX) % kTY;
-                        lz = e / (kTX * kTY);
-                    } else if (e < NTILE + NSX) {
-                        const int f = e - NTILE;
-                        lx = (f & 1) ? kTX : -1;
-                        ly = (f >> 1) % kTY;
-                        lz = (f >> 1) / kTY;
-                    } else if (e < NTILE + NSX + NSY) {
-                        const int f = e - NTILE - NSX;
-                        lx = f % kTX;
-                        ly = ((f / kTX) & 1) ? kTY : -1;
-                        lz = f / (2 * kTX);
-                    } else {
-                        const int f = e - NTILE - NSX - NSY;
-                        lx = f % kTX;
-                        ly = (f / kTX) % kTY;
-                        lz = (f / (kTX * kTY)) ? kTZ : -1;
-                    }
+                // every cell of the tile and of the six face slabs around it (ring edges and corners
+                // have no tile neighbour)
+                for (int e = tid; e < TB::TS; e += kTileThreads) {
+                    const int lx = e % kDX - 1, ly = (e / kDX) % (kTY + 2) - 1, lz = e / kDXY - 1;
+                    const bool ox = lx < 0 || lx >= kTX, oy = ly < 0 || ly >= kTY, oz = lz < 0 || lz >= kTZ;
+                    if (ox + oy + oz >= 2) continue;
                     if (!IN) {  // K must be an active cell of the level
                         const int gx = x0 + lx, gy = y0 + ly, gz = g.gz(z0 + lz);
                         if (gx < 0 || gy < 0 || gz < 0 || gx >= g.nx || gy >= g.ny || gz >= g.gnz) continue;
                     }
                     const int k = (lx & 1) + 2 * (ly & 1) + 4 * (lz & 1);
-                    // colours whose terms K already took: below k, if K relaxed in this launch
-                    const bool relaxed = k >= cfirst && k <= c && tile_v2<IN>(L, x0, y0, z0, lx, ly, lz);
-                    const int lo = relaxed ? k + 1 : cfirst;
                     const int li = TB::li(lx, ly, lz);
-                    Ps[li] = tile_gathers<IN>(L, ts, Ps[li], x0, y0, z0, lx, ly, lz, k, lo, c);
+                    if (full && IN) {
+                        if (!(ox || oy || oz)) {  // relaxed tile cell: the colours above k
+                            Ps[li] = gath_k<false>(k, Ps[li], ts, e, L.eta_h2);
+                        } else {  // face-slab cell: the one term of its inward neighbour's colour
+                            const double d = ts[e + (ox ? (lx < 0 ? 1 : -1) : oy ? (ly < 0 ? kDX : -kDX)
+                                                                              : (lz < 0 ? kDXY : -kDXY))];
+                            const bool low = ox ? lx < 0 : oy ? ly < 0 : lz < 0;
+                            const double a = low ? 0.0 : d, bb = low ? d : 0.0;  // the (-, +) pair
+                            double sn;
+                            if (ox) {
+                                sn = a + bb;
+                                sn = sn + 0.0;
+                                sn = sn + 0.0;
+                                sn = sn + 0.0;
+                                sn = sn + 0.0;
+                            } else if (oy) {
+                                sn = 0.0 + 0.0;
+                                sn = sn + a;
+                                sn = sn + bb;
+                                sn = sn + 0.0;
+                                sn = sn + 0.0;
+                            } else {
+                                sn = 0.0 + 0.0;
+                                sn = sn + 0.0;
+                                sn = sn + 0.0;
+                                sn = sn + a;
+                                sn = sn + bb;
+                            }
+                            Ps[li] = Ps[li] + L.eta_h2 * (6.0 * 0.0 - sn);
+                        }
+                    } else {  // boundary tiles and partial ranges (single-phase entry points)
+                        const bool relaxed = k >= cfirst && k <= c && tile_v2<IN>(L, x0, y0, z0, lx, ly, lz);
+                        Ps[li] = tile_gathers<IN>(L, ts, Ps[li], x0, y0, z0, lx, ly, lz, k, relaxed ? k + 1 : cfirst, c);
+                    }
                 }
                 __syncthreads();
-                (void)EX;
-                (void)EY;
             }
         } else {  // reverse (left-preconditioned) pressure colour c; ts = m^T b of the tile
             const int c = 17 - ph;
@@ -1842,7 +1918,7 @@ __global__ void __launch_bounds__(kTileThreads, 2)
     double* xs = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(tsm_raw) + 127) & ~uintptr_t(127));
     double* bs = xs + 4 * TB::BOX;          // b of the tile, NB fields
     double* ts = bs + TB::NB * kTileCells;  // deltas (FWD) / m^T b (REV)
-    uint64_t* bar = reinterpret_cast<uint64_t*>(ts + kTileCells);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(ts + TB::TS);
     const Geom& g = L.g;
     const int tid = threadIdx.x;
     // tile of colour T for this CTA (z parity on global tile indices: slab parts start on a tile)
@@ -1866,12 +1942,12 @@ __global__ void __launch_bounds__(kTileThreads, 2)
         if (!FWD) tma_load(ts, &tmc, x0 + g.xo, y0 + 1, z0 + g.zg, 0, bar);
     }
     if (FWD)
-        for (int k = tid; k < kTileCells; k += kTileThreads) ts[k] = 0.0;
-    if (tid == 0) {
+        for (int k = tid; k < TB::TS; k += kTileThreads) ts[k] = 0.0;
+    if (tid == 0) {  // one waiter (with a suspend hint), the others wait at the barrier
         const uint32_t ba = smem_u32(bar);
         asm volatile(
-            "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n @!p bra WAIT_%=;\n}" ::"r"(
-                ba)
+            "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0, 1000000;\n @!p bra "
+            "WAIT_%=;\n}" ::"r"(ba)
             : "memory");
     }
     __syncthreads();
