@@ -1700,13 +1700,6 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-// cell e (0 .. kTileCells/8 - 1) of parity colour c inside a tile (tile origins are even)
-__device__ __forceinline__ void tile_pcell(int e, int c, int& x, int& y, int& z) {
-    x = 2 * (e % (kTX / 2)) + (c & 1);
-    y = 2 * ((e / (kTX / 2)) % (kTY / 2)) + ((c >> 1) & 1);
-    z = 2 * (e / (kTX * kTY / 4)) + ((c >> 2) & 1);
-}
-
 // The phases of one tile.  IN: an interior tile (no band cell in the tile or one cell around
 // it, every cell of the extended box active): no band or bounds tests at all.
 template <bool IN>
@@ -1763,39 +1756,81 @@ __device__ __forceinline__ double tile_gathers(const LevelK& L, const double* __
     return p;
 }
 
+// Box operators: mom / cont / prev_core of the contract (same operand order) on
+// the shared-memory box, 32-bit indices and compile-time strides.
+template <int SY, int SZ>
+struct BoxOps {
+    static __device__ __forceinline__ double mom(const double* __restrict__ F, const double* __restrict__ P, int i,
+                                                 int sn, double e2, double ih) {
+        double s = F[i - 1] + F[i + 1];
+        s = s + F[i - SY];
+        s = s + F[i + SY];
+        s = s + F[i - SZ];
+        s = s + F[i + SZ];
+        const double lap = 6.0 * F[i] - s;
+        return e2 * lap + (P[i] - P[i - sn]) * ih;
+    }
+    static __device__ __forceinline__ double cont(const double* __restrict__ U, const double* __restrict__ V,
+                                                  const double* __restrict__ W, const double* __restrict__ P, int i,
+                                                  double gamma, double ih) {
+        const double div = (U[i + 1] - U[i]) + (V[i + SY] - V[i]) + (W[i + SZ] - W[i]);
+        return -div * ih - gamma * P[i];
+    }
+};
+
 template <bool FWD, bool IN>
-__device__ __forceinline__ void tile_phases(const LevelK& L, const LevelK& Ls, double* __restrict__ xs,
-                                            const double* __restrict__ bs, double* __restrict__ ts, int x0, int y0,
-                                            int z0, int ph0, int ph1) {
+__device__ __forceinline__ void tile_phases(const LevelK& L, double* __restrict__ xs, const double* __restrict__ bs,
+                                            double* __restrict__ ts, int x0, int y0, int z0, int ph0, int ph1) {
     using TB = TileBox<FWD>;
+    constexpr int SY = TB::BX, SZ = TB::BX * TB::BY, BOX = TB::BOX;
+    using Ops = BoxOps<SY, SZ>;
     const Geom& g = L.g;
     const int tid = threadIdx.x;
-    constexpr int SY = TB::BX, SZ = TB::BX * TB::BY;
-    double *Us = xs, *Vs = xs + TB::BOX, *Ws = xs + 2 * TB::BOX, *Ps = xs + 3 * TB::BOX;
+    const double e2 = L.eta_h2, ih = L.inv_h, dv = L.dv, dp = L.dp, gam = L.gamma;
+    double *Us = xs, *Vs = xs + BOX, *Ws = xs + 2 * BOX, *Ps = xs + 3 * BOX;
     const int cfirst = ph0 > 2 ? ph0 - 2 : 0;  // first forward pressure colour of this launch
     const bool full = ph0 <= 2 && ph1 >= 10;    // all eight colours run in this launch
+    // velocity phases: this thread's cells e = tid + k * threads, x pair 2 (e % 8) (+1 by parity)
+    int vli[kTileCells / 2 / kTileThreads], vti[kTileCells / 2 / kTileThreads], vpar[kTileCells / 2 / kTileThreads];
+#pragma unroll
+    for (int k = 0; k < kTileCells / 2 / kTileThreads; ++k) {
+        const int e = tid + k * kTileThreads;
+        const int lz = e / (kTX * kTY / 2), ly = (e / (kTX / 2)) % kTY, lx0 = 2 * (e % (kTX / 2));
+        vli[k] = TB::li(lx0, ly, lz);
+        vti[k] = tile_ti(lx0, ly, lz);
+        vpar[k] = (ly + lz + g.gz(z0)) & 1;  // global parity of (lx0, ly, lz) (x0 even)
+    }
+    // pressure phases: this thread's cell of colour c = base + offset(c) (tid < kTileCells / 8)
+    const int px0 = 2 * (tid % (kTX / 2)), py0 = 2 * ((tid / (kTX / 2)) % (kTY / 2)), pz0 = 2 * (tid / (kTX * kTY / 4));
+    const int pli = TB::li(px0, py0, pz0), pti = tile_ti(px0, py0, pz0), ptd = tile_td(px0, py0, pz0);
     for (int ph = ph0; ph < ph1; ++ph) {
         if (ph <= 1 || ph >= 18) {  // velocity colour (red-black on global parity)
             const int c = ph <= 1 ? ph : 19 - ph;
 #pragma unroll
             for (int k = 0; k < kTileCells / 2 / kTileThreads; ++k) {
-                const int e = tid + k * kTileThreads;
-                const int lz = e / (kTX * kTY / 2), ly = (e / (kTX / 2)) % kTY;
-                const int lx = 2 * (e % (kTX / 2)) + ((ly + lz + c + g.z0) & 1);
-                const int li = TB::li(lx, ly, lz), ti = tile_ti(lx, ly, lz);
-                const int gx = x0 + lx, gy = y0 + ly, zl = z0 + lz;
-                const bool here = !IN && band_cell(L, gx, gy, zl);
-                if (IN || (gx >= 1 && !here && !band_cell(L, gx - 1, gy, zl))) {
-                    const double r = bs[ti] - mom(Ls, Us, Ps, li, 1);
-                    Us[li] = Us[li] + r / L.dv;
+                const int ox = vpar[k] ^ c;  // x offset of the colour-c cell of the pair
+                const int li = vli[k] + ox, ti = vti[k] + ox;
+                bool du = true, dv_ = true, dw = true;
+                if (!IN) {
+                    const int e = tid + k * kTileThreads;
+                    const int gx = x0 + 2 * (e % (kTX / 2)) + ox, gy = y0 + (e / (kTX / 2)) % kTY,
+                              zl = z0 + e / (kTX * kTY / 2);
+                    const bool here = band_cell(L, gx, gy, zl);
+                    du = gx >= 1 && !here && !band_cell(L, gx - 1, gy, zl);
+                    dv_ = gy >= 1 && !here && !band_cell(L, gx, gy - 1, zl);
+                    dw = g.gz(zl) >= 1 && !here && !band_cell(L, gx, gy, zl - 1);
                 }
-                if (IN || (gy >= 1 && !here && !band_cell(L, gx, gy - 1, zl))) {
-                    const double r = bs[kTileCells + ti] - mom(Ls, Vs, Ps, li, SY);
-                    Vs[li] = Vs[li] + r / L.dv;
+                if (du) {
+                    const double r = bs[ti] - Ops::mom(Us, Ps, li, 1, e2, ih);
+                    Us[li] = Us[li] + r / dv;
                 }
-                if (IN || (g.gz(zl) >= 1 && !here && !band_cell(L, gx, gy, zl - 1))) {
-                    const double r = bs[2 * kTileCells + ti] - mom(Ls, Ws, Ps, li, SZ);
-                    Ws[li] = Ws[li] + r / L.dv;
+                if (dv_) {
+                    const double r = bs[kTileCells + ti] - Ops::mom(Vs, Ps, li, SY, e2, ih);
+                    Vs[li] = Vs[li] + r / dv;
+                }
+                if (dw) {
+                    const double r = bs[2 * kTileCells + ti] - Ops::mom(Ws, Ps, li, SZ, e2, ih);
+                    Ws[li] = Ws[li] + r / dv;
                 }
             }
             __syncthreads();
@@ -1808,28 +1843,31 @@ __device__ __forceinline__ void tile_phases(const LevelK& L, const LevelK& Ls, d
             // in the same order, hence bit-identical, with 9 barriers instead of 16.
             const int c = ph - 2;
             if (tid < kTileCells / 8) {
-                int lx, ly, lz;
-                tile_pcell(tid, c, lx, ly, lz);
-                if (tile_v2<IN>(L, x0, y0, z0, lx, ly, lz)) {
-                    const int li = TB::li(lx, ly, lz), ti = tile_ti(lx, ly, lz), td = tile_td(lx, ly, lz);
-                    const double p = full ? gath_k<true>(c, Ps[li], ts, td, L.eta_h2)
-                                          : tile_gathers<IN>(L, ts, Ps[li], x0, y0, z0, lx, ly, lz, c, cfirst, c);
+                const int cx = c & 1, cy = (c >> 1) & 1, cz = c >> 2;
+                const bool v2 = IN || tile_v2<false>(L, x0, y0, z0, px0 + cx, py0 + cy, pz0 + cz);
+                if (v2) {
+                    const int li = pli + cx + cy * SY + cz * SZ;
+                    const int ti = pti + cx + cy * kTX + cz * kTX * kTY;
+                    const int td = ptd + cx + cy * kDX + cz * kDXY;
+                    const double p =
+                        full ? gath_k<true>(c, Ps[li], ts, td, e2)
+                             : tile_gathers<IN>(L, ts, Ps[li], x0, y0, z0, px0 + cx, py0 + cy, pz0 + cz, c, cfirst, c);
                     const double div = (Us[li + 1] - Us[li]) + (Vs[li + SY] - Vs[li]) + (Ws[li + SZ] - Ws[li]);
-                    const double rr = bs[3 * kTileCells + ti] - (-div * L.inv_h - L.gamma * p);
-                    const double dc = rr / L.dp;
+                    const double rr = bs[3 * kTileCells + ti] - (-div * ih - gam * p);
+                    const double dc = rr / dp;
                     ts[td] = dc;
-                    Us[li] = Us[li] + (0.0 - dc) * L.inv_h;
-                    Us[li + 1] = Us[li + 1] + (dc - 0.0) * L.inv_h;
-                    Vs[li] = Vs[li] + (0.0 - dc) * L.inv_h;
-                    Vs[li + SY] = Vs[li + SY] + (dc - 0.0) * L.inv_h;
-                    Ws[li] = Ws[li] + (0.0 - dc) * L.inv_h;
-                    Ws[li + SZ] = Ws[li + SZ] + (dc - 0.0) * L.inv_h;
+                    Us[li] = Us[li] + (0.0 - dc) * ih;
+                    Us[li + 1] = Us[li + 1] + (dc - 0.0) * ih;
+                    Vs[li] = Vs[li] + (0.0 - dc) * ih;
+                    Vs[li + SY] = Vs[li + SY] + (dc - 0.0) * ih;
+                    Ws[li] = Ws[li] + (0.0 - dc) * ih;
+                    Ws[li + SZ] = Ws[li + SZ] + (dc - 0.0) * ih;
                     double sn = 0.0 + 0.0;  // the colour-c neighbour sum of a colour-c cell: six zeros
                     sn = sn + 0.0;
                     sn = sn + 0.0;
                     sn = sn + 0.0;
                     sn = sn + 0.0;
-                    Ps[li] = p + L.eta_h2 * (6.0 * dc - sn);
+                    Ps[li] = p + e2 * (6.0 * dc - sn);
                 }
             }
             __syncthreads();
@@ -1848,7 +1886,7 @@ __device__ __forceinline__ void tile_phases(const LevelK& L, const LevelK& Ls, d
                     const int li = TB::li(lx, ly, lz);
                     if (full && IN) {
                         if (!(ox || oy || oz)) {  // relaxed tile cell: the colours above k
-                            Ps[li] = gath_k<false>(k, Ps[li], ts, e, L.eta_h2);
+                            Ps[li] = gath_k<false>(k, Ps[li], ts, e, e2);
                         } else {  // face-slab cell: the one term of its inward neighbour's colour
                             const double d = ts[e + (ox ? (lx < 0 ? 1 : -1) : oy ? (ly < 0 ? kDX : -kDX)
                                                                               : (lz < 0 ? kDXY : -kDXY))];
@@ -1874,7 +1912,7 @@ __device__ __forceinline__ void tile_phases(const LevelK& L, const LevelK& Ls, d
                                 sn = sn + a;
                                 sn = sn + bb;
                             }
-                            Ps[li] = Ps[li] + L.eta_h2 * (6.0 * 0.0 - sn);
+                            Ps[li] = Ps[li] + e2 * (6.0 * 0.0 - sn);
                         }
                     } else {  // boundary tiles and partial ranges (single-phase entry points)
                         const bool relaxed = k >= cfirst && k <= c && tile_v2<IN>(L, x0, y0, z0, lx, ly, lz);
@@ -1884,14 +1922,41 @@ __device__ __forceinline__ void tile_phases(const LevelK& L, const LevelK& Ls, d
                 __syncthreads();
             }
         } else {  // reverse (left-preconditioned) pressure colour c; ts = m^T b of the tile
+            // Two threads per colour-c cell: the even one evaluates the six momentum rows at the
+            // cell's faces (flux part), the odd one the seven continuity rows (C and its six
+            // neighbours) and hands (lc, s) over by shuffle; the even one finishes prev_core's
+            // expression in its operand order.
             const int c = 17 - ph;
-            if (tid < kTileCells / 8) {
-                int lx, ly, lz;
-                tile_pcell(tid, c, lx, ly, lz);
-                if (tile_v2<IN>(L, x0, y0, z0, lx, ly, lz)) {
-                    const int li = TB::li(lx, ly, lz);
-                    Ps[li] = prev_core(Ls, xs, li, ts[tile_ti(lx, ly, lz)]);
+            const int cell = tid >> 1, half = tid & 1;
+            const int qx = 2 * (cell % (kTX / 2)) + (c & 1), qy = 2 * ((cell / (kTX / 2)) % (kTY / 2)) + ((c >> 1) & 1),
+                      qz = 2 * (cell / (kTX * kTY / 4)) + (c >> 2);
+            const bool v2 = IN || tile_v2<false>(L, x0, y0, z0, qx, qy, qz);
+            const int i = TB::li(qx, qy, qz);
+            double fl = 0.0, lc = 0.0, s = 0.0;
+            if (v2) {
+                if (half == 0) {
+                    const double luL = Ops::mom(Us, Ps, i, 1, e2, ih);
+                    const double luR = Ops::mom(Us, Ps, i + 1, 1, e2, ih);
+                    const double lvL = Ops::mom(Vs, Ps, i, SY, e2, ih);
+                    const double lvR = Ops::mom(Vs, Ps, i + SY, SY, e2, ih);
+                    const double lwL = Ops::mom(Ws, Ps, i, SZ, e2, ih);
+                    const double lwR = Ops::mom(Ws, Ps, i + SZ, SZ, e2, ih);
+                    fl = ((luR - luL) + (lvR - lvL)) + (lwR - lwL);
+                } else {
+                    lc = Ops::cont(Us, Vs, Ws, Ps, i, gam, ih);
+                    s = Ops::cont(Us, Vs, Ws, Ps, i - 1, gam, ih) + Ops::cont(Us, Vs, Ws, Ps, i + 1, gam, ih);
+                    s = s + Ops::cont(Us, Vs, Ws, Ps, i - SY, gam, ih);
+                    s = s + Ops::cont(Us, Vs, Ws, Ps, i + SY, gam, ih);
+                    s = s + Ops::cont(Us, Vs, Ws, Ps, i - SZ, gam, ih);
+                    s = s + Ops::cont(Us, Vs, Ws, Ps, i + SZ, gam, ih);
                 }
+            }
+            lc = __shfl_down_sync(0xffffffffu, lc, 1);
+            s = __shfl_down_sync(0xffffffffu, s, 1);
+            // same-colour cells never read each other's pressure: the update goes in place
+            if (v2 && half == 0) {
+                const double cl = fl * ih + e2 * (6.0 * lc - s);
+                Ps[i] = Ps[i] + (ts[tile_ti(qx, qy, qz)] - cl) / dp;
             }
             __syncthreads();
         }
@@ -1951,16 +2016,12 @@ __global__ void __launch_bounds__(kTileThreads, 2)
             : "memory");
     }
     __syncthreads();
-    LevelK Ls = L;  // the same operators on the box (strides of the shared-memory box)
-    Ls.g.sy = TB::BX;
-    Ls.g.sz = TB::BX * TB::BY;
-    Ls.g.fs = TB::BOX;
     // interior: every cell of the tile and of the cell layer around it is a V2 cell of the level
     const int gz0 = g.gz(z0), bw = L.bw;
     const bool interior = x0 - 1 >= bw && y0 - 1 >= bw && gz0 - 1 >= bw && x0 + kTX + 1 <= g.nx - bw &&
                           y0 + kTY + 1 <= g.ny - bw && gz0 + kTZ + 1 <= g.gnz - bw;
-    if (interior) tile_phases<FWD, true>(L, Ls, xs, bs, ts, x0, y0, z0, ph0, ph1);
-    else tile_phases<FWD, false>(L, Ls, xs, bs, ts, x0, y0, z0, ph0, ph1);
+    if (interior) tile_phases<FWD, true>(L, xs, bs, ts, x0, y0, z0, ph0, ph1);
+    else tile_phases<FWD, false>(L, xs, bs, ts, x0, y0, z0, ph0, ph1);
     // Write back the DOFs the phases may have changed: the tile's own, plus (after forward
     // pressure phases) its high faces and the pressures of the six neighbouring slabs.  Rows of
     // 16 go out as 16-byte stores.  Every slot written was loaded by this CTA and no other CTA
