@@ -1627,8 +1627,8 @@ struct TileBox {
     static constexpr int BOX = BX * BY * BZ;
     static constexpr int NB = FWD ? 4 : 3;  // fields of b staged
     // FWD: pressure deltas on the tile plus a ring of zeros (the neighbours outside the tile carry
-    // no delta, so gathers need no bounds tests); REV: m^T b of the tile
-    static constexpr int TS = FWD ? (kTX + 2) * (kTY + 2) * (kTZ + 2) : kTileCells;
+    // no delta, so gathers need no bounds tests); REV: m^T b of the tile + the (lc, s) exchange
+    static constexpr int TS = FWD ? (kTX + 2) * (kTY + 2) * (kTZ + 2) : kTileCells + kTileCells / 4;
     // x box (4 fields), b (NB fields of the tile), ts, mbarrier
     static constexpr size_t SMEM = (4 * BOX + NB * kTileCells + TS) * sizeof(double) + 128 + 16;
     static __device__ __forceinline__ int li(int x, int y, int z) { return ((z + OZ) * BY + (y + OY)) * BX + (x + OX); }
@@ -1800,8 +1800,9 @@ __device__ __forceinline__ void tile_phases(const LevelK& L, double* __restrict_
         vti[k] = tile_ti(lx0, ly, lz);
         vpar[k] = (ly + lz + g.gz(z0)) & 1;  // global parity of (lx0, ly, lz) (x0 even)
     }
-    // pressure phases: this thread's cell of colour c = base + offset(c) (tid < kTileCells / 8)
-    const int px0 = 2 * (tid % (kTX / 2)), py0 = 2 * ((tid / (kTX / 2)) % (kTY / 2)), pz0 = 2 * (tid / (kTX * kTY / 4));
+    // pressure phases: this thread's cell of colour c = base + offset(c), cell index m = tid % 128
+    const int pm = tid % (kTileCells / 8);
+    const int px0 = 2 * (pm % (kTX / 2)), py0 = 2 * ((pm / (kTX / 2)) % (kTY / 2)), pz0 = 2 * (pm / (kTX * kTY / 4));
     const int pli = TB::li(px0, py0, pz0), pti = tile_ti(px0, py0, pz0), ptd = tile_td(px0, py0, pz0);
     for (int ph = ph0; ph < ph1; ++ph) {
         if (ph <= 1 || ph >= 18) {  // velocity colour (red-black on global parity)
@@ -1841,36 +1842,62 @@ __device__ __forceinline__ void tile_phases(const LevelK& L, double* __restrict_
             // the neighbour terms are added when K is next read -- those of earlier colours at the
             // start of K's phase, the rest in the flush after the last colour: the same additions
             // in the same order, hence bit-identical, with 9 barriers instead of 16.
-            const int c = ph - 2;
-            if (tid < kTileCells / 8) {
-                const int cx = c & 1, cy = (c >> 1) & 1, cz = c >> 2;
+            int c = ph - 2;
+            // one colour-cc cell (this thread's cell index m = tid % 128)
+            auto pcell = [&](int cc) {
+                const int cx = cc & 1, cy = (cc >> 1) & 1, cz = cc >> 2;
                 const bool v2 = IN || tile_v2<false>(L, x0, y0, z0, px0 + cx, py0 + cy, pz0 + cz);
-                if (v2) {
-                    const int li = pli + cx + cy * SY + cz * SZ;
-                    const int ti = pti + cx + cy * kTX + cz * kTX * kTY;
-                    const int td = ptd + cx + cy * kDX + cz * kDXY;
-                    const double p =
-                        full ? gath_k<true>(c, Ps[li], ts, td, e2)
-                             : tile_gathers<IN>(L, ts, Ps[li], x0, y0, z0, px0 + cx, py0 + cy, pz0 + cz, c, cfirst, c);
-                    const double div = (Us[li + 1] - Us[li]) + (Vs[li + SY] - Vs[li]) + (Ws[li + SZ] - Ws[li]);
-                    const double rr = bs[3 * kTileCells + ti] - (-div * ih - gam * p);
-                    const double dc = rr / dp;
-                    ts[td] = dc;
-                    Us[li] = Us[li] + (0.0 - dc) * ih;
-                    Us[li + 1] = Us[li + 1] + (dc - 0.0) * ih;
-                    Vs[li] = Vs[li] + (0.0 - dc) * ih;
-                    Vs[li + SY] = Vs[li + SY] + (dc - 0.0) * ih;
-                    Ws[li] = Ws[li] + (0.0 - dc) * ih;
-                    Ws[li + SZ] = Ws[li + SZ] + (dc - 0.0) * ih;
-                    double sn = 0.0 + 0.0;  // the colour-c neighbour sum of a colour-c cell: six zeros
-                    sn = sn + 0.0;
-                    sn = sn + 0.0;
-                    sn = sn + 0.0;
-                    sn = sn + 0.0;
-                    Ps[li] = p + e2 * (6.0 * dc - sn);
+                if (!v2) return;
+                const int li = pli + cx + cy * SY + cz * SZ;
+                const int ti = pti + cx + cy * kTX + cz * kTX * kTY;
+                const int td = ptd + cx + cy * kDX + cz * kDXY;
+                const double p =
+                    full ? gath_k<true>(cc, Ps[li], ts, td, e2)
+                         : tile_gathers<IN>(L, ts, Ps[li], x0, y0, z0, px0 + cx, py0 + cy, pz0 + cz, cc, cfirst, cc);
+                const double div = (Us[li + 1] - Us[li]) + (Vs[li + SY] - Vs[li]) + (Ws[li + SZ] - Ws[li]);
+                const double rr = bs[3 * kTileCells + ti] - (-div * ih - gam * p);
+                const double dc = rr / dp;
+                ts[td] = dc;
+                Us[li] = Us[li] + (0.0 - dc) * ih;
+                Us[li + 1] = Us[li + 1] + (dc - 0.0) * ih;
+                Vs[li] = Vs[li] + (0.0 - dc) * ih;
+                Vs[li + SY] = Vs[li + SY] + (dc - 0.0) * ih;
+                Ws[li] = Ws[li] + (0.0 - dc) * ih;
+                Ws[li + SZ] = Ws[li + SZ] + (dc - 0.0) * ih;
+                double sn = 0.0 + 0.0;  // the colour-cc neighbour sum of a colour-cc cell: six zeros
+                sn = sn + 0.0;
+                sn = sn + 0.0;
+                sn = sn + 0.0;
+                sn = sn + 0.0;
+                Ps[li] = p + e2 * (6.0 * dc - sn);
+            };
+            if (full) {
+                // Colours of equal popcount never touch each other's faces or pressures, nor does a
+                // cell read a same-group colour's delta: 0 | 1,2,4 | 3,5,6 | 7 run as four steps
+                // (per cell the same operations; bit-identical).
+                const int hi = tid >= kTileCells / 8;
+                if (!hi) pcell(0);
+                __syncthreads();
+                if (hi) pcell(2);
+                else {
+                    pcell(1);
+                    pcell(4);
                 }
+                __syncthreads();
+                if (hi) pcell(5);
+                else {
+                    pcell(3);
+                    pcell(6);
+                }
+                __syncthreads();
+                if (!hi) pcell(7);
+                __syncthreads();
+                ph = 9;
+                c = 7;
+            } else {
+                if (tid < kTileCells / 8) pcell(c);
+                __syncthreads();
             }
-            __syncthreads();
             if (ph == 9 || ph + 1 == ph1) {  // flush: the terms of colours [cfirst, c] still pending
                 // every cell of the tile and of the six face slabs around it (ring edges and corners
                 // have no tile neighbour)
@@ -1922,17 +1949,19 @@ __device__ __forceinline__ void tile_phases(const LevelK& L, double* __restrict_
                 __syncthreads();
             }
         } else {  // reverse (left-preconditioned) pressure colour c; ts = m^T b of the tile
-            // Two threads per colour-c cell: the even one evaluates the six momentum rows at the
-            // cell's faces (flux part), the odd one the seven continuity rows (C and its six
-            // neighbours) and hands (lc, s) over by shuffle; the even one finishes prev_core's
-            // expression in its operand order.
+            // Two warps per 32 colour-c cells: warps 0, 2, 4, 6 evaluate the six momentum rows at
+            // the cells' faces (flux part), warps 1, 3, 5, 7 the seven continuity rows (C and its
+            // six neighbours) and hand (lc, s) over through shared memory; the first finish
+            // prev_core's expression in its operand order.  Same-colour cells never read each
+            // other's pressure, so the update goes in place.
             const int c = 17 - ph;
-            const int cell = tid >> 1, half = tid & 1;
+            const int half = (tid >> 5) & 1, cell = ((tid >> 6) << 5) | (tid & 31);
             const int qx = 2 * (cell % (kTX / 2)) + (c & 1), qy = 2 * ((cell / (kTX / 2)) % (kTY / 2)) + ((c >> 1) & 1),
                       qz = 2 * (cell / (kTX * kTY / 4)) + (c >> 2);
             const bool v2 = IN || tile_v2<false>(L, x0, y0, z0, qx, qy, qz);
             const int i = TB::li(qx, qy, qz);
-            double fl = 0.0, lc = 0.0, s = 0.0;
+            double* xch = ts + kTileCells;  // [2][kTileCells / 8]: lc, s
+            double fl = 0.0;
             if (v2) {
                 if (half == 0) {
                     const double luL = Ops::mom(Us, Ps, i, 1, e2, ih);
@@ -1943,19 +1972,19 @@ __device__ __forceinline__ void tile_phases(const LevelK& L, double* __restrict_
                     const double lwR = Ops::mom(Ws, Ps, i + SZ, SZ, e2, ih);
                     fl = ((luR - luL) + (lvR - lvL)) + (lwR - lwL);
                 } else {
-                    lc = Ops::cont(Us, Vs, Ws, Ps, i, gam, ih);
-                    s = Ops::cont(Us, Vs, Ws, Ps, i - 1, gam, ih) + Ops::cont(Us, Vs, Ws, Ps, i + 1, gam, ih);
-                    s = s + Ops::cont(Us, Vs, Ws, Ps, i - SY, gam, ih);
-                    s = s + Ops::cont(Us, Vs, Ws, Ps, i + SY, gam, ih);
-                    s = s + Ops::cont(Us, Vs, Ws, Ps, i - SZ, gam, ih);
-                    s = s + Ops::cont(Us, Vs, Ws, Ps, i + SZ, gam, ih);
+                    const double lc = Ops::cont(Us, Vs, Ws, Ps, i, gam, ih);
+                    double sn = Ops::cont(Us, Vs, Ws, Ps, i - 1, gam, ih) + Ops::cont(Us, Vs, Ws, Ps, i + 1, gam, ih);
+                    sn = sn + Ops::cont(Us, Vs, Ws, Ps, i - SY, gam, ih);
+                    sn = sn + Ops::cont(Us, Vs, Ws, Ps, i + SY, gam, ih);
+                    sn = sn + Ops::cont(Us, Vs, Ws, Ps, i - SZ, gam, ih);
+                    sn = sn + Ops::cont(Us, Vs, Ws, Ps, i + SZ, gam, ih);
+                    xch[cell] = lc;
+                    xch[kTileCells / 8 + cell] = sn;
                 }
             }
-            lc = __shfl_down_sync(0xffffffffu, lc, 1);
-            s = __shfl_down_sync(0xffffffffu, s, 1);
-            // same-colour cells never read each other's pressure: the update goes in place
+            __syncthreads();
             if (v2 && half == 0) {
-                const double cl = fl * ih + e2 * (6.0 * lc - s);
+                const double cl = fl * ih + e2 * (6.0 * xch[cell] - xch[kTileCells / 8 + cell]);
                 Ps[i] = Ps[i] + (ts[tile_ti(qx, qy, qz)] - cl) / dp;
             }
             __syncthreads();
