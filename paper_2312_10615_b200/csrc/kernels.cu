@@ -2008,8 +2008,10 @@ __global__ void __launch_bounds__(kTileThreads, 2)
                const __grid_constant__ CUtensorMap tmc, LevelK L, double* __restrict__ X, int T, int ph0, int ph1,
                int ntx, int nty) {
     using TB = TileBox<FWD>;
-    extern __shared__ __align__(128) unsigned char tsm_raw[];
-    double* xs = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(tsm_raw) + 127) & ~uintptr_t(127));
+    extern __shared__ __align__(128) double tsm_raw[];
+    // 128-byte aligned by pointer arithmetic on the shared array (an integer round trip would hide
+    // the address space and turn every box access into a generic LD/ST)
+    double* xs = tsm_raw + (((128u - (smem_u32(tsm_raw) & 127u)) & 127u) >> 3);
     double* bs = xs + 4 * TB::BOX;          // b of the tile, NB fields
     double* ts = bs + TB::NB * kTileCells;  // deltas (FWD) / m^T b (REV)
     uint64_t* bar = reinterpret_cast<uint64_t*>(ts + TB::TS);
