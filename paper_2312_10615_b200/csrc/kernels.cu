@@ -1807,32 +1807,39 @@ __device__ __forceinline__ void tile_phases(const LevelK& L, double* __restrict_
     for (int ph = ph0; ph < ph1; ++ph) {
         if (ph <= 1 || ph >= 18) {  // velocity colour (red-black on global parity)
             const int c = ph <= 1 ? ph : 19 - ph;
+            // this thread's colour-c cells are independent: every new value is computed before
+            // any is stored, so the loads of all six face rows can be in flight together
+            constexpr int NV = kTileCells / 2 / kTileThreads;
+            int li[NV], ti[NV];
+            bool du[NV], dv_[NV], dw[NV];
+            double nu[NV], nv[NV], nw[NV];
 #pragma unroll
-            for (int k = 0; k < kTileCells / 2 / kTileThreads; ++k) {
+            for (int k = 0; k < NV; ++k) {
                 const int ox = vpar[k] ^ c;  // x offset of the colour-c cell of the pair
-                const int li = vli[k] + ox, ti = vti[k] + ox;
-                bool du = true, dv_ = true, dw = true;
+                li[k] = vli[k] + ox;
+                ti[k] = vti[k] + ox;
+                du[k] = dv_[k] = dw[k] = true;
                 if (!IN) {
                     const int e = tid + k * kTileThreads;
                     const int gx = x0 + 2 * (e % (kTX / 2)) + ox, gy = y0 + (e / (kTX / 2)) % kTY,
                               zl = z0 + e / (kTX * kTY / 2);
                     const bool here = band_cell(L, gx, gy, zl);
-                    du = gx >= 1 && !here && !band_cell(L, gx - 1, gy, zl);
-                    dv_ = gy >= 1 && !here && !band_cell(L, gx, gy - 1, zl);
-                    dw = g.gz(zl) >= 1 && !here && !band_cell(L, gx, gy, zl - 1);
+                    du[k] = gx >= 1 && !here && !band_cell(L, gx - 1, gy, zl);
+                    dv_[k] = gy >= 1 && !here && !band_cell(L, gx, gy - 1, zl);
+                    dw[k] = g.gz(zl) >= 1 && !here && !band_cell(L, gx, gy, zl - 1);
                 }
-                if (du) {
-                    const double r = bs[ti] - Ops::mom(Us, Ps, li, 1, e2, ih);
-                    Us[li] = Us[li] + r / dv;
-                }
-                if (dv_) {
-                    const double r = bs[kTileCells + ti] - Ops::mom(Vs, Ps, li, SY, e2, ih);
-                    Vs[li] = Vs[li] + r / dv;
-                }
-                if (dw) {
-                    const double r = bs[2 * kTileCells + ti] - Ops::mom(Ws, Ps, li, SZ, e2, ih);
-                    Ws[li] = Ws[li] + r / dv;
-                }
+            }
+#pragma unroll
+            for (int k = 0; k < NV; ++k) {
+                nu[k] = Us[li[k]] + (bs[ti[k]] - Ops::mom(Us, Ps, li[k], 1, e2, ih)) / dv;
+                nv[k] = Vs[li[k]] + (bs[kTileCells + ti[k]] - Ops::mom(Vs, Ps, li[k], SY, e2, ih)) / dv;
+                nw[k] = Ws[li[k]] + (bs[2 * kTileCells + ti[k]] - Ops::mom(Ws, Ps, li[k], SZ, e2, ih)) / dv;
+            }
+#pragma unroll
+            for (int k = 0; k < NV; ++k) {
+                if (du[k]) Us[li[k]] = nu[k];
+                if (dv_[k]) Vs[li[k]] = nv[k];
+                if (dw[k]) Ws[li[k]] = nw[k];
             }
             __syncthreads();
         } else if (FWD) {  // forward pressure colour c, lazy gathers; ts = deltas of the colours so far
@@ -1843,33 +1850,60 @@ __device__ __forceinline__ void tile_phases(const LevelK& L, double* __restrict_
             // start of K's phase, the rest in the flush after the last colour: the same additions
             // in the same order, hence bit-identical, with 9 barriers instead of 16.
             int c = ph - 2;
-            // one colour-cc cell (this thread's cell index m = tid % 128)
-            auto pcell = [&](int cc) {
+            // one colour-cc cell (this thread's cell index m = tid % 128): load + compute, then store
+            struct PNew {
+                int li, td;
+                bool on;
+                double dc, u0, u1, v0, v1, w0, w1, p;
+            };
+            auto pload = [&](int cc) {
+                PNew r;
                 const int cx = cc & 1, cy = (cc >> 1) & 1, cz = cc >> 2;
-                const bool v2 = IN || tile_v2<false>(L, x0, y0, z0, px0 + cx, py0 + cy, pz0 + cz);
-                if (!v2) return;
+                r.on = IN || tile_v2<false>(L, x0, y0, z0, px0 + cx, py0 + cy, pz0 + cz);
                 const int li = pli + cx + cy * SY + cz * SZ;
                 const int ti = pti + cx + cy * kTX + cz * kTX * kTY;
                 const int td = ptd + cx + cy * kDX + cz * kDXY;
+                r.li = li;
+                r.td = td;
+                if (!r.on) return r;
                 const double p =
                     full ? gath_k<true>(cc, Ps[li], ts, td, e2)
                          : tile_gathers<IN>(L, ts, Ps[li], x0, y0, z0, px0 + cx, py0 + cy, pz0 + cz, cc, cfirst, cc);
-                const double div = (Us[li + 1] - Us[li]) + (Vs[li + SY] - Vs[li]) + (Ws[li + SZ] - Ws[li]);
+                const double uL = Us[li], uR = Us[li + 1], vL = Vs[li], vR = Vs[li + SY], wL = Ws[li], wR = Ws[li + SZ];
+                const double div = (uR - uL) + (vR - vL) + (wR - wL);
                 const double rr = bs[3 * kTileCells + ti] - (-div * ih - gam * p);
                 const double dc = rr / dp;
-                ts[td] = dc;
-                Us[li] = Us[li] + (0.0 - dc) * ih;
-                Us[li + 1] = Us[li + 1] + (dc - 0.0) * ih;
-                Vs[li] = Vs[li] + (0.0 - dc) * ih;
-                Vs[li + SY] = Vs[li + SY] + (dc - 0.0) * ih;
-                Ws[li] = Ws[li] + (0.0 - dc) * ih;
-                Ws[li + SZ] = Ws[li + SZ] + (dc - 0.0) * ih;
+                r.dc = dc;
+                r.u0 = uL + (0.0 - dc) * ih;
+                r.u1 = uR + (dc - 0.0) * ih;
+                r.v0 = vL + (0.0 - dc) * ih;
+                r.v1 = vR + (dc - 0.0) * ih;
+                r.w0 = wL + (0.0 - dc) * ih;
+                r.w1 = wR + (dc - 0.0) * ih;
                 double sn = 0.0 + 0.0;  // the colour-cc neighbour sum of a colour-cc cell: six zeros
                 sn = sn + 0.0;
                 sn = sn + 0.0;
                 sn = sn + 0.0;
                 sn = sn + 0.0;
-                Ps[li] = p + e2 * (6.0 * dc - sn);
+                r.p = p + e2 * (6.0 * dc - sn);
+                return r;
+            };
+            auto pstore = [&](const PNew& r) {
+                if (!r.on) return;
+                ts[r.td] = r.dc;
+                Us[r.li] = r.u0;
+                Us[r.li + 1] = r.u1;
+                Vs[r.li] = r.v0;
+                Vs[r.li + SY] = r.v1;
+                Ws[r.li] = r.w0;
+                Ws[r.li + SZ] = r.w1;
+                Ps[r.li] = r.p;
+            };
+            auto pcell = [&](int cc) { pstore(pload(cc)); };
+            auto pcell2 = [&](int ca, int cb) {  // two independent cells: both computed before stores
+                const PNew ra = pload(ca), rb = pload(cb);
+                pstore(ra);
+                pstore(rb);
             };
             if (full) {
                 // Colours of equal popcount never touch each other's faces or pressures, nor does a
@@ -1879,16 +1913,10 @@ __device__ __forceinline__ void tile_phases(const LevelK& L, double* __restrict_
                 if (!hi) pcell(0);
                 __syncthreads();
                 if (hi) pcell(2);
-                else {
-                    pcell(1);
-                    pcell(4);
-                }
+                else pcell2(1, 4);
                 __syncthreads();
                 if (hi) pcell(5);
-                else {
-                    pcell(3);
-                    pcell(6);
-                }
+                else pcell2(3, 6);
                 __syncthreads();
                 if (!hi) pcell(7);
                 __syncthreads();
