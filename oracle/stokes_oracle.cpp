@@ -1017,13 +1017,15 @@ static void vcycle(const Hierarchy& H, int l, const vec& b, vec& x) {
 }
 
 // ----------------------------------------------------- canonical dot -------
-// Fixed reduction order of every SQMR inner product (OD-12), the
-// one the GPU computes natively: for each field (u, v, w, p), plane z, row y of
-// the field's storage box, 32 lane accumulators take x = lane, lane+32, ... in
-// ascending order and are combined by the tree acc[l] += acc[l+o], o = 16..1;
-// row sums are added in ascending y to a plane sum; plane sums (fields in
-// order, z ascending) go through the same 32-lane scheme.  Zero slots (walls,
-// inactive) contribute exactly +0 and are skipped here.
+// Fixed reduction order of every SQMR inner product (OD-12 rev. 2), the one the
+// GPU's fused kernels produce natively (kernels.cu k_cdot / k_apply_q / k_apply_x / final2):
+//   * blocks of 32 x-lanes x 8 y-rows x 4 z-planes; a lane adds, over its cell's planes in
+//     ascending z, ((p_u + p_v) + p_w) + p_p, the products of the four DOFs stored at the cell
+//     (the u, v, w faces on the cell's low side and its pressure; an inactive one gives +0);
+//   * the 32 lanes of a row combine by the tree acc[l] += acc[l + o], o = 16..1 (lane 0), the 8
+//     rows are added in ascending order: the block partial, at ((zb GY + by) GX + bx);
+//   * final: 256 accumulators take partials k = t, t + 256, ... ascending, each warp of 32
+//     combines by the same tree, the 8 warp sums are added in ascending order.
 static double lane_tree(double* acc) {
     for (int o = 16; o > 0; o >>= 1)
         for (int l = 0; l < o; ++l) acc[l] = acc[l] + acc[l + o];
@@ -1032,31 +1034,42 @@ static double lane_tree(double* acc) {
 
 static double cdot(const Level& L, const vec& a, const vec& b) {
     const DofMap& m = L.map;
-    std::vector<double> planes;
-    for (int c = 0; c < 4; ++c) {
-        const int ex = c < 3 ? m.fext[c][0] : m.n[0], ey = c < 3 ? m.fext[c][1] : m.n[1];
-        const int ez = c < 3 ? m.fext[c][2] : m.n[2];
-        const size_t base = planes.size();
-        planes.resize(base + ez);
-        parallel_for(ez, g_threads, [&](int64_t z) {
-            double p = 0.0;
-            for (int y = 0; y < ey; ++y) {
-                double acc[32];
-                for (int l = 0; l < 32; ++l) acc[l] = 0.0;
-                for (int x = 0; x < ex; ++x) {
-                    const int32_t id = c < 3 ? m.face(c, x, y, static_cast<int>(z)) : m.cell(x, y, static_cast<int>(z));
-                    if (id < 0) continue;
-                    acc[x & 31] = acc[x & 31] + a[id] * b[id];
+    const int nx = m.n[0], ny = m.n[1], nz = m.n[2];
+    const int GX = (nx + 31) / 32, GY = (ny + 7) / 8, GZ = (nz + 3) / 4;
+    std::vector<double> part(static_cast<size_t>(GX) * GY * GZ);
+    auto prod = [&](int32_t id) { return id >= 0 ? a[id] * b[id] : 0.0 * 0.0; };
+    parallel_for(GZ, g_threads, [&](int64_t zb) {
+        for (int by = 0; by < GY; ++by)
+            for (int bx = 0; bx < GX; ++bx) {
+                double ws[8];
+                for (int w = 0; w < 8; ++w) {
+                    double acc[32];
+                    for (int l = 0; l < 32; ++l) {
+                        const int x = bx * 32 + l, y = by * 8 + w;
+                        double v = 0.0;
+                        if (x < nx && y < ny)
+                            for (int z = static_cast<int>(zb) * 4; z < std::min(nz, static_cast<int>(zb) * 4 + 4); ++z) {
+                                const double pu = prod(m.face(0, x, y, z)), pv = prod(m.face(1, x, y, z));
+                                const double pw = prod(m.face(2, x, y, z)), pp = prod(m.cell(x, y, z));
+                                v = v + (((pu + pv) + pw) + pp);
+                            }
+                        acc[l] = v;
+                    }
+                    ws[w] = lane_tree(acc);
                 }
-                p = p + lane_tree(acc);
+                double s = ws[0];
+                for (int w = 1; w < 8; ++w) s = s + ws[w];
+                part[(static_cast<size_t>(zb) * GY + by) * GX + bx] = s;
             }
-            planes[base + z] = p;
-        });
-    }
-    double acc[32];
-    for (int l = 0; l < 32; ++l) acc[l] = 0.0;
-    for (size_t q = 0; q < planes.size(); ++q) acc[q & 31] = acc[q & 31] + planes[q];
-    return lane_tree(acc);
+    });
+    double acc[256];
+    for (int t = 0; t < 256; ++t) acc[t] = 0.0;
+    for (size_t k = 0; k < part.size(); ++k) acc[k & 255] = acc[k & 255] + part[k];
+    double ws[8];
+    for (int w = 0; w < 8; ++w) ws[w] = lane_tree(acc + 32 * w);
+    double s = ws[0];
+    for (int w = 1; w < 8; ++w) s = s + ws[w];
+    return s;
 }
 
 // -------------------------------------------------------------- krylov ------

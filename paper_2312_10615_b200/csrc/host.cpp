@@ -255,23 +255,21 @@ struct smg_ctx {
     int nc = 0;
     double* vk_delta = nullptr;
     // SQMR vectors on the fine level (s = lv[0].b, t = lv[0].x, scratch = lv[0].r)
+    // q, d and x_sqmr ping-pong between iterations (the fused kernels read the old and write the
+    // new vector): buffer [j & 1] holds the values after iteration j
     double *q = nullptr, *d = nullptr, *xs = nullptr, *rhs = nullptr;
+    double *q2 = nullptr, *d2 = nullptr, *xs2 = nullptr;
+    int xcur = 0;  // buffer holding the current solution (0: xs, 1: xs2)
     double* compact = nullptr;
     double* partials = nullptr;
     double* dscal = nullptr;
     double* hscal = nullptr;  // pinned
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-    cudaGraphExec_t graph = nullptr;  // one SQMR iteration
+    cudaGraphExec_t graph = nullptr, graph2 = nullptr;  // one SQMR iteration (even / odd parity)
     int64_t graph_kernels = 0;
     bool graph_captured_now = false;
-    // device-side SQMR loop: a WHILE conditional node around the iteration + k_sqmr_loop_ctl
-    cudaGraphExec_t init_graph = nullptr;  // SQMR lines 1-4 (initial V-cycle)
+    cudaGraphExec_t init_graph = nullptr;  // SQMR lines 1-4 (initial V-cycle), opt-in
     int64_t init_kernels = 0;
-    cudaGraphExec_t loop_graph = nullptr;
-    bool loop_failed = false;
-    int* dloop = nullptr;                  // {iterations, maxit, last code}
-    double* dhist = nullptr;               // rel per iteration (kLoopCap)
-    unsigned long long* dstamp = nullptr;  // globaltimer: [0] loop start, [j] iteration j
     std::string err;
     smg_timing timing{};
     std::vector<void*> allocs;
@@ -304,7 +302,7 @@ struct smg_ctx {
         for (void* p : allocs) cudaFree(p);
         if (hscal) cudaFreeHost(hscal);
         if (graph) cudaGraphExecDestroy(graph);
-        if (loop_graph) cudaGraphExecDestroy(loop_graph);
+        if (graph2) cudaGraphExecDestroy(graph2);
         if (init_graph) cudaGraphExecDestroy(init_graph);
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);
@@ -317,10 +315,6 @@ namespace {
 
 int64_t vlen(const DevLevel& L) { return L.k.g.vec_len(); }
 
-int env_int(const char* name, int dflt) {
-    const char* e = std::getenv(name);
-    return e ? std::atoi(e) : dflt;
-}
 
 // ---- setup ----
 void build(smg_ctx* c, const std::vector<double>* shared_coarse = nullptr, std::vector<double>* coarse_out = nullptr,
@@ -638,11 +632,14 @@ void build(smg_ctx* c, const std::vector<double>* shared_coarse = nullptr, std::
     c->q = c->dalloc<double>(vl0);
     c->d = c->dalloc<double>(vl0);
     c->xs = c->dalloc<double>(vl0);
+    c->q2 = c->dalloc<double>(vl0);
+    c->d2 = c->dalloc<double>(vl0);
+    c->xs2 = c->dalloc<double>(vl0);
     c->rhs = c->dalloc<double>(vl0);
     int64_t maxN = 0;
     for (auto& L : c->lv) maxN = std::max(maxN, L.N);
     c->compact = c->dalloc<double>(maxN);
-    c->partials = c->dalloc<double>(kPartials);
+    c->partials = c->dalloc<double>(dot_partials(c->lv[0].k.g));  // zero outside this part's blocks
     c->dscal = c->dalloc<double>(S_COUNT);
     CK(cudaMallocHost(&c->hscal, 8 * sizeof(double)));
     CK(cudaStreamSynchronize(c->st));
@@ -748,220 +745,6 @@ void vcycle(smg_ctx* c, int l, const double* b, double* x) {
     }
     launch_prolong_add(L.k, C.k, C.x, x, c->st);
     smooth(c, l, x, b, cb);
-}
-
-// ---- SQMR, Alg. 4; b in c->rhs, x into c->xs ----
-// One iteration (lines 5-10) is a fixed kernel sequence with its scalars on
-// the device; it is captured once as a CUDA graph and replayed.  The host
-// reads back only (rel, status) per iteration for the convergence test.
-void sqmr_iteration(smg_ctx* c) {
-    DevLevel& F = c->lv[0];
-    const int64_t n = vlen(F);
-    double *s = F.b, *t = F.x, *r = F.r, *sc = c->dscal;
-    const Geom& g = F.k.g;
-    launch_apply(F.k, c->q, nullptr, t, 0.0, c->st);                     // t = L q
-    launch_cdot2(g, c->q, t, nullptr, nullptr, c->partials, sc + S_D0, c->st);  // sigma
-    launch_sqmr_scalar(1, sc, c->st);                                    // alpha
-    launch_axpy_s(s, t, sc, n, c->st);                                   // s -= alpha t
-    vcycle(c, 0, s, t);                                                  // t = V(s)
-    launch_cdot2(g, t, t, s, t, c->partials, sc + S_D0, c->st);          // ||t||^2, rho_j
-    launch_sqmr_scalar(2, sc, c->st);                                    // nu, c, tau, cd, cq
-    launch_dx_dev(c->d, c->xs, c->q, sc, n, c->st);                      // d, x
-    launch_apply(F.k, c->xs, c->rhs, r, 0.0, c->st);                     // r = b - L x
-    launch_cdot2(g, r, r, nullptr, nullptr, c->partials, sc + S_D0, c->st);
-    launch_sqmr_scalar(3, sc, c->st);                                    // rel, beta
-    launch_xpby_dev(c->q, t, sc, n, c->st);                              // q = t + beta q
-}
-
-// Device-side loop (opt-in, SMG_DEVICE_LOOP=1): one graph launch runs every iteration; the host
-// no longer syncs, reads (rel, status) and relaunches the iteration graph per iteration.  Built on
-// first use; any failure falls back to the host loop for the context's lifetime.  Bit-identical
-// (same kernels, same order), but measured neutral on cfg 1 (18.85 ms host loop vs 18.89 ms,
-// profiles/r1s5_devloop_cfg1.txt): the per-iteration sync and relaunch were already hidden.
-constexpr int kLoopCap = 1 << 16;
-static bool build_loop_graph(smg_ctx* c) {
-    if (c->loop_graph) return true;
-    if (c->loop_failed || env_int("SMG_DEVICE_LOOP", 0) == 0) return false;
-    cudaGraph_t g = nullptr;
-    bool ok = false;
-    do {
-        if (!c->dloop) {
-            c->dloop = c->dalloc<int>(4);
-            c->dhist = c->dalloc<double>(kLoopCap);
-            c->dstamp = c->dalloc<unsigned long long>(kLoopCap + 1);
-        }
-        if (cudaGraphCreate(&g, 0) != cudaSuccess) break;
-        cudaGraphConditionalHandle h;
-        if (cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault) != cudaSuccess) break;
-        cudaGraphNodeParams p = {};
-        p.type = cudaGraphNodeTypeConditional;
-        p.conditional.handle = h;
-        p.conditional.type = cudaGraphCondTypeWhile;
-        p.conditional.size = 1;
-        cudaGraphNode_t node;
-        if (cudaGraphAddNode(&node, g, nullptr, 0, &p) != cudaSuccess) break;
-        cudaGraph_t body = p.conditional.phGraph_out[0];
-        if (cudaStreamBeginCaptureToGraph(c->st, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed) !=
-            cudaSuccess)
-            break;
-        sqmr_iteration(c);
-        launch_sqmr_loop_ctl(h, c->dscal, c->dhist, c->dstamp, c->dloop, c->st);
-        cudaGraph_t out = nullptr;
-        const cudaError_t ec = cudaStreamEndCapture(c->st, &out);
-        if (ec != cudaSuccess || take_launch_error() != 0) break;
-        if (cudaGraphInstantiate(&c->loop_graph, g, 0) != cudaSuccess) break;
-        ok = true;
-    } while (false);
-    if (g) cudaGraphDestroy(g);
-    if (!ok) {
-        c->loop_failed = true;
-        c->loop_graph = nullptr;
-        cudaGetLastError();  // clear the sticky-free error of the failed build
-        std::fprintf(stderr, "smg: device-side SQMR loop unavailable, using the host loop\n");
-    }
-    return ok;
-}
-
-int sqmr(smg_ctx* c, double tol, int maxit, smg_history* hist, int* status) {
-    DevLevel& F = c->lv[0];
-    const int64_t n = vlen(F);
-    double* s = F.b;
-    double* t = F.x;
-    double* sc = c->dscal;
-    const int64_t l0 = launch_count();
-    int64_t graph_launches = 0;
-    auto t0 = std::chrono::steady_clock::now();
-    CK(cudaEventRecord(c->ev0, c->st));
-    if (hist) hist->count = 0;
-    CK(cudaMemsetAsync(c->xs, 0, n * sizeof(double), c->st));
-    CK(cudaMemsetAsync(c->d, 0, n * sizeof(double), c->st));
-    CK(cudaMemsetAsync(sc, 0, S_COUNT * sizeof(double), c->st));
-    launch_cdot2(F.k.g, c->rhs, c->rhs, nullptr, nullptr, c->partials, sc + S_D0, c->st);
-    CK(cudaMemcpyAsync(c->hscal, sc, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->st));
-    CK(cudaStreamSynchronize(c->st));
-    const double bnorm = std::sqrt(c->hscal[0]);
-    int iters = 0;
-    int st = SMG_MAX_ITERATIONS;
-    if (bnorm == 0.0) {
-        st = SMG_CONVERGED;
-    } else {
-        c->hscal[2] = bnorm;
-        c->hscal[3] = tol;
-        CK(cudaMemcpyAsync(sc + S_BNORM, &c->hscal[2], sizeof(double), cudaMemcpyHostToDevice, c->st));
-        CK(cudaMemcpyAsync(sc + S_TOL, &c->hscal[3], sizeof(double), cudaMemcpyHostToDevice, c->st));
-        // lines 1-4 of Alg. 4 (s = b, t = V(s), q = t, first scalars): opt-in (SMG_INIT_GRAPH=1)
-        // captured once as a graph and replayed instead of ~300 eager launches; bit-identical
-        // (GPU suite green with it on), measured neutral: cfg 1 18.87 ms eager vs 18.88 ms graph
-        // (profiles/r1s5_initgraph_cfg1.txt) -- the eager launches stay ahead of the GPU
-        auto init = [&] {
-            CK(cudaMemcpyAsync(s, c->rhs, n * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
-            vcycle(c, 0, s, t);
-            CK(cudaMemcpyAsync(c->q, t, n * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
-            launch_cdot2(F.k.g, t, t, s, c->q, c->partials, sc + S_D0, c->st);
-            launch_sqmr_scalar(0, sc, c->st);
-        };
-        if (env_int("SMG_INIT_GRAPH", 0)) {
-            if (!c->init_graph) {
-                const int64_t before = launch_count();
-                CK(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeRelaxed));
-                init();
-                cudaGraph_t gr = nullptr;
-                CK(cudaStreamEndCapture(c->st, &gr));
-                CK(cudaGraphInstantiate(&c->init_graph, gr, 0));
-                CK(cudaGraphDestroy(gr));
-                c->init_kernels = launch_count() - before;
-                graph_launches -= c->init_kernels;  // capture-time launches are not executions
-            }
-            CK(cudaGraphLaunch(c->init_graph, c->st));
-            graph_launches += c->init_kernels;
-        } else {
-            init();
-        }
-        CK(cudaMemcpyAsync(c->hscal, sc + S_STATUS, sizeof(double), cudaMemcpyDeviceToHost, c->st));
-        CK(cudaStreamSynchronize(c->st));
-        if (c->hscal[0] != 0.0) st = SMG_BREAKDOWN;
-        if (st == SMG_MAX_ITERATIONS && maxit > 0 && !c->graph) {
-            const int64_t before = launch_count();
-            CK(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeRelaxed));
-            sqmr_iteration(c);
-            cudaGraph_t gr = nullptr;
-            CK(cudaStreamEndCapture(c->st, &gr));
-            CK(cudaGraphInstantiate(&c->graph, gr, 0));
-            CK(cudaGraphDestroy(gr));
-            c->graph_kernels = launch_count() - before;
-            c->graph_captured_now = true;
-        }
-        const int64_t lc0 = launch_count();
-        const bool dev_loop = st == SMG_MAX_ITERATIONS && maxit > 0 && maxit <= kLoopCap && build_loop_graph(c);
-        const int64_t loop_capture = launch_count() - lc0;  // launches recorded while building (not run)
-        if (dev_loop) {
-            const double t_start = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-            int h4[4] = {0, maxit, 0, 0};
-            static_assert(sizeof(h4) <= 4 * sizeof(double), "pinned scratch");
-            std::memcpy(&c->hscal[4], h4, sizeof(h4));
-            CK(cudaMemcpyAsync(c->dloop, &c->hscal[4], sizeof(h4), cudaMemcpyHostToDevice, c->st));
-            launch_stamp(c->dstamp, c->st);
-            CK(cudaGraphLaunch(c->loop_graph, c->st));
-            if (const int e = take_launch_error())
-                throw SmgError(SMG_ECUDA, std::string("kernel launch rejected: ") +
-                                              cudaGetErrorString(static_cast<cudaError_t>(e)));
-            CK(cudaMemcpyAsync(&c->hscal[4], c->dloop, sizeof(h4), cudaMemcpyDeviceToHost, c->st));
-            CK(cudaStreamSynchronize(c->st));
-            std::memcpy(h4, &c->hscal[4], sizeof(h4));
-            iters = h4[0];
-            const int code = h4[2];
-            std::vector<double> rel(iters);
-            std::vector<unsigned long long> stamp(iters + 1);
-            if (iters > 0) {
-                CK(cudaMemcpy(rel.data(), c->dhist, iters * sizeof(double), cudaMemcpyDeviceToHost));
-                CK(cudaMemcpy(stamp.data(), c->dstamp, (iters + 1) * sizeof(unsigned long long),
-                              cudaMemcpyDeviceToHost));
-            }
-            for (int j = 0; j < iters && hist && hist->count < hist->capacity; ++j) {
-                hist->rel_residual[hist->count] = rel[j];
-                hist->seconds[hist->count] = t_start + 1e-9 * static_cast<double>(stamp[j + 1] - stamp[0]);
-                hist->count++;
-            }
-            graph_launches += static_cast<int64_t>(iters + (code == 2 ? 1 : 0)) * (c->graph_kernels + 1);
-            // eager-launch accounting below subtracts the capture-time launches of this call
-            graph_launches -= loop_capture;
-            if (code == 2 || code == 3) st = SMG_BREAKDOWN;
-            else if (code == 1) st = SMG_CONVERGED;
-        }
-        for (int j = 1; !dev_loop && j <= maxit && st == SMG_MAX_ITERATIONS; ++j) {
-            CK(cudaGraphLaunch(c->graph, c->st));
-            graph_launches += c->graph_kernels;
-            if (const int e = take_launch_error())
-                throw SmgError(SMG_ECUDA, std::string("kernel launch rejected: ") +
-                                              cudaGetErrorString(static_cast<cudaError_t>(e)));
-            CK(cudaMemcpyAsync(c->hscal, sc + S_REL, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->st));
-            CK(cudaStreamSynchronize(c->st));
-            const double rel = c->hscal[0];
-            const int code = static_cast<int>(c->hscal[1]);
-            if (code == 2) { st = SMG_BREAKDOWN; break; }  // sigma breakdown: no residual this iteration
-            iters = j;
-            if (hist && hist->count < hist->capacity) {
-                hist->rel_residual[hist->count] = rel;
-                hist->seconds[hist->count] =
-                    std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-                hist->count++;
-            }
-            if (code == 1) st = SMG_CONVERGED;
-            else if (code == 3) st = SMG_BREAKDOWN;
-        }
-    }
-    CK(cudaEventRecord(c->ev1, c->st));
-    CK(cudaEventSynchronize(c->ev1));
-    float ms = 0.f;
-    CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
-    c->timing.solve_ms = ms;
-    c->timing.iterations = iters;
-    // eager launches of this solve (capture-time launches are not executions) + graph replays
-    const int64_t eager = (launch_count() - l0) - (c->graph_captured_now ? c->graph_kernels : 0);
-    c->timing.kernel_launches = eager + graph_launches;
-    c->graph_captured_now = false;
-    *status = st;
-    return 0;
 }
 
 // ---- host <-> device compact vectors ----
@@ -1245,27 +1028,8 @@ void dist_vcycle(smg_ctx* m, int l) {
     dist_smooth(m, l);
 }
 
-// canonical dot across parts: plane partials of every part into the shared buffer
-// (global plane indices), barrier, then the fixed-order final on every part.
-void dist_dot2(smg_ctx* m, double* (*a)(smg_ctx*), double* (*b)(smg_ctx*), double* (*c2)(smg_ctx*),
-               double* (*d)(smg_ctx*)) {
-    if (m->mp) {  // own planes' partials (zeros elsewhere), summed over ranks: x + 0 = x exactly
-        const Geom& g = m->lv[0].k.g;
-        CK(cudaMemsetAsync(m->shared_partials, 0, kPartials * sizeof(double), m->st));
-        launch_cdot_planes(g, a(m), b(m), c2 ? c2(m) : nullptr, d ? d(m) : nullptr, m->shared_partials, m->st);
-        NK(nccl().allReduce(m->shared_partials, m->shared_partials, kPartials, ncclDouble, ncclSum, m->comm, m->st));
-        launch_cdot_final(g, m->shared_partials, m->dscal + S_D0, m->st);
-        return;
-    }
-    each(m, [&](smg_ctx* p) {
-        launch_cdot_planes(p->lv[0].k.g, a(p), b(p), c2 ? c2(p) : nullptr, d ? d(p) : nullptr, m->shared_partials, p->st);
-    });
-    part_barrier(m);
-    each(m, [&](smg_ctx* p) { launch_cdot_final(p->lv[0].k.g, m->shared_partials, p->dscal + S_D0, p->st); });
-}
-
 double* v_q(smg_ctx* p) { return p->q; }
-double* v_xs(smg_ctx* p) { return p->xs; }
+double* v_xs(smg_ctx* p) { return p->xcur ? p->xs2 : p->xs; }
 double* v_rhs(smg_ctx* p) { return p->rhs; }
 double* v_s(smg_ctx* p) { return p->lv[0].b; }
 double* v_t(smg_ctx* p) { return p->lv[0].x; }
@@ -1343,9 +1107,85 @@ void dist_download(smg_ctx* m, double* (*v)(smg_ctx*), double* host) {
     each(m, [&](smg_ctx* p) { CK(cudaStreamSynchronize(p->st)); });
 }
 
-int dist_sqmr(smg_ctx* m, double tol, int maxit, smg_history* hist, int* status) {
+// ======================================================= SQMR, Alg. 4 ====
+// One code path for a single part and for the z-slab parts (m = the master context).  Per
+// iteration (lines 5-10), with the north_star's fusion of the AXPYs into the inner products:
+//   k_apply_q   q = t + beta q, t' = L q, partials of sigma = q.t'      -> final: alpha
+//   k_axpy_s    s = s - alpha t'
+//   V-cycle     t = V(s)
+//   k_cdot      partials of ||t||^2 and rho = s.t                      -> final: nu, c, tau
+//   k_apply_x   d = cd d + cq q, x = x + d, partials of ||b - L x||^2   -> final: rel, beta
+// Every scalar lives on the device; a single part replays the iteration as a CUDA graph (one
+// per parity of the q / d / x ping-pong) and reads back (rel, status) once per iteration.
+// Slab parts: block partials at global block indices are combined by a shared buffer (parts of
+// one process) or one NCCL all-reduce (one process per GPU); every part runs the same final,
+// so all parts hold identical scalars.  The fused kernels also write q, d and x on the ghost
+// planes, so only s needs a halo exchange.
+
+// where a part's block partials go
+double* part_out(smg_ctx* m, smg_ctx* p) { return (m->ndist > 0 && !m->mp) ? m->shared_partials : p->partials; }
+
+// combine the block partials of all parts, then the final + scalar update `which` on every part
+void finalize(smg_ctx* m, int which) {
+    const Geom& g = m->lv[0].k.g;
+    if (m->ndist == 0) {
+        launch_final_scalar(g, m->partials, m->dscal, which, m->st);
+        return;
+    }
+    if (m->mp) {  // own blocks' partials (zeros elsewhere) summed over ranks: x + 0 = x exactly
+        NK(nccl().allReduce(m->partials, m->shared_partials, dot_partials(g), ncclDouble, ncclSum, m->comm, m->st));
+        launch_final_scalar(g, m->shared_partials, m->dscal, which, m->st);
+        return;
+    }
+    part_barrier(m);
+    each(m, [&](smg_ctx* p) { launch_final_scalar(p->lv[0].k.g, m->shared_partials, p->dscal, which, p->st); });
+}
+
+// block partials of a.b (and c.d) on every part
+void dots(smg_ctx* m, double* (*a)(smg_ctx*), double* (*b)(smg_ctx*), double* (*c2)(smg_ctx*),
+          double* (*d)(smg_ctx*)) {
+    each(m, [&](smg_ctx* p) {
+        launch_cdot_planes(p->lv[0].k.g, a(p), b(p), c2 ? c2(p) : nullptr, d ? d(p) : nullptr, part_out(m, p), p->st);
+    });
+}
+
+void pc_vcycle(smg_ctx* m) {  // t = V(s) on the fine level
+    if (m->ndist > 0) dist_vcycle(m, 0);
+    else vcycle(m, 0, m->lv[0].b, m->lv[0].x);
+}
+
+void sqmr_iteration(smg_ctx* m, int par) {
+    auto halo = [&](smg_ctx* p, int& lo, int& hi) {
+        lo = m->ndist > 0 && p->rank > 0;
+        hi = m->ndist > 0 && p->rank + 1 < p->nparts;
+    };
+    each(m, [&](smg_ctx* p) {  // lines 9 + 5: q = t + beta q, t' = L q, sigma
+        DevLevel& F = p->lv[0];
+        int lo, hi;
+        halo(p, lo, hi);
+        launch_apply_q(F.k, F.x, par ? p->q2 : p->q, par ? p->q : p->q2, F.r, p->dscal, part_out(m, p), lo, hi, p->st);
+    });
+    finalize(m, 1);
+    each(m, [&](smg_ctx* p) { launch_axpy_s(p->lv[0].b, p->lv[0].r, p->dscal, vlen(p->lv[0]), p->st); });
+    if (m->ndist > 0) exchange_vec(m, v_s);
+    pc_vcycle(m);                   // line 6: t = V(s)
+    dots(m, v_t, v_t, v_s, v_t);    // ||t||^2, rho_j
+    finalize(m, 2);                 // nu, c, tau, cd, cq
+    each(m, [&](smg_ctx* p) {       // lines 7 + 8: d, x and the true residual
+        DevLevel& F = p->lv[0];
+        int lo, hi;
+        halo(p, lo, hi);
+        launch_apply_x(F.k, par ? p->xs2 : p->xs, par ? p->d2 : p->d, par ? p->q : p->q2, p->rhs, par ? p->xs : p->xs2,
+                       par ? p->d : p->d2, p->dscal, part_out(m, p), lo, hi, p->st);
+    });
+    finalize(m, 3);                 // rel, convergence, beta
+}
+
+int sqmr(smg_ctx* m, double tol, int maxit, smg_history* hist, int* status) {
     auto t0 = std::chrono::steady_clock::now();
     const int64_t l0 = launch_count();
+    int64_t graph_launches = 0;
+    const bool single = m->ndist == 0;
     CK(cudaEventRecord(m->ev0, m->st));
     if (hist) hist->count = 0;
     each(m, [&](smg_ctx* p) {
@@ -1353,9 +1193,11 @@ int dist_sqmr(smg_ctx* m, double tol, int maxit, smg_history* hist, int* status)
         CK(cudaMemsetAsync(p->xs, 0, n * sizeof(double), p->st));
         CK(cudaMemsetAsync(p->d, 0, n * sizeof(double), p->st));
         CK(cudaMemsetAsync(p->dscal, 0, S_COUNT * sizeof(double), p->st));
+        p->xcur = 0;
     });
-    dist_dot2(m, v_rhs, v_rhs, nullptr, nullptr);
-    CK(cudaMemcpyAsync(m->hscal, m->dscal, sizeof(double), cudaMemcpyDeviceToHost, m->st));
+    dots(m, v_rhs, v_rhs, nullptr, nullptr);
+    finalize(m, -1);
+    CK(cudaMemcpyAsync(m->hscal, m->dscal + S_D0, sizeof(double), cudaMemcpyDeviceToHost, m->st));
     each(m, [&](smg_ctx* p) { CK(cudaStreamSynchronize(p->st)); });
     const double bnorm = std::sqrt(m->hscal[0]);
     int st = SMG_MAX_ITERATIONS, iters = 0;
@@ -1364,67 +1206,68 @@ int dist_sqmr(smg_ctx* m, double tol, int maxit, smg_history* hist, int* status)
     } else {
         m->hscal[2] = bnorm;
         m->hscal[3] = tol;
-        each(m, [&](smg_ctx* p) {
+        each(m, [&](smg_ctx* p) {  // lines 1-4: s = b, t = V(s), q = t, tau, rho
             CK(cudaMemcpyAsync(p->dscal + S_BNORM, &m->hscal[2], sizeof(double), cudaMemcpyHostToDevice, p->st));
             CK(cudaMemcpyAsync(p->dscal + S_TOL, &m->hscal[3], sizeof(double), cudaMemcpyHostToDevice, p->st));
             CK(cudaMemcpyAsync(v_s(p), p->rhs, vlen(p->lv[0]) * sizeof(double), cudaMemcpyDeviceToDevice, p->st));
         });
-        exchange_vec(m, v_s);
-        dist_vcycle(m, 0);
+        if (m->ndist > 0) exchange_vec(m, v_s);
+        pc_vcycle(m);
         each(m, [&](smg_ctx* p) {
             CK(cudaMemcpyAsync(p->q, v_t(p), vlen(p->lv[0]) * sizeof(double), cudaMemcpyDeviceToDevice, p->st));
         });
-        dist_dot2(m, v_t, v_t, v_s, v_q);
-        each(m, [&](smg_ctx* p) { launch_sqmr_scalar(0, p->dscal, p->st); });
+        dots(m, v_t, v_t, v_s, v_q);
+        finalize(m, 0);
         CK(cudaMemcpyAsync(m->hscal, m->dscal + S_STATUS, sizeof(double), cudaMemcpyDeviceToHost, m->st));
-        CK(cudaStreamSynchronize(m->st));
+        each(m, [&](smg_ctx* p) { CK(cudaStreamSynchronize(p->st)); });
         if (m->hscal[0] != 0.0) st = SMG_BREAKDOWN;
+        if (single && st == SMG_MAX_ITERATIONS && maxit > 0 && !m->graph) {
+            for (int par = 0; par < 2; ++par) {
+                const int64_t before = launch_count();
+                CK(cudaStreamBeginCapture(m->st, cudaStreamCaptureModeRelaxed));
+                sqmr_iteration(m, par);
+                cudaGraph_t gr = nullptr;
+                CK(cudaStreamEndCapture(m->st, &gr));
+                CK(cudaGraphInstantiate(par ? &m->graph2 : &m->graph, gr, 0));
+                CK(cudaGraphDestroy(gr));
+                m->graph_kernels = launch_count() - before;
+                graph_launches -= m->graph_kernels;  // capture-time launches are not executions
+            }
+        }
         for (int j = 1; j <= maxit && st == SMG_MAX_ITERATIONS; ++j) {
-            exchange_vec(m, v_q);
-            each(m, [&](smg_ctx* p) { launch_apply(p->lv[0].k, p->q, nullptr, v_t(p), 0.0, p->st); });
-            dist_dot2(m, v_q, v_t, nullptr, nullptr);
-            each(m, [&](smg_ctx* p) {
-                const int64_t n = vlen(p->lv[0]);
-                launch_sqmr_scalar(1, p->dscal, p->st);
-                launch_axpy_s(v_s(p), v_t(p), p->dscal, n, p->st);
-            });
-            exchange_vec(m, v_s);
-            dist_vcycle(m, 0);
-            dist_dot2(m, v_t, v_t, v_s, v_t);
-            each(m, [&](smg_ctx* p) {
-                launch_sqmr_scalar(2, p->dscal, p->st);
-                launch_dx_dev(p->d, p->xs, p->q, p->dscal, vlen(p->lv[0]), p->st);
-            });
-            exchange_vec(m, v_xs);
-            each(m, [&](smg_ctx* p) { launch_apply(p->lv[0].k, p->xs, p->rhs, v_r(p), 0.0, p->st); });
-            dist_dot2(m, v_r, v_r, nullptr, nullptr);
-            each(m, [&](smg_ctx* p) {
-                launch_sqmr_scalar(3, p->dscal, p->st);
-                launch_xpby_dev(p->q, v_t(p), p->dscal, vlen(p->lv[0]), p->st);
-            });
+            const int par = (j - 1) & 1;
+            if (single) {
+                CK(cudaGraphLaunch(par ? m->graph2 : m->graph, m->st));
+                graph_launches += m->graph_kernels;
+            } else {
+                sqmr_iteration(m, par);
+            }
+            if (const int e = take_launch_error())
+                throw SmgError(SMG_ECUDA, std::string("kernel launch rejected: ") +
+                                              cudaGetErrorString(static_cast<cudaError_t>(e)));
             CK(cudaMemcpyAsync(m->hscal, m->dscal + S_REL, 2 * sizeof(double), cudaMemcpyDeviceToHost, m->st));
             each(m, [&](smg_ctx* p) { CK(cudaStreamSynchronize(p->st)); });
             const double rel = m->hscal[0];
             const int code = static_cast<int>(m->hscal[1]);
-            if (code == 2) { st = SMG_BREAKDOWN; break; }
+            if (code == 2) { st = SMG_BREAKDOWN; break; }  // sigma breakdown: no residual this iteration
             iters = j;
             if (hist && hist->count < hist->capacity) {
                 hist->rel_residual[hist->count] = rel;
-                hist->seconds[hist->count] =
-                    std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+                hist->seconds[hist->count] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
                 hist->count++;
             }
             if (code == 1) st = SMG_CONVERGED;
             else if (code == 3) st = SMG_BREAKDOWN;
         }
     }
+    each(m, [&](smg_ctx* p) { p->xcur = iters & 1; });  // iteration j wrote buffer [j & 1]
     CK(cudaEventRecord(m->ev1, m->st));
     CK(cudaEventSynchronize(m->ev1));
     float ms = 0.f;
     CK(cudaEventElapsedTime(&ms, m->ev0, m->ev1));
     m->timing.solve_ms = ms;
     m->timing.iterations = iters;
-    m->timing.kernel_launches = launch_count() - l0;
+    m->timing.kernel_launches = (launch_count() - l0) + graph_launches;
     *status = st;
     return 0;
 }
@@ -1511,6 +1354,7 @@ static int slab_levels(const smg_grid_desc* grid, int levels, int nparts, int64_
         // always sit in one slab, so restriction into a slab (or into the replicated first
         // level, coarse planes z0/2 .. (z0 + nzl)/2) covers every coarse plane
         if (nz % nparts || nz / nparts < 2 || (nz / nparts) % 2) break;
+        if (l == 0 && (nz / nparts) % kDotZBlock) break;  // inner-product blocks never straddle parts
         nd = l + 1;
     }
     return nd;
@@ -1582,7 +1426,7 @@ int smg_create(const smg_grid_desc* grid, const smg_params* params, int ngpu, co
             c->owned.push_back(std::move(q));
         }
         CK(cudaSetDevice(c->device));
-        if (ngpu > 1) c->shared_partials = c->dalloc<double>(kPartials);
+        if (ngpu > 1) c->shared_partials = c->dalloc<double>(dot_partials(c->lv[0].k.g));
     });
     if (rc != 0) {
         std::fprintf(stderr, "smg_create: %s\n", c->err.c_str());
@@ -1636,7 +1480,7 @@ int smg_create_rank(const smg_grid_desc* grid, const smg_params* params, int ran
             ncclUniqueId u;
             std::memcpy(&u, id, sizeof(u));
             NK(nccl().commInitRank(&c->comm, nranks, u, rank));
-            c->shared_partials = c->dalloc<double>(kPartials);
+            c->shared_partials = c->dalloc<double>(dot_partials(c->lv[0].k.g));
         }
     });
     if (rc != 0) {
@@ -1847,15 +1691,14 @@ int smg_solve_resident(smg_ctx* c, double tol, int maxit, smg_history* hist, int
     return guard(c, [&] {
         if (!c->rhs_set) throw SmgError(SMG_EINVAL, "smg_set_rhs not called");
         if (!status) throw SmgError(SMG_EINVAL, "status is null");
-        if (c->ndist > 0) dist_sqmr(c, tol, maxit, hist, status);
-        else sqmr(c, tol, maxit, hist, status);
+        sqmr(c, tol, maxit, hist, status);
     });
 }
 
 int smg_get_solution(smg_ctx* c, double* x) {
     return guard(c, [&] {
         if (c->ndist > 0) dist_download(c, v_xs, x);
-        else download(c, 0, c->xs, x);
+        else download(c, 0, v_xs(c), x);
     });
 }
 
@@ -1865,7 +1708,7 @@ int smg_sqmr_solve(smg_ctx* c, const double* b, double* x, double tol, int maxit
         if (c->ndist > 0) {
             dist_upload(c, b, v_rhs);
             c->rhs_set = true;
-            dist_sqmr(c, tol, maxit, hist, status);
+            sqmr(c, tol, maxit, hist, status);
             dist_download(c, v_xs, x);
             return;
         }
@@ -1878,7 +1721,7 @@ int smg_sqmr_solve(smg_ctx* c, const double* b, double* x, double tol, int maxit
         c->rhs_set = true;
         sqmr(c, tol, maxit, hist, status);
         CK(cudaEventRecord(c->ev0, c->st));
-        download(c, 0, c->xs, x);
+        download(c, 0, v_xs(c), x);
         CK(cudaEventRecord(c->ev1, c->st));
         CK(cudaEventSynchronize(c->ev1));
         float d2h = 0.f;

@@ -543,65 +543,216 @@ __global__ void k_pack(LevelK L, const double* __restrict__ X, double* __restric
 // ------------------------------------------------------------- BLAS-1 ------
 constexpr int RED_T = 256;
 
-// Canonical inner product (OD-12) — bit-identical to the oracle:
-// block (z, field): each warp owns rows y (stride 8); lane l accumulates
-// x = l, l+32, ... ascending; lanes combine through the shuffle-down tree
-// (o = 16..1); row sums are added in ascending y by one thread; plane sums
-// are reduced by k_cdot_final with the same 32-lane scheme.
-constexpr int kMaxPlanes = 4 * 1025 + 4;
+// Canonical inner product (OD-12 rev. 2) -- the order the fused SQMR kernels
+// produce natively, restated by the oracle (cdot in oracle/stokes_oracle.cpp):
+//   * a block is 32 x-lanes by 8 y-rows of one z-block of kDotZB planes (the k_apply grid);
+//   * a thread adds, over its cell's planes in ascending z, ((p_u + p_v) + p_w) + p_p, the
+//     products of the four fields at the cell's slot (inactive slots hold 0: product +0);
+//   * the 32 lanes of a row combine by the shuffle-down tree (o = 16..1), the 8 row sums are
+//     added in ascending row order into the block partial, stored at the global block index
+//     ((zb * GY + by) * GX + bx) -- so z-slab parts fill disjoint entries;
+//   * k_final: thread t of 256 adds partials t, t + 256, ... in ascending order, then the
+//     shuffle-down tree per warp, then the 8 warp sums in ascending order.
+constexpr int kDotZB = kDotZBlock;
+__device__ __forceinline__ double cell4(double pu, double pv, double pw, double pp) { return ((pu + pv) + pw) + pp; }
+
+// block partials of up to two products, written to part[blk] and part[nblk + blk]
+__device__ __forceinline__ void block_partial2(double v0, double v1, double* __restrict__ part, int64_t nblk,
+                                               int64_t blk) {
+    __shared__ double ws0[8], ws1[8];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        v0 = v0 + __shfl_down_sync(0xffffffffu, v0, o);
+        v1 = v1 + __shfl_down_sync(0xffffffffu, v1, o);
+    }
+    if (threadIdx.x == 0) {
+        ws0[threadIdx.y] = v0;
+        ws1[threadIdx.y] = v1;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && threadIdx.y == 0) {
+        double s0 = ws0[0], s1 = ws1[0];
+#pragma unroll
+        for (int w = 1; w < 8; ++w) {
+            s0 = s0 + ws0[w];
+            s1 = s1 + ws1[w];
+        }
+        part[blk] = s0;
+        part[nblk + blk] = s1;
+    }
+}
+// global block index of this CTA; grid (GX, GY, local z-blocks), slab parts start on a z-block
+__device__ __forceinline__ int64_t dot_blk(const Geom& g) {
+    const int64_t GX = gridDim.x, GY = gridDim.y;
+    const int64_t zb = blockIdx.z + g.z0 / kDotZB;
+    return (zb * GY + blockIdx.y) * GX + blockIdx.x;
+}
+__host__ __device__ inline int64_t dot_nblk(const Geom& g) {
+    return static_cast<int64_t>((g.nx + 31) / 32) * ((g.ny + 7) / 8) * ((g.gnz + kDotZB - 1) / kDotZB);
+}
+
 __global__ void __launch_bounds__(RED_T) k_cdot(Geom g, const double* __restrict__ a, const double* __restrict__ b,
                                                 const double* __restrict__ c, const double* __restrict__ d,
                                                 double* __restrict__ partials) {
     pdl_wait();
-    __shared__ double rows0[1040], rows1[1040];
-    const int z = blockIdx.x, f = blockIdx.y;
-    // local planes; the slab holding the global top plane also owns the top w wall plane
-    const int ex = g.nx + (f == 0), ey = g.ny + (f == 1);
-    const int ez = g.nz + ((f == 2 && g.z0 + g.nz == g.gnz) ? 1 : 0);
-    if (z >= ez) return;
-    const int q = f * g.gnz + (f == 3 ? 1 : 0) + g.gz(z);  // global plane index: u gnz, v gnz, w gnz+1, p gnz
-    const int64_t off = f * g.fs;
-    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-    for (int y = w; y < ey; y += RED_T / 32) {
-        const int64_t row = off + g.slot(0, y, z);
-        double s0 = 0.0, s1 = 0.0;
-        // unrolled: loads of several chunks in flight, additions still in ascending x
-#pragma unroll 4
-        for (int x = l; x < ex; x += 32) {
-            s0 = s0 + a[row + x] * b[row + x];
-            if (c) s1 = s1 + c[row + x] * d[row + x];
+    const int x = blockIdx.x * 32 + threadIdx.x, y = blockIdx.y * 8 + threadIdx.y;
+    const int zl = blockIdx.z * kDotZB, zh = min(g.nz, zl + kDotZB);
+    const int64_t fs = g.fs;
+    double v0 = 0.0, v1 = 0.0;
+    if (x < g.nx && y < g.ny)
+        for (int z = zl; z < zh; ++z) {
+            const int64_t i = g.slot(x, y, z);
+            v0 = v0 + cell4(a[i] * b[i], a[fs + i] * b[fs + i], a[2 * fs + i] * b[2 * fs + i],
+                            a[3 * fs + i] * b[3 * fs + i]);
+            if (c)
+                v1 = v1 + cell4(c[i] * d[i], c[fs + i] * d[fs + i], c[2 * fs + i] * d[2 * fs + i],
+                                c[3 * fs + i] * d[3 * fs + i]);
         }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            s0 = s0 + __shfl_down_sync(0xffffffffu, s0, o);
-            s1 = s1 + __shfl_down_sync(0xffffffffu, s1, o);
-        }
-        if (l == 0) {
-            rows0[y] = s0;
-            rows1[y] = s1;
-        }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double p0 = 0.0, p1 = 0.0;
-        for (int y = 0; y < ey; ++y) {
-            p0 = p0 + rows0[y];
-            p1 = p1 + rows1[y];
-        }
-        partials[q] = p0;
-        partials[kMaxPlanes + q] = p1;
-    }
+    block_partial2(v0, v1, partials, dot_nblk(g), dot_blk(g));
 }
 
-__global__ void k_cdot_final(const double* __restrict__ partials, int nq, double* __restrict__ out) {
-    pdl_wait();
-    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-    const double* p = partials + w * kMaxPlanes;
-    double s = 0.0;
-    for (int k = l; k < nq; k += 32) s = s + p[k];
+// the final combination of nblk partials (two products); result to out[0], out[1]
+__device__ __forceinline__ void final2(const double* __restrict__ part, int64_t nblk, double* out) {
+    __shared__ double ws0[8], ws1[8];
+    const int t = threadIdx.x;
+    double s0 = 0.0, s1 = 0.0;
+    for (int64_t k = t; k < nblk; k += 256) {
+        s0 = s0 + part[k];
+        s1 = s1 + part[nblk + k];
+    }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s = s + __shfl_down_sync(0xffffffffu, s, o);
-    if (l == 0) out[w] = s;
+    for (int o = 16; o > 0; o >>= 1) {
+        s0 = s0 + __shfl_down_sync(0xffffffffu, s0, o);
+        s1 = s1 + __shfl_down_sync(0xffffffffu, s1, o);
+    }
+    if ((t & 31) == 0) {
+        ws0[t >> 5] = s0;
+        ws1[t >> 5] = s1;
+    }
+    __syncthreads();
+    if (t == 0) {
+        double a = ws0[0], b = ws1[0];
+#pragma unroll
+        for (int w = 1; w < 8; ++w) {
+            a = a + ws0[w];
+            b = b + ws1[w];
+        }
+        out[0] = a;
+        out[1] = b;
+    }
+}
+__global__ void __launch_bounds__(256) k_cdot_final(const double* __restrict__ partials, int64_t nblk,
+                                                    double* __restrict__ out) {
+    pdl_wait();
+    final2(partials, nblk, out);
+}
+
+// ---- fused SQMR steps (Alg. 4; north_star: AXPYs fused with the inner products) ----
+// Accessors evaluating a vector update on the fly at any slot, with the oracle's per-element
+// expressions: q_new = t + beta q (line 9), x_new = x + (cd d + cq q) (line 7).  The stencils
+// read them at radius 1; each thread stores the new values of its own cell only.
+struct QNew {
+    const double* __restrict__ T;
+    const double* __restrict__ Q;
+    double beta;
+    __device__ __forceinline__ double operator[](int64_t i) const { return T[i] + beta * Q[i]; }
+    __device__ __forceinline__ QNew operator+(int64_t o) const { return QNew{T + o, Q + o, beta}; }
+};
+struct XNew {
+    const double* __restrict__ X;
+    const double* __restrict__ D;
+    const double* __restrict__ Q;
+    double cd, cq;
+    __device__ __forceinline__ double dnew(int64_t i) const { return cd * D[i] + cq * Q[i]; }
+    __device__ __forceinline__ double operator[](int64_t i) const { return X[i] + dnew(i); }
+    __device__ __forceinline__ XNew operator+(int64_t o) const { return XNew{X + o, D + o, Q + o, cd, cq}; }
+};
+
+// Lines 9 + 5 of iteration j: q = t + beta q (written to Q1), t = L q (to Tn), sigma = q.t as
+// block partials.  Grid = the dot grid; on slab parts with a neighbour below / above, the
+// first / last z-block also writes q on the ghost plane -1 / nz (its inputs are valid there),
+// so the next iteration needs no exchange of q.
+__global__ void __launch_bounds__(256) k_apply_q(LevelK L, const double* __restrict__ T,
+                                                 const double* __restrict__ Q0, double* __restrict__ Q1,
+                                                 double* __restrict__ Tn, const double* __restrict__ sc,
+                                                 double* __restrict__ partials, int halo_lo, int halo_hi) {
+    pdl_wait();
+    if (sc[S_STATUS] != 0.0) return;
+    const Geom& g = L.g;
+    const int64_t fs = g.fs;
+    const QNew X{T, Q0, sc[S_BETA]};
+    const QNew U = X, V = X + fs, W = X + 2 * fs, P = X + 3 * fs;
+    const int x = blockIdx.x * 32 + threadIdx.x, y = blockIdx.y * 8 + threadIdx.y;
+    const int zl = blockIdx.z * kDotZB, zh = min(g.nz, zl + kDotZB);
+    double v = 0.0;
+    const bool in = x < g.nx && y < g.ny;
+    if (in) {
+        auto put_q = [&](int64_t i) {
+#pragma unroll
+            for (int f = 0; f < 4; ++f) Q1[f * fs + i] = X[f * fs + i];
+        };
+        if (halo_lo && blockIdx.z == 0) put_q(g.slot(x, y, -1));
+        if (halo_hi && zh == g.nz) put_q(g.slot(x, y, g.nz));
+        for (int z = zl; z < zh; ++z) {
+            const int64_t i = g.slot(x, y, z);
+            const double qu = U[i], qv = V[i], qw = W[i], qp = P[i];
+            double tu = 0.0, tv = 0.0, tw = 0.0;
+            if (x >= 1) Tn[i] = tu = mom(L, U, P, i, 1);
+            if (y >= 1) Tn[fs + i] = tv = mom(L, V, P, i, g.sy);
+            if (g.gz(z) >= 1) Tn[2 * fs + i] = tw = mom(L, W, P, i, g.sz);
+            const double tp = cont(L, U, V, W, P, i, 0.0);
+            Tn[3 * fs + i] = tp;
+            Q1[i] = qu;
+            Q1[fs + i] = qv;
+            Q1[2 * fs + i] = qw;
+            Q1[3 * fs + i] = qp;
+            v = v + cell4(qu * tu, qv * tv, qw * tw, qp * tp);
+        }
+    }
+    block_partial2(v, 0.0, partials, dot_nblk(g), dot_blk(g));
+}
+
+// Lines 7 + 8 of iteration j: d = cd d + cq q, x = x + d (written to D1, X1), then the true
+// residual r = b - L x as block partials of ||r||^2 (r itself is never stored).  Ghost planes
+// as in k_apply_q.
+__global__ void __launch_bounds__(256) k_apply_x(LevelK L, const double* __restrict__ X0,
+                                                 const double* __restrict__ D0, const double* __restrict__ Q,
+                                                 const double* __restrict__ B, double* __restrict__ X1,
+                                                 double* __restrict__ D1, const double* __restrict__ sc,
+                                                 double* __restrict__ partials, int halo_lo, int halo_hi) {
+    pdl_wait();
+    if (sc[S_STATUS] != 0.0) return;
+    const Geom& g = L.g;
+    const int64_t fs = g.fs;
+    const XNew X{X0, D0, Q, sc[S_CD], sc[S_CQ]};
+    const XNew U = X, V = X + fs, W = X + 2 * fs, P = X + 3 * fs;
+    const int x = blockIdx.x * 32 + threadIdx.x, y = blockIdx.y * 8 + threadIdx.y;
+    const int zl = blockIdx.z * kDotZB, zh = min(g.nz, zl + kDotZB);
+    double v = 0.0;
+    const bool in = x < g.nx && y < g.ny;
+    if (in) {
+        auto put_xd = [&](int64_t i) {
+#pragma unroll
+            for (int f = 0; f < 4; ++f) {
+                const double dn = X.dnew(f * fs + i);
+                D1[f * fs + i] = dn;
+                X1[f * fs + i] = X0[f * fs + i] + dn;
+            }
+        };
+        if (halo_lo && blockIdx.z == 0) put_xd(g.slot(x, y, -1));
+        if (halo_hi && zh == g.nz) put_xd(g.slot(x, y, g.nz));
+        for (int z = zl; z < zh; ++z) {
+            const int64_t i = g.slot(x, y, z);
+            double ru = 0.0, rv = 0.0, rw = 0.0;
+            if (x >= 1) ru = B[i] - mom(L, U, P, i, 1);
+            if (y >= 1) rv = B[fs + i] - mom(L, V, P, i, g.sy);
+            if (g.gz(z) >= 1) rw = B[2 * fs + i] - mom(L, W, P, i, g.sz);
+            const double rp = B[3 * fs + i] - cont(L, U, V, W, P, i, 0.0);
+            put_xd(i);
+            v = v + cell4(ru * ru, rv * rv, rw * rw, rp * rp);
+        }
+    }
+    block_partial2(v, 0.0, partials, dot_nblk(g), dot_blk(g));
 }
 
 __global__ void k_axpy(double* __restrict__ y, const double* __restrict__ x, double alpha, int64_t n) {
@@ -1523,40 +1674,16 @@ __global__ void __launch_bounds__(256, SMG_PREV_MINB) k_dgs_prev_c(LevelK L, dou
 // Alg. 4 scalar recurrences evaluated on the device (same expressions and
 // order as the oracle), so one SQMR iteration is a fixed kernel sequence that
 // can be replayed as a CUDA graph.  sc[] layout: see SqmrSlot in smg_internal.h.
-__global__ void k_sqmr_first(double* sc) {  // after dot2(t,t, s,q) of the initial V-cycle
-    pdl_wait();
-    sc[S_TAU] = sqrt(sc[S_D0]);
-    sc[S_NUOLD] = 0.0;
-    sc[S_RHO] = sc[S_D1];
-    sc[S_STATUS] = fabs(sc[S_RHO]) < 1e-300 ? 2.0 : 0.0;
-}
+
 __device__ __forceinline__ void sqmr_alpha(double* sc) {  // after sigma = q.t
     if (sc[S_STATUS] != 0.0) return;
     const double sigma = sc[S_D0];
     if (fabs(sigma) < 1e-300) { sc[S_STATUS] = 2.0; return; }
     sc[S_ALPHA] = sc[S_RHO] / sigma;
 }
-__global__ void k_sqmr_alpha(double* sc) {
-    pdl_wait();
-    sqmr_alpha(sc);
-}
-__global__ void k_sqmr_nu(double* sc) {  // after ||t||^2 and rho_j = s.t
-    pdl_wait();
-    if (sc[S_STATUS] != 0.0) return;
-    const double nu = sqrt(sc[S_D0]) / sc[S_TAU];
-    const double c = 1.0 / sqrt(1.0 + nu * nu);
-    sc[S_TAU] = sc[S_TAU] * nu * c;
-    const double c2 = c * c;
-    sc[S_CD] = c2 * (sc[S_NUOLD] * sc[S_NUOLD]);
-    sc[S_CQ] = c2 * sc[S_ALPHA];
-    sc[S_NU] = nu;
-    sc[S_RHONEW] = sc[S_D1];
-}
-__device__ __forceinline__ void sqmr_beta(double* sc);
-__global__ void k_sqmr_beta(double* sc) {
-    pdl_wait();
-    sqmr_beta(sc);
-}
+
+
+
 __device__ __forceinline__ void sqmr_beta(double* sc) {  // after ||b - L x||^2
     if (sc[S_STATUS] != 0.0) return;
     const double rel = sqrt(sc[S_D0]) / sc[S_BNORM];
@@ -1569,6 +1696,37 @@ __device__ __forceinline__ void sqmr_beta(double* sc) {  // after ||b - L x||^2
     sc[S_NUOLD] = sc[S_NU];
 }
 
+// final combination of the block partials into sc[S_D0], sc[S_D1], then the Alg. 4 scalar update
+// `which` (0 first: tau, rho; 1 alpha; 2 nu, c, tau, cd, cq; 3 rel, convergence, beta; -1 none)
+__device__ __forceinline__ void sqmr_first(double* sc) {
+    sc[S_TAU] = sqrt(sc[S_D0]);
+    sc[S_NUOLD] = 0.0;
+    sc[S_RHO] = sc[S_D1];
+    sc[S_STATUS] = fabs(sc[S_RHO]) < 1e-300 ? 2.0 : 0.0;
+}
+__device__ __forceinline__ void sqmr_nu(double* sc) {
+    if (sc[S_STATUS] != 0.0) return;
+    const double nu = sqrt(sc[S_D0]) / sc[S_TAU];
+    const double c = 1.0 / sqrt(1.0 + nu * nu);
+    sc[S_TAU] = sc[S_TAU] * nu * c;
+    const double c2 = c * c;
+    sc[S_CD] = c2 * (sc[S_NUOLD] * sc[S_NUOLD]);
+    sc[S_CQ] = c2 * sc[S_ALPHA];
+    sc[S_NU] = nu;
+    sc[S_RHONEW] = sc[S_D1];
+}
+__global__ void __launch_bounds__(256) k_final_scalar(const double* __restrict__ partials, int64_t nblk,
+                                                      double* __restrict__ sc, int which) {
+    pdl_wait();
+    if (which > 0 && sc[S_STATUS] != 0.0) return;
+    final2(partials, nblk, sc + S_D0);
+    if (threadIdx.x != 0) return;
+    if (which == 0) sqmr_first(sc);
+    else if (which == 1) sqmr_alpha(sc);
+    else if (which == 2) sqmr_nu(sc);
+    else if (which == 3) sqmr_beta(sc);
+}
+
 __global__ void k_axpy_s(double* __restrict__ s, const double* __restrict__ t, const double* __restrict__ sc,
                          int64_t n) {  // s = s - alpha t
     pdl_wait();
@@ -1576,25 +1734,6 @@ __global__ void k_axpy_s(double* __restrict__ s, const double* __restrict__ t, c
     const double a = sc[S_ALPHA];
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
         s[k] = s[k] - a * t[k];
-}
-__global__ void k_dx_dev(double* __restrict__ d, double* __restrict__ x, const double* __restrict__ q,
-                         const double* __restrict__ sc, int64_t n) {  // d = cd d + cq q; x += d
-    pdl_wait();
-    if (sc[S_STATUS] != 0.0) return;
-    const double cd = sc[S_CD], cq = sc[S_CQ];
-    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
-        const double dn = cd * d[k] + cq * q[k];
-        d[k] = dn;
-        x[k] = x[k] + dn;
-    }
-}
-__global__ void k_xpby_dev(double* __restrict__ q, const double* __restrict__ t, const double* __restrict__ sc,
-                           int64_t n) {  // q = t + beta q
-    pdl_wait();
-    if (sc[S_STATUS] != 0.0) return;
-    const double b = sc[S_BETA];
-    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
-        q[k] = t[k] + b * q[k];
 }
 
 // ------------------------------------------- tile-ordered DGS (large levels) ------
@@ -2228,20 +2367,36 @@ void launch_unpack(const LevelK& L, const double* compact, double* padded, cudaS
     launch_k(k_pack, cell_grid(L.g), dim3(BX, BY), 0, s, L, padded, const_cast<double*>(compact), 1);
     count();
 }
+static dim3 dot_grid(const Geom& g) {
+    return dim3((g.nx + 31) / 32, (g.ny + 7) / 8, (g.nz + kDotZB - 1) / kDotZB);
+}
+int64_t dot_partials(const Geom& g) { return 2 * dot_nblk(g); }
 void launch_cdot_planes(const Geom& g, const double* a, const double* b, const double* c, const double* d,
                         double* partials, cudaStream_t s) {
-    launch_k(k_cdot, dim3(g.nz + 1, 4), RED_T, 0, s, g, a, b, c, d, partials);
+    launch_k(k_cdot, dot_grid(g), dim3(32, 8), 0, s, g, a, b, c, d, partials);
     count();
 }
 void launch_cdot_final(const Geom& g, const double* partials, double* out, cudaStream_t s) {
-    launch_k(k_cdot_final, 1, 64, 0, s, partials, 4 * g.gnz + 1, out);
+    launch_k(k_cdot_final, 1, 256, 0, s, partials, dot_nblk(g), out);
     count();
 }
 void launch_cdot2(const Geom& g, const double* a, const double* b, const double* c, const double* d,
                   double* partials, double* out, cudaStream_t s) {
-    launch_k(k_cdot, dim3(g.nz + 1, 4), RED_T, 0, s, g, a, b, c, d, partials);
-    launch_k(k_cdot_final, 1, 64, 0, s, partials, 4 * g.gnz + 1, out);
+    launch_cdot_planes(g, a, b, c, d, partials, s);
+    launch_cdot_final(g, partials, out, s);
+}
+void launch_final_scalar(const Geom& g, const double* partials, double* sc, int which, cudaStream_t s) {
+    launch_k(k_final_scalar, 1, 256, 0, s, partials, dot_nblk(g), sc, which);
     count();
+}
+void launch_apply_q(const LevelK& L, const double* t, const double* q0, double* q1, double* tn, const double* sc,
+                    double* partials, int halo_lo, int halo_hi, cudaStream_t s) {
+    launch_k(k_apply_q, dot_grid(L.g), dim3(32, 8), 0, s, L, t, q0, q1, tn, sc, partials, halo_lo, halo_hi);
+    count();
+}
+void launch_apply_x(const LevelK& L, const double* x0, const double* d0, const double* q, const double* b, double* x1,
+                    double* d1, const double* sc, double* partials, int halo_lo, int halo_hi, cudaStream_t s) {
+    launch_k(k_apply_x, dot_grid(L.g), dim3(32, 8), 0, s, L, x0, d0, q, b, x1, d1, sc, partials, halo_lo, halo_hi);
     count();
 }
 static int env_int(const char* name, int dflt) {
@@ -2620,61 +2775,8 @@ void launch_vanka_additive(const LevelK& L, double* x, const double* b, const in
     count();
 }
 
-// Device-side SQMR loop (the body of a WHILE conditional graph node, after one captured
-// iteration): records rel into the device history with a globaltimer stamp and keeps the loop
-// running while the status code is 0 and fewer than loop[1] (maxit) iterations ran.  Mirrors the
-// host loop: code 2 (sigma breakdown) records nothing; codes 1 / 3 record the iteration and stop.
-// loop = {iterations, maxit, last code}.
-__global__ void k_sqmr_loop_ctl(cudaGraphConditionalHandle h, const double* __restrict__ sc, double* hist,
-                                unsigned long long* stamp, int* loop) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    const int code = static_cast<int>(sc[S_STATUS]);
-    loop[2] = code;
-    if (code == 2) {
-        cudaGraphSetConditional(h, 0u);
-        return;
-    }
-    const int j = loop[0] + 1;
-    hist[j - 1] = sc[S_REL];
-    stamp[j] = t;
-    loop[0] = j;
-    cudaGraphSetConditional(h, (code == 0 && j < loop[1]) ? 1u : 0u);
-}
-__global__ void k_stamp(unsigned long long* stamp) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    stamp[0] = t;
-}
-void launch_sqmr_loop_ctl(cudaGraphConditionalHandle h, const double* sc, double* hist, unsigned long long* stamp,
-                          int* loop, cudaStream_t s) {
-    k_sqmr_loop_ctl<<<1, 1, 0, s>>>(h, sc, hist, stamp, loop);
-    count();
-}
-void launch_stamp(unsigned long long* stamp, cudaStream_t s) {
-    k_stamp<<<1, 1, 0, s>>>(stamp);
-    count();
-}
-
-void launch_sqmr_scalar(int which, double* sc, cudaStream_t s) {
-    switch (which) {
-        case 0: launch_k(k_sqmr_first, 1, 1, 0, s, sc); break;
-        case 1: launch_k(k_sqmr_alpha, 1, 1, 0, s, sc); break;
-        case 2: launch_k(k_sqmr_nu, 1, 1, 0, s, sc); break;
-        default: launch_k(k_sqmr_beta, 1, 1, 0, s, sc); break;
-    }
-    count();
-}
 void launch_axpy_s(double* s_, const double* t, const double* sc, int64_t n, cudaStream_t s) {
     launch_k(k_axpy_s, stream_blocks(n), 256, 0, s, s_, t, sc, n);
-    count();
-}
-void launch_dx_dev(double* d, double* x, const double* q, const double* sc, int64_t n, cudaStream_t s) {
-    launch_k(k_dx_dev, stream_blocks(n), 256, 0, s, d, x, q, sc, n);
-    count();
-}
-void launch_xpby_dev(double* q, const double* t, const double* sc, int64_t n, cudaStream_t s) {
-    launch_k(k_xpby_dev, stream_blocks(n), 256, 0, s, q, t, sc, n);
     count();
 }
 void launch_axpy(double* y, const double* x, double alpha, int64_t n, cudaStream_t s) {

@@ -125,18 +125,28 @@ void launch_pack(const LevelK& L, const double* padded, double* compact, cudaStr
 void launch_unpack(const LevelK& L, const double* compact, double* padded, cudaStream_t s);
 
 // ---- BLAS-1 (kernels.cu); n = padded vector length (multiple of 32) ----
-constexpr int kPartials = 2 * (4 * 1025 + 4);  // scratch doubles for launch_cdot2
-// Canonical (bit-reproducible, oracle-identical) a.b and, if c != nullptr,
-// c.d over the level geometry g -> out[0], out[1] on the device.  nz <= 1024.
+// Canonical inner products (OD-12 rev. 2): block partials over 32 x 8 cells x
+// 4 planes at global block indices, then one fixed-order final.  dot_partials(g): doubles of a
+// partial buffer for the fine level (two products).
+int64_t dot_partials(const Geom& g);
+constexpr int kDotZBlock = 4;  // planes per dot block: fine-level slabs start and end on a z-block
+// a.b and, if c != nullptr, c.d -> out[0], out[1] on the device
 void launch_cdot2(const Geom& g, const double* a, const double* b, const double* c, const double* d,
                   double* partials, double* out, cudaStream_t s);
-// The two halves of launch_cdot2: per-plane partials of this slab's planes (at
-// global plane indices, kMaxPlanes apart for the second product), and the
-// final fixed-order combination of all 4 gnz + 1 planes.
-constexpr int kMaxPlanesStride = 4 * 1025 + 4;
+// the two halves of launch_cdot2: this part's block partials, and the final over all blocks
 void launch_cdot_planes(const Geom& g, const double* a, const double* b, const double* c, const double* d,
                         double* partials, cudaStream_t s);
 void launch_cdot_final(const Geom& g, const double* partials, double* out, cudaStream_t s);
+// final over the partials into sc[S_D0..1] + the Alg. 4 scalar update `which` (0 first, 1 alpha,
+// 2 nu/c/tau/cd/cq, 3 rel/convergence/beta, -1 none)
+void launch_final_scalar(const Geom& g, const double* partials, double* sc, int which, cudaStream_t s);
+// fused SQMR steps (kernels.cu k_apply_q / k_apply_x): q1 = t + beta q0, tn = L q1 and the
+// partials of q1.tn; x1 = x0 + (cd d0 + cq q), d1 = cd d0 + cq q and the partials of
+// ||b - L x1||^2.  halo_lo/hi (slab parts): also write the ghost plane below / above.
+void launch_apply_q(const LevelK& L, const double* t, const double* q0, double* q1, double* tn, const double* sc,
+                    double* partials, int halo_lo, int halo_hi, cudaStream_t s);
+void launch_apply_x(const LevelK& L, const double* x0, const double* d0, const double* q, const double* b, double* x1,
+                    double* d1, const double* sc, double* partials, int halo_lo, int halo_hi, cudaStream_t s);
 // Tile-ordered DGS (OD-1 rev. 2): a level is tiled iff it has >= tile_min cells (0: 128^3,
 // < 0: never) and its extents are multiples of the tile (16 x 8 x 8) with >= 2 tiles per axis.
 bool dgs_tiled(int nx, int ny, int nz, int64_t tile_min);
@@ -160,19 +170,12 @@ enum SqmrSlot {
     S_D0 = 0, S_D1 = 1, S_BNORM = 2, S_TAU = 3, S_NUOLD = 4, S_RHO = 5, S_ALPHA = 6, S_NU = 7, S_CD = 8,
     S_CQ = 9, S_RHONEW = 10, S_BETA = 11, S_REL = 12, S_STATUS = 13, S_TOL = 14, S_COUNT = 16
 };
-// which: 0 first (tau, rho from the initial dots), 1 alpha, 2 nu/c/tau/cd/cq, 3 rel/convergence/beta.
 // status slot: 0 running, 1 converged, 2 breakdown before the residual (sigma), 3 breakdown after it (rho).
-void launch_sqmr_scalar(int which, double* sc, cudaStream_t s);
-void launch_sqmr_loop_ctl(cudaGraphConditionalHandle h, const double* sc, double* hist, unsigned long long* stamp,
-                          int* loop, cudaStream_t s);
-void launch_stamp(unsigned long long* stamp, cudaStream_t s);
 // One additive Vanka application over all n band blocks (any order);
 // d7: scratch of 7 fields (g.fs each).  Bit-identical to the oracle's fixed order.
 void launch_vanka_additive(const LevelK& L, double* x, const double* b, const int32_t* cells, const uint8_t* masks,
                            int n, const double* ktab, double* d7, double omega, cudaStream_t s);
 void launch_axpy_s(double* s_, const double* t, const double* sc, int64_t n, cudaStream_t s);
-void launch_dx_dev(double* d, double* x, const double* q, const double* sc, int64_t n, cudaStream_t s);
-void launch_xpby_dev(double* q, const double* t, const double* sc, int64_t n, cudaStream_t s);
 
 // Number of our kernels launched so far (per process), for the bench's gpu_launches.
 int64_t launch_count();
