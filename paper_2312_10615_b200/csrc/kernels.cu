@@ -668,6 +668,25 @@ struct XNew {
     __device__ __forceinline__ XNew operator+(int64_t o) const { return XNew{X + o, D + o, Q + o, cd, cq}; }
 };
 
+// The momentum row (mom) and continuity row (cont) of the contract on a vector given by an
+// index functor v(j) (absolute indices, field f at f * fs): the same operand order.
+template <class VF>
+__device__ __forceinline__ double mom_f(const LevelK& L, const VF& v, int64_t i, int64_t sn, int64_t po) {
+    double s = v(i - 1) + v(i + 1);
+    s = s + v(i - L.g.sy);
+    s = s + v(i + L.g.sy);
+    s = s + v(i - L.g.sz);
+    s = s + v(i + L.g.sz);
+    const double lap = 6.0 * v(i) - s;
+    return L.eta_h2 * lap + (v(po) - v(po - sn)) * L.inv_h;
+}
+template <class VF>
+__device__ __forceinline__ double cont_f(const LevelK& L, const VF& v, int64_t i, double gamma) {
+    const int64_t fs = L.g.fs;
+    const double div = (v(i + 1) - v(i)) + (v(fs + i + L.g.sy) - v(fs + i)) + (v(2 * fs + i + L.g.sz) - v(2 * fs + i));
+    return -div * L.inv_h - gamma * v(3 * fs + i);
+}
+
 // Lines 9 + 5 of iteration j: q = t + beta q (written to Q1), t = L q (to Tn), sigma = q.t as
 // block partials.  Grid = the dot grid; on slab parts with a neighbour below / above, the
 // first / last z-block also writes q on the ghost plane -1 / nz (its inputs are valid there),
@@ -680,33 +699,48 @@ __global__ void __launch_bounds__(256) k_apply_q(LevelK L, const double* __restr
     if (sc[S_STATUS] != 0.0) return;
     const Geom& g = L.g;
     const int64_t fs = g.fs;
-    const QNew X{T, Q0, sc[S_BETA]};
-    const QNew U = X, V = X + fs, W = X + 2 * fs, P = X + 3 * fs;
+    const double beta = sc[S_BETA];
+    auto q = [&](int64_t j) { return T[j] + beta * Q0[j]; };  // the oracle's q[i] = t[i] + beta q[i]
     const int x = blockIdx.x * 32 + threadIdx.x, y = blockIdx.y * 8 + threadIdx.y;
     const int zl = blockIdx.z * kDotZB, zh = min(g.nz, zl + kDotZB);
     double v = 0.0;
-    const bool in = x < g.nx && y < g.ny;
-    if (in) {
+    if (x < g.nx && y < g.ny) {
         auto put_q = [&](int64_t i) {
 #pragma unroll
-            for (int f = 0; f < 4; ++f) Q1[f * fs + i] = X[f * fs + i];
+            for (int f = 0; f < 4; ++f) Q1[f * fs + i] = q(f * fs + i);
         };
         if (halo_lo && blockIdx.z == 0) put_q(g.slot(x, y, -1));
         if (halo_hi && zh == g.nz) put_q(g.slot(x, y, g.nz));
+#pragma unroll 1
         for (int z = zl; z < zh; ++z) {
             const int64_t i = g.slot(x, y, z);
-            const double qu = U[i], qv = V[i], qw = W[i], qp = P[i];
-            double tu = 0.0, tv = 0.0, tw = 0.0;
-            if (x >= 1) Tn[i] = tu = mom(L, U, P, i, 1);
-            if (y >= 1) Tn[fs + i] = tv = mom(L, V, P, i, g.sy);
-            if (g.gz(z) >= 1) Tn[2 * fs + i] = tw = mom(L, W, P, i, g.sz);
-            const double tp = cont(L, U, V, W, P, i, 0.0);
+            double c4;
+            {
+                const double qu = q(i);
+                double tu = 0.0;
+                if (x >= 1) Tn[i] = tu = mom_f(L, q, i, 1, 3 * fs + i);
+                Q1[i] = qu;
+                c4 = qu * tu;
+            }
+            {
+                const double qv = q(fs + i);
+                double tv = 0.0;
+                if (y >= 1) Tn[fs + i] = tv = mom_f(L, q, fs + i, g.sy, 3 * fs + i);
+                Q1[fs + i] = qv;
+                c4 = c4 + qv * tv;
+            }
+            {
+                const double qw = q(2 * fs + i);
+                double tw = 0.0;
+                if (g.gz(z) >= 1) Tn[2 * fs + i] = tw = mom_f(L, q, 2 * fs + i, g.sz, 3 * fs + i);
+                Q1[2 * fs + i] = qw;
+                c4 = c4 + qw * tw;
+            }
+            const double qp = q(3 * fs + i);
+            const double tp = cont_f(L, q, i, 0.0);
             Tn[3 * fs + i] = tp;
-            Q1[i] = qu;
-            Q1[fs + i] = qv;
-            Q1[2 * fs + i] = qw;
             Q1[3 * fs + i] = qp;
-            v = v + cell4(qu * tu, qv * tv, qw * tw, qp * tp);
+            v = v + (c4 + qp * tp);  // ((p_u + p_v) + p_w) + p_p
         }
     }
     block_partial2(v, 0.0, partials, dot_nblk(g), dot_blk(g));
@@ -715,7 +749,7 @@ __global__ void __launch_bounds__(256) k_apply_q(LevelK L, const double* __restr
 // Lines 7 + 8 of iteration j: d = cd d + cq q, x = x + d (written to D1, X1), then the true
 // residual r = b - L x as block partials of ||r||^2 (r itself is never stored).  Ghost planes
 // as in k_apply_q.
-__global__ void __launch_bounds__(256) k_apply_x(LevelK L, const double* __restrict__ X0,
+__global__ void __launch_bounds__(256, 4) k_apply_x(LevelK L, const double* __restrict__ X0,
                                                  const double* __restrict__ D0, const double* __restrict__ Q,
                                                  const double* __restrict__ B, double* __restrict__ X1,
                                                  double* __restrict__ D1, const double* __restrict__ sc,
@@ -724,30 +758,31 @@ __global__ void __launch_bounds__(256) k_apply_x(LevelK L, const double* __restr
     if (sc[S_STATUS] != 0.0) return;
     const Geom& g = L.g;
     const int64_t fs = g.fs;
-    const XNew X{X0, D0, Q, sc[S_CD], sc[S_CQ]};
-    const XNew U = X, V = X + fs, W = X + 2 * fs, P = X + 3 * fs;
+    const double cd = sc[S_CD], cq = sc[S_CQ];
+    auto dn = [&](int64_t j) { return cd * D0[j] + cq * Q[j]; };  // the oracle's d[i] = cd d[i] + cq q[i]
+    auto xn = [&](int64_t j) { return X0[j] + dn(j); };           // x[i] = x[i] + d[i]
     const int x = blockIdx.x * 32 + threadIdx.x, y = blockIdx.y * 8 + threadIdx.y;
     const int zl = blockIdx.z * kDotZB, zh = min(g.nz, zl + kDotZB);
     double v = 0.0;
-    const bool in = x < g.nx && y < g.ny;
-    if (in) {
+    if (x < g.nx && y < g.ny) {
         auto put_xd = [&](int64_t i) {
 #pragma unroll
             for (int f = 0; f < 4; ++f) {
-                const double dn = X.dnew(f * fs + i);
-                D1[f * fs + i] = dn;
-                X1[f * fs + i] = X0[f * fs + i] + dn;
+                const double d = dn(f * fs + i);
+                D1[f * fs + i] = d;
+                X1[f * fs + i] = X0[f * fs + i] + d;
             }
         };
         if (halo_lo && blockIdx.z == 0) put_xd(g.slot(x, y, -1));
         if (halo_hi && zh == g.nz) put_xd(g.slot(x, y, g.nz));
+#pragma unroll 1
         for (int z = zl; z < zh; ++z) {
             const int64_t i = g.slot(x, y, z);
             double ru = 0.0, rv = 0.0, rw = 0.0;
-            if (x >= 1) ru = B[i] - mom(L, U, P, i, 1);
-            if (y >= 1) rv = B[fs + i] - mom(L, V, P, i, g.sy);
-            if (g.gz(z) >= 1) rw = B[2 * fs + i] - mom(L, W, P, i, g.sz);
-            const double rp = B[3 * fs + i] - cont(L, U, V, W, P, i, 0.0);
+            if (x >= 1) ru = B[i] - mom_f(L, xn, i, 1, 3 * fs + i);
+            if (y >= 1) rv = B[fs + i] - mom_f(L, xn, fs + i, g.sy, 3 * fs + i);
+            if (g.gz(z) >= 1) rw = B[2 * fs + i] - mom_f(L, xn, 2 * fs + i, g.sz, 3 * fs + i);
+            const double rp = B[3 * fs + i] - cont_f(L, xn, i, 0.0);
             put_xd(i);
             v = v + cell4(ru * ru, rv * rv, rw * rw, rp * rp);
         }
