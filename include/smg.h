@@ -63,7 +63,7 @@ typedef struct smg_params {
     double omega;    /* additive damping in (0, 1]; <= 0 means 1.0 (SPEC default) */
     int64_t dgs_tile_min; /* DGS traversal (OD-1 rev. 2): levels with >= this many cells whose
                              extents are multiples of 16 x 8 x 8 (>= 2 tiles per axis) sweep
-                             their DGS tile by tile; 0: 128^3 (default), < 0: never */
+                             their DGS tile by tile; 0: 256^3 (default), < 0: never */
 } smg_params;
 
 #define SMG_FLAG_SKIP_REVERSE_DGS 1 /* fault injection: symmetry negative control */

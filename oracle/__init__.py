@@ -124,7 +124,7 @@ class Oracle:
 
     def __init__(self, nx, ny=None, nz=None, h=None, eta=1.0, gamma=1e-3, levels=2, nu=1,
                  band_width=1, cycle=0, vanka=0, omega=1.0, tile_min=0, order=ORDER_GPU):
-        """tile_min: cell count from which a level's DGS sweep is tile-ordered (0: 128^3, the
+        """tile_min: cell count from which a level's DGS sweep is tile-ordered (0: 256^3, the
         GPU default; -1: never).  order: ORDER_GPU (the coloured order the GPU reproduces bit
         for bit) or ORDER_SPEC (SPEC-literal sequential lexicographic DGS / colour-major Vanka)."""
         ny = nx if ny is None else ny

@@ -393,7 +393,7 @@ static std::array<double, 49> small_inverse(const std::vector<double>& m, int n)
 // a level is tiled iff its cell count is at least tile_min and every extent is a
 // multiple of the tile extent with at least two tiles per axis.
 constexpr int kTile[3] = {16, 8, 8};
-constexpr int64_t kTileMinDefault = int64_t{1} << 21;  // 128^3
+constexpr int64_t kTileMinDefault = int64_t{1} << 24;  // 256^3
 static bool dgs_tiled(const int* n, int64_t tile_min) {
     if (tile_min <= 0) tile_min = kTileMinDefault;
     const int64_t cells = static_cast<int64_t>(n[0]) * n[1] * n[2];
@@ -1284,7 +1284,7 @@ const char* orc_last_error() { return g_last_err.c_str(); }
 void orc_set_threads(int t) { g_threads = t < 1 ? 1 : t; }
 
 // Walled box with nx*ny*nz interior cells, uniform spacing h.
-// tile_min: cell count from which a level's DGS is tile-ordered (0: default 128^3; < 0: never).
+// tile_min: cell count from which a level's DGS is tile-ordered (0: default 256^3; < 0: never).
 void* orc_create(int nx, int ny, int nz, double h, double eta, double gamma, int levels, int nu, int band_width,
                  int64_t tile_min) {
     try {

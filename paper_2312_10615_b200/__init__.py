@@ -196,7 +196,7 @@ class Solver:
                  flags=0, device=0, devices=None, cycle=0, vanka=0, omega=1.0, tile_min=0):
         """devices: list of CUDA device ids, one z-slab part each (repeat an id to emulate several
         parts on one GPU).  Default: a single part on `device`.  tile_min: cell count from which a
-        level's DGS sweep runs in tile order (0: 128^3, the default; -1: never)."""
+        level's DGS sweep runs in tile order (0: 256^3, the default; -1: never)."""
         ny = nx if ny is None else ny
         nz = nx if nz is None else nz
         h = 1.0 / nx if h is None else h

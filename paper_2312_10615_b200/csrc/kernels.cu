@@ -12,6 +12,7 @@
 #include <atomic>
 #include <cstdint>
 #include <cstdlib>
+#include <cstring>
 
 #include <cooperative_groups.h>
 #include <cuda.h>
@@ -648,26 +649,9 @@ __global__ void __launch_bounds__(256) k_cdot_final(const double* __restrict__ p
 }
 
 // ---- fused SQMR steps (Alg. 4; north_star: AXPYs fused with the inner products) ----
-// Accessors evaluating a vector update on the fly at any slot, with the oracle's per-element
-// expressions: q_new = t + beta q (line 9), x_new = x + (cd d + cq q) (line 7).  The stencils
-// read them at radius 1; each thread stores the new values of its own cell only.
-struct QNew {
-    const double* __restrict__ T;
-    const double* __restrict__ Q;
-    double beta;
-    __device__ __forceinline__ double operator[](int64_t i) const { return T[i] + beta * Q[i]; }
-    __device__ __forceinline__ QNew operator+(int64_t o) const { return QNew{T + o, Q + o, beta}; }
-};
-struct XNew {
-    const double* __restrict__ X;
-    const double* __restrict__ D;
-    const double* __restrict__ Q;
-    double cd, cq;
-    __device__ __forceinline__ double dnew(int64_t i) const { return cd * D[i] + cq * Q[i]; }
-    __device__ __forceinline__ double operator[](int64_t i) const { return X[i] + dnew(i); }
-    __device__ __forceinline__ XNew operator+(int64_t o) const { return XNew{X + o, D + o, Q + o, cd, cq}; }
-};
-
+// The vector updates are evaluated on the fly at every slot a stencil reads, with the oracle's
+// per-element expressions: q_new = t + beta q (line 9), x_new = x + (cd d + cq q) (line 7); each
+// thread stores the new values of its own cell only.
 // The momentum row (mom) and continuity row (cont) of the contract on a vector given by an
 // index functor v(j) (absolute indices, field f at f * fs): the same operand order.
 template <class VF>
@@ -1778,39 +1762,86 @@ __global__ void k_axpy_s(double* __restrict__ s, const double* __restrict__ t, c
 // (reverse phases 10..19 inside each tile): "a given traversal order, then exactly the
 // reverse", so the sweep stays symmetric.  Same-colour tiles are a whole
 // tile apart, farther than any read (radius 2) plus write (radius 1) reach, so they run
-// in parallel exactly as in sequence.  One CTA owns one tile.  TMA (cp.async.bulk.tensor)
-// stages the tile's neighbourhood of x (4-D box: all four fields), the tile's b and (for
-// the reverse half) its m^T b in shared memory; every phase runs there with __syncthreads
-// between phases, and only the DOFs a phase may change go back to HBM.  Per-point
-// arithmetic is the per-step kernels' (mom / cont / prev_core with box strides) and the
-// in-tile order is the oracle's: bit-identical.  A level vector is read once and written
-// once per half sweep (plus the halo), instead of 13 passes of the per-step kernels.
+// in parallel exactly as in sequence.  One CTA owns one tile: the tile's neighbourhood of x
+// (all four fields), its b and (reverse half) its m^T b are staged in shared memory, every
+// phase runs there with __syncthreads between phases, and only the DOFs a phase may change go
+// back to HBM.  Per-point arithmetic is the per-step kernels' (same operand order) and the
+// in-tile order is the oracle's: bit-identical.  A level vector is read once and written once
+// per half sweep (plus the halo) instead of 13 passes of the per-step kernels.
+//
+// Shared-memory layout: every box row keeps its even-x and odd-x cells in two half-rows
+// ("x-parity split"): a phase works on one parity class of cells at a time, so the 32 lanes of
+// a warp read 8 consecutive words of 4 rows two apart (row stride 20 words: the two 8-word
+// groups of a half-warp fall on disjoint banks) -- no bank conflicts, where the natural layout
+// served stride-2 accesses in twice the wavefronts.  The x neighbours of a cell sit in the
+// other half-row (offsets XM / XP, by the cell's x parity).  The box is filled by coalesced
+// 128-bit loads (one even/odd pair each); m^T b, read once per cell, is staged by TMA.
 //
 // Two variants keep two CTAs per SM: FWD (phases 0..9; x box x [-2, TX+2), y, z [-1, T+1),
-// the pressure deltas of the tile) and REV (phases 10..19; x box x [-2, TX+2), y, z [-1, T+2)
-// for the radius-2 reads of the reverse pressure update; m^T b of the tile).
+// the tile's b, pressure deltas on the tile + a zero ring) and REV (phases 10..19; x box y, z
+// [-1, T+2) for the radius-2 reads of the reverse pressure update; b of u, v, w; m^T b).
 constexpr int kTX = 16, kTY = 8, kTZ = 8;
 constexpr int kTileThreads = 256;
 constexpr int kTileCells = kTX * kTY * kTZ;
+constexpr int kBX = kTX + 4, kHX = kBX / 2;  // box row (x from -2) and half-row
 template <bool FWD>
 struct TileBox {
-    // x from -2: a TMA box of 8-byte elements must start 16-byte aligned (tools/tma_probe.cu:
-    // an odd start coordinate raises "illegal instruction" on B200)
-    static constexpr int OX = 2, OY = 1, OZ = 1;
-    static constexpr int BX = kTX + 4, BY = FWD ? kTY + 2 : kTY + 3, BZ = FWD ? kTZ + 2 : kTZ + 3;
-    static constexpr int BOX = BX * BY * BZ;
+    static constexpr int BY = FWD ? kTY + 2 : kTY + 3, BZ = FWD ? kTZ + 2 : kTZ + 3;
+    static constexpr int SY = kBX, SZ = kBX * BY, BOX = kBX * BY * BZ;
     static constexpr int NB = FWD ? 4 : 3;  // fields of b staged
-    // FWD: pressure deltas on the tile plus a ring of zeros (the neighbours outside the tile carry
-    // no delta, so gathers need no bounds tests); REV: m^T b of the tile + the (lc, s) exchange
+    // FWD: deltas on the tile plus a ring of zeros (natural layout, (T+2)^3); REV: m^T b of the
+    // tile (natural, TMA) + the (lc, s) exchange of the split reverse update
     static constexpr int TS = FWD ? (kTX + 2) * (kTY + 2) * (kTZ + 2) : kTileCells + kTileCells / 4;
-    // x box (4 fields), b (NB fields of the tile), ts, mbarrier
     static constexpr size_t SMEM = (4 * BOX + NB * kTileCells + TS) * sizeof(double) + 128 + 16;
-    static __device__ __forceinline__ int li(int x, int y, int z) { return ((z + OZ) * BY + (y + OY)) * BX + (x + OX); }
+    // cell (x, y, z) of the tile (x in [-2, TX + 2), y, z from -1) in the split box
+    static __device__ __forceinline__ int li(int x, int y, int z) {
+        return ((z + 1) * BY + (y + 1)) * kBX + (x & 1) * kHX + ((x + 2) >> 1);
+    }
 };
+// x neighbours in the split layout of a cell of x parity p
+__device__ __forceinline__ int xm_off(int p) { return p ? -kHX : kHX - 1; }
+__device__ __forceinline__ int xp_off(int p) { return p ? -kHX + 1 : kHX; }
+// b of the tile, split by x parity: rows of 16 = two half-rows of 8
+__device__ __forceinline__ int tile_bi(int x, int y, int z) { return ((z * kTY + y) << 4) + (x & 1) * 8 + (x >> 1); }
+// natural tile index (m^T b staged by TMA) and the delta box (tile plus a one-cell ring)
 __device__ __forceinline__ int tile_ti(int x, int y, int z) { return (z * kTY + y) * kTX + x; }
-// delta box (FWD): the tile plus a one-cell ring
 constexpr int kDX = kTX + 2, kDXY = (kTX + 2) * (kTY + 2);
 __device__ __forceinline__ int tile_td(int x, int y, int z) { return ((z + 1) * (kTY + 2) + (y + 1)) * kDX + (x + 1); }
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// The operators of the contract on the split box (operand order of mom / cont).
+// px: x parity of the evaluation point; kind: normal axis of the face (0 u, 1 v, 2 w).
+template <int SY, int SZ>
+struct SplitOps {
+    static __device__ __forceinline__ double mom(const double* __restrict__ F, const double* __restrict__ P, int i,
+                                                 int px, int kind, double e2, double ih) {
+        double s = F[i + xm_off(px)] + F[i + xp_off(px)];
+        s = s + F[i - SY];
+        s = s + F[i + SY];
+        s = s + F[i - SZ];
+        s = s + F[i + SZ];
+        const double lap = 6.0 * F[i] - s;
+        const int pl = kind == 0 ? i + xm_off(px) : (kind == 1 ? i - SY : i - SZ);
+        return e2 * lap + (P[i] - P[pl]) * ih;
+    }
+    static __device__ __forceinline__ double cont(const double* __restrict__ U, const double* __restrict__ V,
+                                                  const double* __restrict__ W, const double* __restrict__ P, int i,
+                                                  int px, double gamma, double ih) {
+        const double div = (U[i + xp_off(px)] - U[i]) + (V[i + SY] - V[i]) + (W[i + SZ] - W[i]);
+        return -div * ih - gamma * P[i];
+    }
+};
+
+// band test of a tile cell (IN: an interior tile, every cell V2)
+template <bool IN>
+__device__ __forceinline__ bool tile_v2(const LevelK& L, int x0, int y0, int z0, int lx, int ly, int lz) {
+    if (IN) return lx >= 0 && ly >= 0 && lz >= 0 && lx < kTX && ly < kTY && lz < kTZ;
+    return lx >= 0 && ly >= 0 && lz >= 0 && lx < kTX && ly < kTY && lz < kTZ &&
+           !band_cell(L, x0 + lx, y0 + ly, z0 + lz);
+}
 
 // eta/h^2 (6 * 0 - s): the forward-pressure term of colour k ^ (1 << AX) on a cell K of colour k,
 // s the six-neighbour delta sum in x-, x+, y-, y+, z-, z+ order whose nonzero entries are the two
@@ -1869,42 +1900,24 @@ __device__ __forceinline__ double gath_k(int k, double p, const double* __restri
         default: return gath<7, LOWER>(p, ts, t, e2);
     }
 }
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-// The phases of one tile.  IN: an interior tile (no band cell in the tile or one cell around
-// it, every cell of the extended box active): no band or bounds tests at all.
-template <bool IN>
-__device__ __forceinline__ bool tile_v2(const LevelK& L, int x0, int y0, int z0, int lx, int ly, int lz) {
-    if (IN) return lx >= 0 && ly >= 0 && lz >= 0 && lx < kTX && ly < kTY && lz < kTZ;
-    return lx >= 0 && ly >= 0 && lz >= 0 && lx < kTX && ly < kTY && lz < kTZ &&
-           !band_cell(L, x0 + lx, y0 + ly, z0 + lz);
-}
-
-// p_K plus the forward-pressure terms of colours c' in [lo, hi] among K's axis-neighbour colours
-// k ^ 1, k ^ 2, k ^ 4 (ascending, as the eager phases add them): eta/h^2 (6 * 0 - sum), the sum
-// over K's six neighbours in x-, x+, y-, y+, z-, z+ order with only the two colour-c' ones
-// nonzero; skipped when neither is a V2 cell of the tile (the oracle touches no other K).
+// Generic form (partial phase ranges, boundary tiles): p_K plus the terms of colours c' in
+// [lo, hi] among k ^ 1, k ^ 2, k ^ 4 (ascending), each only if a neighbour along its axis is a
+// V2 cell of the tile (the oracle touches no other K).
 template <bool IN>
 __device__ __forceinline__ double tile_gathers(const LevelK& L, const double* __restrict__ ts, double p, int x0,
                                                int y0, int z0, int lx, int ly, int lz, int k, int lo, int hi) {
-    int cs[3] = {k ^ 1, k ^ 2, k ^ 4};  // ascending
-    if (cs[0] > cs[1]) { const int t = cs[0]; cs[0] = cs[1]; cs[1] = t; }
-    if (cs[1] > cs[2]) { const int t = cs[1]; cs[1] = cs[2]; cs[2] = t; }
-    if (cs[0] > cs[1]) { const int t = cs[0]; cs[0] = cs[1]; cs[1] = t; }
 #pragma unroll
-    for (int q = 0; q < 3; ++q) {
-        const int cc = cs[q];
+    for (int cc = 0; cc < 8; ++cc) {
+        const int bit = cc ^ k;
+        if (bit != 1 && bit != 2 && bit != 4) continue;
         if (cc < lo || cc > hi) continue;
-        const int bit = cc ^ k, ax = bit == 1 ? 0 : (bit == 2 ? 1 : 2);
+        const int ax = bit == 1 ? 0 : (bit == 2 ? 1 : 2);
         const int dx = ax == 0, dy = ax == 1, dz = ax == 2;
         const bool m0 = tile_v2<IN>(L, x0, y0, z0, lx - dx, ly - dy, lz - dz);
         const bool m1 = tile_v2<IN>(L, x0, y0, z0, lx + dx, ly + dy, lz + dz);
         if (!m0 && !m1) continue;
-        const int ti = tile_td(lx, ly, lz), tst = dx + dy * kDX + dz * kDXY;
-        const double a = m0 ? ts[ti - tst] : 0.0, b = m1 ? ts[ti + tst] : 0.0;
+        const int t = tile_td(lx, ly, lz), st = dx + dy * kDX + dz * kDXY;
+        const double a = m0 ? ts[t - st] : 0.0, b = m1 ? ts[t + st] : 0.0;
         double sn;
         if (ax == 0) {
             sn = a + b;
@@ -1930,87 +1943,51 @@ __device__ __forceinline__ double tile_gathers(const LevelK& L, const double* __
     return p;
 }
 
-// Box operators: mom / cont / prev_core of the contract (same operand order) on
-// the shared-memory box, 32-bit indices and compile-time strides.
-template <int SY, int SZ>
-struct BoxOps {
-    static __device__ __forceinline__ double mom(const double* __restrict__ F, const double* __restrict__ P, int i,
-                                                 int sn, double e2, double ih) {
-        double s = F[i - 1] + F[i + 1];
-        s = s + F[i - SY];
-        s = s + F[i + SY];
-        s = s + F[i - SZ];
-        s = s + F[i + SZ];
-        const double lap = 6.0 * F[i] - s;
-        return e2 * lap + (P[i] - P[i - sn]) * ih;
-    }
-    static __device__ __forceinline__ double cont(const double* __restrict__ U, const double* __restrict__ V,
-                                                  const double* __restrict__ W, const double* __restrict__ P, int i,
-                                                  double gamma, double ih) {
-        const double div = (U[i + 1] - U[i]) + (V[i + SY] - V[i]) + (W[i + SZ] - W[i]);
-        return -div * ih - gamma * P[i];
-    }
-};
-
 template <bool FWD, bool IN>
 __device__ __forceinline__ void tile_phases(const LevelK& L, double* __restrict__ xs, const double* __restrict__ bs,
                                             double* __restrict__ ts, int x0, int y0, int z0, int ph0, int ph1) {
     using TB = TileBox<FWD>;
-    constexpr int SY = TB::BX, SZ = TB::BX * TB::BY, BOX = TB::BOX;
-    using Ops = BoxOps<SY, SZ>;
+    constexpr int SY = TB::SY, SZ = TB::SZ, BOX = TB::BOX;
+    using Ops = SplitOps<SY, SZ>;
     const Geom& g = L.g;
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const double e2 = L.eta_h2, ih = L.inv_h, dv = L.dv, dp = L.dp, gam = L.gamma;
     double *Us = xs, *Vs = xs + BOX, *Ws = xs + 2 * BOX, *Ps = xs + 3 * BOX;
     const int cfirst = ph0 > 2 ? ph0 - 2 : 0;  // first forward pressure colour of this launch
     const bool full = ph0 <= 2 && ph1 >= 10;    // all eight colours run in this launch
-    // velocity phases: this thread's cells e = tid + k * threads, x pair 2 (e % 8) (+1 by parity)
-    int vli[kTileCells / 2 / kTileThreads], vti[kTileCells / 2 / kTileThreads], vpar[kTileCells / 2 / kTileThreads];
-#pragma unroll
-    for (int k = 0; k < kTileCells / 2 / kTileThreads; ++k) {
-        const int e = tid + k * kTileThreads;
-        const int lz = e / (kTX * kTY / 2), ly = (e / (kTX / 2)) % kTY, lx0 = 2 * (e % (kTX / 2));
-        vli[k] = TB::li(lx0, ly, lz);
-        vti[k] = tile_ti(lx0, ly, lz);
-        vpar[k] = (ly + lz + g.gz(z0)) & 1;  // global parity of (lx0, ly, lz) (x0 even)
-    }
-    // pressure phases: this thread's cell of colour c = base + offset(c), cell index m = tid % 128
-    const int pm = tid % (kTileCells / 8);
-    const int px0 = 2 * (pm % (kTX / 2)), py0 = 2 * ((pm / (kTX / 2)) % (kTY / 2)), pz0 = 2 * (pm / (kTX * kTY / 4));
-    const int pli = TB::li(px0, py0, pz0), pti = tile_ti(px0, py0, pz0), ptd = tile_td(px0, py0, pz0);
+    // a parity-class cell of this lane: x = 2 m + cx, y = 2 r + cy (m = lane % 8, r = lane / 8)
+    const int m8 = lane & 7, r4 = lane >> 3;
     for (int ph = ph0; ph < ph1; ++ph) {
-        if (ph <= 1 || ph >= 18) {  // velocity colour (red-black on global parity)
+        if (ph <= 1 || ph >= 18) {  // velocity colour: warp task (z, y parity a) -> 4 rows x 8 cells
             const int c = ph <= 1 ? ph : 19 - ph;
-            // this thread's colour-c cells are independent: every new value is computed before
-            // any is stored, so the loads of all six face rows can be in flight together
-            constexpr int NV = kTileCells / 2 / kTileThreads;
-            int li[NV], ti[NV];
-            bool du[NV], dv_[NV], dw[NV];
-            double nu[NV], nv[NV], nw[NV];
+            int li[2], bi[2], px[2];
+            bool du[2], dv_[2], dw[2];
+            double nu[2], nv[2], nw[2];
 #pragma unroll
-            for (int k = 0; k < NV; ++k) {
-                const int ox = vpar[k] ^ c;  // x offset of the colour-c cell of the pair
-                li[k] = vli[k] + ox;
-                ti[k] = vti[k] + ox;
+            for (int k = 0; k < 2; ++k) {
+                const int task = warp + 8 * k, lz = task >> 1, a = task & 1, ly = a + 2 * r4;
+                px[k] = (c + a + lz + g.z0) & 1;  // x parity of the colour-c cells of these rows
+                const int lx = 2 * m8 + px[k];
+                li[k] = TB::li(lx, ly, lz);
+                bi[k] = tile_bi(lx, ly, lz);
                 du[k] = dv_[k] = dw[k] = true;
                 if (!IN) {
-                    const int e = tid + k * kTileThreads;
-                    const int gx = x0 + 2 * (e % (kTX / 2)) + ox, gy = y0 + (e / (kTX / 2)) % kTY,
-                              zl = z0 + e / (kTX * kTY / 2);
+                    const int gx = x0 + lx, gy = y0 + ly, zl = z0 + lz;
                     const bool here = band_cell(L, gx, gy, zl);
                     du[k] = gx >= 1 && !here && !band_cell(L, gx - 1, gy, zl);
                     dv_[k] = gy >= 1 && !here && !band_cell(L, gx, gy - 1, zl);
                     dw[k] = g.gz(zl) >= 1 && !here && !band_cell(L, gx, gy, zl - 1);
                 }
             }
+            // independent cells: every new value before any store (loads of all six face rows in flight)
 #pragma unroll
-            for (int k = 0; k < NV; ++k) {
-                nu[k] = Us[li[k]] + (bs[ti[k]] - Ops::mom(Us, Ps, li[k], 1, e2, ih)) / dv;
-                nv[k] = Vs[li[k]] + (bs[kTileCells + ti[k]] - Ops::mom(Vs, Ps, li[k], SY, e2, ih)) / dv;
-                nw[k] = Ws[li[k]] + (bs[2 * kTileCells + ti[k]] - Ops::mom(Ws, Ps, li[k], SZ, e2, ih)) / dv;
+            for (int k = 0; k < 2; ++k) {
+                nu[k] = Us[li[k]] + (bs[bi[k]] - Ops::mom(Us, Ps, li[k], px[k], 0, e2, ih)) / dv;
+                nv[k] = Vs[li[k]] + (bs[kTileCells + bi[k]] - Ops::mom(Vs, Ps, li[k], px[k], 1, e2, ih)) / dv;
+                nw[k] = Ws[li[k]] + (bs[2 * kTileCells + bi[k]] - Ops::mom(Ws, Ps, li[k], px[k], 2, e2, ih)) / dv;
             }
 #pragma unroll
-            for (int k = 0; k < NV; ++k) {
+            for (int k = 0; k < 2; ++k) {
                 if (du[k]) Us[li[k]] = nu[k];
                 if (dv_[k]) Vs[li[k]] = nv[k];
                 if (dw[k]) Ws[li[k]] = nw[k];
@@ -2022,30 +1999,30 @@ __device__ __forceinline__ void tile_phases(const LevelK& L, double* __restrict_
             // colour-c cell).  p_K is read only by K's own phase before the pressure phases end, so
             // the neighbour terms are added when K is next read -- those of earlier colours at the
             // start of K's phase, the rest in the flush after the last colour: the same additions
-            // in the same order, hence bit-identical, with 9 barriers instead of 16.
+            // in the same order, hence bit-identical.
             int c = ph - 2;
-            // one colour-cc cell (this thread's cell index m = tid % 128): load + compute, then store
+            // one colour-cc cell of this lane in warp slot s (z = 2 s + cz): load + compute, then store
             struct PNew {
-                int li, td;
+                int li;
+                int td;
                 bool on;
                 double dc, u0, u1, v0, v1, w0, w1, p;
             };
-            auto pload = [&](int cc) {
+            auto pload = [&](int cc, int s) {
                 PNew r;
                 const int cx = cc & 1, cy = (cc >> 1) & 1, cz = cc >> 2;
-                r.on = IN || tile_v2<false>(L, x0, y0, z0, px0 + cx, py0 + cy, pz0 + cz);
-                const int li = pli + cx + cy * SY + cz * SZ;
-                const int ti = pti + cx + cy * kTX + cz * kTX * kTY;
-                const int td = ptd + cx + cy * kDX + cz * kDXY;
+                const int lx = 2 * m8 + cx, ly = 2 * r4 + cy, lz = 2 * s + cz;
+                r.on = IN || tile_v2<false>(L, x0, y0, z0, lx, ly, lz);
+                const int li = TB::li(lx, ly, lz), td = tile_td(lx, ly, lz);
                 r.li = li;
                 r.td = td;
                 if (!r.on) return r;
-                const double p =
-                    full ? gath_k<true>(cc, Ps[li], ts, td, e2)
-                         : tile_gathers<IN>(L, ts, Ps[li], x0, y0, z0, px0 + cx, py0 + cy, pz0 + cz, cc, cfirst, cc);
-                const double uL = Us[li], uR = Us[li + 1], vL = Vs[li], vR = Vs[li + SY], wL = Ws[li], wR = Ws[li + SZ];
+                const double p = full ? gath_k<true>(cc, Ps[li], ts, td, e2)
+                                      : tile_gathers<IN>(L, ts, Ps[li], x0, y0, z0, lx, ly, lz, cc, cfirst, cc);
+                const int xp = li + xp_off(cx);
+                const double uL = Us[li], uR = Us[xp], vL = Vs[li], vR = Vs[li + SY], wL = Ws[li], wR = Ws[li + SZ];
                 const double div = (uR - uL) + (vR - vL) + (wR - wL);
-                const double rr = bs[3 * kTileCells + ti] - (-div * ih - gam * p);
+                const double rr = bs[3 * kTileCells + tile_bi(lx, ly, lz)] - (-div * ih - gam * p);
                 const double dc = rr / dp;
                 r.dc = dc;
                 r.u0 = uL + (0.0 - dc) * ih;
@@ -2062,124 +2039,153 @@ __device__ __forceinline__ void tile_phases(const LevelK& L, double* __restrict_
                 r.p = p + e2 * (6.0 * dc - sn);
                 return r;
             };
-            auto pstore = [&](const PNew& r) {
+            auto pstore = [&](const PNew& r, int cx) {
                 if (!r.on) return;
                 ts[r.td] = r.dc;
                 Us[r.li] = r.u0;
-                Us[r.li + 1] = r.u1;
+                Us[r.li + xp_off(cx)] = r.u1;
                 Vs[r.li] = r.v0;
                 Vs[r.li + SY] = r.v1;
                 Ws[r.li] = r.w0;
                 Ws[r.li + SZ] = r.w1;
                 Ps[r.li] = r.p;
             };
-            auto pcell = [&](int cc) { pstore(pload(cc)); };
-            auto pcell2 = [&](int ca, int cb) {  // two independent cells: both computed before stores
-                const PNew ra = pload(ca), rb = pload(cb);
-                pstore(ra);
-                pstore(rb);
-            };
+            const int s4 = warp & 3;
             if (full) {
                 // Colours of equal popcount never touch each other's faces or pressures, nor does a
                 // cell read a same-group colour's delta: 0 | 1,2,4 | 3,5,6 | 7 run as four steps
-                // (per cell the same operations; bit-identical).
-                const int hi = tid >= kTileCells / 8;
-                if (!hi) pcell(0);
+                // (per cell the same operations; bit-identical).  Warps 0-3 / 4-7 take z slots 0-3.
+                const bool hi = warp >= 4;
+                if (!hi) pstore(pload(0, s4), 0);
                 __syncthreads();
-                if (hi) pcell(2);
-                else pcell2(1, 4);
+                if (hi) {
+                    pstore(pload(2, s4), 0);
+                } else {
+                    const PNew a = pload(1, s4), b = pload(4, s4);
+                    pstore(a, 1);
+                    pstore(b, 0);
+                }
                 __syncthreads();
-                if (hi) pcell(5);
-                else pcell2(3, 6);
+                if (hi) {
+                    pstore(pload(5, s4), 1);
+                } else {
+                    const PNew a = pload(3, s4), b = pload(6, s4);
+                    pstore(a, 1);
+                    pstore(b, 0);
+                }
                 __syncthreads();
-                if (!hi) pcell(7);
+                if (!hi) pstore(pload(7, s4), 1);
                 __syncthreads();
                 ph = 9;
                 c = 7;
             } else {
-                if (tid < kTileCells / 8) pcell(c);
+                if (warp < 4) pstore(pload(c, s4), c & 1);
                 __syncthreads();
             }
             if (ph == 9 || ph + 1 == ph1) {  // flush: the terms of colours [cfirst, c] still pending
-                // every cell of the tile and of the six face slabs around it (ring edges and corners
-                // have no tile neighbour)
-                for (int e = tid; e < TB::TS; e += kTileThreads) {
-                    const int lx = e % kDX - 1, ly = (e / kDX) % (kTY + 2) - 1, lz = e / kDXY - 1;
-                    const bool ox = lx < 0 || lx >= kTX, oy = ly < 0 || ly >= kTY, oz = lz < 0 || lz >= kTZ;
-                    if (ox + oy + oz >= 2) continue;
+                // tile cells by parity class (warp task: class k, z slot s), then the six face slabs
+                // (ring edges and corners have no tile neighbour)
+                for (int task = warp; task < 32; task += 8) {
+                    const int k = task >> 2, s = task & 3;
+                    const int lx = 2 * m8 + (k & 1), ly = 2 * r4 + ((k >> 1) & 1), lz = 2 * s + (k >> 2);
+                    const int li = TB::li(lx, ly, lz), td = tile_td(lx, ly, lz);
+                    if (full && (IN || tile_v2<false>(L, x0, y0, z0, lx, ly, lz))) {
+                        Ps[li] = gath_k<false>(k, Ps[li], ts, td, e2);  // relaxed: the colours above k
+                    } else {
+                        const bool relaxed = k >= cfirst && k <= c && tile_v2<IN>(L, x0, y0, z0, lx, ly, lz);
+                        Ps[li] = tile_gathers<IN>(L, ts, Ps[li], x0, y0, z0, lx, ly, lz, k, relaxed ? k + 1 : cfirst, c);
+                    }
+                }
+                constexpr int NSX = 2 * kTY * kTZ, NSY = 2 * kTX * kTZ, NSZ = 2 * kTX * kTY;
+                for (int e = tid; e < NSX + NSY + NSZ; e += kTileThreads) {
+                    int lx, ly, lz, ax;
+                    if (e < NSX) {
+                        ax = 0;
+                        lx = (e & 1) ? kTX : -1;
+                        ly = (e >> 1) % kTY;
+                        lz = (e >> 1) / kTY;
+                    } else if (e < NSX + NSY) {
+                        const int f = e - NSX;
+                        ax = 1;
+                        lx = f % kTX;
+                        ly = ((f / kTX) & 1) ? kTY : -1;
+                        lz = f / (2 * kTX);
+                    } else {
+                        const int f = e - NSX - NSY;
+                        ax = 2;
+                        lx = f % kTX;
+                        ly = (f / kTX) % kTY;
+                        lz = (f / (kTX * kTY)) ? kTZ : -1;
+                    }
                     if (!IN) {  // K must be an active cell of the level
                         const int gx = x0 + lx, gy = y0 + ly, gz = g.gz(z0 + lz);
                         if (gx < 0 || gy < 0 || gz < 0 || gx >= g.nx || gy >= g.ny || gz >= g.gnz) continue;
                     }
+                    const int li = TB::li(lx, ly, lz), td = tile_td(lx, ly, lz);
                     const int k = (lx & 1) + 2 * (ly & 1) + 4 * (lz & 1);
-                    const int li = TB::li(lx, ly, lz);
-                    if (full && IN) {
-                        if (!(ox || oy || oz)) {  // relaxed tile cell: the colours above k
-                            Ps[li] = gath_k<false>(k, Ps[li], ts, e, e2);
-                        } else {  // face-slab cell: the one term of its inward neighbour's colour
-                            const double d = ts[e + (ox ? (lx < 0 ? 1 : -1) : oy ? (ly < 0 ? kDX : -kDX)
-                                                                              : (lz < 0 ? kDXY : -kDXY))];
-                            const bool low = ox ? lx < 0 : oy ? ly < 0 : lz < 0;
-                            const double a = low ? 0.0 : d, bb = low ? d : 0.0;  // the (-, +) pair
-                            double sn;
-                            if (ox) {
-                                sn = a + bb;
-                                sn = sn + 0.0;
-                                sn = sn + 0.0;
-                                sn = sn + 0.0;
-                                sn = sn + 0.0;
-                            } else if (oy) {
-                                sn = 0.0 + 0.0;
-                                sn = sn + a;
-                                sn = sn + bb;
-                                sn = sn + 0.0;
-                                sn = sn + 0.0;
-                            } else {
-                                sn = 0.0 + 0.0;
-                                sn = sn + 0.0;
-                                sn = sn + 0.0;
-                                sn = sn + a;
-                                sn = sn + bb;
-                            }
-                            Ps[li] = Ps[li] + e2 * (6.0 * 0.0 - sn);
+                    if (full && IN) {  // the one term of its inward neighbour's colour
+                        const bool low = ax == 0 ? lx < 0 : (ax == 1 ? ly < 0 : lz < 0);
+                        const int st = ax == 0 ? 1 : (ax == 1 ? kDX : kDXY);
+                        const double d = ts[td + (low ? st : -st)];
+                        const double a = low ? 0.0 : d, bb = low ? d : 0.0;  // the (-, +) pair
+                        double sn;
+                        if (ax == 0) {
+                            sn = a + bb;
+                            sn = sn + 0.0;
+                            sn = sn + 0.0;
+                            sn = sn + 0.0;
+                            sn = sn + 0.0;
+                        } else if (ax == 1) {
+                            sn = 0.0 + 0.0;
+                            sn = sn + a;
+                            sn = sn + bb;
+                            sn = sn + 0.0;
+                            sn = sn + 0.0;
+                        } else {
+                            sn = 0.0 + 0.0;
+                            sn = sn + 0.0;
+                            sn = sn + 0.0;
+                            sn = sn + a;
+                            sn = sn + bb;
                         }
-                    } else {  // boundary tiles and partial ranges (single-phase entry points)
-                        const bool relaxed = k >= cfirst && k <= c && tile_v2<IN>(L, x0, y0, z0, lx, ly, lz);
-                        Ps[li] = tile_gathers<IN>(L, ts, Ps[li], x0, y0, z0, lx, ly, lz, k, relaxed ? k + 1 : cfirst, c);
+                        Ps[li] = Ps[li] + e2 * (6.0 * 0.0 - sn);
+                    } else {
+                        Ps[li] = tile_gathers<IN>(L, ts, Ps[li], x0, y0, z0, lx, ly, lz, k, cfirst, c);
                     }
                 }
                 __syncthreads();
             }
         } else {  // reverse (left-preconditioned) pressure colour c; ts = m^T b of the tile
-            // Two warps per 32 colour-c cells: warps 0, 2, 4, 6 evaluate the six momentum rows at
-            // the cells' faces (flux part), warps 1, 3, 5, 7 the seven continuity rows (C and its
-            // six neighbours) and hand (lc, s) over through shared memory; the first finish
+            // Two warps per 32 colour-c cells: even warps evaluate the six momentum rows at the
+            // cells' faces (flux part), odd warps the seven continuity rows (C and its six
+            // neighbours) and hand (lc, s) over through shared memory; the even warps finish
             // prev_core's expression in its operand order.  Same-colour cells never read each
             // other's pressure, so the update goes in place.
             const int c = 17 - ph;
-            const int half = (tid >> 5) & 1, cell = ((tid >> 6) << 5) | (tid & 31);
-            const int qx = 2 * (cell % (kTX / 2)) + (c & 1), qy = 2 * ((cell / (kTX / 2)) % (kTY / 2)) + ((c >> 1) & 1),
-                      qz = 2 * (cell / (kTX * kTY / 4)) + (c >> 2);
-            const bool v2 = IN || tile_v2<false>(L, x0, y0, z0, qx, qy, qz);
-            const int i = TB::li(qx, qy, qz);
+            const int half = warp & 1, s = warp >> 1, cell = (s << 5) | lane;
+            const int cx = c & 1, lx = 2 * m8 + cx, ly = 2 * r4 + ((c >> 1) & 1), lz = 2 * s + (c >> 2);
+            const bool v2 = IN || tile_v2<false>(L, x0, y0, z0, lx, ly, lz);
+            const int i = TB::li(lx, ly, lz);
             double* xch = ts + kTileCells;  // [2][kTileCells / 8]: lc, s
             double fl = 0.0;
             if (v2) {
                 if (half == 0) {
-                    const double luL = Ops::mom(Us, Ps, i, 1, e2, ih);
-                    const double luR = Ops::mom(Us, Ps, i + 1, 1, e2, ih);
-                    const double lvL = Ops::mom(Vs, Ps, i, SY, e2, ih);
-                    const double lvR = Ops::mom(Vs, Ps, i + SY, SY, e2, ih);
-                    const double lwL = Ops::mom(Ws, Ps, i, SZ, e2, ih);
-                    const double lwR = Ops::mom(Ws, Ps, i + SZ, SZ, e2, ih);
+                    const int ir = i + xp_off(cx);  // the u face on the right: x parity 1 - cx
+                    const double luL = Ops::mom(Us, Ps, i, cx, 0, e2, ih);
+                    const double luR = Ops::mom(Us, Ps, ir, 1 - cx, 0, e2, ih);
+                    const double lvL = Ops::mom(Vs, Ps, i, cx, 1, e2, ih);
+                    const double lvR = Ops::mom(Vs, Ps, i + SY, cx, 1, e2, ih);
+                    const double lwL = Ops::mom(Ws, Ps, i, cx, 2, e2, ih);
+                    const double lwR = Ops::mom(Ws, Ps, i + SZ, cx, 2, e2, ih);
                     fl = ((luR - luL) + (lvR - lvL)) + (lwR - lwL);
                 } else {
-                    const double lc = Ops::cont(Us, Vs, Ws, Ps, i, gam, ih);
-                    double sn = Ops::cont(Us, Vs, Ws, Ps, i - 1, gam, ih) + Ops::cont(Us, Vs, Ws, Ps, i + 1, gam, ih);
-                    sn = sn + Ops::cont(Us, Vs, Ws, Ps, i - SY, gam, ih);
-                    sn = sn + Ops::cont(Us, Vs, Ws, Ps, i + SY, gam, ih);
-                    sn = sn + Ops::cont(Us, Vs, Ws, Ps, i - SZ, gam, ih);
-                    sn = sn + Ops::cont(Us, Vs, Ws, Ps, i + SZ, gam, ih);
+                    const double lc = Ops::cont(Us, Vs, Ws, Ps, i, cx, gam, ih);
+                    double sn = Ops::cont(Us, Vs, Ws, Ps, i + xm_off(cx), 1 - cx, gam, ih) +
+                                Ops::cont(Us, Vs, Ws, Ps, i + xp_off(cx), 1 - cx, gam, ih);
+                    sn = sn + Ops::cont(Us, Vs, Ws, Ps, i - SY, cx, gam, ih);
+                    sn = sn + Ops::cont(Us, Vs, Ws, Ps, i + SY, cx, gam, ih);
+                    sn = sn + Ops::cont(Us, Vs, Ws, Ps, i - SZ, cx, gam, ih);
+                    sn = sn + Ops::cont(Us, Vs, Ws, Ps, i + SZ, cx, gam, ih);
                     xch[cell] = lc;
                     xch[kTileCells / 8 + cell] = sn;
                 }
@@ -2187,7 +2193,7 @@ __device__ __forceinline__ void tile_phases(const LevelK& L, double* __restrict_
             __syncthreads();
             if (v2 && half == 0) {
                 const double cl = fl * ih + e2 * (6.0 * xch[cell] - xch[kTileCells / 8 + cell]);
-                Ps[i] = Ps[i] + (ts[tile_ti(qx, qy, qz)] - cl) / dp;
+                Ps[i] = Ps[i] + (ts[tile_ti(lx, ly, lz)] - cl) / dp;
             }
             __syncthreads();
         }
@@ -2203,19 +2209,18 @@ __device__ __forceinline__ void tma_load(void* dst, const CUtensorMap* m, int c0
 }
 
 // FWD: phases [ph0, ph1) within 0..9; REV: within 10..19 -- on the tiles of colour T.
-// tmx: x box map; tmb: b (tile box, NB fields); tmc: m^T b (tile box, one field; REV only).
+// tmc: m^T b (tile box, one field, REV only).
 template <bool FWD>
 __global__ void __launch_bounds__(kTileThreads, 2)
-    k_dgs_tile(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmb,
-               const __grid_constant__ CUtensorMap tmc, LevelK L, double* __restrict__ X, int T, int ph0, int ph1,
-               int ntx, int nty) {
+    k_dgs_tile(const __grid_constant__ CUtensorMap tmc, LevelK L, double* __restrict__ X, const double* __restrict__ B,
+               int T, int ph0, int ph1, int ntx, int nty) {
     using TB = TileBox<FWD>;
     extern __shared__ __align__(128) double tsm_raw[];
     // 128-byte aligned by pointer arithmetic on the shared array (an integer round trip would hide
     // the address space and turn every box access into a generic LD/ST)
     double* xs = tsm_raw + (((128u - (smem_u32(tsm_raw) & 127u)) & 127u) >> 3);
-    double* bs = xs + 4 * TB::BOX;          // b of the tile, NB fields
-    double* ts = bs + TB::NB * kTileCells;  // deltas (FWD) / m^T b (REV)
+    double* bs = xs + 4 * TB::BOX;          // b of the tile, NB fields (split rows)
+    double* ts = bs + TB::NB * kTileCells;  // deltas (FWD) / m^T b + exchange (REV)
     uint64_t* bar = reinterpret_cast<uint64_t*>(ts + TB::TS);
     const Geom& g = L.g;
     const int tid = threadIdx.x;
@@ -2225,23 +2230,75 @@ __global__ void __launch_bounds__(kTileThreads, 2)
     const int bi = blockIdx.x;
     const int tx = 2 * (bi % hx) + (T & 1), ty = 2 * ((bi / hx) % hy) + ((T >> 1) & 1), tz = 2 * (bi / (hx * hy)) + pz;
     const int x0 = tx * kTX, y0 = ty * kTY, z0 = tz * kTZ;  // z0: local plane of the part
-    if (tid == 0) {
+    if (!FWD && tid == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
     pdl_wait();  // the previous kernel's writes are visible from here on
-    if (tid == 0) {
-        const uint32_t bytes = (4u * TB::BOX + (TB::NB + (FWD ? 0 : 1)) * kTileCells) * sizeof(double);
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+    if (!FWD && tid == 0) {
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                     "r"(static_cast<uint32_t>(kTileCells * sizeof(double)))
                      : "memory");
-        tma_load(xs, &tmx, x0 - TB::OX + g.xo, y0 - TB::OY + 1, z0 - TB::OZ + g.zg, 0, bar);
-        tma_load(bs, &tmb, x0 + g.xo, y0 + 1, z0 + g.zg, 0, bar);
-        if (!FWD) tma_load(ts, &tmc, x0 + g.xo, y0 + 1, z0 + g.zg, 0, bar);
+        tma_load(ts, &tmc, x0 + g.xo, y0 + 1, z0 + g.zg, 0, bar);
+    }
+    const int64_t fs = g.fs;
+    // x box: rows (f, z, y) of 20 cells from x0 - 2, one 128-bit load per even/odd pair; slots
+    // beyond the allocation (ghost ring exceeded) read as 0
+    {
+        constexpr int NQ = kBX / 2, ROWS = 4 * TB::BZ * TB::BY, N = ROWS * NQ;
+        constexpr int UNR = 8;
+        for (int e0 = tid; e0 < N; e0 += kTileThreads * UNR) {
+            double2 v[UNR];
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) {
+                const int e = e0 + u * kTileThreads;
+                v[u] = make_double2(0.0, 0.0);
+                if (e < N) {
+                    const int q = e % NQ, r = e / NQ, by = r % TB::BY, bz = (r / TB::BY) % TB::BZ, f = r / (TB::BY * TB::BZ);
+                    const int y = y0 - 1 + by, z = z0 - 1 + bz, xo = x0 - 2 + g.xo + 2 * q;
+                    if (y <= g.ny && z >= -g.zg && z < g.nz + g.zg && xo + 1 < g.px)
+                        v[u] = __ldg(reinterpret_cast<const double2*>(X + f * fs + g.slot(x0 - 2 + 2 * q, y, z)));
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) {
+                const int e = e0 + u * kTileThreads;
+                if (e < N) {
+                    const int q = e % NQ, r = e / NQ;
+                    xs[r * kBX + q] = v[u].x;        // even x (2q - 2)
+                    xs[r * kBX + kHX + q] = v[u].y;  // odd x (2q - 1)
+                }
+            }
+        }
+    }
+    {  // b of the tile: rows of 16 (8 pairs), split
+        constexpr int N = TB::NB * kTZ * kTY * (kTX / 2);
+        constexpr int UNR = 4;
+        for (int e0 = tid; e0 < N; e0 += kTileThreads * UNR) {
+            double2 v[UNR];
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) {
+                const int e = e0 + u * kTileThreads;
+                if (e < N) {
+                    const int q = e % (kTX / 2), r = e / (kTX / 2), ly = r % kTY, lz = (r / kTY) % kTZ, f = r / (kTY * kTZ);
+                    v[u] = __ldg(reinterpret_cast<const double2*>(B + f * fs + g.slot(x0 + 2 * q, y0 + ly, z0 + lz)));
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) {
+                const int e = e0 + u * kTileThreads;
+                if (e < N) {
+                    const int q = e % (kTX / 2), r = e / (kTX / 2);
+                    bs[(r << 4) + q] = v[u].x;
+                    bs[(r << 4) + 8 + q] = v[u].y;
+                }
+            }
+        }
     }
     if (FWD)
         for (int k = tid; k < TB::TS; k += kTileThreads) ts[k] = 0.0;
-    if (tid == 0) {  // one waiter (with a suspend hint), the others wait at the barrier
+    if (!FWD && tid == 0) {  // one waiter (with a suspend hint), the others wait at the barrier
         const uint32_t ba = smem_u32(bar);
         asm volatile(
             "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0, 1000000;\n @!p bra "
@@ -2257,16 +2314,19 @@ __global__ void __launch_bounds__(kTileThreads, 2)
     else tile_phases<FWD, false>(L, xs, bs, ts, x0, y0, z0, ph0, ph1);
     // Write back the DOFs the phases may have changed: the tile's own, plus (after forward
     // pressure phases) its high faces and the pressures of the six neighbouring slabs.  Rows of
-    // 16 go out as 16-byte stores.  Every slot written was loaded by this CTA and no other CTA
-    // touches it during the launch; wall and ghost slots were loaded as 0 and never changed.
-    const int64_t fs = g.fs;
+    // 16 go out as 16-byte stores (an even/odd pair each; the lanes of a half-warp read rows two
+    // apart).  Every slot written was loaded by this CTA and no other CTA touches it during the
+    // launch; wall and ghost slots were loaded as 0 and never changed.
     const int hw = (FWD && ph1 > 2) ? 1 : 0;  // a forward pressure phase ran
     auto rows = [&](int f, int ylo, int nyr, int zlo, int nzr) {
         const int n = nyr * nzr * (kTX / 2);
         for (int e = tid; e < n; e += kTileThreads) {
-            const int q = e % (kTX / 2), r = e / (kTX / 2);
-            const int ly = ylo + r % nyr, lz = zlo + r / nyr;
-            const double2 v = *reinterpret_cast<const double2*>(&xs[f * TB::BOX + TB::li(2 * q, ly, lz)]);
+            const int q = e & 7, r = e >> 3;
+            // rows in the order y = 0, 2, 4, ..., 1, 3, ... within each z (nyr even) for conflict-free reads
+            const int ry = r % nyr, lz = zlo + r / nyr;
+            const int ly = ylo + ((nyr & 1) ? ry : (ry < nyr / 2 ? 2 * ry : 2 * (ry - nyr / 2) + 1));
+            const int li = TB::li(2 * q, ly, lz);
+            const double2 v = make_double2(xs[f * TB::BOX + li], xs[f * TB::BOX + li + kHX]);
             *reinterpret_cast<double2*>(&X[f * fs + g.slot(x0 + 2 * q, y0 + ly, z0 + lz)]) = v;
         }
     };
@@ -2722,7 +2782,7 @@ static TmapEncodeFn tmap_encode() {
 }
 
 bool dgs_tiled(int nx, int ny, int nz, int64_t tile_min) {
-    if (tile_min == 0) tile_min = int64_t{1} << 21;  // 128^3 (the oracle's kTileMinDefault)
+    if (tile_min == 0) tile_min = int64_t{1} << 24;  // 256^3 (the oracle's kTileMinDefault)
     if (tile_min < 0) return false;
     if (static_cast<int64_t>(nx) * ny * nz < tile_min) return false;
     return nx % kTX == 0 && ny % kTY == 0 && nz % kTZ == 0 && nx / kTX >= 2 && ny / kTY >= 2 && nz / kTZ >= 2;
@@ -2759,18 +2819,9 @@ void launch_dgs_tile_phases(const LevelK& L, double* x, const double* b, int T, 
         launch_dgs_tile_phases(L, x, b, T, 10, ph1, s);
         return;
     }
-    CUtensorMap mx, mb, mc;
-    bool ok;
-    if (fwd) {
-        using TB = TileBox<true>;
-        ok = level_tmap(g, x, 4, TB::BX, TB::BY, TB::BZ, &mx) && level_tmap(g, b, 4, kTX, kTY, kTZ, &mb);
-        mc = mb;
-    } else {
-        using TB = TileBox<false>;
-        ok = level_tmap(g, x, 4, TB::BX, TB::BY, TB::BZ, &mx) && level_tmap(g, b, 3, kTX, kTY, kTZ, &mb) &&
-             level_tmap(g, L.cb, 1, kTX, kTY, kTZ, &mc);
-    }
-    if (!ok) {
+    CUtensorMap mc;
+    std::memset(&mc, 0, sizeof(mc));
+    if (!fwd && !level_tmap(g, L.cb, 1, kTX, kTY, kTZ, &mc)) {
         note(cudaErrorNotSupported);
         return;
     }
@@ -2783,11 +2834,11 @@ void launch_dgs_tile_phases(const LevelK& L, double* x, const double* b, int T, 
         attr = true;
     }
     if (fwd)
-        launch_k(k_dgs_tile<true>, dim3(hx * hy * hz), dim3(kTileThreads), TileBox<true>::SMEM, s, mx, mb, mc, L, x, T,
-                 ph0, ph1, ntx, nty);
+        launch_k(k_dgs_tile<true>, dim3(hx * hy * hz), dim3(kTileThreads), TileBox<true>::SMEM, s, mc, L, x, b, T, ph0,
+                 ph1, ntx, nty);
     else
-        launch_k(k_dgs_tile<false>, dim3(hx * hy * hz), dim3(kTileThreads), TileBox<false>::SMEM, s, mx, mb, mc, L, x,
-                 T, ph0, ph1, ntx, nty);
+        launch_k(k_dgs_tile<false>, dim3(hx * hy * hz), dim3(kTileThreads), TileBox<false>::SMEM, s, mc, L, x, b, T,
+                 ph0, ph1, ntx, nty);
     count();
 }
 

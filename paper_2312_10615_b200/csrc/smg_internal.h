@@ -147,7 +147,7 @@ void launch_apply_q(const LevelK& L, const double* t, const double* q0, double* 
                     double* partials, int halo_lo, int halo_hi, cudaStream_t s);
 void launch_apply_x(const LevelK& L, const double* x0, const double* d0, const double* q, const double* b, double* x1,
                     double* d1, const double* sc, double* partials, int halo_lo, int halo_hi, cudaStream_t s);
-// Tile-ordered DGS (OD-1 rev. 2): a level is tiled iff it has >= tile_min cells (0: 128^3,
+// Tile-ordered DGS (OD-1 rev. 2): a level is tiled iff it has >= tile_min cells (0: 256^3,
 // < 0: never) and its extents are multiples of the tile (16 x 8 x 8) with >= 2 tiles per axis.
 bool dgs_tiled(int nx, int ny, int nz, int64_t tile_min);
 int dgs_tile_dim(int axis);

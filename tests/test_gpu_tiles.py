@@ -68,14 +68,14 @@ def test_tiled_forward_half_and_phases_bitwise():
 
 
 def test_tiled_matches_untiled_rule_and_default():
-    """The tiling rule is the same function on both sides; 128^3 is tiled by default, 64^3 not."""
+    """The tiling rule is the same function on both sides; 256^3 is tiled by default, 128^3 not."""
     for dims in [(128, 128, 128), (64, 64, 64), (256, 256, 256), (1024, 256, 256), (48, 40, 24), (40, 16, 16)]:
         for lv in range(3):
             for tm in (0, 1, -1):
                 got = smg.dgs_tile(*dims, lv, tm)
                 nx, ny, nz = (d >> lv for d in dims)
                 cells = nx * ny * nz
-                thr = (1 << 21) if tm == 0 else tm
+                thr = (1 << 24) if tm == 0 else tm
                 tiled = tm >= 0 and cells >= thr and nx % 16 == 0 and ny % 8 == 0 and nz % 8 == 0 and \
                     nx >= 32 and ny >= 16 and nz >= 16
                 assert got == ((8, 16, 8, 8) if tiled else (1, 0, 0, 0)), (dims, lv, tm, got)
@@ -100,9 +100,9 @@ def test_tiled_slabs_bitwise(dims, levels, parts):
 
 
 def test_tiled_cfg1_iterations_match_spec_order():
-    """cfg 1 (128^3, 5 levels, tiled fine level): iteration count within +-1 of the SPEC-literal
-    sequential order (lexicographic DGS, colour-major sequential Vanka) -- recorded value 8."""
-    s = smg.Solver(128, levels=5)
+    """cfg 1 (128^3, 5 levels) with its fine level tiled: iteration count within +-1 of the
+    SPEC-literal sequential order (lexicographic DGS, colour-major sequential Vanka) -- recorded 8."""
+    s = smg.Solver(128, levels=5, tile_min=1 << 21)
     b = smg.forcing(128, kind=smg.FORCE_UNIFORM, seed=1)
     _, h, _, st = s.sqmr(b, 1e-6, 100)
     assert st == smg.SMG_CONVERGED and abs(len(h) - 8) <= 1
