@@ -13,6 +13,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 
 #include <cooperative_groups.h>
 #include <cuda.h>
@@ -1799,8 +1800,11 @@ struct TileBox {
     }
 };
 // x neighbours in the split layout of a cell of x parity p
-__device__ __forceinline__ int xm_off(int p) { return p ? -kHX : kHX - 1; }
 __device__ __forceinline__ int xp_off(int p) { return p ? -kHX + 1 : kHX; }
+template <int PX>
+__host__ __device__ constexpr int XM() { return PX ? -kHX : kHX - 1; }
+template <int PX>
+__host__ __device__ constexpr int XP() { return PX ? -kHX + 1 : kHX; }
 // b of the tile, split by x parity: rows of 16 = two half-rows of 8
 __device__ __forceinline__ int tile_bi(int x, int y, int z) { return ((z * kTY + y) << 4) + (x & 1) * 8 + (x >> 1); }
 // natural tile index (m^T b staged by TMA) and the delta box (tile plus a one-cell ring)
@@ -1813,27 +1817,32 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 }
 
 // The operators of the contract on the split box (operand order of mom / cont).
-// px: x parity of the evaluation point; kind: normal axis of the face (0 u, 1 v, 2 w).
+// PX: x parity of the evaluation point (warp-uniform in every phase: immediate offsets);
+// KIND: normal axis of the face (0 u, 1 v, 2 w).
 template <int SY, int SZ>
 struct SplitOps {
+    template <int PX, int KIND>
     static __device__ __forceinline__ double mom(const double* __restrict__ F, const double* __restrict__ P, int i,
-                                                 int px, int kind, double e2, double ih) {
-        double s = F[i + xm_off(px)] + F[i + xp_off(px)];
+                                                 double e2, double ih) {
+        double s = F[i + XM<PX>()] + F[i + XP<PX>()];
         s = s + F[i - SY];
         s = s + F[i + SY];
         s = s + F[i - SZ];
         s = s + F[i + SZ];
         const double lap = 6.0 * F[i] - s;
-        const int pl = kind == 0 ? i + xm_off(px) : (kind == 1 ? i - SY : i - SZ);
-        return e2 * lap + (P[i] - P[pl]) * ih;
+        constexpr int PL = KIND == 0 ? XM<PX>() : (KIND == 1 ? -SY : -SZ);
+        return e2 * lap + (P[i] - P[i + PL]) * ih;
     }
+    template <int PX>
     static __device__ __forceinline__ double cont(const double* __restrict__ U, const double* __restrict__ V,
                                                   const double* __restrict__ W, const double* __restrict__ P, int i,
-                                                  int px, double gamma, double ih) {
-        const double div = (U[i + xp_off(px)] - U[i]) + (V[i + SY] - V[i]) + (W[i + SZ] - W[i]);
+                                                  double gamma, double ih) {
+        const double div = (U[i + XP<PX>()] - U[i]) + (V[i + SY] - V[i]) + (W[i + SZ] - W[i]);
         return -div * ih - gamma * P[i];
     }
 };
+template <int V>
+using IC = std::integral_constant<int, V>;
 
 // band test of a tile cell (IN: an interior tile, every cell V2)
 template <bool IN>
@@ -1980,11 +1989,16 @@ __device__ __forceinline__ void tile_phases(const LevelK& L, double* __restrict_
                 }
             }
             // independent cells: every new value before any store (loads of all six face rows in flight)
+            auto velc = [&](auto pxc, int k) {
+                constexpr int PX = decltype(pxc)::value;
+                nu[k] = Us[li[k]] + (bs[bi[k]] - Ops::template mom<PX, 0>(Us, Ps, li[k], e2, ih)) / dv;
+                nv[k] = Vs[li[k]] + (bs[kTileCells + bi[k]] - Ops::template mom<PX, 1>(Vs, Ps, li[k], e2, ih)) / dv;
+                nw[k] = Ws[li[k]] + (bs[2 * kTileCells + bi[k]] - Ops::template mom<PX, 2>(Ws, Ps, li[k], e2, ih)) / dv;
+            };
 #pragma unroll
             for (int k = 0; k < 2; ++k) {
-                nu[k] = Us[li[k]] + (bs[bi[k]] - Ops::mom(Us, Ps, li[k], px[k], 0, e2, ih)) / dv;
-                nv[k] = Vs[li[k]] + (bs[kTileCells + bi[k]] - Ops::mom(Vs, Ps, li[k], px[k], 1, e2, ih)) / dv;
-                nw[k] = Ws[li[k]] + (bs[2 * kTileCells + bi[k]] - Ops::mom(Ws, Ps, li[k], px[k], 2, e2, ih)) / dv;
+                if (px[k]) velc(IC<1>{}, k);
+                else velc(IC<0>{}, k);
             }
 #pragma unroll
             for (int k = 0; k < 2; ++k) {
@@ -2168,27 +2182,32 @@ __device__ __forceinline__ void tile_phases(const LevelK& L, double* __restrict_
             const int i = TB::li(lx, ly, lz);
             double* xch = ts + kTileCells;  // [2][kTileCells / 8]: lc, s
             double fl = 0.0;
-            if (v2) {
+            auto rev = [&](auto pxc) {
+                constexpr int PX = decltype(pxc)::value, QX = 1 - PX;
                 if (half == 0) {
-                    const int ir = i + xp_off(cx);  // the u face on the right: x parity 1 - cx
-                    const double luL = Ops::mom(Us, Ps, i, cx, 0, e2, ih);
-                    const double luR = Ops::mom(Us, Ps, ir, 1 - cx, 0, e2, ih);
-                    const double lvL = Ops::mom(Vs, Ps, i, cx, 1, e2, ih);
-                    const double lvR = Ops::mom(Vs, Ps, i + SY, cx, 1, e2, ih);
-                    const double lwL = Ops::mom(Ws, Ps, i, cx, 2, e2, ih);
-                    const double lwR = Ops::mom(Ws, Ps, i + SZ, cx, 2, e2, ih);
+                    const int ir = i + XP<PX>();  // the u face on the right: x parity 1 - PX
+                    const double luL = Ops::template mom<PX, 0>(Us, Ps, i, e2, ih);
+                    const double luR = Ops::template mom<QX, 0>(Us, Ps, ir, e2, ih);
+                    const double lvL = Ops::template mom<PX, 1>(Vs, Ps, i, e2, ih);
+                    const double lvR = Ops::template mom<PX, 1>(Vs, Ps, i + SY, e2, ih);
+                    const double lwL = Ops::template mom<PX, 2>(Ws, Ps, i, e2, ih);
+                    const double lwR = Ops::template mom<PX, 2>(Ws, Ps, i + SZ, e2, ih);
                     fl = ((luR - luL) + (lvR - lvL)) + (lwR - lwL);
                 } else {
-                    const double lc = Ops::cont(Us, Vs, Ws, Ps, i, cx, gam, ih);
-                    double sn = Ops::cont(Us, Vs, Ws, Ps, i + xm_off(cx), 1 - cx, gam, ih) +
-                                Ops::cont(Us, Vs, Ws, Ps, i + xp_off(cx), 1 - cx, gam, ih);
-                    sn = sn + Ops::cont(Us, Vs, Ws, Ps, i - SY, cx, gam, ih);
-                    sn = sn + Ops::cont(Us, Vs, Ws, Ps, i + SY, cx, gam, ih);
-                    sn = sn + Ops::cont(Us, Vs, Ws, Ps, i - SZ, cx, gam, ih);
-                    sn = sn + Ops::cont(Us, Vs, Ws, Ps, i + SZ, cx, gam, ih);
+                    const double lc = Ops::template cont<PX>(Us, Vs, Ws, Ps, i, gam, ih);
+                    double sn = Ops::template cont<QX>(Us, Vs, Ws, Ps, i + XM<PX>(), gam, ih) +
+                                Ops::template cont<QX>(Us, Vs, Ws, Ps, i + XP<PX>(), gam, ih);
+                    sn = sn + Ops::template cont<PX>(Us, Vs, Ws, Ps, i - SY, gam, ih);
+                    sn = sn + Ops::template cont<PX>(Us, Vs, Ws, Ps, i + SY, gam, ih);
+                    sn = sn + Ops::template cont<PX>(Us, Vs, Ws, Ps, i - SZ, gam, ih);
+                    sn = sn + Ops::template cont<PX>(Us, Vs, Ws, Ps, i + SZ, gam, ih);
                     xch[cell] = lc;
                     xch[kTileCells / 8 + cell] = sn;
                 }
+            };
+            if (v2) {
+                if (cx) rev(IC<1>{});
+                else rev(IC<0>{});
             }
             __syncthreads();
             if (v2 && half == 0) {
@@ -2209,11 +2228,12 @@ __device__ __forceinline__ void tma_load(void* dst, const CUtensorMap* m, int c0
 }
 
 // FWD: phases [ph0, ph1) within 0..9; REV: within 10..19 -- on the tiles of colour T.
-// tmc: m^T b (tile box, one field, REV only).
+// tmx: x box map; tmb: b (tile box, NB fields); tmc: m^T b (tile box, one field; REV only).
 template <bool FWD>
 __global__ void __launch_bounds__(kTileThreads, 2)
-    k_dgs_tile(const __grid_constant__ CUtensorMap tmc, LevelK L, double* __restrict__ X, const double* __restrict__ B,
-               int T, int ph0, int ph1, int ntx, int nty) {
+    k_dgs_tile(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmb,
+               const __grid_constant__ CUtensorMap tmc, LevelK L, double* __restrict__ X, int T, int ph0, int ph1,
+               int ntx, int nty) {
     using TB = TileBox<FWD>;
     extern __shared__ __align__(128) double tsm_raw[];
     // 128-byte aligned by pointer arithmetic on the shared array (an integer round trip would hide
@@ -2230,75 +2250,23 @@ __global__ void __launch_bounds__(kTileThreads, 2)
     const int bi = blockIdx.x;
     const int tx = 2 * (bi % hx) + (T & 1), ty = 2 * ((bi / hx) % hy) + ((T >> 1) & 1), tz = 2 * (bi / (hx * hy)) + pz;
     const int x0 = tx * kTX, y0 = ty * kTY, z0 = tz * kTZ;  // z0: local plane of the part
-    if (!FWD && tid == 0) {
+    if (tid == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
     pdl_wait();  // the previous kernel's writes are visible from here on
-    if (!FWD && tid == 0) {
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-                     "r"(static_cast<uint32_t>(kTileCells * sizeof(double)))
+    if (tid == 0) {  // TMA: the x box (4 fields), the tile's b (NB fields), m^T b (REV)
+        const uint32_t bytes = (4u * TB::BOX + (TB::NB + (FWD ? 0 : 1)) * kTileCells) * sizeof(double);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                      : "memory");
-        tma_load(ts, &tmc, x0 + g.xo, y0 + 1, z0 + g.zg, 0, bar);
-    }
-    const int64_t fs = g.fs;
-    // x box: rows (f, z, y) of 20 cells from x0 - 2, one 128-bit load per even/odd pair; slots
-    // beyond the allocation (ghost ring exceeded) read as 0
-    {
-        constexpr int NQ = kBX / 2, ROWS = 4 * TB::BZ * TB::BY, N = ROWS * NQ;
-        constexpr int UNR = 8;
-        for (int e0 = tid; e0 < N; e0 += kTileThreads * UNR) {
-            double2 v[UNR];
-#pragma unroll
-            for (int u = 0; u < UNR; ++u) {
-                const int e = e0 + u * kTileThreads;
-                v[u] = make_double2(0.0, 0.0);
-                if (e < N) {
-                    const int q = e % NQ, r = e / NQ, by = r % TB::BY, bz = (r / TB::BY) % TB::BZ, f = r / (TB::BY * TB::BZ);
-                    const int y = y0 - 1 + by, z = z0 - 1 + bz, xo = x0 - 2 + g.xo + 2 * q;
-                    if (y <= g.ny && z >= -g.zg && z < g.nz + g.zg && xo + 1 < g.px)
-                        v[u] = __ldg(reinterpret_cast<const double2*>(X + f * fs + g.slot(x0 - 2 + 2 * q, y, z)));
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < UNR; ++u) {
-                const int e = e0 + u * kTileThreads;
-                if (e < N) {
-                    const int q = e % NQ, r = e / NQ;
-                    xs[r * kBX + q] = v[u].x;        // even x (2q - 2)
-                    xs[r * kBX + kHX + q] = v[u].y;  // odd x (2q - 1)
-                }
-            }
-        }
-    }
-    {  // b of the tile: rows of 16 (8 pairs), split
-        constexpr int N = TB::NB * kTZ * kTY * (kTX / 2);
-        constexpr int UNR = 4;
-        for (int e0 = tid; e0 < N; e0 += kTileThreads * UNR) {
-            double2 v[UNR];
-#pragma unroll
-            for (int u = 0; u < UNR; ++u) {
-                const int e = e0 + u * kTileThreads;
-                if (e < N) {
-                    const int q = e % (kTX / 2), r = e / (kTX / 2), ly = r % kTY, lz = (r / kTY) % kTZ, f = r / (kTY * kTZ);
-                    v[u] = __ldg(reinterpret_cast<const double2*>(B + f * fs + g.slot(x0 + 2 * q, y0 + ly, z0 + lz)));
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < UNR; ++u) {
-                const int e = e0 + u * kTileThreads;
-                if (e < N) {
-                    const int q = e % (kTX / 2), r = e / (kTX / 2);
-                    bs[(r << 4) + q] = v[u].x;
-                    bs[(r << 4) + 8 + q] = v[u].y;
-                }
-            }
-        }
+        tma_load(xs, &tmx, x0 - 2 + g.xo, y0, z0 - 1 + g.zg, 0, bar);
+        tma_load(bs, &tmb, x0 + g.xo, y0 + 1, z0 + g.zg, 0, bar);
+        if (!FWD) tma_load(ts, &tmc, x0 + g.xo, y0 + 1, z0 + g.zg, 0, bar);
     }
     if (FWD)
         for (int k = tid; k < TB::TS; k += kTileThreads) ts[k] = 0.0;
-    if (!FWD && tid == 0) {  // one waiter (with a suspend hint), the others wait at the barrier
+    if (tid == 0) {  // one waiter (with a suspend hint), the others wait at the barrier
         const uint32_t ba = smem_u32(bar);
         asm volatile(
             "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0, 1000000;\n @!p bra "
@@ -2306,6 +2274,38 @@ __global__ void __launch_bounds__(kTileThreads, 2)
             : "memory");
     }
     __syncthreads();
+    {  // x-parity split of every staged row, in place (a warp reads its rows' pairs, then writes)
+        const int lane = tid & 31, warp = tid >> 5;
+        constexpr int ROWS = 4 * TB::BZ * TB::BY;
+        const int lr = lane / kHX, lq = lane % kHX;  // 3 rows of 10 pairs per warp step
+        for (int r0 = warp * 3; r0 < ROWS; r0 += 24) {
+            const int r = r0 + lr;
+            const bool ok = lane < 3 * kHX && r < ROWS;
+            double2 v = make_double2(0.0, 0.0);
+            if (ok) v = *reinterpret_cast<const double2*>(&xs[r * kBX + 2 * lq]);
+            __syncwarp();
+            if (ok) {
+                xs[r * kBX + lq] = v.x;
+                xs[r * kBX + kHX + lq] = v.y;
+            }
+            __syncwarp();
+        }
+        constexpr int BROWS = TB::NB * kTZ * kTY;  // rows of 16: 4 rows of 8 pairs per warp step
+        for (int r0 = warp * 4; r0 < BROWS; r0 += 32) {
+            const int r = r0 + (lane >> 3), q = lane & 7;
+            const bool ok = r < BROWS;
+            double2 v = make_double2(0.0, 0.0);
+            if (ok) v = *reinterpret_cast<const double2*>(&bs[(r << 4) + 2 * q]);
+            __syncwarp();
+            if (ok) {
+                bs[(r << 4) + q] = v.x;
+                bs[(r << 4) + 8 + q] = v.y;
+            }
+            __syncwarp();
+        }
+    }
+    __syncthreads();
+    const int64_t fs = g.fs;
     // interior: every cell of the tile and of the cell layer around it is a V2 cell of the level
     const int gz0 = g.gz(z0), bw = L.bw;
     const bool interior = x0 - 1 >= bw && y0 - 1 >= bw && gz0 - 1 >= bw && x0 + kTX + 1 <= g.nx - bw &&
@@ -2819,9 +2819,18 @@ void launch_dgs_tile_phases(const LevelK& L, double* x, const double* b, int T, 
         launch_dgs_tile_phases(L, x, b, T, 10, ph1, s);
         return;
     }
-    CUtensorMap mc;
-    std::memset(&mc, 0, sizeof(mc));
-    if (!fwd && !level_tmap(g, L.cb, 1, kTX, kTY, kTZ, &mc)) {
+    CUtensorMap mx, mb, mc;
+    bool ok;
+    if (fwd) {
+        using TB = TileBox<true>;
+        ok = level_tmap(g, x, 4, kBX, TB::BY, TB::BZ, &mx) && level_tmap(g, b, 4, kTX, kTY, kTZ, &mb);
+        mc = mb;
+    } else {
+        using TB = TileBox<false>;
+        ok = level_tmap(g, x, 4, kBX, TB::BY, TB::BZ, &mx) && level_tmap(g, b, 3, kTX, kTY, kTZ, &mb) &&
+             level_tmap(g, L.cb, 1, kTX, kTY, kTZ, &mc);
+    }
+    if (!ok) {
         note(cudaErrorNotSupported);
         return;
     }
@@ -2834,11 +2843,11 @@ void launch_dgs_tile_phases(const LevelK& L, double* x, const double* b, int T, 
         attr = true;
     }
     if (fwd)
-        launch_k(k_dgs_tile<true>, dim3(hx * hy * hz), dim3(kTileThreads), TileBox<true>::SMEM, s, mc, L, x, b, T, ph0,
-                 ph1, ntx, nty);
-    else
-        launch_k(k_dgs_tile<false>, dim3(hx * hy * hz), dim3(kTileThreads), TileBox<false>::SMEM, s, mc, L, x, b, T,
+        launch_k(k_dgs_tile<true>, dim3(hx * hy * hz), dim3(kTileThreads), TileBox<true>::SMEM, s, mx, mb, mc, L, x, T,
                  ph0, ph1, ntx, nty);
+    else
+        launch_k(k_dgs_tile<false>, dim3(hx * hy * hz), dim3(kTileThreads), TileBox<false>::SMEM, s, mx, mb, mc, L, x,
+                 T, ph0, ph1, ntx, nty);
     count();
 }
 
