@@ -67,6 +67,8 @@ typedef struct smg_params {
 } smg_params;
 
 #define SMG_FLAG_SKIP_REVERSE_DGS 1 /* fault injection: symmetry negative control */
+#define SMG_FLAG_NO_PRECOND 2       /* solve_driver method `sqmr`: smg_sqmr_solve runs
+                                      Alg. 4 with the identity preconditioner, t = s */
 
 /* ResidualHistory: caller-owned arrays of `capacity` entries. */
 typedef struct smg_history {

@@ -195,12 +195,14 @@ using FieldVector = std::vector<double>;
 // ------------------------------------------------------------------ hierarchy
 class MgHierarchy {
    public:
-    MgHierarchy(const CellGrid& g, double eta, double gamma, int n, const CycleConfig& cfg, int device = 0) {
+    // flags: SMG_FLAG_* (SMG_FLAG_NO_PRECOND: sqmr_solve on this hierarchy runs un-preconditioned)
+    MgHierarchy(const CellGrid& g, double eta, double gamma, int n, const CycleConfig& cfg, int device = 0,
+                int flags = 0) {
         for (auto l : g.labels)
             if (l != CellLabel::Interior)
                 throw std::invalid_argument("build_hierarchy: the GPU path takes the walled box (all cells Interior)");
         grid_ = smg_grid_desc{3, g.extents[0], g.extents[1], g.extents[2], g.h};
-        prm_ = smg_params{eta,  gamma, n, cfg.smoother.nu, cfg.smoother.band_width, 0, static_cast<int>(cfg.kind),
+        prm_ = smg_params{eta,  gamma, n, cfg.smoother.nu, cfg.smoother.band_width, flags, static_cast<int>(cfg.kind),
                           static_cast<int>(cfg.smoother.kind), cfg.smoother.omega, 0};
         const int rc = smg_create(&grid_, &prm_, 1, &device, &ctx_);
         if (rc == SMG_ECAP) throw std::length_error("build_hierarchy: coarsest system above the dense cap (SPEC:365)");
@@ -215,6 +217,7 @@ class MgHierarchy {
     }
     smg_ctx* ctx() const { return ctx_; }
     int levels() const { return smg_num_levels(ctx_); }
+    int flags() const { return prm_.flags; }
     std::int64_t ndof(int level = 0) const { return smg_level_ndof(ctx_, level, nullptr); }
     void check(int rc, const char* what) const {
         if (rc == 0) return;
@@ -235,8 +238,8 @@ class MgHierarchy {
 
 // build_hierarchy
 inline MgHierarchy build_hierarchy(const CellGrid& g, double eta, double gamma, int n, const CycleConfig& cfg = {},
-                                   int device = 0) {
-    return MgHierarchy(g, eta, gamma, n, cfg, device);
+                                   int device = 0, int flags = 0) {
+    return MgHierarchy(g, eta, gamma, n, cfg, device, flags);
 }
 
 // ----------------------------------------------------------- operators
@@ -342,6 +345,19 @@ inline SolveResult sqmr_solve(const LevelOperator& L, const MgHierarchy& precond
     return detail::run_solver(precond, b, maxit, [&](smg_ctx* c, const double* bb, double* x, smg_history* hh, int* st) {
         return smg_sqmr_solve(c, bb, x, tol, maxit, hh, st);
     });
+}
+
+// solve_driver: method mg = mg_solve on L~, mg-sqmr = sqmr_solve with the cycle,
+// sqmr = Alg. 4 with the identity preconditioner (the hierarchy must carry SMG_FLAG_NO_PRECOND:
+// the iteration is captured once per hierarchy, so the method is fixed at build time).
+enum class Method { Mg, MgSqmr, Sqmr };
+inline SolveResult solve_driver(const MgHierarchy& h, Method method, const FieldVector& b, double tol, int maxit) {
+    const bool plain = (h.flags() & SMG_FLAG_NO_PRECOND) != 0;
+    if (method == Method::Mg) return mg_solve(h, b, tol, maxit);
+    if ((method == Method::Sqmr) != plain)
+        throw std::invalid_argument("solve_driver: method sqmr needs a hierarchy built with SMG_FLAG_NO_PRECOND "
+                                    "(and mg-sqmr one without)");
+    return sqmr_solve(LevelOperator{&h, 0, false}, h, b, tol, maxit);
 }
 
 // assemble_rhs for the walled box: body force f (compact order, pressures

@@ -18,6 +18,7 @@ LIB_PATH = os.environ.get("SMG_LIB") or os.path.join(_HERE, "libsmg.so")  # SMG_
 
 SMG_CONVERGED, SMG_MAX_ITERATIONS, SMG_BREAKDOWN = 0, 1, 2
 FLAG_SKIP_REVERSE_DGS = 1
+FLAG_NO_PRECOND = 2  # method `sqmr`: identity preconditioner
 FORCE_UNIFORM, FORCE_FOURIER, FORCE_CHANNEL = 0, 1, 2
 
 # smoother op codes of smg_smoother (include/smg.h)

@@ -23,6 +23,7 @@
 #include <cuda_profiler_api.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges cost nothing unless a tool (nsys / ncu --nvtx) is attached
 #include <nccl.h>  // types only: libnccl.so.2 is loaded at run time (single-process contexts never need it)
 
 #include "../../include/smg.h"
@@ -35,6 +36,20 @@ namespace {
 struct SmgError : std::runtime_error {
     int code;
     SmgError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+// NVTX range of a host-side region (solve / iteration / V-cycle level / smooth / transfers): the
+// tracing hook of SURVEY §5.  Inside a stream capture it marks the capture, not the replay.
+struct Nvtx {
+    explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+    Nvtx(const char* name, int l) {
+        char buf[48];
+        std::snprintf(buf, sizeof buf, "%s L%d", name, l);
+        nvtxRangePushA(buf);
+    }
+    ~Nvtx() { nvtxRangePop(); }
+    Nvtx(const Nvtx&) = delete;
+    Nvtx& operator=(const Nvtx&) = delete;
 };
 
 #define CK(call)                                                                                  \
@@ -710,6 +725,7 @@ void vanka_additive(smg_ctx* c, int l, double* x, const double* b) {
 }
 
 void smooth(smg_ctx* c, int l, double* x, const double* b, bool cb_ready = false) {
+    Nvtx r("smooth", l);
     if (c->prm.vanka == 1) {  // Alg. 3 with additive Vanka on V1
         for (int k = 0; k < c->prm.nu; ++k) vanka_additive(c, l, x, b);
         symmetric_dgs(c, l, x, b, cb_ready);
@@ -726,6 +742,7 @@ void coarse_solve(smg_ctx* c, const double* b, double* x) {
 }
 
 void vcycle(smg_ctx* c, int l, const double* b, double* x) {
+    Nvtx r("vcycle", l);
     DevLevel& L = c->lv[l];
     if (l == static_cast<int>(c->lv.size()) - 1) { coarse_solve(c, b, x); return; }
     CK(cudaMemsetAsync(x, 0, vlen(L) * sizeof(double), c->st));
@@ -821,6 +838,7 @@ void halo_nccl(smg_ctx* m, double* v, const Geom& g, int nf) {
 
 // halo exchange of a slab level: 2 planes each way between neighbours; nf fields
 void exchange(smg_ctx* m, int l, Sel sel, int nf) {
+    Nvtx r("halo_exchange", l);
     if (m->mp) {
         halo_nccl(m, sel(m->lv[l]), m->lv[l].k.g, nf);
         return;
@@ -976,6 +994,7 @@ void dist_dgs_sym(smg_ctx* m, int l) {
 }
 
 void dist_smooth(smg_ctx* m, int l) {
+    Nvtx r("dist_smooth", l);
     dist_vanka_sym(m, l);
     dist_dgs_sym(m, l);
     dist_vanka_sym(m, l);
@@ -983,6 +1002,7 @@ void dist_smooth(smg_ctx* m, int l) {
 
 // V-cycle on the parts; level-l b must hold valid halos
 void dist_vcycle(smg_ctx* m, int l) {
+    Nvtx r("dist_vcycle", l);
     if (l >= m->ndist) {  // replicated: every part runs the identical single-part cycle
         each(m, [&](smg_ctx* p) { vcycle(p, l, p->lv[l].b, p->lv[l].x); });
         return;
@@ -1150,11 +1170,18 @@ void dots(smg_ctx* m, double* (*a)(smg_ctx*), double* (*b)(smg_ctx*), double* (*
 }
 
 void pc_vcycle(smg_ctx* m) {  // t = V(s) on the fine level
+    if (m->prm.flags & SMG_FLAG_NO_PRECOND) {  // method `sqmr`: identity preconditioner
+        each(m, [&](smg_ctx* p) {
+            CK(cudaMemcpyAsync(v_t(p), v_s(p), vlen(p->lv[0]) * sizeof(double), cudaMemcpyDeviceToDevice, p->st));
+        });
+        return;
+    }
     if (m->ndist > 0) dist_vcycle(m, 0);
     else vcycle(m, 0, m->lv[0].b, m->lv[0].x);
 }
 
 void sqmr_iteration(smg_ctx* m, int par) {
+    Nvtx r("sqmr_iteration");
     auto halo = [&](smg_ctx* p, int& lo, int& hi) {
         lo = m->ndist > 0 && p->rank > 0;
         hi = m->ndist > 0 && p->rank + 1 < p->nparts;
@@ -1182,6 +1209,7 @@ void sqmr_iteration(smg_ctx* m, int par) {
 }
 
 int sqmr(smg_ctx* m, double tol, int maxit, smg_history* hist, int* status) {
+    Nvtx r("sqmr_solve");
     auto t0 = std::chrono::steady_clock::now();
     const int64_t l0 = launch_count();
     int64_t graph_launches = 0;
@@ -1236,6 +1264,7 @@ int sqmr(smg_ctx* m, double tol, int maxit, smg_history* hist, int* status) {
         }
         for (int j = 1; j <= maxit && st == SMG_MAX_ITERATIONS; ++j) {
             const int par = (j - 1) & 1;
+            Nvtx rj("sqmr_iter", j);
             if (single) {
                 CK(cudaGraphLaunch(par ? m->graph2 : m->graph, m->st));
                 graph_launches += m->graph_kernels;

@@ -278,6 +278,24 @@ def test_mg_solve_and_wcycle_bitwise(n, levels):
         s.close()
 
 
+@pytest.mark.parametrize("dims,levels,parts", [((16, 16, 16), 2, 1), ((32, 16, 16), 2, 1), ((32, 32, 32), 3, 2)])
+def test_unpreconditioned_sqmr_bitwise(dims, levels, parts):
+    """solve_driver method `sqmr`: Alg. 4 with the identity preconditioner
+    (SMG_FLAG_NO_PRECOND) against the oracle's precond = 0 run, bit for bit -- slow to converge by
+    design (PAPER Fig. 8: "the pure SQMR ... fails"), so the history is compared, not the status."""
+    nx, ny, nz = dims
+    o = oracle.Oracle(nx, ny, nz, h=1 / ny, levels=levels)
+    kw = dict(devices=[0] * parts) if parts > 1 else {}
+    s = smg.Solver(nx, ny, nz, h=1 / ny, levels=levels, flags=smg.FLAG_NO_PRECOND, **kw)
+    b = o.forcing(oracle.FORCE_UNIFORM, 21)
+    xo, ho, _, sto = o.sqmr(b, 1e-6, 60, precond=False)
+    xg, hg, _, stg = s.sqmr(b, 1e-6, 60)
+    assert sto == stg and len(ho) == len(hg) == 60
+    assert np.array_equal(ho, hg) and np.array_equal(xo, xg)
+    assert hg[-1] < hg[0]
+    s.close()
+
+
 def test_wcycle_symmetric_gpu():
     s = smg.Solver(16, levels=4, cycle=1)  # 16 -> 8 -> 4 -> 2: W active at level 1
     o = oracle.Oracle(16, levels=4, cycle=1)

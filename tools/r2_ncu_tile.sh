@@ -14,5 +14,9 @@ for r in $O/${T}_*.ncu-rep; do
   ncu -i $r --page details --csv > ${r%.ncu-rep}_details.csv 2>&1
   ncu -i $r --page source --csv > ${r%.ncu-rep}_source.csv 2>&1
 done
-timeout 1500 python -m pytest tests -m gpu -q > $O/${T}_pytest.log 2>&1; echo "pytest rc=$?" >> $O/${T}_pytest.log
+# cfg 3 golden (first 3 iterations) on the box's host: the oracle needs ~120 GB of RAM
+free -g > $O/${T}_host.txt; nproc >> $O/${T}_host.txt
+if [ "${GOLDEN3:-0}" = 1 ]; then
+  timeout 2400 python tests/golden/make_golden.py cfg3 > $O/${T}_golden_cfg3.log 2>&1 && cp tests/golden/cfg3_history.json $O/
+fi
 ls -la $O
