@@ -413,9 +413,12 @@ def b_iter_model(cnt, nu=1):
 
 
 def roofline(s, levels, peak, peak_kind, iter_ms, config_key=None, share=1.0):
-    """Dominant component: the fine-level smooth (Alg. 3 = nu Vanka + symmetric DGS + nu Vanka), which is
-    ~45% of an iteration at cfg 1.  Algorithmic bytes per SURVEY §8(d): 48 B per V2 DOF (symmetric DGS) +
-    96 nu B per V1 DOF (two symmetric Vanka sweeps)."""
+    """Dominant kernel: the fine-level symmetric DGS sweep (~40% of the cfg-2 iteration) -- on a tiled
+    level 16 launches of k_dgs_tile (8 tile colours forward, 8 reverse) after one k_dgs_cb, else 13
+    per-step kernels.  Algorithmic bytes per SURVEY 8(d): 48 B per V2 DOF per symmetric sweep;
+    `achieved` = those bytes / the sweep's CUDA-event time (the same ratio as bytes per launch / average
+    launch duration).  Components: the whole smooth (Alg. 3, 48 B per V2 DOF + 96 nu B per V1 DOF),
+    the Vanka sweep, apply L, and the whole iteration against B_iter."""
     cnt = level_counts(s, levels)
     n0, v1, v2 = cnt[0]
     if share != 1.0:  # one rank of a z-slab run: its kernels cover its share of the fine level
@@ -425,34 +428,44 @@ def roofline(s, levels, peak, peak_kind, iter_ms, config_key=None, share=1.0):
     dgs_ms = s.time_kernel(2, reps, 0)
     vanka_ms = s.time_kernel(4, reps, 0)
     apply_ms = s.time_kernel(0, 20, 0)
-    alg = 48 * v2 + 96 * v1
-    achieved = alg / (smooth_ms / 1e3) / 1e9
+    alg_smooth = 48 * v2 + 96 * v1
+    alg = 48 * v2
+    achieved = alg / (dgs_ms / 1e3) / 1e9
     biter = b_iter_model(cnt)
-    # measured DRAM bytes of one fine-level smooth (all its kernels), from the committed ncu
-    # launch list of `tools/profile_kernel.py --which 5 --level 0` (profiles/smooth_traffic.json)
-    traffic = None
-    tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "smooth_traffic.json")
+    tiled = s.dgs_tiled(0) if hasattr(s, "dgs_tiled") else False
+    # measured DRAM bytes from the committed ncu launch list of one fine-level smooth
+    # (`tools/profile_kernel.py --which 5 --level 0` -> profiles/smooth_traffic.json)
+    traffic = smooth_traffic = None
+    tpath = os.path.join(ROOT, "profiles", "smooth_traffic.json")
     if os.path.exists(tpath):
         rec = json.load(open(tpath)).get(config_key)
         if rec:
-            traffic = rec["dram_bytes"]
+            smooth_traffic = rec["dram_bytes"]
+            div = rec.get("component_launches_in_range", 1)
+            dgs = [v["dram_bytes"] for k, v in rec["per_kernel_in_range"].items() if "k_dgs_" in k]
+            traffic = sum(dgs) / div if dgs else None
+    nl = 17 if tiled else 14
     return {
         "bound": "hbm",
-        "kernel": "fine-level smooth (Alg. 3: Vanka sweep, symmetric DGS = 20 phases in 13 steps, Vanka sweep)",
+        "kernel": ("k_dgs_tile: fine-level symmetric DGS sweep in tile order (k_dgs_cb + 16 TMA-staged launches)"
+                   if tiled else "fine-level symmetric DGS sweep (k_dgs_cb + 13 per-step kernels)"),
         "achieved": achieved, "peak": peak, "peak_source": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-        "traffic": traffic, "traffic_source": "ncu dram__bytes_read+write, all kernels of one smooth (cold caches)",
-        "algorithmic_bytes_per_launch": alg, "avg_ms": smooth_ms,
+        "traffic": traffic,
+        "traffic_source": "ncu dram__bytes_read+write of the sweep's kernels (cold caches), profiles/smooth_traffic.json",
+        "algorithmic_bytes_per_launch": alg / nl, "avg_launch_ms": dgs_ms / nl, "launches_per_sweep": nl,
+        "algorithmic_bytes_per_sweep": alg, "avg_ms": dgs_ms,
         "units": {"N_V2": v2, "N_V1": v1, "bytes_per_V2_dof": 48, "bytes_per_V1_dof": 96},
         "components": {
-            "dgs_sym_sweep": {"avg_ms": dgs_ms, "alg_bytes": 48 * v2,
-                              "achieved_gbs": 48 * v2 / (dgs_ms / 1e3) / 1e9},
+            "smooth_alg3": {"avg_ms": smooth_ms, "alg_bytes": alg_smooth,
+                            "achieved_gbs": alg_smooth / (smooth_ms / 1e3) / 1e9,
+                            "frac": alg_smooth / (smooth_ms / 1e3) / 1e9 / peak, "traffic": smooth_traffic},
             "vanka_sym_sweep": {"avg_ms": vanka_ms, "alg_bytes": 48 * v1,
                                 "achieved_gbs": 48 * v1 / (vanka_ms / 1e3) / 1e9,
-                                "note": "latency-bound: 16 dependent barrier steps per sweep"},
+                                "note": "V1 shell: sector-bound gathers, 8 dependent phases per sweep"},
             "apply_L": {"avg_ms": apply_ms, "alg_bytes": 16 * n0, "achieved_gbs": 16 * n0 / (apply_ms / 1e3) / 1e9},
         },
         "iteration": {"alg_bytes": biter, "ms": iter_ms, "achieved_gbs": biter / (iter_ms / 1e3) / 1e9,
-                      "frac": biter / (iter_ms / 1e3) / 1e9 / (peak / share), "model": "SURVEY §8(d) B_iter",
+                      "frac": biter / (iter_ms / 1e3) / 1e9 / (peak / share), "model": "SURVEY 8(d) B_iter",
                       "peak_gbs_all_gpus": peak / share},
     }
 

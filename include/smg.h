@@ -59,7 +59,8 @@ typedef struct smg_params {
     int band_width;  /* V1 band width (Chebyshev)                      */
     int flags;       /* SMG_FLAG_*                                     */
     int cycle;       /* 0 V-cycle, 1 W-cycle       */
-    int vanka;       /* 0 symmetric multiplicative, 1 additive */
+    int vanka;       /* 0 symmetric multiplicative, 1 additive, 2 direct solve on V1
+                        (dense, |V1| <= 20000, benchmarking mode) */
     double omega;    /* additive damping in (0, 1]; <= 0 means 1.0 (SPEC default) */
     int64_t dgs_tile_min; /* DGS traversal (OD-1 rev. 2): levels with >= this many cells whose
                              extents are multiples of 16 x 8 x 8 (>= 2 tiles per axis) sweep
@@ -142,7 +143,8 @@ int smg_residual(smg_ctx* ctx, int level, const double* x, const double* b, doub
  * level arg = phase + 32 T acts on the tiles of colour T only), 1
  * symmetric_dgs, 2 one Vanka colour (arg = colour 0..7), 3 symmetric
  * multiplicative Vanka, 4 smooth (Alg. 3, with the params' Vanka flavour), 5 one
- * additive Vanka application.  x is updated in place. */
+ * additive Vanka application, 7 one direct-on-V1 solve (params.vanka = 2).  x is
+ * updated in place. */
 int smg_smoother(smg_ctx* ctx, int level, int op, int arg, double* x, const double* b);
 
 /* transfer between level and level+1: rc = R rf, xf = P xc. */

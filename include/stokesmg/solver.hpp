@@ -177,7 +177,7 @@ inline CellGrid coarsen_grid(const CellGrid& f) {
 }
 
 // ------------------------------------------------------------ configuration
-enum class BoundarySmoother { Multiplicative = 0, Additive = 1 };
+enum class BoundarySmoother { Multiplicative = 0, Additive = 1, Direct = 2 };  // Direct: SPEC:314, 333
 struct SmootherConfig {
     BoundarySmoother kind = BoundarySmoother::Multiplicative;
     int nu = 1;          // boundary sweeps per side

@@ -235,6 +235,10 @@ struct Level {
     std::map<int, std::array<double, 49>> vk_inv;  // factorisation cache keyed by face mask
     // face -> (left cell, right cell) pressure ids, for the distributive update
     std::vector<std::array<int32_t, 2>> fcells;
+    // direct-on-V1 mode: the V1 DOFs ascending and, built on first use, the exactly
+    // symmetrised dense inverse of the V1 x V1 principal sub-block of L~
+    std::vector<int32_t> v1_ids;
+    mutable std::vector<double> v1_inv;
 };
 
 static inline double val(const vec& x, int32_t id) { return id >= 0 ? x[id] : 0.0; }
@@ -485,6 +489,9 @@ static void build_level(Level& L, const CellGrid& g, double eta, double gamma, i
     // Vanka blocks: one per band cell with an active
     // pressure; slots [uL,uR,vL,vR,wL,wR,p]; colour (i&1)+2(j&1)+4(k&1).
     for (int k = 0; k < 8; ++k) L.vk[k].clear();
+    L.v1_ids.clear();
+    for (int64_t q = 0; q < m.N; ++q)
+        if (m.v1[q]) L.v1_ids.push_back(static_cast<int32_t>(q));
     L.vk_all.clear();
     L.vk_inv.clear();
     std::vector<std::pair<int32_t, double>> row;
@@ -807,24 +814,67 @@ static void vanka_additive(const Level& L, vec& x, const vec& b, double omega) {
         if (hit[q]) x[q] = x[q] + omega * acc[q];
 }
 
+// Direct-on-V1 (PAPER section 6 "the ideal scenario where a direct solver is employed
+// for the boundary domains"): x_V1 <- x_V1 + A11^{-1} (b - L~x)_V1 with A11 the V1 x V1 principal
+// sub-block of L~, i.e. the exact solve of the V1 equations with x_V2 frozen.  A11^{-1} is a dense
+// symmetric inverse (the coarsest solve's LU + exact symmetrisation, OD-4) applied with the coarse
+// GEMV's summation order (64-column chunks, ascending); capped like the coarsest system.
+static void vanka_direct(const Level& L, vec& x, const vec& b) {
+    const auto& ids = L.v1_ids;
+    const int64_t n = static_cast<int64_t>(ids.size());
+    if (n == 0) return;
+    if (L.v1_inv.empty()) {
+        if (n > 20000) throw std::runtime_error("direct-on-V1: |V1| above the dense cap 20000 (SPEC:365)");
+        std::vector<int32_t> loc(L.map.N, -1);
+        for (int64_t k = 0; k < n; ++k) loc[ids[k]] = static_cast<int32_t>(k);
+        std::vector<double> a(static_cast<size_t>(n) * n, 0.0);
+        std::vector<std::pair<int32_t, double>> row;
+        for (int64_t k = 0; k < n; ++k) {
+            ltilde_row(L, ids[k], row);
+            for (auto& e : row)
+                if (loc[e.first] >= 0) a[static_cast<size_t>(k) * n + loc[e.first]] += e.second;
+        }
+        L.v1_inv = dense_inverse_sym(std::move(a), static_cast<int>(n), std::max(1, g_threads));
+    }
+    vec r(n);
+    const int64_t nv = L.map.off[3];
+    parallel_for(n, g_threads, [&](int64_t k) {
+        const int32_t id = ids[k];
+        r[k] = b[id] - (id < nv ? mom_row(L, x, id) : cont_row(L, x, id, L.gamma));
+    });
+    parallel_for(n, g_threads, [&](int64_t i) {
+        const double* kk = &L.v1_inv[static_cast<size_t>(i) * n];
+        double sum = 0.0;
+        for (int64_t j0 = 0; j0 < n; j0 += 64) {
+            double part = 0.0;
+            const int64_t j1 = std::min<int64_t>(n, j0 + 64);
+            for (int64_t j = j0; j < j1; ++j) part = part + kk[j] * r[j];
+            sum = sum + part;
+        }
+        x[ids[i]] = x[ids[i]] + sum;
+    });
+}
+
 // Vanka flavour of the smoother (SmootherConfig).
 struct VankaCfg {
-    int kind = 0;        // 0 symmetric multiplicative, 1 additive
+    int kind = 0;        // 0 symmetric multiplicative, 1 additive, 2 direct solve on V1
     double omega = 1.0;  // additive damping
 };
 static VankaCfg g_vanka_default;
 
 static void vanka_apply(const Level& L, vec& x, const vec& b, const VankaCfg& vc, int order = 0) {
     if (vc.kind == 1) vanka_additive(L, x, b, vc.omega);
+    else if (vc.kind == 2) vanka_direct(L, x, b);
     else vanka_symmetric(L, x, b, order);
 }
 
 // smooth, Alg. 3: nu x Vanka(V1), symmetric DGS(V2), nu x Vanka(V1).
 static void smooth(const Level& L, vec& x, const vec& b, int nu, bool skip_reverse = false,
                    const VankaCfg& vc = g_vanka_default, int order = 0) {
-    for (int k = 0; k < nu; ++k) vanka_apply(L, x, b, vc, order);
+    const int reps = vc.kind == 2 ? 1 : nu;  // an exact V1 solve is idempotent: once per side
+    for (int k = 0; k < reps; ++k) vanka_apply(L, x, b, vc, order);
     symmetric_dgs(L, x, b, skip_reverse, order);
-    for (int k = 0; k < nu; ++k) vanka_apply(L, x, b, vc, order);
+    for (int k = 0; k < reps; ++k) vanka_apply(L, x, b, vc, order);
 }
 
 // ------------------------------------------------------------ transfer ------
@@ -1362,7 +1412,7 @@ void orc_residual(void* h, int l, const double* x, const double* b, double* r) {
     out(rr, r);
 }
 // op: 0 one DGS phase (arg = phase 0..19), 1 symmetric DGS, 2 one Vanka colour
-// (arg = colour), 3 symmetric Vanka, 4 smooth (Alg. 3), 5 one additive Vanka.
+// (arg = colour), 3 symmetric Vanka, 4 smooth (Alg. 3), 5 one additive Vanka, 7 one direct-on-V1 solve.
 int orc_smoother(void* h, int l, int op, int arg, double* x, const double* b) {
     try {
         Hierarchy& H = HH(h);
@@ -1375,6 +1425,7 @@ int orc_smoother(void* h, int l, int op, int arg, double* x, const double* b) {
         else if (op == 3) vanka_symmetric(L, xx, bb, H.order);
         else if (op == 4) smooth(L, xx, bb, H.nu, H.skip_reverse, H.vanka, H.order);
         else if (op == 5) vanka_additive(L, xx, bb, H.vanka.omega);
+        else if (op == 7) vanka_direct(L, xx, bb);
         else throw std::runtime_error("bad smoother op");
         out(xx, x);
         return 0;

@@ -23,7 +23,8 @@ FORCE_UNIFORM, FORCE_FOURIER, FORCE_CHANNEL = 0, 1, 2
 
 # smoother op codes of smg_smoother (include/smg.h)
 OP_DGS_PHASE, OP_DGS_SYM, OP_VANKA_COLOUR, OP_VANKA_SYM, OP_SMOOTH, OP_VANKA_ADD = 0, 1, 2, 3, 4, 5
-VANKA_MULTIPLICATIVE, VANKA_ADDITIVE = 0, 1
+VANKA_MULTIPLICATIVE, VANKA_ADDITIVE, VANKA_DIRECT = 0, 1, 2
+OP_VANKA_DIRECT = 7  # one direct-on-V1 solve
 DGS_PHASES = 20
 
 
@@ -253,6 +254,11 @@ class Solver:
     def ndof(self, level=0):
         c = np.zeros(5, np.int64)
         return int(lib().smg_level_ndof(self._ctx, level, c))
+
+    def dgs_tiled(self, level=0):
+        """True if the level's DGS sweep runs in tile order (k_dgs_tile) under this solver's tile_min."""
+        nx, ny, nz = self.dims
+        return dgs_tile(nx, ny, nz, level, self.params.dgs_tile_min)[0] == 8
 
     def counts(self, level=0):
         c = np.zeros(5, np.int64)

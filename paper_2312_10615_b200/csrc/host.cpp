@@ -255,6 +255,11 @@ struct DevLevel {
     int va_n = 0;
     double* va_d7 = nullptr;
     double* ktab = nullptr;  // [64][49]
+    // direct-on-V1 (params.vanka == 2): symmetric dense inverse of the V1 x V1
+    // principal sub-block of L~ and the padded slots of the V1 DOFs (ascending compact order)
+    double* v1_k = nullptr;
+    int32_t* v1_slots = nullptr;
+    int v1_n = 0;
 };
 
 }  // namespace
@@ -331,6 +336,101 @@ namespace {
 int64_t vlen(const DevLevel& L) { return L.k.g.vec_len(); }
 
 
+// Dense rows of L~ on a box level in compact numbering, restricted to the DOFs with
+// sel[id] >= 0 (sel = nullptr: every DOF): A[sel[r] * nsel + sel[c]], and the padded slot of every
+// selected DOF.  Entries accumulate in the oracle's ltilde_row order (diagonal, six neighbours,
+// p_left, p_right; continuity: the six faces, then -gamma), so A is bit-identical to the oracle's.
+void assemble_box_dense(const DevLevel& C, double gamma, const int32_t* sel, int nsel, std::vector<double>& A,
+                        std::vector<int32_t>& slots) {
+    const int nx = C.k.g.nx, ny = C.k.g.ny, nz = C.k.g.nz;
+    const int64_t nu = C.counts[0], nv = C.counts[1], nw = C.counts[2];
+    auto uid = [&](int x, int y, int z) -> int {
+        if (x < 1 || x > nx - 1 || y < 0 || y >= ny || z < 0 || z >= nz) return -1;
+        return static_cast<int>((static_cast<int64_t>(z) * ny + y) * (nx - 1) + (x - 1));
+    };
+    auto vid = [&](int x, int y, int z) -> int {
+        if (x < 0 || x >= nx || y < 1 || y > ny - 1 || z < 0 || z >= nz) return -1;
+        return static_cast<int>(nu + (static_cast<int64_t>(z) * (ny - 1) + (y - 1)) * nx + x);
+    };
+    auto wid = [&](int x, int y, int z) -> int {
+        if (x < 0 || x >= nx || y < 0 || y >= ny || z < 1 || z > nz - 1) return -1;
+        return static_cast<int>(nu + nv + (static_cast<int64_t>(z - 1) * ny + y) * nx + x);
+    };
+    auto pid = [&](int x, int y, int z) -> int {
+        if (x < 0 || x >= nx || y < 0 || y >= ny || z < 0 || z >= nz) return -1;
+        return static_cast<int>(nu + nv + nw + (static_cast<int64_t>(z) * ny + y) * nx + x);
+    };
+    auto loc = [&](int id) { return id < 0 ? -1 : (sel ? sel[id] : id); };
+    A.assign(static_cast<size_t>(nsel) * nsel, 0.0);
+    slots.assign(nsel, 0);
+    const double e2 = C.k.eta_h2, ih = C.k.inv_h;
+    auto put = [&](int r, int col, double v) {
+        const int c = loc(col);
+        if (c >= 0) A[static_cast<size_t>(r) * nsel + c] += v;
+    };
+    for (int z = 0; z < nz; ++z)
+        for (int y = 0; y < ny; ++y)
+            for (int x = 0; x < nx; ++x) {
+                const int64_t sl = C.k.g.slot(x, y, z);
+                for (int comp = 0; comp < 3; ++comp) {
+                    auto fid = [&](int a, int b2, int c3) {
+                        return comp == 0 ? uid(a, b2, c3) : comp == 1 ? vid(a, b2, c3) : wid(a, b2, c3);
+                    };
+                    const int r = loc(fid(x, y, z));
+                    if (r < 0) continue;
+                    slots[r] = static_cast<int32_t>(comp * C.k.g.fs + sl);
+                    put(r, fid(x, y, z), 6.0 * e2);
+                    const int d[6][3] = {{-1, 0, 0}, {1, 0, 0}, {0, -1, 0}, {0, 1, 0}, {0, 0, -1}, {0, 0, 1}};
+                    for (int k = 0; k < 6; ++k) put(r, fid(x + d[k][0], y + d[k][1], z + d[k][2]), -e2);
+                    const int lx = x - (comp == 0), ly = y - (comp == 1), lz = z - (comp == 2);
+                    put(r, pid(lx, ly, lz), -ih);
+                    put(r, pid(x, y, z), ih);
+                }
+                const int r = loc(pid(x, y, z));
+                if (r < 0) continue;
+                slots[r] = static_cast<int32_t>(3 * C.k.g.fs + sl);
+                put(r, uid(x, y, z), ih);
+                put(r, uid(x + 1, y, z), -ih);
+                put(r, vid(x, y, z), ih);
+                put(r, vid(x, y + 1, z), -ih);
+                put(r, wid(x, y, z), ih);
+                put(r, wid(x, y, z + 1), -ih);
+                put(r, pid(x, y, z), -gamma);
+            }
+}
+
+// compact id -> index among the V1 DOFs (ascending), -1 for V2 (partition_band)
+int v1_selection(const DevLevel& L, int bw, std::vector<int32_t>& sel) {
+    const int nx = L.k.g.nx, ny = L.k.g.ny, nz = L.k.g.nz;
+    auto band = [&](int x, int y, int z) {
+        return x < bw || y < bw || z < bw || x >= nx - bw || y >= ny - bw || z >= nz - bw;
+    };
+    sel.assign(static_cast<size_t>(L.N), -1);
+    int n = 0;
+    for (int z = 0; z < nz; ++z)
+        for (int y = 0; y < ny; ++y)
+            for (int x = 1; x < nx; ++x)
+                if (band(x, y, z) || band(x - 1, y, z)) sel[(static_cast<int64_t>(z) * ny + y) * (nx - 1) + (x - 1)] = 0;
+    for (int z = 0; z < nz; ++z)
+        for (int y = 1; y < ny; ++y)
+            for (int x = 0; x < nx; ++x)
+                if (band(x, y, z) || band(x, y - 1, z))
+                    sel[L.counts[0] + (static_cast<int64_t>(z) * (ny - 1) + (y - 1)) * nx + x] = 0;
+    for (int z = 1; z < nz; ++z)
+        for (int y = 0; y < ny; ++y)
+            for (int x = 0; x < nx; ++x)
+                if (band(x, y, z) || band(x, y, z - 1))
+                    sel[L.counts[0] + L.counts[1] + (static_cast<int64_t>(z - 1) * ny + y) * nx + x] = 0;
+    for (int z = 0; z < nz; ++z)
+        for (int y = 0; y < ny; ++y)
+            for (int x = 0; x < nx; ++x)
+                if (band(x, y, z))
+                    sel[L.counts[0] + L.counts[1] + L.counts[2] + (static_cast<int64_t>(z) * ny + y) * nx + x] = 0;
+    for (auto& v : sel)
+        if (v == 0) v = n++;
+    return n;
+}
+
 // ---- setup ----
 void build(smg_ctx* c, const std::vector<double>* shared_coarse = nullptr, std::vector<double>* coarse_out = nullptr,
            cudaStream_t shared_stream = nullptr) {
@@ -341,9 +441,11 @@ void build(smg_ctx* c, const std::vector<double>* shared_coarse = nullptr, std::
     if (p.levels < 1) throw SmgError(SMG_EINVAL, "levels < 1");
     if (p.nu < 1 || p.band_width < 1) throw SmgError(SMG_EINVAL, "nu and band_width must be >= 1");
     if (p.cycle != 0 && p.cycle != 1) throw SmgError(SMG_EINVAL, "cycle must be 0 (V) or 1 (W)");
-    if (p.vanka != 0 && p.vanka != 1) throw SmgError(SMG_EINVAL, "vanka must be 0 (multiplicative) or 1 (additive)");
+    if (p.vanka < 0 || p.vanka > 2)
+        throw SmgError(SMG_EINVAL, "vanka must be 0 (multiplicative), 1 (additive) or 2 (direct solve on V1)");
     if (p.omega > 1.0) throw SmgError(SMG_EINVAL, "omega must lie in (0, 1] (<= 0: default 1)");
-    if (p.vanka == 1 && c->ndist > 0) throw SmgError(SMG_EINVAL, "additive Vanka: single-part contexts only");
+    if (p.vanka != 0 && c->ndist > 0)
+        throw SmgError(SMG_EINVAL, "additive Vanka / direct-on-V1: single-part contexts only");
     if (!(g.h > 0)) throw SmgError(SMG_EINVAL, "h must be > 0");
     const int div = 1 << (p.levels - 1);
     if (g.nx % div || g.ny % div || g.nz % div)
@@ -540,6 +642,20 @@ void build(smg_ctx* c, const std::vector<double>* shared_coarse = nullptr, std::
             CK(cudaMemcpyAsync(L.va_mask, am.data(), am.size(), cudaMemcpyHostToDevice, c->st));
             CK(cudaStreamSynchronize(c->st));
         }
+        if (p.vanka == 2 && !dist && l + 1 < p.levels) {  // direct-on-V1: A11^{-1}, dense (capped like the coarsest)
+            std::vector<int32_t> sel, vslots;
+            const int n1 = v1_selection(L, bw, sel);
+            if (n1 > 20000) throw SmgError(SMG_ECAP, "direct-on-V1: |V1| above the dense cap 20000 (SPEC:365)");
+            std::vector<double> A11;
+            assemble_box_dense(L, p.gamma, sel.data(), n1, A11, vslots);
+            const std::vector<double> K1 = dense_inverse_sym(std::move(A11), n1);
+            L.v1_n = n1;
+            L.v1_k = c->dalloc<double>(static_cast<int64_t>(n1) * n1);
+            L.v1_slots = c->dalloc<int32_t>(n1);
+            CK(cudaMemcpyAsync(L.v1_k, K1.data(), K1.size() * sizeof(double), cudaMemcpyHostToDevice, c->st));
+            CK(cudaMemcpyAsync(L.v1_slots, vslots.data(), vslots.size() * sizeof(int32_t), cudaMemcpyHostToDevice, c->st));
+            CK(cudaStreamSynchronize(c->st));
+        }
         // local inverses C_i L~ C_i^T per face mask, scattered to the 7-slot layout
         std::vector<double> ktab(64 * 49, 0.0);
         for (int m = 0; m < 64; ++m) {
@@ -580,59 +696,9 @@ void build(smg_ctx* c, const std::vector<double>* shared_coarse = nullptr, std::
     if (C.N > 20000) throw SmgError(SMG_ECAP, "coarsest system above dense cap 20000 (SPEC:365): add levels");
     const int n = static_cast<int>(C.N);
     c->nc = n;
-    const int nx = C.k.g.nx, ny = C.k.g.ny, nz = C.k.g.nz;
-    const int64_t nu = C.counts[0], nv = C.counts[1], nw = C.counts[2];
-    auto uid = [&](int x, int y, int z) -> int {
-        if (x < 1 || x > nx - 1 || y < 0 || y >= ny || z < 0 || z >= nz) return -1;
-        return static_cast<int>((static_cast<int64_t>(z) * ny + y) * (nx - 1) + (x - 1));
-    };
-    auto vid = [&](int x, int y, int z) -> int {
-        if (x < 0 || x >= nx || y < 1 || y > ny - 1 || z < 0 || z >= nz) return -1;
-        return static_cast<int>(nu + (static_cast<int64_t>(z) * (ny - 1) + (y - 1)) * nx + x);
-    };
-    auto wid = [&](int x, int y, int z) -> int {
-        if (x < 0 || x >= nx || y < 0 || y >= ny || z < 1 || z > nz - 1) return -1;
-        return static_cast<int>(nu + nv + (static_cast<int64_t>(z - 1) * ny + y) * nx + x);
-    };
-    auto pid = [&](int x, int y, int z) -> int {
-        if (x < 0 || x >= nx || y < 0 || y >= ny || z < 0 || z >= nz) return -1;
-        return static_cast<int>(nu + nv + nw + (static_cast<int64_t>(z) * ny + y) * nx + x);
-    };
-    std::vector<double> A(static_cast<size_t>(n) * n, 0.0);
-    std::vector<int32_t> slots(n);
-    const double e2 = C.k.eta_h2, ih = C.k.inv_h;
-    auto put = [&](int r, int col, double v) {
-        if (col >= 0) A[static_cast<size_t>(r) * n + col] += v;
-    };
-    for (int z = 0; z < nz; ++z)
-        for (int y = 0; y < ny; ++y)
-            for (int x = 0; x < nx; ++x) {
-                const int64_t sl = C.k.g.slot(x, y, z);
-                for (int comp = 0; comp < 3; ++comp) {
-                    auto fid = [&](int a, int b2, int c3) {
-                        return comp == 0 ? uid(a, b2, c3) : comp == 1 ? vid(a, b2, c3) : wid(a, b2, c3);
-                    };
-                    const int id = fid(x, y, z);
-                    if (id < 0) continue;
-                    slots[id] = static_cast<int32_t>(comp * C.k.g.fs + sl);
-                    // row order as ltilde_row of the oracle: diag, 6 nbrs, p_left, p_right
-                    put(id, id, 6.0 * e2);
-                    const int d[6][3] = {{-1, 0, 0}, {1, 0, 0}, {0, -1, 0}, {0, 1, 0}, {0, 0, -1}, {0, 0, 1}};
-                    for (int k = 0; k < 6; ++k) put(id, fid(x + d[k][0], y + d[k][1], z + d[k][2]), -e2);
-                    const int lx = x - (comp == 0), ly = y - (comp == 1), lz = z - (comp == 2);
-                    put(id, pid(lx, ly, lz), -ih);
-                    put(id, pid(x, y, z), ih);
-                }
-                const int id = pid(x, y, z);
-                slots[id] = static_cast<int32_t>(3 * C.k.g.fs + sl);
-                put(id, uid(x, y, z), ih);
-                put(id, uid(x + 1, y, z), -ih);
-                put(id, vid(x, y, z), ih);
-                put(id, vid(x, y + 1, z), -ih);
-                put(id, wid(x, y, z), ih);
-                put(id, wid(x, y, z + 1), -ih);
-                put(id, id, -p.gamma);
-            }
+    std::vector<double> A;
+    std::vector<int32_t> slots;
+    assemble_box_dense(C, p.gamma, nullptr, n, A, slots);
     std::vector<double> K;
     if (shared_coarse) K = *shared_coarse;  // same matrix on every part: factorise once
     else K = dense_inverse_sym(std::move(A), n);
@@ -724,8 +790,23 @@ void vanka_additive(smg_ctx* c, int l, double* x, const double* b) {
     launch_vanka_additive(L.k, x, b, L.va_cells, L.va_mask, L.va_n, L.ktab, L.va_d7, c->prm.omega, c->st);
 }
 
+// direct-on-V1: x_V1 += A11^{-1} (b - L~x)_V1 -- the residual into the level's r
+// scratch, then the dense symmetric inverse applied in the coarse GEMV's summation order
+void vanka_direct(smg_ctx* c, int l, double* x, const double* b) {
+    DevLevel& L = c->lv[l];
+    if (!L.v1_k) throw SmgError(SMG_EINVAL, "direct-on-V1 needs params.vanka = 2 (single-part contexts)");
+    launch_apply(L.k, x, b, L.r, L.k.gamma, c->st);
+    launch_coarse_gemv(L.v1_k, L.v1_slots, L.v1_n, L.r, x, c->st, /*accumulate=*/true);
+}
+
 void smooth(smg_ctx* c, int l, double* x, const double* b, bool cb_ready = false) {
     Nvtx r("smooth", l);
+    if (c->prm.vanka == 2) {  // Alg. 3 with the exact V1 solve (idempotent: once per side)
+        vanka_direct(c, l, x, b);
+        symmetric_dgs(c, l, x, b, cb_ready);
+        vanka_direct(c, l, x, b);
+        return;
+    }
     if (c->prm.vanka == 1) {  // Alg. 3 with additive Vanka on V1
         for (int k = 0; k < c->prm.nu; ++k) vanka_additive(c, l, x, b);
         symmetric_dgs(c, l, x, b, cb_ready);
@@ -1583,6 +1664,8 @@ int smg_smoother(smg_ctx* c, int level, int op, int arg, double* x, const double
                                   L.xb, L.vk_refresh, L.vk_nrefresh, L.sw_pairs);
         } else if (op == 5) {  // one additive Vanka application
             vanka_additive(c, level, L.x, L.b);
+        } else if (op == 7) {  // one direct-on-V1 solve
+            vanka_direct(c, level, L.x, L.b);
         } else if (op == 6) {  // per-phase reference path of the symmetric sweeps (test only)
             if (L.k.tiled) {
                 for (int T = 0; T < 8; ++T)

@@ -494,7 +494,7 @@ __global__ void k_prolong_add(LevelK F, LevelK C, const double* __restrict__ E, 
 // oracle).  K symmetric => column j of K is row j, read coalesced across rows.
 constexpr int CG_ROWS = 32, CG_LANES = 32;
 __global__ void k_coarse_gemv(const double* __restrict__ K, const int32_t* __restrict__ slots, int n,
-                              const double* __restrict__ B, double* __restrict__ X) {
+                              const double* __restrict__ B, double* __restrict__ X, int accumulate) {
     pdl_wait();
     extern __shared__ double part[];  // [nchunks][CG_ROWS]
     const int row = blockIdx.x * CG_ROWS + threadIdx.x;
@@ -511,7 +511,7 @@ __global__ void k_coarse_gemv(const double* __restrict__ K, const int32_t* __res
     if (threadIdx.y == 0 && row < n) {
         double s = 0.0;
         for (int ch = 0; ch < nchunks; ++ch) s = s + part[ch * CG_ROWS + threadIdx.x];
-        X[slots[row]] = s;
+        X[slots[row]] = accumulate ? X[slots[row]] + s : s;
     }
 }
 
@@ -2227,13 +2227,24 @@ __device__ __forceinline__ void tma_load(void* dst, const CUtensorMap* m, int c0
         : "memory");
 }
 
+// L2 prefetch of a box (no shared-memory destination, no barrier): a hint only, always safe
+__device__ __forceinline__ void tma_prefetch(const CUtensorMap* m, int c0, int c1, int c2, int c3) {
+    asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];" ::"l"(
+                     reinterpret_cast<uint64_t>(m)),
+                 "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+                 : "memory");
+}
+
 // FWD: phases [ph0, ph1) within 0..9; REV: within 10..19 -- on the tiles of colour T.
+// pf > 0: the CTA also prefetches into L2 the boxes of tile blockIdx.x + pf (the CTA most likely to
+// take this SM slot next: pf = resident CTAs of the device), so that tile's TMA loads hit L2
+// while this tile computes.
 // tmx: x box map; tmb: b (tile box, NB fields); tmc: m^T b (tile box, one field; REV only).
 template <bool FWD>
 __global__ void __launch_bounds__(kTileThreads, 2)
     k_dgs_tile(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmb,
                const __grid_constant__ CUtensorMap tmc, LevelK L, double* __restrict__ X, int T, int ph0, int ph1,
-               int ntx, int nty) {
+               int ntx, int nty, int pf) {
     using TB = TileBox<FWD>;
     extern __shared__ __align__(128) double tsm_raw[];
     // 128-byte aligned by pointer arithmetic on the shared array (an integer round trip would hide
@@ -2263,6 +2274,14 @@ __global__ void __launch_bounds__(kTileThreads, 2)
         tma_load(xs, &tmx, x0 - 2 + g.xo, y0, z0 - 1 + g.zg, 0, bar);
         tma_load(bs, &tmb, x0 + g.xo, y0 + 1, z0 + g.zg, 0, bar);
         if (!FWD) tma_load(ts, &tmc, x0 + g.xo, y0 + 1, z0 + g.zg, 0, bar);
+        const int bn = bi + pf;
+        if (pf > 0 && bn < static_cast<int>(gridDim.x)) {
+            const int nx0 = (2 * (bn % hx) + (T & 1)) * kTX, ny0 = (2 * ((bn / hx) % hy) + ((T >> 1) & 1)) * kTY,
+                      nz0 = (2 * (bn / (hx * hy)) + pz) * kTZ;
+            tma_prefetch(&tmx, nx0 - 2 + g.xo, ny0, nz0 - 1 + g.zg, 0);
+            tma_prefetch(&tmb, nx0 + g.xo, ny0 + 1, nz0 + g.zg, 0);
+            if (!FWD) tma_prefetch(&tmc, nx0 + g.xo, ny0 + 1, nz0 + g.zg, 0);
+        }
     }
     if (FWD)
         for (int k = tid; k < TB::TS; k += kTileThreads) ts[k] = 0.0;
@@ -2443,7 +2462,7 @@ void launch_prolong_add(const LevelK& F, const LevelK& C, const double* xc, doub
     count();
 }
 void launch_coarse_gemv(const double* ksym, const int32_t* slots, int n, const double* b, double* x,
-                        cudaStream_t s) {
+                        cudaStream_t s, bool accumulate) {
     const int nchunks = (n + 63) / 64;
     const size_t smem = static_cast<size_t>(nchunks) * CG_ROWS * sizeof(double);
     static bool attr_set = false;
@@ -2451,7 +2470,8 @@ void launch_coarse_gemv(const double* ksym, const int32_t* slots, int n, const d
         cudaFuncSetAttribute(k_coarse_gemv, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         attr_set = true;
     }
-    launch_k(k_coarse_gemv, (n + CG_ROWS - 1) / CG_ROWS, dim3(CG_ROWS, CG_LANES), smem, s, ksym, slots, n, b, x);
+    launch_k(k_coarse_gemv, (n + CG_ROWS - 1) / CG_ROWS, dim3(CG_ROWS, CG_LANES), smem, s, ksym, slots, n, b, x,
+             accumulate ? 1 : 0);
     count();
 }
 void launch_pack(const LevelK& L, const double* padded, double* compact, cudaStream_t s) {
@@ -2842,12 +2862,15 @@ void launch_dgs_tile_phases(const LevelK& L, double* x, const double* b, int T, 
                                   static_cast<int>(TileBox<false>::SMEM)));
         attr = true;
     }
+    // SMG_TILE_PF: L2 prefetch distance in CTAs (0 = off, the default: measured 2.19 (off) / 2.16 (148) /
+    // 2.30 (296) / 2.40 ms (592) per cfg-2 fine sweep -- the loads are not latency-exposed)
+    static const int pf = env_int("SMG_TILE_PF", 0);
     if (fwd)
         launch_k(k_dgs_tile<true>, dim3(hx * hy * hz), dim3(kTileThreads), TileBox<true>::SMEM, s, mx, mb, mc, L, x, T,
-                 ph0, ph1, ntx, nty);
+                 ph0, ph1, ntx, nty, pf);
     else
         launch_k(k_dgs_tile<false>, dim3(hx * hy * hz), dim3(kTileThreads), TileBox<false>::SMEM, s, mx, mb, mc, L, x,
-                 T, ph0, ph1, ntx, nty);
+                 T, ph0, ph1, ntx, nty, pf);
     count();
 }
 

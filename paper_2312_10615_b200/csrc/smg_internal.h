@@ -119,8 +119,9 @@ void launch_dgs_sym_coop(const LevelK& L, double* x, const double* b, double* d0
 void launch_restrict(const LevelK& F, const LevelK& C, const double* rf, double* bc, cudaStream_t s, int zc_lo = 0,
                      int nzc = -1);
 void launch_prolong_add(const LevelK& F, const LevelK& C, const double* xc, double* xf, cudaStream_t s);
+// x[slots] = K b[slots] (accumulate: x[slots] += K b[slots], the direct-on-V1 correction)
 void launch_coarse_gemv(const double* ksym, const int32_t* slots, int n, const double* b, double* x,
-                        cudaStream_t s);
+                        cudaStream_t s, bool accumulate = false);
 void launch_pack(const LevelK& L, const double* padded, double* compact, cudaStream_t s);
 void launch_unpack(const LevelK& L, const double* compact, double* padded, cudaStream_t s);
 

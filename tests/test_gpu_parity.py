@@ -296,6 +296,30 @@ def test_unpreconditioned_sqmr_bitwise(dims, levels, parts):
     s.close()
 
 
+@pytest.mark.parametrize("dims,levels", [((8, 8, 8), 2), ((16, 8, 8), 2), ((16, 16, 16), 3)])
+def test_direct_on_v1_bitwise(dims, levels):
+    """Direct-on-V1 boundary smoother (params.vanka = 2): the exact solve of the V1
+    equations through the dense symmetric inverse of the V1 x V1 sub-block of L~ -- one application,
+    Alg. 3 with it, the V-cycle and MG-SQMR bit-identical to the oracle; the V1 residual vanishes."""
+    oracle.set_threads(os.cpu_count() or 1)
+    nx, ny, nz = dims
+    o = oracle.Oracle(nx, ny, nz, h=1 / ny, levels=levels, vanka=2)
+    s = smg.Solver(nx, ny, nz, h=1 / ny, levels=levels, vanka=smg.VANKA_DIRECT)
+    n = o.ndof(0)
+    x, b = rnd(n, 90), rnd(n, 91)
+    y = s.smoother(smg.OP_VANKA_DIRECT, x, b)
+    same(y, o.smoother(7, x, b))
+    y2 = s.smoother(smg.OP_VANKA_DIRECT, y, b)  # idempotent up to rounding
+    assert np.abs(y2 - y).max() <= 1e-10 * np.abs(y).max()
+    same(s.smoother(smg.OP_SMOOTH, x, b), o.smoother(4, x, b))
+    bb = o.forcing(oracle.FORCE_UNIFORM, 13)
+    same(s.vcycle(bb), o.vcycle(bb))
+    xo, ho, _, sto = o.sqmr(bb, 1e-8, 40)
+    xg, hg, _, stg = s.sqmr(bb, 1e-8, 40)
+    assert sto == stg == smg.SMG_CONVERGED and np.array_equal(ho, hg) and np.array_equal(xo, xg)
+    s.close()
+
+
 def test_wcycle_symmetric_gpu():
     s = smg.Solver(16, levels=4, cycle=1)  # 16 -> 8 -> 4 -> 2: W active at level 1
     o = oracle.Oracle(16, levels=4, cycle=1)

@@ -320,3 +320,53 @@ def test_vanka_complementary_colours_commute_bitwise(p):
     d = o.smoother(OP_VCOL, o.smoother(OP_VCOL, x0, b, 0, p), b, 0, p ^ 1)
     e = o.smoother(OP_VCOL, o.smoother(OP_VCOL, x0, b, 0, p ^ 1), b, 0, p)
     assert not np.array_equal(d, e)
+
+
+# ---- SPEC-literal traversal order vs the coloured order the GPU runs ----
+@pytest.mark.parametrize("n,levels,seed", [(32, 3, 0), (64, 4, 7)])
+def test_spec_order_iteration_count_within_one(n, levels, seed):
+    """The oracle's ORDER_SPEC mode runs the SPEC's literal sequential order: DGS over ascending
+    DOF index then its exact reverse, multiplicative Vanka colour-major 0..7 then 7..0, blocks of a
+    colour in sequence.  The coloured / tiled order the GPU reproduces bit for bit (ORDER_GPU) must
+    reach the tolerance within +-1 iteration of it (north_star) and to the same solution.
+    Recorded: 32^3 7 vs 7, 64^3 8 vs 7, cfg 1 (128^3, 5 levels, seed 1) 8 vs 8 iterations."""
+    import os
+    oracle.set_threads(os.cpu_count() or 1)
+    b = oracle.forcing_box(n, n, n, 1 / n, oracle.FORCE_UNIFORM, seed)
+    out = {}
+    for order in (oracle.ORDER_GPU, oracle.ORDER_SPEC):
+        x, h, _, st = oracle.Oracle(n, levels=levels, order=order).sqmr(b, 1e-6, 100)
+        assert st == 0 and h[-1] < 1e-6
+        out[order] = (x, len(h))
+    (xg, kg), (xs, ks) = out[oracle.ORDER_GPU], out[oracle.ORDER_SPEC]
+    assert abs(kg - ks) <= 1, (kg, ks)
+    npres = n ** 3
+    assert np.linalg.norm(xg[:-npres] - xs[:-npres]) <= 2e-5 * np.linalg.norm(xs[:-npres])
+    oracle.set_threads(1)
+
+
+# ---- direct-on-V1 boundary smoother (SPEC:314, 333; SURVEY 8(f)4) ----
+def test_direct_on_v1_exact_and_symmetric():
+    """One application zeroes the V1 rows of the residual (the exact solve of the V1 equations with
+    x_V2 frozen); Alg. 3 and the V-cycle built on it stay symmetric (Theorem 4's argument: the V1
+    solve is a symmetric map); MG-SQMR with it converges at least as fast as with Vanka."""
+    o = oracle.Oracle(8, levels=2, vanka=2)
+    n = o.ndof(0)
+    rng = np.random.default_rng(31)
+    x, b = rng.uniform(-1, 1, n), rng.uniform(-1, 1, n)
+    y = o.smoother(7, x, b)
+    r = b - o.apply(y, penalized=True)
+    om = oracle.Oracle(8, levels=2)
+    # V1 rows: the DOFs a multiplicative Vanka sweep may change
+    v1 = om.smoother(OP_VANKA, x, b) != x
+    assert v1.sum() == o.census()[1] if hasattr(o, "census") else True
+    assert np.abs(r[v1]).max() <= 1e-9 * np.abs(b).max()
+    assert np.array_equal(y[~v1], x[~v1])
+    C = materialize(lambda e: o.smoother(OP_SMOOTH, np.zeros(n), e), n)
+    assert defect(C) < 1e-10
+    W = materialize(o.vcycle, n)
+    assert defect(W) < 1e-10
+    bb = o.forcing(oracle.FORCE_UNIFORM, 3)
+    _, hd, _, sd = o.sqmr(bb, 1e-8, 50)
+    _, hm, _, sm_ = om.sqmr(bb, 1e-8, 50)
+    assert sd == sm_ == 0 and len(hd) <= len(hm) + 1
