@@ -247,6 +247,7 @@ struct DevLevel {
     // then parity 7-m; see VankaPairs)
     int32_t* sw_cells[8] = {};
     uint8_t* sw_mask[8] = {};
+    uint8_t* sw_amask[8] = {};  // z-slab levels: owned slots per block of the (merged) sweep lists
     int sw_n[8] = {};
     VankaPairs sw_pairs;
     // additive Vanka (params.vanka == 1): every block in one list + the 7-field correction scratch
@@ -606,10 +607,13 @@ void build(smg_ctx* c, const std::vector<double>* shared_coarse = nullptr, std::
         for (int col = 0; col < 8; ++col) {
             L.sw_cells[col] = L.vk_cells[col];
             L.sw_mask[col] = L.vk_mask[col];
+            L.sw_amask[col] = L.vk_amask[col];
             L.sw_n[col] = L.vk_n[col];
         }
         L.sw_pairs = VankaPairs{};
-        const int pm = vanka_pairs_pay(L.vk_n);
+        // slab levels run per-phase kernels (no persistent-sweep capacity to respect): always merge,
+        // so every part of a level takes the same 8 phases
+        const int pm = dist ? 0xf : vanka_pairs_pay(L.vk_n);
         for (int pq = 0; pq < 4; ++pq) {
             if (!((pm >> pq) & 1)) continue;
             std::vector<int32_t> mc(cells[pq]);
@@ -623,6 +627,12 @@ void build(smg_ctx* c, const std::vector<double>* shared_coarse = nullptr, std::
             L.sw_mask[pq] = c->dalloc<uint8_t>(L.sw_n[pq]);
             CK(cudaMemcpyAsync(L.sw_cells[pq], mc.data(), mc.size() * sizeof(int32_t), cudaMemcpyHostToDevice, c->st));
             CK(cudaMemcpyAsync(L.sw_mask[pq], mm.data(), mm.size(), cudaMemcpyHostToDevice, c->st));
+            if (dist) {
+                std::vector<uint8_t> ma(amasks[pq]);
+                ma.insert(ma.end(), amasks[7 - pq].begin(), amasks[7 - pq].end());
+                L.sw_amask[pq] = c->dalloc<uint8_t>(L.sw_n[pq]);
+                CK(cudaMemcpyAsync(L.sw_amask[pq], ma.data(), ma.size(), cudaMemcpyHostToDevice, c->st));
+            }
             CK(cudaStreamSynchronize(c->st));
             L.sw_pairs.pairs |= 1 << pq;
             L.sw_pairs.first[pq] = static_cast<int>(cells[pq].size());
@@ -974,15 +984,25 @@ void each(smg_ctx* m, F&& f) {
     CK(cudaSetDevice(m->device));
 }
 
+// Symmetric multiplicative Vanka on a slab level: the merged complementary colour pairs of the
+// single-part sweep (8 Jacobi phases instead of 16 when all four pairs pay, bit-identical), one halo
+// exchange per phase.  The pair decision depends on the level's global list sizes only through
+// vanka_pairs_pay of this part's lists; parts of one level hold the same colours, so every part
+// takes the same phases.
 void dist_vanka_sym(smg_ctx* m, int l) {
+    const int pairs = m->lv[l].sw_pairs.pairs;
+    for (smg_ctx* p : m->parts)
+        if (p->lv[l].sw_pairs.pairs != pairs) throw SmgError(SMG_EINVAL, "slab parts disagree on the merged Vanka pairs");
     for (int sweep = 0; sweep < m->prm.nu; ++sweep)
         for (int k = 0; k < 16; ++k) {
-            const int col = vanka_order(k < 8 ? k : 15 - k);
+            const int j = k < 8 ? k : 15 - k;
+            const int col = vanka_order(j);
+            if ((j & 1) && ((pairs >> (7 - col)) & 1)) continue;  // folded into its partner's phase
             each(m, [&](smg_ctx* p) {
                 DevLevel& L = p->lv[l];
-                launch_vanka_delta(L.k, L.x, L.b, L.vk_cells[col], L.vk_mask[col], L.vk_n[col], L.ktab, p->vk_delta, p->st);
-                launch_vanka_apply(L.k, L.x, L.vk_cells[col], L.vk_mask[col], L.vk_n[col], p->vk_delta, p->st,
-                                   L.vk_amask[col]);
+                launch_vanka_delta(L.k, L.x, L.b, L.sw_cells[col], L.sw_mask[col], L.sw_n[col], L.ktab, p->vk_delta, p->st);
+                launch_vanka_apply(L.k, L.x, L.sw_cells[col], L.sw_mask[col], L.sw_n[col], p->vk_delta, p->st,
+                                   L.sw_amask[col]);
             });
             exchange(m, l, sel_x, 4);
         }
@@ -1294,7 +1314,12 @@ int sqmr(smg_ctx* m, double tol, int maxit, smg_history* hist, int* status) {
     auto t0 = std::chrono::steady_clock::now();
     const int64_t l0 = launch_count();
     int64_t graph_launches = 0;
-    const bool single = m->ndist == 0;
+    // The iteration replays as a CUDA graph for a single part and for one-process-per-GPU slab
+    // ranks (NCCL send/recv, all-reduce and all-gather are captured with the kernels on the rank's
+    // one stream: no host launch latency between the ~10^3 phase kernels and halo groups of a
+    // V-cycle; SMG_DIST_GRAPH=0 keeps eager launches).  In-process parts on several streams stay eager.
+    static const bool dist_graph = !(std::getenv("SMG_DIST_GRAPH") && std::atoi(std::getenv("SMG_DIST_GRAPH")) == 0);
+    const bool single = m->ndist == 0 || (m->mp && dist_graph);
     CK(cudaEventRecord(m->ev0, m->st));
     if (hist) hist->count = 0;
     each(m, [&](smg_ctx* p) {

@@ -111,3 +111,36 @@ def test_restrict_zmarch_slabs_bitwise(zseg, monkeypatch):
     assert np.array_equal(many.vcycle(b), one.vcycle(b))
     one.close()
     many.close()
+
+
+def _ndev():
+    import ctypes
+    try:
+        rt = ctypes.CDLL("libcudart.so")
+    except OSError:
+        try:
+            import torch
+            return torch.cuda.device_count()
+        except Exception:
+            return 1
+    n = ctypes.c_int(0)
+    return n.value if rt.cudaGetDeviceCount(ctypes.byref(n)) == 0 else 1
+
+
+@pytest.mark.skipif(_ndev() < 2, reason="needs >= 2 visible GPUs (peer copies over NVLink between real devices)")
+@pytest.mark.parametrize("n,levels", [(64, 4), (128, 5)])
+def test_two_device_parts_bitwise(n, levels):
+    """In-process z-slab parts on DIFFERENT devices (one stream each, event barriers, peer halo
+    copies): bit-identical to one device.  Runs whenever the box exposes at least two GPUs."""
+    ndev = min(_ndev(), 8)
+    while n % ndev or (n // ndev) % 2:
+        ndev -= 1
+    one = smg.Solver(n, levels=levels)
+    many = smg.Solver(n, levels=levels, devices=list(range(ndev)))
+    b = smg.forcing(n, kind=smg.FORCE_UNIFORM, seed=23)
+    assert np.array_equal(many.vcycle(b), one.vcycle(b))
+    x1, h1, _, s1 = one.sqmr(b, 1e-6, 60)
+    x2, h2, _, s2 = many.sqmr(b, 1e-6, 60)
+    assert s1 == s2 == smg.SMG_CONVERGED and np.array_equal(h1, h2) and np.array_equal(x1, x2)
+    one.close()
+    many.close()
