@@ -94,6 +94,27 @@ typedef struct smg_timing {
  * Results are bit-identical for every ngpu. */
 int smg_create(const smg_grid_desc* grid, const smg_params* params, int ngpu, const int* dev_ids,
                smg_ctx** out);
+/* General labelled domain (PAPER section 5): labels[(z*ny + y)*nx + x] is the CellLabel
+ * of cell (x, y, z) -- 0 Dirichlet, 1 Interior, 2 Exterior -- inside the implicit
+ * Dirichlet ring.  classify_dofs: a face between two Interior cells is
+ * active, a face of a Dirichlet cell carries the value 0, a face touching an Exterior cell is
+ * Inactive (homogeneous Neumann: its stencil legs are dropped); pressures are active
+ * in Interior cells.  coarsen_grid labels the coarser levels, partition_band
+ * gives V1 / V2, Vanka blocks are factorised once per signature class.
+ * Extents must be divisible by 2^(levels-1) (pad with Exterior cells).  One GPU; the
+ * smoother runs one kernel per phase (no DGS tiling), params.vanka 0 or 2.  Every other entry
+ * point works on the context; vectors are the compact FieldVector of this DofMap. */
+int smg_create_labeled(const smg_grid_desc* grid, const uint8_t* labels, const smg_params* params, int device,
+                       smg_ctx** out);
+/* coarsen_grid, host only: out holds (nx/2)(ny/2)(nz/2) labels; even extents. */
+int smg_coarsen_labels(const smg_grid_desc* grid, const uint8_t* labels, uint8_t* out);
+/* classify_dofs + partition_band census of a labelled grid (host only):
+ * out6 = {N, |V1|, n_u, n_v, n_w, n_p}; returns N. */
+int64_t smg_census_labeled(const smg_grid_desc* grid, const uint8_t* labels, int band_width, int64_t* out6);
+/* smg_forcing on the active faces of a labelled grid (same generator: a function of the seed,
+ * the component and the face's storage coordinates). */
+int smg_forcing_labeled(const smg_grid_desc* grid, const uint8_t* labels, int kind, uint64_t seed, double* b);
+
 /* Multi-process z-slab decomposition: one process per GPU, NCCL over NVLink.
  * Rank 0 calls smg_nccl_unique_id and the caller's launcher (torch.distributed,
  * MPI, ...) broadcasts the 128-byte id; every rank then calls smg_create_rank

@@ -20,10 +20,11 @@
 // Errors follow the SPEC: length mismatch throws std::invalid_argument (SPEC:125,
 // 208, 216), the coarse dense cap throws std::length_error, other
 // failures std::runtime_error carrying smg_last_error(); solver outcomes are a
-// status, not an exception.  The GPU path covers the walled box
-// (every labelled cell Interior inside an implicit Dirichlet ring, the BASELINE
-// configurations); build_hierarchy rejects other labellings with
-// std::invalid_argument.  Link with -lsmg (paper_2312_10615_b200/libsmg.so).
+// status, not an exception.  build_hierarchy takes any labelled CellGrid:
+// the walled box (every cell Interior inside the implicit Dirichlet ring, the BASELINE
+// configurations) runs the box kernels (smg_create); a grid with Dirichlet or Exterior cells
+// runs the labelled-domain kernels (smg_create_labeled: obstacles, homogeneous-Neumann
+// faces with dropped stencil legs).  Link with -lsmg (paper_2312_10615_b200/libsmg.so).
 #pragma once
 
 #include <cmath>
@@ -198,13 +199,17 @@ class MgHierarchy {
     // flags: SMG_FLAG_* (SMG_FLAG_NO_PRECOND: sqmr_solve on this hierarchy runs un-preconditioned)
     MgHierarchy(const CellGrid& g, double eta, double gamma, int n, const CycleConfig& cfg, int device = 0,
                 int flags = 0) {
-        for (auto l : g.labels)
-            if (l != CellLabel::Interior)
-                throw std::invalid_argument("build_hierarchy: the GPU path takes the walled box (all cells Interior)");
+        if (g.labels.size() != static_cast<std::size_t>(g.extents[0]) * g.extents[1] * g.extents[2])
+            throw std::invalid_argument("build_hierarchy: labels length != product of extents (SPEC:28)");
+        bool box = true;
+        for (auto l : g.labels) box = box && l == CellLabel::Interior;
         grid_ = smg_grid_desc{3, g.extents[0], g.extents[1], g.extents[2], g.h};
         prm_ = smg_params{eta,  gamma, n, cfg.smoother.nu, cfg.smoother.band_width, flags, static_cast<int>(cfg.kind),
                           static_cast<int>(cfg.smoother.kind), cfg.smoother.omega, 0};
-        const int rc = smg_create(&grid_, &prm_, 1, &device, &ctx_);
+        static_assert(sizeof(CellLabel) == 1, "CellLabel is the C-ABI's uint8 label");
+        const int rc = box ? smg_create(&grid_, &prm_, 1, &device, &ctx_)
+                           : smg_create_labeled(&grid_, reinterpret_cast<const std::uint8_t*>(g.labels.data()), &prm_,
+                                                device, &ctx_);
         if (rc == SMG_ECAP) throw std::length_error("build_hierarchy: coarsest system above the dense cap (SPEC:365)");
         if (rc == SMG_EINVAL) throw std::invalid_argument("build_hierarchy: invalid grid / parameters");
         if (rc != 0) throw std::runtime_error("build_hierarchy: smg_create failed (" + std::to_string(rc) + ")");

@@ -42,6 +42,9 @@ def lib():
         L.orc_create.restype = C.c_void_p
         L.orc_create.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double,
                                  C.c_int, C.c_int, C.c_int, C.c_int64]
+        L.orc_create_labeled.restype = C.c_void_p
+        L.orc_create_labeled.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, _U8, C.c_double, C.c_double,
+                                         C.c_int, C.c_int, C.c_int]
         L.orc_set_order.argtypes = [C.c_void_p, C.c_int]
         L.orc_dgs_tile.argtypes = [C.c_void_p, C.c_int, np.ctypeslib.ndpointer(dtype=np.int32, flags="C_CONTIGUOUS")]
         L.orc_destroy.argtypes = [C.c_void_p]
@@ -123,15 +126,24 @@ class Oracle:
     """Walled box of nx*ny*nz interior cells (implicit Dirichlet ring), spacing h."""
 
     def __init__(self, nx, ny=None, nz=None, h=None, eta=1.0, gamma=1e-3, levels=2, nu=1,
-                 band_width=1, cycle=0, vanka=0, omega=1.0, tile_min=0, order=ORDER_GPU):
-        """tile_min: cell count from which a level's DGS sweep is tile-ordered (0: 256^3, the
+                 band_width=1, cycle=0, vanka=0, omega=1.0, tile_min=0, order=ORDER_GPU, labels=None):
+        """labels (optional): uint8 array shaped (nz, ny, nx), 0 = Dirichlet, 1 = Interior,
+        2 = Exterior (SPEC:22-25) -- a general labelled domain inside the implicit Dirichlet ring;
+        nx, ny, nz are then taken from its shape.
+        tile_min: cell count from which a level's DGS sweep is tile-ordered (0: 256^3, the
         GPU default; -1: never).  order: ORDER_GPU (the coloured order the GPU reproduces bit
         for bit) or ORDER_SPEC (SPEC-literal sequential lexicographic DGS / colour-major Vanka)."""
-        ny = nx if ny is None else ny
-        nz = nx if nz is None else nz
-        h = 1.0 / nx if h is None else h
         L = lib()
-        self._h = L.orc_create(nx, ny, nz, h, eta, gamma, levels, nu, band_width, int(tile_min))
+        if labels is not None:
+            lab = np.ascontiguousarray(labels, dtype=np.uint8)
+            nz, ny, nx = lab.shape
+            h = 1.0 / nx if h is None else h
+            self._h = L.orc_create_labeled(nx, ny, nz, h, lab.ravel(), eta, gamma, levels, nu, band_width)
+        else:
+            ny = nx if ny is None else ny
+            nz = nx if nz is None else nz
+            h = 1.0 / nx if h is None else h
+            self._h = L.orc_create(nx, ny, nz, h, eta, gamma, levels, nu, band_width, int(tile_min))
         if not self._h:
             raise RuntimeError("oracle: " + L.orc_last_error().decode())
         self.dims = (nx, ny, nz)

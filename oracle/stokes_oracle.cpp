@@ -232,7 +232,10 @@ struct Level {
     struct Block { std::array<int32_t, 7> dof; int mask; };
     std::vector<Block> vk[8];
     std::vector<Block> vk_all;  // every block, ascending cell index (additive Vanka's summation order)
-    std::map<int, std::array<double, 49>> vk_inv;  // factorisation cache keyed by face mask
+    // factorisation cache keyed by the block's signature class ("keyed by neighbor-label
+    // signature"): the active-face mask (bits 0-5) and, per active face, its dropped Neumann legs
+    // 6 - vdiag (3 bits each from bit 6) -- everything the local matrix depends on
+    std::map<int, std::array<double, 49>> vk_inv;
     // face -> (left cell, right cell) pressure ids, for the distributive update
     std::vector<std::array<int32_t, 2>> fcells;
     // direct-on-V1 mode: the V1 DOFs ascending and, built on first use, the exactly
@@ -410,8 +413,6 @@ static bool dgs_tiled(const int* n, int64_t tile_min) {
 static void build_level(Level& L, const CellGrid& g, double eta, double gamma, int band_width,
                         int64_t tile_min = 0) {
     if (g.dim != 3) throw std::runtime_error("operator is 3-D only");
-    for (uint8_t l : g.lab)
-        if (l == LAB_E) throw std::runtime_error("operator supports D/I labels only (cube/channel)");
     L.grid = g;
     L.map = classify(g, band_width);
     L.h = g.h;
@@ -508,6 +509,8 @@ static void build_level(Level& L, const CellGrid& g, double eta, double gamma, i
                     if (f[s] >= 0) mask |= 1 << s;
                 }
                 blk.dof[6] = pid;
+                for (int s = 0; s < 6; ++s)
+                    if (f[s] >= 0) mask |= static_cast<int>(6.0 - L.vdiag[f[s]]) << (6 + 3 * s);
                 blk.mask = mask;
                 const int col = (x & 1) + 2 * (y & 1) + 4 * (z & 1);
                 L.vk[col].push_back(blk);
@@ -1348,6 +1351,28 @@ void* orc_create(int nx, int ny, int nz, double h, double eta, double gamma, int
         auto* o = new OrcHandle();
         o->H = build_hierarchy(g, eta, gamma, levels, nu, band_width,
                                tile_min < 0 ? std::numeric_limits<int64_t>::max() : tile_min);
+        return o;
+    } catch (const std::exception& e) {
+        g_last_err = e.what();
+        return nullptr;
+    }
+}
+// General labelled domain: lab[(z * ny + y) * nx + x] in {0 Dirichlet, 1 Interior,
+// 2 Exterior} inside an implicit Dirichlet ring; DGS never tile-ordered.
+void* orc_create_labeled(int nx, int ny, int nz, double h, const uint8_t* lab, double eta, double gamma, int levels,
+                         int nu, int band_width) {
+    try {
+        CellGrid g;
+        g.dim = 3;
+        g.n[0] = nx;
+        g.n[1] = ny;
+        g.n[2] = nz;
+        g.h = h;
+        g.lab.assign(lab, lab + static_cast<size_t>(nx) * ny * nz);
+        for (uint8_t l : g.lab)
+            if (l > LAB_E) throw std::runtime_error("labels must be 0 (D), 1 (I) or 2 (E)");
+        auto* o = new OrcHandle();
+        o->H = build_hierarchy(g, eta, gamma, levels, nu, band_width, std::numeric_limits<int64_t>::max());
         return o;
     } catch (const std::exception& e) {
         g_last_err = e.what();

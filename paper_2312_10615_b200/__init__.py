@@ -59,10 +59,13 @@ EXPORTED = [
     "smg_last_timing", "smg_time_kernel", "smg_host_alloc", "smg_host_free", "smg_forcing",
     "smg_profiler_range", "smg_slab_plan", "smg_mg_solve", "smg_census", "smg_assemble_rhs",
     "smg_nccl_unique_id", "smg_create_rank", "smg_dgs_tile",
+    "smg_create_labeled", "smg_coarsen_labels", "smg_census_labeled", "smg_forcing_labeled",
 ]
+LAB_DIRICHLET, LAB_INTERIOR, LAB_EXTERIOR = 0, 1, 2  # CellLabel
 
 _lib = None
 _D = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
+_U8 = np.ctypeslib.ndpointer(dtype=np.uint8, flags="C_CONTIGUOUS")
 
 
 def lib():
@@ -112,6 +115,12 @@ def lib():
     L.smg_host_alloc.argtypes = [C.c_int64]
     L.smg_host_free.argtypes = [C.c_void_p]
     L.smg_forcing.argtypes = [C.POINTER(GridDesc), C.c_int, C.c_uint64, C.c_void_p, C.c_int]
+    L.smg_create_labeled.argtypes = [C.POINTER(GridDesc), _U8, C.POINTER(Params), C.c_int, C.POINTER(P)]
+    L.smg_coarsen_labels.argtypes = [C.POINTER(GridDesc), _U8, _U8]
+    L.smg_census_labeled.restype = C.c_int64
+    L.smg_census_labeled.argtypes = [C.POINTER(GridDesc), _U8, C.c_int,
+                                     np.ctypeslib.ndpointer(np.int64, flags="C_CONTIGUOUS")]
+    L.smg_forcing_labeled.argtypes = [C.POINTER(GridDesc), _U8, C.c_int, C.c_uint64, _D]
     _lib = L
     return L
 
@@ -132,6 +141,48 @@ def forcing(nx, ny=None, nz=None, h=None, kind=FORCE_UNIFORM, seed=0, threads=No
     rc = lib().smg_forcing(C.byref(g), kind, seed, b.ctypes.data, threads or os.cpu_count() or 1)
     if rc != 0:
         raise SmgError(f"smg_forcing failed ({rc})")
+    return b
+
+
+def _labels3(labels):
+    lab = np.ascontiguousarray(labels, dtype=np.uint8)
+    if lab.ndim != 3:
+        raise ValueError("labels must be shaped (nz, ny, nx)")
+    return lab
+
+
+def census_labels(labels, band_width=1):
+    """classify_dofs + partition_band census of a labelled grid (host only):
+    labels shaped (nz, ny, nx), 0 Dirichlet / 1 Interior / 2 Exterior."""
+    lab = _labels3(labels)
+    nz, ny, nx = lab.shape
+    out = np.zeros(6, np.int64)
+    n = lib().smg_census_labeled(C.byref(GridDesc(3, nx, ny, nz, 1.0)), lab.ravel(), band_width, out)
+    if n < 0:
+        raise SmgError(f"smg_census_labeled failed ({n})")
+    return {"N": int(out[0]), "V1": int(out[1]), "nu": int(out[2]), "nv": int(out[3]), "nw": int(out[4]),
+            "np": int(out[5])}
+
+
+def coarsen_labels(labels):
+    """coarsen_grid of a labelled grid with even extents (host only)."""
+    lab = _labels3(labels)
+    nz, ny, nx = lab.shape
+    out = np.zeros((nz // 2, ny // 2, nx // 2), np.uint8)
+    rc = lib().smg_coarsen_labels(C.byref(GridDesc(3, nx, ny, nz, 1.0)), lab.ravel(), out.reshape(-1))
+    if rc != 0:
+        raise SmgError(f"smg_coarsen_labels failed ({rc}): extents must be even and >= 2")
+    return out
+
+
+def forcing_labels(labels, h, kind=FORCE_UNIFORM, seed=0):
+    """Synthetic forcing on the active faces of a labelled grid (compact order of its DofMap)."""
+    lab = _labels3(labels)
+    nz, ny, nx = lab.shape
+    b = np.zeros(census_labels(lab)["N"])
+    rc = lib().smg_forcing_labeled(C.byref(GridDesc(3, nx, ny, nz, h)), lab.ravel(), kind, seed, b)
+    if rc != 0:
+        raise SmgError(f"smg_forcing_labeled failed ({rc})")
     return b
 
 
@@ -214,6 +265,26 @@ class Solver:
         self._ctx = ctx
         self.levels = L.smg_num_levels(ctx)
         self.dims = (nx, ny, nz)
+
+    @classmethod
+    def from_labels(cls, labels, h=None, eta=1.0, gamma=1e-3, levels=2, nu=1, band_width=1, flags=0, device=0,
+                    cycle=0, vanka=0):
+        """General labelled domain (smg_create_labeled): labels shaped (nz, ny, nx) with
+        0 Dirichlet, 1 Interior, 2 Exterior cells inside the implicit Dirichlet ring."""
+        lab = _labels3(labels)
+        nz, ny, nx = lab.shape
+        h = 1.0 / nx if h is None else h
+        self = cls.__new__(cls)
+        self.grid = GridDesc(3, nx, ny, nz, h)
+        self.params = Params(eta, gamma, levels, nu, band_width, flags, cycle, vanka, 1.0, -1)
+        ctx = C.c_void_p()
+        rc = lib().smg_create_labeled(C.byref(self.grid), lab.ravel(), C.byref(self.params), device, C.byref(ctx))
+        if rc != 0:
+            raise SmgError(f"smg_create_labeled failed ({rc}); see stderr")
+        self._ctx = ctx
+        self.levels = lib().smg_num_levels(ctx)
+        self.dims = (nx, ny, nz)
+        return self
 
     @classmethod
     def for_rank(cls, rank, nranks, nccl_id, nx, ny=None, nz=None, h=None, eta=1.0, gamma=1e-3, levels=2, nu=1,

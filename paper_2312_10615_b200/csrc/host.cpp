@@ -261,6 +261,34 @@ struct DevLevel {
     double* v1_k = nullptr;
     int32_t* v1_slots = nullptr;
     int v1_n = 0;
+    // general labelled domain: DofMap bits per cell slot (LevelK::cls points here),
+    // padded slot of every active DOF in compact order, signature class of every Vanka block
+    uint32_t* cls = nullptr;
+    int32_t* pack_slots = nullptr;
+    uint16_t* vk_kidx[8] = {};
+    std::shared_ptr<struct HostMap> hm;
+};
+
+// classify_dofs + partition_band on a labelled CellGrid: the host-side DofMap of one
+// level.  Cells outside the labelled box are the implicit Dirichlet ring.  A face is
+// stored with the cell on its high side (the u face between cells x-1 and x at cell x), so faces
+// and pressures share one index; ids follow the SPEC numbering (u-lex, v-lex, w-lex, p-lex, x
+// fastest).
+enum : uint8_t { LAB_D = 0, LAB_I = 1, LAB_E = 2 };
+constexpr int32_t ST_DIRICHLET = -1, ST_INACTIVE = -2;
+struct HostMap {
+    int nx = 0, ny = 0, nz = 0;
+    std::vector<uint8_t> lab, band;
+    std::vector<int32_t> id[4];   // per cell: compact id of the low u, v, w face / the pressure, or a status
+    std::vector<uint8_t> drop[3];  // per cell and low face: stencil legs into Inactive faces
+    int64_t cnt[4] = {0, 0, 0, 0}, N = 0, v1 = 0;
+    size_t ci(int x, int y, int z) const { return (static_cast<size_t>(z) * ny + y) * nx + x; }
+    bool inside(int x, int y, int z) const { return x >= 0 && y >= 0 && z >= 0 && x < nx && y < ny && z < nz; }
+    uint8_t at(int x, int y, int z) const { return inside(x, y, z) ? lab[ci(x, y, z)] : static_cast<uint8_t>(LAB_D); }
+    // low face of component c of cell (x, y, z); faces beyond the box belong to ring cells: Dirichlet
+    int32_t face(int c, int x, int y, int z) const { return inside(x, y, z) ? id[c][ci(x, y, z)] : ST_DIRICHLET; }
+    int32_t cell(int x, int y, int z) const { return inside(x, y, z) ? id[3][ci(x, y, z)] : ST_INACTIVE; }
+    bool is_band(int x, int y, int z) const { return inside(x, y, z) && band[ci(x, y, z)]; }
 };
 
 }  // namespace
@@ -306,6 +334,8 @@ struct smg_ctx {
     // plane partials and gathers travel through NCCL on the part's stream
     bool mp = false;
     ncclComm_t comm = nullptr;
+    // general labelled domain (smg_create_labeled): fine-level cell labels, x fastest; empty: walled box
+    std::vector<uint8_t> labels;
 
     template <class T>
     T* dalloc(int64_t count) {
@@ -432,6 +462,276 @@ int v1_selection(const DevLevel& L, int bw, std::vector<int32_t>& sel) {
     return n;
 }
 
+// ---- general labelled domains ----
+// coarsen_grid: a coarse cell is Dirichlet if any child is, else Interior if any child
+// is, else Exterior.
+std::vector<uint8_t> coarsen_labels(const std::vector<uint8_t>& f, int nx, int ny, int nz) {
+    const int cx = nx / 2, cy = ny / 2, cz = nz / 2;
+    std::vector<uint8_t> c(static_cast<size_t>(cx) * cy * cz, LAB_E);
+    for (int z = 0; z < cz; ++z)
+        for (int y = 0; y < cy; ++y)
+            for (int x = 0; x < cx; ++x) {
+                bool anyD = false, anyI = false;
+                for (int k = 0; k < 2; ++k)
+                    for (int j = 0; j < 2; ++j)
+                        for (int i = 0; i < 2; ++i) {
+                            const uint8_t l = f[(static_cast<size_t>(2 * z + k) * ny + (2 * y + j)) * nx + (2 * x + i)];
+                            anyD |= l == LAB_D;
+                            anyI |= l == LAB_I;
+                        }
+                c[(static_cast<size_t>(z) * cy + y) * cx + x] = anyD ? LAB_D : (anyI ? LAB_I : LAB_E);
+            }
+    return c;
+}
+
+// classify_dofs + partition_band of one labelled level.
+std::shared_ptr<HostMap> classify_labeled(std::vector<uint8_t> lab, int nx, int ny, int nz, int bw) {
+    auto hm = std::make_shared<HostMap>();
+    HostMap& m = *hm;
+    m.nx = nx;
+    m.ny = ny;
+    m.nz = nz;
+    m.lab = std::move(lab);
+    const size_t nc = static_cast<size_t>(nx) * ny * nz;
+    int64_t next = 0;
+    for (int c = 0; c < 3; ++c) {
+        m.id[c].assign(nc, ST_DIRICHLET);
+        const int64_t first = next;
+        for (int z = 0; z < nz; ++z)
+            for (int y = 0; y < ny; ++y)
+                for (int x = 0; x < nx; ++x) {
+                    const uint8_t a = m.at(x - (c == 0), y - (c == 1), z - (c == 2)), b = m.at(x, y, z);
+                    int32_t st;
+                    if (a == LAB_D || b == LAB_D) st = ST_DIRICHLET;
+                    else if (a == LAB_I && b == LAB_I) st = static_cast<int32_t>(next++);
+                    else st = ST_INACTIVE;
+                    m.id[c][m.ci(x, y, z)] = st;
+                }
+        m.cnt[c] = next - first;
+    }
+    m.id[3].assign(nc, ST_INACTIVE);
+    for (size_t q = 0; q < nc; ++q)
+        if (m.lab[q] == LAB_I) m.id[3][q] = static_cast<int32_t>(next++);
+    m.cnt[3] = next - (m.cnt[0] + m.cnt[1] + m.cnt[2]);
+    m.N = next;
+    m.band.assign(nc, 0);
+    for (int z = 0; z < nz; ++z)
+        for (int y = 0; y < ny; ++y)
+            for (int x = 0; x < nx; ++x) {
+                bool band = false;
+                for (int k = -bw; k <= bw && !band; ++k)
+                    for (int j = -bw; j <= bw && !band; ++j)
+                        for (int i = -bw; i <= bw && !band; ++i)
+                            if (m.at(x + i, y + j, z + k) != LAB_I) band = true;
+                m.band[m.ci(x, y, z)] = band;
+            }
+    const int d[6][3] = {{-1, 0, 0}, {1, 0, 0}, {0, -1, 0}, {0, 1, 0}, {0, 0, -1}, {0, 0, 1}};
+    for (int c = 0; c < 3; ++c) {
+        m.drop[c].assign(nc, 0);
+        for (int z = 0; z < nz; ++z)
+            for (int y = 0; y < ny; ++y)
+                for (int x = 0; x < nx; ++x) {
+                    if (m.id[c][m.ci(x, y, z)] < 0) continue;
+                    int dr = 0;
+                    for (auto& k : d)
+                        if (m.face(c, x + k[0], y + k[1], z + k[2]) == ST_INACTIVE) ++dr;  // dropped Neumann leg
+                    m.drop[c][m.ci(x, y, z)] = static_cast<uint8_t>(dr);
+                    if (m.is_band(x, y, z) || m.is_band(x - (c == 0), y - (c == 1), z - (c == 2))) ++m.v1;
+                }
+    }
+    for (size_t q = 0; q < nc; ++q)
+        if (m.id[3][q] >= 0 && m.band[q]) ++m.v1;
+    return hm;
+}
+
+// Sparse row r of L~ in the oracle's ltilde_row order (diagonal, six same-component neighbours,
+// p_left, p_right; continuity: the six faces, then -gamma), handed to put(col, value).
+template <class Put>
+void labeled_row(const HostMap& m, double e2, double ih, double gamma, int comp, int x, int y, int z, Put&& put) {
+    if (comp < 3) {
+        put(m.face(comp, x, y, z), (6.0 - m.drop[comp][m.ci(x, y, z)]) * e2);
+        const int d[6][3] = {{-1, 0, 0}, {1, 0, 0}, {0, -1, 0}, {0, 1, 0}, {0, 0, -1}, {0, 0, 1}};
+        for (auto& k : d) put(m.face(comp, x + k[0], y + k[1], z + k[2]), -e2);
+        put(m.cell(x - (comp == 0), y - (comp == 1), z - (comp == 2)), -ih);
+        put(m.cell(x, y, z), ih);
+    } else {
+        put(m.face(0, x, y, z), ih);
+        put(m.face(0, x + 1, y, z), -ih);
+        put(m.face(1, x, y, z), ih);
+        put(m.face(1, x, y + 1, z), -ih);
+        put(m.face(2, x, y, z), ih);
+        put(m.face(2, x, y, z + 1), -ih);
+        put(m.cell(x, y, z), -gamma);
+    }
+}
+
+// Dense L~ of a labelled level restricted to the DOFs with sel[id] >= 0 (nullptr: all), and their
+// padded slots -- assemble_box_dense for a general DofMap.
+void assemble_labeled_dense(const DevLevel& C, double gamma, const int32_t* sel, int nsel, std::vector<double>& A,
+                            std::vector<int32_t>& slots) {
+    const HostMap& m = *C.hm;
+    A.assign(static_cast<size_t>(nsel) * nsel, 0.0);
+    slots.assign(nsel, 0);
+    auto loc = [&](int32_t id) { return id < 0 ? -1 : (sel ? sel[id] : id); };
+    for (int z = 0; z < m.nz; ++z)
+        for (int y = 0; y < m.ny; ++y)
+            for (int x = 0; x < m.nx; ++x)
+                for (int comp = 0; comp < 4; ++comp) {
+                    const int r = loc(m.id[comp][m.ci(x, y, z)]);
+                    if (r < 0) continue;
+                    slots[r] = static_cast<int32_t>(comp * C.k.g.fs + C.k.g.slot(x, y, z));
+                    labeled_row(m, C.k.eta_h2, C.k.inv_h, gamma, comp, x, y, z, [&](int32_t col, double v) {
+                        const int cc = loc(col);
+                        if (cc >= 0) A[static_cast<size_t>(r) * nsel + cc] += v;
+                    });
+                }
+}
+
+// Device tables of one labelled level: DofMap bits, pack list, Vanka blocks by parity colour with
+// their signature classes (the local matrix depends on which faces are active and on
+// each active face's dropped legs) and the class inverses.
+void build_level_labeled(smg_ctx* c, int l, std::vector<uint8_t> lab, int& max_vk) {
+    DevLevel& L = c->lv[l];
+    const smg_params& p = c->prm;
+    const Geom& G = L.k.g;
+    const int nx = G.nx, ny = G.ny, nz = G.nz;
+    L.hm = classify_labeled(std::move(lab), nx, ny, nz, p.band_width);
+    const HostMap& m = *L.hm;
+    for (int k = 0; k < 4; ++k) L.counts[k] = m.cnt[k];
+    L.counts[4] = m.v1;
+    L.N = m.N;
+    std::vector<uint32_t> cls(static_cast<size_t>(G.fs), 0u);
+    std::vector<int32_t> pack(static_cast<size_t>(m.N), 0);
+    for (int z = 0; z < nz; ++z)
+        for (int y = 0; y < ny; ++y)
+            for (int x = 0; x < nx; ++x) {
+                const size_t q = m.ci(x, y, z);
+                const int64_t sl = G.slot(x, y, z);
+                uint32_t b = 0;
+                const bool bc = m.band[q] != 0;
+                if (bc) b |= CLS_BAND;
+                if (m.id[3][q] >= 0) {
+                    b |= CLS_P;
+                    pack[m.id[3][q]] = static_cast<int32_t>(3 * G.fs + sl);
+                }
+                for (int comp = 0; comp < 3; ++comp) {
+                    if (m.id[comp][q] < 0) continue;
+                    b |= CLS_U << comp;
+                    if (!bc && !m.is_band(x - (comp == 0), y - (comp == 1), z - (comp == 2))) b |= CLS_U2 << comp;
+                    b |= static_cast<uint32_t>(6 - m.drop[comp][q]) << (CLS_DIAG_SHIFT + 3 * comp);
+                    pack[m.id[comp][q]] = static_cast<int32_t>(comp * G.fs + sl);
+                }
+                cls[sl] = b;
+            }
+    L.cls = c->dalloc<uint32_t>(G.fs);
+    L.k.cls = L.cls;
+    L.pack_slots = c->dalloc<int32_t>(m.N);
+    CK(cudaMemcpyAsync(L.cls, cls.data(), cls.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemcpyAsync(L.pack_slots, pack.data(), pack.size() * sizeof(int32_t), cudaMemcpyHostToDevice, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    // Vanka blocks: band cells with an active pressure; slots [uL, uR, vL, vR, wL, wR, p]
+    std::vector<int32_t> cells[8];
+    std::vector<uint8_t> masks[8];
+    std::vector<uint16_t> kidx[8];
+    std::vector<int> keys;  // class index -> signature key
+    std::vector<double> ktab;
+    for (int z = 0; z < nz; ++z)
+        for (int y = 0; y < ny; ++y)
+            for (int x = 0; x < nx; ++x) {
+                const size_t q = m.ci(x, y, z);
+                if (m.id[3][q] < 0 || !m.band[q]) continue;
+                const int fx[6][4] = {{0, x, y, z}, {0, x + 1, y, z}, {1, x, y, z}, {1, x, y + 1, z}, {2, x, y, z}, {2, x, y, z + 1}};
+                int mask = 0, key = 0, dr[6] = {};
+                for (int s2 = 0; s2 < 6; ++s2) {
+                    if (m.face(fx[s2][0], fx[s2][1], fx[s2][2], fx[s2][3]) < 0) continue;
+                    mask |= 1 << s2;
+                    dr[s2] = m.drop[fx[s2][0]][m.ci(fx[s2][1], fx[s2][2], fx[s2][3])];
+                    key |= dr[s2] << (6 + 3 * s2);
+                }
+                key |= mask;
+                int ki = -1;
+                for (size_t k = 0; k < keys.size(); ++k)
+                    if (keys[k] == key) ki = static_cast<int>(k);
+                if (ki < 0) {  // new class: invert C_i L~ C_i^T over the active slots, scatter to the 7-slot layout
+                    if (keys.size() >= 65535) throw SmgError(SMG_ECAP, "more than 65535 Vanka signature classes");
+                    ki = static_cast<int>(keys.size());
+                    keys.push_back(key);
+                    int slot[7], nb = 0;
+                    for (int s2 = 0; s2 < 6; ++s2)
+                        if (mask & (1 << s2)) slot[nb++] = s2;
+                    slot[nb++] = 6;
+                    double lm[49] = {}, inv[49];
+                    for (int a = 0; a < nb; ++a)
+                        for (int b2 = 0; b2 < nb; ++b2) {
+                            const int sa = slot[a], sb = slot[b2];
+                            double v = 0.0;
+                            if (sa < 6 && sb < 6) {
+                                if (sa == sb) v = (6.0 - dr[sa]) * L.k.eta_h2;
+                                else if ((sa >> 1) == (sb >> 1)) v = -L.k.eta_h2;  // the cell's two faces of one axis
+                            } else if (sa < 6 && sb == 6) {
+                                v = (sa & 1) ? -L.k.inv_h : L.k.inv_h;  // low face: the cell is its p_right
+                            } else if (sa == 6 && sb < 6) {
+                                v = (sb & 1) ? -L.k.inv_h : L.k.inv_h;
+                            } else {
+                                v = -p.gamma;
+                            }
+                            lm[a * nb + b2] = v;
+                        }
+                    small_inverse(lm, nb, inv);
+                    ktab.resize(ktab.size() + 49, 0.0);
+                    for (int a = 0; a < nb; ++a)
+                        for (int b2 = 0; b2 < nb; ++b2) ktab[static_cast<size_t>(ki) * 49 + slot[a] * 7 + slot[b2]] = inv[a * nb + b2];
+                }
+                const int col = (x & 1) + 2 * (y & 1) + 4 * (z & 1);
+                cells[col].push_back(static_cast<int32_t>(G.slot(x, y, z)));
+                masks[col].push_back(static_cast<uint8_t>(mask));
+                kidx[col].push_back(static_cast<uint16_t>(ki));
+            }
+    for (int col = 0; col < 8; ++col) {
+        const size_t n = cells[col].size();
+        L.vk_n[col] = L.sw_n[col] = static_cast<int>(n);
+        max_vk = std::max(max_vk, L.vk_n[col]);
+        L.vk_cells[col] = L.sw_cells[col] = c->dalloc<int32_t>(n);
+        L.vk_mask[col] = L.sw_mask[col] = c->dalloc<uint8_t>(n);
+        L.vk_kidx[col] = c->dalloc<uint16_t>(n);
+        CK(cudaMemcpyAsync(L.vk_cells[col], cells[col].data(), n * sizeof(int32_t), cudaMemcpyHostToDevice, c->st));
+        CK(cudaMemcpyAsync(L.vk_mask[col], masks[col].data(), n, cudaMemcpyHostToDevice, c->st));
+        CK(cudaMemcpyAsync(L.vk_kidx[col], kidx[col].data(), n * sizeof(uint16_t), cudaMemcpyHostToDevice, c->st));
+        CK(cudaStreamSynchronize(c->st));
+    }
+    L.ktab = c->dalloc<double>(std::max<size_t>(ktab.size(), 49));
+    CK(cudaMemcpyAsync(L.ktab, ktab.data(), ktab.size() * sizeof(double), cudaMemcpyHostToDevice, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    if (p.vanka == 2 && l + 1 < p.levels) {  // direct-on-V1: dense symmetric inverse of the V1 x V1 sub-block
+        std::vector<int32_t> sel(static_cast<size_t>(m.N), -1), vslots;
+        int n1 = 0;
+        // V1 DOFs ascending in compact order
+        std::vector<uint8_t> isv1(static_cast<size_t>(m.N), 0);
+        for (int z = 0; z < nz; ++z)
+            for (int y = 0; y < ny; ++y)
+                for (int x = 0; x < nx; ++x) {
+                    const size_t q = m.ci(x, y, z);
+                    for (int comp = 0; comp < 3; ++comp)
+                        if (m.id[comp][q] >= 0 &&
+                            (m.band[q] || m.is_band(x - (comp == 0), y - (comp == 1), z - (comp == 2))))
+                            isv1[m.id[comp][q]] = 1;
+                    if (m.id[3][q] >= 0 && m.band[q]) isv1[m.id[3][q]] = 1;
+                }
+        for (int64_t k = 0; k < m.N; ++k)
+            if (isv1[k]) sel[k] = n1++;
+        if (n1 > 20000) throw SmgError(SMG_ECAP, "direct-on-V1: |V1| above the dense cap 20000 (SPEC:365)");
+        std::vector<double> A11;
+        assemble_labeled_dense(L, p.gamma, sel.data(), n1, A11, vslots);
+        const std::vector<double> K1 = n1 ? dense_inverse_sym(std::move(A11), n1) : std::vector<double>();
+        L.v1_n = n1;
+        L.v1_k = c->dalloc<double>(static_cast<int64_t>(n1) * n1);
+        L.v1_slots = c->dalloc<int32_t>(n1);
+        CK(cudaMemcpyAsync(L.v1_k, K1.data(), K1.size() * sizeof(double), cudaMemcpyHostToDevice, c->st));
+        CK(cudaMemcpyAsync(L.v1_slots, vslots.data(), vslots.size() * sizeof(int32_t), cudaMemcpyHostToDevice, c->st));
+        CK(cudaStreamSynchronize(c->st));
+    }
+}
+
 // ---- setup ----
 void build(smg_ctx* c, const std::vector<double>* shared_coarse = nullptr, std::vector<double>* coarse_out = nullptr,
            cudaStream_t shared_stream = nullptr) {
@@ -448,6 +748,11 @@ void build(smg_ctx* c, const std::vector<double>* shared_coarse = nullptr, std::
     if (p.vanka != 0 && c->ndist > 0)
         throw SmgError(SMG_EINVAL, "additive Vanka / direct-on-V1: single-part contexts only");
     if (!(g.h > 0)) throw SmgError(SMG_EINVAL, "h must be > 0");
+    const bool labeled = !c->labels.empty();
+    if (labeled && (c->nparts > 1 || c->ndist > 0))
+        throw SmgError(SMG_EINVAL, "labelled domains: single-part contexts only");
+    if (labeled && p.vanka == 1) throw SmgError(SMG_EINVAL, "labelled domains: vanka must be 0 or 2");
+    std::vector<uint8_t> lab = c->labels;  // labels of the level being built
     const int div = 1 << (p.levels - 1);
     if (g.nx % div || g.ny % div || g.nz % div)
         throw SmgError(SMG_EINVAL, "extents must be divisible by 2^(levels-1)");
@@ -478,7 +783,7 @@ void build(smg_ctx* c, const std::vector<double>* shared_coarse = nullptr, std::
         L.k.dv = 6.0 * L.k.eta_h2;
         L.k.dp = -6.0 * (1.0 + p.gamma * p.eta) / (h * h);
         L.k.bw = p.band_width;
-        L.k.tiled = dgs_tiled(nx, ny, nz, p.dgs_tile_min) ? 1 : 0;
+        L.k.tiled = (!labeled && dgs_tiled(nx, ny, nz, p.dgs_tile_min)) ? 1 : 0;
         L.counts[0] = static_cast<int64_t>(nx - 1) * ny * nz;
         L.counts[1] = static_cast<int64_t>(nx) * (ny - 1) * nz;
         L.counts[2] = static_cast<int64_t>(nx) * ny * (nz - 1);
@@ -496,6 +801,11 @@ void build(smg_ctx* c, const std::vector<double>* shared_coarse = nullptr, std::
         L.pd0 = c->dalloc<double>(L.k.g.fs);
         L.pd1 = c->dalloc<double>(L.k.g.fs);
         L.k.cb = c->dalloc<double>(L.k.g.fs);
+        if (labeled) {
+            if (l > 0) lab = coarsen_labels(lab, nx * 2, ny * 2, nz * 2);
+            build_level_labeled(c, l, lab, max_vk);
+            continue;
+        }
         // Vanka blocks: band cells, slot + active-face mask, by colour
         const int bw = p.band_width;
         auto band = [&](int x, int y, int z) {
@@ -708,10 +1018,11 @@ void build(smg_ctx* c, const std::vector<double>* shared_coarse = nullptr, std::
     c->nc = n;
     std::vector<double> A;
     std::vector<int32_t> slots;
-    assemble_box_dense(C, p.gamma, nullptr, n, A, slots);
+    if (labeled) assemble_labeled_dense(C, p.gamma, nullptr, n, A, slots);
+    else assemble_box_dense(C, p.gamma, nullptr, n, A, slots);
     std::vector<double> K;
     if (shared_coarse) K = *shared_coarse;  // same matrix on every part: factorise once
-    else K = dense_inverse_sym(std::move(A), n);
+    else if (n > 0) K = dense_inverse_sym(std::move(A), n);
     if (coarse_out) *coarse_out = K;
     c->coarse_k = c->dalloc<double>(static_cast<int64_t>(n) * n);
     c->coarse_slots = c->dalloc<int32_t>(n);
@@ -742,7 +1053,8 @@ void vanka_sym(smg_ctx* c, int l, double* x, const double* b) {
     for (int pass = 0; pass < 2; ++pass)
         for (int k = 0; k < 8; ++k) {
             const int col = vanka_order(pass == 0 ? k : 7 - k);
-            launch_vanka_delta(L.k, x, b, L.vk_cells[col], L.vk_mask[col], L.vk_n[col], L.ktab, c->vk_delta, c->st);
+            launch_vanka_delta(L.k, x, b, L.vk_cells[col], L.vk_mask[col], L.vk_n[col], L.ktab, c->vk_delta, c->st,
+                               L.vk_kidx[col]);
             launch_vanka_apply(L.k, x, L.vk_cells[col], L.vk_mask[col], L.vk_n[col], c->vk_delta, c->st);
         }
 }
@@ -781,6 +1093,19 @@ void symmetric_dgs(smg_ctx* c, int l, double* x, const double* b, bool cb_ready 
     const int nph = (c->prm.flags & SMG_FLAG_SKIP_REVERSE_DGS) ? kDgsPhases / 2 : kDgsPhases;
     DevLevel& L = c->lv[l];
     if (nph > kDgsPhases / 2 && !cb_ready) launch_dgs_cb(L.k, b, c->st);  // m_C^T b for the reverse steps
+    if (L.k.cls) {  // labelled level: one masked kernel per phase
+        for (int ph = 0; ph < nph; ++ph) {
+            if (ph <= 1 || ph >= 18) {
+                launch_dgs_vel(L.k, x, b, ph <= 1 ? ph : 19 - ph, c->st);
+            } else if (ph <= 9) {
+                launch_dgs_pdelta(L.k, x, b, L.pd, ph - 2, c->st);
+                launch_dgs_papply(L.k, x, L.pd, c->st);
+            } else {
+                launch_dgs_prev(L.k, x, b, 17 - ph, c->st);
+            }
+        }
+        return;
+    }
     if (L.k.tiled) {
         launch_dgs_tiled(L.k, x, b, nph, c->st);
         return;
@@ -790,6 +1115,10 @@ void symmetric_dgs(smg_ctx* c, int l, double* x, const double* b, bool cb_ready 
 
 void vanka_sym_coop(smg_ctx* c, int l, double* x, const double* b) {
     DevLevel& L = c->lv[l];
+    if (L.k.cls) {  // labelled level: per-colour delta / apply launches with the class table
+        for (int k = 0; k < c->prm.nu; ++k) vanka_sym(c, l, x, b);
+        return;
+    }
     launch_vanka_sym_coop(L.k, x, b, L.sw_cells, L.sw_mask, L.sw_n, L.ktab, c->vk_delta, c->prm.nu, c->st, L.xb,
                           L.vk_refresh, L.vk_nrefresh, L.sw_pairs);
 }
@@ -859,11 +1188,13 @@ void vcycle(smg_ctx* c, int l, const double* b, double* x) {
 void upload(smg_ctx* c, int l, const double* host, double* dev_padded) {
     DevLevel& L = c->lv[l];
     CK(cudaMemcpyAsync(c->compact, host, L.N * sizeof(double), cudaMemcpyHostToDevice, c->st));
-    launch_unpack(L.k, c->compact, dev_padded, c->st);
+    if (L.pack_slots) launch_scatter(L.pack_slots, L.N, c->compact, dev_padded, c->st);
+    else launch_unpack(L.k, c->compact, dev_padded, c->st);
 }
 void download(smg_ctx* c, int l, const double* dev_padded, double* host) {
     DevLevel& L = c->lv[l];
-    launch_pack(L.k, dev_padded, c->compact, c->st);
+    if (L.pack_slots) launch_gather(L.pack_slots, L.N, dev_padded, c->compact, c->st);
+    else launch_pack(L.k, dev_padded, c->compact, c->st);
     CK(cudaMemcpyAsync(host, c->compact, L.N * sizeof(double), cudaMemcpyDeviceToHost, c->st));
     CK(cudaStreamSynchronize(c->st));
 }
@@ -1571,6 +1902,61 @@ int smg_create(const smg_grid_desc* grid, const smg_params* params, int ngpu, co
     return 0;
 }
 
+int smg_create_labeled(const smg_grid_desc* grid, const uint8_t* labels, const smg_params* params, int device,
+                       smg_ctx** out) {
+    if (!grid || !labels || !params || !out) return SMG_EINVAL;
+    *out = nullptr;
+    if (grid->dim != 3 || grid->nx < 1 || grid->ny < 1 || grid->nz < 1) return SMG_EINVAL;
+    auto c = std::make_unique<smg_ctx>();
+    c->grid = *grid;
+    c->prm = *params;
+    c->device = device;
+    c->parts.push_back(c.get());
+    const size_t nc = static_cast<size_t>(grid->nx) * grid->ny * grid->nz;
+    c->labels.assign(labels, labels + nc);
+    const int rc = guard(c.get(), [&] {
+        bool any = false;
+        for (uint8_t l : c->labels) {
+            if (l > LAB_E) throw SmgError(SMG_EINVAL, "labels must be 0 (Dirichlet), 1 (Interior) or 2 (Exterior)");
+            any |= l == LAB_I;
+        }
+        if (!any) throw SmgError(SMG_EINVAL, "no Interior cell: the grid has no active DOF (SPEC:52)");
+        build(c.get());
+        if (c->lv.back().N == 0) throw SmgError(SMG_EINVAL, "the coarsest level has no active DOF: use fewer levels");
+    });
+    if (rc != 0) {
+        std::fprintf(stderr, "smg_create_labeled: %s\n", c->err.c_str());
+        return rc;
+    }
+    *out = c.release();
+    return 0;
+}
+
+int smg_coarsen_labels(const smg_grid_desc* grid, const uint8_t* labels, uint8_t* out) {
+    if (!grid || !labels || !out || grid->dim != 3) return SMG_EINVAL;
+    if (grid->nx < 2 || grid->ny < 2 || grid->nz < 2 || (grid->nx | grid->ny | grid->nz) & 1) return SMG_EINVAL;
+    const size_t nc = static_cast<size_t>(grid->nx) * grid->ny * grid->nz;
+    const std::vector<uint8_t> c = coarsen_labels(std::vector<uint8_t>(labels, labels + nc), grid->nx, grid->ny, grid->nz);
+    std::memcpy(out, c.data(), c.size());
+    return 0;
+}
+
+int64_t smg_census_labeled(const smg_grid_desc* grid, const uint8_t* labels, int band_width, int64_t* out6) {
+    if (!grid || !labels || grid->dim != 3 || band_width < 1) return SMG_EINVAL;
+    const size_t nc = static_cast<size_t>(grid->nx) * grid->ny * grid->nz;
+    try {
+        const auto m = classify_labeled(std::vector<uint8_t>(labels, labels + nc), grid->nx, grid->ny, grid->nz, band_width);
+        if (out6) {
+            out6[0] = m->N;
+            out6[1] = m->v1;
+            for (int k = 0; k < 4; ++k) out6[2 + k] = m->cnt[k];
+        }
+        return m->N;
+    } catch (...) {
+        return SMG_EINVAL;
+    }
+}
+
 int smg_nccl_unique_id(unsigned char id[128]) {
     static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
     if (!id) return SMG_EINVAL;
@@ -1682,8 +2068,11 @@ int smg_smoother(smg_ctx* c, int level, int op, int arg, double* x, const double
         else if (op == 1) symmetric_dgs(c, level, L.x, L.b);
         else if (op == 2) {
             if (arg < 0 || arg > 7) throw SmgError(SMG_EINVAL, "colour out of range");
-            launch_vanka_delta(L.k, L.x, L.b, L.vk_cells[arg], L.vk_mask[arg], L.vk_n[arg], L.ktab, c->vk_delta, c->st);
+            launch_vanka_delta(L.k, L.x, L.b, L.vk_cells[arg], L.vk_mask[arg], L.vk_n[arg], L.ktab, c->vk_delta, c->st,
+                               L.vk_kidx[arg]);
             launch_vanka_apply(L.k, L.x, L.vk_cells[arg], L.vk_mask[arg], L.vk_n[arg], c->vk_delta, c->st);
+        } else if (op == 3 && L.k.cls) {
+            vanka_sym(c, level, L.x, L.b);
         } else if (op == 3) {
             launch_vanka_sym_coop(L.k, L.x, L.b, L.sw_cells, L.sw_mask, L.sw_n, L.ktab, c->vk_delta, 1, c->st,
                                   L.xb, L.vk_refresh, L.vk_nrefresh, L.sw_pairs);
@@ -1929,20 +2318,46 @@ void smg_host_free(void* p) {
     if (p) cudaFreeHost(p);
 }
 
+namespace {
+// Synthetic forcing of the BASELINE configs (OD-9) at a face: a pure function of (seed, component,
+// storage coordinates), so it is independent of the numbering and of any decomposition.
+struct Forcing {
+    int kind;
+    uint64_t seed;
+    double h;
+    double amp[3][8];
+    int kw[3][8][3];
+    Forcing(int kind_, uint64_t seed_, double h_) : kind(kind_), seed(seed_), h(h_) {
+        if (kind == 1)
+            for (int c = 0; c < 3; ++c)
+                for (int md = 0; md < 8; ++md) {
+                    for (int a = 0; a < 3; ++a) kw[c][md][a] = 1 + static_cast<int>(key5(seed, 16 + c, md, a, 0) % 8);
+                    const double u1 = 1.0 - unit01(key5(seed, 32 + c, md, 0, 1));
+                    const double u2 = unit01(key5(seed, 32 + c, md, 0, 2));
+                    amp[c][md] = std::sqrt(-2.0 * std::log(u1)) * std::cos(6.283185307179586 * u2);
+                }
+    }
+    double operator()(int c, int x, int y, int z) const {
+        const double u = 2.0 * unit01(key5(seed, c, x, y, z)) - 1.0;
+        if (kind == 0) return u;
+        if (kind == 2) return (c == 0 ? 1.0 : 0.0) + 0.1 * u;
+        const int p[3] = {x, y, z};
+        double xyz[3];
+        for (int a = 0; a < 3; ++a) xyz[a] = (a == c) ? p[a] * h : (p[a] + 0.5) * h;
+        double s = 0.0;
+        for (int md = 0; md < 8; ++md)
+            s = s + amp[c][md] * std::sin(3.141592653589793 * kw[c][md][0] * xyz[0]) *
+                        std::sin(3.141592653589793 * kw[c][md][1] * xyz[1]) *
+                        std::sin(3.141592653589793 * kw[c][md][2] * xyz[2]);
+        return s;
+    }
+};
+}  // namespace
+
 int smg_forcing(const smg_grid_desc* grid, int kind, uint64_t seed, double* b, int threads) {
     if (!grid || !b || kind < 0 || kind > 2 || grid->dim != 3) return SMG_EINVAL;
     const int nx = grid->nx, ny = grid->ny, nz = grid->nz;
-    const double h = grid->h;
-    double amp[3][8];
-    int kw[3][8][3];
-    if (kind == 1)
-        for (int c = 0; c < 3; ++c)
-            for (int md = 0; md < 8; ++md) {
-                for (int a = 0; a < 3; ++a) kw[c][md][a] = 1 + static_cast<int>(key5(seed, 16 + c, md, a, 0) % 8);
-                const double u1 = 1.0 - unit01(key5(seed, 32 + c, md, 0, 1));
-                const double u2 = unit01(key5(seed, 32 + c, md, 0, 2));
-                amp[c][md] = std::sqrt(-2.0 * std::log(u1)) * std::cos(6.283185307179586 * u2);
-            }
+    const Forcing f(kind, seed, grid->h);
     const int64_t nu = static_cast<int64_t>(nx - 1) * ny * nz, nv = static_cast<int64_t>(nx) * (ny - 1) * nz;
     const int64_t nw = static_cast<int64_t>(nx) * ny * (nz - 1), np = static_cast<int64_t>(nx) * ny * nz;
     // one task per (component, z-plane)
@@ -1965,27 +2380,28 @@ int smg_forcing(const smg_grid_desc* grid, int kind, uint64_t seed, double* b, i
                         if (z < 1 || z > nz - 1) continue;
                         id = nu + nv + (static_cast<int64_t>(z - 1) * ny + y) * nx + x;
                     }
-                    const double u = 2.0 * unit01(key5(seed, c, x, y, z)) - 1.0;
-                    double v;
-                    if (kind == 0) v = u;
-                    else if (kind == 2) v = (c == 0 ? 1.0 : 0.0) + 0.1 * u;
-                    else {
-                        const int p[3] = {x, y, z};
-                        double xyz[3];
-                        for (int a = 0; a < 3; ++a) xyz[a] = (a == c) ? p[a] * h : (p[a] + 0.5) * h;
-                        double s = 0.0;
-                        for (int md = 0; md < 8; ++md)
-                            s = s + amp[c][md] * std::sin(3.141592653589793 * kw[c][md][0] * xyz[0]) *
-                                        std::sin(3.141592653589793 * kw[c][md][1] * xyz[1]) *
-                                        std::sin(3.141592653589793 * kw[c][md][2] * xyz[2]);
-                        v = s;
-                    }
-                    b[id] = v;
+                    b[id] = f(c, x, y, z);
                 }
         }
     });
     // pressure rows: b_p = 0 (zero divergence RHS)
     for (int64_t k = 0; k < np; ++k) b[nu + nv + nw + k] = 0.0;
+    return 0;
+}
+
+int smg_forcing_labeled(const smg_grid_desc* grid, const uint8_t* labels, int kind, uint64_t seed, double* b) {
+    if (!grid || !labels || !b || kind < 0 || kind > 2 || grid->dim != 3) return SMG_EINVAL;
+    const size_t nc = static_cast<size_t>(grid->nx) * grid->ny * grid->nz;
+    const auto m = classify_labeled(std::vector<uint8_t>(labels, labels + nc), grid->nx, grid->ny, grid->nz, 1);
+    const Forcing f(kind, seed, grid->h);
+    for (int z = 0; z < m->nz; ++z)
+        for (int y = 0; y < m->ny; ++y)
+            for (int x = 0; x < m->nx; ++x) {
+                const size_t q = m->ci(x, y, z);
+                for (int c = 0; c < 3; ++c)
+                    if (m->id[c][q] >= 0) b[m->id[c][q]] = f(c, x, y, z);
+                if (m->id[3][q] >= 0) b[m->id[3][q]] = 0.0;
+            }
     return 0;
 }
 

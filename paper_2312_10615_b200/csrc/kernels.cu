@@ -95,6 +95,23 @@ __device__ __forceinline__ double cont(const LevelK& L, AU U, AV V, AW W, AP P, 
     return -div * L.inv_h - gamma * P[i];
 }
 
+// Labelled levels: momentum diagonal 6 - (dropped Neumann legs) of the low face `comp` of a cell
+// (SPEC:124, 176), and the momentum row with that diagonal (the oracle's vdiag[f] * x[f] - s).
+__device__ __forceinline__ double cls_diag(uint32_t c, int comp) {
+    return static_cast<double>((c >> (CLS_DIAG_SHIFT + 3 * comp)) & 7u);
+}
+template <class AF, class AP>
+__device__ __forceinline__ double mom_d(const LevelK& L, AF F, AP P, int64_t i, int64_t sn, double diag) {
+    const int64_t sy = L.g.sy, sz = L.g.sz;
+    double s = F[i - 1] + F[i + 1];
+    s = s + F[i - sy];
+    s = s + F[i + sy];
+    s = s + F[i - sz];
+    s = s + F[i + sz];
+    const double lap = diag * F[i] - s;
+    return L.eta_h2 * lap + (P[i] - P[i - sn]) * L.inv_h;
+}
+
 // ------------------------------------------------------------- apply ------
 __global__ void k_apply(LevelK L, const double* __restrict__ X, const double* __restrict__ B,
                         double* __restrict__ Y, double gamma) {
@@ -656,13 +673,14 @@ __global__ void __launch_bounds__(256) k_cdot_final(const double* __restrict__ p
 // The momentum row (mom) and continuity row (cont) of the contract on a vector given by an
 // index functor v(j) (absolute indices, field f at f * fs): the same operand order.
 template <class VF>
-__device__ __forceinline__ double mom_f(const LevelK& L, const VF& v, int64_t i, int64_t sn, int64_t po) {
+__device__ __forceinline__ double mom_f(const LevelK& L, const VF& v, int64_t i, int64_t sn, int64_t po,
+                                        double diag = 6.0) {
     double s = v(i - 1) + v(i + 1);
     s = s + v(i - L.g.sy);
     s = s + v(i + L.g.sy);
     s = s + v(i - L.g.sz);
     s = s + v(i + L.g.sz);
-    const double lap = 6.0 * v(i) - s;
+    const double lap = diag * v(i) - s;
     return L.eta_h2 * lap + (v(po) - v(po - sn)) * L.inv_h;
 }
 template <class VF>
@@ -676,6 +694,8 @@ __device__ __forceinline__ double cont_f(const LevelK& L, const VF& v, int64_t i
 // block partials.  Grid = the dot grid; on slab parts with a neighbour below / above, the
 // first / last z-block also writes q on the ghost plane -1 / nz (its inputs are valid there),
 // so the next iteration needs no exchange of q.
+// M: general labelled level (activity and momentum diagonals from L.cls instead of coordinates).
+template <bool M>
 __global__ void __launch_bounds__(256) k_apply_q(LevelK L, const double* __restrict__ T,
                                                  const double* __restrict__ Q0, double* __restrict__ Q1,
                                                  double* __restrict__ Tn, const double* __restrict__ sc,
@@ -699,31 +719,34 @@ __global__ void __launch_bounds__(256) k_apply_q(LevelK L, const double* __restr
 #pragma unroll 1
         for (int z = zl; z < zh; ++z) {
             const int64_t i = g.slot(x, y, z);
+            const uint32_t cm = M ? L.cls[i] : 0u;
             double c4;
             {
                 const double qu = q(i);
                 double tu = 0.0;
-                if (x >= 1) Tn[i] = tu = mom_f(L, q, i, 1, 3 * fs + i);
+                if (M ? (cm & CLS_U) != 0 : x >= 1) Tn[i] = tu = mom_f(L, q, i, 1, 3 * fs + i, M ? cls_diag(cm, 0) : 6.0);
                 Q1[i] = qu;
                 c4 = qu * tu;
             }
             {
                 const double qv = q(fs + i);
                 double tv = 0.0;
-                if (y >= 1) Tn[fs + i] = tv = mom_f(L, q, fs + i, g.sy, 3 * fs + i);
+                if (M ? (cm & CLS_V) != 0 : y >= 1)
+                    Tn[fs + i] = tv = mom_f(L, q, fs + i, g.sy, 3 * fs + i, M ? cls_diag(cm, 1) : 6.0);
                 Q1[fs + i] = qv;
                 c4 = c4 + qv * tv;
             }
             {
                 const double qw = q(2 * fs + i);
                 double tw = 0.0;
-                if (g.gz(z) >= 1) Tn[2 * fs + i] = tw = mom_f(L, q, 2 * fs + i, g.sz, 3 * fs + i);
+                if (M ? (cm & CLS_W) != 0 : g.gz(z) >= 1)
+                    Tn[2 * fs + i] = tw = mom_f(L, q, 2 * fs + i, g.sz, 3 * fs + i, M ? cls_diag(cm, 2) : 6.0);
                 Q1[2 * fs + i] = qw;
                 c4 = c4 + qw * tw;
             }
             const double qp = q(3 * fs + i);
-            const double tp = cont_f(L, q, i, 0.0);
-            Tn[3 * fs + i] = tp;
+            double tp = 0.0;
+            if (!M || (cm & CLS_P)) Tn[3 * fs + i] = tp = cont_f(L, q, i, 0.0);
             Q1[3 * fs + i] = qp;
             v = v + (c4 + qp * tp);  // ((p_u + p_v) + p_w) + p_p
         }
@@ -734,6 +757,7 @@ __global__ void __launch_bounds__(256) k_apply_q(LevelK L, const double* __restr
 // Lines 7 + 8 of iteration j: d = cd d + cq q, x = x + d (written to D1, X1), then the true
 // residual r = b - L x as block partials of ||r||^2 (r itself is never stored).  Ghost planes
 // as in k_apply_q.
+template <bool M>
 __global__ void __launch_bounds__(256, 4) k_apply_x(LevelK L, const double* __restrict__ X0,
                                                  const double* __restrict__ D0, const double* __restrict__ Q,
                                                  const double* __restrict__ B, double* __restrict__ X1,
@@ -763,11 +787,14 @@ __global__ void __launch_bounds__(256, 4) k_apply_x(LevelK L, const double* __re
 #pragma unroll 1
         for (int z = zl; z < zh; ++z) {
             const int64_t i = g.slot(x, y, z);
-            double ru = 0.0, rv = 0.0, rw = 0.0;
-            if (x >= 1) ru = B[i] - mom_f(L, xn, i, 1, 3 * fs + i);
-            if (y >= 1) rv = B[fs + i] - mom_f(L, xn, fs + i, g.sy, 3 * fs + i);
-            if (g.gz(z) >= 1) rw = B[2 * fs + i] - mom_f(L, xn, 2 * fs + i, g.sz, 3 * fs + i);
-            const double rp = B[3 * fs + i] - cont_f(L, xn, i, 0.0);
+            const uint32_t cm = M ? L.cls[i] : 0u;
+            double ru = 0.0, rv = 0.0, rw = 0.0, rp = 0.0;
+            if (M ? (cm & CLS_U) != 0 : x >= 1) ru = B[i] - mom_f(L, xn, i, 1, 3 * fs + i, M ? cls_diag(cm, 0) : 6.0);
+            if (M ? (cm & CLS_V) != 0 : y >= 1)
+                rv = B[fs + i] - mom_f(L, xn, fs + i, g.sy, 3 * fs + i, M ? cls_diag(cm, 1) : 6.0);
+            if (M ? (cm & CLS_W) != 0 : g.gz(z) >= 1)
+                rw = B[2 * fs + i] - mom_f(L, xn, 2 * fs + i, g.sz, 3 * fs + i, M ? cls_diag(cm, 2) : 6.0);
+            if (!M || (cm & CLS_P)) rp = B[3 * fs + i] - cont_f(L, xn, i, 0.0);
             put_xd(i);
             v = v + cell4(ru * ru, rv * rv, rw * rw, rp * rp);
         }
@@ -2370,6 +2397,218 @@ __global__ void __launch_bounds__(kTileThreads, 2)
     }
 }
 
+// ------------------------------------------ general labelled domains ------
+// SPEC:17-97 (domain), 124/176 (dropped Neumann legs), 245-251 (Vanka signature classes):
+// Dirichlet / Interior / Exterior cells inside the implicit Dirichlet ring.  The padded layout is
+// the box's: Dirichlet-valued and Inactive slots hold 0 forever (never written), so every stencil
+// sum is already right; what changes is WHICH slots are DOFs (L.cls bits instead of coordinate
+// tests), the momentum diagonal 6 - dropped legs (cls_diag), band membership (a mask, not a
+// distance to the wall) and the Vanka class table (kidx -> ktab).  One kernel per phase, per-point
+// arithmetic in the contract's operand order: bit-identical to the oracle on any labelling, and to
+// the box kernels when every cell is Interior.
+__global__ void k_apply_m(LevelK L, const double* __restrict__ X, const double* __restrict__ B,
+                          double* __restrict__ Y, double gamma) {
+    pdl_wait();
+    Cell c;
+    if (!thread_cell(L.g, c)) return;
+    const Geom& g = L.g;
+    const int64_t fs = g.fs, i = c.i;
+    const uint32_t m = L.cls[i];
+    if (!(m & (CLS_P | CLS_U | CLS_V | CLS_W))) return;
+    const double *U = X, *V = X + fs, *W = X + 2 * fs, *P = X + 3 * fs;
+    if (m & CLS_U) {
+        const double y = mom_d(L, U, P, i, 1, cls_diag(m, 0));
+        Y[i] = B ? B[i] - y : y;
+    }
+    if (m & CLS_V) {
+        const double y = mom_d(L, V, P, i, g.sy, cls_diag(m, 1));
+        Y[fs + i] = B ? B[fs + i] - y : y;
+    }
+    if (m & CLS_W) {
+        const double y = mom_d(L, W, P, i, g.sz, cls_diag(m, 2));
+        Y[2 * fs + i] = B ? B[2 * fs + i] - y : y;
+    }
+    if (m & CLS_P) {
+        const double y = cont(L, U, V, W, P, i, gamma);
+        Y[3 * fs + i] = B ? B[3 * fs + i] - y : y;
+    }
+}
+
+// DGS velocity phase on the V2 faces of one red-black colour (their stencils are full: diagonal 6).
+__global__ void k_dgs_vel_m(LevelK L, double* __restrict__ X, const double* __restrict__ B, int colour) {
+    Cell c;
+    if (!thread_cell(L.g, c)) return;
+    const Geom& g = L.g;
+    if (((c.x + c.y + g.gz(c.z)) & 1) != colour) return;
+    const int64_t fs = g.fs, i = c.i;
+    const uint32_t m = L.cls[i];
+    if (!(m & (CLS_U2 | CLS_V2 | CLS_W2))) return;
+    double *U = X, *V = X + fs, *W = X + 2 * fs;
+    const double* P = X + 3 * fs;
+    if (m & CLS_U2) {
+        const double r = B[i] - mom(L, U, P, i, 1);
+        U[i] = U[i] + r / L.dv;
+    }
+    if (m & CLS_V2) {
+        const double r = B[fs + i] - mom(L, V, P, i, g.sy);
+        V[i] = V[i] + r / L.dv;
+    }
+    if (m & CLS_W2) {
+        const double r = B[2 * fs + i] - mom(L, W, P, i, g.sz);
+        W[i] = W[i] + r / L.dv;
+    }
+}
+
+__global__ void k_dgs_pdelta_m(LevelK L, const double* __restrict__ X, const double* __restrict__ B,
+                               double* __restrict__ D, int colour) {
+    Cell c;
+    if (!thread_cell(L.g, c)) return;
+    const int64_t fs = L.g.fs, i = c.i;
+    const uint32_t m = L.cls[i];
+    double d = 0.0;
+    if (pcolour(L.g, c) == colour && (m & (CLS_P | CLS_BAND)) == CLS_P) {
+        const double r = B[3 * fs + i] - cont(L, X, X + fs, X + 2 * fs, X + 3 * fs, i, L.gamma);
+        d = r / L.dp;
+    }
+    D[i] = d;
+}
+
+__global__ void k_dgs_papply_m(LevelK L, double* __restrict__ X, const double* __restrict__ D) {
+    Cell c;
+    if (!thread_cell(L.g, c)) return;
+    const Geom& g = L.g;
+    const int64_t fs = g.fs, i = c.i, sy = g.sy, sz = g.sz;
+    const uint32_t m = L.cls[i];
+    const double dc = D[i];
+    if (m & CLS_U) X[i] = X[i] + (D[i - 1] - dc) * L.inv_h;
+    if (m & CLS_V) X[fs + i] = X[fs + i] + (D[i - sy] - dc) * L.inv_h;
+    if (m & CLS_W) X[2 * fs + i] = X[2 * fs + i] + (D[i - sz] - dc) * L.inv_h;
+    if (m & CLS_P) {
+        double s = D[i - 1] + D[i + 1];
+        s = s + D[i - sy];
+        s = s + D[i + sy];
+        s = s + D[i - sz];
+        s = s + D[i + sz];
+        X[3 * fs + i] = X[3 * fs + i] + L.eta_h2 * (6.0 * dc - s);
+    }
+}
+
+// Reverse pressure phase on V2 cells: prev_core with the six face rows' own diagonals (a face of a
+// V2 cell may be a V1 face with a dropped leg one cell further out).
+__global__ void k_dgs_prev_m(LevelK L, double* __restrict__ X, int colour) {
+    Cell c;
+    if (!thread_cell(L.g, c)) return;
+    const Geom& g = L.g;
+    const int64_t fs = g.fs, sy = g.sy, sz = g.sz, i = c.i;
+    const uint32_t m0 = L.cls[i];
+    if (pcolour(g, c) != colour || (m0 & (CLS_P | CLS_BAND)) != CLS_P) return;
+    const uint32_t mx = L.cls[i + 1], my = L.cls[i + sy], mz = L.cls[i + sz];
+    const double *U = X, *V = X + fs, *W = X + 2 * fs, *P = X + 3 * fs;
+    const double luL = mom_d(L, U, P, i, 1, cls_diag(m0, 0));
+    const double luR = mom_d(L, U, P, i + 1, 1, cls_diag(mx, 0));
+    const double lvL = mom_d(L, V, P, i, sy, cls_diag(m0, 1));
+    const double lvR = mom_d(L, V, P, i + sy, sy, cls_diag(my, 1));
+    const double lwL = mom_d(L, W, P, i, sz, cls_diag(m0, 2));
+    const double lwR = mom_d(L, W, P, i + sz, sz, cls_diag(mz, 2));
+    const double fl = ((luR - luL) + (lvR - lvL)) + (lwR - lwL);
+    const double lc = cont(L, U, V, W, P, i, L.gamma);
+    double s = cont(L, U, V, W, P, i - 1, L.gamma) + cont(L, U, V, W, P, i + 1, L.gamma);
+    s = s + cont(L, U, V, W, P, i - sy, L.gamma);
+    s = s + cont(L, U, V, W, P, i + sy, L.gamma);
+    s = s + cont(L, U, V, W, P, i - sz, L.gamma);
+    s = s + cont(L, U, V, W, P, i + sz, L.gamma);
+    const double cl = fl * L.inv_h + L.eta_h2 * (6.0 * lc - s);
+    X[3 * fs + i] = P[i] + (L.cb[i] - cl) / L.dp;
+}
+
+// Vanka block residuals and corrections of one colour list; kidx picks the block's signature
+// class (active-face mask + the faces' dropped legs) in ktab.
+__global__ void k_vanka_delta_m(LevelK L, const double* __restrict__ X, const double* __restrict__ B,
+                                const int32_t* __restrict__ cells, const uint8_t* __restrict__ masks,
+                                const uint16_t* __restrict__ kidx, int n, const double* __restrict__ ktab,
+                                double* __restrict__ delta) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const Geom& g = L.g;
+    const int64_t fs = g.fs, sy = g.sy, sz = g.sz, i = cells[t];
+    const int m = masks[t];
+    const uint32_t m0 = L.cls[i], mx = L.cls[i + 1], my = L.cls[i + sy], mz = L.cls[i + sz];
+    const double *U = X, *V = X + fs, *W = X + 2 * fs, *P = X + 3 * fs;
+    double r[7];
+    r[0] = (m & 1) ? B[i] - mom_d(L, U, P, i, 1, cls_diag(m0, 0)) : 0.0;
+    r[1] = (m & 2) ? B[i + 1] - mom_d(L, U, P, i + 1, 1, cls_diag(mx, 0)) : 0.0;
+    r[2] = (m & 4) ? B[fs + i] - mom_d(L, V, P, i, sy, cls_diag(m0, 1)) : 0.0;
+    r[3] = (m & 8) ? B[fs + i + sy] - mom_d(L, V, P, i + sy, sy, cls_diag(my, 1)) : 0.0;
+    r[4] = (m & 16) ? B[2 * fs + i] - mom_d(L, W, P, i, sz, cls_diag(m0, 2)) : 0.0;
+    r[5] = (m & 32) ? B[2 * fs + i + sz] - mom_d(L, W, P, i + sz, sz, cls_diag(mz, 2)) : 0.0;
+    r[6] = B[3 * fs + i] - cont(L, U, V, W, P, i, L.gamma);
+    const double* K = ktab + static_cast<int64_t>(kidx[t]) * 49;
+#pragma unroll
+    for (int s = 0; s < 7; ++s) {
+        double acc = 0.0;
+#pragma unroll
+        for (int q = 0; q < 7; ++q) acc = acc + K[s * 7 + q] * r[q];
+        delta[static_cast<int64_t>(t) * 8 + s] = acc;
+    }
+}
+
+// Restriction / prolongation with the coarse / fine DofMap bits deciding which DOFs exist; legs
+// into Dirichlet or Inactive slots read 0 (dropped, no renormalisation).
+__global__ void k_restrict_m(LevelK F, LevelK C, const double* __restrict__ R, double* __restrict__ BC) {
+    pdl_wait();
+    const Geom &fg = F.g, &cg = C.g;
+    Cell c;
+    if (!thread_cell(cg, c)) return;
+    const uint32_t m = C.cls[c.i];
+    if (!(m & (CLS_P | CLS_U | CLS_V | CLS_W))) return;
+    const int64_t ffs = fg.fs, cfs = cg.fs;
+    const int64_t fb = fg.slot(2 * c.x, 2 * c.y, 2 * c.z);
+    const int64_t sx = 1, sy = fg.sy, sz = fg.sz;
+    if (m & CLS_U) BC[c.i] = restrict_face(R, fb, sx, sy, sz);
+    if (m & CLS_V) BC[cfs + c.i] = restrict_face(R + ffs, fb, sy, sx, sz);
+    if (m & CLS_W) BC[2 * cfs + c.i] = restrict_face(R + 2 * ffs, fb, sz, sx, sy);
+    if (m & CLS_P) {
+        const double* RP = R + 3 * ffs;
+        double s = 0.0;
+#pragma unroll
+        for (int k = 0; k < 2; ++k)
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+#pragma unroll
+                for (int ii = 0; ii < 2; ++ii) s = s + RP[fb + k * sz + j * sy + ii];
+        BC[3 * cfs + c.i] = 0.125 * s;
+    }
+}
+
+__global__ void k_prolong_add_m(LevelK F, LevelK C, const double* __restrict__ E, double* __restrict__ X) {
+    pdl_wait();
+    Cell c;
+    if (!thread_cell(F.g, c)) return;
+    const Geom &fg = F.g, &cg = C.g;
+    const uint32_t m = F.cls[c.i];
+    if (!(m & (CLS_P | CLS_U | CLS_V | CLS_W))) return;
+    const int64_t ffs = fg.fs, cfs = cg.fs;
+    const int z = c.z;
+    if (m & CLS_U) X[c.i] = X[c.i] + prolong_face<0>(E, cg, c.x, c.y, z);
+    if (m & CLS_V) X[ffs + c.i] = X[ffs + c.i] + prolong_face<1>(E + cfs, cg, c.x, c.y, z);
+    if (m & CLS_W) X[2 * ffs + c.i] = X[2 * ffs + c.i] + prolong_face<2>(E + 2 * cfs, cg, c.x, c.y, z);
+    if (m & CLS_P) X[3 * ffs + c.i] = X[3 * ffs + c.i] + E[3 * cfs + cg.slot(c.x >> 1, c.y >> 1, z >> 1)];
+}
+
+// compact FieldVector <-> padded layout through the level's slot list (SPEC:48 numbering)
+__global__ void k_gather(const int32_t* __restrict__ slots, int64_t n, const double* __restrict__ X,
+                         double* __restrict__ out) {
+    pdl_wait();
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
+        out[k] = X[slots[k]];
+}
+__global__ void k_scatter(const int32_t* __restrict__ slots, int64_t n, const double* __restrict__ in,
+                          double* __restrict__ X) {
+    pdl_wait();
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
+        X[slots[k]] = in[k];
+}
+
 inline int stream_blocks(int64_t n) {
     const int64_t b = (n + 255) / 256;
     return static_cast<int>(b < 148 * 16 ? b : 148 * 16);
@@ -2398,20 +2637,24 @@ static void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
     note(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...));
 }
 void launch_apply(const LevelK& L, const double* x, const double* b, double* y, double gamma, cudaStream_t s) {
-    launch_k(k_apply, cell_grid(L.g), dim3(BX, BY), 0, s, L, x, b, y, gamma);
+    if (L.cls) launch_k(k_apply_m, cell_grid(L.g), dim3(BX, BY), 0, s, L, x, b, y, gamma);
+    else launch_k(k_apply, cell_grid(L.g), dim3(BX, BY), 0, s, L, x, b, y, gamma);
     count();
 }
 void launch_dgs_vel(const LevelK& L, double* x, const double* b, int colour, cudaStream_t s) {
-    k_dgs_vel<<<cell_grid(L.g), dim3(BX, BY), 0, s>>>(L, x, b, colour);
+    if (L.cls) k_dgs_vel_m<<<cell_grid(L.g), dim3(BX, BY), 0, s>>>(L, x, b, colour);
+    else k_dgs_vel<<<cell_grid(L.g), dim3(BX, BY), 0, s>>>(L, x, b, colour);
     count();
 }
 void launch_dgs_pdelta(const LevelK& L, const double* x, const double* b, double* delta, int colour,
                        cudaStream_t s) {
-    k_dgs_pdelta<<<cell_grid(L.g), dim3(BX, BY), 0, s>>>(L, x, b, delta, colour);
+    if (L.cls) k_dgs_pdelta_m<<<cell_grid(L.g), dim3(BX, BY), 0, s>>>(L, x, b, delta, colour);
+    else k_dgs_pdelta<<<cell_grid(L.g), dim3(BX, BY), 0, s>>>(L, x, b, delta, colour);
     count();
 }
 void launch_dgs_papply(const LevelK& L, double* x, const double* delta, cudaStream_t s) {
-    k_dgs_papply<<<cell_grid(L.g), dim3(BX, BY), 0, s>>>(L, x, delta);
+    if (L.cls) k_dgs_papply_m<<<cell_grid(L.g), dim3(BX, BY), 0, s>>>(L, x, delta);
+    else k_dgs_papply<<<cell_grid(L.g), dim3(BX, BY), 0, s>>>(L, x, delta);
     count();
 }
 void launch_dgs_cb(const LevelK& L, const double* b, cudaStream_t s) {
@@ -2419,13 +2662,16 @@ void launch_dgs_cb(const LevelK& L, const double* b, cudaStream_t s) {
     count();
 }
 void launch_dgs_prev(const LevelK& L, double* x, const double* b, int colour, cudaStream_t s) {
-    k_dgs_prev<<<cell_grid(L.g), dim3(BX, BY), 0, s>>>(L, x, b, colour);
+    if (L.cls) k_dgs_prev_m<<<cell_grid(L.g), dim3(BX, BY), 0, s>>>(L, x, colour);
+    else k_dgs_prev<<<cell_grid(L.g), dim3(BX, BY), 0, s>>>(L, x, b, colour);
     count();
 }
 void launch_vanka_delta(const LevelK& L, const double* x, const double* b, const int32_t* cells,
-                        const uint8_t* masks, int ncells, const double* ktab, double* delta, cudaStream_t s) {
+                        const uint8_t* masks, int ncells, const double* ktab, double* delta, cudaStream_t s,
+                        const uint16_t* kidx) {
     if (ncells <= 0) return;
-    k_vanka_delta<<<(ncells + 127) / 128, 128, 0, s>>>(L, x, b, cells, masks, ncells, ktab, delta);
+    if (L.cls) k_vanka_delta_m<<<(ncells + 127) / 128, 128, 0, s>>>(L, x, b, cells, masks, kidx, ncells, ktab, delta);
+    else k_vanka_delta<<<(ncells + 127) / 128, 128, 0, s>>>(L, x, b, cells, masks, ncells, ktab, delta);
     count();
 }
 void launch_vanka_apply(const LevelK& L, double* x, const int32_t* cells, const uint8_t* masks, int ncells,
@@ -2437,6 +2683,11 @@ void launch_vanka_apply(const LevelK& L, double* x, const int32_t* cells, const 
 void launch_restrict(const LevelK& F, const LevelK& C, const double* rf, double* bc, cudaStream_t s, int zc_lo,
                      int nzc) {
     dim3 grid = cell_grid(C.g);
+    if (F.cls) {  // labelled levels (single part): one thread per coarse cell
+        launch_k(k_restrict_m, grid, dim3(BX, BY), 0, s, F, C, rf, bc);
+        count();
+        return;
+    }
     grid.z = nzc < 0 ? C.g.nz : nzc;
     if (grid.z == 0) return;
     // z-marching variant (SMG_RESTRICT_ZM, default on) when the columns alone leave segments of
@@ -2458,7 +2709,8 @@ void launch_restrict(const LevelK& F, const LevelK& C, const double* rf, double*
 }
 
 void launch_prolong_add(const LevelK& F, const LevelK& C, const double* xc, double* xf, cudaStream_t s) {
-    launch_k(k_prolong_add, cell_grid(F.g), dim3(BX, BY), 0, s, F, C, xc, xf);
+    if (F.cls) launch_k(k_prolong_add_m, cell_grid(F.g), dim3(BX, BY), 0, s, F, C, xc, xf);
+    else launch_k(k_prolong_add, cell_grid(F.g), dim3(BX, BY), 0, s, F, C, xc, xf);
     count();
 }
 void launch_coarse_gemv(const double* ksym, const int32_t* slots, int n, const double* b, double* x,
@@ -2480,6 +2732,16 @@ void launch_pack(const LevelK& L, const double* padded, double* compact, cudaStr
 }
 void launch_unpack(const LevelK& L, const double* compact, double* padded, cudaStream_t s) {
     launch_k(k_pack, cell_grid(L.g), dim3(BX, BY), 0, s, L, padded, const_cast<double*>(compact), 1);
+    count();
+}
+void launch_gather(const int32_t* slots, int64_t n, const double* padded, double* compact, cudaStream_t s) {
+    if (n <= 0) return;
+    launch_k(k_gather, dim3(stream_blocks(n)), dim3(256), 0, s, slots, n, padded, compact);
+    count();
+}
+void launch_scatter(const int32_t* slots, int64_t n, const double* compact, double* padded, cudaStream_t s) {
+    if (n <= 0) return;
+    launch_k(k_scatter, dim3(stream_blocks(n)), dim3(256), 0, s, slots, n, compact, padded);
     count();
 }
 static dim3 dot_grid(const Geom& g) {
@@ -2506,12 +2768,16 @@ void launch_final_scalar(const Geom& g, const double* partials, double* sc, int 
 }
 void launch_apply_q(const LevelK& L, const double* t, const double* q0, double* q1, double* tn, const double* sc,
                     double* partials, int halo_lo, int halo_hi, cudaStream_t s) {
-    launch_k(k_apply_q, dot_grid(L.g), dim3(32, 8), 0, s, L, t, q0, q1, tn, sc, partials, halo_lo, halo_hi);
+    if (L.cls) launch_k(k_apply_q<true>, dot_grid(L.g), dim3(32, 8), 0, s, L, t, q0, q1, tn, sc, partials, halo_lo, halo_hi);
+    else launch_k(k_apply_q<false>, dot_grid(L.g), dim3(32, 8), 0, s, L, t, q0, q1, tn, sc, partials, halo_lo, halo_hi);
     count();
 }
 void launch_apply_x(const LevelK& L, const double* x0, const double* d0, const double* q, const double* b, double* x1,
                     double* d1, const double* sc, double* partials, int halo_lo, int halo_hi, cudaStream_t s) {
-    launch_k(k_apply_x, dot_grid(L.g), dim3(32, 8), 0, s, L, x0, d0, q, b, x1, d1, sc, partials, halo_lo, halo_hi);
+    if (L.cls)
+        launch_k(k_apply_x<true>, dot_grid(L.g), dim3(32, 8), 0, s, L, x0, d0, q, b, x1, d1, sc, partials, halo_lo, halo_hi);
+    else
+        launch_k(k_apply_x<false>, dot_grid(L.g), dim3(32, 8), 0, s, L, x0, d0, q, b, x1, d1, sc, partials, halo_lo, halo_hi);
     count();
 }
 static int env_int(const char* name, int dflt) {

@@ -71,7 +71,17 @@ struct LevelK {
     // is): launch_dgs_cb fills it before a sweep; prev steps then read L~x only
     double* cb = nullptr;
     int tiled = 0;  // DGS sweep in tile order (OD-1 rev. 2, dgs_tiled)
+    // General labelled domain: per cell slot (one field long, ghosts 0) the DofMap
+    // bits CLS_* of the cell's pressure and its three low faces; nullptr on the walled box,
+    // whose statuses are analytic.
+    const uint32_t* cls = nullptr;
 };
+
+// DofMap bits of a cell slot on a labelled level (classify_dofs SPEC:45-53, partition_band
+// SPEC:63-71): active pressure / low u, v, w face; band cell; low faces in V2; and per low face
+// its momentum diagonal 6 - (dropped Neumann legs) in 3 bits from bit 8 + 3 comp.
+constexpr uint32_t CLS_P = 1, CLS_U = 2, CLS_V = 4, CLS_W = 8, CLS_BAND = 16, CLS_U2 = 32, CLS_V2 = 64, CLS_W2 = 128;
+constexpr int CLS_DIAG_SHIFT = 8;
 
 // ---- stencil launchers (kernels.cu) ----
 // y = L~x (gamma) or, with b != nullptr, y = b - L~x, on active slots only.
@@ -95,8 +105,10 @@ struct VankaPairs {
     int pairs = 0;
     int first[4] = {0, 0, 0, 0};
 };
+// kidx (labelled levels): per block the index of its signature class in ktab (nullptr: the face mask)
 void launch_vanka_delta(const LevelK& L, const double* x, const double* b, const int32_t* cells,
-                        const uint8_t* masks, int ncells, const double* ktab, double* delta, cudaStream_t s);
+                        const uint8_t* masks, int ncells, const double* ktab, double* delta, cudaStream_t s,
+                        const uint16_t* kidx = nullptr);
 // amask (z-slabs, optional): per block, the slots this part owns (bit s = slot s, bit 6 = p).
 void launch_vanka_apply(const LevelK& L, double* x, const int32_t* cells, const uint8_t* masks, int ncells,
                         const double* delta, cudaStream_t s, const uint8_t* amask = nullptr);
@@ -124,6 +136,9 @@ void launch_coarse_gemv(const double* ksym, const int32_t* slots, int n, const d
                         cudaStream_t s, bool accumulate = false);
 void launch_pack(const LevelK& L, const double* padded, double* compact, cudaStream_t s);
 void launch_unpack(const LevelK& L, const double* compact, double* padded, cudaStream_t s);
+// labelled levels: compact[k] = padded[slots[k]] / padded[slots[k]] = compact[k], k < n
+void launch_gather(const int32_t* slots, int64_t n, const double* padded, double* compact, cudaStream_t s);
+void launch_scatter(const int32_t* slots, int64_t n, const double* compact, double* padded, cudaStream_t s);
 
 // ---- BLAS-1 (kernels.cu); n = padded vector length (multiple of 32) ----
 // Canonical inner products (OD-12 rev. 2): block partials over 32 x 8 cells x

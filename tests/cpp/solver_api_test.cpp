@@ -41,10 +41,17 @@ static int host_checks() {
     CellGrid ex = CellGrid::box(4, 4, 4, 0.25);
     for (auto& l : ex.labels) l = CellLabel::Exterior;
     if (classify_dofs(ex).N != 0) return fail("all-exterior census");
-    // the GPU path refuses labellings it does not implement
+    // a grid without any active DOF cannot carry a hierarchy; a wrong label count is rejected
     try {
         build_hierarchy(ex, 1.0, 1e-3, 2);
-        return fail("build_hierarchy accepted an exterior labelling");
+        return fail("build_hierarchy accepted an all-exterior labelling");
+    } catch (const std::invalid_argument&) {
+    }
+    try {
+        CellGrid bad = CellGrid::box(4, 4, 4, 0.25);
+        bad.labels.pop_back();
+        build_hierarchy(bad, 1.0, 1e-3, 2);
+        return fail("build_hierarchy accepted a short label array");
     } catch (const std::invalid_argument&) {
     }
     std::printf("host checks ok\n");
@@ -83,9 +90,41 @@ static int gpu_solve() {
     return 0;
 }
 
+// General labelled domain through the same API: a channel with a Dirichlet block
+// and an Exterior outflow column; MG-SQMR converges, the history is the true residual, and the
+// operator drops the legs into Inactive faces (a constant u field has zero momentum residual only
+// where its stencil is full).
+static int gpu_labeled() {
+    const int nx = 32, ny = 16, nz = 16;
+    CellGrid g = CellGrid::box(nx, ny, nz, 1.0 / ny);
+    for (int z = 0; z < nz; ++z)
+        for (int y = 0; y < ny; ++y)
+            for (int x = 0; x < nx; ++x) {
+                CellLabel& l = g.labels[(static_cast<std::size_t>(z) * ny + y) * nx + x];
+                if (x >= 8 && x < 12 && y >= 6 && y < 10) l = CellLabel::Dirichlet;
+                if (x >= nx - 1) l = CellLabel::Exterior;
+            }
+    DofMap m = classify_dofs(g);
+    MgHierarchy h = build_hierarchy(g, 1.0, 1e-3, 3);
+    if (h.ndof() != m.N) return fail("labelled ndof != classify_dofs");
+    const smg_grid_desc d{3, nx, ny, nz, g.h};
+    FieldVector b(static_cast<std::size_t>(h.ndof()));
+    if (smg_forcing_labeled(&d, reinterpret_cast<const std::uint8_t*>(g.labels.data()), 2, 4, b.data()) != 0)
+        return fail("forcing_labeled");
+    SolveResult r = sqmr_solve({&h, 0, false}, h, b, 1e-8, 100);
+    if (r.status != SolveStatus::Converged) return fail("labelled sqmr_solve did not converge");
+    FieldVector lx = apply({&h, 0, false}, r.x);
+    for (std::size_t k = 0; k < lx.size(); ++k) lx[k] = b[k] - lx[k];
+    const double rel = norm2(lx) / norm2(b);
+    if (std::fabs(rel - r.history.back().rel_residual) > 1e-9 * rel) return fail("labelled history != true residual");
+    std::printf("labelled ok: N = %lld, %zu iterations, rel = %.3e\n", static_cast<long long>(m.N), r.history.size(), rel);
+    return 0;
+}
+
 int main(int argc, char** argv) {
     try {
         if (argc > 1 && std::strcmp(argv[1], "gpu") == 0) return gpu_solve();
+        if (argc > 1 && std::strcmp(argv[1], "gpu_labeled") == 0) return gpu_labeled();
         return host_checks();
     } catch (const std::exception& e) {
         std::fprintf(stderr, "exception: %s\n", e.what());

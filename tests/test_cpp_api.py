@@ -41,3 +41,11 @@ def test_cpp_api_solves_cfg0_like_the_golden(binary):
     assert got["history"] == g["history"]  # bit-identical (the oracle's canonical reductions)
     assert abs(got["u_norm"] - g["u_norm"]) <= 1e-12 * g["u_norm"]
     assert np.all(np.diff(np.log(got["history"])) < 1.5)
+
+
+@pytest.mark.gpu
+def test_cpp_api_labelled_domain(binary):
+    """build_hierarchy on a CellGrid with Dirichlet and Exterior cells through the C++ API."""
+    r = subprocess.run([binary, "gpu_labeled"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    assert "labelled ok" in r.stdout
