@@ -198,6 +198,12 @@ int smg_last_timing(const smg_ctx* ctx, smg_timing* out);
  * solve, 9 fused pair of inner products, 10 axpy, 11 one SQMR iteration graph. */
 int smg_time_kernel(smg_ctx* ctx, int which, int level, int reps, double* avg_ms);
 
+/* Debug aid (compute-sanitizer is not available on every GPU pool): with SMG_GUARD=1 in the
+ * environment at smg_create time every device buffer of the context is allocated between two
+ * 4 KiB guard bands; this returns the number of guard bytes any kernel has overwritten so far
+ * (0: no out-of-bounds store; always 0 when the guards are off), or a negative smg_err. */
+int64_t smg_check_guards(smg_ctx* ctx);
+
 /* Brackets a region for ncu --profile-from-start off (cudaProfilerStart/Stop). */
 int smg_profiler_range(int on);
 

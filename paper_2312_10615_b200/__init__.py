@@ -60,6 +60,7 @@ EXPORTED = [
     "smg_profiler_range", "smg_slab_plan", "smg_mg_solve", "smg_census", "smg_assemble_rhs",
     "smg_nccl_unique_id", "smg_create_rank", "smg_dgs_tile",
     "smg_create_labeled", "smg_coarsen_labels", "smg_census_labeled", "smg_forcing_labeled",
+    "smg_check_guards",
 ]
 LAB_DIRICHLET, LAB_INTERIOR, LAB_EXTERIOR = 0, 1, 2  # CellLabel
 
@@ -121,6 +122,8 @@ def lib():
     L.smg_census_labeled.argtypes = [C.POINTER(GridDesc), _U8, C.c_int,
                                      np.ctypeslib.ndpointer(np.int64, flags="C_CONTIGUOUS")]
     L.smg_forcing_labeled.argtypes = [C.POINTER(GridDesc), _U8, C.c_int, C.c_uint64, _D]
+    L.smg_check_guards.restype = C.c_int64
+    L.smg_check_guards.argtypes = [P]
     _lib = L
     return L
 
@@ -321,6 +324,13 @@ class Solver:
     def _check(self, rc):
         if rc != 0:
             raise SmgError(f"smg error {rc}: {lib().smg_last_error(self._ctx).decode()}")
+
+    def check_guards(self):
+        """Guard-band bytes overwritten by any kernel (needs SMG_GUARD=1 at creation; 0 = clean)."""
+        n = lib().smg_check_guards(self._ctx)
+        if n < 0:
+            self._check(int(n))
+        return int(n)
 
     def ndof(self, level=0):
         c = np.zeros(5, np.int64)

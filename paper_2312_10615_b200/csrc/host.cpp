@@ -337,15 +337,46 @@ struct smg_ctx {
     // general labelled domain (smg_create_labeled): fine-level cell labels, x fastest; empty: walled box
     std::vector<uint8_t> labels;
 
+    // SMG_GUARD=1 (debug; compute-sanitizer is closed on the GPU pool): every device buffer sits
+    // between two 4 KiB guard bands filled with 0xA5; smg_check_guards reports any band a kernel
+    // wrote into (an out-of-bounds store of a stencil, list or tile kernel).
+    static constexpr size_t kGuard = 4096;
+    struct GuardRec {
+        unsigned char* base;
+        size_t bytes;
+    };
+    std::vector<GuardRec> guards;
+    bool guard_on = std::getenv("SMG_GUARD") && std::atoi(std::getenv("SMG_GUARD")) != 0;
     template <class T>
     T* dalloc(int64_t count) {
         void* p = nullptr;
-        const size_t bytes = static_cast<size_t>(count) * sizeof(T);
-        cudaError_t e = cudaMalloc(&p, bytes ? bytes : 8);
+        size_t bytes = static_cast<size_t>(count) * sizeof(T);
+        if (!bytes) bytes = 8;
+        const size_t pad = guard_on ? kGuard : 0;
+        const size_t body = (bytes + 255) / 256 * 256;
+        cudaError_t e = cudaMalloc(&p, body + 2 * pad);
         if (e != cudaSuccess) throw SmgError(SMG_ENOMEM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
-        CK(cudaMemsetAsync(p, 0, bytes ? bytes : 8, st));
         allocs.push_back(p);
-        return static_cast<T*>(p);
+        unsigned char* base = static_cast<unsigned char*>(p);
+        if (guard_on) {
+            CK(cudaMemsetAsync(base, 0xA5, body + 2 * pad, st));
+            guards.push_back({base, body});
+        }
+        CK(cudaMemsetAsync(base + pad, 0, bytes, st));
+        return reinterpret_cast<T*>(base + pad);
+    }
+    // number of guard bytes overwritten since creation (0 when the guards are off)
+    int64_t check_guards() {
+        if (!guard_on) return 0;
+        CK(cudaStreamSynchronize(st));
+        std::vector<unsigned char> h(2 * kGuard);
+        int64_t bad = 0;
+        for (const GuardRec& g : guards) {
+            CK(cudaMemcpy(h.data(), g.base, kGuard, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(h.data() + kGuard, g.base + kGuard + g.bytes, kGuard, cudaMemcpyDeviceToHost));
+            for (unsigned char c : h) bad += c != 0xA5;
+        }
+        return bad;
     }
     ~smg_ctx() {
         if (st) cudaStreamSynchronize(st);
@@ -2302,6 +2333,16 @@ int smg_time_kernel(smg_ctx* c, int which, int level, int reps, double* avg_ms) 
         CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
         *avg_ms = ms / reps;
     });
+}
+
+int64_t smg_check_guards(smg_ctx* c) {
+    if (!c) return SMG_EINVAL;
+    int64_t bad = 0;
+    const int rc = guard(c, [&] {
+        bad = c->check_guards();
+        for (auto& q : c->owned) bad += q->check_guards();
+    });
+    return rc != 0 ? rc : bad;
 }
 
 int smg_profiler_range(int on) {

@@ -1,0 +1,19 @@
+"""CUDA-event time of the fine-level symmetric DGS sweep / Vanka sweep / smooth (cfg by id)."""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import bench  # noqa: E402
+import paper_2312_10615_b200 as smg  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", type=int, default=2)
+ap.add_argument("--reps", type=int, default=20)
+a = ap.parse_args()
+nx, ny, nz, h, lv, kind, seed, tol, name = bench.CONFIGS[a.config]
+s = smg.Solver(nx, ny, nz, h=h, levels=lv)
+s.set_rhs(smg.forcing(nx, ny, nz, h=h, kind=kind, seed=seed))
+for rep in range(3):
+    print(name.split(":")[0], "dgs_sym %.4f  vanka_sym %.4f  smooth %.4f  apply %.4f ms" % (
+        s.time_kernel(2, a.reps, 0), s.time_kernel(4, a.reps, 0), s.time_kernel(5, a.reps, 0), s.time_kernel(0, a.reps, 0)))
