@@ -7,6 +7,7 @@ import json
 import os
 import re
 import subprocess
+import sys
 import tempfile
 
 import numpy as np
@@ -130,3 +131,18 @@ def test_cavity_rhs_bitwise_matches_oracle(dims, eta):
     nu = (nx - 1) * ny * nz
     assert np.count_nonzero(got) == (nx - 1) * nz and np.all(got[:nu].reshape(nz, ny, nx - 1)[:, -1, :] > 0)
     assert not got[nu:].any()  # RHS compatibility: continuity entries sum to 0 (tangential lid)
+
+
+def test_util_hpp_matches_reference_golden():
+    """The drop-in include/stokesmg/util.hpp against the REFERENCE's own header: the probe
+    tests/golden/util_probe.cpp was compiled against /root/reference/proj/include (util.hpp:9-47)
+    by tests/golden/make_util_golden.py and its output committed; the same probe compiled against
+    the repo's header must print the same bytes (order-sensitive sums, norm2, the static block
+    partition of parallel_for).  Where the reference is present the golden is re-derived too."""
+    sys.path.insert(0, os.path.join(ROOT, "tests", "golden"))
+    import make_util_golden as mk
+
+    golden = open(os.path.join(ROOT, "tests", "golden", "util_probe_reference.txt")).read()
+    assert mk.run_probe(os.path.join(ROOT, "include")) == golden
+    if os.path.isdir(mk.REF_INC):
+        assert mk.run_probe(mk.REF_INC) == golden
