@@ -303,6 +303,8 @@ def run_ours(args, ws, rank, local):
         for c in [int(v) for v in args.also.split(",") if v.strip()]:
             if c != args.config:
                 also[f"cfg{c}"] = measure_resident(smg, c, 2)
+        if not args.no_labelled:
+            also["labelled_cylinder"] = measure_labelled(smg, 2)
     if rank == 0:
         cpu = None
         if not args.no_cpu_baseline:
@@ -357,6 +359,35 @@ def measure_resident(smg, cfg, steps, warmup=1):
         return {"workload": name, "error": str(e)}
     b = smg.forcing(nx, ny, nz, h=h, kind=kind, seed=seed)
     s.set_rhs(b)
+    for _ in range(warmup):
+        s.solve_resident(tol, 500)
+    ms, its, hist, st = [], [], None, None
+    for _ in range(steps):
+        hist, st = s.solve_resident(tol, 500)
+        t = s.timing()
+        ms.append(t["solve_ms"])
+        its.append(t["iterations"])
+    s.close()
+    tot_ms = sum(ms)
+    return {"workload": name, "N_dof": n, "value": n * sum(its) / (tot_ms / 1e3), "unit": "DOF/s",
+            "ms_per_solve": tot_ms / steps, "iterations_per_solve": sum(its) / steps, "converged": st == 0,
+            "final_rel_residual": float(hist[-1]) if len(hist) else None, "steps": steps, "warmup": warmup}
+
+
+def measure_labelled(smg, steps, warmup=1):
+    """General labelled domain: the cylinder channel of PAPER section 6.2.2 at
+    256 x 128 x 128 cells (Dirichlet cylinder, Exterior outflow column), 5 levels, channel forcing
+    seed 4, tol 1e-6 -- device-resident solves through the labelled-domain kernels."""
+    from paper_2312_10615_b200 import scenarios
+    nx, ny, nz, lv, tol = 256, 128, 128, 5, 1e-6
+    name = f"cylinder3d {nx}x{ny}x{nz}, {lv}-level V, channel forcing seed 4, tol {tol:g}"
+    lab = scenarios.cylinder3d(nx, ny, nz)
+    try:
+        s = smg.Solver.from_labels(lab, h=1.0 / ny, levels=lv)
+    except Exception as e:
+        return {"workload": name, "error": str(e)}
+    s.set_rhs(smg.forcing_labels(lab, 1.0 / ny, smg.FORCE_CHANNEL, 4))
+    n = s.ndof(0)
     for _ in range(warmup):
         s.solve_resident(tol, 500)
     ms, its, hist, st = [], [], None, None
@@ -477,6 +508,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
+    ap.add_argument("--no-labelled", action="store_true", help="skip the labelled-domain (cylinder channel) line "
+                                                               "reported under also.labelled_cylinder")
     ap.add_argument("--also", default="3", help="comma list of extra configs measured device-resident "
                                                 "(2 solves each) and reported under 'also'; '' for none")
     ap.add_argument("--cpu-1thread", action="store_true", help="add a single-thread CPU reference point")

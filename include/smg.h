@@ -115,6 +115,15 @@ int64_t smg_census_labeled(const smg_grid_desc* grid, const uint8_t* labels, int
  * the component and the face's storage coordinates). */
 int smg_forcing_labeled(const smg_grid_desc* grid, const uint8_t* labels, int kind, uint64_t seed, double* b);
 
+/* assemble_rhs on a labelled grid with general BoundaryData, host
+ * only: b += the stencil legs of the active rows into Dirichlet-valued faces.  g_c holds the
+ * Dirichlet velocity of every face of component c over n_a + 1 faces along its own axis and
+ * n_a + 2 along the two others (tangential index shifted by one, so the faces of the ring cells,
+ * coordinates -1 and n_a, are included), x fastest; entries at non-Dirichlet faces are ignored.
+ * b is the compact FieldVector of the grid's DofMap (add the body force before or after). */
+int smg_assemble_rhs_labeled(const smg_grid_desc* grid, const uint8_t* labels, double eta, const double* gu,
+                             const double* gv, const double* gw, double* b);
+
 /* Multi-process z-slab decomposition: one process per GPU, NCCL over NVLink.
  * Rank 0 calls smg_nccl_unique_id and the caller's launcher (torch.distributed,
  * MPI, ...) broadcasts the 128-byte id; every rank then calls smg_create_rank

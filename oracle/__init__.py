@@ -250,6 +250,16 @@ class Oracle:
         st = lib().orc_mg_solve(self._h, b, x, tol, maxit, hist, secs, C.byref(it))
         return x, hist[: it.value].copy(), secs[: it.value].copy(), int(st)
 
+    def dirichlet_rhs(self, gu, gv, gw, b=None):
+        """assemble_rhs with general Dirichlet face data: returns b + the stencil legs
+        into Dirichlet faces; g_c shaped with n_a + 1 along its own axis, n_a + 2 along the others
+        (ring faces included), as (z, y, x) arrays."""
+        L = lib()
+        L.orc_dirichlet_rhs.argtypes = [C.c_void_p, _D, _D, _D, _D]
+        bb = np.zeros(self.ndof(0)) if b is None else np.array(b, np.float64, copy=True)
+        L.orc_dirichlet_rhs(self._h, *(np.ascontiguousarray(g, np.float64).ravel() for g in (gu, gv, gw)), bb)
+        return bb
+
     def forcing(self, kind=FORCE_UNIFORM, seed=0):
         b = np.empty(self.ndof(0))
         lib().orc_forcing(self._h, kind, seed, b)

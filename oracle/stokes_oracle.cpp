@@ -1234,7 +1234,15 @@ static double lid_value(const Level& L, int c, int x, int y, int z) {
 // stencil leg of an active row into a Dirichlet face moves to the right-hand
 // side with the opposite sign of its matrix entry (momentum: -eta/h^2 legs;
 // continuity: +-1/h legs to Dirichlet faces).
+template <class GV>
+static void dirichlet_rhs_g(const Level& L, vec& b, GV&& value);
 static void dirichlet_rhs(const Level& L, vec& b) {
+    dirichlet_rhs_g(L, b, [&](int c, int x, int y, int z) { return lid_value(L, c, x, y, z); });
+}
+// General BoundaryData: value(c, x, y, z) is the Dirichlet velocity of the face of
+// component c at storage coordinates (x, y, z) (ring faces included: tangential coordinates -1 and n).
+template <class GV>
+static void dirichlet_rhs_g(const Level& L, vec& b, GV&& value) {
     const DofMap& m = L.map;
     const int d[6][3] = {{-1, 0, 0}, {1, 0, 0}, {0, -1, 0}, {0, 1, 0}, {0, 0, -1}, {0, 0, 1}};
     for (int64_t q = 0; q < m.off[3]; ++q) {
@@ -1243,7 +1251,7 @@ static void dirichlet_rhs(const Level& L, vec& b) {
         for (int k = 0; k < 6; ++k) {
             const int x = p[0] + d[k][0], y = p[1] + d[k][1], z = p[2] + d[k][2];
             if (m.face(c, x, y, z) != ST_DIRICHLET) continue;
-            const double gv = lid_value(L, c, x, y, z);
+            const double gv = value(c, x, y, z);
             if (gv != 0.0) b[q] = b[q] + L.eta_h2 * gv;  // row entry -eta/h^2 -> rhs +eta/h^2 g
         }
     }
@@ -1254,7 +1262,7 @@ static void dirichlet_rhs(const Level& L, vec& b) {
                 int f3[3] = {p[0], p[1], p[2]};
                 f3[c] += side;
                 if (m.face(c, f3[0], f3[1], f3[2]) != ST_DIRICHLET) continue;
-                const double gv = lid_value(L, c, f3[0], f3[1], f3[2]);
+                const double gv = value(c, f3[0], f3[1], f3[2]);
                 // (L~x)_C = -(x_R - x_L)/h: entry -1/h on the right face, +1/h on the left face
                 if (gv != 0.0) b[q] = b[q] - (side ? -L.inv_h : L.inv_h) * gv;
             }
@@ -1535,6 +1543,29 @@ void orc_forcing_box(int nx, int ny, int nz, double h, int kind, uint64_t seed, 
     forcing(L, kind, seed, bb);
     out(bb, b);
 }
+// assemble_rhs on a labelled grid with general Dirichlet data: b += the stencil
+// legs into Dirichlet faces.  g[c] holds the face values of component c over the extents
+// n_a + 1 along its own axis and n_a + 2 along the others (tangential index shifted by one: the
+// ring faces -1 and n_a are included), x fastest.
+void orc_dirichlet_rhs(void* h, const double* gu, const double* gv, const double* gw, double* b) {
+    Hierarchy& H = HH(h);
+    const Level& L = *H.lv[0];
+    const double* g[3] = {gu, gv, gw};
+    const int n[3] = {L.map.n[0], L.map.n[1], L.map.n[2]};
+    vec bb = V(b, L.map.N);
+    dirichlet_rhs_g(L, bb, [&](int c, int x, int y, int z) {
+        const int p[3] = {x, y, z};
+        int e[3], q[3];
+        for (int a = 0; a < 3; ++a) {
+            e[a] = n[a] + (a == c ? 1 : 2);
+            q[a] = p[a] + (a == c ? 0 : 1);
+            if (q[a] < 0 || q[a] >= e[a]) return 0.0;
+        }
+        return g[c][(static_cast<size_t>(q[2]) * e[1] + q[1]) * e[0] + q[0]];
+    });
+    out(bb, b);
+}
+
 void orc_census_box(int dim, int nx, int ny, int nz, int width, int64_t* out2) {
     census_box(dim, nx, ny, nz, width, out2);
 }

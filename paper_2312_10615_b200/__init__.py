@@ -60,7 +60,7 @@ EXPORTED = [
     "smg_profiler_range", "smg_slab_plan", "smg_mg_solve", "smg_census", "smg_assemble_rhs",
     "smg_nccl_unique_id", "smg_create_rank", "smg_dgs_tile",
     "smg_create_labeled", "smg_coarsen_labels", "smg_census_labeled", "smg_forcing_labeled",
-    "smg_check_guards",
+    "smg_check_guards", "smg_assemble_rhs_labeled",
 ]
 LAB_DIRICHLET, LAB_INTERIOR, LAB_EXTERIOR = 0, 1, 2  # CellLabel
 
@@ -122,6 +122,7 @@ def lib():
     L.smg_census_labeled.argtypes = [C.POINTER(GridDesc), _U8, C.c_int,
                                      np.ctypeslib.ndpointer(np.int64, flags="C_CONTIGUOUS")]
     L.smg_forcing_labeled.argtypes = [C.POINTER(GridDesc), _U8, C.c_int, C.c_uint64, _D]
+    L.smg_assemble_rhs_labeled.argtypes = [C.POINTER(GridDesc), _U8, C.c_double, _D, _D, _D, _D]
     L.smg_check_guards.restype = C.c_int64
     L.smg_check_guards.argtypes = [P]
     _lib = L
@@ -187,6 +188,30 @@ def forcing_labels(labels, h, kind=FORCE_UNIFORM, seed=0):
     if rc != 0:
         raise SmgError(f"smg_forcing_labeled failed ({rc})")
     return b
+
+
+def dirichlet_shapes(labels):
+    """Shapes (z, y, x) of the Dirichlet face-value arrays g_u, g_v, g_w of smg_assemble_rhs_labeled:
+    n + 1 faces along the component's axis, n + 2 along the others (ring faces included)."""
+    nz, ny, nx = np.asarray(labels).shape
+    return (nz + 2, ny + 2, nx + 1), (nz + 2, ny + 1, nx + 2), (nz + 1, ny + 2, nx + 2)
+
+
+def assemble_rhs_labels(labels, h, gu, gv, gw, eta=1.0, b=None):
+    """assemble_rhs with general Dirichlet data on a labelled grid (host only):
+    returns b (default 0) plus the stencil legs into Dirichlet-valued faces."""
+    lab = _labels3(labels)
+    nz, ny, nx = lab.shape
+    gs = [np.ascontiguousarray(g, np.float64) for g in (gu, gv, gw)]
+    for g, shp in zip(gs, dirichlet_shapes(lab)):
+        if g.shape != shp:
+            raise ValueError(f"Dirichlet data shaped {g.shape}, expected {shp}")
+    out = np.zeros(census_labels(lab)["N"]) if b is None else np.array(b, np.float64, copy=True)
+    rc = lib().smg_assemble_rhs_labeled(C.byref(GridDesc(3, nx, ny, nz, h)), lab.ravel(), eta,
+                                        gs[0].ravel(), gs[1].ravel(), gs[2].ravel(), out)
+    if rc != 0:
+        raise SmgError(f"smg_assemble_rhs_labeled failed ({rc})")
+    return out
 
 
 def slab_plan(nx, ny, nz, levels, nparts, rank, h=None):

@@ -9,7 +9,10 @@
 // gamma (1e-3), levels, nu (1), band_width (1), cycle ("V"|"W"), method
 // ("mg-sqmr"|"mg"), tol (1e-8), maxit (200), forcing ("uniform"|"fourier"|
 // "channel"|"cavity": lid-driven, u = lid (1) on the top y face), seed (0), output_dir (env SMG_OUTPUT_DIR, else "."), devices ([0]),
-// vanka ("multiplicative"|"additive"), omega (1), vtk (0; 1 writes fields.vtk).
+// vanka ("multiplicative"|"additive"), omega (1), vtk (0; 1 writes fields.vtk),
+// domain (path of a domain file: header line `dim nx ny nz h`, then one character per
+// cell, D / I / E, row-major with x fastest, whitespace ignored -- a general labelled domain;
+// nx, ny, nz, h then come from the file).
 // Defaults follow SPEC:567-569.  Exit codes: 0 converged,
 // 2 not converged, 1 usage/config error.
 #include <algorithm>
@@ -133,6 +136,31 @@ bool write_vtk(const std::string& path, int nx, int ny, int nz, double h, const 
     return ok;
 }
 
+// Domain file: `3 nx ny nz h` then nx*ny*nz characters D / I / E (whitespace ignored).
+bool read_domain(const std::string& path, smg_grid_desc& g, std::vector<uint8_t>& lab, std::string& err) {
+    std::ifstream f(path);
+    if (!f) { err = "cannot read " + path; return false; }
+    int dim = 0;
+    if (!(f >> dim >> g.nx >> g.ny >> g.nz >> g.h) || dim != 3 || g.nx < 1 || g.ny < 1 || g.nz < 1 || !(g.h > 0)) {
+        err = "bad domain header (expected: 3 nx ny nz h)";
+        return false;
+    }
+    g.dim = 3;
+    const size_t nc = static_cast<size_t>(g.nx) * g.ny * g.nz;
+    lab.clear();
+    lab.reserve(nc);
+    char ch;
+    while (f.get(ch)) {
+        if (std::isspace(static_cast<unsigned char>(ch))) continue;
+        if (ch == 'D') lab.push_back(0);
+        else if (ch == 'I') lab.push_back(1);
+        else if (ch == 'E') lab.push_back(2);
+        else { err = std::string("bad cell label '") + ch + "'"; return false; }
+    }
+    if (lab.size() != nc) { err = "label count != nx*ny*nz (SPEC:28)"; return false; }
+    return true;
+}
+
 int usage() {
     std::fprintf(stderr, "usage: solver run <config.json> | solver census <config.json> | solver verify [--max-n N]\n");
     return 1;
@@ -207,12 +235,24 @@ int main(int argc, char** argv) {
     if (!parse_json(ss.str(), c, err)) { std::fprintf(stderr, "config error: %s\n", err.c_str()); return 1; }
     auto num = [&](const char* k, double d) { return c.num.count(k) ? c.num[k] : d; };
     auto str = [&](const char* k, const char* d) { return c.str.count(k) ? c.str[k] : std::string(d); };
-    if (!c.num.count("nx")) { std::fprintf(stderr, "config error: nx is required\n"); return 1; }
+    std::vector<uint8_t> labels;  // non-empty: a general labelled domain from the "domain" file
     smg_grid_desc g{3, static_cast<int>(num("nx", 0)), 0, 0, 0.0};
-    g.ny = static_cast<int>(num("ny", g.nx));
-    g.nz = static_cast<int>(num("nz", g.nx));
-    g.h = num("h", 1.0 / g.nx);
+    if (c.str.count("domain")) {
+        if (!read_domain(c.str["domain"], g, labels, err)) { std::fprintf(stderr, "config error: %s\n", err.c_str()); return 1; }
+    } else {
+        if (!c.num.count("nx")) { std::fprintf(stderr, "config error: nx (or domain) is required\n"); return 1; }
+        g.ny = static_cast<int>(num("ny", g.nx));
+        g.nz = static_cast<int>(num("nz", g.nx));
+        g.h = num("h", 1.0 / g.nx);
+    }
     const int bw = static_cast<int>(num("band_width", 1));
+    if (cmd == "census" && !labels.empty()) {
+        int64_t out[6];
+        if (smg_census_labeled(&g, labels.data(), bw, out) < 0) { std::fprintf(stderr, "config error: bad grid\n"); return 1; }
+        std::printf("%lld %lld %.2f%%\n", static_cast<long long>(out[0]), static_cast<long long>(out[1]),
+                    out[0] ? 100.0 * static_cast<double>(out[1]) / static_cast<double>(out[0]) : 0.0);
+        return 0;
+    }
     if (cmd == "census") {
         int64_t out[2];
         if (smg_census(&g, bw, out) < 0) { std::fprintf(stderr, "config error: bad grid\n"); return 1; }
@@ -237,14 +277,25 @@ int main(int argc, char** argv) {
     std::vector<int> devs;
     for (double d : c.arr.count("devices") ? c.arr["devices"] : std::vector<double>{0}) devs.push_back(static_cast<int>(d));
     smg_ctx* ctx = nullptr;
-    if (smg_create(&g, &p, static_cast<int>(devs.size()), devs.data(), &ctx) != SMG_OK) {
+    if (!labels.empty()) {
+        if (fk == "cavity" || num("vtk", 0) != 0 || devs.size() != 1) {
+            std::fprintf(stderr, "config error: a domain file takes forcing uniform|fourier|channel, one device, no vtk\n");
+            return 1;
+        }
+        p.dgs_tile_min = -1;
+        if (smg_create_labeled(&g, labels.data(), &p, devs[0], &ctx) != SMG_OK) {
+            std::fprintf(stderr, "config error: smg_create_labeled failed\n");
+            return 1;
+        }
+    } else if (smg_create(&g, &p, static_cast<int>(devs.size()), devs.data(), &ctx) != SMG_OK) {
         std::fprintf(stderr, "config error: smg_create failed\n");
         return 1;
     }
     int64_t cnt[5];
     const int64_t n = smg_level_ndof(ctx, 0, cnt);
     std::vector<double> b(n), x(n), hist(maxit), secs(maxit), lx(n);
-    if (fk == "cavity") smg_assemble_rhs(&g, p.eta, 0, num("lid", 1.0), b.data());  // zero force, lid u
+    if (!labels.empty()) smg_forcing_labeled(&g, labels.data(), kind, static_cast<uint64_t>(num("seed", 0)), b.data());
+    else if (fk == "cavity") smg_assemble_rhs(&g, p.eta, 0, num("lid", 1.0), b.data());  // zero force, lid u
     else smg_forcing(&g, kind, static_cast<uint64_t>(num("seed", 0)), b.data(), 8);
     smg_history h{maxit, 0, hist.data(), secs.data()};
     int status = -1;

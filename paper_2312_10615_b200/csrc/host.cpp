@@ -18,6 +18,7 @@
 #include <string>
 #include <thread>
 #include <type_traits>
+#include <unordered_map>
 #include <vector>
 
 #include <cuda_profiler_api.h>
@@ -266,6 +267,7 @@ struct DevLevel {
     uint32_t* cls = nullptr;
     int32_t* pack_slots = nullptr;
     uint16_t* vk_kidx[8] = {};
+    uint16_t* sw_kidx[4] = {};  // merged complementary pairs (list m = parity m, then parity 7 - m)
     std::shared_ptr<struct HostMap> hm;
 };
 
@@ -664,7 +666,7 @@ void build_level_labeled(smg_ctx* c, int l, std::vector<uint8_t> lab, int& max_v
     std::vector<int32_t> cells[8];
     std::vector<uint8_t> masks[8];
     std::vector<uint16_t> kidx[8];
-    std::vector<int> keys;  // class index -> signature key
+    std::unordered_map<int, int> keys;  // signature key -> class index
     std::vector<double> ktab;
     for (int z = 0; z < nz; ++z)
         for (int y = 0; y < ny; ++y)
@@ -680,13 +682,12 @@ void build_level_labeled(smg_ctx* c, int l, std::vector<uint8_t> lab, int& max_v
                     key |= dr[s2] << (6 + 3 * s2);
                 }
                 key |= mask;
-                int ki = -1;
-                for (size_t k = 0; k < keys.size(); ++k)
-                    if (keys[k] == key) ki = static_cast<int>(k);
+                const auto hit = keys.find(key);
+                int ki = hit == keys.end() ? -1 : hit->second;
                 if (ki < 0) {  // new class: invert C_i L~ C_i^T over the active slots, scatter to the 7-slot layout
                     if (keys.size() >= 65535) throw SmgError(SMG_ECAP, "more than 65535 Vanka signature classes");
                     ki = static_cast<int>(keys.size());
-                    keys.push_back(key);
+                    keys.emplace(key, ki);
                     int slot[7], nb = 0;
                     for (int s2 = 0; s2 < 6; ++s2)
                         if (mask & (1 << s2)) slot[nb++] = s2;
@@ -728,6 +729,27 @@ void build_level_labeled(smg_ctx* c, int l, std::vector<uint8_t> lab, int& max_v
         CK(cudaMemcpyAsync(L.vk_cells[col], cells[col].data(), n * sizeof(int32_t), cudaMemcpyHostToDevice, c->st));
         CK(cudaMemcpyAsync(L.vk_mask[col], masks[col].data(), n, cudaMemcpyHostToDevice, c->st));
         CK(cudaMemcpyAsync(L.vk_kidx[col], kidx[col].data(), n * sizeof(uint16_t), cudaMemcpyHostToDevice, c->st));
+        CK(cudaStreamSynchronize(c->st));
+    }
+    // sweep lists: complementary parities (m, 7 - m) never touch each other's DOFs on any labelling
+    // (a residual stencil reaches along one axis), so each pair is one Jacobi phase (8 per sweep)
+    for (int pq = 0; pq < 4; ++pq) {
+        std::vector<int32_t> mc(cells[pq]);
+        mc.insert(mc.end(), cells[7 - pq].begin(), cells[7 - pq].end());
+        std::vector<uint8_t> mm(masks[pq]);
+        mm.insert(mm.end(), masks[7 - pq].begin(), masks[7 - pq].end());
+        std::vector<uint16_t> mk(kidx[pq]);
+        mk.insert(mk.end(), kidx[7 - pq].begin(), kidx[7 - pq].end());
+        const size_t n = mc.size();
+        L.sw_n[pq] = static_cast<int>(n);
+        L.sw_n[7 - pq] = 0;
+        max_vk = std::max(max_vk, L.sw_n[pq]);
+        L.sw_cells[pq] = c->dalloc<int32_t>(n);
+        L.sw_mask[pq] = c->dalloc<uint8_t>(n);
+        L.sw_kidx[pq] = c->dalloc<uint16_t>(n);
+        CK(cudaMemcpyAsync(L.sw_cells[pq], mc.data(), n * sizeof(int32_t), cudaMemcpyHostToDevice, c->st));
+        CK(cudaMemcpyAsync(L.sw_mask[pq], mm.data(), n, cudaMemcpyHostToDevice, c->st));
+        CK(cudaMemcpyAsync(L.sw_kidx[pq], mk.data(), n * sizeof(uint16_t), cudaMemcpyHostToDevice, c->st));
         CK(cudaStreamSynchronize(c->st));
     }
     L.ktab = c->dalloc<double>(std::max<size_t>(ktab.size(), 49));
@@ -1107,7 +1129,7 @@ void dgs_phase(smg_ctx* c, int l, double* x, const double* b, int ph) {
         launch_dgs_vel(L.k, x, b, ph, c->st);
     } else if (ph >= 2 && ph <= 9) {
         launch_dgs_pdelta(L.k, x, b, L.pd, ph - 2, c->st);
-        launch_dgs_papply(L.k, x, L.pd, c->st);
+        launch_dgs_papply(L.k, x, L.pd, c->st, ph - 2);
     } else if (ph >= 10 && ph <= 17) {
         launch_dgs_cb(L.k, b, c->st);
         launch_dgs_prev(L.k, x, b, 17 - ph, c->st);
@@ -1130,7 +1152,7 @@ void symmetric_dgs(smg_ctx* c, int l, double* x, const double* b, bool cb_ready 
                 launch_dgs_vel(L.k, x, b, ph <= 1 ? ph : 19 - ph, c->st);
             } else if (ph <= 9) {
                 launch_dgs_pdelta(L.k, x, b, L.pd, ph - 2, c->st);
-                launch_dgs_papply(L.k, x, L.pd, c->st);
+                launch_dgs_papply(L.k, x, L.pd, c->st, ph - 2);
             } else {
                 launch_dgs_prev(L.k, x, b, 17 - ph, c->st);
             }
@@ -1146,8 +1168,14 @@ void symmetric_dgs(smg_ctx* c, int l, double* x, const double* b, bool cb_ready 
 
 void vanka_sym_coop(smg_ctx* c, int l, double* x, const double* b) {
     DevLevel& L = c->lv[l];
-    if (L.k.cls) {  // labelled level: per-colour delta / apply launches with the class table
-        for (int k = 0; k < c->prm.nu; ++k) vanka_sym(c, l, x, b);
+    if (L.k.cls) {  // labelled level: merged colour pairs 0..3, then 3..0, a delta / apply launch each
+        for (int k = 0; k < c->prm.nu; ++k)
+            for (int ph = 0; ph < 8; ++ph) {
+                const int pq = ph < 4 ? ph : 7 - ph;
+                launch_vanka_delta(L.k, x, b, L.sw_cells[pq], L.sw_mask[pq], L.sw_n[pq], L.ktab, c->vk_delta, c->st,
+                                   L.sw_kidx[pq]);
+                launch_vanka_apply(L.k, x, L.sw_cells[pq], L.sw_mask[pq], L.sw_n[pq], c->vk_delta, c->st);
+            }
         return;
     }
     launch_vanka_sym_coop(L.k, x, b, L.sw_cells, L.sw_mask, L.sw_n, L.ktab, c->vk_delta, c->prm.nu, c->st, L.xb,
@@ -2427,6 +2455,60 @@ int smg_forcing(const smg_grid_desc* grid, int kind, uint64_t seed, double* b, i
     });
     // pressure rows: b_p = 0 (zero divergence RHS)
     for (int64_t k = 0; k < np; ++k) b[nu + nv + nw + k] = 0.0;
+    return 0;
+}
+
+int smg_assemble_rhs_labeled(const smg_grid_desc* grid, const uint8_t* labels, double eta, const double* gu,
+                             const double* gv, const double* gw, double* b) {
+    // assemble_rhs with general BoundaryData: every stencil leg of an active row into
+    // a Dirichlet face moves to the right-hand side with the opposite sign of its matrix entry
+    // (momentum: -eta/h^2 legs -> + eta/h^2 g; continuity: +1/h on the low face, -1/h on the high).
+    if (!grid || !labels || !gu || !gv || !gw || !b || grid->dim != 3 || !(grid->h > 0)) return SMG_EINVAL;
+    const size_t nc = static_cast<size_t>(grid->nx) * grid->ny * grid->nz;
+    const auto mp = classify_labeled(std::vector<uint8_t>(labels, labels + nc), grid->nx, grid->ny, grid->nz, 1);
+    const HostMap& m = *mp;
+    const double e2 = eta / (grid->h * grid->h), ih = 1.0 / grid->h;
+    const double* g[3] = {gu, gv, gw};
+    const int n[3] = {m.nx, m.ny, m.nz};
+    auto value = [&](int c, int x, int y, int z) {
+        const int p[3] = {x, y, z};
+        int e[3], q[3];
+        for (int a = 0; a < 3; ++a) {
+            e[a] = n[a] + (a == c ? 1 : 2);
+            q[a] = p[a] + (a == c ? 0 : 1);
+            if (q[a] < 0 || q[a] >= e[a]) return 0.0;
+        }
+        return g[c][(static_cast<size_t>(q[2]) * e[1] + q[1]) * e[0] + q[0]];
+    };
+    // status of a face anywhere (ring faces included): Dirichlet iff one of its two cells is
+    auto dirichlet = [&](int c, int x, int y, int z) {
+        return m.at(x - (c == 0), y - (c == 1), z - (c == 2)) == LAB_D || m.at(x, y, z) == LAB_D;
+    };
+    const int d[6][3] = {{-1, 0, 0}, {1, 0, 0}, {0, -1, 0}, {0, 1, 0}, {0, 0, -1}, {0, 0, 1}};
+    for (int z = 0; z < m.nz; ++z)
+        for (int y = 0; y < m.ny; ++y)
+            for (int x = 0; x < m.nx; ++x) {
+                const size_t q = m.ci(x, y, z);
+                for (int c = 0; c < 3; ++c) {
+                    const int32_t id = m.id[c][q];
+                    if (id < 0) continue;
+                    for (auto& k : d) {
+                        const int fx = x + k[0], fy = y + k[1], fz = z + k[2];
+                        if (!dirichlet(c, fx, fy, fz)) continue;
+                        const double gval = value(c, fx, fy, fz);
+                        if (gval != 0.0) b[id] = b[id] + e2 * gval;
+                    }
+                }
+                const int32_t pid = m.id[3][q];
+                if (pid < 0) continue;
+                for (int c = 0; c < 3; ++c)
+                    for (int side = 0; side < 2; ++side) {
+                        const int fx = x + (c == 0) * side, fy = y + (c == 1) * side, fz = z + (c == 2) * side;
+                        if (!dirichlet(c, fx, fy, fz)) continue;
+                        const double gval = value(c, fx, fy, fz);
+                        if (gval != 0.0) b[pid] = b[pid] - (side ? -ih : ih) * gval;
+                    }
+            }
     return 0;
 }
 

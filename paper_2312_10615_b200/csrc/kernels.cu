@@ -758,7 +758,7 @@ __global__ void __launch_bounds__(256) k_apply_q(LevelK L, const double* __restr
 // residual r = b - L x as block partials of ||r||^2 (r itself is never stored).  Ghost planes
 // as in k_apply_q.
 template <bool M>
-__global__ void __launch_bounds__(256, 4) k_apply_x(LevelK L, const double* __restrict__ X0,
+__global__ void __launch_bounds__(256, M ? 3 : 4) k_apply_x(LevelK L, const double* __restrict__ X0,
                                                  const double* __restrict__ D0, const double* __restrict__ Q,
                                                  const double* __restrict__ B, double* __restrict__ X1,
                                                  double* __restrict__ D1, const double* __restrict__ sc,
@@ -2459,37 +2459,79 @@ __global__ void k_dgs_vel_m(LevelK L, double* __restrict__ X, const double* __re
     }
 }
 
+// Forward pressure phase of parity colour `colour`, part 1: delta at the colour's cells only (0 on
+// its band cells); D at cells of other colours is never read as this phase's delta (part 2 knows
+// every neighbour's colour from its coordinates), so nothing else is written.
 __global__ void k_dgs_pdelta_m(LevelK L, const double* __restrict__ X, const double* __restrict__ B,
                                double* __restrict__ D, int colour) {
     Cell c;
     if (!thread_cell(L.g, c)) return;
+    if (pcolour(L.g, c) != colour) return;
     const int64_t fs = L.g.fs, i = c.i;
     const uint32_t m = L.cls[i];
     double d = 0.0;
-    if (pcolour(L.g, c) == colour && (m & (CLS_P | CLS_BAND)) == CLS_P) {
+    if ((m & (CLS_P | CLS_BAND)) == CLS_P) {
         const double r = B[3 * fs + i] - cont(L, X, X + fs, X + 2 * fs, X + 3 * fs, i, L.gamma);
         d = r / L.dp;
     }
     D[i] = d;
 }
 
-__global__ void k_dgs_papply_m(LevelK L, double* __restrict__ X, const double* __restrict__ D) {
+// Part 2: x += sum_C delta_C M_.C in gather form.  Only cells of the colour itself (self term,
+// their low faces) or of a colour one parity bit away (the neighbours of a colour cell along that
+// axis: one low face and the pressure) are touched -- exactly the DOFs the oracle updates; a
+// neighbour of any other colour contributes the literal 0.0 of the reference sum.
+__global__ void k_dgs_papply_m(LevelK L, double* __restrict__ X, const double* __restrict__ D, int colour) {
     Cell c;
     if (!thread_cell(L.g, c)) return;
     const Geom& g = L.g;
+    const int bit = pcolour(g, c) ^ colour;
+    if (bit != 0 && bit != 1 && bit != 2 && bit != 4) return;
     const int64_t fs = g.fs, i = c.i, sy = g.sy, sz = g.sz;
     const uint32_t m = L.cls[i];
-    const double dc = D[i];
-    if (m & CLS_U) X[i] = X[i] + (D[i - 1] - dc) * L.inv_h;
-    if (m & CLS_V) X[fs + i] = X[fs + i] + (D[i - sy] - dc) * L.inv_h;
-    if (m & CLS_W) X[2 * fs + i] = X[2 * fs + i] + (D[i - sz] - dc) * L.inv_h;
+    if (bit == 0) {  // a cell of the colour: its three low faces see (0 - delta), its pressure 6 delta
+        const double dc = D[i];
+        if (m & CLS_U) X[i] = X[i] + (0.0 - dc) * L.inv_h;
+        if (m & CLS_V) X[fs + i] = X[fs + i] + (0.0 - dc) * L.inv_h;
+        if (m & CLS_W) X[2 * fs + i] = X[2 * fs + i] + (0.0 - dc) * L.inv_h;
+        if (m & CLS_P) {
+            double s = 0.0 + 0.0;
+            s = s + 0.0;
+            s = s + 0.0;
+            s = s + 0.0;
+            s = s + 0.0;
+            X[3 * fs + i] = X[3 * fs + i] + L.eta_h2 * (6.0 * dc - s);
+        }
+        return;
+    }
+    // the two neighbours along the differing axis carry the colour
+    const int64_t st = bit == 1 ? 1 : (bit == 2 ? sy : sz);
+    const double dm = D[i - st], dp = D[i + st];
+    const uint32_t fbit = bit == 1 ? CLS_U : (bit == 2 ? CLS_V : CLS_W);
+    const int64_t fo = bit == 1 ? 0 : (bit == 2 ? fs : 2 * fs);
+    if (m & fbit) X[fo + i] = X[fo + i] + (dm - 0.0) * L.inv_h;  // the low face along that axis
     if (m & CLS_P) {
-        double s = D[i - 1] + D[i + 1];
-        s = s + D[i - sy];
-        s = s + D[i + sy];
-        s = s + D[i - sz];
-        s = s + D[i + sz];
-        X[3 * fs + i] = X[3 * fs + i] + L.eta_h2 * (6.0 * dc - s);
+        double s;
+        if (bit == 1) {
+            s = dm + dp;
+            s = s + 0.0;
+            s = s + 0.0;
+            s = s + 0.0;
+            s = s + 0.0;
+        } else if (bit == 2) {
+            s = 0.0 + 0.0;
+            s = s + dm;
+            s = s + dp;
+            s = s + 0.0;
+            s = s + 0.0;
+        } else {
+            s = 0.0 + 0.0;
+            s = s + 0.0;
+            s = s + 0.0;
+            s = s + dm;
+            s = s + dp;
+        }
+        X[3 * fs + i] = X[3 * fs + i] + L.eta_h2 * (6.0 * 0.0 - s);
     }
 }
 
@@ -2500,8 +2542,9 @@ __global__ void k_dgs_prev_m(LevelK L, double* __restrict__ X, int colour) {
     if (!thread_cell(L.g, c)) return;
     const Geom& g = L.g;
     const int64_t fs = g.fs, sy = g.sy, sz = g.sz, i = c.i;
+    if (pcolour(g, c) != colour) return;
     const uint32_t m0 = L.cls[i];
-    if (pcolour(g, c) != colour || (m0 & (CLS_P | CLS_BAND)) != CLS_P) return;
+    if ((m0 & (CLS_P | CLS_BAND)) != CLS_P) return;
     const uint32_t mx = L.cls[i + 1], my = L.cls[i + sy], mz = L.cls[i + sz];
     const double *U = X, *V = X + fs, *W = X + 2 * fs, *P = X + 3 * fs;
     const double luL = mom_d(L, U, P, i, 1, cls_diag(m0, 0));
@@ -2652,8 +2695,8 @@ void launch_dgs_pdelta(const LevelK& L, const double* x, const double* b, double
     else k_dgs_pdelta<<<cell_grid(L.g), dim3(BX, BY), 0, s>>>(L, x, b, delta, colour);
     count();
 }
-void launch_dgs_papply(const LevelK& L, double* x, const double* delta, cudaStream_t s) {
-    if (L.cls) k_dgs_papply_m<<<cell_grid(L.g), dim3(BX, BY), 0, s>>>(L, x, delta);
+void launch_dgs_papply(const LevelK& L, double* x, const double* delta, cudaStream_t s, int colour) {
+    if (L.cls) k_dgs_papply_m<<<cell_grid(L.g), dim3(BX, BY), 0, s>>>(L, x, delta, colour);
     else k_dgs_papply<<<cell_grid(L.g), dim3(BX, BY), 0, s>>>(L, x, delta);
     count();
 }

@@ -89,7 +89,8 @@ void launch_apply(const LevelK& L, const double* x, const double* b, double* y, 
 void launch_dgs_vel(const LevelK& L, double* x, const double* b, int colour, cudaStream_t s);
 void launch_dgs_pdelta(const LevelK& L, const double* x, const double* b, double* delta, int colour,
                        cudaStream_t s);
-void launch_dgs_papply(const LevelK& L, double* x, const double* delta, cudaStream_t s);
+// colour: the parity colour whose deltas `delta` holds (labelled levels touch only its neighbourhood)
+void launch_dgs_papply(const LevelK& L, double* x, const double* delta, cudaStream_t s, int colour = -1);
 void launch_dgs_prev(const LevelK& L, double* x, const double* b, int colour, cudaStream_t s);
 // L.cb[C] = m_C^T b for every cell (reverse pressure phases need it; call when b changes).
 void launch_dgs_cb(const LevelK& L, const double* b, cudaStream_t s);

@@ -93,3 +93,47 @@ def inflow_profile(y, H, ubar, z=None):
     if np.any(z < 0) or np.any(z > H):
         raise ValueError("coordinate outside [0, H]")
     return 16.0 * ubar * y * z * (H - y) * (H - z) / H ** 4
+
+
+def channel_inflow(labels, H, ubar, through=True):
+    """Dirichlet data of the 3-D channel inflow (PAPER section 6.2.2): u = 16 ubar y z (H - y)(H - z) / H^4
+    on the u faces of the inflow plane x = 0 (y, z at the face centres, channel height and depth H
+    over ny and nz cells), 0 on every other Dirichlet face.  through: the same profile is prescribed
+    on the plane x = nx (use a grid without an Exterior outflow column).  Under the SPEC's Neumann
+    rule an Interior|Exterior face is Inactive and carries no normal flux, so an
+    inflow-only data set violates RHS compatibility; prescribing the outflow keeps the
+    net boundary flux zero.  Returns (g_u, g_v, g_w) for `assemble_rhs_labels` /
+    `smg_assemble_rhs_labeled`."""
+    nz, ny, nx = np.asarray(labels).shape
+    gu = np.zeros((nz + 2, ny + 2, nx + 1))
+    y = (np.arange(ny) + 0.5) * H / ny
+    z = (np.arange(nz) + 0.5) * H / nz
+    gu[1:-1, 1:-1, 0] = inflow_profile(y[None, :], H, ubar, z=z[:, None])
+    if through:
+        gu[:, :, -1] = gu[:, :, 0]
+    return gu, np.zeros((nz + 2, ny + 1, nx + 2)), np.zeros((nz + 1, ny + 2, nx + 2))
+
+
+def write_domain_file(path, labels, h):
+    """Domain file of SPEC:88: header `3 nx ny nz h`, then one character per cell (D / I / E),
+    row-major with x fastest, one x row per line.  `solver run|census` reads it ("domain" key)."""
+    lab = np.ascontiguousarray(labels, np.uint8)
+    nz, ny, nx = lab.shape
+    chars = np.array([b"D", b"I", b"E"])[lab]
+    with open(path, "wb") as f:
+        f.write(f"3 {nx} {ny} {nz} {h!r}\n".encode())
+        for z in range(nz):
+            for y in range(ny):
+                f.write(b"".join(chars[z, y]) + b"\n")
+
+
+def read_domain_file(path):
+    """Inverse of write_domain_file: (labels shaped (nz, ny, nx), h)."""
+    with open(path) as f:
+        dim, nx, ny, nz, h = f.readline().split()
+        if int(dim) != 3:
+            raise ValueError("3-D domain files only")
+        body = "".join(f.read().split())
+    lut = {"D": D, "I": I, "E": E}
+    lab = np.array([lut[c] for c in body], np.uint8).reshape(int(nz), int(ny), int(nx))
+    return lab, float(h)

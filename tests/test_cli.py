@@ -93,3 +93,44 @@ def test_verify_symmetry():
 
 def test_verify_usage():
     assert subprocess.run([CLI, "verify", "--max-n"], capture_output=True).returncode == 1
+
+
+def _domain(tmp_path):
+    from paper_2312_10615_b200 import scenarios
+    lab = scenarios.cylinder3d(32, 16, 8)
+    path = str(tmp_path / "cyl.dom")
+    scenarios.write_domain_file(path, lab, 1 / 16)
+    back, h = scenarios.read_domain_file(path)
+    assert np.array_equal(back, lab) and h == 1 / 16
+    return lab, path
+
+
+def test_census_of_a_domain_file(tmp_path):
+    """Domain file format of SPEC:88 (header `dim nx ny nz h`, one D / I / E character per cell)."""
+    lab, path = _domain(tmp_path)
+    r = run(["census"], {"domain": path, "band_width": 1}, str(tmp_path))
+    c = smg.census_labels(lab)
+    assert r.returncode == 0, r.stderr
+    assert r.stdout.split()[:2] == [str(c["N"]), str(c["V1"])]
+    open(path, "a").write("I")  # one label too many
+    assert run(["census"], {"domain": path}, str(tmp_path)).returncode == 1
+    open(path, "w").write("3 4 4 4 0.25\n" + "IIXI" * 16)
+    assert run(["census"], {"domain": path}, str(tmp_path)).returncode == 1
+    assert run(["census"], {"domain": str(tmp_path / "missing.dom")}, str(tmp_path)).returncode == 1
+
+
+@pytest.mark.gpu
+def test_run_on_a_domain_file(tmp_path):
+    lab, path = _domain(tmp_path)
+    cfg = {"domain": path, "levels": 3, "eta": 1.0, "tol": 1e-8, "seed": 4, "forcing": "channel",
+           "output_dir": str(tmp_path)}
+    r = run(["run"], cfg, str(tmp_path))
+    assert r.returncode == 0, r.stderr
+    rows = open(tmp_path / "history_mg-sqmr.csv").read().splitlines()
+    h = np.array([float(x.split(",")[1]) for x in rows[1:]])
+    s = smg.Solver.from_labels(lab, h=1 / 16, levels=3)
+    _, hp, _, st = s.sqmr(smg.forcing_labels(lab, 1 / 16, smg.FORCE_CHANNEL, 4), 1e-8, 200)
+    s.close()
+    assert st == smg.SMG_CONVERGED and np.array_equal(h, hp)
+    summ = dict(l.split(": ") for l in open(tmp_path / "summary.txt").read().splitlines())
+    assert summ["status"] == "converged" and int(summ["dof"]) == smg.census_labels(lab)["N"]

@@ -133,3 +133,28 @@ def test_inflow_profile():
     assert scenarios.inflow_profile(H / 2, H, 0.45, z=H / 2) == pytest.approx(0.45)
     with pytest.raises(ValueError):
         scenarios.inflow_profile(0.5, H, 0.3)
+
+
+def test_assemble_rhs_with_general_dirichlet_data():
+    """assemble_rhs on a labelled grid: the library's host routine against the oracle
+    bit for bit, the cavity lid as a special case, and RHS compatibility."""
+    lab = scenarios.cylinder3d(32, 16, 8)
+    h = 0.41 / 16
+    o = oracle.Oracle(0, levels=2, labels=lab, h=h, eta=1e-3)
+    rng = np.random.default_rng(0)
+    g = [rng.uniform(-1, 1, s) for s in smg.dirichlet_shapes(lab)]
+    assert np.array_equal(smg.assemble_rhs_labels(lab, h, *g, eta=1e-3), o.dirichlet_rhs(*g))
+    b0 = rng.uniform(-1, 1, o.ndof(0))
+    assert np.array_equal(smg.assemble_rhs_labels(lab, h, *g, eta=1e-3, b=b0), o.dirichlet_rhs(*g, b=b0))
+    n = 8
+    box = scenarios.cavity3d(n)
+    gu, gv, gw = [np.zeros(s) for s in smg.dirichlet_shapes(box)]
+    gu[:, n + 1, :] = 1.0  # the u faces of the ring cells above the top (y = ny): the moving lid
+    assert np.array_equal(smg.assemble_rhs_labels(box, 1 / n, gu, gv, gw), smg.cavity_rhs(n))
+    # through-flow channel: inflow profile in, the same profile out -> continuity RHS sums to zero
+    ch = scenarios.cylinder3d(32, 16, 16, outflow=0)
+    b = smg.assemble_rhs_labels(ch, h, *scenarios.channel_inflow(ch, 0.41, 0.45), eta=1e-3)
+    npres = int((ch == 1).sum())
+    assert abs(b[-npres:].sum()) <= 1e-12 * np.abs(b[-npres:]).sum()
+    with pytest.raises(ValueError):
+        smg.assemble_rhs_labels(ch, h, gu, gv, gw)  # wrong shapes
