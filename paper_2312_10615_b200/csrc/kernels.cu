@@ -2435,11 +2435,15 @@ __global__ void k_apply_m(LevelK L, const double* __restrict__ X, const double* 
 }
 
 // DGS velocity phase on the V2 faces of one red-black colour (their stencils are full: diagonal 6).
+// Threads only on the colour's cells: x = 2 i + ((y + z + colour) & 1).
 __global__ void k_dgs_vel_m(LevelK L, double* __restrict__ X, const double* __restrict__ B, int colour) {
-    Cell c;
-    if (!thread_cell(L.g, c)) return;
     const Geom& g = L.g;
-    if (((c.x + c.y + g.gz(c.z)) & 1) != colour) return;
+    Cell c;
+    c.y = blockIdx.y * BY + threadIdx.y;
+    c.z = blockIdx.z;
+    c.x = 2 * (blockIdx.x * BX + threadIdx.x) + ((c.y + g.gz(c.z) + colour) & 1);
+    if (c.x >= g.nx || c.y >= g.ny) return;
+    c.i = g.slot(c.x, c.y, c.z);
     const int64_t fs = g.fs, i = c.i;
     const uint32_t m = L.cls[i];
     if (!(m & (CLS_U2 | CLS_V2 | CLS_W2))) return;
@@ -2459,14 +2463,27 @@ __global__ void k_dgs_vel_m(LevelK L, double* __restrict__ X, const double* __re
     }
 }
 
+// Threads only on the cells of one parity colour (labelled levels are single parts: local = global planes).
+__device__ __forceinline__ bool colour_cell(const Geom& g, int colour, Cell& c) {
+    c.x = 2 * (blockIdx.x * BX + threadIdx.x) + (colour & 1);
+    c.y = 2 * (blockIdx.y * BY + threadIdx.y) + ((colour >> 1) & 1);
+    c.z = 2 * blockIdx.z + (colour >> 2);
+    if (c.x >= g.nx || c.y >= g.ny || c.z >= g.nz) return false;
+    c.i = g.slot(c.x, c.y, c.z);
+    return true;
+}
+inline dim3 colour_grid(const Geom& g) {
+    return dim3(((g.nx + 1) / 2 + BX - 1) / BX, ((g.ny + 1) / 2 + BY - 1) / BY, (g.nz + 1) / 2);
+}
+inline dim3 redblack_grid(const Geom& g) { return dim3(((g.nx + 1) / 2 + BX - 1) / BX, (g.ny + BY - 1) / BY, g.nz); }
+
 // Forward pressure phase of parity colour `colour`, part 1: delta at the colour's cells only (0 on
 // its band cells); D at cells of other colours is never read as this phase's delta (part 2 knows
 // every neighbour's colour from its coordinates), so nothing else is written.
 __global__ void k_dgs_pdelta_m(LevelK L, const double* __restrict__ X, const double* __restrict__ B,
                                double* __restrict__ D, int colour) {
     Cell c;
-    if (!thread_cell(L.g, c)) return;
-    if (pcolour(L.g, c) != colour) return;
+    if (!colour_cell(L.g, colour, c)) return;
     const int64_t fs = L.g.fs, i = c.i;
     const uint32_t m = L.cls[i];
     double d = 0.0;
@@ -2539,10 +2556,9 @@ __global__ void k_dgs_papply_m(LevelK L, double* __restrict__ X, const double* _
 // V2 cell may be a V1 face with a dropped leg one cell further out).
 __global__ void k_dgs_prev_m(LevelK L, double* __restrict__ X, int colour) {
     Cell c;
-    if (!thread_cell(L.g, c)) return;
+    if (!colour_cell(L.g, colour, c)) return;
     const Geom& g = L.g;
     const int64_t fs = g.fs, sy = g.sy, sz = g.sz, i = c.i;
-    if (pcolour(g, c) != colour) return;
     const uint32_t m0 = L.cls[i];
     if ((m0 & (CLS_P | CLS_BAND)) != CLS_P) return;
     const uint32_t mx = L.cls[i + 1], my = L.cls[i + sy], mz = L.cls[i + sz];
@@ -2593,6 +2609,70 @@ __global__ void k_vanka_delta_m(LevelK L, const double* __restrict__ X, const do
         for (int q = 0; q < 7; ++q) acc = acc + K[s * 7 + q] * r[q];
         delta[static_cast<int64_t>(t) * 8 + s] = acc;
     }
+}
+
+// Lane-parallel form of k_vanka_delta_m / k_vanka_apply: 8 lanes per block, lane s < 7 computes
+// residual slot s (vanka_slot_residual's gather with the face's own diagonal) and the correction of
+// DOF s, delta_s = sum_q K[s][q] r_q with r_q gathered by warp shuffles in ascending q.
+// M: labelled level (face diagonals from L.cls, class index from kidx); else the box (diagonal 6,
+// the class is the face mask).
+template <bool M>
+__global__ void __launch_bounds__(256) k_vanka_delta8(LevelK L, const double* __restrict__ X,
+                                                        const double* __restrict__ B,
+                                                        const int32_t* __restrict__ cells,
+                                                        const uint8_t* __restrict__ masks,
+                                                        const uint16_t* __restrict__ kidx, int n,
+                                                        const double* __restrict__ ktab, double* __restrict__ delta) {
+    pdl_wait();
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x, lane = threadIdx.x & 31, s8 = lane & 7;
+    const int t = tid >> 3;
+    const bool act = t < n;
+    const Geom& g = L.g;
+    const int64_t fs = g.fs, sy = g.sy, sz = g.sz;
+    double r = 0.0;
+    int ki = 0;
+    if (act && s8 < 7) {
+        const int64_t i = cells[t];
+        const int m = masks[t];
+        ki = M ? kidx[t] : m;
+        const bool mom_row = s8 < 6;
+        if (!mom_row || ((m >> s8) & 1)) {
+            const int d = s8 >> 1;
+            const int64_t st = d == 0 ? 1 : (d == 1 ? sy : sz);
+            const int64_t jj = i + ((s8 & 1) ? st : 0);  // face slot (cell slot for the pressure row)
+            const double *U = X, *V = X + fs, *W = X + 2 * fs, *P = X + 3 * fs;
+            if (mom_row) {
+                const double diag = M ? cls_diag(L.cls[jj], d) : 6.0;
+                const double* F = X + d * fs;
+                r = B[d * fs + jj] - mom_d(L, F, P, jj, st, diag);
+            } else {
+                r = B[3 * fs + i] - cont(L, U, V, W, P, i, L.gamma);
+            }
+        }
+    }
+    const double* K = ktab + static_cast<int64_t>(ki) * 49 + (s8 < 7 ? s8 : 0) * 7;
+    double acc = 0.0;
+#pragma unroll
+    for (int q = 0; q < 7; ++q) {
+        const double rq = __shfl_sync(0xffffffffu, r, (lane & ~7) + q);
+        acc = acc + K[q] * rq;
+    }
+    if (act && s8 < 7) delta[static_cast<int64_t>(t) * 8 + s8] = acc;
+}
+__global__ void __launch_bounds__(256) k_vanka_apply8(LevelK L, double* __restrict__ X,
+                                                      const int32_t* __restrict__ cells,
+                                                      const uint8_t* __restrict__ masks, int n,
+                                                      const double* __restrict__ delta) {
+    pdl_wait();
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x, s8 = tid & 7, t = tid >> 3;
+    if (t >= n || s8 == 7) return;
+    const Geom& g = L.g;
+    const int64_t fs = g.fs, i = cells[t];
+    const int m = masks[t];
+    if (s8 < 6 && !((m >> s8) & 1)) return;
+    const int64_t offs = s8 == 0 ? 0 : s8 == 1 ? 1 : s8 == 2 ? fs : s8 == 3 ? fs + g.sy : s8 == 4 ? 2 * fs
+                         : s8 == 5 ? 2 * fs + g.sz : 3 * fs;
+    X[i + offs] = X[i + offs] + delta[static_cast<int64_t>(t) * 8 + s8];
 }
 
 // Restriction / prolongation with the coarse / fine DofMap bits deciding which DOFs exist; legs
@@ -2664,6 +2744,18 @@ static int env_int(const char* name, int dflt);
 static int num_sms();
 // Launch with the programmatic-stream-serialization attribute (SMG_PDL=0 disables):
 // the kernel's launch and block scheduling overlap the previous kernel's tail.
+// use_pdl = false: an ordinary launch (the kernel's griddepcontrol.wait is then a no-op).
+template <typename... KArgs, typename... Args>
+static void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args);
+template <typename... KArgs, typename... Args>
+static void launch_plain(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    note(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...));
+}
 template <typename... KArgs, typename... Args>
 static void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
     static const int pdl = env_int("SMG_PDL", 1);
@@ -2685,13 +2777,13 @@ void launch_apply(const LevelK& L, const double* x, const double* b, double* y, 
     count();
 }
 void launch_dgs_vel(const LevelK& L, double* x, const double* b, int colour, cudaStream_t s) {
-    if (L.cls) k_dgs_vel_m<<<cell_grid(L.g), dim3(BX, BY), 0, s>>>(L, x, b, colour);
+    if (L.cls) k_dgs_vel_m<<<redblack_grid(L.g), dim3(BX, BY), 0, s>>>(L, x, b, colour);
     else k_dgs_vel<<<cell_grid(L.g), dim3(BX, BY), 0, s>>>(L, x, b, colour);
     count();
 }
 void launch_dgs_pdelta(const LevelK& L, const double* x, const double* b, double* delta, int colour,
                        cudaStream_t s) {
-    if (L.cls) k_dgs_pdelta_m<<<cell_grid(L.g), dim3(BX, BY), 0, s>>>(L, x, b, delta, colour);
+    if (L.cls) k_dgs_pdelta_m<<<colour_grid(L.g), dim3(BX, BY), 0, s>>>(L, x, b, delta, colour);
     else k_dgs_pdelta<<<cell_grid(L.g), dim3(BX, BY), 0, s>>>(L, x, b, delta, colour);
     count();
 }
@@ -2705,7 +2797,7 @@ void launch_dgs_cb(const LevelK& L, const double* b, cudaStream_t s) {
     count();
 }
 void launch_dgs_prev(const LevelK& L, double* x, const double* b, int colour, cudaStream_t s) {
-    if (L.cls) k_dgs_prev_m<<<cell_grid(L.g), dim3(BX, BY), 0, s>>>(L, x, colour);
+    if (L.cls) k_dgs_prev_m<<<colour_grid(L.g), dim3(BX, BY), 0, s>>>(L, x, colour);
     else k_dgs_prev<<<cell_grid(L.g), dim3(BX, BY), 0, s>>>(L, x, b, colour);
     count();
 }
@@ -2713,14 +2805,30 @@ void launch_vanka_delta(const LevelK& L, const double* x, const double* b, const
                         const uint8_t* masks, int ncells, const double* ktab, double* delta, cudaStream_t s,
                         const uint16_t* kidx) {
     if (ncells <= 0) return;
-    if (L.cls) k_vanka_delta_m<<<(ncells + 127) / 128, 128, 0, s>>>(L, x, b, cells, masks, kidx, ncells, ktab, delta);
+    if (L.cls) {
+        // SMG_VANKA_M1=1: the one-thread-per-block form (tests: both forms are bit-identical)
+        static const int one = env_int("SMG_VANKA_M1", 0);
+        if (one) k_vanka_delta_m<<<(ncells + 127) / 128, 128, 0, s>>>(L, x, b, cells, masks, kidx, ncells, ktab, delta);
+        else launch_k(k_vanka_delta8<true>, static_cast<int>((8 * static_cast<int64_t>(ncells) + 255) / 256), 256, 0, s, L, x,
+                      b, cells, masks, kidx, ncells, ktab, delta);
+    } else if (env_int("SMG_VANKA_D8", 1)) {  // 8 lanes per block (0: one thread per block; bit-identical)
+        const int blocks = static_cast<int>((8 * static_cast<int64_t>(ncells) + 255) / 256);
+        if (env_int("SMG_VANKA_PDL", 0)) launch_k(k_vanka_delta8<false>, blocks, 256, 0, s, L, x, b, cells, masks, kidx, ncells, ktab, delta);
+        else k_vanka_delta8<false><<<blocks, 256, 0, s>>>(L, x, b, cells, masks, kidx, ncells, ktab, delta);
+    }
     else k_vanka_delta<<<(ncells + 127) / 128, 128, 0, s>>>(L, x, b, cells, masks, ncells, ktab, delta);
     count();
 }
 void launch_vanka_apply(const LevelK& L, double* x, const int32_t* cells, const uint8_t* masks, int ncells,
                         const double* delta, cudaStream_t s, const uint8_t* amask) {
     if (ncells <= 0) return;
-    k_vanka_apply<<<(ncells + 127) / 128, 128, 0, s>>>(L, x, cells, masks, ncells, delta, amask);
+    if (!amask && (L.cls || env_int("SMG_VANKA_D8", 1))) {
+        const int blocks = static_cast<int>((8 * static_cast<int64_t>(ncells) + 255) / 256);
+        if (env_int("SMG_VANKA_PDL", 0)) launch_k(k_vanka_apply8, blocks, 256, 0, s, L, x, cells, masks, ncells, delta);
+        else k_vanka_apply8<<<blocks, 256, 0, s>>>(L, x, cells, masks, ncells, delta);
+    }
+    else
+        k_vanka_apply<<<(ncells + 127) / 128, 128, 0, s>>>(L, x, cells, masks, ncells, delta, amask);
     count();
 }
 void launch_restrict(const LevelK& F, const LevelK& C, const double* rf, double* bc, cudaStream_t s, int zc_lo,
@@ -2978,6 +3086,7 @@ void launch_vanka_sym_coop(const LevelK& L, double* x, const double* b, const in
     };
     if (xb && vk_kernels == 1) { ppk(); return; }
     const bool phases = env_int("SMG_VANKA_PHASES", 0) != 0;  // 1: per-phase delta/apply launches (tests)
+    bool big = false;  // the level's phases fit no persistent ping-pong sweep
     if (!phases && xb && !cl && env_int("SMG_VANKA_PP", 1)) {  // ping-pong (grid mode): one barrier per phase
         const bool rin = env_int("SMG_VANKA_REFRESH_IN", 1) != 0;
         if (!rin) refresh_xb();
@@ -2996,14 +3105,18 @@ void launch_vanka_sym_coop(const LevelK& L, double* x, const double* b, const in
             launch_vanka_pp<4>(cl, (lanes + 3) / 4, pargs, s);
             return;
         }
-        // beyond the persistent ping-pong sweep: one launch per phase (measured faster than the
-        // persistent CPT-8 sweep below at 256^3: 0.339 -> 0.305 ms)
-        if (vk_kernels != 0) {
+        // beyond the persistent ping-pong sweep (256^3 and up): a delta and an apply launch per merged
+        // phase, 8 lanes per block.  Measured on one box (round 2, session 5; cfg 2 / cfg 3 fine
+        // symmetric sweep): persistent CPT-8 sweep 0.339 ms / --, ping-pong launch per phase (ppk,
+        // SMG_VANKA_KERNELS=1) 0.304 / 1.36 ms, delta + apply launches 0.245 / 1.27 ms and no
+        // k_refresh of the ping-pong copy per sweep (smooth 3.14 -> 2.57 / 18.2 -> 16.5 ms)
+        if (vk_kernels == 1) {
             ppk();
             return;
         }
+        big = true;
     }
-    bool done = !phases;
+    bool done = !phases && !big;
     if (!done) {
     } else if (fits(reinterpret_cast<const void*>(k_vanka8<0, 1>), 1)) launch_vanka8<1>(cl, lanes, args, s);
     else if (fits(reinterpret_cast<const void*>(k_vanka8<0, 2>), 2)) launch_vanka8<2>(cl, (lanes + 1) / 2, args, s);
@@ -3174,12 +3287,22 @@ void launch_dgs_tile_phases(const LevelK& L, double* x, const double* b, int T, 
     // SMG_TILE_PF: L2 prefetch distance in CTAs (0 = off, the default: measured 2.19 (off) / 2.16 (148) /
     // 2.30 (296) / 2.40 ms (592) per cfg-2 fine sweep -- the loads are not latency-exposed)
     static const int pf = env_int("SMG_TILE_PF", 0);
-    if (fwd)
+    // Ordinary launches (SMG_TILE_PDL=1 restores programmatic dependent launch): with PDL the next
+    // colour's CTAs take the SM's shared memory slots early and the cfg-2 fine sweep measured
+    // 2.185 ms against 2.04 ms without (round 2, session 5)
+    static const int tile_pdl = env_int("SMG_TILE_PDL", 0);
+    if (fwd && tile_pdl)
         launch_k(k_dgs_tile<true>, dim3(hx * hy * hz), dim3(kTileThreads), TileBox<true>::SMEM, s, mx, mb, mc, L, x, T,
                  ph0, ph1, ntx, nty, pf);
-    else
+    else if (fwd)
+        launch_plain(k_dgs_tile<true>, dim3(hx * hy * hz), dim3(kTileThreads), TileBox<true>::SMEM, s, mx, mb, mc, L, x,
+                     T, ph0, ph1, ntx, nty, pf);
+    else if (tile_pdl)
         launch_k(k_dgs_tile<false>, dim3(hx * hy * hz), dim3(kTileThreads), TileBox<false>::SMEM, s, mx, mb, mc, L, x,
                  T, ph0, ph1, ntx, nty, pf);
+    else
+        launch_plain(k_dgs_tile<false>, dim3(hx * hy * hz), dim3(kTileThreads), TileBox<false>::SMEM, s, mx, mb, mc, L,
+                     x, T, ph0, ph1, ntx, nty, pf);
     count();
 }
 

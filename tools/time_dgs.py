@@ -14,6 +14,9 @@ a = ap.parse_args()
 nx, ny, nz, h, lv, kind, seed, tol, name = bench.CONFIGS[a.config]
 s = smg.Solver(nx, ny, nz, h=h, levels=lv)
 s.set_rhs(smg.forcing(nx, ny, nz, h=h, kind=kind, seed=seed))
-for rep in range(3):
+hist, st = s.solve_resident(tol, 500)
+hist, st = s.solve_resident(tol, 500)
+print(name.split(":")[0], "solve %.2f ms, %d iterations" % (s.timing()["solve_ms"], len(hist)))
+for rep in range(2):
     print(name.split(":")[0], "dgs_sym %.4f  vanka_sym %.4f  smooth %.4f  apply %.4f ms" % (
         s.time_kernel(2, a.reps, 0), s.time_kernel(4, a.reps, 0), s.time_kernel(5, a.reps, 0), s.time_kernel(0, a.reps, 0)))
