@@ -695,7 +695,10 @@ __device__ __forceinline__ double cont_f(const LevelK& L, const VF& v, int64_t i
 // first / last z-block also writes q on the ghost plane -1 / nz (its inputs are valid there),
 // so the next iteration needs no exchange of q.
 // M: general labelled level (activity and momentum diagonals from L.cls instead of coordinates).
-template <bool M>
+// UPD: the vector update is evaluated on the fly (one pass over the vectors); !UPD: the update has
+// been written by k_q_upd / k_xd_upd (a streaming pass at copy bandwidth) and the stencil reads the
+// stored vector -- one load per stencil point instead of two or three (same values, same bits).
+template <bool M, bool UPD>
 __global__ void __launch_bounds__(256) k_apply_q(LevelK L, const double* __restrict__ T,
                                                  const double* __restrict__ Q0, double* __restrict__ Q1,
                                                  double* __restrict__ Tn, const double* __restrict__ sc,
@@ -705,7 +708,7 @@ __global__ void __launch_bounds__(256) k_apply_q(LevelK L, const double* __restr
     const Geom& g = L.g;
     const int64_t fs = g.fs;
     const double beta = sc[S_BETA];
-    auto q = [&](int64_t j) { return T[j] + beta * Q0[j]; };  // the oracle's q[i] = t[i] + beta q[i]
+    auto q = [&](int64_t j) { return UPD ? T[j] + beta * Q0[j] : Q1[j]; };  // the oracle's q[i] = t[i] + beta q[i]
     const int x = blockIdx.x * 32 + threadIdx.x, y = blockIdx.y * 8 + threadIdx.y;
     const int zl = blockIdx.z * kDotZB, zh = min(g.nz, zl + kDotZB);
     double v = 0.0;
@@ -714,8 +717,8 @@ __global__ void __launch_bounds__(256) k_apply_q(LevelK L, const double* __restr
 #pragma unroll
             for (int f = 0; f < 4; ++f) Q1[f * fs + i] = q(f * fs + i);
         };
-        if (halo_lo && blockIdx.z == 0) put_q(g.slot(x, y, -1));
-        if (halo_hi && zh == g.nz) put_q(g.slot(x, y, g.nz));
+        if (UPD && halo_lo && blockIdx.z == 0) put_q(g.slot(x, y, -1));
+        if (UPD && halo_hi && zh == g.nz) put_q(g.slot(x, y, g.nz));
 #pragma unroll 1
         for (int z = zl; z < zh; ++z) {
             const int64_t i = g.slot(x, y, z);
@@ -725,7 +728,7 @@ __global__ void __launch_bounds__(256) k_apply_q(LevelK L, const double* __restr
                 const double qu = q(i);
                 double tu = 0.0;
                 if (M ? (cm & CLS_U) != 0 : x >= 1) Tn[i] = tu = mom_f(L, q, i, 1, 3 * fs + i, M ? cls_diag(cm, 0) : 6.0);
-                Q1[i] = qu;
+                if (UPD) Q1[i] = qu;
                 c4 = qu * tu;
             }
             {
@@ -733,7 +736,7 @@ __global__ void __launch_bounds__(256) k_apply_q(LevelK L, const double* __restr
                 double tv = 0.0;
                 if (M ? (cm & CLS_V) != 0 : y >= 1)
                     Tn[fs + i] = tv = mom_f(L, q, fs + i, g.sy, 3 * fs + i, M ? cls_diag(cm, 1) : 6.0);
-                Q1[fs + i] = qv;
+                if (UPD) Q1[fs + i] = qv;
                 c4 = c4 + qv * tv;
             }
             {
@@ -741,13 +744,13 @@ __global__ void __launch_bounds__(256) k_apply_q(LevelK L, const double* __restr
                 double tw = 0.0;
                 if (M ? (cm & CLS_W) != 0 : g.gz(z) >= 1)
                     Tn[2 * fs + i] = tw = mom_f(L, q, 2 * fs + i, g.sz, 3 * fs + i, M ? cls_diag(cm, 2) : 6.0);
-                Q1[2 * fs + i] = qw;
+                if (UPD) Q1[2 * fs + i] = qw;
                 c4 = c4 + qw * tw;
             }
             const double qp = q(3 * fs + i);
             double tp = 0.0;
             if (!M || (cm & CLS_P)) Tn[3 * fs + i] = tp = cont_f(L, q, i, 0.0);
-            Q1[3 * fs + i] = qp;
+            if (UPD) Q1[3 * fs + i] = qp;
             v = v + (c4 + qp * tp);  // ((p_u + p_v) + p_w) + p_p
         }
     }
@@ -757,7 +760,7 @@ __global__ void __launch_bounds__(256) k_apply_q(LevelK L, const double* __restr
 // Lines 7 + 8 of iteration j: d = cd d + cq q, x = x + d (written to D1, X1), then the true
 // residual r = b - L x as block partials of ||r||^2 (r itself is never stored).  Ghost planes
 // as in k_apply_q.
-template <bool M>
+template <bool M, bool UPD>
 __global__ void __launch_bounds__(256, M ? 3 : 4) k_apply_x(LevelK L, const double* __restrict__ X0,
                                                  const double* __restrict__ D0, const double* __restrict__ Q,
                                                  const double* __restrict__ B, double* __restrict__ X1,
@@ -769,7 +772,7 @@ __global__ void __launch_bounds__(256, M ? 3 : 4) k_apply_x(LevelK L, const doub
     const int64_t fs = g.fs;
     const double cd = sc[S_CD], cq = sc[S_CQ];
     auto dn = [&](int64_t j) { return cd * D0[j] + cq * Q[j]; };  // the oracle's d[i] = cd d[i] + cq q[i]
-    auto xn = [&](int64_t j) { return X0[j] + dn(j); };           // x[i] = x[i] + d[i]
+    auto xn = [&](int64_t j) { return UPD ? X0[j] + dn(j) : X1[j]; };  // x[i] = x[i] + d[i]
     const int x = blockIdx.x * 32 + threadIdx.x, y = blockIdx.y * 8 + threadIdx.y;
     const int zl = blockIdx.z * kDotZB, zh = min(g.nz, zl + kDotZB);
     double v = 0.0;
@@ -782,8 +785,8 @@ __global__ void __launch_bounds__(256, M ? 3 : 4) k_apply_x(LevelK L, const doub
                 X1[f * fs + i] = X0[f * fs + i] + d;
             }
         };
-        if (halo_lo && blockIdx.z == 0) put_xd(g.slot(x, y, -1));
-        if (halo_hi && zh == g.nz) put_xd(g.slot(x, y, g.nz));
+        if (UPD && halo_lo && blockIdx.z == 0) put_xd(g.slot(x, y, -1));
+        if (UPD && halo_hi && zh == g.nz) put_xd(g.slot(x, y, g.nz));
 #pragma unroll 1
         for (int z = zl; z < zh; ++z) {
             const int64_t i = g.slot(x, y, z);
@@ -795,11 +798,45 @@ __global__ void __launch_bounds__(256, M ? 3 : 4) k_apply_x(LevelK L, const doub
             if (M ? (cm & CLS_W) != 0 : g.gz(z) >= 1)
                 rw = B[2 * fs + i] - mom_f(L, xn, 2 * fs + i, g.sz, 3 * fs + i, M ? cls_diag(cm, 2) : 6.0);
             if (!M || (cm & CLS_P)) rp = B[3 * fs + i] - cont_f(L, xn, i, 0.0);
-            put_xd(i);
+            if (UPD) put_xd(i);
             v = v + cell4(ru * ru, rv * rv, rw * rw, rp * rp);
         }
     }
     block_partial2(v, 0.0, partials, dot_nblk(g), dot_blk(g));
+}
+
+// The SQMR vector updates as streaming passes (for the !UPD stencil kernels): per cell of the level
+// (and of the ghost planes a slab part fills for its neighbours), all four fields.
+__global__ void __launch_bounds__(256) k_q_upd(Geom g, const double* __restrict__ T, const double* __restrict__ Q0,
+                                               double* __restrict__ Q1, const double* __restrict__ sc, int halo_lo,
+                                               int halo_hi) {
+    pdl_wait();
+    if (sc[S_STATUS] != 0.0) return;
+    const int x = blockIdx.x * BX + threadIdx.x, y = blockIdx.y * BY + threadIdx.y;
+    const int z = static_cast<int>(blockIdx.z) - halo_lo;
+    if (x >= g.nx || y >= g.ny || z >= g.nz + halo_hi) return;
+    const double beta = sc[S_BETA];
+    const int64_t i = g.slot(x, y, z), fs = g.fs;
+#pragma unroll
+    for (int f = 0; f < 4; ++f) Q1[f * fs + i] = T[f * fs + i] + beta * Q0[f * fs + i];
+}
+__global__ void __launch_bounds__(256) k_xd_upd(Geom g, const double* __restrict__ X0, const double* __restrict__ D0,
+                                                const double* __restrict__ Q, double* __restrict__ X1,
+                                                double* __restrict__ D1, const double* __restrict__ sc, int halo_lo,
+                                                int halo_hi) {
+    pdl_wait();
+    if (sc[S_STATUS] != 0.0) return;
+    const int x = blockIdx.x * BX + threadIdx.x, y = blockIdx.y * BY + threadIdx.y;
+    const int z = static_cast<int>(blockIdx.z) - halo_lo;
+    if (x >= g.nx || y >= g.ny || z >= g.nz + halo_hi) return;
+    const double cd = sc[S_CD], cq = sc[S_CQ];
+    const int64_t i = g.slot(x, y, z), fs = g.fs;
+#pragma unroll
+    for (int f = 0; f < 4; ++f) {
+        const double d = cd * D0[f * fs + i] + cq * Q[f * fs + i];
+        D1[f * fs + i] = d;
+        X1[f * fs + i] = X0[f * fs + i] + d;
+    }
 }
 
 __global__ void k_axpy(double* __restrict__ y, const double* __restrict__ x, double alpha, int64_t n) {
@@ -2919,16 +2956,38 @@ void launch_final_scalar(const Geom& g, const double* partials, double* sc, int 
 }
 void launch_apply_q(const LevelK& L, const double* t, const double* q0, double* q1, double* tn, const double* sc,
                     double* partials, int halo_lo, int halo_hi, cudaStream_t s) {
-    if (L.cls) launch_k(k_apply_q<true>, dot_grid(L.g), dim3(32, 8), 0, s, L, t, q0, q1, tn, sc, partials, halo_lo, halo_hi);
-    else launch_k(k_apply_q<false>, dot_grid(L.g), dim3(32, 8), 0, s, L, t, q0, q1, tn, sc, partials, halo_lo, halo_hi);
+    // SMG_SQMR_SPLIT (default 1): the vector update as its own streaming pass, then the stencil + dot
+    // kernel on the stored vector; 0: one kernel evaluating the update at every stencil point
+    static const int split = env_int("SMG_SQMR_SPLIT", 1);
+    if (split) {
+        dim3 ug = cell_grid(L.g);
+        ug.z = L.g.nz + halo_lo + halo_hi;
+        launch_k(k_q_upd, ug, dim3(BX, BY), 0, s, L.g, t, q0, q1, sc, halo_lo, halo_hi);
+        count();
+        if (L.cls) launch_k(k_apply_q<true, false>, dot_grid(L.g), dim3(32, 8), 0, s, L, t, q0, q1, tn, sc, partials, halo_lo, halo_hi);
+        else launch_k(k_apply_q<false, false>, dot_grid(L.g), dim3(32, 8), 0, s, L, t, q0, q1, tn, sc, partials, halo_lo, halo_hi);
+    } else if (L.cls) {
+        launch_k(k_apply_q<true, true>, dot_grid(L.g), dim3(32, 8), 0, s, L, t, q0, q1, tn, sc, partials, halo_lo, halo_hi);
+    } else {
+        launch_k(k_apply_q<false, true>, dot_grid(L.g), dim3(32, 8), 0, s, L, t, q0, q1, tn, sc, partials, halo_lo, halo_hi);
+    }
     count();
 }
 void launch_apply_x(const LevelK& L, const double* x0, const double* d0, const double* q, const double* b, double* x1,
                     double* d1, const double* sc, double* partials, int halo_lo, int halo_hi, cudaStream_t s) {
-    if (L.cls)
-        launch_k(k_apply_x<true>, dot_grid(L.g), dim3(32, 8), 0, s, L, x0, d0, q, b, x1, d1, sc, partials, halo_lo, halo_hi);
-    else
-        launch_k(k_apply_x<false>, dot_grid(L.g), dim3(32, 8), 0, s, L, x0, d0, q, b, x1, d1, sc, partials, halo_lo, halo_hi);
+    static const int split = env_int("SMG_SQMR_SPLIT", 1);
+    if (split) {
+        dim3 ug = cell_grid(L.g);
+        ug.z = L.g.nz + halo_lo + halo_hi;
+        launch_k(k_xd_upd, ug, dim3(BX, BY), 0, s, L.g, x0, d0, q, x1, d1, sc, halo_lo, halo_hi);
+        count();
+        if (L.cls) launch_k(k_apply_x<true, false>, dot_grid(L.g), dim3(32, 8), 0, s, L, x0, d0, q, b, x1, d1, sc, partials, halo_lo, halo_hi);
+        else launch_k(k_apply_x<false, false>, dot_grid(L.g), dim3(32, 8), 0, s, L, x0, d0, q, b, x1, d1, sc, partials, halo_lo, halo_hi);
+    } else if (L.cls) {
+        launch_k(k_apply_x<true, true>, dot_grid(L.g), dim3(32, 8), 0, s, L, x0, d0, q, b, x1, d1, sc, partials, halo_lo, halo_hi);
+    } else {
+        launch_k(k_apply_x<false, true>, dot_grid(L.g), dim3(32, 8), 0, s, L, x0, d0, q, b, x1, d1, sc, partials, halo_lo, halo_hi);
+    }
     count();
 }
 static int env_int(const char* name, int dflt) {
