@@ -2838,6 +2838,10 @@ void launch_dgs_prev(const LevelK& L, double* x, const double* b, int colour, cu
     else k_dgs_prev<<<cell_grid(L.g), dim3(BX, BY), 0, s>>>(L, x, b, colour);
     count();
 }
+static bool vanka_d8() {
+    static const int v = env_int("SMG_VANKA_D8", 1);
+    return v != 0;
+}
 void launch_vanka_delta(const LevelK& L, const double* x, const double* b, const int32_t* cells,
                         const uint8_t* masks, int ncells, const double* ktab, double* delta, cudaStream_t s,
                         const uint16_t* kidx) {
@@ -2848,9 +2852,10 @@ void launch_vanka_delta(const LevelK& L, const double* x, const double* b, const
         if (one) k_vanka_delta_m<<<(ncells + 127) / 128, 128, 0, s>>>(L, x, b, cells, masks, kidx, ncells, ktab, delta);
         else launch_k(k_vanka_delta8<true>, static_cast<int>((8 * static_cast<int64_t>(ncells) + 255) / 256), 256, 0, s, L, x,
                       b, cells, masks, kidx, ncells, ktab, delta);
-    } else if (env_int("SMG_VANKA_D8", 1)) {  // 8 lanes per block (0: one thread per block; bit-identical)
+    } else if (vanka_d8()) {  // 8 lanes per block (SMG_VANKA_D8=0: one thread per block; bit-identical)
         const int blocks = static_cast<int>((8 * static_cast<int64_t>(ncells) + 255) / 256);
-        if (env_int("SMG_VANKA_PDL", 0)) launch_k(k_vanka_delta8<false>, blocks, 256, 0, s, L, x, b, cells, masks, kidx, ncells, ktab, delta);
+        static const int vpdl = env_int("SMG_VANKA_PDL", 0);
+        if (vpdl) launch_k(k_vanka_delta8<false>, blocks, 256, 0, s, L, x, b, cells, masks, kidx, ncells, ktab, delta);
         else k_vanka_delta8<false><<<blocks, 256, 0, s>>>(L, x, b, cells, masks, kidx, ncells, ktab, delta);
     }
     else k_vanka_delta<<<(ncells + 127) / 128, 128, 0, s>>>(L, x, b, cells, masks, ncells, ktab, delta);
@@ -2859,9 +2864,10 @@ void launch_vanka_delta(const LevelK& L, const double* x, const double* b, const
 void launch_vanka_apply(const LevelK& L, double* x, const int32_t* cells, const uint8_t* masks, int ncells,
                         const double* delta, cudaStream_t s, const uint8_t* amask) {
     if (ncells <= 0) return;
-    if (!amask && (L.cls || env_int("SMG_VANKA_D8", 1))) {
+    if (!amask && (L.cls || vanka_d8())) {
         const int blocks = static_cast<int>((8 * static_cast<int64_t>(ncells) + 255) / 256);
-        if (env_int("SMG_VANKA_PDL", 0)) launch_k(k_vanka_apply8, blocks, 256, 0, s, L, x, cells, masks, ncells, delta);
+        static const int vpdl = env_int("SMG_VANKA_PDL", 0);
+        if (vpdl) launch_k(k_vanka_apply8, blocks, 256, 0, s, L, x, cells, masks, ncells, delta);
         else k_vanka_apply8<<<blocks, 256, 0, s>>>(L, x, cells, masks, ncells, delta);
     }
     else
