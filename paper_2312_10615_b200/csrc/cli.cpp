@@ -3,7 +3,10 @@
 //
 //   solver run <config.json>      solve; writes history_<method>.csv and summary.txt
 //   solver census <config.json>   prints "N V1 pct%" (PAPER Table 1 layout)
-//   solver verify [--max-n N]     symmetry of the materialised GPU smoother / V-cycle maps
+//   solver verify [--max-n N]     symmetry of the materialised GPU smoother / V-cycle maps,
+//                                 on the walled cube and on a labelled cube with an obstacle and an outflow
+//   solver matrix <config.json>   dense L of the fine level (N <= 5000) as Matrix Market
+//                                 coordinate text on stdout, materialised through smg_apply
 //
 // RunConfig (JSON, flat): nx, ny, nz (cells), h (default 1/nx), eta (1e-3),
 // gamma (1e-3), levels, nu (1), band_width (1), cycle ("V"|"W"), method
@@ -162,7 +165,8 @@ bool read_domain(const std::string& path, smg_grid_desc& g, std::vector<uint8_t>
 }
 
 int usage() {
-    std::fprintf(stderr, "usage: solver run <config.json> | solver census <config.json> | solver verify [--max-n N]\n");
+    std::fprintf(stderr, "usage: solver run <config.json> | solver census <config.json> | solver matrix <config.json> | "
+                         "solver verify [--max-n N]\n");
     return 1;
 }
 
@@ -210,6 +214,50 @@ int verify(int max_n) {
             }
             smg_destroy(ctx);
         }
+        if (n < 8) continue;
+        // the same maps on a general labelled domain: a Dirichlet block and an Exterior outflow column
+        std::vector<uint8_t> lab(static_cast<size_t>(n) * n * n, 1);
+        for (int z = 0; z < n; ++z)
+            for (int y = 0; y < n; ++y)
+                for (int x = 0; x < n; ++x) {
+                    uint8_t& l = lab[(static_cast<size_t>(z) * n + y) * n + x];
+                    if (x >= n / 4 && x < n / 2 && y >= n / 4 && y < n / 2) l = 0;
+                    if (x == n - 1) l = 2;
+                }
+        smg_params p{1.0, 1e-3, 2, 1, 1, 0, 0, 0, 1.0, -1};
+        smg_ctx* ctx = nullptr;
+        if (smg_create_labeled(&g, lab.data(), &p, 0, &ctx) != SMG_OK) return 1;
+        const int64_t N = smg_level_ndof(ctx, 0, nullptr);
+        struct Map { const char* name; int op; };
+        const Map maps[] = {{"smooth", 4}, {"vanka_symmetric", 3}, {"vcycle", -1}};
+        for (const Map& m : maps) {
+            std::vector<double> C(static_cast<size_t>(N * N)), e(N, 0.0), col(N);
+            for (int64_t j = 0; j < N; ++j) {
+                e[j] = 1.0;
+                int rc;
+                if (m.op < 0) {
+                    rc = smg_vcycle(ctx, e.data(), col.data());
+                } else {
+                    std::fill(col.begin(), col.end(), 0.0);
+                    rc = smg_smoother(ctx, 0, m.op, 0, col.data(), e.data());
+                }
+                if (rc != SMG_OK) { smg_destroy(ctx); return 1; }
+                for (int64_t i = 0; i < N; ++i) C[static_cast<size_t>(i * N + j)] = col[i];
+                e[j] = 0.0;
+            }
+            double d = 0.0, a = 0.0;
+            for (int64_t i = 0; i < N; ++i)
+                for (int64_t j = 0; j < N; ++j) {
+                    const double c = C[static_cast<size_t>(i * N + j)], t = C[static_cast<size_t>(j * N + i)];
+                    d += (c - t) * (c - t);
+                    a += c * c;
+                }
+            const double defect = std::sqrt(d) / std::fmax(std::sqrt(a), 1e-300);
+            const bool pass = defect < 1e-10 && a > 0.0;
+            ok = ok && pass;
+            std::printf("n=%d labelled %s symmetry_defect=%.3e %s\n", n, m.name, defect, pass ? "PASS" : "FAIL");
+        }
+        smg_destroy(ctx);
     }
     return ok ? 0 : 2;
 }
@@ -260,7 +308,7 @@ int main(int argc, char** argv) {
                     100.0 * static_cast<double>(out[1]) / static_cast<double>(out[0]));
         return 0;
     }
-    if (cmd != "run") return usage();
+    if (cmd != "run" && cmd != "matrix") return usage();
     const std::string vk = str("vanka", "multiplicative");  // SmootherConfig.kind
     if (vk != "multiplicative" && vk != "additive") { std::fprintf(stderr, "config error: vanka\n"); return 1; }
     smg_params p{num("eta", 1e-3), num("gamma", 1e-3), static_cast<int>(num("levels", 2)),
@@ -293,6 +341,29 @@ int main(int argc, char** argv) {
     }
     int64_t cnt[5];
     const int64_t n = smg_level_ndof(ctx, 0, cnt);
+    if (cmd == "matrix") {  // assemble_dense through the GPU operator, Matrix Market out
+        if (n > 5000) {
+            std::fprintf(stderr, "matrix: N = %lld above the cap 5000 (SPEC:158)\n", static_cast<long long>(n));
+            smg_destroy(ctx);
+            return 1;
+        }
+        std::vector<double> e(n, 0.0), col(n);
+        std::vector<std::vector<std::pair<int64_t, double>>> cols(n);
+        int64_t nnz = 0;
+        for (int64_t j = 0; j < n; ++j) {
+            e[j] = 1.0;
+            if (smg_apply(ctx, 0, 0, e.data(), col.data()) != SMG_OK) { smg_destroy(ctx); return 1; }
+            e[j] = 0.0;
+            for (int64_t i = 0; i < n; ++i)
+                if (col[i] != 0.0) { cols[j].push_back({i, col[i]}); ++nnz; }
+        }
+        std::printf("%%%%MatrixMarket matrix coordinate real general\n%lld %lld %lld\n", static_cast<long long>(n),
+                    static_cast<long long>(n), static_cast<long long>(nnz));
+        for (int64_t j = 0; j < n; ++j)
+            for (auto& en : cols[j]) std::printf("%lld %lld %.17g\n", static_cast<long long>(en.first + 1), static_cast<long long>(j + 1), en.second);
+        smg_destroy(ctx);
+        return 0;
+    }
     std::vector<double> b(n), x(n), hist(maxit), secs(maxit), lx(n);
     if (!labels.empty()) smg_forcing_labeled(&g, labels.data(), kind, static_cast<uint64_t>(num("seed", 0)), b.data());
     else if (fk == "cavity") smg_assemble_rhs(&g, p.eta, 0, num("lid", 1.0), b.data());  // zero force, lid u

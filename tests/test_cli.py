@@ -88,7 +88,7 @@ def test_verify_symmetry():
     r = subprocess.run([CLI, "verify", "--max-n", "8"], capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout + r.stderr
     lines = r.stdout.splitlines()
-    assert len(lines) == 12 and all(l.endswith("PASS") for l in lines)
+    assert len(lines) == 15 and all(l.endswith("PASS") for l in lines)  # 2 sizes x 2 Vanka kinds x 3 maps + labelled
 
 
 def test_verify_usage():
@@ -134,3 +134,29 @@ def test_run_on_a_domain_file(tmp_path):
     assert st == smg.SMG_CONVERGED and np.array_equal(h, hp)
     summ = dict(l.split(": ") for l in open(tmp_path / "summary.txt").read().splitlines())
     assert summ["status"] == "converged" and int(summ["dof"]) == smg.census_labels(lab)["N"]
+
+
+@pytest.mark.gpu
+def test_matrix_market_export(tmp_path):
+    """`solver matrix`: the fine-level L materialised through the GPU operator as
+    Matrix Market coordinate text: equals the oracle's dense L and is symmetric."""
+    import oracle
+    _, path = _domain(tmp_path)
+    from paper_2312_10615_b200 import scenarios
+    lab = scenarios.cylinder3d(16, 8, 8, cx=0.4, cy=0.5, radius=0.2)
+    scenarios.write_domain_file(path, lab, 1 / 8)
+    r = run(["matrix"], {"domain": path, "levels": 2, "eta": 1.0}, str(tmp_path))
+    assert r.returncode == 0, r.stderr
+    lines = r.stdout.splitlines()
+    assert lines[0] == "%%MatrixMarket matrix coordinate real general"
+    n, n2, nnz = (int(v) for v in lines[1].split())
+    A = np.zeros((n, n))
+    for l in lines[2:]:
+        i, j, v = l.split()
+        A[int(i) - 1, int(j) - 1] = float(v)
+    assert n == n2 and len(lines) == 2 + nnz
+    o = oracle.Oracle(0, levels=2, labels=lab, h=1 / 8)
+    assert np.array_equal(A, o.dense(0, False))
+    assert np.abs(A - A.T).max() <= 1e-12 * np.abs(A).max()
+    big = run(["matrix"], {"nx": 16, "levels": 2}, str(tmp_path))
+    assert big.returncode == 1  # N above the dense cap

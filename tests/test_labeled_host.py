@@ -158,3 +158,24 @@ def test_assemble_rhs_with_general_dirichlet_data():
     assert abs(b[-npres:].sum()) <= 1e-12 * np.abs(b[-npres:]).sum()
     with pytest.raises(ValueError):
         smg.assemble_rhs_labels(ch, h, gu, gv, gw)  # wrong shapes
+
+
+def test_labelled_mgsqmr_matches_dense_direct_solve():
+    """AC 6 / AC 11 analogue on a labelled domain (Dirichlet block, Exterior column and notch): the
+    oracle's MG-SQMR solution against a dense direct solve of the assembled L (pressure constant
+    fixed by a Lagrange multiplier) -- an independent pin of the labelled operator and solver."""
+    o = oracle.Oracle(0, levels=2, labels=small_domain(), h=1 / 8)
+    b = o.forcing(oracle.FORCE_UNIFORM, 3)
+    x, hist, _, st = o.sqmr(b, tol=1e-11, maxit=200)
+    assert st == oracle.ST_CONVERGED
+    L = o.dense(0, False)
+    n, npres = L.shape[0], o.counts(0)["np"]
+    e = np.zeros(n)
+    e[n - npres:] = 1.0
+    A = np.zeros((n + 1, n + 1))
+    A[:n, :n], A[:n, n], A[n, :n] = L, e, e
+    xd = np.linalg.solve(A, np.append(b, 0.0))[:n]
+    u, ud = x[:-npres], xd[:-npres]
+    p, pd = x[-npres:] - x[-npres:].mean(), xd[-npres:] - xd[-npres:].mean()
+    assert np.linalg.norm(u - ud) / np.linalg.norm(ud) < 1e-8
+    assert np.linalg.norm(p - pd) / np.linalg.norm(pd) < 1e-8
