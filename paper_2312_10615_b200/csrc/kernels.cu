@@ -2322,7 +2322,9 @@ __global__ void __launch_bounds__(kTileThreads, 2)
     // tile of colour T for this CTA (z parity on global tile indices: slab parts start on a tile)
     const int pz = ((T >> 2) ^ (g.z0 / kTZ)) & 1;
     const int hx = (ntx - (T & 1) + 1) >> 1, hy = (nty - ((T >> 1) & 1) + 1) >> 1;
-    const int bi = blockIdx.x;
+    // pf < 0: this launch walks its tiles backwards, so it starts where the previous launch (the
+    // neighbouring tile colour, walked forwards) ended -- on data still in L2
+    const int bi = pf < 0 ? static_cast<int>(gridDim.x) - 1 - static_cast<int>(blockIdx.x) : static_cast<int>(blockIdx.x);
     const int tx = 2 * (bi % hx) + (T & 1), ty = 2 * ((bi / hx) % hy) + ((T >> 1) & 1), tz = 2 * (bi / (hx * hy)) + pz;
     const int x0 = tx * kTX, y0 = ty * kTY, z0 = tz * kTZ;  // z0: local plane of the part
     if (tid == 0) {
@@ -3351,7 +3353,11 @@ void launch_dgs_tile_phases(const LevelK& L, double* x, const double* b, int T, 
     }
     // SMG_TILE_PF: L2 prefetch distance in CTAs (0 = off, the default: measured 2.19 (off) / 2.16 (148) /
     // 2.30 (296) / 2.40 ms (592) per cfg-2 fine sweep -- the loads are not latency-exposed)
-    static const int pf = env_int("SMG_TILE_PF", 0);
+    static const int pf0 = env_int("SMG_TILE_PF", 0);
+    // SMG_TILE_ALT (default 1): consecutive launches of a sweep alternate their traversal direction
+    static const int alt = env_int("SMG_TILE_ALT", 1);
+    const int seq = fwd ? T : 15 - T;  // position of this launch in the symmetric sweep
+    const int pf = (alt && (seq & 1)) ? -1 : pf0;
     // Ordinary launches (SMG_TILE_PDL=1 restores programmatic dependent launch): with PDL the next
     // colour's CTAs take the SM's shared memory slots early and the cfg-2 fine sweep measured
     // 2.185 ms against 2.04 ms without (round 2, session 5)
