@@ -2167,8 +2167,12 @@ __device__ __forceinline__ void tile_phases(const LevelK& L, double* __restrict_
                     const int k = task >> 2, s = task & 3;
                     const int lx = 2 * m8 + (k & 1), ly = 2 * r4 + ((k >> 1) & 1), lz = 2 * s + (k >> 2);
                     const int li = TB::li(lx, ly, lz), td = tile_td(lx, ly, lz);
-                    if (full && (IN || tile_v2<false>(L, x0, y0, z0, lx, ly, lz))) {
-                        Ps[li] = gath_k<false>(k, Ps[li], ts, td, e2);  // relaxed: the colours above k
+                    if (full) {
+                        // relaxed cell: the colours above k; a band cell of a boundary tile had no phase
+                        // of its own: the colours below k first (ascending, as the generic form)
+                        double p = Ps[li];
+                        if (!IN && !tile_v2<false>(L, x0, y0, z0, lx, ly, lz)) p = gath_k<true>(k, p, ts, td, e2);
+                        Ps[li] = gath_k<false>(k, p, ts, td, e2);
                     } else {
                         const bool relaxed = k >= cfirst && k <= c && tile_v2<IN>(L, x0, y0, z0, lx, ly, lz);
                         Ps[li] = tile_gathers<IN>(L, ts, Ps[li], x0, y0, z0, lx, ly, lz, k, relaxed ? k + 1 : cfirst, c);
@@ -2201,7 +2205,7 @@ __device__ __forceinline__ void tile_phases(const LevelK& L, double* __restrict_
                     }
                     const int li = TB::li(lx, ly, lz), td = tile_td(lx, ly, lz);
                     const int k = (lx & 1) + 2 * (ly & 1) + 4 * (lz & 1);
-                    if (full && IN) {  // the one term of its inward neighbour's colour
+                    if (full) {  // the one term of its inward neighbour's colour (a band neighbour carries delta 0)
                         const bool low = ax == 0 ? lx < 0 : (ax == 1 ? ly < 0 : lz < 0);
                         const int st = ax == 0 ? 1 : (ax == 1 ? kDX : kDXY);
                         const double d = ts[td + (low ? st : -st)];
