@@ -2844,10 +2844,7 @@ void launch_dgs_prev(const LevelK& L, double* x, const double* b, int colour, cu
     else k_dgs_prev<<<cell_grid(L.g), dim3(BX, BY), 0, s>>>(L, x, b, colour);
     count();
 }
-static bool vanka_d8() {
-    static const int v = env_int("SMG_VANKA_D8", 1);
-    return v != 0;
-}
+static bool vanka_d8() { return env_int("SMG_VANKA_D8", 1) != 0; }  // read per launch: tests toggle it
 void launch_vanka_delta(const LevelK& L, const double* x, const double* b, const int32_t* cells,
                         const uint8_t* masks, int ncells, const double* ktab, double* delta, cudaStream_t s,
                         const uint16_t* kidx) {
@@ -2970,7 +2967,7 @@ void launch_apply_q(const LevelK& L, const double* t, const double* q0, double* 
                     double* partials, int halo_lo, int halo_hi, cudaStream_t s) {
     // SMG_SQMR_SPLIT (default 1): the vector update as its own streaming pass, then the stencil + dot
     // kernel on the stored vector; 0: one kernel evaluating the update at every stencil point
-    static const int split = env_int("SMG_SQMR_SPLIT", 1);
+    const int split = env_int("SMG_SQMR_SPLIT", 1);  // read per launch: tests toggle it in-process
     if (split) {
         dim3 ug = cell_grid(L.g);
         ug.z = L.g.nz + halo_lo + halo_hi;
@@ -2987,7 +2984,7 @@ void launch_apply_q(const LevelK& L, const double* t, const double* q0, double* 
 }
 void launch_apply_x(const LevelK& L, const double* x0, const double* d0, const double* q, const double* b, double* x1,
                     double* d1, const double* sc, double* partials, int halo_lo, int halo_hi, cudaStream_t s) {
-    static const int split = env_int("SMG_SQMR_SPLIT", 1);
+    const int split = env_int("SMG_SQMR_SPLIT", 1);  // read per launch: tests toggle it in-process
     if (split) {
         dim3 ug = cell_grid(L.g);
         ug.z = L.g.nz + halo_lo + halo_hi;

@@ -231,6 +231,22 @@ def test_golden_history_and_solution(name):
     assert abs(np.linalg.norm(x[:-npres]) - g["u_norm"]) / g["u_norm"] < 1e-6
 
 
+@pytest.mark.parametrize("kw", [{}, {"devices": [0, 0]}])
+def test_sqmr_split_and_fused_updates_bitwise(kw, monkeypatch):
+    """The SQMR vector updates as streaming passes before the stencil kernels (default) and evaluated
+    inside them (SMG_SQMR_SPLIT=0) give the same bits -- single part and two z-slab parts (ghost planes)."""
+    out = []
+    for split in ("1", "0"):
+        monkeypatch.setenv("SMG_SQMR_SPLIT", split)
+        s = smg.Solver(32, levels=3, **kw)
+        x, h, _, st = s.sqmr(smg.forcing(32, seed=9), 1e-9, 50)
+        s.close()
+        out.append((x, h, st))
+    assert out[0][2] == out[1][2] == smg.SMG_CONVERGED
+    same(out[0][1], out[1][1])
+    same(out[0][0], out[1][0])
+
+
 def test_edge_cases():
     s = smg.Solver(8, levels=2)
     n = s.ndof()
@@ -363,7 +379,7 @@ def test_lid_driven_cavity_bitwise():
 
 
 @pytest.mark.parametrize("mode", [{}, {"SMG_SYNC_MODE": "1"}, {"SMG_SYNC_MODE": "2"}, {"SMG_VANKA_PP": "0"},
-                                  {"SMG_VANKA_PHASES": "1"},
+                                  {"SMG_VANKA_PHASES": "1"}, {"SMG_VANKA_PHASES": "1", "SMG_VANKA_D8": "0"},
                                   {"SMG_VANKA_KERNELS": "1"},
                                   {"SMG_VANKA_PAIRS": "0"}, {"SMG_VANKA_PAIRS": "2", "SMG_SYNC_MODE": "1"},
                                   {"SMG_VANKA_PAIRS": "2", "SMG_VANKA_KERNELS": "1"},
@@ -405,9 +421,9 @@ def test_vanka_merged_matches_unmerged(n, levels, monkeypatch):
 
 
 def test_vanka_per_launch_large_level_matches_persistent(monkeypatch):
-    """256^3 (lists beyond the persistent ping-pong sweep): default merged persistent sweep ==
-    one ping-pong launch per merged phase (the 512^3 default) == unmerged per-launch phases ==
-    unmerged persistent sweep."""
+    """256^3 (lists beyond the persistent ping-pong sweep): the default -- a delta and an apply launch
+    per merged phase, 8 lanes per block -- == one ping-pong launch per merged phase == unmerged
+    ping-pong launches == unmerged per-phase delta / apply launches."""
     out = []
     for env in ({}, {"SMG_VANKA_KERNELS": "1"}, {"SMG_VANKA_KERNELS": "1", "SMG_VANKA_PAIRS": "0"},
                 {"SMG_VANKA_KERNELS": "0", "SMG_VANKA_PAIRS": "0"}):
