@@ -233,33 +233,6 @@ __global__ void k_dgs_cb(LevelK L, const double* __restrict__ B, double* __restr
     CB[i] = fl * L.inv_h + L.eta_h2 * (6.0 * BP[i] - s);
 }
 
-__global__ void k_vanka_delta(LevelK L, const double* __restrict__ X, const double* __restrict__ B,
-                              const int32_t* __restrict__ cells, const uint8_t* __restrict__ masks, int n,
-                              const double* __restrict__ ktab, double* __restrict__ delta) {
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= n) return;
-    const Geom& g = L.g;
-    const int64_t fs = g.fs, sy = g.sy, sz = g.sz, i = cells[t];
-    const int m = masks[t];
-    const double *U = X, *V = X + fs, *W = X + 2 * fs, *P = X + 3 * fs;
-    double r[7];
-    r[0] = (m & 1) ? B[i] - mom(L, U, P, i, 1) : 0.0;
-    r[1] = (m & 2) ? B[i + 1] - mom(L, U, P, i + 1, 1) : 0.0;
-    r[2] = (m & 4) ? B[fs + i] - mom(L, V, P, i, sy) : 0.0;
-    r[3] = (m & 8) ? B[fs + i + sy] - mom(L, V, P, i + sy, sy) : 0.0;
-    r[4] = (m & 16) ? B[2 * fs + i] - mom(L, W, P, i, sz) : 0.0;
-    r[5] = (m & 32) ? B[2 * fs + i + sz] - mom(L, W, P, i + sz, sz) : 0.0;
-    r[6] = B[3 * fs + i] - cont(L, U, V, W, P, i, L.gamma);
-    const double* K = ktab + m * 49;
-#pragma unroll
-    for (int s = 0; s < 7; ++s) {
-        double acc = 0.0;
-#pragma unroll
-        for (int q = 0; q < 7; ++q) acc = acc + K[s * 7 + q] * r[q];
-        delta[static_cast<int64_t>(t) * 8 + s] = acc;
-    }
-}
-
 __global__ void k_vanka_apply(LevelK L, double* __restrict__ X, const int32_t* __restrict__ cells,
                               const uint8_t* __restrict__ masks, int n, const double* __restrict__ delta,
                               const uint8_t* __restrict__ amask) {
@@ -2623,40 +2596,11 @@ __global__ void k_dgs_prev_m(LevelK L, double* __restrict__ X, int colour) {
     X[3 * fs + i] = P[i] + (L.cb[i] - cl) / L.dp;
 }
 
-// Vanka block residuals and corrections of one colour list; kidx picks the block's signature
-// class (active-face mask + the faces' dropped legs) in ktab.
-__global__ void k_vanka_delta_m(LevelK L, const double* __restrict__ X, const double* __restrict__ B,
-                                const int32_t* __restrict__ cells, const uint8_t* __restrict__ masks,
-                                const uint16_t* __restrict__ kidx, int n, const double* __restrict__ ktab,
-                                double* __restrict__ delta) {
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= n) return;
-    const Geom& g = L.g;
-    const int64_t fs = g.fs, sy = g.sy, sz = g.sz, i = cells[t];
-    const int m = masks[t];
-    const uint32_t m0 = L.cls[i], mx = L.cls[i + 1], my = L.cls[i + sy], mz = L.cls[i + sz];
-    const double *U = X, *V = X + fs, *W = X + 2 * fs, *P = X + 3 * fs;
-    double r[7];
-    r[0] = (m & 1) ? B[i] - mom_d(L, U, P, i, 1, cls_diag(m0, 0)) : 0.0;
-    r[1] = (m & 2) ? B[i + 1] - mom_d(L, U, P, i + 1, 1, cls_diag(mx, 0)) : 0.0;
-    r[2] = (m & 4) ? B[fs + i] - mom_d(L, V, P, i, sy, cls_diag(m0, 1)) : 0.0;
-    r[3] = (m & 8) ? B[fs + i + sy] - mom_d(L, V, P, i + sy, sy, cls_diag(my, 1)) : 0.0;
-    r[4] = (m & 16) ? B[2 * fs + i] - mom_d(L, W, P, i, sz, cls_diag(m0, 2)) : 0.0;
-    r[5] = (m & 32) ? B[2 * fs + i + sz] - mom_d(L, W, P, i + sz, sz, cls_diag(mz, 2)) : 0.0;
-    r[6] = B[3 * fs + i] - cont(L, U, V, W, P, i, L.gamma);
-    const double* K = ktab + static_cast<int64_t>(kidx[t]) * 49;
-#pragma unroll
-    for (int s = 0; s < 7; ++s) {
-        double acc = 0.0;
-#pragma unroll
-        for (int q = 0; q < 7; ++q) acc = acc + K[s * 7 + q] * r[q];
-        delta[static_cast<int64_t>(t) * 8 + s] = acc;
-    }
-}
-
-// Lane-parallel form of k_vanka_delta_m / k_vanka_apply: 8 lanes per block, lane s < 7 computes
-// residual slot s (vanka_slot_residual's gather with the face's own diagonal) and the correction of
-// DOF s, delta_s = sum_q K[s][q] r_q with r_q gathered by warp shuffles in ascending q.
+// One Vanka colour list (a parity colour or a merged complementary pair), part 1: 8 lanes per block,
+// lane s < 7 computes residual slot s (the momentum row with the face's own diagonal / the continuity
+// row) and the correction of DOF s, delta_s = sum_q K[s][q] r_q with r_q gathered by warp shuffles in
+// ascending q (the oracle's order); kidx picks the block's signature class in ktab on labelled levels.
+// Part 2 (k_vanka_apply8 / k_vanka_apply) adds the corrections: Jacobi within the list.
 // M: labelled level (face diagonals from L.cls, class index from kidx); else the box (diagonal 6,
 // the class is the face mask).
 template <bool M>
@@ -2844,37 +2788,34 @@ void launch_dgs_prev(const LevelK& L, double* x, const double* b, int colour, cu
     else k_dgs_prev<<<cell_grid(L.g), dim3(BX, BY), 0, s>>>(L, x, b, colour);
     count();
 }
-static bool vanka_d8() { return env_int("SMG_VANKA_D8", 1) != 0; }  // read per launch: tests toggle it
 void launch_vanka_delta(const LevelK& L, const double* x, const double* b, const int32_t* cells,
                         const uint8_t* masks, int ncells, const double* ktab, double* delta, cudaStream_t s,
                         const uint16_t* kidx) {
     if (ncells <= 0) return;
+    // ordinary launches (no PDL): next to the tile DGS kernel early-scheduled dependents cost more
+    // than they hide (SMG_VANKA_PDL=1 restores PDL; profiles/r2d_experiments.md)
+    const int blocks = static_cast<int>((8 * static_cast<int64_t>(ncells) + 255) / 256);
+    static const int vpdl = env_int("SMG_VANKA_PDL", 0);
     if (L.cls) {
-        // SMG_VANKA_M1=1: the one-thread-per-block form (tests: both forms are bit-identical)
-        static const int one = env_int("SMG_VANKA_M1", 0);
-        if (one) k_vanka_delta_m<<<(ncells + 127) / 128, 128, 0, s>>>(L, x, b, cells, masks, kidx, ncells, ktab, delta);
-        else launch_k(k_vanka_delta8<true>, static_cast<int>((8 * static_cast<int64_t>(ncells) + 255) / 256), 256, 0, s, L, x,
-                      b, cells, masks, kidx, ncells, ktab, delta);
-    } else if (vanka_d8()) {  // 8 lanes per block (SMG_VANKA_D8=0: one thread per block; bit-identical)
-        const int blocks = static_cast<int>((8 * static_cast<int64_t>(ncells) + 255) / 256);
-        static const int vpdl = env_int("SMG_VANKA_PDL", 0);
+        if (vpdl) launch_k(k_vanka_delta8<true>, blocks, 256, 0, s, L, x, b, cells, masks, kidx, ncells, ktab, delta);
+        else k_vanka_delta8<true><<<blocks, 256, 0, s>>>(L, x, b, cells, masks, kidx, ncells, ktab, delta);
+    } else {
         if (vpdl) launch_k(k_vanka_delta8<false>, blocks, 256, 0, s, L, x, b, cells, masks, kidx, ncells, ktab, delta);
         else k_vanka_delta8<false><<<blocks, 256, 0, s>>>(L, x, b, cells, masks, kidx, ncells, ktab, delta);
     }
-    else k_vanka_delta<<<(ncells + 127) / 128, 128, 0, s>>>(L, x, b, cells, masks, ncells, ktab, delta);
     count();
 }
 void launch_vanka_apply(const LevelK& L, double* x, const int32_t* cells, const uint8_t* masks, int ncells,
                         const double* delta, cudaStream_t s, const uint8_t* amask) {
     if (ncells <= 0) return;
-    if (!amask && (L.cls || vanka_d8())) {
+    if (!amask) {
         const int blocks = static_cast<int>((8 * static_cast<int64_t>(ncells) + 255) / 256);
         static const int vpdl = env_int("SMG_VANKA_PDL", 0);
         if (vpdl) launch_k(k_vanka_apply8, blocks, 256, 0, s, L, x, cells, masks, ncells, delta);
         else k_vanka_apply8<<<blocks, 256, 0, s>>>(L, x, cells, masks, ncells, delta);
-    }
-    else
+    } else {  // z-slab parts: per-block ownership masks
         k_vanka_apply<<<(ncells + 127) / 128, 128, 0, s>>>(L, x, cells, masks, ncells, delta, amask);
+    }
     count();
 }
 void launch_restrict(const LevelK& F, const LevelK& C, const double* rf, double* bc, cudaStream_t s, int zc_lo,

@@ -379,7 +379,7 @@ def test_lid_driven_cavity_bitwise():
 
 
 @pytest.mark.parametrize("mode", [{}, {"SMG_SYNC_MODE": "1"}, {"SMG_SYNC_MODE": "2"}, {"SMG_VANKA_PP": "0"},
-                                  {"SMG_VANKA_PHASES": "1"}, {"SMG_VANKA_PHASES": "1", "SMG_VANKA_D8": "0"},
+                                  {"SMG_VANKA_PHASES": "1"},
                                   {"SMG_VANKA_KERNELS": "1"},
                                   {"SMG_VANKA_PAIRS": "0"}, {"SMG_VANKA_PAIRS": "2", "SMG_SYNC_MODE": "1"},
                                   {"SMG_VANKA_PAIRS": "2", "SMG_VANKA_KERNELS": "1"},

@@ -3,7 +3,7 @@
 # cylinder), smooth traffic (cfg 1-3), one full ncu capture of the top kernel (k_dgs_tile FWD, cfg 2)
 # and of the new Vanka delta kernel.  Every ncu command follows the same command run without ncu (&&).
 set -u
-O=gpurun_out; T=${1:-r2g}
+O=gpurun_out; T=${1:-r2i}
 timeout 2400 python -m pytest tests -m gpu -q --durations=10 > $O/${T}_pytest.log 2>&1; echo "pytest rc=$?" >> $O/${T}_pytest.log
 timeout 900 python bench.py > $O/${T}_bench_default.jsonl 2> $O/${T}_bench_default.err
 timeout 600 python bench.py --config 1 --also "" --no-labelled --no-cpu-baseline > $O/${T}_bench_cfg1.jsonl 2> $O/${T}_bench_cfg1.err
