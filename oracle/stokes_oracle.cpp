@@ -16,10 +16,14 @@
 // arithmetic contract in DESIGN.md §4 so results can be compared bit-for-bit
 // (compile with -ffp-contract=off; the GPU side uses -fmad=false).
 //
-// Parity pins (no reference artifact pins residual histories):
+// Parity pins ("parity unpinned" by the reference for residual histories: no reference artifact
+// pins them; the committed goldens are self-pinned):
 //   * Table-1 DOF census, exact — tests/test_oracle_census.py
-//   * structural KATs of SPEC AC 3-6, 11, 12 — tests/test_oracle_*.py
-//   * scipy sparse direct solves at small sizes — tests/test_oracle_direct.py
+//   * structural KATs of SPEC AC 3-6, 8, 9, 11, 12, on the walled box and on labelled domains with
+//     obstacles and Exterior cells — tests/test_oracle_*.py, tests/test_labeled_host.py
+//   * dense / sparse direct solves at small sizes — tests/test_oracle_direct.py, test_labeled_host.py
+//   * the reference's only compiled code, util.hpp (which this file includes through the drop-in
+//     header), against the reference's own header — tests/golden/util_probe_reference.txt
 // =============================================================================
 #include <algorithm>
 #include <array>
