@@ -102,7 +102,7 @@ int smg_create(const smg_grid_desc* grid, const smg_params* params, int ngpu, co
  * in Interior cells.  coarsen_grid labels the coarser levels, partition_band
  * gives V1 / V2, Vanka blocks are factorised once per signature class.
  * Extents must be divisible by 2^(levels-1) (pad with Exterior cells).  One GPU; the
- * smoother runs one kernel per phase (no DGS tiling), params.vanka 0 or 2.  Every other entry
+ * smoother runs one kernel per phase (no DGS tiling), every params.vanka flavour.  Every other entry
  * point works on the context; vectors are the compact FieldVector of this DofMap. */
 int smg_create_labeled(const smg_grid_desc* grid, const uint8_t* labels, const smg_params* params, int device,
                        smg_ctx** out);

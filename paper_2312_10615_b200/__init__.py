@@ -296,7 +296,7 @@ class Solver:
 
     @classmethod
     def from_labels(cls, labels, h=None, eta=1.0, gamma=1e-3, levels=2, nu=1, band_width=1, flags=0, device=0,
-                    cycle=0, vanka=0):
+                    cycle=0, vanka=0, omega=1.0):
         """General labelled domain (smg_create_labeled): labels shaped (nz, ny, nx) with
         0 Dirichlet, 1 Interior, 2 Exterior cells inside the implicit Dirichlet ring."""
         lab = _labels3(labels)
@@ -304,7 +304,7 @@ class Solver:
         h = 1.0 / nx if h is None else h
         self = cls.__new__(cls)
         self.grid = GridDesc(3, nx, ny, nz, h)
-        self.params = Params(eta, gamma, levels, nu, band_width, flags, cycle, vanka, 1.0, -1)
+        self.params = Params(eta, gamma, levels, nu, band_width, flags, cycle, vanka, omega, -1)
         ctx = C.c_void_p()
         rc = lib().smg_create_labeled(C.byref(self.grid), lab.ravel(), C.byref(self.params), device, C.byref(ctx))
         if rc != 0:

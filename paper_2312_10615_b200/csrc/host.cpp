@@ -268,6 +268,7 @@ struct DevLevel {
     int32_t* pack_slots = nullptr;
     uint16_t* vk_kidx[8] = {};
     uint16_t* sw_kidx[4] = {};  // merged complementary pairs (list m = parity m, then parity 7 - m)
+    uint16_t* va_kidx = nullptr;  // additive Vanka: classes of the one list of all blocks
     std::shared_ptr<struct HostMap> hm;
 };
 
@@ -755,6 +756,25 @@ void build_level_labeled(smg_ctx* c, int l, std::vector<uint8_t> lab, int& max_v
     L.ktab = c->dalloc<double>(std::max<size_t>(ktab.size(), 49));
     CK(cudaMemcpyAsync(L.ktab, ktab.data(), ktab.size() * sizeof(double), cudaMemcpyHostToDevice, c->st));
     CK(cudaStreamSynchronize(c->st));
+    if (p.vanka == 1) {  // additive Vanka: every block in one list + the 7-field correction scratch
+        std::vector<int32_t> ac;
+        std::vector<uint8_t> am;
+        std::vector<uint16_t> ak;
+        for (int col = 0; col < 8; ++col) {
+            ac.insert(ac.end(), cells[col].begin(), cells[col].end());
+            am.insert(am.end(), masks[col].begin(), masks[col].end());
+            ak.insert(ak.end(), kidx[col].begin(), kidx[col].end());
+        }
+        L.va_n = static_cast<int>(ac.size());
+        L.va_cells = c->dalloc<int32_t>(L.va_n);
+        L.va_mask = c->dalloc<uint8_t>(L.va_n);
+        L.va_kidx = c->dalloc<uint16_t>(L.va_n);
+        L.va_d7 = c->dalloc<double>(7 * G.fs);
+        CK(cudaMemcpyAsync(L.va_cells, ac.data(), ac.size() * sizeof(int32_t), cudaMemcpyHostToDevice, c->st));
+        CK(cudaMemcpyAsync(L.va_mask, am.data(), am.size(), cudaMemcpyHostToDevice, c->st));
+        CK(cudaMemcpyAsync(L.va_kidx, ak.data(), ak.size() * sizeof(uint16_t), cudaMemcpyHostToDevice, c->st));
+        CK(cudaStreamSynchronize(c->st));
+    }
     if (p.vanka == 2 && l + 1 < p.levels) {  // direct-on-V1: dense symmetric inverse of the V1 x V1 sub-block
         std::vector<int32_t> sel(static_cast<size_t>(m.N), -1), vslots;
         int n1 = 0;
@@ -804,7 +824,6 @@ void build(smg_ctx* c, const std::vector<double>* shared_coarse = nullptr, std::
     const bool labeled = !c->labels.empty();
     if (labeled && (c->nparts > 1 || c->ndist > 0))
         throw SmgError(SMG_EINVAL, "labelled domains: single-part contexts only");
-    if (labeled && p.vanka == 1) throw SmgError(SMG_EINVAL, "labelled domains: vanka must be 0 or 2");
     std::vector<uint8_t> lab = c->labels;  // labels of the level being built
     const int div = 1 << (p.levels - 1);
     if (g.nx % div || g.ny % div || g.nz % div)
@@ -1185,7 +1204,7 @@ void vanka_sym_coop(smg_ctx* c, int l, double* x, const double* b) {
 void vanka_additive(smg_ctx* c, int l, double* x, const double* b) {
     DevLevel& L = c->lv[l];
     if (!L.va_d7) throw SmgError(SMG_EINVAL, "additive Vanka needs params.vanka = 1 (single-part contexts)");
-    launch_vanka_additive(L.k, x, b, L.va_cells, L.va_mask, L.va_n, L.ktab, L.va_d7, c->prm.omega, c->st);
+    launch_vanka_additive(L.k, x, b, L.va_cells, L.va_mask, L.va_n, L.ktab, L.va_d7, c->prm.omega, c->st, L.va_kidx);
 }
 
 // direct-on-V1: x_V1 += A11^{-1} (b - L~x)_V1 -- the residual into the level's r

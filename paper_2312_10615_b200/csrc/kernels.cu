@@ -1211,9 +1211,16 @@ __device__ __forceinline__ void vanka_sweeps_pp(const LevelK& L, double* __restr
 // slot | hi faces u, v, w at the neighbour slot | p].  k_vadd_apply: each V1 DOF
 // is written by one thread, x += omega * ((0.0 + corr of the lower block) + corr
 // of the upper block), i.e. the oracle's ascending-cell summation order.
+// M: labelled level (face diagonals from L.cls, signature class from kidx, "the neighbour has a block"
+// from its DofMap bits instead of its distance to the wall).
+template <bool M>
+__device__ __forceinline__ double vanka_slot_residual_m(const LevelK& L, const double* __restrict__ X,
+                                                        const double* __restrict__ B, int64_t i, int m, int s8);
+template <bool M>
 __global__ void __launch_bounds__(256) k_vadd_delta(LevelK L, const double* __restrict__ X,
                                                     const double* __restrict__ B, const int32_t* __restrict__ cells,
-                                                    const uint8_t* __restrict__ masks, int n,
+                                                    const uint8_t* __restrict__ masks,
+                                                    const uint16_t* __restrict__ kidx, int n,
                                                     const double* __restrict__ ktab, double* __restrict__ D7) {
     pdl_wait();
     const Geom& g = L.g;
@@ -1222,14 +1229,15 @@ __global__ void __launch_bounds__(256) k_vadd_delta(LevelK L, const double* __re
     const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 3;
     const bool act = t < n;
     int64_t i = 0;
-    int m = 0;
+    int m = 0, ki = 0;
     if (act) {
         i = cells[t];
         m = masks[t];
+        ki = M ? kidx[t] : m;
     }
     double r = 0.0, own = 0.0;
-    if (act && s8 < 7) r = vanka_slot_residual(L, X, B, i, m, s8, own);
-    const double* K = ktab + m * 49 + (s8 < 7 ? s8 : 0) * 7;
+    if (act && s8 < 7) r = M ? vanka_slot_residual_m<true>(L, X, B, i, m, s8) : vanka_slot_residual(L, X, B, i, m, s8, own);
+    const double* K = ktab + static_cast<int64_t>(ki) * 49 + (s8 < 7 ? s8 : 0) * 7;
     double acc = 0.0;
 #pragma unroll
     for (int q = 0; q < 7; ++q) {
@@ -1247,6 +1255,7 @@ __global__ void __launch_bounds__(256) k_vadd_delta(LevelK L, const double* __re
     }
 }
 
+template <bool M>
 __global__ void __launch_bounds__(256) k_vadd_apply(LevelK L, double* __restrict__ X,
                                                     const int32_t* __restrict__ cells,
                                                     const uint8_t* __restrict__ masks, int n,
@@ -1268,11 +1277,15 @@ __global__ void __launch_bounds__(256) k_vadd_apply(LevelK L, double* __restrict
         const int dx = ax == 0, dy = ax == 1, dz = ax == 2;
         if (m & (1 << (2 * ax))) {  // low face: the lower cell's block (if band) first, then this one
             double acc = 0.0;
-            if (band_cell(L, x - dx, y - dy, zl - dz)) acc = acc + D7[(3 + ax) * fs + i];
+            const bool lower_block = M ? (L.cls[i - st] & (CLS_P | CLS_BAND)) == (CLS_P | CLS_BAND)
+                                       : band_cell(L, x - dx, y - dy, zl - dz);
+            if (lower_block) acc = acc + D7[(3 + ax) * fs + i];
             acc = acc + D7[ax * fs + i];
             X[ax * fs + i] = X[ax * fs + i] + omega * acc;
         }
-        if ((m & (1 << (2 * ax + 1))) && !band_cell(L, x + dx, y + dy, zl + dz)) {  // high face, this block only
+        const bool upper_block = M ? (L.cls[i + st] & (CLS_P | CLS_BAND)) == (CLS_P | CLS_BAND)
+                                   : band_cell(L, x + dx, y + dy, zl + dz);
+        if ((m & (1 << (2 * ax + 1))) && !upper_block) {  // high face, this block only
             X[ax * fs + i + st] = X[ax * fs + i + st] + omega * (0.0 + D7[(3 + ax) * fs + i + st]);
         }
     }
@@ -2596,6 +2609,25 @@ __global__ void k_dgs_prev_m(LevelK L, double* __restrict__ X, int colour) {
     X[3 * fs + i] = P[i] + (L.cb[i] - cl) / L.dp;
 }
 
+// Residual slot s8 (0..5 the faces uL, uR, vL, vR, wL, wR; 6 the pressure) of the Vanka block at cell
+// slot i with active-face mask m: the momentum row with the face's own diagonal (labelled levels: from
+// the DofMap bits of the face's cell; else 6) or the continuity row; 0 for an inactive face.
+template <bool M>
+__device__ __forceinline__ double vanka_slot_residual_m(const LevelK& L, const double* __restrict__ X,
+                                                        const double* __restrict__ B, int64_t i, int m, int s8) {
+    const Geom& g = L.g;
+    const int64_t fs = g.fs, sy = g.sy, sz = g.sz;
+    const bool mom_row = s8 < 6;
+    if (mom_row && !((m >> s8) & 1)) return 0.0;
+    const double *U = X, *V = X + fs, *W = X + 2 * fs, *P = X + 3 * fs;
+    if (!mom_row) return B[3 * fs + i] - cont(L, U, V, W, P, i, L.gamma);
+    const int d = s8 >> 1;
+    const int64_t st = d == 0 ? 1 : (d == 1 ? sy : sz);
+    const int64_t jj = i + ((s8 & 1) ? st : 0);  // face slot
+    const double diag = M ? cls_diag(L.cls[jj], d) : 6.0;
+    return B[d * fs + jj] - mom_d(L, X + d * fs, P, jj, st, diag);
+}
+
 // One Vanka colour list (a parity colour or a merged complementary pair), part 1: 8 lanes per block,
 // lane s < 7 computes residual slot s (the momentum row with the face's own diagonal / the continuity
 // row) and the correction of DOF s, delta_s = sum_q K[s][q] r_q with r_q gathered by warp shuffles in
@@ -2619,23 +2651,9 @@ __global__ void __launch_bounds__(256) k_vanka_delta8(LevelK L, const double* __
     double r = 0.0;
     int ki = 0;
     if (act && s8 < 7) {
-        const int64_t i = cells[t];
         const int m = masks[t];
         ki = M ? kidx[t] : m;
-        const bool mom_row = s8 < 6;
-        if (!mom_row || ((m >> s8) & 1)) {
-            const int d = s8 >> 1;
-            const int64_t st = d == 0 ? 1 : (d == 1 ? sy : sz);
-            const int64_t jj = i + ((s8 & 1) ? st : 0);  // face slot (cell slot for the pressure row)
-            const double *U = X, *V = X + fs, *W = X + 2 * fs, *P = X + 3 * fs;
-            if (mom_row) {
-                const double diag = M ? cls_diag(L.cls[jj], d) : 6.0;
-                const double* F = X + d * fs;
-                r = B[d * fs + jj] - mom_d(L, F, P, jj, st, diag);
-            } else {
-                r = B[3 * fs + i] - cont(L, U, V, W, P, i, L.gamma);
-            }
-        }
+        r = vanka_slot_residual_m<M>(L, X, B, cells[t], m, s8);
     }
     const double* K = ktab + static_cast<int64_t>(ki) * 49 + (s8 < 7 ? s8 : 0) * 7;
     double acc = 0.0;
@@ -3328,12 +3346,16 @@ void launch_dgs_tiled(const LevelK& L, double* x, const double* b, int nph, cuda
 }
 
 void launch_vanka_additive(const LevelK& L, double* x, const double* b, const int32_t* cells, const uint8_t* masks,
-                           int n, const double* ktab, double* d7, double omega, cudaStream_t s) {
+                           int n, const double* ktab, double* d7, double omega, cudaStream_t s, const uint16_t* kidx) {
     if (n <= 0) return;
-    launch_k(k_vadd_delta, dim3(static_cast<unsigned>((8 * static_cast<int64_t>(n) + 255) / 256)), dim3(256), 0, s, L,
-             x, b, cells, masks, n, ktab, d7);
-    launch_k(k_vadd_apply, dim3(static_cast<unsigned>((n + 255) / 256)), dim3(256), 0, s, L, x, cells, masks, n, d7,
-             omega);
+    const dim3 gd(static_cast<unsigned>((8 * static_cast<int64_t>(n) + 255) / 256)), ga(static_cast<unsigned>((n + 255) / 256));
+    if (L.cls) {
+        launch_k(k_vadd_delta<true>, gd, dim3(256), 0, s, L, x, b, cells, masks, kidx, n, ktab, d7);
+        launch_k(k_vadd_apply<true>, ga, dim3(256), 0, s, L, x, cells, masks, n, d7, omega);
+    } else {
+        launch_k(k_vadd_delta<false>, gd, dim3(256), 0, s, L, x, b, cells, masks, kidx, n, ktab, d7);
+        launch_k(k_vadd_apply<false>, ga, dim3(256), 0, s, L, x, cells, masks, n, d7, omega);
+    }
     count();
     count();
 }

@@ -191,7 +191,8 @@ enum SqmrSlot {
 // One additive Vanka application over all n band blocks (any order);
 // d7: scratch of 7 fields (g.fs each).  Bit-identical to the oracle's fixed order.
 void launch_vanka_additive(const LevelK& L, double* x, const double* b, const int32_t* cells, const uint8_t* masks,
-                           int n, const double* ktab, double* d7, double omega, cudaStream_t s);
+                           int n, const double* ktab, double* d7, double omega, cudaStream_t s,
+                           const uint16_t* kidx = nullptr);
 void launch_axpy_s(double* s_, const double* t, const double* sc, int64_t n, cudaStream_t s);
 
 // Number of our kernels launched so far (per process), for the bench's gpu_launches.

@@ -200,6 +200,30 @@ def test_direct_on_v1_and_wcycle_labeled():
             s.close()
 
 
+def test_additive_vanka_labeled():
+    """Additive Vanka on a labelled domain: one application, Alg. 3 with it, the V-cycle
+    and MG-SQMR bit-identical to the oracle."""
+    lab = mixed_domain()
+    oracle.set_threads(4)
+    o = oracle.Oracle(0, levels=3, labels=lab, h=1 / 16, vanka=1, omega=0.6)
+    s = smg.Solver.from_labels(lab, h=1 / 16, levels=3, vanka=smg.VANKA_ADDITIVE, omega=0.6)
+    try:
+        for level in range(2):
+            n = o.ndof(level)
+            x, b = rnd(n, 40 + level), rnd(n, 41 + level)
+            same(s.smoother(smg.OP_VANKA_ADD, x, b, level), o.smoother(5, x, b, level))
+            same(s.smoother(smg.OP_SMOOTH, x, b, level), o.smoother(4, x, b, level))
+        b = rnd(o.ndof(0), 42)
+        same(s.vcycle(b), o.vcycle(b))
+        xo, ho, _, so = o.sqmr(b, 1e-6, 80)
+        xg, hg, _, sg = s.sqmr(b, 1e-6, 80)
+        assert so == sg
+        same(np.asarray(hg), ho)
+        same(xg, xo)
+    finally:
+        s.close()
+
+
 def test_labeled_errors():
     lab = mixed_domain()
     with pytest.raises(smg.SmgError):
@@ -210,8 +234,6 @@ def test_labeled_errors():
         smg.Solver.from_labels(bad, levels=2)
     with pytest.raises(smg.SmgError):
         smg.Solver.from_labels(np.full((8, 8, 8), scenarios.E, np.uint8), levels=2)  # no active DOF
-    with pytest.raises(smg.SmgError):
-        smg.Solver.from_labels(lab, levels=2, vanka=smg.VANKA_ADDITIVE)
 
 
 def test_through_flow_channel_with_dirichlet_inflow():
