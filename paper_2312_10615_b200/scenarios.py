@@ -95,6 +95,33 @@ def inflow_profile(y, H, ubar, z=None):
     return 16.0 * ubar * y * z * (H - y) * (H - z) / H ** 4
 
 
+def pad_labels(labels, levels, wall=True):
+    """Pad a labelled grid to extents divisible by 2^(levels-1) (SPEC:81: "pad with Exterior cells";
+    smg_create_labeled wants divisible extents).  wall=True first adds one explicit Dirichlet layer on
+    every padded side, so the faces that touched the implicit Dirichlet ring stay Dirichlet-valued
+    (SPEC:38) -- the fine-level DofMap and operator are then exactly those of the unpadded grid;
+    without it the padded side becomes a homogeneous-Neumann boundary."""
+    lab = np.ascontiguousarray(labels, np.uint8)
+    m = 1 << (levels - 1)
+    out = lab
+    for axis in range(3):
+        n = out.shape[axis]
+        extra = (-n) % m
+        if extra == 0:
+            continue
+        if wall and extra < 1:
+            extra += m
+        shape = list(out.shape)
+        shape[axis] = extra
+        pad = np.full(shape, E, np.uint8)
+        if wall:
+            idx = [slice(None)] * 3
+            idx[axis] = slice(0, 1)
+            pad[tuple(idx)] = D
+        out = np.concatenate([out, pad], axis=axis)
+    return out
+
+
 def channel_inflow(labels, H, ubar, through=True):
     """Dirichlet data of the 3-D channel inflow (PAPER section 6.2.2): u = 16 ubar y z (H - y)(H - z) / H^4
     on the u faces of the inflow plane x = 0 (y, z at the face centres, channel height and depth H

@@ -258,3 +258,21 @@ def test_through_flow_channel_with_dirichlet_inflow():
     npres = o.counts(0)["np"]
     div = (o.apply(xg) - b)[-npres:]
     assert np.abs(div).max() <= 1e-8 * np.linalg.norm(b)
+
+
+def test_padded_odd_extents_solve():
+    """a grid with odd extents (30 x 13 x 9) padded by scenarios.pad_labels to 32 x 16 x 12
+    builds a 3-level hierarchy and solves bit-identically to the oracle on the padded grid."""
+    lab = scenarios.pad_labels(scenarios.cylinder3d(30, 13, 9, outflow=1), 3)
+    oracle.set_threads(4)
+    o = oracle.Oracle(0, levels=3, labels=lab, h=1 / 13)
+    s = smg.Solver.from_labels(lab, h=1 / 13, levels=3)
+    try:
+        b = smg.forcing_labels(lab, 1 / 13, smg.FORCE_CHANNEL, 8)
+        xo, ho, _, so = o.sqmr(b, 1e-8, 80)
+        xg, hg, _, sg = s.sqmr(b, 1e-8, 80)
+    finally:
+        s.close()
+    assert so == sg == smg.SMG_CONVERGED
+    same(np.asarray(hg), ho)
+    same(xg, xo)

@@ -179,3 +179,19 @@ def test_labelled_mgsqmr_matches_dense_direct_solve():
     p, pd = x[-npres:] - x[-npres:].mean(), xd[-npres:] - xd[-npres:].mean()
     assert np.linalg.norm(u - ud) / np.linalg.norm(ud) < 1e-8
     assert np.linalg.norm(p - pd) / np.linalg.norm(pd) < 1e-8
+
+
+def test_pad_labels_keeps_the_fine_level_problem():
+    """SPEC:81 padding (Exterior cells behind an explicit Dirichlet layer): extents become divisible by
+    2^(levels-1) and the fine-level DofMap and operator are those of the unpadded grid."""
+    lab = scenarios.cylinder3d(30, 13, 9, outflow=1)
+    pad = scenarios.pad_labels(lab, 3)
+    assert all(n % 4 == 0 for n in pad.shape) and pad.shape == (12, 16, 32)
+    assert np.array_equal(pad[:9, :13, :30], lab) and set(np.unique(pad[9:])) <= {0, 2}
+    c0, c1 = smg.census_labels(lab), smg.census_labels(pad)
+    assert c0 == c1
+    o0 = oracle.Oracle(0, levels=2, labels=lab, h=1 / 13)
+    o1 = oracle.Oracle(0, levels=2, labels=pad, h=1 / 13)
+    x = np.random.default_rng(0).standard_normal(o0.ndof(0))
+    assert np.array_equal(o0.apply(x), o1.apply(x))
+    assert scenarios.pad_labels(pad, 3) is pad or np.array_equal(scenarios.pad_labels(pad, 3), pad)
