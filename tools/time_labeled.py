@@ -18,6 +18,7 @@ ap.add_argument("--nz", type=int, default=128)
 ap.add_argument("--levels", type=int, default=5)
 ap.add_argument("--scenario", default="cylinder")
 ap.add_argument("--tol", type=float, default=1e-6)
+ap.add_argument("--no-box", action="store_true")
 a = ap.parse_args()
 mk = {"cylinder": scenarios.cylinder3d, "porous": scenarios.porous3d, "brancher": scenarios.brancher3d,
       "hollow": scenarios.hollow_square3d}[a.scenario]
@@ -33,7 +34,11 @@ for rep in range(3):
     t = s.timing()
     print(f"  labelled: status {st}, {len(hist)} iterations, {t['solve_ms']:.1f} ms, "
           f"{s.ndof(0) * len(hist) / t['solve_ms'] / 1e6:.2f} GDOF/s, {t['kernel_launches']} launches, rel {hist[-1]:.2e}", flush=True)
+xm, hm, _, stm = s.mg_solve(b, a.tol, 30)  # pure multigrid on L~ (PAPER section 6: the robustness split)
+print(f"  pure MG (30 cycles max): status {stm}, {len(hm)} cycles, rel {hm[-1]:.2e}", flush=True)
 s.close()
+if a.no_box:
+    sys.exit(0)
 sb = smg.Solver(a.nx, a.ny, a.nz, h=h, levels=a.levels, tile_min=-1)
 sb.set_rhs(smg.forcing(a.nx, a.ny, a.nz, h=h, kind=smg.FORCE_CHANNEL, seed=4))
 for rep in range(2):
