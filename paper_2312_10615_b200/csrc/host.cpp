@@ -65,6 +65,7 @@ struct NcclApi {
     decltype(&ncclGetUniqueId) getUniqueId = nullptr;
     decltype(&ncclCommInitRank) commInitRank = nullptr;
     decltype(&ncclCommDestroy) commDestroy = nullptr;
+    decltype(&ncclCommSplit) commSplit = nullptr;  // optional (NCCL >= 2.18): the halo communicator
     decltype(&ncclGroupStart) groupStart = nullptr;
     decltype(&ncclGroupEnd) groupEnd = nullptr;
     decltype(&ncclSend) send = nullptr;
@@ -89,6 +90,7 @@ const NcclApi& nccl() {
         sym(a.getUniqueId, "ncclGetUniqueId");
         sym(a.commInitRank, "ncclCommInitRank");
         sym(a.commDestroy, "ncclCommDestroy");
+        sym(a.commSplit, "ncclCommSplit");
         sym(a.groupStart, "ncclGroupStart");
         sym(a.groupEnd, "ncclGroupEnd");
         sym(a.send, "ncclSend");
@@ -337,6 +339,15 @@ struct smg_ctx {
     // plane partials and gathers travel through NCCL on the part's stream
     bool mp = false;
     ncclComm_t comm = nullptr;
+    // Comm stream (overlap): the halo transfers of a tiled DGS phase run here while the
+    // interior tile layers run on `st`.  evb: boundary tiles done (st -> cst); evc: transfer done
+    // (cst -> st).  Parts sharing the master's stream share its comm stream.  hcomm: a split of
+    // `comm` for the transfers on the comm stream (the same communicator when ncclCommSplit is missing).
+    cudaStream_t cst = nullptr;
+    bool own_cst = false;
+    cudaEvent_t evb = nullptr, evc = nullptr;
+    ncclComm_t hcomm = nullptr;
+    bool on_cst = false;  // master only: transports are being enqueued on the comm streams
     // general labelled domain (smg_create_labeled): fine-level cell labels, x fastest; empty: walled box
     std::vector<uint8_t> labels;
 
@@ -391,6 +402,13 @@ struct smg_ctx {
         if (init_graph) cudaGraphExecDestroy(init_graph);
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);
+        if (evb) cudaEventDestroy(evb);
+        if (evc) cudaEventDestroy(evc);
+        if (cst && own_cst) {
+            cudaStreamSynchronize(cst);
+            cudaStreamDestroy(cst);
+        }
+        if (hcomm && hcomm != comm) nccl().commDestroy(hcomm);
         if (comm) nccl().commDestroy(comm);
         if (st && own_stream) cudaStreamDestroy(st);
     }
@@ -1297,50 +1315,84 @@ bool shared_stream(smg_ctx* m) {
     return true;
 }
 
-// stream-order barrier across parts (no-op when all parts share one stream)
+// stream a transport of part p is enqueued on: the part's compute stream, or its comm stream
+// while the master context is in an overlapped phase (on_cst)
+cudaStream_t tstream(smg_ctx* m, smg_ctx* p) { return m->on_cst ? p->cst : p->st; }
+ncclComm_t tcomm(smg_ctx* m) { return m->on_cst ? m->hcomm : m->comm; }
+
+// stream-order barrier across parts (no-op when all parts share one stream), on the transport streams
 void part_barrier(smg_ctx* m) {
     if (shared_stream(m)) return;
     std::vector<cudaEvent_t> ev(m->parts.size());
     for (size_t k = 0; k < m->parts.size(); ++k) {
         CK(cudaSetDevice(m->parts[k]->device));
         CK(cudaEventCreateWithFlags(&ev[k], cudaEventDisableTiming));
-        CK(cudaEventRecord(ev[k], m->parts[k]->st));
+        CK(cudaEventRecord(ev[k], tstream(m, m->parts[k])));
     }
     for (size_t k = 0; k < m->parts.size(); ++k) {
         CK(cudaSetDevice(m->parts[k]->device));
         for (size_t j = 0; j < ev.size(); ++j)
-            if (j != k) CK(cudaStreamWaitEvent(m->parts[k]->st, ev[j], 0));
+            if (j != k) CK(cudaStreamWaitEvent(tstream(m, m->parts[k]), ev[j], 0));
     }
     for (auto e : ev) cudaEventDestroy(e);
     CK(cudaSetDevice(m->device));
 }
 
+// Comm streams and fork / join events of every part, and (one process per GPU) the halo
+// communicator: created at the first overlapped phase.
+void ensure_comm_streams(smg_ctx* m) {
+    if (m->cst) return;
+    for (smg_ctx* p : m->parts) {
+        CK(cudaSetDevice(p->device));
+        if (p != m && p->st == m->st) {
+            p->cst = m->cst;
+        } else {
+            CK(cudaStreamCreateWithFlags(&p->cst, cudaStreamNonBlocking));
+            p->own_cst = true;
+        }
+        CK(cudaEventCreateWithFlags(&p->evb, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&p->evc, cudaEventDisableTiming));
+    }
+    CK(cudaSetDevice(m->device));
+    if (m->mp && !m->hcomm) {
+        const NcclApi& N = nccl();
+        m->hcomm = m->comm;
+        if (N.commSplit) {
+            ncclComm_t h = nullptr;
+            if (N.commSplit(m->comm, 0, m->rank, &h, nullptr) == ncclSuccess && h) m->hcomm = h;
+        }
+    }
+}
+
 // multi-process halo exchange of this rank's slab vector `v` (geometry g, nf fields):
 // the same 2-plane transfers as the in-process copies below, as NCCL send/recv
-// pairs with the z neighbours (rank -+ 1), grouped into one launch on the part stream
-void halo_nccl(smg_ctx* m, double* v, const Geom& g, int nf) {
+// pairs with the z neighbours (rank -+ 1), grouped into one launch on the transport stream
+void halo_nccl(smg_ctx* m, double* v, const Geom& g, int nf, int f0 = 0) {
     const NcclApi& N = nccl();
     const size_t n2 = static_cast<size_t>(2 * g.sz);
+    cudaStream_t ts = tstream(m, m);
+    ncclComm_t cm = tcomm(m);
     NK(N.groupStart());
-    for (int f = 0; f < nf; ++f) {
+    for (int f = f0; f < f0 + nf; ++f) {
         double* a = v + f * g.fs;
         if (m->rank + 1 < m->nparts) {  // top halo (planes nz, nz+1) <-> upper part's planes 0, 1
-            NK(N.send(a + (g.zg + g.nz - 2) * g.sz, n2, ncclDouble, m->rank + 1, m->comm, m->st));
-            NK(N.recv(a + (g.zg + g.nz) * g.sz, n2, ncclDouble, m->rank + 1, m->comm, m->st));
+            NK(N.send(a + (g.zg + g.nz - 2) * g.sz, n2, ncclDouble, m->rank + 1, cm, ts));
+            NK(N.recv(a + (g.zg + g.nz) * g.sz, n2, ncclDouble, m->rank + 1, cm, ts));
         }
         if (m->rank > 0) {  // bottom halo (planes -2, -1) <-> lower part's planes nz-2, nz-1
-            NK(N.send(a + g.zg * g.sz, n2, ncclDouble, m->rank - 1, m->comm, m->st));
-            NK(N.recv(a, n2, ncclDouble, m->rank - 1, m->comm, m->st));
+            NK(N.send(a + g.zg * g.sz, n2, ncclDouble, m->rank - 1, cm, ts));
+            NK(N.recv(a, n2, ncclDouble, m->rank - 1, cm, ts));
         }
     }
     NK(N.groupEnd());
 }
 
-// halo exchange of a slab level: 2 planes each way between neighbours; nf fields
-void exchange(smg_ctx* m, int l, Sel sel, int nf) {
+// halo exchange of a slab level: 2 planes each way between neighbours; the nf fields from f0
+// (a phase that changed only some fields refreshes only those: the other halos are still current)
+void exchange(smg_ctx* m, int l, Sel sel, int nf, int f0 = 0) {
     Nvtx r("halo_exchange", l);
     if (m->mp) {
-        halo_nccl(m, sel(m->lv[l]), m->lv[l].k.g, nf);
+        halo_nccl(m, sel(m->lv[l]), m->lv[l].k.g, nf, f0);
         return;
     }
     part_barrier(m);
@@ -1348,12 +1400,13 @@ void exchange(smg_ctx* m, int l, Sel sel, int nf) {
         DevLevel &lo = m->parts[p]->lv[l], &hi = m->parts[p + 1]->lv[l];
         const Geom& g = lo.k.g;
         const size_t pitch = g.fs * sizeof(double), width = 2 * g.sz * sizeof(double);
+        double *vlo = sel(lo) + f0 * g.fs, *vhi = sel(hi) + f0 * g.fs;
         // lo top halo (planes nz, nz+1) <- hi owned planes 0, 1
-        CK(cudaMemcpy2DAsync(sel(lo) + (g.nz + g.zg) * g.sz, pitch, sel(hi) + g.zg * g.sz, pitch, width, nf,
-                             cudaMemcpyDefault, m->parts[p]->st));
+        CK(cudaMemcpy2DAsync(vlo + (g.nz + g.zg) * g.sz, pitch, vhi + g.zg * g.sz, pitch, width, nf,
+                             cudaMemcpyDefault, tstream(m, m->parts[p])));
         // hi bottom halo (planes -2, -1) <- lo owned planes nz-2, nz-1
-        CK(cudaMemcpy2DAsync(sel(hi), pitch, sel(lo) + g.nz * g.sz, pitch, width, nf, cudaMemcpyDefault,
-                             m->parts[p + 1]->st));
+        CK(cudaMemcpy2DAsync(vhi, pitch, vlo + g.nz * g.sz, pitch, width, nf, cudaMemcpyDefault,
+                             tstream(m, m->parts[p + 1])));
     }
     part_barrier(m);
 }
@@ -1432,22 +1485,24 @@ void push_ghosts(smg_ctx* m, int l, int T) {
     if (m->mp) {
         const NcclApi& N = nccl();
         const Geom& g = g0;
+        cudaStream_t ts = tstream(m, m);
+        ncclComm_t cm = tcomm(m);
         double* X = m->lv[l].x;
         const size_t n1 = static_cast<size_t>(g.sz);
         NK(N.groupStart());
         const int r = m->rank;
         if (r + 1 < m->nparts) {  // boundary with the upper part
             if (top_ran(r)) {
-                for (int f : {2, 3}) NK(N.send(X + f * g.fs + (g.zg + g.nz) * g.sz, n1, ncclDouble, r + 1, m->comm, m->st));
+                for (int f : {2, 3}) NK(N.send(X + f * g.fs + (g.zg + g.nz) * g.sz, n1, ncclDouble, r + 1, cm, ts));
             } else {
-                NK(N.recv(X + 3 * g.fs + (g.zg + g.nz - 1) * g.sz, n1, ncclDouble, r + 1, m->comm, m->st));
+                NK(N.recv(X + 3 * g.fs + (g.zg + g.nz - 1) * g.sz, n1, ncclDouble, r + 1, cm, ts));
             }
         }
         if (r > 0) {  // boundary with the lower part
             if (top_ran(r - 1)) {
-                for (int f : {2, 3}) NK(N.recv(X + f * g.fs + g.zg * g.sz, n1, ncclDouble, r - 1, m->comm, m->st));
+                for (int f : {2, 3}) NK(N.recv(X + f * g.fs + g.zg * g.sz, n1, ncclDouble, r - 1, cm, ts));
             } else {
-                NK(N.send(X + 3 * g.fs + (g.zg - 1) * g.sz, n1, ncclDouble, r - 1, m->comm, m->st));
+                NK(N.send(X + 3 * g.fs + (g.zg - 1) * g.sz, n1, ncclDouble, r - 1, cm, ts));
             }
         }
         NK(N.groupEnd());
@@ -1460,10 +1515,10 @@ void push_ghosts(smg_ctx* m, int l, int T) {
         const size_t pitch = g.fs * sizeof(double), width = g.sz * sizeof(double);
         if (top_ran(static_cast<int>(p))) {  // W, P of lo's ghost plane nz -> hi's plane 0
             CK(cudaMemcpy2DAsync(hi.x + 2 * g.fs + g.zg * g.sz, pitch, lo.x + 2 * g.fs + (g.zg + g.nz) * g.sz, pitch,
-                                 width, 2, cudaMemcpyDefault, m->parts[p + 1]->st));
+                                 width, 2, cudaMemcpyDefault, tstream(m, m->parts[p + 1])));
         } else {  // P of hi's ghost plane -1 -> lo's plane nz - 1
             CK(cudaMemcpyAsync(lo.x + 3 * g.fs + (g.zg + g.nz - 1) * g.sz, hi.x + 3 * g.fs + (g.zg - 1) * g.sz,
-                               width, cudaMemcpyDefault, m->parts[p]->st));
+                               width, cudaMemcpyDefault, tstream(m, m->parts[p])));
         }
     }
     part_barrier(m);
@@ -1473,10 +1528,41 @@ void dist_dgs_sym(smg_ctx* m, int l) {
     const int nph = (m->prm.flags & SMG_FLAG_SKIP_REVERSE_DGS) ? 10 : 20;
     each(m, [&](smg_ctx* p) { launch_dgs_cb(p->lv[l].k, p->lv[l].b, p->st); });  // b halos are valid here
     if (m->lv[l].k.tiled) {  // tile order (OD-1 rev. 2): one launch + one exchange per tile colour
+        // Overlap (SMG_DIST_OVERLAP, default on): the part's bottom and top tile layers first; their
+        // updates are all a halo transfer reads (owned planes 0, 1, nz - 2, nz - 1 and, for the push,
+        // the adjacent ghost plane), and what it writes (ghost planes, the pushed plane 0 / nz - 1) is
+        // out of reach of the layers in between (a tile reads at most 2 planes beyond its own 8).  So
+        // the transfer runs on the comm stream while the interior layers run on the compute stream;
+        // the next phase waits for both.  Same tiles, same arithmetic: bit-identical.
+        const bool overlap = !(std::getenv("SMG_DIST_OVERLAP") && std::atoi(std::getenv("SMG_DIST_OVERLAP")) == 0);  // read per sweep (tests)
+        const bool ov = overlap && m->lv[l].k.g.nz / dgs_tile_dim(2) >= 3;
+        if (ov) ensure_comm_streams(m);
         auto phase = [&](int T, int ph0, int ph1) {
-            each(m, [&](smg_ctx* p) { launch_dgs_tile_phases(p->lv[l].k, p->lv[l].x, p->lv[l].b, T, ph0, ph1, p->st); });
-            if (ph0 < 10) push_ghosts(m, l, T);
-            exchange(m, l, sel_x, 4);
+            if (!ov) {
+                each(m, [&](smg_ctx* p) { launch_dgs_tile_phases(p->lv[l].k, p->lv[l].x, p->lv[l].b, T, ph0, ph1, p->st); });
+                if (ph0 < 10) push_ghosts(m, l, T);
+                exchange(m, l, sel_x, 4);
+                return;
+            }
+            each(m, [&](smg_ctx* p) {
+                launch_dgs_tile_phases(p->lv[l].k, p->lv[l].x, p->lv[l].b, T, ph0, ph1, p->st, 1);
+                CK(cudaEventRecord(p->evb, p->st));
+                CK(cudaStreamWaitEvent(p->cst, p->evb, 0));
+            });
+            m->on_cst = true;
+            try {
+                if (ph0 < 10) push_ghosts(m, l, T);
+                exchange(m, l, sel_x, 4);
+            } catch (...) {
+                m->on_cst = false;
+                throw;
+            }
+            m->on_cst = false;
+            each(m, [&](smg_ctx* p) {
+                CK(cudaEventRecord(p->evc, p->cst));
+                launch_dgs_tile_phases(p->lv[l].k, p->lv[l].x, p->lv[l].b, T, ph0, ph1, p->st, 2);
+                CK(cudaStreamWaitEvent(p->st, p->evc, 0));
+            });
         };
         for (int T = 0; T < 8; ++T) phase(T, 0, (T == 7 && nph > 10) ? 20 : 10);
         if (nph > 10)
@@ -1484,9 +1570,11 @@ void dist_dgs_sym(smg_ctx* m, int l) {
         return;
     }
     for (int ph = 0; ph < nph; ++ph) {
+        int f0 = 0, nf = 4;  // fields the phase changed: velocity phases u, v, w; reverse pressure phases p
         if (ph == 0 || ph == 1 || ph == 18 || ph == 19) {
             const int col = ph < 2 ? ph : 19 - ph;
             each(m, [&](smg_ctx* p) { launch_dgs_vel_c(p->lv[l].k, p->lv[l].x, p->lv[l].b, col, p->st); });
+            nf = 3;
         } else if (ph <= 9) {
             const int c = ph - 2;
             Sel sd = (c & 1) ? sel_d1 : sel_d0;
@@ -1498,8 +1586,10 @@ void dist_dgs_sym(smg_ctx* m, int l) {
             each(m, [&](smg_ctx* p) { launch_dgs_pf_apply_c(p->lv[l].k, p->lv[l].x, sd(p->lv[l]), c, p->st); });
         } else {
             each(m, [&](smg_ctx* p) { launch_dgs_prev_c(p->lv[l].k, p->lv[l].x, p->lv[l].b, 17 - ph, p->st); });
+            f0 = 3;
+            nf = 1;
         }
-        exchange(m, l, sel_x, 4);
+        exchange(m, l, sel_x, nf, f0);
     }
 }
 
@@ -2080,6 +2170,7 @@ int smg_create_rank(const smg_grid_desc* grid, const smg_params* params, int ran
             std::memcpy(&u, id, sizeof(u));
             NK(nccl().commInitRank(&c->comm, nranks, u, rank));
             c->shared_partials = c->dalloc<double>(dot_partials(c->lv[0].k.g));
+            ensure_comm_streams(c.get());  // comm stream + halo communicator now, never inside a graph capture
         }
     });
     if (rc != 0) {

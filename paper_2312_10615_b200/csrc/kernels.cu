@@ -2298,7 +2298,7 @@ template <bool FWD>
 __global__ void __launch_bounds__(kTileThreads, 2)
     k_dgs_tile(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmb,
                const __grid_constant__ CUtensorMap tmc, LevelK L, double* __restrict__ X, int T, int ph0, int ph1,
-               int ntx, int nty, int pf) {
+               int ntx, int nty, int pf, int kz0, int kzs) {
     using TB = TileBox<FWD>;
     extern __shared__ __align__(128) double tsm_raw[];
     // 128-byte aligned by pointer arithmetic on the shared array (an integer round trip would hide
@@ -2315,7 +2315,10 @@ __global__ void __launch_bounds__(kTileThreads, 2)
     // pf < 0: this launch walks its tiles backwards, so it starts where the previous launch (the
     // neighbouring tile colour, walked forwards) ended -- on data still in L2
     const int bi = pf < 0 ? static_cast<int>(gridDim.x) - 1 - static_cast<int>(blockIdx.x) : static_cast<int>(blockIdx.x);
-    const int tx = 2 * (bi % hx) + (T & 1), ty = 2 * ((bi / hx) % hy) + ((T >> 1) & 1), tz = 2 * (bi / (hx * hy)) + pz;
+    // tile layers of this launch: the colour's layers kz0, kz0 + kzs, ... (all of them: 0, 1; a slab
+    // part's boundary / interior layers when the halo transfer overlaps the interior tiles)
+    const int tx = 2 * (bi % hx) + (T & 1), ty = 2 * ((bi / hx) % hy) + ((T >> 1) & 1),
+              tz = 2 * (kz0 + kzs * (bi / (hx * hy))) + pz;
     const int x0 = tx * kTX, y0 = ty * kTY, z0 = tz * kTZ;  // z0: local plane of the part
     if (tid == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)));
@@ -2333,7 +2336,7 @@ __global__ void __launch_bounds__(kTileThreads, 2)
         const int bn = bi + pf;
         if (pf > 0 && bn < static_cast<int>(gridDim.x)) {
             const int nx0 = (2 * (bn % hx) + (T & 1)) * kTX, ny0 = (2 * ((bn / hx) % hy) + ((T >> 1) & 1)) * kTY,
-                      nz0 = (2 * (bn / (hx * hy)) + pz) * kTZ;
+                      nz0 = (2 * (kz0 + kzs * (bn / (hx * hy))) + pz) * kTZ;
             tma_prefetch(&tmx, nx0 - 2 + g.xo, ny0, nz0 - 1 + g.zg, 0);
             tma_prefetch(&tmb, nx0 + g.xo, ny0 + 1, nz0 + g.zg, 0);
             if (!FWD) tma_prefetch(&tmc, nx0 + g.xo, ny0 + 1, nz0 + g.zg, 0);
@@ -3276,17 +3279,36 @@ static bool level_tmap(const Geom& g, const double* x, int nf, int bx, int by, i
 }
 
 // Phases [ph0, ph1) on the tiles of colour T (a range within one half: 0..9 or 10..19).
-void launch_dgs_tile_phases(const LevelK& L, double* x, const double* b, int T, int ph0, int ph1, cudaStream_t s) {
+// zsel: 0 = every tile layer of the part; 1 = only the part's bottom and top tile layers (the tiles
+// whose updates reach the 2 planes a halo exchange sends and the ghost planes a push reads);
+// 2 = only the layers in between (they touch nothing a halo transfer reads or writes: z-slab
+// parts run them while the transfer is in flight on the comm stream).
+void launch_dgs_tile_phases(const LevelK& L, double* x, const double* b, int T, int ph0, int ph1, cudaStream_t s,
+                            int zsel) {
     const Geom& g = L.g;
     const int ntx = g.nx / kTX, nty = g.ny / kTY, ntz = g.nz / kTZ;
     const int pz = ((T >> 2) ^ (g.z0 / kTZ)) & 1;
-    const int hx = (ntx - (T & 1) + 1) >> 1, hy = (nty - ((T >> 1) & 1) + 1) >> 1, hz = (ntz - pz + 1) >> 1;
+    const int hx = (ntx - (T & 1) + 1) >> 1, hy = (nty - ((T >> 1) & 1) + 1) >> 1;
+    int hz = (ntz - pz + 1) >> 1;  // layers of this colour: tz = pz, pz + 2, ...
     if (hx * hy * hz == 0 || ph1 <= ph0) return;
     const bool fwd = ph1 <= 10;
     if (!fwd && ph0 < 10) {  // split at the half boundary
-        launch_dgs_tile_phases(L, x, b, T, ph0, 10, s);
-        launch_dgs_tile_phases(L, x, b, T, 10, ph1, s);
+        launch_dgs_tile_phases(L, x, b, T, ph0, 10, s, zsel);
+        launch_dgs_tile_phases(L, x, b, T, 10, ph1, s, zsel);
         return;
+    }
+    int kz0 = 0, kzs = 1;
+    if (zsel != 0) {
+        const bool bot = pz == 0, top = hz > (bot ? 1 : 0) && ((ntz - 1 - pz) & 1) == 0;  // top != bottom layer
+        if (zsel == 1) {
+            kz0 = bot ? 0 : hz - 1;
+            kzs = hz > 1 ? hz - 1 : 1;
+            hz = (bot ? 1 : 0) + (top ? 1 : 0);
+        } else {
+            kz0 = bot ? 1 : 0;
+            hz -= (bot ? 1 : 0) + (top ? 1 : 0);
+        }
+        if (hz <= 0) return;
     }
     CUtensorMap mx, mb, mc;
     bool ok;
@@ -3324,16 +3346,16 @@ void launch_dgs_tile_phases(const LevelK& L, double* x, const double* b, int T, 
     static const int tile_pdl = env_int("SMG_TILE_PDL", 0);
     if (fwd && tile_pdl)
         launch_k(k_dgs_tile<true>, dim3(hx * hy * hz), dim3(kTileThreads), TileBox<true>::SMEM, s, mx, mb, mc, L, x, T,
-                 ph0, ph1, ntx, nty, pf);
+                 ph0, ph1, ntx, nty, pf, kz0, kzs);
     else if (fwd)
         launch_plain(k_dgs_tile<true>, dim3(hx * hy * hz), dim3(kTileThreads), TileBox<true>::SMEM, s, mx, mb, mc, L, x,
-                     T, ph0, ph1, ntx, nty, pf);
+                     T, ph0, ph1, ntx, nty, pf, kz0, kzs);
     else if (tile_pdl)
         launch_k(k_dgs_tile<false>, dim3(hx * hy * hz), dim3(kTileThreads), TileBox<false>::SMEM, s, mx, mb, mc, L, x,
-                 T, ph0, ph1, ntx, nty, pf);
+                 T, ph0, ph1, ntx, nty, pf, kz0, kzs);
     else
         launch_plain(k_dgs_tile<false>, dim3(hx * hy * hz), dim3(kTileThreads), TileBox<false>::SMEM, s, mx, mb, mc, L,
-                     x, T, ph0, ph1, ntx, nty, pf);
+                     x, T, ph0, ph1, ntx, nty, pf, kz0, kzs);
     count();
 }
 

@@ -169,7 +169,8 @@ void launch_apply_x(const LevelK& L, const double* x0, const double* d0, const d
 bool dgs_tiled(int nx, int ny, int nz, int64_t tile_min);
 int dgs_tile_dim(int axis);
 // phases [ph0, ph1) of the 20-phase numbering on the tiles of colour T
-void launch_dgs_tile_phases(const LevelK& L, double* x, const double* b, int T, int ph0, int ph1, cudaStream_t s);
+void launch_dgs_tile_phases(const LevelK& L, double* x, const double* b, int T, int ph0, int ph1, cudaStream_t s,
+                            int zsel = 0);
 // symmetric sweep (nph = 20) or forward half (nph = 10) in tile order; L.cb must hold m^T b
 void launch_dgs_tiled(const LevelK& L, double* x, const double* b, int nph, cudaStream_t s);
 // Single colour-compact DGS phases (used by the z-slab path).
