@@ -348,6 +348,8 @@ struct smg_ctx {
     cudaEvent_t evb = nullptr, evc = nullptr;
     ncclComm_t hcomm = nullptr;
     bool on_cst = false;  // master only: transports are being enqueued on the comm streams
+    // halo frames (exchange_frame): send up / send down / received from above / received from below
+    double* fbuf[4] = {nullptr, nullptr, nullptr, nullptr};
     // general labelled domain (smg_create_labeled): fine-level cell labels, x fastest; empty: walled box
     std::vector<uint8_t> labels;
 
@@ -1446,6 +1448,65 @@ void each(smg_ctx* m, F&& f) {
     CK(cudaSetDevice(m->device));
 }
 
+// Halo refresh after a Vanka phase on a slab level: the phase changed band DOFs only, which on the
+// exchanged planes is a frame along the x and y walls (kernels.cu k_frame_copy) unless the planes
+// are within reach of a z wall (thin slabs: the whole planes go).  Pack the frames of the 2 planes x
+// 4 fields, move them (NCCL send/recv or a peer copy), unpack into the ghost planes: ~1.5% of the
+// plane bytes at 512^2.  SMG_DIST_FRAMES=0 sends the planes.
+void exchange_frame(smg_ctx* m, int l) {
+    const Geom& g0 = m->lv[l].k.g;
+    const int bw = m->lv[l].k.bw;
+    const bool frames = !(std::getenv("SMG_DIST_FRAMES") && std::atoi(std::getenv("SMG_DIST_FRAMES")) == 0);
+    if (!frames || g0.nz < bw + 4 || g0.nx < 4 * (bw + 2) || g0.ny < 4 * (bw + 2)) {
+        exchange(m, l, sel_x, 4);
+        return;
+    }
+    Nvtx r("halo_frames", l);
+    if (!m->fbuf[0]) {  // sized for the finest level (the largest planes)
+        each(m, [&](smg_ctx* p) {
+            const int64_t n = frame_doubles(p->lv[0].k.g, p->lv[0].k.bw);
+            for (double*& b : p->fbuf) b = p->dalloc<double>(n);
+        });
+    }
+    const int64_t n = frame_doubles(g0, bw);
+    const int P = m->nparts;
+    auto pack = [&](smg_ctx* p) {  // top planes nz-2, nz-1 -> fbuf[0]; bottom planes 0, 1 -> fbuf[1]
+        const Geom& g = p->lv[l].k.g;
+        if (p->rank + 1 < P) launch_frame_copy(g, bw, p->lv[l].x, p->fbuf[0], g.zg + g.nz - 2, true, p->st);
+        if (p->rank > 0) launch_frame_copy(g, bw, p->lv[l].x, p->fbuf[1], g.zg, true, p->st);
+    };
+    auto unpack = [&](smg_ctx* p) {  // fbuf[2] -> ghost planes nz, nz+1; fbuf[3] -> ghost planes -2, -1
+        const Geom& g = p->lv[l].k.g;
+        if (p->rank + 1 < P) launch_frame_copy(g, bw, p->lv[l].x, p->fbuf[2], g.zg + g.nz, false, p->st);
+        if (p->rank > 0) launch_frame_copy(g, bw, p->lv[l].x, p->fbuf[3], 0, false, p->st);
+    };
+    if (m->mp) {
+        const NcclApi& N = nccl();
+        pack(m);
+        NK(N.groupStart());
+        if (m->rank + 1 < P) {
+            NK(N.send(m->fbuf[0], static_cast<size_t>(n), ncclDouble, m->rank + 1, m->comm, m->st));
+            NK(N.recv(m->fbuf[2], static_cast<size_t>(n), ncclDouble, m->rank + 1, m->comm, m->st));
+        }
+        if (m->rank > 0) {
+            NK(N.send(m->fbuf[1], static_cast<size_t>(n), ncclDouble, m->rank - 1, m->comm, m->st));
+            NK(N.recv(m->fbuf[3], static_cast<size_t>(n), ncclDouble, m->rank - 1, m->comm, m->st));
+        }
+        NK(N.groupEnd());
+        unpack(m);
+        return;
+    }
+    each(m, pack);
+    part_barrier(m);
+    for (size_t q = 0; q + 1 < m->parts.size(); ++q) {
+        smg_ctx *lo = m->parts[q], *hi = m->parts[q + 1];
+        CK(cudaMemcpyAsync(hi->fbuf[3], lo->fbuf[0], n * sizeof(double), cudaMemcpyDefault, hi->st));
+        CK(cudaMemcpyAsync(lo->fbuf[2], hi->fbuf[1], n * sizeof(double), cudaMemcpyDefault, lo->st));
+    }
+    each(m, unpack);
+    part_barrier(m);  // the next pack must not overwrite a frame a neighbour is still copying
+}
+
 // Symmetric multiplicative Vanka on a slab level: the merged complementary colour pairs of the
 // single-part sweep (8 Jacobi phases instead of 16 when all four pairs pay, bit-identical), one halo
 // exchange per phase.  The pair decision depends on the level's global list sizes only through
@@ -1466,7 +1527,7 @@ void dist_vanka_sym(smg_ctx* m, int l) {
                 launch_vanka_apply(L.k, L.x, L.sw_cells[col], L.sw_mask[col], L.sw_n[col], p->vk_delta, p->st,
                                    L.sw_amask[col]);
             });
-            exchange(m, l, sel_x, 4);
+            exchange_frame(m, l);
         }
 }
 

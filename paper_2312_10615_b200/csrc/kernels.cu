@@ -2429,6 +2429,58 @@ __global__ void __launch_bounds__(kTileThreads, 2)
     }
 }
 
+// ------------------------------------------ z-slab halo frames ------
+// A Vanka phase changes only band DOFs.  On the two boundary planes of a z-slab that is a frame
+// around the plane's perimeter (rows / columns within bw + 1 slots of the x and y walls) as long as
+// the planes are not themselves within reach of a z wall, so the halo refresh after a Vanka phase
+// moves the frames of the 2 planes x 4 fields (a few 10 KB at 512^2) instead of the planes.
+// Frame of one padded plane (py rows of px columns): rows [0, RL) and [py - RH, py) whole, and of
+// the rows in between the columns [0, CL) and [px - CH, px).
+struct FrameDims {
+    int RL, RH, CL, CH, px, py;
+    __host__ __device__ int mid_rows() const { return py - RL - RH; }
+    __host__ __device__ int64_t count() const {
+        return static_cast<int64_t>(RL + RH) * px + static_cast<int64_t>(mid_rows()) * (CL + CH);
+    }
+};
+static FrameDims frame_dims(const Geom& g, int bw) {
+    FrameDims f;
+    f.px = g.px;
+    f.py = g.py;
+    f.RL = bw + 2;                      // y slots -1 .. bw (a block at cell y updates faces y and y + 1)
+    f.RH = bw + 1;                      // y slots ny - bw .. ny
+    f.CL = g.xo + bw + 1;               // x slots .. bw
+    f.CH = g.px - g.xo - g.nx + bw;     // x slots nx - bw ..
+    return f;
+}
+// to_buf: buf <- frames of the padded planes zs, zs + 1 of the 4 fields; else the reverse
+__global__ void __launch_bounds__(256) k_frame_copy(Geom g, FrameDims f, double* __restrict__ X,
+                                                    double* __restrict__ buf, int zs, int to_buf) {
+    const int64_t n = f.count();
+    const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (e >= n) return;
+    int row, col;
+    const int64_t top = static_cast<int64_t>(f.RL) * f.px, bot = static_cast<int64_t>(f.RH) * f.px;
+    if (e < top) {
+        row = static_cast<int>(e / f.px);
+        col = static_cast<int>(e % f.px);
+    } else if (e < top + bot) {
+        row = f.py - f.RH + static_cast<int>((e - top) / f.px);
+        col = static_cast<int>((e - top) % f.px);
+    } else {
+        const int64_t r = e - top - bot;
+        const int w = f.CL + f.CH, c = static_cast<int>(r % w);
+        row = f.RL + static_cast<int>(r / w);
+        col = c < f.CL ? c : f.px - f.CH + (c - f.CL);
+    }
+    const int pf = blockIdx.y;  // plane (0, 1) x field (0..3)
+    const int64_t xi = static_cast<int64_t>(pf >> 1) * g.fs + static_cast<int64_t>(zs + (pf & 1)) * g.sz +
+                       static_cast<int64_t>(row) * g.sy + col;
+    double* b = buf + static_cast<int64_t>(pf) * n + e;
+    if (to_buf) *b = X[xi];
+    else X[xi] = *b;
+}
+
 // ------------------------------------------ general labelled domains ------
 // SPEC:17-97 (domain), 124/176 (dropped Neumann legs), 245-251 (Vanka signature classes):
 // Dirichlet / Interior / Exterior cells inside the implicit Dirichlet ring.  The padded layout is
@@ -3384,6 +3436,15 @@ void launch_vanka_additive(const LevelK& L, double* x, const double* b, const in
 
 void launch_axpy_s(double* s_, const double* t, const double* sc, int64_t n, cudaStream_t s) {
     launch_k(k_axpy_s, stream_blocks(n), 256, 0, s, s_, t, sc, n);
+    count();
+}
+// Frame of the two padded planes zs, zs + 1 (all four fields) of a slab vector <-> a contiguous
+// buffer of frame_doubles(g, bw) doubles (z-slab halo refresh after a Vanka phase).
+int64_t frame_doubles(const Geom& g, int bw) { return 8 * frame_dims(g, bw).count(); }
+void launch_frame_copy(const Geom& g, int bw, double* x, double* buf, int zs, bool to_buf, cudaStream_t s) {
+    const FrameDims f = frame_dims(g, bw);
+    const dim3 grid(static_cast<unsigned>((f.count() + 255) / 256), 8);
+    k_frame_copy<<<grid, 256, 0, s>>>(g, f, x, buf, zs, to_buf ? 1 : 0);
     count();
 }
 void launch_axpy(double* y, const double* x, double alpha, int64_t n, cudaStream_t s) {

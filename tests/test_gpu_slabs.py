@@ -35,6 +35,25 @@ def test_sqmr_bitwise(n, levels, parts, kind):
     many.close()
 
 
+@pytest.mark.parametrize("n,levels,parts,bw", [(64, 4, 2, 1), (64, 4, 4, 2), (64, 4, 8, 2), (32, 3, 4, 3)])
+def test_vanka_halo_frames_bitwise(n, levels, parts, bw, monkeypatch):
+    """After a Vanka phase a slab level refreshes only the frames of its boundary planes (the band
+    DOFs along the x and y walls; host.cpp exchange_frame) unless the slab is too thin (whole
+    planes): both == one part, for band widths 1-3 (thin-slab fallback at 32^3 / 4 parts, bw 3)."""
+    one = smg.Solver(n, levels=levels, band_width=bw)
+    b = smg.forcing(n, kind=smg.FORCE_UNIFORM, seed=20 + parts)
+    v1 = one.vcycle(b)
+    x1, h1, _, s1 = one.sqmr(b, 1e-8, 60)
+    one.close()
+    for fr in ("1", "0"):
+        monkeypatch.setenv("SMG_DIST_FRAMES", fr)
+        many = smg.Solver(n, levels=levels, band_width=bw, devices=[0] * parts)
+        assert np.array_equal(many.vcycle(b), v1), fr
+        x2, h2, _, s2 = many.sqmr(b, 1e-8, 60)
+        assert s1 == s2 and np.array_equal(h1, h2) and np.array_equal(x1, x2), fr
+        many.close()
+
+
 @pytest.mark.parametrize("n,levels,parts", [(48, 5, 2), (48, 4, 4)])
 def test_odd_slab_levels_bitwise(n, levels, parts):
     """Levels whose slab would be odd stay replicated: 48^3 with 5 levels on 2 parts
