@@ -1452,12 +1452,17 @@ void each(smg_ctx* m, F&& f) {
 // exchanged planes is a frame along the x and y walls (kernels.cu k_frame_copy) unless the planes
 // are within reach of a z wall (thin slabs: the whole planes go).  Pack the frames of the 2 planes x
 // 4 fields, move them (NCCL send/recv or a peer copy), unpack into the ghost planes: ~1.5% of the
-// plane bytes at 512^2.  SMG_DIST_FRAMES=0 sends the planes.
+// plane bytes at 512^2.
 void exchange_frame(smg_ctx* m, int l) {
     const Geom& g0 = m->lv[l].k.g;
     const int bw = m->lv[l].k.bw;
-    const bool frames = !(std::getenv("SMG_DIST_FRAMES") && std::atoi(std::getenv("SMG_DIST_FRAMES")) == 0);
-    if (!frames || g0.nz < bw + 4 || g0.nx < 4 * (bw + 2) || g0.ny < 4 * (bw + 2)) {
+    // SMG_DIST_FRAMES: 0 = never, 2 = wherever the geometry allows (tests), default: where the planes
+    // are large enough for the saved transfer to pay for the pack and unpack launches (>= 2 MiB per
+    // direction, i.e. planes from about 180^2 slots: ~2 us at NVLink speed against ~3 us of launches
+    // plus the ~10 us either message costs)
+    const int mode = std::getenv("SMG_DIST_FRAMES") ? std::atoi(std::getenv("SMG_DIST_FRAMES")) : 1;
+    const bool large = 8 * g0.sz * static_cast<int64_t>(sizeof(double)) >= (int64_t{2} << 20);
+    if (mode == 0 || (mode == 1 && !large) || g0.nz < bw + 4 || g0.nx < 4 * (bw + 2) || g0.ny < 4 * (bw + 2)) {
         exchange(m, l, sel_x, 4);
         return;
     }

@@ -45,7 +45,7 @@ def test_vanka_halo_frames_bitwise(n, levels, parts, bw, monkeypatch):
     v1 = one.vcycle(b)
     x1, h1, _, s1 = one.sqmr(b, 1e-8, 60)
     one.close()
-    for fr in ("1", "0"):
+    for fr in ("2", "0"):  # 2: frames wherever the geometry allows (default: large planes only)
         monkeypatch.setenv("SMG_DIST_FRAMES", fr)
         many = smg.Solver(n, levels=levels, band_width=bw, devices=[0] * parts)
         assert np.array_equal(many.vcycle(b), v1), fr
