@@ -455,8 +455,12 @@ def roofline(s, levels, peak, peak_kind, iter_ms, config_key=None, share=1.0):
     if share != 1.0:  # one rank of a z-slab run: its kernels cover its share of the fine level
         v1, v2, n0 = v1 * share, v2 * share, n0 * share
     reps = 5
-    smooth_ms = s.time_kernel(5, reps, 0)
-    dgs_ms = s.time_kernel(2, reps, 0)
+    # As the V-cycle runs them: the m^T b pass k_dgs_cb (on a tiled level it also writes the tile-major
+    # copy of b the tiles stage from) runs ONCE per level visit and serves the visit's two smooths, so
+    # a sweep / a smooth carries half of it.
+    cb_ms = s.time_kernel(12, reps, 0)
+    smooth_ms = s.time_kernel(14, reps, 0) + cb_ms / 2
+    dgs_ms = s.time_kernel(13, reps, 0) + cb_ms / 2
     vanka_ms = s.time_kernel(4, reps, 0)
     apply_ms = s.time_kernel(0, 20, 0)
     alg_smooth = 48 * v2 + 96 * v1
@@ -475,16 +479,16 @@ def roofline(s, levels, peak, peak_kind, iter_ms, config_key=None, share=1.0):
             div = rec.get("component_launches_in_range", 1)
             dgs = [v["dram_bytes"] for k, v in rec["per_kernel_in_range"].items() if "k_dgs_" in k]
             traffic = sum(dgs) / div if dgs else None
-    nl = 17 if tiled else 14
+    nl = 16.5 if tiled else 13.5  # launches per sweep: the step kernels + half a k_dgs_cb
     return {
         "bound": "hbm",
-        "kernel": ("k_dgs_tile: fine-level symmetric DGS sweep in tile order (k_dgs_cb + 16 TMA-staged launches)"
-                   if tiled else "fine-level symmetric DGS sweep (k_dgs_cb + 13 per-step kernels)"),
+        "kernel": ("k_dgs_tile: fine-level symmetric DGS sweep in tile order (16 TMA-staged launches + half of the level visit's k_dgs_cb)"
+                   if tiled else "fine-level symmetric DGS sweep (13 per-step kernels + half of the level visit's k_dgs_cb)"),
         "achieved": achieved, "peak": peak, "peak_source": peak_kind, "unit": "GB/s", "frac": achieved / peak,
         "traffic": traffic,
         "traffic_source": "ncu dram__bytes_read+write of the sweep's kernels (cold caches), profiles/smooth_traffic.json",
         "algorithmic_bytes_per_launch": alg / nl, "avg_launch_ms": dgs_ms / nl, "launches_per_sweep": nl,
-        "algorithmic_bytes_per_sweep": alg, "avg_ms": dgs_ms,
+        "algorithmic_bytes_per_sweep": alg, "avg_ms": dgs_ms, "k_dgs_cb_ms_per_level_visit": cb_ms,
         "units": {"N_V2": v2, "N_V1": v1, "bytes_per_V2_dof": 48, "bytes_per_V1_dof": 96},
         "components": {
             "smooth_alg3": {"avg_ms": smooth_ms, "alg_bytes": alg_smooth,

@@ -204,7 +204,9 @@ int smg_last_timing(const smg_ctx* ctx, smg_timing* out);
  * on the solver stream, average ms per launch).  which: 0 apply L, 1 residual,
  * 2 symmetric DGS sweep (20 phases), 3 V-cycle from this level, 4 symmetric
  * Vanka sweep(s), 5 smooth (Alg. 3), 6 restrict, 7 prolong-add, 8 coarse
- * solve, 9 fused pair of inner products, 10 axpy, 11 one SQMR iteration graph. */
+ * solve, 9 fused pair of inner products, 10 axpy, 11 one SQMR iteration graph,
+ * 12 the once-per-level-visit m^T b pass (on tiled levels also the tile-major copy
+ * of b), 13 / 14 the DGS sweep / the smooth as a V-cycle runs them (12 done before). */
 int smg_time_kernel(smg_ctx* ctx, int which, int level, int reps, double* avg_ms);
 
 /* Debug aid (compute-sanitizer is not available on every GPU pool): with SMG_GUARD=1 in the

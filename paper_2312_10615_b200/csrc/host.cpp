@@ -893,6 +893,7 @@ void build(smg_ctx* c, const std::vector<double>* shared_coarse = nullptr, std::
         L.pd0 = c->dalloc<double>(L.k.g.fs);
         L.pd1 = c->dalloc<double>(L.k.g.fs);
         L.k.cb = c->dalloc<double>(L.k.g.fs);
+        if (L.k.tiled) L.k.bp = c->dalloc<double>(static_cast<int64_t>(5) * L.k.g.nx * L.k.g.ny * L.k.g.nz);
         if (labeled) {
             if (l > 0) lab = coarsen_labels(lab, nx * 2, ny * 2, nz * 2);
             build_level_labeled(c, l, lab, max_vk);
@@ -1199,7 +1200,7 @@ void symmetric_dgs(smg_ctx* c, int l, double* x, const double* b, bool cb_ready 
         return;
     }
     if (L.k.tiled) {
-        launch_dgs_tiled(L.k, x, b, nph, c->st);
+        launch_dgs_tiled(L.k, x, b, nph, c->st, /*packed=*/cb_ready || nph > kDgsPhases / 2);
         return;
     }
     launch_dgs_sym_coop(L.k, x, b, L.pd0, L.pd1, nph, c->st, L.xb);
@@ -1605,13 +1606,13 @@ void dist_dgs_sym(smg_ctx* m, int l) {
         if (ov) ensure_comm_streams(m);
         auto phase = [&](int T, int ph0, int ph1) {
             if (!ov) {
-                each(m, [&](smg_ctx* p) { launch_dgs_tile_phases(p->lv[l].k, p->lv[l].x, p->lv[l].b, T, ph0, ph1, p->st); });
+                each(m, [&](smg_ctx* p) { launch_dgs_tile_phases(p->lv[l].k, p->lv[l].x, p->lv[l].b, T, ph0, ph1, p->st, 0, true); });
                 if (ph0 < 10) push_ghosts(m, l, T);
                 exchange(m, l, sel_x, 4);
                 return;
             }
             each(m, [&](smg_ctx* p) {
-                launch_dgs_tile_phases(p->lv[l].k, p->lv[l].x, p->lv[l].b, T, ph0, ph1, p->st, 1);
+                launch_dgs_tile_phases(p->lv[l].k, p->lv[l].x, p->lv[l].b, T, ph0, ph1, p->st, 1, true);
                 CK(cudaEventRecord(p->evb, p->st));
                 CK(cudaStreamWaitEvent(p->cst, p->evb, 0));
             });
@@ -1626,7 +1627,7 @@ void dist_dgs_sym(smg_ctx* m, int l) {
             m->on_cst = false;
             each(m, [&](smg_ctx* p) {
                 CK(cudaEventRecord(p->evc, p->cst));
-                launch_dgs_tile_phases(p->lv[l].k, p->lv[l].x, p->lv[l].b, T, ph0, ph1, p->st, 2);
+                launch_dgs_tile_phases(p->lv[l].k, p->lv[l].x, p->lv[l].b, T, ph0, ph1, p->st, 2, true);
                 CK(cudaStreamWaitEvent(p->st, p->evc, 0));
             });
         };
@@ -2525,9 +2526,13 @@ int smg_time_kernel(smg_ctx* c, int which, int level, int reps, double* avg_ms) 
                     if (!c->graph) throw SmgError(SMG_EINVAL, "no SQMR graph captured yet");
                     CK(cudaGraphLaunch(c->graph, c->st));
                     break;
+                case 12: launch_dgs_cb(L.k, L.b, c->st); break;  // m^T b (+ the tile-major copy of b) of a level visit
+                case 13: symmetric_dgs(c, level, L.x, L.b, /*cb_ready=*/true); break;  // the sweep as the V-cycle runs it
+                case 14: smooth(c, level, L.x, L.b, /*cb_ready=*/true); break;
                 default: throw SmgError(SMG_EINVAL, "bad kernel id");
             }
         };
+        if (which == 13 || which == 14) launch_dgs_cb(L.k, L.b, c->st);
         one();
         CK(cudaEventRecord(c->ev0, c->st));
         for (int k = 0; k < reps; ++k) one();

@@ -217,6 +217,13 @@ __global__ void k_dgs_prev(LevelK L, double* __restrict__ X, const double* __res
 
 // c_b = m_C^T b: the b part of the reverse pressure update, same operation order as
 // the L~x part in prev_value (faces right - left in x, y, z; 6 r_C - neighbours x-, x+, ...).
+// PACK (tiled levels): also L.bp, the level's b and c_b in tile-major order -- per 16 x 8 x 8 tile
+// (x fastest) 5 blocks of 1024 doubles: b_u, b_v, b_w, b_p in the tile kernel's x-parity-split row
+// order (tile_bi) and c_b in natural order (tile_ti), 40 KB contiguous.  b is fixed during a level
+// visit while k_dgs_tile stages a tile's b 32 times (2 smooths x 16 launches): from the padded level
+// vector every 128-byte tile row straddles two DRAM lines (2x over-fetch); from L.bp it is one
+// contiguous bulk copy, already split.
+template <bool PACK>
 __global__ void k_dgs_cb(LevelK L, const double* __restrict__ B, double* __restrict__ CB) {
     pdl_wait();
     Cell c;
@@ -230,7 +237,18 @@ __global__ void k_dgs_cb(LevelK L, const double* __restrict__ B, double* __restr
     s = s + BP[i + sy];
     s = s + BP[i - sz];
     s = s + BP[i + sz];
-    CB[i] = fl * L.inv_h + L.eta_h2 * (6.0 * BP[i] - s);
+    const double cb = fl * L.inv_h + L.eta_h2 * (6.0 * BP[i] - s);
+    CB[i] = cb;
+    if (PACK) {
+        const int tx = c.x >> 4, ty = c.y >> 3, tz = c.z >> 3, lx = c.x & 15, ly = c.y & 7, lz = c.z & 7;
+        double* t = L.bp + (static_cast<int64_t>(tz * (g.ny >> 3) + ty) * (g.nx >> 4) + tx) * 5120;
+        const int bi = ((lz * 8 + ly) << 4) + (lx & 1) * 8 + (lx >> 1);
+        t[bi] = BU[i];
+        t[1024 + bi] = BV[i];
+        t[2048 + bi] = BW[i];
+        t[3072 + bi] = BP[i];
+        t[4096 + (lz * 8 + ly) * 16 + lx] = cb;
+    }
 }
 
 __global__ void k_vanka_apply(LevelK L, double* __restrict__ X, const int32_t* __restrict__ cells,
@@ -2281,6 +2299,14 @@ __device__ __forceinline__ void tma_load(void* dst, const CUtensorMap* m, int c0
         : "memory");
 }
 
+// contiguous global -> shared bulk copy against the same mbarrier (16-byte aligned, size % 16 == 0)
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
 // L2 prefetch of a box (no shared-memory destination, no barrier): a hint only, always safe
 __device__ __forceinline__ void tma_prefetch(const CUtensorMap* m, int c0, int c1, int c2, int c3) {
     asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];" ::"l"(
@@ -2298,7 +2324,7 @@ template <bool FWD>
 __global__ void __launch_bounds__(kTileThreads, 2)
     k_dgs_tile(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmb,
                const __grid_constant__ CUtensorMap tmc, LevelK L, double* __restrict__ X, int T, int ph0, int ph1,
-               int ntx, int nty, int pf, int kz0, int kzs) {
+               int ntx, int nty, int pf, int kz0, int kzs, const double* __restrict__ bpk) {
     using TB = TileBox<FWD>;
     extern __shared__ __align__(128) double tsm_raw[];
     // 128-byte aligned by pointer arithmetic on the shared array (an integer round trip would hide
@@ -2331,8 +2357,14 @@ __global__ void __launch_bounds__(kTileThreads, 2)
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                      : "memory");
         tma_load(xs, &tmx, x0 - 2 + g.xo, y0, z0 - 1 + g.zg, 0, bar);
-        tma_load(bs, &tmb, x0 + g.xo, y0 + 1, z0 + g.zg, 0, bar);
-        if (!FWD) tma_load(ts, &tmc, x0 + g.xo, y0 + 1, z0 + g.zg, 0, bar);
+        if (bpk) {  // tile-major packed b / c_b (k_dgs_cb<true>): contiguous, already parity-split
+            const double* tb = bpk + (static_cast<int64_t>(tz * (g.ny / kTY) + ty) * ntx + tx) * (5 * kTileCells);
+            bulk_load(bs, tb, TB::NB * kTileCells * sizeof(double), bar);
+            if (!FWD) bulk_load(ts, tb + 4 * kTileCells, kTileCells * sizeof(double), bar);
+        } else {
+            tma_load(bs, &tmb, x0 + g.xo, y0 + 1, z0 + g.zg, 0, bar);
+            if (!FWD) tma_load(ts, &tmc, x0 + g.xo, y0 + 1, z0 + g.zg, 0, bar);
+        }
         const int bn = bi + pf;
         if (pf > 0 && bn < static_cast<int>(gridDim.x)) {
             const int nx0 = (2 * (bn % hx) + (T & 1)) * kTX, ny0 = (2 * ((bn / hx) % hy) + ((T >> 1) & 1)) * kTY,
@@ -2369,7 +2401,7 @@ __global__ void __launch_bounds__(kTileThreads, 2)
             __syncwarp();
         }
         constexpr int BROWS = TB::NB * kTZ * kTY;  // rows of 16: 4 rows of 8 pairs per warp step
-        for (int r0 = warp * 4; r0 < BROWS; r0 += 32) {
+        for (int r0 = warp * 4; r0 < (bpk ? 0 : BROWS); r0 += 32) {
             const int r = r0 + (lane >> 3), q = lane & 7;
             const bool ok = r < BROWS;
             double2 v = make_double2(0.0, 0.0);
@@ -2853,7 +2885,8 @@ void launch_dgs_papply(const LevelK& L, double* x, const double* delta, cudaStre
     count();
 }
 void launch_dgs_cb(const LevelK& L, const double* b, cudaStream_t s) {
-    launch_k(k_dgs_cb, cell_grid(L.g), dim3(BX, BY), 0, s, L, b, L.cb);
+    if (L.bp) launch_k(k_dgs_cb<true>, cell_grid(L.g), dim3(BX, BY), 0, s, L, b, L.cb);
+    else launch_k(k_dgs_cb<false>, cell_grid(L.g), dim3(BX, BY), 0, s, L, b, L.cb);
     count();
 }
 void launch_dgs_prev(const LevelK& L, double* x, const double* b, int colour, cudaStream_t s) {
@@ -3335,8 +3368,9 @@ static bool level_tmap(const Geom& g, const double* x, int nf, int bx, int by, i
 // whose updates reach the 2 planes a halo exchange sends and the ghost planes a push reads);
 // 2 = only the layers in between (they touch nothing a halo transfer reads or writes: z-slab
 // parts run them while the transfer is in flight on the comm stream).
+// packed: L.bp holds this b (launch_dgs_cb ran on it): the tiles stage b / c_b from there.
 void launch_dgs_tile_phases(const LevelK& L, double* x, const double* b, int T, int ph0, int ph1, cudaStream_t s,
-                            int zsel) {
+                            int zsel, bool packed) {
     const Geom& g = L.g;
     const int ntx = g.nx / kTX, nty = g.ny / kTY, ntz = g.nz / kTZ;
     const int pz = ((T >> 2) ^ (g.z0 / kTZ)) & 1;
@@ -3345,8 +3379,8 @@ void launch_dgs_tile_phases(const LevelK& L, double* x, const double* b, int T, 
     if (hx * hy * hz == 0 || ph1 <= ph0) return;
     const bool fwd = ph1 <= 10;
     if (!fwd && ph0 < 10) {  // split at the half boundary
-        launch_dgs_tile_phases(L, x, b, T, ph0, 10, s, zsel);
-        launch_dgs_tile_phases(L, x, b, T, 10, ph1, s, zsel);
+        launch_dgs_tile_phases(L, x, b, T, ph0, 10, s, zsel, packed);
+        launch_dgs_tile_phases(L, x, b, T, 10, ph1, s, zsel, packed);
         return;
     }
     int kz0 = 0, kzs = 1;
@@ -3396,27 +3430,30 @@ void launch_dgs_tile_phases(const LevelK& L, double* x, const double* b, int T, 
     // colour's CTAs take the SM's shared memory slots early and the cfg-2 fine sweep measured
     // 2.185 ms against 2.04 ms without (round 2, session 5)
     static const int tile_pdl = env_int("SMG_TILE_PDL", 0);
+    // SMG_TILE_BPACK=0: stage b from the level vector even when the packed copy is valid (A/B, tests)
+    const char* bpe = std::getenv("SMG_TILE_BPACK");
+    const double* bpk = (packed && L.bp && !(bpe && std::atoi(bpe) == 0)) ? L.bp : nullptr;
     if (fwd && tile_pdl)
         launch_k(k_dgs_tile<true>, dim3(hx * hy * hz), dim3(kTileThreads), TileBox<true>::SMEM, s, mx, mb, mc, L, x, T,
-                 ph0, ph1, ntx, nty, pf, kz0, kzs);
+                 ph0, ph1, ntx, nty, pf, kz0, kzs, bpk);
     else if (fwd)
         launch_plain(k_dgs_tile<true>, dim3(hx * hy * hz), dim3(kTileThreads), TileBox<true>::SMEM, s, mx, mb, mc, L, x,
-                     T, ph0, ph1, ntx, nty, pf, kz0, kzs);
+                     T, ph0, ph1, ntx, nty, pf, kz0, kzs, bpk);
     else if (tile_pdl)
         launch_k(k_dgs_tile<false>, dim3(hx * hy * hz), dim3(kTileThreads), TileBox<false>::SMEM, s, mx, mb, mc, L, x,
-                 T, ph0, ph1, ntx, nty, pf, kz0, kzs);
+                 T, ph0, ph1, ntx, nty, pf, kz0, kzs, bpk);
     else
         launch_plain(k_dgs_tile<false>, dim3(hx * hy * hz), dim3(kTileThreads), TileBox<false>::SMEM, s, mx, mb, mc, L,
-                     x, T, ph0, ph1, ntx, nty, pf, kz0, kzs);
+                     x, T, ph0, ph1, ntx, nty, pf, kz0, kzs, bpk);
     count();
 }
 
 // Symmetric sweep (nph = 20) or its forward half (nph = 10): tile colours 0..7 forward, then
 // 7..0 reverse (16 launches; the two halves use different kernel variants).
-void launch_dgs_tiled(const LevelK& L, double* x, const double* b, int nph, cudaStream_t s) {
-    for (int T = 0; T < 8; ++T) launch_dgs_tile_phases(L, x, b, T, 0, 10, s);
+void launch_dgs_tiled(const LevelK& L, double* x, const double* b, int nph, cudaStream_t s, bool packed) {
+    for (int T = 0; T < 8; ++T) launch_dgs_tile_phases(L, x, b, T, 0, 10, s, 0, packed);
     if (nph <= 10) return;
-    for (int T = 7; T >= 0; --T) launch_dgs_tile_phases(L, x, b, T, 10, 20, s);
+    for (int T = 7; T >= 0; --T) launch_dgs_tile_phases(L, x, b, T, 10, 20, s, 0, packed);
 }
 
 void launch_vanka_additive(const LevelK& L, double* x, const double* b, const int32_t* cells, const uint8_t* masks,

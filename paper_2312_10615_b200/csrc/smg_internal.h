@@ -70,6 +70,8 @@ struct LevelK {
     // c_b = m_C^T b per cell (the b part of the reverse DGS pressure update, fixed while b
     // is): launch_dgs_cb fills it before a sweep; prev steps then read L~x only
     double* cb = nullptr;
+    // tiled levels: b and c_b in tile-major order (5 x 1024 doubles per tile), filled by launch_dgs_cb
+    double* bp = nullptr;
     int tiled = 0;  // DGS sweep in tile order (OD-1 rev. 2, dgs_tiled)
     // General labelled domain: per cell slot (one field long, ghosts 0) the DofMap
     // bits CLS_* of the cell's pressure and its three low faces; nullptr on the walled box,
@@ -170,9 +172,9 @@ bool dgs_tiled(int nx, int ny, int nz, int64_t tile_min);
 int dgs_tile_dim(int axis);
 // phases [ph0, ph1) of the 20-phase numbering on the tiles of colour T
 void launch_dgs_tile_phases(const LevelK& L, double* x, const double* b, int T, int ph0, int ph1, cudaStream_t s,
-                            int zsel = 0);
+                            int zsel = 0, bool packed = false);
 // symmetric sweep (nph = 20) or forward half (nph = 10) in tile order; L.cb must hold m^T b
-void launch_dgs_tiled(const LevelK& L, double* x, const double* b, int nph, cudaStream_t s);
+void launch_dgs_tiled(const LevelK& L, double* x, const double* b, int nph, cudaStream_t s, bool packed = false);
 // Single colour-compact DGS phases (used by the z-slab path).
 void launch_dgs_vel_c(const LevelK& L, double* x, const double* b, int colour, cudaStream_t s);
 void launch_dgs_pf_delta_c(const LevelK& L, const double* x, const double* b, double* d, int c, cudaStream_t s);

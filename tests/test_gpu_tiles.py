@@ -136,6 +136,25 @@ def test_tiled_rank_path_overlap_bitwise(monkeypatch):
     one.close()
 
 
+def test_tile_packed_b_bitwise(monkeypatch):
+    """Tiled levels stage b / c_b from the tile-major packed copy k_dgs_cb<true> writes once per level
+    visit (one contiguous bulk copy per tile, already parity-split) instead of TMA boxes of the level
+    vector: same values in the same shared-memory slots, so V-cycle and solve are bit-identical to
+    SMG_TILE_BPACK=0 (and both to the oracle: the tests above run the packed path by default)."""
+    dims = (48, 40, 32)
+    b = smg.forcing(*dims, h=1 / 40, kind=smg.FORCE_UNIFORM, seed=5)
+    out = []
+    for knob in ("1", "0"):
+        monkeypatch.setenv("SMG_TILE_BPACK", knob)
+        s = smg.Solver(*dims, h=1 / 40, levels=3, tile_min=1)
+        v = s.vcycle(b)
+        x, hh, _, st = s.sqmr(b, 1e-8, 40)
+        out.append((v, x, hh, st))
+        s.close()
+    assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
+    assert np.array_equal(out[0][2], out[1][2]) and out[0][3] == out[1][3] == smg.SMG_CONVERGED
+
+
 def test_tiled_cfg1_iterations_match_spec_order():
     """cfg 1 (128^3, 5 levels) with its fine level tiled: iteration count within +-1 of the
     SPEC-literal sequential order (lexicographic DGS, colour-major sequential Vanka) -- recorded 8."""
