@@ -477,7 +477,9 @@ def roofline(s, levels, peak, peak_kind, iter_ms, config_key=None, share=1.0):
         if rec:
             smooth_traffic = rec["dram_bytes"]
             div = rec.get("component_launches_in_range", 1)
-            dgs = [v["dram_bytes"] for k, v in rec["per_kernel_in_range"].items() if "k_dgs_" in k]
+            # half of k_dgs_cb: the pass serves the two smooths of a level visit (as in avg_ms)
+            dgs = [v["dram_bytes"] * (0.5 if "k_dgs_cb" in k else 1.0)
+                   for k, v in rec["per_kernel_in_range"].items() if "k_dgs_" in k]
             traffic = sum(dgs) / div if dgs else None
     nl = 16.5 if tiled else 13.5  # launches per sweep: the step kernels + half a k_dgs_cb
     return {
