@@ -20,3 +20,7 @@ print(name.split(":")[0], "solve %.2f ms, %d iterations" % (s.timing()["solve_ms
 for rep in range(2):
     print(name.split(":")[0], "dgs_sym %.4f  vanka_sym %.4f  smooth %.4f  apply %.4f ms" % (
         s.time_kernel(2, a.reps, 0), s.time_kernel(4, a.reps, 0), s.time_kernel(5, a.reps, 0), s.time_kernel(0, a.reps, 0)))
+# as the V-cycle runs them: k_dgs_cb once per level visit, the sweep / smooth without it
+print(name.split(":")[0], "k_dgs_cb %.4f  dgs_sym(cb ready) %.4f  smooth(cb ready) %.4f  L1 smooth %.4f  vcycle %.4f ms" % (
+    s.time_kernel(12, a.reps, 0), s.time_kernel(13, a.reps, 0), s.time_kernel(14, a.reps, 0),
+    s.time_kernel(5, a.reps, 1) if lv > 2 else 0.0, s.time_kernel(3, a.reps, 0)))
