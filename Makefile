@@ -16,7 +16,13 @@ OBJS := build/kernels.o build/host.o
 
 CLI := $(PKG)/solver
 
-all: $(LIB) $(CLI) oracle
+# test infrastructure: an NCCL stand-in that lets several ranks share one GPU (tests/test_gpu_fake_ranks.py)
+FAKE := tests/fake_nccl/libfakenccl.so
+
+all: $(LIB) $(CLI) oracle $(FAKE)
+
+$(FAKE): tests/fake_nccl/fake_nccl.c
+	gcc -O2 -Wall -shared -fPIC -I/usr/local/cuda/include -o $@ $< -L/usr/local/cuda/lib64 -lcudart_static -lpthread -ldl -lrt
 
 $(CLI): $(CSRC)/cli.cpp include/smg.h $(LIB)
 	$(CXX) -O2 -std=c++17 -Wall -Wextra -o $@ $(CSRC)/cli.cpp -L$(PKG) -lsmg -Wl,-rpath,'$$ORIGIN'
@@ -42,7 +48,7 @@ trace: build/host.o | build
 	$(NVCC) $(ARCH) -shared -o tools/libsmg_trace.so build/kernels_trace.o build/host.o -lcudart_static -lpthread -ldl -lrt
 
 clean:
-	rm -rf build $(LIB) $(CLI)
+	rm -rf build $(LIB) $(CLI) $(FAKE)
 	$(MAKE) -s -C oracle clean
 
 .PHONY: all oracle clean trace

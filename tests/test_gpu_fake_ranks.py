@@ -1,0 +1,93 @@
+"""The one-process-per-GPU z-slab path (smg_create_rank) with world_size > 1 on ONE GPU.
+
+Real NCCL refuses two ranks on one device and the boxes of this project expose one GPU, so the ranks
+load tests/fake_nccl/libfakenccl.so through SMG_NCCL_LIB: a shared-memory stand-in for the NCCL calls
+libsmg makes (send/recv groups, all-reduce, all-gather, broadcast).  Everything above the transport is
+the product code a real multi-GPU run executes: the slab plan, the per-rank build, the halo plane
+ranges and frames, the ghost pushes of the tiled sweep with the comm-stream fork / join, the plane
+partials and the per-rank solution ranges.  Each rank is its own process (spawn); every rank must
+return the full solution, bit-identical to one part.  Eager launches (SMG_DIST_GRAPH=0): the stand-in
+blocks the host, which a graph capture does not allow.
+"""
+import multiprocessing as mp
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+FAKE = os.path.join(ROOT, "tests", "fake_nccl", "libfakenccl.so")
+
+
+def _rank(rank, world, conn, dims, kw, env):
+    try:
+        os.environ["SMG_NCCL_LIB"] = FAKE
+        os.environ["SMG_DIST_GRAPH"] = "0"
+        os.environ.update(env)
+        import sys
+        sys.path.insert(0, ROOT)
+        import paper_2312_10615_b200 as smg
+        if rank == 0:
+            nid = smg.nccl_unique_id()
+            conn.send(nid)          # the launcher's broadcast of the id
+        nid = conn.recv()
+        nx, ny, nz = dims
+        s = smg.Solver.for_rank(rank, world, nid, nx, ny, nz, h=1 / ny, device=0, **kw)
+        b = smg.forcing(nx, ny, nz, h=1 / ny, kind=smg.FORCE_UNIFORM, seed=31)
+        y = s.apply(b)
+        v = s.vcycle(b)
+        x, hist, _, st = s.sqmr(b, 1e-8, 60)
+        s.close()
+        conn.send(("ok", y, v, x, np.asarray(hist), st))
+    except Exception as e:  # noqa: BLE001
+        conn.send(("error", repr(e)))
+
+
+def _run(world, dims, kw, env=None, timeout=420):
+    ctx = mp.get_context("spawn")
+    pipes = [ctx.Pipe() for _ in range(world)]
+    procs = [ctx.Process(target=_rank, args=(r, world, pipes[r][1], dims, kw, env or {})) for r in range(world)]
+    for p in procs:
+        p.start()
+    try:
+        assert pipes[0][0].poll(timeout), "rank 0 produced no NCCL id"
+        nid = pipes[0][0].recv()
+        for r in range(world):
+            pipes[r][0].send(nid)
+        out = []
+        for r in range(world):
+            assert pipes[r][0].poll(timeout), f"rank {r} timed out"
+            out.append(pipes[r][0].recv())
+    finally:
+        for p in procs:
+            p.join(10)
+            if p.is_alive():
+                p.kill()
+    return out
+
+
+@pytest.mark.skipif(not os.path.exists(FAKE), reason="tests/fake_nccl/libfakenccl.so not built (make)")
+@pytest.mark.parametrize("world,dims,kw,env", [
+    (2, (32, 32, 32), dict(levels=3), {}),                                   # untiled levels: 20-phase exchanges, field subsets
+    (2, (64, 64, 64), dict(levels=4, tile_min=1), {"SMG_DIST_FRAMES": "2"}),  # tiled: pushes, comm-stream overlap, frames
+    (4, (32, 32, 64), dict(levels=3, tile_min=1), {"SMG_DIST_FRAMES": "2"}),  # 4 ranks, 2 tile layers each (serial phases)
+    (2, (64, 64, 64), dict(levels=5, cycle=1), {}),                           # W-cycle on rank slabs
+])
+def test_ranks_on_one_gpu_bitwise(world, dims, kw, env):
+    import paper_2312_10615_b200 as smg
+    nx, ny, nz = dims
+    one = smg.Solver(nx, ny, nz, h=1 / ny, **kw)
+    b = smg.forcing(nx, ny, nz, h=1 / ny, kind=smg.FORCE_UNIFORM, seed=31)
+    y1, v1 = one.apply(b), one.vcycle(b)
+    x1, h1, _, s1 = one.sqmr(b, 1e-8, 60)
+    one.close()
+    out = _run(world, dims, kw, env)
+    for r, res in enumerate(out):
+        assert res[0] == "ok", (r, res)
+        _, y, v, x, hist, st = res
+        assert np.array_equal(y, y1), f"rank {r}: apply"
+        assert np.array_equal(v, v1), f"rank {r}: V-cycle"
+        assert st == s1 == smg.SMG_CONVERGED and np.array_equal(hist, np.asarray(h1)), f"rank {r}: history"
+        assert np.array_equal(x, x1), f"rank {r}: solution"
