@@ -1797,11 +1797,14 @@ void dist_download(smg_ctx* m, double* (*v)(smg_ctx*), double* host) {
 // ======================================================= SQMR, Alg. 4 ====
 // One code path for a single part and for the z-slab parts (m = the master context).  Per
 // iteration (lines 5-10), with the north_star's fusion of the AXPYs into the inner products:
-//   k_apply_q   q = t + beta q, t' = L q, partials of sigma = q.t'      -> final: alpha
 //   k_axpy_s    s = s - alpha t'
 //   V-cycle     t = V(s)
-//   k_cdot      partials of ||t||^2 and rho = s.t                      -> final: nu, c, tau
-//   k_apply_x   d = cd d + cq q, x = x + d, partials of ||b - L x||^2   -> final: rel, beta
+//   k_cdot      partials of ||t||^2 and rho = s.t                      -> final: nu, c, tau, beta
+//   k_apply_x   d = cd d + cq q, x = x + d, partials of ||b - L x||^2   (first slot)
+//   k_apply_q   q = t + beta q, t' = L q, partials of sigma = q.t'      (second slot; iteration j + 1's)
+//                                                                       -> final: rel, rho commit, alpha
+// i.e. two reductions per iteration (SURVEY OD-11; slab contexts); the setup runs the first q step on
+// its own.  A single part runs k_apply_q first with its own final (three finals, no wasted q step).
 // Every scalar lives on the device; a single part replays the iteration as a CUDA graph (one
 // per parity of the q / d / x ping-pong) and reads back (rel, status) once per iteration.
 // Slab parts: block partials at global block indices are combined by a shared buffer (parts of
@@ -1847,32 +1850,51 @@ void pc_vcycle(smg_ctx* m) {  // t = V(s) on the fine level
     else vcycle(m, 0, m->lv[0].b, m->lv[0].x);
 }
 
+// lines 9 + 5 of iteration `par`: q = t + beta q, t' = L q (into lv[0].r), partials of sigma = q.t' --
+// in the first slot (second = 0: the setup's own reduction) or in the second slot next to the
+// residual partials of the iteration that just ended
+void sqmr_q_step(smg_ctx* m, int par, int second) {
+    each(m, [&](smg_ctx* p) {
+        DevLevel& F = p->lv[0];
+        const int lo = m->ndist > 0 && p->rank > 0, hi = m->ndist > 0 && p->rank + 1 < p->nparts;
+        launch_apply_q(F.k, F.x, par ? p->q2 : p->q, par ? p->q : p->q2, F.r, p->dscal, part_out(m, p), lo, hi, p->st,
+                       second);
+    });
+}
+
+// Iteration j (par = (j - 1) & 1) from "alpha_j known, t' = L q_j in lv[0].r": the update of s, the
+// V-cycle, {||t||^2, rho} (reduction 1), the d / x update with the true residual, and already the q
+// step of iteration j + 1, whose sigma shares reduction 2 with ||r_j||^2 (SURVEY OD-11: the exact
+// Alg. 4 with two reductions per iteration; same arithmetic as the three-reduction order, only the
+// kernel that forms L q_{j+1} runs before the convergence test of iteration j instead of after it).
+// A single part has no all-reduce to save and would only pay the q step wasted after the converged
+// iteration (0.5% of a cfg-2 solve), so it keeps the order of Alg. 4 with three finals; slab
+// contexts take the two-reduction order.  Both give the same bits.
+bool two_reductions(const smg_ctx* m) { return m->ndist > 0; }
+
 void sqmr_iteration(smg_ctx* m, int par) {
     Nvtx r("sqmr_iteration");
-    auto halo = [&](smg_ctx* p, int& lo, int& hi) {
-        lo = m->ndist > 0 && p->rank > 0;
-        hi = m->ndist > 0 && p->rank + 1 < p->nparts;
-    };
-    each(m, [&](smg_ctx* p) {  // lines 9 + 5: q = t + beta q, t' = L q, sigma
-        DevLevel& F = p->lv[0];
-        int lo, hi;
-        halo(p, lo, hi);
-        launch_apply_q(F.k, F.x, par ? p->q2 : p->q, par ? p->q : p->q2, F.r, p->dscal, part_out(m, p), lo, hi, p->st);
-    });
-    finalize(m, 1);
+    if (!two_reductions(m)) {
+        sqmr_q_step(m, par, /*second=*/0);  // lines 9 + 5: q, t' = L q, sigma
+        finalize(m, 1);                     // alpha
+    }
     each(m, [&](smg_ctx* p) { launch_axpy_s(p->lv[0].b, p->lv[0].r, p->dscal, vlen(p->lv[0]), p->st); });
     if (m->ndist > 0) exchange_vec(m, v_s);
     pc_vcycle(m);                   // line 6: t = V(s)
     dots(m, v_t, v_t, v_s, v_t);    // ||t||^2, rho_j
-    finalize(m, 2);                 // nu, c, tau, cd, cq
+    finalize(m, 2);                 // nu, c, tau, cd, cq, beta_j
     each(m, [&](smg_ctx* p) {       // lines 7 + 8: d, x and the true residual
         DevLevel& F = p->lv[0];
-        int lo, hi;
-        halo(p, lo, hi);
+        const int lo = m->ndist > 0 && p->rank > 0, hi = m->ndist > 0 && p->rank + 1 < p->nparts;
         launch_apply_x(F.k, par ? p->xs2 : p->xs, par ? p->d2 : p->d, par ? p->q : p->q2, p->rhs, par ? p->xs : p->xs2,
                        par ? p->d : p->d2, p->dscal, part_out(m, p), lo, hi, p->st);
     });
-    finalize(m, 3);                 // rel, convergence, beta
+    if (!two_reductions(m)) {
+        finalize(m, 3);             // rel, convergence, beta
+        return;
+    }
+    sqmr_q_step(m, par ^ 1, /*second=*/1);
+    finalize(m, 4);                 // rel_j, convergence, rho commit; alpha_{j+1} (sigma breakdown: status 2)
 }
 
 int sqmr(smg_ctx* m, double tol, int maxit, smg_history* hist, int* status) {
@@ -1918,6 +1940,10 @@ int sqmr(smg_ctx* m, double tol, int maxit, smg_history* hist, int* status) {
         });
         dots(m, v_t, v_t, v_s, v_q);
         finalize(m, 0);
+        if (two_reductions(m)) {
+            sqmr_q_step(m, 0, /*second=*/0);  // iteration 1's q step (beta = 0: q_1 = t), sigma_1 -> alpha_1
+            finalize(m, 1);
+        }
         CK(cudaMemcpyAsync(m->hscal, m->dscal + S_STATUS, sizeof(double), cudaMemcpyDeviceToHost, m->st));
         each(m, [&](smg_ctx* p) { CK(cudaStreamSynchronize(p->st)); });
         if (m->hscal[0] != 0.0) st = SMG_BREAKDOWN;
@@ -1950,7 +1976,8 @@ int sqmr(smg_ctx* m, double tol, int maxit, smg_history* hist, int* status) {
             each(m, [&](smg_ctx* p) { CK(cudaStreamSynchronize(p->st)); });
             const double rel = m->hscal[0];
             const int code = static_cast<int>(m->hscal[1]);
-            if (code == 2) { st = SMG_BREAKDOWN; break; }  // sigma breakdown: no residual this iteration
+            // three-final order: the sigma breakdown belongs to this iteration, which has no residual
+            if (code == 2 && !two_reductions(m)) { st = SMG_BREAKDOWN; break; }
             iters = j;
             if (hist && hist->count < hist->capacity) {
                 hist->rel_residual[hist->count] = rel;
@@ -1959,6 +1986,7 @@ int sqmr(smg_ctx* m, double tol, int maxit, smg_history* hist, int* status) {
             }
             if (code == 1) st = SMG_CONVERGED;
             else if (code == 3) st = SMG_BREAKDOWN;
+            else if (code == 2 && j < maxit) st = SMG_BREAKDOWN;  // sigma of iteration j + 1 (which maxit allows) broke down
         }
     }
     each(m, [&](smg_ctx* p) { p->xcur = iters & 1; });  // iteration j wrote buffer [j & 1]

@@ -591,6 +591,21 @@ __device__ __forceinline__ void block_partial2(double v0, double v1, double* __r
         part[nblk + blk] = s1;
     }
 }
+// the same block reduction of one value, stored as the block's partial of the SECOND inner product
+// (the first one's slot, written by an earlier kernel of the same pair, stays)
+__device__ __forceinline__ void block_partial_second(double v0, double* __restrict__ part, int64_t nblk, int64_t blk) {
+    __shared__ double ws0[8];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v0 = v0 + __shfl_down_sync(0xffffffffu, v0, o);
+    if (threadIdx.x == 0) ws0[threadIdx.y] = v0;
+    __syncthreads();
+    if (threadIdx.x == 0 && threadIdx.y == 0) {
+        double s0 = ws0[0];
+#pragma unroll
+        for (int w = 1; w < 8; ++w) s0 = s0 + ws0[w];
+        part[nblk + blk] = s0;
+    }
+}
 // global block index of this CTA; grid (GX, GY, local z-blocks), slab parts start on a z-block
 __device__ __forceinline__ int64_t dot_blk(const Geom& g) {
     const int64_t GX = gridDim.x, GY = gridDim.y;
@@ -693,7 +708,7 @@ template <bool M, bool UPD>
 __global__ void __launch_bounds__(256) k_apply_q(LevelK L, const double* __restrict__ T,
                                                  const double* __restrict__ Q0, double* __restrict__ Q1,
                                                  double* __restrict__ Tn, const double* __restrict__ sc,
-                                                 double* __restrict__ partials, int halo_lo, int halo_hi) {
+                                                 double* __restrict__ partials, int halo_lo, int halo_hi, int second) {
     pdl_wait();
     if (sc[S_STATUS] != 0.0) return;
     const Geom& g = L.g;
@@ -745,7 +760,9 @@ __global__ void __launch_bounds__(256) k_apply_q(LevelK L, const double* __restr
             v = v + (c4 + qp * tp);  // ((p_u + p_v) + p_w) + p_p
         }
     }
-    block_partial2(v, 0.0, partials, dot_nblk(g), dot_blk(g));
+    // second: sigma of the NEXT iteration rides in the second slot next to this iteration's ||r||^2
+    if (second) block_partial_second(v, partials, dot_nblk(g), dot_blk(g));
+    else block_partial2(v, 0.0, partials, dot_nblk(g), dot_blk(g));
 }
 
 // Lines 7 + 8 of iteration j: d = cd d + cq q, x = x + d (written to D1, X1), then the true
@@ -1763,12 +1780,12 @@ __global__ void __launch_bounds__(256, SMG_PREV_MINB) k_dgs_prev_c(LevelK L, dou
 // order as the oracle), so one SQMR iteration is a fixed kernel sequence that
 // can be replayed as a CUDA graph.  sc[] layout: see SqmrSlot in smg_internal.h.
 
-__device__ __forceinline__ void sqmr_alpha(double* sc) {  // after sigma = q.t
+__device__ __forceinline__ void sqmr_alpha_from(double* sc, double sigma) {  // after sigma = q.t
     if (sc[S_STATUS] != 0.0) return;
-    const double sigma = sc[S_D0];
     if (fabs(sigma) < 1e-300) { sc[S_STATUS] = 2.0; return; }
     sc[S_ALPHA] = sc[S_RHO] / sigma;
 }
+__device__ __forceinline__ void sqmr_alpha(double* sc) { sqmr_alpha_from(sc, sc[S_D0]); }
 
 
 
@@ -1802,6 +1819,9 @@ __device__ __forceinline__ void sqmr_nu(double* sc) {
     sc[S_CQ] = c2 * sc[S_ALPHA];
     sc[S_NU] = nu;
     sc[S_RHONEW] = sc[S_D1];
+    // beta_j = rho_j / rho_{j-1} already here: the q update of the next iteration runs before the
+    // residual's final (sqmr_beta repeats the same division when it commits rho)
+    sc[S_BETA] = sc[S_D1] / sc[S_RHO];
 }
 __global__ void __launch_bounds__(256) k_final_scalar(const double* __restrict__ partials, int64_t nblk,
                                                       double* __restrict__ sc, int which) {
@@ -1813,6 +1833,10 @@ __global__ void __launch_bounds__(256) k_final_scalar(const double* __restrict__
     else if (which == 1) sqmr_alpha(sc);
     else if (which == 2) sqmr_nu(sc);
     else if (which == 3) sqmr_beta(sc);
+    else if (which == 4) {  // ||r_j||^2 in the first slot, sigma_{j+1} in the second: one reduction for both
+        sqmr_beta(sc);
+        sqmr_alpha_from(sc, sc[S_D1]);
+    }
 }
 
 __global__ void k_axpy_s(double* __restrict__ s, const double* __restrict__ t, const double* __restrict__ sc,
@@ -3011,7 +3035,7 @@ void launch_final_scalar(const Geom& g, const double* partials, double* sc, int 
     count();
 }
 void launch_apply_q(const LevelK& L, const double* t, const double* q0, double* q1, double* tn, const double* sc,
-                    double* partials, int halo_lo, int halo_hi, cudaStream_t s) {
+                    double* partials, int halo_lo, int halo_hi, cudaStream_t s, int second) {
     // SMG_SQMR_SPLIT (default 1): the vector update as its own streaming pass, then the stencil + dot
     // kernel on the stored vector; 0: one kernel evaluating the update at every stencil point
     const int split = env_int("SMG_SQMR_SPLIT", 1);  // read per launch: tests toggle it in-process
@@ -3020,12 +3044,12 @@ void launch_apply_q(const LevelK& L, const double* t, const double* q0, double* 
         ug.z = L.g.nz + halo_lo + halo_hi;
         launch_k(k_q_upd, ug, dim3(BX, BY), 0, s, L.g, t, q0, q1, sc, halo_lo, halo_hi);
         count();
-        if (L.cls) launch_k(k_apply_q<true, false>, dot_grid(L.g), dim3(32, 8), 0, s, L, t, q0, q1, tn, sc, partials, halo_lo, halo_hi);
-        else launch_k(k_apply_q<false, false>, dot_grid(L.g), dim3(32, 8), 0, s, L, t, q0, q1, tn, sc, partials, halo_lo, halo_hi);
+        if (L.cls) launch_k(k_apply_q<true, false>, dot_grid(L.g), dim3(32, 8), 0, s, L, t, q0, q1, tn, sc, partials, halo_lo, halo_hi, second);
+        else launch_k(k_apply_q<false, false>, dot_grid(L.g), dim3(32, 8), 0, s, L, t, q0, q1, tn, sc, partials, halo_lo, halo_hi, second);
     } else if (L.cls) {
-        launch_k(k_apply_q<true, true>, dot_grid(L.g), dim3(32, 8), 0, s, L, t, q0, q1, tn, sc, partials, halo_lo, halo_hi);
+        launch_k(k_apply_q<true, true>, dot_grid(L.g), dim3(32, 8), 0, s, L, t, q0, q1, tn, sc, partials, halo_lo, halo_hi, second);
     } else {
-        launch_k(k_apply_q<false, true>, dot_grid(L.g), dim3(32, 8), 0, s, L, t, q0, q1, tn, sc, partials, halo_lo, halo_hi);
+        launch_k(k_apply_q<false, true>, dot_grid(L.g), dim3(32, 8), 0, s, L, t, q0, q1, tn, sc, partials, halo_lo, halo_hi, second);
     }
     count();
 }

@@ -163,7 +163,7 @@ void launch_final_scalar(const Geom& g, const double* partials, double* sc, int 
 // partials of q1.tn; x1 = x0 + (cd d0 + cq q), d1 = cd d0 + cq q and the partials of
 // ||b - L x1||^2.  halo_lo/hi (slab parts): also write the ghost plane below / above.
 void launch_apply_q(const LevelK& L, const double* t, const double* q0, double* q1, double* tn, const double* sc,
-                    double* partials, int halo_lo, int halo_hi, cudaStream_t s);
+                    double* partials, int halo_lo, int halo_hi, cudaStream_t s, int second = 0);
 void launch_apply_x(const LevelK& L, const double* x0, const double* d0, const double* q, const double* b, double* x1,
                     double* d1, const double* sc, double* partials, int halo_lo, int halo_hi, cudaStream_t s);
 // Tile-ordered DGS (OD-1 rev. 2): a level is tiled iff it has >= tile_min cells (0: 256^3,
