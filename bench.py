@@ -118,6 +118,8 @@ def dist_setup():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("SMG_BENCH_ONE_GPU"):  # tests: every rank on cuda:0 (with the NCCL stand-in, tests/fake_nccl)
+        local = 0
     if ws > 1:
         import torch.distributed as dist
 

@@ -91,3 +91,36 @@ def test_ranks_on_one_gpu_bitwise(world, dims, kw, env):
         assert np.array_equal(v, v1), f"rank {r}: V-cycle"
         assert st == s1 == smg.SMG_CONVERGED and np.array_equal(hist, np.asarray(h1)), f"rank {r}: history"
         assert np.array_equal(x, x1), f"rank {r}: solution"
+
+
+@pytest.mark.skipif(not os.path.exists(FAKE), reason="tests/fake_nccl/libfakenccl.so not built (make)")
+def test_bench_two_ranks_one_gpu():
+    """`bench.py --gpus 2` launched the way the driver launches it (torch.distributed.run, one rank per
+    process, rendezvous on 127.0.0.1), both ranks on cuda:0 over the NCCL stand-in: the rank path end to
+    end -- id broadcast over gloo, per-rank z-slab contexts, barrier + max-over-ranks timing, ONE JSON
+    line from rank 0 with the contract's keys, and the same iteration count / residual as one GPU."""
+    import json
+    import socket
+    import subprocess
+    import sys
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    env = dict(os.environ, SMG_NCCL_LIB=FAKE, SMG_DIST_GRAPH="0", SMG_BENCH_ONE_GPU="1")
+    common = ["--config", "0", "--steps", "1", "--warmup", "3", "--also", "", "--no-labelled", "--no-cpu-baseline"]
+    one = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "1"] + common, cwd=ROOT,
+                         capture_output=True, text=True, timeout=600)
+    assert one.returncode == 0, one.stderr[-2000:]
+    ref = json.loads(one.stdout.strip().splitlines()[-1])
+    two = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                          "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
+                          "--gpus", "2"] + common, cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    assert two.returncode == 0, two.stderr[-3000:]
+    lines = [ln for ln in two.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, two.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == "strong" and "z-slab x2" in d["config"]["parallelism"]
+    for key in ("metric", "value", "unit", "ms_per_step", "e2e", "roofline", "gpu_launches", "clocks"):
+        assert key in d, key
+    assert d["config"]["converged"] and d["config"]["iterations_per_solve"] == ref["config"]["iterations_per_solve"]
+    assert d["config"]["final_rel_residual"] == ref["config"]["final_rel_residual"]  # bit-identical solve
