@@ -26,8 +26,8 @@
 #include <unistd.h>
 
 #define MAX_RANKS 16
-#define COLL_CAP ((size_t)24 << 20) /* bytes staged per rank in a collective */
-#define FIFO_CAP ((size_t)32 << 20) /* bytes in flight per ordered pair */
+#define COLL_CAP ((size_t)16 << 20) /* bytes staged per rank in a collective (only touched pages cost /dev/shm) */
+#define FIFO_CAP ((size_t)4 << 20)  /* bytes in flight per ordered pair: > the sends of one group; small so that a 64 MB /dev/shm holds every FIFO */
 #define WAIT_LIMIT_S 120.0          /* a peer that never shows up fails the call instead of hanging the box */
 
 typedef struct {
