@@ -1213,9 +1213,8 @@ void vanka_sym_coop(smg_ctx* c, int l, double* x, const double* b) {
             for (int ph = 0; ph < 8; ++ph) {
                 const int pq = ph < 4 ? ph : 7 - ph;
                 launch_vanka_delta(L.k, x, b, L.sw_cells[pq], L.sw_mask[pq], L.sw_n[pq], L.ktab, c->vk_delta, c->st,
-                                   L.sw_kidx[pq], /*newv=*/true);
-                launch_vanka_apply(L.k, x, L.sw_cells[pq], L.sw_mask[pq], L.sw_n[pq], c->vk_delta, c->st, nullptr,
-                                   /*newv=*/true);
+                                   L.sw_kidx[pq]);
+                launch_vanka_apply(L.k, x, L.sw_cells[pq], L.sw_mask[pq], L.sw_n[pq], c->vk_delta, c->st);
             }
         return;
     }

@@ -2720,11 +2720,6 @@ __global__ void k_dgs_prev_m(LevelK L, double* __restrict__ X, int colour) {
     X[3 * fs + i] = P[i] + (L.cb[i] - cl) / L.dp;
 }
 
-// padded-slot offset of Vanka block slot s8 (uL, uR, vL, vR, wL, wR, p) from the block's cell slot
-__device__ __forceinline__ int64_t vanka_slot_offset(const Geom& g, int s8) {
-    const int64_t fs = g.fs;
-    return s8 == 0 ? 0 : s8 == 1 ? 1 : s8 == 2 ? fs : s8 == 3 ? fs + g.sy : s8 == 4 ? 2 * fs : s8 == 5 ? 2 * fs + g.sz : 3 * fs;
-}
 // Residual slot s8 (0..5 the faces uL, uR, vL, vR, wL, wR; 6 the pressure) of the Vanka block at cell
 // slot i with active-face mask m: the momentum row with the face's own diagonal (labelled levels: from
 // the DofMap bits of the face's cell; else 6) or the continuity row; 0 for an inactive face.
@@ -2757,8 +2752,7 @@ __global__ void __launch_bounds__(256) k_vanka_delta8(LevelK L, const double* __
                                                         const int32_t* __restrict__ cells,
                                                         const uint8_t* __restrict__ masks,
                                                         const uint16_t* __restrict__ kidx, int n,
-                                                        const double* __restrict__ ktab, double* __restrict__ delta,
-                                                        int newv) {
+                                                        const double* __restrict__ ktab, double* __restrict__ delta) {
     pdl_wait();
     const int tid = blockIdx.x * blockDim.x + threadIdx.x, lane = threadIdx.x & 31, s8 = lane & 7;
     const int t = tid >> 3;
@@ -2779,27 +2773,22 @@ __global__ void __launch_bounds__(256) k_vanka_delta8(LevelK L, const double* __
         const double rq = __shfl_sync(0xffffffffu, r, (lane & ~7) + q);
         acc = acc + K[q] * rq;
     }
-    if (act && s8 < 7) {
-        // newv: store the DOF's new value x + delta (the same addition k_vanka_apply8 would make: nothing
-        // writes the DOF between the two launches), so the apply launch scatters without reading x
-        if (newv) acc = X[cells[t] + vanka_slot_offset(g, s8)] + acc;
-        delta[static_cast<int64_t>(t) * 8 + s8] = acc;
-    }
+    if (act && s8 < 7) delta[static_cast<int64_t>(t) * 8 + s8] = acc;
 }
 __global__ void __launch_bounds__(256) k_vanka_apply8(LevelK L, double* __restrict__ X,
                                                       const int32_t* __restrict__ cells,
                                                       const uint8_t* __restrict__ masks, int n,
-                                                      const double* __restrict__ delta, int newv) {
+                                                      const double* __restrict__ delta) {
     pdl_wait();
     const int tid = blockIdx.x * blockDim.x + threadIdx.x, s8 = tid & 7, t = tid >> 3;
     if (t >= n || s8 == 7) return;
     const Geom& g = L.g;
-    const int64_t i = cells[t];
+    const int64_t fs = g.fs, i = cells[t];
     const int m = masks[t];
     if (s8 < 6 && !((m >> s8) & 1)) return;
-    const int64_t offs = vanka_slot_offset(g, s8);
-    const double d = delta[static_cast<int64_t>(t) * 8 + s8];
-    X[i + offs] = newv ? d : X[i + offs] + d;
+    const int64_t offs = s8 == 0 ? 0 : s8 == 1 ? 1 : s8 == 2 ? fs : s8 == 3 ? fs + g.sy : s8 == 4 ? 2 * fs
+                         : s8 == 5 ? 2 * fs + g.sz : 3 * fs;
+    X[i + offs] = X[i + offs] + delta[static_cast<int64_t>(t) * 8 + s8];
 }
 
 // Restriction / prolongation with the coarse / fine DofMap bits deciding which DOFs exist; legs
@@ -2931,31 +2920,29 @@ void launch_dgs_prev(const LevelK& L, double* x, const double* b, int colour, cu
 }
 void launch_vanka_delta(const LevelK& L, const double* x, const double* b, const int32_t* cells,
                         const uint8_t* masks, int ncells, const double* ktab, double* delta, cudaStream_t s,
-                        const uint16_t* kidx, bool newv) {
+                        const uint16_t* kidx) {
     if (ncells <= 0) return;
-    const int nv = newv ? 1 : 0;
     // ordinary launches (no PDL): next to the tile DGS kernel early-scheduled dependents cost more
     // than they hide (SMG_VANKA_PDL=1 restores PDL; profiles/r2d_experiments.md)
     const int blocks = static_cast<int>((8 * static_cast<int64_t>(ncells) + 255) / 256);
     static const int vpdl = env_int("SMG_VANKA_PDL", 0);
     if (L.cls) {
-        if (vpdl) launch_k(k_vanka_delta8<true>, blocks, 256, 0, s, L, x, b, cells, masks, kidx, ncells, ktab, delta, nv);
-        else k_vanka_delta8<true><<<blocks, 256, 0, s>>>(L, x, b, cells, masks, kidx, ncells, ktab, delta, nv);
+        if (vpdl) launch_k(k_vanka_delta8<true>, blocks, 256, 0, s, L, x, b, cells, masks, kidx, ncells, ktab, delta);
+        else k_vanka_delta8<true><<<blocks, 256, 0, s>>>(L, x, b, cells, masks, kidx, ncells, ktab, delta);
     } else {
-        if (vpdl) launch_k(k_vanka_delta8<false>, blocks, 256, 0, s, L, x, b, cells, masks, kidx, ncells, ktab, delta, nv);
-        else k_vanka_delta8<false><<<blocks, 256, 0, s>>>(L, x, b, cells, masks, kidx, ncells, ktab, delta, nv);
+        if (vpdl) launch_k(k_vanka_delta8<false>, blocks, 256, 0, s, L, x, b, cells, masks, kidx, ncells, ktab, delta);
+        else k_vanka_delta8<false><<<blocks, 256, 0, s>>>(L, x, b, cells, masks, kidx, ncells, ktab, delta);
     }
     count();
 }
 void launch_vanka_apply(const LevelK& L, double* x, const int32_t* cells, const uint8_t* masks, int ncells,
-                        const double* delta, cudaStream_t s, const uint8_t* amask, bool newv) {
+                        const double* delta, cudaStream_t s, const uint8_t* amask) {
     if (ncells <= 0) return;
     if (!amask) {
-        const int nv = newv ? 1 : 0;
         const int blocks = static_cast<int>((8 * static_cast<int64_t>(ncells) + 255) / 256);
         static const int vpdl = env_int("SMG_VANKA_PDL", 0);
-        if (vpdl) launch_k(k_vanka_apply8, blocks, 256, 0, s, L, x, cells, masks, ncells, delta, nv);
-        else k_vanka_apply8<<<blocks, 256, 0, s>>>(L, x, cells, masks, ncells, delta, nv);
+        if (vpdl) launch_k(k_vanka_apply8, blocks, 256, 0, s, L, x, cells, masks, ncells, delta);
+        else k_vanka_apply8<<<blocks, 256, 0, s>>>(L, x, cells, masks, ncells, delta);
     } else {  // z-slab parts: per-block ownership masks
         k_vanka_apply<<<(ncells + 127) / 128, 128, 0, s>>>(L, x, cells, masks, ncells, delta, amask);
     }
@@ -3281,10 +3268,8 @@ void launch_vanka_sym_coop(const LevelK& L, double* x, const double* b, const in
             for (int k = 0; k < 16; ++k) {
                 const int col = host_phase_list(pr, k);
                 if (col < 0) continue;  // folded into the list of its complementary colour
-                // SMG_VANKA_NEWV (default 1): the delta launch stores x + delta, the apply launch only scatters
-                const bool nv = env_int("SMG_VANKA_NEWV", 1) != 0;
-                launch_vanka_delta(L, x, b, cells[col], masks[col], n[col], ktab, delta, s, nullptr, nv);
-                launch_vanka_apply(L, x, cells[col], masks[col], n[col], delta, s, nullptr, nv);
+                launch_vanka_delta(L, x, b, cells[col], masks[col], n[col], ktab, delta, s);
+                launch_vanka_apply(L, x, cells[col], masks[col], n[col], delta, s);
             }
     }
 }

@@ -111,10 +111,10 @@ struct VankaPairs {
 // kidx (labelled levels): per block the index of its signature class in ktab (nullptr: the face mask)
 void launch_vanka_delta(const LevelK& L, const double* x, const double* b, const int32_t* cells,
                         const uint8_t* masks, int ncells, const double* ktab, double* delta, cudaStream_t s,
-                        const uint16_t* kidx = nullptr, bool newv = false);
+                        const uint16_t* kidx = nullptr);
 // amask (z-slabs, optional): per block, the slots this part owns (bit s = slot s, bit 6 = p).
 void launch_vanka_apply(const LevelK& L, double* x, const int32_t* cells, const uint8_t* masks, int ncells,
-                        const double* delta, cudaStream_t s, const uint8_t* amask = nullptr, bool newv = false);
+                        const double* delta, cudaStream_t s, const uint8_t* amask = nullptr);
 // Cooperative (persistent, grid-synchronised) symmetric sweeps: nu Vanka sweeps
 // over the 8 colour lists; nph DGS phases (20 = full symmetric sweep).
 // pr: merged complementary colour pairs (list m = parity m + parity 7-m, one phase
