@@ -54,6 +54,26 @@ def test_vanka_halo_frames_bitwise(n, levels, parts, bw, monkeypatch):
         many.close()
 
 
+@pytest.mark.parametrize("maxit", [0, 1, 2, 5])
+def test_slab_two_reduction_order_statuses(maxit):
+    """Slab contexts run SQMR with two reductions per iteration (the q step of iteration j + 1 before the
+    convergence test of iteration j; host.cpp sqmr_iteration), one part with three finals: status,
+    iteration count, history and the returned iterate agree bit for bit when maxit cuts the solve short,
+    and on a zero right-hand side."""
+    one = smg.Solver(32, levels=3)
+    many = smg.Solver(32, levels=3, devices=[0, 0])
+    b = smg.forcing(32, kind=smg.FORCE_UNIFORM, seed=44)
+    x1, h1, _, s1 = one.sqmr(b, 1e-10, maxit)
+    x2, h2, _, s2 = many.sqmr(b, 1e-10, maxit)
+    assert s1 == s2 and len(h1) == len(h2) == maxit and np.array_equal(h1, h2) and np.array_equal(x1, x2)
+    z = np.zeros_like(b)
+    xz1, hz1, _, sz1 = one.sqmr(z, 1e-10, 5)
+    xz2, hz2, _, sz2 = many.sqmr(z, 1e-10, 5)
+    assert sz1 == sz2 == smg.SMG_CONVERGED and len(hz1) == len(hz2) == 0 and not xz1.any() and not xz2.any()
+    one.close()
+    many.close()
+
+
 @pytest.mark.parametrize("n,levels,parts", [(48, 5, 2), (48, 4, 4)])
 def test_odd_slab_levels_bitwise(n, levels, parts):
     """Levels whose slab would be odd stay replicated: 48^3 with 5 levels on 2 parts
