@@ -218,13 +218,16 @@ def run_reference(args, ws, rank):
     for _ in range(args.warmup):
         cpu_sample(cfg, threads, 1, o)
     t_init = t_it = wall = 0.0
+    # bounded sample per step: a step is ~9 s of CPU work per timed iteration at cfg 2, so long runs
+    # (the driver's --steps 20) time one iteration per step and the whole arm stays within a few minutes
+    ref_iters = args.ref_iters if args.steps <= 6 else 1
     for _ in range(args.steps):
-        ti, tt, _, dt = cpu_sample(cfg, threads, args.ref_iters, o)
+        ti, tt, _, dt = cpu_sample(cfg, threads, ref_iters, o)
         t_init += ti / args.steps
         t_it += tt / args.steps
         wall += dt
     val = cpu_dofs(cfg, t_init, t_it, k_solve)
-    sample = (f"per step: Alg. 4 setup (1 V-cycle) + {args.ref_iters} MG-SQMR iterations of {name}, timed apart; "
+    sample = (f"per step: Alg. 4 setup (1 V-cycle) + {ref_iters} MG-SQMR iterations of {name}, timed apart; "
               f"value = N K / (t_setup + K t_iter) with K = {k_solve} (committed golden), "
               f"oracle/stokes_oracle.cpp on {threads} threads, {cpu_model()}")
     line = {
