@@ -16,7 +16,7 @@ OBJS := build/kernels.o build/host.o
 
 CLI := $(PKG)/solver
 
-# test infrastructure: an NCCL stand-in that lets several ranks share one GPU (tests/test_gpu_fake_ranks.py)
+# test infrastructure: an NCCL stand-in that lets several ranks share one GPU (tests/test_gpu_zz_fake_ranks.py)
 FAKE := tests/fake_nccl/libfakenccl.so
 
 all: $(LIB) $(CLI) oracle $(FAKE)

@@ -2,7 +2,7 @@
  * GPU, so the one-process-per-GPU z-slab path of libsmg (smg_create_rank: halo send/recv groups, halo
  * frames, ghost pushes, plane-partial all-reduce, coarse all-gather, solution broadcast) runs with
  * world_size > 1 on the 1-GPU boxes this project is tested on.  Real NCCL refuses two ranks on one
- * device.  Loaded through SMG_NCCL_LIB (host.cpp nccl()); tests/test_gpu_fake_ranks.py drives it.
+ * device.  Loaded through SMG_NCCL_LIB (host.cpp nccl()); tests/test_gpu_zz_fake_ranks.py drives it.
  *
  * Transport: POSIX shared memory.  Every call first drains its CUDA stream (cudaStreamSynchronize),
  * then moves the data with blocking copies through host memory, so stream order is preserved for

@@ -21,6 +21,24 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 FAKE = os.path.join(ROOT, "tests", "fake_nccl", "libfakenccl.so")
 
 
+def _shm_ok():
+    """The stand-in needs POSIX shared memory (a few tens of MB of /dev/shm); without it the tests skip."""
+    try:
+        from multiprocessing import shared_memory
+        seg = shared_memory.SharedMemory(create=True, size=48 << 20)
+        seg.buf[0] = 1
+        seg.buf[(48 << 20) - 1] = 1
+        seg.close()
+        seg.unlink()
+        return True
+    except Exception:  # noqa: BLE001
+        return False
+
+
+needs_env = pytest.mark.skipif(not os.path.exists(FAKE) or not _shm_ok(),
+                               reason="tests/fake_nccl/libfakenccl.so not built (make) or no usable /dev/shm")
+
+
 def _rank(rank, world, conn, dims, kw, env):
     try:
         os.environ["SMG_NCCL_LIB"] = FAKE
@@ -68,7 +86,7 @@ def _run(world, dims, kw, env=None, timeout=420):
     return out
 
 
-@pytest.mark.skipif(not os.path.exists(FAKE), reason="tests/fake_nccl/libfakenccl.so not built (make)")
+@needs_env
 @pytest.mark.parametrize("world,dims,kw,env", [
     (2, (32, 32, 32), dict(levels=3), {}),                                   # untiled levels: 20-phase exchanges, field subsets
     (2, (64, 64, 64), dict(levels=4, tile_min=1), {"SMG_DIST_FRAMES": "2"}),  # tiled: pushes, comm-stream overlap, frames
@@ -93,7 +111,7 @@ def test_ranks_on_one_gpu_bitwise(world, dims, kw, env):
         assert np.array_equal(x, x1), f"rank {r}: solution"
 
 
-@pytest.mark.skipif(not os.path.exists(FAKE), reason="tests/fake_nccl/libfakenccl.so not built (make)")
+@needs_env
 def test_bench_two_ranks_one_gpu():
     """`bench.py --gpus 2` launched the way the driver launches it (torch.distributed.run, one rank per
     process, rendezvous on 127.0.0.1), both ranks on cuda:0 over the NCCL stand-in: the rank path end to
