@@ -2075,8 +2075,15 @@ int64_t smg_census(const smg_grid_desc* grid, int band_width, int64_t* out2) {
 // on DGS-tiled levels a whole number of tiles, so every tile lies in one part)
 static int slab_levels(const smg_grid_desc* grid, int levels, int nparts, int64_t tile_min) {
     int nd = 0;
+    // Levels below 64^3 cells are gathered (BASELINE cfg 3 "coarse levels gathered below 64^3"):
+    // a distributed level visit costs ~90 halo messages whatever its size, a replicated 32^3 sub-cycle
+    // ~0.45 ms of redundant compute.  SMG_SLAB_MIN_CELLS overrides the bound (0: split whatever can be
+    // split -- the tests, which exercise the machinery on small grids); level 0 is always split.
+    const char* mc = std::getenv("SMG_SLAB_MIN_CELLS");
+    const int64_t min_cells = mc ? std::atoll(mc) : int64_t{64} * 64 * 64;
     for (int l = 0; l + 1 < levels; ++l) {
         const int nz = grid->nz >> l;
+        if (l >= 1 && static_cast<int64_t>(grid->nx >> l) * (grid->ny >> l) * nz < min_cells) break;
         if (dgs_tiled(grid->nx >> l, grid->ny >> l, nz, tile_min) && (nz % nparts || (nz / nparts) % dgs_tile_dim(2)))
             break;
         // slab of >= 2 planes (halo depth), and even: the child level's planes 2k, 2k+1 then

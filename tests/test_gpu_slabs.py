@@ -54,6 +54,22 @@ def test_vanka_halo_frames_bitwise(n, levels, parts, bw, monkeypatch):
         many.close()
 
 
+def test_default_gather_below_64_cubed_bitwise(monkeypatch):
+    """Production slab plan (levels below 64^3 cells gathered: here only the fine level is split and the
+    32^3 sub-cycle runs replicated on every part after the all-gather) == one part."""
+    monkeypatch.delenv("SMG_SLAB_MIN_CELLS", raising=False)
+    assert smg.slab_plan(64, 64, 64, 4, 4, 0)[0] == 1
+    one = smg.Solver(64, levels=4)
+    many = smg.Solver(64, levels=4, devices=[0] * 4)
+    b = smg.forcing(64, kind=smg.FORCE_UNIFORM, seed=8)
+    assert np.array_equal(many.vcycle(b), one.vcycle(b))
+    x1, h1, _, s1 = one.sqmr(b, 1e-8, 60)
+    x2, h2, _, s2 = many.sqmr(b, 1e-8, 60)
+    assert s1 == s2 == smg.SMG_CONVERGED and np.array_equal(h1, h2) and np.array_equal(x1, x2)
+    one.close()
+    many.close()
+
+
 @pytest.mark.parametrize("maxit", [0, 1, 2, 5])
 def test_slab_two_reduction_order_statuses(maxit):
     """Slab contexts run SQMR with two reductions per iteration (the q step of iteration j + 1 before the

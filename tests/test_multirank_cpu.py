@@ -33,6 +33,18 @@ def test_slab_plan_covers_and_aligns(nz, levels, parts):
     assert nd <= levels - 1  # coarsest level is always replicated (dense solve)
 
 
+def test_slab_plan_gathers_below_64_cubed_by_default(monkeypatch):
+    """Production default (SMG_SLAB_MIN_CELLS unset): levels below 64^3 cells are gathered (BASELINE cfg 3
+    "coarse levels gathered below 64^3"; cfg 4: 128 x 32 x 32 and smaller); level 0 is always split."""
+    monkeypatch.delenv("SMG_SLAB_MIN_CELLS", raising=False)
+    assert smg.slab_plan(512, 512, 512, 7, 8, 3)[0] == 4       # 512, 256, 128, 64 split; 32^3 and below replicated
+    assert smg.slab_plan(256, 256, 256, 6, 8, 0)[0] == 3       # 256, 128, 64
+    assert smg.slab_plan(1024, 256, 256, 7, 8, 5)[0] == 3      # 1024x256x256, 512x128x128, 256x64x64
+    assert smg.slab_plan(32, 32, 32, 3, 2, 1)[0] == 1          # a small grid: the fine level only
+    monkeypatch.setenv("SMG_SLAB_MIN_CELLS", "0")
+    assert smg.slab_plan(512, 512, 512, 7, 8, 3)[0] == 6
+
+
 def test_slab_plan_stops_before_odd_slab():
     """48^3, 5 levels, 2 parts: slabs 24, 12, 6 are split, the 3-plane slab of level 3 is not
     (its coarse plane 2 would straddle two parts), so levels 3 and 4 are replicated."""
