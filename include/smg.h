@@ -150,7 +150,9 @@ int64_t smg_census(const smg_grid_desc* grid, int band_width, int64_t* out2);
 /* z-slab plan (host only, no device needed): returns the number of leading
  * levels split over nparts (>= 1, or <= 0 if the grid cannot be split), and for
  * `rank` the first global plane z0[l] and plane count nzl[l] of every level
- * (replicated levels: 0 and the whole level).  Either array may be NULL. */
+ * (replicated levels: 0 and the whole level).  Either array may be NULL.  A level is
+ * split while its slab keeps >= 2 planes, an even count, tile alignment on tiled levels, and
+ * (levels >= 1) at least 64^3 cells -- smaller levels are gathered (SMG_SLAB_MIN_CELLS overrides). */
 int smg_slab_plan(const smg_grid_desc* grid, int levels, int nparts, int rank, int* z0, int* nzl);
 /* DGS tiling of a level (host only): out4 = {tile colours (8 tiled, 1 not), tile x, y, z}
  * under the rule of smg_params.dgs_tile_min (the default when tile_min = 0). */
