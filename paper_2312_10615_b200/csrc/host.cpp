@@ -1907,7 +1907,12 @@ int sqmr(smg_ctx* m, double tol, int maxit, smg_history* hist, int* status) {
     // one stream: no host launch latency between the ~10^3 phase kernels and halo groups of a
     // V-cycle; SMG_DIST_GRAPH=0 keeps eager launches).  In-process parts on several streams stay eager.
     static const bool dist_graph = !(std::getenv("SMG_DIST_GRAPH") && std::atoi(std::getenv("SMG_DIST_GRAPH")) == 0);
-    const bool single = m->ndist == 0 || (m->mp && dist_graph);
+    // SMG_EMU_GRAPH=1 (measurement aid, tools/time_slabs.py): in-process parts that share ONE stream (all
+    // parts emulated on one device) also replay the iteration as a graph -- kernels of every part and the
+    // device-local halo copies as nodes -- which takes the host launch cost out of the emulation and leaves
+    // what the slab decomposition itself costs on the GPU (smaller kernels, halo copies, extra phases).
+    static const bool emu_graph = std::getenv("SMG_EMU_GRAPH") && std::atoi(std::getenv("SMG_EMU_GRAPH")) != 0;
+    const bool single = m->ndist == 0 || (m->mp && dist_graph) || (!m->mp && emu_graph && shared_stream(m));
     CK(cudaEventRecord(m->ev0, m->st));
     if (hist) hist->count = 0;
     each(m, [&](smg_ctx* p) {
