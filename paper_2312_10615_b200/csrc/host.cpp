@@ -1478,13 +1478,13 @@ void exchange_frame(smg_ctx* m, int l) {
     const int P = m->nparts;
     auto pack = [&](smg_ctx* p) {  // top planes nz-2, nz-1 -> fbuf[0]; bottom planes 0, 1 -> fbuf[1]
         const Geom& g = p->lv[l].k.g;
-        if (p->rank + 1 < P) launch_frame_copy(g, bw, p->lv[l].x, p->fbuf[0], g.zg + g.nz - 2, true, p->st);
-        if (p->rank > 0) launch_frame_copy(g, bw, p->lv[l].x, p->fbuf[1], g.zg, true, p->st);
+        launch_frame_copy(g, bw, p->lv[l].x, p->rank + 1 < P ? p->fbuf[0] : nullptr, g.zg + g.nz - 2,
+                          p->rank > 0 ? p->fbuf[1] : nullptr, g.zg, true, p->st);
     };
     auto unpack = [&](smg_ctx* p) {  // fbuf[2] -> ghost planes nz, nz+1; fbuf[3] -> ghost planes -2, -1
         const Geom& g = p->lv[l].k.g;
-        if (p->rank + 1 < P) launch_frame_copy(g, bw, p->lv[l].x, p->fbuf[2], g.zg + g.nz, false, p->st);
-        if (p->rank > 0) launch_frame_copy(g, bw, p->lv[l].x, p->fbuf[3], 0, false, p->st);
+        launch_frame_copy(g, bw, p->lv[l].x, p->rank + 1 < P ? p->fbuf[2] : nullptr, g.zg + g.nz,
+                          p->rank > 0 ? p->fbuf[3] : nullptr, 0, false, p->st);
     };
     if (m->mp) {
         const NcclApi& N = nccl();

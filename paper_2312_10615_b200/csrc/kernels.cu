@@ -2510,8 +2510,13 @@ static FrameDims frame_dims(const Geom& g, int bw) {
     return f;
 }
 // to_buf: buf <- frames of the padded planes zs, zs + 1 of the 4 fields; else the reverse
+// blockIdx.z picks the plane pair: (buf0, zs0) or (buf1, zs1); a null buffer means no neighbour there
 __global__ void __launch_bounds__(256) k_frame_copy(Geom g, FrameDims f, double* __restrict__ X,
-                                                    double* __restrict__ buf, int zs, int to_buf) {
+                                                    double* __restrict__ buf0, int zs0, double* __restrict__ buf1,
+                                                    int zs1, int to_buf) {
+    double* __restrict__ buf = blockIdx.z ? buf1 : buf0;
+    const int zs = blockIdx.z ? zs1 : zs0;
+    if (!buf) return;
     const int64_t n = f.count();
     const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (e >= n) return;
@@ -3499,13 +3504,16 @@ void launch_axpy_s(double* s_, const double* t, const double* sc, int64_t n, cud
     launch_k(k_axpy_s, stream_blocks(n), 256, 0, s, s_, t, sc, n);
     count();
 }
-// Frame of the two padded planes zs, zs + 1 (all four fields) of a slab vector <-> a contiguous
-// buffer of frame_doubles(g, bw) doubles (z-slab halo refresh after a Vanka phase).
+// Frames of the padded plane pairs zs0, zs0 + 1 and zs1, zs1 + 1 (all four fields) of a slab vector <->
+// two contiguous buffers of frame_doubles(g, bw) doubles each (z-slab halo refresh after a Vanka phase);
+// a null buffer skips its pair.
 int64_t frame_doubles(const Geom& g, int bw) { return 8 * frame_dims(g, bw).count(); }
-void launch_frame_copy(const Geom& g, int bw, double* x, double* buf, int zs, bool to_buf, cudaStream_t s) {
+void launch_frame_copy(const Geom& g, int bw, double* x, double* buf0, int zs0, double* buf1, int zs1, bool to_buf,
+                       cudaStream_t s) {
+    if (!buf0 && !buf1) return;
     const FrameDims f = frame_dims(g, bw);
-    const dim3 grid(static_cast<unsigned>((f.count() + 255) / 256), 8);
-    k_frame_copy<<<grid, 256, 0, s>>>(g, f, x, buf, zs, to_buf ? 1 : 0);
+    const dim3 grid(static_cast<unsigned>((f.count() + 255) / 256), 8, 2);  // both plane pairs in one launch
+    k_frame_copy<<<grid, 256, 0, s>>>(g, f, x, buf0, zs0, buf1, zs1, to_buf ? 1 : 0);
     count();
 }
 void launch_axpy(double* y, const double* x, double alpha, int64_t n, cudaStream_t s) {

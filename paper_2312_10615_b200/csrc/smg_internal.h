@@ -181,7 +181,8 @@ void launch_dgs_pf_delta_c(const LevelK& L, const double* x, const double* b, do
 void launch_dgs_pf_apply_c(const LevelK& L, double* x, const double* d, int c, cudaStream_t s);
 void launch_dgs_prev_c(const LevelK& L, double* x, const double* b, int c, cudaStream_t s);
 int64_t frame_doubles(const Geom& g, int bw);
-void launch_frame_copy(const Geom& g, int bw, double* x, double* buf, int zs, bool to_buf, cudaStream_t s);
+void launch_frame_copy(const Geom& g, int bw, double* x, double* buf0, int zs0, double* buf1, int zs1, bool to_buf,
+                       cudaStream_t s);
 void launch_axpy(double* y, const double* x, double alpha, int64_t n, cudaStream_t s);          // y += alpha x
 void launch_xpby(double* y, const double* x, double beta, int64_t n, cudaStream_t s);           // y = x + beta y
 void launch_dx_update(double* d, double* x, const double* q, double cd, double cq, int64_t n,
