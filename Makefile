@@ -21,8 +21,9 @@ FAKE := tests/fake_nccl/libfakenccl.so
 
 all: $(LIB) $(CLI) oracle $(FAKE)
 
+# test infrastructure only: a failure here (e.g. no nccl.h) must not fail the product build; its tests skip
 $(FAKE): tests/fake_nccl/fake_nccl.c
-	gcc -O2 -Wall -shared -fPIC -I/usr/local/cuda/include -o $@ $< -L/usr/local/cuda/lib64 -lcudart_static -lpthread -ldl -lrt
+	-gcc -O2 -Wall -shared -fPIC -I/usr/local/cuda/include -o $@ $< -L/usr/local/cuda/lib64 -lcudart_static -lpthread -ldl -lrt
 
 $(CLI): $(CSRC)/cli.cpp include/smg.h $(LIB)
 	$(CXX) -O2 -std=c++17 -Wall -Wextra -o $@ $(CSRC)/cli.cpp -L$(PKG) -lsmg -Wl,-rpath,'$$ORIGIN'
